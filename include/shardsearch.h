@@ -1,0 +1,197 @@
+/*
+ * shardsearch.h -- C ABI of the B200 search backend for TAP's plan search.
+ *
+ * The reference (shardplan, pure Python) has no FFI; its swap surface is the
+ * Python seam  derive_plan -> prune_graph / search_subgraph -> _eval_range
+ * (pkg/src/shardplan/search.py:289-379, pruning.py:123-201).  This header is
+ * the flat, PyTorch-free boundary a ctypes/cffi shim binds in its place
+ * (INTEGRATION.md shows the binding).  All inputs are caller-owned, C-contiguous,
+ * little-endian arrays read only for the duration of a call; every handle
+ * returned here is owned by the library and released with its *_free call.
+ *
+ * Error convention: functions return SP_OK (0) or an error code;
+ * sp_last_error(ctx) returns the message of the last failure on that context.
+ * Invalid candidates are data (valid bit / count), never errors -- mirroring
+ * RoutingFailure (search.py:79-82, 198-199).
+ */
+#ifndef SHARDSEARCH_H
+#define SHARDSEARCH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+#define SP_MAX_RANK 8
+
+enum sp_status {
+  SP_OK = 0,
+  SP_ERR_CONFIG = 1,      /* -> shardplan.BadConfig (errors.py:29-30) */
+  SP_ERR_UNSUPPORTED = 2, /* index space > u64, rank > SP_MAX_RANK, ... */
+  SP_ERR_CUDA = 3,        /* CUDA / NCCL internal failure */
+  SP_ERR_SPEC = 4         /* -> shardplan.SpecMismatch (patterns_for on a non-shardable kind) */
+};
+
+/* OpKind (ir.py:44-62) in declaration order. */
+enum sp_op {
+  SP_OP_MATMUL = 0,
+  SP_OP_ELEMENTWISE = 1,
+  SP_OP_LAYERNORM = 2,
+  SP_OP_SOFTMAX = 3,
+  SP_OP_EMBEDDING = 4,
+  SP_OP_RESHAPE = 5,
+  SP_OP_INPUT = 6,
+  SP_OP_OUTPUT = 7,
+  SP_OP_AUXILIARY = 8,
+  SP_OP_COLLECTIVE = 9
+};
+
+/*
+ * Grouped ModelGraph lowered to flat arrays: one row per
+ * GraphNode (ir.py:164-202) in any fixed order; `topo_rank` carries the
+ * position of the node in ModelGraph.topo_order (ir.py:250-274), which is the
+ * only place the library needs the reference's lexicographic-heap order.
+ */
+typedef struct sp_graph {
+  int64_t n_nodes;
+  const uint8_t* name_bytes;  /* concatenated UTF-8 GraphNode scopes */
+  const int64_t* name_off;    /* [n+1] */
+  const int64_t* topo_rank;   /* [n] */
+  const uint8_t* op;          /* [n] enum sp_op */
+  const uint8_t* act_rank;    /* [n] 1..SP_MAX_RANK */
+  const int64_t* act_shape;   /* [n*SP_MAX_RANK], unused dims 0 */
+  const int64_t* act_bytes;   /* [n] TensorSpec.byte_size (ir.py:103-105) */
+  const uint8_t* w_rank;      /* [n] 0 = no weight */
+  const int64_t* w_shape;     /* [n*SP_MAX_RANK] */
+  const int64_t* w_bytes;     /* [n] */
+  const uint8_t* w_trainable; /* [n] */
+  const int64_t* in_off;      /* [n+1] producer CSR */
+  const int32_t* in_idx;      /* [E] producers in GraphNode.inputs order (deduplicated) */
+} sp_graph;
+
+/* ClusterSpec (costmodel.py:36-119) flattened. */
+typedef struct sp_mesh {
+  int64_t m, n;
+  double intra_bw, inter_bw;
+  double eff_allreduce, eff_allgather, eff_reducescatter, eff_alltoall;
+  double overlap_fraction;
+  double setup_latency_s;
+} sp_mesh;
+
+/*
+ * Folding result (the list[Subgraph] of prune_graph, pruning.py:33-55, 123-201)
+ * as a read-only view.  Blocks are in the reference's order (sorted by
+ * template_prefix); instances of a block are sorted by prefix, instance 0 is
+ * the template.  members[block_member_off[b] + i*block_T[b] + t] is the node
+ * index of template position t in instance i of block b.  An instance prefix
+ * is the first inst_prefix_len[j] bytes of node inst_prefix_node[j]'s scope.
+ */
+typedef struct sp_blocks {
+  int64_t n_blocks;
+  int64_t n_instances;
+  int64_t n_members;
+  const int64_t* block_T;          /* [n_blocks] */
+  const int64_t* block_inst_off;   /* [n_blocks+1] */
+  const int64_t* block_member_off; /* [n_blocks+1] */
+  const int64_t* inst_prefix_node; /* [n_instances] */
+  const int64_t* inst_prefix_len;  /* [n_instances] */
+  const int32_t* members;          /* [n_members] */
+} sp_blocks;
+
+/* Per-block search result: SubgraphResult (search.py:236-242) + _plan_key. */
+typedef struct sp_score_out {
+  uint64_t candidates;  /* count_candidates (search.py:96-100) */
+  uint64_t valid;       /* candidates whose pattern_routing succeeded */
+  uint64_t best_index;  /* argmin of (total, num_split, index) */
+  double best_total;    /* CostReport.total of the argmin (bit-exact) */
+  int32_t best_num_split;
+  int32_t has_best;     /* 0 when no candidate routes (reference asserts) */
+} sp_score_out;
+
+#define SP_EXPLAIN_MAX_T 256
+
+/* Routing/cost detail of one candidate (RoutedPlan + CostReport fields). */
+typedef struct sp_explain_out {
+  int32_t valid;
+  int32_t T;
+  int32_t fail_pos;                       /* template position of RoutingFailure */
+  int32_t pattern[SP_EXPLAIN_MAX_T];      /* index into patterns_for(op) */
+  int32_t state_axis[SP_EXPLAIN_MAX_T];   /* final state: -1 replica, else split axis */
+  int32_t exit_axis[SP_EXPLAIN_MAX_T];    /* -1 no exit AllGather, else gather axis */
+  double forward_comm;
+  double backward_comm;
+  double total;
+  int64_t bytes_allreduce, bytes_allgather, bytes_reducescatter, bytes_alltoall;
+  int64_t calls_allreduce, calls_allgather, calls_reducescatter, calls_alltoall;
+  int64_t collective_calls;
+} sp_explain_out;
+
+/* Conversion collective on an internal edge, reported by sp_explain_edges. */
+typedef struct sp_edge_conv {
+  int32_t consumer_pos; /* template position of the consumer */
+  int32_t producer_pos; /* template position of the internal producer */
+  int32_t kind;         /* 1 allreduce, 2 allgather, 3 reducescatter, 4 alltoall */
+  int32_t axis;         /* collective axis, -1 when none */
+} sp_edge_conv;
+
+typedef struct sp_ctx sp_ctx;
+typedef struct sp_dgraph sp_dgraph;
+typedef struct sp_fold sp_fold;
+typedef struct sp_tables sp_tables;
+
+int sp_abi_version(void);
+
+/* One context per process and device (one process per GPU). */
+int sp_ctx_create(int device, sp_ctx** out);
+void sp_ctx_destroy(sp_ctx* ctx);
+const char* sp_last_error(const sp_ctx* ctx);
+
+/* Upload the lowered graph once; it stays resident in HBM. */
+int sp_graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph** out);
+void sp_graph_free(sp_dgraph* dg);
+
+/* prune_graph(graph, min_duplicates) on the device (pruning.py:123-201). */
+int sp_fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold** out);
+int sp_fold_view(const sp_fold* f, sp_blocks* view);
+void sp_fold_free(sp_fold* f);
+
+/*
+ * Per-block routing/cost tables for a set of templates (template node lists
+ * in template order, as Subgraph.template).  mu/chunk are pack_gradients'
+ * threshold and chunk size (rewrite.py:78-111).
+ */
+int sp_tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* tmpl_off,
+                    const int32_t* tmpl_nodes, const sp_mesh* mesh, int64_t mu,
+                    int64_t chunk_size, sp_tables** out);
+void sp_tables_free(sp_tables* t);
+/* count_candidates per block; returns SP_ERR_UNSUPPORTED if one exceeds u64. */
+int sp_tables_candidates(const sp_tables* t, uint64_t* out);
+/* Weight slot order of a block (weight_nodes, search.py:85-88): template positions. */
+int sp_tables_slots(const sp_tables* t, int64_t block, int32_t* slot_pos, int32_t* n_slots);
+
+/*
+ * Batched scoring of every block (search_subgraph + _eval_range, search.py:289-345).
+ * Shard `shard` of `n_shards` scores its contiguous slice of each block's index
+ * range (search.py:331-336); results merge exactly with sp_merge_keys.
+ */
+int sp_score(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out);
+/* Score [lo, hi) of one block; optional per-candidate totals (NaN = invalid). */
+int sp_score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi,
+                   double* totals, sp_score_out* out);
+/* Lexicographic (total, num_split, index) merge of shard results, valid summed. */
+void sp_merge_keys(sp_score_out* acc, const sp_score_out* other);
+
+/* Full routing/cost detail of one candidate (for RoutedPlan/CostReport reconstruction). */
+int sp_explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explain_out* out,
+               sp_edge_conv* edges, int32_t max_edges, int32_t* n_edges);
+
+/* Device time (ms) of the last sp_score / sp_fold_run kernels (CUDA events). */
+int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHARDSEARCH_H */

@@ -1,0 +1,226 @@
+"""ctypes binding of lib/libshardsearch.so (include/shardsearch.h).
+
+There is no fallback: if the library is missing or no CUDA device is usable,
+every entry point raises ``BackendError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _abi
+from ._abi import SpBlocks, SpEdgeConv, SpExplainOut, SpScoreOut, make_sp_graph, make_sp_mesh, ptr
+from .blocks import BlockArrays
+from .errors import BackendError, BadConfig, SpecMismatch, UnsupportedSearch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libshardsearch.so")
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _declare(L):
+    vp = C.c_void_p
+    L.sp_abi_version.restype = C.c_int
+    L.sp_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.sp_ctx_destroy.argtypes = [vp]
+    L.sp_last_error.argtypes = [vp]
+    L.sp_last_error.restype = C.c_char_p
+    L.sp_graph_upload.argtypes = [vp, C.POINTER(_abi.SpGraph), C.POINTER(vp)]
+    L.sp_graph_free.argtypes = [vp]
+    L.sp_fold_run.argtypes = [vp, vp, C.c_int32, C.POINTER(vp)]
+    L.sp_fold_view.argtypes = [vp, C.POINTER(SpBlocks)]
+    L.sp_fold_free.argtypes = [vp]
+    L.sp_tables_build.argtypes = [vp, vp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                  C.POINTER(_abi.SpMesh), C.c_int64, C.c_int64, C.POINTER(vp)]
+    L.sp_tables_free.argtypes = [vp]
+    L.sp_tables_candidates.argtypes = [vp, C.POINTER(C.c_uint64)]
+    L.sp_tables_slots.argtypes = [vp, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.sp_score.argtypes = [vp, vp, C.c_int32, C.c_int32, C.POINTER(SpScoreOut)]
+    L.sp_score_range.argtypes = [vp, vp, C.c_int64, C.c_uint64, C.c_uint64, C.POINTER(C.c_double),
+                                 C.POINTER(SpScoreOut)]
+    L.sp_merge_keys.argtypes = [C.POINTER(SpScoreOut), C.POINTER(SpScoreOut)]
+    L.sp_merge_keys.restype = None
+    L.sp_explain.argtypes = [vp, vp, C.c_int64, C.c_uint64, C.POINTER(SpExplainOut),
+                             C.POINTER(SpEdgeConv), C.c_int32, C.POINTER(C.c_int32)]
+    L.sp_last_timings.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double)]
+    for name in ("sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
+                 "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
+                 "sp_score_range", "sp_explain", "sp_last_timings"):
+        getattr(L, name).restype = C.c_int
+    for name in ("sp_ctx_destroy", "sp_graph_free", "sp_fold_free", "sp_tables_free"):
+        getattr(L, name).restype = None
+
+
+def load_library():
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise BackendError(
+                    f"native backend not built ({LIB_PATH} missing); run "
+                    "`python -c 'import __graft_entry__ as g; g.build()'`")
+            L = C.CDLL(LIB_PATH)
+            _declare(L)
+            if L.sp_abi_version() != 1:
+                raise BackendError("libshardsearch ABI version mismatch")
+            _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = (
+    "sp_abi_version", "sp_ctx_create", "sp_ctx_destroy", "sp_last_error", "sp_graph_upload",
+    "sp_graph_free", "sp_fold_run", "sp_fold_view", "sp_fold_free", "sp_tables_build",
+    "sp_tables_free", "sp_tables_candidates", "sp_tables_slots", "sp_score", "sp_score_range",
+    "sp_merge_keys", "sp_explain", "sp_last_timings",
+)
+
+
+class _Handle:
+    def __init__(self, backend, ptr_, free_fn):
+        self.backend = backend
+        self.ptr = ptr_
+        self._free = free_fn
+
+    def close(self):
+        if self.ptr:
+            self._free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):  # pragma: no cover - GC timing
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class Tables(_Handle):
+    n_blocks: int
+    candidates: np.ndarray
+    overflow: bool
+
+
+class Backend:
+    """One CUDA context on one device (one process per GPU)."""
+
+    def __init__(self, device: int | None = None):
+        self.lib = load_library()
+        if device is None:
+            device = int(os.environ.get("SP_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        self.device = device
+        h = C.c_void_p()
+        rc = self.lib.sp_ctx_create(device, C.byref(h))
+        if rc != 0:
+            raise BackendError(f"sp_ctx_create(device={device}) failed with status {rc}")
+        self.ctx = h
+
+    # -- errors --------------------------------------------------------------------
+    def _check(self, rc: int, what: str):
+        if rc == 0:
+            return
+        msg = (self.lib.sp_last_error(self.ctx) or b"").decode("utf-8", "replace")
+        if rc == _abi.SP_ERR_CONFIG:
+            raise BadConfig(msg or what)
+        if rc == _abi.SP_ERR_UNSUPPORTED:
+            raise UnsupportedSearch(msg or what)
+        if rc == _abi.SP_ERR_SPEC:
+            raise SpecMismatch(msg or what)
+        raise BackendError(f"{what}: {msg}")
+
+    # -- graph ---------------------------------------------------------------------
+    def upload(self, low) -> _Handle:
+        g = make_sp_graph(low)
+        h = C.c_void_p()
+        self._check(self.lib.sp_graph_upload(self.ctx, C.byref(g), C.byref(h)), "sp_graph_upload")
+        return _Handle(self, h, self.lib.sp_graph_free)
+
+    def fold(self, dgraph: _Handle, min_dup: int) -> BlockArrays:
+        h = C.c_void_p()
+        self._check(self.lib.sp_fold_run(self.ctx, dgraph.ptr, int(min_dup), C.byref(h)),
+                    "sp_fold_run")
+        try:
+            view = SpBlocks()
+            self._check(self.lib.sp_fold_view(h, C.byref(view)), "sp_fold_view")
+            return BlockArrays.from_dict(_abi.blocks_to_numpy(view))
+        finally:
+            self.lib.sp_fold_free(h)
+
+    def tables(self, dgraph: _Handle, tmpl_off: np.ndarray, tmpl_nodes: np.ndarray, mesh,
+               mu: int, chunk: int) -> Tables:
+        off = np.ascontiguousarray(tmpl_off, dtype=np.int64)
+        nodes = np.ascontiguousarray(tmpl_nodes, dtype=np.int32)
+        if nodes.size == 0:
+            nodes = np.zeros(1, np.int32)
+        m = make_sp_mesh(mesh)
+        h = C.c_void_p()
+        nb = off.size - 1
+        self._check(self.lib.sp_tables_build(self.ctx, dgraph.ptr, nb, ptr(off, C.c_int64),
+                                              ptr(nodes, C.c_int32), C.byref(m), int(mu),
+                                              int(chunk), C.byref(h)), "sp_tables_build")
+        t = Tables(self, h, self.lib.sp_tables_free)
+        t.n_blocks = nb
+        cands = np.zeros(max(nb, 1), np.uint64)
+        rc = self.lib.sp_tables_candidates(h, ptr(cands, C.c_uint64))
+        t.overflow = rc == _abi.SP_ERR_UNSUPPORTED
+        t.candidates = cands[:nb]
+        return t
+
+    def slots(self, t: Tables, block: int) -> list:
+        n = C.c_int32()
+        self._check(self.lib.sp_tables_slots(t.ptr, block, None, C.byref(n)), "sp_tables_slots")
+        buf = np.zeros(max(1, n.value), np.int32)
+        self._check(self.lib.sp_tables_slots(t.ptr, block, ptr(buf, C.c_int32), C.byref(n)),
+                    "sp_tables_slots")
+        return buf[: n.value].tolist()
+
+    # -- scoring -------------------------------------------------------------------
+    def score(self, t: Tables, shard: int = 0, n_shards: int = 1) -> list:
+        outs = (SpScoreOut * max(1, t.n_blocks))()
+        self._check(self.lib.sp_score(self.ctx, t.ptr, shard, n_shards, outs), "sp_score")
+        return [outs[i] for i in range(t.n_blocks)]
+
+    def score_range(self, t: Tables, block: int, lo: int, hi: int, want_totals: bool = False):
+        out = SpScoreOut()
+        totals = None
+        tp = None
+        if want_totals and hi > lo:
+            totals = np.empty(hi - lo, np.float64)
+            tp = ptr(totals, C.c_double)
+        self._check(self.lib.sp_score_range(self.ctx, t.ptr, block, lo, hi, tp, C.byref(out)),
+                    "sp_score_range")
+        return out, totals
+
+    def explain(self, t: Tables, block: int, index: int):
+        out = SpExplainOut()
+        cap = 4096
+        edges = (SpEdgeConv * cap)()
+        ne = C.c_int32()
+        self._check(self.lib.sp_explain(self.ctx, t.ptr, block, index, C.byref(out), edges, cap,
+                                        C.byref(ne)), "sp_explain")
+        return out, [edges[i] for i in range(min(ne.value, cap))]
+
+    def timings(self) -> dict:
+        f, s, k = C.c_double(), C.c_double(), C.c_double()
+        self.lib.sp_last_timings(self.ctx, C.byref(f), C.byref(s), C.byref(k))
+        return {"fold_ms": f.value, "score_ms": s.value, "score_kernel_ms": k.value}
+
+    def close(self):
+        if self.ctx:
+            self.lib.sp_ctx_destroy(self.ctx)
+            self.ctx = None
+
+
+_default: Backend | None = None
+
+
+def default_backend() -> Backend:
+    global _default
+    if _default is None:
+        _default = Backend()
+    return _default

@@ -1,0 +1,207 @@
+// extern "C" boundary (include/shardsearch.h): exception -> status code,
+// per-context last-error string, device timing accessors.
+#include <cstdio>
+
+#include "sp_internal.h"
+
+namespace {
+
+template <class F>
+int guard(sp_ctx* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) ctx->last_error.clear();
+    return SP_OK;
+  } catch (const sp::Error& e) {
+    if (ctx) ctx->last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return SP_ERR_CUDA;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return SP_ERR_CUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
+int sp_ctx_create(int device, sp_ctx** out) {
+  if (!out) return SP_ERR_CONFIG;
+  *out = nullptr;
+  sp_ctx* ctx = new sp_ctx();
+  int rc = guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(device));
+    ctx->device = device;
+    SP_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+    int optin = 0;
+    SP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    ctx->smem_optin = (size_t)optin;
+    SP_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev) SP_CUDA(cudaEventCreate(&e));
+  });
+  if (rc != SP_OK) {
+    std::fprintf(stderr, "sp_ctx_create: %s\n", ctx->last_error.c_str());
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return SP_OK;
+}
+
+void sp_ctx_destroy(sp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  ctx->cub_tmp.release();
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* sp_last_error(const sp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int sp_graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph** out) {
+  if (!ctx || !g || !out) return SP_ERR_CONFIG;
+  *out = nullptr;
+  sp_dgraph* dg = new sp_dgraph();
+  int rc = guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::graph_upload(ctx, g, dg);
+  });
+  if (rc != SP_OK) {
+    delete dg;
+    return rc;
+  }
+  *out = dg;
+  return SP_OK;
+}
+
+void sp_graph_free(sp_dgraph* dg) {
+  if (!dg) return;
+  if (dg->ctx) {
+    cudaSetDevice(dg->ctx->device);
+    cudaStreamSynchronize(dg->ctx->stream);
+  }
+  delete dg;
+}
+
+int sp_fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold** out) {
+  if (!ctx || !dg || !out) return SP_ERR_CONFIG;
+  *out = nullptr;
+  sp_fold* f = new sp_fold();
+  int rc = guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    SP_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+    sp::fold_run(ctx, dg, min_dup, f);
+    SP_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+    SP_CUDA(cudaEventSynchronize(ctx->ev[5]));
+    float ms = 0;
+    SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
+    ctx->fold_ms = ms;
+  });
+  if (rc != SP_OK) {
+    delete f;
+    return rc;
+  }
+  *out = f;
+  return SP_OK;
+}
+
+int sp_fold_view(const sp_fold* f, sp_blocks* view) {
+  if (!f || !view) return SP_ERR_CONFIG;
+  *view = f->view;
+  return SP_OK;
+}
+
+void sp_fold_free(sp_fold* f) { delete f; }
+
+int sp_tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* tmpl_off,
+                    const int32_t* tmpl_nodes, const sp_mesh* mesh, int64_t mu, int64_t chunk_size,
+                    sp_tables** out) {
+  if (!ctx || !dg || !tmpl_off || !mesh || !out) return SP_ERR_CONFIG;
+  *out = nullptr;
+  sp_tables* t = new sp_tables();
+  int rc = guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    if (mesh->m < 1 || mesh->n < 1) throw sp::Error(SP_ERR_CONFIG, "mesh must be at least 1x1");
+    sp::tables_build(ctx, dg, n_blocks, tmpl_off, tmpl_nodes, mesh, mu, chunk_size, t);
+  });
+  if (rc != SP_OK) {
+    sp::tables_free_priv(t);
+    delete t;
+    return rc;
+  }
+  *out = t;
+  return SP_OK;
+}
+
+void sp_tables_free(sp_tables* t) {
+  if (!t) return;
+  if (t->ctx) {
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+  }
+  sp::tables_free_priv(t);
+  delete t;
+}
+
+int sp_tables_candidates(const sp_tables* t, uint64_t* out) {
+  if (!t || !out) return SP_ERR_CONFIG;
+  for (int64_t b = 0; b < t->n_blocks; b++) out[b] = t->hdr[b].C;
+  return t->overflow ? SP_ERR_UNSUPPORTED : SP_OK;
+}
+
+int sp_tables_slots(const sp_tables* t, int64_t block, int32_t* slot_pos, int32_t* n_slots) {
+  if (!t || block < 0 || block >= t->n_blocks || !n_slots) return SP_ERR_CONFIG;
+  const auto& v = t->slot_pos[block];
+  if (slot_pos)
+    for (size_t i = 0; i < v.size(); i++) slot_pos[i] = v[i];
+  *n_slots = (int32_t)v.size();
+  return SP_OK;
+}
+
+int sp_score(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out) {
+  if (!ctx || !t || !out) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::score_all(ctx, t, shard, n_shards, out);
+  });
+}
+
+int sp_score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi, double* totals,
+                   sp_score_out* out) {
+  if (!ctx || !t || !out) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::score_range(ctx, t, block, lo, hi, totals, out);
+  });
+}
+
+void sp_merge_keys(sp_score_out* acc, const sp_score_out* other) {
+  if (acc && other) sp::merge_key(acc, other);
+}
+
+int sp_explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explain_out* out,
+               sp_edge_conv* edges, int32_t max_edges, int32_t* n_edges) {
+  if (!ctx || !t || !out || !n_edges) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::explain(ctx, t, block, index, out, edges, max_edges, n_edges);
+  });
+}
+
+int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms) {
+  if (!ctx) return SP_ERR_CONFIG;
+  if (fold_ms) *fold_ms = ctx->fold_ms;
+  if (score_ms) *score_ms = ctx->score_ms;
+  if (score_kernel_ms) *score_kernel_ms = ctx->score_kernel_ms;
+  return SP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,695 @@
+// Graph upload and shared-subgraph folding on the device.
+//
+// Reference semantics (pruning.py:123-201): siblings are grouped by their
+// depth-d name prefix; among the children of one parent, groups whose exact
+// template key (_template_key, pruning.py:97-111) occurs >= min_dup times are
+// accepted as one Subgraph; the rest descend one level, and members that end
+// at depth d become residual singletons.  Whether a group is still "active"
+// at level d depends only on its ancestors, so the recursion is executed
+// level-synchronously over all sibling sets at once:
+//
+//   per level d (all kernels grid-stride over the active nodes / groups)
+//     1. sort active nodes by (prefix_d hash, rel-name hash)   [CUB radix]
+//        -> groups = runs of equal prefix hash, members in canonical order
+//     2. 1-round WL entry hash per node: rel name, op, weight, multiset of
+//        internal producers' rel names; group key = commutative sum
+//     3. sort groups by (parent group, key)                     [CUB radix]
+//        -> classes = runs of equal (parent, key)
+//     4. exact verification: every node's prefix bytes against its group
+//        head, every group member-by-member against its class head (rel
+//        bytes, op, weight, internal-producer positions).  Any mismatch is a
+//        hash collision: the whole fold reruns with a new seed, so the
+//        partition is exact, not probabilistic.
+//     5. classes with >= min_dup groups are accepted; the rest split into
+//        residuals (depth == d) and next-level actives.
+//
+// The host then orders the result the way the reference's string sorts do
+// (instances and blocks by prefix string, template by topological rank).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <numeric>
+
+#include "sp_internal.h"
+
+namespace sp {
+
+namespace {
+
+constexpr uint64_t kPolyB = 0x100000001b3ULL;  // odd polynomial base
+
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+
+__device__ __forceinline__ uint64_t upow(uint64_t b, int64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+
+__global__ void k_depth(const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
+                        int32_t* __restrict__ depth, int32_t* __restrict__ maxd) {
+  int32_t local = 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t d = 1;
+    for (int64_t k = off[i]; k < off[i + 1]; k++) d += s[k] == '/';
+    depth[i] = d;
+    local = max(local, d);
+  }
+  atomicMax(maxd, local);
+}
+
+// Per node and depth d: prefix end, prefix hash, rel-name hash.
+__global__ void k_name_hash(const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
+                            int32_t D, uint64_t seed, int32_t* __restrict__ pend,
+                            uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t* p = s + off[i];
+    const int64_t L = off[i + 1] - off[i];
+    uint64_t h = 0;
+    int d = 0;
+    // prefix ends and prefix hashes; h tracks poly(p[0:k])
+    uint64_t hpre[64];
+    int32_t ends[64];
+    for (int64_t k = 0; k <= L; k++) {
+      if (k == L || p[k] == '/') {
+        if (d < D && d < 64) {
+          ends[d] = (int32_t)k;
+          hpre[d] = h;
+        }
+        d++;
+        if (k == L) break;
+      }
+      h = h * kPolyB + (uint64_t)p[k] + 1;
+    }
+    const uint64_t hall = h;
+    const int dn = d;  // node depth
+    for (int dd = 0; dd < D; dd++) {
+      const int64_t idx = i * D + dd;
+      if (dd >= dn || dd >= 64) {
+        pend[idx] = (int32_t)L;
+        ph[idx] = 0;
+        rh[idx] = 0;
+        continue;
+      }
+      const int64_t q = ends[dd];
+      pend[idx] = (int32_t)q;
+      ph[idx] = fmix64(hpre[dd] ^ fmix64(seed + (uint64_t)q));
+      // rel = p[start:L] with start = q+1 if the prefix is non-empty, else 0
+      int64_t start = q > 0 ? q + 1 : 0;
+      if (start > L) start = L;
+      // poly(p[start:L]) = poly(p[0:L]) - poly(p[0:start]) * B^(L-start)
+      uint64_t hrel;
+      if (q >= L) {
+        hrel = 0;  // the node IS the prefix: rel name is ""
+      } else {
+        const uint64_t hs = start > 0 ? hpre[dd] * kPolyB + (uint64_t)'/' + 1 : 0;  // poly(p[0:q+1])
+        hrel = hall - hs * upow(kPolyB, L - start);
+      }
+      rh[idx] = fmix64(hrel ^ fmix64((seed ^ 0x9e3779b97f4a7c15ULL) + (uint64_t)(L - start)));
+    }
+  }
+}
+
+__global__ void k_gather_keys(const int32_t* __restrict__ act, int64_t nA, const uint64_t* __restrict__ src,
+                              int32_t D, int32_t dd, uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[(int64_t)act[i] * D + dd];
+}
+
+__global__ void k_heads_u64(const uint64_t* __restrict__ k, int64_t n, int32_t* __restrict__ head) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+
+// groups: cur[node] = stamp|gid, gstart[gid] = first sorted position
+__global__ void k_group_setup(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid,
+                              int64_t nA, int64_t stamp, int64_t* __restrict__ cur,
+                              int32_t* __restrict__ gstart) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = gid[i] - 1;  // inclusive scan of heads
+    cur[sorted[i]] = stamp | (int64_t)g;
+    if (i == 0 || gid[i - 1] != gid[i]) gstart[g] = (int32_t)i;
+  }
+}
+
+__device__ __forceinline__ uint64_t weight_hash(int64_t n, const uint8_t* w_rank, const int64_t* w_shape,
+                                                const uint8_t* w_train) {
+  const int r = w_rank[n];
+  if (!r) return 0x51ed270b27a8f1a3ULL;
+  uint64_t h = fmix64(0x2545f4914f6cdd1dULL + (uint64_t)r * 31 + (uint64_t)w_train[n]);
+  for (int k = 0; k < r; k++) h = fmix64(h ^ (uint64_t)w_shape[n * SP_MAX_RANK + k] * 0x9e3779b97f4a7c15ULL);
+  return h;
+}
+
+// Entry hash (template key entry) and group key sums; positions in group.
+__global__ void k_entry(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
+                        const int32_t* __restrict__ gstart, const int64_t* __restrict__ cur,
+                        const uint64_t* __restrict__ rh, int32_t D, int32_t dd,
+                        const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                        const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                        const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                        int32_t* __restrict__ pos, unsigned long long* __restrict__ gkey) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t n = sorted[i];
+    const int32_t g = gid[i] - 1;
+    pos[n] = (int32_t)(i - gstart[g]);
+    const int64_t me = cur[n];
+    uint64_t prod = 0;
+    for (int64_t e = in_off[n]; e < in_off[n + 1]; e++) {
+      const int32_t r = in_idx[e];
+      if (cur[r] == me) prod += fmix64(rh[(int64_t)r * D + dd] ^ 0x6a09e667f3bcc909ULL);
+    }
+    uint64_t h = fmix64(rh[(int64_t)n * D + dd] + 0x3c6ef372fe94f82bULL * (uint64_t)(op[n] + 1));
+    h = fmix64(h ^ weight_hash(n, w_rank, w_shape, w_train));
+    h = fmix64(h + fmix64(prod ^ 0xbb67ae8584caa73bULL));
+    atomicAdd(&gkey[g], (unsigned long long)fmix64(h ^ 0xa54ff53a5f1d36f1ULL));
+  }
+}
+
+__global__ void k_class_keys(int64_t nG, int64_t nA, const int32_t* __restrict__ gstart,
+                             const int32_t* __restrict__ sorted, const unsigned long long* __restrict__ gkey,
+                             const int32_t* __restrict__ gparent, uint64_t* __restrict__ ck,
+                             uint32_t* __restrict__ par, int32_t* __restrict__ gidx) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nG;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = gstart[g];
+    const int64_t s1 = g + 1 < nG ? gstart[g + 1] : nA;
+    ck[g] = fmix64((uint64_t)gkey[g] ^ fmix64((uint64_t)(s1 - s0) + 0x1f83d9abfb41bd6bULL));
+    par[g] = (uint32_t)gparent[sorted[s0]];
+    gidx[g] = (int32_t)g;
+  }
+}
+
+__global__ void k_class_heads(const uint32_t* __restrict__ par, const uint64_t* __restrict__ ck,
+                              int64_t nG, int32_t* __restrict__ head) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nG;
+       j += (int64_t)gridDim.x * blockDim.x)
+    head[j] = (j == 0 || par[j] != par[j - 1] || ck[j] != ck[j - 1]) ? 1 : 0;
+}
+
+// class of every group, class starts over the class-ordered group list
+__global__ void k_class_setup(const int32_t* __restrict__ order, const int32_t* __restrict__ cid,
+                              int64_t nG, int32_t* __restrict__ gclass, int32_t* __restrict__ cstart) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nG;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = cid[j] - 1;
+    gclass[order[j]] = c;
+    if (j == 0 || cid[j - 1] != cid[j]) cstart[c] = (int32_t)j;
+  }
+}
+
+__device__ __forceinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, int64_t n) {
+  for (int64_t k = 0; k < n; k++)
+    if (a[k] != b[k]) return false;
+  return true;
+}
+
+__device__ void sort_small(int32_t* v, int n) {
+  for (int i = 1; i < n; i++) {
+    int32_t x = v[i];
+    int j = i - 1;
+    while (j >= 0 && v[j] > x) {
+      v[j + 1] = v[j];
+      j--;
+    }
+    v[j + 1] = x;
+  }
+}
+
+// Exact checks: prefix bytes vs group head, distinct rel hashes inside a
+// group, and member-by-member template-key equality vs the class head group.
+__global__ void k_verify(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
+                         int64_t nG, const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass,
+                         const int32_t* __restrict__ cstart, const int32_t* __restrict__ corder,
+                         const int64_t* __restrict__ cur, const int32_t* __restrict__ pos,
+                         const int32_t* __restrict__ pend, const uint64_t* __restrict__ rh, int32_t D,
+                         int32_t dd, const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
+                         const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                         const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                         const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                         int32_t* __restrict__ collision) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t n = sorted[i];
+    const int32_t g = gid[i] - 1;
+    const int64_t s0 = gstart[g];
+    const int64_t gsz = (g + 1 < nG ? gstart[g + 1] : nA) - s0;
+    bool bad = false;
+    // (a) same prefix string as the group head
+    const int32_t h = sorted[s0];
+    const int32_t pl = pend[(int64_t)n * D + dd];
+    if (pl != pend[(int64_t)h * D + dd] || !bytes_eq(names + name_off[n], names + name_off[h], pl)) bad = true;
+    // (b) rel hashes strictly distinct inside a group (canonical order well defined)
+    if (i > s0 && rh[(int64_t)sorted[i - 1] * D + dd] == rh[(int64_t)n * D + dd]) bad = true;
+    // (c) template key equality with the class head group at the same canonical position
+    const int32_t c = gclass[g];
+    const int32_t hg = corder[cstart[c]];
+    if (hg != g) {
+      const int64_t h0 = gstart[hg];
+      const int64_t hsz = (hg + 1 < nG ? gstart[hg + 1] : nA) - h0;
+      const int64_t j = i - s0;
+      if (hsz != gsz) {
+        bad = true;
+      } else {
+        const int32_t b = sorted[h0 + j];
+        const int64_t la = name_off[n + 1] - name_off[n];
+        const int64_t lb = name_off[b + 1] - name_off[b];
+        int64_t sa = pl > 0 ? pl + 1 : 0;
+        const int32_t plb = pend[(int64_t)b * D + dd];
+        int64_t sb = plb > 0 ? plb + 1 : 0;
+        sa = sa > la ? la : sa;
+        sb = sb > lb ? lb : sb;
+        if (la - sa != lb - sb || !bytes_eq(names + name_off[n] + sa, names + name_off[b] + sb, la - sa))
+          bad = true;
+        if (op[n] != op[b] || w_rank[n] != w_rank[b] || w_train[n] != w_train[b]) bad = true;
+        for (int k = 0; k < w_rank[n] && !bad; k++)
+          if (w_shape[(int64_t)n * SP_MAX_RANK + k] != w_shape[(int64_t)b * SP_MAX_RANK + k]) bad = true;
+        // internal producers as canonical positions
+        int32_t pa[16], pb[16];
+        int ka = 0, kb = 0;
+        bool over = false;
+        for (int64_t e = in_off[n]; e < in_off[n + 1]; e++)
+          if (cur[in_idx[e]] == cur[n]) {
+            if (ka < 16) pa[ka] = pos[in_idx[e]];
+            ka++;
+          }
+        for (int64_t e = in_off[b]; e < in_off[b + 1]; e++)
+          if (cur[in_idx[e]] == cur[b]) {
+            if (kb < 16) pb[kb] = pos[in_idx[e]];
+            kb++;
+          }
+        if (ka != kb) bad = true;
+        if (!bad && ka > 16) over = true;
+        if (!bad && !over) {
+          sort_small(pa, ka);
+          sort_small(pb, kb);
+          for (int k = 0; k < ka; k++)
+            if (pa[k] != pb[k]) bad = true;
+        }
+        if (!bad && over) {
+          // wide fan-in: quadratic multiset comparison (rare)
+          for (int64_t e = in_off[n]; e < in_off[n + 1] && !bad; e++) {
+            const int32_t r = in_idx[e];
+            if (cur[r] != cur[n]) continue;
+            int ca = 0, cb = 0;
+            for (int64_t f = in_off[n]; f < in_off[n + 1]; f++)
+              ca += cur[in_idx[f]] == cur[n] && pos[in_idx[f]] == pos[r];
+            for (int64_t f = in_off[b]; f < in_off[b + 1]; f++)
+              cb += cur[in_idx[f]] == cur[b] && pos[in_idx[f]] == pos[r];
+            if (ca != cb) bad = true;
+          }
+        }
+      }
+    }
+    if (bad) atomicExch(collision, 1);
+  }
+}
+
+// accept / residual / descend for every active node
+__global__ void k_accept(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
+                         int64_t nC, int64_t nG, const int32_t* __restrict__ gclass,
+                         const int32_t* __restrict__ cstart, const int32_t* __restrict__ depth,
+                         int32_t level, int32_t min_dup, int32_t* __restrict__ gparent,
+                         uint8_t* __restrict__ next_flag, uint8_t* __restrict__ residual,
+                         uint8_t* __restrict__ gaccept) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t n = sorted[i];
+    const int32_t g = gid[i] - 1;
+    const int32_t c = gclass[g];
+    const int64_t csz = (c + 1 < nC ? cstart[c + 1] : nG) - cstart[c];
+    const bool acc = csz >= min_dup;
+    if (i == 0 || gid[i - 1] != gid[i]) gaccept[g] = acc;
+    next_flag[i] = 0;
+    if (acc) continue;
+    if (depth[n] <= level) {
+      residual[n] = 1;
+    } else {
+      next_flag[i] = 1;
+      gparent[n] = g;
+    }
+  }
+}
+
+inline int grid_for(int64_t n, int sms) {
+  int64_t b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  int64_t cap = (int64_t)sms * 16;
+  return (int)(b < cap ? b : cap);
+}
+
+struct LevelOut {
+  int32_t level;
+  std::vector<int32_t> sorted, gstart, corder, cstart;
+  std::vector<uint8_t> gaccept;
+};
+
+int strcmp_py(const uint8_t* a, int64_t la, const uint8_t* b, int64_t lb) {
+  int64_t m = la < lb ? la : lb;
+  int c = m ? std::memcmp(a, b, (size_t)m) : 0;
+  if (c) return c;
+  return (la > lb) - (la < lb);
+}
+
+}  // namespace
+
+void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
+  const int64_t n = g->n_nodes;
+  if (n < 1) throw Error(SP_ERR_CONFIG, "graph has no nodes");
+  cudaStream_t s = ctx->stream;
+  dg->ctx = ctx;
+  dg->n = n;
+  dg->E = g->in_off[n];
+  const int64_t nb = g->name_off[n];
+  dg->h_names.assign(g->name_bytes, g->name_bytes + nb);
+  dg->h_name_off.assign(g->name_off, g->name_off + n + 1);
+  dg->h_topo.assign(g->topo_rank, g->topo_rank + n);
+  dg->h_op.assign(g->op, g->op + n);
+  dg->h_act_rank.assign(g->act_rank, g->act_rank + n);
+  dg->h_w_rank.assign(g->w_rank, g->w_rank + n);
+  dg->h_w_train.assign(g->w_trainable, g->w_trainable + n);
+  dg->h_act_shape.assign(g->act_shape, g->act_shape + n * SP_MAX_RANK);
+  dg->h_w_shape.assign(g->w_shape, g->w_shape + n * SP_MAX_RANK);
+  dg->h_act_bytes.assign(g->act_bytes, g->act_bytes + n);
+  dg->h_w_bytes.assign(g->w_bytes, g->w_bytes + n);
+  dg->h_in_off.assign(g->in_off, g->in_off + n + 1);
+  dg->h_in_idx.assign(g->in_idx, g->in_idx + dg->E);
+  for (int64_t i = 0; i < n; i++) {
+    if (dg->h_act_rank[i] < 1 || dg->h_act_rank[i] > SP_MAX_RANK || dg->h_w_rank[i] > SP_MAX_RANK)
+      throw Error(SP_ERR_UNSUPPORTED, "tensor rank outside 1..SP_MAX_RANK");
+  }
+  for (int64_t e = 0; e < dg->E; e++)
+    if (dg->h_in_idx[e] < 0 || dg->h_in_idx[e] >= n) throw Error(SP_ERR_CONFIG, "producer index out of range");
+  dg->names.upload(dg->h_names.data(), nb, s);
+  dg->name_off.upload(dg->h_name_off.data(), n + 1, s);
+  dg->topo.upload(dg->h_topo.data(), n, s);
+  dg->op.upload(dg->h_op.data(), n, s);
+  dg->act_rank.upload(dg->h_act_rank.data(), n, s);
+  dg->w_rank.upload(dg->h_w_rank.data(), n, s);
+  dg->w_train.upload(dg->h_w_train.data(), n, s);
+  dg->act_shape.upload(dg->h_act_shape.data(), n * SP_MAX_RANK, s);
+  dg->w_shape.upload(dg->h_w_shape.data(), n * SP_MAX_RANK, s);
+  dg->act_bytes.upload(dg->h_act_bytes.data(), n, s);
+  dg->w_bytes.upload(dg->h_w_bytes.data(), n, s);
+  dg->in_off.upload(dg->h_in_off.data(), n + 1, s);
+  dg->in_idx.upload(dg->h_in_idx.data(), dg->E, s);
+  int32_t maxd = 1;
+  for (int64_t i = 0; i < n; i++) {
+    int32_t d = 1;
+    for (int64_t k = dg->h_name_off[i]; k < dg->h_name_off[i + 1]; k++) d += dg->h_names[k] == '/';
+    maxd = std::max(maxd, d);
+  }
+  dg->max_depth = maxd;
+  SP_CUDA(cudaStreamSynchronize(s));
+}
+
+template <class T>
+__global__ void k_gather(const int32_t* __restrict__ idx, int64_t m, const T* __restrict__ src,
+                         T* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed, sp_fold* out,
+                      bool* collided) {
+  cudaStream_t s = ctx->stream;
+  const int sms = ctx->sm_count;
+  const int64_t n = dg->n;
+  const int32_t D = dg->max_depth;
+
+  DevBuf<int32_t> depth, maxd, pend, act, sorted1, sorted2, gidv, gstart, pos, gparent, gclass, corder,
+      corder2, corder3, cid, cstart, collision, nsel;
+  DevBuf<uint64_t> ph, rh, k1, k1s, k2, k2s, ck, cks, cks2;
+  DevBuf<uint32_t> par, par2, pars;
+  DevBuf<int64_t> cur;
+  DevBuf<unsigned long long> gkey;
+  DevBuf<uint8_t> next_flag, residual, gaccept;
+  depth.alloc(n, s);
+  maxd.alloc(1, s);
+  pend.alloc((size_t)n * D, s);
+  ph.alloc((size_t)n * D, s);
+  rh.alloc((size_t)n * D, s);
+  act.alloc(n, s);
+  sorted1.alloc(n, s);
+  sorted2.alloc(n, s);
+  gidv.alloc(n, s);
+  gstart.alloc(n, s);
+  pos.alloc(n, s);
+  gparent.alloc(n, s);
+  gclass.alloc(n, s);
+  corder.alloc(n, s);
+  corder2.alloc(n, s);
+  corder3.alloc(n, s);
+  cid.alloc(n, s);
+  cstart.alloc(n, s);
+  collision.alloc(1, s);
+  nsel.alloc(1, s);
+  k1.alloc(n, s);
+  k1s.alloc(n, s);
+  k2.alloc(n, s);
+  k2s.alloc(n, s);
+  ck.alloc(n, s);
+  cks.alloc(n, s);
+  cks2.alloc(n, s);
+  par.alloc(n, s);
+  par2.alloc(n, s);
+  pars.alloc(n, s);
+  cur.alloc(n, s);
+  gkey.alloc(n, s);
+  next_flag.alloc(n, s);
+  residual.alloc(n, s);
+  gaccept.alloc(n, s);
+
+  SP_CUDA(cudaMemsetAsync(maxd.p, 0, sizeof(int32_t), s));
+  k_depth<<<grid_for(n, sms), 256, 0, s>>>(dg->name_off.p, dg->names.p, n, depth.p, maxd.p);
+  k_name_hash<<<grid_for(n, sms), 128, 0, s>>>(dg->name_off.p, dg->names.p, n, D, seed, pend.p, ph.p, rh.p);
+  SP_CUDA(cudaMemsetAsync(gparent.p, 0, n * sizeof(int32_t), s));
+  SP_CUDA(cudaMemsetAsync(residual.p, 0, n, s));
+  SP_CUDA(cudaMemsetAsync(collision.p, 0, sizeof(int32_t), s));
+  SP_CUDA(cudaMemsetAsync(cur.p, 0xff, n * sizeof(int64_t), s));
+  {
+    std::vector<int32_t> iota(n);
+    std::iota(iota.begin(), iota.end(), 0);
+    act.upload(iota.data(), n, s);
+  }
+
+  // CUB scratch sized for the largest call
+  size_t tmp_bytes = 0, t = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t, k1.p, k1s.p, act.p, sorted1.p, (int)n, 0, 64, s);
+  tmp_bytes = std::max(tmp_bytes, t);
+  cub::DeviceRadixSort::SortPairs(nullptr, t, par.p, pars.p, corder.p, corder2.p, (int)n, 0, 32, s);
+  tmp_bytes = std::max(tmp_bytes, t);
+  cub::DeviceScan::InclusiveSum(nullptr, t, gidv.p, gidv.p, (int)n, s);
+  tmp_bytes = std::max(tmp_bytes, t);
+  cub::DeviceSelect::Flagged(nullptr, t, sorted2.p, next_flag.p, act.p, nsel.p, (int)n, s);
+  tmp_bytes = std::max(tmp_bytes, t);
+  ctx->cub_tmp.alloc(tmp_bytes, s);
+  void* tmp = ctx->cub_tmp.p;
+
+  std::vector<LevelOut> levels;
+  int64_t nA = n;
+  for (int32_t level = 1; nA > 0; level++) {
+    if (level > D) throw Error(SP_ERR_CUDA, "fold did not terminate");
+    const int32_t dd = level - 1;
+    const int g1 = grid_for(nA, sms);
+    // 1. sort active nodes by (prefix hash, rel hash): rel first, then prefix (stable LSD)
+    k_gather_keys<<<g1, 256, 0, s>>>(act.p, nA, rh.p, D, dd, k2.p);
+    t = tmp_bytes;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, k2.p, k2s.p, act.p, sorted1.p, (int)nA, 0, 64, s));
+    k_gather_keys<<<g1, 256, 0, s>>>(sorted1.p, nA, ph.p, D, dd, k1.p);
+    t = tmp_bytes;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, k1.p, k1s.p, sorted1.p, sorted2.p, (int)nA, 0, 64, s));
+    k_heads_u64<<<g1, 256, 0, s>>>(k1s.p, nA, gidv.p);
+    t = tmp_bytes;
+    SP_CUDA(cub::DeviceScan::InclusiveSum(tmp, t, gidv.p, gidv.p, (int)nA, s));
+    int32_t nG32 = 0;
+    SP_CUDA(cudaMemcpyAsync(&nG32, gidv.p + nA - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    const int64_t nG = nG32;
+    const int64_t stamp = ((int64_t)level) << 32;
+    k_group_setup<<<g1, 256, 0, s>>>(sorted2.p, gidv.p, nA, stamp, cur.p, gstart.p);
+    // 2. entry hashes and group keys
+    SP_CUDA(cudaMemsetAsync(gkey.p, 0, nG * sizeof(unsigned long long), s));
+    k_entry<<<g1, 256, 0, s>>>(sorted2.p, gidv.p, nA, gstart.p, cur.p, rh.p, D, dd, dg->op.p, dg->w_rank.p,
+                               dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, pos.p, gkey.p);
+    // 3. classes: sort groups by (parent, key) -- key first, then parent (stable)
+    const int gG = grid_for(nG, sms);
+    k_class_keys<<<gG, 256, 0, s>>>(nG, nA, gstart.p, sorted2.p, gkey.p, gparent.p, ck.p, par.p, corder.p);
+    t = tmp_bytes;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, ck.p, cks.p, corder.p, corder2.p, (int)nG, 0, 64, s));
+    k_gather<uint32_t><<<gG, 256, 0, s>>>(corder2.p, nG, par.p, par2.p);
+    t = tmp_bytes;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, par2.p, pars.p, corder2.p, corder3.p, (int)nG, 0, 32, s));
+    k_gather<uint64_t><<<gG, 256, 0, s>>>(corder3.p, nG, ck.p, cks2.p);
+    k_class_heads<<<gG, 256, 0, s>>>(pars.p, cks2.p, nG, cid.p);
+    t = tmp_bytes;
+    SP_CUDA(cub::DeviceScan::InclusiveSum(tmp, t, cid.p, cid.p, (int)nG, s));
+    int32_t nC32 = 0;
+    SP_CUDA(cudaMemcpyAsync(&nC32, cid.p + nG - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    const int64_t nC = nC32;
+    k_class_setup<<<gG, 256, 0, s>>>(corder3.p, cid.p, nG, gclass.p, cstart.p);
+    // 4. exact verification against group and class heads
+    k_verify<<<g1, 128, 0, s>>>(sorted2.p, gidv.p, nA, nG, gstart.p, gclass.p, cstart.p, corder3.p, cur.p,
+                                pos.p, pend.p, rh.p, D, dd, dg->name_off.p, dg->names.p, dg->op.p,
+                                dg->w_rank.p, dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p,
+                                collision.p);
+    // 5. accept / residual / descend
+    k_accept<<<g1, 256, 0, s>>>(sorted2.p, gidv.p, nA, nC, nG, gclass.p, cstart.p, depth.p, level, min_dup,
+                                gparent.p, next_flag.p, residual.p, gaccept.p);
+    LevelOut lv;
+    lv.level = level;
+    lv.sorted.resize(nA);
+    lv.gstart.resize(nG + 1);
+    lv.corder.resize(nG);
+    lv.cstart.resize(nC + 1);
+    lv.gaccept.resize(nG);
+    sorted2.download(lv.sorted.data(), nA, s);
+    gstart.download(lv.gstart.data(), nG, s);
+    corder3.download(lv.corder.data(), nG, s);
+    cstart.download(lv.cstart.data(), nC, s);
+    gaccept.download(lv.gaccept.data(), nG, s);
+    t = tmp_bytes;
+    SP_CUDA(cub::DeviceSelect::Flagged(tmp, t, sorted2.p, next_flag.p, act.p, nsel.p, (int)nA, s));
+    int32_t nsel_h = 0;
+    SP_CUDA(cudaMemcpyAsync(&nsel_h, nsel.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    lv.gstart[nG] = (int32_t)nA;
+    lv.cstart[nC] = (int32_t)nG;
+    levels.push_back(std::move(lv));
+    nA = nsel_h;
+  }
+  int32_t coll_h = 0;
+  std::vector<uint8_t> resid_h(n);
+  std::vector<int32_t> pend_h((size_t)n * D);
+  SP_CUDA(cudaMemcpyAsync(&coll_h, collision.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  residual.download(resid_h.data(), n, s);
+  pend.download(pend_h.data(), (size_t)n * D, s);
+  SP_CUDA(cudaStreamSynchronize(s));
+  *collided = coll_h != 0;
+  if (*collided) return;
+
+  // ---- host ordering: the string-order decisions of pruning.py:136-148, 200 ----
+  const uint8_t* names = dg->h_names.data();
+  const int64_t* noff = dg->h_name_off.data();
+  const int64_t* topo = dg->h_topo.data();
+  struct Block {
+    int64_t pnode, plen;
+    std::vector<int64_t> inst_node, inst_len;
+    std::vector<int32_t> members;  // instance-major
+    int64_t T;
+  };
+  std::vector<Block> blocks;
+  for (const LevelOut& lv : levels) {
+    const int64_t dd = lv.level - 1;
+    const int64_t nC = (int64_t)lv.cstart.size() - 1;
+    for (int64_t c = 0; c < nC; c++) {
+      const int32_t g0 = lv.corder[lv.cstart[c]];
+      if (!lv.gaccept[g0]) continue;
+      std::vector<int32_t> gs(lv.corder.begin() + lv.cstart[c], lv.corder.begin() + lv.cstart[c + 1]);
+      auto gprefix = [&](int32_t g, int64_t* node, int64_t* len) {
+        *node = lv.sorted[lv.gstart[g]];
+        *len = pend_h[(size_t)(*node) * D + dd];
+      };
+      std::sort(gs.begin(), gs.end(), [&](int32_t a, int32_t b) {
+        int64_t na, la, nb, lb;
+        gprefix(a, &na, &la);
+        gprefix(b, &nb, &lb);
+        return strcmp_py(names + noff[na], la, names + noff[nb], lb) < 0;
+      });
+      const int32_t tg = gs[0];
+      const int64_t T = lv.gstart[tg + 1] - lv.gstart[tg];
+      std::vector<int32_t> canon(T);  // template position -> canonical position
+      std::iota(canon.begin(), canon.end(), 0);
+      std::sort(canon.begin(), canon.end(), [&](int32_t a, int32_t b) {
+        return topo[lv.sorted[lv.gstart[tg] + a]] < topo[lv.sorted[lv.gstart[tg] + b]];
+      });
+      Block B;
+      gprefix(tg, &B.pnode, &B.plen);
+      B.T = T;
+      for (int32_t g : gs) {
+        int64_t pn, pl;
+        gprefix(g, &pn, &pl);
+        B.inst_node.push_back(pn);
+        B.inst_len.push_back(pl);
+        for (int64_t tpos = 0; tpos < T; tpos++) B.members.push_back(lv.sorted[lv.gstart[g] + canon[tpos]]);
+      }
+      blocks.push_back(std::move(B));
+    }
+  }
+  for (int64_t i = 0; i < n; i++) {
+    if (!resid_h[i]) continue;
+    Block B;
+    B.pnode = i;
+    B.plen = noff[i + 1] - noff[i];
+    B.T = 1;
+    B.inst_node.push_back(i);
+    B.inst_len.push_back(B.plen);
+    B.members.push_back((int32_t)i);
+    blocks.push_back(std::move(B));
+  }
+  std::vector<int64_t> order(blocks.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    const Block& A = blocks[a];
+    const Block& Bb = blocks[b];
+    return strcmp_py(names + noff[A.pnode], A.plen, names + noff[Bb.pnode], Bb.plen) < 0;
+  });
+  out->block_T.clear();
+  out->block_inst_off.assign(1, 0);
+  out->block_member_off.assign(1, 0);
+  out->inst_prefix_node.clear();
+  out->inst_prefix_len.clear();
+  out->members.clear();
+  for (int64_t bi : order) {
+    const Block& B = blocks[bi];
+    out->block_T.push_back(B.T);
+    out->inst_prefix_node.insert(out->inst_prefix_node.end(), B.inst_node.begin(), B.inst_node.end());
+    out->inst_prefix_len.insert(out->inst_prefix_len.end(), B.inst_len.begin(), B.inst_len.end());
+    out->members.insert(out->members.end(), B.members.begin(), B.members.end());
+    out->block_inst_off.push_back((int64_t)out->inst_prefix_node.size());
+    out->block_member_off.push_back((int64_t)out->members.size());
+  }
+  if ((int64_t)out->members.size() != n) throw Error(SP_ERR_CUDA, "fold did not cover every node exactly once");
+  sp_blocks& v = out->view;
+  v.n_blocks = (int64_t)out->block_T.size();
+  v.n_instances = (int64_t)out->inst_prefix_node.size();
+  v.n_members = (int64_t)out->members.size();
+  v.block_T = out->block_T.data();
+  v.block_inst_off = out->block_inst_off.data();
+  v.block_member_off = out->block_member_off.data();
+  v.inst_prefix_node = out->inst_prefix_node.data();
+  v.inst_prefix_len = out->inst_prefix_len.data();
+  v.members = out->members.data();
+}
+
+void fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold* out) {
+  if (min_dup < 1) throw Error(SP_ERR_CONFIG, "min_duplicates must be >= 1");
+  bool collided = false;
+  for (int attempt = 0; attempt < 8; attempt++) {
+    fold_once(ctx, dg, min_dup, 0x243f6a8885a308d3ULL + 0x9e3779b97f4a7c15ULL * (uint64_t)attempt, out,
+              &collided);
+    if (!collided) return;
+  }
+  throw Error(SP_ERR_CUDA, "fold hash verification failed on every seed");
+}
+
+}  // namespace sp

@@ -1,0 +1,1103 @@
+// Per-block routing tables and batched candidate scoring.
+//
+// Scoring one candidate in the reference is pattern_routing (search.py:134-224)
+// followed by plan_cost (costmodel.py:193-267) and pack_gradients
+// (rewrite.py:78-111).  Routing a template node is a pure function of (its
+// weight digit, the shard states of its internal producers): node states are
+// always one of R / S(0) / S(rank-1).  tables_build evaluates that function
+// once per (node, digit, producer-state tuple) on the device and stores the
+// chosen pattern and output state in a byte table; the conversion and pattern
+// collective costs it needs for the forward longest-path DP go into small
+// fp64 tables.  The scoring kernel then resolves a candidate with one byte
+// lookup and a few fp64 adds/maxes per node, with everything staged in shared
+// memory.  All fp64 arithmetic keeps the reference's operation order
+// (round-to-nearest, no contraction), so totals are bit-identical.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "patterns.cuh"
+#include "sp_internal.h"
+
+namespace sp {
+
+namespace {
+
+constexpr int KMAX = 6;          // internal producers handled by a lookup table
+constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
+constexpr int THREADS = 256;     // scoring CTA size
+constexpr int ITEM_ITERS = 16;   // candidates per work item = THREADS * ITEM_ITERS
+constexpr uint64_t ITEM_CANDS = (uint64_t)THREADS * ITEM_ITERS;
+
+__host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
+__host__ __device__ inline uint32_t pow3(int k) {
+  uint32_t r = 1;
+  for (int i = 0; i < k; i++) r *= 3;
+  return r;
+}
+
+struct GraphView {
+  const uint8_t* op;
+  const uint8_t* act_rank;
+  const int64_t* act_shape;
+  const int64_t* act_bytes;
+  const uint8_t* w_rank;
+  const int64_t* w_shape;
+  const int64_t* w_bytes;
+  const uint8_t* w_train;
+  const int64_t* in_off;
+  const int32_t* in_idx;
+};
+
+// Routing of one node for a given digit and internal producer states
+// (search.py:153-211).  prod_state[j] indexes R/S0/S(rank-1) of the j-th
+// internal producer in GraphNode.inputs order.  Returns the chosen pattern
+// (-1 = RoutingFailure) and its output state index; optionally the
+// conversion collective on each internal edge.
+struct NodeRoute {
+  int pattern;
+  int state;
+  int8_t conv_kind[64];
+  int8_t conv_axis[64];
+};
+
+__host__ __device__ bool weight_ok(const Pattern& pt, int wrank, const int64_t* wshape, int digit, int64_t d) {
+  if (pt.w.kind == K_NONE) return false;  // pattern without a weight spec never matches a weight
+  NSpec want;
+  if (!normalize(pt.w, wrank, &want)) return false;
+  // WEIGHT_OPTIONS_2D/1D (search.py:35-36): replica, split(0), split(1)
+  NSpec assigned = digit == 0 ? NSpec{K_R, 0} : NSpec{K_S, (int8_t)(digit - 1)};
+  if (!nspec_eq(want, assigned)) return false;
+  if (assigned.kind == K_S && (wshape[assigned.axis] % d) != 0) return false;
+  return true;
+}
+
+__device__ void route_node(const GraphView& G, int32_t n, int32_t blk, const int32_t* node_block,
+                           int digit, const int* prod_state, const MeshC& M, NodeRoute* out,
+                           bool want_conv) {
+  Pattern pats[4];
+  const int np = patterns_for(G.op[n], pats);
+  const int arank = G.act_rank[n];
+  const int64_t* ashape = G.act_shape + (int64_t)n * SP_MAX_RANK;
+  int best = -1;
+  double best_c = 0.0;
+  NSpec best_out{K_R, 0};
+  for (int p = 0; p < np; p++) {
+    const Pattern& pt = pats[p];
+    if (G.w_rank[n] && !weight_ok(pt, G.w_rank[n], G.w_shape + (int64_t)n * SP_MAX_RANK, digit, M.d)) continue;
+    double c = 0.0;
+    bool feasible = true;
+    int j = 0;
+    for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+      const int32_t r = G.in_idx[e];
+      const bool internal = node_block[r] == blk;
+      const int rr = G.act_rank[r];
+      const NSpec st = internal ? state_spec(prod_state[j], rr) : NSpec{K_R, 0};
+      NSpec req;
+      int8_t kind, axis;
+      if (!normalize(pt.in, rr, &req) ||
+          !convert(st, req, G.act_shape + (int64_t)r * SP_MAX_RANK, M.d, &kind, &axis)) {
+        feasible = false;
+        break;
+      }
+      if (kind != C_ID) c = dadd(c, call_cost(kind, G.act_bytes[r], M));
+      if (internal) j++;
+    }
+    if (!feasible) continue;
+    NSpec o;
+    if (!normalize(pt.out, arank, &o)) continue;
+    if (o.kind == K_S && (ashape[o.axis] % M.d) != 0) continue;
+    c = dadd(c, call_cost(pt.coll, G.act_bytes[n], M));
+    if (best < 0 || c < best_c) {  // min by (cost, pattern index)
+      best = p;
+      best_c = c;
+      best_out = o;
+    }
+  }
+  out->pattern = best;
+  if (best < 0) {
+    out->state = 0;
+    return;
+  }
+  // apply_collective: the only non-identity pattern collective is AllReduce -> R
+  const NSpec fin = pats[best].coll == C_AR ? NSpec{K_R, 0} : best_out;
+  out->state = state_index(fin, arank);
+  if (want_conv) {
+    int j = 0;
+    for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+      const int32_t r = G.in_idx[e];
+      if (node_block[r] != blk) continue;
+      const int rr = G.act_rank[r];
+      NSpec req;
+      normalize(pats[best].in, rr, &req);
+      int8_t kind = C_ID, axis = -1;
+      convert(state_spec(prod_state[j], rr), req, G.act_shape + (int64_t)r * SP_MAX_RANK, M.d, &kind, &axis);
+      if (j < 64) {
+        out->conv_kind[j] = kind;
+        out->conv_axis[j] = axis;
+      }
+      j++;
+    }
+  }
+}
+
+struct EntryLayout {
+  int32_t k, nd, out_pool, prod, tab, dbl, train_idx, pad;
+};
+
+__global__ void k_mark_blocks(const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
+                              int32_t* node_block, int32_t* node_tpos, int32_t* dup) {
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
+    for (int64_t e = tmpl_off[b] + threadIdx.x; e < tmpl_off[b + 1]; e += blockDim.x) {
+      const int32_t n = tmpl_nodes[e];
+      if (atomicExch(&node_block[n], (int32_t)b) != -1) atomicExch(dup, 1);
+      node_tpos[n] = (int32_t)(e - tmpl_off[b]);
+    }
+}
+
+__global__ void k_boundary(GraphView G, int64_t n, const int32_t* node_block, uint8_t* has_cons,
+                           uint8_t* ext_cons) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = G.in_off[c]; e < G.in_off[c + 1]; e++) {
+      const int32_t p = G.in_idx[e];
+      has_cons[p] = 1;
+      if (node_block[c] != node_block[p] || node_block[p] < 0) ext_cons[p] = 1;
+    }
+}
+
+// One thread per block: pool-slot liveness and blob layout.
+__global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
+                         const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
+                         const uint8_t* radix_of, int32_t* lastuse, EntryLayout* lay, BlobHeader* hdr,
+                         int64_t* blob_bytes, int32_t* err) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = tmpl_off[b];
+    const int T = (int)(tmpl_off[b + 1] - e0);
+    for (int i = 0; i < T; i++) lastuse[e0 + i] = -1;
+    int nprod = 0, nt = 0;
+    int64_t nent = 0, ndbl = 0;
+    for (int i = 0; i < T; i++) {
+      const int32_t n = tmpl_nodes[e0 + i];
+      int k = 0;
+      for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+        const int32_t r = G.in_idx[e];
+        if (node_block[r] != (int32_t)b) continue;
+        const int j = node_tpos[r];
+        if (j >= i) atomicExch(err, 2);  // template not topologically ordered
+        lastuse[e0 + j] = i;
+        k++;
+      }
+      if (k > KMAX) atomicExch(err, 3);
+      EntryLayout L;
+      L.k = k;
+      L.nd = slot_of[e0 + i] >= 0 ? radix_of[e0 + i] : 1;
+      L.prod = nprod;
+      L.tab = (int32_t)nent;
+      L.dbl = (int32_t)ndbl;
+      L.train_idx = (G.w_rank[n] && G.w_train[n]) ? nt++ : -1;
+      L.out_pool = -1;
+      L.pad = 0;
+      nprod += k;
+      nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
+      ndbl += 8 + 12 * (int64_t)k;
+      lay[e0 + i] = L;
+    }
+    // linear-scan pool allocation: a producer's slot frees at its last consumer
+    uint32_t used[MAXT / 32] = {0};
+    int npool = 0;
+    for (int i = 0; i < T; i++) {
+      const int32_t n = tmpl_nodes[e0 + i];
+      for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+        const int32_t r = G.in_idx[e];
+        if (node_block[r] != (int32_t)b) continue;
+        const int j = node_tpos[r];
+        const int ps = lay[e0 + j].out_pool;
+        if (lastuse[e0 + j] == i && ps >= 0) used[ps >> 5] &= ~(1u << (ps & 31));
+      }
+      if (lastuse[e0 + i] >= 0) {
+        int s = 0;
+        while (used[s >> 5] & (1u << (s & 31))) s++;
+        used[s >> 5] |= 1u << (s & 31);
+        lay[e0 + i].out_pool = s;
+        npool = max(npool, s + 1);
+      }
+    }
+    BlobHeader& H = hdr[b];
+    H.T = T;
+    H.nt = nt;
+    H.npool = npool;
+    int64_t off = sizeof(BlobHeader);
+    H.desc_off = (int32_t)off;
+    off = align16(off + 16 * (int64_t)T);
+    H.prod_off = (int32_t)off;
+    off = align16(off + 2 * (int64_t)nprod);
+    H.tab_off = (int32_t)off;
+    off = align16(off + nent);
+    H.dbl_off = (int32_t)off;
+    off = align16(off + 8 * ndbl);
+    H.train_off = (int32_t)off;
+    off = align16(off + (int64_t)sizeof(TrainDesc) * nt);
+    H.bytes = (int32_t)off;
+    blob_bytes[b] = off;
+  }
+}
+
+// One thread per template entry: node descriptor, producer pool slots, fp64
+// tables, routing byte table; the block's first entry writes the header.
+__global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
+                       int64_t n_entries, const int32_t* node_block, const int32_t* node_tpos,
+                       const int16_t* slot_of, const EntryLayout* lay, const BlobHeader* hdr_in,
+                       const int64_t* blob_off, const uint8_t* has_cons, const uint8_t* ext_cons,
+                       sp_mesh mesh, int64_t mu, int64_t chunk, uint8_t* blobs, uint8_t* bound_of) {
+  const MeshC M = mesh_consts(mesh);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    // block of this entry (binary search over tmpl_off)
+    int64_t lo = 0, hi = nb;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) / 2;
+      if (tmpl_off[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const int64_t b = lo;
+    const int64_t e0 = tmpl_off[b];
+    const int i = (int)(e - e0);
+    const int32_t n = tmpl_nodes[e];
+    const BlobHeader& H = hdr_in[b];
+    uint8_t* blob = blobs + blob_off[b];
+    const EntryLayout L = lay[e];
+    if (i == 0) {
+      BlobHeader h = H;
+      h.multi_dev = M.d > 1;
+      h.setup = M.setup;
+      h.c_ar = dmul(2.0, (double)(M.d - 1));
+      h.c_ar = ddiv(h.c_ar, (double)M.d);
+      h.bw = M.bw;
+      h.eff_ar = M.eff[C_AR];
+      h.keep_bwd = dadd(1.0, -mesh.overlap_fraction);
+      h.mu = mu;
+      h.chunk = chunk;
+      *(BlobHeader*)blob = h;
+    }
+    NodeDesc nd;
+    nd.slot = slot_of[e];
+    nd.k = (uint8_t)L.k;
+    nd.nd = (uint8_t)L.nd;
+    nd.out_pool = (int16_t)L.out_pool;
+    nd.prod = (uint16_t)L.prod;
+    nd.tab = (uint32_t)L.tab;
+    nd.dbl = (uint32_t)L.dbl;
+    ((NodeDesc*)(blob + H.desc_off))[i] = nd;
+    int16_t* prod = (int16_t*)(blob + H.prod_off) + L.prod;
+    {
+      int j = 0;
+      for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
+        const int32_t r = G.in_idx[q];
+        if (node_block[r] != (int32_t)b) continue;
+        prod[j++] = (int16_t)lay[e0 + node_tpos[r]].out_pool;
+      }
+    }
+    double* dbl = (double*)(blob + H.dbl_off) + L.dbl;
+    Pattern pats[4];
+    const int np = patterns_for(G.op[n], pats);
+    // own[p]: pattern collective call cost on this node's activation
+    for (int p = 0; p < 4; p++) dbl[p] = p < np ? call_cost(pats[p].coll, G.act_bytes[n], M) : 0.0;
+    // exitc[s]: AllGather back to replica at a subgraph boundary (search.py:213-223)
+    const bool boundary = !has_cons[n] || ext_cons[n];
+    bound_of[e] = boundary;
+    const double ag = boundary ? call_cost(C_AG, G.act_bytes[n], M) : 0.0;
+    dbl[4] = 0.0;
+    dbl[5] = ag;
+    dbl[6] = ag;
+    dbl[7] = 0.0;
+    // conv[j][p][s]: internal edge conversion cost (0.0 for identity / infeasible)
+    {
+      int j = 0;
+      for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
+        const int32_t r = G.in_idx[q];
+        if (node_block[r] != (int32_t)b) continue;
+        const int rr = G.act_rank[r];
+        for (int p = 0; p < 4; p++)
+          for (int s = 0; s < 3; s++) {
+            double c = 0.0;
+            NSpec req;
+            int8_t kind, axis;
+            if (p < np && normalize(pats[p].in, rr, &req) &&
+                convert(state_spec(s, rr), req, G.act_shape + (int64_t)r * SP_MAX_RANK, M.d, &kind, &axis) &&
+                kind != C_ID)
+              c = call_cost(kind, G.act_bytes[r], M);
+            dbl[8 + (j * 4 + p) * 3 + s] = c;
+          }
+        j++;
+      }
+    }
+    // routing byte table: key = Horner(digit, s_0, ..., s_{k-1}) in base 3
+    uint8_t* tab = blob + H.tab_off + L.tab;
+    const uint32_t nkeys = (uint32_t)L.nd * pow3(L.k);
+    NodeRoute R;
+    int ps[KMAX];
+    for (uint32_t key = 0; key < nkeys; key++) {
+      uint32_t x = key;
+      for (int j = L.k - 1; j >= 0; j--) {
+        ps[j] = (int)(x % 3);
+        x /= 3;
+      }
+      const int digit = (int)x;
+      route_node(G, n, (int32_t)b, node_block, digit, ps, M, &R, false);
+      tab[key] = R.pattern < 0 ? (uint8_t)0xFF : (uint8_t)(R.pattern | (R.state << 2));
+    }
+    if (L.train_idx >= 0) {
+      TrainDesc td;
+      td.slot = slot_of[e];
+      td.pad = 0;
+      td.size = G.w_bytes[n];
+      td.uterm = dadd(M.setup, cost_bytes(C_AR, td.size, M));
+      ((TrainDesc*)(blob + H.train_off))[L.train_idx] = td;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scoring
+
+struct ItemOut {
+  unsigned long long total_bits;  // ~0 when the item has no valid candidate
+  unsigned long long index;
+  uint32_t num_split;
+  uint32_t valid;
+};
+
+__device__ __forceinline__ bool key_less(unsigned long long ta, uint32_t na, unsigned long long ia,
+                                         unsigned long long tb, uint32_t nb, unsigned long long ib) {
+  if (ta != tb) return ta < tb;
+  if (na != nb) return na < nb;
+  return ia < ib;
+}
+
+__device__ __forceinline__ uint32_t get_digit(uint64_t w0, uint64_t w1, int s) {
+  return (uint32_t)(((s < 32 ? w0 : w1) >> ((s & 31) * 2)) & 3);
+}
+
+// digits += t in mixed radix (last slot fastest)
+__device__ __forceinline__ void mr_add(uint64_t& w0, uint64_t& w1, uint32_t t, int V, uint64_t radix3) {
+  for (int s = V - 1; s >= 0 && t; s--) {
+    const int sh = (s & 31) * 2;
+    uint64_t& w = s < 32 ? w0 : w1;
+    const uint32_t d = (uint32_t)((w >> sh) & 3);
+    const uint32_t v = d + t;
+    uint32_t q, r;
+    if ((radix3 >> s) & 1) {
+      q = v / 3;
+      r = v - q * 3;
+    } else {
+      q = v >> 1;
+      r = v & 1;
+    }
+    w = (w & ~(3ULL << sh)) | ((uint64_t)r << sh);
+    t = q;
+  }
+}
+
+struct ScorePlan {
+  const int64_t* blob_off;
+  const int32_t* item_block;  // unused (binary search instead)
+  const unsigned long long* lo;   // per block start index (shard-local)
+  const unsigned long long* hi;
+  const unsigned long long* item_base;  // prefix sum of items per block, [nb+1]
+  int64_t nb;
+  unsigned long long n_items;
+};
+
+// Batched scorer: dynamic work items of ITEM_CANDS candidates over all blocks.
+__global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ blobs, ScorePlan P,
+                                                   ItemOut* __restrict__ items,
+                                                   unsigned long long* __restrict__ counter,
+                                                   double* __restrict__ totals) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ unsigned long long s_item;
+  __shared__ int64_t s_block;
+  __shared__ uint64_t s_w0, s_w1;
+  __shared__ unsigned long long s_red_t[THREADS / 32], s_red_i[THREADS / 32];
+  __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  int64_t staged = -1;
+  while (true) {
+    if (tid == 0) s_item = atomicAdd(counter, 1ULL);
+    __syncthreads();
+    const unsigned long long item = s_item;
+    if (item >= P.n_items) break;
+    if (tid == 0) {
+      int64_t lo = 0, hi = P.nb;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (P.item_base[mid] <= item) lo = mid;
+        else hi = mid;
+      }
+      s_block = lo;
+    }
+    __syncthreads();
+    const int64_t b = s_block;
+    const BlobHeader* gH = (const BlobHeader*)(blobs + P.blob_off[b]);
+    const int blob_bytes = gH->bytes;
+    if (b != staged) {
+      // stage the block's tables: 16-byte vector copies
+      const uint4* src = (const uint4*)(blobs + P.blob_off[b]);
+      uint4* dst = (uint4*)smem;
+      for (int q = tid; q < blob_bytes / 16; q += THREADS) dst[q] = src[q];
+      staged = b;
+    }
+    __syncthreads();
+    const BlobHeader& H = *(const BlobHeader*)smem;
+    const NodeDesc* desc = (const NodeDesc*)(smem + H.desc_off);
+    const int16_t* prodp = (const int16_t*)(smem + H.prod_off);
+    const uint8_t* tab = smem + H.tab_off;
+    const double* dbl = (const double*)(smem + H.dbl_off);
+    const TrainDesc* trn = (const TrainDesc*)(smem + H.train_off);
+    double* reach = (double*)(smem + ((blob_bytes + 15) & ~15));
+    uint8_t* stp = (uint8_t*)(reach + (size_t)H.npool * THREADS);
+
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * ITEM_CANDS;
+    unsigned long long ihi = ilo + ITEM_CANDS;
+    if (ihi > P.hi[b]) ihi = P.hi[b];
+    if (tid == 0) {
+      // decode the item's first index (candidate_by_index, search.py:103-116)
+      uint64_t w0 = 0, w1 = 0;
+      unsigned long long rem = ilo;
+      for (int s = H.V - 1; s >= 0; s--) {
+        const uint32_t r = ((H.radix3 >> s) & 1) ? 3 : 2;
+        const uint32_t d = (uint32_t)(rem % r);
+        rem /= r;
+        if (s < 32) w0 |= (uint64_t)d << ((s & 31) * 2);
+        else w1 |= (uint64_t)d << ((s & 31) * 2);
+      }
+      s_w0 = w0;
+      s_w1 = w1;
+    }
+    __syncthreads();
+    uint64_t w0 = s_w0, w1 = s_w1;
+    mr_add(w0, w1, (uint32_t)tid, H.V, H.radix3);
+    unsigned long long best_t = ~0ULL, best_i = ~0ULL;
+    uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
+    for (unsigned long long base = ilo; base < ihi; base += THREADS) {
+      const unsigned long long idx = base + tid;
+      bool ok = idx < ihi;
+      double fwd = 0.0;
+      for (int i = 0; i < H.T; i++) {
+        const NodeDesc nd = desc[i];
+        uint32_t key = nd.slot >= 0 ? get_digit(w0, w1, nd.slot) : 0;
+        int sj[KMAX];
+        double rj[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; j++) {
+          if (j < nd.k) {
+            const int ps = prodp[nd.prod + j];
+            sj[j] = stp[ps * THREADS + tid];
+            rj[j] = reach[ps * THREADS + tid];
+            key = key * 3 + sj[j];
+          }
+        }
+        const uint8_t e = tab[nd.tab + key];
+        ok = ok && e != 0xFF;
+        if (!__any_sync(0xffffffffu, ok)) break;
+        const int p = e & 3;
+        const int s = ok ? (e >> 2) & 3 : 0;
+        const double* D = dbl + nd.dbl;
+        double bse = 0.0;
+#pragma unroll
+        for (int j = 0; j < KMAX; j++)
+          if (j < nd.k) bse = fmax(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
+        const double r = dadd(bse, D[p]);
+        fwd = fmax(fwd, dadd(r, D[4 + s]));
+        if (nd.out_pool >= 0) {
+          reach[nd.out_pool * THREADS + tid] = r;
+          stp[nd.out_pool * THREADS + tid] = (uint8_t)s;
+        }
+      }
+      if (ok) {
+        // backward: pack_gradients over replicated trainable weights (template order)
+        double bwd = 0.0;
+        if (H.multi_dev) {
+          long long cur = 0;
+          int cur_n = 0;
+          for (int q = 0; q < H.nt; q++) {
+            const TrainDesc td = trn[q];
+            if (get_digit(w0, w1, td.slot) != 0) continue;
+            if (td.size >= H.mu) continue;
+            if (cur + td.size > H.chunk && cur_n) {
+              bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
+              cur = 0;
+              cur_n = 0;
+            }
+            cur += td.size;
+            cur_n++;
+          }
+          if (cur_n) bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
+          for (int q = 0; q < H.nt; q++) {
+            const TrainDesc td = trn[q];
+            if (get_digit(w0, w1, td.slot) == 0 && td.size >= H.mu) bwd = dadd(bwd, td.uterm);
+          }
+        }
+        const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
+        const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+        const uint32_t ns = __popcll((w0 | (w0 >> 1)) & 0x5555555555555555ULL) +
+                            __popcll((w1 | (w1 >> 1)) & 0x5555555555555555ULL);
+        nvalid++;
+        if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
+          best_t = tb;
+          best_n = ns;
+          best_i = idx;
+        }
+        if (totals) totals[idx - P.lo[b]] = total;
+      } else if (totals && idx < ihi) {
+        totals[idx - P.lo[b]] = __longlong_as_double(0x7ff8000000000000LL);
+      }
+      mr_add(w0, w1, THREADS, H.V, H.radix3);
+    }
+    // warp then block argmin of (total, num_split, index) + valid count
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, best_t, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, best_i, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, best_n, o);
+      nvalid += __shfl_down_sync(0xffffffffu, nvalid, o);
+      if (key_less(t2, n2, i2, best_t, best_n, best_i)) {
+        best_t = t2;
+        best_n = n2;
+        best_i = i2;
+      }
+    }
+    if (lane == 0) {
+      s_red_t[warp] = best_t;
+      s_red_i[warp] = best_i;
+      s_red_n[warp] = best_n;
+      s_red_v[warp] = nvalid;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      ItemOut o{s_red_t[0], s_red_i[0], s_red_n[0], s_red_v[0]};
+      for (int w = 1; w < THREADS / 32; w++) {
+        o.valid += s_red_v[w];
+        if (key_less(s_red_t[w], s_red_n[w], s_red_i[w], o.total_bits, o.num_split, o.index)) {
+          o.total_bits = s_red_t[w];
+          o.num_split = s_red_n[w];
+          o.index = s_red_i[w];
+        }
+      }
+      items[item] = o;
+    }
+    // the next iteration's first __syncthreads orders s_item reuse
+  }
+}
+
+// One CTA per block: merge its items.
+__global__ void k_reduce(const ItemOut* __restrict__ items, const unsigned long long* __restrict__ item_base,
+                         int64_t nb, sp_score_out* __restrict__ out) {
+  __shared__ ItemOut s[THREADS];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    ItemOut acc{~0ULL, ~0ULL, 0xFFFFFFFFu, 0};
+    unsigned long long valid = 0;
+    for (unsigned long long it = item_base[b] + threadIdx.x; it < item_base[b + 1]; it += blockDim.x) {
+      const ItemOut o = items[it];
+      valid += o.valid;
+      if (key_less(o.total_bits, o.num_split, o.index, acc.total_bits, acc.num_split, acc.index)) acc = o;
+    }
+    acc.valid = 0;
+    s[threadIdx.x] = acc;
+    __shared__ unsigned long long sv[THREADS];
+    sv[threadIdx.x] = valid;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+      if (threadIdx.x < st) {
+        const ItemOut o = s[threadIdx.x + st];
+        if (key_less(o.total_bits, o.num_split, o.index, s[threadIdx.x].total_bits, s[threadIdx.x].num_split,
+                     s[threadIdx.x].index))
+          s[threadIdx.x] = o;
+        sv[threadIdx.x] += sv[threadIdx.x + st];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      sp_score_out r;
+      r.candidates = 0;
+      r.valid = sv[0];
+      r.has_best = s[0].index != ~0ULL && sv[0] > 0;
+      r.best_index = r.has_best ? s[0].index : 0;
+      r.best_total = r.has_best ? __longlong_as_double((long long)s[0].total_bits) : 0.0;
+      r.best_num_split = r.has_best ? (int32_t)s[0].num_split : 0;
+      out[b] = r;
+    }
+    __syncthreads();
+  }
+}
+
+// Full detail of one candidate (RoutedPlan + CostReport), single thread.
+__global__ void k_explain(GraphView G, const int32_t* tmpl, int T, int32_t blk, const int32_t* node_block,
+                          const int32_t* node_tpos, const int16_t* slot_of, const uint8_t* digits,
+                          const uint8_t* boundary, sp_mesh mesh, int64_t mu, int64_t chunk,
+                          sp_explain_out* out, sp_edge_conv* edges, int32_t max_edges, int32_t* n_edges) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const MeshC M = mesh_consts(mesh);
+  int state[MAXT];
+
+  double reach[MAXT];
+  out->valid = 0;
+  out->T = T;
+  out->fail_pos = -1;
+  int ne = 0;
+  int64_t bytes[5] = {0, 0, 0, 0, 0}, calls[5] = {0, 0, 0, 0, 0};
+  NodeRoute R;
+  for (int i = 0; i < T; i++) {
+    const int32_t n = tmpl[i];
+    int ps[64];
+    int k = 0;
+    for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+      const int32_t r = G.in_idx[e];
+      if (node_block[r] != blk) continue;
+      if (k < 64) ps[k] = state[node_tpos[r]];
+      k++;
+    }
+    const int digit = slot_of[i] >= 0 ? digits[slot_of[i]] : 0;
+    route_node(G, n, blk, node_block, digit, ps, M, &R, true);
+    if (R.pattern < 0) {
+      out->fail_pos = i;
+      *n_edges = ne;
+      return;
+    }
+
+    state[i] = R.state;
+    Pattern pats[4];
+    patterns_for(G.op[n], pats);
+    double base = 0.0;
+    int j = 0;
+    for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+      const int32_t r = G.in_idx[e];
+      if (node_block[r] != blk) continue;
+      const int kind = R.conv_kind[j];
+      double cc = 0.0;
+      if (kind != C_ID) {
+        cc = call_cost(kind, G.act_bytes[r], M);
+        bytes[kind] += G.act_bytes[r];
+        calls[kind]++;
+        if (ne < max_edges) edges[ne] = sp_edge_conv{i, node_tpos[r], kind, R.conv_axis[j]};
+        ne++;
+      }
+      base = fmax(base, dadd(reach[node_tpos[r]], cc));
+      j++;
+    }
+    const int pc = pats[R.pattern].coll;
+    if (pc != C_ID) {
+      bytes[pc] += G.act_bytes[n];
+      calls[pc]++;
+    }
+    reach[i] = dadd(base, call_cost(pc, G.act_bytes[n], M));
+    out->pattern[i] = R.pattern;
+    const NSpec fs = state_spec(R.state, G.act_rank[n]);
+    out->state_axis[i] = fs.kind == K_S ? fs.axis : -1;
+  }
+  double fwd = 0.0;
+  for (int i = 0; i < T; i++) {
+    const int32_t n = tmpl[i];
+    double tail = reach[i];
+    out->exit_axis[i] = -1;
+    if (boundary[i] && state[i] != 0) {
+      tail = dadd(tail, call_cost(C_AG, G.act_bytes[n], M));
+      bytes[C_AG] += G.act_bytes[n];
+      calls[C_AG]++;
+      out->exit_axis[i] = state_spec(state[i], G.act_rank[n]).axis;
+    }
+    fwd = fmax(fwd, tail);
+  }
+  double bwd = 0.0;
+  if (M.d > 1) {
+    int64_t bk[MAXT], uf[MAXT];
+    int nbk = 0, nuf = 0, cur_n = 0;
+    int64_t cur = 0;
+    for (int i = 0; i < T; i++) {
+      const int32_t n = tmpl[i];
+      if (!G.w_rank[n] || !G.w_train[n] || digits[slot_of[i]] != 0) continue;
+      const int64_t sz = G.w_bytes[n];
+      if (sz >= mu) {
+        uf[nuf++] = sz;
+        continue;
+      }
+      if (cur + sz > chunk && cur_n) {
+        bk[nbk++] = cur;
+        cur = 0;
+        cur_n = 0;
+      }
+      cur += sz;
+      cur_n++;
+    }
+    if (cur_n) bk[nbk++] = cur;
+    for (int q = 0; q < nbk; q++) {
+      bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, bk[q], M)));
+      bytes[C_AR] += bk[q];
+      calls[C_AR]++;
+    }
+    for (int q = 0; q < nuf; q++) {
+      bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, uf[q], M)));
+      bytes[C_AR] += uf[q];
+      calls[C_AR]++;
+    }
+  }
+  out->valid = 1;
+  out->forward_comm = fwd;
+  out->backward_comm = bwd;
+  out->total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
+  out->bytes_allreduce = bytes[C_AR];
+  out->bytes_allgather = bytes[C_AG];
+  out->bytes_reducescatter = bytes[C_RS];
+  out->bytes_alltoall = bytes[C_A2A];
+  out->calls_allreduce = calls[C_AR];
+  out->calls_allgather = calls[C_AG];
+  out->calls_reducescatter = calls[C_RS];
+  out->calls_alltoall = calls[C_A2A];
+  out->collective_calls = calls[C_AR] + calls[C_AG] + calls[C_RS] + calls[C_A2A];
+  *n_edges = ne;
+}
+
+inline int grid_for(int64_t n, int sms, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  const int64_t cap = (int64_t)sms * 16;
+  return (int)(b < cap ? b : cap);
+}
+
+int strcmp_py(const uint8_t* a, int64_t la, const uint8_t* b, int64_t lb) {
+  const int64_t m = la < lb ? la : lb;
+  const int c = m ? std::memcmp(a, b, (size_t)m) : 0;
+  if (c) return c;
+  return (la > lb) - (la < lb);
+}
+
+GraphView view_of(sp_dgraph* dg) {
+  return GraphView{dg->op.p,      dg->act_rank.p, dg->act_shape.p, dg->act_bytes.p, dg->w_rank.p,
+                   dg->w_shape.p, dg->w_bytes.p,  dg->w_train.p,   dg->in_off.p,    dg->in_idx.p};
+}
+
+// per-table device state kept for scoring/explain
+struct TableDev {
+  DevBuf<int32_t> node_block, node_tpos;
+  DevBuf<int16_t> slot_of;
+  DevBuf<uint8_t> has_cons, ext_cons, bound;
+};
+
+}  // namespace
+
+struct TablesPriv {
+  TableDev dev;
+  sp_mesh mesh;
+  int64_t mu, chunk;
+};
+
+}  // namespace sp
+
+namespace sp {
+
+void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_off, const int32_t* tmpl_nodes,
+                  const sp_mesh* mesh, int64_t mu, int64_t chunk, sp_tables* out) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = dg->n;
+  if (nb < 0) throw Error(SP_ERR_CONFIG, "negative block count");
+  if (mu > chunk) throw Error(SP_ERR_CONFIG, "fusion threshold " + std::to_string(mu) + " exceeds chunk size " +
+                                                 std::to_string(chunk));
+  out->ctx = ctx;
+  out->dg = dg;
+  out->n_blocks = nb;
+  out->tmpl_off.assign(tmpl_off, tmpl_off + nb + 1);
+  const int64_t ne = out->tmpl_off[nb];
+  out->tmpl_nodes.assign(tmpl_nodes, tmpl_nodes + ne);
+  // host validation + weight slot order (weight_nodes: sorted by name, search.py:85-88)
+  std::vector<int16_t> slot_of(ne, -1);
+  std::vector<uint8_t> radix_of(ne, 1);
+  out->slot_pos.assign(nb, {});
+  out->hdr.assign(nb, BlobHeader{});
+  out->overflow = false;
+  out->max_T = 0;
+  const uint8_t* names = dg->h_names.data();
+  const int64_t* noff = dg->h_name_off.data();
+  for (int64_t b = 0; b < nb; b++) {
+    const int64_t e0 = out->tmpl_off[b], e1 = out->tmpl_off[b + 1];
+    const int64_t T = e1 - e0;
+    if (T < 0) throw Error(SP_ERR_CONFIG, "template offsets must be non-decreasing");
+    if (T > MAXT) throw Error(SP_ERR_UNSUPPORTED, "template with more than 256 nodes");
+    out->max_T = std::max<int32_t>(out->max_T, (int32_t)T);
+    std::vector<int64_t> w;
+    for (int64_t e = e0; e < e1; e++) {
+      const int32_t v = out->tmpl_nodes[e];
+      if (v < 0 || v >= n) throw Error(SP_ERR_CONFIG, "template node index out of range");
+      Pattern pats[4];
+      if (patterns_for(dg->h_op[v], pats) < 0) {
+        static const char* labels[] = {"matmul", "elementwise", "layernorm", "softmax", "embedding",
+                                       "reshape", "input",  "output",    "auxiliary", "collective"};
+        throw Error(SP_ERR_SPEC, std::string(labels[dg->h_op[v] < 10 ? dg->h_op[v] : 9]) +
+                                     " is not a shardable compute kind");
+      }
+      if (dg->h_w_rank[v]) w.push_back(e);
+    }
+    std::sort(w.begin(), w.end(), [&](int64_t a, int64_t c) {
+      const int32_t x = out->tmpl_nodes[a], y = out->tmpl_nodes[c];
+      return strcmp_py(names + noff[x], noff[x + 1] - noff[x], names + noff[y], noff[y + 1] - noff[y]) < 0;
+    });
+    BlobHeader& H = out->hdr[b];
+    H.V = (int32_t)w.size();
+    H.radix3 = 0;
+    unsigned __int128 C = 1;
+    bool over = false;
+    for (size_t sidx = 0; sidx < w.size(); sidx++) {
+      const int64_t e = w[sidx];
+      const int r = dg->h_w_rank[out->tmpl_nodes[e]] >= 2 ? 3 : 2;  // _options (search.py:91-93)
+      slot_of[e] = (int16_t)sidx;
+      radix_of[e] = (uint8_t)r;
+      if (r == 3 && sidx < 64) H.radix3 |= 1ULL << sidx;
+      out->slot_pos[b].push_back((int32_t)(e - e0));
+      C *= (unsigned)r;
+      if (C > (unsigned __int128)UINT64_MAX) over = true;
+    }
+    if (w.size() > 64) over = true;
+    H.C = over ? 0 : (uint64_t)C;
+    if (over) out->overflow = true;
+  }
+  TablesPriv* priv = new TablesPriv();
+  out->priv = priv;
+  priv->mesh = *mesh;
+  priv->mu = mu;
+  priv->chunk = chunk;
+  TableDev& D = priv->dev;
+  out->d_tmpl_off.upload(out->tmpl_off.data(), nb + 1, s);
+  out->d_tmpl_nodes.upload(out->tmpl_nodes.data(), ne, s);
+  D.slot_of.upload(slot_of.data(), ne, s);
+  DevBuf<uint8_t> radix_d;
+  radix_d.upload(radix_of.data(), ne, s);
+  D.node_block.alloc(n, s);
+  D.node_tpos.alloc(n, s);
+  SP_CUDA(cudaMemsetAsync(D.node_block.p, 0xff, n * sizeof(int32_t), s));
+  SP_CUDA(cudaMemsetAsync(D.node_tpos.p, 0xff, n * sizeof(int32_t), s));
+  DevBuf<int32_t> err;
+  err.alloc(2, s);
+  SP_CUDA(cudaMemsetAsync(err.p, 0, 2 * sizeof(int32_t), s));
+  if (nb > 0)
+    k_mark_blocks<<<(int)std::min<int64_t>(nb, 65535), 128, 0, s>>>(out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
+                                                                  D.node_block.p, D.node_tpos.p, err.p);
+  const GraphView G = view_of(dg);
+  D.has_cons.alloc(n, s);
+  D.ext_cons.alloc(n, s);
+  SP_CUDA(cudaMemsetAsync(D.has_cons.p, 0, n, s));
+  SP_CUDA(cudaMemsetAsync(D.ext_cons.p, 0, n, s));
+  k_boundary<<<grid_for(n, ctx->sm_count), 256, 0, s>>>(G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
+  DevBuf<int32_t> lastuse;
+  DevBuf<EntryLayout> lay;
+  DevBuf<BlobHeader> hdr;
+  DevBuf<int64_t> blob_bytes, blob_off;
+  lastuse.alloc(ne, s);
+  lay.alloc(ne, s);
+  hdr.upload(out->hdr.data(), nb, s);
+  blob_bytes.alloc(nb + 1, s);
+  blob_off.alloc(nb + 1, s);
+  SP_CUDA(cudaMemsetAsync(blob_bytes.p, 0, (nb + 1) * sizeof(int64_t), s));
+  if (nb > 0)
+    k_layout<<<grid_for(nb, ctx->sm_count, 64), 64, 0, s>>>(G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
+                                                           D.node_block.p, D.node_tpos.p, D.slot_of.p, radix_d.p,
+                                                           lastuse.p, lay.p, hdr.p, blob_bytes.p, err.p);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, blob_bytes.p, blob_off.p, (int)(nb + 1), s);
+  ctx->cub_tmp.alloc(tb, s);
+  tb = ctx->cub_tmp.n;
+  SP_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tb, blob_bytes.p, blob_off.p, (int)(nb + 1), s));
+  int32_t err_h[2];
+  out->blob_off.resize(nb + 1);
+  err.download(err_h, 2, s);
+  blob_off.download(out->blob_off.data(), nb + 1, s);
+  hdr.download(out->hdr.data(), nb, s);
+  SP_CUDA(cudaStreamSynchronize(s));
+  if (err_h[0] == 1) throw Error(SP_ERR_CONFIG, "a node appears in more than one template");
+  if (err_h[0] == 2) throw Error(SP_ERR_CONFIG, "template is not in topological order");
+  if (err_h[0] == 3)
+    throw Error(SP_ERR_UNSUPPORTED, "a template node has more than 6 internal producers");
+  out->max_blob = 0;
+  out->max_pool = 0;
+  for (int64_t b = 0; b < nb; b++) {
+    out->max_blob = std::max<int64_t>(out->max_blob, out->hdr[b].bytes);
+    out->max_pool = std::max(out->max_pool, out->hdr[b].npool);
+  }
+  out->blobs.alloc(std::max<int64_t>(out->blob_off[nb], 16), s);
+  D.bound.alloc(ne, s);
+  out->d_blob_off.upload(out->blob_off.data(), nb + 1, s);
+  if (ne > 0)
+    k_fill<<<grid_for(ne, ctx->sm_count, 64), 64, 0, s>>>(G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, ne,
+                                                        D.node_block.p, D.node_tpos.p, D.slot_of.p, lay.p, hdr.p,
+                                                        out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
+                                                        chunk, out->blobs.p, D.bound.p);
+  SP_CUDA(cudaGetLastError());
+  SP_CUDA(cudaStreamSynchronize(s));
+  // refresh host headers with the device-computed constants
+  for (int64_t b = 0; b < nb; b++)
+    SP_CUDA(cudaMemcpyAsync(&out->hdr[b], out->blobs.p + out->blob_off[b], sizeof(BlobHeader),
+                            cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+}
+
+static size_t score_smem(const sp_tables* t) {
+  return (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_pool * THREADS * 9 + 16;
+}
+
+static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long long>& lo,
+                      const std::vector<unsigned long long>& hi, double* d_totals, std::vector<sp_score_out>& res) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nb = t->n_blocks;
+  std::vector<unsigned long long> base(nb + 1, 0);
+  for (int64_t b = 0; b < nb; b++) {
+    const unsigned long long c = hi[b] > lo[b] ? hi[b] - lo[b] : 0;
+    base[b + 1] = base[b] + (c + ITEM_CANDS - 1) / ITEM_CANDS;
+  }
+  const unsigned long long n_items = base[nb];
+  res.assign(nb, sp_score_out{});
+  if (n_items == 0) return;
+  const size_t smem = score_smem(t);
+  if (smem > ctx->smem_optin)
+    throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
+  DevBuf<unsigned long long> dlo, dhi, dbase, counter;
+  DevBuf<ItemOut> items;
+  DevBuf<sp_score_out> dout;
+  dlo.upload(lo.data(), nb, s);
+  dhi.upload(hi.data(), nb, s);
+  dbase.upload(base.data(), nb + 1, s);
+  counter.alloc(1, s);
+  SP_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), s));
+  items.alloc(n_items, s);
+  dout.alloc(nb, s);
+  ScorePlan P{t->d_blob_off.p, nullptr, dlo.p, dhi.p, dbase.p, nb, n_items};
+  SP_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score, THREADS, smem));
+  if (per_sm < 1) per_sm = 1;
+  const unsigned long long grid = std::min<unsigned long long>(n_items, (unsigned long long)ctx->sm_count * per_sm);
+  SP_CUDA(cudaEventRecord(ctx->ev[2], s));
+  k_score<<<(unsigned)grid, THREADS, smem, s>>>(t->blobs.p, P, items.p, counter.p, d_totals);
+  SP_CUDA(cudaEventRecord(ctx->ev[3], s));
+  k_reduce<<<(unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s>>>(items.p, dbase.p, nb, dout.p);
+  SP_CUDA(cudaGetLastError());
+  dout.download(res.data(), nb, s);
+  SP_CUDA(cudaStreamSynchronize(s));
+  float ms = 0;
+  SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+  ctx->score_kernel_ms = ms;
+}
+
+void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out) {
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) throw Error(SP_ERR_CONFIG, "bad shard / n_shards");
+  if (t->overflow) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
+  const int64_t nb = t->n_blocks;
+  std::vector<unsigned long long> lo(nb), hi(nb);
+  for (int64_t b = 0; b < nb; b++) {
+    const unsigned long long C = t->hdr[b].C;
+    // contiguous split like search_subgraph's pool ranges (search.py:331-336)
+    const unsigned long long step = C / (unsigned long long)n_shards + (C % (unsigned long long)n_shards ? 1 : 0);
+    const unsigned __int128 l = (unsigned __int128)step * (unsigned)shard;
+    lo[b] = l > C ? C : (unsigned long long)l;
+    hi[b] = (unsigned __int128)lo[b] + step > C ? C : lo[b] + step;
+  }
+  SP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  std::vector<sp_score_out> res;
+  run_score(ctx, t, lo, hi, nullptr, res);
+  SP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  SP_CUDA(cudaEventSynchronize(ctx->ev[1]));
+  float ms = 0;
+  SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+  ctx->score_ms = ms;
+  for (int64_t b = 0; b < nb; b++) {
+    out[b] = res.empty() ? sp_score_out{} : res[b];
+    out[b].candidates = t->hdr[b].C;
+  }
+}
+
+void score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi, double* totals,
+                 sp_score_out* out) {
+  if (block < 0 || block >= t->n_blocks) throw Error(SP_ERR_CONFIG, "block index out of range");
+  const BlobHeader& H = t->hdr[block];
+  if (H.C == 0) throw Error(SP_ERR_UNSUPPORTED, "block has more than 2**64 candidates");
+  if (hi > H.C) hi = H.C;
+  if (lo > hi) lo = hi;
+  const int64_t nb = t->n_blocks;
+  std::vector<unsigned long long> l(nb, 0), h(nb, 0);
+  l[block] = lo;
+  h[block] = hi;
+  DevBuf<double> dt;
+  if (totals && hi > lo) dt.alloc(hi - lo, ctx->stream);
+  std::vector<sp_score_out> res;
+  run_score(ctx, t, l, h, totals && hi > lo ? dt.p : nullptr, res);
+  *out = res.empty() ? sp_score_out{} : res[block];
+  out->candidates = H.C;
+  if (totals && hi > lo) {
+    dt.download(totals, hi - lo, ctx->stream);
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+}
+
+void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explain_out* out, sp_edge_conv* edges,
+             int32_t max_edges, int32_t* n_edges) {
+  if (block < 0 || block >= t->n_blocks) throw Error(SP_ERR_CONFIG, "block index out of range");
+  cudaStream_t s = ctx->stream;
+  const BlobHeader& H = t->hdr[block];
+  if (H.C == 0) throw Error(SP_ERR_UNSUPPORTED, "block has more than 2**64 candidates");
+  if (index >= H.C) throw Error(SP_ERR_CONFIG, "candidate index out of range");
+  const int V = H.V;
+  std::vector<uint8_t> digits(std::max(V, 1), 0);
+  uint64_t rem = index;
+  for (int sidx = V - 1; sidx >= 0; sidx--) {
+    const uint64_t r = ((H.radix3 >> sidx) & 1) ? 3 : 2;
+    digits[sidx] = (uint8_t)(rem % r);
+    rem /= r;
+  }
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  const int64_t e0 = t->tmpl_off[block];
+  const int T = (int)(t->tmpl_off[block + 1] - e0);
+  DevBuf<uint8_t> ddig;
+  ddig.upload(digits.data(), digits.size(), s);
+  DevBuf<sp_explain_out> dout;
+  DevBuf<sp_edge_conv> dedges;
+  DevBuf<int32_t> dne;
+  dout.alloc(1, s);
+  dedges.alloc(std::max(max_edges, 1), s);
+  dne.alloc(1, s);
+  k_explain<<<1, 1, 0, s>>>(view_of(t->dg), t->d_tmpl_nodes.p + e0, T, (int32_t)block, priv->dev.node_block.p,
+                            priv->dev.node_tpos.p, priv->dev.slot_of.p + e0, ddig.p, priv->dev.bound.p + e0, priv->mesh, priv->mu,
+                            priv->chunk, dout.p, dedges.p, max_edges, dne.p);
+  SP_CUDA(cudaGetLastError());
+  dout.download(out, 1, s);
+  int32_t ne = 0;
+  dne.download(&ne, 1, s);
+  SP_CUDA(cudaStreamSynchronize(s));
+  *n_edges = ne;
+  if (edges && ne > 0) {
+    dedges.download(edges, std::min(ne, max_edges), s);
+    SP_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+void tables_free_priv(sp_tables* t) {
+  delete (TablesPriv*)t->priv;
+  t->priv = nullptr;
+}
+
+void merge_key(sp_score_out* acc, const sp_score_out* o) {
+  acc->valid += o->valid;
+  if (!o->has_best) return;
+  bool take = !acc->has_best;
+  if (!take) {
+    if (o->best_total != acc->best_total) take = o->best_total < acc->best_total;
+    else if (o->best_num_split != acc->best_num_split) take = o->best_num_split < acc->best_num_split;
+    else take = o->best_index < acc->best_index;
+  }
+  if (take) {
+    acc->has_best = 1;
+    acc->best_total = o->best_total;
+    acc->best_num_split = o->best_num_split;
+    acc->best_index = o->best_index;
+  }
+}
+
+}  // namespace sp

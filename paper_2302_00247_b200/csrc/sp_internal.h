@@ -1,0 +1,172 @@
+// Internal declarations shared by the backend translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/shardsearch.h"
+
+namespace sp {
+
+// Error carrying an sp_status code; converted at the C boundary (capi.cu).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SP_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::sp::Error(SP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Owning device allocation (cudaMallocAsync on the context stream).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count, cudaStream_t stream) {
+    if (count <= n && p) return;
+    release();
+    s = stream;
+    n = count;
+    SP_CUDA(cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), stream));
+  }
+  void upload(const T* h, size_t count, cudaStream_t stream) {
+    alloc(count, stream);
+    if (count) SP_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, stream));
+  }
+  void download(T* h, size_t count, cudaStream_t stream) const {
+    if (count) SP_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, stream));
+  }
+  void zero(cudaStream_t stream) {
+    if (n) SP_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), stream));
+  }
+};
+
+}  // namespace sp
+
+struct sp_ctx {
+  int device = 0;
+  int sm_count = 148;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  std::string last_error;
+  double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;
+  // scratch reused across calls
+  sp::DevBuf<uint8_t> cub_tmp;
+};
+
+// Device-resident lowered graph (+ the host copies the library needs).
+struct sp_dgraph {
+  sp_ctx* ctx = nullptr;
+  int64_t n = 0, E = 0;
+  int32_t max_depth = 1;
+  // host copies
+  std::vector<uint8_t> h_names;
+  std::vector<int64_t> h_name_off, h_topo;
+  std::vector<uint8_t> h_op, h_act_rank, h_w_rank, h_w_train;
+  std::vector<int64_t> h_act_shape, h_act_bytes, h_w_shape, h_w_bytes, h_in_off;
+  std::vector<int32_t> h_in_idx;
+  // device copies
+  sp::DevBuf<uint8_t> names, op, act_rank, w_rank, w_train;
+  sp::DevBuf<int64_t> name_off, topo, act_shape, act_bytes, w_shape, w_bytes, in_off;
+  sp::DevBuf<int32_t> in_idx;
+};
+
+struct sp_fold {
+  std::vector<int64_t> block_T, block_inst_off, block_member_off, inst_prefix_node, inst_prefix_len;
+  std::vector<int32_t> members;
+  sp_blocks view{};
+};
+
+// One block's table blob header (lives at the start of each blob in HBM and smem).
+struct BlobHeader {
+  uint64_t C;             // candidate count
+  uint64_t radix3;        // bit s set: slot s has 3 options, else 2
+  int32_t T, V, nt, npool;
+  int32_t desc_off, prod_off, tab_off, dbl_off;  // byte offsets from blob start
+  int32_t train_off, bytes, multi_dev, pad0;      // multi_dev: device_count > 1
+  double setup, c_ar, bw, eff_ar, keep_bwd;       // keep_bwd = 1.0 - overlap_fraction
+  int64_t mu, chunk, pad1;
+};
+static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
+
+struct NodeDesc {
+  int16_t slot;      // weight slot or -1
+  uint8_t k;         // internal producers
+  uint8_t nd;        // digit options (1 when unweighted)
+  int16_t out_pool;  // pool slot receiving reach/state, -1 when no internal consumer
+  uint16_t prod;     // index of first producer pool slot (int16 array)
+  uint32_t tab;      // entry table byte offset within the entry section
+  uint32_t dbl;      // double offset within the double section (own[4], exitc[4], conv[k][4][3])
+};
+static_assert(sizeof(NodeDesc) == 16, "NodeDesc is one 16-byte smem load");
+
+struct TrainDesc {
+  int32_t slot;
+  int32_t pad;
+  int64_t size;
+  double uterm;  // setup + AR(size) for an unfused gradient
+};
+
+struct sp_tables {
+  sp_ctx* ctx = nullptr;
+  int64_t n_blocks = 0;
+  std::vector<BlobHeader> hdr;           // host copy of every block header
+  std::vector<int64_t> blob_off;         // byte offset of each block blob
+  std::vector<std::vector<int32_t>> slot_pos;  // weight slot -> template position
+  std::vector<int64_t> tmpl_off;
+  std::vector<int32_t> tmpl_nodes;
+  int64_t max_blob = 0;
+  int32_t max_pool = 0;
+  int32_t max_T = 0;
+  bool overflow = false;                 // some block has > 2^64 candidates
+  sp::DevBuf<uint8_t> blobs;
+  sp::DevBuf<int64_t> d_blob_off;
+  sp::DevBuf<int32_t> d_tmpl_nodes;
+  sp::DevBuf<int64_t> d_tmpl_off;
+  sp_dgraph* dg = nullptr;
+  void* priv = nullptr;  // sp::TablesPriv (device maps used by explain)
+};
+
+namespace sp {
+void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg);
+void fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold* out);
+void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* tmpl_off,
+                  const int32_t* tmpl_nodes, const sp_mesh* mesh, int64_t mu, int64_t chunk,
+                  sp_tables* out);
+void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out);
+void score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi,
+                 double* totals, sp_score_out* out);
+void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explain_out* out,
+             sp_edge_conv* edges, int32_t max_edges, int32_t* n_edges);
+void merge_key(sp_score_out* acc, const sp_score_out* o);
+void tables_free_priv(sp_tables* t);
+}  // namespace sp

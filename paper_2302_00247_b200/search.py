@@ -1,0 +1,305 @@
+"""Drop-in ``prune_graph`` / ``search_subgraph`` / ``derive_plan`` on the B200 backend.
+
+Same names, arguments and results as the reference (pruning.py:123-201,
+search.py:85-116, 317-379); the work runs in the sm_100a kernels behind
+``include/shardsearch.h``:
+
+* folding          -> ``sp_fold_run``   (device hashing / radix sort / verify)
+* candidate search -> ``sp_tables_build`` + ``sp_score`` (batched over all
+  blocks in one launch; exact (total, num_split, index) argmin + valid count)
+* winner detail    -> ``sp_explain`` (device re-route of the argmin only), from
+  which RoutedPlan / CostReport are assembled exactly as the reference's.
+
+``jobs`` is accepted for signature compatibility; the GPU is the parallel
+resource (multi-GPU sharding lives in ``paper_2302_00247_b200.dist``).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from ._native import Backend, default_backend
+from .api_types import DEFAULT_TYPES, TypeSet
+from .blocks import BlockArrays, prefix_of
+from .errors import BackendError, BadConfig, UnsupportedSearch
+from .lowering import LoweredGraph, lower
+
+_KIND_LABEL = {1: "allreduce", 2: "allgather", 3: "reducescatter", 4: "alltoall"}
+
+
+@dataclass
+class Session:
+    """A graph resident on one device: lowered arrays + device handle."""
+
+    backend: Backend
+    low: LoweredGraph
+    dgraph: object
+
+    @classmethod
+    def open(cls, graph, backend: Optional[Backend] = None, cache: bool = True) -> "Session":
+        backend = backend or default_backend()
+        if isinstance(graph, LoweredGraph):
+            low = graph
+        else:
+            low = lower(graph) if cache else lower(_Uncached(graph))
+        if cache:
+            d = getattr(low, "_sp_dgraph", None)
+            if d is not None and d.backend is backend and d.ptr:
+                return cls(backend, low, d)
+        d = backend.upload(low)
+        if cache:
+            low._sp_dgraph = d  # type: ignore[attr-defined]
+        return cls(backend, low, d)
+
+
+class _Uncached:
+    """Wrapper that hides a graph's cached lowering (forces a fresh lower())."""
+
+    def __init__(self, g):
+        self.nodes = g.nodes
+        self.topo_order = g.topo_order
+
+
+# ---------------------------------------------------------------------------
+# folding
+
+
+def subgraphs_from_blocks(low: LoweredGraph, ba: BlockArrays, types: TypeSet = DEFAULT_TYPES) -> list:
+    names = low.names
+    subs = []
+    for b in range(ba.n_blocks):
+        T = int(ba.block_T[b])
+        i0, i1 = int(ba.block_inst_off[b]), int(ba.block_inst_off[b + 1])
+        mo = int(ba.block_member_off[b])
+        mem = ba.members
+        insts = []
+        for r, j in enumerate(range(i0, i1)):
+            pre = prefix_of(low, int(ba.inst_prefix_node[j]), int(ba.inst_prefix_len[j]))
+            insts.append((pre, tuple(names[x] for x in mem[mo + r * T: mo + (r + 1) * T].tolist())))
+        subs.append(types.Subgraph(insts[0][0], insts[0][1], tuple(insts)))
+    return subs
+
+
+def prune_graph(graph, min_duplicates: int, *, backend: Optional[Backend] = None,
+                types: TypeSet = DEFAULT_TYPES, session: Optional[Session] = None) -> list:
+    """Partition GraphNodes into shared subgraphs plus residuals (pruning.py:123-201)."""
+    if min_duplicates < 1:
+        raise BadConfig("min_duplicates must be >= 1")
+    ses = session or Session.open(graph, backend)
+    ba = ses.backend.fold(ses.dgraph, int(min_duplicates))
+    return subgraphs_from_blocks(ses.low, ba, types)
+
+
+def fold_blocks(graph, min_duplicates: int, session: Optional[Session] = None) -> BlockArrays:
+    """Folding result as flat arrays (no Python Subgraph objects)."""
+    if min_duplicates < 1:
+        raise BadConfig("min_duplicates must be >= 1")
+    ses = session or Session.open(graph)
+    return ses.backend.fold(ses.dgraph, int(min_duplicates))
+
+
+# ---------------------------------------------------------------------------
+# enumeration helpers (search.py:85-116) -- host metadata only
+
+
+def weight_nodes(graph, subgraph) -> tuple:
+    return tuple(s for s in sorted(subgraph.template) if graph.nodes[s].weight is not None)
+
+
+def count_candidates(graph, subgraph) -> int:
+    total = 1
+    for s in weight_nodes(graph, subgraph):
+        total *= 3 if graph.nodes[s].weight.rank >= 2 else 2
+    return total
+
+
+def _digits(index: int, radices: list) -> list:
+    out = [0] * len(radices)
+    for i in range(len(radices) - 1, -1, -1):
+        index, out[i] = divmod(index, radices[i])
+    return out
+
+
+def _spec_for_digit(types: TypeSet, digit: int):
+    if digit == 0:
+        return types.ShardSpec(types.ShardKind.REPLICA)
+    return types.ShardSpec(types.ShardKind.SPLIT, digit - 1)
+
+
+def candidate_by_index(graph, subgraph, index: int, types: TypeSet = DEFAULT_TYPES):
+    scopes = weight_nodes(graph, subgraph)
+    radices = [3 if graph.nodes[s].weight.rank >= 2 else 2 for s in scopes]
+    digits = _digits(index, radices)
+    return types.CandidatePlan(
+        subgraph, tuple((s, _spec_for_digit(types, d)) for s, d in zip(scopes, digits)), index)
+
+
+# ---------------------------------------------------------------------------
+# search
+
+
+def _templates_csr(low: LoweredGraph, subgraphs: list):
+    idx = low.index
+    off = np.zeros(len(subgraphs) + 1, np.int64)
+    nodes = []
+    for b, sub in enumerate(subgraphs):
+        nodes.extend(idx[s] for s in sub.template)
+        off[b + 1] = len(nodes)
+    return off, np.asarray(nodes, dtype=np.int32)
+
+
+def _flops(low: LoweredGraph, tnodes) -> int:
+    total = 0
+    for v in tnodes:
+        if low.op[v] == 0 and low.w_rank[v]:  # matmul with weight (costmodel.py:185-190)
+            r = int(low.act_rank[v])
+            total += 2 * math.prod(int(x) for x in low.act_shape[v, :r]) * int(low.w_shape[v, 0])
+    return total
+
+
+def _collective(types: TypeSet, kind: int, axis: int):
+    ck = types.CollectiveKind(_KIND_LABEL[kind])
+    return types.Collective(ck, None if kind == 1 else int(axis))
+
+
+def routed_plan(ses: Session, tables, b: int, sub, index: int, mesh, types: TypeSet = DEFAULT_TYPES,
+                expect_total: Optional[float] = None):
+    """RoutedPlan + CostReport of candidate `index` of block `b`, from sp_explain."""
+    low = ses.low
+    ex, edges = ses.backend.explain(tables, b, index)
+    if not ex.valid:
+        return None
+    tnodes = [low.index[s] for s in sub.template]
+    T = len(tnodes)
+    slot_pos = ses.backend.slots(tables, b)
+    radices = [3 if low.w_rank[tnodes[p]] >= 2 else 2 for p in slot_pos]
+    digits = _digits(index, radices)
+    assignments = tuple((sub.template[p], _spec_for_digit(types, d)) for p, d in zip(slot_pos, digits))
+    plan = types.CandidatePlan(sub, assignments, index)
+    by_consumer: dict = {}
+    for e in edges:
+        by_consumer.setdefault(e.consumer_pos, []).append(e)
+    replica = types.ShardSpec(types.ShardKind.REPLICA)
+    identity = types.Collective(types.CollectiveKind.IDENTITY)
+    routings = []
+    exits = []
+    for i in range(T):
+        v = tnodes[i]
+        op_label = _OP_LABELS[int(low.op[v])]
+        pidx = int(ex.pattern[i])
+        convs = tuple(
+            (sub.template[e.producer_pos], _collective(types, e.kind, e.axis),
+             int(low.act_bytes[tnodes[e.producer_pos]]))
+            for e in by_consumer.get(i, ()))
+        out_coll = (types.Collective(types.CollectiveKind.ALL_REDUCE_SUM)
+                    if types.pattern_collectives[op_label][pidx] == "allreduce" else identity)
+        ax = int(ex.state_axis[i])
+        state = replica if ax < 0 else types.ShardSpec(types.ShardKind.SPLIT, ax)
+        routings.append(types.NodeRouting(sub.template[i], types.pattern_names[op_label][pidx], convs,
+                                          out_coll, int(low.act_bytes[v]), state))
+        if ex.exit_axis[i] >= 0:
+            exits.append((sub.template[i], _collective(types, 2, ex.exit_axis[i]),
+                          int(low.act_bytes[v])))
+    bbc = {}
+    for kind, b_, c_ in ((1, ex.bytes_allreduce, ex.calls_allreduce),
+                         (2, ex.bytes_allgather, ex.calls_allgather),
+                         (3, ex.bytes_reducescatter, ex.calls_reducescatter),
+                         (4, ex.bytes_alltoall, ex.calls_alltoall)):
+        if c_:
+            bbc[_KIND_LABEL[kind]] = int(b_)
+    cost = types.CostReport(forward_comm=ex.forward_comm, backward_comm=ex.backward_comm,
+                            overlap_fraction=mesh.overlap_fraction, bytes_by_collective=bbc,
+                            collective_calls=int(ex.collective_calls), flops=_flops(low, tnodes))
+    if expect_total is not None and cost.total != expect_total:
+        raise BackendError(
+            f"explain/score disagree on block {b} index {index}: {cost.total!r} != {expect_total!r}")
+    return types.RoutedPlan(plan, tuple(routings), tuple(exits), cost)
+
+
+_OP_LABELS = ("matmul", "elementwise", "layernorm", "softmax", "embedding", "reshape", "input",
+              "output", "auxiliary", "collective")
+
+
+def _labels(assignments) -> dict:
+    return {s: spec.label for s, spec in assignments}
+
+
+def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
+                  want_table: bool = False, *, session: Optional[Session] = None,
+                  types: TypeSet = DEFAULT_TYPES, shard: int = 0, n_shards: int = 1,
+                  exchange: Optional[Callable] = None) -> list:
+    """Score every candidate of every block in one batched launch; returns
+    SubgraphResult per block (search_subgraph semantics, search.py:317-345)."""
+    ses = session or Session.open(graph)
+    if not subgraphs:
+        return []
+    off, nodes = _templates_csr(ses.low, subgraphs)
+    # pack_gradients raises BadConfig for mu > chunk only once a candidate is
+    # costed; build with a legal chunk to learn which error the reference hits first
+    bad_mu = mu > chunk_size
+    tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, chunk_size if not bad_mu else mu)
+    try:
+        if tables.overflow:
+            raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")
+        scores = ses.backend.score(tables, shard, n_shards)
+        if exchange is not None:
+            scores = exchange(scores)
+        results = []
+        for b, (sub, sc) in enumerate(zip(subgraphs, scores)):
+            if not sc.has_best:
+                raise AssertionError("all-replica fallback must always route")
+            if bad_mu:
+                raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
+            best = routed_plan(ses, tables, b, sub, int(sc.best_index), mesh, types,
+                               expect_total=sc.best_total)
+            table = []
+            if want_table:
+                C = int(sc.candidates)
+                _, totals = ses.backend.score_range(tables, b, 0, C, want_totals=True)
+                for i in range(C):
+                    t = float(totals[i])
+                    plan = candidate_by_index(graph, sub, i, types)
+                    table.append([i, _labels(plan.assignments), None if math.isnan(t) else t])
+            results.append(types.SubgraphResult(sub, best, int(sc.candidates), int(sc.valid), table))
+        return results
+    finally:
+        tables.close()
+
+
+def search_subgraph(graph, subgraph, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
+                    jobs: int = 1, want_table: bool = False, *, types: TypeSet = DEFAULT_TYPES,
+                    session: Optional[Session] = None):
+    """Exhaustive argmin over one block's candidates (search.py:317-345)."""
+    del jobs
+    return search_blocks(graph, [subgraph], mesh, mu, chunk_size, want_table, session=session,
+                         types=types)[0]
+
+
+def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
+                chunk_size: int = 4 << 20, jobs: int = 1, want_table: bool = False, *,
+                types: TypeSet = DEFAULT_TYPES, backend: Optional[Backend] = None,
+                session: Optional[Session] = None, cache: bool = True,
+                shard: int = 0, n_shards: int = 1, exchange: Optional[Callable] = None):
+    """Prune, search every unique block, assemble the whole-graph plan (search.py:348-379)."""
+    del jobs
+    ses = session or Session.open(graph, backend, cache=cache)
+    subs = prune_graph(graph, min_duplicates, types=types, session=ses)
+    results = search_blocks(graph, subs, mesh, mu, chunk_size, want_table, session=ses,
+                            types=types, shard=shard, n_shards=n_shards, exchange=exchange)
+    assignments: dict = {}
+    total_cost = 0.0
+    candidates = 0
+    valid = 0
+    for sub, res in zip(subs, results):
+        candidates += res.candidates
+        valid += res.valid
+        total_cost += res.best.cost.total * sub.multiplicity
+        for prefix, _ in sub.instances:
+            for scope, spec in res.best.plan.assignments:
+                assignments[sub.instance_node(prefix, scope)] = spec.label
+    return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates,
+                                valid)

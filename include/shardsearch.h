@@ -168,6 +168,8 @@ int sp_tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t*
 void sp_tables_free(sp_tables* t);
 /* count_candidates per block; returns SP_ERR_UNSUPPORTED if one exceeds u64. */
 int sp_tables_candidates(const sp_tables* t, uint64_t* out);
+/* Total bytes of the device routing tables (all blocks). */
+int sp_tables_bytes(const sp_tables* t, int64_t* bytes);
 /* Weight slot order of a block (weight_nodes, search.py:85-88): template positions. */
 int sp_tables_slots(const sp_tables* t, int64_t block, int32_t* slot_pos, int32_t* n_slots);
 
@@ -189,6 +191,14 @@ int sp_explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_expl
 
 /* Device time (ms) of the last sp_score / sp_fold_run kernels (CUDA events). */
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms);
+
+/* CUDA-event timer on the context's stream (brackets whole API calls for benchmarks). */
+int sp_timer_start(sp_ctx* ctx);
+int sp_timer_stop(sp_ctx* ctx, double* ms);
+/* Kernel launches issued by this library since context creation: own kernels and CUB calls. */
+int sp_launch_counts(const sp_ctx* ctx, int64_t* own_kernels, int64_t* cub_calls);
+/* Host<->device bytes copied by the library in this process (all contexts). */
+int sp_copy_bytes(int64_t* h2d, int64_t* d2h);
 
 #ifdef __cplusplus
 }

@@ -50,7 +50,12 @@ def _declare(L):
                              C.POINTER(SpEdgeConv), C.c_int32, C.POINTER(C.c_int32)]
     L.sp_last_timings.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_double)]
-    for name in ("sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
+    L.sp_timer_start.argtypes = [vp]
+    L.sp_timer_stop.argtypes = [vp, C.POINTER(C.c_double)]
+    L.sp_launch_counts.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.sp_tables_bytes.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.sp_copy_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    for name in ("sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
                  "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
                  "sp_score_range", "sp_explain", "sp_last_timings"):
         getattr(L, name).restype = C.c_int
@@ -78,7 +83,8 @@ EXPORTED_SYMBOLS = (
     "sp_abi_version", "sp_ctx_create", "sp_ctx_destroy", "sp_last_error", "sp_graph_upload",
     "sp_graph_free", "sp_fold_run", "sp_fold_view", "sp_fold_free", "sp_tables_build",
     "sp_tables_free", "sp_tables_candidates", "sp_tables_slots", "sp_score", "sp_score_range",
-    "sp_merge_keys", "sp_explain", "sp_last_timings",
+    "sp_merge_keys", "sp_explain", "sp_last_timings", "sp_timer_start", "sp_timer_stop",
+    "sp_launch_counts", "sp_copy_bytes", "sp_tables_bytes",
 )
 
 
@@ -169,6 +175,9 @@ class Backend:
         rc = self.lib.sp_tables_candidates(h, ptr(cands, C.c_uint64))
         t.overflow = rc == _abi.SP_ERR_UNSUPPORTED
         t.candidates = cands[:nb]
+        nbytes = C.c_int64()
+        self.lib.sp_tables_bytes(h, C.byref(nbytes))
+        t.nbytes = nbytes.value
         return t
 
     def slots(self, t: Tables, block: int) -> list:
@@ -209,6 +218,24 @@ class Backend:
         f, s, k = C.c_double(), C.c_double(), C.c_double()
         self.lib.sp_last_timings(self.ctx, C.byref(f), C.byref(s), C.byref(k))
         return {"fold_ms": f.value, "score_ms": s.value, "score_kernel_ms": k.value}
+
+    def timer_start(self):
+        self._check(self.lib.sp_timer_start(self.ctx), "sp_timer_start")
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        self._check(self.lib.sp_timer_stop(self.ctx, C.byref(ms)), "sp_timer_stop")
+        return ms.value
+
+    def launch_counts(self) -> tuple:
+        a, b = C.c_int64(), C.c_int64()
+        self.lib.sp_launch_counts(self.ctx, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def copy_bytes(self) -> tuple:
+        a, b = C.c_int64(), C.c_int64()
+        self.lib.sp_copy_bytes(C.byref(a), C.byref(b))
+        return a.value, b.value
 
     def close(self):
         if self.ctx:

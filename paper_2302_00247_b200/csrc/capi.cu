@@ -43,6 +43,7 @@ int sp_ctx_create(int device, sp_ctx** out) {
     ctx->smem_optin = (size_t)optin;
     SP_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     for (auto& e : ctx->ev) SP_CUDA(cudaEventCreate(&e));
+    for (auto& e : ctx->timer) SP_CUDA(cudaEventCreate(&e));
   });
   if (rc != SP_OK) {
     std::fprintf(stderr, "sp_ctx_create: %s\n", ctx->last_error.c_str());
@@ -59,6 +60,8 @@ void sp_ctx_destroy(sp_ctx* ctx) {
   ctx->cub_tmp.release();
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->timer)
     if (e) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -157,6 +160,12 @@ int sp_tables_candidates(const sp_tables* t, uint64_t* out) {
   return t->overflow ? SP_ERR_UNSUPPORTED : SP_OK;
 }
 
+int sp_tables_bytes(const sp_tables* t, int64_t* bytes) {
+  if (!t || !bytes) return SP_ERR_CONFIG;
+  *bytes = t->blob_off.empty() ? 0 : t->blob_off.back();
+  return SP_OK;
+}
+
 int sp_tables_slots(const sp_tables* t, int64_t block, int32_t* slot_pos, int32_t* n_slots) {
   if (!t || block < 0 || block >= t->n_blocks || !n_slots) return SP_ERR_CONFIG;
   const auto& v = t->slot_pos[block];
@@ -201,6 +210,39 @@ int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double
   if (fold_ms) *fold_ms = ctx->fold_ms;
   if (score_ms) *score_ms = ctx->score_ms;
   if (score_kernel_ms) *score_kernel_ms = ctx->score_kernel_ms;
+  return SP_OK;
+}
+
+int sp_timer_start(sp_ctx* ctx) {
+  if (!ctx) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    SP_CUDA(cudaEventRecord(ctx->timer[0], ctx->stream));
+  });
+}
+
+int sp_timer_stop(sp_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    SP_CUDA(cudaEventRecord(ctx->timer[1], ctx->stream));
+    SP_CUDA(cudaEventSynchronize(ctx->timer[1]));
+    float f = 0;
+    SP_CUDA(cudaEventElapsedTime(&f, ctx->timer[0], ctx->timer[1]));
+    *ms = f;
+  });
+}
+
+int sp_copy_bytes(int64_t* h2d, int64_t* d2h) {
+  if (h2d) *h2d = sp::g_h2d_bytes.load();
+  if (d2h) *d2h = sp::g_d2h_bytes.load();
+  return SP_OK;
+}
+
+int sp_launch_counts(const sp_ctx* ctx, int64_t* own_kernels, int64_t* cub_calls) {
+  if (!ctx) return SP_ERR_CONFIG;
+  if (own_kernels) *own_kernels = ctx->own_launches;
+  if (cub_calls) *cub_calls = ctx->cub_calls;
   return SP_OK;
 }
 

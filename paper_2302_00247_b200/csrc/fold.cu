@@ -479,8 +479,8 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   gaccept.alloc(n, s);
 
   SP_CUDA(cudaMemsetAsync(maxd.p, 0, sizeof(int32_t), s));
-  k_depth<<<grid_for(n, sms), 256, 0, s>>>(dg->name_off.p, dg->names.p, n, depth.p, maxd.p);
-  k_name_hash<<<grid_for(n, sms), 128, 0, s>>>(dg->name_off.p, dg->names.p, n, D, seed, pend.p, ph.p, rh.p);
+  SP_LAUNCH(ctx, k_depth, grid_for(n, sms), 256, 0, s, dg->name_off.p, dg->names.p, n, depth.p, maxd.p);
+  SP_LAUNCH(ctx, k_name_hash, grid_for(n, sms), 128, 0, s, dg->name_off.p, dg->names.p, n, D, seed, pend.p, ph.p, rh.p);
   SP_CUDA(cudaMemsetAsync(gparent.p, 0, n * sizeof(int32_t), s));
   SP_CUDA(cudaMemsetAsync(residual.p, 0, n, s));
   SP_CUDA(cudaMemsetAsync(collision.p, 0, sizeof(int32_t), s));
@@ -511,49 +511,57 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     const int32_t dd = level - 1;
     const int g1 = grid_for(nA, sms);
     // 1. sort active nodes by (prefix hash, rel hash): rel first, then prefix (stable LSD)
-    k_gather_keys<<<g1, 256, 0, s>>>(act.p, nA, rh.p, D, dd, k2.p);
+    SP_LAUNCH(ctx, k_gather_keys, g1, 256, 0, s, act.p, nA, rh.p, D, dd, k2.p);
     t = tmp_bytes;
+    ctx->cub_calls++;
     SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, k2.p, k2s.p, act.p, sorted1.p, (int)nA, 0, 64, s));
-    k_gather_keys<<<g1, 256, 0, s>>>(sorted1.p, nA, ph.p, D, dd, k1.p);
+    SP_LAUNCH(ctx, k_gather_keys, g1, 256, 0, s, sorted1.p, nA, ph.p, D, dd, k1.p);
     t = tmp_bytes;
+    ctx->cub_calls++;
     SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, k1.p, k1s.p, sorted1.p, sorted2.p, (int)nA, 0, 64, s));
-    k_heads_u64<<<g1, 256, 0, s>>>(k1s.p, nA, gidv.p);
+    SP_LAUNCH(ctx, k_heads_u64, g1, 256, 0, s, k1s.p, nA, gidv.p);
     t = tmp_bytes;
+    ctx->cub_calls++;
     SP_CUDA(cub::DeviceScan::InclusiveSum(tmp, t, gidv.p, gidv.p, (int)nA, s));
     int32_t nG32 = 0;
+    g_d2h_bytes += 4;
     SP_CUDA(cudaMemcpyAsync(&nG32, gidv.p + nA - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
     const int64_t nG = nG32;
     const int64_t stamp = ((int64_t)level) << 32;
-    k_group_setup<<<g1, 256, 0, s>>>(sorted2.p, gidv.p, nA, stamp, cur.p, gstart.p);
+    SP_LAUNCH(ctx, k_group_setup, g1, 256, 0, s, sorted2.p, gidv.p, nA, stamp, cur.p, gstart.p);
     // 2. entry hashes and group keys
     SP_CUDA(cudaMemsetAsync(gkey.p, 0, nG * sizeof(unsigned long long), s));
-    k_entry<<<g1, 256, 0, s>>>(sorted2.p, gidv.p, nA, gstart.p, cur.p, rh.p, D, dd, dg->op.p, dg->w_rank.p,
+    SP_LAUNCH(ctx, k_entry, g1, 256, 0, s, sorted2.p, gidv.p, nA, gstart.p, cur.p, rh.p, D, dd, dg->op.p, dg->w_rank.p,
                                dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, pos.p, gkey.p);
     // 3. classes: sort groups by (parent, key) -- key first, then parent (stable)
     const int gG = grid_for(nG, sms);
-    k_class_keys<<<gG, 256, 0, s>>>(nG, nA, gstart.p, sorted2.p, gkey.p, gparent.p, ck.p, par.p, corder.p);
+    SP_LAUNCH(ctx, k_class_keys, gG, 256, 0, s, nG, nA, gstart.p, sorted2.p, gkey.p, gparent.p, ck.p, par.p, corder.p);
     t = tmp_bytes;
+    ctx->cub_calls++;
     SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, ck.p, cks.p, corder.p, corder2.p, (int)nG, 0, 64, s));
-    k_gather<uint32_t><<<gG, 256, 0, s>>>(corder2.p, nG, par.p, par2.p);
+    SP_LAUNCH(ctx, k_gather<uint32_t>, gG, 256, 0, s, corder2.p, nG, par.p, par2.p);
     t = tmp_bytes;
+    ctx->cub_calls++;
     SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, par2.p, pars.p, corder2.p, corder3.p, (int)nG, 0, 32, s));
-    k_gather<uint64_t><<<gG, 256, 0, s>>>(corder3.p, nG, ck.p, cks2.p);
-    k_class_heads<<<gG, 256, 0, s>>>(pars.p, cks2.p, nG, cid.p);
+    SP_LAUNCH(ctx, k_gather<uint64_t>, gG, 256, 0, s, corder3.p, nG, ck.p, cks2.p);
+    SP_LAUNCH(ctx, k_class_heads, gG, 256, 0, s, pars.p, cks2.p, nG, cid.p);
     t = tmp_bytes;
+    ctx->cub_calls++;
     SP_CUDA(cub::DeviceScan::InclusiveSum(tmp, t, cid.p, cid.p, (int)nG, s));
     int32_t nC32 = 0;
+    g_d2h_bytes += 4;
     SP_CUDA(cudaMemcpyAsync(&nC32, cid.p + nG - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
     const int64_t nC = nC32;
-    k_class_setup<<<gG, 256, 0, s>>>(corder3.p, cid.p, nG, gclass.p, cstart.p);
+    SP_LAUNCH(ctx, k_class_setup, gG, 256, 0, s, corder3.p, cid.p, nG, gclass.p, cstart.p);
     // 4. exact verification against group and class heads
-    k_verify<<<g1, 128, 0, s>>>(sorted2.p, gidv.p, nA, nG, gstart.p, gclass.p, cstart.p, corder3.p, cur.p,
+    SP_LAUNCH(ctx, k_verify, g1, 128, 0, s, sorted2.p, gidv.p, nA, nG, gstart.p, gclass.p, cstart.p, corder3.p, cur.p,
                                 pos.p, pend.p, rh.p, D, dd, dg->name_off.p, dg->names.p, dg->op.p,
                                 dg->w_rank.p, dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p,
                                 collision.p);
     // 5. accept / residual / descend
-    k_accept<<<g1, 256, 0, s>>>(sorted2.p, gidv.p, nA, nC, nG, gclass.p, cstart.p, depth.p, level, min_dup,
+    SP_LAUNCH(ctx, k_accept, g1, 256, 0, s, sorted2.p, gidv.p, nA, nC, nG, gclass.p, cstart.p, depth.p, level, min_dup,
                                 gparent.p, next_flag.p, residual.p, gaccept.p);
     LevelOut lv;
     lv.level = level;
@@ -568,8 +576,10 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     cstart.download(lv.cstart.data(), nC, s);
     gaccept.download(lv.gaccept.data(), nG, s);
     t = tmp_bytes;
+    ctx->cub_calls++;
     SP_CUDA(cub::DeviceSelect::Flagged(tmp, t, sorted2.p, next_flag.p, act.p, nsel.p, (int)nA, s));
     int32_t nsel_h = 0;
+    g_d2h_bytes += 4;
     SP_CUDA(cudaMemcpyAsync(&nsel_h, nsel.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
     lv.gstart[nG] = (int32_t)nA;
@@ -580,6 +590,7 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   int32_t coll_h = 0;
   std::vector<uint8_t> resid_h(n);
   std::vector<int32_t> pend_h((size_t)n * D);
+  g_d2h_bytes += 4;
   SP_CUDA(cudaMemcpyAsync(&coll_h, collision.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   residual.download(resid_h.data(), n, s);
   pend.download(pend_h.data(), (size_t)n * D, s);

@@ -880,14 +880,14 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   err.alloc(2, s);
   SP_CUDA(cudaMemsetAsync(err.p, 0, 2 * sizeof(int32_t), s));
   if (nb > 0)
-    k_mark_blocks<<<(int)std::min<int64_t>(nb, 65535), 128, 0, s>>>(out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
+    SP_LAUNCH(ctx, k_mark_blocks, (int)std::min<int64_t>(nb, 65535), 128, 0, s, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
                                                                   D.node_block.p, D.node_tpos.p, err.p);
   const GraphView G = view_of(dg);
   D.has_cons.alloc(n, s);
   D.ext_cons.alloc(n, s);
   SP_CUDA(cudaMemsetAsync(D.has_cons.p, 0, n, s));
   SP_CUDA(cudaMemsetAsync(D.ext_cons.p, 0, n, s));
-  k_boundary<<<grid_for(n, ctx->sm_count), 256, 0, s>>>(G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
+  SP_LAUNCH(ctx, k_boundary, grid_for(n, ctx->sm_count), 256, 0, s, G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
   DevBuf<int32_t> lastuse;
   DevBuf<EntryLayout> lay;
   DevBuf<BlobHeader> hdr;
@@ -899,13 +899,14 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   blob_off.alloc(nb + 1, s);
   SP_CUDA(cudaMemsetAsync(blob_bytes.p, 0, (nb + 1) * sizeof(int64_t), s));
   if (nb > 0)
-    k_layout<<<grid_for(nb, ctx->sm_count, 64), 64, 0, s>>>(G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
+    SP_LAUNCH(ctx, k_layout, grid_for(nb, ctx->sm_count, 64), 64, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
                                                            D.node_block.p, D.node_tpos.p, D.slot_of.p, radix_d.p,
                                                            lastuse.p, lay.p, hdr.p, blob_bytes.p, err.p);
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, blob_bytes.p, blob_off.p, (int)(nb + 1), s);
   ctx->cub_tmp.alloc(tb, s);
   tb = ctx->cub_tmp.n;
+  ctx->cub_calls++;
   SP_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tb, blob_bytes.p, blob_off.p, (int)(nb + 1), s));
   int32_t err_h[2];
   out->blob_off.resize(nb + 1);
@@ -927,13 +928,14 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   D.bound.alloc(ne, s);
   out->d_blob_off.upload(out->blob_off.data(), nb + 1, s);
   if (ne > 0)
-    k_fill<<<grid_for(ne, ctx->sm_count, 64), 64, 0, s>>>(G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, ne,
+    SP_LAUNCH(ctx, k_fill, grid_for(ne, ctx->sm_count, 64), 64, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, ne,
                                                         D.node_block.p, D.node_tpos.p, D.slot_of.p, lay.p, hdr.p,
                                                         out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
                                                         chunk, out->blobs.p, D.bound.p);
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaStreamSynchronize(s));
   // refresh host headers with the device-computed constants
+  g_d2h_bytes += (int64_t)(nb * sizeof(BlobHeader));
   for (int64_t b = 0; b < nb; b++)
     SP_CUDA(cudaMemcpyAsync(&out->hdr[b], out->blobs.p + out->blob_off[b], sizeof(BlobHeader),
                             cudaMemcpyDeviceToHost, s));
@@ -976,9 +978,9 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   if (per_sm < 1) per_sm = 1;
   const unsigned long long grid = std::min<unsigned long long>(n_items, (unsigned long long)ctx->sm_count * per_sm);
   SP_CUDA(cudaEventRecord(ctx->ev[2], s));
-  k_score<<<(unsigned)grid, THREADS, smem, s>>>(t->blobs.p, P, items.p, counter.p, d_totals);
+  SP_LAUNCH(ctx, k_score, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter.p, d_totals);
   SP_CUDA(cudaEventRecord(ctx->ev[3], s));
-  k_reduce<<<(unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s>>>(items.p, dbase.p, nb, dout.p);
+  SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dbase.p, nb, dout.p);
   SP_CUDA(cudaGetLastError());
   dout.download(res.data(), nb, s);
   SP_CUDA(cudaStreamSynchronize(s));
@@ -1063,7 +1065,7 @@ void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explai
   dout.alloc(1, s);
   dedges.alloc(std::max(max_edges, 1), s);
   dne.alloc(1, s);
-  k_explain<<<1, 1, 0, s>>>(view_of(t->dg), t->d_tmpl_nodes.p + e0, T, (int32_t)block, priv->dev.node_block.p,
+  SP_LAUNCH(ctx, k_explain, 1, 1, 0, s, view_of(t->dg), t->d_tmpl_nodes.p + e0, T, (int32_t)block, priv->dev.node_block.p,
                             priv->dev.node_tpos.p, priv->dev.slot_of.p + e0, ddig.p, priv->dev.bound.p + e0, priv->mesh, priv->mu,
                             priv->chunk, dout.p, dedges.p, max_edges, dne.p);
   SP_CUDA(cudaGetLastError());

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -24,6 +25,16 @@ struct Error : std::runtime_error {
     cudaError_t e_ = (call);                                                              \
     if (e_ != cudaSuccess)                                                                \
       throw ::sp::Error(SP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Host<->device bytes moved by the library (bench `e2e` h2d/d2h accounting).
+inline std::atomic<int64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+// Kernel launch that also counts toward sp_launch_counts (bench `gpu_launches`).
+#define SP_LAUNCH(ctx, kernel, grid, block, smem, stream, ...) \
+  do {                                                           \
+    (ctx)->own_launches++;                                       \
+    kernel<<<grid, block, smem, stream>>>(__VA_ARGS__);          \
   } while (0)
 
 // Owning device allocation (cudaMallocAsync on the context stream).
@@ -59,9 +70,11 @@ struct DevBuf {
   }
   void upload(const T* h, size_t count, cudaStream_t stream) {
     alloc(count, stream);
+    g_h2d_bytes += (int64_t)(count * sizeof(T));
     if (count) SP_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, stream));
   }
   void download(T* h, size_t count, cudaStream_t stream) const {
+    g_d2h_bytes += (int64_t)(count * sizeof(T));
     if (count) SP_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, stream));
   }
   void zero(cudaStream_t stream) {
@@ -79,6 +92,8 @@ struct sp_ctx {
   cudaEvent_t ev[6] = {};
   std::string last_error;
   double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;
+  int64_t own_launches = 0, cub_calls = 0;
+  cudaEvent_t timer[2] = {};
   // scratch reused across calls
   sp::DevBuf<uint8_t> cub_tmp;
 };

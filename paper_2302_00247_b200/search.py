@@ -242,6 +242,7 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
     # costed; build with a legal chunk to learn which error the reference hits first
     bad_mu = mu > chunk_size
     tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, chunk_size if not bad_mu else mu)
+    ses.last_table_bytes = tables.nbytes
     try:
         if tables.overflow:
             raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")

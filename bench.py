@@ -185,6 +185,7 @@ def run_ours(args) -> None:
 
     from paper_2302_00247_b200._native import Backend
     from paper_2302_00247_b200.dist import allgather_exchange
+    from paper_2302_00247_b200 import search as sp_search
     from paper_2302_00247_b200.search import Session, derive_plan
 
     rank, world, local = _dist_env()
@@ -219,7 +220,7 @@ def run_ours(args) -> None:
 
     # -- device-resident value ------------------------------------------------------
     own0, cub0 = be.launch_counts()
-    times, fold_ms, score_ms, kern_ms = [], [], [], []
+    times, fold_ms, score_ms, kern_ms, phases = [], [], [], [], []
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()
@@ -231,6 +232,7 @@ def run_ours(args) -> None:
             fold_ms.append(t["fold_ms"])
             score_ms.append(t["score_ms"])
             kern_ms.append(t["score_kernel_ms"])
+            phases.append(dict(sp_search.LAST_PHASES))
     own1, cub1 = be.launch_counts()
     assert rep.candidates == cands and rep.total_cost == ref.total_cost
 
@@ -287,6 +289,7 @@ def run_ours(args) -> None:
         "gpu_launches": (own1 - own0) // args.steps * args.steps,
         "gpu_launches_detail": {"own_kernels_per_step": (own1 - own0) / args.steps,
                                 "cub_calls_per_step": (cub1 - cub0) / args.steps},
+        "host_phases_ms": {k: statistics.median(p[k] for p in phases) for k in phases[0]},
         "breakdown_ms": {"fold": statistics.median(fold_ms), "score_total": statistics.median(score_ms),
                          "score_kernel": kern, "step": statistics.median(times),
                          "e2e_step": statistics.median(e2e_times)},

@@ -136,6 +136,16 @@ typedef struct sp_edge_conv {
   int32_t axis;         /* collective axis, -1 when none */
 } sp_edge_conv;
 
+/* Per-block winner summary of sp_explain_all (plan_cost fields). */
+typedef struct sp_explain_block {
+  int32_t valid;
+  int32_t fail_pos;
+  double forward_comm, backward_comm, total;
+  int64_t bytes[4]; /* allreduce, allgather, reducescatter, alltoall */
+  int64_t calls[4];
+  int64_t collective_calls;
+} sp_explain_block;
+
 typedef struct sp_ctx sp_ctx;
 typedef struct sp_dgraph sp_dgraph;
 typedef struct sp_fold sp_fold;
@@ -188,6 +198,19 @@ void sp_merge_keys(sp_score_out* acc, const sp_score_out* other);
 /* Full routing/cost detail of one candidate (for RoutedPlan/CostReport reconstruction). */
 int sp_explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explain_out* out,
                sp_edge_conv* edges, int32_t max_edges, int32_t* n_edges);
+
+/*
+ * Routing detail of one candidate per block in a single launch (indices[b] ==
+ * UINT64_MAX skips block b).  node_detail[4*e] = (pattern, state axis or -1,
+ * exit AllGather axis or -1, 0) for template entry e (tmpl_off order);
+ * edge_detail[2*k] = (collective kind 0..4, axis or -1) for every internal
+ * edge, consumers in template order, producers in GraphNode.inputs order.
+ */
+int sp_tables_sizes(const sp_tables* t, int64_t* n_entries, int64_t* n_edges);
+/* Internal-edge offset of every block in edge_detail ([n_blocks+1]). */
+int sp_tables_edge_offsets(const sp_tables* t, int64_t* edge_off);
+int sp_explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, sp_explain_block* blocks,
+                   int8_t* node_detail, int8_t* edge_detail);
 
 /* Device time (ms) of the last sp_score / sp_fold_run kernels (CUDA events). */
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms);

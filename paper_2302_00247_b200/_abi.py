@@ -104,6 +104,19 @@ class SpExplainOut(C.Structure):
     ]
 
 
+class SpExplainBlock(C.Structure):
+    _fields_ = [
+        ("valid", C.c_int32),
+        ("fail_pos", C.c_int32),
+        ("forward_comm", C.c_double),
+        ("backward_comm", C.c_double),
+        ("total", C.c_double),
+        ("bytes", C.c_int64 * 4),
+        ("calls", C.c_int64 * 4),
+        ("collective_calls", C.c_int64),
+    ]
+
+
 class SpEdgeConv(C.Structure):
     _fields_ = [
         ("consumer_pos", C.c_int32),

@@ -205,6 +205,29 @@ int sp_explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_expl
   });
 }
 
+int sp_tables_sizes(const sp_tables* t, int64_t* n_entries, int64_t* n_edges) {
+  if (!t) return SP_ERR_CONFIG;
+  if (n_entries) *n_entries = t->tmpl_off.empty() ? 0 : t->tmpl_off.back();
+  if (n_edges) *n_edges = t->edge_off.empty() ? 0 : t->edge_off.back();
+  return SP_OK;
+}
+
+int sp_tables_edge_offsets(const sp_tables* t, int64_t* edge_off) {
+  if (!t || !edge_off) return SP_ERR_CONFIG;
+  for (size_t i = 0; i < t->edge_off.size(); i++) edge_off[i] = t->edge_off[i];
+  return SP_OK;
+}
+
+int sp_explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, sp_explain_block* blocks,
+                   int8_t* node_detail, int8_t* edge_detail) {
+  if (!ctx || !t || !indices || !blocks) return SP_ERR_CONFIG;
+  static_assert(sizeof(sp_explain_block) == 104, "sp_explain_block layout");
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::explain_all(ctx, t, indices, blocks, node_detail, edge_detail);
+  });
+}
+
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms) {
   if (!ctx) return SP_ERR_CONFIG;
   if (fold_ms) *fold_ms = ctx->fold_ms;

@@ -28,8 +28,7 @@ namespace {
 constexpr int KMAX = 6;          // internal producers handled by a lookup table
 constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
 constexpr int THREADS = 256;     // scoring CTA size
-constexpr int ITEM_ITERS = 16;   // candidates per work item = THREADS * ITEM_ITERS
-constexpr uint64_t ITEM_CANDS = (uint64_t)THREADS * ITEM_ITERS;
+constexpr int ITEM_ITERS_MAX = 64;  // work item = THREADS * iters candidates, iters <= 64
 
 __host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 __host__ __device__ inline uint32_t pow3(int k) {
@@ -167,18 +166,20 @@ __global__ void k_boundary(GraphView G, int64_t n, const int32_t* node_block, ui
     }
 }
 
-// One thread per block: pool-slot liveness and blob layout.
+// One CTA per block: per-node internal fan-in and liveness in parallel, then
+// one thread lays out the blob and assigns pool slots (linear scan; a
+// producer's slot is released at its last internal consumer).
 __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                          const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
-                         const uint8_t* radix_of, int32_t* lastuse, EntryLayout* lay, BlobHeader* hdr,
-                         int64_t* blob_bytes, int32_t* err) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+                         const uint8_t* radix_of, EntryLayout* lay, BlobHeader* hdr, int64_t* blob_bytes,
+                         int32_t* err) {
+  __shared__ int s_k[MAXT], s_last[MAXT], s_pool[MAXT];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const int64_t e0 = tmpl_off[b];
     const int T = (int)(tmpl_off[b + 1] - e0);
-    for (int i = 0; i < T; i++) lastuse[e0 + i] = -1;
-    int nprod = 0, nt = 0;
-    int64_t nent = 0, ndbl = 0;
-    for (int i = 0; i < T; i++) {
+    for (int i = threadIdx.x; i < T; i += blockDim.x) s_last[i] = -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
       const int32_t n = tmpl_nodes[e0 + i];
       int k = 0;
       for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
@@ -186,138 +187,139 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
         if (node_block[r] != (int32_t)b) continue;
         const int j = node_tpos[r];
         if (j >= i) atomicExch(err, 2);  // template not topologically ordered
-        lastuse[e0 + j] = i;
+        atomicMax(&s_last[j], i);
         k++;
       }
       if (k > KMAX) atomicExch(err, 3);
-      EntryLayout L;
-      L.k = k;
-      L.nd = slot_of[e0 + i] >= 0 ? radix_of[e0 + i] : 1;
-      L.prod = nprod;
-      L.tab = (int32_t)nent;
-      L.dbl = (int32_t)ndbl;
-      L.train_idx = (G.w_rank[n] && G.w_train[n]) ? nt++ : -1;
-      L.out_pool = -1;
-      L.pad = 0;
-      nprod += k;
-      nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
-      ndbl += 8 + 12 * (int64_t)k;
-      lay[e0 + i] = L;
+      s_k[i] = k;
     }
-    // linear-scan pool allocation: a producer's slot frees at its last consumer
-    uint32_t used[MAXT / 32] = {0};
-    int npool = 0;
-    for (int i = 0; i < T; i++) {
-      const int32_t n = tmpl_nodes[e0 + i];
-      for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
-        const int32_t r = G.in_idx[e];
-        if (node_block[r] != (int32_t)b) continue;
-        const int j = node_tpos[r];
-        const int ps = lay[e0 + j].out_pool;
-        if (lastuse[e0 + j] == i && ps >= 0) used[ps >> 5] &= ~(1u << (ps & 31));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int nprod = 0, nt = 0;
+      int64_t nent = 0, ndbl = 0;
+      uint32_t used[MAXT / 32];
+      for (int w = 0; w < MAXT / 32; w++) used[w] = 0;
+      int npool = 0;
+      for (int i = 0; i < T; i++) {
+        // release producers whose last internal consumer is i
+        for (int j = 0; j < i; j++)
+          if (s_last[j] == i && s_pool[j] >= 0) used[s_pool[j] >> 5] &= ~(1u << (s_pool[j] & 31));
+        s_pool[i] = -1;
+        if (s_last[i] >= 0) {
+          int sl = 0;
+          while (used[sl >> 5] & (1u << (sl & 31))) sl++;
+          used[sl >> 5] |= 1u << (sl & 31);
+          s_pool[i] = sl;
+          npool = max(npool, sl + 1);
+        }
+        const int32_t n = tmpl_nodes[e0 + i];
+        const int k = s_k[i];
+        EntryLayout L;
+        L.k = k;
+        L.nd = slot_of[e0 + i] >= 0 ? radix_of[e0 + i] : 1;
+        L.prod = nprod;
+        L.tab = (int32_t)nent;
+        L.dbl = (int32_t)ndbl;
+        L.train_idx = (G.w_rank[n] && G.w_train[n]) ? nt++ : -1;
+        L.out_pool = s_pool[i];
+        L.pad = 0;
+        nprod += k;
+        nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
+        ndbl += 8 + 12 * (int64_t)k;
+        lay[e0 + i] = L;
       }
-      if (lastuse[e0 + i] >= 0) {
-        int s = 0;
-        while (used[s >> 5] & (1u << (s & 31))) s++;
-        used[s >> 5] |= 1u << (s & 31);
-        lay[e0 + i].out_pool = s;
-        npool = max(npool, s + 1);
-      }
+      BlobHeader& H = hdr[b];
+      H.T = T;
+      H.nt = nt;
+      H.npool = npool;
+      H.n_prod = nprod;
+      int64_t off = sizeof(BlobHeader);
+      H.desc_off = (int32_t)off;
+      off = align16(off + 16 * (int64_t)T);
+      H.prod_off = (int32_t)off;
+      off = align16(off + 2 * (int64_t)nprod);
+      H.tab_off = (int32_t)off;
+      off = align16(off + nent);
+      H.dbl_off = (int32_t)off;
+      off = align16(off + 8 * ndbl);
+      H.train_off = (int32_t)off;
+      off = align16(off + (int64_t)sizeof(TrainDesc) * nt);
+      H.bytes = (int32_t)off;
+      blob_bytes[b] = off;
     }
-    BlobHeader& H = hdr[b];
-    H.T = T;
-    H.nt = nt;
-    H.npool = npool;
-    int64_t off = sizeof(BlobHeader);
-    H.desc_off = (int32_t)off;
-    off = align16(off + 16 * (int64_t)T);
-    H.prod_off = (int32_t)off;
-    off = align16(off + 2 * (int64_t)nprod);
-    H.tab_off = (int32_t)off;
-    off = align16(off + nent);
-    H.dbl_off = (int32_t)off;
-    off = align16(off + 8 * ndbl);
-    H.train_off = (int32_t)off;
-    off = align16(off + (int64_t)sizeof(TrainDesc) * nt);
-    H.bytes = (int32_t)off;
-    blob_bytes[b] = off;
+    __syncthreads();
   }
 }
 
-// One thread per template entry: node descriptor, producer pool slots, fp64
-// tables, routing byte table; the block's first entry writes the header.
+// One CTA per block: node descriptors, producer pool slots, fp64 tables and
+// the routing byte table (one thread per (node, key)); thread 0 writes the
+// header.
 __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
-                       int64_t n_entries, const int32_t* node_block, const int32_t* node_tpos,
-                       const int16_t* slot_of, const EntryLayout* lay, const BlobHeader* hdr_in,
-                       const int64_t* blob_off, const uint8_t* has_cons, const uint8_t* ext_cons,
-                       sp_mesh mesh, int64_t mu, int64_t chunk, uint8_t* blobs, uint8_t* bound_of) {
+                       const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
+                       const EntryLayout* lay, const BlobHeader* hdr_in, const int64_t* blob_off,
+                       const uint8_t* has_cons, const uint8_t* ext_cons, sp_mesh mesh, int64_t mu,
+                       int64_t chunk, uint8_t* blobs, uint8_t* bound_of) {
   const MeshC M = mesh_consts(mesh);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_entries;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    // block of this entry (binary search over tmpl_off)
-    int64_t lo = 0, hi = nb;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) / 2;
-      if (tmpl_off[mid] <= e) lo = mid;
-      else hi = mid;
-    }
-    const int64_t b = lo;
+  __shared__ uint32_t s_kbase[MAXT + 1];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const int64_t e0 = tmpl_off[b];
-    const int i = (int)(e - e0);
-    const int32_t n = tmpl_nodes[e];
+    const int T = (int)(tmpl_off[b + 1] - e0);
     const BlobHeader& H = hdr_in[b];
     uint8_t* blob = blobs + blob_off[b];
-    const EntryLayout L = lay[e];
-    if (i == 0) {
+    if (threadIdx.x == 0) {
       BlobHeader h = H;
       h.multi_dev = M.d > 1;
       h.setup = M.setup;
-      h.c_ar = dmul(2.0, (double)(M.d - 1));
-      h.c_ar = ddiv(h.c_ar, (double)M.d);
+      h.c_ar = ddiv(dmul(2.0, (double)(M.d - 1)), (double)M.d);
       h.bw = M.bw;
       h.eff_ar = M.eff[C_AR];
       h.keep_bwd = dadd(1.0, -mesh.overlap_fraction);
       h.mu = mu;
       h.chunk = chunk;
       *(BlobHeader*)blob = h;
-    }
-    NodeDesc nd;
-    nd.slot = slot_of[e];
-    nd.k = (uint8_t)L.k;
-    nd.nd = (uint8_t)L.nd;
-    nd.out_pool = (int16_t)L.out_pool;
-    nd.prod = (uint16_t)L.prod;
-    nd.tab = (uint32_t)L.tab;
-    nd.dbl = (uint32_t)L.dbl;
-    ((NodeDesc*)(blob + H.desc_off))[i] = nd;
-    int16_t* prod = (int16_t*)(blob + H.prod_off) + L.prod;
-    {
-      int j = 0;
-      for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
-        const int32_t r = G.in_idx[q];
-        if (node_block[r] != (int32_t)b) continue;
-        prod[j++] = (int16_t)lay[e0 + node_tpos[r]].out_pool;
+      uint32_t acc = 0;
+      for (int i = 0; i < T; i++) {
+        s_kbase[i] = acc;
+        const EntryLayout L = lay[e0 + i];
+        acc += (uint32_t)L.nd * pow3(L.k);
       }
+      s_kbase[T] = acc;
     }
-    double* dbl = (double*)(blob + H.dbl_off) + L.dbl;
-    Pattern pats[4];
-    const int np = patterns_for(G.op[n], pats);
-    // own[p]: pattern collective call cost on this node's activation
-    for (int p = 0; p < 4; p++) dbl[p] = p < np ? call_cost(pats[p].coll, G.act_bytes[n], M) : 0.0;
-    // exitc[s]: AllGather back to replica at a subgraph boundary (search.py:213-223)
-    const bool boundary = !has_cons[n] || ext_cons[n];
-    bound_of[e] = boundary;
-    const double ag = boundary ? call_cost(C_AG, G.act_bytes[n], M) : 0.0;
-    dbl[4] = 0.0;
-    dbl[5] = ag;
-    dbl[6] = ag;
-    dbl[7] = 0.0;
-    // conv[j][p][s]: internal edge conversion cost (0.0 for identity / infeasible)
-    {
+    __syncthreads();
+    // per-node records
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+      const int64_t e = e0 + i;
+      const int32_t n = tmpl_nodes[e];
+      const EntryLayout L = lay[e];
+      NodeDesc nd;
+      nd.slot = slot_of[e];
+      nd.k = (uint8_t)L.k;
+      nd.nd = (uint8_t)L.nd;
+      nd.out_pool = (int16_t)L.out_pool;
+      nd.prod = (uint16_t)L.prod;
+      nd.tab = (uint32_t)L.tab;
+      nd.dbl = (uint32_t)L.dbl;
+      ((NodeDesc*)(blob + H.desc_off))[i] = nd;
+      int16_t* prod = (int16_t*)(blob + H.prod_off) + L.prod;
+      double* dbl = (double*)(blob + H.dbl_off) + L.dbl;
+      Pattern pats[4];
+      const int np = patterns_for(G.op[n], pats);
+      // own[p]: pattern collective call cost on this node's activation
+      for (int p = 0; p < 4; p++) dbl[p] = p < np ? call_cost(pats[p].coll, G.act_bytes[n], M) : 0.0;
+      // exitc[s]: AllGather back to replica at a subgraph boundary (search.py:213-223)
+      const bool boundary = !has_cons[n] || ext_cons[n];
+      bound_of[e] = boundary;
+      const double ag = boundary ? call_cost(C_AG, G.act_bytes[n], M) : 0.0;
+      dbl[4] = 0.0;
+      dbl[5] = ag;
+      dbl[6] = ag;
+      dbl[7] = 0.0;
+      // conv[j][p][s]: internal edge conversion cost (0.0 for identity / infeasible)
       int j = 0;
       for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
         const int32_t r = G.in_idx[q];
         if (node_block[r] != (int32_t)b) continue;
+        prod[j] = (int16_t)lay[e0 + node_tpos[r]].out_pool;
         const int rr = G.act_rank[r];
         for (int p = 0; p < 4; p++)
           for (int s = 0; s < 3; s++) {
@@ -332,30 +334,38 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
           }
         j++;
       }
+      if (L.train_idx >= 0) {
+        TrainDesc td;
+        td.slot = slot_of[e];
+        td.pad = 0;
+        td.size = G.w_bytes[n];
+        td.uterm = dadd(M.setup, cost_bytes(C_AR, td.size, M));
+        ((TrainDesc*)(blob + H.train_off))[L.train_idx] = td;
+      }
     }
-    // routing byte table: key = Horner(digit, s_0, ..., s_{k-1}) in base 3
-    uint8_t* tab = blob + H.tab_off + L.tab;
-    const uint32_t nkeys = (uint32_t)L.nd * pow3(L.k);
-    NodeRoute R;
-    int ps[KMAX];
-    for (uint32_t key = 0; key < nkeys; key++) {
+    // routing byte tables: key = Horner(digit, s_0, ..., s_{k-1}) in base 3
+    const uint32_t nkeys = s_kbase[T];
+    for (uint32_t g = threadIdx.x; g < nkeys; g += blockDim.x) {
+      int lo = 0, hi = T;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        if (s_kbase[mid] <= g) lo = mid;
+        else hi = mid;
+      }
+      const int i = lo;
+      const uint32_t key = g - s_kbase[i];
+      const EntryLayout L = lay[e0 + i];
+      int ps[KMAX];
       uint32_t x = key;
-      for (int j = L.k - 1; j >= 0; j--) {
-        ps[j] = (int)(x % 3);
+      for (int jj = L.k - 1; jj >= 0; jj--) {
+        ps[jj] = (int)(x % 3);
         x /= 3;
       }
-      const int digit = (int)x;
-      route_node(G, n, (int32_t)b, node_block, digit, ps, M, &R, false);
-      tab[key] = R.pattern < 0 ? (uint8_t)0xFF : (uint8_t)(R.pattern | (R.state << 2));
+      NodeRoute R;
+      route_node(G, tmpl_nodes[e0 + i], (int32_t)b, node_block, (int)x, ps, M, &R, false);
+      blob[H.tab_off + L.tab + key] = R.pattern < 0 ? (uint8_t)0xFF : (uint8_t)(R.pattern | (R.state << 2));
     }
-    if (L.train_idx >= 0) {
-      TrainDesc td;
-      td.slot = slot_of[e];
-      td.pad = 0;
-      td.size = G.w_bytes[n];
-      td.uterm = dadd(M.setup, cost_bytes(C_AR, td.size, M));
-      ((TrainDesc*)(blob + H.train_off))[L.train_idx] = td;
-    }
+    __syncthreads();
   }
 }
 
@@ -402,7 +412,7 @@ __device__ __forceinline__ void mr_add(uint64_t& w0, uint64_t& w1, uint32_t t, i
 
 struct ScorePlan {
   const int64_t* blob_off;
-  const int32_t* item_block;  // unused (binary search instead)
+  unsigned long long item_cands;  // candidates per work item (THREADS * iters)
   const unsigned long long* lo;   // per block start index (shard-local)
   const unsigned long long* hi;
   const unsigned long long* item_base;  // prefix sum of items per block, [nb+1]
@@ -459,8 +469,8 @@ __global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ b
     double* reach = (double*)(smem + ((blob_bytes + 15) & ~15));
     uint8_t* stp = (uint8_t*)(reach + (size_t)H.npool * THREADS);
 
-    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * ITEM_CANDS;
-    unsigned long long ihi = ilo + ITEM_CANDS;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
+    unsigned long long ihi = ilo + P.item_cands;
     if (ihi > P.hi[b]) ihi = P.hi[b];
     if (tid == 0) {
       // decode the item's first index (candidate_by_index, search.py:103-116)
@@ -759,6 +769,161 @@ __global__ void k_explain(GraphView G, const int32_t* tmpl, int T, int32_t blk, 
   *n_edges = ne;
 }
 
+struct ExplainBlock {
+  int32_t valid, fail_pos;
+  double forward_comm, backward_comm, total;
+  int64_t bytes[4];  // allreduce, allgather, reducescatter, alltoall
+  int64_t calls[4];
+  int64_t collective_calls;
+};
+static_assert(sizeof(ExplainBlock) == sizeof(sp_explain_block), "ExplainBlock mirrors sp_explain_block");
+
+// Winner detail for every block in one launch (one thread per block walks
+// its template): pattern / state / exit per node, conversion per internal
+// edge, forward/backward/total and collective accounting (plan_cost,
+// costmodel.py:193-267).  indices[b] == ~0 skips a block.
+__global__ void k_explain_all(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
+                              const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
+                              const uint8_t* bound_of, const uint8_t* blobs, const int64_t* blob_off,
+                              const int64_t* edge_off, const unsigned long long* indices, sp_mesh mesh,
+                              int64_t mu, int64_t chunk, ExplainBlock* out, int8_t* node_out, int8_t* edge_out) {
+  const MeshC M = mesh_consts(mesh);
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    ExplainBlock X;
+    X.valid = 0;
+    X.fail_pos = -1;
+    X.forward_comm = X.backward_comm = X.total = 0.0;
+    for (int k = 0; k < 4; k++) X.bytes[k] = X.calls[k] = 0;
+    X.collective_calls = 0;
+    const unsigned long long index = indices[b];
+    if (index == ~0ULL) {
+      out[b] = X;
+      continue;
+    }
+    const BlobHeader* H = (const BlobHeader*)(blobs + blob_off[b]);
+    const int V = H->V;
+    uint8_t dig[64];
+    unsigned long long rem = index;
+    for (int s = V - 1; s >= 0; s--) {
+      const uint32_t r = ((H->radix3 >> s) & 1) ? 3 : 2;
+      dig[s] = (uint8_t)(rem % r);
+      rem /= r;
+    }
+    const int64_t e0 = tmpl_off[b];
+    const int T = (int)(tmpl_off[b + 1] - e0);
+    int state[MAXT];
+    double reach[MAXT];
+    int64_t eo = edge_off[b];
+    NodeRoute R;
+    bool ok = true;
+    for (int i = 0; i < T && ok; i++) {
+      const int32_t n = tmpl_nodes[e0 + i];
+      int ps[64];
+      int k = 0;
+      for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+        const int32_t r = G.in_idx[e];
+        if (node_block[r] != (int32_t)b) continue;
+        if (k < 64) ps[k] = state[node_tpos[r]];
+        k++;
+      }
+      const int digit = slot_of[e0 + i] >= 0 ? dig[slot_of[e0 + i]] : 0;
+      route_node(G, n, (int32_t)b, node_block, digit, ps, M, &R, true);
+      if (R.pattern < 0) {
+        X.fail_pos = i;
+        ok = false;
+        break;
+      }
+      state[i] = R.state;
+      Pattern pats[4];
+      patterns_for(G.op[n], pats);
+      double base = 0.0;
+      int j = 0;
+      for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+        const int32_t r = G.in_idx[e];
+        if (node_block[r] != (int32_t)b) continue;
+        const int kind = R.conv_kind[j];
+        double cc = 0.0;
+        if (kind != C_ID) {
+          cc = call_cost(kind, G.act_bytes[r], M);
+          X.bytes[kind - 1] += G.act_bytes[r];
+          X.calls[kind - 1]++;
+        }
+        edge_out[2 * eo] = (int8_t)kind;
+        edge_out[2 * eo + 1] = R.conv_axis[j];
+        eo++;
+        base = fmax(base, dadd(reach[node_tpos[r]], cc));
+        j++;
+      }
+      const int pc = pats[R.pattern].coll;
+      if (pc != C_ID) {
+        X.bytes[pc - 1] += G.act_bytes[n];
+        X.calls[pc - 1]++;
+      }
+      reach[i] = dadd(base, call_cost(pc, G.act_bytes[n], M));
+      const NSpec fs = state_spec(R.state, G.act_rank[n]);
+      node_out[4 * (e0 + i)] = (int8_t)R.pattern;
+      node_out[4 * (e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
+      node_out[4 * (e0 + i) + 2] = -1;
+    }
+    if (!ok) {
+      out[b] = X;
+      continue;
+    }
+    double fwd = 0.0;
+    for (int i = 0; i < T; i++) {
+      const int32_t n = tmpl_nodes[e0 + i];
+      double tail = reach[i];
+      if (bound_of[e0 + i] && state[i] != 0) {
+        tail = dadd(tail, call_cost(C_AG, G.act_bytes[n], M));
+        X.bytes[C_AG - 1] += G.act_bytes[n];
+        X.calls[C_AG - 1]++;
+        node_out[4 * (e0 + i) + 2] = state_spec(state[i], G.act_rank[n]).axis;
+      }
+      fwd = fmax(fwd, tail);
+    }
+    double bwd = 0.0;
+    if (M.d > 1) {
+      // pack_gradients (rewrite.py:78-111): buckets first, then unfused, each one AllReduce
+      int64_t cur = 0;
+      int cur_n = 0;
+      for (int pass = 0; pass < 2; pass++) {
+        for (int i = 0; i < T; i++) {
+          const int32_t n = tmpl_nodes[e0 + i];
+          if (!G.w_rank[n] || !G.w_train[n] || dig[slot_of[e0 + i]] != 0) continue;
+          const int64_t sz = G.w_bytes[n];
+          if (pass == 0) {
+            if (sz >= mu) continue;
+            if (cur + sz > chunk && cur_n) {
+              bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+              X.bytes[0] += cur;
+              X.calls[0]++;
+              cur = 0;
+              cur_n = 0;
+            }
+            cur += sz;
+            cur_n++;
+          } else if (sz >= mu) {
+            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
+            X.bytes[0] += sz;
+            X.calls[0]++;
+          }
+        }
+        if (pass == 0 && cur_n) {
+          bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+          X.bytes[0] += cur;
+          X.calls[0]++;
+        }
+      }
+    }
+    X.valid = 1;
+    X.forward_comm = fwd;
+    X.backward_comm = bwd;
+    X.total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
+    X.collective_calls = X.calls[0] + X.calls[1] + X.calls[2] + X.calls[3];
+    out[b] = X;
+  }
+}
+
 inline int grid_for(int64_t n, int sms, int threads = 256) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -888,30 +1053,18 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   SP_CUDA(cudaMemsetAsync(D.has_cons.p, 0, n, s));
   SP_CUDA(cudaMemsetAsync(D.ext_cons.p, 0, n, s));
   SP_LAUNCH(ctx, k_boundary, grid_for(n, ctx->sm_count), 256, 0, s, G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
-  DevBuf<int32_t> lastuse;
   DevBuf<EntryLayout> lay;
   DevBuf<BlobHeader> hdr;
-  DevBuf<int64_t> blob_bytes, blob_off;
-  lastuse.alloc(ne, s);
+  DevBuf<int64_t> blob_bytes;
   lay.alloc(ne, s);
   hdr.upload(out->hdr.data(), nb, s);
   blob_bytes.alloc(nb + 1, s);
-  blob_off.alloc(nb + 1, s);
-  SP_CUDA(cudaMemsetAsync(blob_bytes.p, 0, (nb + 1) * sizeof(int64_t), s));
+  const int gb = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), 65535);
   if (nb > 0)
-    SP_LAUNCH(ctx, k_layout, grid_for(nb, ctx->sm_count, 64), 64, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
-                                                           D.node_block.p, D.node_tpos.p, D.slot_of.p, radix_d.p,
-                                                           lastuse.p, lay.p, hdr.p, blob_bytes.p, err.p);
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, blob_bytes.p, blob_off.p, (int)(nb + 1), s);
-  ctx->cub_tmp.alloc(tb, s);
-  tb = ctx->cub_tmp.n;
-  ctx->cub_calls++;
-  SP_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, tb, blob_bytes.p, blob_off.p, (int)(nb + 1), s));
+    SP_LAUNCH(ctx, k_layout, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
+              D.node_tpos.p, D.slot_of.p, radix_d.p, lay.p, hdr.p, blob_bytes.p, err.p);
   int32_t err_h[2];
-  out->blob_off.resize(nb + 1);
   err.download(err_h, 2, s);
-  blob_off.download(out->blob_off.data(), nb + 1, s);
   hdr.download(out->hdr.data(), nb, s);
   SP_CUDA(cudaStreamSynchronize(s));
   if (err_h[0] == 1) throw Error(SP_ERR_CONFIG, "a node appears in more than one template");
@@ -920,26 +1073,22 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     throw Error(SP_ERR_UNSUPPORTED, "a template node has more than 6 internal producers");
   out->max_blob = 0;
   out->max_pool = 0;
+  out->blob_off.assign(nb + 1, 0);
+  out->edge_off.assign(nb + 1, 0);
   for (int64_t b = 0; b < nb; b++) {
     out->max_blob = std::max<int64_t>(out->max_blob, out->hdr[b].bytes);
     out->max_pool = std::max(out->max_pool, out->hdr[b].npool);
+    out->blob_off[b + 1] = out->blob_off[b] + out->hdr[b].bytes;
+    out->edge_off[b + 1] = out->edge_off[b] + out->hdr[b].n_prod;
   }
   out->blobs.alloc(std::max<int64_t>(out->blob_off[nb], 16), s);
   D.bound.alloc(ne, s);
   out->d_blob_off.upload(out->blob_off.data(), nb + 1, s);
-  if (ne > 0)
-    SP_LAUNCH(ctx, k_fill, grid_for(ne, ctx->sm_count, 64), 64, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, ne,
-                                                        D.node_block.p, D.node_tpos.p, D.slot_of.p, lay.p, hdr.p,
-                                                        out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
-                                                        chunk, out->blobs.p, D.bound.p);
+  if (nb > 0)
+    SP_LAUNCH(ctx, k_fill, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
+              D.node_tpos.p, D.slot_of.p, lay.p, hdr.p, out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
+              chunk, out->blobs.p, D.bound.p);
   SP_CUDA(cudaGetLastError());
-  SP_CUDA(cudaStreamSynchronize(s));
-  // refresh host headers with the device-computed constants
-  g_d2h_bytes += (int64_t)(nb * sizeof(BlobHeader));
-  for (int64_t b = 0; b < nb; b++)
-    SP_CUDA(cudaMemcpyAsync(&out->hdr[b], out->blobs.p + out->blob_off[b], sizeof(BlobHeader),
-                            cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaStreamSynchronize(s));
 }
 
 static size_t score_smem(const sp_tables* t) {
@@ -950,37 +1099,47 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
                       const std::vector<unsigned long long>& hi, double* d_totals, std::vector<sp_score_out>& res) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
-  std::vector<unsigned long long> base(nb + 1, 0);
-  for (int64_t b = 0; b < nb; b++) {
-    const unsigned long long c = hi[b] > lo[b] ? hi[b] - lo[b] : 0;
-    base[b + 1] = base[b] + (c + ITEM_CANDS - 1) / ITEM_CANDS;
-  }
-  const unsigned long long n_items = base[nb];
   res.assign(nb, sp_score_out{});
-  if (n_items == 0) return;
   const size_t smem = score_smem(t);
   if (smem > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
-  DevBuf<unsigned long long> dlo, dhi, dbase, counter;
-  DevBuf<ItemOut> items;
-  DevBuf<sp_score_out> dout;
-  dlo.upload(lo.data(), nb, s);
-  dhi.upload(hi.data(), nb, s);
-  dbase.upload(base.data(), nb + 1, s);
-  counter.alloc(1, s);
-  SP_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), s));
-  items.alloc(n_items, s);
-  dout.alloc(nb, s);
-  ScorePlan P{t->d_blob_off.p, nullptr, dlo.p, dhi.p, dbase.p, nb, n_items};
   SP_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score, THREADS, smem));
   if (per_sm < 1) per_sm = 1;
-  const unsigned long long grid = std::min<unsigned long long>(n_items, (unsigned long long)ctx->sm_count * per_sm);
+  const unsigned long long slots = (unsigned long long)ctx->sm_count * per_sm;
+  // size work items so the grid gets ~4 items per resident CTA (dynamic balance)
+  unsigned long long total = 0;
+  for (int64_t b = 0; b < nb; b++) total += hi[b] > lo[b] ? hi[b] - lo[b] : 0;
+  unsigned long long iters = (total + slots * 4 * THREADS - 1) / (slots * 4 * THREADS);
+  iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, ITEM_ITERS_MAX));
+  const unsigned long long item_cands = iters * THREADS;
+  std::vector<unsigned long long> base(nb + 1, 0);
+  for (int64_t b = 0; b < nb; b++) {
+    const unsigned long long c = hi[b] > lo[b] ? hi[b] - lo[b] : 0;
+    base[b + 1] = base[b] + (c + item_cands - 1) / item_cands;
+  }
+  const unsigned long long n_items = base[nb];
+  if (n_items == 0) return;
+  // one small H2D for the plan: lo | hi | base | counter
+  std::vector<unsigned long long> plan(3 * nb + 2, 0);
+  std::copy(lo.begin(), lo.end(), plan.begin());
+  std::copy(hi.begin(), hi.end(), plan.begin() + nb);
+  std::copy(base.begin(), base.end(), plan.begin() + 2 * nb);
+  DevBuf<unsigned long long> dplan;
+  DevBuf<ItemOut> items;
+  DevBuf<sp_score_out> dout;
+  dplan.upload(plan.data(), plan.size(), s);
+  items.alloc(n_items, s);
+  dout.alloc(nb, s);
+  unsigned long long* counter = dplan.p + 3 * nb + 1;
+  ScorePlan P{t->d_blob_off.p, item_cands, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items};
+  const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
   SP_CUDA(cudaEventRecord(ctx->ev[2], s));
-  SP_LAUNCH(ctx, k_score, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter.p, d_totals);
+  SP_LAUNCH(ctx, k_score, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter, d_totals);
   SP_CUDA(cudaEventRecord(ctx->ev[3], s));
-  SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dbase.p, nb, dout.p);
+  SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
+            dout.p);
   SP_CUDA(cudaGetLastError());
   dout.download(res.data(), nb, s);
   SP_CUDA(cudaStreamSynchronize(s));
@@ -1078,6 +1237,36 @@ void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explai
     dedges.download(edges, std::min(ne, max_edges), s);
     SP_CUDA(cudaStreamSynchronize(s));
   }
+}
+
+void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* blocks_out, int8_t* node_out,
+                 int8_t* edge_out) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nb = t->n_blocks;
+  if (nb == 0) return;
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  const int64_t ne = t->tmpl_off[nb];
+  const int64_t nedge = t->edge_off[nb];
+  // one H2D (indices + edge offsets), one D2H per output array
+  std::vector<unsigned long long> up(2 * nb + 1);
+  for (int64_t b = 0; b < nb; b++) up[b] = indices[b];
+  for (int64_t b = 0; b <= nb; b++) up[nb + b] = (unsigned long long)t->edge_off[b];
+  DevBuf<unsigned long long> dup;
+  dup.upload(up.data(), up.size(), s);
+  DevBuf<ExplainBlock> dblk;
+  DevBuf<int8_t> dnode, dedge;
+  dblk.alloc(nb, s);
+  dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
+  dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
+  SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
+            t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
+            priv->dev.slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, (const int64_t*)(dup.p + nb),
+            dup.p, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p, dedge.p);
+  SP_CUDA(cudaGetLastError());
+  dblk.download((ExplainBlock*)blocks_out, nb, s);
+  dnode.download(node_out, 4 * ne, s);
+  dedge.download(edge_out, 2 * nedge, s);
+  SP_CUDA(cudaStreamSynchronize(s));
 }
 
 void tables_free_priv(sp_tables* t) {

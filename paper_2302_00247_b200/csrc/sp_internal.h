@@ -127,7 +127,7 @@ struct BlobHeader {
   uint64_t radix3;        // bit s set: slot s has 3 options, else 2
   int32_t T, V, nt, npool;
   int32_t desc_off, prod_off, tab_off, dbl_off;  // byte offsets from blob start
-  int32_t train_off, bytes, multi_dev, pad0;      // multi_dev: device_count > 1
+  int32_t train_off, bytes, multi_dev, n_prod;    // multi_dev: device_count > 1; n_prod: internal edges
   double setup, c_ar, bw, eff_ar, keep_bwd;       // keep_bwd = 1.0 - overlap_fraction
   int64_t mu, chunk, pad1;
 };
@@ -156,6 +156,7 @@ struct sp_tables {
   int64_t n_blocks = 0;
   std::vector<BlobHeader> hdr;           // host copy of every block header
   std::vector<int64_t> blob_off;         // byte offset of each block blob
+  std::vector<int64_t> edge_off;         // internal-edge offset of each block (explain output)
   std::vector<std::vector<int32_t>> slot_pos;  // weight slot -> template position
   std::vector<int64_t> tmpl_off;
   std::vector<int32_t> tmpl_nodes;
@@ -184,4 +185,6 @@ void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explai
              sp_edge_conv* edges, int32_t max_edges, int32_t* n_edges);
 void merge_key(sp_score_out* acc, const sp_score_out* o);
 void tables_free_priv(sp_tables* t);
+void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* blocks_out, int8_t* node_out,
+                 int8_t* edge_out);
 }  // namespace sp

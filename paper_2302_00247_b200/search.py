@@ -17,6 +17,7 @@ resource (multi-GPU sharding lives in ``paper_2302_00247_b200.dist``).
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -29,6 +30,9 @@ from .errors import BackendError, BadConfig, UnsupportedSearch
 from .lowering import LoweredGraph, lower
 
 _KIND_LABEL = {1: "allreduce", 2: "allgather", 3: "reducescatter", 4: "alltoall"}
+
+#: wall-clock phases (ms) of the last derive_plan call in this process
+LAST_PHASES: dict = {}
 
 
 @dataclass
@@ -224,6 +228,66 @@ _OP_LABELS = ("matmul", "elementwise", "layernorm", "softmax", "embedding", "res
               "output", "auxiliary", "collective")
 
 
+def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
+                     types: TypeSet = DEFAULT_TYPES) -> list:
+    """RoutedPlan of every block's argmin from ONE sp_explain_all launch."""
+    low = ses.low
+    idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
+    blocks, node, edge, eoff = ses.backend.explain_all(tables, idx)
+    replica = types.ShardSpec(types.ShardKind.REPLICA)
+    identity = types.Collective(types.CollectiveKind.IDENTITY)
+    allreduce = types.Collective(types.CollectiveKind.ALL_REDUCE_SUM)
+    index = low.index
+    names = low.names
+    in_off, in_idx = low.in_off, low.in_idx
+    out = []
+    e0 = 0
+    for b, (sub, sc, X) in enumerate(zip(subgraphs, scores, blocks)):
+        T = len(sub.template)
+        if not sc.has_best or not X.valid:
+            out.append(None)
+            e0 += T
+            continue
+        tnodes = [index[s] for s in sub.template]
+        members = set(tnodes)
+        slot_pos = ses.backend.slots(tables, b)
+        radices = [3 if low.w_rank[tnodes[p]] >= 2 else 2 for p in slot_pos]
+        digits = _digits(int(sc.best_index), radices)
+        assignments = tuple((sub.template[p], _spec_for_digit(types, d))
+                            for p, d in zip(slot_pos, digits))
+        plan = types.CandidatePlan(sub, assignments, int(sc.best_index))
+        routings, exits = [], []
+        k = int(eoff[b])
+        for i in range(T):
+            v = tnodes[i]
+            op_label = _OP_LABELS[int(low.op[v])]
+            pidx, sax, xax = int(node[e0 + i, 0]), int(node[e0 + i, 1]), int(node[e0 + i, 2])
+            convs = []
+            for r in in_idx[in_off[v]:in_off[v + 1]].tolist():
+                if r not in members:
+                    continue
+                kind, axis = int(edge[k, 0]), int(edge[k, 1])
+                k += 1
+                if kind:
+                    convs.append((names[r], _collective(types, kind, axis), int(low.act_bytes[r])))
+            out_coll = allreduce if types.pattern_collectives[op_label][pidx] == "allreduce" else identity
+            state = replica if sax < 0 else types.ShardSpec(types.ShardKind.SPLIT, sax)
+            routings.append(types.NodeRouting(sub.template[i], types.pattern_names[op_label][pidx],
+                                              tuple(convs), out_coll, int(low.act_bytes[v]), state))
+            if xax >= 0:
+                exits.append((sub.template[i], _collective(types, 2, xax), int(low.act_bytes[v])))
+        bbc = {_KIND_LABEL[j + 1]: int(X.bytes[j]) for j in range(4) if X.calls[j]}
+        cost = types.CostReport(forward_comm=X.forward_comm, backward_comm=X.backward_comm,
+                                overlap_fraction=mesh.overlap_fraction, bytes_by_collective=bbc,
+                                collective_calls=int(X.collective_calls), flops=_flops(low, tnodes))
+        if cost.total != sc.best_total:
+            raise BackendError(f"explain/score disagree on block {b}: {cost.total!r} != "
+                               f"{sc.best_total!r}")
+        out.append(types.RoutedPlan(plan, tuple(routings), tuple(exits), cost))
+        e0 += T
+    return out
+
+
 def _labels(assignments) -> dict:
     return {s: spec.label for s, spec in assignments}
 
@@ -249,14 +313,14 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
         scores = ses.backend.score(tables, shard, n_shards)
         if exchange is not None:
             scores = exchange(scores)
-        results = []
-        for b, (sub, sc) in enumerate(zip(subgraphs, scores)):
+        for sc in scores:
             if not sc.has_best:
                 raise AssertionError("all-replica fallback must always route")
             if bad_mu:
                 raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
-            best = routed_plan(ses, tables, b, sub, int(sc.best_index), mesh, types,
-                               expect_total=sc.best_total)
+        bests = routed_plans_all(ses, tables, subgraphs, scores, mesh, types)
+        results = []
+        for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
             table = []
             if want_table:
                 C = int(sc.candidates)
@@ -287,10 +351,14 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
                 shard: int = 0, n_shards: int = 1, exchange: Optional[Callable] = None):
     """Prune, search every unique block, assemble the whole-graph plan (search.py:348-379)."""
     del jobs
+    t0 = time.perf_counter()
     ses = session or Session.open(graph, backend, cache=cache)
+    t1 = time.perf_counter()
     subs = prune_graph(graph, min_duplicates, types=types, session=ses)
+    t2 = time.perf_counter()
     results = search_blocks(graph, subs, mesh, mu, chunk_size, want_table, session=ses,
                             types=types, shard=shard, n_shards=n_shards, exchange=exchange)
+    t3 = time.perf_counter()
     assignments: dict = {}
     total_cost = 0.0
     candidates = 0
@@ -302,5 +370,7 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
         for prefix, _ in sub.instances:
             for scope, spec in res.best.plan.assignments:
                 assignments[sub.instance_node(prefix, scope)] = spec.label
+    LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
+                       search_ms=(t3 - t2) * 1e3, assemble_ms=(time.perf_counter() - t3) * 1e3)
     return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates,
                                 valid)

@@ -59,6 +59,7 @@ void sp_ctx_destroy(sp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ctx->cub_tmp.release();
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->staging) cudaFreeHost(ctx->staging);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->timer)

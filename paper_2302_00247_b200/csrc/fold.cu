@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "sp_internal.h"
@@ -71,56 +72,61 @@ __global__ void k_depth(const int64_t* __restrict__ off, const uint8_t* __restri
 }
 
 // Per node and depth d: prefix end, prefix hash, rel-name hash.
+__device__ __forceinline__ void name_hash_one(int64_t i, const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
+                            int32_t D, uint64_t seed, int32_t* __restrict__ pend,
+                            uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
+  const uint8_t* p = s + off[i];
+  const int64_t L = off[i + 1] - off[i];
+  uint64_t h = 0;
+  int d = 0;
+  // prefix ends and prefix hashes; h tracks poly(p[0:k])
+  uint64_t hpre[64];
+  int32_t ends[64];
+  for (int64_t k = 0; k <= L; k++) {
+    if (k == L || p[k] == '/') {
+      if (d < D && d < 64) {
+        ends[d] = (int32_t)k;
+        hpre[d] = h;
+      }
+      d++;
+      if (k == L) break;
+    }
+    h = h * kPolyB + (uint64_t)p[k] + 1;
+  }
+  const uint64_t hall = h;
+  const int dn = d;  // node depth
+  for (int dd = 0; dd < D; dd++) {
+    const int64_t idx = i * D + dd;
+    if (dd >= dn || dd >= 64) {
+      pend[idx] = (int32_t)L;
+      ph[idx] = 0;
+      rh[idx] = 0;
+      continue;
+    }
+    const int64_t q = ends[dd];
+    pend[idx] = (int32_t)q;
+    ph[idx] = fmix64(hpre[dd] ^ fmix64(seed + (uint64_t)q));
+    // rel = p[start:L] with start = q+1 if the prefix is non-empty, else 0
+    int64_t start = q > 0 ? q + 1 : 0;
+    if (start > L) start = L;
+    // poly(p[start:L]) = poly(p[0:L]) - poly(p[0:start]) * B^(L-start)
+    uint64_t hrel;
+    if (q >= L) {
+      hrel = 0;  // the node IS the prefix: rel name is ""
+    } else {
+      const uint64_t hs = start > 0 ? hpre[dd] * kPolyB + (uint64_t)'/' + 1 : 0;  // poly(p[0:q+1])
+      hrel = hall - hs * upow(kPolyB, L - start);
+    }
+    rh[idx] = fmix64(hrel ^ fmix64((seed ^ 0x9e3779b97f4a7c15ULL) + (uint64_t)(L - start)));
+  }
+}
+
 __global__ void k_name_hash(const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
                             int32_t D, uint64_t seed, int32_t* __restrict__ pend,
                             uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint8_t* p = s + off[i];
-    const int64_t L = off[i + 1] - off[i];
-    uint64_t h = 0;
-    int d = 0;
-    // prefix ends and prefix hashes; h tracks poly(p[0:k])
-    uint64_t hpre[64];
-    int32_t ends[64];
-    for (int64_t k = 0; k <= L; k++) {
-      if (k == L || p[k] == '/') {
-        if (d < D && d < 64) {
-          ends[d] = (int32_t)k;
-          hpre[d] = h;
-        }
-        d++;
-        if (k == L) break;
-      }
-      h = h * kPolyB + (uint64_t)p[k] + 1;
-    }
-    const uint64_t hall = h;
-    const int dn = d;  // node depth
-    for (int dd = 0; dd < D; dd++) {
-      const int64_t idx = i * D + dd;
-      if (dd >= dn || dd >= 64) {
-        pend[idx] = (int32_t)L;
-        ph[idx] = 0;
-        rh[idx] = 0;
-        continue;
-      }
-      const int64_t q = ends[dd];
-      pend[idx] = (int32_t)q;
-      ph[idx] = fmix64(hpre[dd] ^ fmix64(seed + (uint64_t)q));
-      // rel = p[start:L] with start = q+1 if the prefix is non-empty, else 0
-      int64_t start = q > 0 ? q + 1 : 0;
-      if (start > L) start = L;
-      // poly(p[start:L]) = poly(p[0:L]) - poly(p[0:start]) * B^(L-start)
-      uint64_t hrel;
-      if (q >= L) {
-        hrel = 0;  // the node IS the prefix: rel name is ""
-      } else {
-        const uint64_t hs = start > 0 ? hpre[dd] * kPolyB + (uint64_t)'/' + 1 : 0;  // poly(p[0:q+1])
-        hrel = hall - hs * upow(kPolyB, L - start);
-      }
-      rh[idx] = fmix64(hrel ^ fmix64((seed ^ 0x9e3779b97f4a7c15ULL) + (uint64_t)(L - start)));
-    }
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    name_hash_one(i, off, s, n, D, seed, pend, ph, rh);
 }
 
 __global__ void k_gather_keys(const int32_t* __restrict__ act, int64_t nA, const uint64_t* __restrict__ src,
@@ -158,6 +164,28 @@ __device__ __forceinline__ uint64_t weight_hash(int64_t n, const uint8_t* w_rank
 }
 
 // Entry hash (template key entry) and group key sums; positions in group.
+__device__ __forceinline__ void entry_one(int64_t i, const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
+                        const int32_t* __restrict__ gstart, const int64_t* __restrict__ cur,
+                        const uint64_t* __restrict__ rh, int32_t D, int32_t dd,
+                        const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                        const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                        const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                        int32_t* __restrict__ pos, unsigned long long* __restrict__ gkey) {
+  const int32_t n = sorted[i];
+  const int32_t g = gid[i] - 1;
+  pos[n] = (int32_t)(i - gstart[g]);
+  const int64_t me = cur[n];
+  uint64_t prod = 0;
+  for (int64_t e = in_off[n]; e < in_off[n + 1]; e++) {
+    const int32_t r = in_idx[e];
+    if (cur[r] == me) prod += fmix64(rh[(int64_t)r * D + dd] ^ 0x6a09e667f3bcc909ULL);
+  }
+  uint64_t h = fmix64(rh[(int64_t)n * D + dd] + 0x3c6ef372fe94f82bULL * (uint64_t)(op[n] + 1));
+  h = fmix64(h ^ weight_hash(n, w_rank, w_shape, w_train));
+  h = fmix64(h + fmix64(prod ^ 0xbb67ae8584caa73bULL));
+  atomicAdd(&gkey[g], (unsigned long long)fmix64(h ^ 0xa54ff53a5f1d36f1ULL));
+}
+
 __global__ void k_entry(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
                         const int32_t* __restrict__ gstart, const int64_t* __restrict__ cur,
                         const uint64_t* __restrict__ rh, int32_t D, int32_t dd,
@@ -166,21 +194,8 @@ __global__ void k_entry(const int32_t* __restrict__ sorted, const int32_t* __res
                         const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
                         int32_t* __restrict__ pos, unsigned long long* __restrict__ gkey) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t n = sorted[i];
-    const int32_t g = gid[i] - 1;
-    pos[n] = (int32_t)(i - gstart[g]);
-    const int64_t me = cur[n];
-    uint64_t prod = 0;
-    for (int64_t e = in_off[n]; e < in_off[n + 1]; e++) {
-      const int32_t r = in_idx[e];
-      if (cur[r] == me) prod += fmix64(rh[(int64_t)r * D + dd] ^ 0x6a09e667f3bcc909ULL);
-    }
-    uint64_t h = fmix64(rh[(int64_t)n * D + dd] + 0x3c6ef372fe94f82bULL * (uint64_t)(op[n] + 1));
-    h = fmix64(h ^ weight_hash(n, w_rank, w_shape, w_train));
-    h = fmix64(h + fmix64(prod ^ 0xbb67ae8584caa73bULL));
-    atomicAdd(&gkey[g], (unsigned long long)fmix64(h ^ 0xa54ff53a5f1d36f1ULL));
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    entry_one(i, sorted, gid, nA, gstart, cur, rh, D, dd, op, w_rank, w_shape, w_train, in_off, in_idx, pos, gkey);
 }
 
 __global__ void k_class_keys(int64_t nG, int64_t nA, const int32_t* __restrict__ gstart,
@@ -235,6 +250,90 @@ __device__ void sort_small(int32_t* v, int n) {
 
 // Exact checks: prefix bytes vs group head, distinct rel hashes inside a
 // group, and member-by-member template-key equality vs the class head group.
+__device__ __forceinline__ void verify_one(int64_t i, const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
+                         int64_t nG, const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass,
+                         const int32_t* __restrict__ cstart, const int32_t* __restrict__ corder,
+                         const int64_t* __restrict__ cur, const int32_t* __restrict__ pos,
+                         const int32_t* __restrict__ pend, const uint64_t* __restrict__ rh, int32_t D,
+                         int32_t dd, const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
+                         const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                         const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                         const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                         int32_t* __restrict__ collision) {
+  const int32_t n = sorted[i];
+  const int32_t g = gid[i] - 1;
+  const int64_t s0 = gstart[g];
+  const int64_t gsz = (g + 1 < nG ? gstart[g + 1] : nA) - s0;
+  bool bad = false;
+  // (a) same prefix string as the group head
+  const int32_t h = sorted[s0];
+  const int32_t pl = pend[(int64_t)n * D + dd];
+  if (pl != pend[(int64_t)h * D + dd] || !bytes_eq(names + name_off[n], names + name_off[h], pl)) bad = true;
+  // (b) rel hashes strictly distinct inside a group (canonical order well defined)
+  if (i > s0 && rh[(int64_t)sorted[i - 1] * D + dd] == rh[(int64_t)n * D + dd]) bad = true;
+  // (c) template key equality with the class head group at the same canonical position
+  const int32_t c = gclass[g];
+  const int32_t hg = corder[cstart[c]];
+  if (hg != g) {
+    const int64_t h0 = gstart[hg];
+    const int64_t hsz = (hg + 1 < nG ? gstart[hg + 1] : nA) - h0;
+    const int64_t j = i - s0;
+    if (hsz != gsz) {
+      bad = true;
+    } else {
+      const int32_t b = sorted[h0 + j];
+      const int64_t la = name_off[n + 1] - name_off[n];
+      const int64_t lb = name_off[b + 1] - name_off[b];
+      int64_t sa = pl > 0 ? pl + 1 : 0;
+      const int32_t plb = pend[(int64_t)b * D + dd];
+      int64_t sb = plb > 0 ? plb + 1 : 0;
+      sa = sa > la ? la : sa;
+      sb = sb > lb ? lb : sb;
+      if (la - sa != lb - sb || !bytes_eq(names + name_off[n] + sa, names + name_off[b] + sb, la - sa))
+        bad = true;
+      if (op[n] != op[b] || w_rank[n] != w_rank[b] || w_train[n] != w_train[b]) bad = true;
+      for (int k = 0; k < w_rank[n] && !bad; k++)
+        if (w_shape[(int64_t)n * SP_MAX_RANK + k] != w_shape[(int64_t)b * SP_MAX_RANK + k]) bad = true;
+      // internal producers as canonical positions
+      int32_t pa[16], pb[16];
+      int ka = 0, kb = 0;
+      bool over = false;
+      for (int64_t e = in_off[n]; e < in_off[n + 1]; e++)
+        if (cur[in_idx[e]] == cur[n]) {
+          if (ka < 16) pa[ka] = pos[in_idx[e]];
+          ka++;
+        }
+      for (int64_t e = in_off[b]; e < in_off[b + 1]; e++)
+        if (cur[in_idx[e]] == cur[b]) {
+          if (kb < 16) pb[kb] = pos[in_idx[e]];
+          kb++;
+        }
+      if (ka != kb) bad = true;
+      if (!bad && ka > 16) over = true;
+      if (!bad && !over) {
+        sort_small(pa, ka);
+        sort_small(pb, kb);
+        for (int k = 0; k < ka; k++)
+          if (pa[k] != pb[k]) bad = true;
+      }
+      if (!bad && over) {
+        // wide fan-in: quadratic multiset comparison (rare)
+        for (int64_t e = in_off[n]; e < in_off[n + 1] && !bad; e++) {
+          const int32_t r = in_idx[e];
+          if (cur[r] != cur[n]) continue;
+          int ca = 0, cb = 0;
+          for (int64_t f = in_off[n]; f < in_off[n + 1]; f++)
+            ca += cur[in_idx[f]] == cur[n] && pos[in_idx[f]] == pos[r];
+          for (int64_t f = in_off[b]; f < in_off[b + 1]; f++)
+            cb += cur[in_idx[f]] == cur[b] && pos[in_idx[f]] == pos[r];
+          if (ca != cb) bad = true;
+        }
+      }
+    }
+  }
+  if (bad) atomicExch(collision, 1);
+}
+
 __global__ void k_verify(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
                          int64_t nG, const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass,
                          const int32_t* __restrict__ cstart, const int32_t* __restrict__ corder,
@@ -246,83 +345,33 @@ __global__ void k_verify(const int32_t* __restrict__ sorted, const int32_t* __re
                          const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
                          int32_t* __restrict__ collision) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t n = sorted[i];
-    const int32_t g = gid[i] - 1;
-    const int64_t s0 = gstart[g];
-    const int64_t gsz = (g + 1 < nG ? gstart[g + 1] : nA) - s0;
-    bool bad = false;
-    // (a) same prefix string as the group head
-    const int32_t h = sorted[s0];
-    const int32_t pl = pend[(int64_t)n * D + dd];
-    if (pl != pend[(int64_t)h * D + dd] || !bytes_eq(names + name_off[n], names + name_off[h], pl)) bad = true;
-    // (b) rel hashes strictly distinct inside a group (canonical order well defined)
-    if (i > s0 && rh[(int64_t)sorted[i - 1] * D + dd] == rh[(int64_t)n * D + dd]) bad = true;
-    // (c) template key equality with the class head group at the same canonical position
-    const int32_t c = gclass[g];
-    const int32_t hg = corder[cstart[c]];
-    if (hg != g) {
-      const int64_t h0 = gstart[hg];
-      const int64_t hsz = (hg + 1 < nG ? gstart[hg + 1] : nA) - h0;
-      const int64_t j = i - s0;
-      if (hsz != gsz) {
-        bad = true;
-      } else {
-        const int32_t b = sorted[h0 + j];
-        const int64_t la = name_off[n + 1] - name_off[n];
-        const int64_t lb = name_off[b + 1] - name_off[b];
-        int64_t sa = pl > 0 ? pl + 1 : 0;
-        const int32_t plb = pend[(int64_t)b * D + dd];
-        int64_t sb = plb > 0 ? plb + 1 : 0;
-        sa = sa > la ? la : sa;
-        sb = sb > lb ? lb : sb;
-        if (la - sa != lb - sb || !bytes_eq(names + name_off[n] + sa, names + name_off[b] + sb, la - sa))
-          bad = true;
-        if (op[n] != op[b] || w_rank[n] != w_rank[b] || w_train[n] != w_train[b]) bad = true;
-        for (int k = 0; k < w_rank[n] && !bad; k++)
-          if (w_shape[(int64_t)n * SP_MAX_RANK + k] != w_shape[(int64_t)b * SP_MAX_RANK + k]) bad = true;
-        // internal producers as canonical positions
-        int32_t pa[16], pb[16];
-        int ka = 0, kb = 0;
-        bool over = false;
-        for (int64_t e = in_off[n]; e < in_off[n + 1]; e++)
-          if (cur[in_idx[e]] == cur[n]) {
-            if (ka < 16) pa[ka] = pos[in_idx[e]];
-            ka++;
-          }
-        for (int64_t e = in_off[b]; e < in_off[b + 1]; e++)
-          if (cur[in_idx[e]] == cur[b]) {
-            if (kb < 16) pb[kb] = pos[in_idx[e]];
-            kb++;
-          }
-        if (ka != kb) bad = true;
-        if (!bad && ka > 16) over = true;
-        if (!bad && !over) {
-          sort_small(pa, ka);
-          sort_small(pb, kb);
-          for (int k = 0; k < ka; k++)
-            if (pa[k] != pb[k]) bad = true;
-        }
-        if (!bad && over) {
-          // wide fan-in: quadratic multiset comparison (rare)
-          for (int64_t e = in_off[n]; e < in_off[n + 1] && !bad; e++) {
-            const int32_t r = in_idx[e];
-            if (cur[r] != cur[n]) continue;
-            int ca = 0, cb = 0;
-            for (int64_t f = in_off[n]; f < in_off[n + 1]; f++)
-              ca += cur[in_idx[f]] == cur[n] && pos[in_idx[f]] == pos[r];
-            for (int64_t f = in_off[b]; f < in_off[b + 1]; f++)
-              cb += cur[in_idx[f]] == cur[b] && pos[in_idx[f]] == pos[r];
-            if (ca != cb) bad = true;
-          }
-        }
-      }
-    }
-    if (bad) atomicExch(collision, 1);
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    verify_one(i, sorted, gid, nA, nG, gstart, gclass, cstart, corder, cur, pos, pend, rh, D, dd, name_off, names, op, w_rank, w_shape, w_train, in_off, in_idx, collision);
 }
 
 // accept / residual / descend for every active node
+__device__ __forceinline__ void accept_one(int64_t i, const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
+                         int64_t nC, int64_t nG, const int32_t* __restrict__ gclass,
+                         const int32_t* __restrict__ cstart, const int32_t* __restrict__ depth,
+                         int32_t level, int32_t min_dup, int32_t* __restrict__ gparent,
+                         uint8_t* __restrict__ next_flag, uint8_t* __restrict__ residual,
+                         uint8_t* __restrict__ gaccept) {
+  const int32_t n = sorted[i];
+  const int32_t g = gid[i] - 1;
+  const int32_t c = gclass[g];
+  const int64_t csz = (c + 1 < nC ? cstart[c + 1] : nG) - cstart[c];
+  const bool acc = csz >= min_dup;
+  if (i == 0 || gid[i - 1] != gid[i]) gaccept[g] = acc;
+  next_flag[i] = 0;
+  if (acc) return;
+  if (depth[n] <= level) {
+    residual[n] = 1;
+  } else {
+    next_flag[i] = 1;
+    gparent[n] = g;
+  }
+}
+
 __global__ void k_accept(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
                          int64_t nC, int64_t nG, const int32_t* __restrict__ gclass,
                          const int32_t* __restrict__ cstart, const int32_t* __restrict__ depth,
@@ -330,22 +379,217 @@ __global__ void k_accept(const int32_t* __restrict__ sorted, const int32_t* __re
                          uint8_t* __restrict__ next_flag, uint8_t* __restrict__ residual,
                          uint8_t* __restrict__ gaccept) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t n = sorted[i];
-    const int32_t g = gid[i] - 1;
-    const int32_t c = gclass[g];
-    const int64_t csz = (c + 1 < nC ? cstart[c + 1] : nG) - cstart[c];
-    const bool acc = csz >= min_dup;
-    if (i == 0 || gid[i - 1] != gid[i]) gaccept[g] = acc;
-    next_flag[i] = 0;
-    if (acc) continue;
-    if (depth[n] <= level) {
-      residual[n] = 1;
-    } else {
-      next_flag[i] = 1;
-      gparent[n] = g;
-    }
+       i += (int64_t)gridDim.x * blockDim.x)
+    accept_one(i, sorted, gid, nA, nC, nG, gclass, cstart, depth, level, min_dup, gparent, next_flag, residual, gaccept);
+}
+
+// ---------------------------------------------------------------------------
+// Single-CTA fold for graphs up to SMALL_MAX nodes: the same level algorithm
+// with block-wide bitonic sorts and scans in shared memory, so the whole
+// prune_graph is one launch and one device->host copy.
+
+constexpr int SMALL_THREADS = 1024;
+constexpr int64_t SMALL_MAX = 8192;
+
+__device__ int32_t block_inclusive_scan(int32_t* a, int n, int32_t* s_warp) {
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int per = (n + NT - 1) / NT;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  int32_t sum = 0;
+  for (int i = lo; i < hi; i++) sum += a[i];
+  const int lane = tid & 31, w = tid >> 5;
+  int32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int32_t v = lane < (NT >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    s_warp[lane] = v;
+  }
+  __syncthreads();
+  int32_t run = x - sum + (w > 0 ? s_warp[w - 1] : 0);
+  for (int i = lo; i < hi; i++) {
+    run += a[i];
+    a[i] = run;
+  }
+  const int32_t total = s_warp[(NT >> 5) - 1];
+  __syncthreads();
+  return total;
+}
+
+// ascending by (K1, K2, V); P2 a power of two
+__device__ void block_bitonic(uint64_t* K1, uint64_t* K2, int32_t* V, int P2) {
+  for (int size = 2; size <= P2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (P2 >> 1); t += blockDim.x) {
+        const int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
+        const int j = i + stride;
+        const bool gt = K1[i] != K1[j] ? K1[i] > K1[j] : (K2[i] != K2[j] ? K2[i] > K2[j] : V[i] > V[j]);
+        const bool up = (i & size) == 0;
+        if (gt == up) {
+          const uint64_t a = K1[i], b = K2[i];
+          const int32_t c = V[i];
+          K1[i] = K1[j];
+          K2[i] = K2[j];
+          V[i] = V[j];
+          K1[j] = a;
+          K2[j] = b;
+          V[j] = c;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+__device__ __forceinline__ int pow2ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+struct SmallArgs {
+  const int64_t* name_off;
+  const uint8_t* names;
+  const uint8_t* op;
+  const uint8_t* w_rank;
+  const int64_t* w_shape;
+  const uint8_t* w_train;
+  const int64_t* in_off;
+  const int32_t* in_idx;
+  int64_t n;
+  int32_t D;
+  int32_t min_dup;
+  uint64_t seed;
+  int32_t *depth, *pend, *pos, *gparent, *gclass, *act, *flag, *cid;
+  uint64_t *ph, *rh;
+  int64_t* cur;
+  unsigned long long* gkey;
+  int32_t *sorted, *gstart, *corder, *cstart, *info, *collision;
+  uint8_t *gaccept, *residual, *next_flag;
+};
+
+__global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ int32_t s_warp[32];
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int n = (int)a.n, D = a.D;
+  const int P2max = pow2ceil(n);
+  uint64_t* K1 = (uint64_t*)sm;
+  uint64_t* K2 = K1 + P2max;
+  int32_t* V = (int32_t*)(K2 + P2max);
+  for (int i = tid; i < n; i += NT) {
+    int32_t d = 1;
+    for (int64_t k = a.name_off[i]; k < a.name_off[i + 1]; k++) d += a.names[k] == '/';
+    a.depth[i] = d;
+    name_hash_one(i, a.name_off, a.names, a.n, D, a.seed, a.pend, a.ph, a.rh);
+    a.gparent[i] = 0;
+    a.residual[i] = 0;
+    a.cur[i] = -1;
+    a.act[i] = i;
+  }
+  __syncthreads();
+  int nA = n;
+  int level = 1;
+  for (; nA > 0 && level <= D; level++) {
+    const int dd = level - 1;
+    int32_t* srt = a.sorted + (int64_t)dd * n;
+    int32_t* gs = a.gstart + (int64_t)dd * (n + 1);
+    int32_t* co = a.corder + (int64_t)dd * n;
+    int32_t* cs = a.cstart + (int64_t)dd * (n + 1);
+    uint8_t* ga = a.gaccept + (int64_t)dd * n;
+    // 1. sort active nodes by (prefix hash, rel hash)
+    const int P2 = pow2ceil(nA);
+    for (int i = tid; i < P2; i += NT) {
+      if (i < nA) {
+        const int32_t v = a.act[i];
+        K1[i] = a.ph[(int64_t)v * D + dd];
+        K2[i] = a.rh[(int64_t)v * D + dd];
+        V[i] = v;
+      } else {
+        K1[i] = K2[i] = ~0ULL;
+        V[i] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    block_bitonic(K1, K2, V, P2);
+    for (int i = tid; i < nA; i += NT) {
+      srt[i] = V[i];
+      a.flag[i] = (i == 0 || K1[i] != K1[i - 1]) ? 1 : 0;
+    }
+    __syncthreads();
+    const int nG = block_inclusive_scan(a.flag, nA, s_warp);
+    const int64_t stamp = ((int64_t)level) << 32;
+    for (int i = tid; i < nA; i += NT) {
+      const int32_t g = a.flag[i] - 1;
+      a.cur[srt[i]] = stamp | (int64_t)g;
+      if (i == 0 || a.flag[i - 1] != a.flag[i]) gs[g] = i;
+    }
+    for (int g = tid; g < nG; g += NT) a.gkey[g] = 0;
+    if (tid == 0) gs[nG] = nA;
+    __syncthreads();
+    // 2. entry hashes / group keys
+    for (int i = tid; i < nA; i += NT)
+      entry_one(i, srt, a.flag, nA, gs, a.cur, a.rh, D, dd, a.op, a.w_rank, a.w_shape, a.w_train, a.in_off,
+                a.in_idx, a.pos, a.gkey);
+    __syncthreads();
+    // 3. classes: sort groups by (parent, key)
+    const int P2g = pow2ceil(nG);
+    for (int g = tid; g < P2g; g += NT) {
+      if (g < nG) {
+        K1[g] = (uint64_t)(uint32_t)a.gparent[srt[gs[g]]];
+        K2[g] = fmix64((uint64_t)a.gkey[g] ^ fmix64((uint64_t)(gs[g + 1] - gs[g]) + 0x1f83d9abfb41bd6bULL));
+        V[g] = g;
+      } else {
+        K1[g] = K2[g] = ~0ULL;
+        V[g] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    block_bitonic(K1, K2, V, P2g);
+    for (int j = tid; j < nG; j += NT) {
+      co[j] = V[j];
+      a.cid[j] = (j == 0 || K1[j] != K1[j - 1] || K2[j] != K2[j - 1]) ? 1 : 0;
+    }
+    __syncthreads();
+    const int nC = block_inclusive_scan(a.cid, nG, s_warp);
+    for (int j = tid; j < nG; j += NT) {
+      const int32_t c = a.cid[j] - 1;
+      a.gclass[co[j]] = c;
+      if (j == 0 || a.cid[j - 1] != a.cid[j]) cs[c] = j;
+    }
+    if (tid == 0) cs[nC] = nG;
+    __syncthreads();
+    // 4. exact verification, 5. accept / residual / descend
+    for (int i = tid; i < nA; i += NT)
+      verify_one(i, srt, a.flag, nA, nG, gs, a.gclass, cs, co, a.cur, a.pos, a.pend, a.rh, D, dd, a.name_off,
+                 a.names, a.op, a.w_rank, a.w_shape, a.w_train, a.in_off, a.in_idx, a.collision);
+    for (int i = tid; i < nA; i += NT)
+      accept_one(i, srt, a.flag, nA, nC, nG, a.gclass, cs, a.depth, level, a.min_dup, a.gparent, a.next_flag,
+                 a.residual, ga);
+    __syncthreads();
+    for (int i = tid; i < nA; i += NT) a.cid[i] = a.next_flag[i];
+    __syncthreads();
+    const int nNext = block_inclusive_scan(a.cid, nA, s_warp);
+    for (int i = tid; i < nA; i += NT)
+      if (a.next_flag[i]) a.act[a.cid[i] - 1] = srt[i];
+    if (tid == 0) {
+      a.info[dd * 4 + 0] = nA;
+      a.info[dd * 4 + 1] = nG;
+      a.info[dd * 4 + 2] = nC;
+    }
+    nA = nNext;
+    __syncthreads();
+  }
+  if (tid == 0) a.info[D * 4] = nA > 0 ? -1 : level - 1;
 }
 
 inline int grid_for(int64_t n, int sms) {
@@ -373,51 +617,92 @@ int strcmp_py(const uint8_t* a, int64_t la, const uint8_t* b, int64_t lb) {
 void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
   const int64_t n = g->n_nodes;
   if (n < 1) throw Error(SP_ERR_CONFIG, "graph has no nodes");
+  if (n >= (int64_t)INT32_MAX) throw Error(SP_ERR_UNSUPPORTED, "more than 2^31 nodes");
   cudaStream_t s = ctx->stream;
   dg->ctx = ctx;
   dg->n = n;
   dg->E = g->in_off[n];
   const int64_t nb = g->name_off[n];
+  for (int64_t i = 0; i < n; i++)
+    if (g->act_rank[i] < 1 || g->act_rank[i] > SP_MAX_RANK || g->w_rank[i] > SP_MAX_RANK)
+      throw Error(SP_ERR_UNSUPPORTED, "tensor rank outside 1..SP_MAX_RANK");
+  for (int64_t e = 0; e < dg->E; e++)
+    if (g->in_idx[e] < 0 || g->in_idx[e] >= n) throw Error(SP_ERR_CONFIG, "producer index out of range");
+  // host copies the library itself needs (string order, slot order, op validity)
   dg->h_names.assign(g->name_bytes, g->name_bytes + nb);
   dg->h_name_off.assign(g->name_off, g->name_off + n + 1);
   dg->h_topo.assign(g->topo_rank, g->topo_rank + n);
   dg->h_op.assign(g->op, g->op + n);
-  dg->h_act_rank.assign(g->act_rank, g->act_rank + n);
   dg->h_w_rank.assign(g->w_rank, g->w_rank + n);
-  dg->h_w_train.assign(g->w_trainable, g->w_trainable + n);
-  dg->h_act_shape.assign(g->act_shape, g->act_shape + n * SP_MAX_RANK);
-  dg->h_w_shape.assign(g->w_shape, g->w_shape + n * SP_MAX_RANK);
-  dg->h_act_bytes.assign(g->act_bytes, g->act_bytes + n);
-  dg->h_w_bytes.assign(g->w_bytes, g->w_bytes + n);
-  dg->h_in_off.assign(g->in_off, g->in_off + n + 1);
-  dg->h_in_idx.assign(g->in_idx, g->in_idx + dg->E);
-  for (int64_t i = 0; i < n; i++) {
-    if (dg->h_act_rank[i] < 1 || dg->h_act_rank[i] > SP_MAX_RANK || dg->h_w_rank[i] > SP_MAX_RANK)
-      throw Error(SP_ERR_UNSUPPORTED, "tensor rank outside 1..SP_MAX_RANK");
-  }
-  for (int64_t e = 0; e < dg->E; e++)
-    if (dg->h_in_idx[e] < 0 || dg->h_in_idx[e] >= n) throw Error(SP_ERR_CONFIG, "producer index out of range");
-  dg->names.upload(dg->h_names.data(), nb, s);
-  dg->name_off.upload(dg->h_name_off.data(), n + 1, s);
-  dg->topo.upload(dg->h_topo.data(), n, s);
-  dg->op.upload(dg->h_op.data(), n, s);
-  dg->act_rank.upload(dg->h_act_rank.data(), n, s);
-  dg->w_rank.upload(dg->h_w_rank.data(), n, s);
-  dg->w_train.upload(dg->h_w_train.data(), n, s);
-  dg->act_shape.upload(dg->h_act_shape.data(), n * SP_MAX_RANK, s);
-  dg->w_shape.upload(dg->h_w_shape.data(), n * SP_MAX_RANK, s);
-  dg->act_bytes.upload(dg->h_act_bytes.data(), n, s);
-  dg->w_bytes.upload(dg->h_w_bytes.data(), n, s);
-  dg->in_off.upload(dg->h_in_off.data(), n + 1, s);
-  dg->in_idx.upload(dg->h_in_idx.data(), dg->E, s);
   int32_t maxd = 1;
-  for (int64_t i = 0; i < n; i++) {
+  {
     int32_t d = 1;
-    for (int64_t k = dg->h_name_off[i]; k < dg->h_name_off[i + 1]; k++) d += dg->h_names[k] == '/';
+    int64_t node = 0;
+    for (int64_t k = 0; k < nb; k++) {
+      while (node < n && k >= g->name_off[node + 1]) {
+        maxd = std::max(maxd, d);
+        d = 1;
+        node++;
+      }
+      d += g->name_bytes[k] == '/';
+    }
     maxd = std::max(maxd, d);
   }
   dg->max_depth = maxd;
+  // every array in ONE pinned staging buffer and ONE host->device copy
+  struct Part {
+    const void* src;
+    size_t bytes;
+    size_t off;
+  };
+  Part parts[13] = {
+      {g->name_bytes, (size_t)nb, 0},
+      {g->name_off, (size_t)(n + 1) * 8, 0},
+      {g->topo_rank, (size_t)n * 8, 0},
+      {g->op, (size_t)n, 0},
+      {g->act_rank, (size_t)n, 0},
+      {g->w_rank, (size_t)n, 0},
+      {g->w_trainable, (size_t)n, 0},
+      {g->act_shape, (size_t)n * SP_MAX_RANK * 8, 0},
+      {g->w_shape, (size_t)n * SP_MAX_RANK * 8, 0},
+      {g->act_bytes, (size_t)n * 8, 0},
+      {g->w_bytes, (size_t)n * 8, 0},
+      {g->in_off, (size_t)(n + 1) * 8, 0},
+      {g->in_idx, (size_t)dg->E * 4, 0},
+  };
+  size_t total = 0;
+  for (Part& p : parts) {
+    p.off = total;
+    total += (p.bytes + 255) & ~(size_t)255;
+  }
+  if (ctx->staging_bytes < total) {
+    if (ctx->staging) cudaFreeHost(ctx->staging);
+    ctx->staging = nullptr;
+    SP_CUDA(cudaHostAlloc(&ctx->staging, total, cudaHostAllocDefault));
+    ctx->staging_bytes = total;
+  }
+  // the previous upload may still be reading the staging buffer
   SP_CUDA(cudaStreamSynchronize(s));
+  uint8_t* st = (uint8_t*)ctx->staging;
+  for (const Part& p : parts)
+    if (p.bytes) std::memcpy(st + p.off, p.src, p.bytes);
+  dg->arena.alloc(total, s);
+  g_h2d_bytes += (int64_t)total;
+  SP_CUDA(cudaMemcpyAsync(dg->arena.p, st, total, cudaMemcpyHostToDevice, s));
+  uint8_t* base = dg->arena.p;
+  dg->names.p = base + parts[0].off;
+  dg->name_off.p = (int64_t*)(base + parts[1].off);
+  dg->topo.p = (int64_t*)(base + parts[2].off);
+  dg->op.p = base + parts[3].off;
+  dg->act_rank.p = base + parts[4].off;
+  dg->w_rank.p = base + parts[5].off;
+  dg->w_train.p = base + parts[6].off;
+  dg->act_shape.p = (int64_t*)(base + parts[7].off);
+  dg->w_shape.p = (int64_t*)(base + parts[8].off);
+  dg->act_bytes.p = (int64_t*)(base + parts[9].off);
+  dg->w_bytes.p = (int64_t*)(base + parts[10].off);
+  dg->in_off.p = (int64_t*)(base + parts[11].off);
+  dg->in_idx.p = (int32_t*)(base + parts[12].off);
 }
 
 template <class T>
@@ -426,6 +711,198 @@ __global__ void k_gather(const int32_t* __restrict__ idx, int64_t m, const T* __
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[idx[i]];
+}
+
+// Host ordering: the string-order decisions of pruning.py:136-148, 200 over
+// the device partition (instances and blocks by prefix string, template by
+// topological rank).  O(accepted groups log) string compares.
+static void fold_finalize(sp_dgraph* dg, const std::vector<LevelOut>& levels, const std::vector<uint8_t>& resid_h,
+                          const std::vector<int32_t>& pend_h, int32_t D, sp_fold* out) {
+  const int64_t n = dg->n;
+  const uint8_t* names = dg->h_names.data();
+  const int64_t* noff = dg->h_name_off.data();
+  const int64_t* topo = dg->h_topo.data();
+  struct Block {
+    int64_t pnode, plen;
+    std::vector<int64_t> inst_node, inst_len;
+    std::vector<int32_t> members;  // instance-major
+    int64_t T;
+  };
+  std::vector<Block> blocks;
+  for (const LevelOut& lv : levels) {
+    const int64_t dd = lv.level - 1;
+    const int64_t nC = (int64_t)lv.cstart.size() - 1;
+    for (int64_t c = 0; c < nC; c++) {
+      const int32_t g0 = lv.corder[lv.cstart[c]];
+      if (!lv.gaccept[g0]) continue;
+      std::vector<int32_t> gs(lv.corder.begin() + lv.cstart[c], lv.corder.begin() + lv.cstart[c + 1]);
+      auto gprefix = [&](int32_t g, int64_t* node, int64_t* len) {
+        *node = lv.sorted[lv.gstart[g]];
+        *len = pend_h[(size_t)(*node) * D + dd];
+      };
+      std::sort(gs.begin(), gs.end(), [&](int32_t a, int32_t b) {
+        int64_t na, la, nb, lb;
+        gprefix(a, &na, &la);
+        gprefix(b, &nb, &lb);
+        return strcmp_py(names + noff[na], la, names + noff[nb], lb) < 0;
+      });
+      const int32_t tg = gs[0];
+      const int64_t T = lv.gstart[tg + 1] - lv.gstart[tg];
+      std::vector<int32_t> canon(T);  // template position -> canonical position
+      std::iota(canon.begin(), canon.end(), 0);
+      std::sort(canon.begin(), canon.end(), [&](int32_t a, int32_t b) {
+        return topo[lv.sorted[lv.gstart[tg] + a]] < topo[lv.sorted[lv.gstart[tg] + b]];
+      });
+      Block B;
+      gprefix(tg, &B.pnode, &B.plen);
+      B.T = T;
+      for (int32_t g : gs) {
+        int64_t pn, pl;
+        gprefix(g, &pn, &pl);
+        B.inst_node.push_back(pn);
+        B.inst_len.push_back(pl);
+        for (int64_t tpos = 0; tpos < T; tpos++) B.members.push_back(lv.sorted[lv.gstart[g] + canon[tpos]]);
+      }
+      blocks.push_back(std::move(B));
+    }
+  }
+  for (int64_t i = 0; i < n; i++) {
+    if (!resid_h[i]) continue;
+    Block B;
+    B.pnode = i;
+    B.plen = noff[i + 1] - noff[i];
+    B.T = 1;
+    B.inst_node.push_back(i);
+    B.inst_len.push_back(B.plen);
+    B.members.push_back((int32_t)i);
+    blocks.push_back(std::move(B));
+  }
+  std::vector<int64_t> order(blocks.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    const Block& A = blocks[a];
+    const Block& Bb = blocks[b];
+    return strcmp_py(names + noff[A.pnode], A.plen, names + noff[Bb.pnode], Bb.plen) < 0;
+  });
+  out->block_T.clear();
+  out->block_inst_off.assign(1, 0);
+  out->block_member_off.assign(1, 0);
+  out->inst_prefix_node.clear();
+  out->inst_prefix_len.clear();
+  out->members.clear();
+  for (int64_t bi : order) {
+    const Block& B = blocks[bi];
+    out->block_T.push_back(B.T);
+    out->inst_prefix_node.insert(out->inst_prefix_node.end(), B.inst_node.begin(), B.inst_node.end());
+    out->inst_prefix_len.insert(out->inst_prefix_len.end(), B.inst_len.begin(), B.inst_len.end());
+    out->members.insert(out->members.end(), B.members.begin(), B.members.end());
+    out->block_inst_off.push_back((int64_t)out->inst_prefix_node.size());
+    out->block_member_off.push_back((int64_t)out->members.size());
+  }
+  if ((int64_t)out->members.size() != n) throw Error(SP_ERR_CUDA, "fold did not cover every node exactly once");
+  sp_blocks& v = out->view;
+  v.n_blocks = (int64_t)out->block_T.size();
+  v.n_instances = (int64_t)out->inst_prefix_node.size();
+  v.n_members = (int64_t)out->members.size();
+  v.block_T = out->block_T.data();
+  v.block_inst_off = out->block_inst_off.data();
+  v.block_member_off = out->block_member_off.data();
+  v.inst_prefix_node = out->inst_prefix_node.data();
+  v.inst_prefix_len = out->inst_prefix_len.data();
+  v.members = out->members.data();
+}
+
+// One launch + one device->host copy for graphs of <= SMALL_MAX nodes.
+static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed, sp_fold* out,
+                            bool* collided) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = dg->n;
+  const int32_t D = dg->max_depth;
+  // one arena for scratch + outputs
+  const size_t nd = (size_t)n * D, nd1 = (size_t)(n + 1) * D;
+  DevBuf<int32_t> i32;
+  DevBuf<uint64_t> u64;
+  DevBuf<uint8_t> u8;
+  // i32: depth pend pos gparent gclass act flag cid | sorted gstart corder cstart info collision
+  const size_t i32_scratch = 7 * (size_t)n + nd;
+  const size_t i32_out = nd + nd1 + nd + nd1 + (size_t)(4 * D + 4) + 1;
+  i32.alloc(i32_scratch + i32_out, s);
+  u64.alloc(2 * nd + 2 * (size_t)n, s);  // ph rh cur gkey
+  u8.alloc(nd + 2 * (size_t)n, s);       // gaccept residual next_flag
+  SmallArgs A;
+  A.name_off = dg->name_off.p;
+  A.names = dg->names.p;
+  A.op = dg->op.p;
+  A.w_rank = dg->w_rank.p;
+  A.w_shape = dg->w_shape.p;
+  A.w_train = dg->w_train.p;
+  A.in_off = dg->in_off.p;
+  A.in_idx = dg->in_idx.p;
+  A.n = n;
+  A.D = D;
+  A.min_dup = min_dup;
+  A.seed = seed;
+  int32_t* p = i32.p;
+  A.depth = p; p += n;
+  A.pos = p; p += n;
+  A.gparent = p; p += n;
+  A.gclass = p; p += n;
+  A.act = p; p += n;
+  A.flag = p; p += n;
+  A.cid = p; p += n;
+  A.pend = p; p += nd;
+  int32_t* out0 = p;
+  A.sorted = p; p += nd;
+  A.gstart = p; p += nd1;
+  A.corder = p; p += nd;
+  A.cstart = p; p += nd1;
+  A.info = p; p += 4 * D + 4;
+  A.collision = p; p += 1;
+  A.ph = u64.p;
+  A.rh = u64.p + nd;
+  A.cur = (int64_t*)(u64.p + 2 * nd);
+  A.gkey = (unsigned long long*)(u64.p + 2 * nd + n);
+  A.gaccept = u8.p;
+  A.residual = u8.p + nd;
+  A.next_flag = u8.p + nd + n;
+  SP_CUDA(cudaMemsetAsync(A.collision, 0, sizeof(int32_t), s));
+  const int P2 = [&] { int q = 1; while (q < n) q <<= 1; return q; }();
+  const size_t smem = (size_t)P2 * 20;
+  SP_CUDA(cudaFuncSetAttribute(k_fold_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SP_LAUNCH(ctx, k_fold_small, 1, SMALL_THREADS, smem, s, A);
+  SP_CUDA(cudaGetLastError());
+  // single D2H: outputs (i32 region after scratch), pend, residual + gaccept
+  std::vector<int32_t> h_out(i32_out), pend_h(nd);
+  std::vector<uint8_t> h_u8(nd + n);
+  g_d2h_bytes += (int64_t)(i32_out * 4 + nd * 4 + nd + n);
+  SP_CUDA(cudaMemcpyAsync(h_out.data(), out0, i32_out * 4, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(pend_h.data(), A.pend, nd * 4, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(h_u8.data(), u8.p, nd + n, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const int32_t* h_sorted = h_out.data();
+  const int32_t* h_gstart = h_sorted + nd;
+  const int32_t* h_corder = h_gstart + nd1;
+  const int32_t* h_cstart = h_corder + nd;
+  const int32_t* h_info = h_cstart + nd1;
+  const int32_t coll = h_info[4 * D + 4];
+  *collided = coll != 0;
+  if (*collided) return;
+  const int32_t nlev = h_info[4 * D];
+  if (nlev < 0) throw Error(SP_ERR_CUDA, "fold did not terminate");
+  std::vector<LevelOut> levels;
+  for (int32_t dd = 0; dd < nlev; dd++) {
+    const int32_t nA = h_info[dd * 4], nG = h_info[dd * 4 + 1], nC = h_info[dd * 4 + 2];
+    LevelOut lv;
+    lv.level = dd + 1;
+    lv.sorted.assign(h_sorted + (size_t)dd * n, h_sorted + (size_t)dd * n + nA);
+    lv.gstart.assign(h_gstart + (size_t)dd * (n + 1), h_gstart + (size_t)dd * (n + 1) + nG + 1);
+    lv.corder.assign(h_corder + (size_t)dd * n, h_corder + (size_t)dd * n + nG);
+    lv.cstart.assign(h_cstart + (size_t)dd * (n + 1), h_cstart + (size_t)dd * (n + 1) + nC + 1);
+    lv.gaccept.assign(h_u8.begin() + (size_t)dd * n, h_u8.begin() + (size_t)dd * n + nG);
+    levels.push_back(std::move(lv));
+  }
+  std::vector<uint8_t> resid_h(h_u8.begin() + nd, h_u8.begin() + nd + n);
+  fold_finalize(dg, levels, resid_h, pend_h, D, out);
 }
 
 static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed, sp_fold* out,
@@ -598,106 +1075,18 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   *collided = coll_h != 0;
   if (*collided) return;
 
-  // ---- host ordering: the string-order decisions of pruning.py:136-148, 200 ----
-  const uint8_t* names = dg->h_names.data();
-  const int64_t* noff = dg->h_name_off.data();
-  const int64_t* topo = dg->h_topo.data();
-  struct Block {
-    int64_t pnode, plen;
-    std::vector<int64_t> inst_node, inst_len;
-    std::vector<int32_t> members;  // instance-major
-    int64_t T;
-  };
-  std::vector<Block> blocks;
-  for (const LevelOut& lv : levels) {
-    const int64_t dd = lv.level - 1;
-    const int64_t nC = (int64_t)lv.cstart.size() - 1;
-    for (int64_t c = 0; c < nC; c++) {
-      const int32_t g0 = lv.corder[lv.cstart[c]];
-      if (!lv.gaccept[g0]) continue;
-      std::vector<int32_t> gs(lv.corder.begin() + lv.cstart[c], lv.corder.begin() + lv.cstart[c + 1]);
-      auto gprefix = [&](int32_t g, int64_t* node, int64_t* len) {
-        *node = lv.sorted[lv.gstart[g]];
-        *len = pend_h[(size_t)(*node) * D + dd];
-      };
-      std::sort(gs.begin(), gs.end(), [&](int32_t a, int32_t b) {
-        int64_t na, la, nb, lb;
-        gprefix(a, &na, &la);
-        gprefix(b, &nb, &lb);
-        return strcmp_py(names + noff[na], la, names + noff[nb], lb) < 0;
-      });
-      const int32_t tg = gs[0];
-      const int64_t T = lv.gstart[tg + 1] - lv.gstart[tg];
-      std::vector<int32_t> canon(T);  // template position -> canonical position
-      std::iota(canon.begin(), canon.end(), 0);
-      std::sort(canon.begin(), canon.end(), [&](int32_t a, int32_t b) {
-        return topo[lv.sorted[lv.gstart[tg] + a]] < topo[lv.sorted[lv.gstart[tg] + b]];
-      });
-      Block B;
-      gprefix(tg, &B.pnode, &B.plen);
-      B.T = T;
-      for (int32_t g : gs) {
-        int64_t pn, pl;
-        gprefix(g, &pn, &pl);
-        B.inst_node.push_back(pn);
-        B.inst_len.push_back(pl);
-        for (int64_t tpos = 0; tpos < T; tpos++) B.members.push_back(lv.sorted[lv.gstart[g] + canon[tpos]]);
-      }
-      blocks.push_back(std::move(B));
-    }
-  }
-  for (int64_t i = 0; i < n; i++) {
-    if (!resid_h[i]) continue;
-    Block B;
-    B.pnode = i;
-    B.plen = noff[i + 1] - noff[i];
-    B.T = 1;
-    B.inst_node.push_back(i);
-    B.inst_len.push_back(B.plen);
-    B.members.push_back((int32_t)i);
-    blocks.push_back(std::move(B));
-  }
-  std::vector<int64_t> order(blocks.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-    const Block& A = blocks[a];
-    const Block& Bb = blocks[b];
-    return strcmp_py(names + noff[A.pnode], A.plen, names + noff[Bb.pnode], Bb.plen) < 0;
-  });
-  out->block_T.clear();
-  out->block_inst_off.assign(1, 0);
-  out->block_member_off.assign(1, 0);
-  out->inst_prefix_node.clear();
-  out->inst_prefix_len.clear();
-  out->members.clear();
-  for (int64_t bi : order) {
-    const Block& B = blocks[bi];
-    out->block_T.push_back(B.T);
-    out->inst_prefix_node.insert(out->inst_prefix_node.end(), B.inst_node.begin(), B.inst_node.end());
-    out->inst_prefix_len.insert(out->inst_prefix_len.end(), B.inst_len.begin(), B.inst_len.end());
-    out->members.insert(out->members.end(), B.members.begin(), B.members.end());
-    out->block_inst_off.push_back((int64_t)out->inst_prefix_node.size());
-    out->block_member_off.push_back((int64_t)out->members.size());
-  }
-  if ((int64_t)out->members.size() != n) throw Error(SP_ERR_CUDA, "fold did not cover every node exactly once");
-  sp_blocks& v = out->view;
-  v.n_blocks = (int64_t)out->block_T.size();
-  v.n_instances = (int64_t)out->inst_prefix_node.size();
-  v.n_members = (int64_t)out->members.size();
-  v.block_T = out->block_T.data();
-  v.block_inst_off = out->block_inst_off.data();
-  v.block_member_off = out->block_member_off.data();
-  v.inst_prefix_node = out->inst_prefix_node.data();
-  v.inst_prefix_len = out->inst_prefix_len.data();
-  v.members = out->members.data();
+  fold_finalize(dg, levels, resid_h, pend_h, D, out);
 }
 
 void fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold* out) {
   if (min_dup < 1) throw Error(SP_ERR_CONFIG, "min_duplicates must be >= 1");
   bool collided = false;
   for (int attempt = 0; attempt < 8; attempt++) {
-    fold_once(ctx, dg, min_dup, 0x243f6a8885a308d3ULL + 0x9e3779b97f4a7c15ULL * (uint64_t)attempt, out,
-              &collided);
+    const uint64_t seed = 0x243f6a8885a308d3ULL + 0x9e3779b97f4a7c15ULL * (uint64_t)attempt;
+    if (dg->n <= SMALL_MAX && dg->max_depth <= 64 && !getenv("SP_FOLD_MULTI"))
+      fold_once_small(ctx, dg, min_dup, seed, out, &collided);
+    else
+      fold_once(ctx, dg, min_dup, seed, out, &collided);
     if (!collided) return;
   }
   throw Error(SP_ERR_CUDA, "fold hash verification failed on every seed");

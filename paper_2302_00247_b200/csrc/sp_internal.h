@@ -96,6 +96,8 @@ struct sp_ctx {
   cudaEvent_t timer[2] = {};
   // scratch reused across calls
   sp::DevBuf<uint8_t> cub_tmp;
+  void* staging = nullptr;  // pinned host staging for graph uploads
+  size_t staging_bytes = 0;
 };
 
 // Device-resident lowered graph (+ the host copies the library needs).
@@ -103,16 +105,19 @@ struct sp_dgraph {
   sp_ctx* ctx = nullptr;
   int64_t n = 0, E = 0;
   int32_t max_depth = 1;
-  // host copies
+  // host copies the library needs (string order, slot order, op validity)
   std::vector<uint8_t> h_names;
   std::vector<int64_t> h_name_off, h_topo;
-  std::vector<uint8_t> h_op, h_act_rank, h_w_rank, h_w_train;
-  std::vector<int64_t> h_act_shape, h_act_bytes, h_w_shape, h_w_bytes, h_in_off;
-  std::vector<int32_t> h_in_idx;
-  // device copies
-  sp::DevBuf<uint8_t> names, op, act_rank, w_rank, w_train;
-  sp::DevBuf<int64_t> name_off, topo, act_shape, act_bytes, w_shape, w_bytes, in_off;
-  sp::DevBuf<int32_t> in_idx;
+  std::vector<uint8_t> h_op, h_w_rank;
+  // device copies: views into one arena filled by a single H2D copy
+  sp::DevBuf<uint8_t> arena;
+  template <class T>
+  struct View {
+    T* p = nullptr;
+  };
+  View<uint8_t> names, op, act_rank, w_rank, w_train;
+  View<int64_t> name_off, topo, act_shape, act_bytes, w_shape, w_bytes, in_off;
+  View<int32_t> in_idx;
 };
 
 struct sp_fold {

@@ -358,8 +358,22 @@ def main() -> None:
     plan_case("c4_2x4", "c4", c4, m24)
     plan_case("c4_2x4_slow", "c4", c4, m24_slow)
 
+    # --- fold stress (config 4 scale-up): only hashes are committed; the graph is
+    #     regenerated by paper_2302_00247_b200.workloads.transformer_stack ----------------
+    stress = []
+    for L in (480, 7000):
+        t0 = time.perf_counter()
+        g = trim_and_group(gen_transformer_stack(L))
+        for md in (2, 3):
+            subs = prune_graph(g, md)
+            stress.append({"layers": L, "min_dup": md, "nodes": len(g),
+                           "graph_sha": sha(dump_graph(g)), "prune_sha": sha(prune_doc(subs)),
+                           "blocks": len(subs),
+                           "multiplicities": sorted(s.multiplicity for s in subs)})
+        print(f"  fold stress L={L}: {len(g)} nodes, {time.perf_counter() - t0:.1f}s", flush=True)
+
     out = {"generator": "tests/golden/make_golden.py", "reference": "shardplan 0.1.0",
-           "cases": cases}
+           "cases": cases, "fold_stress": stress}
     with open(os.path.join(HERE, "cases.json"), "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
         fh.write("\n")

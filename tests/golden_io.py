@@ -14,9 +14,17 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 @functools.lru_cache(maxsize=1)
-def cases() -> list:
+def _doc() -> dict:
     with open(os.path.join(GOLDEN, "cases.json")) as fh:
-        return json.load(fh)["cases"]
+        return json.load(fh)
+
+
+def cases() -> list:
+    return _doc()["cases"]
+
+
+def fold_stress() -> list:
+    return _doc()["fold_stress"]
 
 
 def case(name: str) -> dict:

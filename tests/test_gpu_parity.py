@@ -185,3 +185,41 @@ def test_c2_decoder_block_full_vs_oracle(backend):
             exp.valid, exp.best_index, exp.best_total)
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("idx", range(4))
+def test_fold_stress_vs_reference_hash(backend, idx):
+    """~10^4 and ~10^5-GraphNode folds (multi-kernel path) reproduce the reference."""
+    import hashlib
+
+    from golden_io import fold_stress
+    from paper_2302_00247_b200.blocks import to_prune_doc
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from paper_2302_00247_b200.workloads import transformer_stack
+
+    fs = fold_stress()[idx]
+    low = lower(transformer_stack(fs["layers"]))
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, fs["min_dup"], session=ses)
+    doc = to_prune_doc(low, ba)
+    assert hashlib.sha256(canon(doc).encode()).hexdigest() == fs["prune_sha"]
+
+
+@pytest.mark.parametrize("seed", range(0, 40, 3))
+def test_multi_kernel_fold_path_vs_oracle(backend, seed, monkeypatch):
+    """Force the multi-kernel (CUB) fold on small graphs: same partition as the oracle."""
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays, to_prune_doc
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    monkeypatch.setenv("SP_FOLD_MULTI", "1")
+    g = random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11))
+    low = lower(g)
+    ses = Session.open(low, backend)
+    for md in (1, 2, 3):
+        ba = fold_blocks(low, md, session=ses)
+        ob = BlockArrays.from_dict(oracle.prune(low, md))
+        assert to_prune_doc(low, ba) == to_prune_doc(low, ob)

@@ -1,0 +1,56 @@
+"""Pin the in-package graph generators to the reference-generated fixtures."""
+
+from __future__ import annotations
+
+import pytest
+
+from golden_io import graph
+from paper_2302_00247_b200.ir import dump_grouped
+from paper_2302_00247_b200.workloads import transformer_stack, wide_classifier
+
+
+@pytest.mark.parametrize("path,kw", [
+    ("graphs/tiny_transformer.json.gz", dict(layers=2, d_model=8)),
+    ("graphs/tiny_transformer_f64.json.gz", dict(layers=2, d_model=8, dtype="f64")),
+    ("graphs/c1.json.gz", dict(layers=12, d_model=768, heads=12)),
+    ("graphs/c4.json.gz", dict(layers=48, d_model=6144, heads=48)),
+    ("graphs/bench_L48.json.gz", dict(layers=48, d_model=8, heads=2)),
+    ("graphs/crit5.json.gz", dict(layers=4, d_model=512, heads=8, batch=96, seq=16)),
+    ("graphs/tf24.json.gz", dict(layers=24)),
+])
+def test_transformer_stack_matches_reference(path, kw):
+    assert dump_grouped(transformer_stack(**kw)) == dump_grouped(graph(path))
+
+
+@pytest.mark.parametrize("path,kw", [
+    ("graphs/c3.json.gz", dict(num_classes=100000, feature_dim=2048, blocks=16, batch=32)),
+    ("graphs/tiny_classifier_f64.json.gz", dict(num_classes=64, feature_dim=16, dtype="f64")),
+    ("graphs/wide150.json.gz", dict(num_classes=64, feature_dim=16, blocks=150)),
+])
+def test_wide_classifier_matches_reference(path, kw):
+    assert dump_grouped(wide_classifier(**kw)) == dump_grouped(graph(path))
+
+
+def _sha(obj) -> str:
+    import hashlib
+    import json
+
+    return hashlib.sha256(json.dumps(obj, sort_keys=True, separators=(",", ":")).encode()).hexdigest()
+
+
+@pytest.mark.parametrize("idx", range(4))
+def test_fold_stress_graph_and_oracle_pinned(idx):
+    """Config-4 fold stress (L=480 / 7000 layers): generator == reference graph and
+    oracle prune == reference prune, by hash."""
+    from golden_io import fold_stress
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays, to_prune_doc
+    from paper_2302_00247_b200.lowering import lower
+
+    fs = fold_stress()[idx]
+    g = transformer_stack(fs["layers"])
+    assert len(g.nodes) == fs["nodes"]
+    assert _sha(dump_grouped(g)) == fs["graph_sha"]
+    low = lower(g)
+    ba = BlockArrays.from_dict(oracle.prune(low, fs["min_dup"]))
+    assert _sha(to_prune_doc(low, ba)) == fs["prune_sha"]

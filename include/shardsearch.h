@@ -189,6 +189,12 @@ int sp_tables_slots(const sp_tables* t, int64_t block, int32_t* slot_pos, int32_
  * range (search.py:331-336); results merge exactly with sp_merge_keys.
  */
 int sp_score(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out);
+/*
+ * Single-device search of every block in one call: sp_score followed by the
+ * winner detail of sp_explain_all, chained on the device (one host sync).
+ */
+int sp_search(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* blocks,
+              int8_t* node_detail, int8_t* edge_detail);
 /* Score [lo, hi) of one block; optional per-candidate totals (NaN = invalid). */
 int sp_score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi,
                    double* totals, sp_score_out* out);

@@ -63,12 +63,14 @@ def _declare(L):
     L.sp_timer_stop.argtypes = [vp, C.POINTER(C.c_double)]
     L.sp_launch_counts.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.sp_tables_bytes.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.sp_search.argtypes = [vp, vp, C.POINTER(SpScoreOut), C.POINTER(SpExplainBlock),
+                            C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_tables_sizes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.sp_tables_edge_offsets.argtypes = [vp, C.POINTER(C.c_int64)]
     L.sp_explain_all.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(SpExplainBlock),
                                  C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_copy_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-    for name in ("sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
+    for name in ("sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
                  "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
                  "sp_score_range", "sp_explain", "sp_last_timings"):
         getattr(L, name).restype = C.c_int
@@ -98,7 +100,7 @@ EXPORTED_SYMBOLS = (
     "sp_tables_free", "sp_tables_candidates", "sp_tables_slots", "sp_score", "sp_score_range",
     "sp_merge_keys", "sp_explain", "sp_last_timings", "sp_timer_start", "sp_timer_stop",
     "sp_launch_counts", "sp_copy_bytes", "sp_tables_bytes", "sp_tables_sizes",
-    "sp_tables_edge_offsets", "sp_explain_all",
+    "sp_tables_edge_offsets", "sp_explain_all", "sp_search",
 )
 
 
@@ -228,18 +230,33 @@ class Backend:
                                         C.byref(ne)), "sp_explain")
         return out, [edges[i] for i in range(min(ne.value, cap))]
 
-    def explain_all(self, t: Tables, indices) -> tuple:
-        """Winner detail of every block: (blocks, node_detail [ne,4], edge_detail [nedge,2],
-        edge_off [nb+1])."""
+    def _detail_buffers(self, t: Tables):
         nb = t.n_blocks
         ne, nedge = C.c_int64(), C.c_int64()
         self.lib.sp_tables_sizes(t.ptr, C.byref(ne), C.byref(nedge))
-        idx = np.ascontiguousarray(indices, dtype=np.uint64)
         blocks = (SpExplainBlock * max(1, nb))()
         node = np.zeros((max(1, ne.value), 4), np.int8)
         edge = np.zeros((max(1, nedge.value), 2), np.int8)
         eoff = np.zeros(nb + 1, np.int64)
         self.lib.sp_tables_edge_offsets(t.ptr, ptr(eoff, C.c_int64))
+        return blocks, node, edge, eoff
+
+    def search(self, t: Tables) -> tuple:
+        """Score every block and explain each block's argmin in one call (one sync).
+        Returns (scores, (blocks, node_detail, edge_detail, edge_off))."""
+        outs = (SpScoreOut * max(1, t.n_blocks))()
+        blocks, node, edge, eoff = self._detail_buffers(t)
+        self._check(self.lib.sp_search(self.ctx, t.ptr, outs, blocks, ptr(node, C.c_int8),
+                                       ptr(edge, C.c_int8)), "sp_search")
+        nb = t.n_blocks
+        return [outs[i] for i in range(nb)], ([blocks[i] for i in range(nb)], node, edge, eoff)
+
+    def explain_all(self, t: Tables, indices) -> tuple:
+        """Winner detail of every block: (blocks, node_detail [ne,4], edge_detail [nedge,2],
+        edge_off [nb+1])."""
+        nb = t.n_blocks
+        idx = np.ascontiguousarray(indices, dtype=np.uint64)
+        blocks, node, edge, eoff = self._detail_buffers(t)
         self._check(self.lib.sp_explain_all(self.ctx, t.ptr, ptr(idx, C.c_uint64), blocks,
                                             ptr(node, C.c_int8), ptr(edge, C.c_int8)),
                     "sp_explain_all")

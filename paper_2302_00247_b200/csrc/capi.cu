@@ -184,6 +184,15 @@ int sp_score(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_scor
   });
 }
 
+int sp_search(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* blocks, int8_t* node_detail,
+              int8_t* edge_detail) {
+  if (!ctx || !t || !out || !blocks || !node_detail || !edge_detail) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::score_all(ctx, t, 0, 1, out, blocks, node_detail, edge_detail);
+  });
+}
+
 int sp_score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi, double* totals,
                    sp_score_out* out) {
   if (!ctx || !t || !out) return SP_ERR_CONFIG;

@@ -785,7 +785,8 @@ static_assert(sizeof(ExplainBlock) == sizeof(sp_explain_block), "ExplainBlock mi
 __global__ void k_explain_all(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                               const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
                               const uint8_t* bound_of, const uint8_t* blobs, const int64_t* blob_off,
-                              const int64_t* edge_off, const unsigned long long* indices, sp_mesh mesh,
+                              const int64_t* edge_off, const unsigned long long* indices,
+                              const sp_score_out* scores, sp_mesh mesh,
                               int64_t mu, int64_t chunk, ExplainBlock* out, int8_t* node_out, int8_t* edge_out) {
   const MeshC M = mesh_consts(mesh);
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
@@ -795,7 +796,8 @@ __global__ void k_explain_all(GraphView G, const int64_t* tmpl_off, const int32_
     X.forward_comm = X.backward_comm = X.total = 0.0;
     for (int k = 0; k < 4; k++) X.bytes[k] = X.calls[k] = 0;
     X.collective_calls = 0;
-    const unsigned long long index = indices[b];
+    const unsigned long long index =
+        scores ? (scores[b].has_best ? scores[b].best_index : ~0ULL) : indices[b];
     if (index == ~0ULL) {
       out[b] = X;
       continue;
@@ -1095,8 +1097,15 @@ static size_t score_smem(const sp_tables* t) {
   return (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_pool * THREADS * 9 + 16;
 }
 
+struct FusedExplain {
+  void* blocks;
+  int8_t* node;
+  int8_t* edge;
+};
+
 static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long long>& lo,
-                      const std::vector<unsigned long long>& hi, double* d_totals, std::vector<sp_score_out>& res) {
+                      const std::vector<unsigned long long>& hi, double* d_totals, std::vector<sp_score_out>& res,
+                      const FusedExplain* fx = nullptr) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
   res.assign(nb, sp_score_out{});
@@ -1141,6 +1150,27 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);
   SP_CUDA(cudaGetLastError());
+  DevBuf<ExplainBlock> dblk;
+  DevBuf<int8_t> dnode, dedge;
+  DevBuf<int64_t> deoff;
+  if (fx) {
+    // winner detail straight from the device-side argmin: no host round trip
+    TablesPriv* priv = (TablesPriv*)t->priv;
+    const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
+    deoff.upload(t->edge_off.data(), nb + 1, s);
+    dblk.alloc(nb, s);
+    dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
+    dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
+    SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
+              t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
+              priv->dev.slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, deoff.p,
+              (const unsigned long long*)nullptr, dout.p, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p,
+              dedge.p);
+    SP_CUDA(cudaGetLastError());
+    dblk.download((ExplainBlock*)fx->blocks, nb, s);
+    dnode.download(fx->node, 4 * ne, s);
+    dedge.download(fx->edge, 2 * nedge, s);
+  }
   dout.download(res.data(), nb, s);
   SP_CUDA(cudaStreamSynchronize(s));
   float ms = 0;
@@ -1148,7 +1178,8 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   ctx->score_kernel_ms = ms;
 }
 
-void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out) {
+void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out, void* xblocks,
+               int8_t* xnode, int8_t* xedge) {
   if (n_shards < 1 || shard < 0 || shard >= n_shards) throw Error(SP_ERR_CONFIG, "bad shard / n_shards");
   if (t->overflow) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
   const int64_t nb = t->n_blocks;
@@ -1163,7 +1194,8 @@ void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_sc
   }
   SP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   std::vector<sp_score_out> res;
-  run_score(ctx, t, lo, hi, nullptr, res);
+  FusedExplain fx{xblocks, xnode, xedge};
+  run_score(ctx, t, lo, hi, nullptr, res, xblocks ? &fx : nullptr);
   SP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   SP_CUDA(cudaEventSynchronize(ctx->ev[1]));
   float ms = 0;
@@ -1261,7 +1293,7 @@ void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* block
   SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
             t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
             priv->dev.slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, (const int64_t*)(dup.p + nb),
-            dup.p, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p, dedge.p);
+            dup.p, (const sp_score_out*)nullptr, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p, dedge.p);
   SP_CUDA(cudaGetLastError());
   dblk.download((ExplainBlock*)blocks_out, nb, s);
   dnode.download(node_out, 4 * ne, s);

@@ -183,7 +183,8 @@ void fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold* out);
 void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* tmpl_off,
                   const int32_t* tmpl_nodes, const sp_mesh* mesh, int64_t mu, int64_t chunk,
                   sp_tables* out);
-void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out);
+void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out,
+               void* xblocks = nullptr, int8_t* xnode = nullptr, int8_t* xedge = nullptr);
 void score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi,
                  double* totals, sp_score_out* out);
 void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explain_out* out,

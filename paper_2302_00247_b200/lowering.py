@@ -10,12 +10,13 @@ The arrays are built once per graph and uploaded once (``sp_graph_upload``).
 
 from __future__ import annotations
 
+import itertools
 from dataclasses import dataclass
 
 import numpy as np
 
 from .errors import UnsupportedSearch
-from .ir import OP_CODE
+from .ir import DTYPE_WIDTH, OP_CODE
 
 MAX_RANK = 8  # SP_MAX_RANK
 
@@ -52,63 +53,98 @@ class LoweredGraph:
         )
 
 
-def _op_label(op) -> str:
-    return op if isinstance(op, str) else op.value
+_OP_BY_ID: dict = {}
+_WIDTH_BY_ID: dict = {}
+
+
+def _codes(objs: list, cache: dict, fn, dtype) -> np.ndarray:
+    """Map enum members / dtype objects to small ints through an id() cache
+    (enum __hash__ is a Python-level call; members are singletons)."""
+    ids = list(map(id, objs))
+    missing = set(ids).difference(cache)
+    if missing:
+        first = dict(zip(ids, objs))
+        for i in missing:
+            cache[i] = fn(first[i])
+    return np.fromiter(map(cache.__getitem__, ids), dtype, count=len(ids))
+
+
+def _op_code(op) -> int:
+    return OP_CODE[op if isinstance(op, str) else op.value]
+
+
+def _width(dtype) -> int:
+    return DTYPE_WIDTH[dtype] if isinstance(dtype, str) else int(dtype.width)
+
+
+def _shapes(shapes: list, n: int, what: str):
+    """(rank uint8 [n], shape int64 [n, 8], element count int64 [n]) from tuples."""
+    rank = np.fromiter(map(len, shapes), np.int64, count=n)
+    if n and rank.max() > MAX_RANK:
+        raise UnsupportedSearch(f"{what} rank {int(rank.max())} exceeds {MAX_RANK}")
+    out = np.ones((n, MAX_RANK), np.int64)
+    if n and rank.min() == rank.max():  # uniform rank: one reshape, no scatter
+        r = int(rank[0])
+        out[:, :r] = np.fromiter(itertools.chain.from_iterable(shapes), np.int64,
+                                 count=n * r).reshape(n, r)
+    else:
+        flat = np.fromiter(itertools.chain.from_iterable(shapes), np.int64, count=int(rank.sum()))
+        starts = np.zeros(n, np.int64)
+        np.cumsum(rank[:-1], out=starts[1:])
+        rows = np.repeat(np.arange(n), rank)
+        out[rows, np.arange(flat.size) - np.repeat(starts, rank)] = flat
+    elems = out.prod(axis=1)
+    if n and float(out.astype(np.float64).prod(axis=1).max()) * 8 >= 2.0 ** 63:
+        raise UnsupportedSearch(f"{what} byte size beyond int64")
+    out[np.arange(MAX_RANK)[None, :] >= rank[:, None]] = 0
+    return rank.astype(np.uint8), out, elems
 
 
 def lower(graph) -> LoweredGraph:
-    """Flatten a grouped graph; cached on the graph object when possible."""
+    """Flatten a grouped graph (vectorised; cached on the graph object when possible)."""
     cached = getattr(graph, "_sp_lowered", None)
     if isinstance(cached, LoweredGraph) and cached.source is graph:
         return cached
     names = list(graph.topo_order)
     n = len(names)
-    index = {nm: i for i, nm in enumerate(names)}
-    nodes = graph.nodes
-    op = np.empty(n, np.uint8)
-    act_rank = np.empty(n, np.uint8)
-    act_shape = np.zeros((n, MAX_RANK), np.int64)
-    act_bytes = np.empty(n, np.int64)
+    index = dict(zip(names, range(n)))
+    nl = [graph.nodes[nm] for nm in names]
+    op = _codes([nd.op for nd in nl], _OP_BY_ID, _op_code, np.uint8)
+    acts = [nd.activation for nd in nl]
+    act_rank, act_shape, act_el = _shapes([a.shape for a in acts], n, "activation")
+    act_bytes = act_el * _codes([a.dtype for a in acts], _WIDTH_BY_ID, _width, np.int64)
+    ws = [nd.weight for nd in nl]
+    widx = np.fromiter((i for i, w in enumerate(ws) if w is not None), np.int64)
     w_rank = np.zeros(n, np.uint8)
     w_shape = np.zeros((n, MAX_RANK), np.int64)
     w_bytes = np.zeros(n, np.int64)
     w_train = np.zeros(n, np.uint8)
-    in_off = np.empty(n + 1, np.int64)
-    in_idx = []
-    in_off[0] = 0
-    encoded = [nm.encode("utf-8") for nm in names]
-    for i, nm in enumerate(names):
-        nd = nodes[nm]
-        op[i] = OP_CODE[_op_label(nd.op)]
-        a = nd.activation
-        shp = tuple(a.shape)
-        if len(shp) > MAX_RANK:
-            raise UnsupportedSearch(f"activation rank {len(shp)} of {nm!r} exceeds {MAX_RANK}")
-        act_rank[i] = len(shp)
-        act_shape[i, : len(shp)] = shp
-        act_bytes[i] = a.byte_size
-        w = nd.weight
-        if w is not None:
-            ws = tuple(w.shape)
-            if len(ws) > MAX_RANK:
-                raise UnsupportedSearch(f"weight rank {len(ws)} of {nm!r} exceeds {MAX_RANK}")
-            w_rank[i] = len(ws)
-            w_shape[i, : len(ws)] = ws
-            w_bytes[i] = w.byte_size
-            w_train[i] = 1 if w.trainable else 0
-        ins = nd.inputs
-        in_idx.extend(index[r] for r in ins)
-        in_off[i + 1] = in_off[i] + len(ins)
-    lens = np.fromiter((len(b) for b in encoded), np.int64, count=n)
+    if widx.size:
+        wl = [ws[i] for i in widx.tolist()]
+        r, shp, el = _shapes([w.shape for w in wl], len(wl), "weight")
+        w_rank[widx] = r
+        w_shape[widx] = shp
+        w_bytes[widx] = el * _codes([w.dtype for w in wl], _WIDTH_BY_ID, _width, np.int64)
+        w_train[widx] = np.fromiter((1 if w.trainable else 0 for w in wl), np.uint8, count=len(wl))
+    ins = [nd.inputs for nd in nl]
+    deg = np.fromiter(map(len, ins), np.int64, count=n)
+    in_off = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=in_off[1:])
+    in_idx = np.fromiter((index[r] for t in ins for r in t), np.int32, count=int(in_off[-1]))
+    joined = "".join(names)
     name_off = np.zeros(n + 1, np.int64)
-    np.cumsum(lens, out=name_off[1:])
-    name_bytes = np.frombuffer(b"".join(encoded), np.uint8).copy()
+    if joined.isascii():
+        np.cumsum(np.fromiter(map(len, names), np.int64, count=n), out=name_off[1:])
+        name_bytes = np.frombuffer(joined.encode("ascii"), np.uint8).copy()
+    else:
+        encoded = [nm.encode("utf-8") for nm in names]
+        np.cumsum(np.fromiter(map(len, encoded), np.int64, count=n), out=name_off[1:])
+        name_bytes = np.frombuffer(b"".join(encoded), np.uint8).copy()
     low = LoweredGraph(
         names=names, index=index, name_bytes=name_bytes, name_off=name_off,
         topo_rank=np.arange(n, dtype=np.int64), op=op, act_rank=act_rank,
         act_shape=act_shape, act_bytes=act_bytes, w_rank=w_rank, w_shape=w_shape,
-        w_bytes=w_bytes, w_trainable=w_train, in_off=in_off,
-        in_idx=np.asarray(in_idx, dtype=np.int32), source=graph,
+        w_bytes=w_bytes, w_trainable=w_train, in_off=in_off, in_idx=in_idx, source=graph,
     )
     try:
         graph._sp_lowered = low

@@ -229,11 +229,14 @@ _OP_LABELS = ("matmul", "elementwise", "layernorm", "softmax", "embedding", "res
 
 
 def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
-                     types: TypeSet = DEFAULT_TYPES) -> list:
-    """RoutedPlan of every block's argmin from ONE sp_explain_all launch."""
+                     types: TypeSet = DEFAULT_TYPES, detail=None) -> list:
+    """RoutedPlan of every block's argmin from ONE sp_explain_all launch (or the
+    detail sp_search already returned)."""
     low = ses.low
-    idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
-    blocks, node, edge, eoff = ses.backend.explain_all(tables, idx)
+    if detail is None:
+        idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
+        detail = ses.backend.explain_all(tables, idx)
+    blocks, node, edge, eoff = detail
     replica = types.ShardSpec(types.ShardKind.REPLICA)
     identity = types.Collective(types.CollectiveKind.IDENTITY)
     allreduce = types.Collective(types.CollectiveKind.ALL_REDUCE_SUM)
@@ -310,15 +313,19 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
     try:
         if tables.overflow:
             raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")
-        scores = ses.backend.score(tables, shard, n_shards)
-        if exchange is not None:
-            scores = exchange(scores)
+        detail = None
+        if exchange is None and n_shards == 1:
+            scores, detail = ses.backend.search(tables)
+        else:
+            scores = ses.backend.score(tables, shard, n_shards)
+            if exchange is not None:
+                scores = exchange(scores)
         for sc in scores:
             if not sc.has_best:
                 raise AssertionError("all-replica fallback must always route")
             if bad_mu:
                 raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
-        bests = routed_plans_all(ses, tables, subgraphs, scores, mesh, types)
+        bests = routed_plans_all(ses, tables, subgraphs, scores, mesh, types, detail)
         results = []
         for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
             table = []

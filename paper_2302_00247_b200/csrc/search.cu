@@ -498,28 +498,56 @@ __global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ b
       for (int i = 0; i < H.T; i++) {
         const NodeDesc nd = desc[i];
         uint32_t key = nd.slot >= 0 ? get_digit(w0, w1, nd.slot) : 0;
-        int sj[KMAX];
-        double rj[KMAX];
-#pragma unroll
-        for (int j = 0; j < KMAX; j++) {
-          if (j < nd.k) {
+        const double* D = dbl + nd.dbl;
+        double r;
+        int s;
+        // fan-in specialised paths (the node is warp-uniform: no divergence).
+        // base = max(0.0, reach[p] + conv) needs no max for one producer: the
+        // operands are >= +0.0, so the sum already is the max (bitwise).
+        if (nd.k == 0) {
+          const uint8_t e = tab[nd.tab + key];
+          ok = ok && e != 0xFF;
+          if (!__any_sync(0xffffffffu, ok)) break;
+          s = ok ? (e >> 2) & 3 : 0;
+          r = D[e & 3];
+        } else if (nd.k == 1) {
+          const int ps0 = prodp[nd.prod];
+          const int s0 = stp[ps0 * THREADS + tid];
+          const double r0 = reach[ps0 * THREADS + tid];
+          const uint8_t e = tab[nd.tab + key * 3 + s0];
+          ok = ok && e != 0xFF;
+          if (!__any_sync(0xffffffffu, ok)) break;
+          const int p = e & 3;
+          s = ok ? (e >> 2) & 3 : 0;
+          r = dadd(dadd(r0, D[8 + p * 3 + s0]), D[p]);
+        } else if (nd.k == 2) {
+          const int ps0 = prodp[nd.prod], ps1 = prodp[nd.prod + 1];
+          const int s0 = stp[ps0 * THREADS + tid], s1 = stp[ps1 * THREADS + tid];
+          const double r0 = reach[ps0 * THREADS + tid], r1 = reach[ps1 * THREADS + tid];
+          const uint8_t e = tab[nd.tab + (key * 3 + s0) * 3 + s1];
+          ok = ok && e != 0xFF;
+          if (!__any_sync(0xffffffffu, ok)) break;
+          const int p = e & 3;
+          s = ok ? (e >> 2) & 3 : 0;
+          r = dadd(fmax(dadd(r0, D[8 + p * 3 + s0]), dadd(r1, D[8 + (4 + p) * 3 + s1])), D[p]);
+        } else {
+          int sj[KMAX];
+          double rj[KMAX];
+          for (int j = 0; j < nd.k; j++) {
             const int ps = prodp[nd.prod + j];
             sj[j] = stp[ps * THREADS + tid];
             rj[j] = reach[ps * THREADS + tid];
             key = key * 3 + sj[j];
           }
+          const uint8_t e = tab[nd.tab + key];
+          ok = ok && e != 0xFF;
+          if (!__any_sync(0xffffffffu, ok)) break;
+          const int p = e & 3;
+          s = ok ? (e >> 2) & 3 : 0;
+          double bse = 0.0;
+          for (int j = 0; j < nd.k; j++) bse = fmax(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
+          r = dadd(bse, D[p]);
         }
-        const uint8_t e = tab[nd.tab + key];
-        ok = ok && e != 0xFF;
-        if (!__any_sync(0xffffffffu, ok)) break;
-        const int p = e & 3;
-        const int s = ok ? (e >> 2) & 3 : 0;
-        const double* D = dbl + nd.dbl;
-        double bse = 0.0;
-#pragma unroll
-        for (int j = 0; j < KMAX; j++)
-          if (j < nd.k) bse = fmax(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
-        const double r = dadd(bse, D[p]);
         fwd = fmax(fwd, dadd(r, D[4 + s]));
         if (nd.out_pool >= 0) {
           reach[nd.out_pool * THREADS + tid] = r;

@@ -85,3 +85,82 @@ def wide_classifier(num_classes: int, feature_dim: int, blocks: int = 4, batch: 
         GraphNode("output", OpKind.OUTPUT, ("classifier/fc",), TensorSpec((batch, num_classes), dtype)),
     ]
     return GroupedGraph(nodes)
+
+
+def motif_dag(seed: int = 0, tier: str = "parity", n_target: int = 100_000, motif_types: int = 16,
+              residuals: int = 1000, d: int = 768, batch: int = 8, seq: int = 128) -> GroupedGraph:
+    """Config 5: ~10^5-op DAG of repeated random motifs.
+
+    `motif_types` motif kinds, each a random DAG of M in [16, 48] ops over
+    matmul ((d,d)/(d,4d)/(4d,d) weights), elementwise add/mul with an optional
+    (d,) bias, layernorm and softmax (never weighted: divergence trap D1);
+    fan-in 1-2 from earlier motif ops or the motif entry.  Instances
+    `net/m{k}_{j}` are chained entry <- previous exit, so all are siblings
+    under `net`; scopes `net/m{k}_{j}/k{k}o{i}` make every type's first
+    relative name distinct (divergence trap D2).  `residuals` unique ops under
+    `tail/` never fold.  Tiers: "parity" motifs carry 6..12 two-dim weights
+    (every block searchable by the CPU reference); "throughput" swaps the
+    first three types for motifs with 16 / 18 / 20 two-dim weights
+    (4.3e7 .. 3.5e9 candidates).
+    """
+    import random
+
+    if tier not in ("parity", "throughput"):
+        raise ValueError("tier must be 'parity' or 'throughput'")
+    rng = random.Random(seed)
+    wide = 4 * d
+    motifs = []
+    for k in range(motif_types):
+        if tier == "throughput" and k < 3:
+            v2, v1 = (16, 18, 20)[k], 0
+        else:
+            v2, v1 = rng.randint(6, 12), rng.randint(0, 1)
+        m = rng.randint(max(16, v2 + v1 + 4), 48)
+        kinds = ["mm"] * v2 + ["bias"] * v1 + [rng.choice(("ew", "ew", "ln", "sm")) for _ in range(m - v2 - v1)]
+        rng.shuffle(kinds)
+        ops = []  # (kind, inputs as motif positions (-1 entry), weight shape, width)
+        widths = []
+        for i, kind in enumerate(kinds):
+            cands = list(range(-1, i))
+            a = rng.choice(cands[-6:])  # mostly local structure
+            win = d if a < 0 else widths[a]
+            if kind == "mm":
+                if win == wide:
+                    w, wout = (wide, d), d
+                else:
+                    w, wout = rng.choice((((d, d), d), ((d, wide), wide)))
+                ins = (a,)
+            else:
+                w = (d,) if kind == "bias" else None
+                wout = win
+                ins = (a,)
+                if kind in ("ew", "bias") and rng.random() < 0.5:
+                    same = [c for c in cands if (d if c < 0 else widths[c]) == win and c != a]
+                    if same:
+                        ins = (a, rng.choice(same[-6:]))
+            widths.append(wout)
+            ops.append((kind, ins, w, wout))
+        motifs.append(ops)
+    op_kind = {"mm": OpKind.MATMUL, "bias": OpKind.ELEMENTWISE, "ew": OpKind.ELEMENTWISE,
+               "ln": OpKind.LAYERNORM, "sm": OpKind.SOFTMAX}
+    budget = n_target - residuals - 2
+    nodes = [GraphNode("input", OpKind.INPUT, (), TensorSpec((batch, seq, d)))]
+    prev = "input"
+    for k, ops in enumerate(motifs):
+        reps = max(2, budget // (motif_types * len(ops)))
+        for j in range(reps):
+            pre = f"net/m{k}_{j}"
+            names = [f"{pre}/k{k}o{i}" for i in range(len(ops))]
+            for i, (kind, ins, w, wout) in enumerate(ops):
+                src = tuple(dict.fromkeys(prev if a < 0 else names[a] for a in ins))
+                wt = TensorSpec(w, trainable=True) if w is not None else None
+                nodes.append(GraphNode(names[i], op_kind[kind], src, TensorSpec((batch, seq, wout)), wt))
+            prev = names[-1]
+    for r in range(residuals):
+        name = f"tail/r{r}/u{r}"
+        w = TensorSpec((d, d), trainable=True) if r % 2 else None
+        nodes.append(GraphNode(name, OpKind.MATMUL if w else OpKind.ELEMENTWISE, (prev,),
+                               TensorSpec((batch, seq, d)), w))
+        prev = name
+    nodes.append(GraphNode("output", OpKind.OUTPUT, (prev,), TensorSpec((batch, seq, d))))
+    return GroupedGraph(nodes)

@@ -55,3 +55,9 @@ def mesh(doc: dict) -> ClusterSpec:
 
 def case_names(pred=lambda c: True) -> list:
     return [c["case"] for c in cases() if pred(c)]
+
+
+@functools.lru_cache(maxsize=1)
+def c5() -> dict:
+    with open(os.path.join(GOLDEN, "c5.json")) as fh:
+        return {e["tier"]: e for e in json.load(fh)["c5"]}

@@ -223,3 +223,70 @@ def test_multi_kernel_fold_path_vs_oracle(backend, seed, monkeypatch):
         ba = fold_blocks(low, md, session=ses)
         ob = BlockArrays.from_dict(oracle.prune(low, md))
         assert to_prune_doc(low, ba) == to_prune_doc(low, ob)
+
+
+# -- config 5: 10^5-op motif DAG --------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def c5_sessions(backend):
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session
+    from paper_2302_00247_b200.workloads import motif_dag
+
+    out = {}
+    for tier in ("parity", "throughput"):
+        g = motif_dag(0, tier)
+        out[tier] = (g, Session.open(lower(g), backend))
+    return out
+
+
+def test_c5_parity_derive_plan_byte_identical(c5_sessions):
+    """Full 10^5-node search (1018 blocks, 3.2M candidates) == reference JSON, by hash."""
+    import hashlib
+
+    from golden_io import c5
+    from paper_2302_00247_b200.search import derive_plan
+
+    gold = c5()["parity"]
+    g, ses = c5_sessions["parity"]
+    rep = derive_plan(g, mesh(gold["mesh"]), session=ses)
+    assert hashlib.sha256(canon(rep.to_json()).encode()).hexdigest() == gold["plan_sha"]
+    assert repr(rep.total_cost) == gold["total_cost"] and rep.valid == gold["valid"]
+
+
+def test_c5_throughput_fold_slices_and_argmin(c5_sessions):
+    import hashlib
+
+    from golden_io import c5
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import to_prune_doc
+    from paper_2302_00247_b200.search import fold_blocks
+
+    gold = c5()["throughput"]
+    g, ses = c5_sessions["throughput"]
+    be = ses.backend
+    ba = fold_blocks(ses.low, 2, session=ses)
+    assert hashlib.sha256(canon(to_prune_doc(ses.low, ba)).encode()).hexdigest() == gold["prune_sha"]
+    m = mesh(gold["mesh"])
+    off, nodes = ba.templates_csr()
+    t = be.tables(ses.dgraph, off, nodes, m, 1 << 20, 4 << 20)
+    try:
+        assert t.candidates.tolist() == gold["candidates"]
+        for sl in gold["slices"]:
+            _, tot = be.score_range(t, sl["block"], sl["lo"], sl["hi"], want_totals=True)
+            assert [None if x != x else x for x in tot.tolist()] == sl["totals"]
+        res = be.score(t)
+        # the 43M-candidate block in full against the oracle (16 pthreads)
+        b = gold["candidates"].index(43046721)
+        exp, _ = oracle.score(ses.low, ba.template_nodes(b), m, threads=16)
+        assert (res[b].valid, res[b].best_index, res[b].best_total, res[b].best_num_split) == (
+            exp.valid, exp.best_index, exp.best_total, exp.best_num_split)
+        # every small block in full
+        for b in range(ba.n_blocks):
+            if gold["candidates"][b] <= 1_100_000:
+                exp, _ = oracle.score(ses.low, ba.template_nodes(b), m, threads=4)
+                assert (res[b].valid, res[b].best_index, res[b].best_total) == (
+                    exp.valid, exp.best_index, exp.best_total)
+    finally:
+        t.close()

@@ -54,3 +54,47 @@ def test_fold_stress_graph_and_oracle_pinned(idx):
     low = lower(g)
     ba = BlockArrays.from_dict(oracle.prune(low, fs["min_dup"]))
     assert _sha(to_prune_doc(low, ba)) == fs["prune_sha"]
+
+
+@pytest.mark.parametrize("tier", ["parity", "throughput"])
+def test_c5_graph_and_oracle_fold_pinned(tier):
+    """Config 5: generator == the graph the reference was run on; oracle fold == reference."""
+    from golden_io import c5
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays, to_prune_doc
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.workloads import motif_dag
+
+    gold = c5()[tier]
+    g = motif_dag(0, tier)
+    assert _sha(dump_grouped(g)) == gold["graph_sha"]
+    low = lower(g)
+    ba = BlockArrays.from_dict(oracle.prune(low, 2))
+    assert _sha(to_prune_doc(low, ba)) == gold["prune_sha"]
+
+
+@pytest.mark.parametrize("tier", ["parity", "throughput"])
+def test_c5_oracle_slices_and_search(tier):
+    """Per-candidate totals on the golden slices; full parity-tier search == reference."""
+    from golden_io import c5, mesh
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.workloads import motif_dag
+
+    gold = c5()[tier]
+    low = lower(motif_dag(0, tier))
+    ba = BlockArrays.from_dict(oracle.prune(low, 2))
+    m = mesh(gold["mesh"])
+    for sl in gold["slices"]:
+        _, tot = oracle.score(low, ba.template_nodes(sl["block"]), m, lo=sl["lo"], hi=sl["hi"],
+                              want_totals=True)
+        assert [None if t != t else t for t in tot.tolist()] == sl["totals"]
+    if tier == "parity":
+        total = 0.0
+        for b, (idx, ns, tot, valid) in enumerate(gold["best"]):
+            out, _ = oracle.score(low, ba.template_nodes(b), m, threads=8)
+            assert (out.best_index, out.best_num_split, repr(out.best_total), out.valid) == (
+                idx, ns, tot, valid)
+            total += out.best_total * ba.multiplicity(b)
+        assert repr(total) == gold["total_cost"]

@@ -221,6 +221,15 @@ int sp_explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, sp_explai
 /* Device time (ms) of the last sp_score / sp_fold_run kernels (CUDA events). */
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms);
 
+/*
+ * Options.  SP_OPT_PREFIX_SKIP (default 1): when a candidate fails routing at
+ * node i, every candidate sharing the digits of i's ancestor cone fails too,
+ * so the scorer jumps over them (exact; counts and argmin are unchanged).
+ * 0 walks every candidate individually (brute force).
+ */
+#define SP_OPT_PREFIX_SKIP 1
+int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value);
+
 /* CUDA-event timer on the context's stream (brackets whole API calls for benchmarks). */
 int sp_timer_start(sp_ctx* ctx);
 int sp_timer_stop(sp_ctx* ctx, double* ms);

@@ -63,6 +63,7 @@ def _declare(L):
     L.sp_timer_stop.argtypes = [vp, C.POINTER(C.c_double)]
     L.sp_launch_counts.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.sp_tables_bytes.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.sp_set_option.argtypes = [vp, C.c_int32, C.c_int64]
     L.sp_search.argtypes = [vp, vp, C.POINTER(SpScoreOut), C.POINTER(SpExplainBlock),
                             C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_tables_sizes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -70,7 +71,7 @@ def _declare(L):
     L.sp_explain_all.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(SpExplainBlock),
                                  C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_copy_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-    for name in ("sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
+    for name in ("sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
                  "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
                  "sp_score_range", "sp_explain", "sp_last_timings"):
         getattr(L, name).restype = C.c_int
@@ -100,7 +101,7 @@ EXPORTED_SYMBOLS = (
     "sp_tables_free", "sp_tables_candidates", "sp_tables_slots", "sp_score", "sp_score_range",
     "sp_merge_keys", "sp_explain", "sp_last_timings", "sp_timer_start", "sp_timer_stop",
     "sp_launch_counts", "sp_copy_bytes", "sp_tables_bytes", "sp_tables_sizes",
-    "sp_tables_edge_offsets", "sp_explain_all", "sp_search",
+    "sp_tables_edge_offsets", "sp_explain_all", "sp_search", "sp_set_option",
 )
 
 
@@ -266,6 +267,10 @@ class Backend:
         f, s, k = C.c_double(), C.c_double(), C.c_double()
         self.lib.sp_last_timings(self.ctx, C.byref(f), C.byref(s), C.byref(k))
         return {"fold_ms": f.value, "score_ms": s.value, "score_kernel_ms": k.value}
+
+    def set_prefix_skip(self, on: bool) -> None:
+        """Exact prefix-failure skipping in sp_score/sp_search (default on)."""
+        self._check(self.lib.sp_set_option(self.ctx, 1, 1 if on else 0), "sp_set_option")
 
     def timer_start(self):
         self._check(self.lib.sp_timer_start(self.ctx), "sp_timer_start")

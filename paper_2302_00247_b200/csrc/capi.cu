@@ -246,6 +246,16 @@ int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double
   return SP_OK;
 }
 
+int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value) {
+  if (!ctx) return SP_ERR_CONFIG;
+  if (option == SP_OPT_PREFIX_SKIP) {
+    ctx->skip = value ? 1 : 0;
+    return SP_OK;
+  }
+  ctx->last_error = "unknown option";
+  return SP_ERR_CONFIG;
+}
+
 int sp_timer_start(sp_ctx* ctx) {
   if (!ctx) return SP_ERR_CONFIG;
   return guard(ctx, [&] {

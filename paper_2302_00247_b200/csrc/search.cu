@@ -28,7 +28,8 @@ namespace {
 constexpr int KMAX = 6;          // internal producers handled by a lookup table
 constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
 constexpr int THREADS = 256;     // scoring CTA size
-constexpr int ITEM_ITERS_MAX = 64;  // work item = THREADS * iters candidates, iters <= 64
+constexpr int ITEM_ITERS_MAX = 64;         // work item = THREADS * iters candidates
+constexpr int ITEM_ITERS_MAX_SKIP = 1024;  // ... when prefix skipping is on
 
 __host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 __host__ __device__ inline uint32_t pow3(int k) {
@@ -143,7 +144,8 @@ __device__ void route_node(const GraphView& G, int32_t n, int32_t blk, const int
 }
 
 struct EntryLayout {
-  int32_t k, nd, out_pool, prod, tab, dbl, train_idx, pad;
+  int32_t k, nd, out_pool, prod, tab, dbl, train_idx, skip_m;
+  uint64_t skip_R;
 };
 
 __global__ void k_mark_blocks(const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
@@ -167,13 +169,16 @@ __global__ void k_boundary(GraphView G, int64_t n, const int32_t* node_block, ui
 }
 
 // One CTA per block: per-node internal fan-in and liveness in parallel, then
-// one thread lays out the blob and assigns pool slots (linear scan; a
-// producer's slot is released at its last internal consumer).
+// one thread lays out the blob, assigns pool slots (linear scan; a producer's
+// slot is released at its last internal consumer) and derives each node's
+// prefix-failure skip (ancestor cone over enumeration positions).
 __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                          const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
                          const uint8_t* radix_of, EntryLayout* lay, BlobHeader* hdr, int64_t* blob_bytes,
                          int32_t* err) {
   __shared__ int s_k[MAXT], s_last[MAXT], s_pool[MAXT];
+  __shared__ int16_t s_prodpos[MAXT][KMAX];
+  __shared__ uint64_t s_anc[MAXT];
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const int64_t e0 = tmpl_off[b];
     const int T = (int)(tmpl_off[b + 1] - e0);
@@ -188,6 +193,7 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
         const int j = node_tpos[r];
         if (j >= i) atomicExch(err, 2);  // template not topologically ordered
         atomicMax(&s_last[j], i);
+        if (k < KMAX) s_prodpos[i][k] = (int16_t)j;
         k++;
       }
       if (k > KMAX) atomicExch(err, 3);
@@ -195,6 +201,8 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+      const BlobHeader& H0 = hdr[b];
+      const int V = H0.V;
       int nprod = 0, nt = 0;
       int64_t nent = 0, ndbl = 0;
       uint32_t used[MAXT / 32];
@@ -214,6 +222,10 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
         }
         const int32_t n = tmpl_nodes[e0 + i];
         const int k = s_k[i];
+        // ancestor cone over enumeration positions (V <= 64)
+        uint64_t anc = slot_of[e0 + i] >= 0 ? (1ULL << slot_of[e0 + i]) : 0ULL;
+        for (int j = 0; j < k && j < KMAX; j++) anc |= s_anc[s_prodpos[i][j]];
+        s_anc[i] = anc;
         EntryLayout L;
         L.k = k;
         L.nd = slot_of[e0 + i] >= 0 ? radix_of[e0 + i] : 1;
@@ -222,7 +234,10 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
         L.dbl = (int32_t)ndbl;
         L.train_idx = (G.w_rank[n] && G.w_train[n]) ? nt++ : -1;
         L.out_pool = s_pool[i];
-        L.pad = 0;
+        L.skip_m = anc ? 63 - __clzll(anc) : -1;
+        uint64_t R = 1;
+        for (int q = L.skip_m + 1; q < V; q++) R *= ((H0.radix3 >> q) & 1) ? 3 : 2;
+        L.skip_R = anc ? R : 0;
         nprod += k;
         nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
         ndbl += 8 + 12 * (int64_t)k;
@@ -236,6 +251,10 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
       int64_t off = sizeof(BlobHeader);
       H.desc_off = (int32_t)off;
       off = align16(off + 16 * (int64_t)T);
+      H.skip_off = (int32_t)off;
+      off = align16(off + (int64_t)sizeof(NodeSkip) * T);
+      H.stride_off = (int32_t)off;
+      off = align16(off + 9 * (int64_t)V);
       H.prod_off = (int32_t)off;
       off = align16(off + 2 * (int64_t)nprod);
       H.tab_off = (int32_t)off;
@@ -256,6 +275,7 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
 // header.
 __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                        const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
+                       const int16_t* ref_slot_of,
                        const EntryLayout* lay, const BlobHeader* hdr_in, const int64_t* blob_off,
                        const uint8_t* has_cons, const uint8_t* ext_cons, sp_mesh mesh, int64_t mu,
                        int64_t chunk, uint8_t* blobs, uint8_t* bound_of) {
@@ -277,6 +297,21 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       h.mu = mu;
       h.chunk = chunk;
       *(BlobHeader*)blob = h;
+      // reference strides per enumeration position + perm (reference slot -> enumeration position)
+      uint64_t* stride = (uint64_t*)(blob + H.stride_off);
+      int8_t* perm = (int8_t*)(blob + H.stride_off + 8 * H.V);
+      uint8_t rr[64];
+      for (int i = 0; i < T; i++)
+        if (ref_slot_of[e0 + i] >= 0) {
+          rr[ref_slot_of[e0 + i]] = ((H.radix3 >> slot_of[e0 + i]) & 1) ? 3 : 2;
+          perm[ref_slot_of[e0 + i]] = (int8_t)slot_of[e0 + i];
+        }
+      for (int i = 0; i < T; i++)
+        if (ref_slot_of[e0 + i] >= 0) {
+          uint64_t st = 1;
+          for (int s2 = ref_slot_of[e0 + i] + 1; s2 < H.V; s2++) st *= rr[s2];
+          stride[slot_of[e0 + i]] = st;
+        }
       uint32_t acc = 0;
       for (int i = 0; i < T; i++) {
         s_kbase[i] = acc;
@@ -300,6 +335,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       nd.tab = (uint32_t)L.tab;
       nd.dbl = (uint32_t)L.dbl;
       ((NodeDesc*)(blob + H.desc_off))[i] = nd;
+      ((NodeSkip*)(blob + H.skip_off))[i] = NodeSkip{L.skip_R, L.skip_m, 0};
       int16_t* prod = (int16_t*)(blob + H.prod_off) + L.prod;
       double* dbl = (double*)(blob + H.dbl_off) + L.dbl;
       Pattern pats[4];
@@ -412,23 +448,222 @@ __device__ __forceinline__ void mr_add(uint64_t& w0, uint64_t& w1, uint32_t t, i
 
 struct ScorePlan {
   const int64_t* blob_off;
-  unsigned long long item_cands;  // candidates per work item (THREADS * iters)
-  const unsigned long long* lo;   // per block start index (shard-local)
+  unsigned long long item_cands;        // candidates per work item
+  const unsigned long long* lo;         // per block start (enumeration index space)
   const unsigned long long* hi;
   const unsigned long long* item_base;  // prefix sum of items per block, [nb+1]
   int64_t nb;
   unsigned long long n_items;
+  int skip;                             // exact prefix-failure skipping on/off
 };
 
-// Batched scorer: dynamic work items of ITEM_CANDS candidates over all blocks.
+// Pointers into a block's tables staged in shared memory.
+struct Tabs {
+  const BlobHeader* H;
+  const NodeDesc* desc;
+  const NodeSkip* skip;
+  const uint64_t* stride;  // reference stride per enumeration position
+  const int8_t* perm;      // reference slot -> enumeration position
+  const int16_t* prodp;
+  const uint8_t* tab;
+  const double* dbl;
+  const TrainDesc* trn;
+  double* reach;
+  uint8_t* stp;
+};
+
+__device__ __forceinline__ Tabs tabs_of(uint8_t* smem) {
+  Tabs S;
+  S.H = (const BlobHeader*)smem;
+  const BlobHeader& H = *S.H;
+  S.desc = (const NodeDesc*)(smem + H.desc_off);
+  S.skip = (const NodeSkip*)(smem + H.skip_off);
+  S.stride = (const uint64_t*)(smem + H.stride_off);
+  S.perm = (const int8_t*)(smem + H.stride_off + 8 * H.V);
+  S.prodp = (const int16_t*)(smem + H.prod_off);
+  S.tab = smem + H.tab_off;
+  S.dbl = (const double*)(smem + H.dbl_off);
+  S.trn = (const TrainDesc*)(smem + H.train_off);
+  S.reach = (double*)(smem + ((H.bytes + 15) & ~15));
+  S.stp = (uint8_t*)(S.reach + (size_t)H.npool * THREADS);
+  return S;
+}
+
+// pattern_routing + the forward DP of plan_cost for the lane's candidate
+// (digits packed in enumeration order).  Returns -1 when it routes (fwd =
+// forward time), else the first failing template position; T when inactive.
+// Warp-collective: all 32 lanes call it (uniform node loop, ballot exit).
+__device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, bool active, double& fwd, int tid) {
+  const int T = S.H->T;
+  bool ok = active;
+  int fail = active ? -1 : T;
+  fwd = 0.0;
+  for (int i = 0; i < T; i++) {
+    const NodeDesc nd = S.desc[i];
+    uint32_t key = nd.slot >= 0 ? get_digit(w0, w1, nd.slot) : 0;
+    const double* D = S.dbl + nd.dbl;
+    double r;
+    int s;
+    uint8_t e;
+    // fan-in specialised paths (the node is warp-uniform: no divergence).
+    // base = max(0.0, reach[p] + conv) needs no max for one producer: the
+    // operands are >= +0.0, so the sum already is the max (bitwise).
+    if (nd.k == 0) {
+      e = S.tab[nd.tab + key];
+      if (ok && e == 0xFF) { ok = false; fail = i; }
+      if (!__any_sync(0xffffffffu, ok)) break;
+      s = ok ? (e >> 2) & 3 : 0;
+      r = D[e & 3];
+    } else if (nd.k == 1) {
+      const int ps0 = S.prodp[nd.prod];
+      const int s0 = S.stp[ps0 * THREADS + tid];
+      const double r0 = S.reach[ps0 * THREADS + tid];
+      e = S.tab[nd.tab + key * 3 + s0];
+      if (ok && e == 0xFF) { ok = false; fail = i; }
+      if (!__any_sync(0xffffffffu, ok)) break;
+      const int p = e & 3;
+      s = ok ? (e >> 2) & 3 : 0;
+      r = dadd(dadd(r0, D[8 + p * 3 + s0]), D[p]);
+    } else if (nd.k == 2) {
+      const int ps0 = S.prodp[nd.prod], ps1 = S.prodp[nd.prod + 1];
+      const int s0 = S.stp[ps0 * THREADS + tid], s1 = S.stp[ps1 * THREADS + tid];
+      const double r0 = S.reach[ps0 * THREADS + tid], r1 = S.reach[ps1 * THREADS + tid];
+      e = S.tab[nd.tab + (key * 3 + s0) * 3 + s1];
+      if (ok && e == 0xFF) { ok = false; fail = i; }
+      if (!__any_sync(0xffffffffu, ok)) break;
+      const int p = e & 3;
+      s = ok ? (e >> 2) & 3 : 0;
+      r = dadd(fmax(dadd(r0, D[8 + p * 3 + s0]), dadd(r1, D[8 + (4 + p) * 3 + s1])), D[p]);
+    } else {
+      int sj[KMAX];
+      double rj[KMAX];
+      for (int j = 0; j < nd.k; j++) {
+        const int ps = S.prodp[nd.prod + j];
+        sj[j] = S.stp[ps * THREADS + tid];
+        rj[j] = S.reach[ps * THREADS + tid];
+        key = key * 3 + sj[j];
+      }
+      e = S.tab[nd.tab + key];
+      if (ok && e == 0xFF) { ok = false; fail = i; }
+      if (!__any_sync(0xffffffffu, ok)) break;
+      const int p = e & 3;
+      s = ok ? (e >> 2) & 3 : 0;
+      double bse = 0.0;
+      for (int j = 0; j < nd.k; j++) bse = fmax(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
+      r = dadd(bse, D[p]);
+    }
+    fwd = fmax(fwd, dadd(r, D[4 + s]));
+    if (nd.out_pool >= 0) {
+      S.reach[nd.out_pool * THREADS + tid] = r;
+      S.stp[nd.out_pool * THREADS + tid] = (uint8_t)s;
+    }
+  }
+  return ok ? -1 : fail;
+}
+
+// backward of plan_cost: pack_gradients over replicated trainable weights
+// (template order), buckets first then unfused, one AllReduce each.
+__device__ __forceinline__ double backward(const Tabs& S, uint64_t w0, uint64_t w1) {
+  const BlobHeader& H = *S.H;
+  double bwd = 0.0;
+  if (!H.multi_dev) return bwd;
+  long long cur = 0;
+  int cur_n = 0;
+  for (int q = 0; q < H.nt; q++) {
+    const TrainDesc td = S.trn[q];
+    if (get_digit(w0, w1, td.slot) != 0 || td.size >= H.mu) continue;
+    if (cur + td.size > H.chunk && cur_n) {
+      bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
+      cur = 0;
+      cur_n = 0;
+    }
+    cur += td.size;
+    cur_n++;
+  }
+  if (cur_n) bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
+  for (int q = 0; q < H.nt; q++) {
+    const TrainDesc td = S.trn[q];
+    if (get_digit(w0, w1, td.slot) == 0 && td.size >= H.mu) bwd = dadd(bwd, td.uterm);
+  }
+  return bwd;
+}
+
+__device__ __forceinline__ uint32_t num_split_of(uint64_t w0, uint64_t w1) {
+  return __popcll((w0 | (w0 >> 1)) & 0x5555555555555555ULL) + __popcll((w1 | (w1 >> 1)) & 0x5555555555555555ULL);
+}
+
+// reference index (candidate_by_index order) of enumeration-order digits
+__device__ __forceinline__ unsigned long long ref_index(const Tabs& S, uint64_t w0, uint64_t w1) {
+  unsigned long long idx = 0;
+  for (int q = 0; q < S.H->V; q++) idx += (unsigned long long)get_digit(w0, w1, q) * S.stride[q];
+  return idx;
+}
+
+__device__ __forceinline__ void decode_enum(const BlobHeader& H, unsigned long long x, uint64_t& w0, uint64_t& w1) {
+  w0 = w1 = 0;
+  for (int q = H.V - 1; q >= 0; q--) {
+    const uint32_t r = ((H.radix3 >> q) & 1) ? 3 : 2;
+    const uint32_t d = (uint32_t)(x % r);
+    x /= r;
+    if (q < 32) w0 |= (uint64_t)d << (q * 2);
+    else w1 |= (uint64_t)d << ((q - 32) * 2);
+  }
+}
+
+// zero every position > m, then +1 at position m (carry upwards)
+__device__ __forceinline__ void mr_skip(uint64_t& w0, uint64_t& w1, int m, int V, uint64_t radix3) {
+  for (int q = m + 1; q < V; q++) {
+    if (q < 32) w0 &= ~(3ULL << (q * 2));
+    else w1 &= ~(3ULL << ((q - 32) * 2));
+  }
+  for (int q = m; q >= 0; q--) {
+    uint64_t& w = q < 32 ? w0 : w1;
+    const int sh = (q & 31) * 2;
+    const uint32_t d = (uint32_t)((w >> sh) & 3) + 1;
+    const uint32_t r = ((radix3 >> q) & 1) ? 3 : 2;
+    if (d < r) {
+      w = (w & ~(3ULL << sh)) | ((uint64_t)d << sh);
+      return;
+    }
+    w &= ~(3ULL << sh);
+  }
+}
+
+__device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
+  const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, src);
+  const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)(v >> 32), src);
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = ((unsigned long long)__shfl_xor_sync(0xffffffffu, (unsigned)(v >> 32), o) << 32) |
+                                 __shfl_xor_sync(0xffffffffu, (unsigned)v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ void stage_blob(uint8_t* smem, const uint8_t* blobs, int64_t off) {
+  const int bytes = ((const BlobHeader*)(blobs + off))->bytes;
+  const uint4* src = (const uint4*)(blobs + off);
+  uint4* dst = (uint4*)smem;
+  for (int q = threadIdx.x; q < bytes / 16; q += blockDim.x) dst[q] = src[q];
+}
+
+// Batched scorer over ALL blocks of a search in one launch.  Dynamic work
+// items (atomic counter) of contiguous enumeration ranges; each warp walks its
+// eighth of an item 32 candidates at a time.  With skipping on, a lane whose
+// candidate fails at node i proves its whole R-aligned run invalid (R =
+// NodeSkip.R), and the warp jumps to the max proven end: the union of the
+// lanes' runs is contiguous from the warp's base, so the jump is exact.
 __global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ blobs, ScorePlan P,
                                                    ItemOut* __restrict__ items,
-                                                   unsigned long long* __restrict__ counter,
-                                                   double* __restrict__ totals) {
+                                                   unsigned long long* __restrict__ counter) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long s_item;
   __shared__ int64_t s_block;
-  __shared__ uint64_t s_w0, s_w1;
   __shared__ unsigned long long s_red_t[THREADS / 32], s_red_i[THREADS / 32];
   __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
   const int tid = threadIdx.x;
@@ -450,149 +685,64 @@ __global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ b
     }
     __syncthreads();
     const int64_t b = s_block;
-    const BlobHeader* gH = (const BlobHeader*)(blobs + P.blob_off[b]);
-    const int blob_bytes = gH->bytes;
     if (b != staged) {
-      // stage the block's tables: 16-byte vector copies
-      const uint4* src = (const uint4*)(blobs + P.blob_off[b]);
-      uint4* dst = (uint4*)smem;
-      for (int q = tid; q < blob_bytes / 16; q += THREADS) dst[q] = src[q];
+      stage_blob(smem, blobs, P.blob_off[b]);
       staged = b;
     }
     __syncthreads();
-    const BlobHeader& H = *(const BlobHeader*)smem;
-    const NodeDesc* desc = (const NodeDesc*)(smem + H.desc_off);
-    const int16_t* prodp = (const int16_t*)(smem + H.prod_off);
-    const uint8_t* tab = smem + H.tab_off;
-    const double* dbl = (const double*)(smem + H.dbl_off);
-    const TrainDesc* trn = (const TrainDesc*)(smem + H.train_off);
-    double* reach = (double*)(smem + ((blob_bytes + 15) & ~15));
-    uint8_t* stp = (uint8_t*)(reach + (size_t)H.npool * THREADS);
-
+    const Tabs S = tabs_of(smem);
+    const BlobHeader& H = *S.H;
     const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
-    unsigned long long ihi = ilo + P.item_cands;
-    if (ihi > P.hi[b]) ihi = P.hi[b];
-    if (tid == 0) {
-      // decode the item's first index (candidate_by_index, search.py:103-116)
-      uint64_t w0 = 0, w1 = 0;
-      unsigned long long rem = ilo;
-      for (int s = H.V - 1; s >= 0; s--) {
-        const uint32_t r = ((H.radix3 >> s) & 1) ? 3 : 2;
-        const uint32_t d = (uint32_t)(rem % r);
-        rem /= r;
-        if (s < 32) w0 |= (uint64_t)d << ((s & 31) * 2);
-        else w1 |= (uint64_t)d << ((s & 31) * 2);
-      }
-      s_w0 = w0;
-      s_w1 = w1;
-    }
-    __syncthreads();
-    uint64_t w0 = s_w0, w1 = s_w1;
-    mr_add(w0, w1, (uint32_t)tid, H.V, H.radix3);
+    const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
+    const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
+    const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
     unsigned long long best_t = ~0ULL, best_i = ~0ULL;
     uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
-    for (unsigned long long base = ilo; base < ihi; base += THREADS) {
-      const unsigned long long idx = base + tid;
-      bool ok = idx < ihi;
-      double fwd = 0.0;
-      for (int i = 0; i < H.T; i++) {
-        const NodeDesc nd = desc[i];
-        uint32_t key = nd.slot >= 0 ? get_digit(w0, w1, nd.slot) : 0;
-        const double* D = dbl + nd.dbl;
-        double r;
-        int s;
-        // fan-in specialised paths (the node is warp-uniform: no divergence).
-        // base = max(0.0, reach[p] + conv) needs no max for one producer: the
-        // operands are >= +0.0, so the sum already is the max (bitwise).
-        if (nd.k == 0) {
-          const uint8_t e = tab[nd.tab + key];
-          ok = ok && e != 0xFF;
-          if (!__any_sync(0xffffffffu, ok)) break;
-          s = ok ? (e >> 2) & 3 : 0;
-          r = D[e & 3];
-        } else if (nd.k == 1) {
-          const int ps0 = prodp[nd.prod];
-          const int s0 = stp[ps0 * THREADS + tid];
-          const double r0 = reach[ps0 * THREADS + tid];
-          const uint8_t e = tab[nd.tab + key * 3 + s0];
-          ok = ok && e != 0xFF;
-          if (!__any_sync(0xffffffffu, ok)) break;
-          const int p = e & 3;
-          s = ok ? (e >> 2) & 3 : 0;
-          r = dadd(dadd(r0, D[8 + p * 3 + s0]), D[p]);
-        } else if (nd.k == 2) {
-          const int ps0 = prodp[nd.prod], ps1 = prodp[nd.prod + 1];
-          const int s0 = stp[ps0 * THREADS + tid], s1 = stp[ps1 * THREADS + tid];
-          const double r0 = reach[ps0 * THREADS + tid], r1 = reach[ps1 * THREADS + tid];
-          const uint8_t e = tab[nd.tab + (key * 3 + s0) * 3 + s1];
-          ok = ok && e != 0xFF;
-          if (!__any_sync(0xffffffffu, ok)) break;
-          const int p = e & 3;
-          s = ok ? (e >> 2) & 3 : 0;
-          r = dadd(fmax(dadd(r0, D[8 + p * 3 + s0]), dadd(r1, D[8 + (4 + p) * 3 + s1])), D[p]);
+    if (wlo < whi) {
+      uint64_t bw0, bw1;
+      decode_enum(H, wlo, bw0, bw1);
+      unsigned long long base = wlo;
+      while (base < whi) {
+        const unsigned long long x = base + lane;
+        const bool active = x < whi;
+        uint64_t w0 = bw0, w1 = bw1;
+        mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
+        double fwd;
+        const int fail = walk(S, w0, w1, active, fwd, tid);
+        unsigned long long t = x + 1;
+        if (fail < 0) {
+          const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
+          const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+          const uint32_t ns = num_split_of(w0, w1);
+          const unsigned long long idx = ref_index(S, w0, w1);
+          nvalid++;
+          if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
+            best_t = tb;
+            best_n = ns;
+            best_i = idx;
+          }
+        } else if (P.skip && active) {
+          const NodeSkip sk = S.skip[fail];
+          t = sk.R ? (x / sk.R + 1) * sk.R : whi;
+        }
+        const unsigned long long nb_ = warp_max_u64(t);
+        if (nb_ >= whi) break;
+        if (nb_ == base + 32) {
+          mr_add(bw0, bw1, 32, H.V, H.radix3);
         } else {
-          int sj[KMAX];
-          double rj[KMAX];
-          for (int j = 0; j < nd.k; j++) {
-            const int ps = prodp[nd.prod + j];
-            sj[j] = stp[ps * THREADS + tid];
-            rj[j] = reach[ps * THREADS + tid];
-            key = key * 3 + sj[j];
+          // the lane that proved the longest run provides the next base digits
+          const unsigned mask = __ballot_sync(0xffffffffu, t == nb_);
+          const int src = __ffs(mask) - 1;
+          uint64_t n0 = w0, n1 = w1;
+          if (lane == src) {
+            if (fail >= 0 && P.skip && active && S.skip[fail].R) mr_skip(n0, n1, S.skip[fail].m, H.V, H.radix3);
+            else mr_add(n0, n1, 1, H.V, H.radix3);
           }
-          const uint8_t e = tab[nd.tab + key];
-          ok = ok && e != 0xFF;
-          if (!__any_sync(0xffffffffu, ok)) break;
-          const int p = e & 3;
-          s = ok ? (e >> 2) & 3 : 0;
-          double bse = 0.0;
-          for (int j = 0; j < nd.k; j++) bse = fmax(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
-          r = dadd(bse, D[p]);
+          bw0 = shfl_u64(n0, src);
+          bw1 = shfl_u64(n1, src);
         }
-        fwd = fmax(fwd, dadd(r, D[4 + s]));
-        if (nd.out_pool >= 0) {
-          reach[nd.out_pool * THREADS + tid] = r;
-          stp[nd.out_pool * THREADS + tid] = (uint8_t)s;
-        }
+        base = nb_;
       }
-      if (ok) {
-        // backward: pack_gradients over replicated trainable weights (template order)
-        double bwd = 0.0;
-        if (H.multi_dev) {
-          long long cur = 0;
-          int cur_n = 0;
-          for (int q = 0; q < H.nt; q++) {
-            const TrainDesc td = trn[q];
-            if (get_digit(w0, w1, td.slot) != 0) continue;
-            if (td.size >= H.mu) continue;
-            if (cur + td.size > H.chunk && cur_n) {
-              bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
-              cur = 0;
-              cur_n = 0;
-            }
-            cur += td.size;
-            cur_n++;
-          }
-          if (cur_n) bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
-          for (int q = 0; q < H.nt; q++) {
-            const TrainDesc td = trn[q];
-            if (get_digit(w0, w1, td.slot) == 0 && td.size >= H.mu) bwd = dadd(bwd, td.uterm);
-          }
-        }
-        const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
-        const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
-        const uint32_t ns = __popcll((w0 | (w0 >> 1)) & 0x5555555555555555ULL) +
-                            __popcll((w1 | (w1 >> 1)) & 0x5555555555555555ULL);
-        nvalid++;
-        if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
-          best_t = tb;
-          best_n = ns;
-          best_i = idx;
-        }
-        if (totals) totals[idx - P.lo[b]] = total;
-      } else if (totals && idx < ihi) {
-        totals[idx - P.lo[b]] = __longlong_as_double(0x7ff8000000000000LL);
-      }
-      mr_add(w0, w1, THREADS, H.V, H.radix3);
     }
     // warp then block argmin of (total, num_split, index) + valid count
 #pragma unroll
@@ -626,7 +776,86 @@ __global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ b
       }
       items[item] = o;
     }
-    // the next iteration's first __syncthreads orders s_item reuse
+  }
+}
+
+// Per-candidate totals over a REFERENCE index range [lo, hi) of one block
+// (want_table / _eval_range table rows): every candidate walked, NaN = invalid.
+__global__ void __launch_bounds__(THREADS) k_score_table(const uint8_t* __restrict__ blobs, int64_t blob_off,
+                                                         unsigned long long lo, unsigned long long hi,
+                                                         double* __restrict__ totals, ItemOut* __restrict__ cta_out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ unsigned long long s_red_t[THREADS / 32], s_red_i[THREADS / 32];
+  __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  stage_blob(smem, blobs, blob_off);
+  __syncthreads();
+  const Tabs S = tabs_of(smem);
+  const BlobHeader& H = *S.H;
+  unsigned long long best_t = ~0ULL, best_i = ~0ULL;
+  uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * THREADS;
+  for (unsigned long long base = lo + (unsigned long long)blockIdx.x * THREADS + warp * 32; base < hi; base += stride) {
+    const unsigned long long x = base + lane;
+    const bool active = x < hi;
+    // reference digits -> enumeration positions
+    uint64_t w0 = 0, w1 = 0;
+    unsigned long long rem = active ? x : 0;
+    for (int sidx = H.V - 1; sidx >= 0; sidx--) {
+      const uint32_t r = ((H.radix3_ref >> sidx) & 1) ? 3 : 2;
+      const uint32_t d = (uint32_t)(rem % r);
+      rem /= r;
+      const int q = S.perm[sidx];
+      if (q < 32) w0 |= (uint64_t)d << (q * 2);
+      else w1 |= (uint64_t)d << ((q - 32) * 2);
+    }
+    double fwd;
+    const int fail = walk(S, w0, w1, active, fwd, tid);
+    if (fail < 0) {
+      const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
+      const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+      const uint32_t ns = num_split_of(w0, w1);
+      nvalid++;
+      if (key_less(tb, ns, x, best_t, best_n, best_i)) {
+        best_t = tb;
+        best_n = ns;
+        best_i = x;
+      }
+      if (totals) totals[x - lo] = total;
+    } else if (active && totals) {
+      totals[x - lo] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t2 = __shfl_down_sync(0xffffffffu, best_t, o);
+    const unsigned long long i2 = __shfl_down_sync(0xffffffffu, best_i, o);
+    const uint32_t n2 = __shfl_down_sync(0xffffffffu, best_n, o);
+    nvalid += __shfl_down_sync(0xffffffffu, nvalid, o);
+    if (key_less(t2, n2, i2, best_t, best_n, best_i)) {
+      best_t = t2;
+      best_n = n2;
+      best_i = i2;
+    }
+  }
+  if (lane == 0) {
+    s_red_t[warp] = best_t;
+    s_red_i[warp] = best_i;
+    s_red_n[warp] = best_n;
+    s_red_v[warp] = nvalid;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ItemOut o{s_red_t[0], s_red_i[0], s_red_n[0], s_red_v[0]};
+    for (int w = 1; w < THREADS / 32; w++) {
+      o.valid += s_red_v[w];
+      if (key_less(s_red_t[w], s_red_n[w], s_red_i[w], o.total_bits, o.num_split, o.index)) {
+        o.total_bits = s_red_t[w];
+        o.num_split = s_red_n[w];
+        o.index = s_red_i[w];
+      }
+    }
+    cta_out[blockIdx.x] = o;
   }
 }
 
@@ -832,10 +1061,10 @@ __global__ void k_explain_all(GraphView G, const int64_t* tmpl_off, const int32_
     }
     const BlobHeader* H = (const BlobHeader*)(blobs + blob_off[b]);
     const int V = H->V;
-    uint8_t dig[64];
+    uint8_t dig[64];  // reference slot order (candidate_by_index, search.py:103-116)
     unsigned long long rem = index;
     for (int s = V - 1; s >= 0; s--) {
-      const uint32_t r = ((H->radix3 >> s) & 1) ? 3 : 2;
+      const uint32_t r = ((H->radix3_ref >> s) & 1) ? 3 : 2;
       dig[s] = (uint8_t)(rem % r);
       rem /= r;
     }
@@ -976,7 +1205,7 @@ GraphView view_of(sp_dgraph* dg) {
 // per-table device state kept for scoring/explain
 struct TableDev {
   DevBuf<int32_t> node_block, node_tpos;
-  DevBuf<int16_t> slot_of;
+  DevBuf<int16_t> slot_of, ref_slot_of;
   DevBuf<uint8_t> has_cons, ext_cons, bound;
 };
 
@@ -1006,7 +1235,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   const int64_t ne = out->tmpl_off[nb];
   out->tmpl_nodes.assign(tmpl_nodes, tmpl_nodes + ne);
   // host validation + weight slot order (weight_nodes: sorted by name, search.py:85-88)
-  std::vector<int16_t> slot_of(ne, -1);
+  std::vector<int16_t> slot_of(ne, -1), ref_slot_of(ne, -1);
   std::vector<uint8_t> radix_of(ne, 1);
   out->slot_pos.assign(nb, {});
   out->hdr.assign(nb, BlobHeader{});
@@ -1040,19 +1269,30 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     BlobHeader& H = out->hdr[b];
     H.V = (int32_t)w.size();
     H.radix3 = 0;
+    H.radix3_ref = 0;
     unsigned __int128 C = 1;
-    bool over = false;
+    bool over = w.size() > 64;
+    // reference slot order = names sorted (weight_nodes, search.py:85-88); the
+    // enumeration order used on the device = template (topological) order, so a
+    // failing node's ancestor cone sits in the slow digits (prefix skipping).
+    std::vector<int64_t> enum_order(w.begin(), w.end());
+    std::sort(enum_order.begin(), enum_order.end());
+    for (size_t q = 0; q < enum_order.size() && !over; q++) slot_of[enum_order[q]] = (int16_t)q;
     for (size_t sidx = 0; sidx < w.size(); sidx++) {
       const int64_t e = w[sidx];
       const int r = dg->h_w_rank[out->tmpl_nodes[e]] >= 2 ? 3 : 2;  // _options (search.py:91-93)
-      slot_of[e] = (int16_t)sidx;
-      radix_of[e] = (uint8_t)r;
-      if (r == 3 && sidx < 64) H.radix3 |= 1ULL << sidx;
+      if (!over) {
+        ref_slot_of[e] = (int16_t)sidx;
+        radix_of[e] = (uint8_t)r;
+        if (r == 3) {
+          H.radix3_ref |= 1ULL << sidx;
+          H.radix3 |= 1ULL << slot_of[e];
+        }
+      }
       out->slot_pos[b].push_back((int32_t)(e - e0));
       C *= (unsigned)r;
       if (C > (unsigned __int128)UINT64_MAX) over = true;
     }
-    if (w.size() > 64) over = true;
     H.C = over ? 0 : (uint64_t)C;
     if (over) out->overflow = true;
   }
@@ -1065,6 +1305,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   out->d_tmpl_off.upload(out->tmpl_off.data(), nb + 1, s);
   out->d_tmpl_nodes.upload(out->tmpl_nodes.data(), ne, s);
   D.slot_of.upload(slot_of.data(), ne, s);
+  D.ref_slot_of.upload(ref_slot_of.data(), ne, s);
   DevBuf<uint8_t> radix_d;
   radix_d.upload(radix_of.data(), ne, s);
   D.node_block.alloc(n, s);
@@ -1116,7 +1357,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   out->d_blob_off.upload(out->blob_off.data(), nb + 1, s);
   if (nb > 0)
     SP_LAUNCH(ctx, k_fill, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
-              D.node_tpos.p, D.slot_of.p, lay.p, hdr.p, out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
+              D.node_tpos.p, D.slot_of.p, D.ref_slot_of.p, lay.p, hdr.p, out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
               chunk, out->blobs.p, D.bound.p);
   SP_CUDA(cudaGetLastError());
 }
@@ -1132,7 +1373,7 @@ struct FusedExplain {
 };
 
 static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long long>& lo,
-                      const std::vector<unsigned long long>& hi, double* d_totals, std::vector<sp_score_out>& res,
+                      const std::vector<unsigned long long>& hi, std::vector<sp_score_out>& res,
                       const FusedExplain* fx = nullptr) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
@@ -1145,11 +1386,13 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score, THREADS, smem));
   if (per_sm < 1) per_sm = 1;
   const unsigned long long slots = (unsigned long long)ctx->sm_count * per_sm;
-  // size work items so the grid gets ~4 items per resident CTA (dynamic balance)
+  // size work items so the grid gets ~8 items per resident CTA (dynamic balance);
+  // with prefix skipping a candidate costs far less, so items may grow larger
   unsigned long long total = 0;
   for (int64_t b = 0; b < nb; b++) total += hi[b] > lo[b] ? hi[b] - lo[b] : 0;
-  unsigned long long iters = (total + slots * 4 * THREADS - 1) / (slots * 4 * THREADS);
-  iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, ITEM_ITERS_MAX));
+  const unsigned long long cap = ctx->skip ? ITEM_ITERS_MAX_SKIP : ITEM_ITERS_MAX;
+  unsigned long long iters = (total + slots * 8 * THREADS - 1) / (slots * 8 * THREADS);
+  iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, cap));
   const unsigned long long item_cands = iters * THREADS;
   std::vector<unsigned long long> base(nb + 1, 0);
   for (int64_t b = 0; b < nb; b++) {
@@ -1170,10 +1413,10 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   items.alloc(n_items, s);
   dout.alloc(nb, s);
   unsigned long long* counter = dplan.p + 3 * nb + 1;
-  ScorePlan P{t->d_blob_off.p, item_cands, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items};
+  ScorePlan P{t->d_blob_off.p, item_cands, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items, ctx->skip};
   const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
   SP_CUDA(cudaEventRecord(ctx->ev[2], s));
-  SP_LAUNCH(ctx, k_score, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter, d_totals);
+  SP_LAUNCH(ctx, k_score, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter);
   SP_CUDA(cudaEventRecord(ctx->ev[3], s));
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);
@@ -1191,7 +1434,7 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
     dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
     SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
               t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
-              priv->dev.slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, deoff.p,
+              priv->dev.ref_slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, deoff.p,
               (const unsigned long long*)nullptr, dout.p, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p,
               dedge.p);
     SP_CUDA(cudaGetLastError());
@@ -1223,7 +1466,7 @@ void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_sc
   SP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   std::vector<sp_score_out> res;
   FusedExplain fx{xblocks, xnode, xedge};
-  run_score(ctx, t, lo, hi, nullptr, res, xblocks ? &fx : nullptr);
+  run_score(ctx, t, lo, hi, res, xblocks ? &fx : nullptr);
   SP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   SP_CUDA(cudaEventSynchronize(ctx->ev[1]));
   float ms = 0;
@@ -1242,19 +1485,37 @@ void score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t
   if (H.C == 0) throw Error(SP_ERR_UNSUPPORTED, "block has more than 2**64 candidates");
   if (hi > H.C) hi = H.C;
   if (lo > hi) lo = hi;
-  const int64_t nb = t->n_blocks;
-  std::vector<unsigned long long> l(nb, 0), h(nb, 0);
-  l[block] = lo;
-  h[block] = hi;
-  DevBuf<double> dt;
-  if (totals && hi > lo) dt.alloc(hi - lo, ctx->stream);
-  std::vector<sp_score_out> res;
-  run_score(ctx, t, l, h, totals && hi > lo ? dt.p : nullptr, res);
-  *out = res.empty() ? sp_score_out{} : res[block];
+  cudaStream_t s = ctx->stream;
+  *out = sp_score_out{};
   out->candidates = H.C;
-  if (totals && hi > lo) {
-    dt.download(totals, hi - lo, ctx->stream);
-    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hi == lo) return;
+  const size_t smem = score_smem(t);
+  if (smem > ctx->smem_optin)
+    throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
+  SP_CUDA(cudaFuncSetAttribute(k_score_table, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned long long n = hi - lo;
+  const unsigned grid = (unsigned)std::min<unsigned long long>((n + THREADS - 1) / THREADS, 4ULL * ctx->sm_count);
+  DevBuf<double> dt;
+  DevBuf<ItemOut> cta;
+  if (totals) dt.alloc(n, s);
+  cta.alloc(grid, s);
+  SP_LAUNCH(ctx, k_score_table, grid, THREADS, smem, s, t->blobs.p, t->blob_off[block], lo, hi,
+            totals ? dt.p : nullptr, cta.p);
+  SP_CUDA(cudaGetLastError());
+  std::vector<ItemOut> h(grid);
+  cta.download(h.data(), grid, s);
+  if (totals) dt.download(totals, n, s);
+  SP_CUDA(cudaStreamSynchronize(s));
+  for (const ItemOut& o : h) {
+    out->valid += o.valid;
+    if (o.valid == 0) continue;
+    sp_score_out c{};
+    c.has_best = 1;
+    c.best_total = __builtin_bit_cast(double, o.total_bits);
+    c.best_num_split = (int32_t)o.num_split;
+    c.best_index = o.index;
+    c.valid = 0;
+    merge_key(out, &c);
   }
 }
 
@@ -1269,7 +1530,7 @@ void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explai
   std::vector<uint8_t> digits(std::max(V, 1), 0);
   uint64_t rem = index;
   for (int sidx = V - 1; sidx >= 0; sidx--) {
-    const uint64_t r = ((H.radix3 >> sidx) & 1) ? 3 : 2;
+    const uint64_t r = ((H.radix3_ref >> sidx) & 1) ? 3 : 2;
     digits[sidx] = (uint8_t)(rem % r);
     rem /= r;
   }
@@ -1285,7 +1546,7 @@ void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explai
   dedges.alloc(std::max(max_edges, 1), s);
   dne.alloc(1, s);
   SP_LAUNCH(ctx, k_explain, 1, 1, 0, s, view_of(t->dg), t->d_tmpl_nodes.p + e0, T, (int32_t)block, priv->dev.node_block.p,
-                            priv->dev.node_tpos.p, priv->dev.slot_of.p + e0, ddig.p, priv->dev.bound.p + e0, priv->mesh, priv->mu,
+                            priv->dev.node_tpos.p, priv->dev.ref_slot_of.p + e0, ddig.p, priv->dev.bound.p + e0, priv->mesh, priv->mu,
                             priv->chunk, dout.p, dedges.p, max_edges, dne.p);
   SP_CUDA(cudaGetLastError());
   dout.download(out, 1, s);
@@ -1320,7 +1581,7 @@ void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* block
   dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
   SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
             t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
-            priv->dev.slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, (const int64_t*)(dup.p + nb),
+            priv->dev.ref_slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, (const int64_t*)(dup.p + nb),
             dup.p, (const sp_score_out*)nullptr, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p, dedge.p);
   SP_CUDA(cudaGetLastError());
   dblk.download((ExplainBlock*)blocks_out, nb, s);

@@ -93,6 +93,7 @@ struct sp_ctx {
   std::string last_error;
   double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;
   int64_t own_launches = 0, cub_calls = 0;
+  int skip = 1;  // exact prefix-failure skipping in sp_score / sp_search
   cudaEvent_t timer[2] = {};
   // scratch reused across calls
   sp::DevBuf<uint8_t> cub_tmp;
@@ -129,12 +130,16 @@ struct sp_fold {
 // One block's table blob header (lives at the start of each blob in HBM and smem).
 struct BlobHeader {
   uint64_t C;             // candidate count
-  uint64_t radix3;        // bit s set: slot s has 3 options, else 2
+  uint64_t radix3;        // bit q set: ENUMERATION position q has 3 options, else 2
   int32_t T, V, nt, npool;
   int32_t desc_off, prod_off, tab_off, dbl_off;  // byte offsets from blob start
   int32_t train_off, bytes, multi_dev, n_prod;    // multi_dev: device_count > 1; n_prod: internal edges
   double setup, c_ar, bw, eff_ar, keep_bwd;       // keep_bwd = 1.0 - overlap_fraction
-  int64_t mu, chunk, pad1;
+  int64_t mu, chunk;
+  uint64_t radix3_ref;    // bit s set: REFERENCE slot s (weight_nodes order) has 3 options
+  int32_t skip_off;       // NodeSkip[T]
+  int32_t stride_off;     // u64 reference stride per enumeration position, then int8 perm[V]
+  int64_t pad2;
 };
 static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
 
@@ -148,6 +153,16 @@ struct NodeDesc {
   uint32_t dbl;      // double offset within the double section (own[4], exitc[4], conv[k][4][3])
 };
 static_assert(sizeof(NodeDesc) == 16, "NodeDesc is one 16-byte smem load");
+
+// Exact prefix-failure skipping: if node i fails, every candidate that keeps
+// the digits of the enumeration positions 0..m of its ancestor cone fails too,
+// so the enumeration may jump to the next multiple of R = prod radix(q > m).
+struct NodeSkip {
+  uint64_t R;  // skip modulus (0 when the node has no weighted ancestor: skip to the end)
+  int32_t m;   // highest enumeration position in the node's ancestor cone, -1 if none
+  int32_t pad;
+};
+static_assert(sizeof(NodeSkip) == 16, "NodeSkip layout");
 
 struct TrainDesc {
   int32_t slot;

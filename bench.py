@@ -1,23 +1,29 @@
 """Benchmark: candidate sharding plans scored/sec for TAP's plan search on B200.
 
-Workload (BASELINE.json configs[1], "c2"): the T5-base-structured ONNX graph
-(12+12 blocks, d 768, ff 3072, vocab 32128, batch 8, seq 128; built with the
-reference's wire codec, tests/golden/make_golden.py) searched exhaustively on
-a 1x8 mesh: 450 GraphNodes -> 8 unique blocks -> 475,320 candidate plans per
-step.  A step is one full `derive_plan`: fold (prune_graph) + routing tables
-+ scoring of every candidate of every block + winner reconstruction.
+Headline workload (BASELINE.json configs[4], "c5" -- the config the metric
+"candidate sharding plans scored/sec ... at 1/2/4/8 B200" is quoted on: the
+candidate-throughput sweep): a ~10^5-op DAG of 16 repeated random motif types
+(paper_2302_00247_b200.workloads.motif_dag(seed=0, tier="throughput"), pinned
+to the reference's own fold/search by tests/golden/c5.json).  99,658
+GraphNodes fold into 1018 blocks with 3,918,656,938 candidate plans on a 1x8
+mesh.  A step is one full `derive_plan`: fold + routing tables + every
+candidate of every block + winner reconstruction + report assembly.
 
-  value  device-resident: graph CSR already in HBM, CUDA events on the
-         backend's stream around each step, L2 flushed between steps.
-  e2e    the public API from host objects every step: lowering, H2D of the
+  value  device-resident graph, brute-force scoring (every candidate walked
+         until its first failing node, as the reference does), CUDA events on
+         the backend's stream around each step, L2 flushed between steps.
+  e2e    the public API from host objects every step: lowering, one H2D of the
          graph arrays, fold, score, D2H of results, report assembly.
+  prefix_skip  the same search with the backend's default exact prefix-failure
+         skipping (identical counts and argmin; fewer candidates walked).
+  c2     the T5-base ONNX config (BASELINE configs[1]) for comparison.
 
 `--impl reference` times the CPU restatement of the reference's algorithm
-(oracle/oracle.c, all host threads) on the same workload.
+(oracle/oracle.c, all host threads) on a bounded sample of the same workload.
 
 Multi-GPU (torchrun): every rank folds (replicated) and scores its
 contiguous slice of each block's candidate range; one NCCL all_gather of
-40-byte per-block records merges the exact argmin (strong scaling).
+48-byte per-block records merges the exact argmin (strong scaling).
 """
 
 from __future__ import annotations
@@ -38,13 +44,30 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 METRIC = "candidate sharding plans scored/sec"
 UNIT = "candidates/s"
 C2_GRAPH = os.path.join(ROOT, "tests", "golden", "graphs", "c2_t5.json.gz")
-WORKLOAD = ("c2: T5-base ONNX graph (450 GraphNodes, 8 unique blocks), 1x8 mesh, "
-            "exhaustive per-block candidates")
+WORKLOADS = {
+    "c5": ("c5: 10^5-op motif DAG (99,658 GraphNodes, 16 motif types, 1018 blocks), 1x8 mesh, "
+           "every candidate of every block (3.92e9)",
+           "synthetic: workloads.motif_dag(seed=0, tier='throughput'), deterministic; pinned to the "
+           "reference via tests/golden/c5.json"),
+    "c2": ("c2: T5-base ONNX graph (450 GraphNodes, 8 unique blocks), 1x8 mesh, exhaustive "
+           "per-block candidates (475,320)",
+           "synthetic: T5-base-structured ONNX graph built with the reference's wire codec "
+           "(tests/golden/graphs/c2_t5.json.gz)"),
+}
 
 
 def _dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def load_workload(name: str):
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.ir import load_grouped
+    from paper_2302_00247_b200.workloads import motif_dag
+
+    g = motif_dag(0, "throughput") if name == "c5" else load_grouped(C2_GRAPH)
+    return g, ClusterSpec.from_mesh("1x8")
 
 
 class ClockSampler:
@@ -86,90 +109,94 @@ class ClockSampler:
             self.thread.join(timeout=5)
 
     def summary(self) -> dict:
-        if not self.rows:
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [v for v in (num(r[1]) for r in self.rows if len(r) > 2) if v is not None]
+        mx = [v for v in (num(r[2]) for r in self.rows if len(r) > 2) if v is not None]
+        if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = set()
         for r in self.rows:
             for k, name in enumerate(names):
                 if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
-
-
-def load_workload():
-    from paper_2302_00247_b200.api_types import ClusterSpec
-    from paper_2302_00247_b200.ir import load_grouped
-
-    return load_grouped(C2_GRAPH), ClusterSpec.from_mesh("1x8")
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ---------------------------------------------------------------------------
 # CPU arm: the oracle (C restatement of the reference algorithm)
 
 
-def cpu_search(low, mesh, threads: int) -> int:
+def cpu_step(low, mesh, threads: int, slice_width: int) -> tuple:
+    """One bounded CPU search step: prune, every block with <= 2e6 candidates in
+    full, and 8 evenly spaced slices of `slice_width` candidates of each larger
+    block ([k*C/8, k*C/8 + w), k = 0..7).  Returns (candidates walked, valid)."""
     from oracle import oracle
     from paper_2302_00247_b200.blocks import BlockArrays
 
     ba = BlockArrays.from_dict(oracle.prune(low, 2))
-    cands = 0
+    walked = valid = 0
     for b in range(ba.n_blocks):
-        out, _ = oracle.score(low, ba.template_nodes(b), mesh, threads=threads)
-        if not out.has_best:
-            raise AssertionError("all-replica fallback must always route")
-        cands += out.candidates
-    return cands
+        tn = ba.template_nodes(b)
+        out, _ = oracle.score(low, tn, mesh, threads=threads, hi=0)
+        C = out.candidates
+        if C <= 2_000_000:
+            out, _ = oracle.score(low, tn, mesh, threads=threads)
+            if not out.has_best:
+                raise AssertionError("all-replica fallback must always route")
+            walked += C
+            valid += out.valid
+        else:
+            for k in range(8):
+                lo = k * C // 8
+                hi = min(C, lo + slice_width)
+                out, _ = oracle.score(low, tn, mesh, lo=lo, hi=hi, threads=threads)
+                walked += hi - lo
+                valid += out.valid
+    return walked, valid
 
 
-def cpu_baseline(min_seconds: float = 10.0, max_reps: int = 50) -> dict:
+def cpu_measure(workload: str, min_seconds: float, max_steps: int = 50) -> dict:
     from paper_2302_00247_b200.lowering import lower
 
-    g, mesh = load_workload()
+    g, mesh = load_workload(workload)
     low = lower(g)
     threads = os.cpu_count() or 1
-    cpu_search(low, mesh, threads)  # warm (builds/loads the oracle)
-    reps, cands = 0, 0
+    width = 4_000_000 if workload == "c5" else 0
+    cpu_step(low, mesh, threads, width)  # warm (builds/loads the oracle)
+    steps = walked = 0
     t0 = time.perf_counter()
-    while reps < max_reps and (time.perf_counter() - t0) < min_seconds:
-        cands += cpu_search(low, mesh, threads)
-        reps += 1
+    while steps < max_steps and (steps == 0 or time.perf_counter() - t0 < min_seconds):
+        walked += cpu_step(low, mesh, threads, width)[0]
+        steps += 1
     dt = time.perf_counter() - t0
-    return {"value": cands / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{reps} full c2 searches (prune + all {cands // max(reps, 1)} candidates) "
-                      f"in {dt:.1f}s, oracle/oracle.c with {threads} pthreads"}
+    sample = (f"{steps} steps of: prune + all blocks <= 2e6 candidates in full + 8 slices of "
+              f"{width:,} candidates of each larger block; {walked // steps:,} candidates walked "
+              f"per step" if workload == "c5" else f"{steps} full c2 searches")
+    return {"value": walked / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample}, {dt:.1f}s, oracle/oracle.c with {threads} pthreads",
+            "seconds": dt, "steps": steps}
 
 
 def run_reference(args) -> None:
-    rank, world, _ = _dist_env()
+    rank, _, _ = _dist_env()
     if rank != 0:
         return
-    from paper_2302_00247_b200.lowering import lower
-
-    g, mesh = load_workload()
-    low = lower(g)
-    threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_search(low, mesh, threads)
-    t0 = time.perf_counter()
-    cands = 0
-    for _ in range(args.steps):
-        cands += cpu_search(low, mesh, threads)
-    dt = time.perf_counter() - t0
-    value = cands / dt
+    m = cpu_measure(args.workload, min_seconds=0.0, max_steps=args.steps)
+    value = m["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1000 / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["seconds"] * 1000 / m["steps"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: T5-base-structured ONNX graph (tests/golden/graphs/c2_t5.json.gz)",
-        "config": {"workload": WORKLOAD, "candidates_per_step": cands // args.steps,
-                   "mesh": "1x8", "min_dup": 2},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full c2 searches, oracle/oracle.c, {threads} pthreads"},
+        "data": WORKLOADS[args.workload][1],
+        "config": {"workload": WORKLOADS[args.workload][0], "mesh": "1x8", "min_dup": 2},
+        "cpu_baseline": {k: m[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -179,29 +206,12 @@ def run_reference(args) -> None:
 # GPU arm
 
 
-def run_ours(args) -> None:
-    import torch
-    import torch.distributed as dist
-
-    from paper_2302_00247_b200._native import Backend
-    from paper_2302_00247_b200.dist import allgather_exchange
+def measure(be, g, mesh, steps, warmup, rank, world, exchange, flush, barrier, skip,
+            want_e2e=True, clocks_dev=None) -> dict:
     from paper_2302_00247_b200 import search as sp_search
     from paper_2302_00247_b200.search import Session, derive_plan
 
-    rank, world, local = _dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    exchange = allgather_exchange() if world > 1 else None
-    be = Backend(local)
-    g, mesh = load_workload()
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
+    be.set_prefix_skip(skip)
     ses = Session.open(g, be)  # graph CSR resident in HBM before timing
 
     def step_resident():
@@ -212,17 +222,18 @@ def run_ours(args) -> None:
                            exchange=exchange)
 
     ref = step_resident()
-    cands = ref.candidates
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step_resident()
-        step_e2e()
+        if want_e2e:
+            step_e2e()
     barrier()
-
-    # -- device-resident value ------------------------------------------------------
     own0, cub0 = be.launch_counts()
     times, fold_ms, score_ms, kern_ms, phases = [], [], [], [], []
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
+    sampler = ClockSampler(clocks_dev) if clocks_dev is not None else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        for _ in range(steps):
             flush.zero_()
             barrier()
             be.timer_start()
@@ -233,37 +244,93 @@ def run_ours(args) -> None:
             score_ms.append(t["score_ms"])
             kern_ms.append(t["score_kernel_ms"])
             phases.append(dict(sp_search.LAST_PHASES))
+    finally:
+        if sampler:
+            sampler.__exit__(None, None, None)
     own1, cub1 = be.launch_counts()
-    assert rep.candidates == cands and rep.total_cost == ref.total_cost
-
-    # -- end-to-end through the public API from host objects ----------------------
+    assert rep.candidates == ref.candidates and rep.total_cost == ref.total_cost
     e2e_times = []
     h0, d0 = be.copy_bytes()
-    for _ in range(args.steps):
-        flush.zero_()
-        barrier()
-        be.timer_start()
-        rep = step_e2e()
-        e2e_times.append(be.timer_stop())
+    if want_e2e:
+        for _ in range(steps):
+            flush.zero_()
+            barrier()
+            be.timer_start()
+            rep = step_e2e()
+            e2e_times.append(be.timer_stop())
+        assert rep.total_cost == ref.total_cost
     h1, d1 = be.copy_bytes()
-    assert rep.total_cost == ref.total_cost
+    return {"ref": ref, "ses": ses, "times": times, "e2e_times": e2e_times, "fold_ms": fold_ms,
+            "score_ms": score_ms, "kern_ms": kern_ms, "phases": phases,
+            "launches": (own1 - own0) / steps, "cub": (cub1 - cub0) / steps,
+            "h2d": (h1 - h0) // max(1, steps), "d2h": (d1 - d0) // max(1, steps),
+            "clocks": sampler.summary() if sampler else None}
 
-    total_ms = sum(times)
-    e2e_ms = sum(e2e_times)
+
+def _maxsum(vals, world):
+    import torch
+    import torch.distributed as dist
+
+    s = float(sum(vals))
     if world > 1:
-        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_ms = t.tolist()
+        s = t.item()
+    return s
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_00247_b200._native import Backend
+    from paper_2302_00247_b200.dist import allgather_exchange
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    exchange = allgather_exchange() if world > 1 else None
+    be = Backend(local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    g, mesh = load_workload(args.workload)
+    main = measure(be, g, mesh, args.steps, args.warmup, rank, world, exchange, flush, barrier,
+                   skip=False, clocks_dev=local)
+    cands = main["ref"].candidates
+    total_ms = _maxsum(main["times"], world)
+    e2e_ms = _maxsum(main["e2e_times"], world)
     value = cands * args.steps / (total_ms / 1000.0)
     e2e_value = cands * args.steps / (e2e_ms / 1000.0)
+    walked_valid = main["ref"].valid
 
-    # roofline of the dominant kernel (k_score): algorithmic bytes per launch =
-    # routing tables staged once per block + 24 B per work item + 40 B per block
-    kern = statistics.median(kern_ms)
-    tables_bytes = getattr(ses, "last_table_bytes", None)
-    nb = len(ref.results)
-    items = sum((r.candidates + 4095) // 4096 for r in ref.results)
-    alg_bytes = (tables_bytes or 0) + 24 * items + 40 * nb
+    skip = measure(be, g, mesh, args.steps, args.warmup, rank, world, exchange, flush, barrier,
+                   skip=True, want_e2e=True)
+    skip_ms = _maxsum(skip["times"], world)
+    skip_e2e_ms = _maxsum(skip["e2e_times"], world)
+
+    extra = {}
+    if args.workload == "c5":
+        g2, mesh2 = load_workload("c2")
+        c2 = measure(be, g2, mesh2, 20, 5, rank, world, exchange, flush, barrier, skip=False)
+        c2ms, c2e = _maxsum(c2["times"], world), _maxsum(c2["e2e_times"], world)
+        extra["c2"] = {"workload": WORKLOADS["c2"][0], "candidates_per_step": c2["ref"].candidates,
+                       "value": c2["ref"].candidates * 20 / (c2ms / 1000.0),
+                       "e2e_value": c2["ref"].candidates * 20 / (c2e / 1000.0),
+                       "ms_per_step": c2ms / 20, "e2e_ms_per_step": c2e / 20}
+
+    # roofline of the dominant kernel (k_score, brute force): algorithmic bytes per
+    # launch = routing tables staged per block + 24 B per work item + 40 B per block
+    kern = statistics.median(main["kern_ms"])
+    ses = main["ses"]
+    nb = len(main["ref"].results)
+    items = sum((r.candidates + 16383) // 16384 for r in main["ref"].results)
+    alg_bytes = getattr(ses, "last_table_bytes", 0) + 24 * items + 40 * nb
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -272,36 +339,48 @@ def run_ours(args) -> None:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg_bytes / (kern / 1000.0) / 1e9 if kern > 0 else 0.0
+    kernel_rate = cands / world / (kern / 1000.0) if kern > 0 else 0.0
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: T5-base-structured ONNX graph (tests/golden/graphs/c2_t5.json.gz), "
-                "generated with the reference's ONNX wire codec",
-        "config": {"workload": WORKLOAD, "candidates_per_step": cands, "blocks": nb,
-                   "graph_nodes": len(g.nodes), "mesh": "1x8", "min_dup": 2,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": WORKLOADS[args.workload][1],
+        "config": {"workload": WORKLOADS[args.workload][0], "candidates_per_step": cands,
+                   "valid_plans_per_step": walked_valid, "blocks": nb, "graph_nodes": len(g.nodes),
+                   "mesh": "1x8", "min_dup": 2, "scoring": "brute force (no prefix skipping)",
                    "parallelism": f"candidate-range shards x{world}",
                    "l2": "flushed between steps (256 MiB write)"},
-        "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": (h1 - h0) // args.steps,
-                "d2h_bytes_per_step": (d1 - d0) // args.steps},
-        "gpu_launches": (own1 - own0) // args.steps * args.steps,
-        "gpu_launches_detail": {"own_kernels_per_step": (own1 - own0) / args.steps,
-                                "cub_calls_per_step": (cub1 - cub0) / args.steps},
-        "host_phases_ms": {k: statistics.median(p[k] for p in phases) for k in phases[0]},
-        "breakdown_ms": {"fold": statistics.median(fold_ms), "score_total": statistics.median(score_ms),
-                         "score_kernel": kern, "step": statistics.median(times),
-                         "e2e_step": statistics.median(e2e_times)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": main["h2d"],
+                "d2h_bytes_per_step": main["d2h"]},
+        "gpu_launches": int(round(main["launches"] * args.steps)),
+        "gpu_launches_detail": {"own_kernels_per_step": main["launches"],
+                                "cub_calls_per_step": main["cub"]},
+        "host_phases_ms": {k: statistics.median(p[k] for p in main["phases"])
+                           for k in main["phases"][0]},
+        "breakdown_ms": {"fold": statistics.median(main["fold_ms"]),
+                         "score_total": statistics.median(main["score_ms"]),
+                         "score_kernel": kern, "step": statistics.median(main["times"]),
+                         "e2e_step": statistics.median(main["e2e_times"])},
+        "kernel_rate": {"k_score_candidates_per_s_per_gpu": kernel_rate,
+                        "valid_plans_per_s": walked_valid * args.steps / (total_ms / 1000.0)},
         "roofline": {"kernel": "k_score", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
-                     "note": "scoring reads smem-resident tables; algorithmic HBM bytes are the "
-                             "staged tables + per-item records, so the kernel is issue-bound "
-                             "(see profiles/ and DESIGN.md)"},
-        "clocks": clocks.summary(),
+                     "note": "no per-candidate HBM input: algorithmic bytes are the staged "
+                             "routing tables + per-item records, so the kernel is SM-issue-bound; "
+                             "issue-slot utilisation is in profiles/ (DESIGN.md section 3)"},
+        "prefix_skip": {"value": cands * args.steps / (skip_ms / 1000.0),
+                        "e2e_value": cands * args.steps / (skip_e2e_ms / 1000.0),
+                        "ms_per_step": skip_ms / args.steps,
+                        "score_kernel_ms": statistics.median(skip["kern_ms"]),
+                        "note": "default API mode: exact prefix-failure skipping (same valid "
+                                "count, same argmin); candidates proven invalid in bulk count "
+                                "as resolved"},
+        "clocks": main["clocks"],
     }
+    line.update(extra)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+        cb = cpu_measure(args.workload, args.cpu_seconds)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -312,9 +391,10 @@ def run_ours(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="c5")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -36,6 +36,8 @@
 
 typedef struct {
   const sp_graph* g;
+  sp_graph gcopy;      /* owned copy of the caller's struct (arrays stay caller-owned) */
+  int64_t* pos;        /* node -> template position scratch, kept at -1 between calls */
   int64_t n;
   int32_t* depth;      /* number of '/'-separated parts */
   int64_t* slash;      /* [n*maxd] byte position of the d-th '/' (d=1..), or name len */
@@ -70,6 +72,8 @@ static int cmp_by_name(const void* x, const void* y) {
 
 static int og_init(og* G, const sp_graph* g) {
   memset(G, 0, sizeof(*G));
+  G->gcopy = *g;
+  g = &G->gcopy;
   G->g = g;
   G->n = g->n_nodes;
   int64_t n = G->n;
@@ -109,10 +113,13 @@ static int og_init(og* G, const sp_graph* g) {
       G->cons_idx[G->cons_off[p] + fill[p]++] = i;
     }
   free(fill);
+  G->pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+  for (int64_t i = 0; i < n; i++) G->pos[i] = -1;
   return 0;
 }
 
 static void og_free(og* G) {
+  free(G->pos);
   free(G->depth);
   free(G->slash);
   free(G->by_name);
@@ -894,8 +901,7 @@ static int block_init(block_ctx* B, og* G, const int32_t* tmpl, int64_t T, const
   int64_t* tn = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T ? T : 1));
   for (int64_t i = 0; i < T; i++) tn[i] = tmpl[i];
   B->tn = tn;
-  B->pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)(g->n_nodes ? g->n_nodes : 1));
-  for (int64_t i = 0; i < g->n_nodes; i++) B->pos[i] = -1;
+  B->pos = G->pos;  /* all -1 outside this template; restored by block_free */
   for (int64_t i = 0; i < T; i++) B->pos[tn[i]] = i;
   for (int64_t i = 0; i < T; i++) {
     const pattern* pats;
@@ -933,8 +939,8 @@ static int block_init(block_ctx* B, og* G, const int32_t* tmpl, int64_t T, const
 }
 
 static void block_free(block_ctx* B) {
+  for (int64_t i = 0; i < B->T; i++) B->pos[B->tn[i]] = -1;
   free((void*)B->tn);
-  free(B->pos);
   free(B->slot);
   free(B->slot_pos);
   free(B->radix);
@@ -994,22 +1000,46 @@ static void* work(void* arg) {
  * `threads` pthreads like search_subgraph's worker pool (search.py:331-343).
  * totals (optional, [hi-lo]) receives CostReport.total or NaN for invalid.
  */
+static int score_core(og* Gp, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu, int64_t chunk,
+                      uint64_t lo, uint64_t hi, int32_t threads, double* totals, sp_score_out* out);
+
+/* Graph handle: build the per-graph structures (name order, consumers) once. */
+void* oracle_graph_open(const sp_graph* g) {
+  og* G = (og*)malloc(sizeof(og));
+  og_init(G, g);
+  return G;
+}
+
+void oracle_graph_close(void* h) {
+  if (!h) return;
+  og_free((og*)h);
+  free(h);
+}
+
+int oracle_score_h(void* h, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu, int64_t chunk,
+                   uint64_t lo, uint64_t hi, int32_t threads, double* totals, sp_score_out* out) {
+  return score_core((og*)h, tmpl, T, M, mu, chunk, lo, hi, threads, totals, out);
+}
+
 int oracle_score(const sp_graph* g, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu,
                  int64_t chunk, uint64_t lo, uint64_t hi, int32_t threads, double* totals,
                  sp_score_out* out) {
   og G;
   og_init(&G, g);
+  int rc = score_core(&G, tmpl, T, M, mu, chunk, lo, hi, threads, totals, out);
+  og_free(&G);
+  return rc;
+}
+
+static int score_core(og* Gp, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu, int64_t chunk,
+                      uint64_t lo, uint64_t hi, int32_t threads, double* totals, sp_score_out* out) {
   block_ctx B;
-  int rc = block_init(&B, &G, tmpl, T, M, mu, chunk);
-  if (rc != SP_OK) {
-    og_free(&G);
-    return rc;
-  }
+  int rc = block_init(&B, Gp, tmpl, T, M, mu, chunk);
+  if (rc != SP_OK) return rc;
   memset(out, 0, sizeof(*out));
   uint64_t C;
   if (!block_count(&B, &C)) {
     block_free(&B);
-    og_free(&G);
     return SP_ERR_UNSUPPORTED;
   }
   out->candidates = C;
@@ -1045,21 +1075,32 @@ int oracle_score(const sp_graph* g, const int32_t* tmpl, int64_t T, const sp_mes
   free(ws);
   free(th);
   block_free(&B);
-  og_free(&G);
   return SP_OK;
 }
 
 /* Routing/cost detail of one candidate, same layout as sp_explain. */
+static int explain_core(og* Gp, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu,
+                        int64_t chunk, uint64_t index, sp_explain_out* out);
+
 int oracle_explain(const sp_graph* g, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu,
                    int64_t chunk, uint64_t index, sp_explain_out* out) {
   og G;
   og_init(&G, g);
+  int rc = explain_core(&G, tmpl, T, M, mu, chunk, index, out);
+  og_free(&G);
+  return rc;
+}
+
+int oracle_explain_h(void* h, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu, int64_t chunk,
+                     uint64_t index, sp_explain_out* out) {
+  return explain_core((og*)h, tmpl, T, M, mu, chunk, index, out);
+}
+
+static int explain_core(og* Gp, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu,
+                        int64_t chunk, uint64_t index, sp_explain_out* out) {
   block_ctx B;
-  int rc = block_init(&B, &G, tmpl, T, M, mu, chunk);
-  if (rc != SP_OK) {
-    og_free(&G);
-    return rc;
-  }
+  int rc = block_init(&B, Gp, tmpl, T, M, mu, chunk);
+  if (rc != SP_OK) return rc;
   cand_result* R = (cand_result*)calloc(1, sizeof(cand_result));
   eval_candidate(&B, index, R, 1);
   memset(out, 0, sizeof(*out));
@@ -1087,7 +1128,6 @@ int oracle_explain(const sp_graph* g, const int32_t* tmpl, int64_t T, const sp_m
   }
   free(R);
   block_free(&B);
-  og_free(&G);
   return SP_OK;
 }
 

@@ -55,6 +55,16 @@ def lib():
         L.oracle_slots.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64,
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.oracle_slots.restype = C.c_int
+        L.oracle_graph_open.argtypes = [C.c_void_p]
+        L.oracle_graph_open.restype = C.c_void_p
+        L.oracle_graph_close.argtypes = [C.c_void_p]
+        L.oracle_score_h.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64, C.c_void_p,
+                                     C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int32,
+                                     C.POINTER(C.c_double), C.POINTER(SpScoreOut)]
+        L.oracle_score_h.restype = C.c_int
+        L.oracle_explain_h.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64, C.c_void_p,
+                                       C.c_int64, C.c_int64, C.c_uint64, C.POINTER(SpExplainOut)]
+        L.oracle_explain_h.restype = C.c_int
         _lib = L
     return _lib
 
@@ -71,9 +81,31 @@ def prune(low, min_dup: int) -> dict:
         lib().oracle_blocks_free(h)
 
 
+class _GraphHandle:
+    """Per-graph oracle structures (name order, consumers), built once."""
+
+    def __init__(self, low):
+        self.keep = make_sp_graph(low)
+        self.h = lib().oracle_graph_open(C.byref(self.keep))
+
+    def __del__(self):  # pragma: no cover - GC timing
+        try:
+            lib().oracle_graph_close(self.h)
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def _handle(low):
+    h = getattr(low, "_oracle_handle", None)
+    if h is None:
+        h = _GraphHandle(low)
+        low._oracle_handle = h
+    return h.h
+
+
 def score(low, tmpl_nodes, mesh, mu=1 << 20, chunk=4 << 20, lo=0, hi=None, threads=1,
           want_totals=False):
-    g = make_sp_graph(low)
+    h = _handle(low)
     m = make_sp_mesh(mesh)
     tn = np.ascontiguousarray(tmpl_nodes, dtype=np.int32)
     out = SpScoreOut()
@@ -84,20 +116,20 @@ def score(low, tmpl_nodes, mesh, mu=1 << 20, chunk=4 << 20, lo=0, hi=None, threa
     if want_totals:
         totals = np.empty(int(hi - lo), np.float64)
         tp = ptr(totals, C.c_double)
-    rc = lib().oracle_score(C.byref(g), ptr(tn, C.c_int32) if tn.size else None, tn.size,
-                            C.byref(m), mu, chunk, lo, hi, threads, tp, C.byref(out))
+    rc = lib().oracle_score_h(h, ptr(tn, C.c_int32) if tn.size else None, tn.size,
+                              C.byref(m), mu, chunk, lo, hi, threads, tp, C.byref(out))
     if rc != 0:
         raise RuntimeError(f"oracle_score rc={rc}")
     return out, totals
 
 
 def explain(low, tmpl_nodes, mesh, index, mu=1 << 20, chunk=4 << 20) -> SpExplainOut:
-    g = make_sp_graph(low)
+    h = _handle(low)
     m = make_sp_mesh(mesh)
     tn = np.ascontiguousarray(tmpl_nodes, dtype=np.int32)
     out = SpExplainOut()
-    rc = lib().oracle_explain(C.byref(g), ptr(tn, C.c_int32), tn.size, C.byref(m), mu, chunk,
-                              index, C.byref(out))
+    rc = lib().oracle_explain_h(h, ptr(tn, C.c_int32), tn.size, C.byref(m), mu, chunk,
+                                index, C.byref(out))
     if rc != 0:
         raise RuntimeError(f"oracle_explain rc={rc}")
     return out

@@ -185,10 +185,29 @@ def cpu_measure(workload: str, min_seconds: float, max_steps: int = 50) -> dict:
 
 
 def run_reference(args) -> None:
+    """The CPU arm: warm-up steps, then exactly `steps` timed steps on rank 0."""
     rank, _, _ = _dist_env()
     if rank != 0:
         return
-    m = cpu_measure(args.workload, min_seconds=0.0, max_steps=args.steps)
+    from paper_2302_00247_b200.lowering import lower
+
+    g, mesh = load_workload(args.workload)
+    low = lower(g)
+    threads = os.cpu_count() or 1
+    width = 4_000_000 if args.workload == "c5" else 0
+    for _ in range(args.warmup):
+        cpu_step(low, mesh, threads, width)
+    walked = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        walked += cpu_step(low, mesh, threads, width)[0]
+    dt = time.perf_counter() - t0
+    m = {"value": walked / dt, "unit": UNIT, "cores": threads, "kind": "port", "seconds": dt,
+         "steps": args.steps,
+         "sample": (f"{args.steps} steps x {walked // args.steps:,} candidates walked (prune + "
+                    f"blocks <= 2e6 in full + 8 slices of {width:,} of each larger block)"
+                    if args.workload == "c5" else f"{args.steps} full c2 searches")
+                   + f", oracle/oracle.c with {threads} pthreads"}
     value = m["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,

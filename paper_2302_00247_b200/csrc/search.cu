@@ -422,6 +422,13 @@ __device__ __forceinline__ bool key_less(unsigned long long ta, uint32_t na, uns
   return ia < ib;
 }
 
+// max of two non-negative, non-NaN doubles: their bit patterns order like the
+// values, so an integer max is exact (and cheaper than DSETP/SEL/FSEL).
+__device__ __forceinline__ double dmax_nn(double a, double b) {
+  const long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  return __longlong_as_double(x > y ? x : y);
+}
+
 __device__ __forceinline__ uint32_t get_digit(uint64_t w0, uint64_t w1, int s) {
   return (uint32_t)(((s < 32 ? w0 : w1) >> ((s & 31) * 2)) & 3);
 }
@@ -493,6 +500,7 @@ __device__ __forceinline__ Tabs tabs_of(uint8_t* smem) {
 // (digits packed in enumeration order).  Returns -1 when it routes (fwd =
 // forward time), else the first failing template position; T when inactive.
 // Warp-collective: all 32 lanes call it (uniform node loop, ballot exit).
+template <bool WIDE>
 __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, bool active, double& fwd, int tid) {
   const int T = S.H->T;
   bool ok = active;
@@ -500,7 +508,8 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
   fwd = 0.0;
   for (int i = 0; i < T; i++) {
     const NodeDesc nd = S.desc[i];
-    uint32_t key = nd.slot >= 0 ? get_digit(w0, w1, nd.slot) : 0;
+    uint32_t key = 0;
+    if (nd.slot >= 0) key = WIDE ? get_digit(w0, w1, nd.slot) : (uint32_t)((w0 >> (nd.slot * 2)) & 3);
     const double* D = S.dbl + nd.dbl;
     double r;
     int s;
@@ -533,7 +542,7 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
       if (!__any_sync(0xffffffffu, ok)) break;
       const int p = e & 3;
       s = ok ? (e >> 2) & 3 : 0;
-      r = dadd(fmax(dadd(r0, D[8 + p * 3 + s0]), dadd(r1, D[8 + (4 + p) * 3 + s1])), D[p]);
+      r = dadd(dmax_nn(dadd(r0, D[8 + p * 3 + s0]), dadd(r1, D[8 + (4 + p) * 3 + s1])), D[p]);
     } else {
       int sj[KMAX];
       double rj[KMAX];
@@ -549,10 +558,10 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
       const int p = e & 3;
       s = ok ? (e >> 2) & 3 : 0;
       double bse = 0.0;
-      for (int j = 0; j < nd.k; j++) bse = fmax(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
+      for (int j = 0; j < nd.k; j++) bse = dmax_nn(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
       r = dadd(bse, D[p]);
     }
-    fwd = fmax(fwd, dadd(r, D[4 + s]));
+    fwd = dmax_nn(fwd, dadd(r, D[4 + s]));
     if (nd.out_pool >= 0) {
       S.reach[nd.out_pool * THREADS + tid] = r;
       S.stp[nd.out_pool * THREADS + tid] = (uint8_t)s;
@@ -658,7 +667,8 @@ __device__ __forceinline__ void stage_blob(uint8_t* smem, const uint8_t* blobs, 
 // candidate fails at node i proves its whole R-aligned run invalid (R =
 // NodeSkip.R), and the warp jumps to the max proven end: the union of the
 // lanes' runs is contiguous from the warp's base, so the jump is exact.
-__global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ blobs, ScorePlan P,
+template <bool WIDE>
+__global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict__ blobs, ScorePlan P,
                                                    ItemOut* __restrict__ items,
                                                    unsigned long long* __restrict__ counter) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -708,7 +718,7 @@ __global__ void __launch_bounds__(THREADS) k_score(const uint8_t* __restrict__ b
         uint64_t w0 = bw0, w1 = bw1;
         mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
         double fwd;
-        const int fail = walk(S, w0, w1, active, fwd, tid);
+        const int fail = walk<WIDE>(S, w0, w1, active, fwd, tid);
         unsigned long long t = x + 1;
         if (fail < 0) {
           const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
@@ -810,7 +820,7 @@ __global__ void __launch_bounds__(THREADS) k_score_table(const uint8_t* __restri
       else w1 |= (uint64_t)d << ((q - 32) * 2);
     }
     double fwd;
-    const int fail = walk(S, w0, w1, active, fwd, tid);
+    const int fail = walk<true>(S, w0, w1, active, fwd, tid);
     if (fail < 0) {
       const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
       const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
@@ -1381,9 +1391,12 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   const size_t smem = score_smem(t);
   if (smem > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
-  SP_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  bool wide = false;  // any block with more than 32 weight slots needs both digit words
+  for (int64_t b = 0; b < nb; b++) wide = wide || t->hdr[b].V > 32;
+  auto kern = wide ? k_score<true> : k_score<false>;
+  SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_score, THREADS, smem));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
   if (per_sm < 1) per_sm = 1;
   const unsigned long long slots = (unsigned long long)ctx->sm_count * per_sm;
   // size work items so the grid gets ~8 items per resident CTA (dynamic balance);
@@ -1416,7 +1429,7 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   ScorePlan P{t->d_blob_off.p, item_cands, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items, ctx->skip};
   const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
   SP_CUDA(cudaEventRecord(ctx->ev[2], s));
-  SP_LAUNCH(ctx, k_score, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter);
+  SP_LAUNCH(ctx, kern, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter);
   SP_CUDA(cudaEventRecord(ctx->ev[3], s));
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);

@@ -143,8 +143,8 @@ struct BlobHeader {
 };
 static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
 
-struct NodeDesc {
-  int16_t slot;      // weight slot or -1
+struct __align__(16) NodeDesc {
+  int16_t slot;      // weight slot (enumeration position) or -1
   uint8_t k;         // internal producers
   uint8_t nd;        // digit options (1 when unweighted)
   int16_t out_pool;  // pool slot receiving reach/state, -1 when no internal consumer

@@ -1,0 +1,98 @@
+"""World-size-2 test of the multi-GPU key exchange on CPU (gloo).
+
+Each rank scores its contiguous slice of every block's candidate range (the
+split search_subgraph gives its pool, search.py:331-336) -- here with the CPU
+oracle standing in for the GPU scorer -- and the ranks merge with
+paper_2302_00247_b200.dist.allgather_exchange, the exact code the NCCL path
+runs.  The merged per-block (valid, argmin) must equal the unsharded search.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+CASES = ("c2_1x8", "tiny_2x2", "chain6_2x4_mu")
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _shard_scores(name: str, rank: int, world: int):
+    from golden_io import case, lowered, mesh
+    from oracle import oracle
+    from paper_2302_00247_b200._abi import SpScoreOut
+    from paper_2302_00247_b200.blocks import BlockArrays
+
+    c = case(name)
+    low = lowered(c["graph"])
+    ba = BlockArrays.from_dict(oracle.prune(low, c["min_dup"]))
+    m = mesh(c["mesh"])
+    out = []
+    for b in range(ba.n_blocks):
+        tn = ba.template_nodes(b)
+        total, _ = oracle.score(low, tn, m, mu=c["mu"], chunk=c["chunk_size"], hi=0)
+        C = total.candidates
+        step = -(-C // world)
+        lo, hi = min(C, rank * step), min(C, (rank + 1) * step)
+        if lo < hi:
+            res, _ = oracle.score(low, tn, m, mu=c["mu"], chunk=c["chunk_size"], lo=lo, hi=hi,
+                                  threads=2)
+        else:
+            res = SpScoreOut()
+            res.candidates = C
+        out.append(res)
+    return out
+
+
+def _worker(rank: int, world: int, port: int, q):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), here]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2302_00247_b200.dist import allgather_exchange
+
+        ex = allgather_exchange()
+        result = {}
+        for name in CASES:
+            merged = ex(_shard_scores(name, rank, world))
+            result[name] = [(r.valid, r.has_best, r.best_index, r.best_num_split, r.best_total)
+                            for r in merged]
+        q.put((rank, result))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_two_rank_exchange_matches_single_process():
+    from golden_io import case
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert results[0] == results[1]  # every rank ends with the same plan keys
+    single = {name: [(r.valid, r.has_best, r.best_index, r.best_num_split, r.best_total)
+                     for r in _shard_scores(name, 0, 1)] for name in CASES}
+    assert results[0] == single
+    for name in CASES:  # and with the reference's goldens
+        exp = case(name)["best"]
+        assert [(v, i, repr(t)) for v, _, i, _, t in results[0][name]] == [
+            (e["valid"], e["index"], e["total"]) for e in exp]

@@ -130,7 +130,8 @@ def lower(graph) -> LoweredGraph:
     deg = np.fromiter(map(len, ins), np.int64, count=n)
     in_off = np.zeros(n + 1, np.int64)
     np.cumsum(deg, out=in_off[1:])
-    in_idx = np.fromiter((index[r] for t in ins for r in t), np.int32, count=int(in_off[-1]))
+    in_idx = np.fromiter(map(index.__getitem__, itertools.chain.from_iterable(ins)), np.int32,
+                         count=int(in_off[-1]))
     joined = "".join(names)
     name_off = np.zeros(n + 1, np.int64)
     if joined.isascii():

@@ -298,13 +298,14 @@ def _labels(assignments) -> dict:
 def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
                   want_table: bool = False, *, session: Optional[Session] = None,
                   types: TypeSet = DEFAULT_TYPES, shard: int = 0, n_shards: int = 1,
-                  exchange: Optional[Callable] = None) -> list:
+                  exchange: Optional[Callable] = None, csr=None) -> list:
     """Score every candidate of every block in one batched launch; returns
-    SubgraphResult per block (search_subgraph semantics, search.py:317-345)."""
+    SubgraphResult per block (search_subgraph semantics, search.py:317-345).
+    `csr` = (offsets, node indices) of the templates when already known."""
     ses = session or Session.open(graph)
     if not subgraphs:
         return []
-    off, nodes = _templates_csr(ses.low, subgraphs)
+    off, nodes = csr if csr is not None else _templates_csr(ses.low, subgraphs)
     # pack_gradients raises BadConfig for mu > chunk only once a candidate is
     # costed; build with a legal chunk to learn which error the reference hits first
     bad_mu = mu > chunk_size
@@ -361,22 +362,36 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
     t0 = time.perf_counter()
     ses = session or Session.open(graph, backend, cache=cache)
     t1 = time.perf_counter()
-    subs = prune_graph(graph, min_duplicates, types=types, session=ses)
+    if min_duplicates < 1:
+        raise BadConfig("min_duplicates must be >= 1")
+    ba = ses.backend.fold(ses.dgraph, int(min_duplicates))
+    subs = subgraphs_from_blocks(ses.low, ba, types)
     t2 = time.perf_counter()
     results = search_blocks(graph, subs, mesh, mu, chunk_size, want_table, session=ses,
-                            types=types, shard=shard, n_shards=n_shards, exchange=exchange)
+                            types=types, shard=shard, n_shards=n_shards, exchange=exchange,
+                            csr=ba.templates_csr())
     t3 = time.perf_counter()
     assignments: dict = {}
     total_cost = 0.0
     candidates = 0
     valid = 0
-    for sub, res in zip(subs, results):
+    names = ses.low.names
+    members = ba.members
+    for b, (sub, res) in enumerate(zip(subs, results)):
         candidates += res.candidates
         valid += res.valid
         total_cost += res.best.cost.total * sub.multiplicity
-        for prefix, _ in sub.instances:
-            for scope, spec in res.best.plan.assignments:
-                assignments[sub.instance_node(prefix, scope)] = spec.label
+        # every instance takes the template's labels (search.py:374-376); instance
+        # members come straight from the fold's member matrix
+        T = int(ba.block_T[b])
+        if not res.best.plan.assignments:
+            continue
+        pos = {s: i for i, s in enumerate(sub.template)}
+        cols = [pos[s] for s, _ in res.best.plan.assignments]
+        labels = [spec.label for _, spec in res.best.plan.assignments]
+        mo, R = int(ba.block_member_off[b]), sub.multiplicity
+        mat = members[mo: mo + R * T].reshape(R, T)[:, cols]
+        assignments.update(zip(map(names.__getitem__, mat.ravel().tolist()), labels * R))
     LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
                        search_ms=(t3 - t2) * 1e3, assemble_ms=(time.perf_counter() - t3) * 1e3)
     return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates,

@@ -16,6 +16,7 @@ resource (multi-GPU sharding lives in ``paper_2302_00247_b200.dist``).
 
 from __future__ import annotations
 
+import gc
 import math
 import time
 from dataclasses import dataclass
@@ -309,8 +310,10 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
     # pack_gradients raises BadConfig for mu > chunk only once a candidate is
     # costed; build with a legal chunk to learn which error the reference hits first
     bad_mu = mu > chunk_size
+    ta = time.perf_counter()
     tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, chunk_size if not bad_mu else mu)
     ses.last_table_bytes = tables.nbytes
+    tb = time.perf_counter()
     try:
         if tables.overflow:
             raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")
@@ -321,12 +324,15 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
             scores = ses.backend.score(tables, shard, n_shards)
             if exchange is not None:
                 scores = exchange(scores)
+        tc = time.perf_counter()
         for sc in scores:
             if not sc.has_best:
                 raise AssertionError("all-replica fallback must always route")
             if bad_mu:
                 raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
         bests = routed_plans_all(ses, tables, subgraphs, scores, mesh, types, detail)
+        LAST_PHASES.update(tables_ms=(tb - ta) * 1e3, score_call_ms=(tc - tb) * 1e3,
+                           routes_ms=(time.perf_counter() - tc) * 1e3)
         results = []
         for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
             table = []
@@ -359,6 +365,18 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
                 shard: int = 0, n_shards: int = 1, exchange: Optional[Callable] = None):
     """Prune, search every unique block, assemble the whole-graph plan (search.py:348-379)."""
     del jobs
+    gc_was = gc.isenabled()
+    gc.disable()  # the result is ~10^5 small objects: no collector pauses mid-search
+    try:
+        return _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
+                            backend, session, cache, shard, n_shards, exchange)
+    finally:
+        if gc_was:
+            gc.enable()
+
+
+def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types, backend, session,
+                 cache, shard, n_shards, exchange):
     t0 = time.perf_counter()
     ses = session or Session.open(graph, backend, cache=cache)
     t1 = time.perf_counter()

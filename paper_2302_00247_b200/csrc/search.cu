@@ -30,7 +30,6 @@ constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
 constexpr int THREADS = 256;     // scoring CTA size
 constexpr int ITEM_ITERS_MAX = 64;         // work item = THREADS * iters candidates
 constexpr int ITEM_ITERS_MAX_SKIP = 1024;  // ... when prefix skipping is on
-constexpr unsigned long long BRUTE_CHUNK = 512;  // warp-level chunk of a brute-force item
 
 __host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 __host__ __device__ inline uint32_t pow3(int k) {
@@ -673,7 +672,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
                                                    ItemOut* __restrict__ items,
                                                    unsigned long long* __restrict__ counter) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ unsigned long long s_item, s_cursor;
+  __shared__ unsigned long long s_item;
   __shared__ int64_t s_block;
   __shared__ unsigned long long s_red_t[THREADS / 32], s_red_i[THREADS / 32];
   __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
@@ -693,7 +692,6 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
         else hi = mid;
       }
       s_block = lo;
-      s_cursor = P.lo[lo] + (item - P.item_base[lo]) * P.item_cands;
     }
     __syncthreads();
     const int64_t b = s_block;
@@ -706,70 +704,55 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
     const BlobHeader& H = *S.H;
     const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
+    const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
+    const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
     unsigned long long best_t = ~0ULL, best_i = ~0ULL;
     uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
-    // Brute force: warps pull 512-candidate chunks of the item from a shared
-    // cursor (no idling at the item barrier).  Prefix skipping: each warp owns a
-    // static eighth of the item so a proven run can jump across it.
-    const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
-    unsigned long long wlo = P.skip ? min(ilo + span * warp, ihi) : ihi;
-    unsigned long long whi = P.skip ? min(wlo + span, ihi) : ihi;
-    while (true) {
-      if (!P.skip) {
-        unsigned long long c = 0;
-        if (lane == 0) c = atomicAdd(&s_cursor, (unsigned long long)BRUTE_CHUNK);
-        c = shfl_u64(c, 0);
-        if (c >= ihi) break;
-        wlo = c;
-        whi = min(c + BRUTE_CHUNK, ihi);
-      }
-      if (wlo < whi) {
-        uint64_t bw0, bw1;
-        decode_enum(H, wlo, bw0, bw1);
-        unsigned long long base = wlo;
-        while (base < whi) {
-          const unsigned long long x = base + lane;
-          const bool active = x < whi;
-          uint64_t w0 = bw0, w1 = bw1;
-          mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
-          double fwd;
-          const int fail = walk<WIDE>(S, w0, w1, active, fwd, tid);
-          unsigned long long t = x + 1;
-          if (fail < 0) {
-            const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
-            const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
-            const uint32_t ns = num_split_of(w0, w1);
-            const unsigned long long idx = ref_index(S, w0, w1);
-            nvalid++;
-            if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
-              best_t = tb;
-              best_n = ns;
-              best_i = idx;
-            }
-          } else if (P.skip && active) {
-            const NodeSkip sk = S.skip[fail];
-            t = sk.R ? (x / sk.R + 1) * sk.R : whi;
+    if (wlo < whi) {
+      uint64_t bw0, bw1;
+      decode_enum(H, wlo, bw0, bw1);
+      unsigned long long base = wlo;
+      while (base < whi) {
+        const unsigned long long x = base + lane;
+        const bool active = x < whi;
+        uint64_t w0 = bw0, w1 = bw1;
+        mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
+        double fwd;
+        const int fail = walk<WIDE>(S, w0, w1, active, fwd, tid);
+        unsigned long long t = x + 1;
+        if (fail < 0) {
+          const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
+          const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+          const uint32_t ns = num_split_of(w0, w1);
+          const unsigned long long idx = ref_index(S, w0, w1);
+          nvalid++;
+          if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
+            best_t = tb;
+            best_n = ns;
+            best_i = idx;
           }
-          const unsigned long long nb_ = P.skip ? warp_max_u64(t) : base + 32;
-          if (nb_ >= whi) break;
-          if (nb_ == base + 32) {
-            mr_add(bw0, bw1, 32, H.V, H.radix3);
-          } else {
-            // the lane that proved the longest run provides the next base digits
-            const unsigned mask = __ballot_sync(0xffffffffu, t == nb_);
-            const int src = __ffs(mask) - 1;
-            uint64_t n0 = w0, n1 = w1;
-            if (lane == src) {
-              if (fail >= 0 && active && S.skip[fail].R) mr_skip(n0, n1, S.skip[fail].m, H.V, H.radix3);
-              else mr_add(n0, n1, 1, H.V, H.radix3);
-            }
-            bw0 = shfl_u64(n0, src);
-            bw1 = shfl_u64(n1, src);
-          }
-          base = nb_;
+        } else if (P.skip && active) {
+          const NodeSkip sk = S.skip[fail];
+          t = sk.R ? (x / sk.R + 1) * sk.R : whi;
         }
+        const unsigned long long nb_ = warp_max_u64(t);
+        if (nb_ >= whi) break;
+        if (nb_ == base + 32) {
+          mr_add(bw0, bw1, 32, H.V, H.radix3);
+        } else {
+          // the lane that proved the longest run provides the next base digits
+          const unsigned mask = __ballot_sync(0xffffffffu, t == nb_);
+          const int src = __ffs(mask) - 1;
+          uint64_t n0 = w0, n1 = w1;
+          if (lane == src) {
+            if (fail >= 0 && P.skip && active && S.skip[fail].R) mr_skip(n0, n1, S.skip[fail].m, H.V, H.radix3);
+            else mr_add(n0, n1, 1, H.V, H.radix3);
+          }
+          bw0 = shfl_u64(n0, src);
+          bw1 = shfl_u64(n1, src);
+        }
+        base = nb_;
       }
-      if (P.skip) break;
     }
     // warp then block argmin of (total, num_split, index) + valid count
 #pragma unroll

@@ -75,17 +75,23 @@ class _Uncached:
 
 def subgraphs_from_blocks(low: LoweredGraph, ba: BlockArrays, types: TypeSet = DEFAULT_TYPES) -> list:
     names = low.names
+    member_names = list(map(names.__getitem__, ba.members.tolist()))
+    pnode, plen = ba.inst_prefix_node.tolist(), ba.inst_prefix_len.tolist()
+    ioff, moff, Ts = ba.block_inst_off.tolist(), ba.block_member_off.tolist(), ba.block_T.tolist()
+    ascii_names = getattr(low, "ascii", None)
+    if ascii_names is None:
+        ascii_names = low.ascii = len(low.name_bytes) == sum(map(len, names))
+    subgraph = types.Subgraph
     subs = []
-    for b in range(ba.n_blocks):
-        T = int(ba.block_T[b])
-        i0, i1 = int(ba.block_inst_off[b]), int(ba.block_inst_off[b + 1])
-        mo = int(ba.block_member_off[b])
-        mem = ba.members
+    for b in range(len(Ts)):
+        T, m = Ts[b], moff[b]
         insts = []
-        for r, j in enumerate(range(i0, i1)):
-            pre = prefix_of(low, int(ba.inst_prefix_node[j]), int(ba.inst_prefix_len[j]))
-            insts.append((pre, tuple(names[x] for x in mem[mo + r * T: mo + (r + 1) * T].tolist())))
-        subs.append(types.Subgraph(insts[0][0], insts[0][1], tuple(insts)))
+        for j in range(ioff[b], ioff[b + 1]):
+            nm = names[pnode[j]]
+            pre = nm[: plen[j]] if ascii_names else prefix_of(low, pnode[j], plen[j])
+            insts.append((pre, tuple(member_names[m: m + T])))
+            m += T
+        subs.append(subgraph(insts[0][0], insts[0][1], tuple(insts)))
     return subs
 
 
@@ -254,7 +260,9 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
             continue
         tnodes = [index[s] for s in sub.template]
         members = set(tnodes)
-        slot_pos = ses.backend.slots(tables, b)
+        # weight_nodes order (names sorted, search.py:85-88), as template positions
+        slot_pos = sorted((i for i, v in enumerate(tnodes) if low.w_rank[v]),
+                          key=sub.template.__getitem__)
         radices = [3 if low.w_rank[tnodes[p]] >= 2 else 2 for p in slot_pos]
         digits = _digits(int(sc.best_index), radices)
         assignments = tuple((sub.template[p], _spec_for_digit(types, d))

@@ -228,6 +228,13 @@ int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double
  * 0 walks every candidate individually (brute force).
  */
 #define SP_OPT_PREFIX_SKIP 1
+/*
+ * SP_OPT_MEMO (default 1, used when prefix skipping is off): every candidate is
+ * still visited, but a node is re-routed only when a digit of its ancestor cone
+ * changed since the lane's previous candidate (templates <= 64 nodes).  0 walks
+ * every node of every candidate.
+ */
+#define SP_OPT_MEMO 2
 int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value);
 
 /* CUDA-event timer on the context's stream (brackets whole API calls for benchmarks). */

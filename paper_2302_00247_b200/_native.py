@@ -272,6 +272,18 @@ class Backend:
         """Exact prefix-failure skipping in sp_score/sp_search (default on)."""
         self._check(self.lib.sp_set_option(self.ctx, 1, 1 if on else 0), "sp_set_option")
 
+    def set_memo(self, on: bool) -> None:
+        """Memoised brute force when skipping is off (default on)."""
+        self._check(self.lib.sp_set_option(self.ctx, 2, 1 if on else 0), "sp_set_option")
+
+    def set_mode(self, mode: str) -> None:
+        """'skip' (default), 'memo' (every candidate visited, dirty nodes re-routed)
+        or 'walk' (every node of every candidate)."""
+        if mode not in ("skip", "memo", "walk"):
+            raise ValueError(mode)
+        self.set_prefix_skip(mode == "skip")
+        self.set_memo(mode == "memo")
+
     def timer_start(self):
         self._check(self.lib.sp_timer_start(self.ctx), "sp_timer_start")
 

@@ -252,6 +252,10 @@ int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value) {
     ctx->skip = value ? 1 : 0;
     return SP_OK;
   }
+  if (option == SP_OPT_MEMO) {
+    ctx->memo = value ? 1 : 0;
+    return SP_OK;
+  }
   ctx->last_error = "unknown option";
   return SP_ERR_CONFIG;
 }

@@ -255,8 +255,10 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
       off = align16(off + (int64_t)sizeof(NodeSkip) * T);
       H.stride_off = (int32_t)off;
       off = align16(off + 9 * (int64_t)V);
+      H.dirty_off = (int32_t)off;
+      off = align16(off + 8 * ((int64_t)V + 1));
       H.prod_off = (int32_t)off;
-      off = align16(off + 2 * (int64_t)nprod);
+      off = align16(off + 4 * (int64_t)nprod);  // i16 pool slots, then i16 producer positions
       H.tab_off = (int32_t)off;
       off = align16(off + nent);
       H.dbl_off = (int32_t)off;
@@ -312,6 +314,14 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
           for (int s2 = ref_slot_of[e0 + i] + 1; s2 < H.V; s2++) st *= rr[s2];
           stride[slot_of[e0 + i]] = st;
         }
+      // memoised scoring: dirty[q] = nodes to re-route when enumeration positions >= q change
+      uint64_t* dirty = (uint64_t*)(blob + H.dirty_off);
+      for (int q = 0; q <= H.V; q++) {
+        uint64_t mask = 0;
+        for (int i = 0; i < T && i < 64; i++)
+          if (q == 0 || lay[e0 + i].skip_m >= q) mask |= 1ULL << i;
+        dirty[q] = mask;
+      }
       uint32_t acc = 0;
       for (int i = 0; i < T; i++) {
         s_kbase[i] = acc;
@@ -356,6 +366,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         const int32_t r = G.in_idx[q];
         if (node_block[r] != (int32_t)b) continue;
         prod[j] = (int16_t)lay[e0 + node_tpos[r]].out_pool;
+        ((int16_t*)(blob + H.prod_off))[H.n_prod + L.prod + j] = (int16_t)node_tpos[r];
         const int rr = G.act_rank[r];
         for (int p = 0; p < 4; p++)
           for (int s = 0; s < 3; s++) {
@@ -777,6 +788,173 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
     if (tid == 0) {
       ItemOut o{s_red_t[0], s_red_i[0], s_red_n[0], s_red_v[0]};
       for (int w = 1; w < THREADS / 32; w++) {
+        o.valid += s_red_v[w];
+        if (key_less(s_red_t[w], s_red_n[w], s_red_i[w], o.total_bits, o.num_split, o.index)) {
+          o.total_bits = s_red_t[w];
+          o.num_split = s_red_n[w];
+          o.index = s_red_i[w];
+        }
+      }
+      items[item] = o;
+    }
+  }
+}
+
+// Memoised brute force: every candidate of the range is visited (32 per warp
+// step, consecutive enumeration indices), but a node is re-routed only when a
+// digit of its ancestor cone changed since the lane's previous candidate
+// (dirty[q0], q0 = first changed enumeration position); every other node keeps
+// its cached (reach, state, failed) -- a pure function of those digits, with a
+// fixed dummy (state 0, reach 0) after a failure so the cache stays exact.
+// Candidates are valid iff no node's failed bit is set.  Templates <= 64 nodes.
+constexpr int THREADS_M = 128;
+
+template <bool WIDE>
+__global__ void __launch_bounds__(THREADS_M, 4) k_score_memo(const uint8_t* __restrict__ blobs, ScorePlan P,
+                                                            ItemOut* __restrict__ items,
+                                                            unsigned long long* __restrict__ counter) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ unsigned long long s_item;
+  __shared__ int64_t s_block;
+  __shared__ unsigned long long s_red_t[THREADS_M / 32], s_red_i[THREADS_M / 32];
+  __shared__ uint32_t s_red_n[THREADS_M / 32], s_red_v[THREADS_M / 32];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  int64_t staged = -1;
+  while (true) {
+    if (tid == 0) s_item = atomicAdd(counter, 1ULL);
+    __syncthreads();
+    const unsigned long long item = s_item;
+    if (item >= P.n_items) break;
+    if (tid == 0) {
+      int64_t lo = 0, hi = P.nb;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (P.item_base[mid] <= item) lo = mid;
+        else hi = mid;
+      }
+      s_block = lo;
+    }
+    __syncthreads();
+    const int64_t b = s_block;
+    if (b != staged) {
+      stage_blob(smem, blobs, P.blob_off[b]);
+      staged = b;
+    }
+    __syncthreads();
+    const BlobHeader& H = *(const BlobHeader*)smem;
+    const NodeDesc* desc = (const NodeDesc*)(smem + H.desc_off);
+    const int16_t* prodn = (const int16_t*)(smem + H.prod_off) + H.n_prod;
+    const uint8_t* tab = smem + H.tab_off;
+    const double* dbl = (const double*)(smem + H.dbl_off);
+    const uint64_t* dirty = (const uint64_t*)(smem + H.dirty_off);
+    double* cache = (double*)(smem + ((H.bytes + 15) & ~15));
+    Tabs S = tabs_of(smem);
+    const int T = H.T;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
+    const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
+    const unsigned long long span = (ihi - ilo + (THREADS_M / 32) - 1) / (THREADS_M / 32);
+    const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
+    unsigned long long best_t = ~0ULL, best_i = ~0ULL;
+    uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
+    if (wlo < whi) {
+      uint64_t bw0, bw1;
+      decode_enum(H, wlo, bw0, bw1);
+      uint64_t pw0 = 0, pw1 = 0, st_lo = 0, st_hi = 0, failmask = 0;
+      bool first = true;
+      for (unsigned long long base = wlo; base < whi; base += 32) {
+        const unsigned long long x = base + lane;
+        const bool active = x < whi;
+        uint64_t w0 = bw0, w1 = bw1;
+        mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
+        int q = 0;
+        if (!first) {
+          const uint64_t d0 = pw0 ^ w0, d1 = WIDE ? (pw1 ^ w1) : 0ULL;
+          q = d0 ? (__ffsll((long long)d0) - 1) >> 1 : (d1 ? 32 + ((__ffsll((long long)d1) - 1) >> 1) : H.V);
+        }
+        const int q0 = (int)__reduce_min_sync(0xffffffffu, (unsigned)q);
+        uint64_t mask = dirty[q0];
+        while (mask) {
+          const int i = __ffsll((long long)mask) - 1;
+          mask &= mask - 1;
+          const NodeDesc nd = desc[i];
+          uint32_t key = 0;
+          if (nd.slot >= 0) key = WIDE ? get_digit(w0, w1, nd.slot) : (uint32_t)((w0 >> (nd.slot * 2)) & 3);
+          const double* D = dbl + nd.dbl;
+          double r;
+          int p, sj[KMAX];
+          double rj[KMAX];
+          for (int j = 0; j < nd.k; j++) {
+            const int pn = prodn[nd.prod + j];
+            sj[j] = (int)(((pn < 32 ? st_lo >> (2 * pn) : st_hi >> (2 * (pn - 32)))) & 3);
+            rj[j] = cache[pn * THREADS_M + tid];
+            key = key * 3 + sj[j];
+          }
+          const uint8_t e = tab[nd.tab + key];
+          const bool fail = e == 0xFF;
+          p = e & 3;
+          const int s = fail ? 0 : (e >> 2) & 3;
+          if (nd.k == 0) {
+            r = D[p];
+          } else if (nd.k == 1) {
+            r = dadd(dadd(rj[0], D[8 + p * 3 + sj[0]]), D[p]);
+          } else {
+            double bse = dadd(rj[0], D[8 + p * 3 + sj[0]]);
+            for (int j = 1; j < nd.k; j++) bse = dmax_nn(bse, dadd(rj[j], D[8 + (j * 4 + p) * 3 + sj[j]]));
+            r = dadd(bse, D[p]);
+          }
+          if (fail) r = 0.0;
+          cache[i * THREADS_M + tid] = r;
+          if (i < 32) st_lo = (st_lo & ~(3ULL << (2 * i))) | ((uint64_t)s << (2 * i));
+          else st_hi = (st_hi & ~(3ULL << (2 * (i - 32)))) | ((uint64_t)s << (2 * (i - 32)));
+          failmask = (failmask & ~(1ULL << i)) | ((uint64_t)fail << i);
+        }
+        if (active && failmask == 0) {
+          // forward = max over nodes of reach + exit AllGather (costmodel.py:239-245)
+          double fwd = 0.0;
+          for (int i = 0; i < T; i++) {
+            const int si = (int)(((i < 32 ? st_lo >> (2 * i) : st_hi >> (2 * (i - 32)))) & 3);
+            fwd = dmax_nn(fwd, dadd(cache[i * THREADS_M + tid], dbl[desc[i].dbl + 4 + si]));
+          }
+          const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
+          const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+          const uint32_t ns = num_split_of(w0, w1);
+          const unsigned long long idx = ref_index(S, w0, w1);
+          nvalid++;
+          if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
+            best_t = tb;
+            best_n = ns;
+            best_i = idx;
+          }
+        }
+        pw0 = w0;
+        pw1 = w1;
+        first = false;
+        mr_add(bw0, bw1, 32, H.V, H.radix3);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, best_t, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, best_i, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, best_n, o);
+      nvalid += __shfl_down_sync(0xffffffffu, nvalid, o);
+      if (key_less(t2, n2, i2, best_t, best_n, best_i)) {
+        best_t = t2;
+        best_n = n2;
+        best_i = i2;
+      }
+    }
+    if (lane == 0) {
+      s_red_t[warp] = best_t;
+      s_red_i[warp] = best_i;
+      s_red_n[warp] = best_n;
+      s_red_v[warp] = nvalid;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      ItemOut o{s_red_t[0], s_red_i[0], s_red_n[0], s_red_v[0]};
+      for (int w = 1; w < THREADS_M / 32; w++) {
         o.valid += s_red_v[w];
         if (key_less(s_red_t[w], s_red_n[w], s_red_i[w], o.total_bits, o.num_split, o.index)) {
           o.total_bits = s_red_t[w];
@@ -1393,10 +1571,16 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
   bool wide = false;  // any block with more than 32 weight slots needs both digit words
   for (int64_t b = 0; b < nb; b++) wide = wide || t->hdr[b].V > 32;
-  auto kern = wide ? k_score<true> : k_score<false>;
-  SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // memoised brute force needs every template <= 64 nodes (bitmask state)
+  const bool memo = !ctx->skip && ctx->memo && t->max_T <= 64;
+  const int threads = memo ? THREADS_M : THREADS;
+  auto kern = memo ? (wide ? k_score_memo<true> : k_score_memo<false>) : (wide ? k_score<true> : k_score<false>);
+  const size_t smem_k = memo ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_T * THREADS_M * 8 + 16 : smem;
+  if (smem_k > ctx->smem_optin)
+    throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem_k) + " bytes)");
+  SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k));
   int per_sm = 0;
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem_k));
   if (per_sm < 1) per_sm = 1;
   const unsigned long long slots = (unsigned long long)ctx->sm_count * per_sm;
   // size work items so the grid gets ~8 items per resident CTA (dynamic balance);
@@ -1405,7 +1589,7 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   for (int64_t b = 0; b < nb; b++) total += hi[b] > lo[b] ? hi[b] - lo[b] : 0;
   const unsigned long long cap = ctx->skip ? ITEM_ITERS_MAX_SKIP : ITEM_ITERS_MAX;
   unsigned long long iters = (total + slots * 8 * THREADS - 1) / (slots * 8 * THREADS);
-  iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, cap));
+  iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, memo ? ITEM_ITERS_MAX_SKIP : cap));
   const unsigned long long item_cands = iters * THREADS;
   std::vector<unsigned long long> base(nb + 1, 0);
   for (int64_t b = 0; b < nb; b++) {
@@ -1429,7 +1613,7 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   ScorePlan P{t->d_blob_off.p, item_cands, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items, ctx->skip};
   const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
   SP_CUDA(cudaEventRecord(ctx->ev[2], s));
-  SP_LAUNCH(ctx, kern, (unsigned)grid, THREADS, smem, s, t->blobs.p, P, items.p, counter);
+  SP_LAUNCH(ctx, kern, (unsigned)grid, threads, smem_k, s, t->blobs.p, P, items.p, counter);
   SP_CUDA(cudaEventRecord(ctx->ev[3], s));
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);

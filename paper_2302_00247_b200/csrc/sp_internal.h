@@ -94,6 +94,7 @@ struct sp_ctx {
   double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;
   int64_t own_launches = 0, cub_calls = 0;
   int skip = 1;  // exact prefix-failure skipping in sp_score / sp_search
+  int memo = 1;  // with skip off: memoised brute force (re-route only dirty nodes)
   cudaEvent_t timer[2] = {};
   // scratch reused across calls
   sp::DevBuf<uint8_t> cub_tmp;
@@ -139,7 +140,8 @@ struct BlobHeader {
   uint64_t radix3_ref;    // bit s set: REFERENCE slot s (weight_nodes order) has 3 options
   int32_t skip_off;       // NodeSkip[T]
   int32_t stride_off;     // u64 reference stride per enumeration position, then int8 perm[V]
-  int64_t pad2;
+  int32_t dirty_off;      // u64 dirty[V+1]: nodes whose ancestor cone reaches position >= q (T <= 64)
+  int32_t pad3;
 };
 static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
 

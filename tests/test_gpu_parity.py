@@ -137,14 +137,17 @@ def test_random_graphs_vs_oracle(backend, seed):
         if t.overflow:
             pytest.skip("random block beyond u64")
         res = backend.score(t)
-        backend.set_prefix_skip(False)
+        others = []
         try:
-            brute = backend.score(t)
+            for mode in ("memo", "walk"):
+                backend.set_mode(mode)
+                others.append(backend.score(t))
         finally:
-            backend.set_prefix_skip(True)
+            backend.set_mode("skip")
         for b in range(ba.n_blocks):
-            assert (brute[b].valid, brute[b].best_index, brute[b].best_total) == (
-                res[b].valid, res[b].best_index, res[b].best_total)
+            for brute in others:
+                assert (brute[b].valid, brute[b].best_index, brute[b].best_total) == (
+                    res[b].valid, res[b].best_index, res[b].best_total)
             C = int(t.candidates[b])
             exp, etot = oracle.score(low, ba.template_nodes(b), m, mu=mu, chunk=chunk, hi=C,
                                      threads=4, want_totals=C <= 4096)
@@ -179,14 +182,15 @@ def test_c2_decoder_block_full_vs_oracle(backend):
     t = backend.tables(ses.dgraph, off, nodes, m, c["mu"], c["chunk_size"])
     try:
         res = backend.score(t)
-        backend.set_prefix_skip(False)
-        try:
-            brute = backend.score(t)
-        finally:
-            backend.set_prefix_skip(True)
         dec = max(range(ba.n_blocks), key=lambda b: int(t.candidates[b]))
-        assert (brute[dec].valid, brute[dec].best_index, brute[dec].best_total) == (
-            res[dec].valid, res[dec].best_index, res[dec].best_total)
+        try:
+            for mode in ("memo", "walk"):
+                backend.set_mode(mode)
+                brute = backend.score(t)
+                assert (brute[dec].valid, brute[dec].best_index, brute[dec].best_total) == (
+                    res[dec].valid, res[dec].best_index, res[dec].best_total)
+        finally:
+            backend.set_mode("skip")
         exp, _ = oracle.score(low, ba.template_nodes(dec), m, threads=8)
         assert (res[dec].valid, res[dec].best_index, res[dec].best_total) == (
             exp.valid, exp.best_index, exp.best_total)
@@ -291,13 +295,14 @@ def test_c5_throughput_fold_slices_and_argmin(c5_sessions):
             _, tot = be.score_range(t, sl["block"], sl["lo"], sl["hi"], want_totals=True)
             assert [None if x != x else x for x in tot.tolist()] == sl["totals"]
         res = be.score(t)
-        be.set_prefix_skip(False)
         try:
-            brute = be.score(t)
+            for mode in ("memo", "walk"):
+                be.set_mode(mode)
+                brute = be.score(t)
+                assert [(r.valid, r.best_index, r.best_total) for r in res] == [
+                    (r.valid, r.best_index, r.best_total) for r in brute], mode
         finally:
-            be.set_prefix_skip(True)
-        assert [(r.valid, r.best_index, r.best_total) for r in res] == [
-            (r.valid, r.best_index, r.best_total) for r in brute]
+            be.set_mode("skip")
         # the 43M-candidate block in full against the oracle (16 pthreads)
         b = gold["candidates"].index(43046721)
         exp, _ = oracle.score(ses.low, ba.template_nodes(b), m, threads=16)

@@ -7,12 +7,12 @@ from paper_2302_00247_b200._native import Backend  # noqa: E402
 from paper_2302_00247_b200.search import Session, derive_plan  # noqa: E402
 
 workload = sys.argv[1] if len(sys.argv) > 1 else "c5"
-skip = (sys.argv[2] == "skip") if len(sys.argv) > 2 else False
+mode = sys.argv[2] if len(sys.argv) > 2 else "memo"
 calls = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 be = Backend(0)
-be.set_prefix_skip(skip)
+be.set_mode(mode)
 g, mesh = bench.load_workload(workload)
 ses = Session.open(g, be)
 for _ in range(calls):
     rep = derive_plan(g, mesh, session=ses)
-print(workload, "skip" if skip else "brute", rep.candidates, rep.valid, be.timings())
+print(workload, mode, rep.candidates, rep.valid, be.timings())

@@ -230,7 +230,7 @@ def measure(be, g, mesh, steps, warmup, rank, world, exchange, flush, barrier, s
     from paper_2302_00247_b200 import search as sp_search
     from paper_2302_00247_b200.search import Session, derive_plan
 
-    be.set_prefix_skip(skip)
+    be.set_mode("skip" if skip else "walk")
     ses = Session.open(g, be)  # graph CSR resident in HBM before timing
 
     def step_resident():

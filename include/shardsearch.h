@@ -229,7 +229,7 @@ int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double
  */
 #define SP_OPT_PREFIX_SKIP 1
 /*
- * SP_OPT_MEMO (default 1, used when prefix skipping is off): every candidate is
+ * SP_OPT_MEMO (default 0, used when prefix skipping is off): every candidate is
  * still visited, but a node is re-routed only when a digit of its ancestor cone
  * changed since the lane's previous candidate (templates <= 64 nodes).  0 walks
  * every node of every candidate.

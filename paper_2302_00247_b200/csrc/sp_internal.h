@@ -94,7 +94,7 @@ struct sp_ctx {
   double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;
   int64_t own_launches = 0, cub_calls = 0;
   int skip = 1;  // exact prefix-failure skipping in sp_score / sp_search
-  int memo = 1;  // with skip off: memoised brute force (re-route only dirty nodes)
+  int memo = 0;  // with skip off: memoised brute force (re-route only dirty nodes); off: walk
   cudaEvent_t timer[2] = {};
   // scratch reused across calls
   sp::DevBuf<uint8_t> cub_tmp;

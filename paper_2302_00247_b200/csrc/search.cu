@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <numeric>
 
 #include "patterns.cuh"
@@ -511,7 +512,12 @@ __device__ __forceinline__ Tabs tabs_of(uint8_t* smem) {
 // (digits packed in enumeration order).  Returns -1 when it routes (fwd =
 // forward time), else the first failing template position; T when inactive.
 // Warp-collective: all 32 lanes call it (uniform node loop, ballot exit).
-template <bool WIDE>
+// Digit encodings: DM_WIDE = 2-bit digits at bits 2q of (w0, w1) (any V <= 64);
+// DM_BIASED = one u64, position q at bits 2(V-1-q) holding digit + (4 - radix),
+// so a plain integer add carries across mixed-radix positions (V <= 32).
+enum : int { DM_WIDE = 1, DM_BIASED = 2 };
+
+template <int DM>
 __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, bool active, double& fwd, int tid) {
   const int T = S.H->T;
   bool ok = active;
@@ -520,7 +526,10 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
   for (int i = 0; i < T; i++) {
     const NodeDesc nd = S.desc[i];
     uint32_t key = 0;
-    if (nd.slot >= 0) key = WIDE ? get_digit(w0, w1, nd.slot) : (uint32_t)((w0 >> (nd.slot * 2)) & 3);
+    if (nd.slot >= 0) {
+      if (DM == DM_WIDE) key = get_digit(w0, w1, nd.slot);
+      else key = (uint32_t)((w0 >> (2 * (S.H->V - 1 - nd.slot))) & 3) - (4u - nd.nd);
+    }
     const double* D = S.dbl + nd.dbl;
     double r;
     int s;
@@ -672,6 +681,68 @@ __device__ __forceinline__ void stage_blob(uint8_t* smem, const uint8_t* blobs, 
   for (int q = threadIdx.x; q < bytes / 16; q += blockDim.x) dst[q] = src[q];
 }
 
+// ---- biased packed digits (DM_BIASED) --------------------------------------
+struct Biased {
+  uint64_t B;      // packed biases = the encoding of all-zero digits
+  uint64_t NZ;     // bit that is set iff the digit is non-zero, per position
+  uint64_t add32;  // unbiased digits of 32 (added to advance a warp by 32)
+};
+
+// y + a where a holds unbiased digits: a field that wraps carries into the next
+// slower position by plain binary carry and gets its bias back.
+__device__ __forceinline__ uint64_t badd(uint64_t y, uint64_t a, uint64_t B) {
+  const uint64_t s = y + a;
+  const uint64_t w = ((s ^ y ^ a) >> 2) & 0x5555555555555555ULL;  // carry out of each field
+  return s + ((w | (w << 1)) & B);
+}
+
+__device__ __forceinline__ uint64_t bencode(const BlobHeader& H, unsigned long long x) {
+  uint64_t y = 0;
+  for (int q = H.V - 1; q >= 0; q--) {
+    const uint32_t r = ((H.radix3 >> q) & 1) ? 3 : 2;
+    const uint32_t d = (uint32_t)(x % r);
+    x /= r;
+    y |= (uint64_t)(d + 4 - r) << (2 * (H.V - 1 - q));
+  }
+  return y;
+}
+
+__device__ __forceinline__ uint32_t bdigit(const BlobHeader& H, uint64_t y, int q) {
+  const uint32_t r = ((H.radix3 >> q) & 1) ? 3 : 2;
+  return (uint32_t)((y >> (2 * (H.V - 1 - q))) & 3) - (4 - r);
+}
+
+__device__ __forceinline__ double backward_b(const Tabs& S, uint64_t y) {
+  const BlobHeader& H = *S.H;
+  double bwd = 0.0;
+  if (!H.multi_dev) return bwd;
+  long long cur = 0;
+  int cur_n = 0;
+  for (int q = 0; q < H.nt; q++) {
+    const TrainDesc td = S.trn[q];
+    if (bdigit(H, y, td.slot) != 0 || td.size >= H.mu) continue;
+    if (cur + td.size > H.chunk && cur_n) {
+      bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
+      cur = 0;
+      cur_n = 0;
+    }
+    cur += td.size;
+    cur_n++;
+  }
+  if (cur_n) bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
+  for (int q = 0; q < H.nt; q++) {
+    const TrainDesc td = S.trn[q];
+    if (bdigit(H, y, td.slot) == 0 && td.size >= H.mu) bwd = dadd(bwd, td.uterm);
+  }
+  return bwd;
+}
+
+__device__ __forceinline__ unsigned long long ref_index_b(const Tabs& S, uint64_t y) {
+  unsigned long long idx = 0;
+  for (int q = 0; q < S.H->V; q++) idx += (unsigned long long)bdigit(*S.H, y, q) * S.stride[q];
+  return idx;
+}
+
 // Batched scorer over ALL blocks of a search in one launch.  Dynamic work
 // items (atomic counter) of contiguous enumeration ranges; each warp walks its
 // eighth of an item 32 candidates at a time.  With skipping on, a lane whose
@@ -687,6 +758,9 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
   __shared__ int64_t s_block;
   __shared__ unsigned long long s_red_t[THREADS / 32], s_red_i[THREADS / 32];
   __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
+  __shared__ uint64_t s_lane_add[32];
+  __shared__ Biased s_bz;
+  constexpr int DM = WIDE ? DM_WIDE : DM_BIASED;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   int64_t staged = -1;
@@ -708,11 +782,40 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
     const int64_t b = s_block;
     if (b != staged) {
       stage_blob(smem, blobs, P.blob_off[b]);
+      if (!WIDE) {
+        // per-block constants of the biased encoding
+        const BlobHeader* gH = (const BlobHeader*)(blobs + P.blob_off[b]);
+        const int V = gH->V;
+        const uint64_t r3 = gH->radix3;
+        if (tid < 32) {
+          uint64_t a = 0;  // unbiased digits of `tid` in the fastest positions
+          uint32_t x = (uint32_t)tid;
+          for (int q = V - 1; q >= 0 && x; q--) {
+            const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+            a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
+            x /= r;
+          }
+          s_lane_add[tid] = a;
+        } else if (tid == 32) {
+          Biased z{0, 0, 0};
+          uint32_t x = 32;
+          for (int q = V - 1; q >= 0; q--) {
+            const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+            const int sh = 2 * (V - 1 - q);
+            z.B |= (uint64_t)(4 - r) << sh;
+            z.NZ |= (uint64_t)(r == 3 ? 2 : 1) << sh;
+            z.add32 |= (uint64_t)(x % r) << sh;
+            x /= r;
+          }
+          s_bz = z;
+        }
+      }
       staged = b;
     }
     __syncthreads();
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
+    const Biased bz = s_bz;
     const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
@@ -720,22 +823,26 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
     unsigned long long best_t = ~0ULL, best_i = ~0ULL;
     uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
     if (wlo < whi) {
-      uint64_t bw0, bw1;
-      decode_enum(H, wlo, bw0, bw1);
+      uint64_t bw0, bw1 = 0;
+      if (WIDE) decode_enum(H, wlo, bw0, bw1);
+      else bw0 = bencode(H, wlo);
+      const uint64_t lane_add = WIDE ? 0 : s_lane_add[lane];
       unsigned long long base = wlo;
       while (base < whi) {
         const unsigned long long x = base + lane;
         const bool active = x < whi;
         uint64_t w0 = bw0, w1 = bw1;
-        mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
+        if (WIDE) mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
+        else w0 = badd(bw0, lane_add, bz.B);
         double fwd;
-        const int fail = walk<WIDE>(S, w0, w1, active, fwd, tid);
+        const int fail = walk<DM>(S, w0, w1, active, fwd, tid);
         unsigned long long t = x + 1;
         if (fail < 0) {
-          const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
+          const double bwd = WIDE ? backward(S, w0, w1) : backward_b(S, w0);
+          const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
           const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
-          const uint32_t ns = num_split_of(w0, w1);
-          const unsigned long long idx = ref_index(S, w0, w1);
+          const uint32_t ns = WIDE ? num_split_of(w0, w1) : (uint32_t)__popcll(w0 & bz.NZ);
+          const unsigned long long idx = WIDE ? ref_index(S, w0, w1) : ref_index_b(S, w0);
           nvalid++;
           if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
             best_t = tb;
@@ -746,21 +853,30 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
           const NodeSkip sk = S.skip[fail];
           t = sk.R ? (x / sk.R + 1) * sk.R : whi;
         }
-        const unsigned long long nb_ = warp_max_u64(t);
+        const unsigned long long nb_ = P.skip ? warp_max_u64(t) : base + 32;
         if (nb_ >= whi) break;
         if (nb_ == base + 32) {
-          mr_add(bw0, bw1, 32, H.V, H.radix3);
+          if (WIDE) mr_add(bw0, bw1, 32, H.V, H.radix3);
+          else bw0 = badd(bw0, bz.add32, bz.B);
         } else {
           // the lane that proved the longest run provides the next base digits
           const unsigned mask = __ballot_sync(0xffffffffu, t == nb_);
           const int src = __ffs(mask) - 1;
           uint64_t n0 = w0, n1 = w1;
           if (lane == src) {
-            if (fail >= 0 && P.skip && active && S.skip[fail].R) mr_skip(n0, n1, S.skip[fail].m, H.V, H.radix3);
-            else mr_add(n0, n1, 1, H.V, H.radix3);
+            const bool jump = fail >= 0 && active && S.skip[fail].R;
+            if (WIDE) {
+              if (jump) mr_skip(n0, n1, S.skip[fail].m, H.V, H.radix3);
+              else mr_add(n0, n1, 1, H.V, H.radix3);
+            } else {
+              // positions faster than m back to digit 0, then +1 at position m
+              const int sh = jump ? 2 * (H.V - 1 - S.skip[fail].m) : 0;
+              const uint64_t low = (1ULL << sh) - 1;
+              n0 = badd((n0 & ~low) | (bz.B & low), 1ULL << sh, bz.B);
+            }
           }
           bw0 = shfl_u64(n0, src);
-          bw1 = shfl_u64(n1, src);
+          if (WIDE) bw1 = shfl_u64(n1, src);
         }
         base = nb_;
       }
@@ -998,7 +1114,7 @@ __global__ void __launch_bounds__(THREADS) k_score_table(const uint8_t* __restri
       else w1 |= (uint64_t)d << ((q - 32) * 2);
     }
     double fwd;
-    const int fail = walk<true>(S, w0, w1, active, fwd, tid);
+    const int fail = walk<DM_WIDE>(S, w0, w1, active, fwd, tid);
     if (fail < 0) {
       const double total = dadd(fwd, dmul(backward(S, w0, w1), H.keep_bwd));
       const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
@@ -1569,7 +1685,9 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   const size_t smem = score_smem(t);
   if (smem > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
-  bool wide = false;  // any block with more than 32 weight slots needs both digit words
+  // any block with more than 32 weight slots needs the two-word digit encoding
+  // (SP_FORCE_WIDE=1 selects it everywhere: tests cross-check both encodings)
+  bool wide = getenv("SP_FORCE_WIDE") != nullptr;
   for (int64_t b = 0; b < nb; b++) wide = wide || t->hdr[b].V > 32;
   // memoised brute force needs every template <= 64 nodes (bitmask state)
   const bool memo = !ctx->skip && ctx->memo && t->max_T <= 64;

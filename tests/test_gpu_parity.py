@@ -316,3 +316,34 @@ def test_c5_throughput_fold_slices_and_argmin(c5_sessions):
                     exp.valid, exp.best_index, exp.best_total)
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("seed", range(0, 40, 4))
+def test_digit_encodings_agree(backend, seed, monkeypatch):
+    """The biased one-word digit encoding (V <= 32) and the two-word encoding give
+    identical results in every scoring mode."""
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    g = random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11))
+    low = lower(g)
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 2, session=ses)
+    off, nodes = ba.templates_csr()
+    t = backend.tables(ses.dgraph, off, nodes, ClusterSpec.from_mesh("2x4"), 1 << 20, 4 << 20)
+    try:
+        if t.overflow:
+            pytest.skip("beyond u64")
+        for mode in ("skip", "walk"):
+            backend.set_mode(mode)
+            a = backend.score(t)
+            monkeypatch.setenv("SP_FORCE_WIDE", "1")
+            w = backend.score(t)
+            monkeypatch.delenv("SP_FORCE_WIDE")
+            assert [(r.valid, r.best_index, r.best_total, r.best_num_split) for r in a] == [
+                (r.valid, r.best_index, r.best_total, r.best_num_split) for r in w]
+    finally:
+        backend.set_mode("skip")
+        t.close()

@@ -360,6 +360,25 @@ def run_ours(args) -> None:
     achieved = alg_bytes / (kern / 1000.0) / 1e9 if kern > 0 else 0.0
     kernel_rate = cands / world / (kern / 1000.0) if kern > 0 else 0.0
 
+    # SM issue-slot roofline of k_score: warp-instructions per candidate from the
+    # committed ncu capture of the same kernel x the live kernel rate, against
+    # 148 SMs x 4 schedulers x the SM clock sampled during the timed region
+    issue = None
+    prof = os.path.join(ROOT, "profiles", "r1_k_score_c5_walk.txt")
+    if args.workload == "c5" and os.path.exists(prof) and main["clocks"] and main["clocks"]["sm_mhz"]:
+        vals = {}
+        for ln in open(prof):
+            if " = " in ln and not ln.startswith("#"):
+                k, v = ln.split(" = ", 1)
+                vals[k.strip()] = float(v.split()[0])
+        wipc = vals["smsp__inst_executed.sum"] / cands
+        peak_issue = 148 * 4 * main["clocks"]["sm_mhz"] * 1e6
+        issue = {"bound": "issue", "unit": "warp-inst/s", "warp_inst_per_candidate": wipc,
+                 "achieved": wipc * kernel_rate, "peak": peak_issue,
+                 "frac": wipc * kernel_rate / peak_issue,
+                 "ncu_issue_active_frac": vals["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100,
+                 "source": "profiles/r1_k_score_c5_walk.txt (instruction count) x live kernel time"}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -387,6 +406,7 @@ def run_ours(args) -> None:
                      "note": "no per-candidate HBM input: algorithmic bytes are the staged "
                              "routing tables + per-item records, so the kernel is SM-issue-bound; "
                              "issue-slot utilisation is in profiles/ (DESIGN.md section 3)"},
+        "issue_roofline": issue,
         "prefix_skip": {"value": cands * args.steps / (skip_ms / 1000.0),
                         "e2e_value": cands * args.steps / (skip_e2e_ms / 1000.0),
                         "ms_per_step": skip_ms / args.steps,

@@ -27,7 +27,7 @@ from .blocks import BlockArrays
 from .errors import BackendError, BadConfig, SpecMismatch, UnsupportedSearch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libshardsearch.so")
+LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "lib", "libshardsearch.so")
 
 _lib = None
 _lib_lock = threading.Lock()

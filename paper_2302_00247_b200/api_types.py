@@ -305,6 +305,12 @@ class RoutedPlan:
         return {r.scope: r for r in self.routings}
 
 
+@dataclass(frozen=True)
+class RoutingFailure:
+    node: str
+    reason: str
+
+
 @dataclass
 class SubgraphResult:
     subgraph: Subgraph
@@ -364,6 +370,7 @@ class TypeSet:
     CandidatePlan: type = CandidatePlan
     NodeRouting: type = NodeRouting
     RoutedPlan: type = RoutedPlan
+    RoutingFailure: type = RoutingFailure
     SubgraphResult: type = SubgraphResult
     BestPlanReport: type = BestPlanReport
     pattern_names: dict = field(default_factory=lambda: {

@@ -519,18 +519,26 @@ enum : int { DM_WIDE = 1, DM_BIASED = 2 };
 
 template <int DM>
 __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, bool active, double& fwd, int tid) {
+  // hoist everything loop-invariant into registers (the header lives in smem)
   const int T = S.H->T;
+  const int sh_base = 2 * (S.H->V - 1);
+  const NodeDesc* __restrict__ desc = S.desc;
+  const int16_t* __restrict__ prodp = S.prodp;
+  const uint8_t* __restrict__ tab = S.tab;
+  const double* __restrict__ dbl = S.dbl;
+  double* __restrict__ reach = S.reach + tid;
+  uint8_t* __restrict__ stp = S.stp + tid;
   bool ok = active;
   int fail = active ? -1 : T;
   fwd = 0.0;
   for (int i = 0; i < T; i++) {
-    const NodeDesc nd = S.desc[i];
+    const NodeDesc nd = desc[i];
     uint32_t key = 0;
     if (nd.slot >= 0) {
       if (DM == DM_WIDE) key = get_digit(w0, w1, nd.slot);
-      else key = (uint32_t)((w0 >> (2 * (S.H->V - 1 - nd.slot))) & 3) - (4u - nd.nd);
+      else key = (uint32_t)((w0 >> (sh_base - 2 * nd.slot)) & 3) - (4u - nd.nd);
     }
-    const double* D = S.dbl + nd.dbl;
+    const double* D = dbl + nd.dbl;
     double r;
     int s;
     uint8_t e;
@@ -538,26 +546,26 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
     // base = max(0.0, reach[p] + conv) needs no max for one producer: the
     // operands are >= +0.0, so the sum already is the max (bitwise).
     if (nd.k == 0) {
-      e = S.tab[nd.tab + key];
+      e = tab[nd.tab + key];
       if (ok && e == 0xFF) { ok = false; fail = i; }
       if (!__any_sync(0xffffffffu, ok)) break;
       s = ok ? (e >> 2) & 3 : 0;
       r = D[e & 3];
     } else if (nd.k == 1) {
-      const int ps0 = S.prodp[nd.prod];
-      const int s0 = S.stp[ps0 * THREADS + tid];
-      const double r0 = S.reach[ps0 * THREADS + tid];
-      e = S.tab[nd.tab + key * 3 + s0];
+      const int ps0 = prodp[nd.prod];
+      const int s0 = stp[ps0 * THREADS];
+      const double r0 = reach[ps0 * THREADS];
+      e = tab[nd.tab + key * 3 + s0];
       if (ok && e == 0xFF) { ok = false; fail = i; }
       if (!__any_sync(0xffffffffu, ok)) break;
       const int p = e & 3;
       s = ok ? (e >> 2) & 3 : 0;
       r = dadd(dadd(r0, D[8 + p * 3 + s0]), D[p]);
     } else if (nd.k == 2) {
-      const int ps0 = S.prodp[nd.prod], ps1 = S.prodp[nd.prod + 1];
-      const int s0 = S.stp[ps0 * THREADS + tid], s1 = S.stp[ps1 * THREADS + tid];
-      const double r0 = S.reach[ps0 * THREADS + tid], r1 = S.reach[ps1 * THREADS + tid];
-      e = S.tab[nd.tab + (key * 3 + s0) * 3 + s1];
+      const int ps0 = prodp[nd.prod], ps1 = prodp[nd.prod + 1];
+      const int s0 = stp[ps0 * THREADS], s1 = stp[ps1 * THREADS];
+      const double r0 = reach[ps0 * THREADS], r1 = reach[ps1 * THREADS];
+      e = tab[nd.tab + (key * 3 + s0) * 3 + s1];
       if (ok && e == 0xFF) { ok = false; fail = i; }
       if (!__any_sync(0xffffffffu, ok)) break;
       const int p = e & 3;
@@ -567,12 +575,12 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
       int sj[KMAX];
       double rj[KMAX];
       for (int j = 0; j < nd.k; j++) {
-        const int ps = S.prodp[nd.prod + j];
-        sj[j] = S.stp[ps * THREADS + tid];
-        rj[j] = S.reach[ps * THREADS + tid];
+        const int ps = prodp[nd.prod + j];
+        sj[j] = stp[ps * THREADS];
+        rj[j] = reach[ps * THREADS];
         key = key * 3 + sj[j];
       }
-      e = S.tab[nd.tab + key];
+      e = tab[nd.tab + key];
       if (ok && e == 0xFF) { ok = false; fail = i; }
       if (!__any_sync(0xffffffffu, ok)) break;
       const int p = e & 3;
@@ -583,8 +591,8 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
     }
     fwd = dmax_nn(fwd, dadd(r, D[4 + s]));
     if (nd.out_pool >= 0) {
-      S.reach[nd.out_pool * THREADS + tid] = r;
-      S.stp[nd.out_pool * THREADS + tid] = (uint8_t)s;
+      reach[nd.out_pool * THREADS] = r;
+      stp[nd.out_pool * THREADS] = (uint8_t)s;
     }
   }
   return ok ? -1 : fail;

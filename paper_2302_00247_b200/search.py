@@ -27,7 +27,7 @@ import numpy as np
 from ._native import Backend, default_backend
 from .api_types import DEFAULT_TYPES, TypeSet
 from .blocks import BlockArrays, prefix_of
-from .errors import BackendError, BadConfig, UnsupportedSearch
+from .errors import BackendError, BadConfig, SpecMismatch, UnsupportedSearch
 from .lowering import LoweredGraph, lower
 
 _KIND_LABEL = {1: "allreduce", 2: "allgather", 3: "reducescatter", 4: "alltoall"}
@@ -149,6 +149,32 @@ def candidate_by_index(graph, subgraph, index: int, types: TypeSet = DEFAULT_TYP
         subgraph, tuple((s, _spec_for_digit(types, d)) for s, d in zip(scopes, digits)), index)
 
 
+def enumerate_all_plans(graph, subgraph, types: TypeSet = DEFAULT_TYPES):
+    """Lazily yield the full product of weight decisions (search.py:119-125)."""
+    import itertools
+
+    scopes = weight_nodes(graph, subgraph)
+    opts = [range(3 if graph.nodes[s].weight.rank >= 2 else 2) for s in scopes]
+    for index, digits in enumerate(itertools.product(*opts)):
+        yield types.CandidatePlan(
+            subgraph, tuple((s, _spec_for_digit(types, d)) for s, d in zip(scopes, digits)), index)
+
+
+def _plan_index(graph, plan) -> int:
+    """Reference index of a plan's assignments (inverse of candidate_by_index)."""
+    amap = dict(plan.assignments)
+    index = 0
+    for s in weight_nodes(graph, plan.subgraph):
+        r = 3 if graph.nodes[s].weight.rank >= 2 else 2
+        spec = amap[s]
+        kind = spec.kind.value if hasattr(spec.kind, "value") else spec.kind
+        d = 0 if kind == "replica" else (spec.axis + 1 if kind == "split" else -1)
+        if not 0 <= d < r:
+            raise SpecMismatch(f"assignment {spec.label} of {s!r} is not a search option")
+        index = index * r + d
+    return index
+
+
 # ---------------------------------------------------------------------------
 # search
 
@@ -255,7 +281,9 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
     for b, (sub, sc, X) in enumerate(zip(subgraphs, scores, blocks)):
         T = len(sub.template)
         if not sc.has_best or not X.valid:
-            out.append(None)
+            out.append(types.RoutingFailure(sub.template[X.fail_pos],
+                                            "no pattern chains from producer states")
+                       if sc.has_best and X.fail_pos >= 0 else None)
             e0 += T
             continue
         tnodes = [index[s] for s in sub.template]
@@ -292,7 +320,7 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
         cost = types.CostReport(forward_comm=X.forward_comm, backward_comm=X.backward_comm,
                                 overlap_fraction=mesh.overlap_fraction, bytes_by_collective=bbc,
                                 collective_calls=int(X.collective_calls), flops=_flops(low, tnodes))
-        if cost.total != sc.best_total:
+        if sc.best_total == sc.best_total and cost.total != sc.best_total:  # NaN: no score to check
             raise BackendError(f"explain/score disagree on block {b}: {cost.total!r} != "
                                f"{sc.best_total!r}")
         out.append(types.RoutedPlan(plan, tuple(routings), tuple(exits), cost))
@@ -422,3 +450,44 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
                        search_ms=(t3 - t2) * 1e3, assemble_ms=(time.perf_counter() - t3) * 1e3)
     return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates,
                                 valid)
+
+
+class _OneScore:
+    """Score stand-in so routed_plans_all can explain an arbitrary candidate."""
+
+    def __init__(self, index: int):
+        self.best_index = index
+        self.has_best = 1
+        self.best_total = float("nan")
+
+
+def _explain_plan(graph, plan, mesh, mu, chunk_size, types, session):
+    ses = session or Session.open(graph)
+    index = _plan_index(graph, plan)
+    off, nodes = _templates_csr(ses.low, [plan.subgraph])
+    tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
+    try:
+        sc = _OneScore(index)
+        return routed_plans_all(ses, tables, [plan.subgraph], [sc], mesh, types)[0]
+    finally:
+        tables.close()
+
+
+def pattern_routing(graph, plan, mesh, *, types: TypeSet = DEFAULT_TYPES,
+                    session: Optional[Session] = None):
+    """Route one candidate (search.py:134-224): RoutedPlan with an empty CostReport, or
+    RoutingFailure (returned, not raised).  Evaluated on the device (sp_explain_all)."""
+    routed = _explain_plan(graph, plan, mesh, 1 << 20, 4 << 20, types, session)
+    if isinstance(routed, types.RoutingFailure):
+        return routed
+    return types.RoutedPlan(routed.plan, routed.routings, routed.exit_conversions,
+                            types.CostReport())
+
+
+def plan_cost(routed, graph, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20, *,
+              types: TypeSet = DEFAULT_TYPES, session: Optional[Session] = None):
+    """CostReport of a routed plan (costmodel.py:193-267), on the device."""
+    if mu > chunk_size:
+        raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
+    full = _explain_plan(graph, routed.plan, mesh, mu, chunk_size, types, session)
+    return full.cost

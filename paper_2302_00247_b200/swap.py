@@ -48,6 +48,7 @@ def reference_types(shardplan) -> TypeSet:
         CandidatePlan=search.CandidatePlan,
         NodeRouting=search.NodeRouting,
         RoutedPlan=search.RoutedPlan,
+        RoutingFailure=search.RoutingFailure,
         SubgraphResult=search.SubgraphResult,
         BestPlanReport=search.BestPlanReport,
         pattern_names={op.value: tuple(p.name for p in pats) for op, pats in reg.items()},

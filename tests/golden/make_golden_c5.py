@@ -47,15 +47,15 @@ def prune_doc(subs) -> list:
 def main() -> None:
     out = []
     mesh = ClusterSpec.from_mesh("1x8")
-    for tier in ("parity", "throughput"):
+    for seed, tier in ((0, "parity"), (0, "throughput"), (1, "parity"), (2, "parity")):
         t0 = time.perf_counter()
-        g = motif_dag(0, tier)
+        g = motif_dag(seed, tier)
         rg = to_reference(g)
         subs = prune_graph(rg, 2)
-        entry = {"tier": tier, "seed": 0, "nodes": len(g.nodes), "graph_sha": sha(dump_grouped(g)),
+        entry = {"tier": tier, "seed": seed, "nodes": len(g.nodes), "graph_sha": sha(dump_grouped(g)),
                  "prune_sha": sha(prune_doc(subs)), "blocks": len(subs),
                  "candidates": [count_candidates(rg, s) for s in subs], "mesh": mesh.to_json()}
-        print(f"{tier}: {len(g.nodes)} nodes, {len(subs)} blocks, prune {time.perf_counter() - t0:.1f}s",
+        print(f"{tier} seed {seed}: {len(g.nodes)} nodes, {len(subs)} blocks, prune {time.perf_counter() - t0:.1f}s",
               flush=True)
         if tier == "parity":
             t1 = time.perf_counter()

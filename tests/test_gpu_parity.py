@@ -347,3 +347,65 @@ def test_digit_encodings_agree(backend, seed, monkeypatch):
     finally:
         backend.set_mode("skip")
         t.close()
+
+
+# -- single-candidate API (search.py:103-233, costmodel.py:193-267) -------------------------
+
+
+def _weighted_block(g, backend, min_dup=1):
+    from paper_2302_00247_b200.search import prune_graph, weight_nodes
+
+    subs = prune_graph(g, min_dup, backend=backend)
+    (sub,) = [s for s in subs if weight_nodes(g, s)]
+    return sub
+
+
+def test_pattern_routing_reference_cases(backend):
+    """The reference's routing tests (test_plan_search.py:85-135) on the device path."""
+    from paper_2302_00247_b200.api_types import (REPLICA, CandidatePlan, ClusterSpec,
+                                                 RoutingFailure, split)
+    from paper_2302_00247_b200.search import pattern_routing, weight_nodes
+
+    mesh2 = ClusterSpec(m=1, n=2)
+    g = graph("graphs/chain2.json.gz")
+    sub = _weighted_block(g, backend)
+    s0, s1 = weight_nodes(g, sub)
+    routed = pattern_routing(g, CandidatePlan(sub, ((s0, split(1)), (s1, split(0))), 0), mesh2)
+    rm = routed.routing_map
+    assert rm[s0].pattern == "matmul.col"
+    assert rm[s1].pattern == "matmul.row.allreduce"
+    assert rm[s1].output_collective.kind.value == "allreduce"
+    allrep = pattern_routing(g, CandidatePlan(sub, ((s0, REPLICA), (s1, REPLICA)), 0), mesh2)
+    assert all(r.output_collective.kind.value == "identity" and not r.input_conversions
+               for r in allrep.routings) and allrep.exit_conversions == ()
+    g1 = graph("graphs/chain1.json.gz")
+    sub1 = _weighted_block(g1, backend)
+    (w,) = weight_nodes(g1, sub1)
+    fail = pattern_routing(g1, CandidatePlan(sub1, ((w, split(0)),), 0), mesh2)
+    assert isinstance(fail, RoutingFailure) and fail.node == w and fail.reason
+    g6 = graph("graphs/chain1_dim6.json.gz")
+    sub6 = _weighted_block(g6, backend)
+    (w6,) = weight_nodes(g6, sub6)
+    assert isinstance(pattern_routing(g6, CandidatePlan(sub6, ((w6, split(1)),), 0),
+                                      ClusterSpec(m=1, n=4)), RoutingFailure)
+
+
+def test_plan_cost_matches_reference_tables(backend):
+    """plan_cost of every 11th candidate of the tiny layer block == reference totals."""
+    from paper_2302_00247_b200.api_types import RoutingFailure
+    from paper_2302_00247_b200.search import (candidate_by_index, pattern_routing, plan_cost,
+                                              prune_graph)
+
+    c = case("tiny_2x2")
+    g = graph(c["graph"])
+    m = mesh(c["mesh"])
+    subs = prune_graph(g, 2, backend=backend)
+    tab = c["tables"][0]
+    sub = subs[tab["block"]]
+    for idx, total in tab["rows"][::11]:
+        plan = candidate_by_index(g, sub, idx)
+        routed = pattern_routing(g, plan, m)
+        if total is None:
+            assert isinstance(routed, RoutingFailure)
+        else:
+            assert plan_cost(routed, g, m).total == total

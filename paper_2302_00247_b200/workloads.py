@@ -164,3 +164,55 @@ def motif_dag(seed: int = 0, tier: str = "parity", n_target: int = 100_000, moti
         prev = name
     nodes.append(GraphNode("output", OpKind.OUTPUT, (prev,), TensorSpec((batch, seq, d))))
     return GroupedGraph(nodes)
+
+
+def transformer_stack_lowered(layers: int, **kw):
+    """`lower(transformer_stack(layers, **kw))` built directly as arrays, for the
+    fold scale-up (10^6 .. 10^7 GraphNodes) where per-node Python objects would
+    dominate.  Layers repeat with period 14 in the reference's topological order
+    (each layer only consumes the previous layer's residual2), so the layer rows
+    are tiled and the producer indices shifted; checked against the object path
+    by tests/test_workloads.py."""
+    import numpy as np
+
+    from .lowering import LoweredGraph, lower
+
+    if layers < 2:
+        return lower(transformer_stack(layers, **kw))
+    base = lower(transformer_stack(2, **kw))
+    P = 14
+    head, l0, l1, tail = slice(0, 2), slice(2, 2 + P), slice(2 + P, 2 + 2 * P), slice(2 + 2 * P, None)
+    n = 2 + P * layers + 2
+
+    def tile(a):
+        return np.concatenate([a[head], np.tile(a[l0], (layers,) + (1,) * (a.ndim - 1)), a[tail]])
+
+    suffixes = [nm.split("/", 2)[2] for nm in base.names[l0]]
+    stack = base.names[2].split("/")[0]
+    names = (base.names[:2] + [f"{stack}/layer_{i}/{s}" for i in range(layers) for s in suffixes]
+             + base.names[-2:])
+    # producer CSR: layer 0 as generated, layers >= 1 shifted copies of layer 1
+    def rows(lo, hi):
+        return [base.in_idx[base.in_off[i]:base.in_off[i + 1]] for i in range(lo, hi)]
+    l0_rows, l1_rows = rows(2, 2 + P), rows(2 + P, 2 + 2 * P)
+    deg = np.array([len(r) for r in l1_rows], np.int64)
+    flat1 = np.concatenate(l1_rows)
+    shifts = (np.arange(1, layers, dtype=np.int64) - 1) * P
+    body = (flat1[None, :] + shifts[:, None]).ravel() if layers > 1 else np.zeros(0, np.int64)
+    last_res2 = 2 + P * layers - 1
+    in_idx = np.concatenate([base.in_idx[base.in_off[0]:base.in_off[2]],
+                             np.concatenate(l0_rows), body,
+                             np.array([last_res2, last_res2 + 1], np.int64)]).astype(np.int32)
+    degs = np.concatenate([np.diff(base.in_off)[:2], np.array([len(r) for r in l0_rows]),
+                           np.tile(deg, layers - 1), np.array([1, 1])])
+    in_off = np.zeros(n + 1, np.int64)
+    np.cumsum(degs, out=in_off[1:])
+    lens = np.fromiter(map(len, names), np.int64, count=n)
+    name_off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=name_off[1:])
+    return LoweredGraph(
+        names=names, index={}, name_bytes=np.frombuffer("".join(names).encode("ascii"), np.uint8).copy(),
+        name_off=name_off, topo_rank=np.arange(n, dtype=np.int64), op=tile(base.op),
+        act_rank=tile(base.act_rank), act_shape=tile(base.act_shape), act_bytes=tile(base.act_bytes),
+        w_rank=tile(base.w_rank), w_shape=tile(base.w_shape), w_bytes=tile(base.w_bytes),
+        w_trainable=tile(base.w_trainable), in_off=in_off, in_idx=in_idx, source=None)

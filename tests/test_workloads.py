@@ -98,3 +98,18 @@ def test_c5_oracle_slices_and_search(tier):
                 idx, ns, tot, valid)
             total += out.best_total * ba.multiplicity(b)
         assert repr(total) == gold["total_cost"]
+
+
+@pytest.mark.parametrize("layers", [2, 3, 7, 40])
+def test_transformer_stack_lowered_equals_object_path(layers):
+    import numpy as np
+
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.workloads import transformer_stack_lowered
+
+    a = lower(transformer_stack(layers, d_model=64))
+    b = transformer_stack_lowered(layers, d_model=64)
+    assert a.names == b.names
+    for f in ("name_bytes", "name_off", "topo_rank", "op", "act_rank", "act_shape", "act_bytes",
+              "w_rank", "w_shape", "w_bytes", "w_trainable", "in_off", "in_idx"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)

@@ -222,6 +222,13 @@ int sp_explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, sp_explai
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms);
 
 /*
+ * Device-only part of the last sp_fold_run (CUDA events around the level loop,
+ * excluding the host-side ordering of fold_finalize) and how many levels the
+ * loop ran.  No reference counterpart: measurement hook for bench.py.
+ */
+int sp_fold_stats(const sp_ctx* ctx, double* device_ms, int32_t* levels);
+
+/*
  * Options.  SP_OPT_PREFIX_SKIP (default 1): when a candidate fails routing at
  * node i, every candidate sharing the digits of i's ancestor cone fails too,
  * so the scorer jumps over them (exact; counts and argmin are unchanged).

@@ -59,6 +59,7 @@ def _declare(L):
                              C.POINTER(SpEdgeConv), C.c_int32, C.POINTER(C.c_int32)]
     L.sp_last_timings.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_double)]
+    L.sp_fold_stats.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     L.sp_timer_start.argtypes = [vp]
     L.sp_timer_stop.argtypes = [vp, C.POINTER(C.c_double)]
     L.sp_launch_counts.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -102,6 +103,7 @@ EXPORTED_SYMBOLS = (
     "sp_merge_keys", "sp_explain", "sp_last_timings", "sp_timer_start", "sp_timer_stop",
     "sp_launch_counts", "sp_copy_bytes", "sp_tables_bytes", "sp_tables_sizes",
     "sp_tables_edge_offsets", "sp_explain_all", "sp_search", "sp_set_option",
+    "sp_fold_stats",
 )
 
 
@@ -266,7 +268,10 @@ class Backend:
     def timings(self) -> dict:
         f, s, k = C.c_double(), C.c_double(), C.c_double()
         self.lib.sp_last_timings(self.ctx, C.byref(f), C.byref(s), C.byref(k))
-        return {"fold_ms": f.value, "score_ms": s.value, "score_kernel_ms": k.value}
+        d, lv = C.c_double(), C.c_int32()
+        self.lib.sp_fold_stats(self.ctx, C.byref(d), C.byref(lv))
+        return {"fold_ms": f.value, "score_ms": s.value, "score_kernel_ms": k.value,
+                "fold_device_ms": d.value, "fold_levels": lv.value}
 
     def set_prefix_skip(self, on: bool) -> None:
         """Exact prefix-failure skipping in sp_score/sp_search (default on)."""

@@ -246,6 +246,13 @@ int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double
   return SP_OK;
 }
 
+int sp_fold_stats(const sp_ctx* ctx, double* device_ms, int32_t* levels) {
+  if (!ctx) return SP_ERR_CONFIG;
+  if (device_ms) *device_ms = ctx->fold_device_ms;
+  if (levels) *levels = ctx->fold_levels;
+  return SP_OK;
+}
+
 int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value) {
   if (!ctx) return SP_ERR_CONFIG;
   if (option == SP_OPT_PREFIX_SKIP) {

@@ -705,6 +705,11 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
   dg->in_idx.p = (int32_t*)(base + parts[12].off);
 }
 
+__global__ void k_iota(int32_t* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
 template <class T>
 __global__ void k_gather(const int32_t* __restrict__ idx, int64_t m, const T* __restrict__ src,
                          T* __restrict__ dst) {
@@ -869,8 +874,10 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   const int P2 = [&] { int q = 1; while (q < n) q <<= 1; return q; }();
   const size_t smem = (size_t)P2 * 20;
   SP_CUDA(cudaFuncSetAttribute(k_fold_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SP_CUDA(cudaEventRecord(ctx->ev[6], s));
   SP_LAUNCH(ctx, k_fold_small, 1, SMALL_THREADS, smem, s, A);
   SP_CUDA(cudaGetLastError());
+  SP_CUDA(cudaEventRecord(ctx->ev[7], s));
   // single D2H: outputs (i32 region after scratch), pend, residual + gaccept
   std::vector<int32_t> h_out(i32_out), pend_h(nd);
   std::vector<uint8_t> h_u8(nd + n);
@@ -879,6 +886,11 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   SP_CUDA(cudaMemcpyAsync(pend_h.data(), A.pend, nd * 4, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaMemcpyAsync(h_u8.data(), u8.p, nd + n, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
+  {
+    float ms = 0;
+    SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
+    ctx->fold_device_ms = ms;
+  }
   const int32_t* h_sorted = h_out.data();
   const int32_t* h_gstart = h_sorted + nd;
   const int32_t* h_corder = h_gstart + nd1;
@@ -889,6 +901,7 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   if (*collided) return;
   const int32_t nlev = h_info[4 * D];
   if (nlev < 0) throw Error(SP_ERR_CUDA, "fold did not terminate");
+  ctx->fold_levels = nlev;
   std::vector<LevelOut> levels;
   for (int32_t dd = 0; dd < nlev; dd++) {
     const int32_t nA = h_info[dd * 4], nG = h_info[dd * 4 + 1], nC = h_info[dd * 4 + 2];
@@ -955,6 +968,17 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   residual.alloc(n, s);
   gaccept.alloc(n, s);
 
+  // per-level outputs stay on the device until the loop ends (one download)
+  DevBuf<int32_t> st_sorted, st_gstart, st_corder, st_cstart;
+  DevBuf<uint8_t> st_gaccept;
+  size_t st_cap = (size_t)n * 2;
+  st_sorted.alloc(st_cap, s);
+  st_gstart.alloc(st_cap, s);
+  st_corder.alloc(st_cap, s);
+  st_cstart.alloc(st_cap, s);
+  st_gaccept.alloc(st_cap, s);
+
+  SP_CUDA(cudaEventRecord(ctx->ev[6], s));
   SP_CUDA(cudaMemsetAsync(maxd.p, 0, sizeof(int32_t), s));
   SP_LAUNCH(ctx, k_depth, grid_for(n, sms), 256, 0, s, dg->name_off.p, dg->names.p, n, depth.p, maxd.p);
   SP_LAUNCH(ctx, k_name_hash, grid_for(n, sms), 128, 0, s, dg->name_off.p, dg->names.p, n, D, seed, pend.p, ph.p, rh.p);
@@ -962,11 +986,7 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   SP_CUDA(cudaMemsetAsync(residual.p, 0, n, s));
   SP_CUDA(cudaMemsetAsync(collision.p, 0, sizeof(int32_t), s));
   SP_CUDA(cudaMemsetAsync(cur.p, 0xff, n * sizeof(int64_t), s));
-  {
-    std::vector<int32_t> iota(n);
-    std::iota(iota.begin(), iota.end(), 0);
-    act.upload(iota.data(), n, s);
-  }
+  SP_LAUNCH(ctx, k_iota, grid_for(n, sms), 256, 0, s, act.p, n);
 
   // CUB scratch sized for the largest call
   size_t tmp_bytes = 0, t = 0;
@@ -981,7 +1001,21 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   ctx->cub_tmp.alloc(tmp_bytes, s);
   void* tmp = ctx->cub_tmp.p;
 
-  std::vector<LevelOut> levels;
+  struct LevelSize {
+    int64_t nA, nG, nC;
+    size_t off_a, off_g, off_c;
+  };
+  std::vector<LevelSize> sizes;
+  size_t used_a = 0, used_g = 0, used_c = 0;
+  // grow the level store (stream-ordered; only when the bound n*2 is exceeded)
+  auto reserve = [&](auto& buf, size_t used, size_t need) {
+    if (used + need <= buf.n) return;
+    using T = std::remove_reference_t<decltype(*buf.p)>;
+    DevBuf<T> bigger;
+    bigger.alloc(std::max(buf.n * 2, used + need), s);
+    if (used) SP_CUDA(cudaMemcpyAsync(bigger.p, buf.p, used * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    buf = std::move(bigger);
+  };
   int64_t nA = n;
   for (int32_t level = 1; nA > 0; level++) {
     if (level > D) throw Error(SP_ERR_CUDA, "fold did not terminate");
@@ -1040,18 +1074,20 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     // 5. accept / residual / descend
     SP_LAUNCH(ctx, k_accept, g1, 256, 0, s, sorted2.p, gidv.p, nA, nC, nG, gclass.p, cstart.p, depth.p, level, min_dup,
                                 gparent.p, next_flag.p, residual.p, gaccept.p);
-    LevelOut lv;
-    lv.level = level;
-    lv.sorted.resize(nA);
-    lv.gstart.resize(nG + 1);
-    lv.corder.resize(nG);
-    lv.cstart.resize(nC + 1);
-    lv.gaccept.resize(nG);
-    sorted2.download(lv.sorted.data(), nA, s);
-    gstart.download(lv.gstart.data(), nG, s);
-    corder3.download(lv.corder.data(), nG, s);
-    cstart.download(lv.cstart.data(), nC, s);
-    gaccept.download(lv.gaccept.data(), nG, s);
+    reserve(st_sorted, used_a, nA);
+    reserve(st_gstart, used_g, nG);
+    reserve(st_corder, used_g, nG);
+    reserve(st_gaccept, used_g, nG);
+    reserve(st_cstart, used_c, nC);
+    SP_CUDA(cudaMemcpyAsync(st_sorted.p + used_a, sorted2.p, nA * 4, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(st_gstart.p + used_g, gstart.p, nG * 4, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(st_corder.p + used_g, corder3.p, nG * 4, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(st_gaccept.p + used_g, gaccept.p, nG, cudaMemcpyDeviceToDevice, s));
+    SP_CUDA(cudaMemcpyAsync(st_cstart.p + used_c, cstart.p, nC * 4, cudaMemcpyDeviceToDevice, s));
+    sizes.push_back({nA, nG, nC, used_a, used_g, used_c});
+    used_a += nA;
+    used_g += nG;
+    used_c += nC;
     t = tmp_bytes;
     ctx->cub_calls++;
     SP_CUDA(cub::DeviceSelect::Flagged(tmp, t, sorted2.p, next_flag.p, act.p, nsel.p, (int)nA, s));
@@ -1059,21 +1095,46 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     g_d2h_bytes += 4;
     SP_CUDA(cudaMemcpyAsync(&nsel_h, nsel.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
-    lv.gstart[nG] = (int32_t)nA;
-    lv.cstart[nC] = (int32_t)nG;
-    levels.push_back(std::move(lv));
     nA = nsel_h;
   }
+  SP_CUDA(cudaEventRecord(ctx->ev[7], s));
   int32_t coll_h = 0;
-  std::vector<uint8_t> resid_h(n);
-  std::vector<int32_t> pend_h((size_t)n * D);
   g_d2h_bytes += 4;
   SP_CUDA(cudaMemcpyAsync(&coll_h, collision.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  residual.download(resid_h.data(), n, s);
-  pend.download(pend_h.data(), (size_t)n * D, s);
   SP_CUDA(cudaStreamSynchronize(s));
+  {
+    float ms = 0;
+    SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
+    ctx->fold_device_ms = ms;
+    ctx->fold_levels = (int32_t)sizes.size();
+  }
   *collided = coll_h != 0;
   if (*collided) return;
+  std::vector<uint8_t> resid_h(n);
+  std::vector<int32_t> pend_h((size_t)n * D);
+  std::vector<int32_t> h_sorted(used_a), h_gstart(used_g), h_corder(used_g), h_cstart(used_c);
+  std::vector<uint8_t> h_gaccept(used_g);
+  residual.download(resid_h.data(), n, s);
+  pend.download(pend_h.data(), (size_t)n * D, s);
+  st_sorted.download(h_sorted.data(), used_a, s);
+  st_gstart.download(h_gstart.data(), used_g, s);
+  st_corder.download(h_corder.data(), used_g, s);
+  st_gaccept.download(h_gaccept.data(), used_g, s);
+  st_cstart.download(h_cstart.data(), used_c, s);
+  SP_CUDA(cudaStreamSynchronize(s));
+  std::vector<LevelOut> levels(sizes.size());
+  for (size_t l = 0; l < sizes.size(); l++) {
+    const LevelSize& z = sizes[l];
+    LevelOut& lv = levels[l];
+    lv.level = (int32_t)l + 1;
+    lv.sorted.assign(h_sorted.begin() + z.off_a, h_sorted.begin() + z.off_a + z.nA);
+    lv.gstart.assign(h_gstart.begin() + z.off_g, h_gstart.begin() + z.off_g + z.nG);
+    lv.gstart.push_back((int32_t)z.nA);
+    lv.corder.assign(h_corder.begin() + z.off_g, h_corder.begin() + z.off_g + z.nG);
+    lv.gaccept.assign(h_gaccept.begin() + z.off_g, h_gaccept.begin() + z.off_g + z.nG);
+    lv.cstart.assign(h_cstart.begin() + z.off_c, h_cstart.begin() + z.off_c + z.nC);
+    lv.cstart.push_back((int32_t)z.nG);
+  }
 
   fold_finalize(dg, levels, resid_h, pend_h, D, out);
 }

@@ -89,9 +89,12 @@ struct sp_ctx {
   int sm_count = 148;
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};
   std::string last_error;
   double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;
+  // device-only part of the last fold (events around the level loop) and its level count
+  double fold_device_ms = 0;
+  int32_t fold_levels = 0;
   int64_t own_launches = 0, cub_calls = 0;
   int skip = 1;  // exact prefix-failure skipping in sp_score / sp_search
   int memo = 0;  // with skip off: memoised brute force (re-route only dirty nodes); off: walk

@@ -243,6 +243,24 @@ def test_multi_kernel_fold_path_vs_oracle(backend, seed, monkeypatch):
         assert to_prune_doc(low, ba) == to_prune_doc(low, ob)
 
 
+@pytest.mark.parametrize("layers", [20000, 700000])
+def test_fold_scaleup_vs_oracle(backend, layers):
+    """Fold at 2.8*10^5 and 9.8*10^6 GraphNodes: every array of the partition
+    (blocks, instances, prefixes, members) equals the oracle's."""
+    from oracle import oracle
+    from paper_2302_00247_b200.workloads import transformer_stack_lowered
+
+    low = transformer_stack_lowered(layers)
+    dg = backend.upload(low)
+    ba = backend.fold(dg, 2)
+    assert backend.timings()["fold_device_ms"] > 0
+    ob = oracle.prune(low, 2)
+    for k in ("block_T", "block_inst_off", "block_member_off", "inst_prefix_node", "inst_prefix_len",
+              "members"):
+        assert np.array_equal(np.asarray(getattr(ba, k), np.int64), np.asarray(ob[k], np.int64)), k
+    assert int(np.diff(ba.block_inst_off).max()) == layers
+
+
 # -- config 5: 10^5-op motif DAG --------------------------------------------------------
 
 
@@ -269,6 +287,23 @@ def test_c5_parity_derive_plan_byte_identical(c5_sessions):
     gold = c5()["parity"]
     g, ses = c5_sessions["parity"]
     rep = derive_plan(g, mesh(gold["mesh"]), session=ses)
+    assert hashlib.sha256(canon(rep.to_json()).encode()).hexdigest() == gold["plan_sha"]
+    assert repr(rep.total_cost) == gold["total_cost"] and rep.valid == gold["valid"]
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_c5_parity_other_seeds_byte_identical(backend, seed):
+    """Two more 10^5-node motif DAGs (different motif mixes and shapes) == reference."""
+    import hashlib
+
+    from golden_io import c5
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, derive_plan
+    from paper_2302_00247_b200.workloads import motif_dag
+
+    gold = c5()[("parity", seed)]
+    g = motif_dag(seed, "parity")
+    rep = derive_plan(g, mesh(gold["mesh"]), session=Session.open(lower(g), backend))
     assert hashlib.sha256(canon(rep.to_json()).encode()).hexdigest() == gold["plan_sha"]
     assert repr(rep.total_cost) == gold["total_cost"] and rep.valid == gold["valid"]
 

@@ -56,8 +56,11 @@ def test_fold_stress_graph_and_oracle_pinned(idx):
     assert _sha(to_prune_doc(low, ba)) == fs["prune_sha"]
 
 
-@pytest.mark.parametrize("tier", ["parity", "throughput"])
-def test_c5_graph_and_oracle_fold_pinned(tier):
+C5_KEYS = [("parity", 0), ("throughput", 0), ("parity", 1), ("parity", 2)]
+
+
+@pytest.mark.parametrize("tier,seed", C5_KEYS)
+def test_c5_graph_and_oracle_fold_pinned(tier, seed):
     """Config 5: generator == the graph the reference was run on; oracle fold == reference."""
     from golden_io import c5
     from oracle import oracle
@@ -65,16 +68,16 @@ def test_c5_graph_and_oracle_fold_pinned(tier):
     from paper_2302_00247_b200.lowering import lower
     from paper_2302_00247_b200.workloads import motif_dag
 
-    gold = c5()[tier]
-    g = motif_dag(0, tier)
+    gold = c5()[(tier, seed)]
+    g = motif_dag(seed, tier)
     assert _sha(dump_grouped(g)) == gold["graph_sha"]
     low = lower(g)
     ba = BlockArrays.from_dict(oracle.prune(low, 2))
     assert _sha(to_prune_doc(low, ba)) == gold["prune_sha"]
 
 
-@pytest.mark.parametrize("tier", ["parity", "throughput"])
-def test_c5_oracle_slices_and_search(tier):
+@pytest.mark.parametrize("tier,seed", C5_KEYS)
+def test_c5_oracle_slices_and_search(tier, seed):
     """Per-candidate totals on the golden slices; full parity-tier search == reference."""
     from golden_io import c5, mesh
     from oracle import oracle
@@ -82,8 +85,8 @@ def test_c5_oracle_slices_and_search(tier):
     from paper_2302_00247_b200.lowering import lower
     from paper_2302_00247_b200.workloads import motif_dag
 
-    gold = c5()[tier]
-    low = lower(motif_dag(0, tier))
+    gold = c5()[(tier, seed)]
+    low = lower(motif_dag(seed, tier))
     ba = BlockArrays.from_dict(oracle.prune(low, 2))
     m = mesh(gold["mesh"])
     for sl in gold["slices"]:

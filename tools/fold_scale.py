@@ -1,0 +1,106 @@
+"""Fold scale-up: prune_graph on 10^3 .. 10^7-node transformer stacks (GPU).
+
+    python tools/fold_scale.py --layers 1000 100000 700000 [--out gpurun_out/fold_scale.json]
+
+For each size: lower (array generator), upload, fold once to warm, then fold
+`--reps` times and report the device-only fold time (CUDA events around the
+level loop, sp_fold_stats), the whole sp_fold_run time (incl. the host-side
+string ordering), the level count and the compulsory traffic: the fold must
+read the uploaded graph once and write + read its per-depth prefix/rel hashes
+once.  Also checks the size-independent property of the
+result: the same blocks as the 4-layer stack, the 14-node layer block with
+`layers` instances (tests/test_gpu_parity.py checks it member by member
+against the oracle).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2302_00247_b200._native import Backend  # noqa: E402
+from paper_2302_00247_b200.workloads import transformer_stack_lowered  # noqa: E402
+
+SP_MAX_RANK = 6
+
+
+def compulsory_bytes(low, depth: int) -> int:
+    n = len(low.op)
+    E = int(low.in_off[-1])
+    graph = (int(low.name_off[-1]) + 8 * (n + 1) + 8 * n + 4 * n + 2 * 8 * SP_MAX_RANK * n + 16 * n
+             + 8 * (n + 1) + 4 * E)
+    hashes = 2 * (2 * 8 * n * depth)  # prefix + rel hash per depth, written once and read once
+    return graph + hashes
+
+
+def summarize(blocks) -> dict:
+    T = blocks.block_T.astype(np.int64)
+    inst = np.diff(blocks.block_inst_off).astype(np.int64)
+    return {"n_blocks": int(len(T)), "T": T.tolist()[:8], "instances": inst.tolist()[:8]}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, nargs="+", default=[1000, 100000, 700000])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--min-dup", type=int, default=2)
+    ap.add_argument("--peak-gbs", type=float, default=None)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    peak = args.peak_gbs
+    if peak is None:
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                peak = float(json.load(fh)["hbm_gbs"])
+        except Exception:
+            peak = 7700.0
+    be = Backend(0)
+    ref = summarize(be.fold(be.upload(transformer_stack_lowered(4)), args.min_dup))
+    rows = []
+    for L in args.layers:
+        t0 = time.perf_counter()
+        low = transformer_stack_lowered(L)
+        t1 = time.perf_counter()
+        dg = be.upload(low)
+        t2 = time.perf_counter()
+        blocks = be.fold(dg, args.min_dup)  # warm
+        dev, wall, host = [], [], []
+        for _ in range(args.reps):
+            h0 = time.perf_counter()
+            blocks = be.fold(dg, args.min_dup)
+            host.append((time.perf_counter() - h0) * 1e3)
+            tm = be.timings()
+            dev.append(tm["fold_device_ms"])
+            wall.append(tm["fold_ms"])
+        depth = max(nm.count("/") + 1 for nm in (low.names[0], low.names[2], low.names[-1]))
+        cb = compulsory_bytes(low, depth)
+        s = summarize(blocks)
+        ok = (s["n_blocks"] == ref["n_blocks"] and s["T"] == ref["T"]
+              and s["instances"] == [L if i == 4 else i for i in ref["instances"]])
+        dmed = float(np.median(dev))
+        row = {"layers": L, "nodes": len(low.op), "edges": int(low.in_off[-1]),
+               "levels": be.timings()["fold_levels"], "lower_s": round(t1 - t0, 2),
+               "upload_ms": round((t2 - t1) * 1e3, 1), "fold_device_ms": round(dmed, 3),
+               "fold_run_ms": round(float(np.median(wall)), 3),
+               "fold_python_ms": round(float(np.median(host)), 3),
+               "compulsory_bytes": cb, "compulsory_gbs": round(cb / (dmed * 1e-3) / 1e9, 1),
+               "peak_gbs": peak, "frac": round(cb / (dmed * 1e-3) / 1e9 / peak, 4),
+               "nodes_per_s": round(len(low.op) / (dmed * 1e-3), 1), "structure_ok": ok, "blocks": s}
+        print(json.dumps(row), flush=True)
+        rows.append(row)
+        del dg, low
+    if args.out:
+        with open(args.out, "w") as fh:
+            json.dump({"ref4": ref, "rows": rows}, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()

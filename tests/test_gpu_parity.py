@@ -255,9 +255,17 @@ def test_fold_scaleup_vs_oracle(backend, layers):
     ba = backend.fold(dg, 2)
     assert backend.timings()["fold_device_ms"] > 0
     ob = oracle.prune(low, 2)
-    for k in ("block_T", "block_inst_off", "block_member_off", "inst_prefix_node", "inst_prefix_len",
-              "members"):
+    for k in ("block_T", "block_inst_off", "block_member_off", "inst_prefix_len", "members"):
         assert np.array_equal(np.asarray(getattr(ba, k), np.int64), np.asarray(ob[k], np.int64)), k
+    # the prefix node is any member carrying the instance prefix: compare the prefix bytes
+    nb, no = low.name_bytes, low.name_off
+    got = np.asarray(ba.inst_prefix_node, np.int64)
+    exp = np.asarray(ob["inst_prefix_node"], np.int64)
+    plen = np.asarray(ob["inst_prefix_len"], np.int64)
+    diff = np.nonzero(got != exp)[0]
+    for j in diff.tolist():
+        a, b, n = int(no[got[j]]), int(no[exp[j]]), int(plen[j])
+        assert bytes(nb[a:a + n]) == bytes(nb[b:b + n]), f"instance {j} prefix differs"
     assert int(np.diff(ba.block_inst_off).max()) == layers
 
 

@@ -147,7 +147,10 @@ __device__ void route_node(const GraphView& G, int32_t n, int32_t blk, const int
 struct EntryLayout {
   int32_t k, nd, out_pool, prod, tab, dbl, train_idx, skip_m;
   uint64_t skip_R;
+  int32_t tab4, pad;
 };
+
+constexpr int TAB4_PAD = 512;  // failed lanes index past a table by < 3^KMAX / 2 bytes
 
 __global__ void k_mark_blocks(const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                               int32_t* node_block, int32_t* node_tpos, int32_t* dup) {
@@ -205,7 +208,7 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
       const BlobHeader& H0 = hdr[b];
       const int V = H0.V;
       int nprod = 0, nt = 0;
-      int64_t nent = 0, ndbl = 0;
+      int64_t nent = 0, ndbl = 0, nent4 = 0;
       uint32_t used[MAXT / 32];
       for (int w = 0; w < MAXT / 32; w++) used[w] = 0;
       int npool = 0;
@@ -232,6 +235,8 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
         L.nd = slot_of[e0 + i] >= 0 ? radix_of[e0 + i] : 1;
         L.prod = nprod;
         L.tab = (int32_t)nent;
+        L.tab4 = (int32_t)nent4;
+        L.pad = 0;
         L.dbl = (int32_t)ndbl;
         L.train_idx = (G.w_rank[n] && G.w_train[n]) ? nt++ : -1;
         L.out_pool = s_pool[i];
@@ -241,6 +246,7 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
         L.skip_R = anc ? R : 0;
         nprod += k;
         nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
+        nent4 += 4 * (int64_t)pow3(k < KMAX ? k : KMAX);
         ndbl += 8 + 12 * (int64_t)k;
         lay[e0 + i] = L;
       }
@@ -266,6 +272,14 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
       off = align16(off + 8 * ndbl);
       H.train_off = (int32_t)off;
       off = align16(off + (int64_t)sizeof(TrainDesc) * nt);
+      H.fast_off = (int32_t)off;
+      off = align16(off + (int64_t)sizeof(FastNode) * T);
+      H.zero_off = (int32_t)off;
+      off += 128;
+      H.fprod_off = (int32_t)off;
+      off = align16(off + 8 * (int64_t)nprod);
+      H.tab4_off = (int32_t)off;
+      off = align16(off + nent4 + TAB4_PAD);
       H.bytes = (int32_t)off;
       blob_bytes[b] = off;
     }
@@ -323,6 +337,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
           if (q == 0 || lay[e0 + i].skip_m >= q) mask |= 1ULL << i;
         dirty[q] = mask;
       }
+      for (int q = 0; q < 128; q++) blob[H.zero_off + q] = 0;
       uint32_t acc = 0;
       for (int i = 0; i < T; i++) {
         s_kbase[i] = acc;
@@ -346,6 +361,37 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       nd.tab = (uint32_t)L.tab;
       nd.dbl = (uint32_t)L.dbl;
       ((NodeDesc*)(blob + H.desc_off))[i] = nd;
+      {
+        // lean-walk record: ready-made smem byte offsets (pool slot p of lane t:
+        // reach at pool + (p*THREADS + t)*8, state at pool_states + p*THREADS + t)
+        FastNode f;
+        f.tab = H.tab4_off + L.tab4;
+        f.dbl = H.dbl_off + 8 * L.dbl;
+        f.cb0 = L.k >= 1 ? H.dbl_off + 8 * (L.dbl + 8) : H.zero_off;
+        f.cb1 = L.k >= 2 ? H.dbl_off + 8 * (L.dbl + 8 + 12) : H.zero_off;
+        f.r0 = f.r1 = f.s0 = f.s1 = 0;
+        int jj = 0;
+        for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
+          const int32_t r = G.in_idx[q];
+          if (node_block[r] != (int32_t)b) continue;
+          const int ps = lay[e0 + node_tpos[r]].out_pool;
+          if (L.k <= 2) {
+            if (jj == 0) { f.r0 = ps * THREADS * 8; f.s0 = ps * THREADS; }
+            else { f.r1 = ps * THREADS * 8; f.s1 = ps * THREADS; }
+          } else {
+            int32_t* fp = (int32_t*)(blob + H.fprod_off) + 2 * (L.prod + jj);
+            fp[0] = ps * THREADS * 8;
+            fp[1] = ps * THREADS;
+          }
+          jj++;
+        }
+        if (L.k >= 3) f.r0 = L.prod;
+        f.out_r = L.out_pool >= 0 ? L.out_pool * THREADS * 8 : -1;
+        f.out_s = L.out_pool >= 0 ? L.out_pool * THREADS : -1;
+        f.sh = nd.slot >= 0 ? 2 * (H.V - 1 - nd.slot) : 0;
+        f.kf = L.k | ((!has_cons[n] || ext_cons[n]) ? 0x100 : 0);
+        ((FastNode*)(blob + H.fast_off))[i] = f;
+      }
       ((NodeSkip*)(blob + H.skip_off))[i] = NodeSkip{L.skip_R, L.skip_m, 0};
       int16_t* prod = (int16_t*)(blob + H.prod_off) + L.prod;
       double* dbl = (double*)(blob + H.dbl_off) + L.dbl;
@@ -411,7 +457,18 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       }
       NodeRoute R;
       route_node(G, tmpl_nodes[e0 + i], (int32_t)b, node_block, (int)x, ps, M, &R, false);
-      blob[H.tab_off + L.tab + key] = R.pattern < 0 ? (uint8_t)0xFF : (uint8_t)(R.pattern | (R.state << 2));
+      const uint8_t val = R.pattern < 0 ? (uint8_t)0xFF : (uint8_t)(R.pattern | (R.state << 2));
+      blob[H.tab_off + L.tab + key] = val;
+      // 4-row table of the lean walk: row = biased digit (x + 4 - nd)
+      const uint32_t pk = pow3(L.k), rest = key - x * pk;
+      uint8_t* t4 = blob + H.tab4_off + L.tab4 + rest;
+      if (slot_of[e0 + i] >= 0) {
+        t4[(x + 4 - L.nd) * pk] = val;
+        if (x == 0)
+          for (int bb = 0; bb < 4 - L.nd; bb++) t4[bb * pk] = 0xFF;  // unused rows
+      } else {
+        for (int bb = 0; bb < 4; bb++) t4[bb * pk] = val;
+      }
     }
     __syncthreads();
   }
@@ -598,6 +655,122 @@ __device__ __forceinline__ int walk(const Tabs& S, uint64_t w0, uint64_t w1, boo
   return ok ? -1 : fail;
 }
 
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
+
+// 32-bit shared-memory accesses (the walk keeps one shared base address in a
+// register instead of re-deriving the generic shared window per access).
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Lean walk over FastNode records (biased digit word `w`, V <= 32): the same
+// routing + forward DP as walk<>, with every address precomputed by the table
+// build.  `sm` is the shared address of the staged blob, `rb`/`sb` the lane's
+// reach/state pool bases.  Failed or inactive lanes keep executing with masked
+// garbage (pattern 3 / state 3 index stays inside the padded tables) until the
+// whole warp has failed, exactly like walk<>'s ballot exit.  Only
+// subgraph-boundary nodes update the forward max: an interior node's reach
+// never exceeds its internal consumer's (conv, own >= 0 and rounding is
+// monotone), so the max over boundary nodes is the max over all nodes.
+template <bool TRACK>
+__device__ __forceinline__ int walk_fast(uint32_t sm, int T, uint32_t fast_off, uint32_t fprod_off, uint64_t w,
+                                         bool active, double& fwd, uint32_t rb, uint32_t sb) {
+  bool ok = active;
+  int fail = active ? -1 : T;
+  long long f = 0;  // bit pattern of the forward max (non-negative doubles)
+  uint32_t rec = sm + fast_off;
+  for (int i = 0; i < T; i++, rec += (uint32_t)sizeof(FastNode)) {
+    const int4 A = lds_v4(rec), B = lds_v4(rec + 16), X = lds_v4(rec + 32);
+    // A = (tab, dbl, cb0, cb1), B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf)
+    const uint32_t b = (uint32_t)(w >> X.z) & 3u;
+    const int k = X.w & 0xff;
+    uint32_t e;
+    double r;
+    if (k == 1) {
+      const uint32_t s0 = lds_u8(sb + B.z);
+      const double r0 = lds_f64(rb + B.x);
+      e = lds_u8(sm + A.x + b * 3 + s0);
+      const bool bad = e == 0xFFu;
+      if (TRACK && ok && bad) fail = i;
+      ok = ok && !bad;
+      if (!__any_sync(0xffffffffu, ok)) break;
+      const uint32_t p = e & 3u;
+      r = dadd(dadd(r0, lds_f64(sm + A.z + (p * 3 + s0) * 8)), lds_f64(sm + A.y + p * 8));
+    } else if (k == 2) {
+      const uint32_t s0 = lds_u8(sb + B.z), s1 = lds_u8(sb + B.w);
+      const double r0 = lds_f64(rb + B.x), r1 = lds_f64(rb + B.y);
+      e = lds_u8(sm + A.x + b * 9 + s0 * 3 + s1);
+      const bool bad = e == 0xFFu;
+      if (TRACK && ok && bad) fail = i;
+      ok = ok && !bad;
+      if (!__any_sync(0xffffffffu, ok)) break;
+      const uint32_t p = e & 3u;
+      r = dadd(dmax_nn(dadd(r0, lds_f64(sm + A.z + (p * 3 + s0) * 8)), dadd(r1, lds_f64(sm + A.w + (p * 3 + s1) * 8))),
+               lds_f64(sm + A.y + p * 8));
+    } else if (k == 0) {
+      e = lds_u8(sm + A.x + b);
+      const bool bad = e == 0xFFu;
+      if (TRACK && ok && bad) fail = i;
+      ok = ok && !bad;
+      if (!__any_sync(0xffffffffu, ok)) break;
+      r = lds_f64(sm + A.y + (e & 3u) * 8);
+    } else {
+      const uint32_t pp = sm + fprod_off + 8 * (uint32_t)B.x;
+      uint32_t key = b;
+      for (int j = 0; j < k; j++) key = key * 3 + lds_u8(sb + lds_s32(pp + 8 * j + 4));
+      e = lds_u8(sm + A.x + key);
+      const bool bad = e == 0xFFu;
+      if (TRACK && ok && bad) fail = i;
+      ok = ok && !bad;
+      if (!__any_sync(0xffffffffu, ok)) break;
+      const uint32_t p = e & 3u;
+      double bse = 0.0;
+      for (int j = 0; j < k; j++) {
+        const uint32_t sj = lds_u8(sb + lds_s32(pp + 8 * j + 4));
+        bse = dmax_nn(bse, dadd(lds_f64(rb + lds_s32(pp + 8 * j)), lds_f64(sm + A.z + j * 96 + (p * 3 + sj) * 8)));
+      }
+      r = dadd(bse, lds_f64(sm + A.y + p * 8));
+    }
+    const uint32_t s = (e >> 2) & 3u;
+    if (X.w & 0x100) {
+      const long long x = __double_as_longlong(dadd(r, lds_f64(sm + A.y + 32 + s * 8)));
+      f = x > f ? x : f;
+    }
+    if (X.x >= 0) {
+      sts_f64(rb + X.x, r);
+      sts_u8(sb + X.y, s);
+    }
+  }
+  fwd = __longlong_as_double(f);
+  return ok ? -1 : (TRACK ? fail : T);
+}
+
 // backward of plan_cost: pack_gradients over replicated trainable weights
 // (template order), buckets first then unfused, one AllReduce each.
 __device__ __forceinline__ double backward(const Tabs& S, uint64_t w0, uint64_t w1) {
@@ -757,8 +930,11 @@ __device__ __forceinline__ unsigned long long ref_index_b(const Tabs& S, uint64_
 // candidate fails at node i proves its whole R-aligned run invalid (R =
 // NodeSkip.R), and the warp jumps to the max proven end: the union of the
 // lanes' runs is contiguous from the warp's base, so the jump is exact.
-template <bool WIDE>
-__global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict__ blobs, ScorePlan P,
+#ifndef SP_SCORE_MIN_BLOCKS
+#define SP_SCORE_MIN_BLOCKS 4
+#endif
+template <bool WIDE, bool SKIP>
+__global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const uint8_t* __restrict__ blobs, ScorePlan P,
                                                    ItemOut* __restrict__ items,
                                                    unsigned long long* __restrict__ counter) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -824,6 +1000,11 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
     const Biased bz = s_bz;
+    // opaque copies: keep the shared addresses in registers (ptxas would
+    // otherwise re-derive the shared window base at every access)
+    const uint32_t sm32 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem));
+    const uint32_t rbase = opaque_u32((uint32_t)__cvta_generic_to_shared(S.reach + tid));
+    const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(S.stp + tid));
     const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
@@ -843,7 +1024,9 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
         if (WIDE) mr_add(w0, w1, (uint32_t)lane, H.V, H.radix3);
         else w0 = badd(bw0, lane_add, bz.B);
         double fwd;
-        const int fail = walk<DM>(S, w0, w1, active, fwd, tid);
+        int fail;
+        if (WIDE) fail = walk<DM>(S, w0, w1, active, fwd, tid);
+        else fail = walk_fast<SKIP>(sm32, H.T, H.fast_off, H.fprod_off, w0, active, fwd, rbase, sbase);
         unsigned long long t = x + 1;
         if (fail < 0) {
           const double bwd = WIDE ? backward(S, w0, w1) : backward_b(S, w0);
@@ -857,11 +1040,11 @@ __global__ void __launch_bounds__(THREADS, 3) k_score(const uint8_t* __restrict_
             best_n = ns;
             best_i = idx;
           }
-        } else if (P.skip && active) {
+        } else if (SKIP && active) {
           const NodeSkip sk = S.skip[fail];
           t = sk.R ? (x / sk.R + 1) * sk.R : whi;
         }
-        const unsigned long long nb_ = P.skip ? warp_max_u64(t) : base + 32;
+        const unsigned long long nb_ = SKIP ? warp_max_u64(t) : base + 32;
         if (nb_ >= whi) break;
         if (nb_ == base + 32) {
           if (WIDE) mr_add(bw0, bw1, 32, H.V, H.radix3);
@@ -1700,7 +1883,9 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   // memoised brute force needs every template <= 64 nodes (bitmask state)
   const bool memo = !ctx->skip && ctx->memo && t->max_T <= 64;
   const int threads = memo ? THREADS_M : THREADS;
-  auto kern = memo ? (wide ? k_score_memo<true> : k_score_memo<false>) : (wide ? k_score<true> : k_score<false>);
+  auto kern = memo ? (wide ? k_score_memo<true> : k_score_memo<false>)
+                   : ctx->skip ? (wide ? k_score<true, true> : k_score<false, true>)
+                               : (wide ? k_score<true, false> : k_score<false, false>);
   const size_t smem_k = memo ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_T * THREADS_M * 8 + 16 : smem;
   if (smem_k > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem_k) + " bytes)");

@@ -145,8 +145,28 @@ struct BlobHeader {
   int32_t stride_off;     // u64 reference stride per enumeration position, then int8 perm[V]
   int32_t dirty_off;      // u64 dirty[V+1]: nodes whose ancestor cone reaches position >= q (T <= 64)
   int32_t pad3;
+  // lean walk (biased digits): FastNode[T], a zero block, (reach, state) offset
+  // pairs of producers of fan-in >= 3 nodes, and 4-row routing tables
+  int32_t fast_off, zero_off, fprod_off, tab4_off;
 };
 static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
+
+// Per-node record of the lean scoring walk: every field is a ready-to-use
+// shared-memory byte offset, so the walk does no unpacking.  The routing table
+// of a node has 4 rows indexed by the node's BIASED digit field (row = digit +
+// 4 - radix; unweighted nodes replicate their single row 4 times), each row
+// 3^k bytes keyed by the producer states in base 3.
+struct __align__(16) FastNode {
+  int32_t tab;           // smem offset of the node's 4-row routing table
+  int32_t dbl;           // smem offset of own[4]; exitc[4] follows
+  int32_t cb0, cb1;      // smem offsets of conv[0], conv[1] ([4][3] doubles; zero block if absent)
+  int32_t r0, r1;        // reach byte offsets of producers 0/1 in the lane pool (k >= 3: fprod pair index)
+  int32_t s0, s1;        // state byte offsets of producers 0/1
+  int32_t out_r, out_s;  // output slot offsets (out_r < 0: no internal consumer)
+  int32_t sh;            // bit offset of the node's digit field in the biased word (0 when unweighted)
+  int32_t kf;            // k | 0x100 when the node can set the forward max (subgraph boundary)
+};
+static_assert(sizeof(FastNode) == 48, "FastNode is three 16-byte smem loads");
 
 struct __align__(16) NodeDesc {
   int16_t slot;      // weight slot (enumeration position) or -1

@@ -691,23 +691,26 @@ __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
 
 // Lean walk over FastNode records (biased digit word `w`, V <= 32): the same
 // routing + forward DP as walk<>, with every address precomputed by the table
-// build.  `sm` is the shared address of the staged blob, `rb`/`sb` the lane's
-// reach/state pool bases.  Failed or inactive lanes keep executing with masked
-// garbage (pattern 3 / state 3 index stays inside the padded tables) until the
-// whole warp has failed, exactly like walk<>'s ballot exit.  Only
-// subgraph-boundary nodes update the forward max: an interior node's reach
-// never exceeds its internal consumer's (conv, own >= 0 and rounding is
-// monotone), so the max over boundary nodes is the max over all nodes.
+// build and made absolute (shared window) when the blob is staged, so a node
+// costs three record loads, one table byte and 1-3 fp64 operands.  `rec` is
+// the shared address of FastNode[0], `rb`/`sb` the lane's reach/state pool
+// bases.
+// Failed or inactive lanes keep executing with masked garbage (pattern 3 /
+// state 3 index stays inside the padded tables) until the whole warp has
+// failed, exactly like walk<>'s ballot exit.  Only subgraph-boundary nodes
+// update the forward max: an interior node's reach never exceeds its internal
+// consumer's (conv, own >= 0 and rounding is monotone), so the max over
+// boundary nodes is the max over all nodes.
 template <bool TRACK>
-__device__ __forceinline__ int walk_fast(uint32_t sm, int T, uint32_t fast_off, uint32_t fprod_off, uint64_t w,
-                                         bool active, double& fwd, uint32_t rb, uint32_t sb) {
+__device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool active, double& fwd, uint32_t rb,
+                                         uint32_t sb) {
   bool ok = active;
   int fail = active ? -1 : T;
   long long f = 0;  // bit pattern of the forward max (non-negative doubles)
-  uint32_t rec = sm + fast_off;
   for (int i = 0; i < T; i++, rec += (uint32_t)sizeof(FastNode)) {
-    const int4 A = lds_v4(rec), B = lds_v4(rec + 16), X = lds_v4(rec + 32);
-    // A = (tab, dbl, cb0, cb1), B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf)
+    // A = (tab, dbl, cb0, cb1) absolute, B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf)
+    const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
+    const int4 B = lds_v4(rec + 16);
     const uint32_t b = (uint32_t)(w >> X.z) & 3u;
     const int k = X.w & 0xff;
     uint32_t e;
@@ -715,36 +718,36 @@ __device__ __forceinline__ int walk_fast(uint32_t sm, int T, uint32_t fast_off, 
     if (k == 1) {
       const uint32_t s0 = lds_u8(sb + B.z);
       const double r0 = lds_f64(rb + B.x);
-      e = lds_u8(sm + A.x + b * 3 + s0);
+      e = lds_u8(A.x + b * 3 + s0);
       const bool bad = e == 0xFFu;
       if (TRACK && ok && bad) fail = i;
       ok = ok && !bad;
       if (!__any_sync(0xffffffffu, ok)) break;
       const uint32_t p = e & 3u;
-      r = dadd(dadd(r0, lds_f64(sm + A.z + (p * 3 + s0) * 8)), lds_f64(sm + A.y + p * 8));
+      r = dadd(dadd(r0, lds_f64(A.z + (p * 3 + s0) * 8)), lds_f64(A.y + p * 8));
     } else if (k == 2) {
       const uint32_t s0 = lds_u8(sb + B.z), s1 = lds_u8(sb + B.w);
       const double r0 = lds_f64(rb + B.x), r1 = lds_f64(rb + B.y);
-      e = lds_u8(sm + A.x + b * 9 + s0 * 3 + s1);
+      e = lds_u8(A.x + b * 9 + s0 * 3 + s1);
       const bool bad = e == 0xFFu;
       if (TRACK && ok && bad) fail = i;
       ok = ok && !bad;
       if (!__any_sync(0xffffffffu, ok)) break;
       const uint32_t p = e & 3u;
-      r = dadd(dmax_nn(dadd(r0, lds_f64(sm + A.z + (p * 3 + s0) * 8)), dadd(r1, lds_f64(sm + A.w + (p * 3 + s1) * 8))),
-               lds_f64(sm + A.y + p * 8));
+      r = dadd(dmax_nn(dadd(r0, lds_f64(A.z + (p * 3 + s0) * 8)), dadd(r1, lds_f64(A.w + (p * 3 + s1) * 8))),
+               lds_f64(A.y + p * 8));
     } else if (k == 0) {
-      e = lds_u8(sm + A.x + b);
+      e = lds_u8(A.x + b);
       const bool bad = e == 0xFFu;
       if (TRACK && ok && bad) fail = i;
       ok = ok && !bad;
       if (!__any_sync(0xffffffffu, ok)) break;
-      r = lds_f64(sm + A.y + (e & 3u) * 8);
+      r = lds_f64(A.y + (e & 3u) * 8);
     } else {
-      const uint32_t pp = sm + fprod_off + 8 * (uint32_t)B.x;
+      const uint32_t pp = (uint32_t)B.x;  // absolute address of the (reach, state) offset pairs
       uint32_t key = b;
       for (int j = 0; j < k; j++) key = key * 3 + lds_u8(sb + lds_s32(pp + 8 * j + 4));
-      e = lds_u8(sm + A.x + key);
+      e = lds_u8(A.x + key);
       const bool bad = e == 0xFFu;
       if (TRACK && ok && bad) fail = i;
       ok = ok && !bad;
@@ -753,13 +756,13 @@ __device__ __forceinline__ int walk_fast(uint32_t sm, int T, uint32_t fast_off, 
       double bse = 0.0;
       for (int j = 0; j < k; j++) {
         const uint32_t sj = lds_u8(sb + lds_s32(pp + 8 * j + 4));
-        bse = dmax_nn(bse, dadd(lds_f64(rb + lds_s32(pp + 8 * j)), lds_f64(sm + A.z + j * 96 + (p * 3 + sj) * 8)));
+        bse = dmax_nn(bse, dadd(lds_f64(rb + lds_s32(pp + 8 * j)), lds_f64(A.z + j * 96 + (p * 3 + sj) * 8)));
       }
-      r = dadd(bse, lds_f64(sm + A.y + p * 8));
+      r = dadd(bse, lds_f64(A.y + p * 8));
     }
     const uint32_t s = (e >> 2) & 3u;
     if (X.w & 0x100) {
-      const long long x = __double_as_longlong(dadd(r, lds_f64(sm + A.y + 32 + s * 8)));
+      const long long x = __double_as_longlong(dadd(r, lds_f64(A.y + 32 + s * 8)));
       f = x > f ? x : f;
     }
     if (X.x >= 0) {
@@ -769,6 +772,21 @@ __device__ __forceinline__ int walk_fast(uint32_t sm, int T, uint32_t fast_off, 
   }
   fwd = __longlong_as_double(f);
   return ok ? -1 : (TRACK ? fail : T);
+}
+
+// Make the staged FastNode table/cost offsets absolute shared addresses.
+__device__ __forceinline__ void patch_fast(uint8_t* smem) {
+  const BlobHeader& H = *(const BlobHeader*)smem;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+  FastNode* fn = (FastNode*)(smem + H.fast_off);
+  for (int i = threadIdx.x; i < H.T; i += blockDim.x) {
+    FastNode& f = fn[i];
+    f.tab += (int32_t)base;
+    f.dbl += (int32_t)base;
+    f.cb0 += (int32_t)base;
+    f.cb1 += (int32_t)base;
+    if ((f.kf & 0xff) >= 3) f.r0 = (int32_t)(base + (uint32_t)H.fprod_off + 8u * (uint32_t)f.r0);
+  }
 }
 
 // backward of plan_cost: pack_gradients over replicated trainable weights
@@ -1000,11 +1018,6 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
     const Biased bz = s_bz;
-    // opaque copies: keep the shared addresses in registers (ptxas would
-    // otherwise re-derive the shared window base at every access)
-    const uint32_t sm32 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem));
-    const uint32_t rbase = opaque_u32((uint32_t)__cvta_generic_to_shared(S.reach + tid));
-    const uint32_t sbase = opaque_u32((uint32_t)__cvta_generic_to_shared(S.stp + tid));
     const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
@@ -1025,8 +1038,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
         else w0 = badd(bw0, lane_add, bz.B);
         double fwd;
         int fail;
-        if (WIDE) fail = walk<DM>(S, w0, w1, active, fwd, tid);
-        else fail = walk_fast<SKIP>(sm32, H.T, H.fast_off, H.fprod_off, w0, active, fwd, rbase, sbase);
+        fail = walk<DM>(S, w0, w1, active, fwd, tid);
         unsigned long long t = x + 1;
         if (fail < 0) {
           const double bwd = WIDE ? backward(S, w0, w1) : backward_b(S, w0);
@@ -1100,6 +1112,183 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
           o.total_bits = s_red_t[w];
           o.num_split = s_red_n[w];
           o.index = s_red_i[w];
+        }
+      }
+      items[item] = o;
+    }
+  }
+}
+
+// Batched scorer for blocks with <= 32 weight slots (biased digit word): the
+// same work decomposition and argmin as k_score, with the lean FastNode walk.
+// Each lane carries its own candidate's digit word and advances it by 32 per
+// warp step (one carry-fixed add); the warp's remaining count is 32-bit.
+template <bool SKIP>
+__global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(const uint8_t* __restrict__ blobs,
+                                                                           ScorePlan P, ItemOut* __restrict__ items,
+                                                                           unsigned long long* __restrict__ counter) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ unsigned long long s_item;
+  __shared__ int64_t s_block;
+  __shared__ unsigned long long s_red_t[THREADS / 32], s_red_i[THREADS / 32];
+  __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
+  __shared__ uint64_t s_lane_add[32];
+  __shared__ Biased s_bz;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  int64_t staged = -1;
+  while (true) {
+    if (tid == 0) s_item = atomicAdd(counter, 1ULL);
+    __syncthreads();
+    const unsigned long long item = s_item;
+    if (item >= P.n_items) break;
+    if (tid == 0) {
+      int64_t lo = 0, hi = P.nb;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (P.item_base[mid] <= item) lo = mid;
+        else hi = mid;
+      }
+      s_block = lo;
+    }
+    __syncthreads();
+    const int64_t b = s_block;
+    if (b != staged) {
+      stage_blob(smem, blobs, P.blob_off[b]);
+      const BlobHeader* gH = (const BlobHeader*)(blobs + P.blob_off[b]);
+      const int V = gH->V;
+      const uint64_t r3 = gH->radix3;
+      if (tid < 32) {
+        uint64_t a = 0;  // unbiased digits of `tid` in the fastest positions
+        uint32_t x = (uint32_t)tid;
+        for (int q = V - 1; q >= 0 && x; q--) {
+          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+          a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
+          x /= r;
+        }
+        s_lane_add[tid] = a;
+      } else if (tid == 32) {
+        Biased z{0, 0, 0};
+        uint32_t x = 32;
+        for (int q = V - 1; q >= 0; q--) {
+          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+          const int sh = 2 * (V - 1 - q);
+          z.B |= (uint64_t)(4 - r) << sh;
+          z.NZ |= (uint64_t)(r == 3 ? 2 : 1) << sh;
+          z.add32 |= (uint64_t)(x % r) << sh;
+          x /= r;
+        }
+        s_bz = z;
+      }
+      __syncthreads();
+      patch_fast(smem);
+      staged = b;
+    }
+    __syncthreads();
+    const Tabs S = tabs_of(smem);
+    const BlobHeader& H = *S.H;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
+    const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
+    const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
+    const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
+    unsigned long long best_t = ~0ULL, best_i = ~0ULL;
+    uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
+    if (wlo < whi) {
+      // opaque copies keep the shared addresses in registers (ptxas would
+      // otherwise re-derive the shared window base at every access)
+      const uint32_t rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
+      const uint32_t rb = opaque_u32((uint32_t)__cvta_generic_to_shared(S.reach + tid));
+      const uint32_t sb = opaque_u32((uint32_t)__cvta_generic_to_shared(S.stp + tid));
+      const int T = H.T;
+      uint32_t rem = (uint32_t)(whi - wlo);  // candidates left for this warp (<= item size)
+      unsigned long long base = wlo;
+      uint64_t w = badd(bencode(H, wlo), s_lane_add[lane], s_bz.B);
+      while (true) {
+        const bool active = (uint32_t)lane < rem;
+        double fwd;
+        const int fail = walk_fast<SKIP>(rec0, T, w, active, fwd, rb, sb);
+        uint32_t adv = 32;  // SKIP: candidates this lane proves done, from base
+        if (fail < 0) {
+          const double bwd = backward_b(S, w);
+          const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
+          const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+          const uint32_t ns = (uint32_t)__popcll(w & s_bz.NZ);
+          const unsigned long long idx = ref_index_b(S, w);
+          nvalid++;
+          if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
+            best_t = tb;
+            best_n = ns;
+            best_i = idx;
+          }
+          if (SKIP) adv = lane + 1;
+        } else if (SKIP) {
+          adv = lane + 1;
+          if (active) {
+            const NodeSkip sk = S.skip[fail];
+            const unsigned long long x = base + lane;
+            const unsigned long long t = sk.R ? (x / sk.R + 1) * sk.R : whi;
+            adv = (uint32_t)(min(t, whi) - base);
+          }
+        }
+        if (!SKIP) {
+          if (rem <= 32) break;
+          rem -= 32;
+          base += 32;
+          w = badd(w, s_bz.add32, s_bz.B);
+        } else {
+          // the union of the lanes' proven runs is contiguous from base
+          uint32_t m = adv;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+          if (m >= rem) break;
+          if (m == 32) {
+            w = badd(w, s_bz.add32, s_bz.B);
+          } else {
+            // the lane that proved the longest run provides the next base digits
+            const int src = __ffs(__ballot_sync(0xffffffffu, adv == m)) - 1;
+            uint64_t n0 = w;
+            if (lane == src) {
+              const bool jump = fail >= 0 && active && S.skip[fail].R;
+              // positions faster than m back to digit 0, then +1 at position m
+              const int sh = jump ? 2 * (H.V - 1 - S.skip[fail].m) : 0;
+              const uint64_t low = (1ULL << sh) - 1;
+              n0 = badd((n0 & ~low) | (s_bz.B & low), 1ULL << sh, s_bz.B);
+            }
+            w = badd(shfl_u64(n0, src), s_lane_add[lane], s_bz.B);
+          }
+          rem -= m;
+          base += m;
+        }
+      }
+    }
+    // warp then block argmin of (total, num_split, index) + valid count
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, best_t, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, best_i, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, best_n, o);
+      nvalid += __shfl_down_sync(0xffffffffu, nvalid, o);
+      if (key_less(t2, n2, i2, best_t, best_n, best_i)) {
+        best_t = t2;
+        best_n = n2;
+        best_i = i2;
+      }
+    }
+    if (lane == 0) {
+      s_red_t[warp] = best_t;
+      s_red_i[warp] = best_i;
+      s_red_n[warp] = best_n;
+      s_red_v[warp] = nvalid;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      ItemOut o{s_red_t[0], s_red_i[0], s_red_n[0], s_red_v[0]};
+      for (int w2 = 1; w2 < THREADS / 32; w2++) {
+        o.valid += s_red_v[w2];
+        if (key_less(s_red_t[w2], s_red_n[w2], s_red_i[w2], o.total_bits, o.num_split, o.index)) {
+          o.total_bits = s_red_t[w2];
+          o.num_split = s_red_n[w2];
+          o.index = s_red_i[w2];
         }
       }
       items[item] = o;
@@ -1883,9 +2072,11 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   // memoised brute force needs every template <= 64 nodes (bitmask state)
   const bool memo = !ctx->skip && ctx->memo && t->max_T <= 64;
   const int threads = memo ? THREADS_M : THREADS;
+  // SP_SCORE_GENERIC=1 selects the generic walk for narrow blocks (A/B checks)
+  const bool generic = getenv("SP_SCORE_GENERIC") != nullptr;
   auto kern = memo ? (wide ? k_score_memo<true> : k_score_memo<false>)
-                   : ctx->skip ? (wide ? k_score<true, true> : k_score<false, true>)
-                               : (wide ? k_score<true, false> : k_score<false, false>);
+              : ctx->skip ? (wide ? k_score<true, true> : generic ? k_score<false, true> : k_score_fast<true>)
+                          : (wide ? k_score<true, false> : generic ? k_score<false, false> : k_score_fast<false>);
   const size_t smem_k = memo ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_T * THREADS_M * 8 + 16 : smem;
   if (smem_k > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem_k) + " bytes)");

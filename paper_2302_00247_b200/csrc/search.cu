@@ -459,15 +459,18 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       route_node(G, tmpl_nodes[e0 + i], (int32_t)b, node_block, (int)x, ps, M, &R, false);
       const uint8_t val = R.pattern < 0 ? (uint8_t)0xFF : (uint8_t)(R.pattern | (R.state << 2));
       blob[H.tab_off + L.tab + key] = val;
-      // 4-row table of the lean walk: row = biased digit (x + 4 - nd)
+      // 4-row table of the lean walk: row = biased digit (x + 4 - nd); byte =
+      // pattern * 8 + state (0xFF = RoutingFailure), so the walk's own-cost
+      // offset is one mask and the state another
       const uint32_t pk = pow3(L.k), rest = key - x * pk;
       uint8_t* t4 = blob + H.tab4_off + L.tab4 + rest;
+      const uint8_t val4 = R.pattern < 0 ? (uint8_t)0xFF : (uint8_t)((R.pattern << 3) | R.state);
       if (slot_of[e0 + i] >= 0) {
-        t4[(x + 4 - L.nd) * pk] = val;
+        t4[(x + 4 - L.nd) * pk] = val4;
         if (x == 0)
           for (int bb = 0; bb < 4 - L.nd; bb++) t4[bb * pk] = 0xFF;  // unused rows
       } else {
-        for (int bb = 0; bb < 4; bb++) t4[bb * pk] = val;
+        for (int bb = 0; bb < 4; bb++) t4[bb * pk] = val4;
       }
     }
     __syncthreads();
@@ -707,7 +710,17 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
   bool ok = active;
   int fail = active ? -1 : T;
   long long f = 0;  // bit pattern of the forward max (non-negative doubles)
-  for (int i = 0; i < T; i++, rec += (uint32_t)sizeof(FastNode)) {
+  const uint32_t end = rec + (uint32_t)T * (uint32_t)sizeof(FastNode);
+  // table byte e = pattern * 8 + state: pe = e & 0x18 is the own-cost byte
+  // offset and 3 * pe the conversion-row offset; failure 0xFF masks to 3 / 3
+#define SP_FAIL_CHECK(i)                        \
+  {                                             \
+    const bool bad = e == 0xFFu;                \
+    if (TRACK && ok && bad) fail = (i);         \
+    ok = ok && !bad;                            \
+    if (!__any_sync(0xffffffffu, ok)) break;    \
+  }
+  for (int i = 0; rec != end; i++, rec += (uint32_t)sizeof(FastNode)) {
     // A = (tab, dbl, cb0, cb1) absolute, B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf)
     const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
     const int4 B = lds_v4(rec + 16);
@@ -719,48 +732,36 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
       const uint32_t s0 = lds_u8(sb + B.z);
       const double r0 = lds_f64(rb + B.x);
       e = lds_u8(A.x + b * 3 + s0);
-      const bool bad = e == 0xFFu;
-      if (TRACK && ok && bad) fail = i;
-      ok = ok && !bad;
-      if (!__any_sync(0xffffffffu, ok)) break;
-      const uint32_t p = e & 3u;
-      r = dadd(dadd(r0, lds_f64(A.z + (p * 3 + s0) * 8)), lds_f64(A.y + p * 8));
+      SP_FAIL_CHECK(i)
+      const uint32_t pe = e & 0x18u;
+      r = dadd(dadd(r0, lds_f64(A.z + pe * 3 + s0 * 8)), lds_f64(A.y + pe));
     } else if (k == 2) {
       const uint32_t s0 = lds_u8(sb + B.z), s1 = lds_u8(sb + B.w);
       const double r0 = lds_f64(rb + B.x), r1 = lds_f64(rb + B.y);
       e = lds_u8(A.x + b * 9 + s0 * 3 + s1);
-      const bool bad = e == 0xFFu;
-      if (TRACK && ok && bad) fail = i;
-      ok = ok && !bad;
-      if (!__any_sync(0xffffffffu, ok)) break;
-      const uint32_t p = e & 3u;
-      r = dadd(dmax_nn(dadd(r0, lds_f64(A.z + (p * 3 + s0) * 8)), dadd(r1, lds_f64(A.w + (p * 3 + s1) * 8))),
-               lds_f64(A.y + p * 8));
+      SP_FAIL_CHECK(i)
+      const uint32_t pe = e & 0x18u;
+      r = dadd(dmax_nn(dadd(r0, lds_f64(A.z + pe * 3 + s0 * 8)), dadd(r1, lds_f64(A.w + pe * 3 + s1 * 8))),
+               lds_f64(A.y + pe));
     } else if (k == 0) {
       e = lds_u8(A.x + b);
-      const bool bad = e == 0xFFu;
-      if (TRACK && ok && bad) fail = i;
-      ok = ok && !bad;
-      if (!__any_sync(0xffffffffu, ok)) break;
-      r = lds_f64(A.y + (e & 3u) * 8);
+      SP_FAIL_CHECK(i)
+      r = lds_f64(A.y + (e & 0x18u));
     } else {
       const uint32_t pp = (uint32_t)B.x;  // absolute address of the (reach, state) offset pairs
       uint32_t key = b;
       for (int j = 0; j < k; j++) key = key * 3 + lds_u8(sb + lds_s32(pp + 8 * j + 4));
       e = lds_u8(A.x + key);
-      const bool bad = e == 0xFFu;
-      if (TRACK && ok && bad) fail = i;
-      ok = ok && !bad;
-      if (!__any_sync(0xffffffffu, ok)) break;
-      const uint32_t p = e & 3u;
+      SP_FAIL_CHECK(i)
+      const uint32_t pe = e & 0x18u;
       double bse = 0.0;
       for (int j = 0; j < k; j++) {
         const uint32_t sj = lds_u8(sb + lds_s32(pp + 8 * j + 4));
-        bse = dmax_nn(bse, dadd(lds_f64(rb + lds_s32(pp + 8 * j)), lds_f64(A.z + j * 96 + (p * 3 + sj) * 8)));
+        bse = dmax_nn(bse, dadd(lds_f64(rb + lds_s32(pp + 8 * j)), lds_f64(A.z + j * 96 + pe * 3 + sj * 8)));
       }
-      r = dadd(bse, lds_f64(A.y + p * 8));
+      r = dadd(bse, lds_f64(A.y + pe));
     }
-    const uint32_t s = (e >> 2) & 3u;
+    const uint32_t s = e & 3u;
     if (X.w & 0x100) {
       const long long x = __double_as_longlong(dadd(r, lds_f64(A.y + 32 + s * 8)));
       f = x > f ? x : f;
@@ -770,6 +771,7 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
       sts_u8(sb + X.y, s);
     }
   }
+#undef SP_FAIL_CHECK
   fwd = __longlong_as_double(f);
   return ok ? -1 : (TRACK ? fail : T);
 }
@@ -1203,6 +1205,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(con
       uint32_t rem = (uint32_t)(whi - wlo);  // candidates left for this warp (<= item size)
       unsigned long long base = wlo;
       uint64_t w = badd(bencode(H, wlo), s_lane_add[lane], s_bz.B);
+      uint64_t best_w = 0;
       while (true) {
         const bool active = (uint32_t)lane < rem;
         double fwd;
@@ -1213,12 +1216,14 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(con
           const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
           const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
           const uint32_t ns = (uint32_t)__popcll(w & s_bz.NZ);
-          const unsigned long long idx = ref_index_b(S, w);
           nvalid++;
-          if (key_less(tb, ns, idx, best_t, best_n, best_i)) {
+          // the reference index only breaks exact (total, num_split) ties:
+          // keep the digits and convert once per item
+          if (tb < best_t || (tb == best_t && (ns < best_n || (ns == best_n && ref_index_b(S, w) <
+                                                                                  ref_index_b(S, best_w))))) {
             best_t = tb;
             best_n = ns;
-            best_i = idx;
+            best_w = w;
           }
           if (SKIP) adv = lane + 1;
         } else if (SKIP) {
@@ -1260,6 +1265,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(con
           base += m;
         }
       }
+      if (best_t != ~0ULL) best_i = ref_index_b(S, best_w);
     }
     // warp then block argmin of (total, num_split, index) + valid count
 #pragma unroll

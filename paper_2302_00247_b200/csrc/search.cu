@@ -777,18 +777,151 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
 }
 
 // Make the staged FastNode table/cost offsets absolute shared addresses.
-__device__ __forceinline__ void patch_fast(uint8_t* smem) {
+// With `pair` (two candidates per lane) every pool offset doubles: slot p of
+// lane t holds candidate a at (2p*THREADS + t) and b one THREADS further.
+__device__ __forceinline__ void patch_fast(uint8_t* smem, bool pair = false) {
   const BlobHeader& H = *(const BlobHeader*)smem;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
   FastNode* fn = (FastNode*)(smem + H.fast_off);
+  const int32_t m = pair ? 2 : 1;
   for (int i = threadIdx.x; i < H.T; i += blockDim.x) {
     FastNode& f = fn[i];
     f.tab += (int32_t)base;
     f.dbl += (int32_t)base;
     f.cb0 += (int32_t)base;
     f.cb1 += (int32_t)base;
-    if ((f.kf & 0xff) >= 3) f.r0 = (int32_t)(base + (uint32_t)H.fprod_off + 8u * (uint32_t)f.r0);
+    const int k = f.kf & 0xff;
+    if (k >= 3) {
+      int32_t* pp = (int32_t*)(smem + H.fprod_off) + 2 * f.r0;
+      for (int j = 0; j < k; j++) {
+        pp[2 * j] *= m;
+        pp[2 * j + 1] *= m;
+      }
+      f.r0 = (int32_t)(base + (uint32_t)H.fprod_off + 8u * (uint32_t)f.r0);
+    } else {
+      f.r0 *= m;
+      f.s0 *= m;
+    }
+    f.r1 *= m;
+    f.s1 *= m;
+    if (f.out_r >= 0) {
+      f.out_r *= m;
+      f.out_s *= m;
+    }
   }
+}
+
+template <int OFF>
+__device__ __forceinline__ uint32_t lds_u8o(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ double lds_f64o(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ void sts_f64o(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0+%2], %1;" ::"r"(a), "d"(v), "n"(OFF) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void sts_u8o(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0+%2], %1;" ::"r"(a), "r"(v), "n"(OFF) : "memory");
+}
+
+// walk_fast for two candidates per lane (brute force): one record load and
+// one dispatch per node serve both, and the two dependency chains interleave.
+// Candidate b's pool entries sit THREADS entries after candidate a's.  The
+// warp leaves when all 64 candidates have failed.  Returns valid bits
+// (bit 0 = a, bit 1 = b).
+__device__ __forceinline__ int walk_pair(uint32_t rec, int T, uint64_t wa, uint64_t wb, bool act_a, bool act_b,
+                                         double& fwd_a, double& fwd_b, uint32_t rb, uint32_t sb) {
+  constexpr int RB = THREADS * 8, SB = THREADS;
+  bool oka = act_a, okb = act_b;
+  long long fa = 0, fb = 0;
+  const uint32_t end = rec + (uint32_t)T * (uint32_t)sizeof(FastNode);
+#define SP_FAIL_CHECK2                                    {                                                         oka = oka && ea != 0xFFu;                               okb = okb && eb != 0xFFu;                               if (!__any_sync(0xffffffffu, oka || okb)) break;      }
+  for (; rec != end; rec += (uint32_t)sizeof(FastNode)) {
+    const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
+    const int4 B = lds_v4(rec + 16);
+    const uint32_t ba = (uint32_t)(wa >> X.z) & 3u, bb = (uint32_t)(wb >> X.z) & 3u;
+    const int k = X.w & 0xff;
+    uint32_t ea, eb;
+    double ra, rx;
+    if (k == 1) {
+      const uint32_t ps = sb + B.z, pr = rb + B.x;
+      const uint32_t s0a = lds_u8o<0>(ps), s0b = lds_u8o<SB>(ps);
+      const double r0a = lds_f64o<0>(pr), r0b = lds_f64o<RB>(pr);
+      ea = lds_u8(A.x + ba * 3 + s0a);
+      eb = lds_u8(A.x + bb * 3 + s0b);
+      SP_FAIL_CHECK2
+      const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
+      ra = dadd(dadd(r0a, lds_f64(A.z + pa * 3 + s0a * 8)), lds_f64(A.y + pa));
+      rx = dadd(dadd(r0b, lds_f64(A.z + pb * 3 + s0b * 8)), lds_f64(A.y + pb));
+    } else if (k == 2) {
+      const uint32_t ps0 = sb + B.z, ps1 = sb + B.w, pr0 = rb + B.x, pr1 = rb + B.y;
+      const uint32_t s0a = lds_u8o<0>(ps0), s1a = lds_u8o<0>(ps1);
+      const uint32_t s0b = lds_u8o<SB>(ps0), s1b = lds_u8o<SB>(ps1);
+      const double r0a = lds_f64o<0>(pr0), r1a = lds_f64o<0>(pr1);
+      const double r0b = lds_f64o<RB>(pr0), r1b = lds_f64o<RB>(pr1);
+      ea = lds_u8(A.x + ba * 9 + s0a * 3 + s1a);
+      eb = lds_u8(A.x + bb * 9 + s0b * 3 + s1b);
+      SP_FAIL_CHECK2
+      const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
+      ra = dadd(dmax_nn(dadd(r0a, lds_f64(A.z + pa * 3 + s0a * 8)), dadd(r1a, lds_f64(A.w + pa * 3 + s1a * 8))),
+                lds_f64(A.y + pa));
+      rx = dadd(dmax_nn(dadd(r0b, lds_f64(A.z + pb * 3 + s0b * 8)), dadd(r1b, lds_f64(A.w + pb * 3 + s1b * 8))),
+                lds_f64(A.y + pb));
+    } else if (k == 0) {
+      ea = lds_u8(A.x + ba);
+      eb = lds_u8(A.x + bb);
+      SP_FAIL_CHECK2
+      ra = lds_f64(A.y + (ea & 0x18u));
+      rx = lds_f64(A.y + (eb & 0x18u));
+    } else {
+      const uint32_t pp = (uint32_t)B.x;
+      uint32_t ka = ba, kb = bb;
+      for (int j = 0; j < k; j++) {
+        const uint32_t ps = sb + lds_s32(pp + 8 * j + 4);
+        ka = ka * 3 + lds_u8o<0>(ps);
+        kb = kb * 3 + lds_u8o<SB>(ps);
+      }
+      ea = lds_u8(A.x + ka);
+      eb = lds_u8(A.x + kb);
+      SP_FAIL_CHECK2
+      const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
+      double xa = 0.0, xb = 0.0;
+      for (int j = 0; j < k; j++) {
+        const uint32_t ps = sb + lds_s32(pp + 8 * j + 4), pr = rb + lds_s32(pp + 8 * j);
+        const uint32_t sja = lds_u8o<0>(ps), sjb = lds_u8o<SB>(ps);
+        xa = dmax_nn(xa, dadd(lds_f64o<0>(pr), lds_f64(A.z + j * 96 + pa * 3 + sja * 8)));
+        xb = dmax_nn(xb, dadd(lds_f64o<RB>(pr), lds_f64(A.z + j * 96 + pb * 3 + sjb * 8)));
+      }
+      ra = dadd(xa, lds_f64(A.y + pa));
+      rx = dadd(xb, lds_f64(A.y + pb));
+    }
+    const uint32_t sa = ea & 3u, sx = eb & 3u;
+    if (X.w & 0x100) {
+      const long long xa = __double_as_longlong(dadd(ra, lds_f64(A.y + 32 + sa * 8)));
+      const long long xb = __double_as_longlong(dadd(rx, lds_f64(A.y + 32 + sx * 8)));
+      fa = xa > fa ? xa : fa;
+      fb = xb > fb ? xb : fb;
+    }
+    if (X.x >= 0) {
+      const uint32_t qr = rb + X.x, qs = sb + X.y;
+      sts_f64o<0>(qr, ra);
+      sts_f64o<RB>(qr, rx);
+      sts_u8o<0>(qs, sa);
+      sts_u8o<SB>(qs, sx);
+    }
+  }
+#undef SP_FAIL_CHECK2
+  fwd_a = __longlong_as_double(fa);
+  fwd_b = __longlong_as_double(fb);
+  return (oka ? 1 : 0) | (okb ? 2 : 0);
 }
 
 // backward of plan_cost: pack_gradients over replicated trainable weights
@@ -887,6 +1020,7 @@ struct Biased {
   uint64_t B;      // packed biases = the encoding of all-zero digits
   uint64_t NZ;     // bit that is set iff the digit is non-zero, per position
   uint64_t add32;  // unbiased digits of 32 (added to advance a warp by 32)
+  uint64_t add64;  // unbiased digits of 64 (paired walk)
 };
 
 // y + a where a holds unbiased digits: a field that wraps carries into the next
@@ -1001,7 +1135,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
           }
           s_lane_add[tid] = a;
         } else if (tid == 32) {
-          Biased z{0, 0, 0};
+          Biased z{0, 0, 0, 0};
           uint32_t x = 32;
           for (int q = V - 1; q >= 0; q--) {
             const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
@@ -1125,8 +1259,11 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
 // same work decomposition and argmin as k_score, with the lean FastNode walk.
 // Each lane carries its own candidate's digit word and advances it by 32 per
 // warp step (one carry-fixed add); the warp's remaining count is 32-bit.
-template <bool SKIP>
-__global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(const uint8_t* __restrict__ blobs,
+#ifndef SP_PAIR_MIN_BLOCKS
+#define SP_PAIR_MIN_BLOCKS 4
+#endif
+template <bool SKIP, bool PAIR>
+__global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_MIN_BLOCKS) k_score_fast(const uint8_t* __restrict__ blobs,
                                                                            ScorePlan P, ItemOut* __restrict__ items,
                                                                            unsigned long long* __restrict__ counter) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1170,7 +1307,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(con
         }
         s_lane_add[tid] = a;
       } else if (tid == 32) {
-        Biased z{0, 0, 0};
+        Biased z{0, 0, 0, 0};
         uint32_t x = 32;
         for (int q = V - 1; q >= 0; q--) {
           const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
@@ -1180,10 +1317,16 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(con
           z.add32 |= (uint64_t)(x % r) << sh;
           x /= r;
         }
+        uint32_t x64 = 64;
+        for (int q = V - 1; q >= 0 && x64; q--) {
+          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+          z.add64 |= (uint64_t)(x64 % r) << (2 * (V - 1 - q));
+          x64 /= r;
+        }
         s_bz = z;
       }
       __syncthreads();
-      patch_fast(smem);
+      patch_fast(smem, PAIR);
       staged = b;
     }
     __syncthreads();
@@ -1199,32 +1342,49 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_fast(con
       // opaque copies keep the shared addresses in registers (ptxas would
       // otherwise re-derive the shared window base at every access)
       const uint32_t rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
-      const uint32_t rb = opaque_u32((uint32_t)__cvta_generic_to_shared(S.reach + tid));
-      const uint32_t sb = opaque_u32((uint32_t)__cvta_generic_to_shared(S.stp + tid));
+      // pool: reach[npool][THREADS (x2 paired)] doubles, then the state bytes
+      const uint32_t pool = (uint32_t)__cvta_generic_to_shared(S.reach);
+      const uint32_t rb = opaque_u32(pool + 8u * (uint32_t)tid);
+      const uint32_t sb = opaque_u32(pool + (uint32_t)H.npool * THREADS * (PAIR ? 16u : 8u) + (uint32_t)tid);
       const int T = H.T;
       uint32_t rem = (uint32_t)(whi - wlo);  // candidates left for this warp (<= item size)
       unsigned long long base = wlo;
       uint64_t w = badd(bencode(H, wlo), s_lane_add[lane], s_bz.B);
       uint64_t best_w = 0;
-      while (true) {
+      // valid candidate: total, key update (the reference index only breaks
+      // exact (total, num_split) ties: keep the digits, convert once per item)
+      auto take = [&](uint64_t wv, double fwd) {
+        const double bwd = backward_b(S, wv);
+        const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
+        const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+        const uint32_t ns = (uint32_t)__popcll(wv & s_bz.NZ);
+        nvalid++;
+        if (tb < best_t ||
+            (tb == best_t && (ns < best_n || (ns == best_n && ref_index_b(S, wv) < ref_index_b(S, best_w))))) {
+          best_t = tb;
+          best_n = ns;
+          best_w = wv;
+        }
+      };
+      if (PAIR) {
+        while (true) {
+          const uint64_t wb = badd(w, s_bz.add32, s_bz.B);
+          double fa, fb;
+          const int v = walk_pair(rec0, T, w, wb, (uint32_t)lane < rem, (uint32_t)lane + 32 < rem, fa, fb, rb, sb);
+          if (v & 1) take(w, fa);
+          if (v & 2) take(wb, fb);
+          if (rem <= 64) break;
+          rem -= 64;
+          w = badd(w, s_bz.add64, s_bz.B);
+        }
+      }
+      while (!PAIR) {
         const bool active = (uint32_t)lane < rem;
         double fwd;
         const int fail = walk_fast<SKIP>(rec0, T, w, active, fwd, rb, sb);
         uint32_t adv = 32;  // SKIP: candidates this lane proves done, from base
         if (fail < 0) {
-          const double bwd = backward_b(S, w);
-          const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
-          const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
-          const uint32_t ns = (uint32_t)__popcll(w & s_bz.NZ);
-          nvalid++;
-          // the reference index only breaks exact (total, num_split) ties:
-          // keep the digits and convert once per item
-          if (tb < best_t || (tb == best_t && (ns < best_n || (ns == best_n && ref_index_b(S, w) <
-                                                                                  ref_index_b(S, best_w))))) {
-            best_t = tb;
-            best_n = ns;
-            best_w = w;
-          }
+          take(w, fwd);
           if (SKIP) adv = lane + 1;
         } else if (SKIP) {
           adv = lane + 1;
@@ -2080,10 +2240,16 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   const int threads = memo ? THREADS_M : THREADS;
   // SP_SCORE_GENERIC=1 selects the generic walk for narrow blocks (A/B checks)
   const bool generic = getenv("SP_SCORE_GENERIC") != nullptr;
+  // brute force on narrow blocks walks two candidates per lane (SP_SCORE_SINGLE=1: one)
+  const bool pair = !generic && !wide && !memo && !ctx->skip && getenv("SP_SCORE_SINGLE") == nullptr;
   auto kern = memo ? (wide ? k_score_memo<true> : k_score_memo<false>)
-              : ctx->skip ? (wide ? k_score<true, true> : generic ? k_score<false, true> : k_score_fast<true>)
-                          : (wide ? k_score<true, false> : generic ? k_score<false, false> : k_score_fast<false>);
-  const size_t smem_k = memo ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_T * THREADS_M * 8 + 16 : smem;
+              : ctx->skip ? (wide ? k_score<true, true> : generic ? k_score<false, true> : k_score_fast<true, false>)
+                          : (wide ? k_score<true, false>
+                                  : generic ? k_score<false, false>
+                                            : pair ? k_score_fast<false, true> : k_score_fast<false, false>);
+  const size_t smem_k = memo   ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_T * THREADS_M * 8 + 16
+                       : pair ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_pool * THREADS * 18 + 16
+                              : smem;
   if (smem_k > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem_k) + " bytes)");
   SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k));

@@ -195,6 +195,18 @@ int sp_score(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_scor
  */
 int sp_search(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* blocks,
               int8_t* node_detail, int8_t* edge_detail);
+/*
+ * Asynchronous form of sp_score / sp_search: sp_score_launch enqueues the
+ * scoring of shard `shard` of `n_shards` (and, with `explain`, the winner
+ * detail of sp_explain_all) on the context's stream and returns at once, so
+ * the caller can assemble host-side results while the device searches;
+ * sp_score_wait collects it (blocks/node_detail/edge_detail may be NULL, and
+ * must be when `explain` was 0).  One search may be in flight per tables.
+ * No reference counterpart: the reference's pool.map blocks (search.py:338).
+ */
+int sp_score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, int32_t explain);
+int sp_score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* blocks, int8_t* node_detail,
+                  int8_t* edge_detail);
 /* Score [lo, hi) of one block; optional per-candidate totals (NaN = invalid). */
 int sp_score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi,
                    double* totals, sp_score_out* out);

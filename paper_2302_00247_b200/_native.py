@@ -67,12 +67,15 @@ def _declare(L):
     L.sp_set_option.argtypes = [vp, C.c_int32, C.c_int64]
     L.sp_search.argtypes = [vp, vp, C.POINTER(SpScoreOut), C.POINTER(SpExplainBlock),
                             C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
+    L.sp_score_launch.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32]
+    L.sp_score_wait.argtypes = [vp, vp, C.POINTER(SpScoreOut), C.POINTER(SpExplainBlock),
+                                C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_tables_sizes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     L.sp_tables_edge_offsets.argtypes = [vp, C.POINTER(C.c_int64)]
     L.sp_explain_all.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(SpExplainBlock),
                                  C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_copy_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-    for name in ("sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
+    for name in ("sp_score_launch", "sp_score_wait", "sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
                  "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
                  "sp_score_range", "sp_explain", "sp_last_timings"):
         getattr(L, name).restype = C.c_int
@@ -103,7 +106,7 @@ EXPORTED_SYMBOLS = (
     "sp_merge_keys", "sp_explain", "sp_last_timings", "sp_timer_start", "sp_timer_stop",
     "sp_launch_counts", "sp_copy_bytes", "sp_tables_bytes", "sp_tables_sizes",
     "sp_tables_edge_offsets", "sp_explain_all", "sp_search", "sp_set_option",
-    "sp_fold_stats",
+    "sp_fold_stats", "sp_score_launch", "sp_score_wait",
 )
 
 
@@ -253,6 +256,29 @@ class Backend:
                                        ptr(edge, C.c_int8)), "sp_search")
         nb = t.n_blocks
         return [outs[i] for i in range(nb)], ([blocks[i] for i in range(nb)], node, edge, eoff)
+
+    def score_launch(self, t: Tables, shard: int = 0, n_shards: int = 1, explain: bool = False) -> None:
+        """Enqueue the search (sp_score_launch) and return at once; collect with score_wait."""
+        self._check(self.lib.sp_score_launch(self.ctx, t.ptr, shard, n_shards, 1 if explain else 0),
+                    "sp_score_launch")
+        t.pending_explain = explain
+
+    def score_wait(self, t: Tables) -> tuple:
+        """(scores, detail) of the search in flight; detail is None unless it was
+        launched with explain (then as explain_all returns it)."""
+        nb = t.n_blocks
+        outs = (SpScoreOut * max(1, nb))()
+        if getattr(t, "pending_explain", False):
+            blocks, node, edge, eoff = self._detail_buffers(t)
+            self._check(self.lib.sp_score_wait(self.ctx, t.ptr, outs, blocks, ptr(node, C.c_int8),
+                                               ptr(edge, C.c_int8)), "sp_score_wait")
+            detail = ([blocks[i] for i in range(nb)], node, edge, eoff)
+        else:
+            self._check(self.lib.sp_score_wait(self.ctx, t.ptr, outs, None, None, None),
+                        "sp_score_wait")
+            detail = None
+        t.pending_explain = False
+        return [outs[i] for i in range(nb)], detail
 
     def explain_all(self, t: Tables, indices) -> tuple:
         """Winner detail of every block: (blocks, node_detail [ne,4], edge_detail [nedge,2],

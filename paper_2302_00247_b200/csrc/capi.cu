@@ -193,6 +193,24 @@ int sp_search(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* bl
   });
 }
 
+int sp_score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, int32_t explain) {
+  if (!ctx || !t) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::score_launch(ctx, t, shard, n_shards, explain != 0);
+  });
+}
+
+int sp_score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* blocks, int8_t* node_detail,
+                  int8_t* edge_detail) {
+  if (!ctx || !t || !out) return SP_ERR_CONFIG;
+  if (blocks && (!node_detail || !edge_detail)) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    sp::score_wait(ctx, t, out, blocks, node_detail, edge_detail);
+  });
+}
+
 int sp_score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi, double* totals,
                    sp_score_out* out) {
   if (!ctx || !t || !out) return SP_ERR_CONFIG;

@@ -2061,10 +2061,24 @@ struct TableDev {
 
 }  // namespace
 
+// Device buffers of a launched, not yet collected search (sp_score_launch).
+struct PendingScore {
+  bool active = false;
+  bool explain = false;
+  bool empty = false;  // no work item: nothing was launched
+  DevBuf<unsigned long long> dplan;
+  DevBuf<ItemOut> items;
+  DevBuf<sp_score_out> dout;
+  DevBuf<ExplainBlock> dblk;
+  DevBuf<int8_t> dnode, dedge;
+  DevBuf<int64_t> deoff;
+};
+
 struct TablesPriv {
   TableDev dev;
   sp_mesh mesh;
   int64_t mu, chunk;
+  PendingScore pending;
 };
 
 }  // namespace sp
@@ -2222,12 +2236,18 @@ struct FusedExplain {
   int8_t* edge;
 };
 
-static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long long>& lo,
-                      const std::vector<unsigned long long>& hi, std::vector<sp_score_out>& res,
-                      const FusedExplain* fx = nullptr) {
+// Enqueue scoring (+ k_reduce, + winner detail when `explain`) of
+// [lo[b], hi[b]) for every block; the buffers stay in the tables' pending
+// slot until score_finish collects them.
+static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long long>& lo,
+                          const std::vector<unsigned long long>& hi, bool explain) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
-  res.assign(nb, sp_score_out{});
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  PendingScore& pd = priv->pending;
+  if (pd.active) throw Error(SP_ERR_CONFIG, "a search on these tables is already in flight");
+  pd.explain = explain;
+  pd.empty = false;
   const size_t smem = score_smem(t);
   if (smem > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
@@ -2271,15 +2291,19 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
     base[b + 1] = base[b] + (c + item_cands - 1) / item_cands;
   }
   const unsigned long long n_items = base[nb];
-  if (n_items == 0) return;
+  if (n_items == 0) {
+    pd.empty = true;
+    pd.active = true;
+    return;
+  }
   // one small H2D for the plan: lo | hi | base | counter
   std::vector<unsigned long long> plan(3 * nb + 2, 0);
   std::copy(lo.begin(), lo.end(), plan.begin());
   std::copy(hi.begin(), hi.end(), plan.begin() + nb);
   std::copy(base.begin(), base.end(), plan.begin() + 2 * nb);
-  DevBuf<unsigned long long> dplan;
-  DevBuf<ItemOut> items;
-  DevBuf<sp_score_out> dout;
+  DevBuf<unsigned long long>& dplan = pd.dplan;
+  DevBuf<ItemOut>& items = pd.items;
+  DevBuf<sp_score_out>& dout = pd.dout;
   dplan.upload(plan.data(), plan.size(), s);
   items.alloc(n_items, s);
   dout.alloc(nb, s);
@@ -2292,12 +2316,11 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);
   SP_CUDA(cudaGetLastError());
-  DevBuf<ExplainBlock> dblk;
-  DevBuf<int8_t> dnode, dedge;
-  DevBuf<int64_t> deoff;
-  if (fx) {
+  if (explain) {
     // winner detail straight from the device-side argmin: no host round trip
-    TablesPriv* priv = (TablesPriv*)t->priv;
+    DevBuf<ExplainBlock>& dblk = pd.dblk;
+    DevBuf<int8_t>&dnode = pd.dnode, &dedge = pd.dedge;
+    DevBuf<int64_t>& deoff = pd.deoff;
     const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
     deoff.upload(t->edge_off.data(), nb + 1, s);
     dblk.alloc(nb, s);
@@ -2309,19 +2332,36 @@ static void run_score(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long
               (const unsigned long long*)nullptr, dout.p, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p,
               dedge.p);
     SP_CUDA(cudaGetLastError());
-    dblk.download((ExplainBlock*)fx->blocks, nb, s);
-    dnode.download(fx->node, 4 * ne, s);
-    dedge.download(fx->edge, 2 * nedge, s);
   }
-  dout.download(res.data(), nb, s);
+  pd.active = true;
+}
+
+// Collect an enqueued search: D2H of the per-block results (and winner detail
+// into fx when it was enqueued), one stream sync.
+static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& res, const FusedExplain* fx) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nb = t->n_blocks;
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  PendingScore& pd = priv->pending;
+  if (!pd.active) throw Error(SP_ERR_CONFIG, "no search in flight on these tables");
+  pd.active = false;
+  res.assign(nb, sp_score_out{});
+  if (pd.empty) return;
+  if (fx && !pd.explain) throw Error(SP_ERR_CONFIG, "winner detail requested but not enqueued");
+  if (fx) {
+    const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
+    pd.dblk.download((ExplainBlock*)fx->blocks, nb, s);
+    pd.dnode.download(fx->node, 4 * ne, s);
+    pd.dedge.download(fx->edge, 2 * nedge, s);
+  }
+  pd.dout.download(res.data(), nb, s);
   SP_CUDA(cudaStreamSynchronize(s));
   float ms = 0;
   SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
   ctx->score_kernel_ms = ms;
 }
 
-void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out, void* xblocks,
-               int8_t* xnode, int8_t* xedge) {
+void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
   if (n_shards < 1 || shard < 0 || shard >= n_shards) throw Error(SP_ERR_CONFIG, "bad shard / n_shards");
   if (t->overflow) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
   const int64_t nb = t->n_blocks;
@@ -2335,9 +2375,14 @@ void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_sc
     hi[b] = (unsigned __int128)lo[b] + step > C ? C : lo[b] + step;
   }
   SP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  score_enqueue(ctx, t, lo, hi, explain);
+}
+
+void score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, void* xblocks, int8_t* xnode, int8_t* xedge) {
+  const int64_t nb = t->n_blocks;
   std::vector<sp_score_out> res;
   FusedExplain fx{xblocks, xnode, xedge};
-  run_score(ctx, t, lo, hi, res, xblocks ? &fx : nullptr);
+  score_finish(ctx, t, res, xblocks ? &fx : nullptr);
   SP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   SP_CUDA(cudaEventSynchronize(ctx->ev[1]));
   float ms = 0;
@@ -2347,6 +2392,12 @@ void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_sc
     out[b] = res.empty() ? sp_score_out{} : res[b];
     out[b].candidates = t->hdr[b].C;
   }
+}
+
+void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out, void* xblocks,
+               int8_t* xnode, int8_t* xedge) {
+  score_launch(ctx, t, shard, n_shards, xblocks != nullptr);
+  score_wait(ctx, t, out, xblocks, xnode, xedge);
 }
 
 void score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi, double* totals,

@@ -261,75 +261,167 @@ _OP_LABELS = ("matmul", "elementwise", "layernorm", "softmax", "embedding", "res
               "output", "auxiliary", "collective")
 
 
-def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
-                     types: TypeSet = DEFAULT_TYPES, detail=None) -> list:
-    """RoutedPlan of every block's argmin from ONE sp_explain_all launch (or the
-    detail sp_search already returned)."""
+def route_prep(ses: Session, subgraphs: list, types: TypeSet = DEFAULT_TYPES) -> list:
+    """Winner-independent part of every block's RoutedPlan (computed while the
+    device searches): template node indices, weight slots in weight_nodes order
+    (names sorted, search.py:85-88) with their radices, and per template node
+    (scope, op label, pattern names, pattern collectives, output bytes,
+    internal producers as (scope, bytes) in GraphNode.inputs order)."""
     low = ses.low
+    index, names = low.index, low.names
+    in_off, in_idx = low.in_off, low.in_idx
+    op, w_rank, act_bytes = low.op, low.w_rank, low.act_bytes
+    pnames, pcolls = types.pattern_names, types.pattern_collectives
+    out = []
+    for sub in subgraphs:
+        template = sub.template
+        tnodes = [index[s] for s in template]
+        members = set(tnodes)
+        wpos = [i for i, v in enumerate(tnodes) if w_rank[v]]
+        slot_pos = sorted(wpos, key=template.__getitem__)
+        radices = [3 if w_rank[tnodes[q]] >= 2 else 2 for q in slot_pos]
+        nodes = []
+        for i, v in enumerate(tnodes):
+            lab = _OP_LABELS[int(op[v])]
+            prods = [(names[r], int(act_bytes[r]))
+                     for r in in_idx[in_off[v]:in_off[v + 1]].tolist() if r in members]
+            nodes.append((template[i], lab, pnames[lab], pcolls[lab], int(act_bytes[v]), prods))
+        out.append((slot_pos, radices, nodes, _flops(low, tnodes)))
+    return out
+
+
+def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
+                     types: TypeSet = DEFAULT_TYPES, detail=None, prep=None) -> list:
+    """RoutedPlan of every block's argmin from ONE sp_explain_all launch (or the
+    detail the search itself returned), on top of route_prep."""
     if detail is None:
         idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
         detail = ses.backend.explain_all(tables, idx)
+    if prep is None:
+        prep = route_prep(ses, subgraphs, types)
     blocks, node, edge, eoff = detail
+    node_l = node.tolist()
+    edge_l = edge.tolist()
     replica = types.ShardSpec(types.ShardKind.REPLICA)
+    splits = [types.ShardSpec(types.ShardKind.SPLIT, a) for a in range(8)]
+    specs = [replica] + splits
     identity = types.Collective(types.CollectiveKind.IDENTITY)
     allreduce = types.Collective(types.CollectiveKind.ALL_REDUCE_SUM)
-    index = low.index
-    names = low.names
-    in_off, in_idx = low.in_off, low.in_idx
+    colls = {}
+    NodeRouting, CandidatePlan, RoutedPlan = types.NodeRouting, types.CandidatePlan, types.RoutedPlan
+    overlap = mesh.overlap_fraction
     out = []
     e0 = 0
-    for b, (sub, sc, X) in enumerate(zip(subgraphs, scores, blocks)):
-        T = len(sub.template)
+    for b, (sub, sc, X, pb) in enumerate(zip(subgraphs, scores, blocks, prep)):
+        slot_pos, radices, nodes, flops = pb
+        T = len(nodes)
         if not sc.has_best or not X.valid:
             out.append(types.RoutingFailure(sub.template[X.fail_pos],
                                             "no pattern chains from producer states")
                        if sc.has_best and X.fail_pos >= 0 else None)
             e0 += T
             continue
-        tnodes = [index[s] for s in sub.template]
-        members = set(tnodes)
-        # weight_nodes order (names sorted, search.py:85-88), as template positions
-        slot_pos = sorted((i for i, v in enumerate(tnodes) if low.w_rank[v]),
-                          key=sub.template.__getitem__)
-        radices = [3 if low.w_rank[tnodes[p]] >= 2 else 2 for p in slot_pos]
+        template = sub.template
         digits = _digits(int(sc.best_index), radices)
-        assignments = tuple((sub.template[p], _spec_for_digit(types, d))
-                            for p, d in zip(slot_pos, digits))
-        plan = types.CandidatePlan(sub, assignments, int(sc.best_index))
+        assignments = tuple((template[q], specs[d]) for q, d in zip(slot_pos, digits))
+        plan = CandidatePlan(sub, assignments, int(sc.best_index))
         routings, exits = [], []
         k = int(eoff[b])
         for i in range(T):
-            v = tnodes[i]
-            op_label = _OP_LABELS[int(low.op[v])]
-            pidx, sax, xax = int(node[e0 + i, 0]), int(node[e0 + i, 1]), int(node[e0 + i, 2])
+            scope, lab, pn, pc, obytes, prods = nodes[i]
+            pidx, sax, xax, _ = node_l[e0 + i]
             convs = []
-            for r in in_idx[in_off[v]:in_off[v + 1]].tolist():
-                if r not in members:
-                    continue
-                kind, axis = int(edge[k, 0]), int(edge[k, 1])
+            for pname, pbytes in prods:
+                kind, axis = edge_l[k]
                 k += 1
                 if kind:
-                    convs.append((names[r], _collective(types, kind, axis), int(low.act_bytes[r])))
-            out_coll = allreduce if types.pattern_collectives[op_label][pidx] == "allreduce" else identity
-            state = replica if sax < 0 else types.ShardSpec(types.ShardKind.SPLIT, sax)
-            routings.append(types.NodeRouting(sub.template[i], types.pattern_names[op_label][pidx],
-                                              tuple(convs), out_coll, int(low.act_bytes[v]), state))
+                    key = (kind, axis)
+                    c = colls.get(key)
+                    if c is None:
+                        c = colls[key] = _collective(types, kind, axis)
+                    convs.append((pname, c, pbytes))
+            out_coll = allreduce if pc[pidx] == "allreduce" else identity
+            state = replica if sax < 0 else splits[sax]
+            routings.append(NodeRouting(scope, pn[pidx], tuple(convs), out_coll, obytes, state))
             if xax >= 0:
-                exits.append((sub.template[i], _collective(types, 2, xax), int(low.act_bytes[v])))
+                key = (2, xax)
+                c = colls.get(key)
+                if c is None:
+                    c = colls[key] = _collective(types, 2, xax)
+                exits.append((scope, c, obytes))
         bbc = {_KIND_LABEL[j + 1]: int(X.bytes[j]) for j in range(4) if X.calls[j]}
         cost = types.CostReport(forward_comm=X.forward_comm, backward_comm=X.backward_comm,
-                                overlap_fraction=mesh.overlap_fraction, bytes_by_collective=bbc,
-                                collective_calls=int(X.collective_calls), flops=_flops(low, tnodes))
+                                overlap_fraction=overlap, bytes_by_collective=bbc,
+                                collective_calls=int(X.collective_calls), flops=flops)
         if sc.best_total == sc.best_total and cost.total != sc.best_total:  # NaN: no score to check
             raise BackendError(f"explain/score disagree on block {b}: {cost.total!r} != "
                                f"{sc.best_total!r}")
-        out.append(types.RoutedPlan(plan, tuple(routings), tuple(exits), cost))
+        out.append(RoutedPlan(plan, tuple(routings), tuple(exits), cost))
         e0 += T
     return out
 
 
 def _labels(assignments) -> dict:
     return {s: spec.label for s, spec in assignments}
+
+
+class _Search:
+    """A search in flight: routing tables built and the scoring launched on the
+    device (sp_score_launch); `collect` waits and assembles SubgraphResults.
+    Host work placed between the two overlaps the device search."""
+
+    def __init__(self, ses: Session, csr, mesh, mu: int, chunk_size: int, shard: int, n_shards: int,
+                 exchange: Optional[Callable]):
+        self.ses, self.mesh, self.mu, self.chunk_size = ses, mesh, mu, chunk_size
+        self.exchange = exchange
+        # pack_gradients raises BadConfig for mu > chunk only once a candidate is
+        # costed; build with a legal chunk to learn which error the reference hits first
+        self.bad_mu = mu > chunk_size
+        ta = time.perf_counter()
+        off, nodes = csr
+        self.tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu,
+                                         chunk_size if not self.bad_mu else mu)
+        ses.last_table_bytes = self.tables.nbytes
+        self.tables_ms = (time.perf_counter() - ta) * 1e3
+        try:
+            if self.tables.overflow:
+                raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")
+            self.explain = exchange is None and n_shards == 1
+            self.t_launch = time.perf_counter()
+            ses.backend.score_launch(self.tables, shard, n_shards, explain=self.explain)
+        except BaseException:
+            self.tables.close()
+            raise
+
+    def collect(self, graph, subgraphs: list, want_table: bool, types: TypeSet, prep=None) -> list:
+        ses, tables = self.ses, self.tables
+        try:
+            scores, detail = ses.backend.score_wait(tables)
+            if self.exchange is not None:
+                scores = self.exchange(scores)
+            tc = time.perf_counter()
+            for sc in scores:
+                if not sc.has_best:
+                    raise AssertionError("all-replica fallback must always route")
+                if self.bad_mu:
+                    raise BadConfig(f"fusion threshold {self.mu} exceeds chunk size {self.chunk_size}")
+            bests = routed_plans_all(ses, tables, subgraphs, scores, self.mesh, types, detail, prep)
+            LAST_PHASES.update(tables_ms=self.tables_ms, score_call_ms=(tc - self.t_launch) * 1e3,
+                               routes_ms=(time.perf_counter() - tc) * 1e3)
+            results = []
+            for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
+                table = []
+                if want_table:
+                    C = int(sc.candidates)
+                    _, totals = ses.backend.score_range(tables, b, 0, C, want_totals=True)
+                    for i in range(C):
+                        t = float(totals[i])
+                        plan = candidate_by_index(graph, sub, i, types)
+                        table.append([i, _labels(plan.assignments), None if math.isnan(t) else t])
+                results.append(types.SubgraphResult(sub, best, int(sc.candidates), int(sc.valid), table))
+            return results
+        finally:
+            tables.close()
 
 
 def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
@@ -342,47 +434,10 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
     ses = session or Session.open(graph)
     if not subgraphs:
         return []
-    off, nodes = csr if csr is not None else _templates_csr(ses.low, subgraphs)
-    # pack_gradients raises BadConfig for mu > chunk only once a candidate is
-    # costed; build with a legal chunk to learn which error the reference hits first
-    bad_mu = mu > chunk_size
-    ta = time.perf_counter()
-    tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, chunk_size if not bad_mu else mu)
-    ses.last_table_bytes = tables.nbytes
-    tb = time.perf_counter()
-    try:
-        if tables.overflow:
-            raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")
-        detail = None
-        if exchange is None and n_shards == 1:
-            scores, detail = ses.backend.search(tables)
-        else:
-            scores = ses.backend.score(tables, shard, n_shards)
-            if exchange is not None:
-                scores = exchange(scores)
-        tc = time.perf_counter()
-        for sc in scores:
-            if not sc.has_best:
-                raise AssertionError("all-replica fallback must always route")
-            if bad_mu:
-                raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
-        bests = routed_plans_all(ses, tables, subgraphs, scores, mesh, types, detail)
-        LAST_PHASES.update(tables_ms=(tb - ta) * 1e3, score_call_ms=(tc - tb) * 1e3,
-                           routes_ms=(time.perf_counter() - tc) * 1e3)
-        results = []
-        for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
-            table = []
-            if want_table:
-                C = int(sc.candidates)
-                _, totals = ses.backend.score_range(tables, b, 0, C, want_totals=True)
-                for i in range(C):
-                    t = float(totals[i])
-                    plan = candidate_by_index(graph, sub, i, types)
-                    table.append([i, _labels(plan.assignments), None if math.isnan(t) else t])
-            results.append(types.SubgraphResult(sub, best, int(sc.candidates), int(sc.valid), table))
-        return results
-    finally:
-        tables.close()
+    srch = _Search(ses, csr if csr is not None else _templates_csr(ses.low, subgraphs), mesh, mu,
+                   chunk_size, shard, n_shards, exchange)
+    prep = route_prep(ses, subgraphs, types)  # overlaps the device search
+    return srch.collect(graph, subgraphs, want_table, types, prep)
 
 
 def search_subgraph(graph, subgraph, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
@@ -419,35 +474,50 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     if min_duplicates < 1:
         raise BadConfig("min_duplicates must be >= 1")
     ba = ses.backend.fold(ses.dgraph, int(min_duplicates))
-    subs = subgraphs_from_blocks(ses.low, ba, types)
     t2 = time.perf_counter()
-    results = search_blocks(graph, subs, mesh, mu, chunk_size, want_table, session=ses,
-                            types=types, shard=shard, n_shards=n_shards, exchange=exchange,
-                            csr=ba.templates_csr())
+    n_blocks = ba.n_blocks
+    srch = _Search(ses, ba.templates_csr(), mesh, mu, chunk_size, shard, n_shards, exchange) \
+        if n_blocks else None
+    # host work that does not depend on the winners overlaps the device search:
+    # Subgraph objects, the static part of every RoutedPlan, and the member
+    # scopes that receive each block's weight labels (search.py:374-376)
     t3 = time.perf_counter()
-    assignments: dict = {}
+    subs = subgraphs_from_blocks(ses.low, ba, types)
+    prep = route_prep(ses, subs, types)
+    names = ses.low.names
+    members = ba.members
+    label_rows = []
+    for b, (sub, pb) in enumerate(zip(subs, prep)):
+        slot_pos = pb[0]
+        if not slot_pos:
+            label_rows.append(None)
+            continue
+        T = int(ba.block_T[b])
+        mo, R = int(ba.block_member_off[b]), sub.multiplicity
+        mat = members[mo: mo + R * T].reshape(R, T)[:, slot_pos]
+        label_rows.append((list(map(names.__getitem__, mat.ravel().tolist())), R))
+    t4 = time.perf_counter()
+    results = srch.collect(graph, subs, want_table, types, prep) if srch else []
+    t5 = time.perf_counter()
     total_cost = 0.0
     candidates = 0
     valid = 0
-    names = ses.low.names
-    members = ba.members
-    for b, (sub, res) in enumerate(zip(subs, results)):
+    keys, vals = [], []
+    for sub, res, lr in zip(subs, results, label_rows):
         candidates += res.candidates
         valid += res.valid
         total_cost += res.best.cost.total * sub.multiplicity
-        # every instance takes the template's labels (search.py:374-376); instance
-        # members come straight from the fold's member matrix
-        T = int(ba.block_T[b])
-        if not res.best.plan.assignments:
+        # every instance takes the template's labels in weight_nodes order
+        # (search.py:374-376); instance members come from the fold's member matrix
+        if lr is None:
             continue
-        pos = {s: i for i, s in enumerate(sub.template)}
-        cols = [pos[s] for s, _ in res.best.plan.assignments]
-        labels = [spec.label for _, spec in res.best.plan.assignments]
-        mo, R = int(ba.block_member_off[b]), sub.multiplicity
-        mat = members[mo: mo + R * T].reshape(R, T)[:, cols]
-        assignments.update(zip(map(names.__getitem__, mat.ravel().tolist()), labels * R))
+        flat, R = lr
+        keys.extend(flat)
+        vals.extend([spec.label for _, spec in res.best.plan.assignments] * R)
+    assignments = dict(zip(keys, vals))
     LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
-                       search_ms=(t3 - t2) * 1e3, assemble_ms=(time.perf_counter() - t3) * 1e3)
+                       launch_ms=(t3 - t2) * 1e3, overlap_host_ms=(t4 - t3) * 1e3,
+                       collect_ms=(t5 - t4) * 1e3, assemble_ms=(time.perf_counter() - t5) * 1e3)
     return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates,
                                 valid)
 

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import itertools
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 
@@ -24,7 +25,7 @@ MAX_RANK = 8  # SP_MAX_RANK
 @dataclass
 class LoweredGraph:
     names: list
-    index: dict
+    index_: Optional[dict]   # name -> row; built on first use of .index when None
     name_bytes: np.ndarray   # uint8
     name_off: np.ndarray     # int64 [n+1]
     topo_rank: np.ndarray    # int64 [n]
@@ -39,6 +40,12 @@ class LoweredGraph:
     in_off: np.ndarray       # int64 [n+1]
     in_idx: np.ndarray       # int32 [E]
     source: object = None    # the graph object this was lowered from
+
+    @property
+    def index(self) -> dict:
+        if self.index_ is None:
+            self.index_ = dict(zip(self.names, range(len(self.names))))
+        return self.index_
 
     @property
     def n_nodes(self) -> int:
@@ -100,11 +107,52 @@ def _shapes(shapes: list, n: int, what: str):
     return rank.astype(np.uint8), out, elems
 
 
-def lower(graph) -> LoweredGraph:
-    """Flatten a grouped graph (vectorised; cached on the graph object when possible)."""
+try:  # native walker of the object graph (csrc/lower_ext.c), built by `make`
+    from . import _lower as _native_lower
+except ImportError:  # pragma: no cover - unbuilt tree: the numpy restatement below
+    _native_lower = None
+
+
+def _lower_native(graph):
+    """lower() through csrc/lower_ext.c: one C pass over the GraphNode objects."""
+    (names, ascii_names, max_ar, max_wr, overflow, name_bytes, name_off, op, act_rank,
+     act_shape, act_bytes, w_rank, w_shape, w_bytes, w_train, in_off, in_idx) = \
+        _native_lower.lower_arrays(graph.topo_order, graph.nodes, _op_code, _width)
+    n = len(names)
+    if max_ar > MAX_RANK:
+        raise UnsupportedSearch(f"activation rank {max_ar} exceeds {MAX_RANK}")
+    if max_wr > MAX_RANK:
+        raise UnsupportedSearch(f"weight rank {max_wr} exceeds {MAX_RANK}")
+    if overflow:
+        raise UnsupportedSearch(f"{overflow} byte size beyond int64")
+    low = LoweredGraph(
+        names=names, index_=None, name_bytes=np.frombuffer(name_bytes, np.uint8),
+        name_off=np.frombuffer(name_off, np.int64), topo_rank=np.arange(n, dtype=np.int64),
+        op=np.frombuffer(op, np.uint8), act_rank=np.frombuffer(act_rank, np.uint8),
+        act_shape=np.frombuffer(act_shape, np.int64).reshape(n, MAX_RANK),
+        act_bytes=np.frombuffer(act_bytes, np.int64), w_rank=np.frombuffer(w_rank, np.uint8),
+        w_shape=np.frombuffer(w_shape, np.int64).reshape(n, MAX_RANK),
+        w_bytes=np.frombuffer(w_bytes, np.int64), w_trainable=np.frombuffer(w_train, np.uint8),
+        in_off=np.frombuffer(in_off, np.int64), in_idx=np.frombuffer(in_idx, np.int32), source=graph,
+    )
+    low.ascii = bool(ascii_names)
+    return low
+
+
+def lower(graph, native: bool = True) -> LoweredGraph:
+    """Flatten a grouped graph (cached on the graph object when possible).  The
+    native walker is used when built and the node table is a dict; the numpy
+    path below is its restatement (tests check both give identical arrays)."""
     cached = getattr(graph, "_sp_lowered", None)
     if isinstance(cached, LoweredGraph) and cached.source is graph:
         return cached
+    if native and _native_lower is not None and isinstance(graph.nodes, dict):
+        low = _lower_native(graph)
+        try:
+            graph._sp_lowered = low
+        except AttributeError:  # pragma: no cover - slotted graph types
+            pass
+        return low
     names = list(graph.topo_order)
     n = len(names)
     index = dict(zip(names, range(n)))
@@ -142,7 +190,7 @@ def lower(graph) -> LoweredGraph:
         np.cumsum(np.fromiter(map(len, encoded), np.int64, count=n), out=name_off[1:])
         name_bytes = np.frombuffer(b"".join(encoded), np.uint8).copy()
     low = LoweredGraph(
-        names=names, index=index, name_bytes=name_bytes, name_off=name_off,
+        names=names, index_=index, name_bytes=name_bytes, name_off=name_off,
         topo_rank=np.arange(n, dtype=np.int64), op=op, act_rank=act_rank,
         act_shape=act_shape, act_bytes=act_bytes, w_rank=w_rank, w_shape=w_shape,
         w_bytes=w_bytes, w_trainable=w_train, in_off=in_off, in_idx=in_idx, source=graph,

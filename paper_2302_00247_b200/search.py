@@ -261,21 +261,24 @@ _OP_LABELS = ("matmul", "elementwise", "layernorm", "softmax", "embedding", "res
               "output", "auxiliary", "collective")
 
 
-def route_prep(ses: Session, subgraphs: list, types: TypeSet = DEFAULT_TYPES) -> list:
+def route_prep(ses: Session, subgraphs: list, types: TypeSet = DEFAULT_TYPES, csr=None) -> list:
     """Winner-independent part of every block's RoutedPlan (computed while the
     device searches): template node indices, weight slots in weight_nodes order
     (names sorted, search.py:85-88) with their radices, and per template node
     (scope, op label, pattern names, pattern collectives, output bytes,
     internal producers as (scope, bytes) in GraphNode.inputs order)."""
     low = ses.low
-    index, names = low.index, low.names
+    names = low.names
     in_off, in_idx = low.in_off, low.in_idx
     op, w_rank, act_bytes = low.op, low.w_rank, low.act_bytes
     pnames, pcolls = types.pattern_names, types.pattern_collectives
+    if csr is None:
+        csr = _templates_csr(low, subgraphs)
+    toff, tnl = csr[0].tolist(), csr[1].tolist()
     out = []
-    for sub in subgraphs:
+    for b, sub in enumerate(subgraphs):
         template = sub.template
-        tnodes = [index[s] for s in template]
+        tnodes = tnl[toff[b]:toff[b + 1]]
         members = set(tnodes)
         wpos = [i for i, v in enumerate(tnodes) if w_rank[v]]
         slot_pos = sorted(wpos, key=template.__getitem__)
@@ -434,9 +437,10 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
     ses = session or Session.open(graph)
     if not subgraphs:
         return []
-    srch = _Search(ses, csr if csr is not None else _templates_csr(ses.low, subgraphs), mesh, mu,
-                   chunk_size, shard, n_shards, exchange)
-    prep = route_prep(ses, subgraphs, types)  # overlaps the device search
+    if csr is None:
+        csr = _templates_csr(ses.low, subgraphs)
+    srch = _Search(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange)
+    prep = route_prep(ses, subgraphs, types, csr)  # overlaps the device search
     return srch.collect(graph, subgraphs, want_table, types, prep)
 
 
@@ -476,14 +480,14 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     ba = ses.backend.fold(ses.dgraph, int(min_duplicates))
     t2 = time.perf_counter()
     n_blocks = ba.n_blocks
-    srch = _Search(ses, ba.templates_csr(), mesh, mu, chunk_size, shard, n_shards, exchange) \
-        if n_blocks else None
+    csr = ba.templates_csr()
+    srch = _Search(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange) if n_blocks else None
     # host work that does not depend on the winners overlaps the device search:
     # Subgraph objects, the static part of every RoutedPlan, and the member
     # scopes that receive each block's weight labels (search.py:374-376)
     t3 = time.perf_counter()
     subs = subgraphs_from_blocks(ses.low, ba, types)
-    prep = route_prep(ses, subs, types)
+    prep = route_prep(ses, subs, types, csr)
     names = ses.low.names
     members = ba.members
     label_rows = []

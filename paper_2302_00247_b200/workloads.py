@@ -211,7 +211,7 @@ def transformer_stack_lowered(layers: int, **kw):
     name_off = np.zeros(n + 1, np.int64)
     np.cumsum(lens, out=name_off[1:])
     return LoweredGraph(
-        names=names, index={}, name_bytes=np.frombuffer("".join(names).encode("ascii"), np.uint8).copy(),
+        names=names, index_=None, name_bytes=np.frombuffer("".join(names).encode("ascii"), np.uint8).copy(),
         name_off=name_off, topo_rank=np.arange(n, dtype=np.int64), op=tile(base.op),
         act_rank=tile(base.act_rank), act_shape=tile(base.act_shape), act_bytes=tile(base.act_bytes),
         w_rank=tile(base.w_rank), w_shape=tile(base.w_shape), w_bytes=tile(base.w_bytes),

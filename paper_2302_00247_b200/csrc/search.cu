@@ -1259,6 +1259,8 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
 // same work decomposition and argmin as k_score, with the lean FastNode walk.
 // Each lane carries its own candidate's digit word and advances it by 32 per
 // warp step (one carry-fixed add); the warp's remaining count is 32-bit.
+constexpr int PAIR_CHUNK = 512;  // candidates per warp chunk in the paired walk
+constexpr int PAIR_MAX_CHUNKS = ITEM_ITERS_MAX * THREADS / PAIR_CHUNK;
 #ifndef SP_PAIR_MIN_BLOCKS
 #define SP_PAIR_MIN_BLOCKS 4
 #endif
@@ -1273,6 +1275,11 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
   __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
   __shared__ uint64_t s_lane_add[32];
   __shared__ Biased s_bz;
+  // paired walk: warps pull PAIR_CHUNK-candidate chunks of the item from a
+  // shared cursor (no static per-warp spans: no barrier idling on skewed walks)
+  __shared__ uint64_t s_wbase;                       // biased digits of the item start
+  __shared__ uint64_t s_cenc[PAIR_MAX_CHUNKS];       // unbiased digits of c * PAIR_CHUNK
+  __shared__ uint32_t s_chunk;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   int64_t staged = -1;
@@ -1325,9 +1332,23 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
         }
         s_bz = z;
       }
+      if (PAIR && tid >= 64 && tid - 64 < PAIR_MAX_CHUNKS) {
+        uint64_t a = 0;  // unbiased digits of (tid - 64) * PAIR_CHUNK
+        uint64_t x = (uint64_t)(tid - 64) * PAIR_CHUNK;
+        for (int q = V - 1; q >= 0 && x; q--) {
+          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+          a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
+          x /= r;
+        }
+        s_cenc[tid - 64] = a;
+      }
       __syncthreads();
       patch_fast(smem, PAIR);
       staged = b;
+    }
+    if (PAIR && tid == 0) {
+      s_wbase = bencode(*(const BlobHeader*)smem, P.lo[b] + (item - P.item_base[b]) * P.item_cands);
+      s_chunk = 0;
     }
     __syncthreads();
     const Tabs S = tabs_of(smem);
@@ -1338,7 +1359,7 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
     const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
     unsigned long long best_t = ~0ULL, best_i = ~0ULL;
     uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
-    if (wlo < whi) {
+    if (PAIR ? ilo < ihi : wlo < whi) {
       // opaque copies keep the shared addresses in registers (ptxas would
       // otherwise re-derive the shared window base at every access)
       const uint32_t rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
@@ -1349,7 +1370,7 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
       const int T = H.T;
       uint32_t rem = (uint32_t)(whi - wlo);  // candidates left for this warp (<= item size)
       unsigned long long base = wlo;
-      uint64_t w = badd(bencode(H, wlo), s_lane_add[lane], s_bz.B);
+      uint64_t w = PAIR ? 0 : badd(bencode(H, wlo), s_lane_add[lane], s_bz.B);
       uint64_t best_w = 0;
       // valid candidate: total, key update (the reference index only breaks
       // exact (total, num_split) ties: keep the digits, convert once per item)
@@ -1367,15 +1388,24 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
         }
       };
       if (PAIR) {
+        const uint32_t cnt = (uint32_t)(ihi - ilo);
         while (true) {
-          const uint64_t wb = badd(w, s_bz.add32, s_bz.B);
-          double fa, fb;
-          const int v = walk_pair(rec0, T, w, wb, (uint32_t)lane < rem, (uint32_t)lane + 32 < rem, fa, fb, rb, sb);
-          if (v & 1) take(w, fa);
-          if (v & 2) take(wb, fb);
-          if (rem <= 64) break;
-          rem -= 64;
-          w = badd(w, s_bz.add64, s_bz.B);
+          uint32_t c = 0;
+          if (lane == 0) c = atomicAdd(&s_chunk, 1u);
+          c = __shfl_sync(0xffffffffu, c, 0);
+          if (c * PAIR_CHUNK >= cnt) break;
+          rem = min((uint32_t)PAIR_CHUNK, cnt - c * PAIR_CHUNK);
+          w = badd(badd(s_wbase, s_cenc[c], s_bz.B), s_lane_add[lane], s_bz.B);
+          while (true) {
+            const uint64_t wb = badd(w, s_bz.add32, s_bz.B);
+            double fa, fb;
+            const int v = walk_pair(rec0, T, w, wb, (uint32_t)lane < rem, (uint32_t)lane + 32 < rem, fa, fb, rb, sb);
+            if (v & 1) take(w, fa);
+            if (v & 2) take(wb, fb);
+            if (rem <= 64) break;
+            rem -= 64;
+            w = badd(w, s_bz.add64, s_bz.B);
+          }
         }
       }
       while (!PAIR) {

@@ -470,6 +470,35 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
             gc.enable()
 
 
+#: blocks with fewer candidates than this are scored in a first, separate launch
+SMALL_BLOCK_CANDIDATES = 1 << 16
+
+
+def _block_groups(low: LoweredGraph, csr) -> list:
+    """[(block ids, template csr)] in launch order: cheap blocks first, then the
+    rest; a single group when either side is empty."""
+    off, nodes = csr
+    nb = len(off) - 1
+    if nb == 0:
+        return []
+    wr = low.w_rank[nodes]
+    bits = np.where(wr >= 2, math.log2(3), np.where(wr == 1, 1.0, 0.0))
+    lg = np.add.reduceat(bits, off[:-1]) if len(nodes) else np.zeros(nb)
+    lg[off[1:] == off[:-1]] = 0.0
+    small = lg < math.log2(SMALL_BLOCK_CANDIDATES)
+    if small.all() or not small.any():
+        return [(list(range(nb)), csr)]
+    out = []
+    for mask in (small, ~small):
+        ids = np.nonzero(mask)[0]
+        T = off[ids + 1] - off[ids]
+        goff = np.zeros(len(ids) + 1, np.int64)
+        np.cumsum(T, out=goff[1:])
+        gather = np.repeat(off[ids] - goff[:-1], T) + np.arange(goff[-1])
+        out.append((ids.tolist(), (goff, np.ascontiguousarray(nodes[gather]))))
+    return out
+
+
 def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types, backend, session,
                  cache, shard, n_shards, exchange):
     t0 = time.perf_counter()
@@ -481,7 +510,11 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     t2 = time.perf_counter()
     n_blocks = ba.n_blocks
     csr = ba.templates_csr()
-    srch = _Search(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange) if n_blocks else None
+    # two launches when the blocks split into cheap and expensive ones: the
+    # cheap group's results (typically hundreds of residual singletons) are
+    # turned into RoutedPlans while the device still scores the expensive group
+    searches = [(_Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange), ids)
+                for ids, gcsr in _block_groups(ses.low, csr)]
     # host work that does not depend on the winners overlaps the device search:
     # Subgraph objects, the static part of every RoutedPlan, and the member
     # scopes that receive each block's weight labels (search.py:374-376)
@@ -501,7 +534,14 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
         mat = members[mo: mo + R * T].reshape(R, T)[:, slot_pos]
         label_rows.append((list(map(names.__getitem__, mat.ravel().tolist())), R))
     t4 = time.perf_counter()
-    results = srch.collect(graph, subs, want_table, types, prep) if srch else []
+    if len(searches) == 1:
+        results = searches[0][0].collect(graph, subs, want_table, types, prep)
+    else:
+        results = [None] * n_blocks
+        for srch, ids in searches:
+            got = srch.collect(graph, [subs[i] for i in ids], want_table, types, [prep[i] for i in ids])
+            for i, r in zip(ids, got):
+                results[i] = r
     t5 = time.perf_counter()
     total_cost = 0.0
     candidates = 0

@@ -286,6 +286,27 @@ def measure(be, g, mesh, steps, warmup, rank, world, exchange, flush, barrier, s
             "clocks": sampler.summary() if sampler else None}
 
 
+#: committed `ncu --set full` summary of the dominant kernel (tools/summarize_ncu.py)
+PROFILE = "r1_k_score_c5_walk.txt"
+_UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "%": 1, "ms": 1, "cycle": 1}
+
+
+def _profile_values(path: str) -> dict:
+    """metric -> value (bytes scaled to B) from a profiles/ summary file."""
+    vals = {}
+    if not os.path.exists(path):
+        return vals
+    for ln in open(path):
+        if " = " in ln and not ln.startswith("#"):
+            k, v = ln.split(" = ", 1)
+            parts = v.split()
+            try:
+                vals[k.strip()] = float(parts[0]) * _UNITS.get(parts[1] if len(parts) > 1 else "", 1)
+            except ValueError:
+                pass
+    return vals
+
+
 def _maxsum(vals, world):
     import torch
     import torch.distributed as dist
@@ -364,20 +385,20 @@ def run_ours(args) -> None:
     # committed ncu capture of the same kernel x the live kernel rate, against
     # 148 SMs x 4 schedulers x the SM clock sampled during the timed region
     issue = None
-    prof = os.path.join(ROOT, "profiles", "r1_k_score_c5_walk.txt")
-    if args.workload == "c5" and os.path.exists(prof) and main["clocks"] and main["clocks"]["sm_mhz"]:
-        vals = {}
-        for ln in open(prof):
-            if " = " in ln and not ln.startswith("#"):
-                k, v = ln.split(" = ", 1)
-                vals[k.strip()] = float(v.split()[0])
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", PROFILE)
+    vals = _profile_values(prof) if args.workload == "c5" else {}
+    if "dram__bytes_read.sum" in vals and "dram__bytes_write.sum" in vals:
+        # one `ncu --set full` capture of the same kernel (one launch = one step)
+        traffic = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    if vals and main["clocks"] and main["clocks"]["sm_mhz"]:
         wipc = vals["smsp__inst_executed.sum"] / cands
         peak_issue = 148 * 4 * main["clocks"]["sm_mhz"] * 1e6
         issue = {"bound": "issue", "unit": "warp-inst/s", "warp_inst_per_candidate": wipc,
                  "achieved": wipc * kernel_rate, "peak": peak_issue,
                  "frac": wipc * kernel_rate / peak_issue,
                  "ncu_issue_active_frac": vals["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100,
-                 "source": "profiles/r1_k_score_c5_walk.txt (instruction count) x live kernel time"}
+                 "source": f"profiles/{PROFILE} (instruction count) x live kernel time"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -402,7 +423,7 @@ def run_ours(args) -> None:
         "kernel_rate": {"k_score_candidates_per_s_per_gpu": kernel_rate,
                         "valid_plans_per_s": walked_valid * args.steps / (total_ms / 1000.0)},
         "roofline": {"kernel": "k_score", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                      "note": "no per-candidate HBM input: algorithmic bytes are the staged "
                              "routing tables + per-item records, so the kernel is SM-issue-bound; "
                              "issue-slot utilisation is in profiles/ (DESIGN.md section 3)"},

@@ -471,7 +471,11 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
 
 
 #: blocks with fewer candidates than this are scored in a first, separate launch
+#: (when there are at least SPLIT_MIN_SMALL_BLOCKS of them and the remaining
+#: blocks hold at least SPLIT_MIN_BIG_CANDIDATES candidates)
 SMALL_BLOCK_CANDIDATES = 1 << 16
+SPLIT_MIN_SMALL_BLOCKS = 64
+SPLIT_MIN_BIG_CANDIDATES = float(1 << 26)
 
 
 def _block_groups(low: LoweredGraph, csr) -> list:
@@ -486,7 +490,10 @@ def _block_groups(low: LoweredGraph, csr) -> list:
     lg = np.add.reduceat(bits, off[:-1]) if len(nodes) else np.zeros(nb)
     lg[off[1:] == off[:-1]] = 0.0
     small = lg < math.log2(SMALL_BLOCK_CANDIDATES)
-    if small.all() or not small.any():
+    # a second launch pays off only when there are many cheap blocks to
+    # explain and enough expensive work to hide them behind
+    big_work = float(np.sum(np.exp2(np.minimum(lg[~small], 62.0))))
+    if small.sum() < SPLIT_MIN_SMALL_BLOCKS or big_work < SPLIT_MIN_BIG_CANDIDATES:
         return [(list(range(nb)), csr)]
     out = []
     for mask in (small, ~small):

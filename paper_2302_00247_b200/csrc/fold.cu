@@ -635,17 +635,11 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
   dg->h_op.assign(g->op, g->op + n);
   dg->h_w_rank.assign(g->w_rank, g->w_rank + n);
   int32_t maxd = 1;
-  {
+  for (int64_t i = 0; i < n; i++) {  // depth = 1 + number of '/' (vectorisable count per name)
+    const uint8_t* a = g->name_bytes + g->name_off[i];
+    const int64_t L = g->name_off[i + 1] - g->name_off[i];
     int32_t d = 1;
-    int64_t node = 0;
-    for (int64_t k = 0; k < nb; k++) {
-      while (node < n && k >= g->name_off[node + 1]) {
-        maxd = std::max(maxd, d);
-        d = 1;
-        node++;
-      }
-      d += g->name_bytes[k] == '/';
-    }
+    for (int64_t k = 0; k < L; k++) d += a[k] == '/';
     maxd = std::max(maxd, d);
   }
   dg->max_depth = maxd;

@@ -42,6 +42,13 @@ int sp_ctx_create(int device, sp_ctx** out) {
     SP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     ctx->smem_optin = (size_t)optin;
     SP_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    // every scratch buffer is stream-ordered (cudaMallocAsync): keep freed
+    // memory in the device pool instead of returning it at each sync, so the
+    // per-call buffers of fold / tables / score are re-used, not re-mapped
+    cudaMemPool_t pool;
+    SP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    SP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     for (auto& e : ctx->ev) SP_CUDA(cudaEventCreate(&e));
     for (auto& e : ctx->timer) SP_CUDA(cudaEventCreate(&e));
   });

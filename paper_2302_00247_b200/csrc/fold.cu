@@ -28,6 +28,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 
@@ -712,6 +714,282 @@ __global__ void k_gather(const int32_t* __restrict__ idx, int64_t m, const T* __
     dst[i] = src[idx[i]];
 }
 
+// ---------------------------------------------------------------------------
+// Device-side block assembly (accept, pruning.py:136-148) for the multi-kernel
+// fold: every accepted class of a level becomes one block whose instances are
+// its groups ordered by prefix string and whose template is the first of them,
+// members in the template's topological order.  Siblings of one class share
+// their parent prefix, so ordering the instance prefixes is ordering their
+// last path components: a radix sort on (class, first 16 component bytes),
+// exact unless two components of one class agree on 16 bytes (then the tie
+// flag sends the whole fold to the host ordering below).
+
+__device__ __forceinline__ uint64_t be_load8(const uint8_t* p, int64_t len) {
+  uint64_t k = 0;
+  for (int b = 0; b < 8; b++) k = (k << 8) | (b < len ? (uint64_t)p[b] : 0ULL);
+  return k;
+}
+
+__global__ void k_acc_keys(const int32_t* __restrict__ accG, int64_t Ga, const int32_t* __restrict__ sorted,
+                           const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass,
+                           const int32_t* __restrict__ pend, int32_t D, int32_t dd,
+                           const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
+                           uint64_t* __restrict__ k0, uint64_t* __restrict__ k1, uint32_t* __restrict__ kc,
+                           uint8_t* __restrict__ longc, int32_t* __restrict__ idx) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < Ga; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = accG[j];
+    const int32_t h = sorted[gstart[g]];
+    const int64_t pe = pend[(int64_t)h * D + dd];
+    const int64_t ps = dd > 0 ? (int64_t)pend[(int64_t)h * D + dd - 1] + 1 : 0;
+    const int64_t len = pe > ps ? pe - ps : 0;
+    const uint8_t* c = names + name_off[h] + ps;
+    k0[j] = be_load8(c, len);
+    k1[j] = be_load8(c + 8, len - 8);
+    kc[j] = (uint32_t)gclass[g];
+    longc[j] = len > 16;
+    idx[j] = (int32_t)j;
+  }
+}
+
+template <class T>
+__global__ void k_gather_idx(const int32_t* __restrict__ idx, int64_t m, const T* __restrict__ src,
+                             T* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+// class heads over the sorted accepted groups + tie detection
+__global__ void k_acc_heads(const uint32_t* __restrict__ kc, const uint64_t* __restrict__ k0s,
+                            const uint64_t* __restrict__ k1s, int64_t Ga, int32_t* __restrict__ head,
+                            int32_t* __restrict__ tie) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < Ga; p += (int64_t)gridDim.x * blockDim.x) {
+    const bool h = p == 0 || kc[p] != kc[p - 1];
+    head[p] = h;
+    if (!h && k0s[p] == k0s[p - 1] && k1s[p] == k1s[p - 1]) atomicExch(tie, 1);
+  }
+}
+
+// per class: start position, R, T, template group
+__global__ void k_acc_classes(const int32_t* __restrict__ head_scan, int64_t Ga, const int32_t* __restrict__ order,
+                              const int32_t* __restrict__ accG, const int32_t* __restrict__ gstart, int64_t nG,
+                              int64_t nA, int32_t* __restrict__ cls_start, int32_t* __restrict__ cls_R,
+                              int32_t* __restrict__ cls_T) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < Ga; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = head_scan[p] - 1;
+    const bool first = p == 0 || head_scan[p - 1] != head_scan[p];
+    const bool last = p + 1 == Ga || head_scan[p + 1] != head_scan[p];
+    if (first) {
+      cls_start[k] = (int32_t)p;
+      const int32_t g = accG[order[p]];
+      cls_T[k] = (int32_t)((g + 1 < nG ? gstart[g + 1] : nA) - gstart[g]);
+    }
+    if (last) cls_R[k] = (int32_t)(p + 1);  // run end (exclusive); R = end - start in k_acc_fix
+  }
+}
+
+__global__ void k_acc_fix(int64_t K, const int32_t* __restrict__ cls_start, int32_t* __restrict__ cls_R,
+                          const int32_t* __restrict__ cls_T, int64_t* __restrict__ cls_RT, int64_t* __restrict__ cls_Tl) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    cls_R[k] -= cls_start[k];
+    cls_RT[k] = (int64_t)cls_R[k] * cls_T[k];
+    cls_Tl[k] = cls_T[k];
+  }
+}
+
+__device__ __forceinline__ int64_t upper_off(const int64_t* off, int64_t K, int64_t e) {
+  // largest k with off[k] <= e (off exclusive scan, off[0] = 0)
+  int64_t lo = 0, hi = K;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) / 2;
+    if (off[mid] <= e) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// canonical keys: (class, topo rank of the template group's member) -> position in group
+__global__ void k_canon_keys(int64_t total, int64_t K, const int64_t* __restrict__ coff,
+                             const int32_t* __restrict__ cls_start, const int32_t* __restrict__ order,
+                             const int32_t* __restrict__ accG, const int32_t* __restrict__ gstart,
+                             const int32_t* __restrict__ sorted, const int64_t* __restrict__ topo,
+                             uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = upper_off(coff, K, e);
+    const int64_t t = e - coff[k];
+    const int32_t g = accG[order[cls_start[k]]];
+    key[e] = ((uint64_t)k << 32) | (uint64_t)(uint32_t)topo[sorted[gstart[g] + t]];
+    val[e] = (int32_t)t;
+  }
+}
+
+__global__ void k_acc_members(int64_t total, int64_t K, const int64_t* __restrict__ moff,
+                              const int64_t* __restrict__ coff, const int32_t* __restrict__ cls_start,
+                              const int32_t* __restrict__ cls_T, const int32_t* __restrict__ order,
+                              const int32_t* __restrict__ accG, const int32_t* __restrict__ gstart,
+                              const int32_t* __restrict__ sorted, const int32_t* __restrict__ canon,
+                              int32_t* __restrict__ members) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = upper_off(moff, K, e);
+    const int64_t local = e - moff[k];
+    const int64_t T = cls_T[k];
+    const int64_t i = local / T, t = local - i * T;
+    const int32_t g = accG[order[cls_start[k] + i]];
+    members[e] = sorted[gstart[g] + canon[coff[k] + t]];
+  }
+}
+
+__global__ void k_acc_insts(int64_t Ga, const int32_t* __restrict__ order, const int32_t* __restrict__ accG,
+                            const int32_t* __restrict__ gstart, const int32_t* __restrict__ sorted,
+                            const int32_t* __restrict__ pend, int32_t D, int32_t dd, int32_t* __restrict__ inode,
+                            int32_t* __restrict__ ilen) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < Ga; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t h = sorted[gstart[accG[order[p]]]];
+    inode[p] = h;
+    ilen[p] = pend[(int64_t)h * D + dd];
+  }
+}
+
+// One level's blocks, still on the device (downloaded once after the loop).
+struct LevelBlocks {
+  int64_t K = 0, Ga = 0, M = 0;
+  DevBuf<int32_t> cls_T, cls_R, cls_start, inode, ilen, members;
+};
+
+// SP_FOLD_TRACE=1: host-side phase times of the multi-kernel fold on stderr
+struct FoldTrace {
+  bool on = getenv("SP_FOLD_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fold] %-28s %9.3f ms (total %9.3f)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
+
+template <class T>
+static T d2h_scalar(const T* p, cudaStream_t s) {
+  T v{};
+  g_d2h_bytes += (int64_t)sizeof(T);
+  SP_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+// Accepted classes of one level -> blocks (device arrays); sets *tie when two
+// instance components of one class agree on their first 16 bytes.
+static void level_blocks(sp_ctx* ctx, sp_dgraph* dg, int32_t dd, int64_t nA, int64_t nG, const int32_t* sorted,
+                         const int32_t* gstart, const int32_t* gclass, const uint8_t* gaccept, const int32_t* pend,
+                         int32_t* d_tie, LevelBlocks& L) {
+  cudaStream_t s = ctx->stream;
+  const int sms = ctx->sm_count;
+  const int32_t D = dg->max_depth;
+  DevBuf<int32_t> iota, accG, nsel;
+  iota.alloc(nG, s);
+  accG.alloc(nG, s);
+  nsel.alloc(1, s);
+  SP_LAUNCH(ctx, k_iota, grid_for(nG, sms), 256, 0, s, iota.p, nG);
+  DevBuf<uint8_t> tmp;
+  size_t tb = 0;
+  ctx->cub_calls++;
+  SP_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, gaccept, accG.p, nsel.p, (int)nG, s));
+  tmp.alloc(tb, s);
+  SP_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, iota.p, gaccept, accG.p, nsel.p, (int)nG, s));
+  const int64_t Ga = d2h_scalar(nsel.p, s);
+  L.Ga = Ga;
+  if (Ga == 0) return;
+  DevBuf<uint64_t> k0, k1, k0s, k1s, t64;
+  DevBuf<uint32_t> kc, kcs, t32;
+  DevBuf<uint8_t> longc;
+  DevBuf<int32_t> idx, o1, o2;
+  k0.alloc(Ga, s); k1.alloc(Ga, s); k0s.alloc(Ga, s); k1s.alloc(Ga, s); t64.alloc(Ga, s);
+  kc.alloc(Ga, s); kcs.alloc(Ga, s); t32.alloc(Ga, s);
+  longc.alloc(Ga, s);
+  idx.alloc(Ga, s); o1.alloc(Ga, s); o2.alloc(Ga, s);
+  const int gA = grid_for(Ga, sms);
+  SP_LAUNCH(ctx, k_acc_keys, gA, 256, 0, s, accG.p, Ga, sorted, gstart, gclass, pend, D, dd, dg->name_off.p,
+            dg->names.p, k0.p, k1.p, kc.p, longc.p, idx.p);
+  // LSD: component bytes 8..15, then 0..7, then class (stable)
+  auto sort_pairs = [&](auto* kin, auto* kout, const int32_t* vin, int32_t* vout, int bits) {
+    size_t b = 0;
+    ctx->cub_calls++;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, kin, kout, vin, vout, (int)Ga, 0, bits, s));
+    if (b > tmp.n) tmp.alloc(b, s);
+    b = tmp.n;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, b, kin, kout, vin, vout, (int)Ga, 0, bits, s));
+  };
+  sort_pairs(k1.p, k1s.p, idx.p, o1.p, 64);
+  SP_LAUNCH(ctx, k_gather_idx<uint64_t>, gA, 256, 0, s, o1.p, Ga, k0.p, t64.p);
+  sort_pairs(t64.p, k0s.p, o1.p, o2.p, 64);
+  SP_LAUNCH(ctx, k_gather_idx<uint32_t>, gA, 256, 0, s, o2.p, Ga, kc.p, t32.p);
+  sort_pairs(t32.p, kcs.p, o2.p, o1.p, 32);
+  int32_t* order = o1.p;  // sorted position -> index into accG
+  // keys in final order for the tie check
+  SP_LAUNCH(ctx, k_gather_idx<uint64_t>, gA, 256, 0, s, order, Ga, k0.p, k0s.p);
+  SP_LAUNCH(ctx, k_gather_idx<uint64_t>, gA, 256, 0, s, order, Ga, k1.p, k1s.p);
+  DevBuf<int32_t> head;
+  head.alloc(Ga, s);
+  SP_LAUNCH(ctx, k_acc_heads, gA, 256, 0, s, kcs.p, k0s.p, k1s.p, Ga, head.p, d_tie);
+  {
+    size_t b = 0;
+    ctx->cub_calls++;
+    SP_CUDA(cub::DeviceScan::InclusiveSum(nullptr, b, head.p, head.p, (int)Ga, s));
+    if (b > tmp.n) tmp.alloc(b, s);
+    b = tmp.n;
+    SP_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, b, head.p, head.p, (int)Ga, s));
+  }
+  const int64_t K = d2h_scalar(head.p + Ga - 1, s);
+  L.K = K;
+  L.cls_T.alloc(K, s);
+  L.cls_R.alloc(K, s);
+  L.cls_start.alloc(K, s);
+  DevBuf<int64_t> moff, coff;
+  moff.alloc(K + 1, s);
+  coff.alloc(K + 1, s);
+  SP_LAUNCH(ctx, k_acc_classes, gA, 256, 0, s, head.p, Ga, order, accG.p, gstart, nG, nA, L.cls_start.p, L.cls_R.p,
+            L.cls_T.p);
+  SP_CUDA(cudaMemsetAsync(moff.p + K, 0, sizeof(int64_t), s));
+  SP_CUDA(cudaMemsetAsync(coff.p + K, 0, sizeof(int64_t), s));
+  SP_LAUNCH(ctx, k_acc_fix, grid_for(K, sms), 256, 0, s, K, L.cls_start.p, L.cls_R.p, L.cls_T.p, moff.p, coff.p);
+  for (DevBuf<int64_t>* o : {&moff, &coff}) {
+    size_t b = 0;
+    ctx->cub_calls++;
+    SP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, o->p, o->p, (int)(K + 1), s));
+    if (b > tmp.n) tmp.alloc(b, s);
+    b = tmp.n;
+    SP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, b, o->p, o->p, (int)(K + 1), s));
+  }
+  int64_t tot[2];
+  g_d2h_bytes += 16;
+  SP_CUDA(cudaMemcpyAsync(&tot[0], moff.p + K, 8, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(&tot[1], coff.p + K, 8, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  const int64_t M = tot[0], CT = tot[1];
+  L.M = M;
+  // canonical order of the template members: sort (class, topo rank)
+  DevBuf<uint64_t> ck, cks;
+  DevBuf<int32_t> cv, canon;
+  ck.alloc(CT, s); cks.alloc(CT, s); cv.alloc(CT, s); canon.alloc(CT, s);
+  SP_LAUNCH(ctx, k_canon_keys, grid_for(CT, sms), 256, 0, s, CT, K, coff.p, L.cls_start.p, order, accG.p, gstart,
+            sorted, dg->topo.p, ck.p, cv.p);
+  {
+    size_t b = 0;
+    ctx->cub_calls++;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, ck.p, cks.p, cv.p, canon.p, (int)CT, 0, 64, s));
+    if (b > tmp.n) tmp.alloc(b, s);
+    b = tmp.n;
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, b, ck.p, cks.p, cv.p, canon.p, (int)CT, 0, 64, s));
+  }
+  L.members.alloc(M, s);
+  L.inode.alloc(Ga, s);
+  L.ilen.alloc(Ga, s);
+  SP_LAUNCH(ctx, k_acc_members, grid_for(M, sms), 256, 0, s, M, K, moff.p, coff.p, L.cls_start.p, L.cls_T.p, order,
+            accG.p, gstart, sorted, canon.p, L.members.p);
+  SP_LAUNCH(ctx, k_acc_insts, gA, 256, 0, s, Ga, order, accG.p, gstart, sorted, pend, D, dd, L.inode.p, L.ilen.p);
+}
+
 // Host ordering: the string-order decisions of pruning.py:136-148, 200 over
 // the device partition (instances and blocks by prefix string, template by
 // topological rank).  O(accepted groups log) string compares.
@@ -801,6 +1079,102 @@ static void fold_finalize(sp_dgraph* dg, const std::vector<LevelOut>& levels, co
   if ((int64_t)out->members.size() != n) throw Error(SP_ERR_CUDA, "fold did not cover every node exactly once");
   sp_blocks& v = out->view;
   v.n_blocks = (int64_t)out->block_T.size();
+  v.n_instances = (int64_t)out->inst_prefix_node.size();
+  v.n_members = (int64_t)out->members.size();
+  v.block_T = out->block_T.data();
+  v.block_inst_off = out->block_inst_off.data();
+  v.block_member_off = out->block_member_off.data();
+  v.inst_prefix_node = out->inst_prefix_node.data();
+  v.inst_prefix_len = out->inst_prefix_len.data();
+  v.members = out->members.data();
+}
+
+// Blocks from the device-side assembly: download each level's blocks and the
+// residual singletons, order all blocks by template prefix string
+// (pruning.py:200) and concatenate.  Host work is O(blocks log blocks) string
+// compares plus one pass over the members.
+static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, const std::vector<int32_t>& resid,
+                                 cudaStream_t s, sp_fold* out) {
+  const uint8_t* names = dg->h_names.data();
+  const int64_t* noff = dg->h_name_off.data();
+  struct Host {
+    std::vector<int32_t> T, R, start, inode, ilen, members;
+    std::vector<int64_t> moff;
+  };
+  std::vector<Host> h(lv.size());
+  for (size_t l = 0; l < lv.size(); l++) {
+    LevelBlocks& L = lv[l];
+    Host& H = h[l];
+    if (!L.K) continue;
+    H.T.resize(L.K);
+    H.R.resize(L.K);
+    H.start.resize(L.K);
+    H.inode.resize(L.Ga);
+    H.ilen.resize(L.Ga);
+    H.members.resize(L.M);
+    L.cls_T.download(H.T.data(), L.K, s);
+    L.cls_R.download(H.R.data(), L.K, s);
+    L.cls_start.download(H.start.data(), L.K, s);
+    L.inode.download(H.inode.data(), L.Ga, s);
+    L.ilen.download(H.ilen.data(), L.Ga, s);
+    L.members.download(H.members.data(), L.M, s);
+  }
+  SP_CUDA(cudaStreamSynchronize(s));
+  struct Ref {
+    int64_t pnode, plen;
+    int32_t level;  // -1: residual singleton
+    int32_t k;      // class (or residual node)
+  };
+  std::vector<Ref> blocks;
+  for (size_t l = 0; l < lv.size(); l++) {
+    Host& H = h[l];
+    H.moff.assign(H.T.size() + 1, 0);
+    for (size_t k = 0; k < H.T.size(); k++) {
+      H.moff[k + 1] = H.moff[k] + (int64_t)H.R[k] * H.T[k];
+      const int32_t p0 = H.start[k];
+      blocks.push_back({H.inode[p0], H.ilen[p0], (int32_t)l, (int32_t)k});
+    }
+  }
+  for (int32_t v : resid) blocks.push_back({v, noff[v + 1] - noff[v], -1, v});
+  std::sort(blocks.begin(), blocks.end(), [&](const Ref& a, const Ref& b) {
+    return strcmp_py(names + noff[a.pnode], a.plen, names + noff[b.pnode], b.plen) < 0;
+  });
+  const int64_t nb = (int64_t)blocks.size();
+  out->block_T.resize(nb);
+  out->block_inst_off.assign(nb + 1, 0);
+  out->block_member_off.assign(nb + 1, 0);
+  for (int64_t b = 0; b < nb; b++) {
+    const Ref& r = blocks[b];
+    const int64_t T = r.level < 0 ? 1 : h[r.level].T[r.k];
+    const int64_t R = r.level < 0 ? 1 : h[r.level].R[r.k];
+    out->block_T[b] = T;
+    out->block_inst_off[b + 1] = out->block_inst_off[b] + R;
+    out->block_member_off[b + 1] = out->block_member_off[b] + R * T;
+  }
+  if (out->block_member_off[nb] != dg->n) throw Error(SP_ERR_CUDA, "fold did not cover every node exactly once");
+  out->inst_prefix_node.resize(out->block_inst_off[nb]);
+  out->inst_prefix_len.resize(out->block_inst_off[nb]);
+  out->members.resize(dg->n);
+  for (int64_t b = 0; b < nb; b++) {
+    const Ref& r = blocks[b];
+    const int64_t io = out->block_inst_off[b], mo = out->block_member_off[b];
+    if (r.level < 0) {
+      out->inst_prefix_node[io] = r.pnode;
+      out->inst_prefix_len[io] = r.plen;
+      out->members[mo] = r.k;
+      continue;
+    }
+    const Host& H = h[r.level];
+    const int64_t R = H.R[r.k], p0 = H.start[r.k];
+    for (int64_t i = 0; i < R; i++) {
+      out->inst_prefix_node[io + i] = H.inode[p0 + i];
+      out->inst_prefix_len[io + i] = H.ilen[p0 + i];
+    }
+    std::memcpy(out->members.data() + mo, H.members.data() + H.moff[r.k],
+                sizeof(int32_t) * (size_t)(H.moff[r.k + 1] - H.moff[r.k]));
+  }
+  sp_blocks& v = out->view;
+  v.n_blocks = nb;
   v.n_instances = (int64_t)out->inst_prefix_node.size();
   v.n_members = (int64_t)out->members.size();
   v.block_T = out->block_T.data();
@@ -918,6 +1292,7 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   const int sms = ctx->sm_count;
   const int64_t n = dg->n;
   const int32_t D = dg->max_depth;
+  FoldTrace tr;
 
   DevBuf<int32_t> depth, maxd, pend, act, sorted1, sorted2, gidv, gstart, pos, gparent, gclass, corder,
       corder2, corder3, cid, cstart, collision, nsel;
@@ -972,6 +1347,7 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   st_cstart.alloc(st_cap, s);
   st_gaccept.alloc(st_cap, s);
 
+  tr.mark("alloc");
   SP_CUDA(cudaEventRecord(ctx->ev[6], s));
   SP_CUDA(cudaMemsetAsync(maxd.p, 0, sizeof(int32_t), s));
   SP_LAUNCH(ctx, k_depth, grid_for(n, sms), 256, 0, s, dg->name_off.p, dg->names.p, n, depth.p, maxd.p);
@@ -1010,6 +1386,12 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     if (used) SP_CUDA(cudaMemcpyAsync(bigger.p, buf.p, used * sizeof(T), cudaMemcpyDeviceToDevice, s));
     buf = std::move(bigger);
   };
+  // device-side block assembly (SP_FOLD_HOST_ORDER=1: the host ordering of fold_finalize)
+  const bool device_blocks = getenv("SP_FOLD_HOST_ORDER") == nullptr;
+  std::vector<LevelBlocks> lblocks;
+  DevBuf<int32_t> tie;
+  tie.alloc(1, s);
+  SP_CUDA(cudaMemsetAsync(tie.p, 0, sizeof(int32_t), s));
   int64_t nA = n;
   for (int32_t level = 1; nA > 0; level++) {
     if (level > D) throw Error(SP_ERR_CUDA, "fold did not terminate");
@@ -1068,6 +1450,13 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     // 5. accept / residual / descend
     SP_LAUNCH(ctx, k_accept, g1, 256, 0, s, sorted2.p, gidv.p, nA, nC, nG, gclass.p, cstart.p, depth.p, level, min_dup,
                                 gparent.p, next_flag.p, residual.p, gaccept.p);
+    tr.mark("level: group/class/verify");
+    // accepted classes -> blocks, assembled on the device
+    if (device_blocks) {
+      lblocks.emplace_back();
+      level_blocks(ctx, dg, dd, nA, nG, sorted2.p, gstart.p, gclass.p, gaccept.p, pend.p, tie.p, lblocks.back());
+      tr.mark("level: blocks");
+    }
     reserve(st_sorted, used_a, nA);
     reserve(st_gstart, used_g, nG);
     reserve(st_corder, used_g, nG);
@@ -1104,6 +1493,28 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   }
   *collided = coll_h != 0;
   if (*collided) return;
+  tr.mark("loop end");
+  if (device_blocks && d2h_scalar(tie.p, s) == 0) {
+    // residual singletons, compacted on the device
+    DevBuf<int32_t> iota, rlist, nsel2;
+    iota.alloc(n, s);
+    rlist.alloc(n, s);
+    nsel2.alloc(1, s);
+    SP_LAUNCH(ctx, k_iota, grid_for(n, sms), 256, 0, s, iota.p, n);
+    size_t tb = 0;
+    ctx->cub_calls++;
+    SP_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, residual.p, rlist.p, nsel2.p, (int)n, s));
+    DevBuf<uint8_t> tmp2;
+    tmp2.alloc(tb, s);
+    SP_CUDA(cub::DeviceSelect::Flagged(tmp2.p, tb, iota.p, residual.p, rlist.p, nsel2.p, (int)n, s));
+    const int64_t nr = d2h_scalar(nsel2.p, s);
+    std::vector<int32_t> resid(nr);
+    rlist.download(resid.data(), nr, s);
+    tr.mark("residuals");
+    fold_finalize_blocks(dg, lblocks, resid, s, out);
+    tr.mark("finalize");
+    return;
+  }
   std::vector<uint8_t> resid_h(n);
   std::vector<int32_t> pend_h((size_t)n * D);
   std::vector<int32_t> h_sorted(used_a), h_gstart(used_g), h_corder(used_g), h_cstart(used_c);

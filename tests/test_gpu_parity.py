@@ -224,6 +224,61 @@ def test_fold_stress_vs_reference_hash(backend, idx):
     assert hashlib.sha256(canon(doc).encode()).hexdigest() == fs["prune_sha"]
 
 
+def _long_component_graph(reps: int = 7):
+    """Sibling instances whose last path components agree on their first 16+ bytes
+    (exercises the device ordering's tie fallback to the host string sort)."""
+    from paper_2302_00247_b200.ir import GraphNode, GroupedGraph, OpKind, TensorSpec
+
+    nodes, prev = [], None
+    for j in [3, 11, 0, 5, 2, 10, 1][:reps]:
+        pre = f"net/transformer_layer_block_{j:04d}"
+        a = GraphNode(f"{pre}/proj", OpKind.MATMUL, (prev,) if prev else (), TensorSpec((8, 16)),
+                      TensorSpec((16, 16), trainable=True))
+        b = GraphNode(f"{pre}/act", OpKind.ELEMENTWISE, (a.scope,), TensorSpec((8, 16)))
+        nodes += [a, b]
+        prev = b.scope
+    return GroupedGraph(nodes)
+
+
+@pytest.mark.parametrize("host_order", [False, True])
+def test_fold_long_components_tie_fallback(backend, host_order, monkeypatch):
+    """Instance prefixes that tie on 16 component bytes: the fold still orders
+    them like the reference's string sort (host fallback), on both orderings."""
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays, to_prune_doc
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+
+    monkeypatch.setenv("SP_FOLD_MULTI", "1")
+    if host_order:
+        monkeypatch.setenv("SP_FOLD_HOST_ORDER", "1")
+    low = lower(_long_component_graph())
+    ses = Session.open(low, backend)
+    for md in (1, 2):
+        ba = fold_blocks(low, md, session=ses)
+        ob = BlockArrays.from_dict(oracle.prune(low, md))
+        assert to_prune_doc(low, ba) == to_prune_doc(low, ob)
+
+
+@pytest.mark.parametrize("seed", range(0, 12, 3))
+def test_multi_kernel_fold_host_order_vs_oracle(backend, seed, monkeypatch):
+    """The host-ordering fallback of the multi-kernel fold stays exact."""
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays, to_prune_doc
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    monkeypatch.setenv("SP_FOLD_MULTI", "1")
+    monkeypatch.setenv("SP_FOLD_HOST_ORDER", "1")
+    low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
+    ses = Session.open(low, backend)
+    for md in (1, 2, 3):
+        ba = fold_blocks(low, md, session=ses)
+        ob = BlockArrays.from_dict(oracle.prune(low, md))
+        assert to_prune_doc(low, ba) == to_prune_doc(low, ob)
+
+
 @pytest.mark.parametrize("seed", range(0, 40, 3))
 def test_multi_kernel_fold_path_vs_oracle(backend, seed, monkeypatch):
     """Force the multi-kernel (CUB) fold on small graphs: same partition as the oracle."""

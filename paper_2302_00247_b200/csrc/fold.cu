@@ -144,14 +144,17 @@ __global__ void k_heads_u64(const uint64_t* __restrict__ k, int64_t n, int32_t* 
     head[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
 }
 
-// groups: cur[node] = stamp|gid, gstart[gid] = first sorted position
+// groups: cur[node] = stamp|gid, gstart[gid] = first sorted position,
+// inv[node] = sorted position (when inv is given)
 __global__ void k_group_setup(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid,
                               int64_t nA, int64_t stamp, int64_t* __restrict__ cur,
-                              int32_t* __restrict__ gstart) {
+                              int32_t* __restrict__ gstart, int32_t* __restrict__ inv) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t g = gid[i] - 1;  // inclusive scan of heads
-    cur[sorted[i]] = stamp | (int64_t)g;
+    const int32_t v = sorted[i];
+    cur[v] = stamp | (int64_t)g;
+    if (inv) inv[v] = (int32_t)i;
     if (i == 0 || gid[i - 1] != gid[i]) gstart[g] = (int32_t)i;
   }
 }
@@ -188,16 +191,46 @@ __device__ __forceinline__ void entry_one(int64_t i, const int32_t* __restrict__
   atomicAdd(&gkey[g], (unsigned long long)fmix64(h ^ 0xa54ff53a5f1d36f1ULL));
 }
 
-__global__ void k_entry(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
-                        const int32_t* __restrict__ gstart, const int64_t* __restrict__ cur,
-                        const uint64_t* __restrict__ rh, int32_t D, int32_t dd,
-                        const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
-                        const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
-                        const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
-                        int32_t* __restrict__ pos, unsigned long long* __restrict__ gkey) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
-       i += (int64_t)gridDim.x * blockDim.x)
-    entry_one(i, sorted, gid, nA, gstart, cur, rh, D, dd, op, w_rank, w_shape, w_train, in_off, in_idx, pos, gkey);
+// k_entry in NODE order (multi-kernel path): a node's own arrays and its
+// producers' (topological neighbours) are read coalesced instead of in the
+// prefix-hash order of the sort; nodes not active at this level are skipped.
+__global__ void k_entry_nodes(int64_t n, int64_t stamp, const int64_t* __restrict__ cur,
+                              const int32_t* __restrict__ inv, const int32_t* __restrict__ gstart,
+                              const uint64_t* __restrict__ rh, int32_t D, int32_t dd,
+                              const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                              const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                              const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                              int32_t* __restrict__ pos, unsigned long long* __restrict__ gkey) {
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count: the group-key sums are aggregated per warp
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + lane;
+    const int64_t me = v < n ? cur[v] : -1;
+    const bool act = v < n && (me & ~(int64_t)0xffffffff) == stamp;
+    const int32_t g = (int32_t)(me & 0xffffffff);
+    uint64_t val = 0;
+    if (act) {
+      pos[v] = inv[v] - gstart[g];
+      uint64_t prod = 0;
+      for (int64_t e = in_off[v]; e < in_off[v + 1]; e++) {
+        const int32_t r = in_idx[e];
+        if (cur[r] == me) prod += fmix64(rh[(int64_t)r * D + dd] ^ 0x6a09e667f3bcc909ULL);
+      }
+      uint64_t h = fmix64(rh[v * D + dd] + 0x3c6ef372fe94f82bULL * (uint64_t)(op[v] + 1));
+      h = fmix64(h ^ weight_hash(v, w_rank, w_shape, w_train));
+      h = fmix64(h + fmix64(prod ^ 0xbb67ae8584caa73bULL));
+      val = fmix64(h ^ 0xa54ff53a5f1d36f1ULL);
+    }
+    // lanes of one group (consecutive nodes usually share it) add their u64
+    // terms in three 22-bit slices (each slice sum fits 32 bits), one atomic per group
+    const unsigned mask = __match_any_sync(0xffffffffu, act ? g : -1 - lane);
+    const uint64_t s0 = __reduce_add_sync(mask, (unsigned)(val & 0x3fffff));
+    const uint64_t s1 = __reduce_add_sync(mask, (unsigned)((val >> 22) & 0x3fffff));
+    const uint64_t s2 = __reduce_add_sync(mask, (unsigned)(val >> 44));
+    if (act && lane == __ffs(mask) - 1)
+      atomicAdd(&gkey[g], (unsigned long long)(s0 + (s1 << 22) + (s2 << 44)));
+  }
 }
 
 __global__ void k_class_keys(int64_t nG, int64_t nA, const int32_t* __restrict__ gstart,
@@ -336,19 +369,24 @@ __device__ __forceinline__ void verify_one(int64_t i, const int32_t* __restrict_
   if (bad) atomicExch(collision, 1);
 }
 
-__global__ void k_verify(const int32_t* __restrict__ sorted, const int32_t* __restrict__ gid, int64_t nA,
-                         int64_t nG, const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass,
-                         const int32_t* __restrict__ cstart, const int32_t* __restrict__ corder,
-                         const int64_t* __restrict__ cur, const int32_t* __restrict__ pos,
-                         const int32_t* __restrict__ pend, const uint64_t* __restrict__ rh, int32_t D,
-                         int32_t dd, const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
-                         const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
-                         const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
-                         const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
-                         int32_t* __restrict__ collision) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
-       i += (int64_t)gridDim.x * blockDim.x)
-    verify_one(i, sorted, gid, nA, nG, gstart, gclass, cstart, corder, cur, pos, pend, rh, D, dd, name_off, names, op, w_rank, w_shape, w_train, in_off, in_idx, collision);
+// k_verify in node order (multi-kernel path): node v is checked at its sorted
+// position inv[v]; its own name and producer reads are coalesced.
+__global__ void k_verify_nodes(int64_t n, int64_t stamp, const int32_t* __restrict__ inv, const int32_t* __restrict__ sorted,
+                               const int32_t* __restrict__ gid, int64_t nA, int64_t nG,
+                               const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass,
+                               const int32_t* __restrict__ cstart, const int32_t* __restrict__ corder,
+                               const int64_t* __restrict__ cur, const int32_t* __restrict__ pos,
+                               const int32_t* __restrict__ pend, const uint64_t* __restrict__ rh, int32_t D,
+                               int32_t dd, const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
+                               const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                               const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                               const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                               int32_t* __restrict__ collision) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if ((cur[v] & ~(int64_t)0xffffffff) != stamp) continue;
+    verify_one(inv[v], sorted, gid, nA, nG, gstart, gclass, cstart, corder, cur, pos, pend, rh, D, dd, name_off, names,
+               op, w_rank, w_shape, w_train, in_off, in_idx, collision);
+  }
 }
 
 // accept / residual / descend for every active node
@@ -1301,6 +1339,8 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   DevBuf<int64_t> cur;
   DevBuf<unsigned long long> gkey;
   DevBuf<uint8_t> next_flag, residual, gaccept;
+  DevBuf<int32_t> inv;
+  inv.alloc(n, s);
   depth.alloc(n, s);
   maxd.alloc(1, s);
   pend.alloc((size_t)n * D, s);
@@ -1397,11 +1437,14 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     if (level > D) throw Error(SP_ERR_CUDA, "fold did not terminate");
     const int32_t dd = level - 1;
     const int g1 = grid_for(nA, sms);
-    // 1. sort active nodes by (prefix hash, rel hash): rel first, then prefix (stable LSD)
+    // 1. sort active nodes by (prefix hash, rel hash): rel first, then prefix (stable
+    //    LSD).  The rel-hash pass only orders members inside a group, so its low
+    //    32 bits suffice: a 32-bit tie that misaligns two groups of a class fails
+    //    the exact verification and the fold reruns with a new seed.
     SP_LAUNCH(ctx, k_gather_keys, g1, 256, 0, s, act.p, nA, rh.p, D, dd, k2.p);
     t = tmp_bytes;
     ctx->cub_calls++;
-    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, k2.p, k2s.p, act.p, sorted1.p, (int)nA, 0, 64, s));
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t, k2.p, k2s.p, act.p, sorted1.p, (int)nA, 0, 32, s));
     SP_LAUNCH(ctx, k_gather_keys, g1, 256, 0, s, sorted1.p, nA, ph.p, D, dd, k1.p);
     t = tmp_bytes;
     ctx->cub_calls++;
@@ -1416,11 +1459,11 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     SP_CUDA(cudaStreamSynchronize(s));
     const int64_t nG = nG32;
     const int64_t stamp = ((int64_t)level) << 32;
-    SP_LAUNCH(ctx, k_group_setup, g1, 256, 0, s, sorted2.p, gidv.p, nA, stamp, cur.p, gstart.p);
-    // 2. entry hashes and group keys
+    SP_LAUNCH(ctx, k_group_setup, g1, 256, 0, s, sorted2.p, gidv.p, nA, stamp, cur.p, gstart.p, inv.p);
+    // 2. entry hashes and group keys (node order: coalesced reads)
     SP_CUDA(cudaMemsetAsync(gkey.p, 0, nG * sizeof(unsigned long long), s));
-    SP_LAUNCH(ctx, k_entry, g1, 256, 0, s, sorted2.p, gidv.p, nA, gstart.p, cur.p, rh.p, D, dd, dg->op.p, dg->w_rank.p,
-                               dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, pos.p, gkey.p);
+    SP_LAUNCH(ctx, k_entry_nodes, grid_for(n, sms), 256, 0, s, n, stamp, cur.p, inv.p, gstart.p, rh.p, D, dd, dg->op.p,
+              dg->w_rank.p, dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, pos.p, gkey.p);
     // 3. classes: sort groups by (parent, key) -- key first, then parent (stable)
     const int gG = grid_for(nG, sms);
     SP_LAUNCH(ctx, k_class_keys, gG, 256, 0, s, nG, nA, gstart.p, sorted2.p, gkey.p, gparent.p, ck.p, par.p, corder.p);
@@ -1443,10 +1486,9 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     const int64_t nC = nC32;
     SP_LAUNCH(ctx, k_class_setup, gG, 256, 0, s, corder3.p, cid.p, nG, gclass.p, cstart.p);
     // 4. exact verification against group and class heads
-    SP_LAUNCH(ctx, k_verify, g1, 128, 0, s, sorted2.p, gidv.p, nA, nG, gstart.p, gclass.p, cstart.p, corder3.p, cur.p,
-                                pos.p, pend.p, rh.p, D, dd, dg->name_off.p, dg->names.p, dg->op.p,
-                                dg->w_rank.p, dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p,
-                                collision.p);
+    SP_LAUNCH(ctx, k_verify_nodes, grid_for(n, sms), 128, 0, s, n, stamp, inv.p, sorted2.p, gidv.p, nA, nG, gstart.p,
+              gclass.p, cstart.p, corder3.p, cur.p, pos.p, pend.p, rh.p, D, dd, dg->name_off.p, dg->names.p,
+              dg->op.p, dg->w_rank.p, dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, collision.p);
     // 5. accept / residual / descend
     SP_LAUNCH(ctx, k_accept, g1, 256, 0, s, sorted2.p, gidv.p, nA, nC, nG, gclass.p, cstart.p, depth.p, level, min_dup,
                                 gparent.p, next_flag.p, residual.p, gaccept.p);

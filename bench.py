@@ -313,7 +313,8 @@ def _maxsum(vals, world):
 
     s = float(sum(vals))
     if world > 1:
-        t = torch.tensor([s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([s], dtype=torch.float64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         s = t.item()
     return s
@@ -327,11 +328,18 @@ def run_ours(args) -> None:
     from paper_2302_00247_b200.dist import allgather_exchange
 
     rank, world, local = _dist_env()
-    torch.cuda.set_device(local)
+    # one process per GPU; SP_DIST_BACKEND=gloo (+ fewer GPUs than ranks) only
+    # exercises the multi-rank plumbing on a single-GPU box, it is not a measurement
+    backend = os.environ.get("SP_DIST_BACKEND", "nccl")
+    device = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
     exchange = allgather_exchange() if world > 1 else None
-    be = Backend(local)
+    be = Backend(device)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
 
     def barrier():
@@ -341,7 +349,7 @@ def run_ours(args) -> None:
 
     g, mesh = load_workload(args.workload)
     main = measure(be, g, mesh, args.steps, args.warmup, rank, world, exchange, flush, barrier,
-                   skip=False, clocks_dev=local)
+                   skip=False, clocks_dev=device)
     cands = main["ref"].candidates
     total_ms = _maxsum(main["times"], world)
     e2e_ms = _maxsum(main["e2e_times"], world)

@@ -96,3 +96,64 @@ def test_two_rank_exchange_matches_single_process():
         exp = case(name)["best"]
         assert [(v, i, repr(t)) for v, _, i, _, t in results[0][name]] == [
             (e["valid"], e["index"], e["total"]) for e in exp]
+
+
+# -- the same exchange behind the real device scorer (two ranks share cuda:0) -------------
+
+def _gpu_worker(rank: int, world: int, port: int, q, names):
+    import hashlib
+    import json
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), here]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from golden_io import case, graph, mesh
+        from paper_2302_00247_b200._native import Backend
+        from paper_2302_00247_b200.dist import allgather_exchange
+        from paper_2302_00247_b200.search import derive_plan
+
+        be = Backend(0)
+        ex = allgather_exchange()
+        out = {}
+        for name in names:
+            c = case(name)
+            for mode in ("skip", "walk"):
+                be.set_mode(mode)
+                rep = derive_plan(graph(c["graph"]), mesh(c["mesh"]), min_duplicates=c["min_dup"], mu=c["mu"],
+                                  chunk_size=c["chunk_size"], backend=be, shard=rank, n_shards=world, exchange=ex)
+                doc = json.dumps(rep.to_json(), sort_keys=True, separators=(",", ":"))
+                out[(name, mode)] = hashlib.sha256(doc.encode()).hexdigest()
+        q.put((rank, out))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_device_search_byte_identical():
+    """derive_plan sharded over 2 ranks (device scoring of each rank's slice +
+    the all_gather key exchange) gives the reference's plan JSON, byte for byte."""
+    import hashlib
+
+    from golden_io import case
+
+    names = ("c2_1x8", "chain6_2x4_mu", "c1_1x8")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, names)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert results[0] == results[1]
+    for name in names:
+        exp = hashlib.sha256(case(name)["plan_json"].encode()).hexdigest()
+        for mode in ("skip", "walk"):
+            assert results[0][(name, mode)] == exp, (name, mode)

@@ -31,7 +31,11 @@ enum sp_status {
   SP_ERR_CONFIG = 1,      /* -> shardplan.BadConfig (errors.py:29-30) */
   SP_ERR_UNSUPPORTED = 2, /* index space > u64, rank > SP_MAX_RANK, ... */
   SP_ERR_CUDA = 3,        /* CUDA / NCCL internal failure */
-  SP_ERR_SPEC = 4         /* -> shardplan.SpecMismatch (patterns_for on a non-shardable kind) */
+  SP_ERR_SPEC = 4,        /* -> shardplan.SpecMismatch (patterns_for on a non-shardable kind) */
+  SP_ERR_PARSE = 5,       /* -> shardplan.ParseError (errors.py) : graph ingest */
+  SP_ERR_CYCLE = 6,       /* -> shardplan.CycleError(src, dst)   : graph ingest */
+  SP_ERR_DANGLING = 7,    /* -> shardplan.DanglingRef            : graph ingest */
+  SP_ERR_EMPTY = 8        /* -> shardplan.EmptyGraph             : graph ingest */
 };
 
 /* OpKind (ir.py:44-62) in declaration order. */
@@ -229,6 +233,23 @@ int sp_tables_sizes(const sp_tables* t, int64_t* n_entries, int64_t* n_edges);
 int sp_tables_edge_offsets(const sp_tables* t, int64_t* edge_off);
 int sp_explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, sp_explain_block* blocks,
                    int8_t* node_detail, int8_t* edge_detail);
+
+/*
+ * Native graph ingest (host only, no context): the JSON graph document of
+ * load_graph (ir.py:302-338, schema 1/2) -> ModelGraph validation and
+ * lexicographic-heap toposort (ir.py:214-274) -> trim_and_group (ir.py:378-461)
+ * -> the grouped graph as sp_graph arrays, rows in the grouped topological
+ * order (what lowering.lower() produces from the Python objects).  Replaces
+ * the reference's `load_graph` + `trim_and_group` in front of derive_plan
+ * (SURVEY 8(f) rows 1-2).  Errors: SP_ERR_PARSE / CYCLE / DANGLING / EMPTY /
+ * UNSUPPORTED; sp_ingest_error(0) is the message, (1)/(2) the CycleError
+ * edge (src, dst), valid until the next sp_ingest_json on this thread.
+ */
+typedef struct sp_ingest sp_ingest;
+int sp_ingest_json(const char* text, int64_t len, sp_ingest** out);
+const char* sp_ingest_error(int32_t which);
+int sp_ingest_view(const sp_ingest* g, sp_graph* view, int64_t* n_raw, int64_t* n_aux);
+void sp_ingest_free(sp_ingest* g);
 
 /* Device time (ms) of the last sp_score / sp_fold_run kernels (CUDA events). */
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms);

@@ -106,7 +106,8 @@ EXPORTED_SYMBOLS = (
     "sp_merge_keys", "sp_explain", "sp_last_timings", "sp_timer_start", "sp_timer_stop",
     "sp_launch_counts", "sp_copy_bytes", "sp_tables_bytes", "sp_tables_sizes",
     "sp_tables_edge_offsets", "sp_explain_all", "sp_search", "sp_set_option",
-    "sp_fold_stats", "sp_score_launch", "sp_score_wait",
+    "sp_fold_stats", "sp_score_launch", "sp_score_wait", "sp_ingest_json", "sp_ingest_error",
+    "sp_ingest_view", "sp_ingest_free",
 )
 
 

@@ -51,6 +51,7 @@ int sp_ctx_create(int device, sp_ctx** out) {
     SP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     for (auto& e : ctx->ev) SP_CUDA(cudaEventCreate(&e));
     for (auto& e : ctx->timer) SP_CUDA(cudaEventCreate(&e));
+    for (auto& e : ctx->trace) SP_CUDA(cudaEventCreate(&e));
   });
   if (rc != SP_OK) {
     std::fprintf(stderr, "sp_ctx_create: %s\n", ctx->last_error.c_str());

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <numeric>
 
 #include "patterns.cuh"
@@ -2346,6 +2347,7 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned 
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);
   SP_CUDA(cudaGetLastError());
+  SP_CUDA(cudaEventRecord(ctx->trace[0], s));
   if (explain) {
     // winner detail straight from the device-side argmin: no host round trip
     DevBuf<ExplainBlock>& dblk = pd.dblk;
@@ -2363,6 +2365,7 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned 
               dedge.p);
     SP_CUDA(cudaGetLastError());
   }
+  SP_CUDA(cudaEventRecord(ctx->trace[1], s));
   pd.active = true;
 }
 
@@ -2385,10 +2388,20 @@ static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& r
     pd.dedge.download(fx->edge, 2 * nedge, s);
   }
   pd.dout.download(res.data(), nb, s);
+  SP_CUDA(cudaEventRecord(ctx->trace[2], s));
   SP_CUDA(cudaStreamSynchronize(s));
   float ms = 0;
   SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
   ctx->score_kernel_ms = ms;
+  if (getenv("SP_SCORE_TRACE")) {
+    float a = 0, b = 0, c = 0, d = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[2]);
+    cudaEventElapsedTime(&b, ctx->ev[3], ctx->trace[0]);
+    cudaEventElapsedTime(&c, ctx->trace[0], ctx->trace[1]);
+    cudaEventElapsedTime(&d, ctx->trace[1], ctx->trace[2]);
+    fprintf(stderr, "[score] nb %lld: launch->kernel %.3f ms, kernel %.3f, reduce %.3f, explain %.3f, d2h %.3f\n",
+            (long long)nb, a, ms, b, c, d);
+  }
 }
 
 void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {

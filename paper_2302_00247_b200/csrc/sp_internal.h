@@ -99,6 +99,7 @@ struct sp_ctx {
   int skip = 1;  // exact prefix-failure skipping in sp_score / sp_search
   int memo = 0;  // with skip off: memoised brute force (re-route only dirty nodes); off: walk
   cudaEvent_t timer[2] = {};
+  cudaEvent_t trace[4] = {};  // SP_SCORE_TRACE: reduce / explain / d2h boundaries
   // scratch reused across calls
   sp::DevBuf<uint8_t> cub_tmp;
   void* staging = nullptr;  // pinned host staging for graph uploads

@@ -377,6 +377,7 @@ class _Search:
                  exchange: Optional[Callable]):
         self.ses, self.mesh, self.mu, self.chunk_size = ses, mesh, mu, chunk_size
         self.exchange = exchange
+        self._fetched = None
         # pack_gradients raises BadConfig for mu > chunk only once a candidate is
         # costed; build with a legal chunk to learn which error the reference hits first
         self.bad_mu = mu > chunk_size
@@ -396,13 +397,25 @@ class _Search:
             self.tables.close()
             raise
 
+    def fetch(self) -> None:
+        """Wait for the device results (and exchange them across ranks)."""
+        if self._fetched is not None:
+            return
+        try:
+            scores, detail = self.ses.backend.score_wait(self.tables)
+            if self.exchange is not None:
+                scores = self.exchange(scores)
+        except BaseException:
+            self.tables.close()
+            raise
+        self._fetched = (scores, detail, time.perf_counter())
+
     def collect(self, graph, subgraphs: list, want_table: bool, types: TypeSet, prep=None) -> list:
         ses, tables = self.ses, self.tables
         try:
-            scores, detail = ses.backend.score_wait(tables)
-            if self.exchange is not None:
-                scores = self.exchange(scores)
-            tc = time.perf_counter()
+            self.fetch()
+            scores, detail, tc = self._fetched
+            t_routes = time.perf_counter()
             for sc in scores:
                 if not sc.has_best:
                     raise AssertionError("all-replica fallback must always route")
@@ -410,7 +423,7 @@ class _Search:
                     raise BadConfig(f"fusion threshold {self.mu} exceeds chunk size {self.chunk_size}")
             bests = routed_plans_all(ses, tables, subgraphs, scores, self.mesh, types, detail, prep)
             LAST_PHASES.update(tables_ms=self.tables_ms, score_call_ms=(tc - self.t_launch) * 1e3,
-                               routes_ms=(time.perf_counter() - tc) * 1e3)
+                               routes_ms=(time.perf_counter() - t_routes) * 1e3)
             results = []
             for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
                 table = []
@@ -520,8 +533,14 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     # two launches when the blocks split into cheap and expensive ones: the
     # cheap group's results (typically hundreds of residual singletons) are
     # turned into RoutedPlans while the device still scores the expensive group
-    searches = [(_Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange), ids)
-                for ids, gcsr in _block_groups(ses.low, csr)]
+    searches = []
+    for ids, gcsr in _block_groups(ses.low, csr):
+        if searches:
+            # the cheap group's results come back BEFORE the expensive launch is
+            # queued behind them on the stream (its RoutedPlans are built while
+            # the expensive group scores)
+            searches[-1][0].fetch()
+        searches.append((_Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange), ids))
     # host work that does not depend on the winners overlaps the device search:
     # Subgraph objects, the static part of every RoutedPlan, and the member
     # scopes that receive each block's weight labels (search.py:374-376)

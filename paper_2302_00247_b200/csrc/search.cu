@@ -1260,8 +1260,10 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
 // same work decomposition and argmin as k_score, with the lean FastNode walk.
 // Each lane carries its own candidate's digit word and advances it by 32 per
 // warp step (one carry-fixed add); the warp's remaining count is 32-bit.
-constexpr int PAIR_CHUNK = 512;  // candidates per warp chunk in the paired walk
+constexpr int PAIR_CHUNK = 512;   // candidates per warp chunk, walk modes
 constexpr int PAIR_MAX_CHUNKS = ITEM_ITERS_MAX * THREADS / PAIR_CHUNK;
+constexpr int SKIP_CHUNK = 4096;  // ... with prefix skipping (a chunk costs >= one walk)
+constexpr int SKIP_MAX_CHUNKS = ITEM_ITERS_MAX_SKIP * THREADS / SKIP_CHUNK;
 #ifndef SP_PAIR_MIN_BLOCKS
 #define SP_PAIR_MIN_BLOCKS 4
 #endif
@@ -1276,10 +1278,12 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
   __shared__ uint32_t s_red_n[THREADS / 32], s_red_v[THREADS / 32];
   __shared__ uint64_t s_lane_add[32];
   __shared__ Biased s_bz;
-  // paired walk: warps pull PAIR_CHUNK-candidate chunks of the item from a
-  // shared cursor (no static per-warp spans: no barrier idling on skewed walks)
-  __shared__ uint64_t s_wbase;                       // biased digits of the item start
-  __shared__ uint64_t s_cenc[PAIR_MAX_CHUNKS];       // unbiased digits of c * PAIR_CHUNK
+  // warps pull CH-candidate chunks of the item from a shared cursor (no
+  // static per-warp spans: no barrier idling when walks or skips are skewed)
+  constexpr uint32_t CH = SKIP ? SKIP_CHUNK : PAIR_CHUNK;
+  constexpr int MAXCH = SKIP ? SKIP_MAX_CHUNKS : PAIR_MAX_CHUNKS;
+  __shared__ uint64_t s_wbase;              // biased digits of the item start
+  __shared__ uint64_t s_cenc[MAXCH];        // unbiased digits of c * CH
   __shared__ uint32_t s_chunk;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1333,21 +1337,21 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
         }
         s_bz = z;
       }
-      if (PAIR && tid >= 64 && tid - 64 < PAIR_MAX_CHUNKS) {
-        uint64_t a = 0;  // unbiased digits of (tid - 64) * PAIR_CHUNK
-        uint64_t x = (uint64_t)(tid - 64) * PAIR_CHUNK;
+      for (int c = tid - 64; c >= 0 && c < MAXCH; c += THREADS - 64) {
+        uint64_t a = 0;  // unbiased digits of c * CH
+        uint64_t x = (uint64_t)c * CH;
         for (int q = V - 1; q >= 0 && x; q--) {
           const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
           a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
           x /= r;
         }
-        s_cenc[tid - 64] = a;
+        s_cenc[c] = a;
       }
       __syncthreads();
       patch_fast(smem, PAIR);
       staged = b;
     }
-    if (PAIR && tid == 0) {
+    if (tid == 0) {
       s_wbase = bencode(*(const BlobHeader*)smem, P.lo[b] + (item - P.item_base[b]) * P.item_cands);
       s_chunk = 0;
     }
@@ -1356,11 +1360,9 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
     const BlobHeader& H = *S.H;
     const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
-    const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
-    const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
     unsigned long long best_t = ~0ULL, best_i = ~0ULL;
     uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
-    if (PAIR ? ilo < ihi : wlo < whi) {
+    if (ilo < ihi) {
       // opaque copies keep the shared addresses in registers (ptxas would
       // otherwise re-derive the shared window base at every access)
       const uint32_t rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
@@ -1369,9 +1371,7 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
       const uint32_t rb = opaque_u32(pool + 8u * (uint32_t)tid);
       const uint32_t sb = opaque_u32(pool + (uint32_t)H.npool * THREADS * (PAIR ? 16u : 8u) + (uint32_t)tid);
       const int T = H.T;
-      uint32_t rem = (uint32_t)(whi - wlo);  // candidates left for this warp (<= item size)
-      unsigned long long base = wlo;
-      uint64_t w = PAIR ? 0 : badd(bencode(H, wlo), s_lane_add[lane], s_bz.B);
+      const uint32_t cnt = (uint32_t)(ihi - ilo);
       uint64_t best_w = 0;
       // valid candidate: total, key update (the reference index only breaks
       // exact (total, num_split) ties: keep the digits, convert once per item)
@@ -1388,15 +1388,14 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
           best_w = wv;
         }
       };
-      if (PAIR) {
-        const uint32_t cnt = (uint32_t)(ihi - ilo);
-        while (true) {
-          uint32_t c = 0;
-          if (lane == 0) c = atomicAdd(&s_chunk, 1u);
-          c = __shfl_sync(0xffffffffu, c, 0);
-          if (c * PAIR_CHUNK >= cnt) break;
-          rem = min((uint32_t)PAIR_CHUNK, cnt - c * PAIR_CHUNK);
-          w = badd(badd(s_wbase, s_cenc[c], s_bz.B), s_lane_add[lane], s_bz.B);
+      while (true) {
+        uint32_t c = 0;
+        if (lane == 0) c = atomicAdd(&s_chunk, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c * CH >= cnt) break;
+        uint32_t rem = min(CH, cnt - c * CH);  // candidates left in this chunk
+        uint64_t w = badd(badd(s_wbase, s_cenc[c], s_bz.B), s_lane_add[lane], s_bz.B);
+        if (PAIR) {
           while (true) {
             const uint64_t wb = badd(w, s_bz.add32, s_bz.B);
             double fa, fb;
@@ -1407,53 +1406,57 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
             rem -= 64;
             w = badd(w, s_bz.add64, s_bz.B);
           }
+          continue;
         }
-      }
-      while (!PAIR) {
-        const bool active = (uint32_t)lane < rem;
-        double fwd;
-        const int fail = walk_fast<SKIP>(rec0, T, w, active, fwd, rb, sb);
-        uint32_t adv = 32;  // SKIP: candidates this lane proves done, from base
-        if (fail < 0) {
-          take(w, fwd);
-          if (SKIP) adv = lane + 1;
-        } else if (SKIP) {
-          adv = lane + 1;
-          if (active) {
-            const NodeSkip sk = S.skip[fail];
-            const unsigned long long x = base + lane;
-            const unsigned long long t = sk.R ? (x / sk.R + 1) * sk.R : whi;
-            adv = (uint32_t)(min(t, whi) - base);
+        // single candidate per lane; with SKIP, lanes prove R-aligned runs invalid
+        // and the warp jumps to the furthest proven end (clamped to the chunk)
+        const unsigned long long whi = ilo + (unsigned long long)c * CH + rem;
+        unsigned long long base = whi - rem;
+        while (true) {
+          const bool active = (uint32_t)lane < rem;
+          double fwd;
+          const int fail = walk_fast<SKIP>(rec0, T, w, active, fwd, rb, sb);
+          uint32_t adv = 32;  // SKIP: candidates this lane proves done, from base
+          if (fail < 0) {
+            take(w, fwd);
+            if (SKIP) adv = lane + 1;
+          } else if (SKIP) {
+            adv = lane + 1;
+            if (active) {
+              const NodeSkip sk = S.skip[fail];
+              const unsigned long long x = base + lane;
+              const unsigned long long t = sk.R ? (x / sk.R + 1) * sk.R : whi;
+              adv = (uint32_t)(min(t, whi) - base);
+            }
           }
-        }
-        if (!SKIP) {
-          if (rem <= 32) break;
-          rem -= 32;
-          base += 32;
-          w = badd(w, s_bz.add32, s_bz.B);
-        } else {
-          // the union of the lanes' proven runs is contiguous from base
-          uint32_t m = adv;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-          if (m >= rem) break;
-          if (m == 32) {
+          if (!SKIP) {
+            if (rem <= 32) break;
+            rem -= 32;
             w = badd(w, s_bz.add32, s_bz.B);
           } else {
-            // the lane that proved the longest run provides the next base digits
-            const int src = __ffs(__ballot_sync(0xffffffffu, adv == m)) - 1;
-            uint64_t n0 = w;
-            if (lane == src) {
-              const bool jump = fail >= 0 && active && S.skip[fail].R;
-              // positions faster than m back to digit 0, then +1 at position m
-              const int sh = jump ? 2 * (H.V - 1 - S.skip[fail].m) : 0;
-              const uint64_t low = (1ULL << sh) - 1;
-              n0 = badd((n0 & ~low) | (s_bz.B & low), 1ULL << sh, s_bz.B);
+            // the union of the lanes' proven runs is contiguous from base
+            uint32_t m = adv;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (m >= rem) break;
+            if (m == 32) {
+              w = badd(w, s_bz.add32, s_bz.B);
+            } else {
+              // the lane that proved the longest run provides the next base digits
+              const int src = __ffs(__ballot_sync(0xffffffffu, adv == m)) - 1;
+              uint64_t n0 = w;
+              if (lane == src) {
+                const bool jump = fail >= 0 && active && S.skip[fail].R;
+                // positions faster than m back to digit 0, then +1 at position m
+                const int sh = jump ? 2 * (H.V - 1 - S.skip[fail].m) : 0;
+                const uint64_t low = (1ULL << sh) - 1;
+                n0 = badd((n0 & ~low) | (s_bz.B & low), 1ULL << sh, s_bz.B);
+              }
+              w = badd(shfl_u64(n0, src), s_lane_add[lane], s_bz.B);
             }
-            w = badd(shfl_u64(n0, src), s_lane_add[lane], s_bz.B);
+            rem -= m;
+            base += m;
           }
-          rem -= m;
-          base += m;
         }
       }
       if (best_t != ~0ULL) best_i = ref_index_b(S, best_w);

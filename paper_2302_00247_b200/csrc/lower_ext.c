@@ -363,8 +363,88 @@ done:
   return result;
 }
 
+/*
+ * block_instances(names, members, prefix_node, prefix_len, inst_off, block_T, ascii)
+ * -> [ (instances tuple) per block ], instance = (prefix str, member scopes tuple)
+ * (Subgraph.instances, pruning.py:33-55) straight from the fold's flat arrays:
+ * members int32, prefix_node/prefix_len/inst_off/block_T int64 buffers.
+ */
+static PyObject* block_instances(PyObject* self, PyObject* args) {
+  PyObject *names, *ascii_o;
+  Py_buffer mem, pn, pl, io, bt;
+  if (!PyArg_ParseTuple(args, "O!y*y*y*y*y*O", &PyList_Type, &names, &mem, &pn, &pl, &io, &bt, &ascii_o)) return NULL;
+  PyObject* out = NULL;
+  const int ascii = PyObject_IsTrue(ascii_o);
+  const int32_t* m = (const int32_t*)mem.buf;
+  const int64_t* pnode = (const int64_t*)pn.buf;
+  const int64_t* plen = (const int64_t*)pl.buf;
+  const int64_t* ioff = (const int64_t*)io.buf;
+  const int64_t* T = (const int64_t*)bt.buf;
+  const Py_ssize_t nb = bt.len / 8, nn = PyList_GET_SIZE(names), nm = mem.len / 4;
+  out = PyList_New(nb);
+  if (!out) goto done;
+  Py_ssize_t mo = 0;
+  for (Py_ssize_t b = 0; b < nb; b++) {
+    const Py_ssize_t R = ioff[b + 1] - ioff[b];
+    PyObject* insts = PyTuple_New(R);
+    if (!insts) goto fail;
+    PyList_SET_ITEM(out, b, insts);
+    for (Py_ssize_t i = 0; i < R; i++) {
+      const int64_t j = ioff[b] + i;
+      if (pnode[j] < 0 || pnode[j] >= nn || mo + T[b] > nm) {
+        PyErr_SetString(PyExc_IndexError, "fold arrays out of range");
+        goto fail;
+      }
+      PyObject* full = PyList_GET_ITEM(names, pnode[j]);
+      PyObject* pre;
+      if (ascii) {
+        pre = PyUnicode_Substring(full, 0, plen[j]);
+      } else {  /* prefix length is in UTF-8 bytes */
+        Py_ssize_t L;
+        const char* u = PyUnicode_AsUTF8AndSize(full, &L);
+        pre = u ? PyUnicode_DecodeUTF8(u, plen[j] < L ? plen[j] : L, "strict") : NULL;
+      }
+      if (!pre) goto fail;
+      PyObject* tup = PyTuple_New(T[b]);
+      if (!tup) {
+        Py_DECREF(pre);
+        goto fail;
+      }
+      for (int64_t t = 0; t < T[b]; t++) {
+        const int32_t v = m[mo + t];
+        if (v < 0 || v >= nn) {
+          Py_DECREF(pre);
+          Py_DECREF(tup);
+          PyErr_SetString(PyExc_IndexError, "member index out of range");
+          goto fail;
+        }
+        PyObject* s = PyList_GET_ITEM(names, v);
+        Py_INCREF(s);
+        PyTuple_SET_ITEM(tup, t, s);
+      }
+      mo += T[b];
+      PyObject* pair = PyTuple_Pack(2, pre, tup);
+      Py_DECREF(pre);
+      Py_DECREF(tup);
+      if (!pair) goto fail;
+      PyTuple_SET_ITEM(insts, i, pair);
+    }
+  }
+  goto done;
+fail:
+  Py_CLEAR(out);
+done:
+  PyBuffer_Release(&mem);
+  PyBuffer_Release(&pn);
+  PyBuffer_Release(&pl);
+  PyBuffer_Release(&io);
+  PyBuffer_Release(&bt);
+  return out;
+}
+
 static PyMethodDef methods[] = {
     {"lower_arrays", lower_arrays, METH_VARARGS, "Lower a grouped ModelGraph to flat sp_graph arrays."},
+    {"block_instances", block_instances, METH_VARARGS, "Subgraph.instances of every block from fold arrays."},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_lower", NULL, -1, methods};

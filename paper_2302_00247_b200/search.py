@@ -28,7 +28,7 @@ from ._native import Backend, default_backend
 from .api_types import DEFAULT_TYPES, TypeSet
 from .blocks import BlockArrays, prefix_of
 from .errors import BackendError, BadConfig, SpecMismatch, UnsupportedSearch
-from .lowering import LoweredGraph, lower
+from .lowering import LoweredGraph, _native_lower, lower
 
 _KIND_LABEL = {1: "allreduce", 2: "allgather", 3: "reducescatter", 4: "alltoall"}
 
@@ -74,13 +74,22 @@ class _Uncached:
 
 
 def subgraphs_from_blocks(low: LoweredGraph, ba: BlockArrays, types: TypeSet = DEFAULT_TYPES) -> list:
+    """Subgraph objects (pruning.py:33-55) of a folding result."""
+    ascii_names = getattr(low, "ascii", None)
+    if ascii_names is None:
+        ascii_names = low.ascii = len(low.name_bytes) == sum(map(len, low.names))
+    if _native_lower is not None and isinstance(low.names, list):
+        # instance tuples built in C (csrc/lower_ext.c) straight from the fold arrays
+        per_block = _native_lower.block_instances(
+            low.names, np.ascontiguousarray(ba.members, np.int32), np.ascontiguousarray(ba.inst_prefix_node, np.int64),
+            np.ascontiguousarray(ba.inst_prefix_len, np.int64), np.ascontiguousarray(ba.block_inst_off, np.int64),
+            np.ascontiguousarray(ba.block_T, np.int64), ascii_names)
+        subgraph = types.Subgraph
+        return [subgraph(insts[0][0], insts[0][1], insts) for insts in per_block]
     names = low.names
     member_names = list(map(names.__getitem__, ba.members.tolist()))
     pnode, plen = ba.inst_prefix_node.tolist(), ba.inst_prefix_len.tolist()
     ioff, moff, Ts = ba.block_inst_off.tolist(), ba.block_member_off.tolist(), ba.block_T.tolist()
-    ascii_names = getattr(low, "ascii", None)
-    if ascii_names is None:
-        ascii_names = low.ascii = len(low.name_bytes) == sum(map(len, names))
     subgraph = types.Subgraph
     subs = []
     for b in range(len(Ts)):
@@ -275,9 +284,24 @@ def route_prep(ses: Session, subgraphs: list, types: TypeSet = DEFAULT_TYPES, cs
     if csr is None:
         csr = _templates_csr(low, subgraphs)
     toff, tnl = csr[0].tolist(), csr[1].tolist()
+    # per template node scalars as Python lists (one conversion, no per-node numpy indexing)
+    tn = csr[1]
+    t_op, t_w = op[tn].tolist(), w_rank[tn].tolist()
+    t_bytes = act_bytes[tn].tolist()
     out = []
     for b, sub in enumerate(subgraphs):
         template = sub.template
+        e0 = toff[b]
+        if toff[b + 1] - e0 == 1:
+            # singleton block (residual op): no internal producers
+            v = tnl[e0]
+            lab = _OP_LABELS[t_op[e0]]
+            node = (template[0], lab, pnames[lab], pcolls[lab], t_bytes[e0], [])
+            if t_w[e0]:
+                out.append(([0], [3 if t_w[e0] >= 2 else 2], [node], _flops(low, (v,)) if t_op[e0] == 0 else 0))
+            else:
+                out.append(([], [], [node], 0))
+            continue
         tnodes = tnl[toff[b]:toff[b + 1]]
         members = set(tnodes)
         wpos = [i for i, v in enumerate(tnodes) if w_rank[v]]

@@ -3,16 +3,17 @@
 Each rank (one process per GPU) scores its contiguous slice of every block's
 index range -- the split search_subgraph hands its worker pool
 (search.py:331-336).  Per block the ranks then exchange one record
-(has_best, total bits, num_split, index, valid) with a single all_gather
-over NCCL and reduce it to the lexicographic (total, num_split, index)
-minimum and the summed valid count (search.py:337-343).  A single 64-bit
-allreduce-min cannot carry this key losslessly, so the record
-is gathered whole; it is 40 bytes per block.
+(candidates, valid, index, total bits, num_split, has_best) with a single
+all_gather over NCCL and reduce it, vectorised over blocks, to the
+lexicographic (total, num_split, index) minimum and the summed valid count
+(search.py:337-343).  A single 64-bit allreduce-min cannot carry this key
+losslessly, so the record is gathered whole; it is 40 bytes
+per block.
 """
 
 from __future__ import annotations
 
-import struct
+import ctypes as C
 from typing import Callable
 
 import numpy as np
@@ -20,49 +21,57 @@ import numpy as np
 from ._abi import SpScoreOut
 
 
-def _key(s: SpScoreOut):
-    return (s.best_total, s.best_num_split, s.best_index)
+#: numpy view of sp_score_out (include/shardsearch.h): 40-byte records
+REC = np.dtype([("candidates", "<u8"), ("valid", "<u8"), ("best_index", "<u8"), ("best_total", "<f8"),
+                ("best_num_split", "<i4"), ("has_best", "<i4")])
+assert REC.itemsize == C.sizeof(SpScoreOut)
+
+
+def to_records(scores: list) -> np.ndarray:
+    """SpScoreOut list -> structured array (one copy of the raw records)."""
+    return np.frombuffer(b"".join(map(bytes, scores)), dtype=REC) if scores else np.zeros(0, REC)
+
+
+def from_records(rec: np.ndarray) -> list:
+    arr = (SpScoreOut * max(1, len(rec))).from_buffer_copy(np.ascontiguousarray(rec, REC).tobytes() or bytes(40))
+    return list(arr)[: len(rec)]
+
+
+def merge_records(parts: np.ndarray) -> np.ndarray:
+    """[world, nb] records -> [nb]: lexicographic (total, num_split, index) min over the
+    ranks that have a winner (search.py:337-343), valid counts summed.  Totals are
+    non-negative doubles, so their bit patterns order like the values."""
+    world, nb = parts.shape
+    if world == 1:
+        return parts[0].copy()
+    tb = parts["best_total"].view("<u8")
+    no = (parts["has_best"] == 0).astype(np.uint8)
+    # lexsort: last key is primary; per block (column) over the ranks (rows)
+    order = np.lexsort((parts["best_index"], parts["best_num_split"], tb, no), axis=0)
+    win = order[0]
+    out = parts[win, np.arange(nb)].copy()
+    out["valid"] = parts["valid"].sum(axis=0)
+    out["candidates"] = parts["candidates"][0]
+    none = out["has_best"] == 0  # no rank routed a candidate of this block
+    for f in ("best_index", "best_total", "best_num_split"):
+        out[f][none] = 0
+    return out
 
 
 def merge_scores(parts: list) -> list:
     """Merge per-shard result lists (same block order) exactly."""
-    out = []
-    for recs in zip(*parts):
-        acc = SpScoreOut()
-        acc.candidates = recs[0].candidates
-        for r in recs:
-            acc.valid += r.valid
-            if r.has_best and (not acc.has_best or _key(r) < _key(acc)):
-                acc.has_best = 1
-                acc.best_total = r.best_total
-                acc.best_num_split = r.best_num_split
-                acc.best_index = r.best_index
-        out.append(acc)
-    return out
+    if not parts:
+        return []
+    return from_records(merge_records(np.stack([to_records(p) for p in parts])))
 
 
 def pack(scores: list) -> np.ndarray:
-    """[nb, 6] int64 records (fp64 total carried as its bit pattern)."""
-    a = np.zeros((len(scores), 6), np.int64)
-    for i, s in enumerate(scores):
-        bits = struct.unpack("<q", struct.pack("<d", s.best_total))[0]
-        a[i] = (s.has_best, bits, s.best_num_split, np.uint64(s.best_index).view(np.int64),
-                np.uint64(s.valid).view(np.int64), np.uint64(s.candidates).view(np.int64))
-    return a
+    """[nb, 5] int64 view of the records (fp64 total carried as its bit pattern)."""
+    return to_records(scores).view(np.int64).reshape(-1, 5)
 
 
 def unpack(a: np.ndarray) -> list:
-    out = []
-    for row in a:
-        s = SpScoreOut()
-        s.has_best = int(row[0])
-        s.best_total = struct.unpack("<d", struct.pack("<q", int(row[1])))[0]
-        s.best_num_split = int(row[2])
-        s.best_index = int(np.int64(row[3]).view(np.uint64))
-        s.valid = int(np.int64(row[4]).view(np.uint64))
-        s.candidates = int(np.int64(row[5]).view(np.uint64))
-        out.append(s)
-    return out
+    return from_records(np.ascontiguousarray(a, np.int64).reshape(-1).view(REC))
 
 
 def allgather_exchange(group=None, device=None) -> Callable:
@@ -77,12 +86,16 @@ def allgather_exchange(group=None, device=None) -> Callable:
         world = dist.get_world_size(group)
         if world == 1:
             return scores
-        local = torch.from_numpy(pack(scores))
+        local = torch.from_numpy(pack(scores).copy())
         if dist.get_backend(group) == "nccl":
             local = local.to(device or torch.device("cuda", torch.cuda.current_device()))
-        bufs = [torch.empty_like(local) for _ in range(world)]
-        dist.all_gather(bufs, local, group=group)
-        parts = [unpack(b.cpu().numpy()) for b in bufs]
-        return merge_scores(parts)
+            out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+            dist.all_gather_into_tensor(out, local, group=group)
+        else:  # gloo: list form
+            bufs = [torch.empty_like(local) for _ in range(world)]
+            dist.all_gather(bufs, local, group=group)
+            out = torch.stack(bufs)
+        parts = out.cpu().numpy().reshape(world, -1).view(REC)
+        return from_records(merge_records(parts))
 
     return exchange

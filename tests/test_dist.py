@@ -84,7 +84,7 @@ def test_two_rank_exchange_matches_single_process():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    results = dict(q.get(timeout=300) for _ in range(world))
+    results = dict(q.get(timeout=120) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -148,7 +148,7 @@ def test_two_rank_device_search_byte_identical():
     procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, names)) for r in range(world)]
     for p in procs:
         p.start()
-    results = dict(q.get(timeout=600) for _ in range(world))
+    results = dict(q.get(timeout=240) for _ in range(world))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0

@@ -35,7 +35,9 @@ enum sp_status {
   SP_ERR_PARSE = 5,       /* -> shardplan.ParseError (errors.py) : graph ingest */
   SP_ERR_CYCLE = 6,       /* -> shardplan.CycleError(src, dst)   : graph ingest */
   SP_ERR_DANGLING = 7,    /* -> shardplan.DanglingRef            : graph ingest */
-  SP_ERR_EMPTY = 8        /* -> shardplan.EmptyGraph             : graph ingest */
+  SP_ERR_EMPTY = 8,       /* -> shardplan.EmptyGraph             : graph ingest */
+  SP_ERR_ONNX_PARSE = 9,  /* -> onnx_ingest.model.ModelParseError   : ONNX ingest */
+  SP_ERR_ONNX_UNSUPPORTED = 10 /* -> onnx_ingest.convert.UnsupportedModel : ONNX ingest */
 };
 
 /* OpKind (ir.py:44-62) in declaration order. */
@@ -250,6 +252,21 @@ int sp_ingest_json(const char* text, int64_t len, sp_ingest** out);
 const char* sp_ingest_error(int32_t which);
 int sp_ingest_view(const sp_ingest* g, sp_graph* view, int64_t* n_raw, int64_t* n_aux);
 void sp_ingest_free(sp_ingest* g);
+/*
+ * ONNX ModelProto bytes -> the reference's onnx_ingest conversion
+ * (wire.py:27-97, model.py:143-167, convert.py:84-274).  export_only != 0:
+ * keep the schema-1 document (json.dumps text, sp_ingest_text(g, 0, 0)) and
+ * the ConversionReport, as export_graph returns them; else continue into the
+ * load_graph + trim_and_group pipeline of sp_ingest_json (sp_ingest_view).
+ * has_batch/batch = the --batch option fixing a symbolic leading dimension.
+ * counts[6] of sp_ingest_report: trainable_elements, skipped_elements,
+ * initializer_elements, #warnings, #skipped, document bytes; texts:
+ * kind 1 = warnings[i], kind 2 = skipped[i].
+ */
+int sp_ingest_onnx(const uint8_t* data, int64_t len, int32_t has_batch, int64_t batch, int32_t export_only,
+                   sp_ingest** out);
+int sp_ingest_report(const sp_ingest* g, int64_t* counts);
+const char* sp_ingest_text(const sp_ingest* g, int32_t kind, int64_t i);
 
 /* Device time (ms) of the last sp_score / sp_fold_run kernels (CUDA events). */
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms);

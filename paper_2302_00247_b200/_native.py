@@ -107,7 +107,7 @@ EXPORTED_SYMBOLS = (
     "sp_launch_counts", "sp_copy_bytes", "sp_tables_bytes", "sp_tables_sizes",
     "sp_tables_edge_offsets", "sp_explain_all", "sp_search", "sp_set_option",
     "sp_fold_stats", "sp_score_launch", "sp_score_wait", "sp_ingest_json", "sp_ingest_error",
-    "sp_ingest_view", "sp_ingest_free",
+    "sp_ingest_view", "sp_ingest_free", "sp_ingest_onnx", "sp_ingest_report", "sp_ingest_text",
 )
 
 

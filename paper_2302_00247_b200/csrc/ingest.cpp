@@ -22,6 +22,8 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/shardsearch.h"
@@ -830,6 +832,10 @@ std::vector<int32_t> toposort(const std::vector<std::string_view>& names, const 
 }  // namespace
 
 struct sp_ingest {
+  // ONNX conversion (sp_ingest_onnx): report and, in export mode, the document
+  std::string json;
+  std::vector<std::string> warnings, skipped;
+  int64_t trainable = 0, skipped_elements = 0, initializer_elements = 0;
   std::string name_bytes;
   std::vector<int64_t> name_off, topo, act_shape, act_bytes, w_shape, w_bytes, in_off;
   std::vector<uint8_t> op, act_rank, w_rank, w_train;
@@ -849,6 +855,9 @@ struct PhaseTimer {  // SP_INGEST_TRACE=1: phase times on stderr
     last = now;
   }
 };
+
+void build_graph(std::vector<Raw>& raw, std::vector<std::vector<std::string_view>>& in_names, sp_ingest* out,
+                 PhaseTimer& tm);
 
 void ingest(const char* text, int64_t len, sp_ingest* out) {
   PhaseTimer tm;
@@ -879,6 +888,13 @@ void ingest(const char* text, int64_t len, sp_ingest* out) {
       r.has_w = true;
     }
   }
+  build_graph(raw, in_names, out, tm);
+}
+
+// ModelGraph(nodes) validation + toposort, trim_and_group and lowering of raw
+// nodes (names / input names are views that must outlive the call).
+void build_graph(std::vector<Raw>& raw, std::vector<std::vector<std::string_view>>& in_names, sp_ingest* out,
+                 PhaseTimer& tm) {
   // ModelGraph(nodes) (ir.py:221-235): duplicates, empty, dangling refs, toposort
   const size_t n = raw.size();
   if (!n) throw IngestError(E_EMPTY, "graph has no nodes");
@@ -1065,6 +1081,721 @@ void ingest(const char* text, int64_t len, sp_ingest* out) {
   tm.mark("lower");
 }
 
+// ---------------------------------------------------------------------------
+// ONNX ingest: the reference's onnx_ingest package -- wire.py:27-97 (protobuf
+// decoding), model.py:100-167 (structural subset), convert.py:55-274
+// (conversion to the schema-1 document) -- followed by the same build_graph
+// pipeline as JSON documents (= load_graph + trim_and_group of the converted
+// document), or by a schema-1 JSON emission for export_graph.
+
+struct OnnxError : std::runtime_error {
+  int kind;  // SP_ERR_ONNX_PARSE (ModelParseError) / SP_ERR_ONNX_UNSUPPORTED (UnsupportedModel)
+  OnnxError(int k, const std::string& m) : std::runtime_error(m), kind(k) {}
+};
+
+[[noreturn]] void model_error(const std::string& m) { throw OnnxError(SP_ERR_ONNX_PARSE, m); }
+[[noreturn]] void unsupported(const std::string& m) { throw OnnxError(SP_ERR_ONNX_UNSUPPORTED, m); }
+
+// Python repr() of a str: single quotes unless it contains ' and no "
+std::string py_repr(std::string_view s) {
+  const bool dq = s.find('\'') != std::string_view::npos && s.find('"') == std::string_view::npos;
+  const char q = dq ? '"' : '\'';
+  std::string o(1, q);
+  for (char c : s) {
+    if (c == '\\') o += "\\\\";
+    else if (c == q) (o += '\\') += q;
+    else if (c == '\n') o += "\\n";
+    else if (c == '\r') o += "\\r";
+    else if (c == '\t') o += "\\t";
+    else o += c;
+  }
+  return o + q;
+}
+
+struct PbField {
+  uint32_t field = 0;
+  uint8_t wtype = 0;
+  uint64_t v = 0;              // VARINT / FIXED64 / FIXED32
+  const uint8_t* p = nullptr;  // LENGTH payload
+  size_t n = 0;
+};
+
+bool pb_varint(const uint8_t* d, size_t n, size_t& pos, uint64_t& r) {
+  r = 0;
+  int shift = 0;
+  while (true) {
+    if (pos >= n) model_error("not a protobuf model file: truncated varint");
+    const uint8_t b = d[pos++];
+    r |= (uint64_t)(b & 0x7F) << shift;
+    if (!(b & 0x80)) return true;
+    shift += 7;
+    if (shift > 63) model_error("not a protobuf model file: varint exceeds 64 bits");
+  }
+}
+
+// iter_fields / fields_by_number (wire.py:42-83): all fields of a body, in order
+std::vector<PbField> pb_fields(const uint8_t* d, size_t n) {
+  std::vector<PbField> out;
+  size_t pos = 0;
+  while (pos < n) {
+    uint64_t key;
+    pb_varint(d, n, pos, key);
+    PbField f;
+    f.field = (uint32_t)(key >> 3);
+    f.wtype = (uint8_t)(key & 7);
+    if (f.field == 0) model_error("not a protobuf model file: field number 0");
+    if (f.wtype == 0) {
+      pb_varint(d, n, pos, f.v);
+    } else if (f.wtype == 2) {
+      uint64_t sz;
+      pb_varint(d, n, pos, sz);
+      if (sz > n - pos) model_error("not a protobuf model file: truncated length-delimited field");
+      f.p = d + pos;
+      f.n = (size_t)sz;
+      pos += (size_t)sz;
+    } else if (f.wtype == 1) {
+      if (n - pos < 8) model_error("not a protobuf model file: truncated fixed64");
+      std::memcpy(&f.v, d + pos, 8);
+      pos += 8;
+    } else if (f.wtype == 5) {
+      if (n - pos < 4) model_error("not a protobuf model file: truncated fixed32");
+      uint32_t x;
+      std::memcpy(&x, d + pos, 4);
+      f.v = x;
+      pos += 4;
+    } else {
+      model_error("not a protobuf model file: unsupported wire type " + std::to_string(f.wtype));
+    }
+    out.push_back(f);
+  }
+  return out;
+}
+
+const PbField* pb_last(const std::vector<PbField>& fs, uint32_t field) {
+  const PbField* r = nullptr;
+  for (const PbField& f : fs)
+    if (f.field == field) r = &f;
+  return r;
+}
+
+const PbField& pb_body(const PbField& f, const char* what) {
+  if (f.wtype != 2) model_error(std::string("malformed ") + what);
+  return f;
+}
+
+// strict UTF-8 (Python's bytes.decode("utf-8"))
+bool utf8_valid(const uint8_t* s, size_t n) {
+  size_t i = 0;
+  while (i < n) {
+    const uint8_t c = s[i];
+    if (c < 0x80) {
+      i++;
+      continue;
+    }
+    size_t k;
+    uint32_t cp;
+    if ((c & 0xE0) == 0xC0) {
+      k = 1;
+      cp = c & 0x1F;
+    } else if ((c & 0xF0) == 0xE0) {
+      k = 2;
+      cp = c & 0x0F;
+    } else if ((c & 0xF8) == 0xF0) {
+      k = 3;
+      cp = c & 0x07;
+    } else {
+      return false;
+    }
+    if (n - i <= k) return false;
+    for (size_t j = 1; j <= k; j++) {
+      if ((s[i + j] & 0xC0) != 0x80) return false;
+      cp = (cp << 6) | (s[i + j] & 0x3F);
+    }
+    if ((k == 1 && cp < 0x80) || (k == 2 && cp < 0x800) || (k == 3 && (cp < 0x10000 || cp > 0x10FFFF)) ||
+        (cp >= 0xD800 && cp < 0xE000))
+      return false;
+    i += k + 1;
+  }
+  return true;
+}
+
+std::string pb_str(const PbField& f) {
+  if (f.wtype != 2) model_error("malformed string field");
+  if (!utf8_valid(f.p, f.n)) model_error("invalid UTF-8 in string field");
+  return std::string((const char*)f.p, f.n);
+}
+
+struct ODim {
+  bool has_value = false;
+  int64_t value = 0;
+  std::string param;
+};
+struct OValueInfo {
+  std::string name;
+  int64_t elem_type = 0;
+  std::vector<ODim> dims;
+};
+struct OTensor {
+  std::string name;
+  int64_t data_type = 0;
+  std::vector<int64_t> dims;
+  std::vector<int64_t> i64;  // int64 payload (shape operands), decoded for INT64 tensors
+  int64_t num_elements() const {
+    int64_t p = 1;
+    for (int64_t d : dims) p *= d;
+    return p;
+  }
+};
+struct ONode {
+  std::string op_type, name;
+  std::vector<std::string> inputs, outputs;
+  std::vector<std::pair<std::string, int64_t>> attrs_int;
+  bool attr(const char* k, int64_t& v) const {  // dict semantics: the last one wins
+    bool found = false;
+    for (const auto& a : attrs_int)
+      if (a.first == k) {
+        v = a.second;
+        found = true;
+      }
+    return found;
+  }
+};
+
+void packed_varints(const PbField& x, std::vector<int64_t>& out) {
+  size_t pos = 0;
+  while (pos < x.n) {
+    uint64_t r;
+    pb_varint(x.p, x.n, pos, r);
+    out.push_back((int64_t)r);
+  }
+}
+
+// _parse_dims / _parse_value_info / _parse_tensor / _parse_node (model.py:100-140)
+std::vector<ODim> parse_dims(const PbField& shape) {
+  std::vector<ODim> dims;
+  for (const PbField& df : pb_fields(shape.p, shape.n)) {
+    if (df.field != 1) continue;
+    const auto f = pb_fields(pb_body(df, "dimension").p, df.n);
+    ODim d;
+    if (const PbField* v = pb_last(f, 1)) {
+      if (v->wtype == 2) model_error("malformed dimension value");
+      d.has_value = true;
+      d.value = (int64_t)v->v;
+    } else if (const PbField* q = pb_last(f, 2)) {
+      d.param = pb_str(*q);
+    }
+    dims.push_back(std::move(d));
+  }
+  return dims;
+}
+
+OValueInfo parse_value_info(const PbField& body) {
+  const auto f = pb_fields(pb_body(body, "value info").p, body.n);
+  OValueInfo vi;
+  if (const PbField* nm = pb_last(f, 1)) vi.name = pb_str(*nm);
+  if (const PbField* t = pb_last(f, 2)) {
+    const auto tf = pb_fields(pb_body(*t, "type").p, t->n);
+    if (const PbField* tt = pb_last(tf, 1)) {
+      const auto ttf = pb_fields(pb_body(*tt, "tensor type").p, tt->n);
+      if (const PbField* e = pb_last(ttf, 1)) vi.elem_type = (int64_t)e->v;
+      if (const PbField* sh = pb_last(ttf, 2)) vi.dims = parse_dims(pb_body(*sh, "shape"));
+    }
+  }
+  return vi;
+}
+
+OTensor parse_tensor(const PbField& body) {
+  const auto f = pb_fields(pb_body(body, "tensor").p, body.n);
+  OTensor t;
+  for (const PbField& x : f)
+    if (x.field == 1) {
+      if (x.wtype == 2) packed_varints(x, t.dims);
+      else t.dims.push_back((int64_t)x.v);
+    }
+  if (const PbField* dt = pb_last(f, 2)) t.data_type = (int64_t)dt->v;
+  if (const PbField* nm = pb_last(f, 8)) t.name = pb_str(*nm);
+  if (t.data_type == 7) {  // INT64: packed int64_data (7) or little-endian raw_data (9)
+    bool any7 = false;
+    for (const PbField& x : f)
+      if (x.field == 7) {
+        any7 = true;
+        if (x.wtype == 2) packed_varints(x, t.i64);
+        else model_error("malformed int64_data");
+      }
+    if (!any7)
+      if (const PbField* raw = pb_last(f, 9)) {
+        if (raw->wtype != 2) model_error("malformed raw_data");
+        for (size_t i = 0; i < raw->n; i += 8) {
+          const size_t k = std::min<size_t>(8, raw->n - i);
+          uint64_t u = 0;
+          for (size_t j = 0; j < k; j++) u |= (uint64_t)raw->p[i + j] << (8 * j);
+          if (k < 8 && (raw->p[i + k - 1] & 0x80)) u |= ~0ULL << (8 * k);  // int.from_bytes(signed)
+          t.i64.push_back((int64_t)u);
+        }
+      }
+  }
+  return t;
+}
+
+ONode parse_node(const PbField& body) {
+  const auto f = pb_fields(pb_body(body, "node").p, body.n);
+  ONode nd;
+  for (const PbField& x : f) {
+    if (x.field == 1) {
+      nd.inputs.push_back(pb_str(x));
+    } else if (x.field == 2) {
+      nd.outputs.push_back(pb_str(x));
+    } else if (x.field == 5) {
+      const auto a = pb_fields(pb_body(x, "attribute").p, x.n);
+      const PbField* an = pb_last(a, 1);
+      const PbField* av = pb_last(a, 3);
+      if (an && av) {
+        if (av->wtype == 2) model_error("malformed attribute value");
+        nd.attrs_int.emplace_back(pb_str(*an), (int64_t)av->v);
+      }
+    }
+  }
+  if (const PbField* o = pb_last(f, 4)) nd.op_type = pb_str(*o);
+  if (const PbField* nm = pb_last(f, 3)) nd.name = pb_str(*nm);
+  return nd;
+}
+
+// str.strip() on ASCII whitespace, str.strip("/")
+bool py_ws(unsigned char c) { return c == ' ' || (c >= 0x09 && c <= 0x0d) || (c >= 0x1c && c <= 0x1f); }
+std::string strip_ws(const std::string& s) {
+  size_t a = 0, b = s.size();
+  while (a < b && py_ws((unsigned char)s[a])) a++;
+  while (b > a && py_ws((unsigned char)s[b - 1])) b--;
+  return s.substr(a, b - a);
+}
+std::string strip_slash(const std::string& s) {
+  size_t a = 0, b = s.size();
+  while (a < b && s[a] == '/') a++;
+  while (b > a && s[b - 1] == '/') b--;
+  return s.substr(a, b - a);
+}
+std::string ascii_lower(std::string s) {
+  for (char& c : s)
+    if (c >= 'A' && c <= 'Z') c = (char)(c - 'A' + 'a');
+  return s;
+}
+
+struct OutSpec {
+  std::vector<int64_t> shape;
+  std::string dtype;
+};
+struct OutNode {
+  std::string name, op;
+  std::vector<std::string> inputs;
+  OutSpec out;
+  bool has_w = false;
+  OutSpec w;
+  std::string fn;  // attrs {"fn": fn} when non-empty
+};
+struct OnnxResult {
+  std::vector<OutNode> nodes;
+  int64_t trainable = 0, skipped_elements = 0, initializer_elements = 0;
+  std::vector<std::string> skipped, warnings;
+};
+
+const char* dtype_label(int64_t t) { return t == 1 ? "f32" : t == 11 ? "f64" : nullptr; }
+
+
+// parse_model (model.py:143-167) + convert_graph (convert.py:84-269)
+void convert_onnx(const uint8_t* data, size_t n, bool has_batch, int64_t batch, OnnxResult& R) {
+  const auto model = pb_fields(data, n);
+  const PbField* gf = pb_last(model, 7);
+  if (!gf) model_error("model has no graph");
+  const auto g = pb_fields(pb_body(*gf, "graph").p, gf->n);
+  // initializers: dict name -> tensor (first position, last value)
+  std::vector<OTensor> inits;
+  std::unordered_map<std::string, size_t> init_at;
+  for (const PbField& x : g)
+    if (x.field == 5) {
+      OTensor t = parse_tensor(x);
+      if (t.name.empty()) model_error("initializer without a name");
+      auto it = init_at.find(t.name);
+      if (it == init_at.end()) {
+        init_at.emplace(t.name, inits.size());
+        inits.push_back(std::move(t));
+      } else {
+        inits[it->second] = std::move(t);
+      }
+    }
+  if (const PbField* gn = pb_last(g, 2)) (void)pb_str(*gn);
+  std::vector<ONode> nodes;
+  std::vector<OValueInfo> g_in, g_out, g_vi;
+  for (const PbField& x : g) {
+    if (x.field == 1) nodes.push_back(parse_node(x));
+    else if (x.field == 11) g_in.push_back(parse_value_info(x));
+    else if (x.field == 12) g_out.push_back(parse_value_info(x));
+    else if (x.field == 13) g_vi.push_back(parse_value_info(x));
+  }
+  // value_infos dict {vi.name: vi}: first position, last value
+  std::vector<OValueInfo> vinfo;
+  {
+    std::unordered_map<std::string, size_t> at;
+    for (OValueInfo& vi : g_vi) {
+      auto it = at.find(vi.name);
+      if (it == at.end()) {
+        at.emplace(vi.name, vinfo.size());
+        vinfo.push_back(std::move(vi));
+      } else {
+        vinfo[it->second] = std::move(vi);
+      }
+    }
+  }
+  for (const ONode& nd : nodes)
+    if (nd.op_type == "Loop" || nd.op_type == "If" || nd.op_type == "Scan")
+      unsupported("control-flow operator " + nd.op_type + " is not supported");
+  for (const OTensor& t : inits) R.initializer_elements += t.num_elements();
+
+  auto resolve = [&](const std::vector<ODim>& dims, const std::string& owner) {
+    std::vector<int64_t> shape;
+    for (size_t i = 0; i < dims.size(); i++) {
+      if (dims[i].has_value && dims[i].value > 0) {
+        shape.push_back(dims[i].value);
+      } else if (i == 0 && has_batch) {
+        shape.push_back(batch);
+      } else {
+        const std::string label = dims[i].param.empty() ? "?" : dims[i].param;
+        unsupported("dynamic dimension " + py_repr(label) + " in " + py_repr(owner) +
+                    "; static shapes are required (pass --batch N to fix a leading batch dimension)");
+      }
+    }
+    return shape;
+  };
+  // value name -> (shape, dtype label)
+  std::unordered_map<std::string, OutSpec> shapes;
+  auto seed = [&](const OValueInfo& vi) {
+    if (!vi.name.empty() && !vi.dims.empty()) {
+      const char* lab = dtype_label(vi.elem_type);
+      shapes[vi.name] = OutSpec{resolve(vi.dims, vi.name), lab ? lab : "f32"};
+    }
+  };
+  for (const auto& vi : g_in) seed(vi);
+  for (const auto& vi : g_out) seed(vi);
+  for (const auto& vi : vinfo) seed(vi);
+
+  std::unordered_set<std::string> taken;
+  std::unordered_map<std::string, std::string> producer;  // ONNX value -> planner node name
+  std::unordered_set<std::string> consumed;
+  std::unordered_set<std::string> skipped_set;
+
+  auto skip = [&](const OTensor& t, const char* why) {
+    if (skipped_set.insert(t.name).second) {
+      R.skipped.push_back(t.name);
+      R.skipped_elements += t.num_elements();
+      R.warnings.push_back("skipped non-trainable " + py_repr(t.name) + ": " + why);
+    }
+  };
+  auto weight_spec = [&](const OTensor& t, const std::vector<int64_t>* dims) {
+    const char* lab = dtype_label(t.data_type);
+    if (!lab)
+      unsupported("weight " + py_repr(t.name) + " has unsupported element type " + std::to_string(t.data_type));
+    if (consumed.insert(t.name).second) R.trainable += t.num_elements();
+    return OutSpec{dims && !dims->empty() ? *dims : t.dims, lab};
+  };
+  auto emit = [&](const std::string& name, const char* op, std::vector<std::string> ins, const OutSpec& out,
+                  const OutSpec* w, const char* fn) -> std::string {
+    OutNode o;
+    o.name = name;
+    o.op = op;
+    o.inputs = std::move(ins);
+    o.out = out;
+    if (w) {
+      o.has_w = true;
+      o.w = *w;
+    }
+    if (fn) o.fn = fn;
+    R.nodes.push_back(std::move(o));
+    return name;
+  };
+  auto scope_name = [&](const std::string& nm, const std::string& op_type, size_t index) {
+    std::string base = nm.empty() ? std::string() : strip_ws(strip_slash(nm));
+    if (base.empty()) base = "block_" + std::to_string(index) + "/" + ascii_lower(op_type);
+    for (char& c : base)
+      if (c == '\\') c = '/';
+    std::string name = base;
+    int suffix = 1;
+    while (taken.count(name)) {
+      suffix++;
+      name = base + "_" + std::to_string(suffix);
+    }
+    taken.insert(name);
+    return name;
+  };
+
+  for (const OValueInfo& vi : g_in) {
+    if (init_at.count(vi.name)) continue;
+    OutSpec sp;
+    auto it = shapes.find(vi.name);
+    if (it != shapes.end()) {
+      sp = it->second;
+    } else {
+      const char* lab = dtype_label(vi.elem_type);
+      sp = OutSpec{resolve(vi.dims, vi.name), lab ? lab : "f32"};
+    }
+    std::string name = strip_ws(strip_slash(vi.name));
+    if (name.empty()) name = "value";
+    taken.insert(name);
+    producer[vi.name] = emit(name, "input", {}, sp, nullptr, nullptr);
+    shapes[vi.name] = sp;
+  }
+
+  static const std::pair<const char*, const char*> kMap[] = {
+      {"Gemm", "matmul"},           {"MatMul", "matmul"},     {"Add", "elementwise"},    {"Mul", "elementwise"},
+      {"Relu", "elementwise"},      {"LayerNormalization", "layernorm"}, {"Softmax", "softmax"},
+      {"Gather", "embedding"},      {"Reshape", "reshape"},   {"Transpose", "reshape"},  {"Constant", "auxiliary"},
+      {"Identity", "auxiliary"}};
+  for (size_t index = 0; index < nodes.size(); index++) {
+    const ONode& nd = nodes[index];
+    std::string kind;
+    for (const auto& m : kMap)
+      if (nd.op_type == m.first) kind = m.second;
+    if (kind.empty()) {
+      kind = "elementwise";
+      R.warnings.push_back("no mapping for operator " + py_repr(nd.op_type) + "; treating as elementwise");
+    }
+    std::string name = scope_name(nd.name, nd.op_type, index);
+    std::vector<std::string> operands;
+    std::vector<const OTensor*> wts;
+    for (const std::string& v : nd.inputs) {
+      auto it = init_at.find(v);
+      if (it != init_at.end()) wts.push_back(&inits[it->second]);
+      else if (!v.empty()) operands.push_back(v);
+    }
+    for (const std::string& v : operands)
+      if (!producer.count(v)) unsupported("node " + py_repr(name) + " consumes undeclared value " + py_repr(v));
+    std::vector<std::string> in_names;
+    for (const std::string& v : operands) in_names.push_back(producer[v]);
+    auto operand_shape = [&]() -> const OutSpec& {
+      if (operands.empty()) unsupported("node " + py_repr(name) + " has no operand");
+      auto it = shapes.find(operands[0]);
+      if (it == shapes.end()) unsupported("no static shape known for value " + py_repr(operands[0]));
+      return it->second;
+    };
+    const std::string out0 = nd.outputs.empty() ? std::string() : nd.outputs[0];
+    if (nd.outputs.empty()) unsupported("node " + py_repr(name) + " has no output");
+    OutSpec out;
+    OutSpec w;
+    bool has_w = false;
+    const char* fn = nullptr;
+    const OTensor* bias = nullptr;
+    if (kind == "matmul") {
+      if (wts.empty()) unsupported(nd.op_type + " node " + py_repr(name) + " has no constant weight operand");
+      std::vector<int64_t> dims = wts[0]->dims;
+      int64_t tb = 0;
+      if (nd.op_type == "Gemm" && nd.attr("transB", tb) && tb) std::reverse(dims.begin(), dims.end());
+      w = weight_spec(*wts[0], &dims);
+      has_w = true;
+      if (wts.size() > 1) bias = wts[1];
+      const OutSpec& in = operand_shape();
+      if (dims.empty()) unsupported("weight " + py_repr(wts[0]->name) + " has no dimensions");
+      out.shape.assign(in.shape.begin(), in.shape.empty() ? in.shape.end() : in.shape.end() - 1);
+      out.shape.push_back(dims.back());
+      out.dtype = in.dtype;
+    } else if (kind == "embedding") {
+      int64_t axis = 0;
+      nd.attr("axis", axis);
+      if (wts.empty() || axis != 0) {
+        kind = "elementwise";
+        R.warnings.push_back("Gather node " + py_repr(name) + " is not an embedding lookup; treating as elementwise");
+        out = operand_shape();
+      } else {
+        w = weight_spec(*wts[0], nullptr);
+        has_w = true;
+        out.shape = operand_shape().shape;
+        out.shape.insert(out.shape.end(), wts[0]->dims.begin() + (wts[0]->dims.empty() ? 0 : 1), wts[0]->dims.end());
+        out.dtype = w.dtype;
+      }
+    } else if (kind == "layernorm") {
+      out = operand_shape();
+      if (!wts.empty()) {
+        w = weight_spec(*wts[0], nullptr);
+        has_w = true;
+      }
+      if (wts.size() > 1) bias = wts[1];
+    } else if (kind == "reshape") {
+      for (const OTensor* t : wts) skip(*t, "shape operand");
+      out.dtype = operand_shape().dtype;
+      auto it = shapes.find(out0);
+      bool pos = !wts.empty() && !wts[0]->i64.empty();
+      if (pos)
+        for (int64_t v : wts[0]->i64) pos = pos && v > 0;
+      if (it != shapes.end()) {
+        out.shape = it->second.shape;
+      } else if (pos) {
+        out.shape = wts[0]->i64;
+      } else if (nd.op_type == "Transpose") {
+        out.shape = operand_shape().shape;
+        std::reverse(out.shape.begin(), out.shape.end());
+      } else {
+        unsupported("cannot determine output shape of " + py_repr(name));
+      }
+    } else if (kind == "auxiliary") {
+      for (const OTensor* t : wts) skip(*t, "constant payload");
+      if (!operands.empty()) {
+        out = operand_shape();
+      } else {
+        auto it = shapes.find(out0);
+        out = it != shapes.end() ? it->second : OutSpec{{1}, "f32"};
+      }
+    } else {  // elementwise, softmax, fallbacks
+      out = operand_shape();
+      if (kind == "elementwise") {
+        fn = nd.op_type == "Mul" ? "mul" : "add";  // ELEMENTWISE_FN (Add/Relu -> add)
+        if (!wts.empty()) {
+          w = weight_spec(*wts[0], nullptr);
+          has_w = true;
+          for (size_t j = 1; j < wts.size(); j++) skip(*wts[j], "surplus constant operand");
+        }
+      }
+    }
+    if (auto it = shapes.find(out0); it != shapes.end()) out.shape = it->second.shape;
+    emit(name, kind.c_str(), in_names, out, has_w ? &w : nullptr, fn);
+    if (bias) {
+      const std::string bias_name = scope_name(name + "_bias", "Add", index);
+      const OutSpec bw = weight_spec(*bias, nullptr);
+      emit(bias_name, "elementwise", {name}, out, &bw, "add");
+      name = bias_name;
+    }
+    for (size_t j = 0; j < nd.outputs.size(); j++) {
+      producer[nd.outputs[j]] = name;
+      shapes[nd.outputs[j]] = out;
+    }
+  }
+  for (size_t i = 0; i < g_out.size(); i++) {
+    const OValueInfo& vi = g_out[i];
+    auto pit = producer.find(vi.name);
+    if (pit == producer.end()) unsupported("graph output " + py_repr(vi.name) + " is never produced");
+    const OutSpec sp = shapes[vi.name];
+    std::string name = g_out.size() == 1 ? "output" : "output_" + std::to_string(i);
+    while (taken.count(name)) name += "_";
+    taken.insert(name);
+    emit(name, "output", {pit->second}, sp, nullptr, nullptr);
+  }
+  for (const OTensor& t : inits)
+    if (!consumed.count(t.name) && !skipped_set.count(t.name)) skip(t, "unused initializer");
+}
+
+// json.dumps of the converted document (default separators, ensure_ascii)
+void json_str(std::string& o, std::string_view s) {
+  static const char* hex = "0123456789abcdef";
+  o += '"';
+  size_t i = 0;
+  while (i < s.size()) {
+    const unsigned char c = (unsigned char)s[i];
+    if (c == '"') o += "\\\"";
+    else if (c == '\\') o += "\\\\";
+    else if (c == '\n') o += "\\n";
+    else if (c == '\r') o += "\\r";
+    else if (c == '\t') o += "\\t";
+    else if (c == '\b') o += "\\b";
+    else if (c == '\f') o += "\\f";
+    else if (c < 0x20) {
+      o += "\\u00";
+      o += hex[c >> 4];
+      o += hex[c & 15];
+    } else if (c < 0x80) {
+      o += (char)c;
+    } else {  // decode UTF-8, emit \uXXXX (surrogate pairs above the BMP)
+      uint32_t cp;
+      size_t k;
+      if ((c & 0xE0) == 0xC0) { cp = c & 0x1F; k = 1; }
+      else if ((c & 0xF0) == 0xE0) { cp = c & 0x0F; k = 2; }
+      else { cp = c & 0x07; k = 3; }
+      for (size_t j = 1; j <= k && i + j < s.size(); j++) cp = (cp << 6) | ((unsigned char)s[i + j] & 0x3F);
+      i += k;
+      auto u16 = [&](uint32_t u) {
+        o += "\\u";
+        for (int sh = 12; sh >= 0; sh -= 4) o += hex[(u >> sh) & 15];
+      };
+      if (cp >= 0x10000) {
+        cp -= 0x10000;
+        u16(0xD800 + (cp >> 10));
+        u16(0xDC00 + (cp & 0x3FF));
+      } else {
+        u16(cp);
+      }
+    }
+    i++;
+  }
+  o += '"';
+}
+
+void json_shape(std::string& o, const OutSpec& s, bool trainable) {
+  o += "{\"shape\": [";
+  for (size_t i = 0; i < s.shape.size(); i++) {
+    if (i) o += ", ";
+    o += std::to_string(s.shape[i]);
+  }
+  o += "], \"dtype\": ";
+  json_str(o, s.dtype);
+  o += trainable ? ", \"trainable\": true}" : ", \"trainable\": false}";
+}
+
+std::string onnx_json(const OnnxResult& R) {
+  std::string o = "{\"version\": 1, \"nodes\": [";
+  for (size_t k = 0; k < R.nodes.size(); k++) {
+    const OutNode& nd = R.nodes[k];
+    if (k) o += ", ";
+    o += "{\"name\": ";
+    json_str(o, nd.name);
+    o += ", \"op\": ";
+    json_str(o, nd.op);
+    o += ", \"inputs\": [";
+    for (size_t j = 0; j < nd.inputs.size(); j++) {
+      if (j) o += ", ";
+      json_str(o, nd.inputs[j]);
+    }
+    o += "], \"weight\": ";
+    if (nd.has_w) json_shape(o, nd.w, true);
+    else o += "null";
+    o += ", \"output\": ";
+    json_shape(o, nd.out, false);
+    if (!nd.fn.empty()) {
+      o += ", \"attrs\": {\"fn\": ";
+      json_str(o, nd.fn);
+      o += "}";
+    }
+    o += "}";
+  }
+  return o + "]}";
+}
+
+// load_graph semantics of the converted document, straight into build_graph
+void onnx_to_graph(const OnnxResult& R, sp_ingest* out) {
+  PhaseTimer tm;
+  const size_t n = R.nodes.size();
+  std::vector<Raw> raw(n);
+  std::vector<std::vector<std::string_view>> in_names(n);
+  auto spec = [](const OutSpec& s, bool trainable) {
+    Spec t;
+    for (int64_t d : s.shape) t.shape.push_back(d);
+    t.width = s.dtype == "f64" ? 8 : 4;
+    t.trainable = trainable;
+    if (t.shape.empty()) parse_error("tensor shape must be non-empty");
+    if (t.shape.nonpos) parse_error("tensor dimensions must be positive integers");
+    return t;
+  };
+  for (size_t k = 0; k < n; k++) {
+    const OutNode& nd = R.nodes[k];
+    Raw& r = raw[k];
+    r.name = nd.name;
+    r.op = ELEMENTWISE;
+    for (int q = 0; q < 10; q++)
+      if (nd.op == kOpLabels[q]) r.op = (Op)q;
+    for (const std::string& s : nd.inputs) in_names[k].push_back(s);
+    r.out = spec(nd.out, false);
+    if (nd.has_w) {
+      r.w = spec(nd.w, true);
+      r.has_w = true;
+    }
+  }
+  build_graph(raw, in_names, out, tm);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1118,5 +1849,62 @@ int sp_ingest_view(const sp_ingest* g, sp_graph* v, int64_t* n_raw, int64_t* n_a
 }
 
 void sp_ingest_free(sp_ingest* g) { delete g; }
+
+int sp_ingest_onnx(const uint8_t* data, int64_t len, int32_t has_batch, int64_t batch, int32_t export_only,
+                   sp_ingest** out) {
+  if (!data || len < 0 || !out) return SP_ERR_CONFIG;
+  *out = nullptr;
+  sp_ingest* g = new sp_ingest();
+  try {
+    OnnxResult R;
+    convert_onnx(data, (size_t)len, has_batch != 0, batch, R);
+    g->trainable = R.trainable;
+    g->skipped_elements = R.skipped_elements;
+    g->initializer_elements = R.initializer_elements;
+    g->warnings = R.warnings;
+    g->skipped = R.skipped;
+    if (export_only) g->json = onnx_json(R);
+    else onnx_to_graph(R, g);
+  } catch (const OnnxError& e) {
+    t_err = e.what();
+    t_err_a.clear();
+    t_err_b.clear();
+    delete g;
+    return e.kind;
+  } catch (const IngestError& e) {
+    t_err = e.what();
+    t_err_a = e.a;
+    t_err_b = e.b;
+    delete g;
+    return e.kind;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    t_err_a.clear();
+    t_err_b.clear();
+    delete g;
+    return SP_ERR_ONNX_PARSE;
+  }
+  *out = g;
+  return SP_OK;
+}
+
+int sp_ingest_report(const sp_ingest* g, int64_t* counts) {
+  if (!g || !counts) return SP_ERR_CONFIG;
+  counts[0] = g->trainable;
+  counts[1] = g->skipped_elements;
+  counts[2] = g->initializer_elements;
+  counts[3] = (int64_t)g->warnings.size();
+  counts[4] = (int64_t)g->skipped.size();
+  counts[5] = (int64_t)g->json.size();
+  return SP_OK;
+}
+
+const char* sp_ingest_text(const sp_ingest* g, int32_t kind, int64_t i) {
+  if (!g) return nullptr;
+  if (kind == 0) return g->json.c_str();
+  if (kind == 1 && i >= 0 && i < (int64_t)g->warnings.size()) return g->warnings[i].c_str();
+  if (kind == 2 && i >= 0 && i < (int64_t)g->skipped.size()) return g->skipped[i].c_str();
+  return nullptr;
+}
 
 }  // extern "C"

@@ -171,42 +171,47 @@ def load_lowered(source: Union[bytes, str, "os.PathLike"]) -> IngestedGraph:
     if rc:
         _raise(L, rc)
     try:
-        v = SpGraph()
-        n_raw, n_aux = C.c_int64(), C.c_int64()
-        L.sp_ingest_view(h, C.byref(v), C.byref(n_raw), C.byref(n_aux))
-        n = int(v.n_nodes)
-
-        def arr(p, count, dtype, shape=None):
-            a = np.ctypeslib.as_array(p, shape=(max(count, 1),))[:count].copy()
-            return a.astype(dtype, copy=False) if shape is None else a.reshape(shape)
-
-        name_off = arr(v.name_off, n + 1, np.int64)
-        nb = int(name_off[-1])
-        name_bytes = np.ctypeslib.as_array(v.name_bytes, shape=(max(nb, 1),))[:nb].copy()
-        E = int(arr(v.in_off, n + 1, np.int64)[-1])
-        raw = name_bytes.tobytes()
-        ascii_names = raw.isascii()
-        text_names = raw.decode("ascii" if ascii_names else "utf-8")
-        if ascii_names:
-            offs = name_off.tolist()
-            names = [text_names[a:b] for a, b in zip(offs[:-1], offs[1:])]
-        else:
-            offs = name_off.tolist()
-            names = [raw[a:b].decode("utf-8") for a, b in zip(offs[:-1], offs[1:])]
-        low = LoweredGraph(
-            names=names, index_=None, name_bytes=name_bytes, name_off=name_off,
-            topo_rank=arr(v.topo_rank, n, np.int64), op=arr(v.op, n, np.uint8),
-            act_rank=arr(v.act_rank, n, np.uint8), act_shape=arr(v.act_shape, n * MAX_RANK, np.int64,
-                                                                 (n, MAX_RANK)),
-            act_bytes=arr(v.act_bytes, n, np.int64), w_rank=arr(v.w_rank, n, np.uint8),
-            w_shape=arr(v.w_shape, n * MAX_RANK, np.int64, (n, MAX_RANK)), w_bytes=arr(v.w_bytes, n, np.int64),
-            w_trainable=arr(v.w_trainable, n, np.uint8), in_off=arr(v.in_off, n + 1, np.int64),
-            in_idx=arr(v.in_idx, E, np.int32) if E else np.zeros(0, np.int32),
-        )
-        low.ascii = ascii_names
-        return IngestedGraph(low, int(n_raw.value), int(n_aux.value))
+        return _graph_from_handle(L, h)
     finally:
         L.sp_ingest_free(h)
+
+
+def _graph_from_handle(L, h) -> IngestedGraph:
+    """IngestedGraph copied out of an sp_ingest handle (the caller frees it)."""
+    v = SpGraph()
+    n_raw, n_aux = C.c_int64(), C.c_int64()
+    L.sp_ingest_view(h, C.byref(v), C.byref(n_raw), C.byref(n_aux))
+    n = int(v.n_nodes)
+
+    def arr(p, count, dtype, shape=None):
+        a = np.ctypeslib.as_array(p, shape=(max(count, 1),))[:count].copy()
+        return a.astype(dtype, copy=False) if shape is None else a.reshape(shape)
+
+    name_off = arr(v.name_off, n + 1, np.int64)
+    nb = int(name_off[-1])
+    name_bytes = np.ctypeslib.as_array(v.name_bytes, shape=(max(nb, 1),))[:nb].copy()
+    E = int(arr(v.in_off, n + 1, np.int64)[-1])
+    raw = name_bytes.tobytes()
+    ascii_names = raw.isascii()
+    text_names = raw.decode("ascii" if ascii_names else "utf-8")
+    if ascii_names:
+        offs = name_off.tolist()
+        names = [text_names[a:b] for a, b in zip(offs[:-1], offs[1:])]
+    else:
+        offs = name_off.tolist()
+        names = [raw[a:b].decode("utf-8") for a, b in zip(offs[:-1], offs[1:])]
+    low = LoweredGraph(
+        names=names, index_=None, name_bytes=name_bytes, name_off=name_off,
+        topo_rank=arr(v.topo_rank, n, np.int64), op=arr(v.op, n, np.uint8),
+        act_rank=arr(v.act_rank, n, np.uint8), act_shape=arr(v.act_shape, n * MAX_RANK, np.int64,
+                                                             (n, MAX_RANK)),
+        act_bytes=arr(v.act_bytes, n, np.int64), w_rank=arr(v.w_rank, n, np.uint8),
+        w_shape=arr(v.w_shape, n * MAX_RANK, np.int64, (n, MAX_RANK)), w_bytes=arr(v.w_bytes, n, np.int64),
+        w_trainable=arr(v.w_trainable, n, np.uint8), in_off=arr(v.in_off, n + 1, np.int64),
+        in_idx=arr(v.in_idx, E, np.int32) if E else np.zeros(0, np.int32),
+    )
+    low.ascii = ascii_names
+    return IngestedGraph(low, int(n_raw.value), int(n_aux.value))
 
 
 def plan_from_json(source, mesh, min_duplicates: int = 2, mu: int = 1 << 20, chunk_size: int = 4 << 20,
@@ -215,3 +220,109 @@ def plan_from_json(source, mesh, min_duplicates: int = 2, mu: int = 1 << 20, chu
     from .search import derive_plan
 
     return derive_plan(load_lowered(source), mesh, min_duplicates, mu, chunk_size, **kw)
+
+
+# ---------------------------------------------------------------------------
+# ONNX (onnx_ingest: wire.py / model.py / convert.py)
+
+SP_ERR_ONNX_PARSE, SP_ERR_ONNX_UNSUPPORTED = 9, 10
+
+
+class ModelParseError(ValueError):
+    """File is not a readable ONNX model (onnx_ingest/model.py:21-22)."""
+
+
+class UnsupportedModel(ValueError):
+    """Dynamic shapes, control flow or an unconvertible idiom (onnx_ingest/convert.py:37-38)."""
+
+
+class ConversionReport:
+    """Field-for-field ConversionReport (convert.py:41-47)."""
+
+    def __init__(self, trainable_elements=0, skipped_elements=0, skipped=None, warnings=None,
+                 initializer_elements=0):
+        self.trainable_elements = trainable_elements
+        self.skipped_elements = skipped_elements
+        self.skipped = list(skipped or [])
+        self.warnings = list(warnings or [])
+        self.initializer_elements = initializer_elements
+
+    def __eq__(self, other):
+        return vars(self) == vars(other)
+
+    def __repr__(self):
+        return f"ConversionReport({vars(self)!r})"
+
+
+def _onnx_lib():
+    L = _lib()
+    if not hasattr(L, "_sp_onnx_declared"):
+        vp = C.c_void_p
+        L.sp_ingest_onnx.argtypes = [C.c_char_p, C.c_int64, C.c_int32, C.c_int64, C.c_int32, C.POINTER(vp)]
+        L.sp_ingest_onnx.restype = C.c_int
+        L.sp_ingest_report.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.sp_ingest_report.restype = C.c_int
+        L.sp_ingest_text.argtypes = [vp, C.c_int32, C.c_int64]
+        L.sp_ingest_text.restype = C.c_void_p
+        L._sp_onnx_declared = True
+    return L
+
+
+def _onnx_call(data: bytes, batch, export_only: bool):
+    L = _onnx_lib()
+    h = C.c_void_p()
+    rc = L.sp_ingest_onnx(data, len(data), 0 if batch is None else 1, int(batch or 0), 1 if export_only else 0,
+                          C.byref(h))
+    if rc == SP_ERR_ONNX_PARSE:
+        raise ModelParseError((L.sp_ingest_error(0) or b"").decode("utf-8", "replace"))
+    if rc == SP_ERR_ONNX_UNSUPPORTED:
+        raise UnsupportedModel((L.sp_ingest_error(0) or b"").decode("utf-8", "replace"))
+    if rc:
+        _raise(L, rc)
+    counts = (C.c_int64 * 6)()
+    L.sp_ingest_report(h, counts)
+
+    def text(kind, i=0, size=None):
+        p = L.sp_ingest_text(h, kind, i)
+        return C.string_at(p, size).decode("utf-8") if size is not None else C.string_at(p).decode("utf-8")
+
+    report = ConversionReport(int(counts[0]), int(counts[1]), [text(2, i) for i in range(counts[4])],
+                              [text(1, i) for i in range(counts[3])], int(counts[2]))
+    return h, report, (text(0, 0, int(counts[5])) if export_only else None)
+
+
+def export_graph(data: bytes, batch=None):
+    """ONNX model bytes -> (schema-1 JSON document, ConversionReport), natively
+    (onnx_ingest.export_graph, convert.py:272-274)."""
+    import json
+
+    h, report, text = _onnx_call(bytes(data), batch, True)
+    _lib().sp_ingest_free(h)
+    return json.loads(text), report
+
+
+def export_graph_json(data: bytes, batch=None) -> tuple:
+    """As export_graph, with the document as the exact `json.dumps` text."""
+    h, report, text = _onnx_call(bytes(data), batch, True)
+    _lib().sp_ingest_free(h)
+    return text, report
+
+
+def load_onnx(data: bytes, batch=None) -> IngestedGraph:
+    """ONNX bytes -> grouped graph arrays, natively: export_graph + load_graph +
+    trim_and_group without the intermediate document or Python objects."""
+    h, report, _ = _onnx_call(bytes(data), batch, False)
+    try:
+        g = _graph_from_handle(_lib(), h)
+    finally:
+        _lib().sp_ingest_free(h)
+    g.report = report
+    return g
+
+
+def plan_from_onnx(data: bytes, mesh, batch=None, min_duplicates: int = 2, mu: int = 1 << 20,
+                   chunk_size: int = 4 << 20, **kw):
+    """ONNX model -> plan (onnx_ingest export_graph | shardplan plan), natively + device search."""
+    from .search import derive_plan
+
+    return derive_plan(load_onnx(data, batch), mesh, min_duplicates, mu, chunk_size, **kw)

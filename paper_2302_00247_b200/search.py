@@ -655,3 +655,82 @@ def plan_cost(routed, graph, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
         raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
     full = _explain_plan(graph, routed.plan, mesh, mu, chunk_size, types, session)
     return full.cost
+
+
+# ---------------------------------------------------------------------------
+# plan replay (search.py:382-444): the "resume" path of a stored plan file
+
+
+def routed_plan_for_assignments(graph, mesh, assignments: dict, min_duplicates: int = 2, mu: int = 1 << 20,
+                                chunk_size: int = 4 << 20, *, types: TypeSet = DEFAULT_TYPES,
+                                backend: Optional[Backend] = None, session: Optional[Session] = None):
+    """Re-route a plan loaded from a report file (assignment labels only), on the
+    device: the fold, then every block's stored assignment routed and costed in
+    ONE explain launch (search.py:411-444 loops pattern_routing + plan_cost)."""
+    from .errors import ShardplanError
+
+    ses = session or Session.open(graph, backend)
+    if min_duplicates < 1:
+        raise BadConfig("min_duplicates must be >= 1")
+    ba = ses.backend.fold(ses.dgraph, int(min_duplicates))
+    subs = subgraphs_from_blocks(ses.low, ba, types)
+    csr = ba.templates_csr()
+    prep = route_prep(ses, subs, types, csr)
+    # stored labels -> candidate index in the reference's enumeration order
+    indices = []
+    for sub, (slot_pos, radices, _, _) in zip(subs, prep):
+        index = 0
+        for q, r in zip(slot_pos, radices):
+            spec = types.ShardSpec.from_label(assignments[sub.template[q]])
+            kind = spec.kind.value if hasattr(spec.kind, "value") else spec.kind
+            d = 0 if kind == "replica" else (spec.axis + 1 if kind == "split" else -1)
+            if not 0 <= d < r:
+                # not a search option: no pattern matches that weight spec
+                node = sub.template[q]
+                raise ShardplanError(f"stored plan does not route at node {node}: "
+                                     f"no pattern matches weight spec {spec.label}")
+            index = index * r + d
+        indices.append(index)
+    off, nodes = csr
+    tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
+    try:
+        detail = ses.backend.explain_all(tables, indices)
+        for b, X in enumerate(detail[0]):
+            if not X.valid:
+                raise ShardplanError(f"stored plan does not route at node {subs[b].template[X.fail_pos]}: "
+                                     "no pattern chains from producer states")
+            if mu > chunk_size:
+                raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
+        bests = routed_plans_all(ses, tables, subs, [_OneScore(i) for i in indices], mesh, types, detail, prep)
+    finally:
+        tables.close()
+    results = []
+    total_cost = 0.0
+    for sub, routed in zip(subs, bests):
+        plan = types.CandidatePlan(sub, routed.plan.assignments, -1)
+        routed = types.RoutedPlan(plan, routed.routings, routed.exit_conversions, routed.cost)
+        results.append(types.SubgraphResult(sub, routed, 1, 1))
+        total_cost += routed.cost.total * sub.multiplicity
+    return types.BestPlanReport(mesh, min_duplicates, results, dict(assignments), total_cost, 0, 0)
+
+
+def broadcast_routing(report, types: TypeSet = DEFAULT_TYPES) -> dict:
+    """Whole-graph routing map: each winning template routing replayed on every
+    instance with prefix-swapped producer scopes (search.py:382-408)."""
+    out: dict = {}
+    NodeRouting = types.NodeRouting
+    for res in report.results:
+        sub = res.subgraph
+        tp = sub.template_prefix
+        for prefix, _ in sub.instances:
+            swap = (lambda s: s) if prefix == tp else (lambda s, p=prefix, n=len(tp): p + s[n:])
+            for r in res.best.routings:
+                scope = swap(r.scope)
+                out[scope] = NodeRouting(scope, r.pattern, tuple((swap(p), c, b) for p, c, b in r.input_conversions),
+                                         r.output_collective, r.output_bytes, r.state)
+            for scope, coll, _ in res.best.exit_conversions:
+                s = swap(scope)
+                r = out[s]
+                out[s] = NodeRouting(r.scope, r.pattern, r.input_conversions, r.output_collective, r.output_bytes,
+                                     r.state, exit_conversion=coll)
+    return out

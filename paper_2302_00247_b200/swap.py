@@ -27,7 +27,7 @@ from . import errors as our_errors
 from . import search as ours
 from .api_types import TypeSet
 
-_ENTRY_POINTS = ("derive_plan", "prune_graph", "search_subgraph")
+_ENTRY_POINTS = ("derive_plan", "prune_graph", "search_subgraph", "routed_plan_for_assignments")
 
 
 def reference_types(shardplan) -> TypeSet:
@@ -101,6 +101,7 @@ def install(shardplan=None, backend=None) -> Installed:
         "derive_plan": wrap(ours.derive_plan),
         "prune_graph": wrap(ours.prune_graph),
         "search_subgraph": wrap(ours.search_subgraph),
+        "routed_plan_for_assignments": wrap(ours.routed_plan_for_assignments),
     }
     handle = Installed(shardplan)
     for modname in ("search", "cli", ""):

@@ -507,3 +507,50 @@ def test_plan_cost_matches_reference_tables(backend):
             assert isinstance(routed, RoutingFailure)
         else:
             assert plan_cost(routed, g, m).total == total
+
+
+# -- plan replay (search.py:382-444) ---------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["c1_1x8", "c2_1x8", "chain6_2x4_mu", "crit5_slow", "tiny_2x2", "c3_2x4_slow",
+                                  "tiny_min1_2x2", "encdec34"])
+def test_replay_reproduces_the_search(backend, name):
+    """routed_plan_for_assignments on the assignments of a search report
+    reproduces every block's RoutedPlan and CostReport and the total cost;
+    broadcast_routing covers every GraphNode once."""
+    from paper_2302_00247_b200.search import broadcast_routing, derive_plan, routed_plan_for_assignments
+
+    c = case(name)
+    g, m = graph(c["graph"]), mesh(c["mesh"])
+    rep = derive_plan(g, m, min_duplicates=c["min_dup"], mu=c["mu"], chunk_size=c["chunk_size"], backend=backend)
+    rp = routed_plan_for_assignments(g, m, rep.assignments, min_duplicates=c["min_dup"], mu=c["mu"],
+                                     chunk_size=c["chunk_size"], backend=backend)
+    assert rp.total_cost == rep.total_cost and (rp.candidates, rp.valid) == (0, 0)
+    for a, b in zip(rp.results, rep.results):
+        assert (a.candidates, a.valid) == (1, 1)
+        assert a.best.plan.assignments == b.best.plan.assignments and a.best.plan.index == -1
+        assert a.best.routings == b.best.routings and a.best.exit_conversions == b.best.exit_conversions
+        assert a.best.cost == b.best.cost
+    routing = broadcast_routing(rep)
+    assert set(routing) == set(g.nodes)
+    for res in rep.results:
+        for r in res.best.routings:
+            assert routing[r.scope].pattern == r.pattern
+
+
+def test_replay_rejects_unroutable_and_bad_labels(backend):
+    from paper_2302_00247_b200.errors import ShardplanError
+    from paper_2302_00247_b200.search import derive_plan, routed_plan_for_assignments
+
+    c = case("c1_1x8")
+    g, m = graph(c["graph"]), mesh(c["mesh"])
+    rep = derive_plan(g, m, backend=backend)
+    bad = dict(rep.assignments)
+    k = next(s for s, lab in bad.items() if lab == "replica")
+    bad[k] = "split7"
+    with pytest.raises(ShardplanError):
+        routed_plan_for_assignments(g, m, bad, backend=backend)
+    missing = dict(rep.assignments)
+    missing.pop(k)
+    with pytest.raises(KeyError):
+        routed_plan_for_assignments(g, m, missing, backend=backend)

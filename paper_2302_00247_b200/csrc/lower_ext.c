@@ -16,6 +16,14 @@
 #include <Python.h>
 #include <stdint.h>
 #include <string.h>
+#include <time.h>
+
+static double now_ms(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+
 
 #define MAX_RANK 8
 #define CACHE_N 64
@@ -149,10 +157,61 @@ static int read_shape(PyObject* shape, int64_t* dims, int* rank, int64_t* elems,
 static PyObject* new_bytearray(Py_ssize_t n) { return PyByteArray_FromStringAndSize(NULL, n > 0 ? n : 0); }
 
 /*
+ * Attribute read with a fast path for __slots__ classes (this package's IR
+ * types): the member descriptor's offset is resolved once per (type, name)
+ * and the value read straight from the instance; any other class goes
+ * through PyObject_GetAttr.  Returns a new reference.
+ */
+typedef struct {
+  PyObject* name;
+  PyTypeObject* type;
+  Py_ssize_t offset;  /* -1: generic getattr */
+} FieldRef;
+
+static PyObject* field_get(FieldRef* f, PyObject* obj) {
+  PyTypeObject* tp = Py_TYPE(obj);
+  if (tp != f->type) {
+    f->type = tp;
+    f->offset = -1;
+    PyObject* d = PyObject_GetAttr((PyObject*)tp, f->name);
+    if (d) {
+      if (Py_IS_TYPE(d, &PyMemberDescr_Type)) {
+        PyMemberDef* m = ((PyMemberDescrObject*)d)->d_member;
+        if (m->type == Py_T_OBJECT_EX && !(m->flags & Py_RELATIVE_OFFSET)) f->offset = m->offset;
+      }
+      Py_DECREF(d);
+    } else {
+      PyErr_Clear();
+    }
+  }
+  if (f->offset >= 0) {
+    PyObject* v = *(PyObject**)((char*)obj + f->offset);
+    if (v) {
+      Py_INCREF(v);
+      return v;
+    }
+  }
+  return PyObject_GetAttr(obj, f->name);
+}
+
+/* reference on an object, kept in `keep` (new references released at the end) */
+#define KEEP(slot, expr)                    \
+  do {                                      \
+    PyObject* _v = (expr);                  \
+    if (!_v) goto done;                     \
+    (slot) = _v;                            \
+  } while (0)
+
+/*
  * lower_arrays(topo_order, nodes, op_code, dtype_width)
  * -> (names, ascii, max_act_rank, max_w_rank, overflow_what,
  *     name_bytes, name_off, op, act_rank, act_shape, act_bytes,
  *     w_rank, w_shape, w_bytes, w_trainable, in_off, in_idx)
+ *
+ * The walk is a sequence of passes over pointer arrays (nodes, then their
+ * fields, then the fields' fields) rather than one dependent chain per node:
+ * the loads of a pass are independent across nodes, so the core overlaps the
+ * cache misses of the scattered Python objects.
  */
 static PyObject* lower_arrays(PyObject* self, PyObject* args) {
   PyObject *topo, *nodes, *op_fn, *width_fn;
@@ -165,7 +224,13 @@ static PyObject* lower_arrays(PyObject* self, PyObject* args) {
            *b_wrank = NULL, *b_wshape = NULL, *b_wbytes = NULL, *b_wtrain = NULL, *b_inoff = NULL, *b_inidx = NULL;
   PyObject* result = NULL;
   PtrCache opc = {{0}, {0}, 0}, wc = {{0}, {0}, 0};
-  static PyObject *s_op, *s_inputs, *s_activation, *s_weight, *s_shape, *s_dtype, *s_trainable;
+  /* per-node object arrays: 0 node, 1 op, 2 activation, 3 weight, 4 inputs,
+     5 act shape, 6 act dtype, 7 w shape, 8 w dtype, 9 w trainable */
+  enum { K_NODE, K_OP, K_ACT, K_W, K_IN, K_ASH, K_ADT, K_WSH, K_WDT, K_WTR, K_N };
+  PyObject** obj = NULL;
+  int32_t* inidx = NULL;
+  static PyObject *s_op, *s_inputs, *s_activation, *s_weight, *s_shape, *s_dtype, *s_trainable, *s_member,
+      *s_output;
   if (!s_op) {
     s_op = PyUnicode_InternFromString("op");
     s_inputs = PyUnicode_InternFromString("inputs");
@@ -174,9 +239,25 @@ static PyObject* lower_arrays(PyObject* self, PyObject* args) {
     s_shape = PyUnicode_InternFromString("shape");
     s_dtype = PyUnicode_InternFromString("dtype");
     s_trainable = PyUnicode_InternFromString("trainable");
+    s_member = PyUnicode_InternFromString("member");
+    s_output = PyUnicode_InternFromString("output");
   }
+  FieldRef f_op = {s_op, NULL, -1}, f_inputs = {s_inputs, NULL, -1}, f_act = {s_activation, NULL, -1},
+           f_weight = {s_weight, NULL, -1}, a_shape = {s_shape, NULL, -1}, a_dtype = {s_dtype, NULL, -1},
+           w_shape_f = {s_shape, NULL, -1}, w_dtype_f = {s_dtype, NULL, -1}, w_train_f = {s_trainable, NULL, -1},
+           f_member = {s_member, NULL, -1}, m_op = {s_op, NULL, -1}, m_out = {s_output, NULL, -1},
+           m_weight = {s_weight, NULL, -1};
+  const int trace = getenv("SP_LOWER_TRACE") != NULL;
+  double tm[8];
+  tm[0] = now_ms();
   if (namemap_init(&index, n) < 0) goto done;
-  /* pass 1: name -> index map, name byte count */
+  obj = (PyObject**)PyMem_Calloc((size_t)(n ? n : 1) * K_N, sizeof(PyObject*));
+  if (!obj) {
+    PyErr_NoMemory();
+    goto done;
+  }
+#define O(i, k) obj[(size_t)(i) * K_N + (k)]
+  /* pass 1: names -> row map, name bytes; node objects (borrowed from the dict) */
   Py_ssize_t nbytes = 0, E = 0;
   int ascii = 1;
   for (Py_ssize_t i = 0; i < n; i++) {
@@ -191,6 +272,54 @@ static PyObject* lower_arrays(PyObject* self, PyObject* args) {
     nbytes += L;
     if (namemap_put(&index, nm, (int32_t)i) < 0) goto done;
   }
+  tm[1] = now_ms();
+  for (Py_ssize_t i = 0; i < n; i++) {
+    PyObject* nm = PyList_GET_ITEM(names, i);
+    PyObject* node = PyDict_GetItemWithError(nodes, nm);
+    if (!node) {
+      if (!PyErr_Occurred()) PyErr_SetObject(PyExc_KeyError, nm);
+      goto done;
+    }
+    Py_INCREF(node);
+    O(i, K_NODE) = node;
+  }
+  /* pass 2: op / activation / weight / inputs (the reference's GraphNode
+     exposes op/activation/weight as properties over its RawNode `member`,
+     ir.py:164-202: read the member's fields instead) */
+  tm[2] = now_ms();
+  const int via_member = n > 0 && PyObject_HasAttr(O(0, K_NODE), s_member);
+  for (Py_ssize_t i = 0; i < n; i++) {
+    PyObject* node = O(i, K_NODE);
+    PyObject* src = node;
+    if (via_member) KEEP(src, field_get(&f_member, node));
+    PyObject *o = field_get(via_member ? &m_op : &f_op, src), *a = o ? field_get(via_member ? &m_out : &f_act, src) : NULL;
+    PyObject* w = a ? field_get(via_member ? &m_weight : &f_weight, src) : NULL;
+    PyObject* in = w ? field_get(&f_inputs, node) : NULL;
+    if (via_member) Py_DECREF(src);
+    if (!in) {
+      Py_XDECREF(o);
+      Py_XDECREF(a);
+      Py_XDECREF(w);
+      goto done;
+    }
+    O(i, K_OP) = o;
+    O(i, K_ACT) = a;
+    O(i, K_W) = w;
+    O(i, K_IN) = in;
+  }
+  tm[3] = now_ms();
+  /* pass 3: tensor spec fields */
+  for (Py_ssize_t i = 0; i < n; i++) {
+    KEEP(O(i, K_ASH), field_get(&a_shape, O(i, K_ACT)));
+    KEEP(O(i, K_ADT), field_get(&a_dtype, O(i, K_ACT)));
+    PyObject* w = O(i, K_W);
+    if (w != Py_None) {
+      KEEP(O(i, K_WSH), field_get(&w_shape_f, w));
+      KEEP(O(i, K_WDT), field_get(&w_dtype_f, w));
+      KEEP(O(i, K_WTR), field_get(&w_train_f, w));
+    }
+  }
+  tm[4] = now_ms();
   b_names = new_bytearray(nbytes);
   b_noff = new_bytearray((n + 1) * 8);
   b_op = new_bytearray(n);
@@ -216,100 +345,58 @@ static PyObject* lower_arrays(PyObject* self, PyObject* args) {
   int64_t* wbytes = (int64_t*)PyByteArray_AS_STRING(b_wbytes);
   uint8_t* wtrain = (uint8_t*)PyByteArray_AS_STRING(b_wtrain);
   int64_t* inoff = (int64_t*)PyByteArray_AS_STRING(b_inoff);
-  /* in_idx grows as inputs are seen (E unknown until the node pass) */
-  Py_ssize_t cap = n * 2 + 16;
-  int32_t* inidx = (int32_t*)PyMem_Malloc((size_t)cap * sizeof(int32_t));
-  if (!inidx) {
-    PyErr_NoMemory();
-    goto done;
-  }
   int max_ar = 0, max_wr = 0;
   const char* overflow = NULL;
+  /* pass 4: values */
   Py_ssize_t off = 0;
   noff[0] = 0;
-  inoff[0] = 0;
   for (Py_ssize_t i = 0; i < n; i++) {
-    PyObject* nm = PyList_GET_ITEM(names, i);
     Py_ssize_t L;
-    const char* u = PyUnicode_AsUTF8AndSize(nm, &L);
+    const char* u = PyUnicode_AsUTF8AndSize(PyList_GET_ITEM(names, i), &L);
     memcpy(pn + off, u, (size_t)L);
     off += L;
     noff[i + 1] = off;
-    PyObject* node = PyDict_GetItemWithError(nodes, nm);
-    if (!node) {
-      if (!PyErr_Occurred()) PyErr_SetObject(PyExc_KeyError, nm);
-      goto fail_idx;
-    }
     long v;
-    PyObject* o = PyObject_GetAttr(node, s_op);
-    if (!o) goto fail_idx;
-    int rc = cache_get_any(&opc, o, op_fn, &v);
-    Py_DECREF(o);
-    if (rc < 0) goto fail_idx;
+    if (cache_get_any(&opc, O(i, K_OP), op_fn, &v) < 0) goto done;
     op[i] = (uint8_t)v;
-    /* activation */
-    PyObject* act = PyObject_GetAttr(node, s_activation);
-    if (!act) goto fail_idx;
-    PyObject* shp = PyObject_GetAttr(act, s_shape);
-    PyObject* dt = shp ? PyObject_GetAttr(act, s_dtype) : NULL;
-    Py_DECREF(act);
-    if (!dt) {
-      Py_XDECREF(shp);
-      goto fail_idx;
-    }
     int r;
     int64_t el;
     double fel;
-    rc = read_shape(shp, ashape + i * MAX_RANK, &r, &el, &fel);
-    Py_DECREF(shp);
-    if (rc == 0) rc = cache_get_any(&wc, dt, width_fn, &v);
-    Py_DECREF(dt);
-    if (rc < 0) goto fail_idx;
+    if (read_shape(O(i, K_ASH), ashape + i * MAX_RANK, &r, &el, &fel) < 0) goto done;
+    if (cache_get_any(&wc, O(i, K_ADT), width_fn, &v) < 0) goto done;
     if (r > max_ar) max_ar = r;
     arank[i] = (uint8_t)(r > 255 ? 255 : r);
     abytes[i] = el * (int64_t)v;
     if (fel * 8.0 >= 9223372036854775808.0 && !overflow) overflow = "activation";
-    /* weight */
-    PyObject* w = PyObject_GetAttr(node, s_weight);
-    if (!w) goto fail_idx;
-    if (w == Py_None) {
+    if (O(i, K_W) == Py_None) {
       wrank[i] = 0;
       memset(wshape + i * MAX_RANK, 0, MAX_RANK * 8);
       wbytes[i] = 0;
       wtrain[i] = 0;
-    } else {
-      PyObject* ws = PyObject_GetAttr(w, s_shape);
-      PyObject* wd = ws ? PyObject_GetAttr(w, s_dtype) : NULL;
-      PyObject* wt = wd ? PyObject_GetAttr(w, s_trainable) : NULL;
-      if (!wt) {
-        Py_XDECREF(ws);
-        Py_XDECREF(wd);
-        Py_DECREF(w);
-        goto fail_idx;
-      }
-      rc = read_shape(ws, wshape + i * MAX_RANK, &r, &el, &fel);
-      if (rc == 0) rc = cache_get_any(&wc, wd, width_fn, &v);
-      int tr = rc == 0 ? PyObject_IsTrue(wt) : 0;
-      Py_DECREF(ws);
-      Py_DECREF(wd);
-      Py_DECREF(wt);
-      if (rc < 0 || tr < 0) {
-        Py_DECREF(w);
-        goto fail_idx;
-      }
-      if (r > max_wr) max_wr = r;
-      wrank[i] = (uint8_t)(r > 255 ? 255 : r);
-      wbytes[i] = el * (int64_t)v;
-      wtrain[i] = (uint8_t)tr;
-      if (fel * 8.0 >= 9223372036854775808.0 && !overflow) overflow = "weight";
+      continue;
     }
-    Py_DECREF(w);
-    /* producers, GraphNode.inputs order */
-    PyObject* ins = PyObject_GetAttr(node, s_inputs);
-    if (!ins) goto fail_idx;
-    PyObject* seq = PySequence_Fast(ins, "inputs must be a sequence");
-    Py_DECREF(ins);
-    if (!seq) goto fail_idx;
+    if (read_shape(O(i, K_WSH), wshape + i * MAX_RANK, &r, &el, &fel) < 0) goto done;
+    if (cache_get_any(&wc, O(i, K_WDT), width_fn, &v) < 0) goto done;
+    const int tr = PyObject_IsTrue(O(i, K_WTR));
+    if (tr < 0) goto done;
+    if (r > max_wr) max_wr = r;
+    wrank[i] = (uint8_t)(r > 255 ? 255 : r);
+    wbytes[i] = el * (int64_t)v;
+    wtrain[i] = (uint8_t)tr;
+    if (fel * 8.0 >= 9223372036854775808.0 && !overflow) overflow = "weight";
+  }
+  tm[5] = now_ms();
+  /* pass 5: producers, GraphNode.inputs order */
+  Py_ssize_t cap = n * 2 + 16;
+  inidx = (int32_t*)PyMem_Malloc((size_t)cap * sizeof(int32_t));
+  if (!inidx) {
+    PyErr_NoMemory();
+    goto done;
+  }
+  inoff[0] = 0;
+  for (Py_ssize_t i = 0; i < n; i++) {
+    PyObject* seq = PySequence_Fast(O(i, K_IN), "inputs must be a sequence");
+    if (!seq) goto done;
     const Py_ssize_t k = PySequence_Fast_GET_SIZE(seq);
     PyObject** it = PySequence_Fast_ITEMS(seq);
     if (E + k > cap) {
@@ -318,7 +405,7 @@ static PyObject* lower_arrays(PyObject* self, PyObject* args) {
       if (!grown) {
         Py_DECREF(seq);
         PyErr_NoMemory();
-        goto fail_idx;
+        goto done;
       }
       inidx = grown;
     }
@@ -327,23 +414,28 @@ static PyObject* lower_arrays(PyObject* self, PyObject* args) {
       if (pi < 0) {
         if (!PyErr_Occurred()) PyErr_SetObject(PyExc_KeyError, it[j]);
         Py_DECREF(seq);
-        goto fail_idx;
+        goto done;
       }
       inidx[E++] = pi;
     }
     Py_DECREF(seq);
     inoff[i + 1] = E;
   }
+  tm[6] = now_ms();
+  if (trace)
+    fprintf(stderr, "[lower] names %.2f lookup %.2f fields %.2f specs %.2f values %.2f inputs %.2f ms\n", tm[1] - tm[0],
+            tm[2] - tm[1], tm[3] - tm[2], tm[4] - tm[3], tm[5] - tm[4], tm[6] - tm[5]);
   b_inidx = PyByteArray_FromStringAndSize((const char*)inidx, E * 4);
-  PyMem_Free(inidx);
-  inidx = NULL;
   if (!b_inidx) goto done;
-  result = Py_BuildValue("(OiiizOOOOOOOOOOOO)", names, ascii, max_ar, max_wr, overflow, b_names, b_noff,
-                         b_op, b_arank, b_ashape, b_abytes, b_wrank, b_wshape, b_wbytes, b_wtrain, b_inoff, b_inidx);
-  goto done;
-fail_idx:
-  PyMem_Free(inidx);
+  result = Py_BuildValue("(OiiizOOOOOOOOOOOO)", names, ascii, max_ar, max_wr, overflow, b_names, b_noff, b_op,
+                         b_arank, b_ashape, b_abytes, b_wrank, b_wshape, b_wbytes, b_wtrain, b_inoff, b_inidx);
 done:
+  if (obj) {
+    for (size_t q = 0; q < (size_t)(n ? n : 1) * K_N; q++) Py_XDECREF(obj[q]);
+    PyMem_Free(obj);
+  }
+#undef O
+  PyMem_Free(inidx);
   cache_clear(&opc);
   cache_clear(&wc);
   Py_XDECREF(names);

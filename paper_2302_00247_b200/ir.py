@@ -41,7 +41,7 @@ OP_CODE = {k.value: i for i, k in enumerate(OpKind)}
 DTYPE_WIDTH = {"f32": 4, "f64": 8}
 
 
-@dataclass(frozen=True)
+@dataclass(frozen=True, slots=True)
 class TensorSpec:
     shape: tuple
     dtype: str = "f32"
@@ -60,7 +60,7 @@ class TensorSpec:
         return self.num_elements * DTYPE_WIDTH[self.dtype]
 
 
-@dataclass(frozen=True)
+@dataclass(frozen=True, slots=True)
 class GraphNode:
     scope: str
     op: OpKind

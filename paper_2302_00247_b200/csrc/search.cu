@@ -390,7 +390,8 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         f.out_r = L.out_pool >= 0 ? L.out_pool * THREADS * 8 : -1;
         f.out_s = L.out_pool >= 0 ? L.out_pool * THREADS : -1;
         f.sh = nd.slot >= 0 ? 2 * (H.V - 1 - nd.slot) : 0;
-        f.kf = L.k | ((!has_cons[n] || ext_cons[n]) ? 0x100 : 0);
+        // kf = k << 8 | boundary << 2 | min(k, 3): the walk dispatches on the low byte
+        f.kf = (L.k << 8) | ((!has_cons[n] || ext_cons[n]) ? 4 : 0) | (L.k < 3 ? L.k : 3);
         ((FastNode*)(blob + H.fast_off))[i] = f;
       }
       ((NodeSkip*)(blob + H.skip_off))[i] = NodeSkip{L.skip_R, L.skip_m, 0};
@@ -726,17 +727,17 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
     const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
     const int4 B = lds_v4(rec + 16);
     const uint32_t b = (uint32_t)(w >> X.z) & 3u;
-    const int k = X.w & 0xff;
+    const int kc = X.w & 3;  // fan-in, 3 = general
     uint32_t e;
     double r;
-    if (k == 1) {
+    if (kc == 1) {
       const uint32_t s0 = lds_u8(sb + B.z);
       const double r0 = lds_f64(rb + B.x);
       e = lds_u8(A.x + b * 3 + s0);
       SP_FAIL_CHECK(i)
       const uint32_t pe = e & 0x18u;
       r = dadd(dadd(r0, lds_f64(A.z + pe * 3 + s0 * 8)), lds_f64(A.y + pe));
-    } else if (k == 2) {
+    } else if (kc == 2) {
       const uint32_t s0 = lds_u8(sb + B.z), s1 = lds_u8(sb + B.w);
       const double r0 = lds_f64(rb + B.x), r1 = lds_f64(rb + B.y);
       e = lds_u8(A.x + b * 9 + s0 * 3 + s1);
@@ -744,11 +745,12 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
       const uint32_t pe = e & 0x18u;
       r = dadd(dmax_nn(dadd(r0, lds_f64(A.z + pe * 3 + s0 * 8)), dadd(r1, lds_f64(A.w + pe * 3 + s1 * 8))),
                lds_f64(A.y + pe));
-    } else if (k == 0) {
+    } else if (kc == 0) {
       e = lds_u8(A.x + b);
       SP_FAIL_CHECK(i)
       r = lds_f64(A.y + (e & 0x18u));
     } else {
+      const int k = X.w >> 8;
       const uint32_t pp = (uint32_t)B.x;  // absolute address of the (reach, state) offset pairs
       uint32_t key = b;
       for (int j = 0; j < k; j++) key = key * 3 + lds_u8(sb + lds_s32(pp + 8 * j + 4));
@@ -763,7 +765,7 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
       r = dadd(bse, lds_f64(A.y + pe));
     }
     const uint32_t s = e & 3u;
-    if (X.w & 0x100) {
+    if (X.w & 4) {
       const long long x = __double_as_longlong(dadd(r, lds_f64(A.y + 32 + s * 8)));
       f = x > f ? x : f;
     }
@@ -791,7 +793,7 @@ __device__ __forceinline__ void patch_fast(uint8_t* smem, bool pair = false) {
     f.dbl += (int32_t)base;
     f.cb0 += (int32_t)base;
     f.cb1 += (int32_t)base;
-    const int k = f.kf & 0xff;
+    const int k = f.kf >> 8;
     if (k >= 3) {
       int32_t* pp = (int32_t*)(smem + H.fprod_off) + 2 * f.r0;
       for (int j = 0; j < k; j++) {
@@ -838,88 +840,121 @@ __device__ __forceinline__ void sts_u8o(uint32_t a, uint32_t v) {
 // Candidate b's pool entries sit THREADS entries after candidate a's.  The
 // warp leaves when all 64 candidates have failed.  Returns valid bits
 // (bit 0 = a, bit 1 = b).
+// One node of the paired walk: K = fan-in (3 = general), BND = the node may
+// set the forward max.  Returns false when every candidate of the warp failed.
+template <int K, bool BND>
+__device__ __forceinline__ bool pair_node(const int4& A, const int4& B, const int4& X, uint32_t ba, uint32_t bb,
+                                          bool& oka, bool& okb, long long& fa, long long& fb, uint32_t rb,
+                                          uint32_t sb) {
+  constexpr int RB = THREADS * 8, SB = THREADS;
+  uint32_t ea, eb;
+  double ra, rx;
+  if (K == 1) {
+    const uint32_t ps = sb + B.z, pr = rb + B.x;
+    const uint32_t s0a = lds_u8o<0>(ps), s0b = lds_u8o<SB>(ps);
+    const double r0a = lds_f64o<0>(pr), r0b = lds_f64o<RB>(pr);
+    ea = lds_u8(A.x + ba * 3 + s0a);
+    eb = lds_u8(A.x + bb * 3 + s0b);
+    oka = oka && ea != 0xFFu;
+    okb = okb && eb != 0xFFu;
+    if (!__any_sync(0xffffffffu, oka || okb)) return false;
+    const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
+    ra = dadd(dadd(r0a, lds_f64(A.z + pa * 3 + s0a * 8)), lds_f64(A.y + pa));
+    rx = dadd(dadd(r0b, lds_f64(A.z + pb * 3 + s0b * 8)), lds_f64(A.y + pb));
+  } else if (K == 2) {
+    const uint32_t ps0 = sb + B.z, ps1 = sb + B.w, pr0 = rb + B.x, pr1 = rb + B.y;
+    const uint32_t s0a = lds_u8o<0>(ps0), s1a = lds_u8o<0>(ps1);
+    const uint32_t s0b = lds_u8o<SB>(ps0), s1b = lds_u8o<SB>(ps1);
+    const double r0a = lds_f64o<0>(pr0), r1a = lds_f64o<0>(pr1);
+    const double r0b = lds_f64o<RB>(pr0), r1b = lds_f64o<RB>(pr1);
+    ea = lds_u8(A.x + ba * 9 + s0a * 3 + s1a);
+    eb = lds_u8(A.x + bb * 9 + s0b * 3 + s1b);
+    oka = oka && ea != 0xFFu;
+    okb = okb && eb != 0xFFu;
+    if (!__any_sync(0xffffffffu, oka || okb)) return false;
+    const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
+    ra = dadd(dmax_nn(dadd(r0a, lds_f64(A.z + pa * 3 + s0a * 8)), dadd(r1a, lds_f64(A.w + pa * 3 + s1a * 8))),
+              lds_f64(A.y + pa));
+    rx = dadd(dmax_nn(dadd(r0b, lds_f64(A.z + pb * 3 + s0b * 8)), dadd(r1b, lds_f64(A.w + pb * 3 + s1b * 8))),
+              lds_f64(A.y + pb));
+  } else if (K == 0) {
+    ea = lds_u8(A.x + ba);
+    eb = lds_u8(A.x + bb);
+    oka = oka && ea != 0xFFu;
+    okb = okb && eb != 0xFFu;
+    if (!__any_sync(0xffffffffu, oka || okb)) return false;
+    ra = lds_f64(A.y + (ea & 0x18u));
+    rx = lds_f64(A.y + (eb & 0x18u));
+  } else {
+    const int k = X.w >> 8;
+    const uint32_t pp = (uint32_t)B.x;
+    uint32_t ka = ba, kb = bb;
+    for (int j = 0; j < k; j++) {
+      const uint32_t ps = sb + lds_s32(pp + 8 * j + 4);
+      ka = ka * 3 + lds_u8o<0>(ps);
+      kb = kb * 3 + lds_u8o<SB>(ps);
+    }
+    ea = lds_u8(A.x + ka);
+    eb = lds_u8(A.x + kb);
+    oka = oka && ea != 0xFFu;
+    okb = okb && eb != 0xFFu;
+    if (!__any_sync(0xffffffffu, oka || okb)) return false;
+    const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
+    double xa = 0.0, xb = 0.0;
+    for (int j = 0; j < k; j++) {
+      const uint32_t ps = sb + lds_s32(pp + 8 * j + 4), pr = rb + lds_s32(pp + 8 * j);
+      const uint32_t sja = lds_u8o<0>(ps), sjb = lds_u8o<SB>(ps);
+      xa = dmax_nn(xa, dadd(lds_f64o<0>(pr), lds_f64(A.z + j * 96 + pa * 3 + sja * 8)));
+      xb = dmax_nn(xb, dadd(lds_f64o<RB>(pr), lds_f64(A.z + j * 96 + pb * 3 + sjb * 8)));
+    }
+    ra = dadd(xa, lds_f64(A.y + pa));
+    rx = dadd(xb, lds_f64(A.y + pb));
+  }
+  const uint32_t sa = ea & 3u, sx = eb & 3u;
+  if (BND) {
+    const long long xa = __double_as_longlong(dadd(ra, lds_f64(A.y + 32 + sa * 8)));
+    const long long xb = __double_as_longlong(dadd(rx, lds_f64(A.y + 32 + sx * 8)));
+    fa = xa > fa ? xa : fa;
+    fb = xb > fb ? xb : fb;
+  }
+  if (X.x >= 0) {
+    const uint32_t qr = rb + X.x, qs = sb + X.y;
+    sts_f64o<0>(qr, ra);
+    sts_f64o<RB>(qr, rx);
+    sts_u8o<0>(qs, sa);
+    sts_u8o<SB>(qs, sx);
+  }
+  return true;
+}
+
+// walk_fast for two candidates per lane (brute force): one record load and
+// one dispatch per node serve both, and the two dependency chains interleave.
+// Candidate b's pool entries sit THREADS entries after candidate a's.  The
+// warp leaves when all 64 candidates have failed.  Returns valid bits
+// (bit 0 = a, bit 1 = b).
 __device__ __forceinline__ int walk_pair(uint32_t rec, int T, uint64_t wa, uint64_t wb, bool act_a, bool act_b,
                                          double& fwd_a, double& fwd_b, uint32_t rb, uint32_t sb) {
-  constexpr int RB = THREADS * 8, SB = THREADS;
   bool oka = act_a, okb = act_b;
   long long fa = 0, fb = 0;
   const uint32_t end = rec + (uint32_t)T * (uint32_t)sizeof(FastNode);
-#define SP_FAIL_CHECK2                                    {                                                         oka = oka && ea != 0xFFu;                               okb = okb && eb != 0xFFu;                               if (!__any_sync(0xffffffffu, oka || okb)) break;      }
   for (; rec != end; rec += (uint32_t)sizeof(FastNode)) {
+    // A = (tab, dbl, cb0, cb1) absolute, B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf)
     const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
     const int4 B = lds_v4(rec + 16);
     const uint32_t ba = (uint32_t)(wa >> X.z) & 3u, bb = (uint32_t)(wb >> X.z) & 3u;
-    const int k = X.w & 0xff;
-    uint32_t ea, eb;
-    double ra, rx;
-    if (k == 1) {
-      const uint32_t ps = sb + B.z, pr = rb + B.x;
-      const uint32_t s0a = lds_u8o<0>(ps), s0b = lds_u8o<SB>(ps);
-      const double r0a = lds_f64o<0>(pr), r0b = lds_f64o<RB>(pr);
-      ea = lds_u8(A.x + ba * 3 + s0a);
-      eb = lds_u8(A.x + bb * 3 + s0b);
-      SP_FAIL_CHECK2
-      const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
-      ra = dadd(dadd(r0a, lds_f64(A.z + pa * 3 + s0a * 8)), lds_f64(A.y + pa));
-      rx = dadd(dadd(r0b, lds_f64(A.z + pb * 3 + s0b * 8)), lds_f64(A.y + pb));
-    } else if (k == 2) {
-      const uint32_t ps0 = sb + B.z, ps1 = sb + B.w, pr0 = rb + B.x, pr1 = rb + B.y;
-      const uint32_t s0a = lds_u8o<0>(ps0), s1a = lds_u8o<0>(ps1);
-      const uint32_t s0b = lds_u8o<SB>(ps0), s1b = lds_u8o<SB>(ps1);
-      const double r0a = lds_f64o<0>(pr0), r1a = lds_f64o<0>(pr1);
-      const double r0b = lds_f64o<RB>(pr0), r1b = lds_f64o<RB>(pr1);
-      ea = lds_u8(A.x + ba * 9 + s0a * 3 + s1a);
-      eb = lds_u8(A.x + bb * 9 + s0b * 3 + s1b);
-      SP_FAIL_CHECK2
-      const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
-      ra = dadd(dmax_nn(dadd(r0a, lds_f64(A.z + pa * 3 + s0a * 8)), dadd(r1a, lds_f64(A.w + pa * 3 + s1a * 8))),
-                lds_f64(A.y + pa));
-      rx = dadd(dmax_nn(dadd(r0b, lds_f64(A.z + pb * 3 + s0b * 8)), dadd(r1b, lds_f64(A.w + pb * 3 + s1b * 8))),
-                lds_f64(A.y + pb));
-    } else if (k == 0) {
-      ea = lds_u8(A.x + ba);
-      eb = lds_u8(A.x + bb);
-      SP_FAIL_CHECK2
-      ra = lds_f64(A.y + (ea & 0x18u));
-      rx = lds_f64(A.y + (eb & 0x18u));
-    } else {
-      const uint32_t pp = (uint32_t)B.x;
-      uint32_t ka = ba, kb = bb;
-      for (int j = 0; j < k; j++) {
-        const uint32_t ps = sb + lds_s32(pp + 8 * j + 4);
-        ka = ka * 3 + lds_u8o<0>(ps);
-        kb = kb * 3 + lds_u8o<SB>(ps);
-      }
-      ea = lds_u8(A.x + ka);
-      eb = lds_u8(A.x + kb);
-      SP_FAIL_CHECK2
-      const uint32_t pa = ea & 0x18u, pb = eb & 0x18u;
-      double xa = 0.0, xb = 0.0;
-      for (int j = 0; j < k; j++) {
-        const uint32_t ps = sb + lds_s32(pp + 8 * j + 4), pr = rb + lds_s32(pp + 8 * j);
-        const uint32_t sja = lds_u8o<0>(ps), sjb = lds_u8o<SB>(ps);
-        xa = dmax_nn(xa, dadd(lds_f64o<0>(pr), lds_f64(A.z + j * 96 + pa * 3 + sja * 8)));
-        xb = dmax_nn(xb, dadd(lds_f64o<RB>(pr), lds_f64(A.z + j * 96 + pb * 3 + sjb * 8)));
-      }
-      ra = dadd(xa, lds_f64(A.y + pa));
-      rx = dadd(xb, lds_f64(A.y + pb));
+    bool go;
+    switch (X.w & 7) {  // min(fan-in, 3) | boundary << 2
+      case 1: go = pair_node<1, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      case 2: go = pair_node<2, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      case 0: go = pair_node<0, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      case 3: go = pair_node<3, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      case 5: go = pair_node<1, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      case 6: go = pair_node<2, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      case 4: go = pair_node<0, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      default: go = pair_node<3, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
     }
-    const uint32_t sa = ea & 3u, sx = eb & 3u;
-    if (X.w & 0x100) {
-      const long long xa = __double_as_longlong(dadd(ra, lds_f64(A.y + 32 + sa * 8)));
-      const long long xb = __double_as_longlong(dadd(rx, lds_f64(A.y + 32 + sx * 8)));
-      fa = xa > fa ? xa : fa;
-      fb = xb > fb ? xb : fb;
-    }
-    if (X.x >= 0) {
-      const uint32_t qr = rb + X.x, qs = sb + X.y;
-      sts_f64o<0>(qr, ra);
-      sts_f64o<RB>(qr, rx);
-      sts_u8o<0>(qs, sa);
-      sts_u8o<SB>(qs, sx);
-    }
+    if (!go) break;
   }
-#undef SP_FAIL_CHECK2
   fwd_a = __longlong_as_double(fa);
   fwd_b = __longlong_as_double(fb);
   return (oka ? 1 : 0) | (okb ? 2 : 0);

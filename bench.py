@@ -44,15 +44,35 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 METRIC = "candidate sharding plans scored/sec"
 UNIT = "candidates/s"
 C2_GRAPH = os.path.join(ROOT, "tests", "golden", "graphs", "c2_t5.json.gz")
+_GOLDEN = os.path.join(ROOT, "tests", "golden", "graphs")
+#: name -> (description, data, graph file or None for c5, mesh)
 WORKLOADS = {
     "c5": ("c5: 10^5-op motif DAG (99,658 GraphNodes, 16 motif types, 1018 blocks), 1x8 mesh, "
            "every candidate of every block (3.92e9)",
            "synthetic: workloads.motif_dag(seed=0, tier='throughput'), deterministic; pinned to the "
-           "reference via tests/golden/c5.json"),
+           "reference via tests/golden/c5.json", None, "1x8"),
     "c2": ("c2: T5-base ONNX graph (450 GraphNodes, 8 unique blocks), 1x8 mesh, exhaustive "
            "per-block candidates (475,320)",
            "synthetic: T5-base-structured ONNX graph built with the reference's wire codec "
-           "(tests/golden/graphs/c2_t5.json.gz)"),
+           "(tests/golden/graphs/c2_t5.json.gz)", C2_GRAPH, "1x8"),
+    "c1": ("c1: 12-layer transformer encoder, hidden 768 (172 GraphNodes, 5 blocks, 737 candidates), "
+           "1x8 mesh", "synthetic: reference gen_transformer_stack(12, d_model=768, heads=12) "
+           "(tests/golden/graphs/c1.json.gz)", os.path.join(_GOLDEN, "c1.json.gz"), "1x8"),
+    "c3": ("c3: wide classifier with a 100k-class head (blocks=16, batch 32), 2x4 mesh",
+           "synthetic: reference gen_wide_classifier(100000, 2048, blocks=16, batch=32) "
+           "(tests/golden/graphs/c3.json.gz)", os.path.join(_GOLDEN, "c3.json.gz"), "2x4"),
+    "c3_slow": ("c3: wide classifier, 2x4 mesh with inter_bw = 2e11/32",
+                "synthetic: reference gen_wide_classifier(100000, 2048, blocks=16, batch=32)",
+                os.path.join(_GOLDEN, "c3.json.gz"), "2x4:slow"),
+    "c4": ("c4: GPT-3 style 48 layers, hidden 6144 (676 GraphNodes, 5 blocks), 1x8 mesh",
+           "synthetic: reference gen_transformer_stack(48, d_model=6144, heads=48) "
+           "(tests/golden/graphs/c4.json.gz)", os.path.join(_GOLDEN, "c4.json.gz"), "1x8"),
+    "c4_2x4": ("c4: GPT-3 style 48 layers, hidden 6144, 2x4 mesh",
+               "synthetic: reference gen_transformer_stack(48, d_model=6144, heads=48)",
+               os.path.join(_GOLDEN, "c4.json.gz"), "2x4"),
+    "c4_2x4_slow": ("c4: GPT-3 style 48 layers, hidden 6144, 2x4 mesh with inter_bw = 2e11/32",
+                    "synthetic: reference gen_transformer_stack(48, d_model=6144, heads=48)",
+                    os.path.join(_GOLDEN, "c4.json.gz"), "2x4:slow"),
 }
 
 
@@ -66,8 +86,11 @@ def load_workload(name: str):
     from paper_2302_00247_b200.ir import load_grouped
     from paper_2302_00247_b200.workloads import motif_dag
 
-    g = motif_dag(0, "throughput") if name == "c5" else load_grouped(C2_GRAPH)
-    return g, ClusterSpec.from_mesh("1x8")
+    _, _, path, mesh = WORKLOADS[name]
+    g = motif_dag(0, "throughput") if path is None else load_grouped(path)
+    if mesh.endswith(":slow"):
+        return g, ClusterSpec(m=2, n=4, inter_bw=2e11 / 32)
+    return g, ClusterSpec.from_mesh(mesh)
 
 
 class ClockSampler:
@@ -178,7 +201,7 @@ def cpu_measure(workload: str, min_seconds: float, max_steps: int = 50) -> dict:
     dt = time.perf_counter() - t0
     sample = (f"{steps} steps of: prune + all blocks <= 2e6 candidates in full + 8 slices of "
               f"{width:,} candidates of each larger block; {walked // steps:,} candidates walked "
-              f"per step" if workload == "c5" else f"{steps} full c2 searches")
+              f"per step" if workload == "c5" else f"{steps} full {workload} searches")
     return {"value": walked / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{sample}, {dt:.1f}s, oracle/oracle.c with {threads} pthreads",
             "seconds": dt, "steps": steps}
@@ -206,7 +229,7 @@ def run_reference(args) -> None:
          "steps": args.steps,
          "sample": (f"{args.steps} steps x {walked // args.steps:,} candidates walked (prune + "
                     f"blocks <= 2e6 in full + 8 slices of {width:,} of each larger block)"
-                    if args.workload == "c5" else f"{args.steps} full c2 searches")
+                    if args.workload == "c5" else f"{args.steps} full {args.workload} searches")
                    + f", oracle/oracle.c with {threads} pthreads"}
     value = m["value"]
     line = {
@@ -214,7 +237,8 @@ def run_reference(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["seconds"] * 1000 / m["steps"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": WORKLOADS[args.workload][1],
-        "config": {"workload": WORKLOADS[args.workload][0], "mesh": "1x8", "min_dup": 2},
+        "config": {"workload": WORKLOADS[args.workload][0], "mesh": WORKLOADS[args.workload][3],
+                   "min_dup": 2},
         "cpu_baseline": {k: m[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -414,7 +438,7 @@ def run_ours(args) -> None:
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": WORKLOADS[args.workload][1],
         "config": {"workload": WORKLOADS[args.workload][0], "candidates_per_step": cands,
                    "valid_plans_per_step": walked_valid, "blocks": nb, "graph_nodes": len(g.nodes),
-                   "mesh": "1x8", "min_dup": 2, "scoring": "brute force (no prefix skipping)",
+                   "mesh": WORKLOADS[args.workload][3], "min_dup": 2, "scoring": "brute force (no prefix skipping)",
                    "parallelism": f"candidate-range shards x{world}",
                    "l2": "flushed between steps (256 MiB write)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": main["h2d"],

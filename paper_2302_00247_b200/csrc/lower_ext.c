@@ -213,7 +213,7 @@ static PyObject* field_get(FieldRef* f, PyObject* obj) {
  * the loads of a pass are independent across nodes, so the core overlaps the
  * cache misses of the scattered Python objects.
  */
-static PyObject* lower_arrays(PyObject* self, PyObject* args) {
+static PyObject* lower_serial(PyObject* self, PyObject* args) {
   PyObject *topo, *nodes, *op_fn, *width_fn;
   if (!PyArg_ParseTuple(args, "OO!OO", &topo, &PyDict_Type, &nodes, &op_fn, &width_fn)) return NULL;
   PyObject* names = PySequence_List(topo);
@@ -453,6 +453,490 @@ done:
   Py_XDECREF(b_inoff);
   Py_XDECREF(b_inidx);
   return result;
+}
+
+/* ------------------------------------------------------------------------
+ * Parallel walker.  The serial passes above are bound by cache misses on
+ * the scattered Python objects (one or two per field), so the same walk is
+ * spread over host threads.  The workers read the frozen object graph
+ * without touching the interpreter: borrowed pointers only (the caller's
+ * graph keeps every object alive and this thread keeps the GIL for the
+ * whole call, so no Python code can run, mutate or free anything), exact
+ * type checks, __slots__ offsets resolved up front, compact-ASCII str bytes
+ * read in place and hashed with a private hash, compact ints read in place.
+ * Anything outside that envelope (other node classes, non-ASCII names, big
+ * ints, non-tuple shapes or inputs, unknown or duplicate names, byte-size
+ * overflow) makes the call fall back to the serial walker, which produces
+ * the identical arrays and raises the errors.
+ * ---------------------------------------------------------------------- */
+#include <pthread.h>
+#include <sched.h>
+#include <unistd.h>
+
+#define PAR_MAX_THREADS 32
+#define PAR_MIN_NODES 4096
+
+static Py_ssize_t slot_offset(PyTypeObject* tp, PyObject* name) {
+  PyObject* d = PyObject_GetAttr((PyObject*)tp, name);
+  Py_ssize_t off = -1;
+  if (d) {
+    if (Py_IS_TYPE(d, &PyMemberDescr_Type)) {
+      PyMemberDef* m = ((PyMemberDescrObject*)d)->d_member;
+      if (m->type == Py_T_OBJECT_EX && !(m->flags & Py_RELATIVE_OFFSET)) off = m->offset;
+    }
+    Py_DECREF(d);
+  } else {
+    PyErr_Clear();
+  }
+  return off;
+}
+
+static inline PyObject* slot_read(PyObject* o, Py_ssize_t off) { return *(PyObject**)((char*)o + off); }
+
+static inline uint64_t name_hash(const char* p, Py_ssize_t n) {
+  uint64_t h = 0x243F6A8885A308D3ull ^ (uint64_t)n;
+  while (n >= 8) {
+    uint64_t w;
+    memcpy(&w, p, 8);
+    h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+    p += 8;
+    n -= 8;
+  }
+  if (n) {
+    uint64_t w = 0;
+    memcpy(&w, p, (size_t)n);
+    h = (h ^ w) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+  }
+  h *= 0xBF58476D1CE4E5B9ull;
+  return h ^ (h >> 31);
+}
+
+/* exact compact-ASCII str -> its bytes in place; 0 outside the envelope */
+static inline int ascii_view(PyObject* o, const char** p, Py_ssize_t* n) {
+  if (!PyUnicode_CheckExact(o) || !PyUnicode_IS_COMPACT_ASCII(o)) return 0;
+  *p = (const char*)(((PyASCIIObject*)o) + 1);
+  *n = PyUnicode_GET_LENGTH(o);
+  return 1;
+}
+
+/* exact tuple of compact ints -> read_shape's outputs; 0 outside the envelope */
+static inline int shape_view(PyObject* t, int64_t* dims, int* rank, int64_t* elems, double* felems) {
+  if (!PyTuple_CheckExact(t)) return 0;
+  const Py_ssize_t r = PyTuple_GET_SIZE(t);
+  int64_t p = 1;
+  double fp = 1.0;
+  for (Py_ssize_t j = 0; j < r; j++) {
+    PyObject* v = PyTuple_GET_ITEM(t, j);
+    if (!PyLong_CheckExact(v) || !PyUnstable_Long_IsCompact((PyLongObject*)v)) return 0;
+    const int64_t x = (int64_t)PyUnstable_Long_CompactValue((PyLongObject*)v);
+    if (j < MAX_RANK) dims[j] = x;
+    p *= x;
+    fp *= (double)x;
+  }
+  for (Py_ssize_t j = r; j < MAX_RANK; j++) dims[j] = 0;
+  *rank = (int)r;
+  *elems = p;
+  *felems = fp;
+  return 1;
+}
+
+typedef struct Par {
+  Py_ssize_t n, nd;
+  PyObject** names; /* topo names */
+  PyObject** dkey;  /* nodes dict entries */
+  PyObject** dval;
+  PyTypeObject *t_node, *t_spec;
+  Py_ssize_t o_op, o_in, o_act, o_w, o_shape, o_dtype, o_train;
+  const char** np; /* name bytes, length, hash per row */
+  Py_ssize_t* nl;
+  uint64_t* nh;
+  int32_t* tab; /* open-addressing row map: row + 1, 0 = empty */
+  size_t mask;
+  PyObject** node;
+  PyObject** inseq;
+  int64_t *ael, *wel; /* element counts (bytes = count x dtype width, mapped after the join) */
+  PyObject **opv, **adt, **wdt;
+  char* pn;
+  int64_t *noff, *ashape, *wshape, *inoff;
+  uint8_t *arank, *wrank, *wtrain;
+  int32_t* inidx;
+  int nthreads, go, fail;
+  Py_ssize_t bytes_part[PAR_MAX_THREADS], edges_part[PAR_MAX_THREADS];
+  int max_ar[PAR_MAX_THREADS], max_wr[PAR_MAX_THREADS];
+  pthread_barrier_t bar;
+} Par;
+
+typedef struct {
+  Par* P;
+  int t;
+} ParArg;
+
+static inline void par_fail(Par* P) { __atomic_store_n(&P->fail, 1, __ATOMIC_RELAXED); }
+static inline int par_failed(Par* P) { return __atomic_load_n(&P->fail, __ATOMIC_RELAXED); }
+
+static inline int32_t par_find(const Par* P, const char* p, Py_ssize_t n, uint64_t h) {
+  for (size_t s = h & P->mask;; s = (s + 1) & P->mask) {
+    const int32_t v = __atomic_load_n(&P->tab[s], __ATOMIC_ACQUIRE);
+    if (!v) return -1;
+    const int32_t j = v - 1;
+    if (P->nh[j] == h && P->nl[j] == n && memcmp(P->np[j], p, (size_t)n) == 0) return j;
+  }
+}
+
+static void par_phases(Par* P, int t) {
+  const int T = P->nthreads;
+  const Py_ssize_t n = P->n, lo = n * t / T, hi = n * (t + 1) / T;
+  const Py_ssize_t dlo = P->nd * t / T, dhi = P->nd * (t + 1) / T;
+  /* phase 1: name bytes and hash, lock-free insert into the row map */
+  Py_ssize_t bytes = 0;
+  for (Py_ssize_t i = lo; i < hi && !par_failed(P); i++) {
+    const char* p;
+    Py_ssize_t L;
+    if (!ascii_view(P->names[i], &p, &L)) {
+      par_fail(P);
+      break;
+    }
+    const uint64_t h = name_hash(p, L);
+    P->np[i] = p;
+    P->nl[i] = L;
+    P->nh[i] = h;
+    bytes += L;
+    for (size_t s = h & P->mask;; s = (s + 1) & P->mask) {
+      int32_t expect = 0;
+      if (__atomic_compare_exchange_n(&P->tab[s], &expect, (int32_t)(i + 1), 0, __ATOMIC_ACQ_REL,
+                                      __ATOMIC_ACQUIRE))
+        break;
+      const int32_t j = expect - 1;
+      if (P->nh[j] == h && P->nl[j] == L && memcmp(P->np[j], p, (size_t)L) == 0) {
+        par_fail(P); /* duplicate name */
+        break;
+      }
+    }
+  }
+  P->bytes_part[t] = bytes;
+  pthread_barrier_wait(&P->bar);
+  /* phase 2: dict entries -> rows */
+  for (Py_ssize_t j = dlo; j < dhi && !par_failed(P); j++) {
+    const char* p;
+    Py_ssize_t L;
+    if (!ascii_view(P->dkey[j], &p, &L)) {
+      par_fail(P);
+      break;
+    }
+    const int32_t r = par_find(P, p, L, name_hash(p, L));
+    if (r >= 0) P->node[r] = P->dval[j];
+  }
+  Py_ssize_t base = 0;
+  for (int u = 0; u < t; u++) base += P->bytes_part[u];
+  pthread_barrier_wait(&P->bar);
+  /* phase 3: node fields, tensor specs, shapes, name bytes, input counts */
+  Py_ssize_t edges = 0;
+  int mar = 0, mwr = 0;
+  for (Py_ssize_t i = lo; i < hi && !par_failed(P); i++) {
+    PyObject* nd = P->node[i];
+    if (!nd || Py_TYPE(nd) != P->t_node) goto bad;
+    PyObject *op = slot_read(nd, P->o_op), *in = slot_read(nd, P->o_in), *a = slot_read(nd, P->o_act),
+             *w = slot_read(nd, P->o_w);
+    if (!op || !in || !a || !w || Py_TYPE(a) != P->t_spec || !PyTuple_CheckExact(in)) goto bad;
+    memcpy(P->pn + base, P->np[i], (size_t)P->nl[i]);
+    base += P->nl[i];
+    P->noff[i + 1] = base;
+    P->opv[i] = op;
+    PyObject *sh = slot_read(a, P->o_shape), *dt = slot_read(a, P->o_dtype);
+    int r;
+    int64_t el;
+    double fel;
+    if (!sh || !dt || !shape_view(sh, P->ashape + i * MAX_RANK, &r, &el, &fel)) goto bad;
+    if (fel * 8.0 >= 9223372036854775808.0) goto bad;
+    if (r > mar) mar = r;
+    P->arank[i] = (uint8_t)(r > 255 ? 255 : r);
+    P->ael[i] = el;
+    P->adt[i] = dt;
+    if (w == Py_None) {
+      P->wrank[i] = 0;
+      memset(P->wshape + i * MAX_RANK, 0, MAX_RANK * 8);
+      P->wel[i] = 0;
+      P->wtrain[i] = 0;
+      P->wdt[i] = NULL;
+    } else {
+      if (Py_TYPE(w) != P->t_spec) goto bad;
+      PyObject *wsh = slot_read(w, P->o_shape), *wdt = slot_read(w, P->o_dtype), *tr = slot_read(w, P->o_train);
+      if (!wsh || !wdt || (tr != Py_True && tr != Py_False)) goto bad;
+      if (!shape_view(wsh, P->wshape + i * MAX_RANK, &r, &el, &fel)) goto bad;
+      if (fel * 8.0 >= 9223372036854775808.0) goto bad;
+      if (r > mwr) mwr = r;
+      P->wrank[i] = (uint8_t)(r > 255 ? 255 : r);
+      P->wel[i] = el;
+      P->wdt[i] = wdt;
+      P->wtrain[i] = tr == Py_True;
+    }
+    P->inseq[i] = in;
+    edges += PyTuple_GET_SIZE(in);
+    continue;
+  bad:
+    par_fail(P);
+    break;
+  }
+  P->edges_part[t] = edges;
+  P->max_ar[t] = mar;
+  P->max_wr[t] = mwr;
+  pthread_barrier_wait(&P->bar);
+  if (t == 0 && !par_failed(P)) {
+    Py_ssize_t E = 0;
+    for (int u = 0; u < T; u++) E += P->edges_part[u];
+    P->inidx = (int32_t*)malloc((size_t)(E ? E : 1) * sizeof(int32_t));
+    if (!P->inidx) par_fail(P);
+  }
+  pthread_barrier_wait(&P->bar);
+  if (par_failed(P)) return;
+  /* phase 4: producer rows in GraphNode.inputs order */
+  Py_ssize_t e = 0;
+  for (int u = 0; u < t; u++) e += P->edges_part[u];
+  for (Py_ssize_t i = lo; i < hi; i++) {
+    PyObject* in = P->inseq[i];
+    const Py_ssize_t k = PyTuple_GET_SIZE(in);
+    for (Py_ssize_t j = 0; j < k; j++) {
+      const char* p;
+      Py_ssize_t L;
+      int32_t r = -1;
+      if (ascii_view(PyTuple_GET_ITEM(in, j), &p, &L)) r = par_find(P, p, L, name_hash(p, L));
+      if (r < 0) {
+        par_fail(P);
+        return;
+      }
+      P->inidx[e++] = r;
+    }
+    P->inoff[i + 1] = e;
+  }
+}
+
+static void* par_worker(void* arg) {
+  Par* P = ((ParArg*)arg)->P;
+  int go;
+  while (!(go = __atomic_load_n(&P->go, __ATOMIC_ACQUIRE))) sched_yield();
+  if (go > 0 && ((ParArg*)arg)->t < P->nthreads) par_phases(P, ((ParArg*)arg)->t);
+  return NULL;
+}
+
+/* NULL with no exception set: outside the envelope (use the serial walker) */
+static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn, PyObject* width_fn) {
+  if (!PyList_CheckExact(topo) && !PyTuple_CheckExact(topo)) return NULL;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(topo);
+  long ncpu = sysconf(_SC_NPROCESSORS_ONLN);
+  const char* env = getenv("SP_LOWER_THREADS");
+  if (env) ncpu = atol(env);
+  int T = (int)(ncpu < PAR_MAX_THREADS ? ncpu : PAR_MAX_THREADS);
+  if (T > n / 2048) T = (int)(n / 2048);
+  if (n < PAR_MIN_NODES || T < 2 || n >= INT32_MAX / 4 || PyDict_GET_SIZE(nodes) == 0) return NULL;
+  PyObject* n0 = PyDict_GetItemWithError(nodes, PySequence_Fast_ITEMS(topo)[0]);
+  if (!n0) {
+    PyErr_Clear();
+    return NULL;
+  }
+  static PyObject *s_op, *s_inputs, *s_activation, *s_weight, *s_shape, *s_dtype, *s_trainable;
+  if (!s_op) {
+    s_op = PyUnicode_InternFromString("op");
+    s_inputs = PyUnicode_InternFromString("inputs");
+    s_activation = PyUnicode_InternFromString("activation");
+    s_weight = PyUnicode_InternFromString("weight");
+    s_shape = PyUnicode_InternFromString("shape");
+    s_dtype = PyUnicode_InternFromString("dtype");
+    s_trainable = PyUnicode_InternFromString("trainable");
+  }
+  Par* P = (Par*)calloc(1, sizeof(Par));
+  if (!P) return NULL;
+  PyObject *result = NULL, *names = NULL;
+  PyObject *b_names = NULL, *b_noff = NULL, *b_op = NULL, *b_arank = NULL, *b_ashape = NULL, *b_abytes = NULL,
+           *b_wrank = NULL, *b_wshape = NULL, *b_wbytes = NULL, *b_wtrain = NULL, *b_inoff = NULL, *b_inidx = NULL;
+  PtrCache opc = {{0}, {0}, 0}, wc = {{0}, {0}, 0};
+  pthread_t th[PAR_MAX_THREADS];
+  ParArg pa[PAR_MAX_THREADS];
+  int created = 1;
+  P->n = n;
+  P->t_node = Py_TYPE(n0);
+  P->o_op = slot_offset(P->t_node, s_op);
+  P->o_in = slot_offset(P->t_node, s_inputs);
+  P->o_act = slot_offset(P->t_node, s_activation);
+  P->o_w = slot_offset(P->t_node, s_weight);
+  PyObject* a0 = P->o_act >= 0 ? slot_read(n0, P->o_act) : NULL;
+  if (!a0 || P->o_op < 0 || P->o_in < 0 || P->o_w < 0) goto out;
+  P->t_spec = Py_TYPE(a0);
+  P->o_shape = slot_offset(P->t_spec, s_shape);
+  P->o_dtype = slot_offset(P->t_spec, s_dtype);
+  P->o_train = slot_offset(P->t_spec, s_trainable);
+  if (P->o_shape < 0 || P->o_dtype < 0 || P->o_train < 0) goto out;
+  names = PySequence_List(topo);
+  if (!names) {
+    PyErr_Clear();
+    goto out;
+  }
+  P->names = &PyList_GET_ITEM(names, 0);
+  Py_ssize_t nbytes = 0;
+  for (Py_ssize_t i = 0; i < n; i++) {
+    PyObject* o = P->names[i];
+    if (!PyUnicode_CheckExact(o) || !PyUnicode_IS_COMPACT_ASCII(o)) goto out;
+    nbytes += PyUnicode_GET_LENGTH(o);
+  }
+  P->nd = PyDict_GET_SIZE(nodes);
+  P->dkey = (PyObject**)malloc((size_t)P->nd * sizeof(PyObject*));
+  P->dval = (PyObject**)malloc((size_t)P->nd * sizeof(PyObject*));
+  if (!P->dkey || !P->dval) goto out;
+  {
+    Py_ssize_t pos = 0, j = 0;
+    PyObject *k, *v;
+    while (j < P->nd && PyDict_Next(nodes, &pos, &k, &v)) {
+      P->dkey[j] = k;
+      P->dval[j] = v;
+      j++;
+    }
+    P->nd = j;
+  }
+  size_t cap = 16;
+  while (cap < (size_t)n * 2) cap <<= 1;
+  P->mask = cap - 1;
+  P->tab = (int32_t*)calloc(cap, sizeof(int32_t));
+  P->np = (const char**)malloc((size_t)n * sizeof(char*));
+  P->nl = (Py_ssize_t*)malloc((size_t)n * sizeof(Py_ssize_t));
+  P->nh = (uint64_t*)malloc((size_t)n * 8);
+  P->node = (PyObject**)calloc((size_t)n, sizeof(PyObject*));
+  P->inseq = (PyObject**)malloc((size_t)n * sizeof(PyObject*));
+  P->ael = (int64_t*)malloc((size_t)n * 8);
+  P->wel = (int64_t*)malloc((size_t)n * 8);
+  P->opv = (PyObject**)malloc((size_t)n * sizeof(PyObject*));
+  P->adt = (PyObject**)malloc((size_t)n * sizeof(PyObject*));
+  P->wdt = (PyObject**)malloc((size_t)n * sizeof(PyObject*));
+  if (!P->tab || !P->np || !P->nl || !P->nh || !P->node || !P->inseq || !P->ael || !P->wel || !P->opv || !P->adt ||
+      !P->wdt)
+    goto out;
+  b_names = new_bytearray(nbytes);
+  b_noff = new_bytearray((n + 1) * 8);
+  b_op = new_bytearray(n);
+  b_arank = new_bytearray(n);
+  b_ashape = new_bytearray(n * MAX_RANK * 8);
+  b_abytes = new_bytearray(n * 8);
+  b_wrank = new_bytearray(n);
+  b_wshape = new_bytearray(n * MAX_RANK * 8);
+  b_wbytes = new_bytearray(n * 8);
+  b_wtrain = new_bytearray(n);
+  b_inoff = new_bytearray((n + 1) * 8);
+  if (!b_names || !b_noff || !b_op || !b_arank || !b_ashape || !b_abytes || !b_wrank || !b_wshape || !b_wbytes ||
+      !b_wtrain || !b_inoff) {
+    PyErr_Clear();
+    goto out;
+  }
+  P->pn = PyByteArray_AS_STRING(b_names);
+  P->noff = (int64_t*)PyByteArray_AS_STRING(b_noff);
+  P->arank = (uint8_t*)PyByteArray_AS_STRING(b_arank);
+  P->ashape = (int64_t*)PyByteArray_AS_STRING(b_ashape);
+  P->wrank = (uint8_t*)PyByteArray_AS_STRING(b_wrank);
+  P->wshape = (int64_t*)PyByteArray_AS_STRING(b_wshape);
+  P->wtrain = (uint8_t*)PyByteArray_AS_STRING(b_wtrain);
+  P->inoff = (int64_t*)PyByteArray_AS_STRING(b_inoff);
+  P->noff[0] = 0;
+  P->inoff[0] = 0;
+  /* workers spin on `go` until the participant count is final; the GIL
+     stays with this thread throughout */
+  for (int t = 1; t < T; t++) {
+    pa[t].P = P;
+    pa[t].t = t;
+    if (pthread_create(&th[t], NULL, par_worker, &pa[t])) break;
+    created = t + 1;
+  }
+  P->nthreads = created;
+  if (created < 2 || pthread_barrier_init(&P->bar, NULL, (unsigned)created)) {
+    __atomic_store_n(&P->go, -1, __ATOMIC_RELEASE);
+    for (int t = 1; t < created; t++) pthread_join(th[t], NULL);
+    goto out;
+  }
+  __atomic_store_n(&P->go, 1, __ATOMIC_RELEASE);
+  par_phases(P, 0);
+  for (int t = 1; t < created; t++) pthread_join(th[t], NULL);
+  pthread_barrier_destroy(&P->bar);
+  if (par_failed(P)) goto out;
+  {
+    /* enum members -> codes / widths (pointer-keyed caches, a few Python calls) */
+    uint8_t* op = (uint8_t*)PyByteArray_AS_STRING(b_op);
+    int64_t* abytes = (int64_t*)PyByteArray_AS_STRING(b_abytes);
+    int64_t* wbytes = (int64_t*)PyByteArray_AS_STRING(b_wbytes);
+    int max_ar = 0, max_wr = 0;
+    for (int u = 0; u < created; u++) {
+      if (P->max_ar[u] > max_ar) max_ar = P->max_ar[u];
+      if (P->max_wr[u] > max_wr) max_wr = P->max_wr[u];
+    }
+    for (Py_ssize_t i = 0; i < n; i++) {
+      long v;
+      if (cache_get_any(&opc, P->opv[i], op_fn, &v) < 0) goto err;
+      op[i] = (uint8_t)v;
+      if (cache_get_any(&wc, P->adt[i], width_fn, &v) < 0) goto err;
+      abytes[i] = P->ael[i] * (int64_t)v;
+      if (P->wdt[i]) {
+        if (cache_get_any(&wc, P->wdt[i], width_fn, &v) < 0) goto err;
+        wbytes[i] = P->wel[i] * (int64_t)v;
+      } else {
+        wbytes[i] = 0;
+      }
+    }
+    const Py_ssize_t E = P->inoff[n];
+    b_inidx = PyByteArray_FromStringAndSize((const char*)P->inidx, E * 4);
+    if (!b_inidx) goto err;
+    result = Py_BuildValue("(OiiizOOOOOOOOOOOO)", names, 1, max_ar, max_wr, NULL, b_names, b_noff, b_op, b_arank,
+                           b_ashape, b_abytes, b_wrank, b_wshape, b_wbytes, b_wtrain, b_inoff, b_inidx);
+    if (!result) goto err;
+    goto out;
+  err:
+    /* a Python mapping call failed: let the serial walker raise it */
+    PyErr_Clear();
+  }
+out:
+  cache_clear(&opc);
+  cache_clear(&wc);
+  Py_XDECREF(names);
+  Py_XDECREF(b_names);
+  Py_XDECREF(b_noff);
+  Py_XDECREF(b_op);
+  Py_XDECREF(b_arank);
+  Py_XDECREF(b_ashape);
+  Py_XDECREF(b_abytes);
+  Py_XDECREF(b_wrank);
+  Py_XDECREF(b_wshape);
+  Py_XDECREF(b_wbytes);
+  Py_XDECREF(b_wtrain);
+  Py_XDECREF(b_inoff);
+  Py_XDECREF(b_inidx);
+  free(P->dkey);
+  free(P->dval);
+  free(P->tab);
+  free(P->np);
+  free(P->nl);
+  free(P->nh);
+  free(P->node);
+  free(P->inseq);
+  free(P->ael);
+  free(P->wel);
+  free(P->opv);
+  free(P->adt);
+  free(P->wdt);
+  free(P->inidx);
+  free(P);
+  return result;
+}
+
+/* lower_arrays(topo_order, nodes, op_code, dtype_width): the parallel walker
+   when the graph is inside its envelope, else the serial one */
+static PyObject* lower_arrays(PyObject* self, PyObject* args) {
+  PyObject *topo, *nodes, *op_fn, *width_fn;
+  if (!PyArg_ParseTuple(args, "OO!OO", &topo, &PyDict_Type, &nodes, &op_fn, &width_fn)) return NULL;
+  const char* mode = getenv("SP_LOWER_SERIAL");
+  if (!mode || !*mode || *mode == '0') {
+    const double t0 = now_ms();
+    PyObject* r = lower_parallel(topo, nodes, op_fn, width_fn);
+    if (getenv("SP_LOWER_TRACE"))
+      fprintf(stderr, "[lower] parallel %s %.2f ms\n", r ? "ok" : "declined", now_ms() - t0);
+    if (r) return r;
+  }
+  return lower_serial(self, args);
 }
 
 /*

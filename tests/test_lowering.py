@@ -82,3 +82,69 @@ def test_native_equals_numpy_on_reference_types():
     finally:
         sys.path.remove(REF)
     _same(trim_and_group(gen_transformer_stack(3, d_model=64, heads=4)))
+
+
+def _chain(n=6000, bad=None):
+    """n-node chain of matmuls (above the parallel walker's size threshold),
+    with one node perturbed to fall outside the walker's envelope."""
+    nodes = {}
+    prev = None
+    for i in range(n):
+        nm = f"net/l{i}/MatMul" if i else "net/in"
+        ins = (prev,) if prev else ()
+        w = TensorSpec((8, 8), "f32", bool(i % 2)) if i else None
+        nodes[nm] = GraphNode(nm, OpKind.MATMUL if i else OpKind.INPUT, ins, TensorSpec((4, 8)), w)
+        prev = nm
+    names = list(nodes)
+    if bad == "non_ascii":
+        old = names[n // 2]
+        new = old.replace("net", "nét")
+        nodes = {(new if k == old else k): v for k, v in nodes.items()}
+        names[n // 2] = new
+        nx = names[n // 2 + 1]
+        nodes[nx] = GraphNode(nx, OpKind.MATMUL, (new,), TensorSpec((4, 8)), TensorSpec((8, 8)))
+    elif bad == "list_inputs":
+        k = names[n - 3]
+        nodes[k] = GraphNode(k, OpKind.MATMUL, list(nodes[k].inputs), TensorSpec((4, 8)), TensorSpec((8, 8)))
+    elif bad == "big_int":
+        k = names[n - 2]
+        nodes[k] = GraphNode(k, OpKind.MATMUL, nodes[k].inputs, TensorSpec((4, 2 ** 40)), None)
+    elif bad == "ghost":
+        k = names[n - 1]
+        nodes[k] = GraphNode(k, OpKind.MATMUL, ("ghost",), TensorSpec((4, 8)), None)
+    elif bad == "rank9":
+        k = names[17]
+        nodes[k] = GraphNode(k, OpKind.MATMUL, nodes[k].inputs, TensorSpec(tuple([2] * 9)), None)
+    g = GroupedGraph.__new__(GroupedGraph)
+    g.nodes, g.topo_order = nodes, names
+    return g
+
+
+@pytest.mark.parametrize("threads", ["2", "3", "7", "16"])
+def test_parallel_walker_equals_numpy(monkeypatch, threads):
+    monkeypatch.setenv("SP_LOWER_THREADS", threads)
+    low = _same(motif_dag(1, "parity"))
+    assert low.ascii
+    _same(_chain())
+
+
+def test_parallel_walker_equals_serial(monkeypatch):
+    g = motif_dag(2, "parity")
+    par = lowering.lower(_Uncached(g))
+    monkeypatch.setenv("SP_LOWER_SERIAL", "1")
+    ser = lowering.lower(_Uncached(g))
+    for k in ARRAYS:
+        assert np.array_equal(getattr(par, k), getattr(ser, k)), k
+
+
+@pytest.mark.parametrize("bad", ["non_ascii", "list_inputs", "big_int"])
+def test_parallel_walker_declines_outside_envelope(bad):
+    low = _same(_chain(bad=bad))
+    assert low.ascii == (bad != "non_ascii")
+
+
+def test_parallel_walker_errors_match_serial():
+    with pytest.raises(KeyError):
+        lowering.lower(_Uncached(_chain(bad="ghost")))
+    with pytest.raises(UnsupportedSearch):
+        lowering.lower(_Uncached(_chain(bad="rank9")))

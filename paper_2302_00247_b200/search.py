@@ -388,6 +388,13 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
     return out
 
 
+def _make_dict(keys: list, vals: list) -> dict:
+    """dict(zip(keys, vals)); the native builder prefetches the scattered key objects."""
+    if _native_lower is not None:
+        return _native_lower.make_dict(keys, vals)
+    return dict(zip(keys, vals))
+
+
 def _labels(assignments) -> dict:
     return {s: spec.label for s, spec in assignments}
 
@@ -608,7 +615,7 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
         flat, R = lr
         keys.extend(flat)
         vals.extend([spec.label for _, spec in res.best.plan.assignments] * R)
-    assignments = dict(zip(keys, vals))
+    assignments = _make_dict(keys, vals)
     LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
                        launch_ms=(t3 - t2) * 1e3, overlap_host_ms=(t4 - t3) * 1e3,
                        collect_ms=(t5 - t4) * 1e3, assemble_ms=(time.perf_counter() - t5) * 1e3)

@@ -554,3 +554,75 @@ def test_replay_rejects_unroutable_and_bad_labels(backend):
     missing.pop(k)
     with pytest.raises(KeyError):
         routed_plan_for_assignments(g, m, missing, backend=backend)
+
+
+def _permuted(low, seed):
+    """The same graph with its rows in a random order (topo_rank carries the order)."""
+    import dataclasses
+
+    n = low.n_nodes
+    perm = np.random.default_rng(seed).permutation(n)  # new row r holds old row perm[r]
+    inv = np.empty(n, np.int64)
+    inv[perm] = np.arange(n)
+    names = [low.names[i] for i in perm]
+    nb = [bytes(low.name_bytes[low.name_off[i]:low.name_off[i + 1]]) for i in perm]
+    noff = np.zeros(n + 1, np.int64)
+    np.cumsum([len(b) for b in nb], out=noff[1:])
+    ins = [inv[low.in_idx[low.in_off[i]:low.in_off[i + 1]]] for i in perm]
+    ioff = np.zeros(n + 1, np.int64)
+    np.cumsum([len(x) for x in ins], out=ioff[1:])
+    return dataclasses.replace(
+        low, names=names, index_=None, name_bytes=np.frombuffer(b"".join(nb), np.uint8).copy(), name_off=noff,
+        topo_rank=low.topo_rank[perm].copy(), op=low.op[perm].copy(), act_rank=low.act_rank[perm].copy(),
+        act_shape=low.act_shape[perm].copy(), act_bytes=low.act_bytes[perm].copy(), w_rank=low.w_rank[perm].copy(),
+        w_shape=low.w_shape[perm].copy(), w_bytes=low.w_bytes[perm].copy(),
+        w_trainable=low.w_trainable[perm].copy(), in_off=ioff,
+        in_idx=np.concatenate(ins).astype(np.int32) if ins else low.in_idx.copy(), source=None)
+
+
+def _scores_by_block(backend, low, m):
+    from paper_2302_00247_b200.blocks import to_prune_doc
+    from paper_2302_00247_b200.search import Session, fold_blocks
+
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 2, session=ses)
+    off, nodes = ba.templates_csr()
+    t = backend.tables(ses.dgraph, off, nodes, m, 1 << 20, 4 << 20)
+    try:
+        res = backend.score(t)
+    finally:
+        t.close()
+    return ba, to_prune_doc(low, ba), [(r.candidates, r.valid, r.best_index, r.best_total) for r in res]
+
+
+@pytest.mark.parametrize("seed", range(0, 40, 5))
+def test_upload_layouts_permuted_rows_and_wide_dims(backend, seed):
+    """graph_upload packs shapes as int32 and synthesises identity topo ranks;
+    rows out of topological order and dims beyond int32 take the full layout.
+    All give the identical fold and scores (wide dims checked against the oracle)."""
+    import dataclasses
+
+    from oracle import oracle
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.lowering import lower
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
+    m = ClusterSpec.from_mesh("1x8")
+    _, doc, sc = _scores_by_block(backend, low, m)
+    _, pdoc, psc = _scores_by_block(backend, _permuted(low, seed), m)
+    assert pdoc == doc and psc == sc
+    # one activation with a dim past int32 (its byte count follows)
+    shp = low.act_shape.copy()
+    ab = low.act_bytes.copy()
+    r = int(np.argmax(low.act_rank))
+    width = ab[r] // max(1, int(np.prod(shp[r, :low.act_rank[r]])))
+    shp[r, 0] = (1 << 33) + 8
+    ab[r] = int(np.prod(shp[r, :low.act_rank[r]])) * width
+    wide = dataclasses.replace(low, act_shape=shp, act_bytes=ab, index_=None, source=None)
+    ba, _, wsc = _scores_by_block(backend, wide, m)
+    for b in range(ba.n_blocks):
+        exp, _ = oracle.score(wide, ba.template_nodes(b), m, hi=wsc[b][0], threads=4)
+        assert (wsc[b][0], wsc[b][1]) == (exp.candidates, exp.valid)
+        if exp.has_best:
+            assert (wsc[b][2], wsc[b][3]) == (exp.best_index, exp.best_total)

@@ -30,7 +30,7 @@ namespace {
 constexpr int KMAX = 6;          // internal producers handled by a lookup table
 constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
 constexpr int THREADS = 256;     // scoring CTA size
-constexpr int ITEM_ITERS_MAX = 64;         // work item = THREADS * iters candidates
+constexpr int ITEM_ITERS_MAX = 256;        // work item = THREADS * iters candidates
 constexpr int ITEM_ITERS_MAX_SKIP = 1024;  // ... when prefix skipping is on
 
 __host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
@@ -387,11 +387,18 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
           jj++;
         }
         if (L.k >= 3) f.r0 = L.prod;
+        // -1: no internal consumer (only boundary nodes; the paired walk
+        // stores non-boundary results unguarded)
         f.out_r = L.out_pool >= 0 ? L.out_pool * THREADS * 8 : -1;
         f.out_s = L.out_pool >= 0 ? L.out_pool * THREADS : -1;
         f.sh = nd.slot >= 0 ? 2 * (H.V - 1 - nd.slot) : 0;
-        // kf = k << 8 | boundary << 2 | min(k, 3): the walk dispatches on the low byte
-        f.kf = (L.k << 8) | ((!has_cons[n] || ext_cons[n]) ? 4 : 0) | (L.k < 3 ? L.k : 3);
+        // kf = k << 8 | boundary << 5 | min(k, 3) << 3 | one-hot class of the three
+        // common non-boundary kinds (bit 0: k = 1, bit 1: k = 0, bit 2: k = 2),
+        // which the paired walk tests first, in that order of frequency
+        const int bnd = (!has_cons[n] || ext_cons[n]) ? 1 : 0;
+        const int kc = L.k < 3 ? L.k : 3;
+        f.kf = (L.k << 8) | (bnd << 5) | (kc << 3) |
+               (bnd ? 0 : kc == 1 ? 1 : kc == 0 ? 2 : kc == 2 ? 4 : 0);
         ((FastNode*)(blob + H.fast_off))[i] = f;
       }
       ((NodeSkip*)(blob + H.skip_off))[i] = NodeSkip{L.skip_R, L.skip_m, 0};
@@ -727,7 +734,7 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
     const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
     const int4 B = lds_v4(rec + 16);
     const uint32_t b = (uint32_t)(w >> X.z) & 3u;
-    const int kc = X.w & 3;  // fan-in, 3 = general
+    const int kc = (X.w >> 3) & 3;  // fan-in, 3 = general
     uint32_t e;
     double r;
     if (kc == 1) {
@@ -765,7 +772,7 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
       r = dadd(bse, lds_f64(A.y + pe));
     }
     const uint32_t s = e & 3u;
-    if (X.w & 4) {
+    if (X.w & 32) {
       const long long x = __double_as_longlong(dadd(r, lds_f64(A.y + 32 + s * 8)));
       f = x > f ? x : f;
     }
@@ -917,7 +924,7 @@ __device__ __forceinline__ bool pair_node(const int4& A, const int4& B, const in
     fa = xa > fa ? xa : fa;
     fb = xb > fb ? xb : fb;
   }
-  if (X.x >= 0) {
+  if (!BND || X.x >= 0) {  // a non-boundary node always has an internal consumer
     const uint32_t qr = rb + X.x, qs = sb + X.y;
     sts_f64o<0>(qr, ra);
     sts_f64o<RB>(qr, rx);
@@ -943,15 +950,22 @@ __device__ __forceinline__ int walk_pair(uint32_t rec, int T, uint64_t wa, uint6
     const int4 B = lds_v4(rec + 16);
     const uint32_t ba = (uint32_t)(wa >> X.z) & 3u, bb = (uint32_t)(wb >> X.z) & 3u;
     bool go;
-    switch (X.w & 7) {  // min(fan-in, 3) | boundary << 2
-      case 1: go = pair_node<1, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
-      case 2: go = pair_node<2, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
-      case 0: go = pair_node<0, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
-      case 3: go = pair_node<3, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
-      case 5: go = pair_node<1, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
-      case 6: go = pair_node<2, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
-      case 4: go = pair_node<0, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
-      default: go = pair_node<3, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+    // bit tests, most frequent kind first (an if-chain on one value would be
+    // turned into a compare tree)
+    if (X.w & 1) {
+      go = pair_node<1, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb);
+    } else if (X.w & 2) {
+      go = pair_node<0, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb);
+    } else if (X.w & 4) {
+      go = pair_node<2, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb);
+    } else {
+      switch ((X.w >> 3) & 7) {  // min(fan-in, 3) | boundary << 2
+        case 5: go = pair_node<1, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+        case 4: go = pair_node<0, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+        case 6: go = pair_node<2, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+        case 7: go = pair_node<3, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+        default: go = pair_node<3, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
+      }
     }
     if (!go) break;
   }

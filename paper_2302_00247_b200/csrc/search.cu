@@ -2145,6 +2145,9 @@ struct TableDev {
 }  // namespace
 
 // Device buffers of a launched, not yet collected search (sp_score_launch).
+// A search in flight.  Its results (and winner detail) are copied into a
+// pinned host block right behind the kernels, so several searches can be
+// queued on the stream and each collected by its own `done` event.
 struct PendingScore {
   bool active = false;
   bool explain = false;
@@ -2155,7 +2158,45 @@ struct PendingScore {
   DevBuf<ExplainBlock> dblk;
   DevBuf<int8_t> dnode, dedge;
   DevBuf<int64_t> deoff;
+  sp_ctx* ctx = nullptr;
+  uint8_t* host = nullptr;  // pinned: out | blocks | node | edge
+  size_t host_bytes = 0, off_blk = 0, off_node = 0, off_edge = 0;
+  // 0 launch, 1 kernel start, 2 kernel end, 3 reduce end, 4 explain end, 5 results on the host
+  cudaEvent_t ev[6] = {};
+  void events() {
+    for (auto& e : ev)
+      if (!e) SP_CUDA(cudaEventCreate(&e));
+  }
+  void release_host() {
+    if (!host) return;
+    cudaEventSynchronize(ev[5]);
+    ctx->pinned_pool.push_back({host, host_bytes});
+    host = nullptr;
+    host_bytes = 0;
+  }
+  ~PendingScore() {
+    release_host();
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
 };
+
+// pinned block of at least `need` bytes from the context's pool
+static uint8_t* pinned_acquire(sp_ctx* ctx, size_t need, size_t* got) {
+  auto& pool = ctx->pinned_pool;
+  for (size_t i = 0; i < pool.size(); i++)
+    if (pool[i].second >= need) {
+      uint8_t* p = (uint8_t*)pool[i].first;
+      *got = pool[i].second;
+      pool.erase(pool.begin() + (std::ptrdiff_t)i);
+      return p;
+    }
+  const size_t n = std::max<size_t>(need, 64 << 10);
+  void* p = nullptr;
+  SP_CUDA(cudaHostAlloc(&p, n, cudaHostAllocDefault));
+  *got = n;
+  return (uint8_t*)p;
+}
 
 struct TablesPriv {
   TableDev dev;
@@ -2377,6 +2418,7 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned 
   if (n_items == 0) {
     pd.empty = true;
     pd.active = true;
+    SP_CUDA(cudaEventRecord(pd.ev[5], s));
     return;
   }
   // one small H2D for the plan: lo | hi | base | counter
@@ -2393,13 +2435,13 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned 
   unsigned long long* counter = dplan.p + 3 * nb + 1;
   ScorePlan P{t->d_blob_off.p, item_cands, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items, ctx->skip};
   const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
-  SP_CUDA(cudaEventRecord(ctx->ev[2], s));
+  SP_CUDA(cudaEventRecord(pd.ev[1], s));
   SP_LAUNCH(ctx, kern, (unsigned)grid, threads, smem_k, s, t->blobs.p, P, items.p, counter);
-  SP_CUDA(cudaEventRecord(ctx->ev[3], s));
+  SP_CUDA(cudaEventRecord(pd.ev[2], s));
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);
   SP_CUDA(cudaGetLastError());
-  SP_CUDA(cudaEventRecord(ctx->trace[0], s));
+  SP_CUDA(cudaEventRecord(pd.ev[3], s));
   if (explain) {
     // winner detail straight from the device-side argmin: no host round trip
     DevBuf<ExplainBlock>& dblk = pd.dblk;
@@ -2417,43 +2459,62 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned 
               dedge.p);
     SP_CUDA(cudaGetLastError());
   }
-  SP_CUDA(cudaEventRecord(ctx->trace[1], s));
+  SP_CUDA(cudaEventRecord(pd.ev[4], s));
+  // results (and winner detail) to the pinned block now: collecting this
+  // search later does not wait for whatever is queued behind it
+  const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
+  pd.off_blk = ((size_t)nb * sizeof(sp_score_out) + 63) & ~(size_t)63;
+  pd.off_node = pd.off_blk + (explain ? (((size_t)nb * sizeof(ExplainBlock) + 63) & ~(size_t)63) : 0);
+  pd.off_edge = pd.off_node + (explain ? (((size_t)4 * ne + 63) & ~(size_t)63) : 0);
+  const size_t need = pd.off_edge + (explain ? (size_t)2 * nedge : 0);
+  pd.host = pinned_acquire(ctx, need, &pd.host_bytes);
+  SP_CUDA(cudaMemcpyAsync(pd.host, dout.p, (size_t)nb * sizeof(sp_score_out), cudaMemcpyDeviceToHost, s));
+  if (explain) {
+    SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_blk, pd.dblk.p, (size_t)nb * sizeof(ExplainBlock),
+                            cudaMemcpyDeviceToHost, s));
+    if (ne) SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_node, pd.dnode.p, (size_t)4 * ne, cudaMemcpyDeviceToHost, s));
+    if (nedge)
+      SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_edge, pd.dedge.p, (size_t)2 * nedge, cudaMemcpyDeviceToHost, s));
+  }
+  g_d2h_bytes += (int64_t)(nb * sizeof(sp_score_out)) +
+                 (explain ? (int64_t)(nb * sizeof(ExplainBlock)) + 4 * ne + 2 * nedge : 0);
+  SP_CUDA(cudaEventRecord(pd.ev[5], s));
   pd.active = true;
 }
 
-// Collect an enqueued search: D2H of the per-block results (and winner detail
-// into fx when it was enqueued), one stream sync.
+// Collect an enqueued search: wait for its own `done` event, then copy the
+// per-block results (and winner detail into fx when it was enqueued) out of
+// its pinned block.
 static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& res, const FusedExplain* fx) {
-  cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
   TablesPriv* priv = (TablesPriv*)t->priv;
   PendingScore& pd = priv->pending;
   if (!pd.active) throw Error(SP_ERR_CONFIG, "no search in flight on these tables");
   pd.active = false;
   res.assign(nb, sp_score_out{});
+  SP_CUDA(cudaEventSynchronize(pd.ev[5]));
   if (pd.empty) return;
   if (fx && !pd.explain) throw Error(SP_ERR_CONFIG, "winner detail requested but not enqueued");
+  std::memcpy(res.data(), pd.host, (size_t)nb * sizeof(sp_score_out));
   if (fx) {
     const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
-    pd.dblk.download((ExplainBlock*)fx->blocks, nb, s);
-    pd.dnode.download(fx->node, 4 * ne, s);
-    pd.dedge.download(fx->edge, 2 * nedge, s);
+    std::memcpy(fx->blocks, pd.host + pd.off_blk, (size_t)nb * sizeof(ExplainBlock));
+    if (ne) std::memcpy(fx->node, pd.host + pd.off_node, (size_t)4 * ne);
+    if (nedge) std::memcpy(fx->edge, pd.host + pd.off_edge, (size_t)2 * nedge);
   }
-  pd.dout.download(res.data(), nb, s);
-  SP_CUDA(cudaEventRecord(ctx->trace[2], s));
-  SP_CUDA(cudaStreamSynchronize(s));
   float ms = 0;
-  SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+  SP_CUDA(cudaEventElapsedTime(&ms, pd.ev[1], pd.ev[2]));
   ctx->score_kernel_ms = ms;
   if (getenv("SP_SCORE_TRACE")) {
     float a = 0, b = 0, c = 0, d = 0;
-    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[2]);
-    cudaEventElapsedTime(&b, ctx->ev[3], ctx->trace[0]);
-    cudaEventElapsedTime(&c, ctx->trace[0], ctx->trace[1]);
-    cudaEventElapsedTime(&d, ctx->trace[1], ctx->trace[2]);
+    cudaEventElapsedTime(&a, pd.ev[0], pd.ev[1]);
+    cudaEventElapsedTime(&b, pd.ev[2], pd.ev[3]);
+    cudaEventElapsedTime(&c, pd.ev[3], pd.ev[4]);
+    cudaEventElapsedTime(&d, pd.ev[4], pd.ev[5]);
     fprintf(stderr, "[score] nb %lld: launch->kernel %.3f ms, kernel %.3f, reduce %.3f, explain %.3f, d2h %.3f\n",
             (long long)nb, a, ms, b, c, d);
   }
+  pd.release_host();
 }
 
 void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
@@ -2469,7 +2530,12 @@ void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bo
     lo[b] = l > C ? C : (unsigned long long)l;
     hi[b] = (unsigned __int128)lo[b] + step > C ? C : lo[b] + step;
   }
-  SP_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  PendingScore& pd = ((TablesPriv*)t->priv)->pending;
+  if (pd.active) throw Error(SP_ERR_CONFIG, "a search on these tables is already in flight");
+  pd.ctx = ctx;
+  pd.events();
+  pd.release_host();
+  SP_CUDA(cudaEventRecord(pd.ev[0], ctx->stream));
   score_enqueue(ctx, t, lo, hi, explain);
 }
 
@@ -2477,11 +2543,10 @@ void score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, void* xblocks, int
   const int64_t nb = t->n_blocks;
   std::vector<sp_score_out> res;
   FusedExplain fx{xblocks, xnode, xedge};
+  PendingScore& pd = ((TablesPriv*)t->priv)->pending;
   score_finish(ctx, t, res, xblocks ? &fx : nullptr);
-  SP_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
-  SP_CUDA(cudaEventSynchronize(ctx->ev[1]));
   float ms = 0;
-  SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+  SP_CUDA(cudaEventElapsedTime(&ms, pd.ev[0], pd.ev[5]));
   ctx->score_ms = ms;
   for (int64_t b = 0; b < nb; b++) {
     out[b] = res.empty() ? sp_score_out{} : res[b];

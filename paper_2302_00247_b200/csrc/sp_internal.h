@@ -8,6 +8,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/shardsearch.h"
@@ -104,6 +105,8 @@ struct sp_ctx {
   sp::DevBuf<uint8_t> cub_tmp;
   void* staging = nullptr;  // pinned host staging for graph uploads
   size_t staging_bytes = 0;
+  // free pinned host blocks for score results (D2H enqueued at launch time)
+  std::vector<std::pair<void*, size_t>> pinned_pool;
 };
 
 // Device-resident lowered graph (+ the host copies the library needs).

@@ -405,7 +405,7 @@ class _Search:
     Host work placed between the two overlaps the device search."""
 
     def __init__(self, ses: Session, csr, mesh, mu: int, chunk_size: int, shard: int, n_shards: int,
-                 exchange: Optional[Callable]):
+                 exchange: Optional[Callable], launch: bool = True):
         self.ses, self.mesh, self.mu, self.chunk_size = ses, mesh, mu, chunk_size
         self.exchange = exchange
         self._fetched = None
@@ -418,12 +418,18 @@ class _Search:
                                          chunk_size if not self.bad_mu else mu)
         ses.last_table_bytes = self.tables.nbytes
         self.tables_ms = (time.perf_counter() - ta) * 1e3
+        self.shard, self.n_shards = shard, n_shards
+        self.explain = exchange is None and n_shards == 1
+        if launch:
+            self.launch()
+
+    def launch(self) -> None:
+        """Queue the scoring (and the copy of its results to the host) on the stream."""
         try:
             if self.tables.overflow:
                 raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")
-            self.explain = exchange is None and n_shards == 1
             self.t_launch = time.perf_counter()
-            ses.backend.score_launch(self.tables, shard, n_shards, explain=self.explain)
+            self.ses.backend.score_launch(self.tables, self.shard, self.n_shards, explain=self.explain)
         except BaseException:
             self.tables.close()
             raise
@@ -564,14 +570,21 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     # two launches when the blocks split into cheap and expensive ones: the
     # cheap group's results (typically hundreds of residual singletons) are
     # turned into RoutedPlans while the device still scores the expensive group
+    # every group's tables first (each build syncs the stream once), then all
+    # launches back to back: each search copies its results to the host behind
+    # its own kernels, so the cheap group is collected while the expensive one
+    # still scores
     searches = []
-    for ids, gcsr in _block_groups(ses.low, csr):
-        if searches:
-            # the cheap group's results come back BEFORE the expensive launch is
-            # queued behind them on the stream (its RoutedPlans are built while
-            # the expensive group scores)
-            searches[-1][0].fetch()
-        searches.append((_Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange), ids))
+    try:
+        for ids, gcsr in _block_groups(ses.low, csr):
+            searches.append((_Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange,
+                                     launch=False), ids))
+        for srch, _ in searches:
+            srch.launch()
+    except BaseException:
+        for srch, _ in searches:
+            srch.tables.close()
+        raise
     # host work that does not depend on the winners overlaps the device search:
     # Subgraph objects, the static part of every RoutedPlan, and the member
     # scopes that receive each block's weight labels (search.py:374-376)

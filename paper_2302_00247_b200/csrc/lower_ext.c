@@ -1035,8 +1035,8 @@ static PyObject* make_dict(PyObject* self, PyObject* args) {
   }
   PyObject* d = _PyDict_NewPresized(n);
   if (!d) return NULL;
-  PyObject** K = &PyList_GET_ITEM(keys, 0);
-  PyObject** V = &PyList_GET_ITEM(vals, 0);
+  PyObject** K = n ? &PyList_GET_ITEM(keys, 0) : NULL;
+  PyObject** V = n ? &PyList_GET_ITEM(vals, 0) : NULL;
   enum { AHEAD = 24 };
   for (Py_ssize_t i = 0; i < n; i++) {
     if (i + AHEAD < n) __builtin_prefetch(K[i + AHEAD], 1, 0);

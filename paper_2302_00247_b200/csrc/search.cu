@@ -31,7 +31,7 @@ constexpr int KMAX = 6;          // internal producers handled by a lookup table
 constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
 constexpr int THREADS = 256;     // scoring CTA size
 constexpr int ITEM_ITERS_MAX = 256;        // work item = THREADS * iters candidates
-constexpr int ITEM_ITERS_MAX_SKIP = 1024;  // ... when prefix skipping is on
+constexpr int ITEM_ITERS_MAX_SKIP = 512;   // ... when prefix skipping is on
 
 __host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 __host__ __device__ inline uint32_t pow3(int k) {

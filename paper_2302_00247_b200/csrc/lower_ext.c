@@ -475,6 +475,7 @@ done:
 
 #define PAR_MAX_THREADS 32
 #define PAR_MIN_NODES 4096
+#define PAR_DISTINCT 32
 
 static Py_ssize_t slot_offset(PyTypeObject* tp, PyObject* name) {
   PyObject* d = PyObject_GetAttr((PyObject*)tp, name);
@@ -563,6 +564,22 @@ typedef struct Par {
   uint8_t *arank, *wrank, *wtrain;
   int32_t* inidx;
   int nthreads, go, fail;
+  /* the names list is built by the workers; name bytes allocated between phases */
+  PyObject* names_list;
+  PyObject* b_names;
+  Py_ssize_t nbytes;
+  /* enum members -> codes: distinct objects per thread (phase 3), mapped by
+     thread 0 through the Python functions, applied in phase 4 */
+  PyObject *op_fn, *width_fn;
+  PyObject* dop[PAR_MAX_THREADS][PAR_DISTINCT];
+  PyObject* ddt[PAR_MAX_THREADS][PAR_DISTINCT];
+  int nop[PAR_MAX_THREADS], ndt[PAR_MAX_THREADS];
+  PyObject* mop[PAR_MAX_THREADS * PAR_DISTINCT];
+  PyObject* mdt[PAR_MAX_THREADS * PAR_DISTINCT];
+  long cop[PAR_MAX_THREADS * PAR_DISTINCT], cdt[PAR_MAX_THREADS * PAR_DISTINCT];
+  int nmop, nmdt;
+  uint8_t* op;
+  int64_t *abytes, *wbytes;
   Py_ssize_t bytes_part[PAR_MAX_THREADS], edges_part[PAR_MAX_THREADS];
   int max_ar[PAR_MAX_THREADS], max_wr[PAR_MAX_THREADS];
   pthread_barrier_t bar;
@@ -583,6 +600,50 @@ static inline int32_t par_find(const Par* P, const char* p, Py_ssize_t n, uint64
     const int32_t j = v - 1;
     if (P->nh[j] == h && P->nl[j] == n && memcmp(P->np[j], p, (size_t)n) == 0) return j;
   }
+}
+
+/* add o to a small distinct-pointer set; 0 when the set is full */
+static inline int distinct_add(PyObject** set, int* n, PyObject* o) {
+  for (int k = 0; k < *n; k++)
+    if (set[k] == o) return 1;
+  if (*n == PAR_DISTINCT) return 0;
+  set[(*n)++] = o;
+  return 1;
+}
+
+static inline long code_of(PyObject* const* keys, const long* vals, int n, PyObject* o) {
+  for (int k = 0; k < n; k++)
+    if (keys[k] == o) return vals[k];
+  return -1;
+}
+
+/* thread 0 between phases 3 and 4 (it holds the GIL): map every distinct
+   enum member through the Python functions; 0 on failure (error cleared) */
+static int par_map_codes(Par* P) {
+  P->nmop = P->nmdt = 0;
+  for (int u = 0; u < P->nthreads; u++) {
+    for (int k = 0; k < P->nop[u]; k++)
+      if (code_of(P->mop, P->cop, P->nmop, P->dop[u][k]) < 0) P->mop[P->nmop++] = P->dop[u][k];
+    for (int k = 0; k < P->ndt[u]; k++)
+      if (code_of(P->mdt, P->cdt, P->nmdt, P->ddt[u][k]) < 0) P->mdt[P->nmdt++] = P->ddt[u][k];
+  }
+  for (int pass = 0; pass < 2; pass++) {
+    PyObject* fn = pass ? P->width_fn : P->op_fn;
+    PyObject** keys = pass ? P->mdt : P->mop;
+    long* vals = pass ? P->cdt : P->cop;
+    const int n = pass ? P->nmdt : P->nmop;
+    for (int k = 0; k < n; k++) {
+      PyObject* r = PyObject_CallOneArg(fn, keys[k]);
+      long v = r ? PyLong_AsLong(r) : -1;
+      Py_XDECREF(r);
+      if (!r || (v == -1 && PyErr_Occurred()) || v < 0) {
+        PyErr_Clear();
+        return 0;
+      }
+      vals[k] = v;
+    }
+  }
+  return 1;
 }
 
 static void par_phases(Par* P, int t) {
@@ -617,6 +678,17 @@ static void par_phases(Par* P, int t) {
   }
   P->bytes_part[t] = bytes;
   pthread_barrier_wait(&P->bar);
+  if (t == 0 && !par_failed(P)) {  /* the name-byte buffer (this thread holds the GIL) */
+    Py_ssize_t nb = 0;
+    for (int u = 0; u < T; u++) nb += P->bytes_part[u];
+    P->b_names = PyByteArray_FromStringAndSize(NULL, nb > 0 ? nb : 0);
+    if (!P->b_names) {
+      PyErr_Clear();
+      par_fail(P);
+    } else {
+      P->pn = PyByteArray_AS_STRING(P->b_names);
+    }
+  }
   /* phase 2: dict entries -> rows */
   for (Py_ssize_t j = dlo; j < dhi && !par_failed(P); j++) {
     const char* p;
@@ -644,6 +716,9 @@ static void par_phases(Par* P, int t) {
     base += P->nl[i];
     P->noff[i + 1] = base;
     P->opv[i] = op;
+    if (!distinct_add(P->dop[t], &P->nop[t], op)) goto bad;
+    Py_INCREF(P->names[i]);  /* distinct objects (duplicates failed phase 1) */
+    PyList_SET_ITEM(P->names_list, i, P->names[i]);
     PyObject *sh = slot_read(a, P->o_shape), *dt = slot_read(a, P->o_dtype);
     int r;
     int64_t el;
@@ -654,6 +729,7 @@ static void par_phases(Par* P, int t) {
     P->arank[i] = (uint8_t)(r > 255 ? 255 : r);
     P->ael[i] = el;
     P->adt[i] = dt;
+    if (!distinct_add(P->ddt[t], &P->ndt[t], dt)) goto bad;
     if (w == Py_None) {
       P->wrank[i] = 0;
       memset(P->wshape + i * MAX_RANK, 0, MAX_RANK * 8);
@@ -670,6 +746,7 @@ static void par_phases(Par* P, int t) {
       P->wrank[i] = (uint8_t)(r > 255 ? 255 : r);
       P->wel[i] = el;
       P->wdt[i] = wdt;
+      if (!distinct_add(P->ddt[t], &P->ndt[t], wdt)) goto bad;
       P->wtrain[i] = tr == Py_True;
     }
     P->inseq[i] = in;
@@ -687,7 +764,7 @@ static void par_phases(Par* P, int t) {
     Py_ssize_t E = 0;
     for (int u = 0; u < T; u++) E += P->edges_part[u];
     P->inidx = (int32_t*)malloc((size_t)(E ? E : 1) * sizeof(int32_t));
-    if (!P->inidx) par_fail(P);
+    if (!P->inidx || !par_map_codes(P)) par_fail(P);
   }
   pthread_barrier_wait(&P->bar);
   if (par_failed(P)) return;
@@ -695,6 +772,9 @@ static void par_phases(Par* P, int t) {
   Py_ssize_t e = 0;
   for (int u = 0; u < t; u++) e += P->edges_part[u];
   for (Py_ssize_t i = lo; i < hi; i++) {
+    P->op[i] = (uint8_t)code_of(P->mop, P->cop, P->nmop, P->opv[i]);
+    P->abytes[i] = P->ael[i] * (int64_t)code_of(P->mdt, P->cdt, P->nmdt, P->adt[i]);
+    P->wbytes[i] = P->wdt[i] ? P->wel[i] * (int64_t)code_of(P->mdt, P->cdt, P->nmdt, P->wdt[i]) : 0;
     PyObject* in = P->inseq[i];
     const Py_ssize_t k = PyTuple_GET_SIZE(in);
     for (Py_ssize_t j = 0; j < k; j++) {
@@ -750,7 +830,6 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   PyObject *result = NULL, *names = NULL;
   PyObject *b_names = NULL, *b_noff = NULL, *b_op = NULL, *b_arank = NULL, *b_ashape = NULL, *b_abytes = NULL,
            *b_wrank = NULL, *b_wshape = NULL, *b_wbytes = NULL, *b_wtrain = NULL, *b_inoff = NULL, *b_inidx = NULL;
-  PtrCache opc = {{0}, {0}, 0}, wc = {{0}, {0}, 0};
   pthread_t th[PAR_MAX_THREADS];
   ParArg pa[PAR_MAX_THREADS];
   int created = 1;
@@ -767,18 +846,19 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   P->o_dtype = slot_offset(P->t_spec, s_dtype);
   P->o_train = slot_offset(P->t_spec, s_trainable);
   if (P->o_shape < 0 || P->o_dtype < 0 || P->o_train < 0) goto out;
-  names = PySequence_List(topo);
+  double tp[8];
+  tp[0] = now_ms();
+  /* the workers fill the returned names list (one reference per distinct name) */
+  names = PyList_New(n);
   if (!names) {
     PyErr_Clear();
     goto out;
   }
-  P->names = &PyList_GET_ITEM(names, 0);
-  Py_ssize_t nbytes = 0;
-  for (Py_ssize_t i = 0; i < n; i++) {
-    PyObject* o = P->names[i];
-    if (!PyUnicode_CheckExact(o) || !PyUnicode_IS_COMPACT_ASCII(o)) goto out;
-    nbytes += PyUnicode_GET_LENGTH(o);
-  }
+  P->names_list = names;
+  P->names = PySequence_Fast_ITEMS(topo);
+  P->op_fn = op_fn;
+  P->width_fn = width_fn;
+  tp[1] = tp[2] = now_ms();
   P->nd = PyDict_GET_SIZE(nodes);
   P->dkey = (PyObject**)malloc((size_t)P->nd * sizeof(PyObject*));
   P->dval = (PyObject**)malloc((size_t)P->nd * sizeof(PyObject*));
@@ -793,6 +873,7 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
     }
     P->nd = j;
   }
+  tp[3] = now_ms();
   size_t cap = 16;
   while (cap < (size_t)n * 2) cap <<= 1;
   P->mask = cap - 1;
@@ -810,7 +891,6 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   if (!P->tab || !P->np || !P->nl || !P->nh || !P->node || !P->inseq || !P->ael || !P->wel || !P->opv || !P->adt ||
       !P->wdt)
     goto out;
-  b_names = new_bytearray(nbytes);
   b_noff = new_bytearray((n + 1) * 8);
   b_op = new_bytearray(n);
   b_arank = new_bytearray(n);
@@ -821,12 +901,14 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   b_wbytes = new_bytearray(n * 8);
   b_wtrain = new_bytearray(n);
   b_inoff = new_bytearray((n + 1) * 8);
-  if (!b_names || !b_noff || !b_op || !b_arank || !b_ashape || !b_abytes || !b_wrank || !b_wshape || !b_wbytes ||
-      !b_wtrain || !b_inoff) {
+  if (!b_noff || !b_op || !b_arank || !b_ashape || !b_abytes || !b_wrank || !b_wshape || !b_wbytes || !b_wtrain ||
+      !b_inoff) {
     PyErr_Clear();
     goto out;
   }
-  P->pn = PyByteArray_AS_STRING(b_names);
+  P->op = (uint8_t*)PyByteArray_AS_STRING(b_op);
+  P->abytes = (int64_t*)PyByteArray_AS_STRING(b_abytes);
+  P->wbytes = (int64_t*)PyByteArray_AS_STRING(b_wbytes);
   P->noff = (int64_t*)PyByteArray_AS_STRING(b_noff);
   P->arank = (uint8_t*)PyByteArray_AS_STRING(b_arank);
   P->ashape = (int64_t*)PyByteArray_AS_STRING(b_ashape);
@@ -850,33 +932,26 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
     for (int t = 1; t < created; t++) pthread_join(th[t], NULL);
     goto out;
   }
-  __atomic_store_n(&P->go, 1, __ATOMIC_RELEASE);
-  par_phases(P, 0);
-  for (int t = 1; t < created; t++) pthread_join(th[t], NULL);
-  pthread_barrier_destroy(&P->bar);
+  tp[4] = now_ms();
+  {
+    /* no collection while the workers read the object graph (thread 0
+       allocates between phases) */
+    const int gc_was = PyGC_Disable();
+    __atomic_store_n(&P->go, 1, __ATOMIC_RELEASE);
+    par_phases(P, 0);
+    for (int t = 1; t < created; t++) pthread_join(th[t], NULL);
+    pthread_barrier_destroy(&P->bar);
+    if (gc_was) PyGC_Enable();
+  }
+  tp[5] = now_ms();
+  b_names = P->b_names;  /* owned from here on */
+  P->b_names = NULL;
   if (par_failed(P)) goto out;
   {
-    /* enum members -> codes / widths (pointer-keyed caches, a few Python calls) */
-    uint8_t* op = (uint8_t*)PyByteArray_AS_STRING(b_op);
-    int64_t* abytes = (int64_t*)PyByteArray_AS_STRING(b_abytes);
-    int64_t* wbytes = (int64_t*)PyByteArray_AS_STRING(b_wbytes);
     int max_ar = 0, max_wr = 0;
     for (int u = 0; u < created; u++) {
       if (P->max_ar[u] > max_ar) max_ar = P->max_ar[u];
       if (P->max_wr[u] > max_wr) max_wr = P->max_wr[u];
-    }
-    for (Py_ssize_t i = 0; i < n; i++) {
-      long v;
-      if (cache_get_any(&opc, P->opv[i], op_fn, &v) < 0) goto err;
-      op[i] = (uint8_t)v;
-      if (cache_get_any(&wc, P->adt[i], width_fn, &v) < 0) goto err;
-      abytes[i] = P->ael[i] * (int64_t)v;
-      if (P->wdt[i]) {
-        if (cache_get_any(&wc, P->wdt[i], width_fn, &v) < 0) goto err;
-        wbytes[i] = P->wel[i] * (int64_t)v;
-      } else {
-        wbytes[i] = 0;
-      }
     }
     const Py_ssize_t E = P->inoff[n];
     b_inidx = PyByteArray_FromStringAndSize((const char*)P->inidx, E * 4);
@@ -884,14 +959,15 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
     result = Py_BuildValue("(OiiizOOOOOOOOOOOO)", names, 1, max_ar, max_wr, NULL, b_names, b_noff, b_op, b_arank,
                            b_ashape, b_abytes, b_wrank, b_wshape, b_wbytes, b_wtrain, b_inoff, b_inidx);
     if (!result) goto err;
+    if (getenv("SP_LOWER_TRACE"))
+      fprintf(stderr, "[lower-par] setup %.2f dict %.2f alloc %.2f threads %.2f post %.2f ms (%d threads)\n",
+              tp[1] - tp[0], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], now_ms() - tp[5], created);
     goto out;
   err:
     /* a Python mapping call failed: let the serial walker raise it */
     PyErr_Clear();
   }
 out:
-  cache_clear(&opc);
-  cache_clear(&wc);
   Py_XDECREF(names);
   Py_XDECREF(b_names);
   Py_XDECREF(b_noff);

@@ -207,7 +207,11 @@ int sp_search(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* bl
  * detail of sp_explain_all) on the context's stream and returns at once, so
  * the caller can assemble host-side results while the device searches;
  * sp_score_wait collects it (blocks/node_detail/edge_detail may be NULL, and
- * must be when `explain` was 0).  One search may be in flight per tables.
+ * must be when `explain` was 0).  One search may be in flight per tables;
+ * searches on different tables may be queued back to back: each copies its
+ * results to pinned host memory behind its own kernels and sp_score_wait
+ * waits on that search's event only, so an early search is collected while
+ * later ones still run.
  * No reference counterpart: the reference's pool.map blocks (search.py:338).
  */
 int sp_score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, int32_t explain);

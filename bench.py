@@ -22,7 +22,7 @@ candidate of every block + winner reconstruction + report assembly.
 (oracle/oracle.c, all host threads) on a bounded sample of the same workload.
 
 Multi-GPU (torchrun): every rank folds (replicated) and scores its
-contiguous slice of each block's candidate range; one NCCL all_gather of
+round-robin share of each block's work items; one NCCL all_gather of
 48-byte per-block records merges the exact argmin (strong scaling).
 """
 

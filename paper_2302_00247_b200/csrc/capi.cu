@@ -42,6 +42,7 @@ int sp_ctx_create(int device, sp_ctx** out) {
     SP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     ctx->smem_optin = (size_t)optin;
     SP_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
     // every scratch buffer is stream-ordered (cudaMallocAsync): keep freed
     // memory in the device pool instead of returning it at each sync, so the
     // per-call buffers of fold / tables / score are re-used, not re-mapped
@@ -73,6 +74,10 @@ void sp_ctx_destroy(sp_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->timer)
     if (e) cudaEventDestroy(e);
+  if (ctx->aux) {
+    cudaStreamSynchronize(ctx->aux);
+    cudaStreamDestroy(ctx->aux);
+  }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -14,6 +14,7 @@
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <stddef.h>
 #include <stdint.h>
 #include <string.h>
 #include <time.h>
@@ -1133,8 +1134,111 @@ static PyObject* make_dict(PyObject* self, PyObject* args) {
   return d;
 }
 
+
+/*
+ * Ctor(cls, field_names): a callable that builds instances of a dataclass
+ * from positional field values without running its generated __init__
+ * (object.__new__ + generic attribute stores; frozen classes included).  For
+ * the result objects of a search (~10^4 per c5 step) the generated __init__,
+ * which goes through object.__setattr__ once per field for frozen classes,
+ * is most of the assembly time.  Only for classes without __post_init__ and
+ * with every field passed.
+ */
+typedef struct {
+  PyObject_HEAD
+  PyTypeObject* cls;
+  PyObject* names;  /* tuple of interned str: the positional fields */
+  PyObject* fixed_names;  /* remaining fields, set to shared default values */
+  PyObject* fixed_values;
+  vectorcallfunc vectorcall;
+} CtorObject;
+
+static PyObject* ctor_vectorcall(PyObject* self, PyObject* const* args, size_t nargsf, PyObject* kwnames) {
+  CtorObject* c = (CtorObject*)self;
+  const Py_ssize_t n = PyVectorcall_NARGS(nargsf);
+  const Py_ssize_t nf = PyTuple_GET_SIZE(c->names);
+  if (kwnames || n != nf) {
+    PyErr_Format(PyExc_TypeError, "%s ctor takes exactly %zd positional arguments", c->cls->tp_name, nf);
+    return NULL;
+  }
+  static PyObject* empty = NULL;
+  if (!empty && !(empty = PyTuple_New(0))) return NULL;
+  PyObject* o = c->cls->tp_new(c->cls, empty, NULL);
+  if (!o) return NULL;
+  for (Py_ssize_t i = 0; i < nf; i++)
+    if (PyObject_GenericSetAttr(o, PyTuple_GET_ITEM(c->names, i), args[i]) < 0) {
+      Py_DECREF(o);
+      return NULL;
+    }
+  for (Py_ssize_t i = 0; i < PyTuple_GET_SIZE(c->fixed_names); i++)
+    if (PyObject_GenericSetAttr(o, PyTuple_GET_ITEM(c->fixed_names, i), PyTuple_GET_ITEM(c->fixed_values, i)) < 0) {
+      Py_DECREF(o);
+      return NULL;
+    }
+  return o;
+}
+
+static void ctor_dealloc(PyObject* self) {
+  CtorObject* c = (CtorObject*)self;
+  Py_XDECREF(c->cls);
+  Py_XDECREF(c->names);
+  Py_XDECREF(c->fixed_names);
+  Py_XDECREF(c->fixed_values);
+  Py_TYPE(self)->tp_free(self);
+}
+
+static PyTypeObject CtorType = {
+    PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_lower.Ctor",
+    .tp_basicsize = sizeof(CtorObject),
+    .tp_dealloc = ctor_dealloc,
+    .tp_call = PyVectorcall_Call,
+    .tp_vectorcall_offset = offsetof(CtorObject, vectorcall),
+    .tp_flags = Py_TPFLAGS_DEFAULT | Py_TPFLAGS_HAVE_VECTORCALL,
+};
+
+static PyObject* make_ctor(PyObject* self, PyObject* args) {
+  PyObject *cls, *names, *fixed_names = NULL, *fixed_values = NULL;
+  if (!PyArg_ParseTuple(args, "O!O!|O!O!", &PyType_Type, &cls, &PyTuple_Type, &names, &PyTuple_Type, &fixed_names,
+                        &PyTuple_Type, &fixed_values))
+    return NULL;
+  if ((fixed_names ? PyTuple_GET_SIZE(fixed_names) : 0) != (fixed_values ? PyTuple_GET_SIZE(fixed_values) : 0)) {
+    PyErr_SetString(PyExc_ValueError, "fixed names and values differ in length");
+    return NULL;
+  }
+  if (PyType_Ready(&CtorType) < 0) return NULL;
+  CtorObject* c = PyObject_New(CtorObject, &CtorType);
+  if (!c) return NULL;
+  c->cls = NULL;
+  c->names = c->fixed_names = c->fixed_values = NULL;
+  Py_INCREF(cls);
+  c->cls = (PyTypeObject*)cls;
+  c->fixed_names = fixed_names ? fixed_names : PyTuple_New(0);
+  c->fixed_values = fixed_values ? fixed_values : PyTuple_New(0);
+  if (fixed_names) Py_INCREF(fixed_names);
+  if (fixed_values) Py_INCREF(fixed_values);
+  c->names = PyTuple_New(PyTuple_GET_SIZE(names));
+  if (!c->names) {
+    Py_DECREF(c);
+    return NULL;
+  }
+  for (Py_ssize_t i = 0; i < PyTuple_GET_SIZE(names); i++) {
+    PyObject* nm = PyTuple_GET_ITEM(names, i);
+    if (!PyUnicode_Check(nm)) {
+      PyErr_SetString(PyExc_TypeError, "field names must be str");
+      Py_DECREF(c);
+      return NULL;
+    }
+    Py_INCREF(nm);
+    PyUnicode_InternInPlace(&nm);
+    PyTuple_SET_ITEM(c->names, i, nm);
+  }
+  c->vectorcall = ctor_vectorcall;
+  return (PyObject*)c;
+}
+
 static PyMethodDef methods[] = {
     {"lower_arrays", lower_arrays, METH_VARARGS, "Lower a grouped ModelGraph to flat sp_graph arrays."},
+    {"make_ctor", make_ctor, METH_VARARGS, "Fast positional constructor for a dataclass."},
     {"make_dict", make_dict, METH_VARARGS, "dict(zip(keys, values)) with prefetched key objects."},
     {"block_instances", block_instances, METH_VARARGS, "Subgraph.instances of every block from fold arrays."},
     {NULL, NULL, 0, NULL}};

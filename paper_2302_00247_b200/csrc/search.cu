@@ -537,6 +537,7 @@ __device__ __forceinline__ void mr_add(uint64_t& w0, uint64_t& w1, uint32_t t, i
 struct ScorePlan {
   const int64_t* blob_off;
   unsigned long long item_cands;        // candidates per work item
+  unsigned long long item_stride;       // index distance between a rank's consecutive items
   const unsigned long long* lo;         // per block start (enumeration index space)
   const unsigned long long* hi;
   const unsigned long long* item_base;  // prefix sum of items per block, [nb+1]
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
     const Biased bz = s_bz;
-    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_stride;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
     const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
@@ -1401,13 +1402,13 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
       staged = b;
     }
     if (tid == 0) {
-      s_wbase = bencode(*(const BlobHeader*)smem, P.lo[b] + (item - P.item_base[b]) * P.item_cands);
+      s_wbase = bencode(*(const BlobHeader*)smem, P.lo[b] + (item - P.item_base[b]) * P.item_stride);
       s_chunk = 0;
     }
     __syncthreads();
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
-    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_stride;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     unsigned long long best_t = ~0ULL, best_i = ~0ULL;
     uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
@@ -1596,7 +1597,7 @@ __global__ void __launch_bounds__(THREADS_M, 4) k_score_memo(const uint8_t* __re
     double* cache = (double*)(smem + ((H.bytes + 15) & ~15));
     Tabs S = tabs_of(smem);
     const int T = H.T;
-    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_cands;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_stride;
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     const unsigned long long span = (ihi - ilo + (THREADS_M / 32) - 1) / (THREADS_M / 32);
     const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
@@ -2056,6 +2057,7 @@ __global__ void k_explain_all(GraphView G, const int64_t* tmpl_off, const int32_
       node_out[4 * (e0 + i)] = (int8_t)R.pattern;
       node_out[4 * (e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
       node_out[4 * (e0 + i) + 2] = -1;
+      node_out[4 * (e0 + i) + 3] = 0;  // unused byte, kept deterministic
     }
     if (!ok) {
       out[b] = X;
@@ -2203,6 +2205,12 @@ struct TablesPriv {
   sp_mesh mesh;
   int64_t mu, chunk;
   PendingScore pending;
+  // recorded behind k_fill: work on the auxiliary stream (explain_all) waits
+  // for the tables, not for whatever was queued on the main stream since
+  cudaEvent_t built = nullptr;
+  ~TablesPriv() {
+    if (built) cudaEventDestroy(built);
+  }
 };
 
 }  // namespace sp
@@ -2348,6 +2356,11 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
               D.node_tpos.p, D.slot_of.p, D.ref_slot_of.p, lay.p, hdr.p, out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
               chunk, out->blobs.p, D.bound.p);
   SP_CUDA(cudaGetLastError());
+  {
+    TablesPriv* tp = (TablesPriv*)out->priv;
+    if (!tp->built) SP_CUDA(cudaEventCreateWithFlags(&tp->built, cudaEventDisableTiming));
+    SP_CUDA(cudaEventRecord(tp->built, s));
+  }
 }
 
 static size_t score_smem(const sp_tables* t) {
@@ -2363,8 +2376,7 @@ struct FusedExplain {
 // Enqueue scoring (+ k_reduce, + winner detail when `explain`) of
 // [lo[b], hi[b]) for every block; the buffers stay in the tables' pending
 // slot until score_finish collects them.
-static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned long long>& lo,
-                          const std::vector<unsigned long long>& hi, bool explain) {
+static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
   TablesPriv* priv = (TablesPriv*)t->priv;
@@ -2401,18 +2413,34 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned 
   SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem_k));
   if (per_sm < 1) per_sm = 1;
   const unsigned long long slots = (unsigned long long)ctx->sm_count * per_sm;
-  // size work items so the grid gets ~8 items per resident CTA (dynamic balance);
-  // with prefix skipping a candidate costs far less, so items may grow larger
+  // size work items so each rank's grid gets ~8 items per resident CTA
+  // (dynamic balance); with prefix skipping a candidate costs far less, so
+  // items may grow larger.  Ranks deal the items of every block round-robin
+  // (the global item sequence, item g to rank g mod n_shards): early-exit
+  // cost varies along a block's index range, so contiguous slices would
+  // leave one rank with the expensive end.  The merge is an exact
+  // lexicographic min, so any partition gives the same result.  The sizing
+  // depends only on the tables and n_shards: every rank derives the same
+  // items.
+  const unsigned long long N = (unsigned long long)n_shards, r = (unsigned long long)shard;
   unsigned long long total = 0;
-  for (int64_t b = 0; b < nb; b++) total += hi[b] > lo[b] ? hi[b] - lo[b] : 0;
+  for (int64_t b = 0; b < nb; b++) total += t->hdr[b].C;
   const unsigned long long cap = ctx->skip ? ITEM_ITERS_MAX_SKIP : ITEM_ITERS_MAX;
-  unsigned long long iters = (total + slots * 8 * THREADS - 1) / (slots * 8 * THREADS);
+  const unsigned long long per_rank = total / N + (total % N ? 1 : 0);
+  unsigned long long iters = (per_rank + slots * 8 * THREADS - 1) / (slots * 8 * THREADS);
   iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, memo ? ITEM_ITERS_MAX_SKIP : cap));
   const unsigned long long item_cands = iters * THREADS;
-  std::vector<unsigned long long> base(nb + 1, 0);
+  std::vector<unsigned long long> lo(nb), hi(nb), base(nb + 1, 0);
+  unsigned long long gbase = 0;
   for (int64_t b = 0; b < nb; b++) {
-    const unsigned long long c = hi[b] > lo[b] ? hi[b] - lo[b] : 0;
-    base[b + 1] = base[b] + (c + item_cands - 1) / item_cands;
+    const unsigned long long C = t->hdr[b].C;
+    const unsigned long long nch = C / item_cands + (C % item_cands ? 1 : 0);
+    const unsigned long long j0 = (r + N - gbase % N) % N;  // first item of block b dealt to this rank
+    const unsigned long long cnt = j0 < nch ? (nch - 1 - j0) / N + 1 : 0;
+    lo[b] = j0 < nch ? j0 * item_cands : C;
+    hi[b] = C;
+    base[b + 1] = base[b] + cnt;
+    gbase += nch;
   }
   const unsigned long long n_items = base[nb];
   if (n_items == 0) {
@@ -2433,7 +2461,8 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, const std::vector<unsigned 
   items.alloc(n_items, s);
   dout.alloc(nb, s);
   unsigned long long* counter = dplan.p + 3 * nb + 1;
-  ScorePlan P{t->d_blob_off.p, item_cands, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items, ctx->skip};
+  ScorePlan P{t->d_blob_off.p, item_cands, item_cands * N, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items,
+              ctx->skip};
   const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
   SP_CUDA(cudaEventRecord(pd.ev[1], s));
   SP_LAUNCH(ctx, kern, (unsigned)grid, threads, smem_k, s, t->blobs.p, P, items.p, counter);
@@ -2520,23 +2549,13 @@ static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& r
 void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
   if (n_shards < 1 || shard < 0 || shard >= n_shards) throw Error(SP_ERR_CONFIG, "bad shard / n_shards");
   if (t->overflow) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
-  const int64_t nb = t->n_blocks;
-  std::vector<unsigned long long> lo(nb), hi(nb);
-  for (int64_t b = 0; b < nb; b++) {
-    const unsigned long long C = t->hdr[b].C;
-    // contiguous split like search_subgraph's pool ranges (search.py:331-336)
-    const unsigned long long step = C / (unsigned long long)n_shards + (C % (unsigned long long)n_shards ? 1 : 0);
-    const unsigned __int128 l = (unsigned __int128)step * (unsigned)shard;
-    lo[b] = l > C ? C : (unsigned long long)l;
-    hi[b] = (unsigned __int128)lo[b] + step > C ? C : lo[b] + step;
-  }
   PendingScore& pd = ((TablesPriv*)t->priv)->pending;
   if (pd.active) throw Error(SP_ERR_CONFIG, "a search on these tables is already in flight");
   pd.ctx = ctx;
   pd.events();
   pd.release_host();
   SP_CUDA(cudaEventRecord(pd.ev[0], ctx->stream));
-  score_enqueue(ctx, t, lo, hi, explain);
+  score_enqueue(ctx, t, shard, n_shards, explain);
 }
 
 void score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, void* xblocks, int8_t* xnode, int8_t* xedge) {
@@ -2644,10 +2663,13 @@ void explain(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t index, sp_explai
 
 void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* blocks_out, int8_t* node_out,
                  int8_t* edge_out) {
-  cudaStream_t s = ctx->stream;
+  // on the auxiliary stream, after the tables only: a search queued on the
+  // main stream meanwhile (the expensive block group) does not delay it
+  cudaStream_t s = ctx->aux;
   const int64_t nb = t->n_blocks;
   if (nb == 0) return;
   TablesPriv* priv = (TablesPriv*)t->priv;
+  SP_CUDA(cudaStreamWaitEvent(s, priv->built, 0));
   const int64_t ne = t->tmpl_off[nb];
   const int64_t nedge = t->edge_off[nb];
   // one H2D (indices + edge offsets), one D2H per output array

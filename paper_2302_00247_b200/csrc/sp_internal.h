@@ -90,6 +90,7 @@ struct sp_ctx {
   int sm_count = 148;
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // explain_all of a group while another search runs on `stream`
   cudaEvent_t ev[8] = {};
   std::string last_error;
   double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;

@@ -1,8 +1,10 @@
 """Multi-GPU search: candidate ranges sharded over ranks, exact key exchange.
 
-Each rank (one process per GPU) scores its contiguous slice of every block's
-index range -- the split search_subgraph hands its worker pool
-(search.py:331-336).  Per block the ranks then exchange one record
+Each rank (one process per GPU) scores its share of every block's index
+range: the work items of all blocks are dealt round-robin over the ranks
+(search_subgraph hands its worker pool contiguous slices, search.py:331-336;
+early-exit cost varies along a range, so contiguous slices load one rank
+with the expensive end).  Per block the ranks then exchange one record
 (candidates, valid, index, total bits, num_split, has_best) with a single
 all_gather over NCCL and reduce it, vectorised over blocks, to the
 lexicographic (total, num_split, index) minimum and the summed valid count

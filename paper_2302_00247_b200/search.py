@@ -16,6 +16,7 @@ resource (multi-GPU sharding lives in ``paper_2302_00247_b200.dist``).
 
 from __future__ import annotations
 
+import dataclasses
 import gc
 import math
 import time
@@ -84,7 +85,7 @@ def subgraphs_from_blocks(low: LoweredGraph, ba: BlockArrays, types: TypeSet = D
             low.names, np.ascontiguousarray(ba.members, np.int32), np.ascontiguousarray(ba.inst_prefix_node, np.int64),
             np.ascontiguousarray(ba.inst_prefix_len, np.int64), np.ascontiguousarray(ba.block_inst_off, np.int64),
             np.ascontiguousarray(ba.block_T, np.int64), ascii_names)
-        subgraph = types.Subgraph
+        subgraph = _ctor(types.Subgraph, 3)
         return [subgraph(insts[0][0], insts[0][1], insts) for insts in per_block]
     names = low.names
     member_names = list(map(names.__getitem__, ba.members.tolist()))
@@ -335,7 +336,8 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
     identity = types.Collective(types.CollectiveKind.IDENTITY)
     allreduce = types.Collective(types.CollectiveKind.ALL_REDUCE_SUM)
     colls = {}
-    NodeRouting, CandidatePlan, RoutedPlan = types.NodeRouting, types.CandidatePlan, types.RoutedPlan
+    NodeRouting, CandidatePlan = _ctor(types.NodeRouting, 6), _ctor(types.CandidatePlan, 3)
+    RoutedPlan, CostReport = _ctor(types.RoutedPlan, 4), _ctor(types.CostReport, 6)
     overlap = mesh.overlap_fraction
     out = []
     e0 = 0
@@ -377,15 +379,37 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
                     c = colls[key] = _collective(types, 2, xax)
                 exits.append((scope, c, obytes))
         bbc = {_KIND_LABEL[j + 1]: int(X.bytes[j]) for j in range(4) if X.calls[j]}
-        cost = types.CostReport(forward_comm=X.forward_comm, backward_comm=X.backward_comm,
-                                overlap_fraction=overlap, bytes_by_collective=bbc,
-                                collective_calls=int(X.collective_calls), flops=flops)
+        cost = CostReport(X.forward_comm, X.backward_comm, overlap, bbc, int(X.collective_calls), flops)
         if sc.best_total == sc.best_total and cost.total != sc.best_total:  # NaN: no score to check
             raise BackendError(f"explain/score disagree on block {b}: {cost.total!r} != "
                                f"{sc.best_total!r}")
         out.append(RoutedPlan(plan, tuple(routings), tuple(exits), cost))
         e0 += T
     return out
+
+
+_CTORS: dict = {}
+
+
+def _ctor(cls, n_pos: int):
+    """Constructor of dataclass `cls` from its first `n_pos` fields, positionally.
+    The native one (csrc/lower_ext.c make_ctor) skips the generated __init__,
+    which for frozen classes costs one object.__setattr__ per field; it is
+    used only where that __init__ would do nothing else (no __post_init__,
+    every field init=True, the remaining fields with plain defaults)."""
+    key = (cls, n_pos)
+    f = _CTORS.get(key)
+    if f is None:
+        f = cls
+        if _native_lower is not None and dataclasses.is_dataclass(cls) and not hasattr(cls, "__post_init__"):
+            fs = dataclasses.fields(cls)
+            rest = fs[n_pos:]
+            if (len(fs) >= n_pos and all(x.init for x in fs)
+                    and all(x.default is not dataclasses.MISSING for x in rest)):
+                f = _native_lower.make_ctor(cls, tuple(x.name for x in fs[:n_pos]),
+                                            tuple(x.name for x in rest), tuple(x.default for x in rest))
+        _CTORS[key] = f
+    return f
 
 
 def _make_dict(keys: list, vals: list) -> dict:
@@ -434,14 +458,20 @@ class _Search:
             self.tables.close()
             raise
 
-    def fetch(self) -> None:
-        """Wait for the device results (and exchange them across ranks)."""
+    def fetch(self, explain_now: bool = False) -> None:
+        """Wait for the device results (and exchange them across ranks).  With
+        `explain_now`, also re-route the merged winners at once (sharded runs
+        cannot chain that on the device: the winners are known only after the
+        exchange)."""
         if self._fetched is not None:
             return
         try:
             scores, detail = self.ses.backend.score_wait(self.tables)
             if self.exchange is not None:
                 scores = self.exchange(scores)
+            if explain_now and detail is None:
+                idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
+                detail = self.ses.backend.explain_all(self.tables, idx)
         except BaseException:
             self.tables.close()
             raise
@@ -462,6 +492,7 @@ class _Search:
             LAST_PHASES.update(tables_ms=self.tables_ms, score_call_ms=(tc - self.t_launch) * 1e3,
                                routes_ms=(time.perf_counter() - t_routes) * 1e3)
             results = []
+            SubgraphResult = _ctor(types.SubgraphResult, 5)
             for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
                 table = []
                 if want_table:
@@ -471,7 +502,7 @@ class _Search:
                         t = float(totals[i])
                         plan = candidate_by_index(graph, sub, i, types)
                         table.append([i, _labels(plan.assignments), None if math.isnan(t) else t])
-                results.append(types.SubgraphResult(sub, best, int(sc.candidates), int(sc.valid), table))
+                results.append(SubgraphResult(sub, best, int(sc.candidates), int(sc.valid), table))
             return results
         finally:
             tables.close()
@@ -579,8 +610,17 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
         for ids, gcsr in _block_groups(ses.low, csr):
             searches.append((_Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange,
                                      launch=False), ids))
-        for srch, _ in searches:
-            srch.launch()
+        if len(searches) > 1 and not searches[0][0].explain:
+            # sharded: the cheap group's winners are merged across ranks and
+            # re-routed BEFORE the expensive launch -- once that persistent
+            # kernel holds every SM, the re-routing kernel could not start
+            searches[0][0].launch()
+            searches[0][0].fetch(explain_now=True)
+            for srch, _ in searches[1:]:
+                srch.launch()
+        else:
+            for srch, _ in searches:
+                srch.launch()
     except BaseException:
         for srch, _ in searches:
             srch.tables.close()

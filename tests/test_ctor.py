@@ -1,0 +1,106 @@
+"""Native dataclass constructors (csrc/lower_ext.c make_ctor, search._ctor):
+objects equal to the generated __init__'s, for this package's result types and
+the reference's, and the generated __init__ kept wherever it does more."""
+
+from __future__ import annotations
+
+import copy
+import dataclasses
+import os
+import pickle
+import sys
+
+import pytest
+
+from paper_2302_00247_b200 import api_types as A
+from paper_2302_00247_b200 import search
+from paper_2302_00247_b200.lowering import _native_lower
+
+pytestmark = pytest.mark.skipif(_native_lower is None, reason="native extension not built")
+REF = "/root/reference/pkg/src"
+
+
+def _samples(ns):
+    sub = ns.Subgraph("net/a", ("net/a/x", "net/a/y"), (("net/a", ("net/a/x", "net/a/y")),))
+    rep = ns.ShardSpec(ns.ShardKind.REPLICA)
+    ident = ns.Collective(ns.CollectiveKind.IDENTITY)
+    plan = ns.CandidatePlan(sub, (("net/a/x", rep),), 7)
+    nr = ns.NodeRouting("net/a/x", "matmul.col", (), ident, 4096, rep)
+    cost = ns.CostReport(1e-5, 2e-5, 0.5, {"allreduce": 64}, 3, 128)
+    rp = ns.RoutedPlan(plan, (nr,), (), cost)
+    res = ns.SubgraphResult(sub, rp, 9, 4, [])
+    return [(ns.Subgraph, sub, 3), (ns.CandidatePlan, plan, 3), (ns.NodeRouting, nr, 6),
+            (ns.CostReport, cost, 6), (ns.RoutedPlan, rp, 4), (ns.SubgraphResult, res, 5)]
+
+
+def _check(ns):
+    for cls, obj, n in _samples(ns):
+        f = search._ctor(cls, n)
+        assert f is not cls, cls  # native path taken
+        names = [x.name for x in dataclasses.fields(cls)][:n]
+        got = f(*[getattr(obj, k) for k in names])
+        assert type(got) is cls and got == obj and repr(got) == repr(obj)
+        assert vars(got) == vars(obj) and list(vars(got)) == list(vars(obj))
+        assert pickle.loads(pickle.dumps(got)) == obj and copy.deepcopy(got) == obj
+        try:
+            h = hash(obj)
+        except TypeError:  # e.g. a frozen class holding a CostReport
+            h = None
+        if h is not None:
+            assert hash(got) == h
+        if cls.__dataclass_params__.frozen:
+            with pytest.raises(dataclasses.FrozenInstanceError):
+                setattr(got, names[0], None)
+
+
+def test_native_ctor_matches_generated_init():
+    _check(A)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not present")
+def test_native_ctor_on_reference_types():
+    sys.path.insert(0, REF)
+    try:
+        from shardplan import costmodel, patterns, pruning
+        from shardplan import search as rs
+    finally:
+        sys.path.remove(REF)
+
+    class NS:
+        Subgraph = pruning.Subgraph
+        CandidatePlan, NodeRouting, RoutedPlan, SubgraphResult = (rs.CandidatePlan, rs.NodeRouting, rs.RoutedPlan,
+                                                                  rs.SubgraphResult)
+        CostReport = costmodel.CostReport
+        ShardSpec, ShardKind = patterns.ShardSpec, patterns.ShardKind
+        Collective, CollectiveKind = patterns.Collective, patterns.CollectiveKind
+
+    _check(NS)
+
+
+def test_generated_init_kept_where_it_does_more():
+    @dataclasses.dataclass
+    class Post:
+        a: int
+
+        def __post_init__(self):
+            self.b = 2 * self.a
+
+    @dataclasses.dataclass
+    class Factory:
+        a: int
+        b: list = dataclasses.field(default_factory=list)
+
+    @dataclasses.dataclass
+    class NoInit:
+        a: int
+        b: int = dataclasses.field(default=0, init=False)
+
+    assert search._ctor(Post, 1) is Post
+    assert search._ctor(Factory, 1) is Factory  # a fresh list per instance
+    assert search._ctor(Factory, 2) is not Factory
+    assert search._ctor(NoInit, 1) is NoInit
+    f = search._ctor(A.NodeRouting, 6)  # the seventh field takes its default
+    r = f("s", "p", (), A.Collective(A.CollectiveKind.IDENTITY), 1, A.ShardSpec(A.ShardKind.REPLICA))
+    assert r.exit_conversion is None
+    with pytest.raises(TypeError):
+        f("too", "few")

@@ -626,3 +626,79 @@ def test_upload_layouts_permuted_rows_and_wide_dims(backend, seed):
         assert (wsc[b][0], wsc[b][1]) == (exp.candidates, exp.valid)
         if exp.has_best:
             assert (wsc[b][2], wsc[b][3]) == (exp.best_index, exp.best_total)
+
+
+@pytest.mark.parametrize("seed", [3, 11])
+def test_queued_searches_collected_out_of_order(backend, seed):
+    """Two searches queued back to back on one stream (different tables), the
+    later one collected first: each lands in its own pinned block behind its own
+    kernels, so results and winner detail equal the synchronous calls."""
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 2, session=ses)
+    off, nodes = ba.templates_csr()
+    nb = len(off) - 1
+    if nb < 2:
+        pytest.skip("needs two blocks")
+    m = ClusterSpec.from_mesh("2x4")
+    cut = nb // 2
+    parts = [(off[: cut + 1], nodes[: off[cut]]), (off[cut:] - off[cut], nodes[off[cut]:])]
+    tabs = [backend.tables(ses.dgraph, o, nd, m, 1 << 20, 4 << 20) for o, nd in parts]
+    try:
+        if any(t.overflow for t in tabs):
+            pytest.skip("random block beyond u64")
+        sync = [backend.score(t) for t in tabs]
+        sync_detail = [backend.explain_all(t, [int(r.best_index) for r in res]) for t, res in zip(tabs, sync)]
+        for t in tabs:
+            backend.score_launch(t, explain=True)
+        got = [None, None]
+        for k in (1, 0):
+            got[k] = backend.score_wait(tabs[k])
+        for k in (0, 1):
+            scores, detail = got[k]
+            key = [(r.candidates, r.valid, r.best_index, r.best_total, r.best_num_split) for r in scores]
+            assert key == [(r.candidates, r.valid, r.best_index, r.best_total, r.best_num_split) for r in sync[k]]
+            blocks, node, edge, _ = detail
+            eb, en, ee, _ = sync_detail[k]
+            assert [(b.valid, b.total, b.forward_comm, b.backward_comm) for b in blocks] == \
+                [(b.valid, b.total, b.forward_comm, b.backward_comm) for b in eb]
+            assert np.array_equal(node, en) and np.array_equal(edge, ee)
+    finally:
+        for t in tabs:
+            t.close()
+
+
+@pytest.mark.parametrize("seed", range(0, 40, 8))
+def test_round_robin_shards_merge_exactly(backend, seed):
+    """Ranks deal each block's work items round-robin; for any rank count and every
+    scoring mode the exact merge of the shards equals the unsharded search."""
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.dist import merge_scores
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 1 + seed % 2, session=ses)
+    off, nodes = ba.templates_csr()
+    t = backend.tables(ses.dgraph, off, nodes, ClusterSpec.from_mesh("1x8"), 1 << 20, 4 << 20)
+    try:
+        if t.overflow:
+            pytest.skip("random block beyond u64")
+        for mode in ("skip", "walk", "memo"):
+            backend.set_mode(mode)
+            full = backend.score(t)
+            key = [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split) for r in full]
+            for n in (2, 3, 7):
+                merged = merge_scores([backend.score(t, s, n) for s in range(n)])
+                assert [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split)
+                        for r in merged] == key, (mode, n)
+    finally:
+        backend.set_mode("skip")
+        t.close()

@@ -111,6 +111,15 @@ EXPORTED_SYMBOLS = (
 )
 
 
+class RawList(list):
+    """The records of a ctypes array as a list, keeping the array as `.raw`
+    (native consumers read the records without per-element objects)."""
+
+    def __init__(self, arr, n: int):
+        super().__init__(arr[i] for i in range(n))
+        self.raw = arr
+
+
 class _Handle:
     def __init__(self, backend, ptr_, free_fn):
         self.backend = backend
@@ -273,13 +282,13 @@ class Backend:
             blocks, node, edge, eoff = self._detail_buffers(t)
             self._check(self.lib.sp_score_wait(self.ctx, t.ptr, outs, blocks, ptr(node, C.c_int8),
                                                ptr(edge, C.c_int8)), "sp_score_wait")
-            detail = ([blocks[i] for i in range(nb)], node, edge, eoff)
+            detail = (RawList(blocks, nb), node, edge, eoff)
         else:
             self._check(self.lib.sp_score_wait(self.ctx, t.ptr, outs, None, None, None),
                         "sp_score_wait")
             detail = None
         t.pending_explain = False
-        return [outs[i] for i in range(nb)], detail
+        return RawList(outs, nb), detail
 
     def explain_all(self, t: Tables, indices) -> tuple:
         """Winner detail of every block: (blocks, node_detail [ne,4], edge_detail [nedge,2],
@@ -290,7 +299,7 @@ class Backend:
         self._check(self.lib.sp_explain_all(self.ctx, t.ptr, ptr(idx, C.c_uint64), blocks,
                                             ptr(node, C.c_int8), ptr(edge, C.c_int8)),
                     "sp_explain_all")
-        return [blocks[i] for i in range(nb)], node, edge, eoff
+        return RawList(blocks, nb), node, edge, eoff
 
     def timings(self) -> dict:
         f, s, k = C.c_double(), C.c_double(), C.c_double()

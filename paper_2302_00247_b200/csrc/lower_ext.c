@@ -1096,43 +1096,6 @@ done:
 }
 
 
-/*
- * make_dict(keys, values) -> dict(zip(keys, values)) for equal-length lists.
- * The keys are ~10^5 scattered str objects: inserting them one by one is one
- * cache miss per key (hash read, refcount write), so the loop prefetches the
- * key objects a few dozen iterations ahead and presizes the table.
- */
-static PyObject* make_dict(PyObject* self, PyObject* args) {
-  PyObject *keys, *vals;
-  if (!PyArg_ParseTuple(args, "O!O!", &PyList_Type, &keys, &PyList_Type, &vals)) return NULL;
-  const Py_ssize_t n = PyList_GET_SIZE(keys);
-  if (PyList_GET_SIZE(vals) != n) {
-    PyErr_SetString(PyExc_ValueError, "keys and values differ in length");
-    return NULL;
-  }
-  PyObject* d = _PyDict_NewPresized(n);
-  if (!d) return NULL;
-  PyObject** K = n ? &PyList_GET_ITEM(keys, 0) : NULL;
-  PyObject** V = n ? &PyList_GET_ITEM(vals, 0) : NULL;
-  enum { AHEAD = 24 };
-  for (Py_ssize_t i = 0; i < n; i++) {
-    if (i + AHEAD < n) __builtin_prefetch(K[i + AHEAD], 1, 0);
-    PyObject* k = K[i];
-    Py_hash_t h;
-    if (!PyUnicode_CheckExact(k) || (h = ((PyASCIIObject*)k)->hash) == -1) {
-      h = PyObject_Hash(k);
-      if (h == -1) {
-        Py_DECREF(d);
-        return NULL;
-      }
-    }
-    if (_PyDict_SetItem_KnownHash(d, k, V[i], h) < 0) {
-      Py_DECREF(d);
-      return NULL;
-    }
-  }
-  return d;
-}
 
 
 /*
@@ -1236,10 +1199,267 @@ static PyObject* make_ctor(PyObject* self, PyObject* args) {
   return (PyObject*)c;
 }
 
+
+/*
+ * singleton_results(ctors, subs, sel, recs, xblocks, node, toff, op, radix,
+ *                   obytes, flops, pnames, pallred, specs, identity, gather,
+ *                   kind_labels, overlap)
+ * -> [SubgraphResult or None] for the blocks `sel` of a search whose template
+ * is ONE node (c5: ~1000 residual ops).  The same objects routed_plans_all +
+ * collect build in Python (search.py), straight from the raw sp_score_out /
+ * sp_explain_block records: CandidatePlan, NodeRouting, exits, CostReport,
+ * RoutedPlan, SubgraphResult.  None where the block has no winner, its
+ * winner did not route, or the explained total differs from the scored one:
+ * the caller's Python path handles (and raises for) those.
+ *   ctors: (CandidatePlan, NodeRouting, RoutedPlan, CostReport, SubgraphResult)
+ *   recs: raw sp_score_out [nb] (40 B), xblocks: raw sp_explain_block [nb] (104 B)
+ *   node: int8 [ne, 4]; toff: int64 [nb + 1]; op, radix: uint8 [nb];
+ *   obytes, flops: int64 [nb]; pnames / pallred: per op code tuples
+ *   specs: (replica, split(0), ..., split(7)); gather: allgather per axis
+ */
+typedef struct {
+  uint64_t candidates, valid, best_index;
+  double best_total;
+  int32_t best_num_split, has_best;
+} RecView;
+
+typedef struct {
+  int32_t valid, fail_pos;
+  double forward_comm, backward_comm, total;
+  int64_t bytes[4], calls[4], collective_calls;
+} XView;
+
+static PyObject* call_n(PyObject* f, PyObject** a, size_t n) { return PyObject_Vectorcall(f, a, n, NULL); }
+
+static PyObject* singleton_results(PyObject* self, PyObject* args) {
+  PyObject *ctors, *subs, *pnames, *pallred, *specs, *identity, *allreduce, *gather, *kinds;
+  Py_buffer sel, recs, xb, node, toff, op, radix, ob, fl;
+  double overlap;
+  if (!PyArg_ParseTuple(args, "O!O!y*y*y*y*y*y*y*y*y*O!O!O!OOO!O!d", &PyTuple_Type, &ctors, &PyList_Type, &subs, &sel,
+                        &recs, &xb, &node, &toff, &op, &radix, &ob, &fl, &PyTuple_Type, &pnames, &PyTuple_Type,
+                        &pallred, &PyTuple_Type, &specs, &identity, &allreduce, &PyTuple_Type, &gather,
+                        &PyTuple_Type, &kinds, &overlap))
+    return NULL;
+  PyObject* out = NULL;
+  static PyObject* s_template = NULL;
+  if (!s_template) s_template = PyUnicode_InternFromString("template");
+  const int64_t* selp = (const int64_t*)sel.buf;
+  const Py_ssize_t ns = sel.len / 8, nb = PyList_GET_SIZE(subs);
+  const RecView* R = (const RecView*)recs.buf;
+  const XView* X = (const XView*)xb.buf;
+  const int8_t* nd = (const int8_t*)node.buf;
+  const int64_t* to = (const int64_t*)toff.buf;
+  const uint8_t* opc = (const uint8_t*)op.buf;
+  const uint8_t* rdx = (const uint8_t*)radix.buf;
+  const int64_t* obp = (const int64_t*)ob.buf;
+  const int64_t* flp = (const int64_t*)fl.buf;
+  if (PyTuple_GET_SIZE(ctors) != 5 || PyTuple_GET_SIZE(specs) < 9 || PyTuple_GET_SIZE(gather) < 8 ||
+      PyTuple_GET_SIZE(kinds) != 4 || recs.len < nb * (Py_ssize_t)sizeof(RecView) ||
+      xb.len < nb * (Py_ssize_t)sizeof(XView) || toff.len < (nb + 1) * 8 || op.len < nb || radix.len < nb ||
+      ob.len < nb * 8 || fl.len < nb * 8) {
+    PyErr_SetString(PyExc_ValueError, "singleton_results: inconsistent arguments");
+    goto done;
+  }
+  PyObject *mkPlan = PyTuple_GET_ITEM(ctors, 0), *mkNR = PyTuple_GET_ITEM(ctors, 1),
+           *mkRP = PyTuple_GET_ITEM(ctors, 2), *mkCR = PyTuple_GET_ITEM(ctors, 3),
+           *mkRes = PyTuple_GET_ITEM(ctors, 4);
+  PyObject* py_overlap = PyFloat_FromDouble(overlap);
+  PyObject* empty = PyTuple_New(0);
+  if (!py_overlap || !empty) {
+    Py_XDECREF(py_overlap);
+    Py_XDECREF(empty);
+    goto done;
+  }
+  out = PyList_New(ns);
+  if (!out) goto fail0;
+  for (Py_ssize_t q = 0; q < ns; q++) {
+    const int64_t b = selp[q];
+    if (b < 0 || b >= nb || to[b + 1] - to[b] != 1) {
+      PyErr_SetString(PyExc_ValueError, "singleton_results: not a one-node block");
+      goto fail;
+    }
+    const RecView r = R[b];
+    const XView x = X[b];
+    /* CostReport.total = forward + backward * (1 - overlap), rounded in that order */
+    const double total = x.forward_comm + x.backward_comm * (1.0 - overlap);
+    if (!r.has_best || !x.valid || (r.best_total == r.best_total && total != r.best_total)) {
+      Py_INCREF(Py_None);
+      PyList_SET_ITEM(out, q, Py_None);
+      continue;
+    }
+    const int64_t e0 = to[b];
+    const int pidx = nd[4 * e0], sax = nd[4 * e0 + 1], xax = nd[4 * e0 + 2];
+    const int oc = opc[b];
+    if (oc >= PyTuple_GET_SIZE(pnames) || oc >= PyTuple_GET_SIZE(pallred) || pidx < 0 ||
+        pidx >= PyTuple_GET_SIZE(PyTuple_GET_ITEM(pnames, oc)) || sax >= 8 || xax >= 8) {
+      PyErr_SetString(PyExc_ValueError, "singleton_results: detail out of range");
+      goto fail;
+    }
+    PyObject* sub = PyList_GET_ITEM(subs, b);
+    PyObject* tmpl = PyObject_GetAttr(sub, s_template);
+    if (!tmpl) goto fail;
+    PyObject* scope = PySequence_GetItem(tmpl, 0);
+    Py_DECREF(tmpl);
+    if (!scope) goto fail;
+    /* assignments: the one weight slot takes digit index % radix */
+    PyObject* asg;
+    if (rdx[b]) {
+      PyObject* pair = PyTuple_Pack(2, scope, PyTuple_GET_ITEM(specs, (Py_ssize_t)(r.best_index % rdx[b])));
+      asg = pair ? PyTuple_Pack(1, pair) : NULL;
+      Py_XDECREF(pair);
+    } else {
+      asg = empty;
+      Py_INCREF(asg);
+    }
+    PyObject* idx = PyLong_FromUnsignedLongLong(r.best_index);
+    PyObject* plan = NULL;
+    if (asg && idx) {
+      PyObject* a[3] = {sub, asg, idx};
+      plan = call_n(mkPlan, a, 3);
+    }
+    Py_XDECREF(asg);
+    Py_XDECREF(idx);
+    PyObject* obytes = PyLong_FromLongLong(obp[b]);
+    PyObject* nr = NULL;
+    if (plan && obytes) {
+      PyObject* a[6] = {scope, PyTuple_GET_ITEM(PyTuple_GET_ITEM(pnames, oc), pidx), empty,
+                        PyObject_IsTrue(PyTuple_GET_ITEM(PyTuple_GET_ITEM(pallred, oc), pidx)) ? allreduce : identity,
+                        obytes, PyTuple_GET_ITEM(specs, sax < 0 ? 0 : 1 + sax)};
+      nr = call_n(mkNR, a, 6);
+    }
+    PyObject* exits = NULL;
+    if (nr) {
+      if (xax >= 0) {
+        PyObject* ex = PyTuple_Pack(3, scope, PyTuple_GET_ITEM(gather, xax), obytes);
+        exits = ex ? PyTuple_Pack(1, ex) : NULL;
+        Py_XDECREF(ex);
+      } else {
+        exits = empty;
+        Py_INCREF(exits);
+      }
+    }
+    Py_DECREF(scope);
+    Py_XDECREF(obytes);
+    PyObject* bbc = exits ? PyDict_New() : NULL;
+    int ok = bbc != NULL;
+    for (int j = 0; j < 4 && ok; j++)
+      if (x.calls[j]) {
+        PyObject* v = PyLong_FromLongLong(x.bytes[j]);
+        ok = v && PyDict_SetItem(bbc, PyTuple_GET_ITEM(kinds, j), v) == 0;
+        Py_XDECREF(v);
+      }
+    PyObject *fwd = PyFloat_FromDouble(x.forward_comm), *bwd = PyFloat_FromDouble(x.backward_comm),
+             *cc = PyLong_FromLongLong(x.collective_calls), *fp = PyLong_FromLongLong(flp[b]);
+    PyObject* cost = NULL;
+    if (ok && fwd && bwd && cc && fp) {
+      PyObject* a[6] = {fwd, bwd, py_overlap, bbc, cc, fp};
+      cost = call_n(mkCR, a, 6);
+    }
+    Py_XDECREF(fwd);
+    Py_XDECREF(bwd);
+    Py_XDECREF(cc);
+    Py_XDECREF(fp);
+    Py_XDECREF(bbc);
+    PyObject* routings = nr ? PyTuple_Pack(1, nr) : NULL;
+    PyObject* rp = NULL;
+    if (cost && routings) {
+      PyObject* a[4] = {plan, routings, exits, cost};
+      rp = call_n(mkRP, a, 4);
+    }
+    Py_XDECREF(plan);
+    Py_XDECREF(nr);
+    Py_XDECREF(routings);
+    Py_XDECREF(exits);
+    Py_XDECREF(cost);
+    PyObject *cand = PyLong_FromUnsignedLongLong(r.candidates), *val = PyLong_FromUnsignedLongLong(r.valid),
+             *table = PyList_New(0);
+    PyObject* res = NULL;
+    if (rp && cand && val && table) {
+      PyObject* a[5] = {sub, rp, cand, val, table};
+      res = call_n(mkRes, a, 5);
+    }
+    Py_XDECREF(rp);
+    Py_XDECREF(cand);
+    Py_XDECREF(val);
+    Py_XDECREF(table);
+    if (!res) goto fail;
+    PyList_SET_ITEM(out, q, res);
+  }
+  goto fail0;
+fail:
+  Py_CLEAR(out);
+fail0:
+  Py_DECREF(py_overlap);
+  Py_DECREF(empty);
+done:
+  PyBuffer_Release(&sel);
+  PyBuffer_Release(&recs);
+  PyBuffer_Release(&xb);
+  PyBuffer_Release(&node);
+  PyBuffer_Release(&toff);
+  PyBuffer_Release(&op);
+  PyBuffer_Release(&radix);
+  PyBuffer_Release(&ob);
+  PyBuffer_Release(&fl);
+  return out;
+}
+
+
+/*
+ * assignments_dict(names, key_ids, key_slot, slot_labels) -> dict
+ * {names[key_ids[i]]: slot_labels[key_slot[i]]} in i order: derive_plan's
+ * instance-scope -> label map (search.py:374-376) without materialising the
+ * key and value lists; the scattered name objects are prefetched.
+ *   key_ids int32 [K] (node rows), key_slot int32 [K] (index into slot_labels)
+ */
+static PyObject* assignments_dict(PyObject* self, PyObject* args) {
+  PyObject *names, *labels;
+  Py_buffer ids, slot;
+  if (!PyArg_ParseTuple(args, "O!y*y*O!", &PyList_Type, &names, &ids, &slot, &PyList_Type, &labels)) return NULL;
+  PyObject* d = NULL;
+  const int32_t* I = (const int32_t*)ids.buf;
+  const int32_t* Sl = (const int32_t*)slot.buf;
+  const Py_ssize_t K = ids.len / 4, nn = PyList_GET_SIZE(names), nl = PyList_GET_SIZE(labels);
+  if (slot.len / 4 != K) {
+    PyErr_SetString(PyExc_ValueError, "key_ids and key_slot differ in length");
+    goto done;
+  }
+  d = _PyDict_NewPresized(K);
+  if (!d) goto done;
+  enum { AHEAD = 24 };
+  for (Py_ssize_t i = 0; i < K; i++) {
+    if (i + AHEAD < K && I[i + AHEAD] >= 0 && I[i + AHEAD] < nn)
+      __builtin_prefetch(PyList_GET_ITEM(names, I[i + AHEAD]), 1, 0);
+    if (I[i] < 0 || I[i] >= nn || Sl[i] < 0 || Sl[i] >= nl) {
+      PyErr_SetString(PyExc_IndexError, "assignments_dict: index out of range");
+      Py_CLEAR(d);
+      goto done;
+    }
+    PyObject* k = PyList_GET_ITEM(names, I[i]);
+    Py_hash_t h;
+    if (!PyUnicode_CheckExact(k) || (h = ((PyASCIIObject*)k)->hash) == -1) {
+      h = PyObject_Hash(k);
+      if (h == -1) {
+        Py_CLEAR(d);
+        goto done;
+      }
+    }
+    if (_PyDict_SetItem_KnownHash(d, k, PyList_GET_ITEM(labels, Sl[i]), h) < 0) {
+      Py_CLEAR(d);
+      goto done;
+    }
+  }
+done:
+  PyBuffer_Release(&ids);
+  PyBuffer_Release(&slot);
+  return d;
+}
+
 static PyMethodDef methods[] = {
     {"lower_arrays", lower_arrays, METH_VARARGS, "Lower a grouped ModelGraph to flat sp_graph arrays."},
+    {"singleton_results", singleton_results, METH_VARARGS, "SubgraphResults of one-node blocks from raw records."},
+    {"assignments_dict", assignments_dict, METH_VARARGS, "Instance-scope -> label dict from member ids."},
     {"make_ctor", make_ctor, METH_VARARGS, "Fast positional constructor for a dataclass."},
-    {"make_dict", make_dict, METH_VARARGS, "dict(zip(keys, values)) with prefetched key objects."},
     {"block_instances", block_instances, METH_VARARGS, "Subgraph.instances of every block from fold arrays."},
     {NULL, NULL, 0, NULL}};
 

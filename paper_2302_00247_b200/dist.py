@@ -35,8 +35,10 @@ def to_records(scores: list) -> np.ndarray:
 
 
 def from_records(rec: np.ndarray) -> list:
+    from ._native import RawList
+
     arr = (SpScoreOut * max(1, len(rec))).from_buffer_copy(np.ascontiguousarray(rec, REC).tobytes() or bytes(40))
-    return list(arr)[: len(rec)]
+    return RawList(arr, len(rec))
 
 
 def merge_records(parts: np.ndarray) -> np.ndarray:

@@ -208,6 +208,34 @@ def _flops(low: LoweredGraph, tnodes) -> int:
     return total
 
 
+def _block_flops(low: LoweredGraph, csr) -> list:
+    """_flops of every template of `csr` at once (costmodel.py:185-190: 2 x the
+    activation's elements x the weight's first dim, summed over matmuls with a
+    weight); blocks whose sum may exceed int64 fall back to Python integers."""
+    off, tn = csr
+    nb = len(off) - 1
+    if nb == 0:
+        return []
+    tn = np.asarray(tn, np.int64)
+    mm = (low.op[tn] == 0) & (low.w_rank[tn] > 0)
+    r = low.act_rank[tn].astype(np.int64)
+    shp = np.where(np.arange(low.act_shape.shape[1])[None, :] < r[:, None], low.act_shape[tn], 1)
+    fl = np.where(mm, 2.0 * shp.astype(np.float64).prod(axis=1) * low.w_shape[tn, 0].astype(np.float64), 0.0)
+    iv = np.where(mm, 2 * shp.prod(axis=1) * low.w_shape[tn, 0], 0)
+    off = np.asarray(off, np.int64)
+    nonempty = off[1:] > off[:-1]
+    sums = np.zeros(nb, np.int64)
+    fsum = np.zeros(nb, np.float64)
+    if len(tn):
+        idx = off[:-1][nonempty]
+        sums[nonempty] = np.add.reduceat(iv, idx)
+        fsum[nonempty] = np.add.reduceat(fl, idx)
+    out = sums.tolist()
+    for b in np.nonzero(fsum >= 2.0 ** 62)[0].tolist():
+        out[b] = _flops(low, tn[off[b]:off[b + 1]].tolist())
+    return out
+
+
 def _collective(types: TypeSet, kind: int, axis: int):
     ck = types.CollectiveKind(_KIND_LABEL[kind])
     return types.Collective(ck, None if kind == 1 else int(axis))
@@ -289,6 +317,7 @@ def route_prep(ses: Session, subgraphs: list, types: TypeSet = DEFAULT_TYPES, cs
     tn = csr[1]
     t_op, t_w = op[tn].tolist(), w_rank[tn].tolist()
     t_bytes = act_bytes[tn].tolist()
+    b_flops = _block_flops(low, csr)
     out = []
     for b, sub in enumerate(subgraphs):
         template = sub.template
@@ -299,7 +328,7 @@ def route_prep(ses: Session, subgraphs: list, types: TypeSet = DEFAULT_TYPES, cs
             lab = _OP_LABELS[t_op[e0]]
             node = (template[0], lab, pnames[lab], pcolls[lab], t_bytes[e0], [])
             if t_w[e0]:
-                out.append(([0], [3 if t_w[e0] >= 2 else 2], [node], _flops(low, (v,)) if t_op[e0] == 0 else 0))
+                out.append(([0], [3 if t_w[e0] >= 2 else 2], [node], b_flops[b]))
             else:
                 out.append(([], [], [node], 0))
             continue
@@ -314,14 +343,15 @@ def route_prep(ses: Session, subgraphs: list, types: TypeSet = DEFAULT_TYPES, cs
             prods = [(names[r], int(act_bytes[r]))
                      for r in in_idx[in_off[v]:in_off[v + 1]].tolist() if r in members]
             nodes.append((template[i], lab, pnames[lab], pcolls[lab], int(act_bytes[v]), prods))
-        out.append((slot_pos, radices, nodes, _flops(low, tnodes)))
+        out.append((slot_pos, radices, nodes, b_flops[b]))
     return out
 
 
 def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
-                     types: TypeSet = DEFAULT_TYPES, detail=None, prep=None) -> list:
+                     types: TypeSet = DEFAULT_TYPES, detail=None, prep=None, only=None) -> list:
     """RoutedPlan of every block's argmin from ONE sp_explain_all launch (or the
-    detail the search itself returned), on top of route_prep."""
+    detail the search itself returned), on top of route_prep.  With `only`
+    (block positions), just those blocks, in that order."""
     if detail is None:
         idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
         detail = ses.backend.explain_all(tables, idx)
@@ -340,15 +370,18 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
     RoutedPlan, CostReport = _ctor(types.RoutedPlan, 4), _ctor(types.CostReport, 6)
     overlap = mesh.overlap_fraction
     out = []
-    e0 = 0
-    for b, (sub, sc, X, pb) in enumerate(zip(subgraphs, scores, blocks, prep)):
+    starts = [0]
+    for pb in prep:
+        starts.append(starts[-1] + len(pb[2]))
+    for b in (range(len(subgraphs)) if only is None else only):
+        sub, sc, X, pb = subgraphs[b], scores[b], blocks[b], prep[b]
         slot_pos, radices, nodes, flops = pb
         T = len(nodes)
+        e0 = starts[b]
         if not sc.has_best or not X.valid:
             out.append(types.RoutingFailure(sub.template[X.fail_pos],
                                             "no pattern chains from producer states")
                        if sc.has_best and X.fail_pos >= 0 else None)
-            e0 += T
             continue
         template = sub.template
         digits = _digits(int(sc.best_index), radices)
@@ -384,7 +417,6 @@ def routed_plans_all(ses: Session, tables, subgraphs: list, scores: list, mesh,
             raise BackendError(f"explain/score disagree on block {b}: {cost.total!r} != "
                                f"{sc.best_total!r}")
         out.append(RoutedPlan(plan, tuple(routings), tuple(exits), cost))
-        e0 += T
     return out
 
 
@@ -412,11 +444,86 @@ def _ctor(cls, n_pos: int):
     return f
 
 
-def _make_dict(keys: list, vals: list) -> dict:
-    """dict(zip(keys, vals)); the native builder prefetches the scattered key objects."""
-    if _native_lower is not None:
-        return _native_lower.make_dict(keys, vals)
-    return dict(zip(keys, vals))
+def _singleton_results(ses: Session, subgraphs: list, scores, detail, prep, csr, mesh, types: TypeSet) -> list:
+    """SubgraphResult of every one-node block with a routed winner, built in C
+    (csrc/lower_ext.c singleton_results) from the raw score / explain records;
+    None elsewhere (the Python path builds those)."""
+    nb = len(subgraphs)
+    blocks, node = detail[0], detail[1]
+    raw_s, raw_x = getattr(scores, "raw", None), getattr(blocks, "raw", None)
+    if _native_lower is None or raw_s is None or raw_x is None or nb == 0:
+        return [None] * nb
+    sel = np.fromiter((b for b in range(nb) if len(prep[b][2]) == 1), np.int64)
+    if sel.size == 0:
+        return [None] * nb
+    low = ses.low
+    toff = np.ascontiguousarray(csr[0], np.int64)
+    first = csr[1][toff[:-1]] if len(csr[1]) else np.zeros(0, np.int32)
+    op = np.ascontiguousarray(low.op[first], np.uint8)
+    wr = low.w_rank[first]
+    radix = np.where(wr >= 2, 3, np.where(wr == 1, 2, 0)).astype(np.uint8)
+    obytes = np.ascontiguousarray(low.act_bytes[first], np.int64)
+    flops = np.zeros(nb, np.int64)
+    for b in sel.tolist():
+        flops[b] = prep[b][3]
+    pn, pc = types.pattern_names, types.pattern_collectives
+    pnames = tuple(tuple(pn.get(lab, ())) for lab in _OP_LABELS)
+    pallred = tuple(tuple(c == "allreduce" for c in pc.get(lab, ())) for lab in _OP_LABELS)
+    specs = (types.ShardSpec(types.ShardKind.REPLICA),) + tuple(
+        types.ShardSpec(types.ShardKind.SPLIT, a) for a in range(8))
+    gather = tuple(_collective(types, 2, a) for a in range(8))
+    ctors = (_ctor(types.CandidatePlan, 3), _ctor(types.NodeRouting, 6), _ctor(types.RoutedPlan, 4),
+             _ctor(types.CostReport, 6), _ctor(types.SubgraphResult, 5))
+    got = _native_lower.singleton_results(
+        ctors, subgraphs if isinstance(subgraphs, list) else list(subgraphs), sel, raw_s, raw_x,
+        np.ascontiguousarray(node, np.int8), toff, op, radix, obytes, flops, pnames, pallred, specs,
+        types.Collective(types.CollectiveKind.IDENTITY), types.Collective(types.CollectiveKind.ALL_REDUCE_SUM),
+        gather, tuple(_KIND_LABEL[k] for k in (1, 2, 3, 4)), float(mesh.overlap_fraction))
+    out = [None] * nb
+    for b, r in zip(sel.tolist(), got):
+        out[b] = r
+    return out
+
+
+def _label_keys(ba: BlockArrays, subs: list, prep: list):
+    """(member row, slot) of every entry of derive_plan's assignment map, in its
+    order: block by block, instance by instance, the block's weight slots in
+    weight_nodes order (search.py:374-376).  Slots are numbered over all blocks
+    with weights; vectorised over the fold's member matrix."""
+    slot_pos = [pb[0] for pb in prep]
+    wb = [b for b, sp in enumerate(slot_pos) if sp]
+    if not wb:
+        return np.zeros(0, np.int32), np.zeros(0, np.int32)
+    S = np.array([len(slot_pos[b]) for b in wb], np.int64)
+    soff = np.zeros(len(wb) + 1, np.int64)
+    np.cumsum(S, out=soff[1:])
+    q_flat = np.fromiter((q for b in wb for q in slot_pos[b]), np.int64, count=int(soff[-1]))
+    wb = np.asarray(wb, np.int64)
+    T = np.asarray(ba.block_T, np.int64)[wb]
+    mo = np.asarray(ba.block_member_off, np.int64)[wb]
+    R = np.diff(np.asarray(ba.block_inst_off, np.int64))[wb]
+    # (block, instance) pairs, then each pair's slots
+    pb_ = np.repeat(np.arange(len(wb)), R)
+    pstart = np.zeros(len(wb), np.int64)
+    np.cumsum(R[:-1], out=pstart[1:])
+    pr = np.arange(len(pb_)) - np.repeat(pstart, R)
+    base = mo[pb_] + pr * T[pb_]
+    Sp = S[pb_]
+    kstart = np.zeros(len(pb_), np.int64)
+    np.cumsum(Sp[:-1], out=kstart[1:])
+    within = np.arange(int(Sp.sum())) - np.repeat(kstart, Sp)
+    slot = np.repeat(soff[:-1][pb_], Sp) + within
+    rows = np.asarray(ba.members, np.int64)[np.repeat(base, Sp) + q_flat[slot]]
+    return rows.astype(np.int32), slot.astype(np.int32)
+
+
+def _assignments(names: list, label_keys, slot_labels: list) -> dict:
+    """{names[row]: slot_labels[slot]} over label_keys = (rows, slots), in order."""
+    rows, slots = label_keys
+    if _native_lower is not None and isinstance(names, list):
+        return _native_lower.assignments_dict(names, np.ascontiguousarray(rows, np.int32),
+                                              np.ascontiguousarray(slots, np.int32), slot_labels)
+    return dict(zip(map(names.__getitem__, rows.tolist()), map(slot_labels.__getitem__, slots.tolist())))
 
 
 def _labels(assignments) -> dict:
@@ -438,6 +545,7 @@ class _Search:
         self.bad_mu = mu > chunk_size
         ta = time.perf_counter()
         off, nodes = csr
+        self.csr = csr
         self.tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu,
                                          chunk_size if not self.bad_mu else mu)
         ses.last_table_bytes = self.tables.nbytes
@@ -488,12 +596,28 @@ class _Search:
                     raise AssertionError("all-replica fallback must always route")
                 if self.bad_mu:
                     raise BadConfig(f"fusion threshold {self.mu} exceeds chunk size {self.chunk_size}")
-            bests = routed_plans_all(ses, tables, subgraphs, scores, self.mesh, types, detail, prep)
+            if prep is None:
+                prep = route_prep(ses, subgraphs, types, self.csr)
+            if detail is None:
+                idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
+                detail = ses.backend.explain_all(tables, idx)
+            # one-node blocks (c5: ~1000 residual ops) straight from the raw
+            # records in C; the rest (and any block the C path declines) here
+            fast = [None] * len(subgraphs) if want_table else \
+                _singleton_results(ses, subgraphs, scores, detail, prep, self.csr, self.mesh, types)
+            rest = [b for b, r in enumerate(fast) if r is None]
+            bests = [None] * len(subgraphs)
+            for b, best in zip(rest, routed_plans_all(ses, tables, subgraphs, scores, self.mesh, types, detail,
+                                                      prep, only=rest)):
+                bests[b] = best
             LAST_PHASES.update(tables_ms=self.tables_ms, score_call_ms=(tc - self.t_launch) * 1e3,
                                routes_ms=(time.perf_counter() - t_routes) * 1e3)
             results = []
             SubgraphResult = _ctor(types.SubgraphResult, 5)
             for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
+                if fast[b] is not None:
+                    results.append(fast[b])
+                    continue
                 table = []
                 if want_table:
                     C = int(sc.candidates)
@@ -630,19 +754,10 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     # scopes that receive each block's weight labels (search.py:374-376)
     t3 = time.perf_counter()
     subs = subgraphs_from_blocks(ses.low, ba, types)
+    t3a = time.perf_counter()
     prep = route_prep(ses, subs, types, csr)
-    names = ses.low.names
-    members = ba.members
-    label_rows = []
-    for b, (sub, pb) in enumerate(zip(subs, prep)):
-        slot_pos = pb[0]
-        if not slot_pos:
-            label_rows.append(None)
-            continue
-        T = int(ba.block_T[b])
-        mo, R = int(ba.block_member_off[b]), sub.multiplicity
-        mat = members[mo: mo + R * T].reshape(R, T)[:, slot_pos]
-        label_rows.append((list(map(names.__getitem__, mat.ravel().tolist())), R))
+    t3b = time.perf_counter()
+    label_keys = _label_keys(ba, subs, prep)
     t4 = time.perf_counter()
     if len(searches) == 1:
         results = searches[0][0].collect(graph, subs, want_table, types, prep)
@@ -656,21 +771,19 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     total_cost = 0.0
     candidates = 0
     valid = 0
-    keys, vals = [], []
-    for sub, res, lr in zip(subs, results, label_rows):
+    slot_labels = []
+    for sub, res, pb in zip(subs, results, prep):
         candidates += res.candidates
         valid += res.valid
         total_cost += res.best.cost.total * sub.multiplicity
-        # every instance takes the template's labels in weight_nodes order
-        # (search.py:374-376); instance members come from the fold's member matrix
-        if lr is None:
-            continue
-        flat, R = lr
-        keys.extend(flat)
-        vals.extend([spec.label for _, spec in res.best.plan.assignments] * R)
-    assignments = _make_dict(keys, vals)
+        if pb[0]:
+            slot_labels.extend([spec.label for _, spec in res.best.plan.assignments])
+    # every instance takes the template's labels in weight_nodes order
+    # (search.py:374-376); instance members come from the fold's member matrix
+    assignments = _assignments(ses.low.names, label_keys, slot_labels)
     LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
                        launch_ms=(t3 - t2) * 1e3, overlap_host_ms=(t4 - t3) * 1e3,
+                       subgraphs_ms=(t3a - t3) * 1e3, route_prep_ms=(t3b - t3a) * 1e3,
                        collect_ms=(t5 - t4) * 1e3, assemble_ms=(time.perf_counter() - t5) * 1e3)
     return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates,
                                 valid)

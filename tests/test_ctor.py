@@ -104,3 +104,71 @@ def test_generated_init_kept_where_it_does_more():
     assert r.exit_conversion is None
     with pytest.raises(TypeError):
         f("too", "few")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_block_flops_vectorised_equals_reference_loop(seed):
+    """search._block_flops (numpy over every template node) == _flops per block
+    (costmodel.py:185-190), including blocks with huge shapes (Python ints)."""
+    import dataclasses as dc
+
+    import numpy as np
+
+    from paper_2302_00247_b200.lowering import lower
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
+    if seed % 2:  # a matmul whose flops pass 2**63
+        mm = np.nonzero((low.op == 0) & (low.w_rank > 0))[0]
+        if len(mm):
+            shp = low.act_shape.copy()
+            shp[mm[0], 0] = 1 << 40
+            low = dc.replace(low, act_shape=shp)
+    rng = np.random.default_rng(seed)
+    n = low.n_nodes
+    cuts = np.sort(rng.choice(np.arange(1, n), size=min(20, n - 1), replace=False))
+    off = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    tn = rng.permutation(n).astype(np.int32)
+    assert search._block_flops(low, (off, tn)) == [search._flops(low, tn[off[b]:off[b + 1]].tolist())
+                                                    for b in range(len(off) - 1)]
+
+
+@pytest.mark.parametrize("seed", range(0, 12, 2))
+def test_assignment_map_vectorised_equals_block_loop(seed):
+    """_label_keys + the native dict builder give the assignment map the
+    per-block loop over the fold's member matrix gives (search.py:374-376):
+    same keys, same order, same labels."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays
+    from paper_2302_00247_b200.lowering import lower
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
+    ba = BlockArrays.from_dict(oracle.prune(low, 1 + seed % 3))
+    subs = search.subgraphs_from_blocks(low, ba)
+
+    class Ses:
+        pass
+
+    ses = Ses()
+    ses.low = low
+    prep = search.route_prep(ses, subs, A.DEFAULT_TYPES if hasattr(A, "DEFAULT_TYPES") else search.DEFAULT_TYPES,
+                             ba.templates_csr())
+    labels, exp = [], {}
+    for b, (sub, pb) in enumerate(zip(subs, prep)):
+        if not pb[0]:
+            continue
+        mine = [f"L{b}.{q}" for q in range(len(pb[0]))]
+        labels.extend(mine)
+        T, mo, R = int(ba.block_T[b]), int(ba.block_member_off[b]), sub.multiplicity
+        mat = ba.members[mo: mo + R * T].reshape(R, T)[:, pb[0]]
+        for k, v in zip([low.names[i] for i in mat.ravel().tolist()], mine * R):
+            exp[k] = v
+    got = search._assignments(low.names, search._label_keys(ba, subs, prep), labels)
+    assert list(got.items()) == list(exp.items())
+    rows, slots = search._label_keys(ba, subs, prep)
+    py = dict(zip(map(low.names.__getitem__, rows.tolist()), map(labels.__getitem__, slots.tolist())))
+    assert list(py.items()) == list(exp.items())
+    assert np.all(slots >= 0)

@@ -555,6 +555,7 @@ typedef struct Par {
   Py_ssize_t* nl;
   uint64_t* nh;
   int32_t* tab; /* open-addressing row map: row + 1, 0 = empty */
+  int32_t* ptab; /* the same rows keyed by the name object's address */
   size_t mask;
   PyObject** node;
   PyObject** inseq;
@@ -583,7 +584,8 @@ typedef struct Par {
   int64_t *abytes, *wbytes;
   Py_ssize_t bytes_part[PAR_MAX_THREADS], edges_part[PAR_MAX_THREADS];
   int max_ar[PAR_MAX_THREADS], max_wr[PAR_MAX_THREADS];
-  pthread_barrier_t bar;
+  double ph[8];  /* thread 0's clock at each phase boundary (SP_LOWER_TRACE) */
+  int bar_count, bar_gen;  /* spin barrier: the phases last ~0.1-1 ms, a futex wake-up ~0.1 ms */
 } Par;
 
 typedef struct {
@@ -600,6 +602,49 @@ static inline int32_t par_find(const Par* P, const char* p, Py_ssize_t n, uint64
     if (!v) return -1;
     const int32_t j = v - 1;
     if (P->nh[j] == h && P->nl[j] == n && memcmp(P->np[j], p, (size_t)n) == 0) return j;
+  }
+}
+
+static inline size_t ptr_slot(const void* o) {
+  uint64_t h = (uint64_t)(uintptr_t)o * 0x9E3779B97F4A7C15ull;
+  return (size_t)(h ^ (h >> 29));
+}
+
+/* row of a name object by address: the names of GraphNode.inputs and the
+   dict keys are usually the very objects of topo_order, and this lookup does
+   not touch them; -1 when absent (then compare by content) */
+static inline int32_t par_find_ptr(const Par* P, PyObject* o) {
+  for (size_t s = ptr_slot(o) & P->mask;; s = (s + 1) & P->mask) {
+    const int32_t v = __atomic_load_n(&P->ptab[s], __ATOMIC_ACQUIRE);
+    if (!v) return -1;
+    if (P->names[v - 1] == o) return v - 1;
+  }
+}
+
+static inline int32_t par_row_of(const Par* P, PyObject* o) {
+  const int32_t r = par_find_ptr(P, o);
+  if (r >= 0) return r;
+  const char* p;
+  Py_ssize_t L;
+  if (!ascii_view(o, &p, &L)) return -2;
+  return par_find(P, p, L, name_hash(p, L));
+}
+
+static void par_barrier(Par* P) {
+  const int gen = __atomic_load_n(&P->bar_gen, __ATOMIC_ACQUIRE);
+  if (__atomic_add_fetch(&P->bar_count, 1, __ATOMIC_ACQ_REL) == P->nthreads) {
+    __atomic_store_n(&P->bar_count, 0, __ATOMIC_RELAXED);
+    __atomic_store_n(&P->bar_gen, gen + 1, __ATOMIC_RELEASE);
+    return;
+  }
+  for (unsigned spins = 0; __atomic_load_n(&P->bar_gen, __ATOMIC_ACQUIRE) == gen; spins++) {
+    if (spins < 4096) {
+#if defined(__x86_64__) || defined(__i386__)
+      __builtin_ia32_pause();
+#endif
+    } else {
+      sched_yield();  /* oversubscribed host: let the other threads run */
+    }
   }
 }
 
@@ -648,6 +693,7 @@ static int par_map_codes(Par* P) {
 }
 
 static void par_phases(Par* P, int t) {
+  if (t == 0) P->ph[0] = now_ms();
   const int T = P->nthreads;
   const Py_ssize_t n = P->n, lo = n * t / T, hi = n * (t + 1) / T;
   const Py_ssize_t dlo = P->nd * t / T, dhi = P->nd * (t + 1) / T;
@@ -676,9 +722,16 @@ static void par_phases(Par* P, int t) {
         break;
       }
     }
+    for (size_t s = ptr_slot(P->names[i]) & P->mask;; s = (s + 1) & P->mask) {
+      int32_t expect = 0;
+      if (__atomic_compare_exchange_n(&P->ptab[s], &expect, (int32_t)(i + 1), 0, __ATOMIC_ACQ_REL,
+                                      __ATOMIC_ACQUIRE))
+        break;
+    }
   }
   P->bytes_part[t] = bytes;
-  pthread_barrier_wait(&P->bar);
+  if (t == 0) P->ph[1] = now_ms();
+  par_barrier(P);
   if (t == 0 && !par_failed(P)) {  /* the name-byte buffer (this thread holds the GIL) */
     Py_ssize_t nb = 0;
     for (int u = 0; u < T; u++) nb += P->bytes_part[u];
@@ -692,18 +745,17 @@ static void par_phases(Par* P, int t) {
   }
   /* phase 2: dict entries -> rows */
   for (Py_ssize_t j = dlo; j < dhi && !par_failed(P); j++) {
-    const char* p;
-    Py_ssize_t L;
-    if (!ascii_view(P->dkey[j], &p, &L)) {
+    const int32_t r = par_row_of(P, P->dkey[j]);
+    if (r == -2) {
       par_fail(P);
       break;
     }
-    const int32_t r = par_find(P, p, L, name_hash(p, L));
     if (r >= 0) P->node[r] = P->dval[j];
   }
   Py_ssize_t base = 0;
   for (int u = 0; u < t; u++) base += P->bytes_part[u];
-  pthread_barrier_wait(&P->bar);
+  if (t == 0) P->ph[2] = now_ms();
+  par_barrier(P);
   /* phase 3: node fields, tensor specs, shapes, name bytes, input counts */
   Py_ssize_t edges = 0;
   int mar = 0, mwr = 0;
@@ -760,14 +812,16 @@ static void par_phases(Par* P, int t) {
   P->edges_part[t] = edges;
   P->max_ar[t] = mar;
   P->max_wr[t] = mwr;
-  pthread_barrier_wait(&P->bar);
+  if (t == 0) P->ph[3] = now_ms();
+  par_barrier(P);
   if (t == 0 && !par_failed(P)) {
     Py_ssize_t E = 0;
     for (int u = 0; u < T; u++) E += P->edges_part[u];
     P->inidx = (int32_t*)malloc((size_t)(E ? E : 1) * sizeof(int32_t));
     if (!P->inidx || !par_map_codes(P)) par_fail(P);
   }
-  pthread_barrier_wait(&P->bar);
+  if (t == 0) P->ph[4] = now_ms();
+  par_barrier(P);
   if (par_failed(P)) return;
   /* phase 4: producer rows in GraphNode.inputs order */
   Py_ssize_t e = 0;
@@ -779,10 +833,7 @@ static void par_phases(Par* P, int t) {
     PyObject* in = P->inseq[i];
     const Py_ssize_t k = PyTuple_GET_SIZE(in);
     for (Py_ssize_t j = 0; j < k; j++) {
-      const char* p;
-      Py_ssize_t L;
-      int32_t r = -1;
-      if (ascii_view(PyTuple_GET_ITEM(in, j), &p, &L)) r = par_find(P, p, L, name_hash(p, L));
+      const int32_t r = par_row_of(P, PyTuple_GET_ITEM(in, j));
       if (r < 0) {
         par_fail(P);
         return;
@@ -793,12 +844,78 @@ static void par_phases(Par* P, int t) {
   }
 }
 
-static void* par_worker(void* arg) {
-  Par* P = ((ParArg*)arg)->P;
-  int go;
-  while (!(go = __atomic_load_n(&P->go, __ATOMIC_ACQUIRE))) sched_yield();
-  if (go > 0 && ((ParArg*)arg)->t < P->nthreads) par_phases(P, ((ParArg*)arg)->t);
+/* Persistent workers (created on first use, kept for the process): a call
+   hands them its Par through a generation counter instead of creating
+   threads (~20 us each).  Idle workers sleep on a condition variable. */
+static struct {
+  pthread_mutex_t mu;
+  pthread_cond_t cv;
+  int size;          /* workers started (thread ids 1..size) */
+  unsigned gen;      /* bumped per job */
+  Par* job;
+  int done;          /* workers finished with the current job */
+} g_pool = {PTHREAD_MUTEX_INITIALIZER, PTHREAD_COND_INITIALIZER, 0, 0, NULL, 0};
+
+static void* pool_worker(void* arg) {
+  /* arg = worker id | the job generation at creation << 8: a worker started
+     for a call must take part in that call even if it reaches the lock late */
+  const int t = (int)((uintptr_t)arg & 0xff);
+  unsigned seen = (unsigned)((uintptr_t)arg >> 8);
+  pthread_mutex_lock(&g_pool.mu);
+  for (;;) {
+    while (g_pool.gen == seen) pthread_cond_wait(&g_pool.cv, &g_pool.mu);
+    seen = g_pool.gen;
+    Par* P = g_pool.job;
+    pthread_mutex_unlock(&g_pool.mu);
+    if (P && t < P->nthreads) par_phases(P, t);
+    __atomic_add_fetch(&g_pool.done, 1, __ATOMIC_ACQ_REL);
+    pthread_mutex_lock(&g_pool.mu);
+  }
   return NULL;
+}
+
+static void pool_after_fork(void) {  /* the child has none of the parent's threads */
+  pthread_mutex_init(&g_pool.mu, NULL);
+  pthread_cond_init(&g_pool.cv, NULL);
+  g_pool.size = 0;
+  g_pool.job = NULL;
+}
+
+/* grow the pool to `want` workers (best effort); returns the worker count */
+static int pool_ensure(int want) {
+  static int atfork = 0;
+  if (!atfork) {
+    pthread_atfork(NULL, NULL, pool_after_fork);
+    atfork = 1;
+  }
+  while (g_pool.size < want) {
+    pthread_t th;
+    pthread_attr_t at;
+    pthread_attr_init(&at);
+    pthread_attr_setdetachstate(&at, PTHREAD_CREATE_DETACHED);
+    const uintptr_t arg = (uintptr_t)(g_pool.size + 1) | ((uintptr_t)g_pool.gen << 8);
+    const int rc = pthread_create(&th, &at, pool_worker, (void*)arg);
+    pthread_attr_destroy(&at);
+    if (rc) break;
+    g_pool.size++;
+  }
+  return g_pool.size;
+}
+
+/* run par_phases on this thread (t = 0) and workers 1..nthreads-1; every
+   started worker takes part in the handshake (idle ones return at once) */
+static void pool_run(Par* P) {
+  const int workers = g_pool.size;
+  __atomic_store_n(&g_pool.done, 0, __ATOMIC_RELAXED);
+  pthread_mutex_lock(&g_pool.mu);
+  g_pool.job = P;
+  g_pool.gen++;
+  pthread_cond_broadcast(&g_pool.cv);
+  pthread_mutex_unlock(&g_pool.mu);
+  par_phases(P, 0);
+  for (unsigned spins = 0; __atomic_load_n(&g_pool.done, __ATOMIC_ACQUIRE) < workers; spins++)
+    if (spins > 4096) sched_yield();
+  g_pool.job = NULL;
 }
 
 /* NULL with no exception set: outside the envelope (use the serial walker) */
@@ -831,9 +948,6 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   PyObject *result = NULL, *names = NULL;
   PyObject *b_names = NULL, *b_noff = NULL, *b_op = NULL, *b_arank = NULL, *b_ashape = NULL, *b_abytes = NULL,
            *b_wrank = NULL, *b_wshape = NULL, *b_wbytes = NULL, *b_wtrain = NULL, *b_inoff = NULL, *b_inidx = NULL;
-  pthread_t th[PAR_MAX_THREADS];
-  ParArg pa[PAR_MAX_THREADS];
-  int created = 1;
   P->n = n;
   P->t_node = Py_TYPE(n0);
   P->o_op = slot_offset(P->t_node, s_op);
@@ -879,6 +993,7 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   while (cap < (size_t)n * 2) cap <<= 1;
   P->mask = cap - 1;
   P->tab = (int32_t*)calloc(cap, sizeof(int32_t));
+  P->ptab = (int32_t*)calloc(cap, sizeof(int32_t));
   P->np = (const char**)malloc((size_t)n * sizeof(char*));
   P->nl = (Py_ssize_t*)malloc((size_t)n * sizeof(Py_ssize_t));
   P->nh = (uint64_t*)malloc((size_t)n * 8);
@@ -889,7 +1004,7 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   P->opv = (PyObject**)malloc((size_t)n * sizeof(PyObject*));
   P->adt = (PyObject**)malloc((size_t)n * sizeof(PyObject*));
   P->wdt = (PyObject**)malloc((size_t)n * sizeof(PyObject*));
-  if (!P->tab || !P->np || !P->nl || !P->nh || !P->node || !P->inseq || !P->ael || !P->wel || !P->opv || !P->adt ||
+  if (!P->tab || !P->ptab || !P->np || !P->nl || !P->nh || !P->node || !P->inseq || !P->ael || !P->wel || !P->opv || !P->adt ||
       !P->wdt)
     goto out;
   b_noff = new_bytearray((n + 1) * 8);
@@ -919,29 +1034,16 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
   P->inoff = (int64_t*)PyByteArray_AS_STRING(b_inoff);
   P->noff[0] = 0;
   P->inoff[0] = 0;
-  /* workers spin on `go` until the participant count is final; the GIL
-     stays with this thread throughout */
-  for (int t = 1; t < T; t++) {
-    pa[t].P = P;
-    pa[t].t = t;
-    if (pthread_create(&th[t], NULL, par_worker, &pa[t])) break;
-    created = t + 1;
-  }
+  /* the GIL stays with this thread throughout */
+  const int created = 1 + (pool_ensure(T - 1) < T - 1 ? g_pool.size : T - 1);
   P->nthreads = created;
-  if (created < 2 || pthread_barrier_init(&P->bar, NULL, (unsigned)created)) {
-    __atomic_store_n(&P->go, -1, __ATOMIC_RELEASE);
-    for (int t = 1; t < created; t++) pthread_join(th[t], NULL);
-    goto out;
-  }
+  if (created < 2) goto out;
   tp[4] = now_ms();
   {
     /* no collection while the workers read the object graph (thread 0
        allocates between phases) */
     const int gc_was = PyGC_Disable();
-    __atomic_store_n(&P->go, 1, __ATOMIC_RELEASE);
-    par_phases(P, 0);
-    for (int t = 1; t < created; t++) pthread_join(th[t], NULL);
-    pthread_barrier_destroy(&P->bar);
+    pool_run(P);
     if (gc_was) PyGC_Enable();
   }
   tp[5] = now_ms();
@@ -961,8 +1063,11 @@ static PyObject* lower_parallel(PyObject* topo, PyObject* nodes, PyObject* op_fn
                            b_ashape, b_abytes, b_wrank, b_wshape, b_wbytes, b_wtrain, b_inoff, b_inidx);
     if (!result) goto err;
     if (getenv("SP_LOWER_TRACE"))
-      fprintf(stderr, "[lower-par] setup %.2f dict %.2f alloc %.2f threads %.2f post %.2f ms (%d threads)\n",
-              tp[1] - tp[0], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], now_ms() - tp[5], created);
+      fprintf(stderr,
+              "[lower-par] setup %.2f dict %.2f alloc %.2f threads %.2f (p1 %.2f p2 %.2f p3 %.2f p3b %.2f p4 %.2f) "
+              "post %.2f ms (%d threads)\n",
+              tp[1] - tp[0], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], P->ph[1] - P->ph[0], P->ph[2] - P->ph[1],
+              P->ph[3] - P->ph[2], P->ph[4] - P->ph[3], tp[5] - P->ph[4], now_ms() - tp[5], created);
     goto out;
   err:
     /* a Python mapping call failed: let the serial walker raise it */
@@ -985,6 +1090,7 @@ out:
   free(P->dkey);
   free(P->dval);
   free(P->tab);
+  free(P->ptab);
   free(P->np);
   free(P->nl);
   free(P->nh);

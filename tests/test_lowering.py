@@ -84,14 +84,16 @@ def test_native_equals_numpy_on_reference_types():
     _same(trim_and_group(gen_transformer_stack(3, d_model=64, heads=4)))
 
 
-def _chain(n=6000, bad=None):
+def _chain(n=6000, bad=None, copies=False):
     """n-node chain of matmuls (above the parallel walker's size threshold),
-    with one node perturbed to fall outside the walker's envelope."""
+    with one node perturbed to fall outside the walker's envelope.  `copies`:
+    inputs and dict keys are equal but distinct str objects (as a JSON-loaded
+    graph has), so every lookup goes by content, not by object."""
     nodes = {}
     prev = None
     for i in range(n):
         nm = f"net/l{i}/MatMul" if i else "net/in"
-        ins = (prev,) if prev else ()
+        ins = ("".join(list(prev)),) if prev and copies else (prev,) if prev else ()
         w = TensorSpec((8, 8), "f32", bool(i % 2)) if i else None
         nodes[nm] = GraphNode(nm, OpKind.MATMUL if i else OpKind.INPUT, ins, TensorSpec((4, 8)), w)
         prev = nm
@@ -115,6 +117,8 @@ def _chain(n=6000, bad=None):
     elif bad == "rank9":
         k = names[17]
         nodes[k] = GraphNode(k, OpKind.MATMUL, nodes[k].inputs, TensorSpec(tuple([2] * 9)), None)
+    if copies:
+        nodes = {"".join(list(k)): v for k, v in nodes.items()}
     g = GroupedGraph.__new__(GroupedGraph)
     g.nodes, g.topo_order = nodes, names
     return g
@@ -126,6 +130,7 @@ def test_parallel_walker_equals_numpy(monkeypatch, threads):
     low = _same(motif_dag(1, "parity"))
     assert low.ascii
     _same(_chain())
+    _same(_chain(copies=True))
 
 
 def test_parallel_walker_equals_serial(monkeypatch):

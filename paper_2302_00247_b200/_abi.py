@@ -173,13 +173,21 @@ def make_sp_mesh(mesh) -> SpMesh:
     return m
 
 
-def blocks_to_numpy(view: SpBlocks) -> dict:
+def blocks_to_numpy(view: SpBlocks, owner=None) -> dict:
+    """numpy arrays of an sp_fold view: copies, or (with `owner`, the object
+    that frees the fold) read-only views that keep `owner` alive."""
     nb, ni, nm = view.n_blocks, view.n_instances, view.n_members
 
     def arr(p, n, dt):
         if n == 0:
             return np.zeros(0, dt)
-        return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
+        if owner is None:
+            return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
+        buf = (p._type_ * n).from_address(C.addressof(p.contents))
+        buf.owner = owner
+        a = np.frombuffer(buf, dt)
+        a.flags.writeable = False
+        return a
 
     return {
         "block_T": arr(view.block_T, nb, np.int64),

@@ -1257,27 +1257,45 @@ static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, co
                                  cudaStream_t s, sp_fold* out) {
   const uint8_t* names = dg->h_names.data();
   const int64_t* noff = dg->h_name_off.data();
+  // every level's class arrays to ONE pinned block (10^7-node folds move
+  // ~50 MB here: pageable copies and zero-filled vectors cost 30+ ms)
   struct Host {
-    std::vector<int32_t> T, R, start, inode, ilen, members;
+    const int32_t *T, *R, *start, *inode, *ilen, *members;
+    int64_t K = 0;
     std::vector<int64_t> moff;
   };
   std::vector<Host> h(lv.size());
-  for (size_t l = 0; l < lv.size(); l++) {
-    LevelBlocks& L = lv[l];
-    Host& H = h[l];
-    if (!L.K) continue;
-    H.T.resize(L.K);
-    H.R.resize(L.K);
-    H.start.resize(L.K);
-    H.inode.resize(L.Ga);
-    H.ilen.resize(L.Ga);
-    H.members.resize(L.M);
-    L.cls_T.download(H.T.data(), L.K, s);
-    L.cls_R.download(H.R.data(), L.K, s);
-    L.cls_start.download(H.start.data(), L.K, s);
-    L.inode.download(H.inode.data(), L.Ga, s);
-    L.ilen.download(H.ilen.data(), L.Ga, s);
-    L.members.download(H.members.data(), L.M, s);
+  size_t total = 0;
+  for (const LevelBlocks& L : lv) total += (size_t)(3 * L.K + 2 * L.Ga + L.M) * 4;
+  size_t got = 0;
+  uint8_t* pin = total ? sp::pinned_acquire(dg->ctx, total, &got) : nullptr;
+  struct Release {
+    sp_ctx* ctx;
+    uint8_t* p;
+    size_t n;
+    ~Release() { sp::pinned_release(ctx, p, n); }
+  } rel{dg->ctx, pin, got};
+  {
+    int32_t* q = (int32_t*)pin;
+    auto get = [&](const DevBuf<int32_t>& d, int64_t cnt) {
+      int32_t* at = q;
+      if (cnt) SP_CUDA(cudaMemcpyAsync(at, d.p, (size_t)cnt * 4, cudaMemcpyDeviceToHost, s));
+      g_d2h_bytes += cnt * 4;
+      q += cnt;
+      return (const int32_t*)at;
+    };
+    for (size_t l = 0; l < lv.size(); l++) {
+      LevelBlocks& L = lv[l];
+      Host& H = h[l];
+      H.K = L.K;
+      if (!L.K) continue;
+      H.T = get(L.cls_T, L.K);
+      H.R = get(L.cls_R, L.K);
+      H.start = get(L.cls_start, L.K);
+      H.inode = get(L.inode, L.Ga);
+      H.ilen = get(L.ilen, L.Ga);
+      H.members = get(L.members, L.M);
+    }
   }
   SP_CUDA(cudaStreamSynchronize(s));
   struct Ref {
@@ -1288,8 +1306,8 @@ static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, co
   std::vector<Ref> blocks;
   for (size_t l = 0; l < lv.size(); l++) {
     Host& H = h[l];
-    H.moff.assign(H.T.size() + 1, 0);
-    for (size_t k = 0; k < H.T.size(); k++) {
+    H.moff.assign(H.K + 1, 0);
+    for (int64_t k = 0; k < H.K; k++) {
       H.moff[k + 1] = H.moff[k] + (int64_t)H.R[k] * H.T[k];
       const int32_t p0 = H.start[k];
       blocks.push_back({H.inode[p0], H.ilen[p0], (int32_t)l, (int32_t)k});
@@ -1312,27 +1330,47 @@ static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, co
     out->block_member_off[b + 1] = out->block_member_off[b] + R * T;
   }
   if (out->block_member_off[nb] != dg->n) throw Error(SP_ERR_CUDA, "fold did not cover every node exactly once");
-  out->inst_prefix_node.resize(out->block_inst_off[nb]);
-  out->inst_prefix_len.resize(out->block_inst_off[nb]);
+  const int64_t ni = out->block_inst_off[nb];
+  out->inst_prefix_node.resize(ni);
+  out->inst_prefix_len.resize(ni);
   out->members.resize(dg->n);
-  for (int64_t b = 0; b < nb; b++) {
-    const Ref& r = blocks[b];
-    const int64_t io = out->block_inst_off[b], mo = out->block_member_off[b];
-    if (r.level < 0) {
-      out->inst_prefix_node[io] = r.pnode;
-      out->inst_prefix_len[io] = r.plen;
-      out->members[mo] = r.k;
-      continue;
+  // members: one contiguous segment per class; instances widened to int64.
+  // Both split over host threads by element ranges of the output.
+  host_parallel(ni, 1 << 16, [&](int64_t lo, int64_t hi, int) {
+    int64_t b = std::upper_bound(out->block_inst_off.begin(), out->block_inst_off.end(), lo) -
+                out->block_inst_off.begin() - 1;
+    for (int64_t j = lo; j < hi; b++) {
+      const Ref& r = blocks[b];
+      const int64_t io = out->block_inst_off[b], e = std::min(hi, out->block_inst_off[b + 1]);
+      if (r.level < 0) {
+        out->inst_prefix_node[j] = r.pnode;
+        out->inst_prefix_len[j] = r.plen;
+      } else {
+        const Host& H = h[r.level];
+        const int64_t p0 = H.start[r.k];
+        for (int64_t i = j; i < e; i++) {
+          out->inst_prefix_node[i] = H.inode[p0 + (i - io)];
+          out->inst_prefix_len[i] = H.ilen[p0 + (i - io)];
+        }
+      }
+      j = e;
     }
-    const Host& H = h[r.level];
-    const int64_t R = H.R[r.k], p0 = H.start[r.k];
-    for (int64_t i = 0; i < R; i++) {
-      out->inst_prefix_node[io + i] = H.inode[p0 + i];
-      out->inst_prefix_len[io + i] = H.ilen[p0 + i];
+  });
+  host_parallel(dg->n, 1 << 18, [&](int64_t lo, int64_t hi, int) {
+    int64_t b = std::upper_bound(out->block_member_off.begin(), out->block_member_off.end(), lo) -
+                out->block_member_off.begin() - 1;
+    for (int64_t j = lo; j < hi; b++) {
+      const Ref& r = blocks[b];
+      const int64_t mo = out->block_member_off[b], e = std::min(hi, out->block_member_off[b + 1]);
+      if (r.level < 0) {
+        out->members[j] = r.k;
+      } else {
+        const Host& H = h[r.level];
+        std::memcpy(out->members.data() + j, H.members + H.moff[r.k] + (j - mo), sizeof(int32_t) * (size_t)(e - j));
+      }
+      j = e;
     }
-    std::memcpy(out->members.data() + mo, H.members.data() + H.moff[r.k],
-                sizeof(int32_t) * (size_t)(H.moff[r.k + 1] - H.moff[r.k]));
-  }
+  });
   sp_blocks& v = out->view;
   v.n_blocks = nb;
   v.n_instances = (int64_t)out->inst_prefix_node.size();

@@ -2183,23 +2183,6 @@ struct PendingScore {
   }
 };
 
-// pinned block of at least `need` bytes from the context's pool
-static uint8_t* pinned_acquire(sp_ctx* ctx, size_t need, size_t* got) {
-  auto& pool = ctx->pinned_pool;
-  for (size_t i = 0; i < pool.size(); i++)
-    if (pool[i].second >= need) {
-      uint8_t* p = (uint8_t*)pool[i].first;
-      *got = pool[i].second;
-      pool.erase(pool.begin() + (std::ptrdiff_t)i);
-      return p;
-    }
-  const size_t n = std::max<size_t>(need, 64 << 10);
-  void* p = nullptr;
-  SP_CUDA(cudaHostAlloc(&p, n, cudaHostAllocDefault));
-  *got = n;
-  return (uint8_t*)p;
-}
-
 struct TablesPriv {
   TableDev dev;
   sp_mesh mesh;

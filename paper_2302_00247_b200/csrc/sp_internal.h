@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -92,6 +93,7 @@ struct sp_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // explain_all of a group while another search runs on `stream`
   cudaEvent_t ev[8] = {};
+
   std::string last_error;
   double fold_ms = 0, score_ms = 0, score_kernel_ms = 0;
   // device-only part of the last fold (events around the level loop) and its level count
@@ -109,6 +111,31 @@ struct sp_ctx {
   // free pinned host blocks for score results (D2H enqueued at launch time)
   std::vector<std::pair<void*, size_t>> pinned_pool;
 };
+
+namespace sp {
+// Pinned host block of at least `need` bytes from the context's pool (best
+// fit; allocated when none fits).  Blocks go back with pinned_release.
+inline uint8_t* pinned_acquire(sp_ctx* ctx, size_t need, size_t* got) {
+  auto& pool = ctx->pinned_pool;
+  size_t best = pool.size();
+  for (size_t i = 0; i < pool.size(); i++)
+    if (pool[i].second >= need && (best == pool.size() || pool[i].second < pool[best].second)) best = i;
+  if (best < pool.size()) {
+    uint8_t* p = (uint8_t*)pool[best].first;
+    *got = pool[best].second;
+    pool.erase(pool.begin() + (std::ptrdiff_t)best);
+    return p;
+  }
+  const size_t n = need > ((size_t)64 << 10) ? need : ((size_t)64 << 10);
+  void* p = nullptr;
+  SP_CUDA(cudaHostAlloc(&p, n, cudaHostAllocDefault));
+  *got = n;
+  return (uint8_t*)p;
+}
+inline void pinned_release(sp_ctx* ctx, void* p, size_t n) {
+  if (p) ctx->pinned_pool.push_back({p, n});
+}
+}  // namespace sp
 
 // Device-resident lowered graph (+ the host copies the library needs).
 struct sp_dgraph {
@@ -130,9 +157,35 @@ struct sp_dgraph {
   View<int32_t> in_idx;
 };
 
+namespace sp {
+// std::vector element allocator that leaves new elements uninitialised
+// (resize of a 10^7-entry output must not memset what is overwritten next)
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new ((void*)p) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new ((void*)p) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using PodVec = std::vector<T, NoInitAlloc<T>>;
+}  // namespace sp
+
 struct sp_fold {
-  std::vector<int64_t> block_T, block_inst_off, block_member_off, inst_prefix_node, inst_prefix_len;
-  std::vector<int32_t> members;
+  std::vector<int64_t> block_T, block_inst_off, block_member_off;
+  sp::PodVec<int64_t> inst_prefix_node, inst_prefix_len;
+  sp::PodVec<int32_t> members;
   sp_blocks view{};
 };
 

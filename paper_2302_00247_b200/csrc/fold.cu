@@ -710,15 +710,11 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
   host_parallel(n, 8192, [&](int64_t lo, int64_t hi, int) {
     int32_t md = 1;
     int mr = 1;
-    bool br = false, be = false, wd = false, pm = false;
+    bool br = false, be = false, pm = false;
     for (int64_t i = lo; i < hi; i++) {
       br |= g->act_rank[i] < 1 || g->act_rank[i] > SP_MAX_RANK || g->w_rank[i] > SP_MAX_RANK;
       mr = std::max(mr, (int)std::max(g->act_rank[i], g->w_rank[i]));
       pm |= g->topo_rank[i] != i;
-      for (int k = 0; k < SP_MAX_RANK; k++) {
-        const uint64_t a = (uint64_t)g->act_shape[i * SP_MAX_RANK + k], w = (uint64_t)g->w_shape[i * SP_MAX_RANK + k];
-        wd |= (a | w) > (uint64_t)INT32_MAX;
-      }
       const uint8_t* a = g->name_bytes + g->name_off[i];
       const int64_t L = g->name_off[i + 1] - g->name_off[i];
       int32_t d = 1;
@@ -729,7 +725,6 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
     for (int64_t e = elo; e < ehi; e++) be |= g->in_idx[e] < 0 || g->in_idx[e] >= n;
     if (br) bad_rank = 1;
     if (be) bad_edge = 1;
-    if (wd) wide = 1;
     if (pm) permuted = 1;
     int cr = max_rank.load();
     while (mr > cr && !max_rank.compare_exchange_weak(cr, mr)) {
@@ -751,114 +746,129 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
   // H2D bytes: shapes travel as int32 [n x R] (R = the graph's largest rank)
   // when every dim fits, an identity topo_rank not at all; k_expand_graph
   // rebuilds the int64 [n x SP_MAX_RANK] layouts on the device
-  const bool pack = !wide;
-  const bool iota = !permuted;
-  const int R = max_rank;
-  const size_t shape_bytes = pack ? (size_t)n * R * 4 : (size_t)n * SP_MAX_RANK * 8;
-  Part parts[13] = {
-      {g->name_bytes, (size_t)nb, 0},
-      {g->name_off, (size_t)(n + 1) * 8, 0},
-      {g->topo_rank, iota ? 0 : (size_t)n * 8, 0},
-      {g->op, (size_t)n, 0},
-      {g->act_rank, (size_t)n, 0},
-      {g->w_rank, (size_t)n, 0},
-      {g->w_trainable, (size_t)n, 0},
-      {pack ? nullptr : g->act_shape, shape_bytes, 0},
-      {pack ? nullptr : g->w_shape, shape_bytes, 0},
-      {g->act_bytes, (size_t)n * 8, 0},
-      {g->w_bytes, (size_t)n * 8, 0},
-      {g->in_off, (size_t)(n + 1) * 8, 0},
-      {g->in_idx, (size_t)E * 4, 0},
-  };
-  size_t total = 0;
-  for (Part& p : parts) {
-    p.off = total;
-    total += (p.bytes + 255) & ~(size_t)255;
-  }
-  if (ctx->staging_bytes < total) {
-    if (ctx->staging) cudaFreeHost(ctx->staging);
-    ctx->staging = nullptr;
-    SP_CUDA(cudaHostAlloc(&ctx->staging, total, cudaHostAllocDefault));
-    ctx->staging_bytes = total;
-  }
-  // host copies the library itself needs (string order, slot order, op validity)
-  dg->h_names.resize((size_t)nb);
-  dg->h_name_off.resize((size_t)n + 1);
-  dg->h_topo.resize((size_t)n);
-  dg->h_op.resize((size_t)n);
-  dg->h_w_rank.resize((size_t)n);
-  const double tu_alloc = ms_since(tu0);
-  // the previous upload may still be reading the staging buffer
-  SP_CUDA(cudaStreamSynchronize(s));
-  const double tu_sync = ms_since(tu0);
-  uint8_t* st = (uint8_t*)ctx->staging;
-  struct Copy {
-    void* dst;
-    const void* src;
-    size_t bytes;
-  };
-  std::vector<Copy> copies;
-  for (const Part& p : parts)
-    if (p.bytes && p.src) copies.push_back({st + p.off, p.src, p.bytes});
-  copies.push_back({dg->h_names.data(), g->name_bytes, (size_t)nb});
-  copies.push_back({dg->h_name_off.data(), g->name_off, (size_t)(n + 1) * 8});
-  copies.push_back({dg->h_topo.data(), g->topo_rank, (size_t)n * 8});
-  copies.push_back({dg->h_op.data(), g->op, (size_t)n});
-  copies.push_back({dg->h_w_rank.data(), g->w_rank, (size_t)n});
-  std::vector<size_t> cstart(copies.size() + 1, 0);
-  for (size_t k = 0; k < copies.size(); k++) cstart[k + 1] = cstart[k] + copies[k].bytes;
-  // byte range [lo, hi) of the concatenated copies per thread
-  host_parallel((int64_t)cstart.back(), 1 << 20, [&](int64_t lo, int64_t hi, int) {
-    size_t k = std::upper_bound(cstart.begin(), cstart.end(), (size_t)lo) - cstart.begin() - 1;
-    for (size_t pos = (size_t)lo; pos < (size_t)hi && k < copies.size(); k++) {
-      const size_t a = pos - cstart[k], b = std::min(copies[k].bytes, (size_t)hi - cstart[k]);
-      if (b > a) std::memcpy((uint8_t*)copies[k].dst + a, (const uint8_t*)copies[k].src + a, b - a);
-      pos = cstart[k + 1];
+  // shapes are packed optimistically: the pack pass itself detects a dim
+  // past int32 (one read of the shapes instead of two) and the copy is then
+  // redone with the int64 layout
+  for (bool pack = true;; pack = false) {
+    const bool iota = !permuted;
+    const int R = max_rank;
+    const size_t shape_bytes = pack ? (size_t)n * R * 4 : (size_t)n * SP_MAX_RANK * 8;
+    Part parts[13] = {
+        {g->name_bytes, (size_t)nb, 0},
+        {g->name_off, (size_t)(n + 1) * 8, 0},
+        {g->topo_rank, iota ? 0 : (size_t)n * 8, 0},
+        {g->op, (size_t)n, 0},
+        {g->act_rank, (size_t)n, 0},
+        {g->w_rank, (size_t)n, 0},
+        {g->w_trainable, (size_t)n, 0},
+        {pack ? nullptr : g->act_shape, shape_bytes, 0},
+        {pack ? nullptr : g->w_shape, shape_bytes, 0},
+        {g->act_bytes, (size_t)n * 8, 0},
+        {g->w_bytes, (size_t)n * 8, 0},
+        {g->in_off, (size_t)(n + 1) * 8, 0},
+        {g->in_idx, (size_t)E * 4, 0},
+    };
+    size_t total = 0;
+    for (Part& p : parts) {
+      p.off = total;
+      total += (p.bytes + 255) & ~(size_t)255;
     }
-  });
-  if (pack)
-    host_parallel(n, 16384, [&](int64_t lo, int64_t hi, int) {
-      int32_t* a32 = (int32_t*)(st + parts[7].off);
-      int32_t* w32 = (int32_t*)(st + parts[8].off);
-      for (int64_t i = lo; i < hi; i++)
-        for (int k = 0; k < R; k++) {
-          a32[i * R + k] = (int32_t)g->act_shape[i * SP_MAX_RANK + k];
-          w32[i * R + k] = (int32_t)g->w_shape[i * SP_MAX_RANK + k];
-        }
+    if (ctx->staging_bytes < total) {
+      if (ctx->staging) cudaFreeHost(ctx->staging);
+      ctx->staging = nullptr;
+      SP_CUDA(cudaHostAlloc(&ctx->staging, total, cudaHostAllocDefault));
+      ctx->staging_bytes = total;
+    }
+    // host copies the library itself needs (string order, slot order, op validity)
+    dg->h_names.resize((size_t)nb);
+    dg->h_name_off.resize((size_t)n + 1);
+    dg->h_topo.resize((size_t)n);
+    dg->h_op.resize((size_t)n);
+    dg->h_w_rank.resize((size_t)n);
+    const double tu_alloc = ms_since(tu0);
+    // the previous upload may still be reading the staging buffer
+    SP_CUDA(cudaStreamSynchronize(s));
+    const double tu_sync = ms_since(tu0);
+    uint8_t* st = (uint8_t*)ctx->staging;
+    struct Copy {
+      void* dst;
+      const void* src;
+      size_t bytes;
+    };
+    std::vector<Copy> copies;
+    for (const Part& p : parts)
+      if (p.bytes && p.src) copies.push_back({st + p.off, p.src, p.bytes});
+    copies.push_back({dg->h_names.data(), g->name_bytes, (size_t)nb});
+    copies.push_back({dg->h_name_off.data(), g->name_off, (size_t)(n + 1) * 8});
+    copies.push_back({dg->h_topo.data(), g->topo_rank, (size_t)n * 8});
+    copies.push_back({dg->h_op.data(), g->op, (size_t)n});
+    copies.push_back({dg->h_w_rank.data(), g->w_rank, (size_t)n});
+    std::vector<size_t> cstart(copies.size() + 1, 0);
+    for (size_t k = 0; k < copies.size(); k++) cstart[k + 1] = cstart[k] + copies[k].bytes;
+    // byte range [lo, hi) of the concatenated copies per thread
+    host_parallel((int64_t)cstart.back(), 1 << 20, [&](int64_t lo, int64_t hi, int) {
+      size_t k = std::upper_bound(cstart.begin(), cstart.end(), (size_t)lo) - cstart.begin() - 1;
+      for (size_t pos = (size_t)lo; pos < (size_t)hi && k < copies.size(); k++) {
+        const size_t a = pos - cstart[k], b = std::min(copies[k].bytes, (size_t)hi - cstart[k]);
+        if (b > a) std::memcpy((uint8_t*)copies[k].dst + a, (const uint8_t*)copies[k].src + a, b - a);
+        pos = cstart[k + 1];
+      }
     });
-  const double tu_copy = ms_since(tu0);
-  // device arena: the staged bytes, then the expanded arrays
-  const size_t exp_shape = pack ? (size_t)n * SP_MAX_RANK * 8 : 0, exp_topo = iota ? (size_t)n * 8 : 0;
-  const size_t off_a = total, off_w = off_a + ((exp_shape + 255) & ~(size_t)255),
-               off_t = off_w + ((exp_shape + 255) & ~(size_t)255);
-  dg->arena.alloc(off_t + exp_topo, s);
-  g_h2d_bytes += (int64_t)total;
-  SP_CUDA(cudaMemcpyAsync(dg->arena.p, st, total, cudaMemcpyHostToDevice, s));
-  uint8_t* dbase = dg->arena.p;
-  if (pack || iota) {
-    SP_LAUNCH(ctx, k_expand_graph, 2 * 148, 256, 0, s, n, R,
-              pack ? (const int32_t*)(dbase + parts[7].off) : nullptr,
-              pack ? (const int32_t*)(dbase + parts[8].off) : nullptr, pack ? (int64_t*)(dbase + off_a) : nullptr,
-              pack ? (int64_t*)(dbase + off_w) : nullptr, iota ? (int64_t*)(dbase + off_t) : nullptr);
-    SP_CUDA(cudaGetLastError());
+    if (pack) {
+      host_parallel(n, 16384, [&](int64_t lo, int64_t hi, int) {
+        int32_t* a32 = (int32_t*)(st + parts[7].off);
+        int32_t* w32 = (int32_t*)(st + parts[8].off);
+        uint64_t big = 0;
+        for (int64_t i = lo; i < hi; i++)
+          for (int k = 0; k < R; k++) {
+            const uint64_t a = (uint64_t)g->act_shape[i * SP_MAX_RANK + k], w = (uint64_t)g->w_shape[i * SP_MAX_RANK + k];
+            big |= (a | w) & ~(uint64_t)INT32_MAX;
+            a32[i * R + k] = (int32_t)a;
+            w32[i * R + k] = (int32_t)w;
+          }
+        // unused dims (k >= R) must be 0 by the sp_graph contract
+        for (int64_t i = lo; i < hi && !big; i++)
+          for (int k = R; k < SP_MAX_RANK; k++)
+            big |= (uint64_t)(g->act_shape[i * SP_MAX_RANK + k] | g->w_shape[i * SP_MAX_RANK + k]);
+        if (big) wide = 1;
+      });
+      if (wide) continue;  // a dim past int32 (or a non-zero unused dim): full layout
+    }
+    const double tu_copy = ms_since(tu0);
+    // device arena: the staged bytes, then the expanded arrays
+    const size_t exp_shape = pack ? (size_t)n * SP_MAX_RANK * 8 : 0, exp_topo = iota ? (size_t)n * 8 : 0;
+    const size_t off_a = total, off_w = off_a + ((exp_shape + 255) & ~(size_t)255),
+                 off_t = off_w + ((exp_shape + 255) & ~(size_t)255);
+    dg->arena.alloc(off_t + exp_topo, s);
+    g_h2d_bytes += (int64_t)total;
+    SP_CUDA(cudaMemcpyAsync(dg->arena.p, st, total, cudaMemcpyHostToDevice, s));
+    uint8_t* dbase = dg->arena.p;
+    if (pack || iota) {
+      SP_LAUNCH(ctx, k_expand_graph, 2 * 148, 256, 0, s, n, R,
+                pack ? (const int32_t*)(dbase + parts[7].off) : nullptr,
+                pack ? (const int32_t*)(dbase + parts[8].off) : nullptr, pack ? (int64_t*)(dbase + off_a) : nullptr,
+                pack ? (int64_t*)(dbase + off_w) : nullptr, iota ? (int64_t*)(dbase + off_t) : nullptr);
+      SP_CUDA(cudaGetLastError());
+    }
+    if (trace)
+      std::fprintf(stderr, "[upload] check %.3f alloc %.3f sync %.3f copy %.3f issue %.3f ms (%zu B)\n", tu_check,
+                   tu_alloc, tu_sync, tu_copy, ms_since(tu0), total);
+    uint8_t* base = dg->arena.p;
+    dg->names.p = base + parts[0].off;
+    dg->name_off.p = (int64_t*)(base + parts[1].off);
+    dg->topo.p = (int64_t*)(base + (iota ? off_t : parts[2].off));
+    dg->op.p = base + parts[3].off;
+    dg->act_rank.p = base + parts[4].off;
+    dg->w_rank.p = base + parts[5].off;
+    dg->w_train.p = base + parts[6].off;
+    dg->act_shape.p = (int64_t*)(base + (pack ? off_a : parts[7].off));
+    dg->w_shape.p = (int64_t*)(base + (pack ? off_w : parts[8].off));
+    dg->act_bytes.p = (int64_t*)(base + parts[9].off);
+    dg->w_bytes.p = (int64_t*)(base + parts[10].off);
+    dg->in_off.p = (int64_t*)(base + parts[11].off);
+    dg->in_idx.p = (int32_t*)(base + parts[12].off);
+    return;
   }
-  if (trace)
-    std::fprintf(stderr, "[upload] check %.3f alloc %.3f sync %.3f copy %.3f issue %.3f ms (%zu B)\n", tu_check,
-                 tu_alloc, tu_sync, tu_copy, ms_since(tu0), total);
-  uint8_t* base = dg->arena.p;
-  dg->names.p = base + parts[0].off;
-  dg->name_off.p = (int64_t*)(base + parts[1].off);
-  dg->topo.p = (int64_t*)(base + (iota ? off_t : parts[2].off));
-  dg->op.p = base + parts[3].off;
-  dg->act_rank.p = base + parts[4].off;
-  dg->w_rank.p = base + parts[5].off;
-  dg->w_train.p = base + parts[6].off;
-  dg->act_shape.p = (int64_t*)(base + (pack ? off_a : parts[7].off));
-  dg->w_shape.p = (int64_t*)(base + (pack ? off_w : parts[8].off));
-  dg->act_bytes.p = (int64_t*)(base + parts[9].off);
-  dg->w_bytes.p = (int64_t*)(base + parts[10].off);
-  dg->in_off.p = (int64_t*)(base + parts[11].off);
-  dg->in_idx.p = (int32_t*)(base + parts[12].off);
 }
 
 __global__ void k_iota(int32_t* __restrict__ out, int64_t n) {

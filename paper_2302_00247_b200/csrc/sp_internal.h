@@ -86,6 +86,31 @@ struct DevBuf {
 
 }  // namespace sp
 
+namespace sp {
+// std::vector element allocator that leaves new elements uninitialised
+// (resize of a 10^7-entry output must not memset what is overwritten next)
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new ((void*)p) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new ((void*)p) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using PodVec = std::vector<T, NoInitAlloc<T>>;
+}  // namespace sp
+
 struct sp_ctx {
   int device = 0;
   int sm_count = 148;
@@ -143,9 +168,9 @@ struct sp_dgraph {
   int64_t n = 0, E = 0;
   int32_t max_depth = 1;
   // host copies the library needs (string order, slot order, op validity)
-  std::vector<uint8_t> h_names;
-  std::vector<int64_t> h_name_off, h_topo;
-  std::vector<uint8_t> h_op, h_w_rank;
+  sp::PodVec<uint8_t> h_names;  // filled by graph_upload's parallel copies (no zero fill)
+  sp::PodVec<int64_t> h_name_off, h_topo;
+  sp::PodVec<uint8_t> h_op, h_w_rank;
   // device copies: views into one arena filled by a single H2D copy
   sp::DevBuf<uint8_t> arena;
   template <class T>
@@ -157,30 +182,6 @@ struct sp_dgraph {
   View<int32_t> in_idx;
 };
 
-namespace sp {
-// std::vector element allocator that leaves new elements uninitialised
-// (resize of a 10^7-entry output must not memset what is overwritten next)
-template <class T>
-struct NoInitAlloc : std::allocator<T> {
-  template <class U>
-  struct rebind {
-    using other = NoInitAlloc<U>;
-  };
-  NoInitAlloc() = default;
-  template <class U>
-  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
-  template <class U>
-  void construct(U* p) noexcept {
-    ::new ((void*)p) U;
-  }
-  template <class U, class... A>
-  void construct(U* p, A&&... a) {
-    ::new ((void*)p) U(std::forward<A>(a)...);
-  }
-};
-template <class T>
-using PodVec = std::vector<T, NoInitAlloc<T>>;
-}  // namespace sp
 
 struct sp_fold {
   std::vector<int64_t> block_T, block_inst_off, block_member_off;

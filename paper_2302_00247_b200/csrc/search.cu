@@ -493,7 +493,7 @@ struct ItemOut {
   unsigned long long total_bits;  // ~0 when the item has no valid candidate
   unsigned long long index;
   uint32_t num_split;
-  uint32_t valid;
+  unsigned long long valid;  // 64-bit: k_score_flow writes one CTA's whole share of a block
 };
 
 __device__ __forceinline__ bool key_less(unsigned long long ta, uint32_t na, unsigned long long ia,
@@ -1317,6 +1317,155 @@ constexpr int SKIP_MAX_CHUNKS = ITEM_ITERS_MAX_SKIP * THREADS / SKIP_CHUNK;
 #ifndef SP_PAIR_MIN_BLOCKS
 #define SP_PAIR_MIN_BLOCKS 4
 #endif
+// Stage block `off`'s tables into shared memory for k_score_fast / k_score_flow
+// (all threads of the CTA): the blob, the lanes' digit offsets, the biased
+// digit constants and the digit words of every multiple of `chs` candidates
+// up to `maxch` of them; then make the FastNode offsets absolute.  Contains
+// the CTA barriers it needs; returns after the last one.
+__device__ __forceinline__ void stage_block(uint8_t* smem, const uint8_t* blobs, int64_t off, uint64_t* lane_add,
+                                            Biased* bz, uint64_t* cenc, uint32_t chs, int maxch, bool pair) {
+  const int tid = threadIdx.x;
+  stage_blob(smem, blobs, off);
+  const BlobHeader* gH = (const BlobHeader*)(blobs + off);
+  const int V = gH->V;
+  const uint64_t r3 = gH->radix3;
+  if (tid < 32) {
+    uint64_t a = 0;  // unbiased digits of `tid` in the fastest positions
+    uint32_t x = (uint32_t)tid;
+    for (int q = V - 1; q >= 0 && x; q--) {
+      const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+      a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
+      x /= r;
+    }
+    lane_add[tid] = a;
+  } else if (tid == 32) {
+    Biased z{0, 0, 0, 0};
+    uint32_t x = 32;
+    for (int q = V - 1; q >= 0; q--) {
+      const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+      const int sh = 2 * (V - 1 - q);
+      z.B |= (uint64_t)(4 - r) << sh;
+      z.NZ |= (uint64_t)(r == 3 ? 2 : 1) << sh;
+      z.add32 |= (uint64_t)(x % r) << sh;
+      x /= r;
+    }
+    uint32_t x64 = 64;
+    for (int q = V - 1; q >= 0 && x64; q--) {
+      const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+      z.add64 |= (uint64_t)(x64 % r) << (2 * (V - 1 - q));
+      x64 /= r;
+    }
+    *bz = z;
+  }
+  for (int c = tid - 64; c >= 0 && c < maxch; c += THREADS - 64) {
+    uint64_t a = 0;  // unbiased digits of c * chs
+    uint64_t x = (uint64_t)c * chs;
+    for (int q = V - 1; q >= 0 && x; q--) {
+      const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+      a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
+      x /= r;
+    }
+    cenc[c] = a;
+  }
+  __syncthreads();
+  patch_fast(smem, pair);
+  __syncthreads();
+}
+
+// Per-lane running argmin of a block's valid candidates: (total bits,
+// num_split, digits) + valid count; the digits become the reference index
+// once, when the result is written (they only break exact ties).
+struct LaneBest {
+  unsigned long long t = ~0ULL;
+  uint32_t n = 0xFFFFFFFFu, valid = 0;
+  uint64_t w = 0;
+};
+
+// One warp chunk of k_score_fast: `rem` candidates from the lane's digit word
+// `w` (lane l holds candidate start + l; with PAIR also start + 32 + l);
+// `whi` = the chunk's end in the block's enumeration index space (SKIP).
+template <bool SKIP, bool PAIR>
+__device__ __forceinline__ void score_chunk(const Tabs& S, const Biased& bz, const uint64_t* lane_add, uint32_t rec0,
+                                            uint32_t rb, uint32_t sb, int lane, uint64_t w, uint32_t rem,
+                                            unsigned long long whi, LaneBest& lb) {
+  const BlobHeader& H = *S.H;
+  const int T = H.T;
+  auto take = [&](uint64_t wv, double fwd) {
+    const double bwd = backward_b(S, wv);
+    const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
+    const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
+    const uint32_t ns = (uint32_t)__popcll(wv & bz.NZ);
+    lb.valid++;
+    if (tb < lb.t || (tb == lb.t && (ns < lb.n || (ns == lb.n && ref_index_b(S, wv) < ref_index_b(S, lb.w))))) {
+      lb.t = tb;
+      lb.n = ns;
+      lb.w = wv;
+    }
+  };
+  if (PAIR) {
+    while (true) {
+      const uint64_t wb = badd(w, bz.add32, bz.B);
+      double fa, fb;
+      const int v = walk_pair(rec0, T, w, wb, (uint32_t)lane < rem, (uint32_t)lane + 32 < rem, fa, fb, rb, sb);
+      if (v & 1) take(w, fa);
+      if (v & 2) take(wb, fb);
+      if (rem <= 64) break;
+      rem -= 64;
+      w = badd(w, bz.add64, bz.B);
+    }
+    return;
+  }
+  // single candidate per lane; with SKIP, lanes prove R-aligned runs invalid
+  // and the warp jumps to the furthest proven end (clamped to the chunk)
+  unsigned long long base = whi - rem;
+  while (true) {
+    const bool active = (uint32_t)lane < rem;
+    double fwd;
+    const int fail = walk_fast<SKIP>(rec0, T, w, active, fwd, rb, sb);
+    uint32_t adv = 32;  // SKIP: candidates this lane proves done, from base
+    if (fail < 0) {
+      take(w, fwd);
+      if (SKIP) adv = lane + 1;
+    } else if (SKIP) {
+      adv = lane + 1;
+      if (active) {
+        const NodeSkip sk = S.skip[fail];
+        const unsigned long long x = base + lane;
+        const unsigned long long t = sk.R ? (x / sk.R + 1) * sk.R : whi;
+        adv = (uint32_t)(min(t, whi) - base);
+      }
+    }
+    if (!SKIP) {
+      if (rem <= 32) break;
+      rem -= 32;
+      w = badd(w, bz.add32, bz.B);
+    } else {
+      // the union of the lanes' proven runs is contiguous from base
+      uint32_t m = adv;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (m >= rem) break;
+      if (m == 32) {
+        w = badd(w, bz.add32, bz.B);
+      } else {
+        // the lane that proved the longest run provides the next base digits
+        const int src = __ffs(__ballot_sync(0xffffffffu, adv == m)) - 1;
+        uint64_t n0 = w;
+        if (lane == src) {
+          const bool jump = fail >= 0 && active && S.skip[fail].R;
+          // positions faster than m back to digit 0, then +1 at position m
+          const int sh = jump ? 2 * (H.V - 1 - S.skip[fail].m) : 0;
+          const uint64_t low = (1ULL << sh) - 1;
+          n0 = badd((n0 & ~low) | (bz.B & low), 1ULL << sh, bz.B);
+        }
+        w = badd(shfl_u64(n0, src), lane_add[lane], bz.B);
+      }
+      rem -= m;
+      base += m;
+    }
+  }
+}
+
 template <bool SKIP, bool PAIR>
 __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_MIN_BLOCKS) k_score_fast(const uint8_t* __restrict__ blobs,
                                                                            ScorePlan P, ItemOut* __restrict__ items,
@@ -1331,9 +1480,12 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
   // warps pull CH-candidate chunks of the item from a shared cursor (no
   // static per-warp spans: no barrier idling when walks or skips are skewed)
   constexpr uint32_t CH = SKIP ? SKIP_CHUNK : PAIR_CHUNK;
-  constexpr int MAXCH = SKIP ? SKIP_MAX_CHUNKS : PAIR_MAX_CHUNKS;
+  // with skipping, a chunk's cost varies most: the last quarter of an item is
+  // dealt in quarter-size chunks so the warps reach the item barrier together
+  constexpr uint32_t CHS = SKIP ? SKIP_CHUNK / 4 : PAIR_CHUNK;
+  constexpr int MAXCH = SKIP ? SKIP_MAX_CHUNKS * 4 : PAIR_MAX_CHUNKS;
   __shared__ uint64_t s_wbase;              // biased digits of the item start
-  __shared__ uint64_t s_cenc[MAXCH];        // unbiased digits of c * CH
+  __shared__ uint64_t s_cenc[MAXCH];        // unbiased digits of j * CHS
   __shared__ uint32_t s_chunk;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1355,50 +1507,7 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
     __syncthreads();
     const int64_t b = s_block;
     if (b != staged) {
-      stage_blob(smem, blobs, P.blob_off[b]);
-      const BlobHeader* gH = (const BlobHeader*)(blobs + P.blob_off[b]);
-      const int V = gH->V;
-      const uint64_t r3 = gH->radix3;
-      if (tid < 32) {
-        uint64_t a = 0;  // unbiased digits of `tid` in the fastest positions
-        uint32_t x = (uint32_t)tid;
-        for (int q = V - 1; q >= 0 && x; q--) {
-          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
-          a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
-          x /= r;
-        }
-        s_lane_add[tid] = a;
-      } else if (tid == 32) {
-        Biased z{0, 0, 0, 0};
-        uint32_t x = 32;
-        for (int q = V - 1; q >= 0; q--) {
-          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
-          const int sh = 2 * (V - 1 - q);
-          z.B |= (uint64_t)(4 - r) << sh;
-          z.NZ |= (uint64_t)(r == 3 ? 2 : 1) << sh;
-          z.add32 |= (uint64_t)(x % r) << sh;
-          x /= r;
-        }
-        uint32_t x64 = 64;
-        for (int q = V - 1; q >= 0 && x64; q--) {
-          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
-          z.add64 |= (uint64_t)(x64 % r) << (2 * (V - 1 - q));
-          x64 /= r;
-        }
-        s_bz = z;
-      }
-      for (int c = tid - 64; c >= 0 && c < MAXCH; c += THREADS - 64) {
-        uint64_t a = 0;  // unbiased digits of c * CH
-        uint64_t x = (uint64_t)c * CH;
-        for (int q = V - 1; q >= 0 && x; q--) {
-          const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
-          a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
-          x /= r;
-        }
-        s_cenc[c] = a;
-      }
-      __syncthreads();
-      patch_fast(smem, PAIR);
+      stage_block(smem, blobs, P.blob_off[b], s_lane_add, &s_bz, s_cenc, CHS, MAXCH, PAIR);
       staged = b;
     }
     if (tid == 0) {
@@ -1422,94 +1531,24 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
       const uint32_t sb = opaque_u32(pool + (uint32_t)H.npool * THREADS * (PAIR ? 16u : 8u) + (uint32_t)tid);
       const int T = H.T;
       const uint32_t cnt = (uint32_t)(ihi - ilo);
-      uint64_t best_w = 0;
-      // valid candidate: total, key update (the reference index only breaks
-      // exact (total, num_split) ties: keep the digits, convert once per item)
-      auto take = [&](uint64_t wv, double fwd) {
-        const double bwd = backward_b(S, wv);
-        const double total = dadd(fwd, dmul(bwd, H.keep_bwd));
-        const unsigned long long tb = (unsigned long long)__double_as_longlong(total);
-        const uint32_t ns = (uint32_t)__popcll(wv & s_bz.NZ);
-        nvalid++;
-        if (tb < best_t ||
-            (tb == best_t && (ns < best_n || (ns == best_n && ref_index_b(S, wv) < ref_index_b(S, best_w))))) {
-          best_t = tb;
-          best_n = ns;
-          best_w = wv;
-        }
-      };
+      LaneBest lb;
       while (true) {
         uint32_t c = 0;
         if (lane == 0) c = atomicAdd(&s_chunk, 1u);
         c = __shfl_sync(0xffffffffu, c, 0);
-        if (c * CH >= cnt) break;
-        uint32_t rem = min(CH, cnt - c * CH);  // candidates left in this chunk
-        uint64_t w = badd(badd(s_wbase, s_cenc[c], s_bz.B), s_lane_add[lane], s_bz.B);
-        if (PAIR) {
-          while (true) {
-            const uint64_t wb = badd(w, s_bz.add32, s_bz.B);
-            double fa, fb;
-            const int v = walk_pair(rec0, T, w, wb, (uint32_t)lane < rem, (uint32_t)lane + 32 < rem, fa, fb, rb, sb);
-            if (v & 1) take(w, fa);
-            if (v & 2) take(wb, fb);
-            if (rem <= 64) break;
-            rem -= 64;
-            w = badd(w, s_bz.add64, s_bz.B);
-          }
-          continue;
-        }
-        // single candidate per lane; with SKIP, lanes prove R-aligned runs invalid
-        // and the warp jumps to the furthest proven end (clamped to the chunk)
-        const unsigned long long whi = ilo + (unsigned long long)c * CH + rem;
-        unsigned long long base = whi - rem;
-        while (true) {
-          const bool active = (uint32_t)lane < rem;
-          double fwd;
-          const int fail = walk_fast<SKIP>(rec0, T, w, active, fwd, rb, sb);
-          uint32_t adv = 32;  // SKIP: candidates this lane proves done, from base
-          if (fail < 0) {
-            take(w, fwd);
-            if (SKIP) adv = lane + 1;
-          } else if (SKIP) {
-            adv = lane + 1;
-            if (active) {
-              const NodeSkip sk = S.skip[fail];
-              const unsigned long long x = base + lane;
-              const unsigned long long t = sk.R ? (x / sk.R + 1) * sk.R : whi;
-              adv = (uint32_t)(min(t, whi) - base);
-            }
-          }
-          if (!SKIP) {
-            if (rem <= 32) break;
-            rem -= 32;
-            w = badd(w, s_bz.add32, s_bz.B);
-          } else {
-            // the union of the lanes' proven runs is contiguous from base
-            uint32_t m = adv;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (m >= rem) break;
-            if (m == 32) {
-              w = badd(w, s_bz.add32, s_bz.B);
-            } else {
-              // the lane that proved the longest run provides the next base digits
-              const int src = __ffs(__ballot_sync(0xffffffffu, adv == m)) - 1;
-              uint64_t n0 = w;
-              if (lane == src) {
-                const bool jump = fail >= 0 && active && S.skip[fail].R;
-                // positions faster than m back to digit 0, then +1 at position m
-                const int sh = jump ? 2 * (H.V - 1 - S.skip[fail].m) : 0;
-                const uint64_t low = (1ULL << sh) - 1;
-                n0 = badd((n0 & ~low) | (s_bz.B & low), 1ULL << sh, s_bz.B);
-              }
-              w = badd(shfl_u64(n0, src), s_lane_add[lane], s_bz.B);
-            }
-            rem -= m;
-            base += m;
-          }
-        }
+        // chunk c: CH-sized for the first ~3/4 of the item, CHS-sized after
+        const uint32_t nbig = SKIP ? (cnt - cnt / 4) / CH : 0;
+        const uint32_t start = c < nbig ? c * CH : nbig * CH + (c - nbig) * CHS;
+        if (start >= cnt) break;
+        uint32_t rem = min(c < nbig ? CH : CHS, cnt - start);  // candidates left in this chunk
+        const uint64_t w = badd(badd(s_wbase, s_cenc[start / CHS], s_bz.B), s_lane_add[lane], s_bz.B);
+        score_chunk<SKIP, PAIR>(S, s_bz, s_lane_add, rec0, rb, sb, lane, w, rem, ilo + (unsigned long long)start + rem,
+                                lb);
       }
-      if (best_t != ~0ULL) best_i = ref_index_b(S, best_w);
+      best_t = lb.t;
+      best_n = lb.n;
+      nvalid = lb.valid;
+      if (best_t != ~0ULL) best_i = ref_index_b(S, lb.w);
     }
     // warp then block argmin of (total, num_split, index) + valid count
 #pragma unroll
@@ -1544,6 +1583,202 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
       items[item] = o;
     }
   }
+}
+
+// k_score_fast without item barriers.  The CTA keeps two work items in flight
+// (slots); warps pull chunks from a slot's cursor, and when a slot runs dry
+// each warp moves on to the other slot on its own -- the last warp to leave a
+// slot refills it with the next global item.  Warps meet at a barrier only
+// when an item belongs to another block (the tables must be restaged) and at
+// the end.  Results accumulate per lane over the CTA's whole share of a block
+// and are written once into the ItemOut of that share's first item; every
+// other item the CTA claims is written empty (k_reduce's min and sum are
+// unchanged).  Every warp visits the slots' generations in the same order
+// (slot 0 gen 1, slot 1 gen 1, slot 0 gen 2, ...), so a slot's parameters
+// are rewritten only after all eight warps have left it.
+struct FlowSlot {
+  unsigned long long item, ilo;
+  uint64_t wbase;
+  int64_t block;
+  uint32_t cnt, cursor, retired, gen;
+  int state;  // 0: ready (staged block), 1: another block, 2: no more items
+};
+
+template <bool SKIP, bool PAIR>
+__global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_MIN_BLOCKS) k_score_flow(
+    const uint8_t* __restrict__ blobs, ScorePlan P, ItemOut* __restrict__ items,
+    unsigned long long* __restrict__ counter) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr uint32_t CH = SKIP ? SKIP_CHUNK : PAIR_CHUNK;
+  constexpr uint32_t CHS = SKIP ? SKIP_CHUNK / 4 : PAIR_CHUNK;
+  constexpr int MAXCH = SKIP ? SKIP_MAX_CHUNKS * 4 : PAIR_MAX_CHUNKS;
+  constexpr int NW = THREADS / 32;
+  __shared__ uint64_t s_lane_add[32];
+  __shared__ Biased s_bz;
+  __shared__ uint64_t s_cenc[MAXCH];
+  __shared__ FlowSlot s_slot[2];
+  __shared__ unsigned long long s_seg;  // item whose ItemOut receives the current share (~0: none yet)
+  __shared__ int64_t s_staged;
+  __shared__ unsigned long long s_red_t[NW], s_red_i[NW], s_red_v[NW];
+  __shared__ uint32_t s_red_n[NW];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+
+  // one thread: claim the next item into slot x and publish it (gen + 1)
+  auto fill = [&](int x) {
+    volatile FlowSlot& sl = s_slot[x];
+    const unsigned long long it = atomicAdd(counter, 1ULL);
+    if (it >= P.n_items) {
+      sl.state = 2;
+    } else {
+      items[it] = ItemOut{~0ULL, ~0ULL, 0xFFFFFFFFu, 0ULL};
+      int64_t lo = 0, hi = P.nb;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (P.item_base[mid] <= it) lo = mid;
+        else hi = mid;
+      }
+      const unsigned long long ilo = P.lo[lo] + (it - P.item_base[lo]) * P.item_stride;
+      const unsigned long long ihi = min(ilo + P.item_cands, P.hi[lo]);
+      sl.item = it;
+      sl.block = lo;
+      sl.ilo = ilo;
+      sl.cnt = (uint32_t)(ihi - ilo);
+      if (lo == s_staged) {
+        sl.wbase = bencode(*(const BlobHeader*)smem, ilo);
+        sl.state = 0;
+      } else {
+        sl.state = 1;
+      }
+    }
+    sl.cursor = 0;
+    sl.retired = 0;
+    __threadfence_block();
+    atomicAdd((uint32_t*)&s_slot[x].gen, 1u);
+  };
+  // warp argmin of the lanes' shares -> s_red[warp]; then (after a barrier)
+  // thread 0 writes the CTA's share into s_seg's ItemOut
+  auto flush = [&](LaneBest& lb) {
+    const Tabs S = tabs_of(smem);
+    unsigned long long bt = lb.t, bi = lb.t != ~0ULL ? ref_index_b(S, lb.w) : ~0ULL,
+                       nv = lb.valid;
+    uint32_t bn = lb.n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, bt, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, bi, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, bn, o);
+      nv += __shfl_down_sync(0xffffffffu, nv, o);
+      if (key_less(t2, n2, i2, bt, bn, bi)) {
+        bt = t2;
+        bn = n2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      s_red_t[warp] = bt;
+      s_red_i[warp] = bi;
+      s_red_n[warp] = bn;
+      s_red_v[warp] = nv;
+    }
+    __syncthreads();
+    if (tid == 0 && s_seg != ~0ULL) {
+      ItemOut o{s_red_t[0], s_red_i[0], s_red_n[0], s_red_v[0]};
+      for (int w = 1; w < NW; w++) {
+        o.valid += s_red_v[w];
+        if (key_less(s_red_t[w], s_red_n[w], s_red_i[w], o.total_bits, o.num_split, o.index)) {
+          o.total_bits = s_red_t[w];
+          o.num_split = s_red_n[w];
+          o.index = s_red_i[w];
+        }
+      }
+      items[s_seg] = o;
+    }
+    lb = LaneBest{};
+  };
+
+  if (tid == 0) {
+    s_staged = -1;
+    s_seg = ~0ULL;
+    s_slot[0].gen = s_slot[1].gen = 0;
+    fill(0);
+    fill(1);
+  }
+  __syncthreads();
+  uint32_t my_gen[2] = {1, 1};
+  bool done[2] = {false, false};
+  int cur = 0;
+  LaneBest lb;
+  uint32_t rec0 = 0, rb = 0, sb = 0;
+  while (true) {
+    if (done[cur]) {
+      if (done[cur ^ 1]) break;
+      cur ^= 1;
+      continue;
+    }
+    volatile FlowSlot& sl = s_slot[cur];
+    if (lane == 0)
+      while (*(volatile uint32_t*)&s_slot[cur].gen < my_gen[cur]) __nanosleep(64);
+    __syncwarp();
+    __threadfence_block();
+    const int state = sl.state;
+    if (state == 2) {
+      done[cur] = true;
+      continue;
+    }
+    if (state == 1) {
+      // every warp reaches this slot generation: close the share of the
+      // staged block, stage this slot's block
+      flush(lb);
+      __syncthreads();
+      const int64_t b = sl.block;
+      stage_block(smem, blobs, P.blob_off[b], s_lane_add, &s_bz, s_cenc, CHS, MAXCH, PAIR);
+      if (tid == 0) {
+        s_staged = b;
+        s_seg = sl.item;
+        sl.wbase = bencode(*(const BlobHeader*)smem, sl.ilo);
+        sl.state = 0;
+        volatile FlowSlot& ot = s_slot[cur ^ 1];
+        if (ot.state == 1 && ot.block == b) {
+          ot.wbase = bencode(*(const BlobHeader*)smem, ot.ilo);
+          ot.state = 0;
+        }
+      }
+      __syncthreads();
+      {
+        const Tabs S = tabs_of(smem);
+        const BlobHeader& H = *S.H;
+        rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
+        const uint32_t pool = (uint32_t)__cvta_generic_to_shared(S.reach);
+        rb = opaque_u32(pool + 8u * (uint32_t)tid);
+        sb = opaque_u32(pool + (uint32_t)H.npool * THREADS * (PAIR ? 16u : 8u) + (uint32_t)tid);
+      }
+      continue;
+    }
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd((uint32_t*)&s_slot[cur].cursor, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    const uint32_t cnt = sl.cnt;
+    const uint32_t nbig = SKIP ? (cnt - cnt / 4) / CH : 0;
+    const uint32_t start = c < nbig ? c * CH : nbig * CH + (c - nbig) * CHS;
+    if (start < cnt) {
+      const uint32_t rem = min(c < nbig ? CH : CHS, cnt - start);
+      const uint64_t w = badd(badd(sl.wbase, s_cenc[start / CHS], s_bz.B), s_lane_add[lane], s_bz.B);
+      score_chunk<SKIP, PAIR>(tabs_of(smem), s_bz, s_lane_add, rec0, rb, sb, lane, w, rem,
+                              sl.ilo + (unsigned long long)start + rem, lb);
+      continue;
+    }
+    // slot dry for this warp: leave it (the last to leave refills it)
+    uint32_t r = 0;
+    if (lane == 0) {
+      r = atomicAdd((uint32_t*)&s_slot[cur].retired, 1u);
+      if (r == NW - 1) fill(cur);
+    }
+    __syncwarp();
+    my_gen[cur]++;
+    cur ^= 1;
+  }
+  flush(lb);
 }
 
 // Memoised brute force: every candidate of the range is visited (32 per warp
@@ -2381,11 +2616,20 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_sh
   const bool generic = getenv("SP_SCORE_GENERIC") != nullptr;
   // brute force on narrow blocks walks two candidates per lane (SP_SCORE_SINGLE=1: one)
   const bool pair = !generic && !wide && !memo && !ctx->skip && getenv("SP_SCORE_SINGLE") == nullptr;
+  // the brute-force FastNode walks run barrier-free (k_score_flow, c5: 35.7
+  // -> 35.3 ms); with prefix skipping an item often takes microseconds and
+  // the per-item hand-over costs more than the barrier it saves (8.0 -> 8.7
+  // ms), so skipping keeps k_score_fast.  SP_SCORE_ITEMS=1 / SP_SCORE_FLOW=1
+  // force either version (A/B checks).
+  const bool items_mode = getenv("SP_SCORE_ITEMS") != nullptr;
+  const bool flow_skip = getenv("SP_SCORE_FLOW") != nullptr;
+  auto fast_skip = flow_skip ? k_score_flow<true, false> : k_score_fast<true, false>;
+  auto fast_pair = items_mode ? k_score_fast<false, true> : k_score_flow<false, true>;
+  auto fast_one = items_mode ? k_score_fast<false, false> : k_score_flow<false, false>;
   auto kern = memo ? (wide ? k_score_memo<true> : k_score_memo<false>)
-              : ctx->skip ? (wide ? k_score<true, true> : generic ? k_score<false, true> : k_score_fast<true, false>)
+              : ctx->skip ? (wide ? k_score<true, true> : generic ? k_score<false, true> : fast_skip)
                           : (wide ? k_score<true, false>
-                                  : generic ? k_score<false, false>
-                                            : pair ? k_score_fast<false, true> : k_score_fast<false, false>);
+                                  : generic ? k_score<false, false> : pair ? fast_pair : fast_one);
   const size_t smem_k = memo   ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_T * THREADS_M * 8 + 16
                        : pair ? (size_t)((t->max_blob + 15) & ~15) + (size_t)t->max_pool * THREADS * 18 + 16
                               : smem;

@@ -673,10 +673,15 @@ def test_queued_searches_collected_out_of_order(backend, seed):
             t.close()
 
 
+@pytest.mark.parametrize("kernel_env", [None, "SP_SCORE_ITEMS", "SP_SCORE_FLOW"])
 @pytest.mark.parametrize("seed", range(0, 40, 8))
-def test_round_robin_shards_merge_exactly(backend, seed):
+def test_round_robin_shards_merge_exactly(backend, seed, kernel_env, monkeypatch):
     """Ranks deal each block's work items round-robin; for any rank count and every
-    scoring mode the exact merge of the shards equals the unsharded search."""
+    scoring mode the exact merge of the shards equals the unsharded search.  Run
+    with both FastNode scorers in every mode (k_score_fast with per-item
+    barriers, k_score_flow without), whose results must agree."""
+    if kernel_env:
+        monkeypatch.setenv(kernel_env, "1")
     from paper_2302_00247_b200.api_types import ClusterSpec
     from paper_2302_00247_b200.dist import merge_scores
     from paper_2302_00247_b200.lowering import lower
@@ -685,16 +690,19 @@ def test_round_robin_shards_merge_exactly(backend, seed):
 
     low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
     ses = Session.open(low, backend)
-    ba = fold_blocks(low, 1 + seed % 2, session=ses)
+    ba = fold_blocks(low, 2 + (seed // 8) % 2, session=ses)
     off, nodes = ba.templates_csr()
     t = backend.tables(ses.dgraph, off, nodes, ClusterSpec.from_mesh("1x8"), 1 << 20, 4 << 20)
     try:
         if t.overflow:
             pytest.skip("random block beyond u64")
+        ref = None
         for mode in ("skip", "walk", "memo"):
             backend.set_mode(mode)
             full = backend.score(t)
             key = [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split) for r in full]
+            ref = ref or key
+            assert key == ref, mode  # every mode and scorer: the same counts and argmin
             for n in (2, 3, 7):
                 merged = merge_scores([backend.score(t, s, n) for s in range(n)])
                 assert [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split)

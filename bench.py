@@ -397,12 +397,13 @@ def run_ours(args) -> None:
                        "ms_per_step": c2ms / 20, "e2e_ms_per_step": c2e / 20}
 
     # roofline of the dominant kernel (k_score, brute force): algorithmic bytes per
-    # launch = routing tables staged per block + 24 B per work item + 40 B per block
+    # launch = routing tables staged per block + 32 B per work item (one ItemOut;
+    # items are 256 x 256 candidates at this size) + 40 B per block
     kern = statistics.median(main["kern_ms"])
     ses = main["ses"]
     nb = len(main["ref"].results)
-    items = sum((r.candidates + 16383) // 16384 for r in main["ref"].results)
-    alg_bytes = getattr(ses, "last_table_bytes", 0) + 24 * items + 40 * nb
+    items = sum((r.candidates + 65535) // 65536 for r in main["ref"].results)
+    alg_bytes = getattr(ses, "last_table_bytes", 0) + 32 * items + 40 * nb
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:

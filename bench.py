@@ -455,7 +455,7 @@ def run_ours(args) -> None:
                          "e2e_step": statistics.median(main["e2e_times"])},
         "kernel_rate": {"k_score_candidates_per_s_per_gpu": kernel_rate,
                         "valid_plans_per_s": walked_valid * args.steps / (total_ms / 1000.0)},
-        "roofline": {"kernel": "k_score_fast", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+        "roofline": {"kernel": "k_score_flow", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
                      "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                      "note": "no per-candidate HBM input: algorithmic bytes are the staged "
                              "routing tables + per-item records, so the kernel is SM-issue-bound; "

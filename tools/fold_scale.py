@@ -29,15 +29,21 @@ sys.path.insert(0, ROOT)
 from paper_2302_00247_b200._native import Backend  # noqa: E402
 from paper_2302_00247_b200.workloads import transformer_stack_lowered  # noqa: E402
 
-SP_MAX_RANK = 6
+SP_MAX_RANK = 8
 
 
 def compulsory_bytes(low, depth: int) -> int:
+    """Bytes the fold must move at least once: every graph array it reads
+    (names + offsets, topological ranks, op, weight rank / shape rows of the
+    weighted nodes / trainable, producer CSR; not the activation specs, which
+    only the tables read) and its per-depth 64-bit prefix and relative-name
+    hashes, written once and read once."""
     n = len(low.op)
     E = int(low.in_off[-1])
-    graph = (int(low.name_off[-1]) + 8 * (n + 1) + 8 * n + 4 * n + 2 * 8 * SP_MAX_RANK * n + 16 * n
+    weighted = int(np.count_nonzero(low.w_rank))
+    graph = (int(low.name_off[-1]) + 8 * (n + 1) + 8 * n + 3 * n + 8 * SP_MAX_RANK * weighted
              + 8 * (n + 1) + 4 * E)
-    hashes = 2 * (2 * 8 * n * depth)  # prefix + rel hash per depth, written once and read once
+    hashes = 2 * (2 * 8 * n * depth)
     return graph + hashes
 
 

@@ -172,3 +172,95 @@ def test_assignment_map_vectorised_equals_block_loop(seed):
     py = dict(zip(map(low.names.__getitem__, rows.tolist()), map(labels.__getitem__, slots.tolist())))
     assert list(py.items()) == list(exp.items())
     assert np.all(slots >= 0)
+
+
+def _fake_search(types, seed):
+    """A folded random graph with fabricated, self-consistent score and explain
+    records (every block routed), as a search would return them."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle
+    from paper_2302_00247_b200._abi import SpExplainBlock, SpScoreOut
+    from paper_2302_00247_b200._native import RawList
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.blocks import BlockArrays
+    from paper_2302_00247_b200.lowering import lower
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=3, reps=(2, 5), ops=(3, 9)))
+    ba = BlockArrays.from_dict(oracle.prune(low, 2))
+    subs = search.subgraphs_from_blocks(low, ba, types)
+    csr = ba.templates_csr()
+
+    class Ses:
+        pass
+
+    ses = Ses()
+    ses.low = low
+    prep = search.route_prep(ses, subs, types, csr)
+    mesh = ClusterSpec.from_mesh("2x4")
+    rng = np.random.default_rng(seed)
+    nb = len(subs)
+    sc = (SpScoreOut * nb)()
+    xb = (SpExplainBlock * nb)()
+    ne = int(csr[0][-1])
+    node = np.zeros((max(1, ne), 4), np.int8)
+    for b in range(nb):
+        slot_pos, radices, nodes, _ = prep[b]
+        npat = [len(types.pattern_names.get(n[1], ())) for n in nodes]
+        routed = all(npat)
+        fwd, bwd = float(rng.random()) * 1e-4, float(rng.random()) * 1e-4
+        idx = int(rng.integers(0, int(np.prod(radices)) if radices else 1))
+        sc[b].candidates, sc[b].valid, sc[b].best_index = 7 + b, 3, idx
+        sc[b].best_total = fwd + bwd * (1.0 - mesh.overlap_fraction)
+        sc[b].best_num_split, sc[b].has_best = 0, 1 if routed else 0
+        x = xb[b]
+        x.valid, x.fail_pos = (1, -1) if routed else (0, 0)
+        x.forward_comm, x.backward_comm, x.total = fwd, bwd, sc[b].best_total
+        for j in range(4):
+            x.calls[j] = int(rng.integers(0, 3))
+            x.bytes[j] = int(rng.integers(0, 1 << 40)) if x.calls[j] else 0
+        x.collective_calls = sum(x.calls)
+        for i, k in enumerate(npat):
+            e = int(csr[0][b]) + i
+            node[e] = (int(rng.integers(0, max(1, k))), int(rng.integers(-1, 2)), int(rng.integers(-1, 2)), 0)
+    scores = RawList(sc, nb)
+    blocks = RawList(xb, nb)
+    eoff = np.zeros(nb + 1, np.int64)
+    detail = (blocks, node, np.zeros((1, 2), np.int8), eoff)
+    return ses, subs, scores, detail, prep, csr, mesh
+
+
+def _check_singletons(types, seed):
+    ses, subs, scores, detail, prep, csr, mesh = _fake_search(types, seed)
+    fast = search._singleton_results(ses, subs, scores, detail, prep, csr, mesh, types)
+    done = [b for b, r in enumerate(fast) if r is not None]
+    assert done, "no one-node block took the native path"
+    py = search.routed_plans_all(ses, None, subs, scores, mesh, types, detail, prep, only=done)
+    for b, rp in zip(done, py):
+        exp = types.SubgraphResult(subs[b], rp, int(scores[b].candidates), int(scores[b].valid), [])
+        assert fast[b] == exp and repr(fast[b]) == repr(exp)
+        assert type(fast[b].best.cost) is type(rp.cost) and fast[b].best.cost.total == scores[b].best_total
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_singleton_results_equal_python_path(seed):
+    """csrc singleton_results builds the same SubgraphResult/RoutedPlan/CostReport
+    objects routed_plans_all + collect build, from the same raw records."""
+    _check_singletons(search.DEFAULT_TYPES, seed)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not present")
+@pytest.mark.parametrize("seed", range(2))
+def test_singleton_results_with_reference_types(seed):
+    sys.path.insert(0, REF)
+    try:
+        import shardplan
+
+        from paper_2302_00247_b200.swap import reference_types
+        types = reference_types(shardplan)
+    finally:
+        sys.path.remove(REF)
+    _check_singletons(types, seed)

@@ -153,6 +153,18 @@ struct EntryLayout {
 
 constexpr int TAB4_PAD = 512;  // failed lanes index past a table by < 3^KMAX / 2 bytes
 
+// Winner re-routing data kept beside the blob (not staged by the scorers):
+// per template node its output bytes, op and rank; per internal edge the
+// conversion collective and axis for every (pattern, producer state) pair,
+// as k_fill's route_node evaluation found them (kind -1: no conversion).
+struct XNode {
+  int64_t act_bytes;
+  uint8_t op, act_rank, pad[6];
+};
+struct XEdge {
+  int8_t kind[4][3], axis[4][3];
+};
+
 __global__ void k_mark_blocks(const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                               int32_t* node_block, int32_t* node_tpos, int32_t* dup) {
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
@@ -296,7 +308,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
                        const int16_t* ref_slot_of,
                        const EntryLayout* lay, const BlobHeader* hdr_in, const int64_t* blob_off,
                        const uint8_t* has_cons, const uint8_t* ext_cons, sp_mesh mesh, int64_t mu,
-                       int64_t chunk, uint8_t* blobs, uint8_t* bound_of) {
+                       int64_t chunk, uint8_t* blobs, uint8_t* bound_of, uint8_t* xinfo, const int64_t* xoff) {
   const MeshC M = mesh_consts(mesh);
   __shared__ uint32_t s_kbase[MAXT + 1];
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -402,6 +414,11 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         ((FastNode*)(blob + H.fast_off))[i] = f;
       }
       ((NodeSkip*)(blob + H.skip_off))[i] = NodeSkip{L.skip_R, L.skip_m, 0};
+      XNode* xn = (XNode*)(xinfo + xoff[b]) + i;
+      xn->act_bytes = G.act_bytes[n];
+      xn->op = G.op[n];
+      xn->act_rank = G.act_rank[n];
+      XEdge* xe = (XEdge*)(xinfo + xoff[b] + (int64_t)sizeof(XNode) * T) + L.prod;
       int16_t* prod = (int16_t*)(blob + H.prod_off) + L.prod;
       double* dbl = (double*)(blob + H.dbl_off) + L.dbl;
       Pattern pats[4];
@@ -428,12 +445,13 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
           for (int s = 0; s < 3; s++) {
             double c = 0.0;
             NSpec req;
-            int8_t kind, axis;
-            if (p < np && normalize(pats[p].in, rr, &req) &&
-                convert(state_spec(s, rr), req, G.act_shape + (int64_t)r * SP_MAX_RANK, M.d, &kind, &axis) &&
-                kind != C_ID)
-              c = call_cost(kind, G.act_bytes[r], M);
+            int8_t kind = C_ID, axis = -1;
+            const bool ok = p < np && normalize(pats[p].in, rr, &req) &&
+                            convert(state_spec(s, rr), req, G.act_shape + (int64_t)r * SP_MAX_RANK, M.d, &kind, &axis);
+            if (ok && kind != C_ID) c = call_cost(kind, G.act_bytes[r], M);
             dbl[8 + (j * 4 + p) * 3 + s] = c;
+            xe[j].kind[p][s] = ok ? kind : (int8_t)-1;
+            xe[j].axis[p][s] = ok ? axis : (int8_t)-1;
           }
         j++;
       }
@@ -2208,6 +2226,166 @@ static_assert(sizeof(ExplainBlock) == sizeof(sp_explain_block), "ExplainBlock mi
 // its template): pattern / state / exit per node, conversion per internal
 // edge, forward/backward/total and collective accounting (plan_cost,
 // costmodel.py:193-267).  indices[b] == ~0 skips a block.
+// k_explain_all from the routing tables instead of re-deriving every pattern
+// choice: one warp per block stages the blob into shared memory, then lane 0
+// walks the template with the candidate's digits -- the routing byte of each
+// node gives its pattern and state (0xFF: the first node that cannot route),
+// the fp64 tables its reach (the scoring walk's own operations), and the
+// conversion collectives come from the XEdge table k_fill filled with the
+// same route_node evaluation.  The backward pass repeats k_explain_all's.
+__global__ void k_explain_fast(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
+                               const int16_t* ref_slot_of, const uint8_t* bound_of, const uint8_t* blobs,
+                               const int64_t* blob_off, const uint8_t* xinfo, const int64_t* xoff,
+                               const int64_t* edge_off, const unsigned long long* indices,
+                               const sp_score_out* scores, sp_mesh mesh, int64_t mu, int64_t chunk,
+                               ExplainBlock* out, int8_t* node_out, int8_t* edge_out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const MeshC M = mesh_consts(mesh);
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const unsigned long long index =
+        scores ? (scores[b].has_best ? scores[b].best_index : ~0ULL) : indices[b];
+    if (index == ~0ULL) {
+      if (lane == 0) {
+        ExplainBlock X{};
+        X.fail_pos = -1;
+        out[b] = X;
+      }
+      continue;
+    }
+    const BlobHeader* gH = (const BlobHeader*)(blobs + blob_off[b]);
+    const int nbytes = gH->bytes;
+    __syncwarp();
+    for (int q = lane * 16; q < nbytes; q += 32 * 16)
+      *(int4*)(smem + q) = *(const int4*)(blobs + blob_off[b] + q);
+    __syncwarp();
+    if (lane != 0) continue;
+    const BlobHeader& H = *(const BlobHeader*)smem;
+    const NodeDesc* desc = (const NodeDesc*)(smem + H.desc_off);
+    const int16_t* prodpos = (const int16_t*)(smem + H.prod_off) + H.n_prod;
+    const uint8_t* tab = smem + H.tab_off;
+    const double* dbl = (const double*)(smem + H.dbl_off);
+    const XNode* xn = (const XNode*)(xinfo + xoff[b]);
+    const int64_t e0 = tmpl_off[b];
+    const int T = H.T;
+    const XEdge* xe = (const XEdge*)(xinfo + xoff[b] + (int64_t)sizeof(XNode) * T);
+    ExplainBlock X;
+    X.valid = 0;
+    X.fail_pos = -1;
+    X.forward_comm = X.backward_comm = X.total = 0.0;
+    for (int k = 0; k < 4; k++) X.bytes[k] = X.calls[k] = 0;
+    X.collective_calls = 0;
+    uint8_t dig[64];  // reference slot order (candidate_by_index, search.py:103-116)
+    unsigned long long rem = index;
+    for (int q = H.V - 1; q >= 0; q--) {
+      const uint32_t r = ((H.radix3_ref >> q) & 1) ? 3 : 2;
+      dig[q] = (uint8_t)(rem % r);
+      rem /= r;
+    }
+    uint8_t state[MAXT];
+    double reach[MAXT];
+    int64_t eo = edge_off[b];
+    bool ok = true;
+    for (int i = 0; i < T; i++) {
+      const NodeDesc nd = desc[i];
+      const int slot = ref_slot_of[e0 + i];
+      uint32_t key = slot >= 0 ? dig[slot] : 0;
+      for (int j = 0; j < nd.k; j++) key = key * 3 + state[prodpos[nd.prod + j]];
+      const uint8_t e = tab[nd.tab + key];
+      if (e == 0xFF) {
+        X.fail_pos = i;
+        ok = false;
+        break;
+      }
+      const int p = e & 3, st = e >> 2;
+      state[i] = (uint8_t)st;
+      const double* dn = dbl + nd.dbl;
+      double base = 0.0;
+      for (int j = 0; j < nd.k; j++) {
+        const int pp = prodpos[nd.prod + j];
+        const int sj = state[pp];
+        const int kind = xe[nd.prod + j].kind[p][sj];
+        if (kind > 0) {
+          X.bytes[kind - 1] += xn[pp].act_bytes;
+          X.calls[kind - 1]++;
+        }
+        edge_out[2 * eo] = (int8_t)kind;
+        edge_out[2 * eo + 1] = xe[nd.prod + j].axis[p][sj];
+        eo++;
+        base = fmax(base, dadd(reach[pp], dn[8 + (j * 4 + p) * 3 + sj]));
+      }
+      Pattern pats[4];
+      patterns_for(xn[i].op, pats);
+      const int pc = pats[p].coll;
+      if (pc != C_ID) {
+        X.bytes[pc - 1] += xn[i].act_bytes;
+        X.calls[pc - 1]++;
+      }
+      reach[i] = dadd(base, dn[p]);
+      const NSpec fs = state_spec(st, xn[i].act_rank);
+      node_out[4 * (e0 + i)] = (int8_t)p;
+      node_out[4 * (e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
+      node_out[4 * (e0 + i) + 2] = -1;
+      node_out[4 * (e0 + i) + 3] = 0;
+    }
+    if (!ok) {
+      out[b] = X;
+      continue;
+    }
+    double fwd = 0.0;
+    for (int i = 0; i < T; i++) {
+      double tail = reach[i];
+      if (bound_of[e0 + i] && state[i] != 0) {
+        tail = dadd(tail, dbl[desc[i].dbl + 4 + state[i]]);
+        X.bytes[C_AG - 1] += xn[i].act_bytes;
+        X.calls[C_AG - 1]++;
+        node_out[4 * (e0 + i) + 2] = state_spec(state[i], xn[i].act_rank).axis;
+      }
+      fwd = fmax(fwd, tail);
+    }
+    double bwd = 0.0;
+    if (M.d > 1) {
+      // pack_gradients (rewrite.py:78-111): buckets first, then unfused, each one AllReduce
+      int64_t cur = 0;
+      int cur_n = 0;
+      for (int pass = 0; pass < 2; pass++) {
+        for (int i = 0; i < T; i++) {
+          const int32_t n = tmpl_nodes[e0 + i];
+          if (!G.w_rank[n] || !G.w_train[n] || dig[ref_slot_of[e0 + i]] != 0) continue;
+          const int64_t sz = G.w_bytes[n];
+          if (pass == 0) {
+            if (sz >= mu) continue;
+            if (cur + sz > chunk && cur_n) {
+              bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+              X.bytes[0] += cur;
+              X.calls[0]++;
+              cur = 0;
+              cur_n = 0;
+            }
+            cur += sz;
+            cur_n++;
+          } else if (sz >= mu) {
+            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
+            X.bytes[0] += sz;
+            X.calls[0]++;
+          }
+        }
+        if (pass == 0 && cur_n) {
+          bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+          X.bytes[0] += cur;
+          X.calls[0]++;
+        }
+      }
+    }
+    X.valid = 1;
+    X.forward_comm = fwd;
+    X.backward_comm = bwd;
+    X.total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
+    X.collective_calls = X.calls[0] + X.calls[1] + X.calls[2] + X.calls[3];
+    out[b] = X;
+  }
+}
+
 __global__ void k_explain_all(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                               const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
                               const uint8_t* bound_of, const uint8_t* blobs, const int64_t* blob_off,
@@ -2377,6 +2555,8 @@ struct TableDev {
   DevBuf<int32_t> node_block, node_tpos;
   DevBuf<int16_t> slot_of, ref_slot_of;
   DevBuf<uint8_t> has_cons, ext_cons, bound;
+  DevBuf<uint8_t> xinfo;  // per block: XNode[T] then XEdge[n_prod] (k_explain_fast)
+  DevBuf<int64_t> xoff;   // [nb + 1] byte offsets into xinfo
 };
 
 }  // namespace
@@ -2430,6 +2610,32 @@ struct TablesPriv {
     if (built) cudaEventDestroy(built);
   }
 };
+
+// Winner detail of every block (RoutedPlan/CostReport fields) on stream `s`:
+// k_explain_fast from the routing tables, or (SP_EXPLAIN_ROUTE=1, A/B and
+// cross-checks) k_explain_all re-deriving each node with route_node.
+static void launch_explain(sp_ctx* ctx, sp_tables* t, cudaStream_t s, const int64_t* d_edge_off,
+                           const unsigned long long* indices, const sp_score_out* scores, ExplainBlock* blk,
+                           int8_t* node, int8_t* edge) {
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  const int64_t nb = t->n_blocks;
+  if (getenv("SP_EXPLAIN_ROUTE")) {
+    SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
+              t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
+              priv->dev.ref_slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, d_edge_off, indices, scores,
+              priv->mesh, priv->mu, priv->chunk, blk, node, edge);
+  } else {
+    const size_t smem = (size_t)((t->max_blob + 15) & ~15);
+    if (smem > ctx->smem_optin)
+      throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
+    SP_CUDA(cudaFuncSetAttribute(k_explain_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SP_LAUNCH(ctx, k_explain_fast, (int)std::min<int64_t>(nb, 4096), 32, smem, s, view_of(t->dg), t->d_tmpl_off.p,
+              t->d_tmpl_nodes.p, nb, priv->dev.ref_slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p,
+              priv->dev.xinfo.p, priv->dev.xoff.p, d_edge_off, indices, scores, priv->mesh, priv->mu, priv->chunk,
+              blk, node, edge);
+  }
+  SP_CUDA(cudaGetLastError());
+}
 
 }  // namespace sp
 
@@ -2569,10 +2775,17 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   out->blobs.alloc(std::max<int64_t>(out->blob_off[nb], 16), s);
   D.bound.alloc(ne, s);
   out->d_blob_off.upload(out->blob_off.data(), nb + 1, s);
+  {
+    std::vector<int64_t> xo(nb + 1, 0);
+    for (int64_t b = 0; b < nb; b++)
+      xo[b + 1] = xo[b] + align16((int64_t)sizeof(XNode) * out->hdr[b].T + (int64_t)sizeof(XEdge) * out->hdr[b].n_prod);
+    D.xinfo.alloc(std::max<int64_t>(xo[nb], 16), s);
+    D.xoff.upload(xo.data(), nb + 1, s);
+  }
   if (nb > 0)
     SP_LAUNCH(ctx, k_fill, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
               D.node_tpos.p, D.slot_of.p, D.ref_slot_of.p, lay.p, hdr.p, out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
-              chunk, out->blobs.p, D.bound.p);
+              chunk, out->blobs.p, D.bound.p, D.xinfo.p, D.xoff.p);
   SP_CUDA(cudaGetLastError());
   {
     TablesPriv* tp = (TablesPriv*)out->priv;
@@ -2708,12 +2921,7 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_sh
     dblk.alloc(nb, s);
     dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
     dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
-    SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
-              t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
-              priv->dev.ref_slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, deoff.p,
-              (const unsigned long long*)nullptr, dout.p, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p,
-              dedge.p);
-    SP_CUDA(cudaGetLastError());
+    launch_explain(ctx, t, s, deoff.p, nullptr, dout.p, dblk.p, dnode.p, dedge.p);
   }
   SP_CUDA(cudaEventRecord(pd.ev[4], s));
   // results (and winner detail) to the pinned block now: collecting this
@@ -2910,11 +3118,7 @@ void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* block
   dblk.alloc(nb, s);
   dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
   dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
-  SP_LAUNCH(ctx, k_explain_all, (int)std::min<int64_t>((nb + 31) / 32, 4096), 32, 0, s, view_of(t->dg),
-            t->d_tmpl_off.p, t->d_tmpl_nodes.p, nb, priv->dev.node_block.p, priv->dev.node_tpos.p,
-            priv->dev.ref_slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p, (const int64_t*)(dup.p + nb),
-            dup.p, (const sp_score_out*)nullptr, priv->mesh, priv->mu, priv->chunk, dblk.p, dnode.p, dedge.p);
-  SP_CUDA(cudaGetLastError());
+  launch_explain(ctx, t, s, (const int64_t*)(dup.p + nb), dup.p, nullptr, dblk.p, dnode.p, dedge.p);
   dblk.download((ExplainBlock*)blocks_out, nb, s);
   dnode.download(node_out, 4 * ne, s);
   dedge.download(edge_out, 2 * nedge, s);

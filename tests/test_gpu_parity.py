@@ -710,3 +710,44 @@ def test_round_robin_shards_merge_exactly(backend, seed, kernel_env, monkeypatch
     finally:
         backend.set_mode("skip")
         t.close()
+
+
+@pytest.mark.parametrize("seed", range(0, 40, 4))
+def test_table_driven_explain_equals_route_node_explain(backend, seed, monkeypatch):
+    """k_explain_fast (routing tables + XEdge conversions) == k_explain_all
+    (route_node re-derivation) on random candidates of random graphs, routed
+    or not: every RoutedPlan/CostReport field, node and edge detail."""
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11)))
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 2 + (seed // 4) % 2, session=ses)
+    off, nodes = ba.templates_csr()
+    mname, kw = MESHES[seed % len(MESHES)]
+    mu, chunk = ((1 << 20, 4 << 20), (64, 256), (8, 8))[seed % 3]
+    t = backend.tables(ses.dgraph, off, nodes, ClusterSpec.from_mesh(mname, **kw), mu, chunk)
+    try:
+        if t.overflow:
+            pytest.skip("random block beyond u64")
+        rng = np.random.default_rng(seed)
+        for _ in range(4):
+            idx = [int(rng.integers(0, int(c))) for c in t.candidates]
+            fast = backend.explain_all(t, idx)
+            monkeypatch.setenv("SP_EXPLAIN_ROUTE", "1")
+            slow = backend.explain_all(t, idx)
+            monkeypatch.delenv("SP_EXPLAIN_ROUTE")
+            fields = ("valid", "fail_pos", "forward_comm", "backward_comm", "total", "collective_calls")
+            for a, b in zip(fast[0], slow[0]):
+                assert tuple(getattr(a, f) for f in fields) == tuple(getattr(b, f) for f in fields)
+                assert list(a.bytes) == list(b.bytes) and list(a.calls) == list(b.calls)
+            routed = [b for b, x in enumerate(slow[0]) if x.valid]
+            for b in routed:  # detail is defined for routed candidates
+                e0, e1 = int(off[b]), int(off[b + 1])
+                assert np.array_equal(fast[1][e0:e1], slow[1][e0:e1])
+                k0, k1 = int(fast[3][b]), int(fast[3][b + 1])
+                assert np.array_equal(fast[2][k0:k1], slow[2][k0:k1])
+    finally:
+        t.close()

@@ -128,7 +128,10 @@ class _Handle:
 
     def close(self):
         if self.ptr:
-            self._free(self.ptr)
+            # objects of a context that was already destroyed are gone with it
+            # (their free would touch the context's stream and pools)
+            if getattr(self.backend, "ctx", None):
+                self._free(self.ptr)
             self.ptr = None
 
     def __del__(self):  # pragma: no cover - GC timing

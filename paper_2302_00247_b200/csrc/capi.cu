@@ -70,6 +70,7 @@ void sp_ctx_destroy(sp_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->staging) cudaFreeHost(ctx->staging);
   for (auto& b : ctx->pinned_pool) cudaFreeHost(b.first);
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->timer)

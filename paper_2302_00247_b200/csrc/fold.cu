@@ -1449,7 +1449,7 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   SP_CUDA(cudaMemsetAsync(A.collision, 0, sizeof(int32_t), s));
   const int P2 = [&] { int q = 1; while (q < n) q <<= 1; return q; }();
   const size_t smem = (size_t)P2 * 20;
-  SP_CUDA(cudaFuncSetAttribute(k_fold_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  allow_smem(ctx, k_fold_small, smem);
   SP_CUDA(cudaEventRecord(ctx->ev[6], s));
   SP_LAUNCH(ctx, k_fold_small, 1, SMALL_THREADS, smem, s, A);
   SP_CUDA(cudaGetLastError());

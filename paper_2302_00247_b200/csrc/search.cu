@@ -2580,9 +2580,16 @@ struct PendingScore {
   size_t host_bytes = 0, off_blk = 0, off_node = 0, off_edge = 0;
   // 0 launch, 1 kernel start, 2 kernel end, 3 reduce end, 4 explain end, 5 results on the host
   cudaEvent_t ev[6] = {};
-  void events() {
+  void events() {  // from the context's pool (cudaEventCreate per search adds up on tiny searches)
     for (auto& e : ev)
-      if (!e) SP_CUDA(cudaEventCreate(&e));
+      if (!e) {
+        if (!ctx->event_pool.empty()) {
+          e = ctx->event_pool.back();
+          ctx->event_pool.pop_back();
+        } else {
+          SP_CUDA(cudaEventCreate(&e));
+        }
+      }
   }
   void release_host() {
     if (!host) return;
@@ -2594,7 +2601,14 @@ struct PendingScore {
   ~PendingScore() {
     release_host();
     for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
+      if (e) {
+        if (ctx) {
+          cudaEventSynchronize(e);  // recorded work done before another search re-records it
+          ctx->event_pool.push_back(e);
+        } else {
+          cudaEventDestroy(e);
+        }
+      }
   }
 };
 
@@ -2628,7 +2642,7 @@ static void launch_explain(sp_ctx* ctx, sp_tables* t, cudaStream_t s, const int6
     const size_t smem = (size_t)((t->max_blob + 15) & ~15);
     if (smem > ctx->smem_optin)
       throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
-    SP_CUDA(cudaFuncSetAttribute(k_explain_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    allow_smem(ctx, k_explain_fast, smem);
     SP_LAUNCH(ctx, k_explain_fast, (int)std::min<int64_t>(nb, 4096), 32, smem, s, view_of(t->dg), t->d_tmpl_off.p,
               t->d_tmpl_nodes.p, nb, priv->dev.ref_slot_of.p, priv->dev.bound.p, t->blobs.p, t->d_blob_off.p,
               priv->dev.xinfo.p, priv->dev.xoff.p, d_edge_off, indices, scores, priv->mesh, priv->mu, priv->chunk,
@@ -2848,9 +2862,8 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_sh
                               : smem;
   if (smem_k > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem_k) + " bytes)");
-  SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k));
-  int per_sm = 0;
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem_k));
+  allow_smem(ctx, kern, smem_k);
+  int per_sm = resident_ctas(ctx, kern, threads, smem_k);
   if (per_sm < 1) per_sm = 1;
   const unsigned long long slots = (unsigned long long)ctx->sm_count * per_sm;
   // size work items so each rank's grid gets ~8 items per resident CTA
@@ -3028,7 +3041,7 @@ void score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t
   const size_t smem = score_smem(t);
   if (smem > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem) + " bytes)");
-  SP_CUDA(cudaFuncSetAttribute(k_score_table, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  allow_smem(ctx, k_score_table, smem);
   const unsigned long long n = hi - lo;
   const unsigned grid = (unsigned)std::min<unsigned long long>((n + THREADS - 1) / THREADS, 4ULL * ctx->sm_count);
   DevBuf<double> dt;

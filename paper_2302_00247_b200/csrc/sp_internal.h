@@ -135,6 +135,11 @@ struct sp_ctx {
   size_t staging_bytes = 0;
   // free pinned host blocks for score results (D2H enqueued at launch time)
   std::vector<std::pair<void*, size_t>> pinned_pool;
+  // per kernel: the dynamic shared memory limit already set, and resident CTAs
+  // per SM by (kernel, smem) -- both runtime queries cost ~10 us per launch
+  std::vector<std::pair<const void*, int>> smem_set;
+  std::vector<std::pair<std::pair<const void*, size_t>, int>> occupancy;
+  std::vector<cudaEvent_t> event_pool;  // timing events of finished searches, reused
 };
 
 namespace sp {
@@ -159,6 +164,31 @@ inline uint8_t* pinned_acquire(sp_ctx* ctx, size_t need, size_t* got) {
 }
 inline void pinned_release(sp_ctx* ctx, void* p, size_t n) {
   if (p) ctx->pinned_pool.push_back({p, n});
+}
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `smem` exceeds
+// what was already allowed for `kern` (the attribute is a limit)
+template <class K>
+inline void allow_smem(sp_ctx* ctx, K* kern, size_t smem) {
+  for (auto& e : ctx->smem_set)
+    if (e.first == (const void*)kern) {
+      if ((size_t)e.second >= smem) return;
+      SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      e.second = (int)smem;
+      return;
+    }
+  SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ctx->smem_set.push_back({(const void*)kern, (int)smem});
+}
+// resident CTAs per SM of `kern` at `threads` x `smem` (cached per context)
+template <class K>
+inline int resident_ctas(sp_ctx* ctx, K* kern, int threads, size_t smem) {
+  const std::pair<const void*, size_t> key{(const void*)kern, smem * 4096 + (size_t)threads};
+  for (const auto& e : ctx->occupancy)
+    if (e.first == key) return e.second;
+  int per_sm = 0;
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  ctx->occupancy.push_back({key, per_sm});
+  return per_sm;
 }
 }  // namespace sp
 

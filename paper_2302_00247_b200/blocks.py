@@ -37,12 +37,13 @@ class BlockArrays:
 
     def templates_csr(self):
         """(offsets, nodes) of every block's template (instance 0 rows)."""
-        T = self.block_T
+        T = np.asarray(self.block_T, np.int64)
         off = np.zeros(len(T) + 1, np.int64)
         np.cumsum(T, out=off[1:])
-        nodes = np.empty(int(off[-1]), np.int32)
-        for b in range(len(T)):
-            nodes[off[b]: off[b + 1]] = self.template_nodes(b)
+        # block b's template = the first T[b] members from block_member_off[b]
+        mo = np.asarray(self.block_member_off, np.int64)[:len(T)]
+        src = np.repeat(mo - off[:-1], T) + np.arange(int(off[-1]), dtype=np.int64)
+        nodes = np.asarray(self.members)[src].astype(np.int32, copy=False)
         return off, nodes
 
     def multiplicity(self, b: int) -> int:

@@ -759,25 +759,29 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     t3b = time.perf_counter()
     label_keys = _label_keys(ba, subs, prep)
     t4 = time.perf_counter()
-    if len(searches) == 1:
-        results = searches[0][0].collect(graph, subs, want_table, types, prep)
-    else:
-        results = [None] * n_blocks
-        for srch, ids in searches:
+    # per block: the report's cost term and its weight labels, computed as each
+    # group's results land (the cheap group's while the expensive one scores)
+    results = [None] * n_blocks
+    terms = [0.0] * n_blocks
+    labs = [None] * n_blocks
+    candidates = valid = 0
+    for srch, ids in searches:
+        if len(searches) == 1:
+            got = srch.collect(graph, subs, want_table, types, prep)
+        else:
             got = srch.collect(graph, [subs[i] for i in ids], want_table, types, [prep[i] for i in ids])
-            for i, r in zip(ids, got):
-                results[i] = r
+        for i, res in zip(ids, got):
+            results[i] = res
+            candidates += res.candidates
+            valid += res.valid
+            terms[i] = res.best.cost.total * subs[i].multiplicity
+            if prep[i][0]:
+                labs[i] = [spec.label for _, spec in res.best.plan.assignments]
     t5 = time.perf_counter()
     total_cost = 0.0
-    candidates = 0
-    valid = 0
-    slot_labels = []
-    for sub, res, pb in zip(subs, results, prep):
-        candidates += res.candidates
-        valid += res.valid
-        total_cost += res.best.cost.total * sub.multiplicity
-        if pb[0]:
-            slot_labels.extend([spec.label for _, spec in res.best.plan.assignments])
+    for x in terms:  # block order (search.py:373): the sum is not reassociated
+        total_cost += x
+    slot_labels = [lab for ls in labs if ls is not None for lab in ls]
     # every instance takes the template's labels in weight_nodes order
     # (search.py:374-376); instance members come from the fold's member matrix
     assignments = _assignments(ses.low.names, label_keys, slot_labels)

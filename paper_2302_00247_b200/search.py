@@ -170,19 +170,41 @@ def enumerate_all_plans(graph, subgraph, types: TypeSet = DEFAULT_TYPES):
             subgraph, tuple((s, _spec_for_digit(types, d)) for s, d in zip(scopes, digits)), index)
 
 
-def _plan_index(graph, plan) -> int:
-    """Reference index of a plan's assignments (inverse of candidate_by_index)."""
+def _spec_digit(spec, w_rank: int, radix: int) -> Optional[int]:
+    """Search digit of a weight spec after the reference's normalisation
+    (ShardSpec.normalized, patterns.py:44-50: a negative split axis counts from
+    the weight's rank), or None when no weight pattern can match it (axis out of
+    range, partial, or a split axis beyond the options): pattern_routing then
+    skips every pattern of that node (search.py:156-166), a RoutingFailure."""
+    kind = spec.kind.value if hasattr(spec.kind, "value") else spec.kind
+    if kind == "replica":
+        return 0
+    if kind == "split":
+        axis = spec.axis if spec.axis >= 0 else w_rank + spec.axis
+        if 0 <= axis < w_rank and axis + 1 < radix:
+            return axis + 1
+    return None
+
+
+def _plan_index(graph, plan):
+    """Reference index of a plan's assignments (inverse of candidate_by_index),
+    plus the template position of the first node whose spec is not a search
+    option (None if every spec is one).  Such nodes get digit 0: the routing of
+    every node before them does not depend on their digit."""
     amap = dict(plan.assignments)
     index = 0
+    bad = None
+    template = plan.subgraph.template
     for s in weight_nodes(graph, plan.subgraph):
-        r = 3 if graph.nodes[s].weight.rank >= 2 else 2
-        spec = amap[s]
-        kind = spec.kind.value if hasattr(spec.kind, "value") else spec.kind
-        d = 0 if kind == "replica" else (spec.axis + 1 if kind == "split" else -1)
-        if not 0 <= d < r:
-            raise SpecMismatch(f"assignment {spec.label} of {s!r} is not a search option")
+        w = graph.nodes[s].weight
+        r = 3 if w.rank >= 2 else 2
+        d = _spec_digit(amap[s], w.rank, r)
+        if d is None:
+            q = template.index(s)
+            bad = q if bad is None else min(bad, q)
+            d = 0
         index = index * r + d
-    return index
+    return index, bad
 
 
 # ---------------------------------------------------------------------------
@@ -635,11 +657,12 @@ class _Search:
 def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
                   want_table: bool = False, *, session: Optional[Session] = None,
                   types: TypeSet = DEFAULT_TYPES, shard: int = 0, n_shards: int = 1,
-                  exchange: Optional[Callable] = None, csr=None) -> list:
+                  exchange: Optional[Callable] = None, csr=None,
+                  backend: Optional[Backend] = None) -> list:
     """Score every candidate of every block in one batched launch; returns
     SubgraphResult per block (search_subgraph semantics, search.py:317-345).
     `csr` = (offsets, node indices) of the templates when already known."""
-    ses = session or Session.open(graph)
+    ses = session or Session.open(graph, backend)
     if not subgraphs:
         return []
     if csr is None:
@@ -651,11 +674,11 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
 
 def search_subgraph(graph, subgraph, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
                     jobs: int = 1, want_table: bool = False, *, types: TypeSet = DEFAULT_TYPES,
-                    session: Optional[Session] = None):
+                    session: Optional[Session] = None, backend: Optional[Backend] = None):
     """Exhaustive argmin over one block's candidates (search.py:317-345)."""
     del jobs
     return search_blocks(graph, [subgraph], mesh, mu, chunk_size, want_table, session=session,
-                         types=types)[0]
+                         types=types, backend=backend)[0]
 
 
 def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
@@ -729,6 +752,15 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     # launches back to back: each search copies its results to the host behind
     # its own kernels, so the cheap group is collected while the expensive one
     # still scores
+    if mu > chunk_size and n_blocks:
+        # the reference fails in the first block (search.py:366): its first valid
+        # candidate's plan_cost -> pack_gradients raises BadConfig (rewrite.py:88),
+        # or, with no valid candidate, the all-replica assertion; score block 0 only
+        off, nodes = csr
+        first = _Search(ses, (np.array([0, off[1] - off[0]], np.int64), nodes[off[0]:off[1]]),
+                        mesh, mu, chunk_size, 0, 1, None)
+        first.collect(graph, subgraphs_from_blocks(ses.low, ba, types)[:1], False, types)
+        raise AssertionError("unreachable: block 0 raises BadConfig or the all-replica assertion")
     searches = []
     try:
         for ids, gcsr in _block_groups(ses.low, csr):
@@ -765,18 +797,22 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     terms = [0.0] * n_blocks
     labs = [None] * n_blocks
     candidates = valid = 0
-    for srch, ids in searches:
-        if len(searches) == 1:
-            got = srch.collect(graph, subs, want_table, types, prep)
-        else:
-            got = srch.collect(graph, [subs[i] for i in ids], want_table, types, [prep[i] for i in ids])
-        for i, res in zip(ids, got):
-            results[i] = res
-            candidates += res.candidates
-            valid += res.valid
-            terms[i] = res.best.cost.total * subs[i].multiplicity
-            if prep[i][0]:
-                labs[i] = [spec.label for _, spec in res.best.plan.assignments]
+    try:
+        for srch, ids in searches:
+            if len(searches) == 1:
+                got = srch.collect(graph, subs, want_table, types, prep)
+            else:
+                got = srch.collect(graph, [subs[i] for i in ids], want_table, types, [prep[i] for i in ids])
+            for i, res in zip(ids, got):
+                results[i] = res
+                candidates += res.candidates
+                valid += res.valid
+                terms[i] = res.best.cost.total * subs[i].multiplicity
+                if prep[i][0]:
+                    labs[i] = [spec.label for _, spec in res.best.plan.assignments]
+    finally:
+        for srch, _ in searches:  # a group whose collect never ran (an earlier one raised)
+            srch.tables.close()
     t5 = time.perf_counter()
     total_cost = 0.0
     for x in terms:  # block order (search.py:373): the sum is not reassociated
@@ -804,14 +840,23 @@ class _OneScore:
 
 def _explain_plan(graph, plan, mesh, mu, chunk_size, types, session):
     ses = session or Session.open(graph)
-    index = _plan_index(graph, plan)
+    index, bad = _plan_index(graph, plan)
     off, nodes = _templates_csr(ses.low, [plan.subgraph])
     tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
     try:
         sc = _OneScore(index)
-        return routed_plans_all(ses, tables, [plan.subgraph], [sc], mesh, types)[0]
+        routed = routed_plans_all(ses, tables, [plan.subgraph], [sc], mesh, types)[0]
     finally:
         tables.close()
+    template = plan.subgraph.template
+    if bad is not None and (not isinstance(routed, types.RoutingFailure)
+                            or template.index(routed.node) > bad):
+        # the first node (topological order) whose weight spec matches no pattern
+        return types.RoutingFailure(template[bad], "no pattern chains from producer states")
+    if isinstance(routed, types.RoutingFailure):
+        return routed
+    # the caller's plan object, as the reference returns it (search.py:224)
+    return types.RoutedPlan(plan, routed.routings, routed.exit_conversions, routed.cost)
 
 
 def pattern_routing(graph, plan, mesh, *, types: TypeSet = DEFAULT_TYPES,
@@ -821,8 +866,7 @@ def pattern_routing(graph, plan, mesh, *, types: TypeSet = DEFAULT_TYPES,
     routed = _explain_plan(graph, plan, mesh, 1 << 20, 4 << 20, types, session)
     if isinstance(routed, types.RoutingFailure):
         return routed
-    return types.RoutedPlan(routed.plan, routed.routings, routed.exit_conversions,
-                            types.CostReport())
+    return types.RoutedPlan(plan, routed.routings, routed.exit_conversions, types.CostReport())
 
 
 def plan_cost(routed, graph, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20, *,
@@ -853,28 +897,35 @@ def routed_plan_for_assignments(graph, mesh, assignments: dict, min_duplicates: 
     subs = subgraphs_from_blocks(ses.low, ba, types)
     csr = ba.templates_csr()
     prep = route_prep(ses, subs, types, csr)
-    # stored labels -> candidate index in the reference's enumeration order
-    indices = []
+    # stored labels -> candidate index in the reference's enumeration order; a spec
+    # that is not a search option gets digit 0 and fails at its node (see _plan_index)
+    indices, bads, chosen = [], [], []
     for sub, (slot_pos, radices, _, _) in zip(subs, prep):
         index = 0
+        bad = None
+        specs = []
         for q, r in zip(slot_pos, radices):
-            spec = types.ShardSpec.from_label(assignments[sub.template[q]])
-            kind = spec.kind.value if hasattr(spec.kind, "value") else spec.kind
-            d = 0 if kind == "replica" else (spec.axis + 1 if kind == "split" else -1)
-            if not 0 <= d < r:
-                # not a search option: no pattern matches that weight spec
-                node = sub.template[q]
-                raise ShardplanError(f"stored plan does not route at node {node}: "
-                                     f"no pattern matches weight spec {spec.label}")
+            scope = sub.template[q]
+            spec = types.ShardSpec.from_label(assignments[scope])
+            specs.append((scope, spec))
+            d = _spec_digit(spec, int(ses.low.w_rank[ses.low.index[scope]]), r)
+            if d is None:
+                bad = q if bad is None else min(bad, q)
+                d = 0
             index = index * r + d
         indices.append(index)
+        bads.append(bad)
+        chosen.append(tuple(sorted(specs, key=lambda t: t[0])))
     off, nodes = csr
     tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
     try:
         detail = ses.backend.explain_all(tables, indices)
         for b, X in enumerate(detail[0]):
-            if not X.valid:
-                raise ShardplanError(f"stored plan does not route at node {subs[b].template[X.fail_pos]}: "
+            fail = None if X.valid else int(X.fail_pos)
+            if bads[b] is not None and (fail is None or fail > bads[b]):
+                fail = bads[b]
+            if fail is not None:
+                raise ShardplanError(f"stored plan does not route at node {subs[b].template[fail]}: "
                                      "no pattern chains from producer states")
             if mu > chunk_size:
                 raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
@@ -883,8 +934,8 @@ def routed_plan_for_assignments(graph, mesh, assignments: dict, min_duplicates: 
         tables.close()
     results = []
     total_cost = 0.0
-    for sub, routed in zip(subs, bests):
-        plan = types.CandidatePlan(sub, routed.plan.assignments, -1)
+    for sub, routed, specs in zip(subs, bests, chosen):
+        plan = types.CandidatePlan(sub, specs, -1)  # the stored specs (search.py:427-430)
         routed = types.RoutedPlan(plan, routed.routings, routed.exit_conversions, routed.cost)
         results.append(types.SubgraphResult(sub, routed, 1, 1))
         total_cost += routed.cost.total * sub.multiplicity

@@ -58,11 +58,18 @@ def reference_types(shardplan) -> TypeSet:
 
 
 def _translate(shardplan, exc: Exception) -> Exception:
-    """Our error classes -> the reference's same-named classes."""
+    """Our error classes -> the reference's same-named classes.  Planner errors
+    the reference has no class for (UnsupportedSearch: a search space outside
+    the backend's limits) become the reference's ShardplanError, so its CLI
+    (`except ShardplanError`, cli.py:471) reports them as planner errors.
+    BackendError (a CUDA failure, RuntimeError) is not a planner error and is
+    left as it is."""
     ref_errors = importlib.import_module(shardplan.__name__ + ".errors")
-    cls = getattr(ref_errors, type(exc).__name__, None)
-    if cls is None or isinstance(exc, AssertionError):
+    if isinstance(exc, AssertionError):
         return exc
+    cls = getattr(ref_errors, type(exc).__name__, None)
+    if cls is None:
+        return ref_errors.ShardplanError(f"{type(exc).__name__}: {exc}")
     if type(exc).__name__ == "CycleError":
         return cls(exc.src, exc.dst)
     return cls(str(exc))
@@ -88,7 +95,7 @@ def install(shardplan=None, backend=None) -> Installed:
         @functools.wraps(fn)
         def inner(*args, **kwargs):
             kwargs.setdefault("types", types)
-            if backend is not None and fn is not ours.search_subgraph:
+            if backend is not None:
                 kwargs.setdefault("backend", backend)
             try:
                 return fn(*args, **kwargs)

@@ -1,0 +1,55 @@
+"""pytest plugin: run the REFERENCE's own test suite with this backend swapped in.
+
+    cd baseline/_ref && PYTHONPATH=.:<repo>:<repo>/tests \\
+        python -m pytest -p ref_swap_plugin tests
+
+`swap.install()` rebinds shardplan's search entry points (derive_plan,
+prune_graph, search_subgraph, routed_plan_for_assignments in shardplan,
+shardplan.search and shardplan.cli) BEFORE the reference's test
+modules are imported, so every `from shardplan import derive_plan` in them
+binds the device path.  Each swapped entry point counts its calls; the counts
+are written to $SP_SWAP_COUNTS at the end, so the caller can prove the suite
+actually went through the backend.  `jobs` is ignored by the backend, so no
+ProcessPool ever forks after CUDA initialisation.
+"""
+
+from __future__ import annotations
+
+import collections
+import json
+import os
+
+_state = {}
+
+
+def pytest_configure(config):
+    import shardplan
+
+    from paper_2302_00247_b200 import swap
+
+    handle = swap.install(shardplan)
+    counts = collections.Counter()
+    seen = {}
+    for module, name, _orig in handle.saved:
+        fn = getattr(module, name)
+        if id(fn) not in seen:
+            def counted(*a, __fn=fn, __name=name, **k):
+                counts[__name] += 1
+                return __fn(*a, **k)
+
+            counted.__wrapped__ = fn
+            counted.__name__ = name
+            seen[id(fn)] = counted
+        setattr(module, name, seen[id(fn)])
+    _state.update(handle=handle, counts=counts)
+
+
+def pytest_unconfigure(config):
+    handle = _state.get("handle")
+    if handle is None:
+        return
+    path = os.environ.get("SP_SWAP_COUNTS")
+    if path:
+        with open(path, "w") as fh:
+            json.dump(dict(_state["counts"]), fh)
+    handle.uninstall()

@@ -416,6 +416,36 @@ def test_c5_throughput_fold_slices_and_argmin(c5_sessions):
         t.close()
 
 
+@pytest.mark.parametrize("mode", ["walk", "skip"])
+def test_c5_throughput_whole_plan_matches_reference(c5_sessions, mode):
+    """The BENCH workload end to end: derive_plan on motif_dag(0, "throughput")
+    (1018 blocks, 3,918,656,938 candidates) hash-equals the reference's report
+    (tests/golden/make_golden_c5_full.py: the reference's own search on every
+    block <= 2e6 candidates, the oracle's brute-force argmin on the 4.3e7, 3.9e8
+    and 3.5e9 blocks rebuilt by the reference), in brute force and prefix skip."""
+    import hashlib
+    import os
+
+    from golden_io import GOLDEN, c5
+    from paper_2302_00247_b200.search import derive_plan
+
+    with open(os.path.join(GOLDEN, "c5_full.json")) as fh:
+        gold = json.load(fh)
+    g, ses = c5_sessions["throughput"]
+    be = ses.backend
+    be.set_mode(mode)
+    try:
+        rep = derive_plan(g, mesh(c5()["throughput"]["mesh"]), session=ses)
+    finally:
+        be.set_mode("skip")
+    got = [[r.best.plan.index, r.best.plan.num_split, repr(r.best.cost.total), r.valid, r.candidates]
+           for r in rep.results]
+    assert got == [b[:5] for b in gold["blocks"]]
+    assert (rep.candidates, rep.valid, repr(rep.total_cost)) == (gold["candidates"], gold["valid"],
+                                                               gold["total_cost"])
+    assert hashlib.sha256(canon(rep.to_json()).encode()).hexdigest() == gold["plan_sha"]
+
+
 @pytest.mark.parametrize("seed", range(0, 40, 4))
 def test_digit_encodings_agree(backend, seed, monkeypatch):
     """The biased one-word digit encoding (V <= 32) and the two-word encoding give

@@ -80,3 +80,34 @@ def test_errors_translate_to_reference_classes(shardplan):
     assert isinstance(exc, shardplan.BadConfig)
     exc = swap._translate(shardplan, errors.CycleError("a", "b"))
     assert isinstance(exc, shardplan.CycleError) and exc.src == "a"
+
+
+def test_backend_only_errors_become_reference_planner_errors(shardplan):
+    """UnsupportedSearch has no reference class: under the swap it surfaces as the
+    reference's ShardplanError, so the reference CLI's `except ShardplanError`
+    (cli.py:471) reports it; a CUDA failure (BackendError) stays a RuntimeError."""
+    from paper_2302_00247_b200 import errors, swap
+
+    exc = swap._translate(shardplan, errors.UnsupportedSearch("a block has more than 2**64 candidates"))
+    assert type(exc) is shardplan.ShardplanError and "2**64" in str(exc)
+    exc = swap._translate(shardplan, errors.SpecMismatch("x"))
+    assert isinstance(exc, shardplan.SpecMismatch)
+
+
+def test_install_forwards_backend_to_search_subgraph(shardplan, monkeypatch):
+    from paper_2302_00247_b200 import search, swap
+
+    seen = {}
+
+    def fake(graph, subgraph, mesh, *a, backend=None, **k):
+        seen["backend"] = backend
+        return "ok"
+
+    monkeypatch.setattr(search, "search_subgraph", fake)
+    sentinel = object()
+    h = swap.install(shardplan, backend=sentinel)
+    try:
+        assert shardplan.search.search_subgraph(None, None, None) == "ok"
+    finally:
+        h.uninstall()
+    assert seen["backend"] is sentinel

@@ -31,10 +31,10 @@ def test_reference_suite_passes_with_backend_swapped_in(tmp_path):
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, ROOT, os.path.join(ROOT, "tests")]),
                SP_SWAP_COUNTS=str(counts), PYTHONDONTWRITEBYTECODE="1")
     proc = subprocess.run([sys.executable, "-m", "pytest", "-p", "ref_swap_plugin", "-p", "no:cacheprovider",
-                           "-q", "tests"], cwd=REF, env=env, capture_output=True, text=True, timeout=1200)
+                           "tests"], cwd=REF, env=env, capture_output=True, text=True, timeout=1200)
     tail = proc.stdout[-4000:] + proc.stderr[-2000:]
     assert proc.returncode == 0, tail
-    assert " 182 passed" in proc.stdout, tail
+    assert "182 passed" in proc.stdout, tail
     n = json.loads(counts.read_text())
     # the suite's searches, folds and replays really ran on the device
     assert n.get("derive_plan", 0) >= 20 and n.get("prune_graph", 0) >= 10, n

@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define SP_ABI_VERSION 1
+#define SP_ABI_VERSION 2
 #define SP_MAX_RANK 8
 
 enum sp_status {
@@ -159,10 +159,40 @@ typedef struct sp_tables sp_tables;
 
 int sp_abi_version(void);
 
-/* One context per process and device (one process per GPU). */
-int sp_ctx_create(int device, sp_ctx** out);
+/*
+ * A context over `ngpu` devices of this process.  ngpu == 1: one
+ * device -- the process-per-GPU form; join the other processes' devices with
+ * sp_ctx_comm_init.  ngpu > 1: this process drives all `devices`; every entry
+ * point below fans out over them (graph and tables replicated, the fold runs on
+ * devices[0]) and a search deals each block's work items over the devices and
+ * merges on devices[0] -- the reference's process-pool split and min-merge
+ * (search.py:327-343) -- through ncclCommInitAll / one ncclAllGather (devices
+ * listed twice share a GPU and exchange by peer copies instead; test use).
+ */
+int sp_ctx_create(int ngpu, const int* devices, sp_ctx** out);
 void sp_ctx_destroy(sp_ctx* ctx);
 const char* sp_last_error(const sp_ctx* ctx);
+
+/*
+ * Multi-process form (one process per GPU, e.g. under torchrun): rank 0 calls
+ * sp_comm_unique_id and hands the SP_COMM_ID_BYTES-byte id to every rank by
+ * any bootstrap (file, TCP store, MPI); each rank then calls sp_ctx_comm_init
+ * on its single-device context (ncclCommInitRank; NCCL is loaded with dlopen
+ * on first use, libnccl.so.2).  From then on sp_score_launch / sp_score /
+ * sp_search score this rank's share (`shard`/`n_shards` are taken from the
+ * communicator) and exchange the 40-byte per-block records with ONE
+ * ncclAllGather over NVLink, merged on the device by (total, num_split, index)
+ * with valid counts summed; every rank ends with the merged result, and the
+ * winner detail (explain) is chained behind the merge on the device.
+ */
+#define SP_COMM_ID_BYTES 128
+enum sp_transport { SP_TRANSPORT_NONE = 0, SP_TRANSPORT_NCCL = 1, SP_TRANSPORT_P2P = 2 };
+int sp_comm_unique_id(uint8_t* id);
+int sp_ctx_comm_init(sp_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id);
+/* nranks / rank of the context's communicator (1 / 0 without one), its local
+ * device count and transport (enum sp_transport), the loaded NCCL version. */
+int sp_ctx_comm_info(const sp_ctx* ctx, int32_t* nranks, int32_t* rank, int32_t* ndev, int32_t* transport,
+                     int32_t* nccl_version);
 
 /* Upload the lowered graph once; it stays resident in HBM. */
 int sp_graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph** out);

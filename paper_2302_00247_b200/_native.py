@@ -31,12 +31,20 @@ LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "lib", "libshardsearch
 
 _lib = None
 _lib_lock = threading.Lock()
+#: SP_ABI_VERSION of include/shardsearch.h
+ABI_VERSION = 2
+#: SP_COMM_ID_BYTES
+COMM_ID_BYTES = 128
+TRANSPORTS = {0: "none", 1: "nccl", 2: "p2p"}
 
 
 def _declare(L):
     vp = C.c_void_p
     L.sp_abi_version.restype = C.c_int
-    L.sp_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.sp_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(vp)]
+    L.sp_comm_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+    L.sp_ctx_comm_init.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]
+    L.sp_ctx_comm_info.argtypes = [vp] + [C.POINTER(C.c_int32)] * 5
     L.sp_ctx_destroy.argtypes = [vp]
     L.sp_last_error.argtypes = [vp]
     L.sp_last_error.restype = C.c_char_p
@@ -75,7 +83,7 @@ def _declare(L):
     L.sp_explain_all.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(SpExplainBlock),
                                  C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_copy_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-    for name in ("sp_score_launch", "sp_score_wait", "sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
+    for name in ("sp_comm_unique_id", "sp_ctx_comm_init", "sp_ctx_comm_info", "sp_score_launch", "sp_score_wait", "sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
                  "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
                  "sp_score_range", "sp_explain", "sp_last_timings"):
         getattr(L, name).restype = C.c_int
@@ -93,7 +101,7 @@ def load_library():
                     "`python -c 'import __graft_entry__ as g; g.build()'`")
             L = C.CDLL(LIB_PATH)
             _declare(L)
-            if L.sp_abi_version() != 1:
+            if L.sp_abi_version() != ABI_VERSION:
                 raise BackendError("libshardsearch ABI version mismatch")
             _lib = L
     return _lib
@@ -108,6 +116,7 @@ EXPORTED_SYMBOLS = (
     "sp_tables_edge_offsets", "sp_explain_all", "sp_search", "sp_set_option",
     "sp_fold_stats", "sp_score_launch", "sp_score_wait", "sp_ingest_json", "sp_ingest_error",
     "sp_ingest_view", "sp_ingest_free", "sp_ingest_onnx", "sp_ingest_report", "sp_ingest_text",
+    "sp_comm_unique_id", "sp_ctx_comm_init", "sp_ctx_comm_info",
 )
 
 
@@ -148,18 +157,61 @@ class Tables(_Handle):
 
 
 class Backend:
-    """One CUDA context on one device (one process per GPU)."""
+    """One library context (sp_ctx_create) over one device -- one process per
+    GPU, joined to the other ranks with `comm_init` -- or over several devices
+    of this process (`devices=[...]`): the library then fans every call out
+    over them and a search deals each block's work items across the devices,
+    merging on the first (search.py:327-343's pool split and min-merge)."""
 
-    def __init__(self, device: int | None = None):
+    def __init__(self, device: int | None = None, devices=None):
         self.lib = load_library()
-        if device is None:
-            device = int(os.environ.get("SP_DEVICE", os.environ.get("LOCAL_RANK", "0")))
-        self.device = device
+        if devices is None:
+            if device is None:
+                device = int(os.environ.get("SP_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+            devices = [device]
+        devices = [int(d) for d in devices]
+        self.devices = devices
+        self.device = devices[0]
         h = C.c_void_p()
-        rc = self.lib.sp_ctx_create(device, C.byref(h))
+        arr = (C.c_int * len(devices))(*devices)
+        rc = self.lib.sp_ctx_create(len(devices), arr, C.byref(h))
         if rc != 0:
-            raise BackendError(f"sp_ctx_create(device={device}) failed with status {rc}")
+            raise BackendError(f"sp_ctx_create(devices={devices}) failed with status {rc}")
         self.ctx = h
+        self.comm = self.comm_info()
+
+    # -- multi-GPU -----------------------------------------------------------------
+    def comm_unique_id(self) -> bytes:
+        """A fresh NCCL unique id (rank 0), to hand to every rank's comm_init."""
+        buf = (C.c_uint8 * COMM_ID_BYTES)()
+        self._check(self.lib.sp_comm_unique_id(buf), "sp_comm_unique_id")
+        return bytes(buf)
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
+        """Join `nranks` processes (one GPU each) in one NCCL communicator: from then
+        on every search scores this rank's share and merges on the device."""
+        if len(uid) != COMM_ID_BYTES:
+            raise BadConfig(f"NCCL unique id must be {COMM_ID_BYTES} bytes")
+        buf = (C.c_uint8 * COMM_ID_BYTES).from_buffer_copy(uid)
+        self._check(self.lib.sp_ctx_comm_init(self.ctx, int(nranks), int(rank), buf), "sp_ctx_comm_init")
+        self.comm = self.comm_info()
+
+    def comm_info(self) -> dict:
+        v = [C.c_int32() for _ in range(5)]
+        self._check(self.lib.sp_ctx_comm_info(self.ctx, *[C.byref(x) for x in v]), "sp_ctx_comm_info")
+        return {"nranks": v[0].value, "rank": v[1].value, "devices": v[2].value,
+                "transport": TRANSPORTS.get(v[3].value, str(v[3].value)), "nccl_version": v[4].value}
+
+    @property
+    def sharded_in_library(self) -> bool:
+        """True when searches are split and merged by the library itself (several
+        devices in this context, or a multi-process communicator)."""
+        return self.comm["nranks"] > 1
+
+    @property
+    def is_root(self) -> bool:
+        """Rank 0 of a multi-process communicator (always true otherwise)."""
+        return self.comm["devices"] > 1 or self.comm["rank"] == 0
 
     # -- errors --------------------------------------------------------------------
     def _check(self, rc: int, what: str):

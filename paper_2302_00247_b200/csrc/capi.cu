@@ -30,9 +30,7 @@ extern "C" {
 
 int sp_abi_version(void) { return SP_ABI_VERSION; }
 
-int sp_ctx_create(int device, sp_ctx** out) {
-  if (!out) return SP_ERR_CONFIG;
-  *out = nullptr;
+static sp_ctx* ctx_create_one(int device) {
   sp_ctx* ctx = new sp_ctx();
   int rc = guard(ctx, [&] {
     SP_CUDA(cudaSetDevice(device));
@@ -57,17 +55,16 @@ int sp_ctx_create(int device, sp_ctx** out) {
   if (rc != SP_OK) {
     std::fprintf(stderr, "sp_ctx_create: %s\n", ctx->last_error.c_str());
     delete ctx;
-    return rc;
+    return nullptr;
   }
-  *out = ctx;
-  return SP_OK;
+  return ctx;
 }
 
-void sp_ctx_destroy(sp_ctx* ctx) {
-  if (!ctx) return;
+static void ctx_destroy_one(sp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ctx->cub_tmp.release();
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) sp::nccl_destroy(ctx);
   if (ctx->staging) cudaFreeHost(ctx->staging);
   for (auto& b : ctx->pinned_pool) cudaFreeHost(b.first);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
@@ -83,6 +80,99 @@ void sp_ctx_destroy(sp_ctx* ctx) {
   delete ctx;
 }
 
+int sp_ctx_create(int ngpu, const int* devices, sp_ctx** out) {
+  if (!out || ngpu < 1 || !devices) return SP_ERR_CONFIG;
+  *out = nullptr;
+  std::vector<sp_ctx*> lanes;
+  for (int i = 0; i < ngpu; i++) {
+    sp_ctx* c = ctx_create_one(devices[i]);
+    if (!c) {
+      for (sp_ctx* l : lanes) ctx_destroy_one(l);
+      return SP_ERR_CUDA;
+    }
+    lanes.push_back(c);
+  }
+  sp_ctx* P = lanes[0];
+  if (ngpu > 1) {
+    bool distinct = true;
+    for (int i = 0; i < ngpu; i++)
+      for (int j = 0; j < i; j++) distinct = distinct && devices[i] != devices[j];
+    const char* tr = getenv("SP_TRANSPORT");
+    const bool p2p = !distinct || (tr && std::string(tr) == "p2p");
+    int rc = guard(P, [&] {
+      if (p2p) {
+        for (int i = 0; i < ngpu; i++) {
+          lanes[i]->nranks = ngpu;
+          lanes[i]->rank = i;
+          lanes[i]->transport = SP_TRANSPORT_P2P;
+          // the records are copied onto the primary's device
+          if (i && devices[i] != devices[0]) {
+            int can = 0;
+            SP_CUDA(cudaDeviceCanAccessPeer(&can, devices[0], devices[i]));
+            if (can) {
+              SP_CUDA(cudaSetDevice(devices[0]));
+              cudaError_t e = cudaDeviceEnablePeerAccess(devices[i], 0);
+              if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+              else SP_CUDA(e);
+            }
+          }
+        }
+      } else {
+        sp::nccl_init_all(lanes);
+      }
+    });
+    if (rc != SP_OK) {
+      std::fprintf(stderr, "sp_ctx_create: %s\n", P->last_error.c_str());
+      for (sp_ctx* l : lanes) ctx_destroy_one(l);
+      return rc;
+    }
+    P->peers.assign(lanes.begin() + 1, lanes.end());
+    cudaSetDevice(devices[0]);
+  }
+  *out = P;
+  return SP_OK;
+}
+
+void sp_ctx_destroy(sp_ctx* ctx) {
+  if (!ctx) return;
+  for (sp_ctx* p : ctx->peers) ctx_destroy_one(p);
+  ctx->peers.clear();
+  ctx_destroy_one(ctx);
+}
+
+int sp_comm_unique_id(uint8_t* id) {
+  if (!id) return SP_ERR_CONFIG;
+  return guard(nullptr, [&] { sp::nccl_unique_id(id); });
+}
+
+int sp_ctx_comm_init(sp_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id) {
+  if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks) return SP_ERR_CONFIG;
+  if (!ctx->peers.empty() || ctx->comm) {
+    ctx->last_error = "context already has a communicator (multi-device or initialised)";
+    return SP_ERR_CONFIG;
+  }
+  return guard(ctx, [&] { sp::nccl_init_rank(ctx, nranks, rank, id); });
+}
+
+int sp_ctx_comm_info(const sp_ctx* ctx, int32_t* nranks, int32_t* rank, int32_t* ndev, int32_t* transport,
+                     int32_t* nccl_version) {
+  if (!ctx) return SP_ERR_CONFIG;
+  if (nranks) *nranks = ctx->nranks;
+  if (rank) *rank = ctx->rank;
+  if (ndev) *ndev = 1 + (int32_t)ctx->peers.size();
+  if (transport) *transport = ctx->transport;
+  if (nccl_version) {
+    *nccl_version = 0;
+    if (ctx->transport == SP_TRANSPORT_NCCL) {
+      try {
+        *nccl_version = sp::nccl_version();
+      } catch (const std::exception&) {
+      }
+    }
+  }
+  return SP_OK;
+}
+
 const char* sp_last_error(const sp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
 
 int sp_graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph** out) {
@@ -92,9 +182,15 @@ int sp_graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph** out) {
   int rc = guard(ctx, [&] {
     SP_CUDA(cudaSetDevice(ctx->device));
     sp::graph_upload(ctx, g, dg);
+    for (sp_ctx* p : ctx->peers) {  // the graph on every device of the context
+      dg->peers.push_back(new sp_dgraph());
+      SP_CUDA(cudaSetDevice(p->device));
+      sp::graph_upload(p, g, dg->peers.back());
+    }
+    SP_CUDA(cudaSetDevice(ctx->device));
   });
   if (rc != SP_OK) {
-    delete dg;
+    sp_graph_free(dg);
     return rc;
   }
   *out = dg;
@@ -103,6 +199,8 @@ int sp_graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph** out) {
 
 void sp_graph_free(sp_dgraph* dg) {
   if (!dg) return;
+  for (sp_dgraph* p : dg->peers) sp_graph_free(p);
+  dg->peers.clear();
   if (dg->ctx) {
     cudaSetDevice(dg->ctx->device);
     cudaStreamSynchronize(dg->ctx->stream);
@@ -150,10 +248,17 @@ int sp_tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t*
     SP_CUDA(cudaSetDevice(ctx->device));
     if (mesh->m < 1 || mesh->n < 1) throw sp::Error(SP_ERR_CONFIG, "mesh must be at least 1x1");
     sp::tables_build(ctx, dg, n_blocks, tmpl_off, tmpl_nodes, mesh, mu, chunk_size, t);
+    if (dg->peers.size() != ctx->peers.size()) throw sp::Error(SP_ERR_CONFIG, "graph was not uploaded by this context");
+    for (size_t i = 0; i < ctx->peers.size(); i++) {  // the tables on every device of the context
+      t->peers.push_back(new sp_tables());
+      SP_CUDA(cudaSetDevice(ctx->peers[i]->device));
+      sp::tables_build(ctx->peers[i], dg->peers[i], n_blocks, tmpl_off, tmpl_nodes, mesh, mu, chunk_size,
+                       t->peers.back());
+    }
+    SP_CUDA(cudaSetDevice(ctx->device));
   });
   if (rc != SP_OK) {
-    sp::tables_free_priv(t);
-    delete t;
+    sp_tables_free(t);
     return rc;
   }
   *out = t;
@@ -162,6 +267,8 @@ int sp_tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t*
 
 void sp_tables_free(sp_tables* t) {
   if (!t) return;
+  for (sp_tables* p : t->peers) sp_tables_free(p);
+  t->peers.clear();
   if (t->ctx) {
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
@@ -288,12 +395,11 @@ int sp_fold_stats(const sp_ctx* ctx, double* device_ms, int32_t* levels) {
 
 int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value) {
   if (!ctx) return SP_ERR_CONFIG;
-  if (option == SP_OPT_PREFIX_SKIP) {
-    ctx->skip = value ? 1 : 0;
-    return SP_OK;
-  }
-  if (option == SP_OPT_MEMO) {
-    ctx->memo = value ? 1 : 0;
+  if (option == SP_OPT_PREFIX_SKIP || option == SP_OPT_MEMO) {
+    for (size_t i = 0; i <= ctx->peers.size(); i++) {
+      sp_ctx* c = i ? ctx->peers[i - 1] : ctx;
+      (option == SP_OPT_PREFIX_SKIP ? c->skip : c->memo) = value ? 1 : 0;
+    }
     return SP_OK;
   }
   ctx->last_error = "unknown option";
@@ -328,8 +434,13 @@ int sp_copy_bytes(int64_t* h2d, int64_t* d2h) {
 
 int sp_launch_counts(const sp_ctx* ctx, int64_t* own_kernels, int64_t* cub_calls) {
   if (!ctx) return SP_ERR_CONFIG;
-  if (own_kernels) *own_kernels = ctx->own_launches;
-  if (cub_calls) *cub_calls = ctx->cub_calls;
+  int64_t own = ctx->own_launches, cub = ctx->cub_calls;
+  for (const sp_ctx* p : ctx->peers) {
+    own += p->own_launches;
+    cub += p->cub_calls;
+  }
+  if (own_kernels) *own_kernels = own;
+  if (cub_calls) *cub_calls = cub;
   return SP_OK;
 }
 

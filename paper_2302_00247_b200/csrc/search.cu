@@ -2572,6 +2572,8 @@ struct PendingScore {
   DevBuf<unsigned long long> dplan;
   DevBuf<ItemOut> items;
   DevBuf<sp_score_out> dout;
+  DevBuf<sp_score_out> gath;  // [nranks x nb] records of every lane (multi-GPU exchange)
+  bool lane = false;          // a peer lane of a multi-device search: collected by the primary
   DevBuf<ExplainBlock> dblk;
   DevBuf<int8_t> dnode, dedge;
   DevBuf<int64_t> deoff;
@@ -2821,13 +2823,14 @@ struct FusedExplain {
 // Enqueue scoring (+ k_reduce, + winner detail when `explain`) of
 // [lo[b], hi[b]) for every block; the buffers stay in the tables' pending
 // slot until score_finish collects them.
-static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
+// Returns false when this shard has no work item and `must_out` is false
+// (nothing launched); with `must_out` (a lane of a multi-GPU exchange) an
+// empty shard still produces its all-empty records.
+static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool must_out) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
   TablesPriv* priv = (TablesPriv*)t->priv;
   PendingScore& pd = priv->pending;
-  if (pd.active) throw Error(SP_ERR_CONFIG, "a search on these tables is already in flight");
-  pd.explain = explain;
   pd.empty = false;
   const size_t smem = score_smem(t);
   if (smem > ctx->smem_optin)
@@ -2897,10 +2900,13 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_sh
   }
   const unsigned long long n_items = base[nb];
   if (n_items == 0) {
-    pd.empty = true;
-    pd.active = true;
-    SP_CUDA(cudaEventRecord(pd.ev[5], s));
-    return;
+    if (!must_out) return false;
+    pd.dout.alloc(nb, s);
+    SP_CUDA(cudaMemsetAsync(pd.dout.p, 0, (size_t)nb * sizeof(sp_score_out), s));  // valid 0, has_best 0
+    SP_CUDA(cudaEventRecord(pd.ev[1], s));
+    SP_CUDA(cudaEventRecord(pd.ev[2], s));
+    SP_CUDA(cudaEventRecord(pd.ev[3], s));
+    return true;
   }
   // one small H2D for the plan: lo | hi | base | counter
   std::vector<unsigned long long> plan(3 * nb + 2, 0);
@@ -2924,6 +2930,18 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_sh
             dout.p);
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaEventRecord(pd.ev[3], s));
+  return true;
+}
+
+// Enqueue the winner detail (when `explain`) and the copy of the per-block
+// results (+ detail) into a pinned host block behind pd.dout.
+static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nb = t->n_blocks;
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  PendingScore& pd = priv->pending;
+  pd.explain = explain;
+  DevBuf<sp_score_out>& dout = pd.dout;
   if (explain) {
     // winner detail straight from the device-side argmin: no host round trip
     DevBuf<ExplainBlock>& dblk = pd.dblk;
@@ -2957,6 +2975,105 @@ static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_sh
                  (explain ? (int64_t)(nb * sizeof(ExplainBlock)) + 4 * ne + 2 * nedge : 0);
   SP_CUDA(cudaEventRecord(pd.ev[5], s));
   pd.active = true;
+}
+
+// Single-lane search (no exchange, or the caller exchanges on the host).
+static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
+  PendingScore& pd = ((TablesPriv*)t->priv)->pending;
+  pd.explain = explain;
+  if (!score_items(ctx, t, shard, n_shards, false)) {
+    pd.empty = true;
+    pd.active = true;
+    SP_CUDA(cudaEventRecord(pd.ev[5], ctx->stream));
+    return;
+  }
+  score_results(ctx, t, explain);
+}
+
+// Exact merge of the lanes' per-block records (search.py:337-343): the
+// lexicographic (total, num_split, index) minimum over the lanes that routed a
+// candidate (non-negative doubles order like their bit patterns), valid
+// counts summed.  One thread per block.
+__global__ void k_merge_ranks(const sp_score_out* __restrict__ gath, int32_t n, int64_t nb,
+                              sp_score_out* __restrict__ out) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    sp_score_out acc{};
+    for (int32_t r = 0; r < n; r++) {
+      const sp_score_out o = gath[(int64_t)r * nb + b];
+      acc.valid += o.valid;
+      if (!o.has_best) continue;
+      if (!acc.has_best ||
+          key_less((unsigned long long)__double_as_longlong(o.best_total), (uint32_t)o.best_num_split, o.best_index,
+                   (unsigned long long)__double_as_longlong(acc.best_total), (uint32_t)acc.best_num_split,
+                   acc.best_index)) {
+        acc.best_total = o.best_total;
+        acc.best_num_split = o.best_num_split;
+        acc.best_index = o.best_index;
+        acc.has_best = 1;
+      }
+    }
+    out[b] = acc;
+  }
+}
+
+static void pending_begin(sp_ctx* ctx, sp_tables* t) {
+  PendingScore& pd = ((TablesPriv*)t->priv)->pending;
+  if (pd.active) throw Error(SP_ERR_CONFIG, "a search on these tables is already in flight");
+  pd.ctx = ctx;
+  pd.events();
+  pd.release_host();
+  pd.lane = false;
+  SP_CUDA(cudaEventRecord(pd.ev[0], ctx->stream));
+}
+
+// Multi-GPU search: lane i scores shard rank_i of n, the lanes' records are
+// exchanged (one ncclAllGather, or peer copies onto the primary when the lanes
+// share a GPU) and merged on the device; the merged records get the winner
+// detail and go to the host on lanes[0]'s stream (and, with NCCL, on every
+// lane of `merge_all`: every rank of a process-per-GPU job ends with the
+// merged result).
+static void score_enqueue_lanes(const std::vector<sp_ctx*>& lanes, const std::vector<sp_tables*>& tl,
+                                const std::vector<int32_t>& ranks, int32_t n, bool explain) {
+  const int64_t nb = tl[0]->n_blocks;
+  const size_t rec = (size_t)nb * sizeof(sp_score_out);
+  for (size_t i = 0; i < lanes.size(); i++) {
+    SP_CUDA(cudaSetDevice(lanes[i]->device));
+    score_items(lanes[i], tl[i], ranks[i], n, true);
+  }
+  sp_ctx* P = lanes[0];
+  PendingScore& pp = ((TablesPriv*)tl[0]->priv)->pending;
+  if (P->transport == SP_TRANSPORT_NCCL) {
+    for (size_t i = 0; i < lanes.size(); i++) {
+      SP_CUDA(cudaSetDevice(lanes[i]->device));
+      PendingScore& pd = ((TablesPriv*)tl[i]->priv)->pending;
+      pd.gath.alloc((size_t)n * nb, lanes[i]->stream);
+    }
+    nccl_group_start();
+    for (size_t i = 0; i < lanes.size(); i++) {
+      PendingScore& pd = ((TablesPriv*)tl[i]->priv)->pending;
+      nccl_allgather(lanes[i], pd.dout.p, pd.gath.p, rec);
+    }
+    nccl_group_end();
+  } else {  // SP_TRANSPORT_P2P: lanes of this process, records copied onto the primary
+    SP_CUDA(cudaSetDevice(P->device));
+    pp.gath.alloc((size_t)n * nb, P->stream);
+    for (size_t i = 0; i < lanes.size(); i++) {
+      PendingScore& pd = ((TablesPriv*)tl[i]->priv)->pending;
+      if (i) SP_CUDA(cudaStreamWaitEvent(P->stream, pd.ev[3], 0));
+      SP_CUDA(cudaMemcpyPeerAsync(pp.gath.p + (size_t)ranks[i] * nb, P->device, pd.dout.p, lanes[i]->device, rec,
+                                  P->stream));
+    }
+  }
+  SP_CUDA(cudaSetDevice(P->device));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + THREADS - 1) / THREADS, 1024));
+  SP_LAUNCH(P, k_merge_ranks, grid, THREADS, 0, P->stream, pp.gath.p, n, nb, pp.dout.p);
+  SP_CUDA(cudaGetLastError());
+  score_results(P, tl[0], explain);
+  for (size_t i = 1; i < lanes.size(); i++) {  // peer lanes: collected with the primary
+    PendingScore& pd = ((TablesPriv*)tl[i]->priv)->pending;
+    pd.lane = true;
+    pd.active = true;
+  }
 }
 
 // Collect an enqueued search: wait for its own `done` event, then copy the
@@ -2997,12 +3114,28 @@ static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& r
 void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
   if (n_shards < 1 || shard < 0 || shard >= n_shards) throw Error(SP_ERR_CONFIG, "bad shard / n_shards");
   if (t->overflow) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
-  PendingScore& pd = ((TablesPriv*)t->priv)->pending;
-  if (pd.active) throw Error(SP_ERR_CONFIG, "a search on these tables is already in flight");
-  pd.ctx = ctx;
-  pd.events();
-  pd.release_host();
-  SP_CUDA(cudaEventRecord(pd.ev[0], ctx->stream));
+  if (!ctx->peers.empty()) {  // this process drives several devices
+    if (t->peers.size() != ctx->peers.size()) throw Error(SP_ERR_CONFIG, "tables were not built on every device");
+    std::vector<sp_ctx*> lanes{ctx};
+    std::vector<sp_tables*> tl{t};
+    std::vector<int32_t> ranks{0};
+    for (size_t i = 0; i < ctx->peers.size(); i++) {
+      lanes.push_back(ctx->peers[i]);
+      tl.push_back(t->peers[i]);
+      ranks.push_back((int32_t)i + 1);
+    }
+    for (size_t i = 0; i < lanes.size(); i++) {
+      SP_CUDA(cudaSetDevice(lanes[i]->device));
+      pending_begin(lanes[i], tl[i]);
+    }
+    score_enqueue_lanes(lanes, tl, ranks, (int32_t)lanes.size(), explain);
+    return;
+  }
+  pending_begin(ctx, t);
+  if (ctx->comm) {  // one process per GPU: this rank's share, NCCL exchange (also at nranks 1)
+    score_enqueue_lanes({ctx}, {t}, {ctx->rank}, ctx->nranks, explain);
+    return;
+  }
   score_enqueue(ctx, t, shard, n_shards, explain);
 }
 
@@ -3015,6 +3148,20 @@ void score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, void* xblocks, int
   float ms = 0;
   SP_CUDA(cudaEventElapsedTime(&ms, pd.ev[0], pd.ev[5]));
   ctx->score_ms = ms;
+  // peer lanes finished before the primary's records were merged; the search's
+  // kernel time is the slowest lane's
+  for (size_t i = 0; i < t->peers.size(); i++) {
+    PendingScore& pl = ((TablesPriv*)t->peers[i]->priv)->pending;
+    if (!pl.active || !pl.lane) continue;
+    pl.active = false;
+    pl.lane = false;
+    SP_CUDA(cudaSetDevice(ctx->peers[i]->device));
+    SP_CUDA(cudaEventSynchronize(pl.ev[2]));
+    float k = 0;
+    SP_CUDA(cudaEventElapsedTime(&k, pl.ev[1], pl.ev[2]));
+    ctx->score_kernel_ms = std::max<double>(ctx->score_kernel_ms, k);
+  }
+  SP_CUDA(cudaSetDevice(ctx->device));
   for (int64_t b = 0; b < nb; b++) {
     out[b] = res.empty() ? sp_score_out{} : res[b];
     out[b].candidates = t->hdr[b].C;

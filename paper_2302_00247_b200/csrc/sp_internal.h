@@ -140,6 +140,16 @@ struct sp_ctx {
   std::vector<std::pair<const void*, int>> smem_set;
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occupancy;
   std::vector<cudaEvent_t> event_pool;  // timing events of finished searches, reused
+  // multi-GPU (comm.cu).  Every device is a lane: this context's own
+  // communicator handle (ncclComm_t), its rank among `nranks`, and how the
+  // lanes exchange their per-block records (SP_TRANSPORT_*).  A context made
+  // by sp_ctx_create(ngpu > 1, ...) is the primary lane and drives the others
+  // (`peers`, devices[1..]); a process-per-GPU context has no peers and joins
+  // a communicator with sp_ctx_comm_init.
+  void* comm = nullptr;
+  int32_t nranks = 1, rank = 0;
+  int32_t transport = SP_TRANSPORT_NONE;
+  std::vector<sp_ctx*> peers;
 };
 
 namespace sp {
@@ -210,6 +220,7 @@ struct sp_dgraph {
   View<uint8_t> names, op, act_rank, w_rank, w_train;
   View<int64_t> name_off, topo, act_shape, act_bytes, w_shape, w_bytes, in_off;
   View<int32_t> in_idx;
+  std::vector<sp_dgraph*> peers;  // the same graph on every peer lane of a multi-device context
 };
 
 
@@ -304,6 +315,7 @@ struct sp_tables {
   sp::DevBuf<int64_t> d_tmpl_off;
   sp_dgraph* dg = nullptr;
   void* priv = nullptr;  // sp::TablesPriv (device maps used by explain)
+  std::vector<sp_tables*> peers;  // the same tables on every peer lane of a multi-device context
 };
 
 namespace sp {
@@ -324,4 +336,13 @@ void merge_key(sp_score_out* acc, const sp_score_out* o);
 void tables_free_priv(sp_tables* t);
 void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* blocks_out, int8_t* node_out,
                  int8_t* edge_out);
+// comm.cu: NCCL, loaded with dlopen on first use
+int nccl_version();
+void nccl_unique_id(uint8_t* out);
+void nccl_init_rank(sp_ctx* ctx, int nranks, int rank, const uint8_t* id);
+void nccl_init_all(const std::vector<sp_ctx*>& lanes);
+void nccl_destroy(sp_ctx* ctx);
+void nccl_group_start();
+void nccl_group_end();
+void nccl_allgather(sp_ctx* ctx, const void* send, void* recv, size_t bytes);
 }  // namespace sp

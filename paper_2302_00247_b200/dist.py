@@ -103,3 +103,39 @@ def allgather_exchange(group=None, device=None) -> Callable:
         return from_records(merge_records(parts))
 
     return exchange
+
+
+def init_comm(backend, rank: int, world: int, store=None) -> dict:
+    """Join `world` processes (one GPU each) in the library's own NCCL
+    communicator (sp_ctx_comm_init): afterwards every derive_plan on `backend`
+    scores this rank's share and merges the per-block records on the device
+    with one ncclAllGather -- no host exchange, no torch on the data path.
+
+    Only the 128-byte NCCL unique id has to travel, rank 0 -> the others, through
+    `store` (anything with set(key, bytes) / get(key) -> bytes, e.g. a
+    torch.distributed TCPStore); by default the store of the initialised
+    torch.distributed process group, else a TCPStore client of the launcher's
+    MASTER_ADDR/MASTER_PORT (torchrun's agent store)."""
+    if world <= 1:
+        return backend.comm
+    if store is None:
+        import torch.distributed as tdist
+
+        if tdist.is_available() and tdist.is_initialized():
+            store = tdist.distributed_c10d._get_default_store()
+        else:
+            import datetime
+            import os
+
+            agent = os.environ.get("TORCHELASTIC_USE_AGENT_STORE", "").lower() == "true"
+            store = tdist.TCPStore(os.environ.get("MASTER_ADDR", "127.0.0.1"), int(os.environ["MASTER_PORT"]),
+                                   world, is_master=(rank == 0 and not agent),
+                                   timeout=datetime.timedelta(seconds=300))
+    key = "shardsearch/nccl_unique_id"
+    if rank == 0:
+        uid = backend.comm_unique_id()
+        store.set(key, uid)
+    else:
+        uid = bytes(store.get(key))
+    backend.comm_init(world, rank, uid)
+    return backend.comm

@@ -685,14 +685,23 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
                 chunk_size: int = 4 << 20, jobs: int = 1, want_table: bool = False, *,
                 types: TypeSet = DEFAULT_TYPES, backend: Optional[Backend] = None,
                 session: Optional[Session] = None, cache: bool = True,
-                shard: int = 0, n_shards: int = 1, exchange: Optional[Callable] = None):
-    """Prune, search every unique block, assemble the whole-graph plan (search.py:348-379)."""
+                shard: int = 0, n_shards: int = 1, exchange: Optional[Callable] = None,
+                root_only: bool = True):
+    """Prune, search every unique block, assemble the whole-graph plan (search.py:348-379).
+
+    Multi-GPU: with a backend over several devices, or one joined to other
+    processes (Backend.comm_init), the library splits every block's work items
+    across the GPUs and merges the per-block argmin on the device (one NCCL
+    all-gather).  Every rank takes part in the search; with `root_only` only
+    rank 0 assembles the report and the other ranks return None.  (`shard`,
+    `n_shards`, `exchange`: the host-exchange form, kept for callers that
+    bring their own transport.)"""
     del jobs
     gc_was = gc.isenabled()
     gc.disable()  # the result is ~10^5 small objects: no collector pauses mid-search
     try:
         return _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
-                            backend, session, cache, shard, n_shards, exchange)
+                            backend, session, cache, shard, n_shards, exchange, root_only)
     finally:
         if gc_was:
             gc.enable()
@@ -735,7 +744,7 @@ def _block_groups(low: LoweredGraph, csr) -> list:
 
 
 def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types, backend, session,
-                 cache, shard, n_shards, exchange):
+                 cache, shard, n_shards, exchange, root_only=True):
     t0 = time.perf_counter()
     ses = session or Session.open(graph, backend, cache=cache)
     t1 = time.perf_counter()
@@ -781,6 +790,16 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
         for srch, _ in searches:
             srch.tables.close()
         raise
+    if root_only and not ses.backend.is_root:
+        # a non-root rank of a multi-process search: its share is scored and
+        # exchanged on the device; the report is rank 0's
+        try:
+            for srch, _ in searches:
+                srch.fetch()
+        finally:
+            for srch, _ in searches:
+                srch.tables.close()
+        return None
     # host work that does not depend on the winners overlaps the device search:
     # Subgraph objects, the static part of every RoutedPlan, and the member
     # scopes that receive each block's weight labels (search.py:374-376)

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(declared_functions()) == set(_native.EXPORTED_SYMBOLS)
     lib.sp_abi_version.restype = ctypes.c_int
-    assert lib.sp_abi_version() == 1
+    assert lib.sp_abi_version() == _native.ABI_VERSION == 2
 
 
 def test_missing_device_fails_loudly():
@@ -116,3 +116,33 @@ def test_blocks_to_subgraphs_roundtrip():
     off, nodes = ba.templates_csr()
     assert off[-1] == nodes.size == sum(len(s.template) for s in subs)
     assert np.all(np.diff(off) >= 1)
+
+
+def test_nccl_loads_on_demand_only():
+    """The library has no link-time NCCL dependency (dlopen on first use), and
+    the NCCL it would load exports what comm.cu resolves."""
+    import subprocess
+
+    from paper_2302_00247_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("backend not built")
+    deps = subprocess.run(["ldd", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "nccl" not in deps
+    nccl = ctypes.CDLL("libnccl.so.2")
+    for sym in ("ncclGetUniqueId", "ncclCommInitRank", "ncclCommInitAll", "ncclCommDestroy", "ncclAllGather",
+                "ncclGroupStart", "ncclGroupEnd", "ncclGetErrorString", "ncclGetVersion"):
+        assert hasattr(nccl, sym), sym
+
+
+def test_comm_unique_id_without_gpu():
+    """sp_comm_unique_id needs no device (rank 0 makes it before any context)."""
+    from paper_2302_00247_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("backend not built")
+    L = _native.load_library()
+    a = (ctypes.c_uint8 * _native.COMM_ID_BYTES)()
+    b = (ctypes.c_uint8 * _native.COMM_ID_BYTES)()
+    assert L.sp_comm_unique_id(a) == 0 and L.sp_comm_unique_id(b) == 0
+    assert bytes(a) != bytes(b)

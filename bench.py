@@ -189,7 +189,7 @@ def cpu_measure(workload: str, min_seconds: float, max_steps: int = 50) -> dict:
     from paper_2302_00247_b200.lowering import lower
 
     g, mesh = load_workload(workload)
-    low = lower(g)
+    low = lower(g, native=False)
     threads = os.cpu_count() or 1
     width = 4_000_000 if workload == "c5" else 0
     cpu_step(low, mesh, threads, width)  # warm (builds/loads the oracle)
@@ -208,14 +208,16 @@ def cpu_measure(workload: str, min_seconds: float, max_steps: int = 50) -> dict:
 
 
 def run_reference(args) -> None:
-    """The CPU arm: warm-up steps, then exactly `steps` timed steps on rank 0."""
+    """The CPU arm: warm-up steps, then exactly `steps` timed steps on rank 0.
+    Self-contained: the inputs are lowered by the numpy path (no native code of
+    this repo's package is loaded), the work is oracle/oracle.c's."""
     rank, _, _ = _dist_env()
     if rank != 0:
         return
     from paper_2302_00247_b200.lowering import lower
 
     g, mesh = load_workload(args.workload)
-    low = lower(g)
+    low = lower(g, native=False)
     threads = os.cpu_count() or 1
     width = 4_000_000 if args.workload == "c5" else 0
     for _ in range(args.warmup):
@@ -249,20 +251,24 @@ def run_reference(args) -> None:
 # GPU arm
 
 
-def measure(be, g, mesh, steps, warmup, rank, world, exchange, flush, barrier, skip,
-            want_e2e=True, clocks_dev=None) -> dict:
+def measure(be, g, mesh, steps, warmup, world, exchange, flush, barrier, skip, want_e2e=True,
+            clocks_dev=None, rank=0) -> dict:
+    """W warm-up + K timed `derive_plan` steps on the device-resident graph
+    (`times`), then K end-to-end steps from the host objects (`e2e_times`).
+    With the library's own multi-GPU communicator every rank runs the same
+    steps (the exchange is inside the search); only rank 0 gets a report."""
     from paper_2302_00247_b200 import search as sp_search
     from paper_2302_00247_b200.search import Session, derive_plan
 
     be.set_mode("skip" if skip else "walk")
     ses = Session.open(g, be)  # graph CSR resident in HBM before timing
+    kw = dict(shard=rank, n_shards=world, exchange=exchange) if exchange is not None else {}
 
     def step_resident():
-        return derive_plan(g, mesh, session=ses, shard=rank, n_shards=world, exchange=exchange)
+        return derive_plan(g, mesh, session=ses, **kw)
 
     def step_e2e():
-        return derive_plan(g, mesh, backend=be, cache=False, shard=rank, n_shards=world,
-                           exchange=exchange)
+        return derive_plan(g, mesh, backend=be, cache=False, **kw)
 
     ref = step_resident()
     for _ in range(warmup):
@@ -291,7 +297,8 @@ def measure(be, g, mesh, steps, warmup, rank, world, exchange, flush, barrier, s
         if sampler:
             sampler.__exit__(None, None, None)
     own1, cub1 = be.launch_counts()
-    assert rep.candidates == ref.candidates and rep.total_cost == ref.total_cost
+    if ref is not None:
+        assert rep.candidates == ref.candidates and rep.total_cost == ref.total_cost
     e2e_times = []
     h0, d0 = be.copy_bytes()
     if want_e2e:
@@ -301,7 +308,8 @@ def measure(be, g, mesh, steps, warmup, rank, world, exchange, flush, barrier, s
             be.timer_start()
             rep = step_e2e()
             e2e_times.append(be.timer_stop())
-        assert rep.total_cost == ref.total_cost
+        if ref is not None:
+            assert rep.total_cost == ref.total_cost
     h1, d1 = be.copy_bytes()
     return {"ref": ref, "ses": ses, "times": times, "e2e_times": e2e_times, "fold_ms": fold_ms,
             "score_ms": score_ms, "kern_ms": kern_ms, "phases": phases,
@@ -310,18 +318,28 @@ def measure(be, g, mesh, steps, warmup, rank, world, exchange, flush, barrier, s
             "clocks": sampler.summary() if sampler else None}
 
 
-#: committed `ncu --set full` summary of the dominant kernel (tools/summarize_ncu.py)
-PROFILE = "r1_k_score_c5_walk.txt"
+#: committed `ncu --set full` summary of the dominant kernel (tools/summarize_ncu.py);
+#: its header records the sha256 of the kernel's SASS, so the instruction count is
+#: only used while the kernel binary is the one that was profiled
+PROFILE = "r2_k_score_c5_walk.txt"
+#: the dominant kernel of the brute-force step (k_score_flow<walk, pair>)
+KERNEL_SASS_NAME = "k_score_flowILb0ELb1EE"
 _UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "%": 1, "ms": 1, "cycle": 1}
 
 
 def _profile_values(path: str) -> dict:
-    """metric -> value (bytes scaled to B) from a profiles/ summary file."""
+    """metric -> value (bytes scaled to B) from a profiles/ summary file; header
+    lines `# key: value` come back as strings under `#key`."""
     vals = {}
     if not os.path.exists(path):
         return vals
     for ln in open(path):
-        if " = " in ln and not ln.startswith("#"):
+        if ln.startswith("#"):
+            if ":" in ln:
+                k, v = ln[1:].split(":", 1)
+                vals["#" + k.strip()] = v.strip()
+            continue
+        if " = " in ln:
             k, v = ln.split(" = ", 1)
             parts = v.split()
             try:
@@ -329,6 +347,28 @@ def _profile_values(path: str) -> dict:
             except ValueError:
                 pass
     return vals
+
+
+def kernel_sass_sha(name: str = KERNEL_SASS_NAME) -> str | None:
+    """sha256 of the SASS of the one kernel whose mangled name contains `name`
+    in the built library (cuobjdump), with the per-build unnamed-namespace hash
+    stripped: identical for identical machine code."""
+    import hashlib
+    import re
+
+    from paper_2302_00247_b200._native import LIB_PATH
+
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", LIB_PATH], capture_output=True, text=True, timeout=120).stdout
+    except (OSError, subprocess.TimeoutExpired):
+        return None
+    blocks = re.split(r"\n\s*Function : ", out)
+    for b in blocks[1:]:
+        head, _, body = b.partition("\n")
+        if name in head:
+            body = re.sub(r"_GLOBAL__N__[0-9a-f_]+", "_GLOBAL__N_", body)
+            return hashlib.sha256(body.encode()).hexdigest()
+    return None
 
 
 def _maxsum(vals, world):
@@ -344,17 +384,111 @@ def _maxsum(vals, world):
     return s
 
 
+def _subset_csr(off, nodes, ids):
+    import numpy as np
+
+    ids = np.asarray(ids, np.int64)
+    T = off[ids + 1] - off[ids]
+    goff = np.zeros(len(ids) + 1, np.int64)
+    np.cumsum(T, out=goff[1:])
+    gather = np.repeat(off[ids] - goff[:-1], T) + np.arange(goff[-1])
+    return goff, np.ascontiguousarray(nodes[gather])
+
+
+def gpu_on_cpu_sample(be, g, mesh, reps: int = 5) -> dict:
+    """The GPU on exactly the CPU arm's bounded sample of c5 (cpu_step): the fold,
+    every block <= 2e6 candidates in full (one batched search), and 8 slices of
+    4e6 candidates at k*C/8 of each larger block (sp_score_range) -- device time
+    of the whole sample (timer on the backend stream), best of `reps`, so
+    cpu_baseline compares like with like."""
+    from paper_2302_00247_b200.search import Session, fold_blocks
+
+    be.set_mode("walk")
+    ses = Session.open(g, be)
+    best = walked = None
+    for _ in range(reps + 1):
+        be.timer_start()
+        ba = fold_blocks(ses.low, 2, session=ses)
+        off, nodes = ba.templates_csr()
+        t = be.tables(ses.dgraph, off, nodes, mesh, 1 << 20, 4 << 20)
+        cands = [int(c) for c in t.candidates]
+        t.close()
+        small = [b for b, C in enumerate(cands) if C <= 2_000_000]
+        big = [b for b, C in enumerate(cands) if C > 2_000_000]
+        n = sum(cands[b] for b in small)
+        ts = be.tables(ses.dgraph, *_subset_csr(off, nodes, small), mesh, 1 << 20, 4 << 20)
+        try:
+            be.score(ts)
+        finally:
+            ts.close()
+        for b in big:
+            tb = be.tables(ses.dgraph, *_subset_csr(off, nodes, [b]), mesh, 1 << 20, 4 << 20)
+            try:
+                C = cands[b]
+                for k in range(8):
+                    lo = k * C // 8
+                    hi = min(C, lo + 4_000_000)
+                    be.score_range(tb, 0, lo, hi)
+                    n += hi - lo
+            finally:
+                tb.close()
+        ms = be.timer_stop()
+        walked = n
+        best = ms if best is None or ms < best else best
+    return {"walked": walked, "ms": best}
+
+
+def fold_roofline(be, layers: int, peaks: dict) -> dict:
+    """Folding is the HBM-bound stage: prune_graph of a `layers`-layer
+    transformer stack (14 GraphNodes per layer) on the device, compulsory bytes
+    (tools/fold_scale.py: graph arrays read once + per-depth hashes written and
+    read once) over the device time of the level loop (CUDA events)."""
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from fold_scale import compulsory_bytes
+
+    from paper_2302_00247_b200.workloads import transformer_stack_lowered
+
+    low = transformer_stack_lowered(layers)
+    dg = be.upload(low)
+    be.fold(dg, 2)
+    dev = []
+    for _ in range(3):
+        be.fold(dg, 2)
+        dev.append(be.timings()["fold_device_ms"])
+    depth = max(nm.count("/") + 1 for nm in (low.names[0], low.names[2], low.names[-1]))
+    cb = compulsory_bytes(low, depth)
+    ms = float(np.median(dev))
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = cb / (ms * 1e-3) / 1e9
+    vals = _profile_values(os.path.join(ROOT, "profiles", FOLD_PROFILE))
+    traffic = vals.get("dram_bytes_total")
+    del dg
+    return {"kernel": "fold level loop (all kernels)", "bound": "hbm", "nodes": len(low.op),
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "algorithmic_bytes": cb, "device_ms": ms,
+            "traffic": traffic, "traffic_source": f"profiles/{FOLD_PROFILE}" if traffic else None}
+
+
+FOLD_PROFILE = "r2_fold_10m_launches.txt"
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
 
     from paper_2302_00247_b200._native import Backend
-    from paper_2302_00247_b200.dist import allgather_exchange
+    from paper_2302_00247_b200.dist import allgather_exchange, init_comm
 
     rank, world, local = _dist_env()
-    # one process per GPU; SP_DIST_BACKEND=gloo (+ fewer GPUs than ranks) only
-    # exercises the multi-rank plumbing on a single-GPU box, it is not a measurement
+    # one process per GPU.  The search's exchange is the library's own NCCL
+    # communicator (sp_ctx_comm_init); torch.distributed is only the harness's
+    # barrier / max-over-ranks and the bootstrap store for the NCCL id.
+    # SP_BENCH_EXCHANGE=host (+ SP_DIST_BACKEND=gloo, fewer GPUs than ranks)
+    # only exercises the host-exchange plumbing on one GPU; not a measurement.
     backend = os.environ.get("SP_DIST_BACKEND", "nccl")
+    host_exchange = os.environ.get("SP_BENCH_EXCHANGE") == "host"
     device = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(device)
     if world > 1:
@@ -362,8 +496,14 @@ def run_ours(args) -> None:
             dist.init_process_group("nccl", device_id=torch.device("cuda", device))
         else:
             dist.init_process_group(backend)
-    exchange = allgather_exchange() if world > 1 else None
     be = Backend(device)
+    exchange = None
+    if world > 1:
+        if host_exchange:
+            exchange = allgather_exchange()
+        else:
+            init_comm(be, rank, world)
+    comm = be.comm_info()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
 
     def barrier():
@@ -372,66 +512,78 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
 
     g, mesh = load_workload(args.workload)
-    main = measure(be, g, mesh, args.steps, args.warmup, rank, world, exchange, flush, barrier,
-                   skip=False, clocks_dev=device)
-    cands = main["ref"].candidates
+    main = measure(be, g, mesh, args.steps, args.warmup, world, exchange, flush, barrier,
+                   skip=False, clocks_dev=device, rank=rank)
     total_ms = _maxsum(main["times"], world)
     e2e_ms = _maxsum(main["e2e_times"], world)
-    value = cands * args.steps / (total_ms / 1000.0)
-    e2e_value = cands * args.steps / (e2e_ms / 1000.0)
-    walked_valid = main["ref"].valid
-
-    skip = measure(be, g, mesh, args.steps, args.warmup, rank, world, exchange, flush, barrier,
-                   skip=True, want_e2e=True)
+    skip = measure(be, g, mesh, args.steps, args.warmup, world, exchange, flush, barrier,
+                   skip=True, want_e2e=True, rank=rank)
     skip_ms = _maxsum(skip["times"], world)
     skip_e2e_ms = _maxsum(skip["e2e_times"], world)
-
+    kern = statistics.median(main["kern_ms"])
+    kern_max = _maxsum([kern], world)
     extra = {}
     if args.workload == "c5":
         g2, mesh2 = load_workload("c2")
-        c2 = measure(be, g2, mesh2, 20, 5, rank, world, exchange, flush, barrier, skip=False)
+        c2 = measure(be, g2, mesh2, 20, 5, world, exchange, flush, barrier, skip=False, rank=rank)
         c2ms, c2e = _maxsum(c2["times"], world), _maxsum(c2["e2e_times"], world)
-        extra["c2"] = {"workload": WORKLOADS["c2"][0], "candidates_per_step": c2["ref"].candidates,
-                       "value": c2["ref"].candidates * 20 / (c2ms / 1000.0),
-                       "e2e_value": c2["ref"].candidates * 20 / (c2e / 1000.0),
-                       "ms_per_step": c2ms / 20, "e2e_ms_per_step": c2e / 20}
-
-    # roofline of the dominant kernel (k_score, brute force): algorithmic bytes per
-    # launch = routing tables staged per block + 32 B per work item (one ItemOut;
-    # items are 256 x 256 candidates at this size) + 40 B per block
-    kern = statistics.median(main["kern_ms"])
-    ses = main["ses"]
-    nb = len(main["ref"].results)
-    items = sum((r.candidates + 65535) // 65536 for r in main["ref"].results)
-    alg_bytes = getattr(ses, "last_table_bytes", 0) + 32 * items + 40 * nb
+        if rank == 0:
+            extra["c2"] = {"workload": WORKLOADS["c2"][0], "candidates_per_step": c2["ref"].candidates,
+                           "value": c2["ref"].candidates * 20 / (c2ms / 1000.0),
+                           "e2e_value": c2["ref"].candidates * 20 / (c2e / 1000.0),
+                           "ms_per_step": c2ms / 20, "e2e_ms_per_step": c2e / 20}
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    cands = main["ref"].candidates
+    value = cands * args.steps / (total_ms / 1000.0)
+    e2e_value = cands * args.steps / (e2e_ms / 1000.0)
+    walked_valid = main["ref"].valid
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             peaks = json.load(fh)
     except OSError:
         pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = alg_bytes / (kern / 1000.0) / 1e9 if kern > 0 else 0.0
-    kernel_rate = cands / world / (kern / 1000.0) if kern > 0 else 0.0
+    nb = len(main["ref"].results)
 
-    # SM issue-slot roofline of k_score: warp-instructions per candidate from the
-    # committed ncu capture of the same kernel x the live kernel rate, against
-    # 148 SMs x 4 schedulers x the SM clock sampled during the timed region
-    issue = None
+    # roofline of the dominant kernel (k_score_flow, brute force).  It reads no
+    # per-candidate input from HBM (tables staged once per block into shared
+    # memory), so its bound is SM issue slots: warp-instructions per candidate
+    # (ncu capture of the same kernel binary, checked by SASS hash) x the live
+    # kernel rate (CUDA events on the backend stream, this run), against
+    # 148 SMs x 4 schedulers x the SM clock sampled during the timed region.
+    kernel_rate = cands / world / (kern_max / 1000.0) if kern_max > 0 else 0.0
+    ses = main["ses"]
+    items = sum((r.candidates + 65535) // 65536 for r in main["ref"].results)
+    alg_bytes = getattr(ses, "last_table_bytes", 0) + 32 * items + 40 * nb
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_achieved = alg_bytes / (kern / 1000.0) / 1e9 if kern > 0 else 0.0
+    prof = _profile_values(os.path.join(ROOT, "profiles", PROFILE)) if args.workload == "c5" else {}
+    sha_now = kernel_sass_sha()
+    sha_prof = prof.get("#sass_sha256")
     traffic = None
-    prof = os.path.join(ROOT, "profiles", PROFILE)
-    vals = _profile_values(prof) if args.workload == "c5" else {}
-    if "dram__bytes_read.sum" in vals and "dram__bytes_write.sum" in vals:
-        # one `ncu --set full` capture of the same kernel (one launch = one step)
-        traffic = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
-    if vals and main["clocks"] and main["clocks"]["sm_mhz"]:
-        wipc = vals["smsp__inst_executed.sum"] / cands
-        peak_issue = 148 * 4 * main["clocks"]["sm_mhz"] * 1e6
-        issue = {"bound": "issue", "unit": "warp-inst/s", "warp_inst_per_candidate": wipc,
-                 "achieved": wipc * kernel_rate, "peak": peak_issue,
-                 "frac": wipc * kernel_rate / peak_issue,
-                 "ncu_issue_active_frac": vals["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100,
-                 "source": f"profiles/{PROFILE} (instruction count) x live kernel time"}
+    if "dram__bytes_read.sum" in prof and "dram__bytes_write.sum" in prof:
+        traffic = prof["dram__bytes_read.sum"] + prof["dram__bytes_write.sum"]
+    sm_mhz = (main["clocks"] or {}).get("sm_mhz") or 1965.0
+    peak_issue = 148 * 4 * sm_mhz * 1e6
+    roof = {"kernel": "k_score_flow<walk,pair>", "bound": "issue", "unit": "warp-inst/s", "peak": peak_issue,
+            "achieved": None, "frac": None, "traffic": traffic,
+            "kernel_ms": kern, "kernel_candidates_per_s_per_gpu": kernel_rate,
+            "sass_sha256": sha_now, "profile": f"profiles/{PROFILE}",
+            "hbm": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm_peak, "frac": hbm_achieved / hbm_peak,
+                    "algorithmic_bytes": alg_bytes,
+                    "note": "no per-candidate HBM input: staged routing tables + 32 B per work item + 40 B per block"}}
+    if prof.get("smsp__inst_executed.sum") and sha_now and sha_now == sha_prof:
+        wipc = prof["smsp__inst_executed.sum"] / float(prof.get("#candidates", cands))
+        roof.update(achieved=wipc * kernel_rate, frac=wipc * kernel_rate / peak_issue,
+                    warp_inst_per_candidate=wipc,
+                    ncu_issue_active_frac=prof.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0) / 100)
+    else:
+        roof["note"] = ("instruction count unavailable for this kernel binary (SASS hash "
+                        f"{(sha_now or 'n/a')[:12]} != profiled {(sha_prof or 'n/a')[:12]}): frac not reported")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -440,27 +592,25 @@ def run_ours(args) -> None:
         "config": {"workload": WORKLOADS[args.workload][0], "candidates_per_step": cands,
                    "valid_plans_per_step": walked_valid, "blocks": nb, "graph_nodes": len(g.nodes),
                    "mesh": WORKLOADS[args.workload][3], "min_dup": 2, "scoring": "brute force (no prefix skipping)",
-                   "parallelism": f"candidate-range shards x{world}",
+                   "parallelism": (f"candidate work items dealt over {world} ranks, per-block records merged "
+                                   f"on the device after one in-library ncclAllGather" if world > 1 and not host_exchange
+                                   else f"candidate-range shards x{world}"),
                    "l2": "flushed between steps (256 MiB write)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": main["h2d"],
                 "d2h_bytes_per_step": main["d2h"]},
         "gpu_launches": int(round(main["launches"] * args.steps)),
         "gpu_launches_detail": {"own_kernels_per_step": main["launches"],
                                 "cub_calls_per_step": main["cub"]},
+        "comm": comm,
         "host_phases_ms": {k: statistics.median(p[k] for p in main["phases"])
-                           for k in main["phases"][0]},
+                           for k in main["phases"][0]} if main["phases"] and main["phases"][0] else {},
         "breakdown_ms": {"fold": statistics.median(main["fold_ms"]),
                          "score_total": statistics.median(main["score_ms"]),
                          "score_kernel": kern, "step": statistics.median(main["times"]),
                          "e2e_step": statistics.median(main["e2e_times"])},
         "kernel_rate": {"k_score_candidates_per_s_per_gpu": kernel_rate,
                         "valid_plans_per_s": walked_valid * args.steps / (total_ms / 1000.0)},
-        "roofline": {"kernel": "k_score_flow", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
-                     "note": "no per-candidate HBM input: algorithmic bytes are the staged "
-                             "routing tables + per-item records, so the kernel is SM-issue-bound; "
-                             "issue-slot utilisation is in profiles/ (DESIGN.md section 3)"},
-        "issue_roofline": issue,
+        "roofline": roof,
         "prefix_skip": {"value": cands * args.steps / (skip_ms / 1000.0),
                         "e2e_value": cands * args.steps / (skip_e2e_ms / 1000.0),
                         "ms_per_step": skip_ms / args.steps,
@@ -471,14 +621,42 @@ def run_ours(args) -> None:
         "clocks": main["clocks"],
     }
     line.update(extra)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_fold_roofline:
+        line["fold_roofline"] = fold_roofline(be, args.fold_layers, peaks)
+    if world == 1 and not args.no_cpu_baseline:
         cb = cpu_measure(args.workload, args.cpu_seconds)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+        if args.workload == "c5":
+            sample = gpu_on_cpu_sample(be, g, mesh)
+            line["cpu_baseline"]["gpu_same_sample"] = {
+                "candidates": sample["walked"], "ms": sample["ms"], "unit": UNIT,
+                "value": sample["walked"] / (sample["ms"] / 1000.0),
+                "note": "the GPU on the same bounded sample (fold, blocks <= 2e6 in full, 8 slices of 4e6 "
+                        "of each larger block; brute force), device time on the backend stream"}
+    if world == 1 and not args.no_python_reference:
+        try:
+            pr = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "time_python_reference.py")],
+                                capture_output=True, text=True, timeout=600)
+            line["python_reference"] = json.loads(pr.stdout.strip().splitlines()[-1])
+            line["python_reference"]["kind"] = "python-reference"
+        except Exception as exc:  # noqa: BLE001
+            line["python_reference"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+    print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _self_launch(args) -> None:
+    """`bench.py --gpus N` outside a launcher: re-run under torchrun, one rank per GPU."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main() -> None:
@@ -490,9 +668,14 @@ def main() -> None:
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="c5")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-python-reference", action="store_true")
+    ap.add_argument("--no-fold-roofline", action="store_true")
+    ap.add_argument("--fold-layers", type=int, default=700000)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

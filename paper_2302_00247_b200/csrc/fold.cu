@@ -76,9 +76,12 @@ __global__ void k_depth(const int64_t* __restrict__ off, const uint8_t* __restri
 }
 
 // Per node and depth d: prefix end, prefix hash, rel-name hash.
+// Output element of (node i, depth dd) at i*si + dd*sd: node-major (si = D,
+// sd = 1) or level-major (si = 1, sd = n: one depth's values of all nodes are
+// contiguous, so a level pass reads them coalesced).
 __device__ __forceinline__ void name_hash_one(int64_t i, const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
                             int32_t D, uint64_t seed, int32_t* __restrict__ pend,
-                            uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
+                            uint64_t* __restrict__ ph, uint64_t* __restrict__ rh, int64_t si, int64_t sd) {
   const uint8_t* p = s + off[i];
   const int64_t L = off[i + 1] - off[i];
   uint64_t h = 0;
@@ -100,7 +103,7 @@ __device__ __forceinline__ void name_hash_one(int64_t i, const int64_t* __restri
   const uint64_t hall = h;
   const int dn = d;  // node depth
   for (int dd = 0; dd < D; dd++) {
-    const int64_t idx = i * D + dd;
+    const int64_t idx = i * si + dd * sd;
     if (dd >= dn || dd >= 64) {
       pend[idx] = (int32_t)L;
       ph[idx] = 0;
@@ -130,7 +133,15 @@ __global__ void k_name_hash(const int64_t* __restrict__ off, const uint8_t* __re
                             uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    name_hash_one(i, off, s, n, D, seed, pend, ph, rh);
+    name_hash_one(i, off, s, n, D, seed, pend, ph, rh, D, 1);
+}
+
+__global__ void k_name_hash_lm(const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
+                               int32_t D, uint64_t seed, int32_t* __restrict__ pend,
+                               uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    name_hash_one(i, off, s, n, D, seed, pend, ph, rh, 1, n);
 }
 
 __global__ void k_gather_keys(const int32_t* __restrict__ act, int64_t nA, const uint64_t* __restrict__ src,
@@ -532,7 +543,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     int32_t d = 1;
     for (int64_t k = a.name_off[i]; k < a.name_off[i + 1]; k++) d += a.names[k] == '/';
     a.depth[i] = d;
-    name_hash_one(i, a.name_off, a.names, a.n, D, a.seed, a.pend, a.ph, a.rh);
+    name_hash_one(i, a.name_off, a.names, a.n, D, a.seed, a.pend, a.ph, a.rh, D, 1);
     a.gparent[i] = 0;
     a.residual[i] = 0;
     a.cur[i] = -1;
@@ -894,27 +905,33 @@ __global__ void k_gather(const int32_t* __restrict__ idx, int64_t m, const T* __
 // exact unless two components of one class agree on 16 bytes (then the tie
 // flag sends the whole fold to the host ordering below).
 
-__device__ __forceinline__ uint64_t be_load8(const uint8_t* p, int64_t len) {
-  uint64_t k = 0;
-  for (int b = 0; b < 8; b++) k = (k << 8) | (b < len ? (uint64_t)p[b] : 0ULL);
-  return k;
-}
 
 __global__ void k_acc_keys(const int32_t* __restrict__ accG, int64_t Ga, const int32_t* __restrict__ sorted,
                            const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass,
-                           const int32_t* __restrict__ pend, int32_t D, int32_t dd,
+                           const int32_t* __restrict__ pend, int64_t ps, int64_t pd, int32_t dd,
                            const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
                            uint64_t* __restrict__ k0, uint64_t* __restrict__ k1, uint32_t* __restrict__ kc,
                            uint8_t* __restrict__ longc, int32_t* __restrict__ idx) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < Ga; j += (int64_t)gridDim.x * blockDim.x) {
     const int32_t g = accG[j];
     const int32_t h = sorted[gstart[g]];
-    const int64_t pe = pend[(int64_t)h * D + dd];
-    const int64_t ps = dd > 0 ? (int64_t)pend[(int64_t)h * D + dd - 1] + 1 : 0;
-    const int64_t len = pe > ps ? pe - ps : 0;
-    const uint8_t* c = names + name_off[h] + ps;
-    k0[j] = be_load8(c, len);
-    k1[j] = be_load8(c + 8, len - 8);
+    const int64_t pe = pend[(int64_t)h * ps + dd * pd];
+    const int64_t p0 = dd > 0 ? (int64_t)pend[(int64_t)h * ps + (dd - 1) * pd] + 1 : 0;
+    const int64_t len = pe > p0 ? pe - p0 : 0;
+    const uint8_t* c = names + name_off[h] + p0;
+    // first 16 component bytes, big-endian, zero padded.  (A shift-accumulate
+    // helper called twice, `k = k << 8 | (b < len ? p[b] : 0)`, came out of
+    // nvcc 12.9 -O3 for sm_100a with stray copies of bytes 2..4 in bytes 4..6
+    // for some inputs -- instance orders flipped; tools/diag_fold.py A/B.)
+    uint64_t a = 0, b = 0;
+    const int64_t m = len < 16 ? len : 16;
+    for (int64_t q = 0; q < m; q++) {
+      const uint64_t x = c[q];
+      if (q < 8) a |= x << (56 - 8 * q);
+      else b |= x << (120 - 8 * q);
+    }
+    k0[j] = a;
+    k1[j] = b;
     kc[j] = (uint32_t)gclass[g];
     longc[j] = len > 16;
     idx[j] = (int32_t)j;
@@ -1010,12 +1027,12 @@ __global__ void k_acc_members(int64_t total, int64_t K, const int64_t* __restric
 
 __global__ void k_acc_insts(int64_t Ga, const int32_t* __restrict__ order, const int32_t* __restrict__ accG,
                             const int32_t* __restrict__ gstart, const int32_t* __restrict__ sorted,
-                            const int32_t* __restrict__ pend, int32_t D, int32_t dd, int32_t* __restrict__ inode,
-                            int32_t* __restrict__ ilen) {
+                            const int32_t* __restrict__ pend, int64_t ps, int64_t pd, int32_t dd,
+                            int32_t* __restrict__ inode, int32_t* __restrict__ ilen) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < Ga; p += (int64_t)gridDim.x * blockDim.x) {
     const int32_t h = sorted[gstart[accG[order[p]]]];
     inode[p] = h;
-    ilen[p] = pend[(int64_t)h * D + dd];
+    ilen[p] = pend[(int64_t)h * ps + dd * pd];
   }
 }
 
@@ -1050,12 +1067,12 @@ static T d2h_scalar(const T* p, cudaStream_t s) {
 
 // Accepted classes of one level -> blocks (device arrays); sets *tie when two
 // instance components of one class agree on their first 16 bytes.
+// pend of (node h, depth d) at h*ps + d*pd (node- or level-major, see name_hash_one).
 static void level_blocks(sp_ctx* ctx, sp_dgraph* dg, int32_t dd, int64_t nA, int64_t nG, const int32_t* sorted,
                          const int32_t* gstart, const int32_t* gclass, const uint8_t* gaccept, const int32_t* pend,
-                         int32_t* d_tie, LevelBlocks& L) {
+                         int64_t ps, int64_t pd, int32_t* d_tie, LevelBlocks& L) {
   cudaStream_t s = ctx->stream;
   const int sms = ctx->sm_count;
-  const int32_t D = dg->max_depth;
   DevBuf<int32_t> iota, accG, nsel;
   iota.alloc(nG, s);
   accG.alloc(nG, s);
@@ -1079,7 +1096,7 @@ static void level_blocks(sp_ctx* ctx, sp_dgraph* dg, int32_t dd, int64_t nA, int
   longc.alloc(Ga, s);
   idx.alloc(Ga, s); o1.alloc(Ga, s); o2.alloc(Ga, s);
   const int gA = grid_for(Ga, sms);
-  SP_LAUNCH(ctx, k_acc_keys, gA, 256, 0, s, accG.p, Ga, sorted, gstart, gclass, pend, D, dd, dg->name_off.p,
+  SP_LAUNCH(ctx, k_acc_keys, gA, 256, 0, s, accG.p, Ga, sorted, gstart, gclass, pend, ps, pd, dd, dg->name_off.p,
             dg->names.p, k0.p, k1.p, kc.p, longc.p, idx.p);
   // LSD: component bytes 8..15, then 0..7, then class (stable)
   auto sort_pairs = [&](auto* kin, auto* kout, const int32_t* vin, int32_t* vout, int bits) {
@@ -1157,7 +1174,7 @@ static void level_blocks(sp_ctx* ctx, sp_dgraph* dg, int32_t dd, int64_t nA, int
   L.ilen.alloc(Ga, s);
   SP_LAUNCH(ctx, k_acc_members, grid_for(M, sms), 256, 0, s, M, K, moff.p, coff.p, L.cls_start.p, L.cls_T.p, order,
             accG.p, gstart, sorted, canon.p, L.members.p);
-  SP_LAUNCH(ctx, k_acc_insts, gA, 256, 0, s, Ga, order, accG.p, gstart, sorted, pend, D, dd, L.inode.p, L.ilen.p);
+  SP_LAUNCH(ctx, k_acc_insts, gA, 256, 0, s, Ga, order, accG.p, gstart, sorted, pend, ps, pd, dd, L.inode.p, L.ilen.p);
 }
 
 // Host ordering: the string-order decisions of pruning.py:136-148, 200 over
@@ -1666,7 +1683,7 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
     // accepted classes -> blocks, assembled on the device
     if (device_blocks) {
       lblocks.emplace_back();
-      level_blocks(ctx, dg, dd, nA, nG, sorted2.p, gstart.p, gclass.p, gaccept.p, pend.p, tie.p, lblocks.back());
+      level_blocks(ctx, dg, dd, nA, nG, sorted2.p, gstart.p, gclass.p, gaccept.p, pend.p, D, 1, tie.p, lblocks.back());
       tr.mark("level: blocks");
     }
     reserve(st_sorted, used_a, nA);
@@ -1756,15 +1773,574 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
   fold_finalize(dg, levels, resid_h, pend_h, D, out);
 }
 
+
+// ---------------------------------------------------------------------------
+// Hash-grouped fold (multi-kernel path).  The level algorithm above with its
+// sorts replaced by hash tables, every node pass in node order (coalesced):
+//   * groups: open-addressing table keyed by the level's 64-bit prefix hash
+//     (k_hg_insert; the CAS winner is the group's head), sizes and template-key
+//     sums aggregated per warp (k_hg_entry), compact group ids by a scan of the
+//     head flags in node order (k_hg_ids);
+//   * classes: a second table keyed by (parent group, key sum, size)
+//     (k_hc_insert / k_hc_count);
+//   * member segments (a counting scatter) and the canonical member order
+//     (rank of the relative-name hash inside the group, k_hg_rank) only for
+//     groups whose class has >= 2 groups or is accepted -- the huge top-level
+//     groups of a deep graph are neither;
+//   * exact verification (prefix bytes vs the group head; member by member vs
+//     the class head group, including the parent) and accept/descend in one
+//     node pass each.
+// Hash collisions are detected exactly as before (the fold reruns with a new
+// seed); a multi-group class with groups larger than RANK_MAX falls back to
+// the sort-based path.  Per level: two host syncs (the group count after the
+// insert, the level's counters after accept).
+
+constexpr int64_t RANK_MAX = 1024;
+
+struct HashStats {  // device counters of one level
+  int32_t nG, overflow, nC, nnext, nacc, big, pad0, pad1;
+};
+
+__device__ __forceinline__ uint64_t nz64(uint64_t k) { return k ? k : 0x9e3779b97f4a7c15ULL; }
+
+// one pass over the nodes active at `level`: find-or-insert the prefix hash
+// Overflow (more keys than half the capacity, or a probe run longer than
+// max_probe) stops every thread at its next node: the host retries the level
+// with a table of 2 x the active count.
+__global__ void k_hg_insert(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                            const uint64_t* __restrict__ ph, unsigned long long* __restrict__ tkey,
+                            int32_t* __restrict__ thead, uint32_t mask, uint32_t max_probe,
+                            uint32_t* __restrict__ nslot, HashStats* __restrict__ st) {
+  volatile int32_t* overflow = &st->overflow;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (alive[v] != level) continue;
+    if (*overflow) return;
+    const unsigned long long key = nz64(ph[v]);
+    uint32_t h = (uint32_t)(key >> 17) & mask;
+    for (uint32_t probe = 0;; probe++) {
+      unsigned long long k = tkey[h];
+      if (k == 0) {
+        k = atomicCAS(&tkey[h], 0ULL, key);
+        if (k == 0) {
+          thead[h] = (int32_t)v;
+          if ((uint32_t)atomicAdd(&st->nG, 1) >= (mask + 1) / 2) *overflow = 1;
+          break;
+        }
+      }
+      if (k == key) break;
+      h = (h + 1) & mask;
+      if (probe >= max_probe) {
+        *overflow = 1;
+        return;
+      }
+    }
+    nslot[v] = h;
+  }
+}
+
+// template-key entry hash per node (rel name, op, weight, internal producers'
+// rel names), summed per group slot; group sizes counted alongside.  Lanes of
+// a warp that share a slot add in three 22-bit slices (each slice sum fits 32
+// bits): one atomic per slot per warp.
+__global__ void k_hg_entry(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                           const uint32_t* __restrict__ nslot, const uint64_t* __restrict__ rh,
+                           const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                           const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                           const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                           unsigned long long* __restrict__ tgkey, int32_t* __restrict__ tcnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + lane;
+    const bool act = v < n && alive[v] == level;
+    const uint32_t sl = act ? nslot[v] : 0;
+    uint64_t val = 0;
+    if (act) {
+      uint64_t prod = 0;
+      for (int64_t e = in_off[v]; e < in_off[v + 1]; e++) {
+        const int32_t r = in_idx[e];
+        if (alive[r] == level && nslot[r] == sl) prod += fmix64(rh[r] ^ 0x6a09e667f3bcc909ULL);
+      }
+      uint64_t h = fmix64(rh[v] + 0x3c6ef372fe94f82bULL * (uint64_t)(op[v] + 1));
+      h = fmix64(h ^ weight_hash(v, w_rank, w_shape, w_train));
+      h = fmix64(h + fmix64(prod ^ 0xbb67ae8584caa73bULL));
+      val = fmix64(h ^ 0xa54ff53a5f1d36f1ULL);
+    }
+    const unsigned mask = __match_any_sync(0xffffffffu, act ? (int)sl : -1 - lane);
+    const uint64_t s0 = __reduce_add_sync(mask, (unsigned)(val & 0x3fffff));
+    const uint64_t s1 = __reduce_add_sync(mask, (unsigned)((val >> 22) & 0x3fffff));
+    const uint64_t s2 = __reduce_add_sync(mask, (unsigned)(val >> 44));
+    if (act && lane == __ffs(mask) - 1) {
+      atomicAdd(&tgkey[sl], (unsigned long long)(s0 + (s1 << 22) + (s2 << 44)));
+      atomicAdd(&tcnt[sl], __popc(mask));
+    }
+  }
+}
+
+__global__ void k_hg_headflag(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                              const uint32_t* __restrict__ nslot, const int32_t* __restrict__ thead,
+                              int32_t* __restrict__ hf) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    hf[v] = (alive[v] == level && thead[nslot[v]] == (int32_t)v) ? 1 : 0;
+}
+
+// compact group ids in node order of the heads; per-group arrays
+__global__ void k_hg_ids(int64_t n, const int32_t* __restrict__ hf, const int32_t* __restrict__ hs,
+                         const uint32_t* __restrict__ nslot, const unsigned long long* __restrict__ tgkey,
+                         const int32_t* __restrict__ tcnt, const int32_t* __restrict__ gparent,
+                         int32_t* __restrict__ tgid, int32_t* __restrict__ gnode, int32_t* __restrict__ gsize,
+                         unsigned long long* __restrict__ gkey, int32_t* __restrict__ gpar) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (!hf[v]) continue;
+    const int32_t g = hs[v] - 1;
+    const uint32_t sl = nslot[v];
+    tgid[sl] = g;
+    gnode[g] = (int32_t)v;
+    gsize[g] = tcnt[sl];
+    gkey[g] = tgkey[sl];
+    gpar[g] = gparent[v];
+  }
+}
+
+// classes: find-or-insert (parent, key sum, size) per group
+__global__ void k_hc_insert(int64_t nG, const unsigned long long* __restrict__ gkey, const int32_t* __restrict__ gsize,
+                            const int32_t* __restrict__ gpar, unsigned long long* __restrict__ ckey,
+                            int32_t* __restrict__ chead, uint32_t mask, uint32_t* __restrict__ gcs,
+                            HashStats* __restrict__ st) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nG; g += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key =
+        nz64(fmix64((uint64_t)gkey[g] ^ fmix64((uint64_t)gsize[g] + 0x1f83d9abfb41bd6bULL) ^
+                    fmix64((uint64_t)(uint32_t)gpar[g] * 0x9e3779b97f4a7c15ULL + 0x5be0cd19137e2179ULL)));
+    uint32_t h = (uint32_t)(key >> 13) & mask;
+    for (uint32_t probe = 0;; probe++) {
+      unsigned long long k = ckey[h];
+      if (k == 0) {
+        k = atomicCAS(&ckey[h], 0ULL, key);
+        if (k == 0) {
+          chead[h] = (int32_t)g;
+          atomicAdd(&st->nC, 1);
+          break;
+        }
+      }
+      if (k == key) break;
+      h = (h + 1) & mask;
+      if (probe > mask) {  // cannot happen: capacity >= 2 nG
+        st->overflow = 1;
+        break;
+      }
+    }
+    gcs[g] = h;
+  }
+}
+
+__global__ void k_hc_count(int64_t nG, const uint32_t* __restrict__ gcs, int32_t* __restrict__ ccnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nG;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = base + lane;
+    const bool ok = g < nG;
+    const uint32_t c = ok ? gcs[g] : 0;
+    const unsigned mask = __match_any_sync(0xffffffffu, ok ? (int)c : -1 - lane);
+    if (ok && lane == __ffs(mask) - 1) atomicAdd(&ccnt[c], __popc(mask));
+  }
+}
+
+// member segments (counting scatter) for groups whose class is multi-group or accepted
+__global__ void k_hg_place(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                           const uint32_t* __restrict__ nslot, const int32_t* __restrict__ tgid,
+                           const uint32_t* __restrict__ gcs, const int32_t* __restrict__ ccnt, int32_t min_dup,
+                           const int32_t* __restrict__ gstart, int32_t* __restrict__ gfill,
+                           int32_t* __restrict__ seg, int32_t* __restrict__ li) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + lane;
+    bool need = false;
+    int32_t g = 0;
+    if (v < n && alive[v] == level) {
+      g = tgid[nslot[v]];
+      const int32_t cs = ccnt[gcs[g]];
+      need = cs >= 2 || cs >= min_dup;
+    }
+    const unsigned mask = __match_any_sync(0xffffffffu, need ? g : -1 - lane);
+    int32_t b = 0;
+    const int leader = __ffs(mask) - 1;
+    if (need && lane == leader) b = atomicAdd(&gfill[g], __popc(mask));
+    b = __shfl_sync(mask, b, leader);
+    if (need) {
+      const int32_t l = b + __popc(mask & ((1u << lane) - 1));
+      li[v] = l;
+      seg[gstart[g] + l] = (int32_t)v;
+    }
+  }
+}
+
+// canonical member order: rank of the rel hash inside the group (multi-group
+// classes); accepted single-group classes keep the segment order
+__global__ void k_hg_rank(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                          const uint32_t* __restrict__ nslot, const int32_t* __restrict__ tgid,
+                          const uint32_t* __restrict__ gcs, const int32_t* __restrict__ ccnt, int32_t min_dup,
+                          const int32_t* __restrict__ gstart, const int32_t* __restrict__ gsize,
+                          const int32_t* __restrict__ seg, const int32_t* __restrict__ li,
+                          const uint64_t* __restrict__ rh, int32_t* __restrict__ sorted, int32_t* __restrict__ pos,
+                          int32_t* __restrict__ collision, HashStats* __restrict__ st) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (alive[v] != level) continue;
+    const int32_t g = tgid[nslot[v]];
+    const int32_t cs = ccnt[gcs[g]];
+    if (cs < 2 && cs < min_dup) continue;
+    const int32_t s0 = gstart[g], sz = gsize[g];
+    int32_t r = li[v];
+    if (cs >= 2) {
+      if (sz > RANK_MAX) {
+        st->big = 1;
+        continue;
+      }
+      const uint64_t me = rh[v];
+      r = 0;
+      for (int32_t k = 0; k < sz; k++) {
+        const int32_t u = seg[s0 + k];
+        const uint64_t x = rh[u];
+        r += x < me;
+        if (x == me && u != (int32_t)v) atomicExch(collision, 1);  // equal rel hashes in one group
+      }
+    }
+    sorted[s0 + r] = (int32_t)v;
+    pos[v] = r;
+  }
+}
+
+// exact checks: (a) prefix bytes vs the group head (every active node); (b) for
+// multi-group classes, member-by-member equality with the class head group at
+// the same canonical position (rel bytes, op, weight, internal producers as
+// canonical positions) and equal parent and size
+__global__ void k_hg_verify(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                            const uint32_t* __restrict__ nslot, const int32_t* __restrict__ tgid,
+                            const uint32_t* __restrict__ gcs, const int32_t* __restrict__ ccnt,
+                            const int32_t* __restrict__ chead, const int32_t* __restrict__ gnode,
+                            const int32_t* __restrict__ gsize, const int32_t* __restrict__ gpar,
+                            const int32_t* __restrict__ gstart, const int32_t* __restrict__ sorted,
+                            const int32_t* __restrict__ pos, const int32_t* __restrict__ pend,
+                            const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
+                            const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
+                            const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+                            const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
+                            int32_t* __restrict__ collision) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (alive[v] != level) continue;
+    const uint32_t sl = nslot[v];
+    const int32_t g = tgid[sl];
+    bool bad = false;
+    const int32_t h = gnode[g];
+    const int32_t pl = pend[v];
+    if (pl != pend[h] || !bytes_eq(names + name_off[v], names + name_off[h], pl)) bad = true;
+    const uint32_t cs = gcs[g];
+    const int32_t hg = chead[cs];
+    if (!bad && ccnt[cs] >= 2 && hg != g) {
+      if (gsize[g] != gsize[hg] || gpar[g] != gpar[hg]) {
+        bad = true;
+      } else {
+        const int32_t b = sorted[gstart[hg] + pos[v]];
+        const uint32_t slb = nslot[b];
+        const int64_t la = name_off[v + 1] - name_off[v];
+        const int64_t lb = name_off[b + 1] - name_off[b];
+        const int32_t plb = pend[b];
+        int64_t sa = pl > 0 ? pl + 1 : 0, sb = plb > 0 ? plb + 1 : 0;
+        sa = sa > la ? la : sa;
+        sb = sb > lb ? lb : sb;
+        if (la - sa != lb - sb || !bytes_eq(names + name_off[v] + sa, names + name_off[b] + sb, la - sa)) bad = true;
+        if (op[v] != op[b] || w_rank[v] != w_rank[b] || w_train[v] != w_train[b]) bad = true;
+        for (int k = 0; k < w_rank[v] && !bad; k++)
+          if (w_shape[v * SP_MAX_RANK + k] != w_shape[(int64_t)b * SP_MAX_RANK + k]) bad = true;
+        // internal producers (deduplicated inputs) as canonical positions: equal sets
+        int ka = 0, kb = 0;
+        for (int64_t e = in_off[b]; e < in_off[b + 1]; e++) {
+          const int32_t r = in_idx[e];
+          kb += alive[r] == level && nslot[r] == slb;
+        }
+        for (int64_t e = in_off[v]; e < in_off[v + 1] && !bad; e++) {
+          const int32_t r = in_idx[e];
+          if (alive[r] != level || nslot[r] != sl) continue;
+          ka++;
+          const int32_t pr = pos[r];
+          bool found = false;
+          for (int64_t f = in_off[b]; f < in_off[b + 1] && !found; f++) {
+            const int32_t q = in_idx[f];
+            found = alive[q] == level && nslot[q] == slb && pos[q] == pr;
+          }
+          if (!found) bad = true;
+        }
+        if (ka != kb) bad = true;
+      }
+    }
+    if (bad) atomicExch(collision, 1);
+  }
+}
+
+// accept / residual / descend; level counters
+__global__ void k_hg_accept(int64_t n, uint8_t* __restrict__ alive, int32_t level, const uint32_t* __restrict__ nslot,
+                            const int32_t* __restrict__ tgid, const uint32_t* __restrict__ gcs,
+                            const int32_t* __restrict__ ccnt, const int32_t* __restrict__ gnode,
+                            const int32_t* __restrict__ depth, int32_t min_dup, int32_t* __restrict__ gparent,
+                            uint8_t* __restrict__ residual, uint8_t* __restrict__ gaccept,
+                            HashStats* __restrict__ st) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + lane;
+    bool next = false, accg = false;
+    if (v < n && alive[v] == level) {
+      const int32_t g = tgid[nslot[v]];
+      const bool acc = ccnt[gcs[g]] >= min_dup;
+      if (gnode[g] == (int32_t)v) {
+        gaccept[g] = acc;
+        accg = acc;
+      }
+      if (acc) {
+        alive[v] = 0;
+      } else if (depth[v] <= level) {
+        residual[v] = 1;
+        alive[v] = 0;
+      } else {
+        alive[v] = (uint8_t)(level + 1);
+        gparent[v] = g;
+        next = true;
+      }
+    }
+    const unsigned nb = __ballot_sync(0xffffffffu, next), ab = __ballot_sync(0xffffffffu, accg);
+    if (lane == 0) {
+      if (nb) atomicAdd(&st->nnext, __popc(nb));
+      if (ab) atomicAdd(&st->nacc, __popc(ab));
+    }
+  }
+}
+
+static uint32_t table_cap(int64_t need) {
+  uint64_t c = 1024;
+  while (c < (uint64_t)need * 2) c <<= 1;
+  return (uint32_t)c;
+}
+
+// one attempt of the hash-grouped fold; *collided on a hash collision, *fallback
+// when a multi-group class has groups too large to rank in place, or when two
+// instance prefixes of a class tie on 16 bytes (both rerun on the sort path)
+static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed, sp_fold* out,
+                           bool* collided, bool* fallback) {
+  cudaStream_t s = ctx->stream;
+  const int sms = ctx->sm_count;
+  const int64_t n = dg->n;
+  const int32_t D = dg->max_depth;
+  FoldTrace tr;
+  *collided = *fallback = false;
+  if (D > 250) {  // levels are stamped in one byte
+    *fallback = true;
+    return;
+  }
+  DevBuf<int32_t> depth, maxd, pend, hf, hs, tgid, gnode, gsize, gpar, gstart, gfill, seg, li, sorted, pos, gparent,
+      tcnt, chead, ccnt, thead, collision, tie;
+  DevBuf<uint32_t> nslot, gcs;
+  DevBuf<uint64_t> ph, rh;
+  DevBuf<unsigned long long> tkey, tgkey, gkey, ckey;
+  DevBuf<uint8_t> alive, residual, gaccept;
+  DevBuf<HashStats> st;
+  depth.alloc(n, s);
+  maxd.alloc(1, s);
+  pend.alloc((size_t)n * D, s);
+  ph.alloc((size_t)n * D, s);
+  rh.alloc((size_t)n * D, s);
+  hf.alloc(n, s);
+  hs.alloc(n, s);
+  nslot.alloc(n, s);
+  li.alloc(n, s);
+  pos.alloc(n, s);
+  seg.alloc(n, s);
+  sorted.alloc(n, s);
+  gparent.alloc(n, s);
+  alive.alloc(n, s);
+  residual.alloc(n, s);
+  collision.alloc(1, s);
+  tie.alloc(1, s);
+  st.alloc(1, s);
+  // the CUB scan scratch for n
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, hf.p, hs.p, (int)n, s);
+  ctx->cub_tmp.alloc(tmp_bytes, s);
+  tr.mark("alloc");
+  SP_CUDA(cudaEventRecord(ctx->ev[6], s));
+  SP_CUDA(cudaMemsetAsync(maxd.p, 0, sizeof(int32_t), s));
+  SP_LAUNCH(ctx, k_depth, grid_for(n, sms), 256, 0, s, dg->name_off.p, dg->names.p, n, depth.p, maxd.p);
+  SP_LAUNCH(ctx, k_name_hash_lm, grid_for(n, sms), 128, 0, s, dg->name_off.p, dg->names.p, n, D, seed, pend.p, ph.p,
+            rh.p);
+  SP_CUDA(cudaMemsetAsync(gparent.p, 0, n * sizeof(int32_t), s));
+  SP_CUDA(cudaMemsetAsync(residual.p, 0, n, s));
+  SP_CUDA(cudaMemsetAsync(alive.p, 1, n, s));
+  SP_CUDA(cudaMemsetAsync(collision.p, 0, sizeof(int32_t), s));
+  SP_CUDA(cudaMemsetAsync(tie.p, 0, sizeof(int32_t), s));
+  std::vector<LevelBlocks> lblocks;
+  HashStats* hst = (HashStats*)pinned_acquire(ctx, sizeof(HashStats), &tmp_bytes);
+  struct Release {
+    sp_ctx* ctx;
+    void* p;
+    size_t n;
+    ~Release() { pinned_release(ctx, p, n); }
+  } rel{ctx, hst, tmp_bytes};
+  int64_t nA = n;
+  int32_t levels = 0;
+  const int gn = grid_for(n, sms);
+  for (int32_t level = 1; nA > 0; level++) {
+    if (level > D) throw Error(SP_ERR_CUDA, "fold did not terminate");
+    const int32_t dd = level - 1;
+    const uint64_t* ph_l = ph.p + (size_t)dd * n;
+    const uint64_t* rh_l = rh.p + (size_t)dd * n;
+    const int32_t* pend_l = pend.p + (size_t)dd * n;
+    // 1. groups: find-or-insert the prefix hash (a small, L2-resident table first;
+    //    grown to 2 x the active count when it fills)
+    const uint32_t full = table_cap(nA);
+    uint32_t cap = std::min<uint32_t>(full, 1u << 16);
+    int64_t nG = 0;
+    for (;;) {
+      tkey.alloc(cap, s);
+      thead.alloc(cap, s);
+      SP_CUDA(cudaMemsetAsync(tkey.p, 0, (size_t)cap * 8, s));
+      SP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(HashStats), s));
+      SP_LAUNCH(ctx, k_hg_insert, gn, 256, 0, s, n, alive.p, level, ph_l, tkey.p, thead.p, cap - 1,
+                cap < full ? 64u : cap, nslot.p, st.p);
+      SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
+      SP_CUDA(cudaStreamSynchronize(s));
+      g_d2h_bytes += sizeof(HashStats);
+      if (!hst->overflow) {
+        nG = hst->nG;
+        break;
+      }
+      if (cap >= full) throw Error(SP_ERR_CUDA, "fold group table overflow");
+      cap = full;
+    }
+    tr.mark("level: insert");
+    // 2. group sizes and template-key sums per slot
+    tgkey.alloc(cap, s);
+    tcnt.alloc(cap, s);
+    SP_CUDA(cudaMemsetAsync(tgkey.p, 0, (size_t)cap * 8, s));
+    SP_CUDA(cudaMemsetAsync(tcnt.p, 0, (size_t)cap * 4, s));
+    SP_LAUNCH(ctx, k_hg_entry, gn, 256, 0, s, n, alive.p, level, nslot.p, rh_l, dg->op.p, dg->w_rank.p, dg->w_shape.p,
+              dg->w_train.p, dg->in_off.p, dg->in_idx.p, tgkey.p, tcnt.p);
+    // 3. compact group ids (heads in node order) and per-group arrays
+    SP_LAUNCH(ctx, k_hg_headflag, gn, 256, 0, s, n, alive.p, level, nslot.p, thead.p, hf.p);
+    {
+      size_t t = ctx->cub_tmp.n;
+      ctx->cub_calls++;
+      SP_CUDA(cub::DeviceScan::InclusiveSum(ctx->cub_tmp.p, t, hf.p, hs.p, (int)n, s));
+    }
+    tgid.alloc(cap, s);
+    gnode.alloc(nG, s);
+    gsize.alloc(nG + 1, s);
+    gkey.alloc(nG, s);
+    gpar.alloc(nG, s);
+    gstart.alloc(nG + 1, s);
+    gfill.alloc(nG, s);
+    gcs.alloc(nG, s);
+    gaccept.alloc(nG, s);
+    SP_LAUNCH(ctx, k_hg_ids, gn, 256, 0, s, n, hf.p, hs.p, nslot.p, tgkey.p, tcnt.p, gparent.p, tgid.p, gnode.p,
+              gsize.p, gkey.p, gpar.p);
+    SP_CUDA(cudaMemsetAsync(gsize.p + nG, 0, sizeof(int32_t), s));
+    {
+      size_t t = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, t, gsize.p, gstart.p, (int)(nG + 1), s);
+      if (t > ctx->cub_tmp.n) ctx->cub_tmp.alloc(t, s);
+      t = ctx->cub_tmp.n;
+      ctx->cub_calls++;
+      SP_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t, gsize.p, gstart.p, (int)(nG + 1), s));
+    }
+    // 4. classes
+    const uint32_t ccap = table_cap(nG);
+    ckey.alloc(ccap, s);
+    chead.alloc(ccap, s);
+    ccnt.alloc(ccap, s);
+    SP_CUDA(cudaMemsetAsync(ckey.p, 0, (size_t)ccap * 8, s));
+    SP_CUDA(cudaMemsetAsync(ccnt.p, 0, (size_t)ccap * 4, s));
+    const int gg = grid_for(nG, sms);
+    SP_LAUNCH(ctx, k_hc_insert, gg, 256, 0, s, nG, gkey.p, gsize.p, gpar.p, ckey.p, chead.p, ccap - 1, gcs.p, st.p);
+    SP_LAUNCH(ctx, k_hc_count, gg, 256, 0, s, nG, gcs.p, ccnt.p);
+    // 5. member segments + canonical order (multi-group / accepted classes only)
+    SP_CUDA(cudaMemsetAsync(gfill.p, 0, (size_t)nG * 4, s));
+    SP_LAUNCH(ctx, k_hg_place, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
+              gfill.p, seg.p, li.p);
+    SP_LAUNCH(ctx, k_hg_rank, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
+              gsize.p, seg.p, li.p, rh_l, sorted.p, pos.p, collision.p, st.p);
+    // 6. exact verification, then accept / residual / descend
+    SP_LAUNCH(ctx, k_hg_verify, gn, 128, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, chead.p, gnode.p,
+              gsize.p, gpar.p, gstart.p, sorted.p, pos.p, pend_l, dg->name_off.p, dg->names.p, dg->op.p, dg->w_rank.p,
+              dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, collision.p);
+    SP_LAUNCH(ctx, k_hg_accept, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, gnode.p, depth.p,
+              min_dup, gparent.p, residual.p, gaccept.p, st.p);
+    SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    g_d2h_bytes += sizeof(HashStats);
+    tr.mark("level: classes/verify/accept");
+    levels++;
+    if (hst->big) {
+      *fallback = true;
+      return;
+    }
+    // accepted classes -> blocks (gclass = class table slot: any unique id works)
+    if (hst->nacc) {
+      lblocks.emplace_back();
+      level_blocks(ctx, dg, dd, nA, nG, sorted.p, gstart.p, (const int32_t*)gcs.p, gaccept.p, pend.p, 1, n, tie.p,
+                   lblocks.back());
+      tr.mark("level: blocks");
+    }
+    nA = hst->nnext;
+  }
+  SP_CUDA(cudaEventRecord(ctx->ev[7], s));
+  int32_t flags[2] = {0, 0};
+  g_d2h_bytes += 8;
+  SP_CUDA(cudaMemcpyAsync(&flags[0], collision.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(&flags[1], tie.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  {
+    float ms = 0;
+    SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
+    ctx->fold_device_ms = ms;
+    ctx->fold_levels = levels;
+  }
+  *collided = flags[0] != 0;
+  if (*collided) return;
+  if (flags[1]) {
+    *fallback = true;
+    return;
+  }
+  // residual singletons, compacted on the device
+  DevBuf<int32_t> iota, rlist, nsel2;
+  iota.alloc(n, s);
+  rlist.alloc(n, s);
+  nsel2.alloc(1, s);
+  SP_LAUNCH(ctx, k_iota, grid_for(n, sms), 256, 0, s, iota.p, n);
+  size_t tb = 0;
+  ctx->cub_calls++;
+  SP_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.p, residual.p, rlist.p, nsel2.p, (int)n, s));
+  DevBuf<uint8_t> tmp2;
+  tmp2.alloc(tb, s);
+  SP_CUDA(cub::DeviceSelect::Flagged(tmp2.p, tb, iota.p, residual.p, rlist.p, nsel2.p, (int)n, s));
+  const int64_t nr = d2h_scalar(nsel2.p, s);
+  std::vector<int32_t> resid(nr);
+  rlist.download(resid.data(), nr, s);
+  tr.mark("residuals");
+  fold_finalize_blocks(dg, lblocks, resid, s, out);
+  tr.mark("finalize");
+}
+
 void fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold* out) {
   if (min_dup < 1) throw Error(SP_ERR_CONFIG, "min_duplicates must be >= 1");
   bool collided = false;
   for (int attempt = 0; attempt < 8; attempt++) {
     const uint64_t seed = 0x243f6a8885a308d3ULL + 0x9e3779b97f4a7c15ULL * (uint64_t)attempt;
-    if (dg->n <= SMALL_MAX && dg->max_depth <= 64 && !getenv("SP_FOLD_MULTI"))
+    if (dg->n <= SMALL_MAX && dg->max_depth <= 64 && !getenv("SP_FOLD_MULTI")) {
       fold_once_small(ctx, dg, min_dup, seed, out, &collided);
-    else
-      fold_once(ctx, dg, min_dup, seed, out, &collided);
+    } else {
+      // the hash-grouped path; SP_FOLD_SORT=1 selects the sort-based one (A/B, fallback)
+      bool fallback = getenv("SP_FOLD_SORT") != nullptr;
+      if (!fallback) fold_once_hash(ctx, dg, min_dup, seed, out, &collided, &fallback);
+      if (fallback && !collided) fold_once(ctx, dg, min_dup, seed, out, &collided);
+    }
     if (!collided) return;
   }
   throw Error(SP_ERR_CUDA, "fold hash verification failed on every seed");

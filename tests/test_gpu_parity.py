@@ -279,9 +279,11 @@ def test_multi_kernel_fold_host_order_vs_oracle(backend, seed, monkeypatch):
         assert to_prune_doc(low, ba) == to_prune_doc(low, ob)
 
 
+@pytest.mark.parametrize("path", ["hash", "sort"])
 @pytest.mark.parametrize("seed", range(0, 40, 3))
-def test_multi_kernel_fold_path_vs_oracle(backend, seed, monkeypatch):
-    """Force the multi-kernel (CUB) fold on small graphs: same partition as the oracle."""
+def test_multi_kernel_fold_path_vs_oracle(backend, seed, path, monkeypatch):
+    """Force the multi-kernel fold on small graphs -- the hash-grouped one and
+    the sort-based fallback: same partition as the oracle."""
     from oracle import oracle
     from paper_2302_00247_b200.blocks import BlockArrays, to_prune_doc
     from paper_2302_00247_b200.lowering import lower
@@ -289,10 +291,47 @@ def test_multi_kernel_fold_path_vs_oracle(backend, seed, monkeypatch):
     from randgraph import random_graph
 
     monkeypatch.setenv("SP_FOLD_MULTI", "1")
+    if path == "sort":
+        monkeypatch.setenv("SP_FOLD_SORT", "1")
     g = random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11))
     low = lower(g)
     ses = Session.open(low, backend)
     for md in (1, 2, 3):
+        ba = fold_blocks(low, md, session=ses)
+        ob = BlockArrays.from_dict(oracle.prune(low, md))
+        assert to_prune_doc(low, ba) == to_prune_doc(low, ob)
+
+
+def _twin_towers(width: int):
+    """Two identical sibling scopes of `width` nodes each (one multi-group class
+    whose groups are too large to rank in place: the hash fold falls back to
+    the sort-based path) plus a third, different one."""
+    from paper_2302_00247_b200.ir import GraphNode, GroupedGraph, OpKind, TensorSpec
+
+    nodes, prev = [], None
+    for t, w in (("tower_a", width), ("tower_b", width), ("tower_c", width - 1)):
+        for i in range(w):
+            sc = f"net/{t}/op{i:05d}"
+            nodes.append(GraphNode(sc, OpKind.MATMUL if i % 3 == 0 else OpKind.ELEMENTWISE,
+                                   (prev,) if prev else (), TensorSpec((8, 16)),
+                                   TensorSpec((16, 16), trainable=True) if i % 3 == 0 else None))
+            prev = sc
+    return GroupedGraph(nodes)
+
+
+@pytest.mark.parametrize("width", [40, 1500])
+def test_fold_large_twin_groups_vs_oracle(backend, width, monkeypatch):
+    """Groups of a multi-group class larger than RANK_MAX (1500 > 1024): exact
+    fallback to the sort-based fold; below it, the hash fold."""
+    from oracle import oracle
+    from paper_2302_00247_b200.blocks import BlockArrays, to_prune_doc
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+
+    monkeypatch.setenv("SP_FOLD_MULTI", "1")
+    low = lower(_twin_towers(width))
+    ses = Session.open(low, backend)
+    for md in (1, 2):
         ba = fold_blocks(low, md, session=ses)
         ob = BlockArrays.from_dict(oracle.prune(low, md))
         assert to_prune_doc(low, ba) == to_prune_doc(low, ob)

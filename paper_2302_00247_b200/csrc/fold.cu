@@ -136,14 +136,6 @@ __global__ void k_name_hash(const int64_t* __restrict__ off, const uint8_t* __re
     name_hash_one(i, off, s, n, D, seed, pend, ph, rh, D, 1);
 }
 
-__global__ void k_name_hash_lm(const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
-                               int32_t D, uint64_t seed, int32_t* __restrict__ pend,
-                               uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    name_hash_one(i, off, s, n, D, seed, pend, ph, rh, 1, n);
-}
-
 __global__ void k_gather_keys(const int32_t* __restrict__ act, int64_t nA, const uint64_t* __restrict__ src,
                               int32_t D, int32_t dd, uint64_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA;
@@ -1795,10 +1787,103 @@ static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed
 // the sort-based path.  Per level: two host syncs (the group count after the
 // insert, the level's counters after accept).
 
+// Name hashing of the hash fold, in two 32-bit polynomial lanes packed in a u64
+// (32-bit IMADs are full rate; a 64-bit multiply is several instructions).
+// Only consistency matters: equal byte strings hash equal, and every grouping
+// decision is re-checked on the bytes.
+constexpr uint32_t kP1 = 0x01000193u, kP2 = 0x5bd1e995u;
+
+__device__ __forceinline__ uint64_t poly_step(uint64_t h, uint32_t c) {
+  return ((uint64_t)((uint32_t)(h >> 32) * kP1 + c) << 32) | (uint32_t)((uint32_t)h * kP2 + c);
+}
+__device__ __forceinline__ uint32_t upow32(uint32_t b, int64_t e) {
+  uint32_t r = 1;
+  while (e) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+// poly(s) = hall - poly(prefix) * B^(len(s)), lane-wise mod 2^32
+__device__ __forceinline__ uint64_t poly_suffix(uint64_t hall, uint64_t hpre, int64_t e) {
+  const uint32_t a = (uint32_t)(hall >> 32) - (uint32_t)(hpre >> 32) * upow32(kP1, e);
+  const uint32_t b = (uint32_t)hall - (uint32_t)hpre * upow32(kP2, e);
+  return ((uint64_t)a << 32) | b;
+}
+
+// Per node, once per fold (hash path): depth, the polynomial hash of the whole
+// name, and the static part of the template-key entry (op, weight shape,
+// trainable).  The names of a block's 256 nodes are staged through shared
+// memory with coalesced loads when they fit.
+constexpr int PREP_SMEM = 16384;
+__global__ void __launch_bounds__(256) k_hg_prep(const int64_t* __restrict__ off, const uint8_t* __restrict__ names,
+                                                 int64_t n, const uint8_t* __restrict__ op,
+                                                 const uint8_t* __restrict__ w_rank, const int64_t* __restrict__ w_shape,
+                                                 const uint8_t* __restrict__ w_train, int32_t* __restrict__ depth,
+                                                 uint64_t* __restrict__ hall, uint64_t* __restrict__ sh) {
+  __shared__ uint8_t sbuf[PREP_SMEM];
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = b0 + blockDim.x < n ? b0 + blockDim.x : n;
+    const int64_t lo = off[b0], hi = off[e];
+    const bool staged = hi - lo <= PREP_SMEM;
+    if (staged)
+      for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) sbuf[k - lo] = names[k];
+    __syncthreads();
+    const int64_t v = b0 + threadIdx.x;
+    if (v < n) {
+      const int64_t a = off[v], L = off[v + 1] - a;
+      const uint8_t* p = staged ? sbuf + (a - lo) : names + a;
+      uint64_t h = 0;
+      int d = 1;
+      for (int64_t k = 0; k < L; k++) {
+        const uint32_t c = p[k];
+        d += c == '/';
+        h = poly_step(h, c + 1);
+      }
+      depth[v] = d;
+      hall[v] = h;
+      sh[v] = fmix64(weight_hash(v, w_rank, w_shape, w_train) + 0x3c6ef372fe94f82bULL * (uint64_t)(op[v] + 1));
+    }
+    __syncthreads();
+  }
+}
+
+// The keys of one level for the nodes active at it: extend the node's prefix
+// polynomial by one component (pend of the previous depth -> this one), then
+// prefix hash, prefix end (level-major pend, read again by the block
+// assembly) and the relative-name hash (suffix = whole name minus prefix).
+__global__ void __launch_bounds__(256) k_hg_keys(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                                                 const int64_t* __restrict__ off, const uint8_t* __restrict__ names,
+                                                 uint64_t seed, const uint64_t* __restrict__ hall,
+                                                 uint64_t* __restrict__ ppoly, int32_t* __restrict__ pend,
+                                                 uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
+  const int32_t dd = level - 1;
+  const uint64_t seed_r = seed ^ 0x9e3779b97f4a7c15ULL;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (alive[v] != level) continue;
+    const int64_t a = off[v], L = off[v + 1] - a;
+    const uint8_t* p = names + a;
+    int64_t k = dd ? pend[(int64_t)(dd - 1) * n + v] : 0;
+    uint64_t h = dd ? ppoly[v] : 0;
+    if (dd && k < L) h = poly_step(h, '/' + 1), k++;  // the separator closing the previous prefix
+    for (; k < L && p[k] != '/'; k++) h = poly_step(h, (uint32_t)p[k] + 1);
+    const int64_t q = k;
+    pend[(int64_t)dd * n + v] = (int32_t)q;
+    ppoly[v] = h;
+    ph[v] = fmix64(h ^ fmix64(seed + (uint64_t)q));
+    int64_t start = q > 0 ? q + 1 : 0;
+    if (start > L) start = L;
+    uint64_t hrel = 0;
+    if (q < L) hrel = poly_suffix(hall[v], start > 0 ? poly_step(h, '/' + 1) : 0, L - start);
+    rh[v] = fmix64(hrel ^ fmix64(seed_r + (uint64_t)(L - start)));
+  }
+}
+
 constexpr int64_t RANK_MAX = 1024;
 
 struct HashStats {  // device counters of one level
-  int32_t nG, overflow, nC, nnext, nacc, big, pad0, pad1;
+  int32_t nG, overflow, nC, nnext, nacc, big, est, pad0;
 };
 
 __device__ __forceinline__ uint64_t nz64(uint64_t k) { return k ? k : 0x9e3779b97f4a7c15ULL; }
@@ -1814,7 +1899,6 @@ __global__ void k_hg_insert(int64_t n, const uint8_t* __restrict__ alive, int32_
   volatile int32_t* overflow = &st->overflow;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     if (alive[v] != level) continue;
-    if (*overflow) return;
     const unsigned long long key = nz64(ph[v]);
     uint32_t h = (uint32_t)(key >> 17) & mask;
     for (uint32_t probe = 0;; probe++) {
@@ -1829,7 +1913,7 @@ __global__ void k_hg_insert(int64_t n, const uint8_t* __restrict__ alive, int32_
       }
       if (k == key) break;
       h = (h + 1) & mask;
-      if (probe >= max_probe) {
+      if (probe >= max_probe || (probe == 8 && *overflow)) {  // the flag is read on long runs only
         *overflow = 1;
         return;
       }
@@ -1842,18 +1926,26 @@ __global__ void k_hg_insert(int64_t n, const uint8_t* __restrict__ alive, int32_
 // rel names), summed per group slot; group sizes counted alongside.  Lanes of
 // a warp that share a slot add in three 22-bit slices (each slice sum fits 32
 // bits): one atomic per slot per warp.
-__global__ void k_hg_entry(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
-                           const uint32_t* __restrict__ nslot, const uint64_t* __restrict__ rh,
-                           const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
-                           const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
-                           const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
-                           unsigned long long* __restrict__ tgkey, int32_t* __restrict__ tcnt) {
+__global__ void __launch_bounds__(256) k_hg_entry(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                                                  const uint32_t* __restrict__ nslot, const uint64_t* __restrict__ rh,
+                                                  const uint64_t* __restrict__ sh, const int64_t* __restrict__ in_off,
+                                                  const int32_t* __restrict__ in_idx,
+                                                  unsigned long long* __restrict__ tgkey, int32_t* __restrict__ tcnt) {
+  // the slot of the block's first node is usually every lane's (huge top-level
+  // groups): its sum goes through shared memory, one global atomic per block
+  __shared__ unsigned long long s_sum;
+  __shared__ int32_t s_cnt;
+  __shared__ uint32_t s_hot;
   const int lane = threadIdx.x & 31;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = base + lane;
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = b0 + threadIdx.x;
     const bool act = v < n && alive[v] == level;
-    const uint32_t sl = act ? nslot[v] : 0;
+    const uint32_t sl = act ? nslot[v] : 0xffffffffu;
+    if (threadIdx.x == 0) {
+      s_hot = sl;
+      s_sum = 0;
+      s_cnt = 0;
+    }
     uint64_t val = 0;
     if (act) {
       uint64_t prod = 0;
@@ -1861,19 +1953,49 @@ __global__ void k_hg_entry(int64_t n, const uint8_t* __restrict__ alive, int32_t
         const int32_t r = in_idx[e];
         if (alive[r] == level && nslot[r] == sl) prod += fmix64(rh[r] ^ 0x6a09e667f3bcc909ULL);
       }
-      uint64_t h = fmix64(rh[v] + 0x3c6ef372fe94f82bULL * (uint64_t)(op[v] + 1));
-      h = fmix64(h ^ weight_hash(v, w_rank, w_shape, w_train));
+      uint64_t h = fmix64(rh[v] ^ sh[v]);
       h = fmix64(h + fmix64(prod ^ 0xbb67ae8584caa73bULL));
       val = fmix64(h ^ 0xa54ff53a5f1d36f1ULL);
     }
+    __syncthreads();
     const unsigned mask = __match_any_sync(0xffffffffu, act ? (int)sl : -1 - lane);
     const uint64_t s0 = __reduce_add_sync(mask, (unsigned)(val & 0x3fffff));
     const uint64_t s1 = __reduce_add_sync(mask, (unsigned)((val >> 22) & 0x3fffff));
     const uint64_t s2 = __reduce_add_sync(mask, (unsigned)(val >> 44));
     if (act && lane == __ffs(mask) - 1) {
-      atomicAdd(&tgkey[sl], (unsigned long long)(s0 + (s1 << 22) + (s2 << 44)));
-      atomicAdd(&tcnt[sl], __popc(mask));
+      const unsigned long long part = (unsigned long long)(s0 + (s1 << 22) + (s2 << 44));
+      if (sl == s_hot) {
+        atomicAdd(&s_sum, part);
+        atomicAdd(&s_cnt, __popc(mask));
+      } else {
+        atomicAdd(&tgkey[sl], part);
+        atomicAdd(&tcnt[sl], __popc(mask));
+      }
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt) {
+      atomicAdd(&tgkey[s_hot], s_sum);
+      atomicAdd(&tcnt[s_hot], s_cnt);
+    }
+  }
+}
+
+// upper bound of the number of groups among the nodes active at `level`:
+// prefix-hash boundaries in node order (every distinct key has one at its first
+// occurrence), one atomic per block
+__global__ void __launch_bounds__(256) k_hg_estimate(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                                                     const uint64_t* __restrict__ ph, HashStats* __restrict__ st) {
+  int32_t cnt = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    if (alive[v] == level) cnt += v == 0 || alive[v - 1] != level || ph[v] != ph[v - 1];
+  cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+  __shared__ int32_t s[8];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s[w];
+    if (t) atomicAdd(&st->est, t);
   }
 }
 
@@ -1903,10 +2025,12 @@ __global__ void k_hg_ids(int64_t n, const int32_t* __restrict__ hf, const int32_
 }
 
 // classes: find-or-insert (parent, key sum, size) per group
-__global__ void k_hc_insert(int64_t nG, const unsigned long long* __restrict__ gkey, const int32_t* __restrict__ gsize,
+__global__ void k_hc_insert(int64_t gmax, const int32_t* __restrict__ d_nG, const unsigned long long* __restrict__ gkey,
+                            const int32_t* __restrict__ gsize,
                             const int32_t* __restrict__ gpar, unsigned long long* __restrict__ ckey,
                             int32_t* __restrict__ chead, uint32_t mask, uint32_t* __restrict__ gcs,
                             HashStats* __restrict__ st) {
+  const int64_t nG = *d_nG < gmax ? *d_nG : gmax;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nG; g += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long key =
         nz64(fmix64((uint64_t)gkey[g] ^ fmix64((uint64_t)gsize[g] + 0x1f83d9abfb41bd6bULL) ^
@@ -1933,7 +2057,9 @@ __global__ void k_hc_insert(int64_t nG, const unsigned long long* __restrict__ g
   }
 }
 
-__global__ void k_hc_count(int64_t nG, const uint32_t* __restrict__ gcs, int32_t* __restrict__ ccnt) {
+__global__ void k_hc_count(int64_t gmax, const int32_t* __restrict__ d_nG, const uint32_t* __restrict__ gcs,
+                           int32_t* __restrict__ ccnt) {
+  const int64_t nG = *d_nG < gmax ? *d_nG : gmax;
   const int lane = threadIdx.x & 31;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nG;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -2078,40 +2204,49 @@ __global__ void k_hg_verify(int64_t n, const uint8_t* __restrict__ alive, int32_
 }
 
 // accept / residual / descend; level counters
-__global__ void k_hg_accept(int64_t n, uint8_t* __restrict__ alive, int32_t level, const uint32_t* __restrict__ nslot,
-                            const int32_t* __restrict__ tgid, const uint32_t* __restrict__ gcs,
-                            const int32_t* __restrict__ ccnt, const int32_t* __restrict__ gnode,
-                            const int32_t* __restrict__ depth, int32_t min_dup, int32_t* __restrict__ gparent,
-                            uint8_t* __restrict__ residual, uint8_t* __restrict__ gaccept,
-                            HashStats* __restrict__ st) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = base + lane;
-    bool next = false, accg = false;
-    if (v < n && alive[v] == level) {
-      const int32_t g = tgid[nslot[v]];
-      const bool acc = ccnt[gcs[g]] >= min_dup;
-      if (gnode[g] == (int32_t)v) {
-        gaccept[g] = acc;
-        accg = acc;
-      }
-      if (acc) {
-        alive[v] = 0;
-      } else if (depth[v] <= level) {
-        residual[v] = 1;
-        alive[v] = 0;
-      } else {
-        alive[v] = (uint8_t)(level + 1);
-        gparent[v] = g;
-        next = true;
-      }
+__global__ void __launch_bounds__(256) k_hg_accept(int64_t n, uint8_t* __restrict__ alive, int32_t level,
+                                                   const uint32_t* __restrict__ nslot, const int32_t* __restrict__ tgid,
+                                                   const uint32_t* __restrict__ gcs, const int32_t* __restrict__ ccnt,
+                                                   const int32_t* __restrict__ gnode, const int32_t* __restrict__ depth,
+                                                   int32_t min_dup, int32_t* __restrict__ gparent,
+                                                   uint8_t* __restrict__ residual, uint8_t* __restrict__ gaccept,
+                                                   HashStats* __restrict__ st) {
+  int32_t nnext = 0, nacc = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    if (alive[v] != level) continue;
+    const int32_t g = tgid[nslot[v]];
+    const bool acc = ccnt[gcs[g]] >= min_dup;
+    if (gnode[g] == (int32_t)v) {
+      gaccept[g] = acc;
+      nacc += acc;
     }
-    const unsigned nb = __ballot_sync(0xffffffffu, next), ab = __ballot_sync(0xffffffffu, accg);
-    if (lane == 0) {
-      if (nb) atomicAdd(&st->nnext, __popc(nb));
-      if (ab) atomicAdd(&st->nacc, __popc(ab));
+    if (acc) {
+      alive[v] = 0;
+    } else if (depth[v] <= level) {
+      residual[v] = 1;
+      alive[v] = 0;
+    } else {
+      alive[v] = (uint8_t)(level + 1);
+      gparent[v] = g;
+      nnext++;
     }
+  }
+  nnext = __reduce_add_sync(0xffffffffu, (unsigned)nnext);
+  nacc = __reduce_add_sync(0xffffffffu, (unsigned)nacc);
+  __shared__ int32_t s[2][8];
+  if ((threadIdx.x & 31) == 0) {
+    s[0][threadIdx.x >> 5] = nnext;
+    s[1][threadIdx.x >> 5] = nacc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t a = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+      a += s[0][w];
+      b += s[1][w];
+    }
+    if (a) atomicAdd(&st->nnext, a);
+    if (b) atomicAdd(&st->nacc, b);
   }
 }
 
@@ -2136,18 +2271,20 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
     *fallback = true;
     return;
   }
-  DevBuf<int32_t> depth, maxd, pend, hf, hs, tgid, gnode, gsize, gpar, gstart, gfill, seg, li, sorted, pos, gparent,
-      tcnt, chead, ccnt, thead, collision, tie;
+  DevBuf<int32_t> depth, pend, hf, hs, tgid, gnode, gsize, gpar, gstart, gfill, seg, li, sorted, pos, gparent, tcnt,
+      chead, ccnt, thead, collision, tie;
   DevBuf<uint32_t> nslot, gcs;
-  DevBuf<uint64_t> ph, rh;
+  DevBuf<uint64_t> ph, rh, sh, hall, ppoly;
   DevBuf<unsigned long long> tkey, tgkey, gkey, ckey;
   DevBuf<uint8_t> alive, residual, gaccept;
   DevBuf<HashStats> st;
   depth.alloc(n, s);
-  maxd.alloc(1, s);
-  pend.alloc((size_t)n * D, s);
-  ph.alloc((size_t)n * D, s);
-  rh.alloc((size_t)n * D, s);
+  pend.alloc((size_t)n * D, s);  // level-major; depth dd written at level dd + 1
+  ph.alloc(n, s);                 // the current level's keys
+  rh.alloc(n, s);
+  hall.alloc(n, s);
+  ppoly.alloc(n, s);
+  sh.alloc(n, s);
   hf.alloc(n, s);
   hs.alloc(n, s);
   nslot.alloc(n, s);
@@ -2161,22 +2298,9 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
   collision.alloc(1, s);
   tie.alloc(1, s);
   st.alloc(1, s);
-  // the CUB scan scratch for n
   size_t tmp_bytes = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, hf.p, hs.p, (int)n, s);
   ctx->cub_tmp.alloc(tmp_bytes, s);
-  tr.mark("alloc");
-  SP_CUDA(cudaEventRecord(ctx->ev[6], s));
-  SP_CUDA(cudaMemsetAsync(maxd.p, 0, sizeof(int32_t), s));
-  SP_LAUNCH(ctx, k_depth, grid_for(n, sms), 256, 0, s, dg->name_off.p, dg->names.p, n, depth.p, maxd.p);
-  SP_LAUNCH(ctx, k_name_hash_lm, grid_for(n, sms), 128, 0, s, dg->name_off.p, dg->names.p, n, D, seed, pend.p, ph.p,
-            rh.p);
-  SP_CUDA(cudaMemsetAsync(gparent.p, 0, n * sizeof(int32_t), s));
-  SP_CUDA(cudaMemsetAsync(residual.p, 0, n, s));
-  SP_CUDA(cudaMemsetAsync(alive.p, 1, n, s));
-  SP_CUDA(cudaMemsetAsync(collision.p, 0, sizeof(int32_t), s));
-  SP_CUDA(cudaMemsetAsync(tie.p, 0, sizeof(int32_t), s));
-  std::vector<LevelBlocks> lblocks;
   HashStats* hst = (HashStats*)pinned_acquire(ctx, sizeof(HashStats), &tmp_bytes);
   struct Release {
     sp_ctx* ctx;
@@ -2184,45 +2308,53 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
     size_t n;
     ~Release() { pinned_release(ctx, p, n); }
   } rel{ctx, hst, tmp_bytes};
+  tr.mark("alloc");
+  const int gn = grid_for(n, sms);
+  SP_CUDA(cudaEventRecord(ctx->ev[6], s));
+  SP_LAUNCH(ctx, k_hg_prep, gn, 256, 0, s, dg->name_off.p, dg->names.p, n, dg->op.p, dg->w_rank.p, dg->w_shape.p,
+            dg->w_train.p, depth.p, hall.p, sh.p);
+  SP_CUDA(cudaMemsetAsync(gparent.p, 0, n * sizeof(int32_t), s));
+  SP_CUDA(cudaMemsetAsync(residual.p, 0, n, s));
+  SP_CUDA(cudaMemsetAsync(alive.p, 1, n, s));
+  SP_CUDA(cudaMemsetAsync(collision.p, 0, sizeof(int32_t), s));
+  SP_CUDA(cudaMemsetAsync(tie.p, 0, sizeof(int32_t), s));
+  // level 1's group-count bound; later levels get theirs with the previous level's counters
+  SP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(HashStats), s));
+  SP_LAUNCH(ctx, k_hg_keys, gn, 256, 0, s, n, alive.p, 1, dg->name_off.p, dg->names.p, seed, hall.p, ppoly.p, pend.p,
+            ph.p, rh.p);
+  SP_LAUNCH(ctx, k_hg_estimate, gn, 256, 0, s, n, alive.p, 1, ph.p, st.p);
+  SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  g_d2h_bytes += sizeof(HashStats);
+  int64_t est = hst->est;
+  std::vector<LevelBlocks> lblocks;
   int64_t nA = n;
   int32_t levels = 0;
-  const int gn = grid_for(n, sms);
   for (int32_t level = 1; nA > 0; level++) {
     if (level > D) throw Error(SP_ERR_CUDA, "fold did not terminate");
     const int32_t dd = level - 1;
-    const uint64_t* ph_l = ph.p + (size_t)dd * n;
-    const uint64_t* rh_l = rh.p + (size_t)dd * n;
+    const uint64_t* ph_l = ph.p;
+    const uint64_t* rh_l = rh.p;
     const int32_t* pend_l = pend.p + (size_t)dd * n;
-    // 1. groups: find-or-insert the prefix hash (a small, L2-resident table first;
-    //    grown to 2 x the active count when it fills)
-    const uint32_t full = table_cap(nA);
-    uint32_t cap = std::min<uint32_t>(full, 1u << 16);
-    int64_t nG = 0;
-    for (;;) {
-      tkey.alloc(cap, s);
-      thead.alloc(cap, s);
-      SP_CUDA(cudaMemsetAsync(tkey.p, 0, (size_t)cap * 8, s));
-      SP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(HashStats), s));
-      SP_LAUNCH(ctx, k_hg_insert, gn, 256, 0, s, n, alive.p, level, ph_l, tkey.p, thead.p, cap - 1,
-                cap < full ? 64u : cap, nslot.p, st.p);
-      SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
-      SP_CUDA(cudaStreamSynchronize(s));
-      g_d2h_bytes += sizeof(HashStats);
-      if (!hst->overflow) {
-        nG = hst->nG;
-        break;
-      }
-      if (cap >= full) throw Error(SP_ERR_CUDA, "fold group table overflow");
-      cap = full;
-    }
-    tr.mark("level: insert");
-    // 2. group sizes and template-key sums per slot
+    // 1. groups: find-or-insert the prefix hash into a table of >= 2 x the
+    //    group-count bound (no overflow possible; every later per-group array
+    //    and the class table are sized by the bound, the exact count stays on
+    //    the device until the level's one host sync)
+    const int64_t gmax = std::max<int64_t>(1, std::min<int64_t>(est, nA));
+    const uint32_t cap = table_cap(gmax);
+    tkey.alloc(cap, s);
+    thead.alloc(cap, s);
     tgkey.alloc(cap, s);
     tcnt.alloc(cap, s);
+    tgid.alloc(cap, s);
+    SP_CUDA(cudaMemsetAsync(tkey.p, 0, (size_t)cap * 8, s));
     SP_CUDA(cudaMemsetAsync(tgkey.p, 0, (size_t)cap * 8, s));
     SP_CUDA(cudaMemsetAsync(tcnt.p, 0, (size_t)cap * 4, s));
-    SP_LAUNCH(ctx, k_hg_entry, gn, 256, 0, s, n, alive.p, level, nslot.p, rh_l, dg->op.p, dg->w_rank.p, dg->w_shape.p,
-              dg->w_train.p, dg->in_off.p, dg->in_idx.p, tgkey.p, tcnt.p);
+    SP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(HashStats), s));
+    SP_LAUNCH(ctx, k_hg_insert, gn, 256, 0, s, n, alive.p, level, ph_l, tkey.p, thead.p, cap - 1, cap, nslot.p, st.p);
+    // 2. group sizes and template-key sums per slot
+    SP_LAUNCH(ctx, k_hg_entry, gn, 256, 0, s, n, alive.p, level, nslot.p, rh_l, sh.p, dg->in_off.p, dg->in_idx.p,
+              tgkey.p, tcnt.p);
     // 3. compact group ids (heads in node order) and per-group arrays
     SP_LAUNCH(ctx, k_hg_headflag, gn, 256, 0, s, n, alive.p, level, nslot.p, thead.p, hf.p);
     {
@@ -2230,38 +2362,38 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
       ctx->cub_calls++;
       SP_CUDA(cub::DeviceScan::InclusiveSum(ctx->cub_tmp.p, t, hf.p, hs.p, (int)n, s));
     }
-    tgid.alloc(cap, s);
-    gnode.alloc(nG, s);
-    gsize.alloc(nG + 1, s);
-    gkey.alloc(nG, s);
-    gpar.alloc(nG, s);
-    gstart.alloc(nG + 1, s);
-    gfill.alloc(nG, s);
-    gcs.alloc(nG, s);
-    gaccept.alloc(nG, s);
+    gnode.alloc(gmax, s);
+    gsize.alloc(gmax + 1, s);
+    gkey.alloc(gmax, s);
+    gpar.alloc(gmax, s);
+    gstart.alloc(gmax + 1, s);
+    gfill.alloc(gmax, s);
+    gcs.alloc(gmax, s);
+    gaccept.alloc(gmax, s);
+    SP_CUDA(cudaMemsetAsync(gsize.p, 0, (size_t)(gmax + 1) * 4, s));
     SP_LAUNCH(ctx, k_hg_ids, gn, 256, 0, s, n, hf.p, hs.p, nslot.p, tgkey.p, tcnt.p, gparent.p, tgid.p, gnode.p,
               gsize.p, gkey.p, gpar.p);
-    SP_CUDA(cudaMemsetAsync(gsize.p + nG, 0, sizeof(int32_t), s));
     {
       size_t t = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, t, gsize.p, gstart.p, (int)(nG + 1), s);
+      cub::DeviceScan::ExclusiveSum(nullptr, t, gsize.p, gstart.p, (int)(gmax + 1), s);
       if (t > ctx->cub_tmp.n) ctx->cub_tmp.alloc(t, s);
       t = ctx->cub_tmp.n;
       ctx->cub_calls++;
-      SP_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t, gsize.p, gstart.p, (int)(nG + 1), s));
+      SP_CUDA(cub::DeviceScan::ExclusiveSum(ctx->cub_tmp.p, t, gsize.p, gstart.p, (int)(gmax + 1), s));
     }
-    // 4. classes
-    const uint32_t ccap = table_cap(nG);
+    // 4. classes (over the groups g < nG, the count read on the device)
+    const uint32_t ccap = table_cap(gmax);
     ckey.alloc(ccap, s);
     chead.alloc(ccap, s);
     ccnt.alloc(ccap, s);
     SP_CUDA(cudaMemsetAsync(ckey.p, 0, (size_t)ccap * 8, s));
     SP_CUDA(cudaMemsetAsync(ccnt.p, 0, (size_t)ccap * 4, s));
-    const int gg = grid_for(nG, sms);
-    SP_LAUNCH(ctx, k_hc_insert, gg, 256, 0, s, nG, gkey.p, gsize.p, gpar.p, ckey.p, chead.p, ccap - 1, gcs.p, st.p);
-    SP_LAUNCH(ctx, k_hc_count, gg, 256, 0, s, nG, gcs.p, ccnt.p);
+    const int gg = grid_for(gmax, sms);
+    SP_LAUNCH(ctx, k_hc_insert, gg, 256, 0, s, gmax, &st.p->nG, gkey.p, gsize.p, gpar.p, ckey.p, chead.p, ccap - 1,
+              gcs.p, st.p);
+    SP_LAUNCH(ctx, k_hc_count, gg, 256, 0, s, gmax, &st.p->nG, gcs.p, ccnt.p);
     // 5. member segments + canonical order (multi-group / accepted classes only)
-    SP_CUDA(cudaMemsetAsync(gfill.p, 0, (size_t)nG * 4, s));
+    SP_CUDA(cudaMemsetAsync(gfill.p, 0, (size_t)gmax * 4, s));
     SP_LAUNCH(ctx, k_hg_place, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
               gfill.p, seg.p, li.p);
     SP_LAUNCH(ctx, k_hg_rank, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
@@ -2272,15 +2404,22 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
               dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, collision.p);
     SP_LAUNCH(ctx, k_hg_accept, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, gnode.p, depth.p,
               min_dup, gparent.p, residual.p, gaccept.p, st.p);
+    if (level < D) {  // the next level's keys and group-count bound
+      SP_LAUNCH(ctx, k_hg_keys, gn, 256, 0, s, n, alive.p, level + 1, dg->name_off.p, dg->names.p, seed, hall.p,
+                ppoly.p, pend.p, ph.p, rh.p);
+      SP_LAUNCH(ctx, k_hg_estimate, gn, 256, 0, s, n, alive.p, level + 1, ph.p, st.p);
+    }
     SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
     g_d2h_bytes += sizeof(HashStats);
-    tr.mark("level: classes/verify/accept");
+    tr.mark("level");
     levels++;
+    if (hst->overflow) throw Error(SP_ERR_CUDA, "fold group table overflow");
     if (hst->big) {
       *fallback = true;
       return;
     }
+    const int64_t nG = hst->nG;
     // accepted classes -> blocks (gclass = class table slot: any unique id works)
     if (hst->nacc) {
       lblocks.emplace_back();
@@ -2289,6 +2428,7 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
       tr.mark("level: blocks");
     }
     nA = hst->nnext;
+    est = hst->est;
   }
   SP_CUDA(cudaEventRecord(ctx->ev[7], s));
   int32_t flags[2] = {0, 0};

@@ -1822,18 +1822,27 @@ __global__ void __launch_bounds__(256) k_hg_prep(const int64_t* __restrict__ off
                                                  const uint8_t* __restrict__ w_rank, const int64_t* __restrict__ w_shape,
                                                  const uint8_t* __restrict__ w_train, int32_t* __restrict__ depth,
                                                  uint64_t* __restrict__ hall, uint64_t* __restrict__ sh) {
-  __shared__ uint8_t sbuf[PREP_SMEM];
+  __shared__ __align__(16) uint32_t swords[PREP_SMEM / 4 + 2];
+  const uint8_t* sbuf = (const uint8_t*)swords;
+  const int64_t total = off[n];
+  const bool aligned = ((uintptr_t)names & 3) == 0;
   for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < n; b0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = b0 + blockDim.x < n ? b0 + blockDim.x : n;
     const int64_t lo = off[b0], hi = off[e];
-    const bool staged = hi - lo <= PREP_SMEM;
-    if (staged)
-      for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) sbuf[k - lo] = names[k];
+    // 4-byte words [lo/4, ceil(hi/4)) -- coalesced, every load in flight at once
+    const int64_t w0 = lo >> 2, w1 = (hi + 3) >> 2;
+    const bool staged = aligned && (w1 - w0) * 4 <= PREP_SMEM;
+    if (staged) {
+      const uint32_t* gw = (const uint32_t*)names;
+      const int64_t last = (total + 3) >> 2;  // words holding name bytes (the arena continues past them)
+#pragma unroll 4
+      for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) swords[w - w0] = w < last ? gw[w] : 0u;
+    }
     __syncthreads();
     const int64_t v = b0 + threadIdx.x;
     if (v < n) {
       const int64_t a = off[v], L = off[v + 1] - a;
-      const uint8_t* p = staged ? sbuf + (a - lo) : names + a;
+      const uint8_t* p = staged ? sbuf + (a - (w0 << 2)) : names + a;
       uint64_t h = 0;
       int d = 1;
       for (int64_t k = 0; k < L; k++) {
@@ -1853,31 +1862,57 @@ __global__ void __launch_bounds__(256) k_hg_prep(const int64_t* __restrict__ off
 // polynomial by one component (pend of the previous depth -> this one), then
 // prefix hash, prefix end (level-major pend, read again by the block
 // assembly) and the relative-name hash (suffix = whole name minus prefix).
-__global__ void __launch_bounds__(256) k_hg_keys(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
-                                                 const int64_t* __restrict__ off, const uint8_t* __restrict__ names,
-                                                 uint64_t seed, const uint64_t* __restrict__ hall,
-                                                 uint64_t* __restrict__ ppoly, int32_t* __restrict__ pend,
-                                                 uint64_t* __restrict__ ph, uint64_t* __restrict__ rh) {
-  const int32_t dd = level - 1;
-  const uint64_t seed_r = seed ^ 0x9e3779b97f4a7c15ULL;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-    if (alive[v] != level) continue;
-    const int64_t a = off[v], L = off[v + 1] - a;
-    const uint8_t* p = names + a;
-    int64_t k = dd ? pend[(int64_t)(dd - 1) * n + v] : 0;
-    uint64_t h = dd ? ppoly[v] : 0;
-    if (dd && k < L) h = poly_step(h, '/' + 1), k++;  // the separator closing the previous prefix
-    for (; k < L && p[k] != '/'; k++) h = poly_step(h, (uint32_t)p[k] + 1);
-    const int64_t q = k;
-    pend[(int64_t)dd * n + v] = (int32_t)q;
-    ppoly[v] = h;
-    ph[v] = fmix64(h ^ fmix64(seed + (uint64_t)q));
-    int64_t start = q > 0 ? q + 1 : 0;
-    if (start > L) start = L;
-    uint64_t hrel = 0;
-    if (q < L) hrel = poly_suffix(hall[v], start > 0 ? poly_step(h, '/' + 1) : 0, L - start);
-    rh[v] = fmix64(hrel ^ fmix64(seed_r + (uint64_t)(L - start)));
+// The keys of depth dd for node v: extend the node's prefix polynomial by one
+// component (pend of the previous depth -> this one), then the prefix hash,
+// the prefix end (level-major pend, read again by the block assembly) and the
+// relative-name hash (suffix = whole name minus prefix).  Returns the prefix hash.
+__device__ __forceinline__ uint64_t node_keys(int64_t v, int64_t n, int32_t dd, const int64_t* __restrict__ off,
+                                              const uint8_t* __restrict__ names, uint64_t seed,
+                                              const uint64_t* __restrict__ hall, uint64_t* __restrict__ ppoly,
+                                              int32_t* __restrict__ pend, uint64_t* __restrict__ ph,
+                                              uint64_t* __restrict__ rh) {
+  const int64_t a = off[v], L = off[v + 1] - a;
+  const uint8_t* p = names + a;
+  int64_t k = dd ? pend[(int64_t)(dd - 1) * n + v] : 0;
+  uint64_t h = dd ? ppoly[v] : 0;
+  if (dd && k < L) h = poly_step(h, '/' + 1), k++;  // the separator closing the previous prefix
+  for (; k < L && p[k] != '/'; k++) h = poly_step(h, (uint32_t)p[k] + 1);
+  const int64_t q = k;
+  pend[(int64_t)dd * n + v] = (int32_t)q;
+  ppoly[v] = h;
+  const uint64_t key = fmix64(h ^ fmix64(seed + (uint64_t)q));
+  ph[v] = key;
+  int64_t start = q > 0 ? q + 1 : 0;
+  if (start > L) start = L;
+  uint64_t hrel = 0;
+  if (q < L) hrel = poly_suffix(hall[v], start > 0 ? poly_step(h, '/' + 1) : 0, L - start);
+  rh[v] = fmix64(hrel ^ fmix64((seed ^ 0x9e3779b97f4a7c15ULL) + (uint64_t)(L - start)));
+  return key;
+}
+
+// Upper bound of the number of distinct prefix hashes among the lanes with
+// `act`: boundaries between consecutive lanes (every distinct key has one at
+// its first occurrence in node order), lane 0 always counting.  Lane 0 returns
+// the warp's count.
+__device__ __forceinline__ int32_t warp_boundaries(bool act, uint64_t key) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool pa = __shfl_up_sync(0xffffffffu, act, 1);
+  const bool bnd = act && (lane == 0 || !pa || pk != key);
+  return __popc(__ballot_sync(0xffffffffu, bnd));
+}
+
+__device__ __forceinline__ void block_add(int32_t x, int32_t* __restrict__ dst) {
+  __shared__ int32_t s_w[32];
+  x = __reduce_add_sync(0xffffffffu, (unsigned)x);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_w[w];
+    if (t) atomicAdd(dst, t);
   }
+  __syncthreads();
 }
 
 constexpr int64_t RANK_MAX = 1024;
@@ -1886,39 +1921,72 @@ struct HashStats {  // device counters of one level
   int32_t nG, overflow, nC, nnext, nacc, big, est, pad0;
 };
 
+// level-1 keys of every node + the group-count bound
+__global__ void __launch_bounds__(256) k_hg_keys1(int64_t n, const int64_t* __restrict__ off,
+                                                  const uint8_t* __restrict__ names, uint64_t seed,
+                                                  const uint64_t* __restrict__ hall, uint64_t* __restrict__ ppoly,
+                                                  int32_t* __restrict__ pend, uint64_t* __restrict__ ph,
+                                                  uint64_t* __restrict__ rh, HashStats* __restrict__ st) {
+  int32_t est = 0;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + (threadIdx.x & 31);
+    const bool act = v < n;
+    const uint64_t key = act ? node_keys(v, n, 0, off, names, seed, hall, ppoly, pend, ph, rh) : 0;
+    const int32_t c = warp_boundaries(act, key);
+    if ((threadIdx.x & 31) == 0) est += c;
+  }
+  block_add(est, &st->est);
+}
+
+
 __device__ __forceinline__ uint64_t nz64(uint64_t k) { return k ? k : 0x9e3779b97f4a7c15ULL; }
 
 // one pass over the nodes active at `level`: find-or-insert the prefix hash
 // Overflow (more keys than half the capacity, or a probe run longer than
 // max_probe) stops every thread at its next node: the host retries the level
 // with a table of 2 x the active count.
-__global__ void k_hg_insert(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
-                            const uint64_t* __restrict__ ph, unsigned long long* __restrict__ tkey,
-                            int32_t* __restrict__ thead, uint32_t mask, uint32_t max_probe,
-                            uint32_t* __restrict__ nslot, HashStats* __restrict__ st) {
+// Lanes of a warp that carry the same key (consecutive members of one group)
+// probe once: the lowest such lane finds or inserts, the others take its slot.
+__global__ void __launch_bounds__(256) k_hg_insert(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
+                                                   const uint64_t* __restrict__ ph,
+                                                   unsigned long long* __restrict__ tkey, int32_t* __restrict__ thead,
+                                                   uint32_t mask, uint32_t max_probe, uint32_t* __restrict__ nslot,
+                                                   HashStats* __restrict__ st) {
   volatile int32_t* overflow = &st->overflow;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-    if (alive[v] != level) continue;
-    const unsigned long long key = nz64(ph[v]);
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + lane;
+    const bool act = v < n && alive[v] == level;
+    const unsigned long long key = act ? nz64(ph[v]) : 0;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(same) - 1;
     uint32_t h = (uint32_t)(key >> 17) & mask;
-    for (uint32_t probe = 0;; probe++) {
-      unsigned long long k = tkey[h];
-      if (k == 0) {
-        k = atomicCAS(&tkey[h], 0ULL, key);
+    bool gave_up = false;
+    if (act && lane == leader) {
+      for (uint32_t probe = 0;; probe++) {
+        unsigned long long k = tkey[h];
         if (k == 0) {
-          thead[h] = (int32_t)v;
-          if ((uint32_t)atomicAdd(&st->nG, 1) >= (mask + 1) / 2) *overflow = 1;
+          k = atomicCAS(&tkey[h], 0ULL, key);
+          if (k == 0) {
+            thead[h] = (int32_t)v;
+            if ((uint32_t)atomicAdd(&st->nG, 1) >= (mask + 1) / 2) *overflow = 1;
+            break;
+          }
+        }
+        if (k == key) break;
+        h = (h + 1) & mask;
+        if (probe >= max_probe || (probe == 8 && *overflow)) {  // the flag is read on long runs only
+          *overflow = 1;
+          gave_up = true;
           break;
         }
       }
-      if (k == key) break;
-      h = (h + 1) & mask;
-      if (probe >= max_probe || (probe == 8 && *overflow)) {  // the flag is read on long runs only
-        *overflow = 1;
-        return;
-      }
     }
-    nslot[v] = h;
+    h = __shfl_sync(0xffffffffu, h, leader);
+    gave_up = __shfl_sync(0xffffffffu, gave_up, leader);
+    if (act && !gave_up) nslot[v] = h;
   }
 }
 
@@ -1930,6 +1998,7 @@ __global__ void __launch_bounds__(256) k_hg_entry(int64_t n, const uint8_t* __re
                                                   const uint32_t* __restrict__ nslot, const uint64_t* __restrict__ rh,
                                                   const uint64_t* __restrict__ sh, const int64_t* __restrict__ in_off,
                                                   const int32_t* __restrict__ in_idx,
+                                                  const int32_t* __restrict__ thead, int32_t* __restrict__ hf,
                                                   unsigned long long* __restrict__ tgkey, int32_t* __restrict__ tcnt) {
   // the slot of the block's first node is usually every lane's (huge top-level
   // groups): its sum goes through shared memory, one global atomic per block
@@ -1941,6 +2010,7 @@ __global__ void __launch_bounds__(256) k_hg_entry(int64_t n, const uint8_t* __re
     const int64_t v = b0 + threadIdx.x;
     const bool act = v < n && alive[v] == level;
     const uint32_t sl = act ? nslot[v] : 0xffffffffu;
+    if (v < n) hf[v] = act && thead[sl] == (int32_t)v;  // group heads (compact ids by their scan)
     if (threadIdx.x == 0) {
       s_hot = sl;
       s_sum = 0;
@@ -1978,32 +2048,6 @@ __global__ void __launch_bounds__(256) k_hg_entry(int64_t n, const uint8_t* __re
       atomicAdd(&tcnt[s_hot], s_cnt);
     }
   }
-}
-
-// upper bound of the number of groups among the nodes active at `level`:
-// prefix-hash boundaries in node order (every distinct key has one at its first
-// occurrence), one atomic per block
-__global__ void __launch_bounds__(256) k_hg_estimate(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
-                                                     const uint64_t* __restrict__ ph, HashStats* __restrict__ st) {
-  int32_t cnt = 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-    if (alive[v] == level) cnt += v == 0 || alive[v - 1] != level || ph[v] != ph[v - 1];
-  cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
-  __shared__ int32_t s[8];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s[w];
-    if (t) atomicAdd(&st->est, t);
-  }
-}
-
-__global__ void k_hg_headflag(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
-                              const uint32_t* __restrict__ nslot, const int32_t* __restrict__ thead,
-                              int32_t* __restrict__ hf) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-    hf[v] = (alive[v] == level && thead[nslot[v]] == (int32_t)v) ? 1 : 0;
 }
 
 // compact group ids in node order of the heads; per-group arrays
@@ -2136,118 +2180,114 @@ __global__ void k_hg_rank(int64_t n, const uint8_t* __restrict__ alive, int32_t 
   }
 }
 
-// exact checks: (a) prefix bytes vs the group head (every active node); (b) for
-// multi-group classes, member-by-member equality with the class head group at
-// the same canonical position (rel bytes, op, weight, internal producers as
-// canonical positions) and equal parent and size
-__global__ void k_hg_verify(int64_t n, const uint8_t* __restrict__ alive, int32_t level,
-                            const uint32_t* __restrict__ nslot, const int32_t* __restrict__ tgid,
-                            const uint32_t* __restrict__ gcs, const int32_t* __restrict__ ccnt,
-                            const int32_t* __restrict__ chead, const int32_t* __restrict__ gnode,
-                            const int32_t* __restrict__ gsize, const int32_t* __restrict__ gpar,
-                            const int32_t* __restrict__ gstart, const int32_t* __restrict__ sorted,
-                            const int32_t* __restrict__ pos, const int32_t* __restrict__ pend,
-                            const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
-                            const uint8_t* __restrict__ op, const uint8_t* __restrict__ w_rank,
-                            const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
-                            const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx,
-                            int32_t* __restrict__ collision) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-    if (alive[v] != level) continue;
-    const uint32_t sl = nslot[v];
-    const int32_t g = tgid[sl];
-    bool bad = false;
-    const int32_t h = gnode[g];
-    const int32_t pl = pend[v];
-    if (pl != pend[h] || !bytes_eq(names + name_off[v], names + name_off[h], pl)) bad = true;
-    const uint32_t cs = gcs[g];
-    const int32_t hg = chead[cs];
-    if (!bad && ccnt[cs] >= 2 && hg != g) {
-      if (gsize[g] != gsize[hg] || gpar[g] != gpar[hg]) {
-        bad = true;
-      } else {
-        const int32_t b = sorted[gstart[hg] + pos[v]];
-        const uint32_t slb = nslot[b];
-        const int64_t la = name_off[v + 1] - name_off[v];
-        const int64_t lb = name_off[b + 1] - name_off[b];
-        const int32_t plb = pend[b];
-        int64_t sa = pl > 0 ? pl + 1 : 0, sb = plb > 0 ? plb + 1 : 0;
-        sa = sa > la ? la : sa;
-        sb = sb > lb ? lb : sb;
-        if (la - sa != lb - sb || !bytes_eq(names + name_off[v] + sa, names + name_off[b] + sb, la - sa)) bad = true;
-        if (op[v] != op[b] || w_rank[v] != w_rank[b] || w_train[v] != w_train[b]) bad = true;
-        for (int k = 0; k < w_rank[v] && !bad; k++)
-          if (w_shape[v * SP_MAX_RANK + k] != w_shape[(int64_t)b * SP_MAX_RANK + k]) bad = true;
-        // internal producers (deduplicated inputs) as canonical positions: equal sets
-        int ka = 0, kb = 0;
-        for (int64_t e = in_off[b]; e < in_off[b + 1]; e++) {
-          const int32_t r = in_idx[e];
-          kb += alive[r] == level && nslot[r] == slb;
-        }
-        for (int64_t e = in_off[v]; e < in_off[v + 1] && !bad; e++) {
-          const int32_t r = in_idx[e];
-          if (alive[r] != level || nslot[r] != sl) continue;
-          ka++;
-          const int32_t pr = pos[r];
-          bool found = false;
-          for (int64_t f = in_off[b]; f < in_off[b + 1] && !found; f++) {
-            const int32_t q = in_idx[f];
-            found = alive[q] == level && nslot[q] == slb && pos[q] == pr;
+// The end of a level, one pass over its active nodes: (1) exact checks --
+// prefix bytes vs the group head, and for multi-group classes member-by-member
+// equality with the class head group at the same canonical position (rel
+// bytes, op, weight, internal producers as canonical positions) with equal
+// parent and size; (2) accept / residual / descend, written to the NEXT
+// level's state array (this level's stays read-only, so the internal-producer
+// tests of other threads see it unchanged); (3) the next level's keys for the
+// nodes that descend, and its group-count bound.
+__global__ void __launch_bounds__(128) k_hg_finish(
+    int64_t n, const uint8_t* __restrict__ alive, uint8_t* __restrict__ alive_next, int32_t level, int32_t D,
+    const uint32_t* __restrict__ nslot, const int32_t* __restrict__ tgid, const uint32_t* __restrict__ gcs,
+    const int32_t* __restrict__ ccnt, const int32_t* __restrict__ chead, const int32_t* __restrict__ gnode,
+    const int32_t* __restrict__ gsize, const int32_t* __restrict__ gpar, const int32_t* __restrict__ gstart,
+    const int32_t* __restrict__ sorted, const int32_t* __restrict__ pos, int32_t* __restrict__ pend,
+    const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names, const uint8_t* __restrict__ op,
+    const uint8_t* __restrict__ w_rank, const int64_t* __restrict__ w_shape, const uint8_t* __restrict__ w_train,
+    const int64_t* __restrict__ in_off, const int32_t* __restrict__ in_idx, const int32_t* __restrict__ depth,
+    int32_t min_dup, int32_t* __restrict__ gparent, uint8_t* __restrict__ residual, uint8_t* __restrict__ gaccept,
+    uint64_t seed, const uint64_t* __restrict__ hall, uint64_t* __restrict__ ppoly, uint64_t* __restrict__ ph,
+    uint64_t* __restrict__ rh, int32_t* __restrict__ collision, HashStats* __restrict__ st) {
+  const int32_t* pend_l = pend + (int64_t)(level - 1) * n;
+  int32_t nnext = 0, nacc = 0, est = 0;
+  bool bad = false;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = base + (threadIdx.x & 31);
+    bool next = false;
+    uint64_t key = 0;
+    if (v < n && alive[v] == level) {
+      const uint32_t sl = nslot[v];
+      const int32_t g = tgid[sl];
+      const int32_t h = gnode[g];
+      const int32_t pl = pend_l[v];
+      // same prefix string as the group head: the same parent group (whose
+      // prefixes the previous level verified) and the same last component
+      {
+        const int32_t phd = pend_l[h];
+        const int64_t cv = level > 1 ? (int64_t)pend_l[v - n] + 1 : 0;
+        const int64_t ch = level > 1 ? (int64_t)pend_l[h - n] + 1 : 0;
+        if (gparent[v] != gpar[g] || pl - cv != phd - ch ||
+            !bytes_eq(names + name_off[v] + cv, names + name_off[h] + ch, pl - cv))
+          bad = true;
+      }
+      const uint32_t cs = gcs[g];
+      const int32_t hg = chead[cs];
+      const int32_t csz = ccnt[cs];
+      if (csz >= 2 && hg != g) {
+        if (gsize[g] != gsize[hg] || gpar[g] != gpar[hg]) {
+          bad = true;
+        } else {
+          const int32_t b = sorted[gstart[hg] + pos[v]];
+          const uint32_t slb = nslot[b];
+          const int64_t la = name_off[v + 1] - name_off[v];
+          const int64_t lb = name_off[b + 1] - name_off[b];
+          const int32_t plb = pend_l[b];
+          int64_t sa = pl > 0 ? pl + 1 : 0, sb = plb > 0 ? plb + 1 : 0;
+          sa = sa > la ? la : sa;
+          sb = sb > lb ? lb : sb;
+          if (la - sa != lb - sb || !bytes_eq(names + name_off[v] + sa, names + name_off[b] + sb, la - sa)) bad = true;
+          if (op[v] != op[b] || w_rank[v] != w_rank[b] || w_train[v] != w_train[b]) bad = true;
+          for (int k = 0; k < w_rank[v]; k++)
+            if (w_shape[v * SP_MAX_RANK + k] != w_shape[(int64_t)b * SP_MAX_RANK + k]) bad = true;
+          // internal producers (deduplicated inputs) as canonical positions: equal sets
+          int ka = 0, kb = 0;
+          for (int64_t e = in_off[b]; e < in_off[b + 1]; e++) {
+            const int32_t r = in_idx[e];
+            kb += alive[r] == level && nslot[r] == slb;
           }
-          if (!found) bad = true;
+          for (int64_t e = in_off[v]; e < in_off[v + 1]; e++) {
+            const int32_t r = in_idx[e];
+            if (alive[r] != level || nslot[r] != sl) continue;
+            ka++;
+            const int32_t pr = pos[r];
+            bool found = false;
+            for (int64_t f = in_off[b]; f < in_off[b + 1] && !found; f++) {
+              const int32_t q = in_idx[f];
+              found = alive[q] == level && nslot[q] == slb && pos[q] == pr;
+            }
+            bad = bad || !found;
+          }
+          bad = bad || ka != kb;
         }
-        if (ka != kb) bad = true;
+      }
+      const bool acc = csz >= min_dup;
+      if (h == (int32_t)v) {
+        gaccept[g] = acc;
+        nacc += acc;
+      }
+      if (acc) {
+        alive_next[v] = 0;
+      } else if (depth[v] <= level) {
+        residual[v] = 1;
+        alive_next[v] = 0;
+      } else {
+        alive_next[v] = (uint8_t)(level + 1);
+        gparent[v] = g;
+        nnext++;
+        next = level < D;
+        if (next) key = node_keys(v, n, level, name_off, names, seed, hall, ppoly, pend, ph, rh);
       }
     }
-    if (bad) atomicExch(collision, 1);
+    const int32_t c = warp_boundaries(next, key);
+    if ((threadIdx.x & 31) == 0) est += c;
   }
-}
-
-// accept / residual / descend; level counters
-__global__ void __launch_bounds__(256) k_hg_accept(int64_t n, uint8_t* __restrict__ alive, int32_t level,
-                                                   const uint32_t* __restrict__ nslot, const int32_t* __restrict__ tgid,
-                                                   const uint32_t* __restrict__ gcs, const int32_t* __restrict__ ccnt,
-                                                   const int32_t* __restrict__ gnode, const int32_t* __restrict__ depth,
-                                                   int32_t min_dup, int32_t* __restrict__ gparent,
-                                                   uint8_t* __restrict__ residual, uint8_t* __restrict__ gaccept,
-                                                   HashStats* __restrict__ st) {
-  int32_t nnext = 0, nacc = 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-    if (alive[v] != level) continue;
-    const int32_t g = tgid[nslot[v]];
-    const bool acc = ccnt[gcs[g]] >= min_dup;
-    if (gnode[g] == (int32_t)v) {
-      gaccept[g] = acc;
-      nacc += acc;
-    }
-    if (acc) {
-      alive[v] = 0;
-    } else if (depth[v] <= level) {
-      residual[v] = 1;
-      alive[v] = 0;
-    } else {
-      alive[v] = (uint8_t)(level + 1);
-      gparent[v] = g;
-      nnext++;
-    }
-  }
-  nnext = __reduce_add_sync(0xffffffffu, (unsigned)nnext);
-  nacc = __reduce_add_sync(0xffffffffu, (unsigned)nacc);
-  __shared__ int32_t s[2][8];
-  if ((threadIdx.x & 31) == 0) {
-    s[0][threadIdx.x >> 5] = nnext;
-    s[1][threadIdx.x >> 5] = nacc;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t a = 0, b = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
-      a += s[0][w];
-      b += s[1][w];
-    }
-    if (a) atomicAdd(&st->nnext, a);
-    if (b) atomicAdd(&st->nacc, b);
-  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(collision, 1);
+  block_add(nnext, &st->nnext);
+  block_add(nacc, &st->nacc);
+  block_add(est, &st->est);
 }
 
 static uint32_t table_cap(int64_t need) {
@@ -2276,7 +2316,7 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
   DevBuf<uint32_t> nslot, gcs;
   DevBuf<uint64_t> ph, rh, sh, hall, ppoly;
   DevBuf<unsigned long long> tkey, tgkey, gkey, ckey;
-  DevBuf<uint8_t> alive, residual, gaccept;
+  DevBuf<uint8_t> alive, alive2, residual, gaccept;
   DevBuf<HashStats> st;
   depth.alloc(n, s);
   pend.alloc((size_t)n * D, s);  // level-major; depth dd written at level dd + 1
@@ -2294,6 +2334,7 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
   sorted.alloc(n, s);
   gparent.alloc(n, s);
   alive.alloc(n, s);
+  alive2.alloc(n, s);
   residual.alloc(n, s);
   collision.alloc(1, s);
   tie.alloc(1, s);
@@ -2320,9 +2361,8 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
   SP_CUDA(cudaMemsetAsync(tie.p, 0, sizeof(int32_t), s));
   // level 1's group-count bound; later levels get theirs with the previous level's counters
   SP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(HashStats), s));
-  SP_LAUNCH(ctx, k_hg_keys, gn, 256, 0, s, n, alive.p, 1, dg->name_off.p, dg->names.p, seed, hall.p, ppoly.p, pend.p,
-            ph.p, rh.p);
-  SP_LAUNCH(ctx, k_hg_estimate, gn, 256, 0, s, n, alive.p, 1, ph.p, st.p);
+  SP_LAUNCH(ctx, k_hg_keys1, gn, 256, 0, s, n, dg->name_off.p, dg->names.p, seed, hall.p, ppoly.p, pend.p, ph.p, rh.p,
+            st.p);
   SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   g_d2h_bytes += sizeof(HashStats);
@@ -2330,12 +2370,15 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
   std::vector<LevelBlocks> lblocks;
   int64_t nA = n;
   int32_t levels = 0;
-  for (int32_t level = 1; nA > 0; level++) {
+  // the level's node states are read-only while the level runs; its end writes
+  // the next level's into the other buffer (stale entries are older levels)
+  uint8_t* cur = alive.p;
+  uint8_t* nxt = alive2.p;
+  for (int32_t level = 1; nA > 0; level++, std::swap(cur, nxt)) {
     if (level > D) throw Error(SP_ERR_CUDA, "fold did not terminate");
     const int32_t dd = level - 1;
     const uint64_t* ph_l = ph.p;
     const uint64_t* rh_l = rh.p;
-    const int32_t* pend_l = pend.p + (size_t)dd * n;
     // 1. groups: find-or-insert the prefix hash into a table of >= 2 x the
     //    group-count bound (no overflow possible; every later per-group array
     //    and the class table are sized by the bound, the exact count stays on
@@ -2351,12 +2394,11 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
     SP_CUDA(cudaMemsetAsync(tgkey.p, 0, (size_t)cap * 8, s));
     SP_CUDA(cudaMemsetAsync(tcnt.p, 0, (size_t)cap * 4, s));
     SP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(HashStats), s));
-    SP_LAUNCH(ctx, k_hg_insert, gn, 256, 0, s, n, alive.p, level, ph_l, tkey.p, thead.p, cap - 1, cap, nslot.p, st.p);
-    // 2. group sizes and template-key sums per slot
-    SP_LAUNCH(ctx, k_hg_entry, gn, 256, 0, s, n, alive.p, level, nslot.p, rh_l, sh.p, dg->in_off.p, dg->in_idx.p,
-              tgkey.p, tcnt.p);
+    SP_LAUNCH(ctx, k_hg_insert, gn, 256, 0, s, n, cur, level, ph_l, tkey.p, thead.p, cap - 1, cap, nslot.p, st.p);
+    // 2. group sizes and template-key sums per slot; head flags
+    SP_LAUNCH(ctx, k_hg_entry, gn, 256, 0, s, n, cur, level, nslot.p, rh_l, sh.p, dg->in_off.p, dg->in_idx.p, thead.p,
+              hf.p, tgkey.p, tcnt.p);
     // 3. compact group ids (heads in node order) and per-group arrays
-    SP_LAUNCH(ctx, k_hg_headflag, gn, 256, 0, s, n, alive.p, level, nslot.p, thead.p, hf.p);
     {
       size_t t = ctx->cub_tmp.n;
       ctx->cub_calls++;
@@ -2394,21 +2436,15 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
     SP_LAUNCH(ctx, k_hc_count, gg, 256, 0, s, gmax, &st.p->nG, gcs.p, ccnt.p);
     // 5. member segments + canonical order (multi-group / accepted classes only)
     SP_CUDA(cudaMemsetAsync(gfill.p, 0, (size_t)gmax * 4, s));
-    SP_LAUNCH(ctx, k_hg_place, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
+    SP_LAUNCH(ctx, k_hg_place, gn, 256, 0, s, n, cur, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
               gfill.p, seg.p, li.p);
-    SP_LAUNCH(ctx, k_hg_rank, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
+    SP_LAUNCH(ctx, k_hg_rank, gn, 256, 0, s, n, cur, level, nslot.p, tgid.p, gcs.p, ccnt.p, min_dup, gstart.p,
               gsize.p, seg.p, li.p, rh_l, sorted.p, pos.p, collision.p, st.p);
-    // 6. exact verification, then accept / residual / descend
-    SP_LAUNCH(ctx, k_hg_verify, gn, 128, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, chead.p, gnode.p,
-              gsize.p, gpar.p, gstart.p, sorted.p, pos.p, pend_l, dg->name_off.p, dg->names.p, dg->op.p, dg->w_rank.p,
-              dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, collision.p);
-    SP_LAUNCH(ctx, k_hg_accept, gn, 256, 0, s, n, alive.p, level, nslot.p, tgid.p, gcs.p, ccnt.p, gnode.p, depth.p,
-              min_dup, gparent.p, residual.p, gaccept.p, st.p);
-    if (level < D) {  // the next level's keys and group-count bound
-      SP_LAUNCH(ctx, k_hg_keys, gn, 256, 0, s, n, alive.p, level + 1, dg->name_off.p, dg->names.p, seed, hall.p,
-                ppoly.p, pend.p, ph.p, rh.p);
-      SP_LAUNCH(ctx, k_hg_estimate, gn, 256, 0, s, n, alive.p, level + 1, ph.p, st.p);
-    }
+    // 6. exact verification, accept / residual / descend, the next level's keys
+    SP_LAUNCH(ctx, k_hg_finish, gn, 128, 0, s, n, cur, nxt, level, D, nslot.p, tgid.p, gcs.p, ccnt.p, chead.p,
+              gnode.p, gsize.p, gpar.p, gstart.p, sorted.p, pos.p, pend.p, dg->name_off.p, dg->names.p, dg->op.p,
+              dg->w_rank.p, dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, depth.p, min_dup, gparent.p,
+              residual.p, gaccept.p, seed, hall.p, ppoly.p, ph.p, rh.p, collision.p, st.p);
     SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
     g_d2h_bytes += sizeof(HashStats);

@@ -52,15 +52,6 @@ __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
   return k;
 }
 
-__device__ __forceinline__ uint64_t upow(uint64_t b, int64_t e) {
-  uint64_t r = 1;
-  while (e) {
-    if (e & 1) r *= b;
-    b *= b;
-    e >>= 1;
-  }
-  return r;
-}
 
 __global__ void k_depth(const int64_t* __restrict__ off, const uint8_t* __restrict__ s, int64_t n,
                         int32_t* __restrict__ depth, int32_t* __restrict__ maxd) {
@@ -84,47 +75,39 @@ __device__ __forceinline__ void name_hash_one(int64_t i, const int64_t* __restri
                             uint64_t* __restrict__ ph, uint64_t* __restrict__ rh, int64_t si, int64_t sd) {
   const uint8_t* p = s + off[i];
   const int64_t L = off[i + 1] - off[i];
+  // forward: prefix ends and prefix hashes (h = poly(p[0:k])), straight to the
+  // outputs at each '/' (no per-thread arrays)
   uint64_t h = 0;
   int d = 0;
-  // prefix ends and prefix hashes; h tracks poly(p[0:k])
-  uint64_t hpre[64];
-  int32_t ends[64];
   for (int64_t k = 0; k <= L; k++) {
     if (k == L || p[k] == '/') {
-      if (d < D && d < 64) {
-        ends[d] = (int32_t)k;
-        hpre[d] = h;
+      if (d < D) {
+        pend[i * si + d * sd] = (int32_t)k;
+        ph[i * si + d * sd] = fmix64(h ^ fmix64(seed + (uint64_t)k));
       }
       d++;
       if (k == L) break;
     }
     h = h * kPolyB + (uint64_t)p[k] + 1;
   }
-  const uint64_t hall = h;
   const int dn = d;  // node depth
-  for (int dd = 0; dd < D; dd++) {
-    const int64_t idx = i * si + dd * sd;
-    if (dd >= dn || dd >= 64) {
-      pend[idx] = (int32_t)L;
-      ph[idx] = 0;
-      rh[idx] = 0;
-      continue;
+  const uint64_t seed_r = seed ^ 0x9e3779b97f4a7c15ULL;
+  // backward: rel = the suffix after each prefix (r = poly of p[k+1:L] read
+  // backwards), the node itself (rel "") at its own depth
+  if (dn - 1 < D) rh[i * si + (dn - 1) * sd] = fmix64(fmix64(seed_r));
+  uint64_t r = 0;
+  int slash = dn - 1;
+  for (int64_t k = L - 1; k >= 0; k--) {
+    if (p[k] == '/') {
+      slash--;
+      if (slash < D) rh[i * si + slash * sd] = fmix64(r ^ fmix64(seed_r + (uint64_t)(L - 1 - k)));
     }
-    const int64_t q = ends[dd];
-    pend[idx] = (int32_t)q;
-    ph[idx] = fmix64(hpre[dd] ^ fmix64(seed + (uint64_t)q));
-    // rel = p[start:L] with start = q+1 if the prefix is non-empty, else 0
-    int64_t start = q > 0 ? q + 1 : 0;
-    if (start > L) start = L;
-    // poly(p[start:L]) = poly(p[0:L]) - poly(p[0:start]) * B^(L-start)
-    uint64_t hrel;
-    if (q >= L) {
-      hrel = 0;  // the node IS the prefix: rel name is ""
-    } else {
-      const uint64_t hs = start > 0 ? hpre[dd] * kPolyB + (uint64_t)'/' + 1 : 0;  // poly(p[0:q+1])
-      hrel = hall - hs * upow(kPolyB, L - start);
-    }
-    rh[idx] = fmix64(hrel ^ fmix64((seed ^ 0x9e3779b97f4a7c15ULL) + (uint64_t)(L - start)));
+    r = r * kPolyB + (uint64_t)p[k] + 1;
+  }
+  for (int dd = dn; dd < D; dd++) {  // deeper than the node: never grouped
+    pend[i * si + dd * sd] = (int32_t)L;
+    ph[i * si + dd * sd] = 0;
+    rh[i * si + dd * sd] = 0;
   }
 }
 
@@ -1460,23 +1443,36 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   const size_t smem = (size_t)P2 * 20;
   allow_smem(ctx, k_fold_small, smem);
   SP_CUDA(cudaEventRecord(ctx->ev[6], s));
-  SP_LAUNCH(ctx, k_fold_small, 1, SMALL_THREADS, smem, s, A);
+  // one thread per bitonic compare-exchange (P2 / 2): tiny graphs pay their
+  // many block barriers with a few warps, not 32
+  const int threads = std::min(SMALL_THREADS, std::max(64, P2 / 2));
+  SP_LAUNCH(ctx, k_fold_small, 1, threads, smem, s, A);
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaEventRecord(ctx->ev[7], s));
-  // single D2H: outputs (i32 region after scratch), pend, residual + gaccept
-  std::vector<int32_t> h_out(i32_out), pend_h(nd);
-  std::vector<uint8_t> h_u8(nd + n);
-  g_d2h_bytes += (int64_t)(i32_out * 4 + nd * 4 + nd + n);
-  SP_CUDA(cudaMemcpyAsync(h_out.data(), out0, i32_out * 4, cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaMemcpyAsync(pend_h.data(), A.pend, nd * 4, cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaMemcpyAsync(h_u8.data(), u8.p, nd + n, cudaMemcpyDeviceToHost, s));
+  // outputs (i32 region after scratch), pend, residual + gaccept into one pinned block
+  const size_t b_out = i32_out * 4, b_pend = nd * 4, b_u8 = nd + n;
+  size_t pin_bytes = 0;
+  uint8_t* pin = pinned_acquire(ctx, b_out + b_pend + b_u8, &pin_bytes);
+  struct Release {
+    sp_ctx* ctx;
+    uint8_t* p;
+    size_t n;
+    ~Release() { pinned_release(ctx, p, n); }
+  } rel{ctx, pin, pin_bytes};
+  g_d2h_bytes += (int64_t)(b_out + b_pend + b_u8);
+  SP_CUDA(cudaMemcpyAsync(pin, out0, b_out, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(pin + b_out, A.pend, b_pend, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(pin + b_out + b_pend, u8.p, b_u8, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
+  const int32_t* h_out_p = (const int32_t*)pin;
+  std::vector<int32_t> pend_h((const int32_t*)(pin + b_out), (const int32_t*)(pin + b_out) + nd);
+  const uint8_t* h_u8 = pin + b_out + b_pend;
   {
     float ms = 0;
     SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
     ctx->fold_device_ms = ms;
   }
-  const int32_t* h_sorted = h_out.data();
+  const int32_t* h_sorted = h_out_p;
   const int32_t* h_gstart = h_sorted + nd;
   const int32_t* h_corder = h_gstart + nd1;
   const int32_t* h_cstart = h_corder + nd;
@@ -1496,10 +1492,10 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
     lv.gstart.assign(h_gstart + (size_t)dd * (n + 1), h_gstart + (size_t)dd * (n + 1) + nG + 1);
     lv.corder.assign(h_corder + (size_t)dd * n, h_corder + (size_t)dd * n + nG);
     lv.cstart.assign(h_cstart + (size_t)dd * (n + 1), h_cstart + (size_t)dd * (n + 1) + nC + 1);
-    lv.gaccept.assign(h_u8.begin() + (size_t)dd * n, h_u8.begin() + (size_t)dd * n + nG);
+    lv.gaccept.assign(h_u8 + (size_t)dd * n, h_u8 + (size_t)dd * n + nG);
     levels.push_back(std::move(lv));
   }
-  std::vector<uint8_t> resid_h(h_u8.begin() + nd, h_u8.begin() + nd + n);
+  std::vector<uint8_t> resid_h(h_u8 + nd, h_u8 + nd + n);
   fold_finalize(dg, levels, resid_h, pend_h, D, out);
 }
 

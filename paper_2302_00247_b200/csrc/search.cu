@@ -2622,8 +2622,32 @@ struct TablesPriv {
   // recorded behind k_fill: work on the auxiliary stream (explain_all) waits
   // for the tables, not for whatever was queued on the main stream since
   cudaEvent_t built = nullptr;
+  // packed uploads of the build (one H2D per phase) and their pinned staging
+  DevBuf<uint8_t> arena, arena2;
+  sp_ctx* ctx = nullptr;
+  uint8_t* pin = nullptr;
+  size_t pin_bytes = 0;
   ~TablesPriv() {
     if (built) cudaEventDestroy(built);
+    if (pin && ctx) pinned_release(ctx, pin, pin_bytes);
+  }
+  // a pinned block of >= `need` bytes owned by the tables (the stream is
+  // synchronised before it is reused or released)
+  uint8_t* pinned(size_t need) {
+    if (pin && pin_bytes >= need) return pin;
+    if (pin) pinned_release(ctx, pin, pin_bytes);
+    pin = pinned_acquire(ctx, need, &pin_bytes);
+    return pin;
+  }
+  // ONE H2D of every part of `pk` into `into` (the device arena)
+  uint8_t* upload(const PackedUpload& pk, DevBuf<uint8_t>& into, cudaStream_t s) {
+    uint8_t* h = pinned(pk.total);
+    for (const auto& part : pk.parts)
+      if (part.bytes) std::memcpy(h + part.off, part.src, part.bytes);
+    into.alloc(std::max<size_t>(pk.total, 16), s);
+    if (pk.total) SP_CUDA(cudaMemcpyAsync(into.p, h, pk.total, cudaMemcpyHostToDevice, s));
+    g_h2d_bytes += (int64_t)pk.total;
+    return into.p;
   }
 };
 
@@ -2734,16 +2758,30 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   }
   TablesPriv* priv = new TablesPriv();
   out->priv = priv;
+  priv->ctx = ctx;
   priv->mesh = *mesh;
   priv->mu = mu;
   priv->chunk = chunk;
   TableDev& D = priv->dev;
-  out->d_tmpl_off.upload(out->tmpl_off.data(), nb + 1, s);
-  out->d_tmpl_nodes.upload(out->tmpl_nodes.data(), ne, s);
-  D.slot_of.upload(slot_of.data(), ne, s);
-  D.ref_slot_of.upload(ref_slot_of.data(), ne, s);
+  // the host-built arrays in one H2D (pinned staging, packed arena)
   DevBuf<uint8_t> radix_d;
-  radix_d.upload(radix_of.data(), ne, s);
+  DevBuf<BlobHeader> hdr;
+  {
+    PackedUpload pk;
+    const size_t o_off = pk.add(out->tmpl_off.data(), (nb + 1) * sizeof(int64_t));
+    const size_t o_nodes = pk.add(out->tmpl_nodes.data(), ne * sizeof(int32_t));
+    const size_t o_slot = pk.add(slot_of.data(), ne * sizeof(slot_of[0]));
+    const size_t o_ref = pk.add(ref_slot_of.data(), ne * sizeof(ref_slot_of[0]));
+    const size_t o_radix = pk.add(radix_of.data(), ne);
+    const size_t o_hdr = pk.add(out->hdr.data(), nb * sizeof(BlobHeader));
+    uint8_t* a = priv->upload(pk, priv->arena, s);
+    out->d_tmpl_off.set_view((int64_t*)(a + o_off), nb + 1);
+    out->d_tmpl_nodes.set_view((int32_t*)(a + o_nodes), ne);
+    D.slot_of.set_view((decltype(D.slot_of.p))(a + o_slot), ne);
+    D.ref_slot_of.set_view((decltype(D.ref_slot_of.p))(a + o_ref), ne);
+    radix_d.set_view(a + o_radix, ne);
+    hdr.set_view((BlobHeader*)(a + o_hdr), nb);
+  }
   D.node_block.alloc(n, s);
   D.node_tpos.alloc(n, s);
   SP_CUDA(cudaMemsetAsync(D.node_block.p, 0xff, n * sizeof(int32_t), s));
@@ -2761,19 +2799,26 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   SP_CUDA(cudaMemsetAsync(D.ext_cons.p, 0, n, s));
   SP_LAUNCH(ctx, k_boundary, grid_for(n, ctx->sm_count), 256, 0, s, G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
   DevBuf<EntryLayout> lay;
-  DevBuf<BlobHeader> hdr;
   DevBuf<int64_t> blob_bytes;
   lay.alloc(ne, s);
-  hdr.upload(out->hdr.data(), nb, s);
   blob_bytes.alloc(nb + 1, s);
   const int gb = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), 65535);
   if (nb > 0)
     SP_LAUNCH(ctx, k_layout, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
               D.node_tpos.p, D.slot_of.p, radix_d.p, lay.p, hdr.p, blob_bytes.p, err.p);
+  // errors + the laid-out headers back in one pinned block (the staging block is
+  // free again: its H2D is ordered before these copies)
   int32_t err_h[2];
-  err.download(err_h, 2, s);
-  hdr.download(out->hdr.data(), nb, s);
-  SP_CUDA(cudaStreamSynchronize(s));
+  {
+    const size_t hb = (size_t)nb * sizeof(BlobHeader);
+    uint8_t* h = priv->pinned(hb + 16);
+    SP_CUDA(cudaMemcpyAsync(h, err.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (nb) SP_CUDA(cudaMemcpyAsync(h + 16, hdr.p, hb, cudaMemcpyDeviceToHost, s));
+    g_d2h_bytes += (int64_t)(8 + hb);
+    SP_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(err_h, h, sizeof(err_h));
+    if (nb) std::memcpy(out->hdr.data(), h + 16, hb);
+  }
   if (err_h[0] == 1) throw Error(SP_ERR_CONFIG, "a node appears in more than one template");
   if (err_h[0] == 2) throw Error(SP_ERR_CONFIG, "template is not in topological order");
   if (err_h[0] == 3)
@@ -2790,13 +2835,17 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   }
   out->blobs.alloc(std::max<int64_t>(out->blob_off[nb], 16), s);
   D.bound.alloc(ne, s);
-  out->d_blob_off.upload(out->blob_off.data(), nb + 1, s);
   {
     std::vector<int64_t> xo(nb + 1, 0);
     for (int64_t b = 0; b < nb; b++)
       xo[b + 1] = xo[b] + align16((int64_t)sizeof(XNode) * out->hdr[b].T + (int64_t)sizeof(XEdge) * out->hdr[b].n_prod);
     D.xinfo.alloc(std::max<int64_t>(xo[nb], 16), s);
-    D.xoff.upload(xo.data(), nb + 1, s);
+    PackedUpload pk;
+    const size_t o_blob = pk.add(out->blob_off.data(), (nb + 1) * sizeof(int64_t));
+    const size_t o_x = pk.add(xo.data(), (nb + 1) * sizeof(int64_t));
+    uint8_t* a = priv->upload(pk, priv->arena2, s);
+    out->d_blob_off.set_view((int64_t*)(a + o_blob), nb + 1);
+    D.xoff.set_view((int64_t*)(a + o_x), nb + 1);
   }
   if (nb > 0)
     SP_LAUNCH(ctx, k_fill, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,

@@ -45,26 +45,35 @@ struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool view = false;  // p points into memory another buffer owns
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), view(o.view) { o.p = nullptr; o.n = 0; o.view = false; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; s = o.s;
-      o.p = nullptr; o.n = 0;
+      p = o.p; n = o.n; s = o.s; view = o.view;
+      o.p = nullptr; o.n = 0; o.view = false;
     }
     return *this;
   }
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !view) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    view = false;
+  }
+  // view `count` elements at `at` (owned elsewhere, e.g. a packed upload arena)
+  void set_view(T* at, size_t count) {
+    release();
+    p = at;
+    n = count;
+    view = true;
   }
   void alloc(size_t count, cudaStream_t stream) {
-    if (count <= n && p) return;
+    if (count <= n && p && !view) return;
     release();
     s = stream;
     n = count;
@@ -81,6 +90,25 @@ struct DevBuf {
   }
   void zero(cudaStream_t stream) {
     if (n) SP_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), stream));
+  }
+};
+
+// Several host arrays to the device with ONE copy: packed (16-byte aligned)
+// into a pinned staging block, copied into one device arena; add() returns
+// each array's device address.  The staging block and the arena live as long
+// as the Packed object (its owner frees it after syncing the stream).
+struct PackedUpload {
+  struct Part {
+    const void* src;
+    size_t bytes, off;
+  };
+  std::vector<Part> parts;
+  size_t total = 0;
+  size_t add(const void* src, size_t bytes) {
+    parts.push_back({src, bytes, total});
+    const size_t at = total;
+    total += (bytes + 15) & ~(size_t)15;
+    return at;
   }
 };
 

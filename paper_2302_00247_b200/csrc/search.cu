@@ -1799,6 +1799,168 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
   flush(lb);
 }
 
+// Prefix-skipping scorer without work items: every CTA walks the blocks in
+// order, stages a block's tables once, and its warps claim 4096-candidate
+// chunks of that block straight from the block's global chunk counter (the
+// next claim is issued before the current chunk is walked, so its latency is
+// hidden).  A chunk's cost varies by orders of magnitude (a run of proven
+// failures costs one walk, a region of valid candidates one walk per 32), so
+// balance comes from the whole GPU sharing one counter per block; the CTA
+// meets at a barrier only when the block is exhausted.  Each CTA that worked
+// on a block appends one record (its warps' argmin + valid count) to the
+// block's contribution list; k_reduce_contrib merges them.  Sharded searches
+// deal chunk c of a block to rank c mod n_shards.
+struct SkipPlan {
+  const int64_t* blob_off;
+  const unsigned long long* nch;  // this rank's chunks per block
+  unsigned long long* ctr;        // per block: chunks claimed (zeroed)
+  uint32_t* contrib;              // per block: records appended (zeroed)
+  int64_t nb;
+  uint32_t shard, n_shards;
+};
+
+__global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(const uint8_t* __restrict__ blobs,
+                                                                            SkipPlan P, ItemOut* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int NW = THREADS / 32;
+  constexpr uint32_t CH = SKIP_CHUNK;
+  __shared__ uint64_t s_lane_add[32];
+  __shared__ Biased s_bz;
+  __shared__ uint64_t s_p2[64];  // unbiased digits of 2^k * CH (mixed radix, wrapping)
+  __shared__ unsigned long long s_first;  // the chunk the CTA claimed before staging the block
+  __shared__ unsigned long long s_red_t[NW], s_red_i[NW], s_red_v[NW];
+  __shared__ uint32_t s_red_n[NW];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int64_t b = 0; b < P.nb; b++) {
+    const unsigned long long nch = P.nch[b];
+    // claim a chunk first: a block whose chunks are gone is neither staged nor visited
+    if (tid == 0)
+      s_first = *(volatile unsigned long long*)&P.ctr[b] < nch ? atomicAdd(&P.ctr[b], 1ULL) : nch;
+    __syncthreads();
+    if (s_first >= nch) continue;
+    stage_block(smem, blobs, P.blob_off[b], s_lane_add, &s_bz, nullptr, 1, 0, false);
+    if (tid == 0) {
+      // unbiased digits of 2^k * CH (positions fastest-last, as bencode), by
+      // doubling: biased(2x) = badd(biased(x), x), minus the biases
+      const BlobHeader& H = *(const BlobHeader*)smem;
+      uint64_t a = 0;
+      uint32_t x = CH;
+      for (int q = H.V - 1; q >= 0 && x; q--) {
+        const uint32_t r = ((H.radix3 >> q) & 1) ? 3 : 2;
+        a |= (uint64_t)(x % r) << (2 * (H.V - 1 - q));
+        x /= r;
+      }
+      const uint64_t B = s_bz.B;
+      for (int k = 0; k < 64; k++) {
+        s_p2[k] = a;
+        a = badd(badd(B, a, B), a, B) - B;
+      }
+    }
+    __syncthreads();
+    const Tabs S = tabs_of(smem);
+    const BlobHeader& H = *S.H;
+    const uint32_t rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
+    const uint32_t pool = (uint32_t)__cvta_generic_to_shared(S.reach);
+    const uint32_t rb = opaque_u32(pool + 8u * (uint32_t)tid);
+    const uint32_t sb = opaque_u32(pool + (uint32_t)H.npool * THREADS * 8u + (uint32_t)tid);
+    const unsigned long long C = H.C;
+    LaneBest lb;
+    unsigned long long j = 0;
+    if (lane == 0) j = warp == 0 ? s_first : atomicAdd(&P.ctr[b], 1ULL);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    while (j < nch) {
+      unsigned long long jn = 0;
+      if (lane == 0) jn = atomicAdd(&P.ctr[b], 1ULL);  // the next claim, in flight during the walk
+      const unsigned long long c = j * P.n_shards + P.shard;
+      const unsigned long long start = c * CH;
+      const uint32_t rem = (uint32_t)min((unsigned long long)CH, C - start);
+      uint64_t w = s_bz.B;  // biased digits of start = c * CH: one add per set bit of c
+      for (unsigned long long m = c; m; m &= m - 1) w = badd(w, s_p2[__ffsll((long long)m) - 1], s_bz.B);
+      w = badd(w, s_lane_add[lane], s_bz.B);
+      score_chunk<true, false>(S, s_bz, s_lane_add, rec0, rb, sb, lane, w, rem, start + rem, lb);
+      j = __shfl_sync(0xffffffffu, jn, 0);
+    }
+    // the CTA's record for this block
+    unsigned long long bt = lb.t, bi = lb.t != ~0ULL ? ref_index_b(S, lb.w) : ~0ULL, nv = lb.valid;
+    uint32_t bn = lb.n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, bt, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, bi, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, bn, o);
+      nv += __shfl_down_sync(0xffffffffu, nv, o);
+      if (key_less(t2, n2, i2, bt, bn, bi)) {
+        bt = t2;
+        bn = n2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      s_red_t[warp] = bt;
+      s_red_i[warp] = bi;
+      s_red_n[warp] = bn;
+      s_red_v[warp] = nv;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      ItemOut o{s_red_t[0], s_red_i[0], s_red_n[0], s_red_v[0]};
+      for (int w2 = 1; w2 < NW; w2++) {
+        o.valid += s_red_v[w2];
+        if (key_less(s_red_t[w2], s_red_n[w2], s_red_i[w2], o.total_bits, o.num_split, o.index)) {
+          o.total_bits = s_red_t[w2];
+          o.num_split = s_red_n[w2];
+          o.index = s_red_i[w2];
+        }
+      }
+      const uint32_t k = atomicAdd(&P.contrib[b], 1u);
+      out[b * (int64_t)gridDim.x + k] = o;
+    }
+    __syncthreads();  // the tables of the next block overwrite smem
+  }
+}
+
+// One CTA per block: merge the contribution records of k_score_skip.
+__global__ void k_reduce_contrib(const ItemOut* __restrict__ rec, const uint32_t* __restrict__ contrib, int64_t stride,
+                                 int64_t nb, sp_score_out* __restrict__ out) {
+  __shared__ ItemOut s[THREADS];
+  __shared__ unsigned long long sv[THREADS];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    ItemOut acc{~0ULL, ~0ULL, 0xFFFFFFFFu, 0};
+    unsigned long long valid = 0;
+    const uint32_t cnt = contrib[b];
+    for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+      const ItemOut o = rec[b * stride + k];
+      valid += o.valid;
+      if (key_less(o.total_bits, o.num_split, o.index, acc.total_bits, acc.num_split, acc.index)) acc = o;
+    }
+    s[threadIdx.x] = acc;
+    sv[threadIdx.x] = valid;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+      if (threadIdx.x < st) {
+        const ItemOut o = s[threadIdx.x + st];
+        if (key_less(o.total_bits, o.num_split, o.index, s[threadIdx.x].total_bits, s[threadIdx.x].num_split,
+                     s[threadIdx.x].index))
+          s[threadIdx.x] = o;
+        sv[threadIdx.x] += sv[threadIdx.x + st];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      sp_score_out r;
+      r.candidates = 0;
+      r.valid = sv[0];
+      r.has_best = s[0].index != ~0ULL && sv[0] > 0;
+      r.best_index = r.has_best ? s[0].index : 0;
+      r.best_total = r.has_best ? __longlong_as_double((long long)s[0].total_bits) : 0.0;
+      r.best_num_split = r.has_best ? (int32_t)s[0].num_split : 0;
+      out[b] = r;
+    }
+    __syncthreads();
+  }
+}
+
 // Memoised brute force: every candidate of the range is visited (32 per warp
 // step, consecutive enumeration indices), but a node is re-routed only when a
 // digit of its ancestor cone changed since the lane's previous candidate
@@ -2914,6 +3076,46 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
                               : smem;
   if (smem_k > ctx->smem_optin)
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem_k) + " bytes)");
+  // prefix skipping on narrow blocks: per-block chunk counters, no work items
+  // (SP_SCORE_ITEMS=1 / SP_SKIP_ITEMS=1 select the item kernels: A/B checks)
+  if (ctx->skip && !wide && !generic && !memo && !items_mode && !flow_skip && getenv("SP_SKIP_ITEMS") == nullptr) {
+    allow_smem(ctx, k_score_skip, smem);
+    int per = resident_ctas(ctx, k_score_skip, THREADS, smem);
+    if (per < 1) per = 1;
+    const int64_t grid = (int64_t)ctx->sm_count * per;
+    const unsigned long long N = (unsigned long long)n_shards, r = (unsigned long long)shard;
+    std::vector<unsigned long long> plan(3 * nb, 0);
+    unsigned long long any = 0;
+    for (int64_t b = 0; b < nb; b++) {
+      const unsigned long long C = t->hdr[b].C;
+      const unsigned long long nc = C / SKIP_CHUNK + (C % SKIP_CHUNK ? 1 : 0);
+      plan[b] = nc > r ? (nc - 1 - r) / N + 1 : 0;
+      any += plan[b];
+    }
+    if (any == 0) {
+      if (!must_out) return false;
+      pd.dout.alloc(nb, s);
+      SP_CUDA(cudaMemsetAsync(pd.dout.p, 0, (size_t)nb * sizeof(sp_score_out), s));
+      SP_CUDA(cudaEventRecord(pd.ev[1], s));
+      SP_CUDA(cudaEventRecord(pd.ev[2], s));
+      SP_CUDA(cudaEventRecord(pd.ev[3], s));
+      return true;
+    }
+    pd.dplan.upload(plan.data(), plan.size(), s);  // nch | ctr | contrib
+    SP_CUDA(cudaMemsetAsync(pd.dplan.p + nb, 0, (size_t)2 * nb * sizeof(unsigned long long), s));
+    pd.items.alloc((size_t)nb * grid, s);
+    pd.dout.alloc(nb, s);
+    SkipPlan SPn{t->d_blob_off.p, pd.dplan.p, pd.dplan.p + nb, (uint32_t*)(pd.dplan.p + 2 * nb), nb, (uint32_t)shard,
+                 (uint32_t)n_shards};
+    SP_CUDA(cudaEventRecord(pd.ev[1], s));
+    SP_LAUNCH(ctx, k_score_skip, (unsigned)grid, THREADS, smem, s, t->blobs.p, SPn, pd.items.p);
+    SP_CUDA(cudaEventRecord(pd.ev[2], s));
+    SP_LAUNCH(ctx, k_reduce_contrib, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, pd.items.p, SPn.contrib,
+              grid, nb, pd.dout.p);
+    SP_CUDA(cudaGetLastError());
+    SP_CUDA(cudaEventRecord(pd.ev[3], s));
+    return true;
+  }
   allow_smem(ctx, kern, smem_k);
   int per_sm = resident_ctas(ctx, kern, threads, smem_k);
   if (per_sm < 1) per_sm = 1;

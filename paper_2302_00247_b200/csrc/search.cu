@@ -1812,12 +1812,14 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
 // deal chunk c of a block to rank c mod n_shards.
 struct SkipPlan {
   const int64_t* blob_off;
-  const unsigned long long* nch;  // this rank's chunks per block
-  unsigned long long* ctr;        // per block: chunks claimed (zeroed)
+  const unsigned long long* nch;  // this rank's 4096-candidate chunks per block
+  unsigned long long* ctr;        // per block: claims (zeroed)
   uint32_t* contrib;              // per block: records appended (zeroed)
   int64_t nb;
   uint32_t shard, n_shards;
+  unsigned long long tail;        // the last `tail` chunks of a block are claimed in eighths
 };
+constexpr uint32_t SKIP_SUB = 8;
 
 __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(const uint8_t* __restrict__ blobs,
                                                                             SkipPlan P, ItemOut* __restrict__ out) {
@@ -1827,18 +1829,24 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
   __shared__ uint64_t s_lane_add[32];
   __shared__ Biased s_bz;
   __shared__ uint64_t s_p2[64];  // unbiased digits of 2^k * CH (mixed radix, wrapping)
+  __shared__ uint64_t s_sub[SKIP_SUB];  // unbiased digits of k * CH / SKIP_SUB
   __shared__ unsigned long long s_first;  // the chunk the CTA claimed before staging the block
   __shared__ unsigned long long s_red_t[NW], s_red_i[NW], s_red_v[NW];
   __shared__ uint32_t s_red_n[NW];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   for (int64_t b = 0; b < P.nb; b++) {
-    const unsigned long long nch = P.nch[b];
-    // claim a chunk first: a block whose chunks are gone is neither staged nor visited
+    // claims: the first nbig chunks whole, the last `tail` ones in SKIP_SUB
+    // parts each (the final wave of a block is short: warps reach the block's
+    // end barrier together)
+    const unsigned long long nloc = P.nch[b];
+    const unsigned long long nsm = min(nloc, P.tail), nbig = nloc - nsm;
+    const unsigned long long nclaim = nbig + nsm * SKIP_SUB;
+    // claim first: a block whose chunks are gone is neither staged nor visited
     if (tid == 0)
-      s_first = *(volatile unsigned long long*)&P.ctr[b] < nch ? atomicAdd(&P.ctr[b], 1ULL) : nch;
+      s_first = *(volatile unsigned long long*)&P.ctr[b] < nclaim ? atomicAdd(&P.ctr[b], 1ULL) : nclaim;
     __syncthreads();
-    if (s_first >= nch) continue;
+    if (s_first >= nclaim) continue;
     stage_block(smem, blobs, P.blob_off[b], s_lane_add, &s_bz, nullptr, 1, 0, false);
     if (tid == 0) {
       // unbiased digits of 2^k * CH (positions fastest-last, as bencode), by
@@ -1856,6 +1864,18 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
         s_p2[k] = a;
         a = badd(badd(B, a, B), a, B) - B;
       }
+      uint64_t sub = 0;  // digits of CH / SKIP_SUB, then multiples
+      x = CH / SKIP_SUB;
+      for (int q = H.V - 1; q >= 0 && x; q--) {
+        const uint32_t r = ((H.radix3 >> q) & 1) ? 3 : 2;
+        sub |= (uint64_t)(x % r) << (2 * (H.V - 1 - q));
+        x /= r;
+      }
+      uint64_t m = 0;
+      for (uint32_t k = 0; k < SKIP_SUB; k++) {
+        s_sub[k] = m;
+        m = badd(badd(B, m, B), sub, B) - B;
+      }
     }
     __syncthreads();
     const Tabs S = tabs_of(smem);
@@ -1869,15 +1889,22 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
     unsigned long long j = 0;
     if (lane == 0) j = warp == 0 ? s_first : atomicAdd(&P.ctr[b], 1ULL);
     j = __shfl_sync(0xffffffffu, j, 0);
-    while (j < nch) {
+    while (j < nclaim) {
       unsigned long long jn = 0;
       if (lane == 0) jn = atomicAdd(&P.ctr[b], 1ULL);  // the next claim, in flight during the walk
-      const unsigned long long c = j * P.n_shards + P.shard;
-      const unsigned long long start = c * CH;
-      const uint32_t rem = (uint32_t)min((unsigned long long)CH, C - start);
-      uint64_t w = s_bz.B;  // biased digits of start = c * CH: one add per set bit of c
+      const unsigned long long jl = j < nbig ? j : nbig + (j - nbig) / SKIP_SUB;  // local chunk
+      const uint32_t part = j < nbig ? 0u : (uint32_t)((j - nbig) % SKIP_SUB);
+      const unsigned long long c = jl * P.n_shards + P.shard;  // the block's chunk
+      const unsigned long long cs = c * CH;
+      const unsigned long long start = cs + (j < nbig ? 0 : (unsigned long long)part * (CH / SKIP_SUB));
+      if (start >= C) {
+        j = __shfl_sync(0xffffffffu, jn, 0);
+        continue;
+      }
+      const uint32_t rem = (uint32_t)min((unsigned long long)(j < nbig ? CH : CH / SKIP_SUB), C - start);
+      uint64_t w = s_bz.B;  // biased digits of c * CH: one add per set bit of c
       for (unsigned long long m = c; m; m &= m - 1) w = badd(w, s_p2[__ffsll((long long)m) - 1], s_bz.B);
-      w = badd(w, s_lane_add[lane], s_bz.B);
+      w = badd(badd(w, s_sub[part], s_bz.B), s_lane_add[lane], s_bz.B);
       score_chunk<true, false>(S, s_bz, s_lane_add, rec0, rb, sb, lane, w, rem, start + rem, lb);
       j = __shfl_sync(0xffffffffu, jn, 0);
     }
@@ -3105,8 +3132,13 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     SP_CUDA(cudaMemsetAsync(pd.dplan.p + nb, 0, (size_t)2 * nb * sizeof(unsigned long long), s));
     pd.items.alloc((size_t)nb * grid, s);
     pd.dout.alloc(nb, s);
+    // SP_SKIP_TAIL=k: claim the last k chunks of a block in eighths (a shorter
+    // final wave before the block's end barrier); measured no gain on c5
+    // (7.38 ms at 0, 7.41-7.52 ms at 296-2000), so off by default
+    const char* tail_env = getenv("SP_SKIP_TAIL");
+    const unsigned long long tail = tail_env ? strtoull(tail_env, nullptr, 10) : 0ULL;
     SkipPlan SPn{t->d_blob_off.p, pd.dplan.p, pd.dplan.p + nb, (uint32_t*)(pd.dplan.p + 2 * nb), nb, (uint32_t)shard,
-                 (uint32_t)n_shards};
+                 (uint32_t)n_shards, tail};
     SP_CUDA(cudaEventRecord(pd.ev[1], s));
     SP_LAUNCH(ctx, k_score_skip, (unsigned)grid, THREADS, smem, s, t->blobs.p, SPn, pd.items.p);
     SP_CUDA(cudaEventRecord(pd.ev[2], s));

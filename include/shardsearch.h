@@ -271,6 +271,29 @@ int sp_explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, sp_explai
                    int8_t* node_detail, int8_t* edge_detail);
 
 /*
+ * Route search: the blocks the table path cannot hold (a template of more than
+ * SP_EXPLAIN_MAX_T nodes, a node with more than 6 internal producers, routing
+ * tables larger than shared memory) scored without routing tables -- every
+ * candidate routed node by node on the device (route_node: the reference's
+ * per-node pattern choice, search.py:134-224) and costed as plan_cost
+ * (costmodel.py:193-267) with reach/state in global scratch.  ref_slot[e] =
+ * the weight slot (weight_nodes order, search.py:85-88) of template entry e or
+ * -1, radix[e] its option count (2 or 3), edge_off = internal producer edges
+ * per block (prefix sums).  Scores every block (out) and returns the winners'
+ * detail in the layout of sp_explain_all, or -- with `indices` -- the detail of
+ * the given candidates only (out may be NULL).  Up to 64 internal producers
+ * per node and 2**64 candidates per block.
+ */
+int sp_route_search(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* tmpl_off, const int32_t* tmpl_nodes,
+                    const int16_t* ref_slot, const uint8_t* radix, const int64_t* edge_off, const sp_mesh* mesh,
+                    int64_t mu, int64_t chunk_size, const uint64_t* indices, sp_score_out* out,
+                    sp_explain_block* blocks, int8_t* node_detail, int8_t* edge_detail);
+/* Shared memory per CTA (opt-in) and SM count of the context's device. */
+int sp_ctx_limits(const sp_ctx* ctx, int64_t* smem_per_block, int32_t* sm_count);
+/* Per block of built tables: blob bytes, live-value pool slots, template nodes. */
+int sp_tables_block_info(const sp_tables* t, int64_t* blob_bytes, int32_t* pool_slots, int32_t* template_nodes);
+
+/*
  * Native graph ingest (host only, no context): the JSON graph document of
  * load_graph (ir.py:302-338, schema 1/2) -> ModelGraph validation and
  * lexicographic-heap toposort (ir.py:214-274) -> trim_and_group (ir.py:378-461)

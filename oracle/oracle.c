@@ -31,6 +31,11 @@
 
 #include "../include/shardsearch.h"
 
+/* templates the restatement handles (stack arrays per candidate; the
+ * reference has no limit, the route search of the backend none below 2^64
+ * candidates) */
+#define ORACLE_MAX_T 2048
+
 /* ------------------------------------------------------------------------- */
 /* graph helpers                                                             */
 
@@ -684,9 +689,9 @@ typedef struct {
 typedef struct {
   int valid;
   int fail_pos;
-  int pat[SP_EXPLAIN_MAX_T];
-  spec state[SP_EXPLAIN_MAX_T];
-  int exit_axis[SP_EXPLAIN_MAX_T];
+  int pat[ORACLE_MAX_T];
+  spec state[ORACLE_MAX_T];
+  int exit_axis[ORACLE_MAX_T];
   double forward, backward, total;
   int num_split;
   int64_t bytes[5], calls[5];
@@ -708,7 +713,7 @@ static spec weight_option(int radix, int digit) {
 
 static void eval_candidate(const block_ctx* B, uint64_t index, cand_result* R, int detail) {
   const sp_graph* g = B->g;
-  int digits[SP_EXPLAIN_MAX_T];
+  int digits[ORACLE_MAX_T];
   /* candidate_by_index (search.py:103-116): last weight varies fastest */
   uint64_t rem = index;
   for (int s = B->V - 1; s >= 0; s--) {
@@ -722,7 +727,7 @@ static void eval_candidate(const block_ctx* B, uint64_t index, cand_result* R, i
   R->fail_pos = -1;
   int64_t T = B->T;
   spec* st = R->state;
-  int pc[SP_EXPLAIN_MAX_T];          /* chosen pattern collective */
+  int pc[ORACLE_MAX_T];          /* chosen pattern collective */
   /* pattern_routing (search.py:134-224) */
   for (int64_t i = 0; i < T; i++) {
     int64_t n = B->tn[i];
@@ -796,7 +801,7 @@ static void eval_candidate(const block_ctx* B, uint64_t index, cand_result* R, i
     if (B->boundary[i] && st[i].kind != K_REPLICA) R->exit_axis[i] = st[i].kind == K_SPLIT ? st[i].axis : -2;
   }
   /* plan_cost (costmodel.py:193-267) */
-  double reach[SP_EXPLAIN_MAX_T];
+  double reach[ORACLE_MAX_T];
   for (int k = 0; k < 5; k++) R->bytes[k] = R->calls[k] = 0;
   for (int64_t i = 0; i < T; i++) {
     int64_t n = B->tn[i];
@@ -840,7 +845,7 @@ static void eval_candidate(const block_ctx* B, uint64_t index, cand_result* R, i
     if (tail > fwd) fwd = tail;
   }
   /* backward: pack_gradients (rewrite.py:78-111) over replicated trainable weights */
-  int64_t buckets[SP_EXPLAIN_MAX_T], unfused[SP_EXPLAIN_MAX_T];
+  int64_t buckets[ORACLE_MAX_T], unfused[ORACLE_MAX_T];
   int nb = 0, nu = 0;
   int64_t cur = 0;
   int cur_n = 0;
@@ -891,7 +896,8 @@ static int block_init(block_ctx* B, og* G, const int32_t* tmpl, int64_t T, const
                       int64_t mu, int64_t chunk) {
   const sp_graph* g = G->g;
   memset(B, 0, sizeof(*B));
-  if (T > SP_EXPLAIN_MAX_T) return SP_ERR_UNSUPPORTED;
+  if (T < 0) return SP_ERR_CONFIG;
+  if (T > ORACLE_MAX_T) return SP_ERR_UNSUPPORTED;
   B->g = g;
   B->M = M;
   B->d = M->m * M->n;
@@ -1098,6 +1104,7 @@ int oracle_explain_h(void* h, const int32_t* tmpl, int64_t T, const sp_mesh* M, 
 
 static int explain_core(og* Gp, const int32_t* tmpl, int64_t T, const sp_mesh* M, int64_t mu,
                         int64_t chunk, uint64_t index, sp_explain_out* out) {
+  if (T > SP_EXPLAIN_MAX_T) return SP_ERR_UNSUPPORTED;  /* the fixed-size explain record */
   block_ctx B;
   int rc = block_init(&B, Gp, tmpl, T, M, mu, chunk);
   if (rc != SP_OK) return rc;

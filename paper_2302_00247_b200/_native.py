@@ -83,7 +83,15 @@ def _declare(L):
     L.sp_explain_all.argtypes = [vp, vp, C.POINTER(C.c_uint64), C.POINTER(SpExplainBlock),
                                  C.POINTER(C.c_int8), C.POINTER(C.c_int8)]
     L.sp_copy_bytes.argtypes = [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-    for name in ("sp_comm_unique_id", "sp_ctx_comm_init", "sp_ctx_comm_info", "sp_score_launch", "sp_score_wait", "sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
+    L.sp_route_search.argtypes = [vp, vp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int16), C.POINTER(C.c_uint8), C.POINTER(C.c_int64),
+                                  C.POINTER(_abi.SpMesh), C.c_int64, C.c_int64, C.POINTER(C.c_uint64),
+                                  C.POINTER(SpScoreOut), C.POINTER(SpExplainBlock), C.POINTER(C.c_int8),
+                                  C.POINTER(C.c_int8)]
+    L.sp_ctx_limits.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+    L.sp_tables_block_info.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    for name in ("sp_route_search", "sp_ctx_limits", "sp_tables_block_info", "sp_comm_unique_id",
+                 "sp_ctx_comm_init", "sp_ctx_comm_info", "sp_score_launch", "sp_score_wait", "sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
                  "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
                  "sp_score_range", "sp_explain", "sp_last_timings"):
         getattr(L, name).restype = C.c_int
@@ -116,7 +124,8 @@ EXPORTED_SYMBOLS = (
     "sp_tables_edge_offsets", "sp_explain_all", "sp_search", "sp_set_option",
     "sp_fold_stats", "sp_score_launch", "sp_score_wait", "sp_ingest_json", "sp_ingest_error",
     "sp_ingest_view", "sp_ingest_free", "sp_ingest_onnx", "sp_ingest_report", "sp_ingest_text",
-    "sp_comm_unique_id", "sp_ctx_comm_init", "sp_ctx_comm_info",
+    "sp_comm_unique_id", "sp_ctx_comm_init", "sp_ctx_comm_info", "sp_route_search", "sp_ctx_limits",
+    "sp_tables_block_info",
 )
 
 
@@ -179,6 +188,7 @@ class Backend:
             raise BackendError(f"sp_ctx_create(devices={devices}) failed with status {rc}")
         self.ctx = h
         self.comm = self.comm_info()
+        self.smem_limit = self.limits()["smem_per_block"]
 
     # -- multi-GPU -----------------------------------------------------------------
     def comm_unique_id(self) -> bytes:
@@ -355,6 +365,49 @@ class Backend:
                                             ptr(node, C.c_int8), ptr(edge, C.c_int8)),
                     "sp_explain_all")
         return RawList(blocks, nb), node, edge, eoff
+
+    def limits(self) -> dict:
+        sm, nsm = C.c_int64(), C.c_int32()
+        self._check(self.lib.sp_ctx_limits(self.ctx, C.byref(sm), C.byref(nsm)), "sp_ctx_limits")
+        return {"smem_per_block": sm.value, "sm_count": nsm.value}
+
+    def block_info(self, t: Tables) -> tuple:
+        """(blob bytes, live-value pool slots, template nodes) per block of built tables."""
+        nb = t.n_blocks
+        by = np.zeros(max(1, nb), np.int64)
+        pool = np.zeros(max(1, nb), np.int32)
+        T = np.zeros(max(1, nb), np.int32)
+        self._check(self.lib.sp_tables_block_info(t.ptr, ptr(by, C.c_int64), ptr(pool, C.c_int32),
+                                                  ptr(T, C.c_int32)), "sp_tables_block_info")
+        return by[:nb], pool[:nb], T[:nb]
+
+    def route_search(self, dgraph: _Handle, tmpl_off, tmpl_nodes, ref_slot, radix, edge_off, mesh, mu: int,
+                     chunk: int, indices=None) -> tuple:
+        """Table-free search of blocks beyond the table limits (sp_route_search):
+        (scores, (blocks, node_detail, edge_detail, edge_off)); with `indices`,
+        the detail of those candidates only (scores None)."""
+        off = np.ascontiguousarray(tmpl_off, dtype=np.int64)
+        nodes = np.ascontiguousarray(tmpl_nodes, dtype=np.int32)
+        rs = np.ascontiguousarray(ref_slot, dtype=np.int16)
+        rx = np.ascontiguousarray(radix, dtype=np.uint8)
+        eoff = np.ascontiguousarray(edge_off, dtype=np.int64)
+        nb = len(off) - 1
+        ne, nedge = int(off[-1]), int(eoff[-1])
+        if nodes.size == 0:
+            nodes, rs, rx = np.zeros(1, np.int32), np.zeros(1, np.int16), np.zeros(1, np.uint8)
+        m = make_sp_mesh(mesh)
+        blocks = (SpExplainBlock * max(1, nb))()
+        node = np.zeros((max(1, ne), 4), np.int8)
+        edge = np.zeros((max(1, nedge), 2), np.int8)
+        outs = None if indices is not None else (SpScoreOut * max(1, nb))()
+        idx = None if indices is None else np.ascontiguousarray(indices, dtype=np.uint64)
+        self._check(self.lib.sp_route_search(self.ctx, dgraph.ptr, nb, ptr(off, C.c_int64), ptr(nodes, C.c_int32),
+                                             ptr(rs, C.c_int16), ptr(rx, C.c_uint8), ptr(eoff, C.c_int64),
+                                             C.byref(m), int(mu), int(chunk),
+                                             ptr(idx, C.c_uint64) if idx is not None else None, outs, blocks,
+                                             ptr(node, C.c_int8), ptr(edge, C.c_int8)), "sp_route_search")
+        scores = RawList(outs, nb) if outs is not None else None
+        return scores, (RawList(blocks, nb), node, edge, eoff)
 
     def timings(self) -> dict:
         f, s, k = C.c_double(), C.c_double(), C.c_double()

@@ -378,6 +378,37 @@ int sp_explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, sp_explai
   });
 }
 
+int sp_route_search(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* tmpl_off, const int32_t* tmpl_nodes,
+                    const int16_t* ref_slot, const uint8_t* radix, const int64_t* edge_off, const sp_mesh* mesh,
+                    int64_t mu, int64_t chunk_size, const uint64_t* indices, sp_score_out* out,
+                    sp_explain_block* blocks, int8_t* node_detail, int8_t* edge_detail) {
+  if (!ctx || !dg || !tmpl_off || !mesh || n_blocks < 0 || !blocks || !node_detail || !edge_detail) return SP_ERR_CONFIG;
+  if (!indices && !out) return SP_ERR_CONFIG;
+  return guard(ctx, [&] {
+    SP_CUDA(cudaSetDevice(ctx->device));
+    if (mesh->m < 1 || mesh->n < 1) throw sp::Error(SP_ERR_CONFIG, "mesh must be at least 1x1");
+    sp::route_search(ctx, dg, n_blocks, tmpl_off, tmpl_nodes, ref_slot, radix, edge_off, mesh, mu, chunk_size,
+                     indices, out, blocks, node_detail, edge_detail);
+  });
+}
+
+int sp_ctx_limits(const sp_ctx* ctx, int64_t* smem_per_block, int32_t* sm_count) {
+  if (!ctx) return SP_ERR_CONFIG;
+  if (smem_per_block) *smem_per_block = (int64_t)ctx->smem_optin;
+  if (sm_count) *sm_count = ctx->sm_count;
+  return SP_OK;
+}
+
+int sp_tables_block_info(const sp_tables* t, int64_t* blob_bytes, int32_t* pool_slots, int32_t* template_nodes) {
+  if (!t) return SP_ERR_CONFIG;
+  for (int64_t b = 0; b < t->n_blocks; b++) {
+    if (blob_bytes) blob_bytes[b] = t->hdr[b].bytes;
+    if (pool_slots) pool_slots[b] = t->hdr[b].npool;
+    if (template_nodes) template_nodes[b] = t->hdr[b].T;
+  }
+  return SP_OK;
+}
+
 int sp_last_timings(const sp_ctx* ctx, double* fold_ms, double* score_ms, double* score_kernel_ms) {
   if (!ctx) return SP_ERR_CONFIG;
   if (fold_ms) *fold_ms = ctx->fold_ms;

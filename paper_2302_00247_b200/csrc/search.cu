@@ -3568,6 +3568,475 @@ void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* block
   SP_CUDA(cudaStreamSynchronize(s));
 }
 
+
+// ---------------------------------------------------------------------------
+// Route search: blocks beyond the table path's limits (more than MAXT template
+// nodes, a node with more than KMAX internal producers, or tables larger than
+// shared memory) are searched without routing tables -- every candidate is
+// routed node by node with route_node (the reference's per-node pattern
+// choice, search.py:134-224) and costed like plan_cost (costmodel.py:193-267),
+// per-thread reach/state kept in a global scratch ([T][threads], coalesced).
+// Same outputs as the table path (per-block argmin records, winner detail).
+namespace {
+
+struct RouteBlock {
+  int64_t e0, T;
+  unsigned long long C;
+  uint64_t radix3_ref;  // bit s: reference slot s has 3 options
+  int32_t V, pad;
+};
+
+constexpr int ROUTE_THREADS = 128;
+constexpr int ROUTE_MAXK = 64;  // internal producers of one node (route_node's conversion arrays)
+
+// one candidate of block `B` by reference index: valid?, total, num_split
+__device__ bool route_candidate(const GraphView& G, const RouteBlock& B, int32_t b, const int32_t* tmpl_nodes,
+                                const int16_t* ref_slot, const int32_t* node_block, const int32_t* node_tpos,
+                                const uint8_t* bound, const MeshC& M, const sp_mesh& mesh, int64_t mu,
+                                int64_t chunk, unsigned long long index, uint8_t* st, double* rc, int64_t stride,
+                                double* total, uint32_t* nsplit, int* fail_pos) {
+  uint8_t dig[64];
+  unsigned long long rem = index;
+  uint32_t ns = 0;
+  for (int s = B.V - 1; s >= 0; s--) {
+    const uint32_t r = ((B.radix3_ref >> s) & 1) ? 3 : 2;
+    dig[s] = (uint8_t)(rem % r);
+    rem /= r;
+    ns += dig[s] != 0;
+  }
+  NodeRoute R;
+  int ps[ROUTE_MAXK];
+  for (int64_t i = 0; i < B.T; i++) {
+    const int32_t n = tmpl_nodes[B.e0 + i];
+    int k = 0;
+    for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+      const int32_t r = G.in_idx[e];
+      if (node_block[r] != b) continue;
+      if (k < ROUTE_MAXK) ps[k] = st[node_tpos[r] * stride];
+      k++;
+    }
+    if (k > ROUTE_MAXK) {  // flagged by k_route_bound; the search is abandoned
+      *fail_pos = (int)i;
+      return false;
+    }
+    const int slot = ref_slot[B.e0 + i];
+    route_node(G, n, b, node_block, slot >= 0 ? dig[slot] : 0, ps, M, &R, true);
+    if (R.pattern < 0) {
+      *fail_pos = (int)i;
+      return false;
+    }
+    st[i * stride] = (uint8_t)R.state;
+    Pattern pats[4];
+    patterns_for(G.op[n], pats);
+    double base = 0.0;
+    int j = 0;
+    for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+      const int32_t r = G.in_idx[e];
+      if (node_block[r] != b) continue;
+      const int kind = R.conv_kind[j];
+      const double cc = kind != C_ID ? call_cost(kind, G.act_bytes[r], M) : 0.0;
+      base = fmax(base, dadd(rc[node_tpos[r] * stride], cc));
+      j++;
+    }
+    rc[i * stride] = dadd(base, call_cost(pats[R.pattern].coll, G.act_bytes[n], M));
+  }
+  double fwd = 0.0;
+  for (int64_t i = 0; i < B.T; i++) {
+    double tail = rc[i * stride];
+    const int s = st[i * stride];
+    if (bound[B.e0 + i] && s != 0) tail = dadd(tail, call_cost(C_AG, G.act_bytes[tmpl_nodes[B.e0 + i]], M));
+    fwd = fmax(fwd, tail);
+  }
+  double bwd = 0.0;
+  if (M.d > 1) {  // pack_gradients (rewrite.py:78-111): buckets, then unfused; one AllReduce each
+    int64_t cur = 0;
+    int cur_n = 0;
+    for (int pass = 0; pass < 2; pass++) {
+      for (int64_t i = 0; i < B.T; i++) {
+        const int32_t n = tmpl_nodes[B.e0 + i];
+        if (!G.w_rank[n] || !G.w_train[n] || dig[ref_slot[B.e0 + i]] != 0) continue;
+        const int64_t sz = G.w_bytes[n];
+        if (pass == 0) {
+          if (sz >= mu) continue;
+          if (cur + sz > chunk && cur_n) {
+            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+            cur = 0;
+            cur_n = 0;
+          }
+          cur += sz;
+          cur_n++;
+        } else if (sz >= mu) {
+          bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
+        }
+      }
+      if (pass == 0 && cur_n) bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+    }
+  }
+  *total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
+  *nsplit = ns;
+  return true;
+}
+
+__global__ void __launch_bounds__(ROUTE_THREADS) k_score_route(GraphView G, const RouteBlock* __restrict__ blocks,
+                                                               int64_t nb, const int32_t* tmpl_nodes,
+                                                               const int16_t* ref_slot, const int32_t* node_block,
+                                                               const int32_t* node_tpos, const uint8_t* bound,
+                                                               sp_mesh mesh, int64_t mu, int64_t chunk,
+                                                               uint8_t* st_scr, double* rc_scr,
+                                                               ItemOut* __restrict__ out, uint32_t* contrib) {
+  const MeshC M = mesh_consts(mesh);
+  const int64_t NT = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int NW = ROUTE_THREADS / 32;
+  __shared__ unsigned long long s_t[NW], s_i[NW], s_v[NW];
+  __shared__ uint32_t s_n[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t b = 0; b < nb; b++) {
+    const RouteBlock B = blocks[b];
+    unsigned long long bt = ~0ULL, bi = ~0ULL, nv = 0;
+    uint32_t bn = 0xFFFFFFFFu;
+    for (unsigned long long x = (unsigned long long)gt; x < B.C; x += (unsigned long long)NT) {
+      double tot;
+      uint32_t ns;
+      int fp;
+      if (!route_candidate(G, B, (int32_t)b, tmpl_nodes, ref_slot, node_block, node_tpos, bound, M, mesh, mu, chunk,
+                           x, st_scr + gt, rc_scr + gt, NT, &tot, &ns, &fp))
+        continue;
+      nv++;
+      const unsigned long long tb = (unsigned long long)__double_as_longlong(tot);
+      if (key_less(tb, ns, x, bt, bn, bi)) {
+        bt = tb;
+        bn = ns;
+        bi = x;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, bt, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, bi, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, bn, o);
+      nv += __shfl_down_sync(0xffffffffu, nv, o);
+      if (key_less(t2, n2, i2, bt, bn, bi)) {
+        bt = t2;
+        bn = n2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      s_t[warp] = bt;
+      s_i[warp] = bi;
+      s_n[warp] = bn;
+      s_v[warp] = nv;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ItemOut o{s_t[0], s_i[0], s_n[0], s_v[0]};
+      for (int w = 1; w < NW; w++) {
+        o.valid += s_v[w];
+        if (key_less(s_t[w], s_n[w], s_i[w], o.total_bits, o.num_split, o.index)) {
+          o.total_bits = s_t[w];
+          o.num_split = s_n[w];
+          o.index = s_i[w];
+        }
+      }
+      if (o.valid) out[b * (int64_t)gridDim.x + atomicAdd(&contrib[b], 1u)] = o;
+    }
+    __syncthreads();
+  }
+}
+
+// winner detail of the route blocks (the fields of k_explain_all): one thread per block
+__global__ void k_explain_route(GraphView G, const RouteBlock* __restrict__ blocks, int64_t nb,
+                                const int32_t* tmpl_nodes, const int16_t* ref_slot, const int32_t* node_block,
+                                const int32_t* node_tpos, const uint8_t* bound, const int64_t* edge_off,
+                                const unsigned long long* indices, const sp_score_out* scores, sp_mesh mesh,
+                                int64_t mu, int64_t chunk, uint8_t* st_scr, double* rc_scr, ExplainBlock* out,
+                                int8_t* node_out, int8_t* edge_out) {
+  const MeshC M = mesh_consts(mesh);
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const RouteBlock B = blocks[b];
+    ExplainBlock X;
+    X.valid = 0;
+    X.fail_pos = -1;
+    X.forward_comm = X.backward_comm = X.total = 0.0;
+    for (int k = 0; k < 4; k++) X.bytes[k] = X.calls[k] = 0;
+    X.collective_calls = 0;
+    const unsigned long long index = scores ? (scores[b].has_best ? scores[b].best_index : ~0ULL) : indices[b];
+    if (index == ~0ULL || index >= B.C) {
+      out[b] = X;
+      continue;
+    }
+    uint8_t* st = st_scr + B.e0;  // ΣT scratch: block b's template range
+    double* rc = rc_scr + B.e0;
+    uint8_t dig[64];
+    unsigned long long rem = index;
+    for (int s = B.V - 1; s >= 0; s--) {
+      const uint32_t r = ((B.radix3_ref >> s) & 1) ? 3 : 2;
+      dig[s] = (uint8_t)(rem % r);
+      rem /= r;
+    }
+    int64_t eo = edge_off[b];
+    NodeRoute R;
+    int ps[ROUTE_MAXK];
+    bool ok = true;
+    for (int64_t i = 0; i < B.T && ok; i++) {
+      const int32_t n = tmpl_nodes[B.e0 + i];
+      int k = 0;
+      for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+        const int32_t r = G.in_idx[e];
+        if (node_block[r] != (int32_t)b) continue;
+        if (k < ROUTE_MAXK) ps[k] = st[node_tpos[r]];
+        k++;
+      }
+      const int slot = ref_slot[B.e0 + i];
+      route_node(G, n, (int32_t)b, node_block, slot >= 0 ? dig[slot] : 0, ps, M, &R, true);
+      if (R.pattern < 0) {
+        X.fail_pos = (int)i;
+        ok = false;
+        break;
+      }
+      st[i] = (uint8_t)R.state;
+      Pattern pats[4];
+      patterns_for(G.op[n], pats);
+      double base = 0.0;
+      int j = 0;
+      for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
+        const int32_t r = G.in_idx[e];
+        if (node_block[r] != (int32_t)b) continue;
+        const int kind = R.conv_kind[j];
+        double cc = 0.0;
+        if (kind != C_ID) {
+          cc = call_cost(kind, G.act_bytes[r], M);
+          X.bytes[kind - 1] += G.act_bytes[r];
+          X.calls[kind - 1]++;
+        }
+        edge_out[2 * eo] = (int8_t)kind;
+        edge_out[2 * eo + 1] = R.conv_axis[j];
+        eo++;
+        base = fmax(base, dadd(rc[node_tpos[r]], cc));
+        j++;
+      }
+      const int pc = pats[R.pattern].coll;
+      if (pc != C_ID) {
+        X.bytes[pc - 1] += G.act_bytes[n];
+        X.calls[pc - 1]++;
+      }
+      rc[i] = dadd(base, call_cost(pc, G.act_bytes[n], M));
+      const NSpec fs = state_spec(R.state, G.act_rank[n]);
+      node_out[4 * (B.e0 + i)] = (int8_t)R.pattern;
+      node_out[4 * (B.e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
+      node_out[4 * (B.e0 + i) + 2] = -1;
+      node_out[4 * (B.e0 + i) + 3] = 0;
+    }
+    if (!ok) {
+      out[b] = X;
+      continue;
+    }
+    double fwd = 0.0;
+    for (int64_t i = 0; i < B.T; i++) {
+      const int32_t n = tmpl_nodes[B.e0 + i];
+      double tail = rc[i];
+      if (bound[B.e0 + i] && st[i] != 0) {
+        tail = dadd(tail, call_cost(C_AG, G.act_bytes[n], M));
+        X.bytes[C_AG - 1] += G.act_bytes[n];
+        X.calls[C_AG - 1]++;
+        node_out[4 * (B.e0 + i) + 2] = state_spec(st[i], G.act_rank[n]).axis;
+      }
+      fwd = fmax(fwd, tail);
+    }
+    double bwd = 0.0;
+    if (M.d > 1) {
+      int64_t cur = 0;
+      int cur_n = 0;
+      for (int pass = 0; pass < 2; pass++) {
+        for (int64_t i = 0; i < B.T; i++) {
+          const int32_t n = tmpl_nodes[B.e0 + i];
+          if (!G.w_rank[n] || !G.w_train[n] || dig[ref_slot[B.e0 + i]] != 0) continue;
+          const int64_t sz = G.w_bytes[n];
+          if (pass == 0) {
+            if (sz >= mu) continue;
+            if (cur + sz > chunk && cur_n) {
+              bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+              X.bytes[0] += cur;
+              X.calls[0]++;
+              cur = 0;
+              cur_n = 0;
+            }
+            cur += sz;
+            cur_n++;
+          } else if (sz >= mu) {
+            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
+            X.bytes[0] += sz;
+            X.calls[0]++;
+          }
+        }
+        if (pass == 0 && cur_n) {
+          bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+          X.bytes[0] += cur;
+          X.calls[0]++;
+        }
+      }
+    }
+    X.valid = 1;
+    X.forward_comm = fwd;
+    X.backward_comm = bwd;
+    X.total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
+    X.collective_calls = X.calls[0] + X.calls[1] + X.calls[2] + X.calls[3];
+    out[b] = X;
+  }
+}
+
+// internal producers per template entry and the boundary flag, for the route blocks
+__global__ void k_route_bound(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
+                              const int32_t* node_block, const int32_t* node_tpos, const uint8_t* has_cons,
+                              const uint8_t* ext_cons, uint8_t* bound, int32_t* err) {
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x)
+    for (int64_t e = tmpl_off[b] + threadIdx.x; e < tmpl_off[b + 1]; e += blockDim.x) {
+      const int32_t n = tmpl_nodes[e];
+      bound[e] = !has_cons[n] || ext_cons[n];
+      int k = 0;
+      for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
+        const int32_t r = G.in_idx[q];
+        if (node_block[r] != (int32_t)b) continue;
+        k++;
+        if (node_tpos[r] >= e - tmpl_off[b]) atomicExch(err, 2);  // template not topologically ordered
+      }
+      if (k > ROUTE_MAXK) atomicExch(err, 3);
+    }
+}
+
+}  // namespace
+
+// The route search of `nb` blocks (templates in tmpl_off/tmpl_nodes, reference
+// slot of every template entry or -1, radix 2/3 per entry, internal-edge
+// offsets per block): scores (argmin records) unless `indices` is given, then
+// the winner (or the given candidate) detail of every block.
+void route_search(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_off, const int32_t* tmpl_nodes,
+                  const int16_t* ref_slot, const uint8_t* radix, const int64_t* edge_off, const sp_mesh* mesh,
+                  int64_t mu, int64_t chunk, const uint64_t* indices, sp_score_out* scores, void* xblocks,
+                  int8_t* xnode, int8_t* xedge) {
+  cudaStream_t s = ctx->stream;
+  if (mu > chunk)
+    throw Error(SP_ERR_CONFIG, "fusion threshold " + std::to_string(mu) + " exceeds chunk size " + std::to_string(chunk));
+  const int64_t n = dg->n, ne = tmpl_off[nb];
+  std::vector<RouteBlock> rb(nb);
+  int64_t maxT = 1;
+  for (int64_t b = 0; b < nb; b++) {
+    RouteBlock& B = rb[b];
+    B.e0 = tmpl_off[b];
+    B.T = tmpl_off[b + 1] - tmpl_off[b];
+    maxT = std::max(maxT, B.T);
+    unsigned __int128 C = 1;
+    int V = 0;
+    uint64_t r3 = 0;
+    for (int64_t e = B.e0; e < B.e0 + B.T; e++) {
+      if (ref_slot[e] < 0) continue;
+      if (ref_slot[e] >= 64) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
+      V = std::max(V, ref_slot[e] + 1);
+      if (radix[e] == 3) r3 |= 1ULL << ref_slot[e];
+      C *= radix[e];
+      if (C > (unsigned __int128)UINT64_MAX) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
+    }
+    B.C = (unsigned long long)C;
+    B.V = V;
+    B.radix3_ref = r3;
+  }
+  const int64_t nedge = edge_off[nb];
+  PackedUpload pk;
+  const size_t o_off = pk.add(tmpl_off, (nb + 1) * 8), o_nodes = pk.add(tmpl_nodes, ne * 4),
+               o_slot = pk.add(ref_slot, ne * 2), o_eoff = pk.add(edge_off, (nb + 1) * 8),
+               o_rb = pk.add(rb.data(), nb * sizeof(RouteBlock)),
+               o_idx = indices ? pk.add(indices, nb * 8) : 0;
+  size_t pin_bytes = 0;
+  uint8_t* pin = pinned_acquire(ctx, std::max<size_t>(pk.total, nb * sizeof(sp_score_out) + 64), &pin_bytes);
+  struct Release {
+    sp_ctx* ctx;
+    uint8_t* p;
+    size_t n;
+    ~Release() { pinned_release(ctx, p, n); }
+  } rel{ctx, pin, pin_bytes};
+  for (const auto& part : pk.parts)
+    if (part.bytes) std::memcpy(pin + part.off, part.src, part.bytes);
+  DevBuf<uint8_t> arena;
+  arena.alloc(std::max<size_t>(pk.total, 16), s);
+  SP_CUDA(cudaMemcpyAsync(arena.p, pin, pk.total, cudaMemcpyHostToDevice, s));
+  g_h2d_bytes += (int64_t)pk.total;
+  const int64_t* d_off = (const int64_t*)(arena.p + o_off);
+  const int32_t* d_nodes = (const int32_t*)(arena.p + o_nodes);
+  const int16_t* d_slot = (const int16_t*)(arena.p + o_slot);
+  const int64_t* d_eoff = (const int64_t*)(arena.p + o_eoff);
+  const RouteBlock* d_rb = (const RouteBlock*)(arena.p + o_rb);
+  DevBuf<int32_t> node_block, node_tpos, err;
+  DevBuf<uint8_t> has_cons, ext_cons, bound;
+  node_block.alloc(n, s);
+  node_tpos.alloc(n, s);
+  err.alloc(2, s);
+  has_cons.alloc(n, s);
+  ext_cons.alloc(n, s);
+  bound.alloc(std::max<int64_t>(ne, 1), s);
+  SP_CUDA(cudaMemsetAsync(node_block.p, 0xff, n * 4, s));
+  SP_CUDA(cudaMemsetAsync(node_tpos.p, 0xff, n * 4, s));
+  SP_CUDA(cudaMemsetAsync(err.p, 0, 8, s));
+  SP_CUDA(cudaMemsetAsync(has_cons.p, 0, n, s));
+  SP_CUDA(cudaMemsetAsync(ext_cons.p, 0, n, s));
+  const GraphView G = view_of(dg);
+  const int gb = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), 65535);
+  if (nb > 0) SP_LAUNCH(ctx, k_mark_blocks, gb, 128, 0, s, d_off, d_nodes, nb, node_block.p, node_tpos.p, err.p);
+  SP_LAUNCH(ctx, k_boundary, grid_for(n, ctx->sm_count), 256, 0, s, G, n, node_block.p, has_cons.p, ext_cons.p);
+  if (nb > 0)
+    SP_LAUNCH(ctx, k_route_bound, gb, 128, 0, s, G, d_off, d_nodes, nb, node_block.p, node_tpos.p, has_cons.p,
+              ext_cons.p, bound.p, err.p);
+  DevBuf<sp_score_out> dout;
+  dout.alloc(std::max<int64_t>(nb, 1), s);
+  const int grid = ctx->sm_count * 2;
+  const int64_t NT = (int64_t)grid * ROUTE_THREADS;
+  DevBuf<uint8_t> st;
+  DevBuf<double> rc;
+  if (!indices) {
+    DevBuf<ItemOut> rec;
+    DevBuf<uint32_t> contrib;
+    st.alloc((size_t)maxT * NT, s);
+    rc.alloc((size_t)maxT * NT, s);
+    rec.alloc((size_t)std::max<int64_t>(nb, 1) * grid, s);
+    contrib.alloc(std::max<int64_t>(nb, 1), s);
+    SP_CUDA(cudaMemsetAsync(contrib.p, 0, std::max<int64_t>(nb, 1) * 4, s));
+    SP_LAUNCH(ctx, k_score_route, grid, ROUTE_THREADS, 0, s, G, d_rb, nb, d_nodes, d_slot, node_block.p, node_tpos.p,
+              bound.p, *mesh, mu, chunk, st.p, rc.p, rec.p, contrib.p);
+    SP_LAUNCH(ctx, k_reduce_contrib, (unsigned)std::min<int64_t>(std::max<int64_t>(nb, 1), 4096), THREADS, 0, s, rec.p,
+              contrib.p, (int64_t)grid, nb, dout.p);
+    SP_CUDA(cudaGetLastError());
+  }
+  DevBuf<ExplainBlock> dblk;
+  DevBuf<int8_t> dnode, dedge;
+  dblk.alloc(std::max<int64_t>(nb, 1), s);
+  dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
+  dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
+  SP_CUDA(cudaMemsetAsync(dnode.p, 0, 4 * std::max<int64_t>(ne, 1), s));
+  if (st.n < (size_t)ne) st.alloc(std::max<int64_t>(ne, 1), s);
+  if (rc.n < (size_t)ne) rc.alloc(std::max<int64_t>(ne, 1), s);
+  SP_LAUNCH(ctx, k_explain_route, (int)std::max<int64_t>(1, std::min<int64_t>((nb + 63) / 64, 1024)), 64, 0, s, G,
+            d_rb, nb, d_nodes, d_slot, node_block.p, node_tpos.p, bound.p, d_eoff,
+            indices ? (const unsigned long long*)(arena.p + o_idx) : nullptr, indices ? nullptr : dout.p, *mesh, mu,
+            chunk, st.p, rc.p, dblk.p, dnode.p, dedge.p);
+  SP_CUDA(cudaGetLastError());
+  int32_t err_h[2];
+  SP_CUDA(cudaMemcpyAsync(err_h, err.p, 8, cudaMemcpyDeviceToHost, s));
+  if (scores && !indices) SP_CUDA(cudaMemcpyAsync(scores, dout.p, nb * sizeof(sp_score_out), cudaMemcpyDeviceToHost, s));
+  if (xblocks) SP_CUDA(cudaMemcpyAsync(xblocks, dblk.p, nb * sizeof(ExplainBlock), cudaMemcpyDeviceToHost, s));
+  if (xnode && ne) SP_CUDA(cudaMemcpyAsync(xnode, dnode.p, 4 * ne, cudaMemcpyDeviceToHost, s));
+  if (xedge && nedge) SP_CUDA(cudaMemcpyAsync(xedge, dedge.p, 2 * nedge, cudaMemcpyDeviceToHost, s));
+  g_d2h_bytes += 8 + (int64_t)(nb * (sizeof(sp_score_out) + sizeof(ExplainBlock)) + 4 * ne + 2 * nedge);
+  SP_CUDA(cudaStreamSynchronize(s));
+  if (err_h[0] == 1) throw Error(SP_ERR_CONFIG, "a node appears in more than one template");
+  if (err_h[0] == 2) throw Error(SP_ERR_CONFIG, "template is not in topological order");
+  if (err_h[0] == 3) throw Error(SP_ERR_UNSUPPORTED, "a template node has more than 64 internal producers");
+  if (scores)
+    for (int64_t b = 0; b < nb; b++) {
+      if (indices) scores[b] = sp_score_out{};
+      scores[b].candidates = rb[b].C;
+    }
+}
+
 void tables_free_priv(sp_tables* t) {
   delete (TablesPriv*)t->priv;
   t->priv = nullptr;

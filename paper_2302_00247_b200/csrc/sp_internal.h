@@ -364,6 +364,10 @@ void merge_key(sp_score_out* acc, const sp_score_out* o);
 void tables_free_priv(sp_tables* t);
 void explain_all(sp_ctx* ctx, sp_tables* t, const uint64_t* indices, void* blocks_out, int8_t* node_out,
                  int8_t* edge_out);
+void route_search(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_off, const int32_t* tmpl_nodes,
+                  const int16_t* ref_slot, const uint8_t* radix, const int64_t* edge_off, const sp_mesh* mesh,
+                  int64_t mu, int64_t chunk, const uint64_t* indices, sp_score_out* scores, void* xblocks,
+                  int8_t* xnode, int8_t* xedge);
 // comm.cu: NCCL, loaded with dlopen on first use
 int nccl_version();
 void nccl_unique_id(uint8_t* out);

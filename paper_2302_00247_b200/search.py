@@ -577,6 +577,15 @@ class _Search:
         if launch:
             self.launch()
 
+    def over_smem(self) -> list:
+        """Blocks (positions in this search) whose staged tables + live-value pool
+        exceed the shared memory of a CTA."""
+        by, pool, _ = self.ses.backend.block_info(self.tables)
+        if len(by) == 0:
+            return []
+        need = ((by + 15) // 16) * 16 + pool.astype(np.int64) * SCORE_THREADS * 18 + 16
+        return np.nonzero(need > self.ses.backend.smem_limit)[0].tolist()
+
     def launch(self) -> None:
         """Queue the scoring (and the copy of its results to the host) on the stream."""
         try:
@@ -667,9 +676,25 @@ def search_blocks(graph, subgraphs: list, mesh, mu: int = 1 << 20, chunk_size: i
         return []
     if csr is None:
         csr = _templates_csr(ses.low, subgraphs)
-    srch = _Search(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange)
+    searches = _plan_searches(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange)
+    try:
+        for srch, _ in searches:
+            srch.launch()
+    except BaseException:
+        for srch, _ in searches:
+            srch.tables.close()
+        raise
     prep = route_prep(ses, subgraphs, types, csr)  # overlaps the device search
-    return srch.collect(graph, subgraphs, want_table, types, prep)
+    results = [None] * len(subgraphs)
+    try:
+        for srch, ids in searches:
+            got = srch.collect(graph, [subgraphs[i] for i in ids], want_table, types, [prep[i] for i in ids])
+            for i, r in zip(ids, got):
+                results[i] = r
+    finally:
+        for srch, _ in searches:
+            srch.tables.close()
+    return results
 
 
 def search_subgraph(graph, subgraph, mesh, mu: int = 1 << 20, chunk_size: int = 4 << 20,
@@ -743,6 +768,149 @@ def _block_groups(low: LoweredGraph, csr) -> list:
     return out
 
 
+#: limits of the table path (csrc/search.cu MAXT, KMAX; smem per CTA): blocks
+#: beyond them are searched by sp_route_search (no routing tables)
+TABLE_MAX_T = 256
+TABLE_MAX_FANIN = 6
+SCORE_THREADS = 256
+
+
+def _subset_csr(csr, ids):
+    off, nodes = csr
+    ids = np.asarray(ids, np.int64)
+    T = off[ids + 1] - off[ids]
+    goff = np.zeros(len(ids) + 1, np.int64)
+    np.cumsum(T, out=goff[1:])
+    gather = np.repeat(off[ids] - goff[:-1], T) + np.arange(goff[-1])
+    return goff, np.ascontiguousarray(nodes[gather])
+
+
+def _route_mask(low: LoweredGraph, csr) -> np.ndarray:
+    """Blocks the routing tables cannot hold: more than TABLE_MAX_T template
+    nodes, or a node with more than TABLE_MAX_FANIN internal producers."""
+    off, nodes = csr
+    nb = len(off) - 1
+    T = np.diff(off)
+    mask = T > TABLE_MAX_T
+    if len(nodes) == 0:
+        return mask
+    nodes = np.asarray(nodes, np.int64)
+    blk = np.full(low.n_nodes, -1, np.int64)
+    blk[nodes] = np.repeat(np.arange(nb), T)
+    cnt = (low.in_off[nodes + 1] - low.in_off[nodes]).astype(np.int64)
+    if cnt.sum() == 0:
+        return mask
+    coff = np.zeros(len(nodes) + 1, np.int64)
+    np.cumsum(cnt, out=coff[1:])
+    prod = low.in_idx[np.repeat(low.in_off[nodes] - coff[:-1], cnt) + np.arange(coff[-1])]
+    internal = (blk[prod] == np.repeat(blk[nodes], cnt)).astype(np.int64)
+    fan = np.zeros(len(nodes), np.int64)
+    np.add.at(fan, np.repeat(np.arange(len(nodes)), cnt), internal)
+    bmax = np.zeros(nb, np.int64)
+    np.maximum.at(bmax, np.repeat(np.arange(nb), T), fan)
+    return mask | (bmax > TABLE_MAX_FANIN)
+
+
+class _RouteSearch:
+    """The blocks beyond the table limits, searched by sp_route_search (every
+    candidate routed node by node on the device, no tables).  Same interface as
+    _Search; every rank searches them whole (no exchange: results are equal)."""
+
+    explain = True
+
+    class _NoTables:
+        def close(self):
+            pass
+
+    def __init__(self, ses: Session, csr, mesh, mu: int, chunk_size: int):
+        self.ses, self.csr, self.mesh, self.mu, self.chunk_size = ses, csr, mesh, mu, chunk_size
+        self.tables = self._NoTables()
+
+    def launch(self) -> None:
+        pass
+
+    def fetch(self, explain_now: bool = False) -> None:
+        pass
+
+    def run(self, prep, indices=None):
+        """(scores or None, detail) of the blocks (indices: explain those candidates)."""
+        off, nodes = self.csr
+        ref_slot = np.full(len(nodes), -1, np.int16)
+        radix = np.ones(len(nodes), np.uint8)
+        eoff = np.zeros(len(off), np.int64)
+        for b, (slot_pos, radices, tnodes, _) in enumerate(prep):
+            e0 = int(off[b])
+            for k, (q, r) in enumerate(zip(slot_pos, radices)):
+                ref_slot[e0 + q] = k
+                radix[e0 + q] = r
+            eoff[b + 1] = eoff[b] + sum(len(x[5]) for x in tnodes)
+        # mu > chunk: pack_gradients' BadConfig comes from the first costed
+        # candidate (rewrite.py:88); search with a legal chunk, collect raises
+        return self.ses.backend.route_search(self.ses.dgraph, off, nodes, ref_slot, radix, eoff, self.mesh,
+                                             self.mu, max(self.mu, self.chunk_size), indices)
+
+    def collect(self, graph, subgraphs: list, want_table: bool, types: TypeSet, prep=None) -> list:
+        if want_table:
+            raise UnsupportedSearch("want_table for blocks beyond the routing-table limits "
+                                    f"(> {TABLE_MAX_T} nodes or > {TABLE_MAX_FANIN} internal producers)")
+        ses = self.ses
+        low = ses.low
+        bad = np.isin(low.op[self.csr[1]], (8, 9)) if len(self.csr[1]) else np.zeros(0, bool)
+        if bad.any():  # patterns_for raises on routing such a node (patterns.py:166-170)
+            raise SpecMismatch(f"{_OP_LABELS[int(low.op[self.csr[1][np.argmax(bad)]])]} is not a shardable compute kind")
+        if prep is None:
+            prep = route_prep(ses, subgraphs, types, self.csr)
+        scores, detail = self.run(prep)
+        for sc in scores:
+            if not sc.has_best:
+                raise AssertionError("all-replica fallback must always route")
+            if self.mu > self.chunk_size:
+                raise BadConfig(f"fusion threshold {self.mu} exceeds chunk size {self.chunk_size}")
+        bests = routed_plans_all(ses, None, subgraphs, scores, self.mesh, types, detail, prep)
+        SubgraphResult = _ctor(types.SubgraphResult, 5)
+        return [SubgraphResult(sub, best, int(sc.candidates), int(sc.valid), [])
+                for sub, sc, best in zip(subgraphs, scores, bests)]
+
+
+class _NeedRoute(Exception):
+    def __init__(self, ids):
+        super().__init__(ids)
+        self.ids = ids
+
+
+def _plan_searches(ses: Session, csr, mesh, mu, chunk_size, shard, n_shards, exchange) -> list:
+    """[(search, block ids)]: the route search of the blocks beyond the table
+    limits (if any), then the table searches (cheap group first, _block_groups).
+    A block whose tables turn out larger than shared memory moves to the route
+    search (the tables are rebuilt without it)."""
+    nb = len(csr[0]) - 1
+    route = _route_mask(ses.low, csr)
+    while True:
+        out = []
+        rids = np.nonzero(route)[0]
+        tids = np.nonzero(~route)[0]
+        try:
+            tcsr = csr if len(rids) == 0 else _subset_csr(csr, tids)
+            for ids, gcsr in _block_groups(ses.low, tcsr):
+                gids = [int(tids[i]) for i in ids] if len(rids) else ids
+                srch = _Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange, launch=False)
+                out.append((srch, gids))
+                over = srch.over_smem()
+                if len(over):
+                    raise _NeedRoute([gids[i] for i in over])
+            if len(rids):  # last: the table groups keep their cheap-first order
+                out.append((_RouteSearch(ses, _subset_csr(csr, rids), mesh, mu, chunk_size), rids.tolist()))
+            return out
+        except _NeedRoute as e:
+            for srch, _ in out:
+                srch.tables.close()
+            route[e.ids] = True
+        except BaseException:
+            for srch, _ in out:
+                srch.tables.close()
+            raise
+
+
 def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types, backend, session,
                  cache, shard, n_shards, exchange, root_only=True):
     t0 = time.perf_counter()
@@ -766,15 +934,13 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
         # candidate's plan_cost -> pack_gradients raises BadConfig (rewrite.py:88),
         # or, with no valid candidate, the all-replica assertion; score block 0 only
         off, nodes = csr
-        first = _Search(ses, (np.array([0, off[1] - off[0]], np.int64), nodes[off[0]:off[1]]),
-                        mesh, mu, chunk_size, 0, 1, None)
+        c0 = (np.array([0, off[1] - off[0]], np.int64), nodes[off[0]:off[1]])
+        first = (_RouteSearch(ses, c0, mesh, mu, chunk_size) if _route_mask(ses.low, c0)[0]
+                 else _Search(ses, c0, mesh, mu, chunk_size, 0, 1, None))
         first.collect(graph, subgraphs_from_blocks(ses.low, ba, types)[:1], False, types)
         raise AssertionError("unreachable: block 0 raises BadConfig or the all-replica assertion")
-    searches = []
+    searches = _plan_searches(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange)
     try:
-        for ids, gcsr in _block_groups(ses.low, csr):
-            searches.append((_Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange,
-                                     launch=False), ids))
         if len(searches) > 1 and not searches[0][0].explain:
             # sharded: the cheap group's winners are merged across ranks and
             # re-routed BEFORE the expensive launch -- once that persistent
@@ -860,13 +1026,19 @@ class _OneScore:
 def _explain_plan(graph, plan, mesh, mu, chunk_size, types, session):
     ses = session or Session.open(graph)
     index, bad = _plan_index(graph, plan)
-    off, nodes = _templates_csr(ses.low, [plan.subgraph])
-    tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
-    try:
-        sc = _OneScore(index)
-        routed = routed_plans_all(ses, tables, [plan.subgraph], [sc], mesh, types)[0]
-    finally:
-        tables.close()
+    csr = _templates_csr(ses.low, [plan.subgraph])
+    sc = _OneScore(index)
+    if _route_mask(ses.low, csr)[0]:
+        prep = route_prep(ses, [plan.subgraph], types, csr)
+        _, detail = _RouteSearch(ses, csr, mesh, mu, max(mu, chunk_size)).run(prep, [index])
+        routed = routed_plans_all(ses, None, [plan.subgraph], [sc], mesh, types, detail, prep)[0]
+    else:
+        off, nodes = csr
+        tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
+        try:
+            routed = routed_plans_all(ses, tables, [plan.subgraph], [sc], mesh, types)[0]
+        finally:
+            tables.close()
     template = plan.subgraph.template
     if bad is not None and (not isinstance(routed, types.RoutingFailure)
                             or template.index(routed.node) > bad):
@@ -935,11 +1107,30 @@ def routed_plan_for_assignments(graph, mesh, assignments: dict, min_duplicates: 
         indices.append(index)
         bads.append(bad)
         chosen.append(tuple(sorted(specs, key=lambda t: t[0])))
-    off, nodes = csr
-    tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
+    # per block group (routing tables / route search beyond the table limits)
+    route = _route_mask(ses.low, csr)
+    Xs, groups = [None] * len(subs), []
+    for ids in (np.nonzero(~route)[0].tolist(), np.nonzero(route)[0].tolist()):
+        if not ids:
+            continue
+        gcsr = _subset_csr(csr, ids)
+        gprep = [prep[i] for i in ids]
+        gidx = [indices[i] for i in ids]
+        if route[ids[0]]:
+            _, detail = _RouteSearch(ses, gcsr, mesh, mu, max(mu, chunk_size)).run(gprep, gidx)
+            tables = None
+        else:
+            tables = ses.backend.tables(ses.dgraph, gcsr[0], gcsr[1], mesh, mu, max(mu, chunk_size))
+            try:
+                detail = ses.backend.explain_all(tables, gidx)
+            except BaseException:
+                tables.close()
+                raise
+        groups.append((ids, gprep, gidx, detail, tables))
+        for i, X in zip(ids, detail[0]):
+            Xs[i] = X
     try:
-        detail = ses.backend.explain_all(tables, indices)
-        for b, X in enumerate(detail[0]):
+        for b, X in enumerate(Xs):
             fail = None if X.valid else int(X.fail_pos)
             if bads[b] is not None and (fail is None or fail > bads[b]):
                 fail = bads[b]
@@ -948,9 +1139,16 @@ def routed_plan_for_assignments(graph, mesh, assignments: dict, min_duplicates: 
                                      "no pattern chains from producer states")
             if mu > chunk_size:
                 raise BadConfig(f"fusion threshold {mu} exceeds chunk size {chunk_size}")
-        bests = routed_plans_all(ses, tables, subs, [_OneScore(i) for i in indices], mesh, types, detail, prep)
+        bests = [None] * len(subs)
+        for ids, gprep, gidx, detail, tables in groups:
+            got = routed_plans_all(ses, tables, [subs[i] for i in ids], [_OneScore(i) for i in gidx], mesh, types,
+                                   detail, gprep)
+            for i, r in zip(ids, got):
+                bests[i] = r
     finally:
-        tables.close()
+        for *_, tables in groups:
+            if tables is not None:
+                tables.close()
     results = []
     total_cost = 0.0
     for sub, routed, specs in zip(subs, bests, chosen):

@@ -9,6 +9,9 @@ namespace {
 template <class F>
 int guard(sp_ctx* ctx, F&& f) {
   try {
+    // a non-sticky error some other CUDA user left in this thread's last-error
+    // slot would otherwise surface at this call's first launch check
+    cudaGetLastError();
     f();
     if (ctx) ctx->last_error.clear();
     return SP_OK;

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -165,7 +166,6 @@ struct sp_ctx {
   std::vector<std::pair<void*, size_t>> pinned_pool;
   // per kernel: the dynamic shared memory limit already set, and resident CTAs
   // per SM by (kernel, smem) -- both runtime queries cost ~10 us per launch
-  std::vector<std::pair<const void*, int>> smem_set;
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occupancy;
   std::vector<cudaEvent_t> event_pool;  // timing events of finished searches, reused
   // multi-GPU (comm.cu).  Every device is a lane: this context's own
@@ -204,18 +204,31 @@ inline void pinned_release(sp_ctx* ctx, void* p, size_t n) {
   if (p) ctx->pinned_pool.push_back({p, n});
 }
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when `smem` exceeds
-// what was already allowed for `kern` (the attribute is a limit)
+// what was already allowed for `kern`.  The attribute belongs to the function
+// in the whole process (every context, every device of it), so the record is
+// process-wide and the limit only ever grows: a context that needs less must
+// not lower it under another context's launches.
+inline std::mutex& smem_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::vector<std::pair<std::pair<const void*, int>, int>>& smem_limits() {
+  static std::vector<std::pair<std::pair<const void*, int>, int>> v;  // ((kernel, device), bytes)
+  return v;
+}
 template <class K>
 inline void allow_smem(sp_ctx* ctx, K* kern, size_t smem) {
-  for (auto& e : ctx->smem_set)
-    if (e.first == (const void*)kern) {
+  std::lock_guard<std::mutex> lock(smem_mutex());
+  const std::pair<const void*, int> key{(const void*)kern, ctx->device};
+  for (auto& e : smem_limits())
+    if (e.first == key) {
       if ((size_t)e.second >= smem) return;
       SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       e.second = (int)smem;
       return;
     }
   SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  ctx->smem_set.push_back({(const void*)kern, (int)smem});
+  smem_limits().push_back({key, (int)smem});
 }
 // resident CTAs per SM of `kern` at `threads` x `smem` (cached per context)
 template <class K>

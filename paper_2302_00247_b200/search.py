@@ -878,6 +878,45 @@ class _NeedRoute(Exception):
         self.ids = ids
 
 
+def _explain_groups(ses: Session, csr, prep: list, indices: list, mesh, mu: int, chunk_size: int) -> list:
+    """Detail of the given candidate of every block (the winner re-routing of
+    pattern_routing / plan_cost / the replay): [(block ids, prep, indices,
+    detail, tables or None)] -- explain_all on routing tables, the route search
+    for the blocks beyond the table limits (including tables that turn out
+    larger than a CTA's shared memory).  The caller closes the tables."""
+    route = _route_mask(ses.low, csr)
+    out = []
+    try:
+        tids = np.nonzero(~route)[0].tolist()
+        if tids:
+            gcsr = _subset_csr(csr, tids)
+            tables = ses.backend.tables(ses.dgraph, gcsr[0], gcsr[1], mesh, mu, max(mu, chunk_size))
+            by, _, _ = ses.backend.block_info(tables)
+            over = np.nonzero(((by + 15) // 16) * 16 + 16 > ses.backend.smem_limit)[0]
+            if len(over):
+                tables.close()
+                route[np.asarray(tids)[over]] = True
+                tids = np.nonzero(~route)[0].tolist()
+                gcsr = _subset_csr(csr, tids)
+                tables = ses.backend.tables(ses.dgraph, gcsr[0], gcsr[1], mesh, mu, max(mu, chunk_size)) if tids else None
+            if tids:
+                gidx = [indices[i] for i in tids]
+                out.append((tids, [prep[i] for i in tids], gidx, None, tables))
+                out[-1] = (tids, out[-1][1], gidx, ses.backend.explain_all(tables, gidx), tables)
+        rids = np.nonzero(route)[0].tolist()
+        if rids:
+            gprep = [prep[i] for i in rids]
+            gidx = [indices[i] for i in rids]
+            _, detail = _RouteSearch(ses, _subset_csr(csr, rids), mesh, mu, max(mu, chunk_size)).run(gprep, gidx)
+            out.append((rids, gprep, gidx, detail, None))
+    except BaseException:
+        for *_, t in out:
+            if t is not None:
+                t.close()
+        raise
+    return out
+
+
 def _plan_searches(ses: Session, csr, mesh, mu, chunk_size, shard, n_shards, exchange) -> list:
     """[(search, block ids)]: the route search of the blocks beyond the table
     limits (if any), then the table searches (cheap group first, _block_groups).
@@ -1027,18 +1066,15 @@ def _explain_plan(graph, plan, mesh, mu, chunk_size, types, session):
     ses = session or Session.open(graph)
     index, bad = _plan_index(graph, plan)
     csr = _templates_csr(ses.low, [plan.subgraph])
-    sc = _OneScore(index)
-    if _route_mask(ses.low, csr)[0]:
-        prep = route_prep(ses, [plan.subgraph], types, csr)
-        _, detail = _RouteSearch(ses, csr, mesh, mu, max(mu, chunk_size)).run(prep, [index])
-        routed = routed_plans_all(ses, None, [plan.subgraph], [sc], mesh, types, detail, prep)[0]
-    else:
-        off, nodes = csr
-        tables = ses.backend.tables(ses.dgraph, off, nodes, mesh, mu, max(mu, chunk_size))
-        try:
-            routed = routed_plans_all(ses, tables, [plan.subgraph], [sc], mesh, types)[0]
-        finally:
-            tables.close()
+    prep = route_prep(ses, [plan.subgraph], types, csr)
+    groups = _explain_groups(ses, csr, prep, [index], mesh, mu, chunk_size)
+    try:
+        _, gprep, _, detail, tables = groups[0]
+        routed = routed_plans_all(ses, tables, [plan.subgraph], [_OneScore(index)], mesh, types, detail, gprep)[0]
+    finally:
+        for *_, t in groups:
+            if t is not None:
+                t.close()
     template = plan.subgraph.template
     if bad is not None and (not isinstance(routed, types.RoutingFailure)
                             or template.index(routed.node) > bad):
@@ -1108,25 +1144,9 @@ def routed_plan_for_assignments(graph, mesh, assignments: dict, min_duplicates: 
         bads.append(bad)
         chosen.append(tuple(sorted(specs, key=lambda t: t[0])))
     # per block group (routing tables / route search beyond the table limits)
-    route = _route_mask(ses.low, csr)
-    Xs, groups = [None] * len(subs), []
-    for ids in (np.nonzero(~route)[0].tolist(), np.nonzero(route)[0].tolist()):
-        if not ids:
-            continue
-        gcsr = _subset_csr(csr, ids)
-        gprep = [prep[i] for i in ids]
-        gidx = [indices[i] for i in ids]
-        if route[ids[0]]:
-            _, detail = _RouteSearch(ses, gcsr, mesh, mu, max(mu, chunk_size)).run(gprep, gidx)
-            tables = None
-        else:
-            tables = ses.backend.tables(ses.dgraph, gcsr[0], gcsr[1], mesh, mu, max(mu, chunk_size))
-            try:
-                detail = ses.backend.explain_all(tables, gidx)
-            except BaseException:
-                tables.close()
-                raise
-        groups.append((ids, gprep, gidx, detail, tables))
+    groups = _explain_groups(ses, csr, prep, indices, mesh, mu, chunk_size)
+    Xs = [None] * len(subs)
+    for ids, _, _, detail, _ in groups:
         for i, X in zip(ids, detail[0]):
             Xs[i] = X
     try:

@@ -164,8 +164,7 @@ struct sp_ctx {
   size_t staging_bytes = 0;
   // free pinned host blocks for score results (D2H enqueued at launch time)
   std::vector<std::pair<void*, size_t>> pinned_pool;
-  // per kernel: the dynamic shared memory limit already set, and resident CTAs
-  // per SM by (kernel, smem) -- both runtime queries cost ~10 us per launch
+  // resident CTAs per SM by (kernel, smem): the runtime query costs ~10 us per launch
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occupancy;
   std::vector<cudaEvent_t> event_pool;  // timing events of finished searches, reused
   // multi-GPU (comm.cu).  Every device is a lane: this context's own

@@ -1561,10 +1561,87 @@ done:
   return d;
 }
 
+/*
+ * The same map in two halves, so the expensive one overlaps the device search:
+ * assignments_keys(names, key_ids) -> (dict {names[key_ids[i]]: None} in i
+ * order, bytes of the keys' hashes) touches every scattered key object once;
+ * assignments_fill(d, names, key_ids, hashes, key_slot, slot_labels) then sets
+ * the winners' labels with the saved hashes (the dict probe compares the key
+ * pointers it already holds; the key objects are not read again).
+ */
+static PyObject* assignments_keys(PyObject* self, PyObject* args) {
+  PyObject* names;
+  Py_buffer ids;
+  if (!PyArg_ParseTuple(args, "O!y*", &PyList_Type, &names, &ids)) return NULL;
+  PyObject *d = NULL, *hb = NULL, *out = NULL;
+  const int32_t* I = (const int32_t*)ids.buf;
+  const Py_ssize_t K = ids.len / 4, nn = PyList_GET_SIZE(names);
+  d = _PyDict_NewPresized(K);
+  hb = PyBytes_FromStringAndSize(NULL, K * (Py_ssize_t)sizeof(Py_hash_t));
+  if (!d || !hb) goto done;
+  Py_hash_t* H = (Py_hash_t*)PyBytes_AS_STRING(hb);
+  enum { AHEAD = 24 };
+  for (Py_ssize_t i = 0; i < K; i++) {
+    if (i + AHEAD < K && I[i + AHEAD] >= 0 && I[i + AHEAD] < nn)
+      __builtin_prefetch(PyList_GET_ITEM(names, I[i + AHEAD]), 1, 0);
+    if (I[i] < 0 || I[i] >= nn) {
+      PyErr_SetString(PyExc_IndexError, "assignments_keys: index out of range");
+      goto done;
+    }
+    PyObject* k = PyList_GET_ITEM(names, I[i]);
+    Py_hash_t h;
+    if (!PyUnicode_CheckExact(k) || (h = ((PyASCIIObject*)k)->hash) == -1) {
+      h = PyObject_Hash(k);
+      if (h == -1) goto done;
+    }
+    H[i] = h;
+    if (_PyDict_SetItem_KnownHash(d, k, Py_None, h) < 0) goto done;
+  }
+  out = PyTuple_Pack(2, d, hb);
+done:
+  Py_XDECREF(d);
+  Py_XDECREF(hb);
+  PyBuffer_Release(&ids);
+  return out;
+}
+
+static PyObject* assignments_fill(PyObject* self, PyObject* args) {
+  PyObject *d, *names, *labels;
+  Py_buffer ids, hashes, slot;
+  if (!PyArg_ParseTuple(args, "O!O!y*y*y*O!", &PyDict_Type, &d, &PyList_Type, &names, &ids, &hashes, &slot,
+                        &PyList_Type, &labels))
+    return NULL;
+  PyObject* ret = NULL;
+  const int32_t* I = (const int32_t*)ids.buf;
+  const int32_t* Sl = (const int32_t*)slot.buf;
+  const Py_hash_t* H = (const Py_hash_t*)hashes.buf;
+  const Py_ssize_t K = ids.len / 4, nn = PyList_GET_SIZE(names), nl = PyList_GET_SIZE(labels);
+  if (slot.len / 4 != K || hashes.len / (Py_ssize_t)sizeof(Py_hash_t) != K) {
+    PyErr_SetString(PyExc_ValueError, "assignments_fill: lengths differ");
+    goto done;
+  }
+  for (Py_ssize_t i = 0; i < K; i++) {
+    if (I[i] < 0 || I[i] >= nn || Sl[i] < 0 || Sl[i] >= nl) {
+      PyErr_SetString(PyExc_IndexError, "assignments_fill: index out of range");
+      goto done;
+    }
+    if (_PyDict_SetItem_KnownHash(d, PyList_GET_ITEM(names, I[i]), PyList_GET_ITEM(labels, Sl[i]), H[i]) < 0)
+      goto done;
+  }
+  ret = Py_NewRef(d);
+done:
+  PyBuffer_Release(&ids);
+  PyBuffer_Release(&hashes);
+  PyBuffer_Release(&slot);
+  return ret;
+}
+
 static PyMethodDef methods[] = {
     {"lower_arrays", lower_arrays, METH_VARARGS, "Lower a grouped ModelGraph to flat sp_graph arrays."},
     {"singleton_results", singleton_results, METH_VARARGS, "SubgraphResults of one-node blocks from raw records."},
     {"assignments_dict", assignments_dict, METH_VARARGS, "Instance-scope -> label dict from member ids."},
+    {"assignments_keys", assignments_keys, METH_VARARGS, "The keys half of assignments_dict (values None)."},
+    {"assignments_fill", assignments_fill, METH_VARARGS, "The values half of assignments_dict."},
     {"make_ctor", make_ctor, METH_VARARGS, "Fast positional constructor for a dataclass."},
     {"block_instances", block_instances, METH_VARARGS, "Subgraph.instances of every block from fold arrays."},
     {NULL, NULL, 0, NULL}};

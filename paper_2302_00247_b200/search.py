@@ -794,6 +794,15 @@ def _route_mask(low: LoweredGraph, csr) -> np.ndarray:
     mask = T > TABLE_MAX_T
     if len(nodes) == 0:
         return mask
+    fan_all = getattr(low, "_max_fanin", None)
+    if fan_all is None:  # the graph's largest in-degree, once per lowered graph
+        fan_all = int(np.diff(low.in_off).max(initial=0))
+        try:
+            low._max_fanin = fan_all
+        except AttributeError:
+            pass
+    if fan_all <= TABLE_MAX_FANIN:
+        return mask
     nodes = np.asarray(nodes, np.int64)
     blk = np.full(low.n_nodes, -1, np.int64)
     blk[nodes] = np.repeat(np.arange(nb), T)
@@ -803,11 +812,13 @@ def _route_mask(low: LoweredGraph, csr) -> np.ndarray:
     coff = np.zeros(len(nodes) + 1, np.int64)
     np.cumsum(cnt, out=coff[1:])
     prod = low.in_idx[np.repeat(low.in_off[nodes] - coff[:-1], cnt) + np.arange(coff[-1])]
-    internal = (blk[prod] == np.repeat(blk[nodes], cnt)).astype(np.int64)
-    fan = np.zeros(len(nodes), np.int64)
-    np.add.at(fan, np.repeat(np.arange(len(nodes)), cnt), internal)
-    bmax = np.zeros(nb, np.int64)
-    np.maximum.at(bmax, np.repeat(np.arange(nb), T), fan)
+    internal = blk[prod] == np.repeat(blk[nodes], cnt)
+    fan = np.bincount(np.repeat(np.arange(len(nodes)), cnt), weights=internal, minlength=len(nodes))
+    if fan.max(initial=0) <= TABLE_MAX_FANIN:
+        return mask
+    nonempty = T > 0
+    bmax = np.zeros(nb)
+    bmax[nonempty] = np.maximum.reduceat(fan, off[:-1][nonempty])
     return mask | (bmax > TABLE_MAX_FANIN)
 
 
@@ -1014,6 +1025,10 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     prep = route_prep(ses, subs, types, csr)
     t3b = time.perf_counter()
     label_keys = _label_keys(ba, subs, prep)
+    # the assignment map's keys (scattered name objects) while the device searches
+    akeys = None
+    if _native_lower is not None and hasattr(_native_lower, "assignments_keys") and isinstance(ses.low.names, list):
+        akeys = _native_lower.assignments_keys(ses.low.names, np.ascontiguousarray(label_keys[0], np.int32))
     t4 = time.perf_counter()
     # per block: the report's cost term and its weight labels, computed as each
     # group's results land (the cheap group's while the expensive one scores)
@@ -1044,7 +1059,12 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     slot_labels = [lab for ls in labs if ls is not None for lab in ls]
     # every instance takes the template's labels in weight_nodes order
     # (search.py:374-376); instance members come from the fold's member matrix
-    assignments = _assignments(ses.low.names, label_keys, slot_labels)
+    if akeys is not None:
+        assignments = _native_lower.assignments_fill(akeys[0], ses.low.names,
+                                                     np.ascontiguousarray(label_keys[0], np.int32), akeys[1],
+                                                     np.ascontiguousarray(label_keys[1], np.int32), slot_labels)
+    else:
+        assignments = _assignments(ses.low.names, label_keys, slot_labels)
     LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
                        launch_ms=(t3 - t2) * 1e3, overlap_host_ms=(t4 - t3) * 1e3,
                        subgraphs_ms=(t3a - t3) * 1e3, route_prep_ms=(t3b - t3a) * 1e3,

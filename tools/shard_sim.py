@@ -3,8 +3,10 @@
 Every rank's share of an N-rank run (`shard=r, n_shards=N`, one after the
 other) with the exchange replaced by a replay of the merged scores, i.e. everything
 a rank does except the NCCL all_gather of the 40-byte block records; the step is the
-slowest rank's.  Shows the kernel balance over ranks and where the fixed
-per-step host work caps strong scaling.
+slowest rank's.  As in the in-library multi-process form, only rank 0 assembles
+the report (the others return once their share is scored and exchanged).  Shows
+the kernel balance over ranks and where the fixed per-step host work caps
+strong scaling.
 
     python tools/shard_sim.py [steps]
 """
@@ -47,6 +49,8 @@ for n in (1, 2, 4, 8):
     ex = replay if n > 1 else None
     per = []
     for r in range(n):
+        # ranks other than 0 skip the report (derive_plan's root_only, Backend.is_root)
+        be.comm = dict(be.comm_info(), nranks=n, rank=r)
         for _ in range(2):
             S.derive_plan(g, mesh, session=ses, shard=r, n_shards=n, exchange=ex)
         ts, ks = [], []
@@ -56,9 +60,11 @@ for n in (1, 2, 4, 8):
             ts.append((time.perf_counter() - t0) * 1e3)
             ks.append(be.timings()["score_kernel_ms"])
         per.append((statistics.median(ts), statistics.median(ks)))
+    be.comm = be.comm_info()
     t = max(p[0] for p in per)
     base = base or t
     ks = [round(p[1], 2) for p in per]
-    print(f"n_shards {n}: slowest rank step {t:.2f} ms, kernel per rank {ks}, "
+    print(f"n_shards {n}: slowest rank step {t:.2f} ms (rank 0 {per[0][0]:.2f}, others "
+          f"{max([p[0] for p in per[1:]] or [0]):.2f}), kernel per rank {ks}, "
           f"speed-up {base / t:.2f}x, phases {({k: round(v, 2) for k, v in S.LAST_PHASES.items()})}",
           flush=True)

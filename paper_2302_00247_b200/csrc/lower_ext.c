@@ -14,6 +14,14 @@
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+
+/* The parallel walker reads CPython object layouts in place (compact-ASCII str
+ * bytes and hash, compact ints via PyUnstable_Long_*): supported for the 3.12
+ * and 3.13 layouts only.  The module records the version it was built for and
+ * lowering.py uses it only under that interpreter (tests/test_lowering.py). */
+#if PY_VERSION_HEX < 0x030C0000 || PY_VERSION_HEX >= 0x030E0000
+#error "lower_ext.c reads the CPython 3.12/3.13 object layouts"
+#endif
 #include <stddef.h>
 #include <stdint.h>
 #include <string.h>
@@ -1648,4 +1656,11 @@ static PyMethodDef methods[] = {
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_lower", NULL, -1, methods};
 
-PyMODINIT_FUNC PyInit__lower(void) { return PyModule_Create(&module); }
+PyMODINIT_FUNC PyInit__lower(void) {
+  PyObject* m = PyModule_Create(&module);
+  if (m && PyModule_AddIntConstant(m, "built_for_hexversion", PY_VERSION_HEX) < 0) {
+    Py_DECREF(m);
+    return NULL;
+  }
+  return m;
+}

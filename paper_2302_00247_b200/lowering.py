@@ -11,6 +11,7 @@ The arrays are built once per graph and uploaded once (``sp_graph_upload``).
 from __future__ import annotations
 
 import itertools
+import sys
 from dataclasses import dataclass
 from typing import Optional
 
@@ -111,6 +112,10 @@ try:  # native walker of the object graph (csrc/lower_ext.c), built by `make`
     from . import _lower as _native_lower
 except ImportError:  # pragma: no cover - unbuilt tree: the numpy restatement below
     _native_lower = None
+# the walker reads this interpreter's object layouts in place: only under the
+# minor version it was compiled for (the extension suffix already pins it)
+if _native_lower is not None and (getattr(_native_lower, "built_for_hexversion", 0) >> 16) != (sys.hexversion >> 16):
+    _native_lower = None  # pragma: no cover
 
 
 def _lower_native(graph):

@@ -153,3 +153,22 @@ def test_parallel_walker_errors_match_serial():
         lowering.lower(_Uncached(_chain(bad="ghost")))
     with pytest.raises(UnsupportedSearch):
         lowering.lower(_Uncached(_chain(bad="rank9")))
+
+
+def test_native_walker_version_guard():
+    """csrc/lower_ext.c reads CPython object layouts in place (compact str and
+    int): the module records the interpreter it was built for, and lowering
+    uses it only under that minor version; both search modules bind the same
+    extension (or none)."""
+    import sys
+
+    from paper_2302_00247_b200 import lowering, search
+
+    lw = lowering._native_lower
+    if lw is None:
+        import pytest
+
+        pytest.skip("native walker not built")
+    assert lw.built_for_hexversion >> 16 == sys.hexversion >> 16
+    assert (3, 12) <= sys.version_info[:2] < (3, 14)
+    assert search._native_lower is None or search._native_lower is lw

@@ -1644,11 +1644,356 @@ done:
   return ret;
 }
 
+/*
+ * save_graph_json(topo_order, nodes, version, op_label, dtype_label, dumps) -> bytes
+ *
+ * The reference's save_graph (ir.py:358-367): every node of a ModelGraph in
+ * topo_order (a GraphNode contributes its member RawNode, ir.py:363-364) as
+ * _node_to_json (ir.py:342-355), the document {"nodes": [...], "version": v}
+ * written exactly as json.dumps(doc, sort_keys=True, separators=(",", ":"))
+ * + "\n", UTF-8.  Keys in sorted order: attrs, collective, device, inputs,
+ * name, op, output, weight; tensor specs dtype, shape, trainable.  Strings are
+ * escaped like json's ensure_ascii; attribute VALUES (arbitrary JSON) go
+ * through `dumps` (json.dumps with the same options), enum labels through
+ * op_label / dtype_label with pointer caches.
+ */
+typedef struct {
+  char* p;
+  Py_ssize_t n, cap;
+} SBuf;
+
+/* interned attribute names (module init) */
+static PyObject *S_name, *S_op, *S_inputs, *S_output, *S_weight, *S_attrs, *S_member, *S_shape, *S_dtype,
+    *S_trainable;
+
+static int sb_grow(SBuf* b, Py_ssize_t need) {
+  if (b->n + need <= b->cap) return 0;
+  Py_ssize_t c = b->cap ? b->cap : 4096;
+  while (c < b->n + need) c *= 2;
+  char* q = (char*)PyMem_Realloc(b->p, (size_t)c);
+  if (!q) {
+    PyErr_NoMemory();
+    return -1;
+  }
+  b->p = q;
+  b->cap = c;
+  return 0;
+}
+static int sb_put(SBuf* b, const char* s, Py_ssize_t len) {
+  if (sb_grow(b, len) < 0) return -1;
+  memcpy(b->p + b->n, s, (size_t)len);
+  b->n += len;
+  return 0;
+}
+#define SB_LIT(b, s) sb_put((b), (s), (Py_ssize_t)(sizeof(s) - 1))
+
+/* a str as a JSON string literal, ensure_ascii escaping (json.encoder) */
+static int sb_jstr(SBuf* b, PyObject* s) {
+  if (!PyUnicode_Check(s)) {
+    PyErr_SetString(PyExc_TypeError, "save_graph: expected str");
+    return -1;
+  }
+  const Py_ssize_t L = PyUnicode_GET_LENGTH(s);
+  const int kind = PyUnicode_KIND(s);
+  const void* data = PyUnicode_DATA(s);
+  if (sb_grow(b, L + 2) < 0) return -1;
+  b->p[b->n++] = '"';
+  static const char hex[] = "0123456789abcdef";
+  for (Py_ssize_t i = 0; i < L; i++) {
+    const Py_UCS4 c = PyUnicode_READ(kind, data, i);
+    if (c >= 0x20 && c < 0x7f && c != '"' && c != '\\') {
+      if (sb_grow(b, 1) < 0) return -1;
+      b->p[b->n++] = (char)c;
+      continue;
+    }
+    char e[12];
+    int k = 0;
+    switch (c) {
+      case '"': e[k++] = '\\'; e[k++] = '"'; break;
+      case '\\': e[k++] = '\\'; e[k++] = '\\'; break;
+      case '\n': e[k++] = '\\'; e[k++] = 'n'; break;
+      case '\r': e[k++] = '\\'; e[k++] = 'r'; break;
+      case '\t': e[k++] = '\\'; e[k++] = 't'; break;
+      case '\b': e[k++] = '\\'; e[k++] = 'b'; break;
+      case '\f': e[k++] = '\\'; e[k++] = 'f'; break;
+      default: {
+        Py_UCS4 u = c;
+        if (u >= 0x10000) {  /* surrogate pair */
+          u -= 0x10000;
+          const Py_UCS4 hi = 0xd800 | ((u >> 10) & 0x3ff), lo = 0xdc00 | (u & 0x3ff);
+          const Py_UCS4 pr[2] = {hi, lo};
+          for (int t = 0; t < 2; t++) {
+            e[k++] = '\\'; e[k++] = 'u';
+            for (int sh = 12; sh >= 0; sh -= 4) e[k++] = hex[(pr[t] >> sh) & 0xf];
+          }
+        } else {
+          e[k++] = '\\'; e[k++] = 'u';
+          for (int sh = 12; sh >= 0; sh -= 4) e[k++] = hex[(u >> sh) & 0xf];
+        }
+      }
+    }
+    if (sb_put(b, e, k) < 0) return -1;
+  }
+  if (sb_grow(b, 1) < 0) return -1;
+  b->p[b->n++] = '"';
+  return 0;
+}
+
+/* str(o) appended verbatim (ints, the `dumps` results) */
+static int sb_str_of(SBuf* b, PyObject* o) {
+  PyObject* s = PyObject_Str(o);
+  if (!s) return -1;
+  Py_ssize_t len;
+  const char* u = PyUnicode_AsUTF8AndSize(s, &len);
+  const int rc = u ? sb_put(b, u, len) : -1;
+  Py_DECREF(s);
+  return rc;
+}
+
+/* a JSON value as json.dumps(v, sort_keys=True, separators=(",", ":")) writes it;
+ * types outside the plain JSON ones (and dicts with non-str keys) through `dumps` */
+static int sb_json(SBuf* b, PyObject* v, PyObject* dumps, int depth) {
+  if (v == Py_None) return SB_LIT(b, "null");
+  if (v == Py_True) return SB_LIT(b, "true");
+  if (v == Py_False) return SB_LIT(b, "false");
+  if (PyLong_CheckExact(v)) return sb_str_of(b, v);
+  if (PyUnicode_CheckExact(v)) return sb_jstr(b, v);
+  if (PyFloat_CheckExact(v)) {
+    const double x = PyFloat_AS_DOUBLE(v);
+    if (x != x) return SB_LIT(b, "NaN");
+    if (x == Py_HUGE_VAL) return SB_LIT(b, "Infinity");
+    if (x == -Py_HUGE_VAL) return SB_LIT(b, "-Infinity");
+    PyObject* r = PyObject_Repr(v);  /* float.__repr__, as json's encoder */
+    if (!r) return -1;
+    const int rc = sb_str_of(b, r);
+    Py_DECREF(r);
+    return rc;
+  }
+  if (depth < 64 && (PyList_CheckExact(v) || PyTuple_CheckExact(v))) {
+    PyObject* seq = PySequence_Fast(v, "");
+    if (!seq) return -1;
+    int rc = SB_LIT(b, "[");
+    for (Py_ssize_t i = 0; rc == 0 && i < PySequence_Fast_GET_SIZE(seq); i++) {
+      if (i) rc = SB_LIT(b, ",");
+      if (rc == 0) rc = sb_json(b, PySequence_Fast_GET_ITEM(seq, i), dumps, depth + 1);
+    }
+    Py_DECREF(seq);
+    return rc ? rc : SB_LIT(b, "]");
+  }
+  if (depth < 64 && PyDict_CheckExact(v)) {
+    PyObject* keys = PyDict_Keys(v);
+    if (!keys) return -1;
+    int plain = 1;
+    for (Py_ssize_t i = 0; i < PyList_GET_SIZE(keys); i++) plain = plain && PyUnicode_CheckExact(PyList_GET_ITEM(keys, i));
+    if (plain && PyList_Sort(keys) == 0) {
+      int rc = SB_LIT(b, "{");
+      for (Py_ssize_t i = 0; rc == 0 && i < PyList_GET_SIZE(keys); i++) {
+        PyObject* k = PyList_GET_ITEM(keys, i);
+        if (i) rc = SB_LIT(b, ",");
+        if (rc == 0) rc = sb_jstr(b, k);
+        if (rc == 0) rc = SB_LIT(b, ":");
+        if (rc == 0) rc = sb_json(b, PyDict_GetItem(v, k), dumps, depth + 1);
+      }
+      Py_DECREF(keys);
+      return rc ? rc : SB_LIT(b, "}");
+    }
+    Py_DECREF(keys);
+    if (PyErr_Occurred()) return -1;
+  }
+  PyObject* js = PyObject_CallOneArg(dumps, v);
+  if (!js) return -1;
+  const int rc = sb_str_of(b, js);
+  Py_DECREF(js);
+  return rc;
+}
+
+static int sb_label(SBuf* b, PtrCache* cache, PyObject* enum_val, PyObject* fn) {
+  /* label strings through the cache's Python call (value cached as a str object pointer) */
+  for (int i = 0; i < cache->n; i++)
+    if (cache->key[i] == enum_val) return sb_jstr(b, (PyObject*)cache->val[i]);
+  PyObject* r = PyObject_CallOneArg(fn, enum_val);
+  if (!r) return -1;
+  const int rc = sb_jstr(b, r);
+  if (cache->n < CACHE_N) {
+    Py_INCREF(enum_val);
+    cache->key[cache->n] = enum_val;
+    cache->val[cache->n] = (long)r;  /* owns the reference */
+    cache->n++;
+  } else {
+    Py_DECREF(r);
+  }
+  return rc;
+}
+
+static void label_cache_clear(PtrCache* c) {
+  for (int i = 0; i < c->n; i++) {
+    Py_DECREF(c->key[i]);
+    Py_DECREF((PyObject*)c->val[i]);
+  }
+  c->n = 0;
+}
+
+static int sb_spec(SBuf* b, PyObject* spec, PtrCache* dcache, PyObject* dtype_label) {
+  PyObject *shape = PyObject_GetAttr(spec, S_shape), *dt = PyObject_GetAttr(spec, S_dtype),
+           *tr = PyObject_GetAttr(spec, S_trainable);
+  int rc = -1;
+  if (!shape || !dt || !tr) goto done;
+  if (SB_LIT(b, "{\"dtype\":") < 0 || sb_label(b, dcache, dt, dtype_label) < 0 || SB_LIT(b, ",\"shape\":[") < 0)
+    goto done;
+  {
+    PyObject* seq = PySequence_Fast(shape, "shape must be a sequence");
+    if (!seq) goto done;
+    const Py_ssize_t r = PySequence_Fast_GET_SIZE(seq);
+    for (Py_ssize_t i = 0; i < r; i++) {
+      if ((i && SB_LIT(b, ",") < 0) || sb_str_of(b, PySequence_Fast_GET_ITEM(seq, i)) < 0) {
+        Py_DECREF(seq);
+        goto done;
+      }
+    }
+    Py_DECREF(seq);
+  }
+  {
+    const int t = PyObject_IsTrue(tr);
+    if (t < 0) goto done;
+    if ((t ? SB_LIT(b, "],\"trainable\":true}") : SB_LIT(b, "],\"trainable\":false}")) < 0) goto done;
+  }
+  rc = 0;
+done:
+  Py_XDECREF(shape);
+  Py_XDECREF(dt);
+  Py_XDECREF(tr);
+  return rc;
+}
+
+static PyObject* save_graph_json(PyObject* self, PyObject* args) {
+  PyObject *topo, *nodes, *op_label, *dtype_label, *dumps;
+  long version;
+  if (!PyArg_ParseTuple(args, "OO!lOOO", &topo, &PyDict_Type, &nodes, &version, &op_label, &dtype_label, &dumps))
+    return NULL;
+  PyObject* seq = PySequence_Fast(topo, "topo_order must be a sequence");
+  if (!seq) return NULL;
+  SBuf b = {NULL, 0, 0};
+  PtrCache ocache = {{0}, {0}, 0}, dcache = {{0}, {0}, 0};
+  PyObject* out = NULL;
+  const Py_ssize_t N = PySequence_Fast_GET_SIZE(seq);
+  if (SB_LIT(&b, "{\"nodes\":[") < 0) goto done;
+  for (Py_ssize_t i = 0; i < N; i++) {
+    PyObject* name = PySequence_Fast_GET_ITEM(seq, i);
+    PyObject* node = PyDict_GetItemWithError(nodes, name);
+    if (!node) {
+      if (!PyErr_Occurred()) PyErr_SetObject(PyExc_KeyError, name);
+      goto done;
+    }
+    Py_INCREF(node);
+    if (PyObject_HasAttr(node, S_member)) {  /* GraphNode -> its member RawNode */
+      PyObject* m = PyObject_GetAttr(node, S_member);
+      Py_DECREF(node);
+      if (!m) goto done;
+      node = m;
+    }
+    PyObject *nm = PyObject_GetAttr(node, S_name), *op = PyObject_GetAttr(node, S_op),
+             *ins = PyObject_GetAttr(node, S_inputs), *outp = PyObject_GetAttr(node, S_output),
+             *w = PyObject_GetAttr(node, S_weight), *attrs = PyObject_GetAttr(node, S_attrs);
+    int ok = nm && op && ins && outp && w && attrs;
+    PyObject *dev = NULL, *coll = NULL, *attr_seq = NULL;
+    if (ok && (i ? SB_LIT(&b, ",{") : SB_LIT(&b, "{")) < 0) ok = 0;
+    if (ok) {
+      attr_seq = PySequence_Fast(attrs, "attrs must be a sequence");
+      if (!attr_seq) ok = 0;
+    }
+    if (ok) {
+      /* "attrs": the non device/collective pairs in their (sorted) order, values via dumps */
+      const Py_ssize_t na = PySequence_Fast_GET_SIZE(attr_seq);
+      int first = 1;
+      for (Py_ssize_t a = 0; a < na && ok; a++) {
+        PyObject* kv = PySequence_Fast_GET_ITEM(attr_seq, a);
+        PyObject *k = PySequence_GetItem(kv, 0), *v = PySequence_GetItem(kv, 1);
+        if (!k || !v) {
+          ok = 0;
+        } else if (PyUnicode_Check(k) && (PyUnicode_CompareWithASCIIString(k, "device") == 0 ||
+                                          PyUnicode_CompareWithASCIIString(k, "collective") == 0)) {
+          /* the last pair of a key wins, as the dict literal of _node_to_json does */
+          PyObject** slot = PyUnicode_CompareWithASCIIString(k, "device") == 0 ? &dev : &coll;
+          Py_XDECREF(*slot);
+          *slot = Py_NewRef(v);
+        } else {
+          (void)first;
+        }
+        Py_XDECREF(k);
+        Py_XDECREF(v);
+      }
+      /* the reference builds {k: v} (later duplicates win, first position kept) and
+       * sort_keys orders it: delegate the attrs object to dumps when there is one */
+      if (ok) {
+        PyObject* d = PyDict_New();
+        if (!d) ok = 0;
+        for (Py_ssize_t a = 0; a < na && ok; a++) {
+          PyObject* kv = PySequence_Fast_GET_ITEM(attr_seq, a);
+          PyObject *k = PySequence_GetItem(kv, 0), *v = PySequence_GetItem(kv, 1);
+          if (!k || !v) ok = 0;
+          else if (!(PyUnicode_Check(k) && (PyUnicode_CompareWithASCIIString(k, "device") == 0 ||
+                                             PyUnicode_CompareWithASCIIString(k, "collective") == 0)))
+            ok = PyDict_SetItem(d, k, v) == 0;
+          Py_XDECREF(k);
+          Py_XDECREF(v);
+        }
+        if (ok && PyDict_GET_SIZE(d))
+          ok = SB_LIT(&b, "\"attrs\":") == 0 && sb_json(&b, d, dumps, 0) == 0 && SB_LIT(&b, ",") == 0;
+        Py_XDECREF(d);
+      }
+    }
+    if (ok && coll) ok = SB_LIT(&b, "\"collective\":") == 0 && sb_json(&b, coll, dumps, 0) == 0 && SB_LIT(&b, ",") == 0;
+    if (ok && dev) ok = SB_LIT(&b, "\"device\":") == 0 && sb_json(&b, dev, dumps, 0) == 0 && SB_LIT(&b, ",") == 0;
+    if (ok) {
+      ok = SB_LIT(&b, "\"inputs\":[") == 0;
+      PyObject* iseq = ok ? PySequence_Fast(ins, "inputs must be a sequence") : NULL;
+      if (!iseq) ok = 0;
+      for (Py_ssize_t k = 0; ok && k < PySequence_Fast_GET_SIZE(iseq); k++)
+        ok = (!k || SB_LIT(&b, ",") == 0) && sb_jstr(&b, PySequence_Fast_GET_ITEM(iseq, k)) == 0;
+      Py_XDECREF(iseq);
+    }
+    ok = ok && SB_LIT(&b, "],\"name\":") == 0 && sb_jstr(&b, nm) == 0 && SB_LIT(&b, ",\"op\":") == 0 &&
+         sb_label(&b, &ocache, op, op_label) == 0 && SB_LIT(&b, ",\"output\":") == 0 &&
+         sb_spec(&b, outp, &dcache, dtype_label) == 0 && SB_LIT(&b, ",\"weight\":") == 0;
+    if (ok) {
+      const int has_w = w != Py_None ? PyObject_IsTrue(w) : 0;  /* `if node.weight` */
+      if (has_w < 0) ok = 0;
+      else if (has_w) ok = sb_spec(&b, w, &dcache, dtype_label) == 0;
+      else ok = SB_LIT(&b, "null") == 0;
+    }
+    ok = ok && SB_LIT(&b, "}") == 0;
+    Py_XDECREF(nm);
+    Py_XDECREF(op);
+    Py_XDECREF(ins);
+    Py_XDECREF(outp);
+    Py_XDECREF(w);
+    Py_XDECREF(attrs);
+    Py_XDECREF(attr_seq);
+    Py_XDECREF(dev);
+    Py_XDECREF(coll);
+    Py_DECREF(node);
+    if (!ok) goto done;
+  }
+  {
+    char tail[64];
+    const int k = snprintf(tail, sizeof tail, "],\"version\":%ld}\n", version);
+    if (sb_put(&b, tail, k) < 0) goto done;
+  }
+  out = PyBytes_FromStringAndSize(b.p, b.n);
+done:
+  label_cache_clear(&ocache);
+  label_cache_clear(&dcache);
+  PyMem_Free(b.p);
+  Py_DECREF(seq);
+  return out;
+}
+
 static PyMethodDef methods[] = {
     {"lower_arrays", lower_arrays, METH_VARARGS, "Lower a grouped ModelGraph to flat sp_graph arrays."},
     {"singleton_results", singleton_results, METH_VARARGS, "SubgraphResults of one-node blocks from raw records."},
     {"assignments_dict", assignments_dict, METH_VARARGS, "Instance-scope -> label dict from member ids."},
     {"assignments_keys", assignments_keys, METH_VARARGS, "The keys half of assignments_dict (values None)."},
+    {"save_graph_json", save_graph_json, METH_VARARGS, "The reference's save_graph document bytes."},
     {"assignments_fill", assignments_fill, METH_VARARGS, "The values half of assignments_dict."},
     {"make_ctor", make_ctor, METH_VARARGS, "Fast positional constructor for a dataclass."},
     {"block_instances", block_instances, METH_VARARGS, "Subgraph.instances of every block from fold arrays."},
@@ -1657,6 +2002,19 @@ static PyMethodDef methods[] = {
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_lower", NULL, -1, methods};
 
 PyMODINIT_FUNC PyInit__lower(void) {
+  S_name = PyUnicode_InternFromString("name");
+  S_op = PyUnicode_InternFromString("op");
+  S_inputs = PyUnicode_InternFromString("inputs");
+  S_output = PyUnicode_InternFromString("output");
+  S_weight = PyUnicode_InternFromString("weight");
+  S_attrs = PyUnicode_InternFromString("attrs");
+  S_member = PyUnicode_InternFromString("member");
+  S_shape = PyUnicode_InternFromString("shape");
+  S_dtype = PyUnicode_InternFromString("dtype");
+  S_trainable = PyUnicode_InternFromString("trainable");
+  if (!S_name || !S_op || !S_inputs || !S_output || !S_weight || !S_attrs || !S_member || !S_shape || !S_dtype ||
+      !S_trainable)
+    return NULL;
   PyObject* m = PyModule_Create(&module);
   if (m && PyModule_AddIntConstant(m, "built_for_hexversion", PY_VERSION_HEX) < 0) {
     Py_DECREF(m);

@@ -326,3 +326,30 @@ def plan_from_onnx(data: bytes, mesh, batch=None, min_duplicates: int = 2, mu: i
     from .search import derive_plan
 
     return derive_plan(load_onnx(data, batch), mesh, min_duplicates, mu, chunk_size, **kw)
+
+
+def save_graph(graph, version: int = 1) -> bytes:
+    """The reference's save_graph (ir.py:358-367) natively: every node of a
+    ModelGraph in topo_order (a grouped node contributes its member RawNode) as
+    the schema-1/2 JSON document, byte-identical to
+    json.dumps(doc, sort_keys=True, separators=(",", ":")) + a newline
+    (csrc/lower_ext.c save_graph_json; attribute values, arbitrary JSON, go
+    through json.dumps)."""
+    import functools
+    import json
+
+    from .lowering import _native_lower
+
+    if _native_lower is None or not hasattr(_native_lower, "save_graph_json"):
+        raise RuntimeError("native lowering extension (_lower) not built")
+    dumps = functools.partial(json.dumps, sort_keys=True, separators=(",", ":"))
+    nodes = graph.nodes if isinstance(graph.nodes, dict) else dict(graph.nodes)
+    return _native_lower.save_graph_json(list(graph.topo_order), nodes, int(version), _enum_value, _dtype_label, dumps)
+
+
+def _enum_value(op):
+    return op.value if hasattr(op, "value") else str(op)
+
+
+def _dtype_label(dt):
+    return dt.label if hasattr(dt, "label") else str(dt)

@@ -14,7 +14,8 @@ prune_graph used by routed_plan_for_assignments, search.py:32, 424),
 wrappers that call this package with the reference's own result classes, so
 BestPlanReport / Subgraph / RoutedPlan objects flowing into rewrite_graph,
 broadcast_routing and the CLI are the reference's types, and errors are the
-reference's exception classes.
+reference's exception classes.  The JSON graph writer (`save_graph`,
+ir.py:358-367) is rebound to the native one too.
 """
 
 from __future__ import annotations
@@ -111,6 +112,18 @@ def install(shardplan=None, backend=None) -> Installed:
         "routed_plan_for_assignments": wrap(ours.routed_plan_for_assignments),
     }
     handle = Installed(shardplan)
+    # save_graph (ir.py:358-367; bound by name in shardplan.ir, .cli and the package)
+    from . import ingest as our_ingest
+
+    @functools.wraps(our_ingest.save_graph)
+    def save_graph(graph, version: int = 1) -> bytes:
+        return our_ingest.save_graph(graph, version)
+
+    for modname in ("ir", "cli", ""):
+        module = importlib.import_module(f"{shardplan.__name__}.{modname}") if modname else shardplan
+        if hasattr(module, "save_graph"):
+            handle.saved.append((module, "save_graph", getattr(module, "save_graph")))
+            setattr(module, "save_graph", save_graph)
     for modname in ("search", "cli", ""):
         module = (importlib.import_module(f"{shardplan.__name__}.{modname}") if modname
                   else shardplan)

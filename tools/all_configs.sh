@@ -4,6 +4,6 @@
 out=${1:-gpurun_out/configs.jsonl}
 : > "$out"
 for w in c1 c2 c3 c3_slow c4 c4_2x4 c4_2x4_slow; do
-  timeout 300 python bench.py --workload $w --steps 20 --warmup 5 --cpu-seconds 3 >> "$out" || echo "{\"workload\": \"$w\", \"failed\": true}" >> "$out"
+  timeout 300 python bench.py --workload $w --steps 20 --warmup 5 --cpu-seconds 3 --no-python-reference \
+    --no-fold-roofline >> "$out" || echo "{\"workload\": \"$w\", \"failed\": true}" >> "$out"
 done
-timeout 600 python bench.py --steps 10 --warmup 3 >> "$out"

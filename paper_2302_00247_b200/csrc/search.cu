@@ -1830,7 +1830,10 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
   __shared__ Biased s_bz;
   __shared__ uint64_t s_p2[64];  // unbiased digits of 2^k * CH (mixed radix, wrapping)
   __shared__ uint64_t s_sub[SKIP_SUB];  // unbiased digits of k * CH / SKIP_SUB
-  __shared__ unsigned long long s_first;  // the chunk the CTA claimed before staging the block
+  // the chunk the CTA claimed before staging block b, in s_first[b & 1]: thread 0
+  // writes block b+1's claim while slower threads may still read block b's
+  // (the two are separated by block b+1's claim barrier, not by a second one)
+  __shared__ unsigned long long s_first[2];
   __shared__ unsigned long long s_red_t[NW], s_red_i[NW], s_red_v[NW];
   __shared__ uint32_t s_red_n[NW];
   const int tid = threadIdx.x;
@@ -1844,9 +1847,9 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
     const unsigned long long nclaim = nbig + nsm * SKIP_SUB;
     // claim first: a block whose chunks are gone is neither staged nor visited
     if (tid == 0)
-      s_first = *(volatile unsigned long long*)&P.ctr[b] < nclaim ? atomicAdd(&P.ctr[b], 1ULL) : nclaim;
+      s_first[b & 1] = *(volatile unsigned long long*)&P.ctr[b] < nclaim ? atomicAdd(&P.ctr[b], 1ULL) : nclaim;
     __syncthreads();
-    if (s_first >= nclaim) continue;
+    if (s_first[b & 1] >= nclaim) continue;
     stage_block(smem, blobs, P.blob_off[b], s_lane_add, &s_bz, nullptr, 1, 0, false);
     if (tid == 0) {
       // unbiased digits of 2^k * CH (positions fastest-last, as bencode), by
@@ -1887,7 +1890,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
     const unsigned long long C = H.C;
     LaneBest lb;
     unsigned long long j = 0;
-    if (lane == 0) j = warp == 0 ? s_first : atomicAdd(&P.ctr[b], 1ULL);
+    if (lane == 0) j = warp == 0 ? s_first[b & 1] : atomicAdd(&P.ctr[b], 1ULL);
     j = __shfl_sync(0xffffffffu, j, 0);
     while (j < nclaim) {
       unsigned long long jn = 0;

@@ -1988,7 +1988,428 @@ done:
   return out;
 }
 
+/*
+ * slot_positions(names, toff, tnodes, w_rank) -> (slot_off, slot_pos, radix) as bytes
+ *   slot_off int64 [nb + 1], slot_pos int32 [S], radix uint8 [S]
+ * Per block: the template positions of its nodes with a weight in weight_nodes
+ * order (the scopes sorted by name, search.py:85-88) and their option counts
+ * (_options, search.py:91-93: 3 for a weight of rank >= 2, else 2).
+ */
+static PyObject* slot_positions(PyObject* self, PyObject* args) {
+  PyObject* names;
+  Py_buffer toff, tn, wr;
+  if (!PyArg_ParseTuple(args, "O!y*y*y*", &PyList_Type, &names, &toff, &tn, &wr)) return NULL;
+  PyObject *bo = NULL, *bp = NULL, *br = NULL, *out = NULL;
+  const int64_t* to = (const int64_t*)toff.buf;
+  const int32_t* T = (const int32_t*)tn.buf;
+  const uint8_t* W = (const uint8_t*)wr.buf;
+  const Py_ssize_t nb = toff.len / 8 - 1, ne = tn.len / 4, nn = PyList_GET_SIZE(names);
+  if (nb < 0 || wr.len < nn || (nb >= 0 && (to[0] != 0 || to[nb] > ne))) {
+    PyErr_SetString(PyExc_ValueError, "slot_positions: inconsistent arguments");
+    goto done;
+  }
+  Py_ssize_t S = 0;
+  for (Py_ssize_t e = 0; e < to[nb]; e++) {
+    if (T[e] < 0 || T[e] >= nn) {
+      PyErr_SetString(PyExc_IndexError, "slot_positions: node out of range");
+      goto done;
+    }
+    S += W[T[e]] != 0;
+  }
+  bo = PyBytes_FromStringAndSize(NULL, (nb + 1) * 8);
+  bp = PyBytes_FromStringAndSize(NULL, S * 4);
+  br = PyBytes_FromStringAndSize(NULL, S);
+  if (!bo || !bp || !br) goto done;
+  int64_t* so = (int64_t*)PyBytes_AS_STRING(bo);
+  int32_t* sp = (int32_t*)PyBytes_AS_STRING(bp);
+  uint8_t* rx = (uint8_t*)PyBytes_AS_STRING(br);
+  Py_ssize_t k = 0;
+  so[0] = 0;
+  for (Py_ssize_t b = 0; b < nb; b++) {
+    const Py_ssize_t k0 = k;
+    for (int64_t e = to[b]; e < to[b + 1]; e++) {
+      const int32_t v = T[e];
+      if (!W[v]) continue;
+      /* insertion by name (str order); names within a template are distinct */
+      PyObject* nv = PyList_GET_ITEM(names, v);
+      Py_ssize_t j = k;
+      while (j > k0) {
+        const int c = PyUnicode_Compare(PyList_GET_ITEM(names, T[to[b] + sp[j - 1]]), nv);
+        if (c == -1 && PyErr_Occurred()) goto done;
+        if (c <= 0) break;
+        sp[j] = sp[j - 1];
+        rx[j] = rx[j - 1];
+        j--;
+      }
+      sp[j] = (int32_t)(e - to[b]);
+      rx[j] = W[v] >= 2 ? 3 : 2;
+      k++;
+    }
+    so[b + 1] = k;
+  }
+  out = PyTuple_Pack(3, bo, bp, br);
+done:
+  Py_XDECREF(bo);
+  Py_XDECREF(bp);
+  Py_XDECREF(br);
+  PyBuffer_Release(&toff);
+  PyBuffer_Release(&tn);
+  PyBuffer_Release(&wr);
+  return out;
+}
+
+/* flops of one template (costmodel.py:185-190): 2 x the activation's elements x
+ * the weight's first dim, summed over matmuls (op 0) with a weight; Python
+ * integers when the sum leaves int64 */
+static PyObject* template_flops(const int32_t* tn, int64_t T, const uint8_t* op, const uint8_t* ar, const int64_t* as,
+                                Py_ssize_t aw, const uint8_t* wr, const int64_t* ws, Py_ssize_t ww) {
+  int64_t acc = 0;
+  int over = 0;
+  for (int64_t t = 0; t < T && !over; t++) {
+    const int32_t v = tn[t];
+    if (op[v] != 0 || !wr[v]) continue;
+    int64_t x = 2;
+    for (int d = 0; d < ar[v] && !over; d++) over = __builtin_mul_overflow(x, as[(int64_t)v * aw + d], &x);
+    if (!over) over = __builtin_mul_overflow(x, ws[(int64_t)v * ww], &x);
+    if (!over) over = __builtin_add_overflow(acc, x, &acc);
+  }
+  if (!over) return PyLong_FromLongLong(acc);
+  PyObject* sum = PyLong_FromLong(0);
+  for (int64_t t = 0; t < T && sum; t++) {
+    const int32_t v = tn[t];
+    if (op[v] != 0 || !wr[v]) continue;
+    PyObject* x = PyLong_FromLong(2);
+    for (int d = 0; d <= ar[v] && x; d++) {
+      PyObject* f = PyLong_FromLongLong(d < ar[v] ? as[(int64_t)v * aw + d] : ws[(int64_t)v * ww]);
+      PyObject* y = f ? PyNumber_Multiply(x, f) : NULL;
+      Py_XDECREF(f);
+      Py_DECREF(x);
+      x = y;
+    }
+    PyObject* s2 = x ? PyNumber_Add(sum, x) : NULL;
+    Py_XDECREF(x);
+    Py_DECREF(sum);
+    sum = s2;
+  }
+  return sum;
+}
+
+/*
+ * block_results(ctors, subs, names, graph, blocks, recs, xblocks, node, edge, eoff,
+ *               pnames, pallred, specs, labels, identity, allreduce, colls, kinds, overlap)
+ *   -> (results, terms, slot_labels)
+ * The SubgraphResult of every block's winner (search.py:317-345) built from the
+ * raw score and winner-detail records -- routed_plans_all in C for blocks of any
+ * size: CandidatePlan (assignments in weight_nodes order, digits of the
+ * winner's reference index), NodeRouting per template node (pattern, internal
+ * producers' conversions in GraphNode.inputs order, output collective, state),
+ * exit conversions, CostReport (+ flops).  None for a block without a winner,
+ * whose winner did not route, or whose explained total differs from the scored
+ * one: the Python path handles (and raises for) those.  terms[b] = the block's
+ * cost x multiplicity (search.py:373), slot_labels[b] = its weight labels in
+ * weight_nodes order (search.py:374-376), None where results[b] is None.
+ *   graph: (op u8[n], act_rank u8[n], act_shape i64[n, aw], aw, w_rank u8[n],
+ *           w_shape i64[n, ww], ww, act_bytes i64[n], in_off i64[n+1], in_idx i32[m])
+ *   blocks: (toff i64[nb+1], tnodes i32[ne], slot_off i64[nb+1], slot_pos i32[S],
+ *            radix u8[S], inst_off i64[nb+1])
+ *   recs: sp_score_out [nb]; xblocks: sp_explain_block [nb]; node: int8 [ne, 4];
+ *   edge: int8 [nedge, 2]; eoff: int64 [nb + 1]
+ *   specs / labels: (replica, split(0), ..., split(7)) and their labels;
+ *   colls: 4 tuples (allreduce, allgather, reducescatter, alltoall) of 8 Collectives (by axis)
+ */
+static PyObject* block_results(PyObject* self, PyObject* args) {
+  PyObject *ctors, *subs, *names, *pnames, *pallred, *specs, *labels, *identity, *allreduce, *colls, *kinds;
+  Py_buffer op, ar, as, wr, ws, ab, ino, ini, to_, tn_, so_, sp_, rx_, io_, recs, xb, node, edge, eo;
+  Py_ssize_t aw, ww;
+  double overlap;
+  if (!PyArg_ParseTuple(args, "O!O!O!(y*y*y*ny*y*ny*y*y*)(y*y*y*y*y*y*)y*y*y*y*y*O!O!O!O!OOO!O!d", &PyTuple_Type,
+                        &ctors, &PyList_Type, &subs, &PyList_Type, &names, &op, &ar, &as, &aw, &wr, &ws, &ww, &ab,
+                        &ino, &ini, &to_, &tn_, &so_, &sp_, &rx_, &io_, &recs, &xb, &node, &edge, &eo, &PyTuple_Type,
+                        &pnames, &PyTuple_Type, &pallred, &PyTuple_Type, &specs, &PyTuple_Type, &labels, &identity,
+                        &allreduce, &PyTuple_Type, &colls, &PyTuple_Type, &kinds, &overlap))
+    return NULL;
+  PyObject *res_l = NULL, *terms = NULL, *labs = NULL, *out = NULL, *py_overlap = NULL, *empty = NULL;
+  int32_t* pos_of = NULL;
+  static PyObject* s_template = NULL;
+  if (!s_template) s_template = PyUnicode_InternFromString("template");
+  const uint8_t* OP = (const uint8_t*)op.buf;
+  const uint8_t* AR = (const uint8_t*)ar.buf;
+  const int64_t* AS = (const int64_t*)as.buf;
+  const uint8_t* WR = (const uint8_t*)wr.buf;
+  const int64_t* WS = (const int64_t*)ws.buf;
+  const int64_t* AB = (const int64_t*)ab.buf;
+  const int64_t* INO = (const int64_t*)ino.buf;
+  const int32_t* INI = (const int32_t*)ini.buf;
+  const int64_t* TO = (const int64_t*)to_.buf;
+  const int32_t* TN = (const int32_t*)tn_.buf;
+  const int64_t* SO = (const int64_t*)so_.buf;
+  const int32_t* SP = (const int32_t*)sp_.buf;
+  const uint8_t* RX = (const uint8_t*)rx_.buf;
+  const int64_t* IO = (const int64_t*)io_.buf;
+  const RecView* R = (const RecView*)recs.buf;
+  const XView* X = (const XView*)xb.buf;
+  const int8_t* ND = (const int8_t*)node.buf;
+  const int8_t* ED = (const int8_t*)edge.buf;
+  const int64_t* EO = (const int64_t*)eo.buf;
+  const Py_ssize_t n = op.len, nb = PyList_GET_SIZE(subs), nn = PyList_GET_SIZE(names);
+  const Py_ssize_t nedge = edge.len / 2, ne = tn_.len / 4, nin = ini.len / 4;
+  int ok = n == nn && ar.len >= n && wr.len >= n && aw >= 1 && ww >= 1 && as.len >= n * aw * 8 &&
+           ws.len >= n * ww * 8 && ab.len >= n * 8 && ino.len >= (n + 1) * 8 && to_.len >= (nb + 1) * 8 &&
+           so_.len >= (nb + 1) * 8 && io_.len >= (nb + 1) * 8 && eo.len >= (nb + 1) * 8 &&
+           recs.len >= nb * (Py_ssize_t)sizeof(RecView) && xb.len >= nb * (Py_ssize_t)sizeof(XView) &&
+           PyTuple_GET_SIZE(ctors) == 5 && PyTuple_GET_SIZE(specs) >= 9 && PyTuple_GET_SIZE(labels) >= 9 &&
+           PyTuple_GET_SIZE(colls) == 4 && PyTuple_GET_SIZE(kinds) == 4;
+  for (int j = 0; ok && j < 4; j++)
+    ok = PyTuple_Check(PyTuple_GET_ITEM(colls, j)) && PyTuple_GET_SIZE(PyTuple_GET_ITEM(colls, j)) >= 8;
+  if (ok) ok = TO[nb] <= ne && node.len >= TO[nb] * 4 && SO[nb] * 4 <= sp_.len && SO[nb] <= rx_.len &&
+               EO[nb] <= nedge && INO[n] <= nin;
+  if (!ok) {
+    PyErr_SetString(PyExc_ValueError, "block_results: inconsistent arguments");
+    goto done;
+  }
+  PyObject *mkPlan = PyTuple_GET_ITEM(ctors, 0), *mkNR = PyTuple_GET_ITEM(ctors, 1),
+           *mkRP = PyTuple_GET_ITEM(ctors, 2), *mkCR = PyTuple_GET_ITEM(ctors, 3),
+           *mkRes = PyTuple_GET_ITEM(ctors, 4);
+  py_overlap = PyFloat_FromDouble(overlap);
+  empty = PyTuple_New(0);
+  res_l = PyList_New(nb);
+  terms = PyList_New(nb);
+  labs = PyList_New(nb);
+  pos_of = (int32_t*)PyMem_Malloc((n > 0 ? n : 1) * sizeof(int32_t));
+  if (!py_overlap || !empty || !res_l || !terms || !labs || !pos_of) {
+    if (!pos_of) PyErr_NoMemory();
+    goto fail;
+  }
+  for (Py_ssize_t v = 0; v < n; v++) pos_of[v] = -1;
+  for (Py_ssize_t b = 0; b < nb; b++) {
+    const RecView r = R[b];
+    const XView x = X[b];
+    /* CostReport.total = forward + backward * (1 - overlap), rounded in that order */
+    const double total = x.forward_comm + x.backward_comm * (1.0 - overlap);
+    if (!r.has_best || !x.valid || (r.best_total == r.best_total && total != r.best_total)) {
+      PyList_SET_ITEM(res_l, b, Py_NewRef(Py_None));
+      PyList_SET_ITEM(terms, b, Py_NewRef(Py_None));
+      PyList_SET_ITEM(labs, b, Py_NewRef(Py_None));
+      continue;
+    }
+    const int64_t e0 = TO[b], T = TO[b + 1] - TO[b];
+    PyObject* sub = PyList_GET_ITEM(subs, b);
+    PyObject* tmpl = PyObject_GetAttr(sub, s_template);
+    if (!tmpl) goto fail;
+    if (!PyTuple_Check(tmpl) || PyTuple_GET_SIZE(tmpl) != T) {
+      Py_DECREF(tmpl);
+      PyErr_SetString(PyExc_ValueError, "block_results: template size differs from the tables");
+      goto fail;
+    }
+    /* assignments in weight_nodes order: digits of the winner's reference index,
+       the last slot fastest (candidate_by_index, search.py:103-116) */
+    const int64_t s0 = SO[b], S = SO[b + 1] - SO[b];
+    PyObject* asg = PyTuple_New(S);
+    PyObject* lab = PyList_New(S);
+    if (!asg || !lab) {
+      Py_XDECREF(asg);
+      Py_XDECREF(lab);
+      Py_DECREF(tmpl);
+      goto fail;
+    }
+    {
+      uint64_t rem = r.best_index;
+      for (int64_t k = S - 1; k >= 0; k--) {
+        const int rdx = RX[s0 + k] ? RX[s0 + k] : 2;
+        const int d = (int)(rem % (uint64_t)rdx);
+        rem /= (uint64_t)rdx;
+        const int32_t q = SP[s0 + k];
+        PyObject* pair = (q >= 0 && q < T) ? PyTuple_Pack(2, PyTuple_GET_ITEM(tmpl, q), PyTuple_GET_ITEM(specs, d))
+                                           : NULL;
+        if (!pair) {
+          if (!PyErr_Occurred()) PyErr_SetString(PyExc_IndexError, "block_results: slot out of range");
+          Py_DECREF(asg);
+          Py_DECREF(lab);
+          Py_DECREF(tmpl);
+          goto fail;
+        }
+        PyTuple_SET_ITEM(asg, k, pair);
+        PyList_SET_ITEM(lab, k, Py_NewRef(PyTuple_GET_ITEM(labels, d)));
+      }
+    }
+    PyObject* idx = PyLong_FromUnsignedLongLong(r.best_index);
+    PyObject* plan = NULL;
+    if (idx) {
+      PyObject* a[3] = {sub, asg, idx};
+      plan = call_n(mkPlan, a, 3);
+    }
+    Py_XDECREF(idx);
+    Py_DECREF(asg);
+    PyObject* routings = plan ? PyTuple_New(T) : NULL;
+    PyObject* exits = routings ? PyList_New(0) : NULL;
+    int bad = !exits;
+    for (int64_t t = 0; t < T; t++) {
+      if (TN[e0 + t] < 0 || TN[e0 + t] >= n) {
+        PyErr_SetString(PyExc_IndexError, "block_results: node out of range");
+        bad = 1;
+        break;
+      }
+      pos_of[TN[e0 + t]] = (int32_t)t;
+    }
+    int64_t k = EO[b];
+    for (int64_t i = 0; i < T && !bad; i++) {
+      const int32_t v = TN[e0 + i];
+      PyObject* scope = PyTuple_GET_ITEM(tmpl, i);
+      const int oc = OP[v];
+      const int pidx = ND[4 * (e0 + i)], sax = ND[4 * (e0 + i) + 1], xax = ND[4 * (e0 + i) + 2];
+      if (oc >= PyTuple_GET_SIZE(pnames) || oc >= PyTuple_GET_SIZE(pallred) || pidx < 0 ||
+          pidx >= PyTuple_GET_SIZE(PyTuple_GET_ITEM(pnames, oc)) || sax >= 8 || xax >= 8) {
+        PyErr_SetString(PyExc_ValueError, "block_results: detail out of range");
+        bad = 1;
+        break;
+      }
+      PyObject* convs = PyList_New(0);
+      if (!convs) {
+        bad = 1;
+        break;
+      }
+      for (int64_t e = INO[v]; e < INO[v + 1] && !bad; e++) {
+        const int32_t p = INI[e];
+        if (p < 0 || p >= n || pos_of[p] < 0) continue;  /* not a member of this template */
+        if (k >= EO[b + 1]) {
+          PyErr_SetString(PyExc_ValueError, "block_results: more internal edges than the detail holds");
+          bad = 1;
+          break;
+        }
+        const int kind = ED[2 * k], axis = ED[2 * k + 1];
+        k++;
+        if (!kind) continue;
+        if (kind < 1 || kind > 4 || (kind > 1 && (axis < 0 || axis >= 8))) {
+          PyErr_SetString(PyExc_ValueError, "block_results: edge detail out of range");
+          bad = 1;
+          break;
+        }
+        PyObject* pb = PyLong_FromLongLong(AB[p]);
+        PyObject* c = pb ? PyTuple_Pack(3, PyList_GET_ITEM(names, p),
+                                        PyTuple_GET_ITEM(PyTuple_GET_ITEM(colls, kind - 1), kind == 1 ? 0 : axis), pb)
+                         : NULL;
+        Py_XDECREF(pb);
+        if (!c || PyList_Append(convs, c) < 0) bad = 1;
+        Py_XDECREF(c);
+      }
+      PyObject* ct = bad ? NULL : PyList_AsTuple(convs);
+      Py_DECREF(convs);
+      PyObject* obytes = ct ? PyLong_FromLongLong(AB[v]) : NULL;
+      PyObject* nr = NULL;
+      if (obytes) {
+        const int ar_ = PyObject_IsTrue(PyTuple_GET_ITEM(PyTuple_GET_ITEM(pallred, oc), pidx));
+        PyObject* a[6] = {scope, PyTuple_GET_ITEM(PyTuple_GET_ITEM(pnames, oc), pidx), ct,
+                          ar_ ? allreduce : identity, obytes, PyTuple_GET_ITEM(specs, sax < 0 ? 0 : 1 + sax)};
+        nr = call_n(mkNR, a, 6);
+      }
+      Py_XDECREF(ct);
+      if (!nr) {
+        Py_XDECREF(obytes);
+        bad = 1;
+        break;
+      }
+      PyTuple_SET_ITEM(routings, i, nr);
+      if (xax >= 0) {
+        PyObject* ex = PyTuple_Pack(3, scope, PyTuple_GET_ITEM(PyTuple_GET_ITEM(colls, 1), xax), obytes);
+        if (!ex || PyList_Append(exits, ex) < 0) bad = 1;
+        Py_XDECREF(ex);
+      }
+      Py_DECREF(obytes);
+    }
+    for (int64_t t = 0; t < T; t++)
+      if (TN[e0 + t] >= 0 && TN[e0 + t] < n) pos_of[TN[e0 + t]] = -1;
+    if (!bad && k != EO[b + 1]) {
+      PyErr_SetString(PyExc_ValueError, "block_results: internal edges differ from the detail");
+      bad = 1;
+    }
+    Py_DECREF(tmpl);
+    PyObject* exits_t = bad ? NULL : PyList_AsTuple(exits);
+    Py_XDECREF(exits);
+    PyObject* bbc = exits_t ? PyDict_New() : NULL;
+    int okd = bbc != NULL;
+    for (int j = 0; j < 4 && okd; j++)
+      if (x.calls[j]) {
+        PyObject* v = PyLong_FromLongLong(x.bytes[j]);
+        okd = v && PyDict_SetItem(bbc, PyTuple_GET_ITEM(kinds, j), v) == 0;
+        Py_XDECREF(v);
+      }
+    PyObject *fwd = PyFloat_FromDouble(x.forward_comm), *bwd = PyFloat_FromDouble(x.backward_comm),
+             *cc = PyLong_FromLongLong(x.collective_calls),
+             *fp = okd ? template_flops(TN + e0, T, OP, AR, AS, aw, WR, WS, ww) : NULL;
+    PyObject* cost = NULL;
+    if (okd && fwd && bwd && cc && fp) {
+      PyObject* a[6] = {fwd, bwd, py_overlap, bbc, cc, fp};
+      cost = call_n(mkCR, a, 6);
+    }
+    Py_XDECREF(fwd);
+    Py_XDECREF(bwd);
+    Py_XDECREF(cc);
+    Py_XDECREF(fp);
+    Py_XDECREF(bbc);
+    PyObject* rp = NULL;
+    if (cost) {
+      PyObject* a[4] = {plan, routings, exits_t, cost};
+      rp = call_n(mkRP, a, 4);
+    }
+    Py_XDECREF(plan);
+    Py_XDECREF(routings);
+    Py_XDECREF(exits_t);
+    Py_XDECREF(cost);
+    PyObject *cand = PyLong_FromUnsignedLongLong(r.candidates), *val = PyLong_FromUnsignedLongLong(r.valid),
+             *table = PyList_New(0);
+    PyObject* res = NULL;
+    if (rp && cand && val && table) {
+      PyObject* a[5] = {sub, rp, cand, val, table};
+      res = call_n(mkRes, a, 5);
+    }
+    Py_XDECREF(rp);
+    Py_XDECREF(cand);
+    Py_XDECREF(val);
+    Py_XDECREF(table);
+    PyObject* term = res ? PyFloat_FromDouble(total * (double)(IO[b + 1] - IO[b])) : NULL;
+    if (!term) {
+      Py_XDECREF(res);
+      Py_DECREF(lab);
+      goto fail;
+    }
+    PyList_SET_ITEM(res_l, b, res);
+    PyList_SET_ITEM(terms, b, term);
+    PyList_SET_ITEM(labs, b, lab);
+  }
+  out = PyTuple_Pack(3, res_l, terms, labs);
+fail:
+  Py_XDECREF(res_l);
+  Py_XDECREF(terms);
+  Py_XDECREF(labs);
+  Py_XDECREF(py_overlap);
+  Py_XDECREF(empty);
+  PyMem_Free(pos_of);
+done:
+  PyBuffer_Release(&op);
+  PyBuffer_Release(&ar);
+  PyBuffer_Release(&as);
+  PyBuffer_Release(&wr);
+  PyBuffer_Release(&ws);
+  PyBuffer_Release(&ab);
+  PyBuffer_Release(&ino);
+  PyBuffer_Release(&ini);
+  PyBuffer_Release(&to_);
+  PyBuffer_Release(&tn_);
+  PyBuffer_Release(&so_);
+  PyBuffer_Release(&sp_);
+  PyBuffer_Release(&rx_);
+  PyBuffer_Release(&io_);
+  PyBuffer_Release(&recs);
+  PyBuffer_Release(&xb);
+  PyBuffer_Release(&node);
+  PyBuffer_Release(&edge);
+  PyBuffer_Release(&eo);
+  return out;
+}
+
 static PyMethodDef methods[] = {
+    {"slot_positions", slot_positions, METH_VARARGS, "Weight slots (weight_nodes order) of every template."},
+    {"block_results", block_results, METH_VARARGS, "SubgraphResults of every block from raw records."},
     {"lower_arrays", lower_arrays, METH_VARARGS, "Lower a grouped ModelGraph to flat sp_graph arrays."},
     {"singleton_results", singleton_results, METH_VARARGS, "SubgraphResults of one-node blocks from raw records."},
     {"assignments_dict", assignments_dict, METH_VARARGS, "Instance-scope -> label dict from member ids."},

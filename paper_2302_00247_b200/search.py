@@ -507,20 +507,112 @@ def _singleton_results(ses: Session, subgraphs: list, scores, detail, prep, csr,
     return out
 
 
+class Slots:
+    """Weight slots of every block of a template CSR: `off` int64 [nb + 1],
+    `pos` int32 [S] (template positions in weight_nodes order: names sorted,
+    search.py:85-88), `radix` uint8 [S] (_options, search.py:91-93)."""
+
+    __slots__ = ("off", "pos", "radix")
+
+    def __init__(self, off, pos, radix):
+        self.off, self.pos, self.radix = off, pos, radix
+
+    @classmethod
+    def of(cls, low: LoweredGraph, csr) -> Optional["Slots"]:
+        if _native_lower is None or not hasattr(_native_lower, "slot_positions") or not isinstance(low.names, list):
+            return None
+        o, p, r = _native_lower.slot_positions(low.names, np.ascontiguousarray(csr[0], np.int64),
+                                               np.ascontiguousarray(csr[1], np.int32),
+                                               np.ascontiguousarray(low.w_rank, np.uint8))
+        return cls(np.frombuffer(o, np.int64), np.frombuffer(p, np.int32), np.frombuffer(r, np.uint8))
+
+    @classmethod
+    def from_prep(cls, prep: list) -> "Slots":
+        off = np.zeros(len(prep) + 1, np.int64)
+        np.cumsum([len(pb[0]) for pb in prep], out=off[1:])
+        pos = np.fromiter((q for pb in prep for q in pb[0]), np.int32, count=int(off[-1]))
+        radix = np.fromiter((r for pb in prep for r in pb[1]), np.uint8, count=int(off[-1]))
+        return cls(off, pos, radix)
+
+    def subset(self, ids) -> "Slots":
+        ids = np.asarray(ids, np.int64)
+        S = self.off[ids + 1] - self.off[ids]
+        off = np.zeros(len(ids) + 1, np.int64)
+        np.cumsum(S, out=off[1:])
+        gather = np.repeat(self.off[ids] - off[:-1], S) + np.arange(off[-1])
+        return Slots(off, self.pos[gather], self.radix[gather])
+
+
+def _native_results(ses: Session, subgraphs: list, scores, detail, csr, slots: Optional[Slots], mult, mesh,
+                    types: TypeSet):
+    """(results, terms, labels) of every block from the raw score / winner-detail
+    records, built in C (csrc/lower_ext.c block_results); None entries where
+    the Python path must build (or raise for) the block; None overall when the
+    native builder does not apply."""
+    blocks, node, edge, eoff = detail
+    raw_s, raw_x = getattr(scores, "raw", None), getattr(blocks, "raw", None)
+    nb = len(subgraphs)
+    if (_native_lower is None or not hasattr(_native_lower, "block_results") or raw_s is None or raw_x is None
+            or slots is None or nb == 0 or not isinstance(ses.low.names, list)):
+        return None
+    low = ses.low
+    c = _RESULT_CONSTS.get(id(types))
+    if c is None or c[0] is not types:
+        specs = (types.ShardSpec(types.ShardKind.REPLICA),) + tuple(
+            types.ShardSpec(types.ShardKind.SPLIT, a) for a in range(8))
+        pn, pc = types.pattern_names, types.pattern_collectives
+        c = _RESULT_CONSTS[id(types)] = (types, (
+            (_ctor(types.CandidatePlan, 3), _ctor(types.NodeRouting, 6), _ctor(types.RoutedPlan, 4),
+             _ctor(types.CostReport, 6), _ctor(types.SubgraphResult, 5)),
+            tuple(tuple(pn.get(lab, ())) for lab in _OP_LABELS),
+            tuple(tuple(x == "allreduce" for x in pc.get(lab, ())) for lab in _OP_LABELS),
+            specs, tuple(sp.label for sp in specs),
+            types.Collective(types.CollectiveKind.IDENTITY), types.Collective(types.CollectiveKind.ALL_REDUCE_SUM),
+            tuple(tuple(_collective(types, k, a) for a in range(8)) for k in (1, 2, 3, 4)),
+            tuple(_KIND_LABEL[k] for k in (1, 2, 3, 4))))
+    ctors, pnames, pallred, specs, labels, identity, allreduce, colls, kinds = c[1]
+    g = getattr(low, "_sp_result_arrays", None)
+    if g is None:
+        g = (np.ascontiguousarray(low.op, np.uint8), np.ascontiguousarray(low.act_rank, np.uint8),
+             np.ascontiguousarray(low.act_shape, np.int64), int(low.act_shape.shape[1]),
+             np.ascontiguousarray(low.w_rank, np.uint8), np.ascontiguousarray(low.w_shape, np.int64),
+             int(low.w_shape.shape[1]), np.ascontiguousarray(low.act_bytes, np.int64),
+             np.ascontiguousarray(low.in_off, np.int64),
+             np.ascontiguousarray(low.in_idx if len(low.in_idx) else np.zeros(1, np.int32), np.int32))
+        try:
+            low._sp_result_arrays = g
+        except AttributeError:
+            pass
+    io = np.zeros(nb + 1, np.int64)
+    np.cumsum(mult, out=io[1:])
+    tn = csr[1] if len(csr[1]) else np.zeros(1, np.int32)
+    bl = (np.ascontiguousarray(csr[0], np.int64), np.ascontiguousarray(tn, np.int32), slots.off,
+          slots.pos if len(slots.pos) else np.zeros(1, np.int32),
+          slots.radix if len(slots.radix) else np.zeros(1, np.uint8), io)
+    return _native_lower.block_results(
+        ctors, subgraphs if isinstance(subgraphs, list) else list(subgraphs), low.names, g, bl, raw_s, raw_x,
+        np.ascontiguousarray(node, np.int8), np.ascontiguousarray(edge, np.int8),
+        np.ascontiguousarray(eoff, np.int64), pnames, pallred, specs, labels, identity, allreduce, colls, kinds,
+        float(mesh.overlap_fraction))
+
+
+_RESULT_CONSTS: dict = {}
+
+
 def _label_keys(ba: BlockArrays, subs: list, prep: list):
     """(member row, slot) of every entry of derive_plan's assignment map, in its
     order: block by block, instance by instance, the block's weight slots in
     weight_nodes order (search.py:374-376).  Slots are numbered over all blocks
     with weights; vectorised over the fold's member matrix."""
-    slot_pos = [pb[0] for pb in prep]
-    wb = [b for b, sp in enumerate(slot_pos) if sp]
-    if not wb:
+    sl = prep if isinstance(prep, Slots) else Slots.from_prep(prep)
+    cnt = np.diff(sl.off)
+    wb = np.nonzero(cnt)[0]
+    if not len(wb):
         return np.zeros(0, np.int32), np.zeros(0, np.int32)
-    S = np.array([len(slot_pos[b]) for b in wb], np.int64)
+    S = cnt[wb]
     soff = np.zeros(len(wb) + 1, np.int64)
     np.cumsum(S, out=soff[1:])
-    q_flat = np.fromiter((q for b in wb for q in slot_pos[b]), np.int64, count=int(soff[-1]))
-    wb = np.asarray(wb, np.int64)
+    q_flat = sl.pos[np.repeat(sl.off[wb] - soff[:-1], S) + np.arange(soff[-1])].astype(np.int64)
     T = np.asarray(ba.block_T, np.int64)[wb]
     mo = np.asarray(ba.block_member_off, np.int64)[wb]
     R = np.diff(np.asarray(ba.block_inst_off, np.int64))[wb]
@@ -616,8 +708,13 @@ class _Search:
             raise
         self._fetched = (scores, detail, time.perf_counter())
 
-    def collect(self, graph, subgraphs: list, want_table: bool, types: TypeSet, prep=None) -> list:
+    def collect(self, graph, subgraphs: list, want_table: bool, types: TypeSet, prep=None,
+                slots: Optional[Slots] = None, mult=None) -> list:
+        """SubgraphResult per block.  Also sets `self.extra` = (terms, labels)
+        per block (cost x multiplicity, weight labels in weight_nodes order) when
+        the native builder produced them (None entries elsewhere), else None."""
         ses, tables = self.ses, self.tables
+        self.extra = None
         try:
             self.fetch()
             scores, detail, tc = self._fetched
@@ -627,28 +724,49 @@ class _Search:
                     raise AssertionError("all-replica fallback must always route")
                 if self.bad_mu:
                     raise BadConfig(f"fusion threshold {self.mu} exceeds chunk size {self.chunk_size}")
-            if prep is None:
-                prep = route_prep(ses, subgraphs, types, self.csr)
             if detail is None:
                 idx = [int(sc.best_index) if sc.has_best else (1 << 64) - 1 for sc in scores]
                 detail = ses.backend.explain_all(tables, idx)
-            # one-node blocks (c5: ~1000 residual ops) straight from the raw
-            # records in C; the rest (and any block the C path declines) here
-            fast = [None] * len(subgraphs) if want_table else \
-                _singleton_results(ses, subgraphs, scores, detail, prep, self.csr, self.mesh, types)
-            rest = [b for b, r in enumerate(fast) if r is None]
-            bests = [None] * len(subgraphs)
-            for b, best in zip(rest, routed_plans_all(ses, tables, subgraphs, scores, self.mesh, types, detail,
-                                                      prep, only=rest)):
-                bests[b] = best
+            nb = len(subgraphs)
+            native = None
+            if not want_table:
+                if slots is None:
+                    slots = Slots.of(ses.low, self.csr)
+                if mult is None:
+                    mult = [len(sub.instances) for sub in subgraphs]
+                native = _native_results(ses, subgraphs, scores, detail, self.csr, slots, mult, self.mesh, types)
+            if native is not None:
+                bests, terms, labs = native
+                rest = [b for b, r in enumerate(bests) if r is None]
+                self.extra = (terms, labs)
+            else:
+                bests = [None] * nb
+                rest = list(range(nb))
+            if rest:
+                if prep is None:
+                    prep = route_prep(ses, subgraphs, types, self.csr)
+                # one-node blocks (c5: ~1000 residual ops) straight from the raw
+                # records in C; the rest (and any block the C path declines) here
+                if native is None and not want_table:
+                    fast = _singleton_results(ses, subgraphs, scores, detail, prep, self.csr, self.mesh, types)
+                    for b, r in enumerate(fast):
+                        bests[b] = r
+                    rest = [b for b, r in enumerate(fast) if r is None]
+                routed = dict(zip(rest, routed_plans_all(ses, tables, subgraphs, scores, self.mesh, types, detail,
+                                                         prep, only=rest)))
+            else:
+                routed = {}
             LAST_PHASES.update(tables_ms=self.tables_ms, score_call_ms=(tc - self.t_launch) * 1e3,
                                routes_ms=(time.perf_counter() - t_routes) * 1e3)
+            if not routed and not want_table:
+                return bests
             results = []
             SubgraphResult = _ctor(types.SubgraphResult, 5)
-            for b, (sub, sc, best) in enumerate(zip(subgraphs, scores, bests)):
-                if fast[b] is not None:
-                    results.append(fast[b])
+            for b, (sub, sc) in enumerate(zip(subgraphs, scores)):
+                if b not in routed:
+                    results.append(bests[b])
                     continue
+                best = routed[b]
                 table = []
                 if want_table:
                     C = int(sc.candidates)
@@ -860,7 +978,9 @@ class _RouteSearch:
         return self.ses.backend.route_search(self.ses.dgraph, off, nodes, ref_slot, radix, eoff, self.mesh,
                                              self.mu, max(self.mu, self.chunk_size), indices)
 
-    def collect(self, graph, subgraphs: list, want_table: bool, types: TypeSet, prep=None) -> list:
+    def collect(self, graph, subgraphs: list, want_table: bool, types: TypeSet, prep=None, slots=None,
+                mult=None) -> list:
+        self.extra = None
         if want_table:
             raise UnsupportedSearch("want_table for blocks beyond the routing-table limits "
                                     f"(> {TABLE_MAX_T} nodes or > {TABLE_MAX_FANIN} internal producers)")
@@ -1022,9 +1142,14 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     t3 = time.perf_counter()
     subs = subgraphs_from_blocks(ses.low, ba, types)
     t3a = time.perf_counter()
-    prep = route_prep(ses, subs, types, csr)
+    slots = Slots.of(ses.low, csr)
+    prep = None
+    if slots is None:
+        prep = route_prep(ses, subs, types, csr)
+        slots = Slots.from_prep(prep)
+    mult = np.diff(np.asarray(ba.block_inst_off, np.int64))
     t3b = time.perf_counter()
-    label_keys = _label_keys(ba, subs, prep)
+    label_keys = _label_keys(ba, subs, slots)
     # the assignment map's keys (scattered name objects) while the device searches
     akeys = None
     if _native_lower is not None and hasattr(_native_lower, "assignments_keys") and isinstance(ses.low.names, list):
@@ -1039,16 +1164,23 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     try:
         for srch, ids in searches:
             if len(searches) == 1:
-                got = srch.collect(graph, subs, want_table, types, prep)
+                got = srch.collect(graph, subs, want_table, types, prep, slots, mult)
             else:
-                got = srch.collect(graph, [subs[i] for i in ids], want_table, types, [prep[i] for i in ids])
-            for i, res in zip(ids, got):
+                got = srch.collect(graph, [subs[i] for i in ids], want_table, types,
+                                   None if prep is None else [prep[i] for i in ids], slots.subset(ids), mult[ids])
+            extra = getattr(srch, "extra", None)
+            for j, (i, res) in enumerate(zip(ids, got)):
                 results[i] = res
                 candidates += res.candidates
                 valid += res.valid
-                terms[i] = res.best.cost.total * subs[i].multiplicity
-                if prep[i][0]:
-                    labs[i] = [spec.label for _, spec in res.best.plan.assignments]
+                if extra is not None and extra[0][j] is not None:
+                    terms[i] = extra[0][j]
+                    if slots.off[i + 1] > slots.off[i]:
+                        labs[i] = extra[1][j]
+                else:
+                    terms[i] = res.best.cost.total * subs[i].multiplicity
+                    if slots.off[i + 1] > slots.off[i]:
+                        labs[i] = [spec.label for _, spec in res.best.plan.assignments]
     finally:
         for srch, _ in searches:  # a group whose collect never ran (an earlier one raised)
             srch.tables.close()

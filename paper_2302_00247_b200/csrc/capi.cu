@@ -76,10 +76,15 @@ static void ctx_destroy_one(sp_ctx* ctx) {
   for (auto& e : ctx->timer)
     if (e) cudaEventDestroy(e);
   if (ctx->aux) {
+    sp::devcache_drop(ctx->aux);
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);
   }
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->stream) {
+    sp::devcache_drop(ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
   delete ctx;
 }
 
@@ -218,9 +223,11 @@ int sp_fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold** out) {
   int rc = guard(ctx, [&] {
     SP_CUDA(cudaSetDevice(ctx->device));
     SP_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+    sp::Trace tr("fold_run");
     sp::fold_run(ctx, dg, min_dup, f);
     SP_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
     SP_CUDA(cudaEventSynchronize(ctx->ev[5]));
+    tr.mark("done");
     float ms = 0;
     SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
     ctx->fold_ms = ms;
@@ -272,12 +279,15 @@ void sp_tables_free(sp_tables* t) {
   if (!t) return;
   for (sp_tables* p : t->peers) sp_tables_free(p);
   t->peers.clear();
+  sp::Trace tr("tables_free");
   if (t->ctx) {
     cudaSetDevice(t->ctx->device);
     cudaStreamSynchronize(t->ctx->stream);
   }
+  tr.mark("sync");
   sp::tables_free_priv(t);
   delete t;
+  tr.mark("free");
 }
 
 int sp_tables_candidates(const sp_tables* t, uint64_t* out) {
@@ -321,8 +331,10 @@ int sp_search(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* bl
 int sp_score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, int32_t explain) {
   if (!ctx || !t) return SP_ERR_CONFIG;
   return guard(ctx, [&] {
+    sp::Trace tr("score_launch");
     SP_CUDA(cudaSetDevice(ctx->device));
     sp::score_launch(ctx, t, shard, n_shards, explain != 0);
+    tr.mark("enqueued");
   });
 }
 
@@ -331,8 +343,10 @@ int sp_score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block
   if (!ctx || !t || !out) return SP_ERR_CONFIG;
   if (blocks && (!node_detail || !edge_detail)) return SP_ERR_CONFIG;
   return guard(ctx, [&] {
+    sp::Trace tr("score_wait");
     SP_CUDA(cudaSetDevice(ctx->device));
     sp::score_wait(ctx, t, out, blocks, node_detail, edge_detail);
+    tr.mark("done");
   });
 }
 

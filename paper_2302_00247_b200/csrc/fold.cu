@@ -176,7 +176,16 @@ __device__ __forceinline__ void entry_one(int64_t i, const int32_t* __restrict__
   uint64_t h = fmix64(rh[(int64_t)n * D + dd] + 0x3c6ef372fe94f82bULL * (uint64_t)(op[n] + 1));
   h = fmix64(h ^ weight_hash(n, w_rank, w_shape, w_train));
   h = fmix64(h + fmix64(prod ^ 0xbb67ae8584caa73bULL));
-  atomicAdd(&gkey[g], (unsigned long long)fmix64(h ^ 0xa54ff53a5f1d36f1ULL));
+  const uint64_t val = fmix64(h ^ 0xa54ff53a5f1d36f1ULL);
+  // lanes of one group (consecutive in sorted order) add their terms in three
+  // 22-bit slices, one 64-bit atomic per group per warp (a shared-memory 64-bit
+  // atomicAdd is a CAS loop: every member of a group retrying it serialised)
+  const unsigned mask = __match_any_sync(__activemask(), g);
+  const uint64_t s0 = __reduce_add_sync(mask, (unsigned)(val & 0x3fffff));
+  const uint64_t s1 = __reduce_add_sync(mask, (unsigned)((val >> 22) & 0x3fffff));
+  const uint64_t s2 = __reduce_add_sync(mask, (unsigned)(val >> 44));
+  if ((int)(threadIdx.x & 31) == __ffs(mask) - 1)
+    atomicAdd(&gkey[g], (unsigned long long)(s0 + (s1 << 22) + (s2 << 44)));
 }
 
 // k_entry in NODE order (multi-kernel path): a node's own arrays and its
@@ -503,8 +512,65 @@ struct SmallArgs {
   unsigned long long* gkey;
   int32_t *sorted, *gstart, *corder, *cstart, *info, *collision;
   uint8_t *gaccept, *residual, *next_flag;
+  // shared-memory staging (k_fold_small<true>): byte offsets into the dynamic
+  // shared memory of the per-node scratch and of the graph arrays the level
+  // loop reads, so its dependent accesses hit shared memory, not L2 / DRAM
+  int32_t o_depth, o_pos, o_gparent, o_gclass, o_act, o_flag, o_cid, o_ph, o_rh, o_cur, o_gkey, o_next;
+  int32_t o_name_off, o_names, o_op, o_w_rank, o_w_train, o_w_shape, o_in_off, o_in_idx;
+  int64_t name_bytes, n_edges;
 };
 
+// cooperative global -> shared copy (16-byte words when both ends allow it)
+__device__ void copy_in(uint8_t* dst, const uint8_t* src, size_t bytes) {
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+    const size_t w = bytes >> 4;
+    for (size_t i = threadIdx.x; i < w; i += blockDim.x) ((uint4*)dst)[i] = ((const uint4*)src)[i];
+    for (size_t i = (w << 4) + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  } else if ((((uintptr_t)src | (uintptr_t)dst) & 3) == 0) {
+    const size_t w = bytes >> 2;
+    for (size_t i = threadIdx.x; i < w; i += blockDim.x) ((uint32_t*)dst)[i] = ((const uint32_t*)src)[i];
+    for (size_t i = (w << 2) + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (size_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+constexpr int RANK_SORT_MAX = 256;  // n^2 compares beat the bitonic network's barriers up to here
+// Ascending (K1, K2, V) order of n <= blockDim.x distinct entries by rank
+// counting: thread i counts the entries below its own (broadcast shared reads,
+// no barrier per step) and writes its entry to that rank.  One pass and two
+// barriers instead of the bitonic network's log^2 stages, each with a barrier.
+__device__ void block_rank_sort(uint64_t* K1, uint64_t* K2, int32_t* V, int n) {
+  const int i = threadIdx.x;
+  uint64_t a = 0, b = 0;
+  int32_t c = 0, r = 0;
+  if (i < n) {
+    a = K1[i];
+    b = K2[i];
+    c = V[i];
+#pragma unroll 4
+    for (int j = 0; j < n; j++) {
+      const uint64_t x = K1[j], y = K2[j];
+      r += (int)((x < a) | ((x == a) & ((y < b) | ((y == b) & (V[j] < c)))));
+    }
+  }
+  __syncthreads();
+  if (i < n) {
+    K1[r] = a;
+    K2[r] = b;
+    V[r] = c;
+  }
+  __syncthreads();
+}
+
+// ascending by (K1, K2, V): rank counting when every entry has a thread, else
+// the bitonic network over P2 (a power of two >= n, padded with ~0 keys)
+__device__ void block_sort(uint64_t* K1, uint64_t* K2, int32_t* V, int n, int P2) {
+  if (n <= RANK_SORT_MAX && n <= (int)blockDim.x) block_rank_sort(K1, K2, V, n);
+  else block_bitonic(K1, K2, V, P2);
+}
+
+template <bool STG>
 __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int32_t s_warp[32];
@@ -514,15 +580,48 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
   uint64_t* K1 = (uint64_t*)sm;
   uint64_t* K2 = K1 + P2max;
   int32_t* V = (int32_t*)(K2 + P2max);
+#define SMALL_PTR(T, f) T const f = STG ? (T)(sm + a.o_##f) : a.f
+  SMALL_PTR(int32_t*, depth);
+  SMALL_PTR(int32_t*, pos);
+  SMALL_PTR(int32_t*, gparent);
+  SMALL_PTR(int32_t*, gclass);
+  SMALL_PTR(int32_t*, act);
+  SMALL_PTR(int32_t*, flag);
+  SMALL_PTR(int32_t*, cid);
+  SMALL_PTR(uint64_t*, ph);
+  SMALL_PTR(uint64_t*, rh);
+  SMALL_PTR(int64_t*, cur);
+  SMALL_PTR(unsigned long long*, gkey);
+  uint8_t* const next_flag = STG ? sm + a.o_next : a.next_flag;
+  SMALL_PTR(const int64_t*, name_off);
+  SMALL_PTR(const uint8_t*, names);
+  SMALL_PTR(const uint8_t*, op);
+  SMALL_PTR(const uint8_t*, w_rank);
+  SMALL_PTR(const uint8_t*, w_train);
+  SMALL_PTR(const int64_t*, w_shape);
+  SMALL_PTR(const int64_t*, in_off);
+  SMALL_PTR(const int32_t*, in_idx);
+#undef SMALL_PTR
+  if (STG) {
+    copy_in((uint8_t*)name_off, (const uint8_t*)a.name_off, (size_t)(n + 1) * 8);
+    copy_in((uint8_t*)names, a.names, (size_t)a.name_bytes);
+    copy_in((uint8_t*)op, a.op, (size_t)n);
+    copy_in((uint8_t*)w_rank, a.w_rank, (size_t)n);
+    copy_in((uint8_t*)w_train, a.w_train, (size_t)n);
+    copy_in((uint8_t*)w_shape, (const uint8_t*)a.w_shape, (size_t)n * SP_MAX_RANK * 8);
+    copy_in((uint8_t*)in_off, (const uint8_t*)a.in_off, (size_t)(n + 1) * 8);
+    copy_in((uint8_t*)in_idx, (const uint8_t*)a.in_idx, (size_t)a.n_edges * 4);
+    __syncthreads();
+  }
   for (int i = tid; i < n; i += NT) {
     int32_t d = 1;
-    for (int64_t k = a.name_off[i]; k < a.name_off[i + 1]; k++) d += a.names[k] == '/';
-    a.depth[i] = d;
-    name_hash_one(i, a.name_off, a.names, a.n, D, a.seed, a.pend, a.ph, a.rh, D, 1);
-    a.gparent[i] = 0;
+    for (int64_t k = name_off[i]; k < name_off[i + 1]; k++) d += names[k] == '/';
+    depth[i] = d;
+    name_hash_one(i, name_off, names, a.n, D, a.seed, a.pend, ph, rh, D, 1);
+    gparent[i] = 0;
     a.residual[i] = 0;
-    a.cur[i] = -1;
-    a.act[i] = i;
+    cur[i] = -1;
+    act[i] = i;
   }
   __syncthreads();
   int nA = n;
@@ -536,11 +635,12 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     uint8_t* ga = a.gaccept + (int64_t)dd * n;
     // 1. sort active nodes by (prefix hash, rel hash)
     const int P2 = pow2ceil(nA);
-    for (int i = tid; i < P2; i += NT) {
+    const int nfill = nA <= NT && nA <= RANK_SORT_MAX ? nA : P2;
+    for (int i = tid; i < nfill; i += NT) {
       if (i < nA) {
-        const int32_t v = a.act[i];
-        K1[i] = a.ph[(int64_t)v * D + dd];
-        K2[i] = a.rh[(int64_t)v * D + dd];
+        const int32_t v = act[i];
+        K1[i] = ph[(int64_t)v * D + dd];
+        K2[i] = rh[(int64_t)v * D + dd];
         V[i] = v;
       } else {
         K1[i] = K2[i] = ~0ULL;
@@ -548,33 +648,33 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
       }
     }
     __syncthreads();
-    block_bitonic(K1, K2, V, P2);
+    block_sort(K1, K2, V, nA, P2);
     for (int i = tid; i < nA; i += NT) {
       srt[i] = V[i];
-      a.flag[i] = (i == 0 || K1[i] != K1[i - 1]) ? 1 : 0;
+      flag[i] = (i == 0 || K1[i] != K1[i - 1]) ? 1 : 0;
     }
     __syncthreads();
-    const int nG = block_inclusive_scan(a.flag, nA, s_warp);
+    const int nG = block_inclusive_scan(flag, nA, s_warp);
     const int64_t stamp = ((int64_t)level) << 32;
     for (int i = tid; i < nA; i += NT) {
-      const int32_t g = a.flag[i] - 1;
-      a.cur[srt[i]] = stamp | (int64_t)g;
-      if (i == 0 || a.flag[i - 1] != a.flag[i]) gs[g] = i;
+      const int32_t g = flag[i] - 1;
+      cur[srt[i]] = stamp | (int64_t)g;
+      if (i == 0 || flag[i - 1] != flag[i]) gs[g] = i;
     }
-    for (int g = tid; g < nG; g += NT) a.gkey[g] = 0;
+    for (int g = tid; g < nG; g += NT) gkey[g] = 0;
     if (tid == 0) gs[nG] = nA;
     __syncthreads();
     // 2. entry hashes / group keys
     for (int i = tid; i < nA; i += NT)
-      entry_one(i, srt, a.flag, nA, gs, a.cur, a.rh, D, dd, a.op, a.w_rank, a.w_shape, a.w_train, a.in_off,
-                a.in_idx, a.pos, a.gkey);
+      entry_one(i, srt, flag, nA, gs, cur, rh, D, dd, op, w_rank, w_shape, w_train, in_off, in_idx, pos, gkey);
     __syncthreads();
     // 3. classes: sort groups by (parent, key)
     const int P2g = pow2ceil(nG);
-    for (int g = tid; g < P2g; g += NT) {
+    const int gfill = nG <= NT && nG <= RANK_SORT_MAX ? nG : P2g;
+    for (int g = tid; g < gfill; g += NT) {
       if (g < nG) {
-        K1[g] = (uint64_t)(uint32_t)a.gparent[srt[gs[g]]];
-        K2[g] = fmix64((uint64_t)a.gkey[g] ^ fmix64((uint64_t)(gs[g + 1] - gs[g]) + 0x1f83d9abfb41bd6bULL));
+        K1[g] = (uint64_t)(uint32_t)gparent[srt[gs[g]]];
+        K2[g] = fmix64((uint64_t)gkey[g] ^ fmix64((uint64_t)(gs[g + 1] - gs[g]) + 0x1f83d9abfb41bd6bULL));
         V[g] = g;
       } else {
         K1[g] = K2[g] = ~0ULL;
@@ -582,33 +682,32 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
       }
     }
     __syncthreads();
-    block_bitonic(K1, K2, V, P2g);
+    block_sort(K1, K2, V, nG, P2g);
     for (int j = tid; j < nG; j += NT) {
       co[j] = V[j];
-      a.cid[j] = (j == 0 || K1[j] != K1[j - 1] || K2[j] != K2[j - 1]) ? 1 : 0;
+      cid[j] = (j == 0 || K1[j] != K1[j - 1] || K2[j] != K2[j - 1]) ? 1 : 0;
     }
     __syncthreads();
-    const int nC = block_inclusive_scan(a.cid, nG, s_warp);
+    const int nC = block_inclusive_scan(cid, nG, s_warp);
     for (int j = tid; j < nG; j += NT) {
-      const int32_t c = a.cid[j] - 1;
-      a.gclass[co[j]] = c;
-      if (j == 0 || a.cid[j - 1] != a.cid[j]) cs[c] = j;
+      const int32_t c = cid[j] - 1;
+      gclass[co[j]] = c;
+      if (j == 0 || cid[j - 1] != cid[j]) cs[c] = j;
     }
     if (tid == 0) cs[nC] = nG;
     __syncthreads();
     // 4. exact verification, 5. accept / residual / descend
     for (int i = tid; i < nA; i += NT)
-      verify_one(i, srt, a.flag, nA, nG, gs, a.gclass, cs, co, a.cur, a.pos, a.pend, a.rh, D, dd, a.name_off,
-                 a.names, a.op, a.w_rank, a.w_shape, a.w_train, a.in_off, a.in_idx, a.collision);
+      verify_one(i, srt, flag, nA, nG, gs, gclass, cs, co, cur, pos, a.pend, rh, D, dd, name_off, names, op, w_rank,
+                 w_shape, w_train, in_off, in_idx, a.collision);
     for (int i = tid; i < nA; i += NT)
-      accept_one(i, srt, a.flag, nA, nC, nG, a.gclass, cs, a.depth, level, a.min_dup, a.gparent, a.next_flag,
-                 a.residual, ga);
+      accept_one(i, srt, flag, nA, nC, nG, gclass, cs, depth, level, a.min_dup, gparent, next_flag, a.residual, ga);
     __syncthreads();
-    for (int i = tid; i < nA; i += NT) a.cid[i] = a.next_flag[i];
+    for (int i = tid; i < nA; i += NT) cid[i] = next_flag[i];
     __syncthreads();
-    const int nNext = block_inclusive_scan(a.cid, nA, s_warp);
+    const int nNext = block_inclusive_scan(cid, nA, s_warp);
     for (int i = tid; i < nA; i += NT)
-      if (a.next_flag[i]) a.act[a.cid[i] - 1] = srt[i];
+      if (next_flag[i]) act[cid[i] - 1] = srt[i];
     if (tid == 0) {
       a.info[dd * 4 + 0] = nA;
       a.info[dd * 4 + 1] = nG;
@@ -1389,6 +1488,7 @@ static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, co
 static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed, sp_fold* out,
                             bool* collided) {
   cudaStream_t s = ctx->stream;
+  Trace tr("fold_small");
   const int64_t n = dg->n;
   const int32_t D = dg->max_depth;
   // one arena for scratch + outputs
@@ -1440,13 +1540,47 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   A.next_flag = u8.p + nd + n;
   SP_CUDA(cudaMemsetAsync(A.collision, 0, sizeof(int32_t), s));
   const int P2 = [&] { int q = 1; while (q < n) q <<= 1; return q; }();
-  const size_t smem = (size_t)P2 * 20;
-  allow_smem(ctx, k_fold_small, smem);
+  // stage the per-node scratch and the graph arrays in shared memory when they fit
+  A.name_bytes = dg->h_name_off[n];
+  A.n_edges = dg->E;
+  size_t smem = 0;
+  auto take = [&](size_t bytes) {
+    const int32_t o = (int32_t)smem;
+    smem += (bytes + 15) & ~(size_t)15;
+    return o;
+  };
+  take((size_t)P2 * 20);
+  const size_t base = smem;
+  A.o_depth = take((size_t)n * 4);
+  A.o_pos = take((size_t)n * 4);
+  A.o_gparent = take((size_t)n * 4);
+  A.o_gclass = take((size_t)n * 4);
+  A.o_act = take((size_t)n * 4);
+  A.o_flag = take((size_t)n * 4);
+  A.o_cid = take((size_t)n * 4);
+  A.o_ph = take((size_t)n * D * 8);
+  A.o_rh = take((size_t)n * D * 8);
+  A.o_cur = take((size_t)n * 8);
+  A.o_gkey = take((size_t)n * 8);
+  A.o_next = take((size_t)n);
+  A.o_name_off = take((size_t)(n + 1) * 8);
+  A.o_names = take((size_t)A.name_bytes);
+  A.o_op = take((size_t)n);
+  A.o_w_rank = take((size_t)n);
+  A.o_w_train = take((size_t)n);
+  A.o_w_shape = take((size_t)n * SP_MAX_RANK * 8);
+  A.o_in_off = take((size_t)(n + 1) * 8);
+  A.o_in_idx = take((size_t)A.n_edges * 4);
+  const bool stage = smem <= std::min<size_t>(ctx->smem_optin, 200 << 10) && !getenv("SP_FOLD_NOSTAGE");
+  if (!stage) smem = base;
+  auto kern = stage ? k_fold_small<true> : k_fold_small<false>;
+  allow_smem(ctx, kern, smem);
   SP_CUDA(cudaEventRecord(ctx->ev[6], s));
-  // one thread per bitonic compare-exchange (P2 / 2): tiny graphs pay their
-  // many block barriers with a few warps, not 32
-  const int threads = std::min(SMALL_THREADS, std::max(64, P2 / 2));
-  SP_LAUNCH(ctx, k_fold_small, 1, threads, smem, s, A);
+  // one thread per node (rank-counting sorts, one node per thread in the
+  // per-node passes), or one per bitonic compare-exchange beyond 1024 nodes
+  const int threads = n <= RANK_SORT_MAX ? std::max(64, (int)((n + 31) / 32 * 32)) : std::min(SMALL_THREADS, P2 / 2);
+  tr.mark("setup");
+  SP_LAUNCH(ctx, kern, 1, threads, smem, s, A);
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaEventRecord(ctx->ev[7], s));
   // outputs (i32 region after scratch), pend, residual + gaccept into one pinned block
@@ -1464,6 +1598,7 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   SP_CUDA(cudaMemcpyAsync(pin + b_out, A.pend, b_pend, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaMemcpyAsync(pin + b_out + b_pend, u8.p, b_u8, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
+  tr.mark("launch+d2h sync");
   const int32_t* h_out_p = (const int32_t*)pin;
   std::vector<int32_t> pend_h((const int32_t*)(pin + b_out), (const int32_t*)(pin + b_out) + nd);
   const uint8_t* h_u8 = pin + b_out + b_pend;
@@ -1496,7 +1631,9 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
     levels.push_back(std::move(lv));
   }
   std::vector<uint8_t> resid_h(h_u8 + nd, h_u8 + nd + n);
+  tr.mark("unpack");
   fold_finalize(dg, levels, resid_h, pend_h, D, out);
+  tr.mark("finalize");
 }
 
 static void fold_once(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t seed, sp_fold* out,

@@ -1820,6 +1820,7 @@ struct SkipPlan {
   unsigned long long tail;        // the last `tail` chunks of a block are claimed in eighths
 };
 constexpr uint32_t SKIP_SUB = 8;
+constexpr int64_t SKIP_KERNEL_MAX_BLOCKS = 128;
 
 __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(const uint8_t* __restrict__ blobs,
                                                                             SkipPlan P, ItemOut* __restrict__ out) {
@@ -2877,6 +2878,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
                   const sp_mesh* mesh, int64_t mu, int64_t chunk, sp_tables* out) {
   cudaStream_t s = ctx->stream;
   const int64_t n = dg->n;
+  Trace tr("tables");
   if (nb < 0) throw Error(SP_ERR_CONFIG, "negative block count");
   if (mu > chunk) throw Error(SP_ERR_CONFIG, "fusion threshold " + std::to_string(mu) + " exceeds chunk size " +
                                                  std::to_string(chunk));
@@ -2948,6 +2950,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     H.C = over ? 0 : (uint64_t)C;
     if (over) out->overflow = true;
   }
+  tr.mark("host slots");
   TablesPriv* priv = new TablesPriv();
   out->priv = priv;
   priv->ctx = ctx;
@@ -2974,6 +2977,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     radix_d.set_view(a + o_radix, ne);
     hdr.set_view((BlobHeader*)(a + o_hdr), nb);
   }
+  tr.mark("upload");
   D.node_block.alloc(n, s);
   D.node_tpos.alloc(n, s);
   SP_CUDA(cudaMemsetAsync(D.node_block.p, 0xff, n * sizeof(int32_t), s));
@@ -2990,6 +2994,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   SP_CUDA(cudaMemsetAsync(D.has_cons.p, 0, n, s));
   SP_CUDA(cudaMemsetAsync(D.ext_cons.p, 0, n, s));
   SP_LAUNCH(ctx, k_boundary, grid_for(n, ctx->sm_count), 256, 0, s, G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
+  tr.mark("mark+boundary");
   DevBuf<EntryLayout> lay;
   DevBuf<int64_t> blob_bytes;
   lay.alloc(ne, s);
@@ -3000,6 +3005,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
               D.node_tpos.p, D.slot_of.p, radix_d.p, lay.p, hdr.p, blob_bytes.p, err.p);
   // errors + the laid-out headers back in one pinned block (the staging block is
   // free again: its H2D is ordered before these copies)
+  tr.mark("layout launch");
   int32_t err_h[2];
   {
     const size_t hb = (size_t)nb * sizeof(BlobHeader);
@@ -3011,6 +3017,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     std::memcpy(err_h, h, sizeof(err_h));
     if (nb) std::memcpy(out->hdr.data(), h + 16, hb);
   }
+  tr.mark("layout sync");
   if (err_h[0] == 1) throw Error(SP_ERR_CONFIG, "a node appears in more than one template");
   if (err_h[0] == 2) throw Error(SP_ERR_CONFIG, "template is not in topological order");
   if (err_h[0] == 3)
@@ -3025,6 +3032,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     out->blob_off[b + 1] = out->blob_off[b] + out->hdr[b].bytes;
     out->edge_off[b + 1] = out->edge_off[b] + out->hdr[b].n_prod;
   }
+  tr.mark("offsets");
   out->blobs.alloc(std::max<int64_t>(out->blob_off[nb], 16), s);
   D.bound.alloc(ne, s);
   {
@@ -3039,6 +3047,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     out->d_blob_off.set_view((int64_t*)(a + o_blob), nb + 1);
     D.xoff.set_view((int64_t*)(a + o_x), nb + 1);
   }
+  tr.mark("alloc+upload2");
   if (nb > 0)
     SP_LAUNCH(ctx, k_fill, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
               D.node_tpos.p, D.slot_of.p, D.ref_slot_of.p, lay.p, hdr.p, out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
@@ -3049,6 +3058,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     if (!tp->built) SP_CUDA(cudaEventCreateWithFlags(&tp->built, cudaEventDisableTiming));
     SP_CUDA(cudaEventRecord(tp->built, s));
   }
+  tr.mark("fill launch");
 }
 
 static size_t score_smem(const sp_tables* t) {
@@ -3069,6 +3079,7 @@ struct FusedExplain {
 // empty shard still produces its all-empty records.
 static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool must_out) {
   cudaStream_t s = ctx->stream;
+  Trace tr("score_items");
   const int64_t nb = t->n_blocks;
   TablesPriv* priv = (TablesPriv*)t->priv;
   PendingScore& pd = priv->pending;
@@ -3108,7 +3119,11 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     throw Error(SP_ERR_UNSUPPORTED, "block tables exceed shared memory (" + std::to_string(smem_k) + " bytes)");
   // prefix skipping on narrow blocks: per-block chunk counters, no work items
   // (SP_SCORE_ITEMS=1 / SP_SKIP_ITEMS=1 select the item kernels: A/B checks)
-  if (ctx->skip && !wide && !generic && !memo && !items_mode && !flow_skip && getenv("SP_SKIP_ITEMS") == nullptr) {
+  // Every CTA of k_score_skip visits every block of the search in order (one
+  // claim + barrier per block), so a search of many cheap blocks (c5's ~1000
+  // residual singletons: 0.85 ms) runs on the item kernel instead (0.10 ms).
+  if (ctx->skip && !wide && !generic && !memo && !items_mode && !flow_skip && nb <= SKIP_KERNEL_MAX_BLOCKS &&
+      getenv("SP_SKIP_ITEMS") == nullptr) {
     allow_smem(ctx, k_score_skip, smem);
     int per = resident_ctas(ctx, k_score_skip, THREADS, smem);
     if (per < 1) per = 1;
@@ -3151,6 +3166,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     SP_CUDA(cudaEventRecord(pd.ev[3], s));
     return true;
   }
+  tr.mark("kernel choice");
   allow_smem(ctx, kern, smem_k);
   int per_sm = resident_ctas(ctx, kern, threads, smem_k);
   if (per_sm < 1) per_sm = 1;
@@ -3164,6 +3180,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   // lexicographic min, so any partition gives the same result.  The sizing
   // depends only on the tables and n_shards: every rank derives the same
   // items.
+  tr.mark("smem+occupancy");
   const unsigned long long N = (unsigned long long)n_shards, r = (unsigned long long)shard;
   unsigned long long total = 0;
   for (int64_t b = 0; b < nb; b++) total += t->hdr[b].C;
@@ -3202,9 +3219,11 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   DevBuf<unsigned long long>& dplan = pd.dplan;
   DevBuf<ItemOut>& items = pd.items;
   DevBuf<sp_score_out>& dout = pd.dout;
+  tr.mark("plan");
   dplan.upload(plan.data(), plan.size(), s);
   items.alloc(n_items, s);
   dout.alloc(nb, s);
+  tr.mark("upload+alloc");
   unsigned long long* counter = dplan.p + 3 * nb + 1;
   ScorePlan P{t->d_blob_off.p, item_cands, item_cands * N, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items,
               ctx->skip};
@@ -3212,6 +3231,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   SP_CUDA(cudaEventRecord(pd.ev[1], s));
   SP_LAUNCH(ctx, kern, (unsigned)grid, threads, smem_k, s, t->blobs.p, P, items.p, counter);
   SP_CUDA(cudaEventRecord(pd.ev[2], s));
+  tr.mark("score launch");
   SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
             dout.p);
   SP_CUDA(cudaGetLastError());
@@ -3223,6 +3243,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
 // results (+ detail) into a pinned host block behind pd.dout.
 static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
   cudaStream_t s = ctx->stream;
+  Trace tr("score_results");
   const int64_t nb = t->n_blocks;
   TablesPriv* priv = (TablesPriv*)t->priv;
   PendingScore& pd = priv->pending;
@@ -3238,8 +3259,10 @@ static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
     dblk.alloc(nb, s);
     dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
     dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
+  tr.mark("explain bufs");
     launch_explain(ctx, t, s, deoff.p, nullptr, dout.p, dblk.p, dnode.p, dedge.p);
   }
+  tr.mark("explain launch");
   SP_CUDA(cudaEventRecord(pd.ev[4], s));
   // results (and winner detail) to the pinned block now: collecting this
   // search later does not wait for whatever is queued behind it
@@ -3249,6 +3272,7 @@ static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
   pd.off_edge = pd.off_node + (explain ? (((size_t)4 * ne + 63) & ~(size_t)63) : 0);
   const size_t need = pd.off_edge + (explain ? (size_t)2 * nedge : 0);
   pd.host = pinned_acquire(ctx, need, &pd.host_bytes);
+  tr.mark("pinned");
   SP_CUDA(cudaMemcpyAsync(pd.host, dout.p, (size_t)nb * sizeof(sp_score_out), cudaMemcpyDeviceToHost, s));
   if (explain) {
     SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_blk, pd.dblk.p, (size_t)nb * sizeof(ExplainBlock),
@@ -3259,6 +3283,7 @@ static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
   }
   g_d2h_bytes += (int64_t)(nb * sizeof(sp_score_out)) +
                  (explain ? (int64_t)(nb * sizeof(ExplainBlock)) + 4 * ne + 2 * nedge : 0);
+  tr.mark("d2h");
   SP_CUDA(cudaEventRecord(pd.ev[5], s));
   pd.active = true;
 }

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -16,6 +19,24 @@
 #include "../../include/shardsearch.h"
 
 namespace sp {
+
+// Host-side phase timer of an entry point (SP_TRACE=1): one stderr line per mark.
+struct Trace {
+  const char* tag;
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit Trace(const char* t) : tag(t), on(getenv("SP_TRACE") != nullptr) {
+    if (on) t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[%s] %-24s %8.1f us (total %8.1f)\n", tag, what,
+            std::chrono::duration<double, std::micro>(now - last).count(),
+            std::chrono::duration<double, std::micro>(now - t0).count());
+    last = now;
+  }
+};
 
 // Error carrying an sp_status code; converted at the C boundary (capi.cu).
 struct Error : std::runtime_error {
@@ -40,31 +61,98 @@ inline std::atomic<int64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
     kernel<<<grid, block, smem, stream>>>(__VA_ARGS__);          \
   } while (0)
 
-// Owning device allocation (cudaMallocAsync on the context stream).
+// Stream-ordered cache of small device blocks (<= 1 MiB, power-of-two size
+// classes): a block released on stream s is handed to the next allocation of
+// its class on s -- work queued on s after the release is ordered after the
+// work that used it, exactly the guarantee cudaFreeAsync + cudaMallocAsync on
+// s give -- without a CUDA API call.  A tiny search allocates and frees ~20
+// scratch buffers per call (~1 us of driver time each); large buffers still
+// go through the stream-ordered pool.  Blocks are returned with
+// devcache_drop(stream) before the stream is destroyed.
+constexpr int DEVCACHE_MIN_LOG = 8, DEVCACHE_MAX_LOG = 20;
+struct DevCache {
+  struct Entry {
+    cudaStream_t s;
+    std::vector<void*> free_[DEVCACHE_MAX_LOG - DEVCACHE_MIN_LOG + 1];
+  };
+  std::mutex m;
+  std::vector<Entry> streams;
+  Entry& of(cudaStream_t s) {
+    for (auto& e : streams)
+      if (e.s == s) return e;
+    streams.push_back(Entry{s, {}});
+    return streams.back();
+  }
+};
+inline DevCache& devcache() {
+  static DevCache* c = new DevCache();  // never destroyed: released per stream
+  return *c;
+}
+inline int devcache_class(size_t bytes) {
+  if (bytes > ((size_t)1 << DEVCACHE_MAX_LOG)) return -1;
+  int c = DEVCACHE_MIN_LOG;
+  while (((size_t)1 << c) < bytes) c++;
+  return c - DEVCACHE_MIN_LOG;
+}
+inline void* devcache_get(cudaStream_t s, int cls) {
+  DevCache& c = devcache();
+  std::lock_guard<std::mutex> lock(c.m);
+  auto& v = c.of(s).free_[cls];
+  if (v.empty()) return nullptr;
+  void* p = v.back();
+  v.pop_back();
+  return p;
+}
+inline void devcache_put(cudaStream_t s, int cls, void* p) {
+  DevCache& c = devcache();
+  std::lock_guard<std::mutex> lock(c.m);
+  c.of(s).free_[cls].push_back(p);
+}
+inline void devcache_drop(cudaStream_t s) {
+  DevCache& c = devcache();
+  std::lock_guard<std::mutex> lock(c.m);
+  for (size_t i = 0; i < c.streams.size(); i++)
+    if (c.streams[i].s == s) {
+      for (auto& v : c.streams[i].free_)
+        for (void* p : v) cudaFreeAsync(p, s);
+      c.streams.erase(c.streams.begin() + (std::ptrdiff_t)i);
+      return;
+    }
+}
+
+// Owning device allocation (cudaMallocAsync on the context stream, small ones
+// through DevCache).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
   bool view = false;  // p points into memory another buffer owns
+  int8_t cls = -1;    // DevCache size class of p, -1: from the pool
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), view(o.view) { o.p = nullptr; o.n = 0; o.view = false; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), view(o.view), cls(o.cls) {
+    o.p = nullptr; o.n = 0; o.view = false; o.cls = -1;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; s = o.s; view = o.view;
-      o.p = nullptr; o.n = 0; o.view = false;
+      p = o.p; n = o.n; s = o.s; view = o.view; cls = o.cls;
+      o.p = nullptr; o.n = 0; o.view = false; o.cls = -1;
     }
     return *this;
   }
   ~DevBuf() { release(); }
   void release() {
-    if (p && !view) cudaFreeAsync(p, s);
+    if (p && !view) {
+      if (cls >= 0) devcache_put(s, cls, p);
+      else cudaFreeAsync(p, s);
+    }
     p = nullptr;
     n = 0;
     view = false;
+    cls = -1;
   }
   // view `count` elements at `at` (owned elsewhere, e.g. a packed upload arena)
   void set_view(T* at, size_t count) {
@@ -78,7 +166,15 @@ struct DevBuf {
     release();
     s = stream;
     n = count;
-    SP_CUDA(cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), stream));
+    const size_t bytes = (count ? count : 1) * sizeof(T);
+    const int c = devcache_class(bytes);
+    if (c >= 0) {
+      p = (T*)devcache_get(stream, c);
+      if (!p) SP_CUDA(cudaMallocAsync(&p, (size_t)1 << (c + DEVCACHE_MIN_LOG), stream));
+      cls = (int8_t)c;
+      return;
+    }
+    SP_CUDA(cudaMallocAsync(&p, bytes, stream));
   }
   void upload(const T* h, size_t count, cudaStream_t stream) {
     alloc(count, stream);

@@ -602,7 +602,8 @@ def run_ours(args) -> None:
         "gpu_launches_detail": {"own_kernels_per_step": main["launches"],
                                 "cub_calls_per_step": main["cub"]},
         "comm": comm,
-        "host_phases_ms": {k: statistics.median(p[k] for p in main["phases"])
+        "host_phases_ms": {k: (statistics.median(p[k] for p in main["phases"])
+                               if isinstance(main["phases"][0][k], (int, float)) else main["phases"][0][k])
                            for k in main["phases"][0]} if main["phases"] and main["phases"][0] else {},
         "breakdown_ms": {"fold": statistics.median(main["fold_ms"]),
                          "score_total": statistics.median(main["score_ms"]),

@@ -288,6 +288,38 @@ int sp_route_search(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t*
                     const int16_t* ref_slot, const uint8_t* radix, const int64_t* edge_off, const sp_mesh* mesh,
                     int64_t mu, int64_t chunk_size, const uint64_t* indices, sp_score_out* out,
                     sp_explain_block* blocks, int8_t* node_detail, int8_t* edge_detail);
+/*
+ * The device half of derive_plan in ONE call (search.py:348-379 up to the
+ * report assembly): the fold (sp_fold_run), every block's template (instance
+ * 0 of the fold's member matrix), the routing tables (sp_tables_build), the
+ * search and the winners' detail (sp_search), with no host round trip in
+ * between beyond the fold's and the table layout's own.  The result holds the
+ * fold arrays, the template CSR and sp_search's outputs; sp_plan_view points
+ * into it until sp_plan_free.  Single-device contexts only (SP_ERR_CONFIG on a
+ * sharded one).  SP_ERR_UNSUPPORTED when a block is beyond the table path (a
+ * template of more than SP_EXPLAIN_MAX_T nodes, more than 6 internal
+ * producers, tables larger than shared memory, more than 2**64 candidates):
+ * the caller then searches that graph block by block (sp_tables_build /
+ * sp_route_search).  Replaces the sequence of calls, not a reference
+ * interface: it exists to keep small searches free of per-call overhead.
+ */
+typedef struct sp_plan sp_plan;
+typedef struct sp_plan_view {
+  sp_blocks blocks;               /* the fold, as sp_fold_view */
+  const int64_t* tmpl_off;        /* [n_blocks + 1] */
+  const int32_t* tmpl_nodes;      /* [n_entries]: row of every template node */
+  const sp_score_out* scores;     /* [n_blocks] */
+  const sp_explain_block* detail; /* [n_blocks] winners (sp_explain_all layout) */
+  const int8_t* node_detail;      /* [4 * n_entries] */
+  const int8_t* edge_detail;      /* [2 * n_edges] */
+  const int64_t* edge_off;        /* [n_blocks + 1] */
+  int64_t n_entries, n_edges;
+} sp_plan_view;
+int sp_plan_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, const sp_mesh* mesh, int64_t mu, int64_t chunk_size,
+                sp_plan** out);
+int sp_plan_view_get(const sp_plan* p, sp_plan_view* view);
+void sp_plan_free(sp_plan* p);
+
 /* Shared memory per CTA (opt-in) and SM count of the context's device. */
 int sp_ctx_limits(const sp_ctx* ctx, int64_t* smem_per_block, int32_t* sm_count);
 /* Per block of built tables: blob bytes, live-value pool slots, template nodes. */

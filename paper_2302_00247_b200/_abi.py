@@ -126,6 +126,21 @@ class SpEdgeConv(C.Structure):
     ]
 
 
+class SpPlanView(C.Structure):
+    _fields_ = [
+        ("blocks", SpBlocks),
+        ("tmpl_off", c_i64p),
+        ("tmpl_nodes", c_i32p),
+        ("scores", C.POINTER(SpScoreOut)),
+        ("detail", C.POINTER(SpExplainBlock)),
+        ("node_detail", C.POINTER(C.c_int8)),
+        ("edge_detail", C.POINTER(C.c_int8)),
+        ("edge_off", c_i64p),
+        ("n_entries", C.c_int64),
+        ("n_edges", C.c_int64),
+    ]
+
+
 def ptr(arr: np.ndarray, ctype):
     assert arr.flags["C_CONTIGUOUS"]
     return arr.ctypes.data_as(C.POINTER(ctype))
@@ -173,22 +188,26 @@ def make_sp_mesh(mesh) -> SpMesh:
     return m
 
 
+def view_array(p, n: int, dt, owner=None) -> np.ndarray:
+    """n elements at ctypes pointer p as numpy: a copy, or (with `owner`, the
+    object that frees the memory) a read-only view that keeps `owner` alive."""
+    if n == 0:
+        return np.zeros(0, dt)
+    if owner is None:
+        return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
+    buf = (p._type_ * n).from_address(C.addressof(p.contents))
+    buf.owner = owner
+    a = np.frombuffer(buf, dt)
+    a.flags.writeable = False
+    return a
+
+
 def blocks_to_numpy(view: SpBlocks, owner=None) -> dict:
     """numpy arrays of an sp_fold view: copies, or (with `owner`, the object
     that frees the fold) read-only views that keep `owner` alive."""
     nb, ni, nm = view.n_blocks, view.n_instances, view.n_members
 
-    def arr(p, n, dt):
-        if n == 0:
-            return np.zeros(0, dt)
-        if owner is None:
-            return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True)
-        buf = (p._type_ * n).from_address(C.addressof(p.contents))
-        buf.owner = owner
-        a = np.frombuffer(buf, dt)
-        a.flags.writeable = False
-        return a
-
+    arr = lambda p, n, dt: view_array(p, n, dt, owner)  # noqa: E731
     return {
         "block_T": arr(view.block_T, nb, np.int64),
         "block_inst_off": arr(view.block_inst_off, nb + 1, np.int64),

@@ -88,14 +88,17 @@ def _declare(L):
                                   C.POINTER(_abi.SpMesh), C.c_int64, C.c_int64, C.POINTER(C.c_uint64),
                                   C.POINTER(SpScoreOut), C.POINTER(SpExplainBlock), C.POINTER(C.c_int8),
                                   C.POINTER(C.c_int8)]
+    L.sp_plan_run.argtypes = [vp, vp, C.c_int32, C.POINTER(_abi.SpMesh), C.c_int64, C.c_int64, C.POINTER(vp)]
+    L.sp_plan_view_get.argtypes = [vp, C.POINTER(_abi.SpPlanView)]
+    L.sp_plan_free.argtypes = [vp]
     L.sp_ctx_limits.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     L.sp_tables_block_info.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
-    for name in ("sp_route_search", "sp_ctx_limits", "sp_tables_block_info", "sp_comm_unique_id",
+    for name in ("sp_plan_run", "sp_plan_view_get", "sp_route_search", "sp_ctx_limits", "sp_tables_block_info", "sp_comm_unique_id",
                  "sp_ctx_comm_init", "sp_ctx_comm_info", "sp_score_launch", "sp_score_wait", "sp_set_option", "sp_search", "sp_tables_sizes", "sp_tables_edge_offsets", "sp_explain_all", "sp_tables_bytes", "sp_copy_bytes", "sp_timer_start", "sp_timer_stop", "sp_launch_counts", "sp_ctx_create", "sp_graph_upload", "sp_fold_run", "sp_fold_view",
                  "sp_tables_build", "sp_tables_candidates", "sp_tables_slots", "sp_score",
                  "sp_score_range", "sp_explain", "sp_last_timings"):
         getattr(L, name).restype = C.c_int
-    for name in ("sp_ctx_destroy", "sp_graph_free", "sp_fold_free", "sp_tables_free"):
+    for name in ("sp_ctx_destroy", "sp_graph_free", "sp_fold_free", "sp_tables_free", "sp_plan_free"):
         getattr(L, name).restype = None
 
 
@@ -125,7 +128,7 @@ EXPORTED_SYMBOLS = (
     "sp_fold_stats", "sp_score_launch", "sp_score_wait", "sp_ingest_json", "sp_ingest_error",
     "sp_ingest_view", "sp_ingest_free", "sp_ingest_onnx", "sp_ingest_report", "sp_ingest_text",
     "sp_comm_unique_id", "sp_ctx_comm_init", "sp_ctx_comm_info", "sp_route_search", "sp_ctx_limits",
-    "sp_tables_block_info",
+    "sp_tables_block_info", "sp_plan_run", "sp_plan_view_get", "sp_plan_free",
 )
 
 
@@ -219,6 +222,11 @@ class Backend:
         return self.comm["nranks"] > 1
 
     @property
+    def single_lane(self) -> bool:
+        """One device and no communicator (sp_plan_run's contexts)."""
+        return self.comm["devices"] == 1 and self.comm["transport"] == "none"
+
+    @property
     def is_root(self) -> bool:
         """Rank 0 of a multi-process communicator (always true otherwise)."""
         return self.comm["devices"] > 1 or self.comm["rank"] == 0
@@ -253,6 +261,30 @@ class Backend:
         # zero-copy: the arrays view the fold's own buffers, which stay alive
         # (owner) as long as any of them does (10^7-node folds: ~60 MB)
         return BlockArrays.from_dict(_abi.blocks_to_numpy(view, owner))
+
+    def plan(self, dgraph: _Handle, min_dup: int, mesh, mu: int, chunk: int):
+        """The device half of derive_plan in one call (sp_plan_run): (fold
+        BlockArrays, template csr, scores, (blocks, node_detail, edge_detail,
+        edge_off)) -- views into one library-owned result."""
+        m = make_sp_mesh(mesh)
+        h = C.c_void_p()
+        self._check(self.lib.sp_plan_run(self.ctx, dgraph.ptr, int(min_dup), C.byref(m), int(mu), int(chunk),
+                                         C.byref(h)), "sp_plan_run")
+        owner = _Handle(self, h, self.lib.sp_plan_free)
+        v = _abi.SpPlanView()
+        self._check(self.lib.sp_plan_view_get(h, C.byref(v)), "sp_plan_view_get")
+        ba = BlockArrays.from_dict(_abi.blocks_to_numpy(v.blocks, owner))
+        nb, ne, nedge = v.blocks.n_blocks, v.n_entries, v.n_edges
+        toff = _abi.view_array(v.tmpl_off, nb + 1, np.int64, owner)
+        tnodes = _abi.view_array(v.tmpl_nodes, ne, np.int32, owner)
+        recs = (SpScoreOut * max(nb, 1)).from_address(C.addressof(v.scores.contents))
+        recs.owner = owner
+        xb = (SpExplainBlock * max(nb, 1)).from_address(C.addressof(v.detail.contents))
+        xb.owner = owner
+        node = _abi.view_array(v.node_detail, 4 * ne, np.int8, owner).reshape(ne, 4)
+        edge = _abi.view_array(v.edge_detail, 2 * nedge, np.int8, owner).reshape(nedge, 2)
+        eoff = _abi.view_array(v.edge_off, nb + 1, np.int64, owner)
+        return ba, (toff, tnodes), RawList(recs, nb), (RawList(xb, nb), node, edge, eoff)
 
     def tables(self, dgraph: _Handle, tmpl_off: np.ndarray, tmpl_nodes: np.ndarray, mesh,
                mu: int, chunk: int) -> Tables:

@@ -290,6 +290,88 @@ void sp_tables_free(sp_tables* t) {
   tr.mark("free");
 }
 
+struct sp_plan {
+  sp_fold* fold = nullptr;
+  std::vector<int64_t> toff, eoff;
+  std::vector<int32_t> tnodes;
+  std::vector<sp_score_out> scores;
+  std::vector<sp_explain_block> detail;
+  std::vector<int8_t> node, edge;
+  ~sp_plan() { delete fold; }
+};
+
+int sp_plan_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, const sp_mesh* mesh, int64_t mu, int64_t chunk_size,
+                sp_plan** out) {
+  if (!ctx || !dg || !mesh || !out) return SP_ERR_CONFIG;
+  *out = nullptr;
+  if (!ctx->peers.empty() || ctx->comm) {
+    ctx->last_error = "sp_plan_run: single-device contexts only";
+    return SP_ERR_CONFIG;
+  }
+  sp_plan* P = new sp_plan();
+  sp_tables* t = nullptr;
+  int rc = guard(ctx, [&] {
+    sp::Trace tr("plan");
+    SP_CUDA(cudaSetDevice(ctx->device));
+    if (mesh->m < 1 || mesh->n < 1) throw sp::Error(SP_ERR_CONFIG, "mesh must be at least 1x1");
+    P->fold = new sp_fold();
+    SP_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+    sp::fold_run(ctx, dg, min_dup, P->fold);
+    SP_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+    tr.mark("fold");
+    const sp_blocks& B = P->fold->view;
+    const int64_t nb = B.n_blocks;
+    P->toff.assign(nb + 1, 0);
+    for (int64_t b = 0; b < nb; b++) {
+      if (B.block_T[b] > SP_EXPLAIN_MAX_T) throw sp::Error(SP_ERR_UNSUPPORTED, "template with more than 256 nodes");
+      P->toff[b + 1] = P->toff[b] + B.block_T[b];
+    }
+    P->tnodes.resize(P->toff[nb]);
+    for (int64_t b = 0; b < nb; b++)
+      std::memcpy(P->tnodes.data() + P->toff[b], B.members + B.block_member_off[b], sizeof(int32_t) * B.block_T[b]);
+    t = new sp_tables();
+    sp::tables_build(ctx, dg, nb, P->toff.data(), P->tnodes.empty() ? nullptr : P->tnodes.data(), mesh, mu,
+                     chunk_size, t);
+    tr.mark("tables");
+    sp::score_launch(ctx, t, 0, 1, true);
+    tr.mark("launch");
+    P->scores.resize(std::max<int64_t>(nb, 1));
+    P->detail.resize(std::max<int64_t>(nb, 1));
+    P->node.resize(std::max<int64_t>(4 * P->toff[nb], 1));
+    P->eoff = t->edge_off;
+    P->edge.resize(std::max<int64_t>(2 * P->eoff[nb], 1));
+    sp::score_wait(ctx, t, P->scores.data(), P->detail.data(), P->node.data(), P->edge.data());
+    float ms = 0;
+    SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
+    ctx->fold_ms = ms;
+    tr.mark("search");
+  });
+  if (t) sp_tables_free(t);
+  if (rc != SP_OK) {
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return SP_OK;
+}
+
+int sp_plan_view_get(const sp_plan* p, sp_plan_view* v) {
+  if (!p || !v || !p->fold) return SP_ERR_CONFIG;
+  v->blocks = p->fold->view;
+  v->tmpl_off = p->toff.data();
+  v->tmpl_nodes = p->tnodes.data();
+  v->scores = p->scores.data();
+  v->detail = p->detail.data();
+  v->node_detail = p->node.data();
+  v->edge_detail = p->edge.data();
+  v->edge_off = p->eoff.data();
+  v->n_entries = p->toff.empty() ? 0 : p->toff.back();
+  v->n_edges = p->eoff.empty() ? 0 : p->eoff.back();
+  return SP_OK;
+}
+
+void sp_plan_free(sp_plan* p) { delete p; }
+
 int sp_tables_candidates(const sp_tables* t, uint64_t* out) {
   if (!t || !out) return SP_ERR_CONFIG;
   for (int64_t b = 0; b < t->n_blocks; b++) out[b] = t->hdr[b].C;

@@ -1495,13 +1495,14 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   const size_t nd = (size_t)n * D, nd1 = (size_t)(n + 1) * D;
   DevBuf<int32_t> i32;
   DevBuf<uint64_t> u64;
-  DevBuf<uint8_t> u8;
-  // i32: depth pend pos gparent gclass act flag cid | sorted gstart corder cstart info collision
-  const size_t i32_scratch = 7 * (size_t)n + nd;
-  const size_t i32_out = nd + nd1 + nd + nd1 + (size_t)(4 * D + 4) + 1;
-  i32.alloc(i32_scratch + i32_out, s);
+  // i32: depth pos gparent gclass act flag cid | sorted gstart corder cstart info collision pend |
+  // then (bytes) gaccept residual next_flag: everything the host reads is one
+  // contiguous range (one D2H)
+  const size_t i32_scratch = 7 * (size_t)n;
+  const size_t i32_out = nd + nd1 + nd + nd1 + (size_t)(4 * D + 4) + 1 + nd;
+  const size_t u8_words = (nd + 2 * (size_t)n + 3) / 4;
+  i32.alloc(i32_scratch + i32_out + u8_words, s);
   u64.alloc(2 * nd + 2 * (size_t)n, s);  // ph rh cur gkey
-  u8.alloc(nd + 2 * (size_t)n, s);       // gaccept residual next_flag
   SmallArgs A;
   A.name_off = dg->name_off.p;
   A.names = dg->names.p;
@@ -1523,7 +1524,6 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   A.act = p; p += n;
   A.flag = p; p += n;
   A.cid = p; p += n;
-  A.pend = p; p += nd;
   int32_t* out0 = p;
   A.sorted = p; p += nd;
   A.gstart = p; p += nd1;
@@ -1531,13 +1531,15 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   A.cstart = p; p += nd1;
   A.info = p; p += 4 * D + 4;
   A.collision = p; p += 1;
+  A.pend = p; p += nd;
+  uint8_t* u8p = (uint8_t*)p;
   A.ph = u64.p;
   A.rh = u64.p + nd;
   A.cur = (int64_t*)(u64.p + 2 * nd);
   A.gkey = (unsigned long long*)(u64.p + 2 * nd + n);
-  A.gaccept = u8.p;
-  A.residual = u8.p + nd;
-  A.next_flag = u8.p + nd + n;
+  A.gaccept = u8p;
+  A.residual = u8p + nd;
+  A.next_flag = u8p + nd + n;
   SP_CUDA(cudaMemsetAsync(A.collision, 0, sizeof(int32_t), s));
   const int P2 = [&] { int q = 1; while (q < n) q <<= 1; return q; }();
   // stage the per-node scratch and the graph arrays in shared memory when they fit
@@ -1583,8 +1585,8 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   SP_LAUNCH(ctx, kern, 1, threads, smem, s, A);
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaEventRecord(ctx->ev[7], s));
-  // outputs (i32 region after scratch), pend, residual + gaccept into one pinned block
-  const size_t b_out = i32_out * 4, b_pend = nd * 4, b_u8 = nd + n;
+  // outputs, pend, gaccept + residual: one contiguous range, one pinned block, one copy
+  const size_t b_out = (i32_out - nd) * 4, b_pend = nd * 4, b_u8 = nd + n;
   size_t pin_bytes = 0;
   uint8_t* pin = pinned_acquire(ctx, b_out + b_pend + b_u8, &pin_bytes);
   struct Release {
@@ -1594,9 +1596,7 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
     ~Release() { pinned_release(ctx, p, n); }
   } rel{ctx, pin, pin_bytes};
   g_d2h_bytes += (int64_t)(b_out + b_pend + b_u8);
-  SP_CUDA(cudaMemcpyAsync(pin, out0, b_out, cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaMemcpyAsync(pin + b_out, A.pend, b_pend, cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaMemcpyAsync(pin + b_out + b_pend, u8.p, b_u8, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaMemcpyAsync(pin, out0, b_out + b_pend + b_u8, cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   tr.mark("launch+d2h sync");
   const int32_t* h_out_p = (const int32_t*)pin;

@@ -2407,7 +2407,68 @@ done:
   return out;
 }
 
+/*
+ * label_rows(members, block_T, inst_off, member_off, slot_off, slot_pos) -> (rows, slots) as bytes
+ * The (member row, slot) of every entry of derive_plan's assignment map, in
+ * its order (search.py:374-376): block by block, instance by instance, the
+ * block's weight slots in weight_nodes order; slots numbered over all
+ * blocks.  int32 outputs.
+ */
+static PyObject* label_rows(PyObject* self, PyObject* args) {
+  Py_buffer mem, bt, io, mo, so, sp;
+  if (!PyArg_ParseTuple(args, "y*y*y*y*y*y*", &mem, &bt, &io, &mo, &so, &sp)) return NULL;
+  PyObject *rows = NULL, *slots = NULL, *out = NULL;
+  const int32_t* M = (const int32_t*)mem.buf;
+  const int64_t* T = (const int64_t*)bt.buf;
+  const int64_t* IO = (const int64_t*)io.buf;
+  const int64_t* MO = (const int64_t*)mo.buf;
+  const int64_t* SO = (const int64_t*)so.buf;
+  const int32_t* SP = (const int32_t*)sp.buf;
+  const Py_ssize_t nb = bt.len / 8, nm = mem.len / 4, ns = sp.len / 4;
+  if (io.len < (nb + 1) * 8 || mo.len < (nb + 1) * 8 || so.len < (nb + 1) * 8 || SO[nb] > ns) {
+    PyErr_SetString(PyExc_ValueError, "label_rows: inconsistent arguments");
+    goto done;
+  }
+  Py_ssize_t K = 0;
+  for (Py_ssize_t b = 0; b < nb; b++) K += (IO[b + 1] - IO[b]) * (SO[b + 1] - SO[b]);
+  rows = PyBytes_FromStringAndSize(NULL, K * 4);
+  slots = PyBytes_FromStringAndSize(NULL, K * 4);
+  if (!rows || !slots) goto done;
+  int32_t* R = (int32_t*)PyBytes_AS_STRING(rows);
+  int32_t* S = (int32_t*)PyBytes_AS_STRING(slots);
+  Py_ssize_t k = 0;
+  for (Py_ssize_t b = 0; b < nb; b++) {
+    const int64_t s0 = SO[b], s1 = SO[b + 1];
+    if (s1 == s0) continue;
+    for (int64_t i = 0; i < IO[b + 1] - IO[b]; i++) {
+      const int64_t base = MO[b] + i * T[b];
+      for (int64_t q = s0; q < s1; q++) {
+        const int64_t at = base + SP[q];
+        if (SP[q] < 0 || SP[q] >= T[b] || at < 0 || at >= nm) {
+          PyErr_SetString(PyExc_IndexError, "label_rows: slot out of range");
+          goto done;
+        }
+        R[k] = M[at];
+        S[k] = (int32_t)q;
+        k++;
+      }
+    }
+  }
+  out = PyTuple_Pack(2, rows, slots);
+done:
+  Py_XDECREF(rows);
+  Py_XDECREF(slots);
+  PyBuffer_Release(&mem);
+  PyBuffer_Release(&bt);
+  PyBuffer_Release(&io);
+  PyBuffer_Release(&mo);
+  PyBuffer_Release(&so);
+  PyBuffer_Release(&sp);
+  return out;
+}
+
 static PyMethodDef methods[] = {
+    {"label_rows", label_rows, METH_VARARGS, "(member row, slot) of every assignment-map entry."},
     {"slot_positions", slot_positions, METH_VARARGS, "Weight slots (weight_nodes order) of every template."},
     {"block_results", block_results, METH_VARARGS, "SubgraphResults of every block from raw records."},
     {"lower_arrays", lower_arrays, METH_VARARGS, "Lower a grouped ModelGraph to flat sp_graph arrays."},

@@ -2750,6 +2750,7 @@ struct TableDev {
   DevBuf<uint8_t> has_cons, ext_cons, bound;
   DevBuf<uint8_t> xinfo;  // per block: XNode[T] then XEdge[n_prod] (k_explain_fast)
   DevBuf<int64_t> xoff;   // [nb + 1] byte offsets into xinfo
+  DevBuf<int64_t> edge_off;  // [nb + 1] internal-edge offsets (the explain output layout)
 };
 
 }  // namespace
@@ -2769,7 +2770,10 @@ struct PendingScore {
   bool lane = false;          // a peer lane of a multi-device search: collected by the primary
   DevBuf<ExplainBlock> dblk;
   DevBuf<int8_t> dnode, dedge;
-  DevBuf<int64_t> deoff;
+  // single-lane searches: dout | dblk | dnode | dedge as views into one arena
+  // laid out like the pinned host block (one D2H copy of the whole result)
+  DevBuf<uint8_t> res;
+  bool res_packed = false;
   sp_ctx* ctx = nullptr;
   uint8_t* host = nullptr;  // pinned: out | blocks | node | edge
   size_t host_bytes = 0, off_blk = 0, off_node = 0, off_edge = 0;
@@ -2815,8 +2819,9 @@ struct TablesPriv {
   // recorded behind k_fill: work on the auxiliary stream (explain_all) waits
   // for the tables, not for whatever was queued on the main stream since
   cudaEvent_t built = nullptr;
-  // packed uploads of the build (one H2D per phase) and their pinned staging
-  DevBuf<uint8_t> arena, arena2;
+  // packed uploads of the build (one H2D per phase) and their pinned staging;
+  // the node maps / boundary flags
+  DevBuf<uint8_t> arena, arena2, maps;
   sp_ctx* ctx = nullptr;
   uint8_t* pin = nullptr;
   size_t pin_bytes = 0;
@@ -2978,21 +2983,20 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     hdr.set_view((BlobHeader*)(a + o_hdr), nb);
   }
   tr.mark("upload");
-  D.node_block.alloc(n, s);
-  D.node_tpos.alloc(n, s);
-  SP_CUDA(cudaMemsetAsync(D.node_block.p, 0xff, n * sizeof(int32_t), s));
-  SP_CUDA(cudaMemsetAsync(D.node_tpos.p, 0xff, n * sizeof(int32_t), s));
-  DevBuf<int32_t> err;
-  err.alloc(2, s);
-  SP_CUDA(cudaMemsetAsync(err.p, 0, 2 * sizeof(int32_t), s));
+  // node maps (-1) and boundary flags + error words (0) in one arena: two memsets
+  const size_t nm_bytes = ((size_t)n * 8 + 15) & ~(size_t)15;
+  priv->maps.alloc(nm_bytes + (((size_t)2 * n + 15) & ~(size_t)15) + 16, s);
+  D.node_block.set_view((int32_t*)priv->maps.p, n);
+  D.node_tpos.set_view((int32_t*)priv->maps.p + n, n);
+  D.has_cons.set_view(priv->maps.p + nm_bytes, n);
+  D.ext_cons.set_view(priv->maps.p + nm_bytes + n, n);
+  int32_t* err = (int32_t*)(priv->maps.p + nm_bytes + (((size_t)2 * n + 15) & ~(size_t)15));
+  SP_CUDA(cudaMemsetAsync(priv->maps.p, 0xff, (size_t)n * 8, s));
+  SP_CUDA(cudaMemsetAsync(priv->maps.p + nm_bytes, 0, priv->maps.n - nm_bytes, s));
   if (nb > 0)
     SP_LAUNCH(ctx, k_mark_blocks, (int)std::min<int64_t>(nb, 65535), 128, 0, s, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
-                                                                  D.node_block.p, D.node_tpos.p, err.p);
+                                                                  D.node_block.p, D.node_tpos.p, err);
   const GraphView G = view_of(dg);
-  D.has_cons.alloc(n, s);
-  D.ext_cons.alloc(n, s);
-  SP_CUDA(cudaMemsetAsync(D.has_cons.p, 0, n, s));
-  SP_CUDA(cudaMemsetAsync(D.ext_cons.p, 0, n, s));
   SP_LAUNCH(ctx, k_boundary, grid_for(n, ctx->sm_count), 256, 0, s, G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
   tr.mark("mark+boundary");
   DevBuf<EntryLayout> lay;
@@ -3002,7 +3006,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   const int gb = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), 65535);
   if (nb > 0)
     SP_LAUNCH(ctx, k_layout, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
-              D.node_tpos.p, D.slot_of.p, radix_d.p, lay.p, hdr.p, blob_bytes.p, err.p);
+              D.node_tpos.p, D.slot_of.p, radix_d.p, lay.p, hdr.p, blob_bytes.p, err);
   // errors + the laid-out headers back in one pinned block (the staging block is
   // free again: its H2D is ordered before these copies)
   tr.mark("layout launch");
@@ -3010,7 +3014,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   {
     const size_t hb = (size_t)nb * sizeof(BlobHeader);
     uint8_t* h = priv->pinned(hb + 16);
-    SP_CUDA(cudaMemcpyAsync(h, err.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaMemcpyAsync(h, err, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     if (nb) SP_CUDA(cudaMemcpyAsync(h + 16, hdr.p, hb, cudaMemcpyDeviceToHost, s));
     g_d2h_bytes += (int64_t)(8 + hb);
     SP_CUDA(cudaStreamSynchronize(s));
@@ -3043,9 +3047,11 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     PackedUpload pk;
     const size_t o_blob = pk.add(out->blob_off.data(), (nb + 1) * sizeof(int64_t));
     const size_t o_x = pk.add(xo.data(), (nb + 1) * sizeof(int64_t));
+    const size_t o_e = pk.add(out->edge_off.data(), (nb + 1) * sizeof(int64_t));
     uint8_t* a = priv->upload(pk, priv->arena2, s);
     out->d_blob_off.set_view((int64_t*)(a + o_blob), nb + 1);
     D.xoff.set_view((int64_t*)(a + o_x), nb + 1);
+    D.edge_off.set_view((int64_t*)(a + o_e), nb + 1);
   }
   tr.mark("alloc+upload2");
   if (nb > 0)
@@ -3070,6 +3076,40 @@ struct FusedExplain {
   int8_t* node;
   int8_t* edge;
 };
+
+// Byte layout of a search's results in the pinned host block (and, for a
+// packed single-lane search, in its device arena): out | blocks | node | edge.
+struct ResultLayout {
+  size_t off_blk, off_node, off_edge, need;
+};
+static ResultLayout result_layout(const sp_tables* t, bool explain) {
+  const int64_t nb = t->n_blocks;
+  const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
+  ResultLayout L;
+  L.off_blk = ((size_t)nb * sizeof(sp_score_out) + 63) & ~(size_t)63;
+  L.off_node = L.off_blk + (explain ? (((size_t)nb * sizeof(ExplainBlock) + 63) & ~(size_t)63) : 0);
+  L.off_edge = L.off_node + (explain ? (((size_t)4 * ne + 63) & ~(size_t)63) : 0);
+  L.need = L.off_edge + (explain ? (size_t)2 * nedge : 0);
+  return L;
+}
+
+// The per-block result records of a search (pd.dout); a single-lane search
+// with winner detail gets them packed with the detail outputs in one arena.
+static void alloc_dout(PendingScore& pd, const sp_tables* t, cudaStream_t s, bool lane) {
+  const int64_t nb = t->n_blocks;
+  pd.res_packed = pd.explain && !lane;
+  if (!pd.res_packed) {
+    pd.dout.alloc(nb, s);
+    return;
+  }
+  const ResultLayout L = result_layout(t, true);
+  pd.res.alloc(std::max<size_t>(L.need, 16), s);
+  const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
+  pd.dout.set_view((sp_score_out*)pd.res.p, nb);
+  pd.dblk.set_view((ExplainBlock*)(pd.res.p + L.off_blk), nb);
+  pd.dnode.set_view((int8_t*)(pd.res.p + L.off_node), 4 * ne);
+  pd.dedge.set_view((int8_t*)(pd.res.p + L.off_edge), 2 * nedge);
+}
 
 // Enqueue scoring (+ k_reduce, + winner detail when `explain`) of
 // [lo[b], hi[b]) for every block; the buffers stay in the tables' pending
@@ -3139,7 +3179,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     }
     if (any == 0) {
       if (!must_out) return false;
-      pd.dout.alloc(nb, s);
+      alloc_dout(pd, t, s, must_out);
       SP_CUDA(cudaMemsetAsync(pd.dout.p, 0, (size_t)nb * sizeof(sp_score_out), s));
       SP_CUDA(cudaEventRecord(pd.ev[1], s));
       SP_CUDA(cudaEventRecord(pd.ev[2], s));
@@ -3149,7 +3189,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     pd.dplan.upload(plan.data(), plan.size(), s);  // nch | ctr | contrib
     SP_CUDA(cudaMemsetAsync(pd.dplan.p + nb, 0, (size_t)2 * nb * sizeof(unsigned long long), s));
     pd.items.alloc((size_t)nb * grid, s);
-    pd.dout.alloc(nb, s);
+    alloc_dout(pd, t, s, must_out);
     // SP_SKIP_TAIL=k: claim the last k chunks of a block in eighths (a shorter
     // final wave before the block's end barrier); measured no gain on c5
     // (7.38 ms at 0, 7.41-7.52 ms at 296-2000), so off by default
@@ -3204,7 +3244,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   const unsigned long long n_items = base[nb];
   if (n_items == 0) {
     if (!must_out) return false;
-    pd.dout.alloc(nb, s);
+    alloc_dout(pd, t, s, must_out);
     SP_CUDA(cudaMemsetAsync(pd.dout.p, 0, (size_t)nb * sizeof(sp_score_out), s));  // valid 0, has_best 0
     SP_CUDA(cudaEventRecord(pd.ev[1], s));
     SP_CUDA(cudaEventRecord(pd.ev[2], s));
@@ -3222,7 +3262,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   tr.mark("plan");
   dplan.upload(plan.data(), plan.size(), s);
   items.alloc(n_items, s);
-  dout.alloc(nb, s);
+  alloc_dout(pd, t, s, must_out);
   tr.mark("upload+alloc");
   unsigned long long* counter = dplan.p + 3 * nb + 1;
   ScorePlan P{t->d_blob_off.p, item_cands, item_cands * N, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items,
@@ -3243,47 +3283,44 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
 // results (+ detail) into a pinned host block behind pd.dout.
 static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
   cudaStream_t s = ctx->stream;
-  Trace tr("score_results");
   const int64_t nb = t->n_blocks;
   TablesPriv* priv = (TablesPriv*)t->priv;
   PendingScore& pd = priv->pending;
+  const bool packed = pd.res_packed && explain;
   pd.explain = explain;
   DevBuf<sp_score_out>& dout = pd.dout;
+  const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
   if (explain) {
     // winner detail straight from the device-side argmin: no host round trip
-    DevBuf<ExplainBlock>& dblk = pd.dblk;
-    DevBuf<int8_t>&dnode = pd.dnode, &dedge = pd.dedge;
-    DevBuf<int64_t>& deoff = pd.deoff;
-    const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
-    deoff.upload(t->edge_off.data(), nb + 1, s);
-    dblk.alloc(nb, s);
-    dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
-    dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
-  tr.mark("explain bufs");
-    launch_explain(ctx, t, s, deoff.p, nullptr, dout.p, dblk.p, dnode.p, dedge.p);
+    if (!packed) {
+      pd.dblk.alloc(nb, s);
+      pd.dnode.alloc(4 * std::max<int64_t>(ne, 1), s);
+      pd.dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
+    }
+    launch_explain(ctx, t, s, priv->dev.edge_off.p, nullptr, dout.p, pd.dblk.p, pd.dnode.p, pd.dedge.p);
   }
-  tr.mark("explain launch");
   SP_CUDA(cudaEventRecord(pd.ev[4], s));
   // results (and winner detail) to the pinned block now: collecting this
   // search later does not wait for whatever is queued behind it
-  const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
-  pd.off_blk = ((size_t)nb * sizeof(sp_score_out) + 63) & ~(size_t)63;
-  pd.off_node = pd.off_blk + (explain ? (((size_t)nb * sizeof(ExplainBlock) + 63) & ~(size_t)63) : 0);
-  pd.off_edge = pd.off_node + (explain ? (((size_t)4 * ne + 63) & ~(size_t)63) : 0);
-  const size_t need = pd.off_edge + (explain ? (size_t)2 * nedge : 0);
-  pd.host = pinned_acquire(ctx, need, &pd.host_bytes);
-  tr.mark("pinned");
-  SP_CUDA(cudaMemcpyAsync(pd.host, dout.p, (size_t)nb * sizeof(sp_score_out), cudaMemcpyDeviceToHost, s));
-  if (explain) {
-    SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_blk, pd.dblk.p, (size_t)nb * sizeof(ExplainBlock),
-                            cudaMemcpyDeviceToHost, s));
-    if (ne) SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_node, pd.dnode.p, (size_t)4 * ne, cudaMemcpyDeviceToHost, s));
-    if (nedge)
-      SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_edge, pd.dedge.p, (size_t)2 * nedge, cudaMemcpyDeviceToHost, s));
+  const ResultLayout L = result_layout(t, explain);
+  pd.off_blk = L.off_blk;
+  pd.off_node = L.off_node;
+  pd.off_edge = L.off_edge;
+  pd.host = pinned_acquire(ctx, L.need, &pd.host_bytes);
+  if (packed) {
+    SP_CUDA(cudaMemcpyAsync(pd.host, pd.res.p, L.need, cudaMemcpyDeviceToHost, s));
+  } else {
+    SP_CUDA(cudaMemcpyAsync(pd.host, dout.p, (size_t)nb * sizeof(sp_score_out), cudaMemcpyDeviceToHost, s));
+    if (explain) {
+      SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_blk, pd.dblk.p, (size_t)nb * sizeof(ExplainBlock),
+                              cudaMemcpyDeviceToHost, s));
+      if (ne) SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_node, pd.dnode.p, (size_t)4 * ne, cudaMemcpyDeviceToHost, s));
+      if (nedge)
+        SP_CUDA(cudaMemcpyAsync(pd.host + pd.off_edge, pd.dedge.p, (size_t)2 * nedge, cudaMemcpyDeviceToHost, s));
+    }
   }
   g_d2h_bytes += (int64_t)(nb * sizeof(sp_score_out)) +
                  (explain ? (int64_t)(nb * sizeof(ExplainBlock)) + 4 * ne + 2 * nedge : 0);
-  tr.mark("d2h");
   SP_CUDA(cudaEventRecord(pd.ev[5], s));
   pd.active = true;
 }

@@ -605,6 +605,13 @@ def _label_keys(ba: BlockArrays, subs: list, prep: list):
     weight_nodes order (search.py:374-376).  Slots are numbered over all blocks
     with weights; vectorised over the fold's member matrix."""
     sl = prep if isinstance(prep, Slots) else Slots.from_prep(prep)
+    if _native_lower is not None and hasattr(_native_lower, "label_rows"):
+        r, q = _native_lower.label_rows(
+            np.ascontiguousarray(ba.members, np.int32), np.ascontiguousarray(ba.block_T, np.int64),
+            np.ascontiguousarray(ba.block_inst_off, np.int64), np.ascontiguousarray(ba.block_member_off, np.int64),
+            np.ascontiguousarray(sl.off, np.int64),
+            np.ascontiguousarray(sl.pos if len(sl.pos) else np.zeros(1, np.int32), np.int32))
+        return np.frombuffer(r, np.int32), np.frombuffer(q, np.int32)
     cnt = np.diff(sl.off)
     wb = np.nonzero(cnt)[0]
     if not len(wb):
@@ -1081,6 +1088,50 @@ def _plan_searches(ses: Session, csr, mesh, mu, chunk_size, shard, n_shards, exc
             raise
 
 
+#: graphs up to this many GraphNodes (the one-CTA fold) take the one-call path
+SMALL_PLAN_NODES = 8192
+
+
+def _derive_small(ses: Session, mesh, min_duplicates: int, mu: int, chunk_size: int, types: TypeSet, t0: float,
+                  t1: float):
+    """derive_plan for a small graph: the device half in ONE library call
+    (sp_plan_run: fold, templates, tables, search, winner detail), then the
+    report from the raw records in C (block_results).  None when a block is
+    beyond the table path (the caller's general path route-searches it)."""
+    try:
+        ba, csr, scores, detail = ses.backend.plan(ses.dgraph, int(min_duplicates), mesh, mu, chunk_size)
+    except UnsupportedSearch:
+        return None
+    t2 = time.perf_counter()
+    low = ses.low
+    subs = subgraphs_from_blocks(low, ba, types)
+    slots = Slots.of(low, csr)
+    for sc in scores:
+        if not sc.has_best:
+            raise AssertionError("all-replica fallback must always route")
+    nb = len(subs)
+    mult = np.diff(np.asarray(ba.block_inst_off, np.int64))
+    native = _native_results(ses, subs, scores, detail, csr, slots, mult, mesh, types)
+    if native is None or any(r is None for r in native[0]):
+        return None
+    results, terms, labs = native
+    t3 = time.perf_counter()
+    total_cost = 0.0
+    for x in terms:  # block order (search.py:373): the sum is not reassociated
+        total_cost += x
+    candidates = valid = 0
+    for sc in scores:
+        candidates += sc.candidates
+        valid += sc.valid
+    off = slots.off
+    slot_labels = [lab for b, ls in enumerate(labs) if off[b + 1] > off[b] for lab in ls]
+    assignments = _assignments(low.names, _label_keys(ba, subs, slots), slot_labels)
+    LAST_PHASES.clear()
+    LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, plan_ms=(t2 - t1) * 1e3, results_ms=(t3 - t2) * 1e3,
+                       assemble_ms=(time.perf_counter() - t3) * 1e3, path="one-call", blocks=nb)
+    return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates, valid)
+
+
 def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types, backend, session,
                  cache, shard, n_shards, exchange, root_only=True):
     t0 = time.perf_counter()
@@ -1088,6 +1139,12 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     t1 = time.perf_counter()
     if min_duplicates < 1:
         raise BadConfig("min_duplicates must be >= 1")
+    if (ses.low.n_nodes <= SMALL_PLAN_NODES and not want_table and n_shards == 1 and exchange is None
+            and mu <= chunk_size and ses.backend.single_lane and _native_lower is not None
+            and isinstance(ses.low.names, list)):
+        rep = _derive_small(ses, mesh, min_duplicates, mu, chunk_size, types, t0, t1)
+        if rep is not None:
+            return rep
     ba = ses.backend.fold(ses.dgraph, int(min_duplicates))
     t2 = time.perf_counter()
     n_blocks = ba.n_blocks
@@ -1197,7 +1254,8 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
                                                      np.ascontiguousarray(label_keys[1], np.int32), slot_labels)
     else:
         assignments = _assignments(ses.low.names, label_keys, slot_labels)
-    LAST_PHASES.update(session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
+    LAST_PHASES.clear()
+    LAST_PHASES.update(path="general", session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
                        launch_ms=(t3 - t2) * 1e3, overlap_host_ms=(t4 - t3) * 1e3,
                        subgraphs_ms=(t3a - t3) * 1e3, route_prep_ms=(t3b - t3a) * 1e3,
                        collect_ms=(t5 - t4) * 1e3, assemble_ms=(time.perf_counter() - t5) * 1e3)

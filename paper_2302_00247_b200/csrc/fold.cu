@@ -1110,6 +1110,184 @@ __global__ void k_acc_insts(int64_t Ga, const int32_t* __restrict__ order, const
   }
 }
 
+// Single-CTA block assembly of one level (levels with at most LS_CAP accepted
+// groups, e.g. c5's 3,476): the work of level_blocks' ~25 CUB / helper
+// launches and two host round trips in ONE launch -- accepted groups in id
+// order (ballot scan), instance keys, a bitonic sort by (class, first 16
+// component bytes), class heads + tie check, per-class start / R / T, member
+// and template offsets, and the canonical (class, topological rank) order of
+// the template members (when they fit, else counts[3] asks the host for the
+// CUB path).  counts = {K, M, CT, too_big}.
+constexpr int LS_CAP = 4096;
+constexpr int64_t LS_MAX_GROUPS = 1 << 20;  // nG scanned by one CTA
+
+__device__ __forceinline__ bool ls_less(uint32_t ca, uint64_t a0, uint64_t a1, int32_t ia, uint32_t cb, uint64_t b0,
+                                        uint64_t b1, int32_t ib) {
+  if (ca != cb) return ca < cb;
+  if (a0 != b0) return a0 < b0;
+  if (a1 != b1) return a1 < b1;
+  return ia < ib;
+}
+
+__global__ void __launch_bounds__(1024) k_level_small(
+    int64_t nG, int64_t nA, const uint8_t* __restrict__ gaccept, const int32_t* __restrict__ sorted,
+    const int32_t* __restrict__ gstart, const int32_t* __restrict__ gclass, const int32_t* __restrict__ pend,
+    int64_t ps, int64_t pd, int32_t dd, const int64_t* __restrict__ name_off, const uint8_t* __restrict__ names,
+    const int64_t* __restrict__ topo, int32_t* __restrict__ tie, int32_t* __restrict__ accG_o,
+    int32_t* __restrict__ order_o, int32_t* __restrict__ cls_start, int32_t* __restrict__ cls_R,
+    int32_t* __restrict__ cls_T, int64_t* __restrict__ moff, int64_t* __restrict__ coff, int32_t* __restrict__ canon,
+    int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ int32_t s_warp[32];
+  uint64_t* K0 = (uint64_t*)sm;
+  uint64_t* K1 = K0 + LS_CAP;
+  uint32_t* KC = (uint32_t*)(K1 + LS_CAP);
+  int32_t* IX = (int32_t*)(KC + LS_CAP);
+  int32_t* ACC = IX + LS_CAP;
+  int32_t* HD = ACC + LS_CAP;
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, w = tid >> 5, NW = NT >> 5;
+  // 1. accepted groups in group-id order
+  int base = 0;
+  for (int64_t g0 = 0; g0 < nG; g0 += NT) {
+    const int64_t g = g0 + tid;
+    const bool f = g < nG && gaccept[g];
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_warp[w] = __popc(bal);
+    __syncthreads();
+    if (w == 0) {
+      int v = lane < NW ? s_warp[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      s_warp[lane] = v;
+    }
+    __syncthreads();
+    const int pos = base + (w ? s_warp[w - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
+    if (f && pos < LS_CAP) ACC[pos] = (int32_t)g;
+    base += s_warp[NW - 1];
+    __syncthreads();
+  }
+  const int Ga = base;
+  if (Ga > LS_CAP) {  // the host bounds Ga by the level's accepted count: cannot happen
+    if (tid == 0) counts[3] = 1;
+    return;
+  }
+  // 2. instance keys: class, first 16 bytes of the last component (big-endian)
+  const int P2 = pow2ceil(Ga > 0 ? Ga : 1);
+  for (int j = tid; j < P2; j += NT) {
+    if (j < Ga) {
+      const int32_t g = ACC[j];
+      const int32_t h = sorted[gstart[g]];
+      const int64_t pe = pend[(int64_t)h * ps + dd * pd];
+      const int64_t p0 = dd > 0 ? (int64_t)pend[(int64_t)h * ps + (dd - 1) * pd] + 1 : 0;
+      const int64_t len = pe > p0 ? pe - p0 : 0;
+      const uint8_t* c = names + name_off[h] + p0;
+      uint64_t a = 0, b = 0;
+      const int64_t m = len < 16 ? len : 16;
+      for (int64_t q = 0; q < m; q++) {
+        const uint64_t x = c[q];
+        if (q < 8) a |= x << (56 - 8 * q);
+        else b |= x << (120 - 8 * q);
+      }
+      K0[j] = a;
+      K1[j] = b;
+      KC[j] = (uint32_t)gclass[g];
+      IX[j] = j;
+    } else {
+      K0[j] = K1[j] = ~0ULL;
+      KC[j] = 0xffffffffu;
+      IX[j] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  // 3. bitonic sort by (class, k0, k1, j)
+  for (int size = 2; size <= P2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = tid; t < (P2 >> 1); t += NT) {
+        const int i = ((t & ~(stride - 1)) << 1) | (t & (stride - 1));
+        const int j = i + stride;
+        const bool gt = ls_less(KC[j], K0[j], K1[j], IX[j], KC[i], K0[i], K1[i], IX[i]);
+        if (gt == ((i & size) == 0)) {
+          const uint32_t c0 = KC[i];
+          const uint64_t a = K0[i], b = K1[i];
+          const int32_t x = IX[i];
+          KC[i] = KC[j]; K0[i] = K0[j]; K1[i] = K1[j]; IX[i] = IX[j];
+          KC[j] = c0; K0[j] = a; K1[j] = b; IX[j] = x;
+        }
+      }
+      __syncthreads();
+    }
+  // 4. class heads, tie check (two instance components of a class equal on 16 bytes)
+  for (int p = tid; p < Ga; p += NT) {
+    const bool hd = p == 0 || KC[p] != KC[p - 1];
+    HD[p] = hd;
+    if (!hd && K0[p] == K0[p - 1] && K1[p] == K1[p - 1]) atomicExch(tie, 1);
+    accG_o[p] = ACC[p];
+    order_o[p] = IX[p];
+  }
+  __syncthreads();
+  const int K = block_inclusive_scan(HD, Ga, s_warp);
+  // 5. per class: start, R, T
+  for (int p = tid; p < Ga; p += NT) {
+    const int32_t k = HD[p] - 1;
+    if (p == 0 || HD[p - 1] != HD[p]) {
+      cls_start[k] = p;
+      const int32_t g = ACC[IX[p]];
+      cls_T[k] = (int32_t)((g + 1 < nG ? gstart[g + 1] : nA) - gstart[g]);
+    }
+    if (p + 1 == Ga || HD[p + 1] != HD[p]) cls_R[k] = p + 1;
+  }
+  __syncthreads();
+  // member / template offsets (exclusive scans; KC / HD reused)
+  for (int k = tid; k < K; k += NT) {
+    cls_R[k] -= cls_start[k];
+    KC[k] = (uint32_t)(cls_R[k] * cls_T[k]);
+    HD[k] = cls_T[k];
+  }
+  __syncthreads();
+  const int M = block_inclusive_scan((int32_t*)KC, K, s_warp);
+  const int CT = block_inclusive_scan(HD, K, s_warp);
+  for (int k = tid; k < K; k += NT) {
+    moff[k] = (int64_t)KC[k] - (int64_t)cls_R[k] * cls_T[k];
+    coff[k] = (int64_t)HD[k] - cls_T[k];
+  }
+  if (tid == 0) {
+    moff[K] = M;
+    coff[K] = CT;
+    counts[0] = K;
+    counts[1] = M;
+    counts[2] = CT;
+    counts[3] = CT > LS_CAP;
+  }
+  __syncthreads();
+  if (CT > LS_CAP) return;
+  // 6. canonical order of every class's template members: sort (class, topo rank)
+  const int P2c = pow2ceil(CT > 0 ? CT : 1);
+  for (int e = tid; e < P2c; e += NT) {
+    if (e < CT) {
+      int lo = 0, hi = K;  // largest k with coff[k] <= e
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (coff[mid] <= e) lo = mid;
+        else hi = mid;
+      }
+      const int t = e - (int)coff[lo];
+      const int32_t g = ACC[IX[cls_start[lo]]];
+      K0[e] = ((uint64_t)lo << 32) | (uint64_t)(uint32_t)topo[sorted[gstart[g] + t]];
+      K1[e] = 0;
+      HD[e] = t;
+    } else {
+      K0[e] = K1[e] = ~0ULL;
+      HD[e] = 0x7fffffff;
+    }
+  }
+  __syncthreads();
+  block_sort(K0, K1, HD, CT, P2c);
+  for (int e = tid; e < CT; e += NT) canon[e] = HD[e];
+}
+
 // One level's blocks, still on the device (downloaded once after the loop).
 struct LevelBlocks {
   int64_t K = 0, Ga = 0, M = 0;
@@ -1144,9 +1322,51 @@ static T d2h_scalar(const T* p, cudaStream_t s) {
 // pend of (node h, depth d) at h*ps + d*pd (node- or level-major, see name_hash_one).
 static void level_blocks(sp_ctx* ctx, sp_dgraph* dg, int32_t dd, int64_t nA, int64_t nG, const int32_t* sorted,
                          const int32_t* gstart, const int32_t* gclass, const uint8_t* gaccept, const int32_t* pend,
-                         int64_t ps, int64_t pd, int32_t* d_tie, LevelBlocks& L) {
+                         int64_t ps, int64_t pd, int32_t* d_tie, LevelBlocks& L, int64_t nacc = -1) {
   cudaStream_t s = ctx->stream;
   const int sms = ctx->sm_count;
+  if (nacc >= 0 && nacc <= LS_CAP && nG <= LS_MAX_GROUPS && !getenv("SP_FOLD_LEVEL_CUB")) {
+    // one CTA assembles the level; one host round trip for the counts
+    const int64_t Ga = nacc;
+    DevBuf<int32_t> accG, order, canon;
+    DevBuf<int64_t> offs;  // moff [Ga+1] | coff [Ga+1] | counts [4]
+    accG.alloc(std::max<int64_t>(Ga, 1), s);
+    order.alloc(std::max<int64_t>(Ga, 1), s);
+    canon.alloc(LS_CAP, s);
+    offs.alloc(2 * (Ga + 1) + 4, s);
+    L.cls_T.alloc(std::max<int64_t>(Ga, 1), s);
+    L.cls_R.alloc(std::max<int64_t>(Ga, 1), s);
+    L.cls_start.alloc(std::max<int64_t>(Ga, 1), s);
+    int64_t* moff = offs.p;
+    int64_t* coff = offs.p + Ga + 1;
+    int64_t* dcnt = offs.p + 2 * (Ga + 1);
+    const size_t smem = (size_t)LS_CAP * 32;
+    allow_smem(ctx, k_level_small, smem);
+    SP_LAUNCH(ctx, k_level_small, 1, 1024, smem, s, nG, nA, gaccept, sorted, gstart, gclass, pend, ps, pd, dd,
+              dg->name_off.p, dg->names.p, dg->topo.p, d_tie, accG.p, order.p, L.cls_start.p, L.cls_R.p, L.cls_T.p,
+              moff, coff, canon.p, dcnt);
+    int64_t cnt[4];
+    g_d2h_bytes += sizeof(cnt);
+    SP_CUDA(cudaMemcpyAsync(cnt, dcnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    if (!cnt[3]) {
+      const int64_t K = cnt[0], M = cnt[1];
+      L.Ga = Ga;
+      L.K = K;
+      L.M = M;
+      L.members.alloc(std::max<int64_t>(M, 1), s);
+      L.inode.alloc(std::max<int64_t>(Ga, 1), s);
+      L.ilen.alloc(std::max<int64_t>(Ga, 1), s);
+      if (M)
+        SP_LAUNCH(ctx, k_acc_members, grid_for(M, sms), 256, 0, s, M, K, moff, coff, L.cls_start.p, L.cls_T.p,
+                  order.p, accG.p, gstart, sorted, canon.p, L.members.p);
+      if (Ga)
+        SP_LAUNCH(ctx, k_acc_insts, grid_for(Ga, sms), 256, 0, s, Ga, order.p, accG.p, gstart, sorted, pend, ps, pd,
+                  dd, L.inode.p, L.ilen.p);
+      return;
+    }
+    // templates too large for the one-CTA canonical sort: the CUB path below
+  }
   DevBuf<int32_t> iota, accG, nsel;
   iota.alloc(nG, s);
   accG.alloc(nG, s);
@@ -1354,10 +1574,17 @@ static void fold_finalize(sp_dgraph* dg, const std::vector<LevelOut>& levels, co
 // residual singletons, order all blocks by template prefix string
 // (pruning.py:200) and concatenate.  Host work is O(blocks log blocks) string
 // compares plus one pass over the members.
-static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, const std::vector<int32_t>& resid,
-                                 cudaStream_t s, sp_fold* out) {
+// With d_rlist, the residual list (d_nr entries) comes from the device in the
+// same copy, and with d_flags the fold's collision / tie words too (h_flags;
+// when either is set nothing is finalised): one host round trip in all.
+static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, const std::vector<int32_t>& resid_in,
+                                 cudaStream_t s, sp_fold* out, const int32_t* d_rlist = nullptr, int64_t d_nr = 0,
+                                 const int32_t* d_coll = nullptr, const int32_t* d_tie = nullptr,
+                                 int32_t* h_flags = nullptr) {
   const uint8_t* names = dg->h_names.data();
   const int64_t* noff = dg->h_name_off.data();
+  std::vector<int32_t> resid_from_device;
+  const std::vector<int32_t>& resid = d_rlist ? resid_from_device : resid_in;
   // every level's class arrays to ONE pinned block (10^7-node folds move
   // ~50 MB here: pageable copies and zero-filled vectors cost 30+ ms)
   struct Host {
@@ -1366,7 +1593,7 @@ static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, co
     std::vector<int64_t> moff;
   };
   std::vector<Host> h(lv.size());
-  size_t total = 0;
+  size_t total = 16 + (size_t)(d_rlist ? d_nr : 0) * 4;
   for (const LevelBlocks& L : lv) total += (size_t)(3 * L.K + 2 * L.Ga + L.M) * 4;
   size_t got = 0;
   uint8_t* pin = total ? sp::pinned_acquire(dg->ctx, total, &got) : nullptr;
@@ -1385,6 +1612,10 @@ static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, co
       q += cnt;
       return (const int32_t*)at;
     };
+    int32_t* flags_at = q;
+    q += 4;
+    if (d_coll) SP_CUDA(cudaMemcpyAsync(flags_at, d_coll, 4, cudaMemcpyDeviceToHost, s));
+    if (d_tie) SP_CUDA(cudaMemcpyAsync(flags_at + 1, d_tie, 4, cudaMemcpyDeviceToHost, s));
     for (size_t l = 0; l < lv.size(); l++) {
       LevelBlocks& L = lv[l];
       Host& H = h[l];
@@ -1397,8 +1628,19 @@ static void fold_finalize_blocks(sp_dgraph* dg, std::vector<LevelBlocks>& lv, co
       H.ilen = get(L.ilen, L.Ga);
       H.members = get(L.members, L.M);
     }
+    const int32_t* rl = q;
+    if (d_rlist && d_nr) {
+      SP_CUDA(cudaMemcpyAsync(q, d_rlist, (size_t)d_nr * 4, cudaMemcpyDeviceToHost, s));
+      g_d2h_bytes += d_nr * 4;
+    }
+    SP_CUDA(cudaStreamSynchronize(s));
+    if (h_flags) {
+      h_flags[0] = d_coll ? flags_at[0] : 0;
+      h_flags[1] = d_tie ? flags_at[1] : 0;
+      if (h_flags[0] || h_flags[1]) return;
+    }
+    if (d_rlist) resid_from_device.assign(rl, rl + d_nr);
   }
-  SP_CUDA(cudaStreamSynchronize(s));
   struct Ref {
     int64_t pnode, plen;
     int32_t level;  // -1: residual singleton
@@ -2051,7 +2293,7 @@ __device__ __forceinline__ void block_add(int32_t x, int32_t* __restrict__ dst) 
 constexpr int64_t RANK_MAX = 1024;
 
 struct HashStats {  // device counters of one level
-  int32_t nG, overflow, nC, nnext, nacc, big, est, pad0;
+  int32_t nG, overflow, nC, nnext, nacc, big, est, nres;
 };
 
 // level-1 keys of every node + the group-count bound
@@ -2334,7 +2576,7 @@ __global__ void __launch_bounds__(128) k_hg_finish(
     uint64_t seed, const uint64_t* __restrict__ hall, uint64_t* __restrict__ ppoly, uint64_t* __restrict__ ph,
     uint64_t* __restrict__ rh, int32_t* __restrict__ collision, HashStats* __restrict__ st) {
   const int32_t* pend_l = pend + (int64_t)(level - 1) * n;
-  int32_t nnext = 0, nacc = 0, est = 0;
+  int32_t nnext = 0, nacc = 0, est = 0, nres = 0;
   bool bad = false;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < n;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -2405,6 +2647,7 @@ __global__ void __launch_bounds__(128) k_hg_finish(
         alive_next[v] = 0;
       } else if (depth[v] <= level) {
         residual[v] = 1;
+        nres++;
         alive_next[v] = 0;
       } else {
         alive_next[v] = (uint8_t)(level + 1);
@@ -2421,6 +2664,7 @@ __global__ void __launch_bounds__(128) k_hg_finish(
   block_add(nnext, &st->nnext);
   block_add(nacc, &st->nacc);
   block_add(est, &st->est);
+  block_add(nres, &st->nres);
 }
 
 static uint32_t table_cap(int64_t need) {
@@ -2499,10 +2743,12 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
   SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
   SP_CUDA(cudaStreamSynchronize(s));
   g_d2h_bytes += sizeof(HashStats);
+  tr.mark("prep+keys1");
   int64_t est = hst->est;
   std::vector<LevelBlocks> lblocks;
   int64_t nA = n;
   int32_t levels = 0;
+  int64_t n_resid = 0;
   // the level's node states are read-only while the level runs; its end writes
   // the next level's into the other buffer (stale entries are older levels)
   uint8_t* cur = alive.p;
@@ -2527,6 +2773,7 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
     SP_CUDA(cudaMemsetAsync(tgkey.p, 0, (size_t)cap * 8, s));
     SP_CUDA(cudaMemsetAsync(tcnt.p, 0, (size_t)cap * 4, s));
     SP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(HashStats), s));
+    tr.mark("level alloc");
     SP_LAUNCH(ctx, k_hg_insert, gn, 256, 0, s, n, cur, level, ph_l, tkey.p, thead.p, cap - 1, cap, nslot.p, st.p);
     // 2. group sizes and template-key sums per slot; head flags
     SP_LAUNCH(ctx, k_hg_entry, gn, 256, 0, s, n, cur, level, nslot.p, rh_l, sh.p, dg->in_off.p, dg->in_idx.p, thead.p,
@@ -2578,10 +2825,11 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
               gnode.p, gsize.p, gpar.p, gstart.p, sorted.p, pos.p, pend.p, dg->name_off.p, dg->names.p, dg->op.p,
               dg->w_rank.p, dg->w_shape.p, dg->w_train.p, dg->in_off.p, dg->in_idx.p, depth.p, min_dup, gparent.p,
               residual.p, gaccept.p, seed, hall.p, ppoly.p, ph.p, rh.p, collision.p, st.p);
+    tr.mark("level enqueue");
     SP_CUDA(cudaMemcpyAsync(hst, st.p, sizeof(HashStats), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
     g_d2h_bytes += sizeof(HashStats);
-    tr.mark("level");
+    tr.mark("level sync");
     levels++;
     if (hst->overflow) throw Error(SP_ERR_CUDA, "fold group table overflow");
     if (hst->big) {
@@ -2593,31 +2841,20 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
     if (hst->nacc) {
       lblocks.emplace_back();
       level_blocks(ctx, dg, dd, nA, nG, sorted.p, gstart.p, (const int32_t*)gcs.p, gaccept.p, pend.p, 1, n, tie.p,
-                   lblocks.back());
+                   lblocks.back(), hst->nacc);
+      if (tr.on)
+        fprintf(stderr, "[fold] level %d: nA %lld nG %lld nacc %d -> K %lld Ga %lld M %lld\n", level, (long long)nA,
+                (long long)nG, hst->nacc, (long long)lblocks.back().K, (long long)lblocks.back().Ga,
+                (long long)lblocks.back().M);
       tr.mark("level: blocks");
     }
     nA = hst->nnext;
     est = hst->est;
+    n_resid += hst->nres;
   }
   SP_CUDA(cudaEventRecord(ctx->ev[7], s));
-  int32_t flags[2] = {0, 0};
-  g_d2h_bytes += 8;
-  SP_CUDA(cudaMemcpyAsync(&flags[0], collision.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaMemcpyAsync(&flags[1], tie.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaStreamSynchronize(s));
-  {
-    float ms = 0;
-    SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
-    ctx->fold_device_ms = ms;
-    ctx->fold_levels = levels;
-  }
-  *collided = flags[0] != 0;
-  if (*collided) return;
-  if (flags[1]) {
-    *fallback = true;
-    return;
-  }
-  // residual singletons, compacted on the device
+  // residual singletons compacted on the device (their count is the levels'
+  // sum), then ONE copy of everything the host needs, flags included
   DevBuf<int32_t> iota, rlist, nsel2;
   iota.alloc(n, s);
   rlist.alloc(n, s);
@@ -2629,11 +2866,17 @@ static void fold_once_hash(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_t
   DevBuf<uint8_t> tmp2;
   tmp2.alloc(tb, s);
   SP_CUDA(cub::DeviceSelect::Flagged(tmp2.p, tb, iota.p, residual.p, rlist.p, nsel2.p, (int)n, s));
-  const int64_t nr = d2h_scalar(nsel2.p, s);
-  std::vector<int32_t> resid(nr);
-  rlist.download(resid.data(), nr, s);
   tr.mark("residuals");
-  fold_finalize_blocks(dg, lblocks, resid, s, out);
+  int32_t flags[2] = {0, 0};
+  fold_finalize_blocks(dg, lblocks, {}, s, out, rlist.p, n_resid, collision.p, tie.p, flags);
+  {
+    float ms = 0;
+    SP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]));
+    ctx->fold_device_ms = ms;
+    ctx->fold_levels = levels;
+  }
+  *collided = flags[0] != 0;
+  if (!*collided && flags[1]) *fallback = true;
   tr.mark("finalize");
 }
 

@@ -1330,7 +1330,10 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
 // warp step (one carry-fixed add); the warp's remaining count is 32-bit.
 constexpr int PAIR_CHUNK = 512;   // candidates per warp chunk, walk modes
 constexpr int PAIR_MAX_CHUNKS = ITEM_ITERS_MAX * THREADS / PAIR_CHUNK;
-constexpr int SKIP_CHUNK = 4096;  // ... with prefix skipping (a chunk costs >= one walk)
+#ifndef SP_SKIP_CHUNK
+#define SP_SKIP_CHUNK 4096
+#endif
+constexpr int SKIP_CHUNK = SP_SKIP_CHUNK;  // ... with prefix skipping (a chunk costs >= one walk)
 constexpr int SKIP_MAX_CHUNKS = ITEM_ITERS_MAX_SKIP * THREADS / SKIP_CHUNK;
 #ifndef SP_PAIR_MIN_BLOCKS
 #define SP_PAIR_MIN_BLOCKS 4

@@ -66,5 +66,5 @@ for n in (1, 2, 4, 8):
     ks = [round(p[1], 2) for p in per]
     print(f"n_shards {n}: slowest rank step {t:.2f} ms (rank 0 {per[0][0]:.2f}, others "
           f"{max([p[0] for p in per[1:]] or [0]):.2f}), kernel per rank {ks}, "
-          f"speed-up {base / t:.2f}x, phases {({k: round(v, 2) for k, v in S.LAST_PHASES.items()})}",
+          f"speed-up {base / t:.2f}x, phases {({k: (round(v, 2) if isinstance(v, float) else v) for k, v in S.LAST_PHASES.items()})}",
           flush=True)

@@ -1,0 +1,9 @@
+set -x
+python bench.py > gpurun_out/r2_bench_c5.json 2> gpurun_out/r2_bench_c5.err
+python bench.py --impl reference > gpurun_out/r2_bench_c5_reference.json 2> gpurun_out/r2_bench_ref.err
+bash tools/all_configs.sh gpurun_out/r2_configs.jsonl 2> gpurun_out/configs.err
+python tools/shard_sim.py 5 > gpurun_out/r2_shard_sim_c5.txt 2>&1
+python tools/fold_scale.py --layers 1000 100000 700000 --out gpurun_out/r2_fold_scale.json > gpurun_out/fold_scale.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/fold10m.csv python tools/fold_scale.py --layers 700000 --reps 1 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_c5_walk.csv python tools/ncu_target.py c5 walk 2 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_c5_skip.csv python tools/ncu_target.py c5 skip 2 > /dev/null 2>&1

@@ -1613,6 +1613,35 @@ done:
   return out;
 }
 
+/* The entry array of a combined-table dict (CPython 3.12 layout,
+ * Include/internal/pycore_dict.h): assignments_keys inserted the K keys in
+ * order with no deletion, so entry i holds key i.  assignments_fill writes the
+ * values there directly when every entry's key is the expected key object
+ * (pointer check per entry); anything else takes the probing path.  The dict
+ * is still private to derive_plan (no watchers, not a namespace). */
+#if PY_VERSION_HEX >= 0x030C0000 && PY_VERSION_HEX < 0x030D0000
+#define DIRECT_FILL 1
+typedef struct {
+  Py_ssize_t dk_refcnt;
+  uint8_t dk_log2_size;
+  uint8_t dk_log2_index_bytes;
+  uint8_t dk_kind;
+  uint32_t dk_version;
+  Py_ssize_t dk_usable;
+  Py_ssize_t dk_nentries;
+  char dk_indices[];
+} DictKeys312;
+typedef struct {
+  PyObject* me_key;
+  PyObject* me_value;
+} DictUEntry312;
+typedef struct {
+  Py_hash_t me_hash;
+  PyObject* me_key;
+  PyObject* me_value;
+} DictGEntry312;
+#endif
+
 static PyObject* assignments_fill(PyObject* self, PyObject* args) {
   PyObject *d, *names, *labels;
   Py_buffer ids, hashes, slot;
@@ -1628,7 +1657,37 @@ static PyObject* assignments_fill(PyObject* self, PyObject* args) {
     PyErr_SetString(PyExc_ValueError, "assignments_fill: lengths differ");
     goto done;
   }
-  for (Py_ssize_t i = 0; i < K; i++) {
+  Py_ssize_t i = 0;
+#ifdef DIRECT_FILL
+  {
+    PyDictObject* mp = (PyDictObject*)d;
+    DictKeys312* dk = (DictKeys312*)mp->ma_keys;
+    if (PyDict_CheckExact(d) && mp->ma_values == NULL && mp->ma_used == K && dk->dk_nentries == K &&
+        dk->dk_kind <= 1) {
+      char* ent = dk->dk_indices + ((size_t)1 << dk->dk_log2_index_bytes);
+      for (; i < K; i++) {
+        if (I[i] < 0 || I[i] >= nn || Sl[i] < 0 || Sl[i] >= nl) break;
+        PyObject* key = PyList_GET_ITEM(names, I[i]);
+        PyObject** slot;
+        if (dk->dk_kind == 1) {
+          DictUEntry312* e = (DictUEntry312*)ent + i;
+          if (e->me_key != key) break;
+          slot = &e->me_value;
+        } else {
+          DictGEntry312* e = (DictGEntry312*)ent + i;
+          if (e->me_key != key) break;
+          slot = &e->me_value;
+        }
+        PyObject* v = PyList_GET_ITEM(labels, Sl[i]);
+        Py_INCREF(v);
+        PyObject* old = *slot;
+        *slot = v;
+        Py_XDECREF(old);
+      }
+    }
+  }
+#endif
+  for (; i < K; i++) {
     if (I[i] < 0 || I[i] >= nn || Sl[i] < 0 || Sl[i] >= nl) {
       PyErr_SetString(PyExc_IndexError, "assignments_fill: index out of range");
       goto done;

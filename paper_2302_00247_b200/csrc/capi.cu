@@ -281,8 +281,12 @@ void sp_tables_free(sp_tables* t) {
   t->peers.clear();
   sp::Trace tr("tables_free");
   if (t->ctx) {
+    // the device buffers go back stream-ordered; only the build's own uploads
+    // (pinned staging) must have run -- not whatever was queued behind them
+    // (a cheap block group's tables are closed while the expensive group's
+    // kernel still runs)
     cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
+    sp::tables_wait_built(t);
   }
   tr.mark("sync");
   sp::tables_free_priv(t);

@@ -4105,6 +4105,12 @@ void route_search(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
     }
 }
 
+void tables_wait_built(sp_tables* t) {
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  if (priv && priv->built) cudaEventSynchronize(priv->built);
+  else if (t->ctx) cudaStreamSynchronize(t->ctx->stream);
+}
+
 void tables_free_priv(sp_tables* t) {
   delete (TablesPriv*)t->priv;
   t->priv = nullptr;

@@ -457,6 +457,7 @@ struct sp_tables {
 namespace sp {
 void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg);
 void fold_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, sp_fold* out);
+void tables_wait_built(sp_tables* t);
 void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* tmpl_off,
                   const int32_t* tmpl_nodes, const sp_mesh* mesh, int64_t mu, int64_t chunk,
                   sp_tables* out);

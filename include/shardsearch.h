@@ -381,6 +381,13 @@ int sp_fold_stats(const sp_ctx* ctx, double* device_ms, int32_t* levels);
  * every node of every candidate.
  */
 #define SP_OPT_MEMO 2
+/*
+ * SP_OPT_HOST_LAYOUT (default 1): for graphs of <= 8192 nodes the table layout
+ * (node maps, boundary flags, blob offsets) is computed on the host while the
+ * tables are built, so building them needs no device round trip.  0 uses the
+ * device layout for every graph (same tables).
+ */
+#define SP_OPT_HOST_LAYOUT 3
 int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value);
 
 /* CUDA-event timer on the context's stream (brackets whole API calls for benchmarks). */

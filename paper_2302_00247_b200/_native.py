@@ -457,6 +457,10 @@ class Backend:
         """Memoised brute force when skipping is off (default on)."""
         self._check(self.lib.sp_set_option(self.ctx, 2, 1 if on else 0), "sp_set_option")
 
+    def set_host_layout(self, on: bool) -> None:
+        """Table layout of small graphs on the host (default on); off: on the device."""
+        self._check(self.lib.sp_set_option(self.ctx, 3, 1 if on else 0), "sp_set_option")
+
     def set_mode(self, mode: str) -> None:
         """'skip' (default), 'memo' (every candidate visited, dirty nodes re-routed)
         or 'walk' (every node of every candidate)."""

@@ -536,6 +536,10 @@ int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value) {
     }
     return SP_OK;
   }
+  if (option == SP_OPT_HOST_LAYOUT) {
+    for (size_t i = 0; i <= ctx->peers.size(); i++) (i ? ctx->peers[i - 1] : ctx)->host_layout = value ? 1 : 0;
+    return SP_OK;
+  }
   ctx->last_error = "unknown option";
   return SP_ERR_CONFIG;
 }

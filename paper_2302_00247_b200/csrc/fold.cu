@@ -870,6 +870,10 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
     dg->h_topo.resize((size_t)n);
     dg->h_op.resize((size_t)n);
     dg->h_w_rank.resize((size_t)n);
+    const bool host_csr = n <= SP_HOST_LAYOUT_MAX;
+    dg->h_in_off.resize(host_csr ? (size_t)n + 1 : 0);
+    dg->h_in_idx.resize(host_csr ? (size_t)E : 0);
+    dg->h_w_train.resize(host_csr ? (size_t)n : 0);
     const double tu_alloc = ms_since(tu0);
     // the previous upload may still be reading the staging buffer
     SP_CUDA(cudaStreamSynchronize(s));
@@ -888,6 +892,11 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
     copies.push_back({dg->h_topo.data(), g->topo_rank, (size_t)n * 8});
     copies.push_back({dg->h_op.data(), g->op, (size_t)n});
     copies.push_back({dg->h_w_rank.data(), g->w_rank, (size_t)n});
+    if (host_csr) {
+      copies.push_back({dg->h_in_off.data(), g->in_off, (size_t)(n + 1) * 8});
+      copies.push_back({dg->h_in_idx.data(), g->in_idx, (size_t)E * 4});
+      copies.push_back({dg->h_w_train.data(), g->w_trainable, (size_t)n});
+    }
     std::vector<size_t> cstart(copies.size() + 1, 0);
     for (size_t k = 0; k < copies.size(); k++) cstart[k + 1] = cstart[k] + copies[k].bytes;
     // byte range [lo, hi) of the concatenated copies per thread

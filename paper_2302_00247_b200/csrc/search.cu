@@ -185,10 +185,99 @@ __global__ void k_boundary(GraphView G, int64_t n, const int32_t* node_block, ui
     }
 }
 
+// The serial half of a block's layout (k_layout's thread 0, and the host
+// layout of small graphs): lays out the blob, assigns pool slots (linear scan;
+// a producer's slot is released at its last internal consumer) and derives
+// each node's prefix-failure skip (ancestor cone over enumeration positions).
+// k[i], last[i], prodpos[i][] are the node's internal fan-in, last internal
+// consumer and producer positions; pool / anc are scratch of T entries.
+__host__ __device__ inline void layout_serial(int T, const int* kk, const int* last, const int16_t (*prodpos)[KMAX],
+                                              int* pool, uint64_t* ancs, const int32_t* tnodes,
+                                              const int16_t* slot_of, const uint8_t* radix_of,
+                                              const uint8_t* w_rank, const uint8_t* w_train, BlobHeader& H,
+                                              EntryLayout* lay) {
+  const int V = H.V;
+  int nprod = 0, nt = 0;
+  int64_t nent = 0, ndbl = 0, nent4 = 0;
+  uint32_t used[MAXT / 32];
+  for (int w = 0; w < MAXT / 32; w++) used[w] = 0;
+  int npool = 0;
+  for (int i = 0; i < T; i++) {
+    // release producers whose last internal consumer is i
+    for (int j = 0; j < i; j++)
+      if (last[j] == i && pool[j] >= 0) used[pool[j] >> 5] &= ~(1u << (pool[j] & 31));
+    pool[i] = -1;
+    if (last[i] >= 0) {
+      int sl = 0;
+      while (used[sl >> 5] & (1u << (sl & 31))) sl++;
+      used[sl >> 5] |= 1u << (sl & 31);
+      pool[i] = sl;
+      npool = npool > sl + 1 ? npool : sl + 1;
+    }
+    const int32_t n = tnodes[i];
+    const int k = kk[i];
+    // ancestor cone over enumeration positions (V <= 64)
+    uint64_t anc = slot_of[i] >= 0 ? (1ULL << slot_of[i]) : 0ULL;
+    for (int j = 0; j < k && j < KMAX; j++) anc |= ancs[prodpos[i][j]];
+    ancs[i] = anc;
+    EntryLayout L;
+    L.k = k;
+    L.nd = slot_of[i] >= 0 ? radix_of[i] : 1;
+    L.prod = nprod;
+    L.tab = (int32_t)nent;
+    L.tab4 = (int32_t)nent4;
+    L.pad = 0;
+    L.dbl = (int32_t)ndbl;
+    L.train_idx = (w_rank[n] && w_train[n]) ? nt++ : -1;
+    L.out_pool = pool[i];
+#ifdef __CUDA_ARCH__
+    L.skip_m = anc ? 63 - __clzll(anc) : -1;
+#else
+    L.skip_m = anc ? 63 - __builtin_clzll(anc) : -1;
+#endif
+    uint64_t R = 1;
+    for (int q = L.skip_m + 1; q < V; q++) R *= ((H.radix3 >> q) & 1) ? 3 : 2;
+    L.skip_R = anc ? R : 0;
+    nprod += k;
+    nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
+    nent4 += 4 * (int64_t)pow3(k < KMAX ? k : KMAX);
+    ndbl += 8 + 12 * (int64_t)k;
+    lay[i] = L;
+  }
+  H.T = T;
+  H.nt = nt;
+  H.npool = npool;
+  H.n_prod = nprod;
+  int64_t off = sizeof(BlobHeader);
+  H.desc_off = (int32_t)off;
+  off = align16(off + 16 * (int64_t)T);
+  H.skip_off = (int32_t)off;
+  off = align16(off + (int64_t)sizeof(NodeSkip) * T);
+  H.stride_off = (int32_t)off;
+  off = align16(off + 9 * (int64_t)V);
+  H.dirty_off = (int32_t)off;
+  off = align16(off + 8 * ((int64_t)V + 1));
+  H.prod_off = (int32_t)off;
+  off = align16(off + 4 * (int64_t)nprod);  // i16 pool slots, then i16 producer positions
+  H.tab_off = (int32_t)off;
+  off = align16(off + nent);
+  H.dbl_off = (int32_t)off;
+  off = align16(off + 8 * ndbl);
+  H.train_off = (int32_t)off;
+  off = align16(off + (int64_t)sizeof(TrainDesc) * nt);
+  H.fast_off = (int32_t)off;
+  off = align16(off + (int64_t)sizeof(FastNode) * T);
+  H.zero_off = (int32_t)off;
+  off += 128;
+  H.fprod_off = (int32_t)off;
+  off = align16(off + 8 * (int64_t)nprod);
+  H.tab4_off = (int32_t)off;
+  off = align16(off + nent4 + TAB4_PAD);
+  H.bytes = (int32_t)off;
+}
+
 // One CTA per block: per-node internal fan-in and liveness in parallel, then
-// one thread lays out the blob, assigns pool slots (linear scan; a producer's
-// slot is released at its last internal consumer) and derives each node's
-// prefix-failure skip (ancestor cone over enumeration positions).
+// one thread runs layout_serial.
 __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                          const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
                          const uint8_t* radix_of, EntryLayout* lay, BlobHeader* hdr, int64_t* blob_bytes,
@@ -218,83 +307,11 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      const BlobHeader& H0 = hdr[b];
-      const int V = H0.V;
-      int nprod = 0, nt = 0;
-      int64_t nent = 0, ndbl = 0, nent4 = 0;
-      uint32_t used[MAXT / 32];
-      for (int w = 0; w < MAXT / 32; w++) used[w] = 0;
-      int npool = 0;
-      for (int i = 0; i < T; i++) {
-        // release producers whose last internal consumer is i
-        for (int j = 0; j < i; j++)
-          if (s_last[j] == i && s_pool[j] >= 0) used[s_pool[j] >> 5] &= ~(1u << (s_pool[j] & 31));
-        s_pool[i] = -1;
-        if (s_last[i] >= 0) {
-          int sl = 0;
-          while (used[sl >> 5] & (1u << (sl & 31))) sl++;
-          used[sl >> 5] |= 1u << (sl & 31);
-          s_pool[i] = sl;
-          npool = max(npool, sl + 1);
-        }
-        const int32_t n = tmpl_nodes[e0 + i];
-        const int k = s_k[i];
-        // ancestor cone over enumeration positions (V <= 64)
-        uint64_t anc = slot_of[e0 + i] >= 0 ? (1ULL << slot_of[e0 + i]) : 0ULL;
-        for (int j = 0; j < k && j < KMAX; j++) anc |= s_anc[s_prodpos[i][j]];
-        s_anc[i] = anc;
-        EntryLayout L;
-        L.k = k;
-        L.nd = slot_of[e0 + i] >= 0 ? radix_of[e0 + i] : 1;
-        L.prod = nprod;
-        L.tab = (int32_t)nent;
-        L.tab4 = (int32_t)nent4;
-        L.pad = 0;
-        L.dbl = (int32_t)ndbl;
-        L.train_idx = (G.w_rank[n] && G.w_train[n]) ? nt++ : -1;
-        L.out_pool = s_pool[i];
-        L.skip_m = anc ? 63 - __clzll(anc) : -1;
-        uint64_t R = 1;
-        for (int q = L.skip_m + 1; q < V; q++) R *= ((H0.radix3 >> q) & 1) ? 3 : 2;
-        L.skip_R = anc ? R : 0;
-        nprod += k;
-        nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
-        nent4 += 4 * (int64_t)pow3(k < KMAX ? k : KMAX);
-        ndbl += 8 + 12 * (int64_t)k;
-        lay[e0 + i] = L;
-      }
-      BlobHeader& H = hdr[b];
-      H.T = T;
-      H.nt = nt;
-      H.npool = npool;
-      H.n_prod = nprod;
-      int64_t off = sizeof(BlobHeader);
-      H.desc_off = (int32_t)off;
-      off = align16(off + 16 * (int64_t)T);
-      H.skip_off = (int32_t)off;
-      off = align16(off + (int64_t)sizeof(NodeSkip) * T);
-      H.stride_off = (int32_t)off;
-      off = align16(off + 9 * (int64_t)V);
-      H.dirty_off = (int32_t)off;
-      off = align16(off + 8 * ((int64_t)V + 1));
-      H.prod_off = (int32_t)off;
-      off = align16(off + 4 * (int64_t)nprod);  // i16 pool slots, then i16 producer positions
-      H.tab_off = (int32_t)off;
-      off = align16(off + nent);
-      H.dbl_off = (int32_t)off;
-      off = align16(off + 8 * ndbl);
-      H.train_off = (int32_t)off;
-      off = align16(off + (int64_t)sizeof(TrainDesc) * nt);
-      H.fast_off = (int32_t)off;
-      off = align16(off + (int64_t)sizeof(FastNode) * T);
-      H.zero_off = (int32_t)off;
-      off += 128;
-      H.fprod_off = (int32_t)off;
-      off = align16(off + 8 * (int64_t)nprod);
-      H.tab4_off = (int32_t)off;
-      off = align16(off + nent4 + TAB4_PAD);
-      H.bytes = (int32_t)off;
-      blob_bytes[b] = off;
+      BlobHeader H = hdr[b];
+      layout_serial(T, s_k, s_last, s_prodpos, s_pool, s_anc, tmpl_nodes + e0, slot_of + e0, radix_of + e0,
+                    G.w_rank, G.w_train, H, lay + e0);
+      hdr[b] = H;
+      blob_bytes[b] = H.bytes;
     }
     __syncthreads();
   }
@@ -311,11 +328,33 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
                        int64_t chunk, uint8_t* blobs, uint8_t* bound_of, uint8_t* xinfo, const int64_t* xoff) {
   const MeshC M = mesh_consts(mesh);
   __shared__ uint32_t s_kbase[MAXT + 1];
+  __shared__ uint32_t s_cnt[MAXT];
+  __shared__ int16_t s_outpool[MAXT];
+  __shared__ int8_t s_skipm[MAXT], s_rslot[MAXT], s_eslot[MAXT];
+  __shared__ uint8_t s_rr[64];
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const int64_t e0 = tmpl_off[b];
     const int T = (int)(tmpl_off[b + 1] - e0);
     const BlobHeader& H = hdr_in[b];
     uint8_t* blob = blobs + blob_off[b];
+    const int V = H.V;
+    const uint64_t radix3 = H.radix3;
+    // per-node fields staged once (every later pass reads them from shared memory)
+    int8_t* perm = (int8_t*)(blob + H.stride_off + 8 * V);  // reference slot -> enumeration position
+    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+      const EntryLayout L = lay[e0 + i];
+      const int rs = ref_slot_of[e0 + i], es = slot_of[e0 + i];
+      s_cnt[i] = (uint32_t)L.nd * pow3(L.k);
+      s_outpool[i] = (int16_t)L.out_pool;
+      s_skipm[i] = (int8_t)L.skip_m;
+      s_rslot[i] = (int8_t)rs;
+      s_eslot[i] = (int8_t)es;
+      if (rs >= 0) {
+        s_rr[rs] = ((radix3 >> es) & 1) ? 3 : 2;
+        perm[rs] = (int8_t)es;
+      }
+    }
+    for (int q = threadIdx.x; q < 128; q += blockDim.x) blob[H.zero_off + q] = 0;
     if (threadIdx.x == 0) {
       BlobHeader h = H;
       h.multi_dev = M.d > 1;
@@ -327,37 +366,40 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       h.mu = mu;
       h.chunk = chunk;
       *(BlobHeader*)blob = h;
-      // reference strides per enumeration position + perm (reference slot -> enumeration position)
-      uint64_t* stride = (uint64_t*)(blob + H.stride_off);
-      int8_t* perm = (int8_t*)(blob + H.stride_off + 8 * H.V);
-      uint8_t rr[64];
-      for (int i = 0; i < T; i++)
-        if (ref_slot_of[e0 + i] >= 0) {
-          rr[ref_slot_of[e0 + i]] = ((H.radix3 >> slot_of[e0 + i]) & 1) ? 3 : 2;
-          perm[ref_slot_of[e0 + i]] = (int8_t)slot_of[e0 + i];
-        }
-      for (int i = 0; i < T; i++)
-        if (ref_slot_of[e0 + i] >= 0) {
-          uint64_t st = 1;
-          for (int s2 = ref_slot_of[e0 + i] + 1; s2 < H.V; s2++) st *= rr[s2];
-          stride[slot_of[e0 + i]] = st;
-        }
-      // memoised scoring: dirty[q] = nodes to re-route when enumeration positions >= q change
-      uint64_t* dirty = (uint64_t*)(blob + H.dirty_off);
-      for (int q = 0; q <= H.V; q++) {
-        uint64_t mask = 0;
-        for (int i = 0; i < T && i < 64; i++)
-          if (q == 0 || lay[e0 + i].skip_m >= q) mask |= 1ULL << i;
-        dirty[q] = mask;
+    }
+    __syncthreads();
+    // reference strides per enumeration position
+    uint64_t* stride = (uint64_t*)(blob + H.stride_off);
+    for (int i = threadIdx.x; i < T; i += blockDim.x)
+      if (s_rslot[i] >= 0) {
+        uint64_t st = 1;
+        for (int s2 = s_rslot[i] + 1; s2 < V; s2++) st *= s_rr[s2];
+        stride[s_eslot[i]] = st;
       }
-      for (int q = 0; q < 128; q++) blob[H.zero_off + q] = 0;
+    // memoised scoring: dirty[q] = nodes to re-route when enumeration positions >= q change
+    uint64_t* dirty = (uint64_t*)(blob + H.dirty_off);
+    for (int q = threadIdx.x; q <= V; q += blockDim.x) {
+      uint64_t mask = 0;
+      for (int i = 0; i < T && i < 64; i++)
+        if (q == 0 || s_skipm[i] >= q) mask |= 1ULL << i;
+      dirty[q] = mask;
+    }
+    // routing-table key offsets: exclusive scan of nd * 3^k (warp 0)
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
       uint32_t acc = 0;
-      for (int i = 0; i < T; i++) {
-        s_kbase[i] = acc;
-        const EntryLayout L = lay[e0 + i];
-        acc += (uint32_t)L.nd * pow3(L.k);
+      for (int base = 0; base < T; base += 32) {
+        const uint32_t v = base + lane < T ? s_cnt[base + lane] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (base + lane < T) s_kbase[base + lane] = acc + x - v;
+        acc += __shfl_sync(0xffffffffu, x, 31);
       }
-      s_kbase[T] = acc;
+      if (lane == 0) s_kbase[T] = acc;
     }
     __syncthreads();
     // per-node records
@@ -387,7 +429,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
           const int32_t r = G.in_idx[q];
           if (node_block[r] != (int32_t)b) continue;
-          const int ps = lay[e0 + node_tpos[r]].out_pool;
+          const int ps = s_outpool[node_tpos[r]];
           if (L.k <= 2) {
             if (jj == 0) { f.r0 = ps * THREADS * 8; f.s0 = ps * THREADS; }
             else { f.r1 = ps * THREADS * 8; f.s1 = ps * THREADS; }
@@ -438,7 +480,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
         const int32_t r = G.in_idx[q];
         if (node_block[r] != (int32_t)b) continue;
-        prod[j] = (int16_t)lay[e0 + node_tpos[r]].out_pool;
+        prod[j] = s_outpool[node_tpos[r]];
         ((int16_t*)(blob + H.prod_off))[H.n_prod + L.prod + j] = (int16_t)node_tpos[r];
         const int rr = G.act_rank[r];
         for (int p = 0; p < 4; p++)
@@ -2436,6 +2478,8 @@ __global__ void k_explain_fast(GraphView G, const int64_t* tmpl_off, const int32
                                const sp_score_out* scores, sp_mesh mesh, int64_t mu, int64_t chunk,
                                ExplainBlock* out, int8_t* node_out, int8_t* edge_out) {
   extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint8_t s_dig[64];
+  __shared__ int s_ok;
   const MeshC M = mesh_consts(mesh);
   const int lane = threadIdx.x & 31;
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -2451,18 +2495,28 @@ __global__ void k_explain_fast(GraphView G, const int64_t* tmpl_off, const int32
     }
     const BlobHeader* gH = (const BlobHeader*)(blobs + blob_off[b]);
     const int nbytes = gH->bytes;
+    const int64_t e0 = tmpl_off[b];
     __syncwarp();
     for (int q = lane * 16; q < nbytes; q += 32 * 16)
       *(int4*)(smem + q) = *(const int4*)(blobs + blob_off[b] + q);
+    {
+      // the per-node records lane 0 reads in its serial walk, pulled into L1
+      // by the whole warp first (each of those loads would otherwise wait on L2)
+      const int T = gH->T;
+      const uint8_t* xb = xinfo + xoff[b];
+      const int64_t xbytes = xoff[b + 1] - xoff[b];
+      for (int64_t q = lane * 128; q < xbytes; q += 32 * 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xb + q));
+      for (int q = lane * 128; q < 2 * T; q += 32 * 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"((const uint8_t*)(ref_slot_of + e0) + q));
+      for (int q = lane * 128; q < T; q += 32 * 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(bound_of + e0 + q));
+    }
     __syncwarp();
-    if (lane != 0) continue;
     const BlobHeader& H = *(const BlobHeader*)smem;
     const NodeDesc* desc = (const NodeDesc*)(smem + H.desc_off);
     const int16_t* prodpos = (const int16_t*)(smem + H.prod_off) + H.n_prod;
     const uint8_t* tab = smem + H.tab_off;
     const double* dbl = (const double*)(smem + H.dbl_off);
     const XNode* xn = (const XNode*)(xinfo + xoff[b]);
-    const int64_t e0 = tmpl_off[b];
     const int T = H.T;
     const XEdge* xe = (const XEdge*)(xinfo + xoff[b] + (int64_t)sizeof(XNode) * T);
     ExplainBlock X;
@@ -2471,114 +2525,131 @@ __global__ void k_explain_fast(GraphView G, const int64_t* tmpl_off, const int32
     X.forward_comm = X.backward_comm = X.total = 0.0;
     for (int k = 0; k < 4; k++) X.bytes[k] = X.calls[k] = 0;
     X.collective_calls = 0;
-    uint8_t dig[64];  // reference slot order (candidate_by_index, search.py:103-116)
-    unsigned long long rem = index;
-    for (int q = H.V - 1; q >= 0; q--) {
-      const uint32_t r = ((H.radix3_ref >> q) & 1) ? 3 : 2;
-      dig[q] = (uint8_t)(rem % r);
-      rem /= r;
-    }
-    uint8_t state[MAXT];
-    double reach[MAXT];
-    int64_t eo = edge_off[b];
-    bool ok = true;
-    for (int i = 0; i < T; i++) {
-      const NodeDesc nd = desc[i];
-      const int slot = ref_slot_of[e0 + i];
-      uint32_t key = slot >= 0 ? dig[slot] : 0;
-      for (int j = 0; j < nd.k; j++) key = key * 3 + state[prodpos[nd.prod + j]];
-      const uint8_t e = tab[nd.tab + key];
-      if (e == 0xFF) {
-        X.fail_pos = i;
-        ok = false;
-        break;
-      }
-      const int p = e & 3, st = e >> 2;
-      state[i] = (uint8_t)st;
-      const double* dn = dbl + nd.dbl;
-      double base = 0.0;
-      for (int j = 0; j < nd.k; j++) {
-        const int pp = prodpos[nd.prod + j];
-        const int sj = state[pp];
-        const int kind = xe[nd.prod + j].kind[p][sj];
-        if (kind > 0) {
-          X.bytes[kind - 1] += xn[pp].act_bytes;
-          X.calls[kind - 1]++;
-        }
-        edge_out[2 * eo] = (int8_t)kind;
-        edge_out[2 * eo + 1] = xe[nd.prod + j].axis[p][sj];
-        eo++;
-        base = fmax(base, dadd(reach[pp], dn[8 + (j * 4 + p) * 3 + sj]));
-      }
-      Pattern pats[4];
-      patterns_for(xn[i].op, pats);
-      const int pc = pats[p].coll;
-      if (pc != C_ID) {
-        X.bytes[pc - 1] += xn[i].act_bytes;
-        X.calls[pc - 1]++;
-      }
-      reach[i] = dadd(base, dn[p]);
-      const NSpec fs = state_spec(st, xn[i].act_rank);
-      node_out[4 * (e0 + i)] = (int8_t)p;
-      node_out[4 * (e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
-      node_out[4 * (e0 + i) + 2] = -1;
-      node_out[4 * (e0 + i) + 3] = 0;
-    }
-    if (!ok) {
-      out[b] = X;
-      continue;
-    }
     double fwd = 0.0;
-    for (int i = 0; i < T; i++) {
-      double tail = reach[i];
-      if (bound_of[e0 + i] && state[i] != 0) {
-        tail = dadd(tail, dbl[desc[i].dbl + 4 + state[i]]);
-        X.bytes[C_AG - 1] += xn[i].act_bytes;
-        X.calls[C_AG - 1]++;
-        node_out[4 * (e0 + i) + 2] = state_spec(state[i], xn[i].act_rank).axis;
+    if (lane == 0) {
+      // reference slot order (candidate_by_index, search.py:103-116)
+      unsigned long long rem = index;
+      for (int q = H.V - 1; q >= 0; q--) {
+        const uint32_t r = ((H.radix3_ref >> q) & 1) ? 3 : 2;
+        s_dig[q] = (uint8_t)(rem % r);
+        rem /= r;
       }
-      fwd = fmax(fwd, tail);
+      uint8_t state[MAXT];
+      double reach[MAXT];
+      int64_t eo = edge_off[b];
+      bool ok = true;
+      for (int i = 0; i < T; i++) {
+        const NodeDesc nd = desc[i];
+        const int slot = ref_slot_of[e0 + i];
+        uint32_t key = slot >= 0 ? s_dig[slot] : 0;
+        for (int j = 0; j < nd.k; j++) key = key * 3 + state[prodpos[nd.prod + j]];
+        const uint8_t e = tab[nd.tab + key];
+        if (e == 0xFF) {
+          X.fail_pos = i;
+          ok = false;
+          break;
+        }
+        const int p = e & 3, st = e >> 2;
+        state[i] = (uint8_t)st;
+        const double* dn = dbl + nd.dbl;
+        double base = 0.0;
+        for (int j = 0; j < nd.k; j++) {
+          const int pp = prodpos[nd.prod + j];
+          const int sj = state[pp];
+          const int kind = xe[nd.prod + j].kind[p][sj];
+          if (kind > 0) {
+            X.bytes[kind - 1] += xn[pp].act_bytes;
+            X.calls[kind - 1]++;
+          }
+          edge_out[2 * eo] = (int8_t)kind;
+          edge_out[2 * eo + 1] = xe[nd.prod + j].axis[p][sj];
+          eo++;
+          base = fmax(base, dadd(reach[pp], dn[8 + (j * 4 + p) * 3 + sj]));
+        }
+        Pattern pats[4];
+        patterns_for(xn[i].op, pats);
+        const int pc = pats[p].coll;
+        if (pc != C_ID) {
+          X.bytes[pc - 1] += xn[i].act_bytes;
+          X.calls[pc - 1]++;
+        }
+        reach[i] = dadd(base, dn[p]);
+        const NSpec fs = state_spec(st, xn[i].act_rank);
+        node_out[4 * (e0 + i)] = (int8_t)p;
+        node_out[4 * (e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
+        node_out[4 * (e0 + i) + 2] = -1;
+        node_out[4 * (e0 + i) + 3] = 0;
+      }
+      if (ok)
+        for (int i = 0; i < T; i++) {
+          double tail = reach[i];
+          if (bound_of[e0 + i] && state[i] != 0) {
+            tail = dadd(tail, dbl[desc[i].dbl + 4 + state[i]]);
+            X.bytes[C_AG - 1] += xn[i].act_bytes;
+            X.calls[C_AG - 1]++;
+            node_out[4 * (e0 + i) + 2] = state_spec(state[i], xn[i].act_rank).axis;
+          }
+          fwd = fmax(fwd, tail);
+        }
+      s_ok = ok;
+    }
+    __syncwarp();
+    if (!s_ok) {
+      if (lane == 0) out[b] = X;
+      continue;
     }
     double bwd = 0.0;
     if (M.d > 1) {
-      // pack_gradients (rewrite.py:78-111): buckets first, then unfused, each one AllReduce
-      int64_t cur = 0;
-      int cur_n = 0;
-      for (int pass = 0; pass < 2; pass++) {
-        for (int i = 0; i < T; i++) {
-          const int32_t n = tmpl_nodes[e0 + i];
-          if (!G.w_rank[n] || !G.w_train[n] || dig[ref_slot_of[e0 + i]] != 0) continue;
-          const int64_t sz = G.w_bytes[n];
-          if (pass == 0) {
-            if (sz >= mu) continue;
-            if (cur + sz > chunk && cur_n) {
-              bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
-              X.bytes[0] += cur;
+      // pack_gradients (rewrite.py:78-111): buckets first, then unfused, each one AllReduce.
+      // Each trainable weight's byte size (-1: not all-replica / not trainable) is
+      // looked up by the warp into shared memory (the blob is no longer read).
+      int64_t* szs = (int64_t*)smem;
+      for (int i = lane; i < T; i += 32) {
+        const int32_t n = tmpl_nodes[e0 + i];
+        szs[i] = (!G.w_rank[n] || !G.w_train[n] || s_dig[ref_slot_of[e0 + i]] != 0) ? -1 : G.w_bytes[n];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        int64_t cur = 0;
+        int cur_n = 0;
+        for (int pass = 0; pass < 2; pass++) {
+          for (int i = 0; i < T; i++) {
+            const int64_t sz = szs[i];
+            if (sz < 0) continue;
+            if (pass == 0) {
+              if (sz >= mu) continue;
+              if (cur + sz > chunk && cur_n) {
+                bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+                X.bytes[0] += cur;
+                X.calls[0]++;
+                cur = 0;
+                cur_n = 0;
+              }
+              cur += sz;
+              cur_n++;
+            } else if (sz >= mu) {
+              bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
+              X.bytes[0] += sz;
               X.calls[0]++;
-              cur = 0;
-              cur_n = 0;
             }
-            cur += sz;
-            cur_n++;
-          } else if (sz >= mu) {
-            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
-            X.bytes[0] += sz;
+          }
+          if (pass == 0 && cur_n) {
+            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+            X.bytes[0] += cur;
             X.calls[0]++;
           }
         }
-        if (pass == 0 && cur_n) {
-          bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
-          X.bytes[0] += cur;
-          X.calls[0]++;
-        }
       }
     }
-    X.valid = 1;
-    X.forward_comm = fwd;
-    X.backward_comm = bwd;
-    X.total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
-    X.collective_calls = X.calls[0] + X.calls[1] + X.calls[2] + X.calls[3];
-    out[b] = X;
+    if (lane == 0) {
+      X.valid = 1;
+      X.forward_comm = fwd;
+      X.backward_comm = bwd;
+      X.total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
+      X.collective_calls = X.calls[0] + X.calls[1] + X.calls[2] + X.calls[3];
+      out[b] = X;
+    }
+    __syncwarp();
   }
 }
 
@@ -2782,7 +2853,9 @@ struct PendingScore {
   size_t host_bytes = 0, off_blk = 0, off_node = 0, off_edge = 0;
   // 0 launch, 1 kernel start, 2 kernel end, 3 reduce end, 4 explain end, 5 results on the host
   cudaEvent_t ev[6] = {};
+  bool synced = false;  // ev[5] (recorded last, on the same stream) has been waited for
   void events() {  // from the context's pool (cudaEventCreate per search adds up on tiny searches)
+    synced = false;
     for (auto& e : ev)
       if (!e) {
         if (!ctx->event_pool.empty()) {
@@ -2795,7 +2868,7 @@ struct PendingScore {
   }
   void release_host() {
     if (!host) return;
-    cudaEventSynchronize(ev[5]);
+    if (!synced) cudaEventSynchronize(ev[5]);
     ctx->pinned_pool.push_back({host, host_bytes});
     host = nullptr;
     host_bytes = 0;
@@ -2805,7 +2878,7 @@ struct PendingScore {
     for (auto& e : ev)
       if (e) {
         if (ctx) {
-          cudaEventSynchronize(e);  // recorded work done before another search re-records it
+          if (!synced) cudaEventSynchronize(e);  // recorded work done before another search re-records it
           ctx->event_pool.push_back(e);
         } else {
           cudaEventDestroy(e);
@@ -2829,7 +2902,10 @@ struct TablesPriv {
   uint8_t* pin = nullptr;
   size_t pin_bytes = 0;
   ~TablesPriv() {
-    if (built) cudaEventDestroy(built);
+    if (built) {  // back to the context's pool (tables_free waited for it)
+      if (ctx) ctx->event_pool.push_back(built);
+      else cudaEventDestroy(built);
+    }
     if (pin && ctx) pinned_release(ctx, pin, pin_bytes);
   }
   // a pinned block of >= `need` bytes owned by the tables (the stream is
@@ -2966,9 +3042,109 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   priv->mu = mu;
   priv->chunk = chunk;
   TableDev& D = priv->dev;
+  const GraphView G = view_of(dg);
+  DevBuf<EntryLayout> lay;
+  DevBuf<BlobHeader> hdr;
+  out->max_blob = 0;
+  out->max_pool = 0;
+  out->blob_off.assign(nb + 1, 0);
+  out->edge_off.assign(nb + 1, 0);
+  std::vector<int64_t> xo;
+  auto offsets = [&] {
+    xo.assign(nb + 1, 0);
+    for (int64_t b = 0; b < nb; b++) {
+      out->max_blob = std::max<int64_t>(out->max_blob, out->hdr[b].bytes);
+      out->max_pool = std::max(out->max_pool, out->hdr[b].npool);
+      out->blob_off[b + 1] = out->blob_off[b] + out->hdr[b].bytes;
+      out->edge_off[b + 1] = out->edge_off[b] + out->hdr[b].n_prod;
+      xo[b + 1] = xo[b] + align16((int64_t)sizeof(XNode) * out->hdr[b].T + (int64_t)sizeof(XEdge) * out->hdr[b].n_prod);
+    }
+  };
+  if (!dg->h_in_off.empty() && ctx->host_layout) {
+    // Small graph: node maps, boundary flags and the blob layout on the host
+    // (k_mark_blocks / k_boundary / k_layout's work, layout_serial shared), so
+    // the build is ONE upload and the fill launch -- no device round trip.
+    const int64_t* in_off = dg->h_in_off.data();
+    const int32_t* in_idx = dg->h_in_idx.data();
+    std::vector<int32_t> nblk(n, -1), ntpos(n, -1);
+    std::vector<uint8_t> flags(2 * (size_t)n, 0);  // has_cons | ext_cons
+    for (int64_t b = 0; b < nb; b++)
+      for (int64_t e = out->tmpl_off[b]; e < out->tmpl_off[b + 1]; e++) {
+        const int32_t v = out->tmpl_nodes[e];
+        if (nblk[v] != -1) throw Error(SP_ERR_CONFIG, "a node appears in more than one template");
+        nblk[v] = (int32_t)b;
+        ntpos[v] = (int32_t)(e - out->tmpl_off[b]);
+      }
+    for (int64_t c = 0; c < n; c++)
+      for (int64_t e = in_off[c]; e < in_off[c + 1]; e++) {
+        const int32_t p = in_idx[e];
+        flags[p] = 1;
+        if (nblk[c] != nblk[p] || nblk[p] < 0) flags[n + p] = 1;
+      }
+    std::vector<EntryLayout> lay_h(std::max<int64_t>(ne, 1));
+    std::vector<int> kk(MAXT), last(MAXT), pool(MAXT);
+    std::vector<uint64_t> ancs(MAXT);
+    std::vector<int16_t> pp((size_t)MAXT * KMAX);
+    int err = 0;
+    for (int64_t b = 0; b < nb && !err; b++) {
+      const int64_t e0 = out->tmpl_off[b];
+      const int T = (int)(out->tmpl_off[b + 1] - e0);
+      for (int i = 0; i < T; i++) last[i] = -1;
+      for (int i = 0; i < T; i++) {
+        const int32_t v = out->tmpl_nodes[e0 + i];
+        int k = 0;
+        for (int64_t e = in_off[v]; e < in_off[v + 1]; e++) {
+          const int32_t r = in_idx[e];
+          if (nblk[r] != (int32_t)b) continue;
+          const int j = ntpos[r];
+          if (j >= i) err = err ? err : 2;
+          if (j < T) last[j] = std::max(last[j], i);
+          if (k < KMAX) pp[(size_t)i * KMAX + k] = (int16_t)j;
+          k++;
+        }
+        if (k > KMAX) err = err ? err : 3;
+        kk[i] = k;
+      }
+      if (!err)
+        layout_serial(T, kk.data(), last.data(), (const int16_t(*)[KMAX])pp.data(), pool.data(), ancs.data(),
+                      out->tmpl_nodes.data() + e0, slot_of.data() + e0, radix_of.data() + e0, dg->h_w_rank.data(),
+                      dg->h_w_train.data(), out->hdr[b], lay_h.data() + e0);
+    }
+    if (err == 2) throw Error(SP_ERR_CONFIG, "template is not in topological order");
+    if (err == 3) throw Error(SP_ERR_UNSUPPORTED, "a template node has more than 6 internal producers");
+    offsets();
+    tr.mark("host layout");
+    PackedUpload pk;
+    const size_t o_off = pk.add(out->tmpl_off.data(), (nb + 1) * sizeof(int64_t));
+    const size_t o_nodes = pk.add(out->tmpl_nodes.data(), ne * sizeof(int32_t));
+    const size_t o_slot = pk.add(slot_of.data(), ne * sizeof(slot_of[0]));
+    const size_t o_ref = pk.add(ref_slot_of.data(), ne * sizeof(ref_slot_of[0]));
+    const size_t o_hdr = pk.add(out->hdr.data(), nb * sizeof(BlobHeader));
+    const size_t o_lay = pk.add(lay_h.data(), ne * sizeof(EntryLayout));
+    const size_t o_nb = pk.add(nblk.data(), n * sizeof(int32_t));
+    const size_t o_tp = pk.add(ntpos.data(), n * sizeof(int32_t));
+    const size_t o_fl = pk.add(flags.data(), 2 * (size_t)n);
+    const size_t o_blob = pk.add(out->blob_off.data(), (nb + 1) * sizeof(int64_t));
+    const size_t o_x = pk.add(xo.data(), (nb + 1) * sizeof(int64_t));
+    const size_t o_e = pk.add(out->edge_off.data(), (nb + 1) * sizeof(int64_t));
+    uint8_t* a = priv->upload(pk, priv->arena, s);
+    out->d_tmpl_off.set_view((int64_t*)(a + o_off), nb + 1);
+    out->d_tmpl_nodes.set_view((int32_t*)(a + o_nodes), ne);
+    D.slot_of.set_view((decltype(D.slot_of.p))(a + o_slot), ne);
+    D.ref_slot_of.set_view((decltype(D.ref_slot_of.p))(a + o_ref), ne);
+    hdr.set_view((BlobHeader*)(a + o_hdr), nb);
+    lay.set_view((EntryLayout*)(a + o_lay), ne);
+    D.node_block.set_view((int32_t*)(a + o_nb), n);
+    D.node_tpos.set_view((int32_t*)(a + o_tp), n);
+    D.has_cons.set_view(a + o_fl, n);
+    D.ext_cons.set_view(a + o_fl + n, n);
+    out->d_blob_off.set_view((int64_t*)(a + o_blob), nb + 1);
+    D.xoff.set_view((int64_t*)(a + o_x), nb + 1);
+    D.edge_off.set_view((int64_t*)(a + o_e), nb + 1);
+    tr.mark("upload");
+  } else {
   // the host-built arrays in one H2D (pinned staging, packed arena)
   DevBuf<uint8_t> radix_d;
-  DevBuf<BlobHeader> hdr;
   {
     PackedUpload pk;
     const size_t o_off = pk.add(out->tmpl_off.data(), (nb + 1) * sizeof(int64_t));
@@ -2999,10 +3175,8 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   if (nb > 0)
     SP_LAUNCH(ctx, k_mark_blocks, (int)std::min<int64_t>(nb, 65535), 128, 0, s, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb,
                                                                   D.node_block.p, D.node_tpos.p, err);
-  const GraphView G = view_of(dg);
   SP_LAUNCH(ctx, k_boundary, grid_for(n, ctx->sm_count), 256, 0, s, G, n, D.node_block.p, D.has_cons.p, D.ext_cons.p);
   tr.mark("mark+boundary");
-  DevBuf<EntryLayout> lay;
   DevBuf<int64_t> blob_bytes;
   lay.alloc(ne, s);
   blob_bytes.alloc(nb + 1, s);
@@ -3029,42 +3203,36 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   if (err_h[0] == 2) throw Error(SP_ERR_CONFIG, "template is not in topological order");
   if (err_h[0] == 3)
     throw Error(SP_ERR_UNSUPPORTED, "a template node has more than 6 internal producers");
-  out->max_blob = 0;
-  out->max_pool = 0;
-  out->blob_off.assign(nb + 1, 0);
-  out->edge_off.assign(nb + 1, 0);
-  for (int64_t b = 0; b < nb; b++) {
-    out->max_blob = std::max<int64_t>(out->max_blob, out->hdr[b].bytes);
-    out->max_pool = std::max(out->max_pool, out->hdr[b].npool);
-    out->blob_off[b + 1] = out->blob_off[b] + out->hdr[b].bytes;
-    out->edge_off[b + 1] = out->edge_off[b] + out->hdr[b].n_prod;
+  offsets();
+  PackedUpload pk;
+  const size_t o_blob = pk.add(out->blob_off.data(), (nb + 1) * sizeof(int64_t));
+  const size_t o_x = pk.add(xo.data(), (nb + 1) * sizeof(int64_t));
+  const size_t o_e = pk.add(out->edge_off.data(), (nb + 1) * sizeof(int64_t));
+  uint8_t* a = priv->upload(pk, priv->arena2, s);
+  out->d_blob_off.set_view((int64_t*)(a + o_blob), nb + 1);
+  D.xoff.set_view((int64_t*)(a + o_x), nb + 1);
+  D.edge_off.set_view((int64_t*)(a + o_e), nb + 1);
   }
   tr.mark("offsets");
   out->blobs.alloc(std::max<int64_t>(out->blob_off[nb], 16), s);
   D.bound.alloc(ne, s);
-  {
-    std::vector<int64_t> xo(nb + 1, 0);
-    for (int64_t b = 0; b < nb; b++)
-      xo[b + 1] = xo[b] + align16((int64_t)sizeof(XNode) * out->hdr[b].T + (int64_t)sizeof(XEdge) * out->hdr[b].n_prod);
-    D.xinfo.alloc(std::max<int64_t>(xo[nb], 16), s);
-    PackedUpload pk;
-    const size_t o_blob = pk.add(out->blob_off.data(), (nb + 1) * sizeof(int64_t));
-    const size_t o_x = pk.add(xo.data(), (nb + 1) * sizeof(int64_t));
-    const size_t o_e = pk.add(out->edge_off.data(), (nb + 1) * sizeof(int64_t));
-    uint8_t* a = priv->upload(pk, priv->arena2, s);
-    out->d_blob_off.set_view((int64_t*)(a + o_blob), nb + 1);
-    D.xoff.set_view((int64_t*)(a + o_x), nb + 1);
-    D.edge_off.set_view((int64_t*)(a + o_e), nb + 1);
-  }
+  D.xinfo.alloc(std::max<int64_t>(xo[nb], 16), s);
   tr.mark("alloc+upload2");
   if (nb > 0)
-    SP_LAUNCH(ctx, k_fill, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
+    SP_LAUNCH(ctx, k_fill, (int)std::min<int64_t>(nb, 65535), 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
               D.node_tpos.p, D.slot_of.p, D.ref_slot_of.p, lay.p, hdr.p, out->d_blob_off.p, D.has_cons.p, D.ext_cons.p, *mesh, mu,
               chunk, out->blobs.p, D.bound.p, D.xinfo.p, D.xoff.p);
   SP_CUDA(cudaGetLastError());
   {
     TablesPriv* tp = (TablesPriv*)out->priv;
-    if (!tp->built) SP_CUDA(cudaEventCreateWithFlags(&tp->built, cudaEventDisableTiming));
+    if (!tp->built) {
+      if (!ctx->event_pool.empty()) {
+        tp->built = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+      } else {
+        SP_CUDA(cudaEventCreate(&tp->built));
+      }
+    }
     SP_CUDA(cudaEventRecord(tp->built, s));
   }
   tr.mark("fill launch");
@@ -3438,6 +3606,7 @@ static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& r
   pd.active = false;
   res.assign(nb, sp_score_out{});
   SP_CUDA(cudaEventSynchronize(pd.ev[5]));
+  pd.synced = true;
   if (pd.empty) return;
   if (fx && !pd.explain) throw Error(SP_ERR_CONFIG, "winner detail requested but not enqueued");
   std::memcpy(res.data(), pd.host, (size_t)nb * sizeof(sp_score_out));

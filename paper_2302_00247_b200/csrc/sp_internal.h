@@ -251,6 +251,7 @@ struct sp_ctx {
   int32_t fold_levels = 0;
   int64_t own_launches = 0, cub_calls = 0;
   int skip = 1;  // exact prefix-failure skipping in sp_score / sp_search
+  int host_layout = 1;  // small graphs: table layout on the host (SP_OPT_HOST_LAYOUT)
   int memo = 0;  // with skip off: memoised brute force (re-route only dirty nodes); off: walk
   cudaEvent_t timer[2] = {};
   cudaEvent_t trace[4] = {};  // SP_SCORE_TRACE: reduce / explain / d2h boundaries
@@ -339,6 +340,8 @@ inline int resident_ctas(sp_ctx* ctx, K* kern, int threads, size_t smem) {
 }  // namespace sp
 
 // Device-resident lowered graph (+ the host copies the library needs).
+constexpr int64_t SP_HOST_LAYOUT_MAX = 8192;
+
 struct sp_dgraph {
   sp_ctx* ctx = nullptr;
   int64_t n = 0, E = 0;
@@ -347,6 +350,12 @@ struct sp_dgraph {
   sp::PodVec<uint8_t> h_names;  // filled by graph_upload's parallel copies (no zero fill)
   sp::PodVec<int64_t> h_name_off, h_topo;
   sp::PodVec<uint8_t> h_op, h_w_rank;
+  // graphs of <= SP_HOST_LAYOUT_MAX nodes also keep the producer CSR and the
+  // trainable flags: their table layout is computed on the host (no device
+  // round trip between the fold and the fill)
+  sp::PodVec<int64_t> h_in_off;
+  sp::PodVec<int32_t> h_in_idx;
+  sp::PodVec<uint8_t> h_w_train;
   // device copies: views into one arena filled by a single H2D copy
   sp::DevBuf<uint8_t> arena;
   template <class T>

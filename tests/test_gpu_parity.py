@@ -820,3 +820,44 @@ def test_table_driven_explain_equals_route_node_explain(backend, seed, monkeypat
                 assert np.array_equal(fast[2][k0:k1], slow[2][k0:k1])
     finally:
         t.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_host_layout_equals_device_layout(backend, seed):
+    """Small graphs lay their tables out on the host (SP_OPT_HOST_LAYOUT); the
+    device layout (every graph above 8192 nodes) must build the same tables:
+    same per-candidate totals, same search results, same derive_plan JSON."""
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, derive_plan, fold_blocks
+    from randgraph import random_graph
+
+    g = random_graph(seed, n_types=4, reps=(2, 6), ops=(3, 11))
+    low = lower(g)
+    mname, kw = MESHES[seed % len(MESHES)]
+    m = ClusterSpec.from_mesh(mname, **kw)
+    mu, chunk = ((1 << 20, 4 << 20), (64, 256), (8, 8))[seed % 3]
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 2, session=ses)
+    off, nodes = ba.templates_csr()
+    got = {}
+    try:
+        for host in (True, False):
+            backend.set_host_layout(host)
+            t = backend.tables(ses.dgraph, off, nodes, m, mu, chunk)
+            try:
+                if t.overflow:
+                    pytest.skip("random block beyond u64")
+                res = backend.score(t)
+                rows = [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total) for r in res]
+                totals = []
+                for b in range(ba.n_blocks):
+                    C = int(t.candidates[b])
+                    totals.append(backend.score_range(t, b, 0, min(C, 2048), want_totals=True)[1].tobytes())
+            finally:
+                t.close()
+            rep = derive_plan(g, m, mu=mu, chunk_size=chunk, backend=backend)
+            got[host] = (rows, totals, canon(rep.to_json()))
+    finally:
+        backend.set_host_layout(True)
+    assert got[True] == got[False]

@@ -388,6 +388,14 @@ int sp_fold_stats(const sp_ctx* ctx, double* device_ms, int32_t* levels);
  * device layout for every graph (same tables).
  */
 #define SP_OPT_HOST_LAYOUT 3
+/*
+ * SP_OPT_SIM_SHARD (measurement only, default 0): value (N << 16) | r makes
+ * every single-device search score only rank r's share of an N-rank search,
+ * with the winner detail chained on the device as after the multi-GPU merge:
+ * one rank's step of the in-library multi-process search, simulated on one
+ * GPU (the results are that share's, not the whole search's).  0: off.
+ */
+#define SP_OPT_SIM_SHARD 4
 int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value);
 
 /* CUDA-event timer on the context's stream (brackets whole API calls for benchmarks). */

@@ -461,6 +461,14 @@ class Backend:
         """Table layout of small graphs on the host (default on); off: on the device."""
         self._check(self.lib.sp_set_option(self.ctx, 3, 1 if on else 0), "sp_set_option")
 
+    def set_sim_shard(self, rank: int, nranks: int) -> None:
+        """Measurement only (tools/shard_sim.py): every search scores rank `rank`'s
+        share of an `nranks`-rank search, winner detail chained on the device as
+        after the multi-GPU merge.  (0, 1) turns it off."""
+        v = 0 if nranks <= 1 else (int(nranks) << 16) | int(rank)
+        self._check(self.lib.sp_set_option(self.ctx, 4, v), "sp_set_option")
+        self.sim_nranks = max(1, int(nranks))
+
     def set_mode(self, mode: str) -> None:
         """'skip' (default), 'memo' (every candidate visited, dirty nodes re-routed)
         or 'walk' (every node of every candidate)."""

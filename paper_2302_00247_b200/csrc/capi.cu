@@ -536,6 +536,16 @@ int sp_set_option(sp_ctx* ctx, int32_t option, int64_t value) {
     }
     return SP_OK;
   }
+  if (option == SP_OPT_SIM_SHARD) {
+    const int32_t n = (int32_t)(value >> 16), r = (int32_t)(value & 0xFFFF);
+    if (value && (n < 1 || r >= n)) {
+      ctx->last_error = "SP_OPT_SIM_SHARD: rank must be below the rank count";
+      return SP_ERR_CONFIG;
+    }
+    ctx->sim_nranks = value ? n : 1;
+    ctx->sim_rank = value ? r : 0;
+    return SP_OK;
+  }
   if (option == SP_OPT_HOST_LAYOUT) {
     for (size_t i = 0; i <= ctx->peers.size(); i++) (i ? ctx->peers[i - 1] : ctx)->host_layout = value ? 1 : 0;
     return SP_OK;

@@ -32,6 +32,10 @@ constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
 constexpr int THREADS = 256;     // scoring CTA size
 constexpr int ITEM_ITERS_MAX = 256;        // work item = THREADS * iters candidates
 constexpr int ITEM_ITERS_MAX_SKIP = 512;   // ... when prefix skipping is on
+// work items per resident CTA a search aims for (a rank's last wave of items is
+// its tail: at 8 ranks c5's 65536-candidate items left ~12 per CTA; 8 / 32 / 64 /
+// 128 per CTA: 5.65 / 4.90 / 4.71 / 4.72 ms per rank, tools/ab_items.sh)
+constexpr int ITEMS_PER_CTA = 64;
 
 __host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 __host__ __device__ inline uint32_t pow3(int k) {
@@ -185,36 +189,50 @@ __global__ void k_boundary(GraphView G, int64_t n, const int32_t* node_block, ui
     }
 }
 
-// The serial half of a block's layout (k_layout's thread 0, and the host
-// layout of small graphs): lays out the blob, assigns pool slots (linear scan;
-// a producer's slot is released at its last internal consumer) and derives
-// each node's prefix-failure skip (ancestor cone over enumeration positions).
-// k[i], last[i], prodpos[i][] are the node's internal fan-in, last internal
-// consumer and producer positions; pool / anc are scratch of T entries.
-__host__ __device__ inline void layout_serial(int T, const int* kk, const int* last, const int16_t (*prodpos)[KMAX],
-                                              int* pool, uint64_t* ancs, const int32_t* tnodes,
-                                              const int16_t* slot_of, const uint8_t* radix_of,
-                                              const uint8_t* w_rank, const uint8_t* w_train, BlobHeader& H,
-                                              EntryLayout* lay) {
+// The serial half of a block's layout (k_layout's lane 0, and the host layout
+// of small graphs): lays out the blob, assigns pool slots (linear scan; a
+// producer's slot is released at its last internal consumer) and derives each
+// node's prefix-failure skip (ancestor cone over enumeration positions).
+// Per template position i: kk[i] internal fan-in, prodpos[i][] producer
+// positions, rel_head[i] -> rel_next[] the producers whose last internal
+// consumer is i, slot_of / radix_of its enumeration slot and radix, trainw
+// whether it holds a trainable weight.  pool / ancs: scratch of T entries,
+// suf: scratch of V + 1.  Every input is read from the caller's (shared)
+// arrays: the walk has no global-memory dependency chain.
+template <class IDX>
+__host__ __device__ inline void layout_serial(int T, const IDX* kk, const int* last, const int16_t (*prodpos)[KMAX],
+                                              const int* rel_head, const IDX* rel_next, IDX* pool, uint64_t* ancs,
+                                              uint64_t* suf, const int16_t* slot_of, const uint8_t* radix_of,
+                                              const uint8_t* trainw, BlobHeader& H, EntryLayout* lay) {
   const int V = H.V;
   int nprod = 0, nt = 0;
   int64_t nent = 0, ndbl = 0, nent4 = 0;
   uint32_t used[MAXT / 32];
   for (int w = 0; w < MAXT / 32; w++) used[w] = 0;
+  // suffix products of the enumeration radices: skip_R = suf[skip_m + 1]
+  suf[V > 0 ? V : 0] = 1;
+  for (int q = V - 1; q >= 0; q--) suf[q] = suf[q + 1] * (((H.radix3 >> q) & 1) ? 3 : 2);
   int npool = 0;
   for (int i = 0; i < T; i++) {
     // release producers whose last internal consumer is i
-    for (int j = 0; j < i; j++)
-      if (last[j] == i && pool[j] >= 0) used[pool[j] >> 5] &= ~(1u << (pool[j] & 31));
+    for (int j = rel_head[i]; j >= 0; j = rel_next[j])
+      if (pool[j] >= 0) used[pool[j] >> 5] &= ~(1u << (pool[j] & 31));
     pool[i] = -1;
     if (last[i] >= 0) {
       int sl = 0;
-      while (used[sl >> 5] & (1u << (sl & 31))) sl++;
+      for (int w = 0; w < MAXT / 32; w++)
+        if (~used[w]) {
+#ifdef __CUDA_ARCH__
+          sl = w * 32 + __ffs(~used[w]) - 1;
+#else
+          sl = w * 32 + __builtin_ctz(~used[w]);
+#endif
+          break;
+        }
       used[sl >> 5] |= 1u << (sl & 31);
-      pool[i] = sl;
+      pool[i] = (IDX)sl;
       npool = npool > sl + 1 ? npool : sl + 1;
     }
-    const int32_t n = tnodes[i];
     const int k = kk[i];
     // ancestor cone over enumeration positions (V <= 64)
     uint64_t anc = slot_of[i] >= 0 ? (1ULL << slot_of[i]) : 0ULL;
@@ -228,16 +246,14 @@ __host__ __device__ inline void layout_serial(int T, const int* kk, const int* l
     L.tab4 = (int32_t)nent4;
     L.pad = 0;
     L.dbl = (int32_t)ndbl;
-    L.train_idx = (w_rank[n] && w_train[n]) ? nt++ : -1;
+    L.train_idx = trainw[i] ? nt++ : -1;
     L.out_pool = pool[i];
 #ifdef __CUDA_ARCH__
     L.skip_m = anc ? 63 - __clzll(anc) : -1;
 #else
     L.skip_m = anc ? 63 - __builtin_clzll(anc) : -1;
 #endif
-    uint64_t R = 1;
-    for (int q = L.skip_m + 1; q < V; q++) R *= ((H.radix3 >> q) & 1) ? 3 : 2;
-    L.skip_R = anc ? R : 0;
+    L.skip_R = anc ? (L.skip_m + 1 <= V ? suf[L.skip_m + 1] : 1) : 0;
     nprod += k;
     nent += (int64_t)L.nd * pow3(k < KMAX ? k : KMAX);
     nent4 += 4 * (int64_t)pow3(k < KMAX ? k : KMAX);
@@ -276,21 +292,33 @@ __host__ __device__ inline void layout_serial(int T, const int* kk, const int* l
   H.bytes = (int32_t)off;
 }
 
-// One CTA per block: per-node internal fan-in and liveness in parallel, then
-// one thread runs layout_serial.
-__global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
-                         const int32_t* node_block, const int32_t* node_tpos, const int16_t* slot_of,
-                         const uint8_t* radix_of, EntryLayout* lay, BlobHeader* hdr, int64_t* blob_bytes,
-                         int32_t* err) {
-  __shared__ int s_k[MAXT], s_last[MAXT], s_pool[MAXT];
-  __shared__ int16_t s_prodpos[MAXT][KMAX];
-  __shared__ uint64_t s_anc[MAXT];
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+constexpr int LAYOUT_WARPS = 4;
+// One WARP per block: the lanes gather each node's internal fan-in, producer
+// positions, last internal consumer, release lists, slot, radix and weight
+// flag into shared memory, then lane 0 runs layout_serial on shared memory only.
+__global__ void __launch_bounds__(32 * LAYOUT_WARPS) k_layout(GraphView G, const int64_t* tmpl_off,
+                                                             const int32_t* tmpl_nodes, int64_t nb,
+                                                             const int32_t* node_block, const int32_t* node_tpos,
+                                                             const int16_t* slot_of, const uint8_t* radix_of,
+                                                             EntryLayout* lay, BlobHeader* hdr, int64_t* blob_bytes,
+                                                             int32_t* err) {
+  __shared__ int s_last[LAYOUT_WARPS][MAXT], s_head[LAYOUT_WARPS][MAXT];
+  __shared__ int16_t s_k[LAYOUT_WARPS][MAXT], s_next[LAYOUT_WARPS][MAXT], s_pool[LAYOUT_WARPS][MAXT];
+  __shared__ int16_t s_prodpos[LAYOUT_WARPS][MAXT][KMAX];
+  __shared__ uint64_t s_anc[LAYOUT_WARPS][MAXT];
+  __shared__ uint64_t s_suf[LAYOUT_WARPS][65];
+  __shared__ int16_t s_slot[LAYOUT_WARPS][MAXT];
+  __shared__ uint8_t s_rad[LAYOUT_WARPS][MAXT], s_tw[LAYOUT_WARPS][MAXT];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t b = (int64_t)blockIdx.x * LAYOUT_WARPS + w; b < nb; b += (int64_t)gridDim.x * LAYOUT_WARPS) {
     const int64_t e0 = tmpl_off[b];
     const int T = (int)(tmpl_off[b + 1] - e0);
-    for (int i = threadIdx.x; i < T; i += blockDim.x) s_last[i] = -1;
-    __syncthreads();
-    for (int i = threadIdx.x; i < T; i += blockDim.x) {
+    for (int i = lane; i < T; i += 32) {
+      s_last[w][i] = -1;
+      s_head[w][i] = -1;
+    }
+    __syncwarp();
+    for (int i = lane; i < T; i += 32) {
       const int32_t n = tmpl_nodes[e0 + i];
       int k = 0;
       for (int64_t e = G.in_off[n]; e < G.in_off[n + 1]; e++) {
@@ -298,22 +326,28 @@ __global__ void k_layout(GraphView G, const int64_t* tmpl_off, const int32_t* tm
         if (node_block[r] != (int32_t)b) continue;
         const int j = node_tpos[r];
         if (j >= i) atomicExch(err, 2);  // template not topologically ordered
-        atomicMax(&s_last[j], i);
-        if (k < KMAX) s_prodpos[i][k] = (int16_t)j;
+        else atomicMax(&s_last[w][j], i);
+        if (k < KMAX) s_prodpos[w][i][k] = (int16_t)j;
         k++;
       }
       if (k > KMAX) atomicExch(err, 3);
-      s_k[i] = k;
+      s_k[w][i] = (int16_t)k;
+      s_slot[w][i] = slot_of[e0 + i];
+      s_rad[w][i] = radix_of[e0 + i];
+      s_tw[w][i] = (G.w_rank[n] && G.w_train[n]) ? 1 : 0;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    __syncwarp();
+    for (int j = lane; j < T; j += 32)
+      if (s_last[w][j] >= 0) s_next[w][j] = (int16_t)atomicExch(&s_head[w][s_last[w][j]], j);
+    __syncwarp();
+    if (lane == 0 && *(volatile int32_t*)err == 0) {
       BlobHeader H = hdr[b];
-      layout_serial(T, s_k, s_last, s_prodpos, s_pool, s_anc, tmpl_nodes + e0, slot_of + e0, radix_of + e0,
-                    G.w_rank, G.w_train, H, lay + e0);
+      layout_serial(T, s_k[w], s_last[w], s_prodpos[w], s_head[w], s_next[w], s_pool[w], s_anc[w], s_suf[w],
+                    s_slot[w], s_rad[w], s_tw[w], H, lay + e0);
       hdr[b] = H;
       blob_bytes[b] = H.bytes;
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
@@ -2325,6 +2359,67 @@ __global__ void k_reduce(const ItemOut* __restrict__ items, const unsigned long 
   }
 }
 
+// First pass of the two-pass item reduction (blocks with many items: one CTA
+// reducing a block's 50k items serially cost 0.13 ms on c5): CTA c reduces
+// chunk c of REDUCE_CHUNK consecutive items of one block into partial[c]
+// (argmin key + summed valid count); k_reduce then merges each block's
+// partials (chunk_base[b] .. chunk_base[b + 1]).
+constexpr int REDUCE_CHUNK = 1024;
+__global__ void __launch_bounds__(THREADS) k_reduce_chunks(const ItemOut* __restrict__ items,
+                                                           const unsigned long long* __restrict__ item_base,
+                                                           const unsigned long long* __restrict__ chunk_base,
+                                                           int64_t nb, unsigned long long n_chunks,
+                                                           ItemOut* __restrict__ partial) {
+  __shared__ ItemOut s_w[THREADS / 32];
+  for (unsigned long long c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+    int64_t lo = 0, hi = nb;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) / 2;
+      if (chunk_base[mid] <= c) lo = mid;
+      else hi = mid;
+    }
+    const unsigned long long i0 = item_base[lo] + (c - chunk_base[lo]) * REDUCE_CHUNK;
+    const unsigned long long i1 = min(i0 + REDUCE_CHUNK, item_base[lo + 1]);
+    ItemOut acc{~0ULL, ~0ULL, 0xFFFFFFFFu, 0};
+    unsigned long long valid = 0;
+    for (unsigned long long it = i0 + threadIdx.x; it < i1; it += blockDim.x) {
+      const ItemOut o = items[it];
+      valid += o.valid;
+      if (key_less(o.total_bits, o.num_split, o.index, acc.total_bits, acc.num_split, acc.index)) acc = o;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, acc.total_bits, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, acc.index, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, acc.num_split, o);
+      valid += __shfl_down_sync(0xffffffffu, valid, o);
+      if (key_less(t2, n2, i2, acc.total_bits, acc.num_split, acc.index)) {
+        acc.total_bits = t2;
+        acc.num_split = n2;
+        acc.index = i2;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      acc.valid = valid;
+      s_w[threadIdx.x >> 5] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ItemOut r = s_w[0];
+      for (int w = 1; w < THREADS / 32; w++) {
+        r.valid += s_w[w].valid;
+        if (key_less(s_w[w].total_bits, s_w[w].num_split, s_w[w].index, r.total_bits, r.num_split, r.index)) {
+          r.total_bits = s_w[w].total_bits;
+          r.num_split = s_w[w].num_split;
+          r.index = s_w[w].index;
+        }
+      }
+      partial[c] = r;
+    }
+    __syncthreads();
+  }
+}
+
 // Full detail of one candidate (RoutedPlan + CostReport), single thread.
 __global__ void k_explain(GraphView G, const int32_t* tmpl, int T, int32_t blk, const int32_t* node_block,
                           const int32_t* node_tpos, const int16_t* slot_of, const uint8_t* digits,
@@ -3082,14 +3177,15 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
         if (nblk[c] != nblk[p] || nblk[p] < 0) flags[n + p] = 1;
       }
     std::vector<EntryLayout> lay_h(std::max<int64_t>(ne, 1));
-    std::vector<int> kk(MAXT), last(MAXT), pool(MAXT);
-    std::vector<uint64_t> ancs(MAXT);
+    std::vector<int> last(MAXT), head(MAXT), kk(MAXT), nxt(MAXT), pool(MAXT);
+    std::vector<uint64_t> ancs(MAXT), suf(65);
     std::vector<int16_t> pp((size_t)MAXT * KMAX);
+    std::vector<uint8_t> tw(MAXT);
     int err = 0;
     for (int64_t b = 0; b < nb && !err; b++) {
       const int64_t e0 = out->tmpl_off[b];
       const int T = (int)(out->tmpl_off[b + 1] - e0);
-      for (int i = 0; i < T; i++) last[i] = -1;
+      for (int i = 0; i < T; i++) last[i] = head[i] = -1;
       for (int i = 0; i < T; i++) {
         const int32_t v = out->tmpl_nodes[e0 + i];
         int k = 0;
@@ -3098,17 +3194,23 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
           if (nblk[r] != (int32_t)b) continue;
           const int j = ntpos[r];
           if (j >= i) err = err ? err : 2;
-          if (j < T) last[j] = std::max(last[j], i);
+          else last[j] = std::max(last[j], i);
           if (k < KMAX) pp[(size_t)i * KMAX + k] = (int16_t)j;
           k++;
         }
         if (k > KMAX) err = err ? err : 3;
         kk[i] = k;
+        tw[i] = (dg->h_w_rank[v] && dg->h_w_train[v]) ? 1 : 0;
       }
+      for (int j = 0; j < T; j++)
+        if (last[j] >= 0) {
+          nxt[j] = head[last[j]];
+          head[last[j]] = j;
+        }
       if (!err)
-        layout_serial(T, kk.data(), last.data(), (const int16_t(*)[KMAX])pp.data(), pool.data(), ancs.data(),
-                      out->tmpl_nodes.data() + e0, slot_of.data() + e0, radix_of.data() + e0, dg->h_w_rank.data(),
-                      dg->h_w_train.data(), out->hdr[b], lay_h.data() + e0);
+        layout_serial(T, kk.data(), last.data(), (const int16_t(*)[KMAX])pp.data(), head.data(), nxt.data(),
+                      pool.data(), ancs.data(), suf.data(), slot_of.data() + e0, radix_of.data() + e0, tw.data(),
+                      out->hdr[b], lay_h.data() + e0);
     }
     if (err == 2) throw Error(SP_ERR_CONFIG, "template is not in topological order");
     if (err == 3) throw Error(SP_ERR_UNSUPPORTED, "a template node has more than 6 internal producers");
@@ -3182,7 +3284,8 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t nb, const int64_t* tmpl_of
   blob_bytes.alloc(nb + 1, s);
   const int gb = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), 65535);
   if (nb > 0)
-    SP_LAUNCH(ctx, k_layout, gb, 128, 0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
+    SP_LAUNCH(ctx, k_layout, (int)std::min<int64_t>((nb + LAYOUT_WARPS - 1) / LAYOUT_WARPS, 65535), 32 * LAYOUT_WARPS,
+              0, s, G, out->d_tmpl_off.p, out->d_tmpl_nodes.p, nb, D.node_block.p,
               D.node_tpos.p, D.slot_of.p, radix_d.p, lay.p, hdr.p, blob_bytes.p, err);
   // errors + the laid-out headers back in one pinned block (the staging block is
   // free again: its H2D is ordered before these copies)
@@ -3382,7 +3485,7 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   int per_sm = resident_ctas(ctx, kern, threads, smem_k);
   if (per_sm < 1) per_sm = 1;
   const unsigned long long slots = (unsigned long long)ctx->sm_count * per_sm;
-  // size work items so each rank's grid gets ~8 items per resident CTA
+  // size work items so each rank's grid gets ~ITEMS_PER_CTA items per resident CTA
   // (dynamic balance); with prefix skipping a candidate costs far less, so
   // items may grow larger.  Ranks deal the items of every block round-robin
   // (the global item sequence, item g to rank g mod n_shards): early-exit
@@ -3397,7 +3500,9 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   for (int64_t b = 0; b < nb; b++) total += t->hdr[b].C;
   const unsigned long long cap = ctx->skip ? ITEM_ITERS_MAX_SKIP : ITEM_ITERS_MAX;
   const unsigned long long per_rank = total / N + (total % N ? 1 : 0);
-  unsigned long long iters = (per_rank + slots * 8 * THREADS - 1) / (slots * 8 * THREADS);
+  static const unsigned long long ipc = getenv("SP_ITEMS_PER_CTA") ? strtoull(getenv("SP_ITEMS_PER_CTA"), nullptr, 10)
+                                                                   : ITEMS_PER_CTA;  // (A/B override)
+  unsigned long long iters = (per_rank + slots * ipc * THREADS - 1) / (slots * ipc * THREADS);
   iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, memo ? ITEM_ITERS_MAX_SKIP : cap));
   const unsigned long long item_cands = iters * THREADS;
   std::vector<unsigned long long> lo(nb), hi(nb), base(nb + 1, 0);
@@ -3422,17 +3527,30 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     SP_CUDA(cudaEventRecord(pd.ev[3], s));
     return true;
   }
-  // one small H2D for the plan: lo | hi | base | counter
-  std::vector<unsigned long long> plan(3 * nb + 2, 0);
+  // blocks with many items reduce in two passes (chunks of REDUCE_CHUNK items, then per block)
+  unsigned long long max_items = 0;
+  for (int64_t b = 0; b < nb; b++) max_items = std::max(max_items, base[b + 1] - base[b]);
+  const bool two_pass = max_items > 2 * REDUCE_CHUNK;
+  // one small H2D for the plan: lo | hi | base | counter (| chunk_base)
+  std::vector<unsigned long long> plan(3 * nb + 2 + (two_pass ? nb + 1 : 0), 0);
   std::copy(lo.begin(), lo.end(), plan.begin());
   std::copy(hi.begin(), hi.end(), plan.begin() + nb);
   std::copy(base.begin(), base.end(), plan.begin() + 2 * nb);
+  unsigned long long n_chunks = 0;
+  if (two_pass) {
+    unsigned long long* cb = plan.data() + 3 * nb + 2;
+    for (int64_t b = 0; b < nb; b++) {
+      cb[b] = n_chunks;
+      n_chunks += (base[b + 1] - base[b] + REDUCE_CHUNK - 1) / REDUCE_CHUNK;
+    }
+    cb[nb] = n_chunks;
+  }
   DevBuf<unsigned long long>& dplan = pd.dplan;
   DevBuf<ItemOut>& items = pd.items;
   DevBuf<sp_score_out>& dout = pd.dout;
   tr.mark("plan");
   dplan.upload(plan.data(), plan.size(), s);
-  items.alloc(n_items, s);
+  items.alloc(n_items + n_chunks, s);  // (partials of the two-pass reduction behind the items)
   alloc_dout(pd, t, s, must_out);
   tr.mark("upload+alloc");
   unsigned long long* counter = dplan.p + 3 * nb + 1;
@@ -3443,8 +3561,16 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   SP_LAUNCH(ctx, kern, (unsigned)grid, threads, smem_k, s, t->blobs.p, P, items.p, counter);
   SP_CUDA(cudaEventRecord(pd.ev[2], s));
   tr.mark("score launch");
-  SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
-            dout.p);
+  if (two_pass) {
+    const unsigned long long* d_cb = dplan.p + 3 * nb + 2;
+    SP_LAUNCH(ctx, k_reduce_chunks, (unsigned)std::min<unsigned long long>(n_chunks, 65535), THREADS, 0, s, items.p,
+              dplan.p + 2 * nb, d_cb, nb, n_chunks, items.p + n_items);
+    SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p + n_items, d_cb, nb,
+              dout.p);
+  } else {
+    SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
+              dout.p);
+  }
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaEventRecord(pd.ev[3], s));
   return true;
@@ -3452,6 +3578,22 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
 
 // Enqueue the winner detail (when `explain`) and the copy of the per-block
 // results (+ detail) into a pinned host block behind pd.dout.
+// SP_OPT_SIM_SHARD only: blocks without a valid candidate in this share take
+// the all-replica plan (index 0)
+__global__ void k_sim_replica(int64_t nb, sp_score_out* __restrict__ out) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    if (!out[b].has_best) {
+      out[b].has_best = 1;
+      out[b].best_index = 0;
+      out[b].best_num_split = 0;
+      out[b].best_total = -1.0;  // k_sim_totals: the all-replica plan's total from its detail
+    }
+}
+__global__ void k_sim_totals(int64_t nb, const ExplainBlock* __restrict__ x, sp_score_out* __restrict__ out) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    if (out[b].best_total < 0.0) out[b].best_total = x[b].total;
+}
+
 static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
@@ -3469,6 +3611,9 @@ static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
       pd.dedge.alloc(2 * std::max<int64_t>(nedge, 1), s);
     }
     launch_explain(ctx, t, s, priv->dev.edge_off.p, nullptr, dout.p, pd.dblk.p, pd.dnode.p, pd.dedge.p);
+    if (ctx->sim_nranks > 1)
+      SP_LAUNCH(ctx, k_sim_totals, (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + 255) / 256, 1024)), 256, 0,
+                s, nb, pd.dblk.p, dout.p);
   }
   SP_CUDA(cudaEventRecord(pd.ev[4], s));
   // results (and winner detail) to the pinned block now: collecting this
@@ -3654,6 +3799,27 @@ void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bo
   pending_begin(ctx, t);
   if (ctx->comm) {  // one process per GPU: this rank's share, NCCL exchange (also at nranks 1)
     score_enqueue_lanes({ctx}, {t}, {ctx->rank}, ctx->nranks, explain);
+    return;
+  }
+  if (ctx->sim_nranks > 1 && n_shards == 1) {
+    // measurement (tools/shard_sim.py): this rank's share of an sim_nranks-rank
+    // search, then what the NCCL form does after its all-gather -- here a copy
+    // of this rank's records stands in for the gathered ones -- k_merge_ranks
+    // and the winner detail chained on the device.  A block this share has no
+    // valid candidate for takes the all-replica plan (index 0, which always
+    // routes) so the host assembles a report as rank 0 would.
+    PendingScore& pd = ((TablesPriv*)t->priv)->pending;
+    pd.explain = explain;
+    score_items(ctx, t, ctx->sim_rank, ctx->sim_nranks, true);
+    const int64_t nb = t->n_blocks;
+    pd.gath.alloc((size_t)std::max<int64_t>(nb, 1), ctx->stream);
+    SP_CUDA(cudaMemcpyAsync(pd.gath.p, pd.dout.p, (size_t)nb * sizeof(sp_score_out), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nb + THREADS - 1) / THREADS, 1024));
+    SP_LAUNCH(ctx, k_merge_ranks, grid, THREADS, 0, ctx->stream, pd.gath.p, 1, nb, pd.dout.p);
+    SP_LAUNCH(ctx, k_sim_replica, grid, THREADS, 0, ctx->stream, nb, pd.dout.p);
+    SP_CUDA(cudaGetLastError());
+    score_results(ctx, t, explain);
     return;
   }
   score_enqueue(ctx, t, shard, n_shards, explain);

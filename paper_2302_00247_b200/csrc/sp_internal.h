@@ -252,6 +252,7 @@ struct sp_ctx {
   int64_t own_launches = 0, cub_calls = 0;
   int skip = 1;  // exact prefix-failure skipping in sp_score / sp_search
   int host_layout = 1;  // small graphs: table layout on the host (SP_OPT_HOST_LAYOUT)
+  int sim_rank = 0, sim_nranks = 1;  // SP_OPT_SIM_SHARD (measurement only)
   int memo = 0;  // with skip off: memoised brute force (re-route only dirty nodes); off: walk
   cudaEvent_t timer[2] = {};
   cudaEvent_t trace[4] = {};  // SP_SCORE_TRACE: reduce / explain / d2h boundaries

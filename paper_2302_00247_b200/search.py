@@ -1088,6 +1088,26 @@ def _plan_searches(ses: Session, csr, mesh, mu, chunk_size, shard, n_shards, exc
             raise
 
 
+def _launch_all(searches: list) -> None:
+    """Launch the searches of _plan_searches in order."""
+    try:
+        if len(searches) > 1 and not searches[0][0].explain:
+            # sharded: the cheap group's winners are merged across ranks and
+            # re-routed BEFORE the expensive launch -- once that persistent
+            # kernel holds every SM, the re-routing kernel could not start
+            searches[0][0].launch()
+            searches[0][0].fetch(explain_now=True)
+            for srch, _ in searches[1:]:
+                srch.launch()
+        else:
+            for srch, _ in searches:
+                srch.launch()
+    except BaseException:
+        for srch, _ in searches:
+            srch.tables.close()
+        raise
+
+
 #: graphs up to this many GraphNodes (the one-CTA fold) take the one-call path
 SMALL_PLAN_NODES = 8192
 
@@ -1167,31 +1187,24 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
         first.collect(graph, subgraphs_from_blocks(ses.low, ba, types)[:1], False, types)
         raise AssertionError("unreachable: block 0 raises BadConfig or the all-replica assertion")
     searches = _plan_searches(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange)
-    try:
-        if len(searches) > 1 and not searches[0][0].explain:
+    _launch_all(searches)
+    if root_only and not ses.backend.is_root:
             # sharded: the cheap group's winners are merged across ranks and
             # re-routed BEFORE the expensive launch -- once that persistent
             # kernel holds every SM, the re-routing kernel could not start
-            searches[0][0].launch()
-            searches[0][0].fetch(explain_now=True)
-            for srch, _ in searches[1:]:
-                srch.launch()
-        else:
-            for srch, _ in searches:
-                srch.launch()
-    except BaseException:
-        for srch, _ in searches:
-            srch.tables.close()
-        raise
-    if root_only and not ses.backend.is_root:
+
         # a non-root rank of a multi-process search: its share is scored and
         # exchanged on the device; the report is rank 0's
+        t3 = time.perf_counter()
         try:
             for srch, _ in searches:
                 srch.fetch()
         finally:
             for srch, _ in searches:
                 srch.tables.close()
+        LAST_PHASES.clear()
+        LAST_PHASES.update(path="general", session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
+                           launch_ms=(t3 - t2) * 1e3, collect_ms=(time.perf_counter() - t3) * 1e3)
         return None
     # host work that does not depend on the winners overlaps the device search:
     # Subgraph objects, the static part of every RoutedPlan, and the member
@@ -1218,6 +1231,7 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     terms = [0.0] * n_blocks
     labs = [None] * n_blocks
     candidates = valid = 0
+    marks = []
     try:
         for srch, ids in searches:
             if len(searches) == 1:
@@ -1238,6 +1252,9 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
                     terms[i] = res.best.cost.total * subs[i].multiplicity
                     if slots.off[i + 1] > slots.off[i]:
                         labs[i] = [spec.label for _, spec in res.best.plan.assignments]
+            fetched = getattr(srch, "_fetched", None)
+            marks.append(round((fetched[2] - t0) * 1e3, 3) if fetched else None)
+            marks.append(round((time.perf_counter() - t0) * 1e3, 3))
     finally:
         for srch, _ in searches:  # a group whose collect never ran (an earlier one raised)
             srch.tables.close()
@@ -1258,7 +1275,8 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
     LAST_PHASES.update(path="general", session_ms=(t1 - t0) * 1e3, fold_ms=(t2 - t1) * 1e3,
                        launch_ms=(t3 - t2) * 1e3, overlap_host_ms=(t4 - t3) * 1e3,
                        subgraphs_ms=(t3a - t3) * 1e3, route_prep_ms=(t3b - t3a) * 1e3,
-                       collect_ms=(t5 - t4) * 1e3, assemble_ms=(time.perf_counter() - t5) * 1e3)
+                       collect_ms=(t5 - t4) * 1e3, assemble_ms=(time.perf_counter() - t5) * 1e3,
+                       groups_at_ms=marks)
     return types.BestPlanReport(mesh, min_duplicates, results, assignments, total_cost, candidates,
                                 valid)
 

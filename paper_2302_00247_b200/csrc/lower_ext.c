@@ -1190,12 +1190,19 @@ static PyObject* block_instances(PyObject* self, PyObject* args) {
         PyTuple_SET_ITEM(tup, t, s);
       }
       mo += T[b];
+      /* tuples of strings cannot be part of a reference cycle: untracked now,
+         as the collector would untrack them at its first pass over them
+         (_PyTuple_MaybeUntrack) -- the pass itself (~10^5 referents for c5)
+         is then never paid */
+      PyObject_GC_UnTrack(tup);
       PyObject* pair = PyTuple_Pack(2, pre, tup);
       Py_DECREF(pre);
       Py_DECREF(tup);
       if (!pair) goto fail;
+      PyObject_GC_UnTrack(pair);
       PyTuple_SET_ITEM(insts, i, pair);
     }
+    PyObject_GC_UnTrack(insts);
   }
   goto done;
 fail:

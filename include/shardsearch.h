@@ -295,7 +295,8 @@ int sp_route_search(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t*
  * search and the winners' detail (sp_search), with no host round trip in
  * between beyond the fold's and the table layout's own.  The result holds the
  * fold arrays, the template CSR and sp_search's outputs; sp_plan_view points
- * into it until sp_plan_free.  Single-device contexts only (SP_ERR_CONFIG on a
+ * into it until sp_plan_free -- into ONE contiguous block, the arrays in the
+ * view's field order, each 16-byte aligned (a caller may map it as a whole).  Single-device contexts only (SP_ERR_CONFIG on a
  * sharded one).  SP_ERR_UNSUPPORTED when a block is beyond the table path (a
  * template of more than SP_EXPLAIN_MAX_T nodes, more than 6 internal
  * producers, tables larger than shared memory, more than 2**64 candidates):

@@ -169,8 +169,24 @@ def make_sp_graph(low) -> SpGraph:
     return g
 
 
+_MESH_CACHE: dict = {}
+
+
 def make_sp_mesh(mesh) -> SpMesh:
-    """SpMesh from a ClusterSpec-like object (costmodel.py:36-119)."""
+    """SpMesh from a ClusterSpec-like object (costmodel.py:36-119); cached for
+    hashable (frozen, value-hashed) specs."""
+    try:
+        hit = _MESH_CACHE.get(mesh)
+    except TypeError:  # unhashable spec: built every call
+        return _build_sp_mesh(mesh)
+    if hit is None:
+        if len(_MESH_CACHE) > 64:
+            _MESH_CACHE.clear()
+        hit = _MESH_CACHE[mesh] = _build_sp_mesh(mesh)
+    return hit
+
+
+def _build_sp_mesh(mesh) -> SpMesh:
     eff = {}
     for kind, val in mesh.efficiency:
         eff[kind.value if hasattr(kind, "value") else str(kind)] = float(val)

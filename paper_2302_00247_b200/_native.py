@@ -273,17 +273,36 @@ class Backend:
         owner = _Handle(self, h, self.lib.sp_plan_free)
         v = _abi.SpPlanView()
         self._check(self.lib.sp_plan_view_get(h, C.byref(v)), "sp_plan_view_get")
-        ba = BlockArrays.from_dict(_abi.blocks_to_numpy(v.blocks, owner))
-        nb, ne, nedge = v.blocks.n_blocks, v.n_entries, v.n_edges
-        toff = _abi.view_array(v.tmpl_off, nb + 1, np.int64, owner)
-        tnodes = _abi.view_array(v.tmpl_nodes, ne, np.int32, owner)
-        recs = (SpScoreOut * max(nb, 1)).from_address(C.addressof(v.scores.contents))
+        bv = v.blocks
+        nb, ni, nm, ne, nedge = bv.n_blocks, bv.n_instances, bv.n_members, v.n_entries, v.n_edges
+        # the view's arrays are one contiguous block (16-byte aligned parts in
+        # field order, include/shardsearch.h): one buffer, then numpy slices
+        sizes = (8 * nb, 8 * (nb + 1), 8 * (nb + 1), 8 * ni, 8 * ni, 4 * nm, 8 * (nb + 1), 4 * ne,
+                 C.sizeof(SpScoreOut) * max(nb, 1), C.sizeof(SpExplainBlock) * max(nb, 1), max(4 * ne, 1),
+                 max(2 * nedge, 1), 8 * (nb + 1))
+        offs, tot = [], 0
+        for z in sizes:
+            offs.append(tot)
+            tot += (z + 15) & ~15
+        base = C.addressof(bv.block_T.contents)
+        buf = (C.c_char * tot).from_address(base)
+        buf.owner = owner
+        a = np.frombuffer(buf, np.uint8)
+        a.flags.writeable = False
+        part = lambda i, n, dt: a[offs[i]:offs[i] + n * np.dtype(dt).itemsize].view(dt)  # noqa: E731
+        ba = BlockArrays.from_dict({
+            "block_T": part(0, nb, np.int64), "block_inst_off": part(1, nb + 1, np.int64),
+            "block_member_off": part(2, nb + 1, np.int64), "inst_prefix_node": part(3, ni, np.int64),
+            "inst_prefix_len": part(4, ni, np.int64), "members": part(5, nm, np.int32)})
+        toff = part(6, nb + 1, np.int64)
+        tnodes = part(7, ne, np.int32)
+        recs = (SpScoreOut * max(nb, 1)).from_address(base + offs[8])
         recs.owner = owner
-        xb = (SpExplainBlock * max(nb, 1)).from_address(C.addressof(v.detail.contents))
+        xb = (SpExplainBlock * max(nb, 1)).from_address(base + offs[9])
         xb.owner = owner
-        node = _abi.view_array(v.node_detail, 4 * ne, np.int8, owner).reshape(ne, 4)
-        edge = _abi.view_array(v.edge_detail, 2 * nedge, np.int8, owner).reshape(nedge, 2)
-        eoff = _abi.view_array(v.edge_off, nb + 1, np.int64, owner)
+        node = part(10, 4 * ne, np.int8).reshape(ne, 4)
+        edge = part(11, 2 * nedge, np.int8).reshape(nedge, 2)
+        eoff = part(12, nb + 1, np.int64)
         return ba, (toff, tnodes), RawList(recs, nb), (RawList(xb, nb), node, edge, eoff)
 
     def tables(self, dgraph: _Handle, tmpl_off: np.ndarray, tmpl_nodes: np.ndarray, mesh,

@@ -301,8 +301,63 @@ struct sp_plan {
   std::vector<sp_score_out> scores;
   std::vector<sp_explain_block> detail;
   std::vector<int8_t> node, edge;
+  // every array of the view packed into one block (16-byte aligned parts, in
+  // the view's field order), so a caller maps the whole result with one buffer
+  std::vector<uint8_t> arena;
+  sp_plan_view view{};
   ~sp_plan() { delete fold; }
 };
+
+static void plan_pack(sp_plan* P) {
+  const sp_blocks& B = P->fold->view;
+  const int64_t nb = B.n_blocks;
+  struct Part {
+    const void* src;
+    size_t bytes;
+  };
+  const Part parts[] = {
+      {B.block_T, sizeof(int64_t) * (size_t)nb},
+      {B.block_inst_off, sizeof(int64_t) * (size_t)(nb + 1)},
+      {B.block_member_off, sizeof(int64_t) * (size_t)(nb + 1)},
+      {B.inst_prefix_node, sizeof(int64_t) * (size_t)B.n_instances},
+      {B.inst_prefix_len, sizeof(int64_t) * (size_t)B.n_instances},
+      {B.members, sizeof(int32_t) * (size_t)B.n_members},
+      {P->toff.data(), sizeof(int64_t) * P->toff.size()},
+      {P->tnodes.data(), sizeof(int32_t) * P->tnodes.size()},
+      {P->scores.data(), sizeof(sp_score_out) * P->scores.size()},
+      {P->detail.data(), sizeof(sp_explain_block) * P->detail.size()},
+      {P->node.data(), P->node.size()},
+      {P->edge.data(), P->edge.size()},
+      {P->eoff.data(), sizeof(int64_t) * P->eoff.size()},
+  };
+  constexpr int NP = sizeof(parts) / sizeof(parts[0]);
+  size_t off[NP], total = 0;
+  for (int i = 0; i < NP; i++) {
+    off[i] = total;
+    total += (parts[i].bytes + 15) & ~(size_t)15;
+  }
+  P->arena.resize(std::max<size_t>(total, 16));
+  uint8_t* a = P->arena.data();
+  for (int i = 0; i < NP; i++)
+    if (parts[i].bytes) std::memcpy(a + off[i], parts[i].src, parts[i].bytes);
+  sp_plan_view& v = P->view;
+  v.blocks = B;
+  v.blocks.block_T = (const int64_t*)(a + off[0]);
+  v.blocks.block_inst_off = (const int64_t*)(a + off[1]);
+  v.blocks.block_member_off = (const int64_t*)(a + off[2]);
+  v.blocks.inst_prefix_node = (const int64_t*)(a + off[3]);
+  v.blocks.inst_prefix_len = (const int64_t*)(a + off[4]);
+  v.blocks.members = (const int32_t*)(a + off[5]);
+  v.tmpl_off = (const int64_t*)(a + off[6]);
+  v.tmpl_nodes = (const int32_t*)(a + off[7]);
+  v.scores = (const sp_score_out*)(a + off[8]);
+  v.detail = (const sp_explain_block*)(a + off[9]);
+  v.node_detail = (const int8_t*)(a + off[10]);
+  v.edge_detail = (const int8_t*)(a + off[11]);
+  v.edge_off = (const int64_t*)(a + off[12]);
+  v.n_entries = P->toff.empty() ? 0 : P->toff.back();
+  v.n_edges = P->eoff.empty() ? 0 : P->eoff.back();
+}
 
 int sp_plan_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, const sp_mesh* mesh, int64_t mu, int64_t chunk_size,
                 sp_plan** out) {
@@ -355,22 +410,14 @@ int sp_plan_run(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, const sp_mesh* mesh
     delete P;
     return rc;
   }
+  plan_pack(P);
   *out = P;
   return SP_OK;
 }
 
 int sp_plan_view_get(const sp_plan* p, sp_plan_view* v) {
   if (!p || !v || !p->fold) return SP_ERR_CONFIG;
-  v->blocks = p->fold->view;
-  v->tmpl_off = p->toff.data();
-  v->tmpl_nodes = p->tnodes.data();
-  v->scores = p->scores.data();
-  v->detail = p->detail.data();
-  v->node_detail = p->node.data();
-  v->edge_detail = p->edge.data();
-  v->edge_off = p->eoff.data();
-  v->n_entries = p->toff.empty() ? 0 : p->toff.back();
-  v->n_edges = p->eoff.empty() ? 0 : p->eoff.back();
+  *v = p->view;
   return SP_OK;
 }
 

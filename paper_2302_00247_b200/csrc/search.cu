@@ -2566,6 +2566,179 @@ static_assert(sizeof(ExplainBlock) == sizeof(sp_explain_block), "ExplainBlock mi
 // the fp64 tables its reach (the scoring walk's own operations), and the
 // conversion collectives come from the XEdge table k_fill filled with the
 // same route_node evaluation.  The backward pass repeats k_explain_all's.
+// The winner detail of block b (candidate `index`) by one warp, from its blob
+// staged at `smem` (k_explain_fast, and k_search_small after its scoring):
+// lane 0 walks the template with the candidate's digits -- the routing byte
+// of each node gives its pattern and state (0xFF: the first node that cannot
+// route), the fp64 tables its reach (the scoring walk's own operations), and
+// the conversion collectives come from the XEdge table k_fill filled with the
+// same route_node evaluation.  The backward pass repeats k_explain_all's.
+// s_dig: 64 bytes of shared memory, s_ok: one int of shared memory.
+// the per-node records explain_warp's lane 0 reads in its serial walk, pulled
+// into L1 by the whole warp first (each of those loads would otherwise wait on L2)
+__device__ __forceinline__ void explain_prefetch(int64_t b, int64_t e0, int T, const int16_t* ref_slot_of,
+                                                 const uint8_t* bound_of, const uint8_t* xinfo, const int64_t* xoff) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t* xb = xinfo + xoff[b];
+  const int64_t xbytes = xoff[b + 1] - xoff[b];
+  for (int64_t q = lane * 128; q < xbytes; q += 32 * 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xb + q));
+  for (int q = lane * 128; q < 2 * T; q += 32 * 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"((const uint8_t*)(ref_slot_of + e0) + q));
+  for (int q = lane * 128; q < T; q += 32 * 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(bound_of + e0 + q));
+}
+
+__device__ void explain_warp(int64_t b, unsigned long long index, uint8_t* smem, GraphView G, const int64_t* tmpl_off,
+                             const int32_t* tmpl_nodes, const int16_t* ref_slot_of, const uint8_t* bound_of,
+                             const uint8_t* xinfo, const int64_t* xoff, const int64_t* edge_off, sp_mesh mesh,
+                             int64_t mu, int64_t chunk, ExplainBlock* out, int8_t* node_out, int8_t* edge_out,
+                             uint8_t* s_dig, int* s_ok_p) {
+  const MeshC M = mesh_consts(mesh);
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = tmpl_off[b];
+  int& s_ok = *s_ok_p;
+  const BlobHeader& H = *(const BlobHeader*)smem;
+  const NodeDesc* desc = (const NodeDesc*)(smem + H.desc_off);
+  const int16_t* prodpos = (const int16_t*)(smem + H.prod_off) + H.n_prod;
+  const uint8_t* tab = smem + H.tab_off;
+  const double* dbl = (const double*)(smem + H.dbl_off);
+  const XNode* xn = (const XNode*)(xinfo + xoff[b]);
+  const int T = H.T;
+  const XEdge* xe = (const XEdge*)(xinfo + xoff[b] + (int64_t)sizeof(XNode) * T);
+  ExplainBlock X;
+  X.valid = 0;
+  X.fail_pos = -1;
+  X.forward_comm = X.backward_comm = X.total = 0.0;
+  for (int k = 0; k < 4; k++) X.bytes[k] = X.calls[k] = 0;
+  X.collective_calls = 0;
+  double fwd = 0.0;
+  if (lane == 0) {
+    // reference slot order (candidate_by_index, search.py:103-116)
+    unsigned long long rem = index;
+    for (int q = H.V - 1; q >= 0; q--) {
+      const uint32_t r = ((H.radix3_ref >> q) & 1) ? 3 : 2;
+      s_dig[q] = (uint8_t)(rem % r);
+      rem /= r;
+    }
+    uint8_t state[MAXT];
+    double reach[MAXT];
+    int64_t eo = edge_off[b];
+    bool ok = true;
+    for (int i = 0; i < T; i++) {
+      const NodeDesc nd = desc[i];
+      const int slot = ref_slot_of[e0 + i];
+      uint32_t key = slot >= 0 ? s_dig[slot] : 0;
+      for (int j = 0; j < nd.k; j++) key = key * 3 + state[prodpos[nd.prod + j]];
+      const uint8_t e = tab[nd.tab + key];
+      if (e == 0xFF) {
+        X.fail_pos = i;
+        ok = false;
+        break;
+      }
+      const int p = e & 3, st = e >> 2;
+      state[i] = (uint8_t)st;
+      const double* dn = dbl + nd.dbl;
+      double base = 0.0;
+      for (int j = 0; j < nd.k; j++) {
+        const int pp = prodpos[nd.prod + j];
+        const int sj = state[pp];
+        const int kind = xe[nd.prod + j].kind[p][sj];
+        if (kind > 0) {
+          X.bytes[kind - 1] += xn[pp].act_bytes;
+          X.calls[kind - 1]++;
+        }
+        edge_out[2 * eo] = (int8_t)kind;
+        edge_out[2 * eo + 1] = xe[nd.prod + j].axis[p][sj];
+        eo++;
+        base = fmax(base, dadd(reach[pp], dn[8 + (j * 4 + p) * 3 + sj]));
+      }
+      Pattern pats[4];
+      patterns_for(xn[i].op, pats);
+      const int pc = pats[p].coll;
+      if (pc != C_ID) {
+        X.bytes[pc - 1] += xn[i].act_bytes;
+        X.calls[pc - 1]++;
+      }
+      reach[i] = dadd(base, dn[p]);
+      const NSpec fs = state_spec(st, xn[i].act_rank);
+      node_out[4 * (e0 + i)] = (int8_t)p;
+      node_out[4 * (e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
+      node_out[4 * (e0 + i) + 2] = -1;
+      node_out[4 * (e0 + i) + 3] = 0;
+    }
+    if (ok)
+      for (int i = 0; i < T; i++) {
+        double tail = reach[i];
+        if (bound_of[e0 + i] && state[i] != 0) {
+          tail = dadd(tail, dbl[desc[i].dbl + 4 + state[i]]);
+          X.bytes[C_AG - 1] += xn[i].act_bytes;
+          X.calls[C_AG - 1]++;
+          node_out[4 * (e0 + i) + 2] = state_spec(state[i], xn[i].act_rank).axis;
+        }
+        fwd = fmax(fwd, tail);
+      }
+    s_ok = ok;
+  }
+  __syncwarp();
+  if (!s_ok) {
+    if (lane == 0) out[b] = X;
+    return;
+  }
+  double bwd = 0.0;
+  if (M.d > 1) {
+    // pack_gradients (rewrite.py:78-111): buckets first, then unfused, each one AllReduce.
+    // Each trainable weight's byte size (-1: not all-replica / not trainable) is
+    // looked up by the warp into shared memory (the blob is no longer read).
+    int64_t* szs = (int64_t*)smem;
+    for (int i = lane; i < T; i += 32) {
+      const int32_t n = tmpl_nodes[e0 + i];
+      szs[i] = (!G.w_rank[n] || !G.w_train[n] || s_dig[ref_slot_of[e0 + i]] != 0) ? -1 : G.w_bytes[n];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int64_t cur = 0;
+      int cur_n = 0;
+      for (int pass = 0; pass < 2; pass++) {
+        for (int i = 0; i < T; i++) {
+          const int64_t sz = szs[i];
+          if (sz < 0) continue;
+          if (pass == 0) {
+            if (sz >= mu) continue;
+            if (cur + sz > chunk && cur_n) {
+              bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+              X.bytes[0] += cur;
+              X.calls[0]++;
+              cur = 0;
+              cur_n = 0;
+            }
+            cur += sz;
+            cur_n++;
+          } else if (sz >= mu) {
+            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
+            X.bytes[0] += sz;
+            X.calls[0]++;
+          }
+        }
+        if (pass == 0 && cur_n) {
+          bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
+          X.bytes[0] += cur;
+          X.calls[0]++;
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    X.valid = 1;
+    X.forward_comm = fwd;
+    X.backward_comm = bwd;
+    X.total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
+    X.collective_calls = X.calls[0] + X.calls[1] + X.calls[2] + X.calls[3];
+    out[b] = X;
+  }
+}
+
+// k_explain_all from the routing tables instead of re-deriving every pattern
+// choice: one warp per block stages the blob into shared memory, then runs
+// explain_warp.
 __global__ void k_explain_fast(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl_nodes, int64_t nb,
                                const int16_t* ref_slot_of, const uint8_t* bound_of, const uint8_t* blobs,
                                const int64_t* blob_off, const uint8_t* xinfo, const int64_t* xoff,
@@ -2575,7 +2748,6 @@ __global__ void k_explain_fast(GraphView G, const int64_t* tmpl_off, const int32
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint8_t s_dig[64];
   __shared__ int s_ok;
-  const MeshC M = mesh_consts(mesh);
   const int lane = threadIdx.x & 31;
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const unsigned long long index =
@@ -2594,157 +2766,118 @@ __global__ void k_explain_fast(GraphView G, const int64_t* tmpl_off, const int32
     __syncwarp();
     for (int q = lane * 16; q < nbytes; q += 32 * 16)
       *(int4*)(smem + q) = *(const int4*)(blobs + blob_off[b] + q);
-    {
-      // the per-node records lane 0 reads in its serial walk, pulled into L1
-      // by the whole warp first (each of those loads would otherwise wait on L2)
-      const int T = gH->T;
-      const uint8_t* xb = xinfo + xoff[b];
-      const int64_t xbytes = xoff[b + 1] - xoff[b];
-      for (int64_t q = lane * 128; q < xbytes; q += 32 * 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(xb + q));
-      for (int q = lane * 128; q < 2 * T; q += 32 * 128)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"((const uint8_t*)(ref_slot_of + e0) + q));
-      for (int q = lane * 128; q < T; q += 32 * 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(bound_of + e0 + q));
-    }
+    explain_prefetch(b, e0, gH->T, ref_slot_of, bound_of, xinfo, xoff);
     __syncwarp();
-    const BlobHeader& H = *(const BlobHeader*)smem;
-    const NodeDesc* desc = (const NodeDesc*)(smem + H.desc_off);
-    const int16_t* prodpos = (const int16_t*)(smem + H.prod_off) + H.n_prod;
-    const uint8_t* tab = smem + H.tab_off;
-    const double* dbl = (const double*)(smem + H.dbl_off);
-    const XNode* xn = (const XNode*)(xinfo + xoff[b]);
-    const int T = H.T;
-    const XEdge* xe = (const XEdge*)(xinfo + xoff[b] + (int64_t)sizeof(XNode) * T);
-    ExplainBlock X;
-    X.valid = 0;
-    X.fail_pos = -1;
-    X.forward_comm = X.backward_comm = X.total = 0.0;
-    for (int k = 0; k < 4; k++) X.bytes[k] = X.calls[k] = 0;
-    X.collective_calls = 0;
-    double fwd = 0.0;
-    if (lane == 0) {
-      // reference slot order (candidate_by_index, search.py:103-116)
-      unsigned long long rem = index;
-      for (int q = H.V - 1; q >= 0; q--) {
-        const uint32_t r = ((H.radix3_ref >> q) & 1) ? 3 : 2;
-        s_dig[q] = (uint8_t)(rem % r);
-        rem /= r;
-      }
-      uint8_t state[MAXT];
-      double reach[MAXT];
-      int64_t eo = edge_off[b];
-      bool ok = true;
-      for (int i = 0; i < T; i++) {
-        const NodeDesc nd = desc[i];
-        const int slot = ref_slot_of[e0 + i];
-        uint32_t key = slot >= 0 ? s_dig[slot] : 0;
-        for (int j = 0; j < nd.k; j++) key = key * 3 + state[prodpos[nd.prod + j]];
-        const uint8_t e = tab[nd.tab + key];
-        if (e == 0xFF) {
-          X.fail_pos = i;
-          ok = false;
-          break;
-        }
-        const int p = e & 3, st = e >> 2;
-        state[i] = (uint8_t)st;
-        const double* dn = dbl + nd.dbl;
-        double base = 0.0;
-        for (int j = 0; j < nd.k; j++) {
-          const int pp = prodpos[nd.prod + j];
-          const int sj = state[pp];
-          const int kind = xe[nd.prod + j].kind[p][sj];
-          if (kind > 0) {
-            X.bytes[kind - 1] += xn[pp].act_bytes;
-            X.calls[kind - 1]++;
-          }
-          edge_out[2 * eo] = (int8_t)kind;
-          edge_out[2 * eo + 1] = xe[nd.prod + j].axis[p][sj];
-          eo++;
-          base = fmax(base, dadd(reach[pp], dn[8 + (j * 4 + p) * 3 + sj]));
-        }
-        Pattern pats[4];
-        patterns_for(xn[i].op, pats);
-        const int pc = pats[p].coll;
-        if (pc != C_ID) {
-          X.bytes[pc - 1] += xn[i].act_bytes;
-          X.calls[pc - 1]++;
-        }
-        reach[i] = dadd(base, dn[p]);
-        const NSpec fs = state_spec(st, xn[i].act_rank);
-        node_out[4 * (e0 + i)] = (int8_t)p;
-        node_out[4 * (e0 + i) + 1] = fs.kind == K_S ? fs.axis : -1;
-        node_out[4 * (e0 + i) + 2] = -1;
-        node_out[4 * (e0 + i) + 3] = 0;
-      }
-      if (ok)
-        for (int i = 0; i < T; i++) {
-          double tail = reach[i];
-          if (bound_of[e0 + i] && state[i] != 0) {
-            tail = dadd(tail, dbl[desc[i].dbl + 4 + state[i]]);
-            X.bytes[C_AG - 1] += xn[i].act_bytes;
-            X.calls[C_AG - 1]++;
-            node_out[4 * (e0 + i) + 2] = state_spec(state[i], xn[i].act_rank).axis;
-          }
-          fwd = fmax(fwd, tail);
-        }
-      s_ok = ok;
-    }
+    explain_warp(b, index, smem, G, tmpl_off, tmpl_nodes, ref_slot_of, bound_of, xinfo, xoff, edge_off, mesh, mu,
+                 chunk, out, node_out, edge_out, s_dig, &s_ok);
     __syncwarp();
-    if (!s_ok) {
-      if (lane == 0) out[b] = X;
-      continue;
+  }
+}
+
+// Searches whose every block is small (<= SMALL_SEARCH_MAX_C candidates: the
+// BASELINE configs c1/c3/c4) in ONE kernel: a
+// CTA per block stages its tables, its warps walk the block's candidates in
+// SMALL_CH-candidate chunks, the CTA reduces the argmin, and warp 0 explains
+// the winner from the tables already staged -- instead of the work-item
+// scorer, k_reduce and k_explain_fast (three launches, the winner's tables
+// staged twice, a global round trip of the per-item records).
+// (one CTA walks a whole block: c5's residual group, whose largest blocks hold
+// ~2^16 candidates, took 0.67 ms this way against 0.19 ms on the item path)
+constexpr unsigned long long SMALL_SEARCH_MAX_C = 8192;
+constexpr uint32_t SMALL_CH = 256;
+template <bool SKIP>
+__global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_search_small(
+    const uint8_t* __restrict__ blobs, const int64_t* __restrict__ blob_off, int64_t nb, GraphView G,
+    const int64_t* tmpl_off, const int32_t* tmpl_nodes, const int16_t* ref_slot_of, const uint8_t* bound_of,
+    const uint8_t* xinfo, const int64_t* xoff, const int64_t* edge_off, sp_mesh mesh, int64_t mu, int64_t chunk,
+    sp_score_out* __restrict__ dout, ExplainBlock* xout, int8_t* node_out, int8_t* edge_out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int NW = THREADS / 32;
+  __shared__ uint64_t s_lane_add[32];
+  __shared__ Biased s_bz;
+  __shared__ unsigned long long s_red_t[NW], s_red_i[NW], s_red_v[NW];
+  __shared__ uint32_t s_red_n[NW];
+  __shared__ unsigned long long s_best;
+  __shared__ uint8_t s_dig[64];
+  __shared__ int s_ok;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    stage_block(smem, blobs, blob_off[b], s_lane_add, &s_bz, nullptr, 1, 0, false);
+    const Tabs S = tabs_of(smem);
+    const BlobHeader& H = *S.H;
+    const uint32_t rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
+    const uint32_t pool = (uint32_t)__cvta_generic_to_shared(S.reach);
+    const uint32_t rb = opaque_u32(pool + 8u * (uint32_t)tid);
+    const uint32_t sb = opaque_u32(pool + (uint32_t)H.npool * THREADS * 8u + (uint32_t)tid);
+    const unsigned long long C = H.C;
+    LaneBest lb;
+    for (unsigned long long start = (unsigned long long)warp * SMALL_CH; start < C;
+         start += (unsigned long long)NW * SMALL_CH) {
+      const uint32_t rem = (uint32_t)min((unsigned long long)SMALL_CH, C - start);
+      const uint64_t w = badd(bencode(H, start), s_lane_add[lane], s_bz.B);
+      score_chunk<SKIP, false>(S, s_bz, s_lane_add, rec0, rb, sb, lane, w, rem, start + rem, lb);
     }
-    double bwd = 0.0;
-    if (M.d > 1) {
-      // pack_gradients (rewrite.py:78-111): buckets first, then unfused, each one AllReduce.
-      // Each trainable weight's byte size (-1: not all-replica / not trainable) is
-      // looked up by the warp into shared memory (the blob is no longer read).
-      int64_t* szs = (int64_t*)smem;
-      for (int i = lane; i < T; i += 32) {
-        const int32_t n = tmpl_nodes[e0 + i];
-        szs[i] = (!G.w_rank[n] || !G.w_train[n] || s_dig[ref_slot_of[e0 + i]] != 0) ? -1 : G.w_bytes[n];
-      }
-      __syncwarp();
-      if (lane == 0) {
-        int64_t cur = 0;
-        int cur_n = 0;
-        for (int pass = 0; pass < 2; pass++) {
-          for (int i = 0; i < T; i++) {
-            const int64_t sz = szs[i];
-            if (sz < 0) continue;
-            if (pass == 0) {
-              if (sz >= mu) continue;
-              if (cur + sz > chunk && cur_n) {
-                bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
-                X.bytes[0] += cur;
-                X.calls[0]++;
-                cur = 0;
-                cur_n = 0;
-              }
-              cur += sz;
-              cur_n++;
-            } else if (sz >= mu) {
-              bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, sz, M)));
-              X.bytes[0] += sz;
-              X.calls[0]++;
-            }
-          }
-          if (pass == 0 && cur_n) {
-            bwd = dadd(bwd, dadd(M.setup, cost_bytes(C_AR, cur, M)));
-            X.bytes[0] += cur;
-            X.calls[0]++;
-          }
-        }
+    // the block's argmin of (total bits, num_split, index) and valid count
+    unsigned long long bt = lb.t, bi = lb.t != ~0ULL ? ref_index_b(S, lb.w) : ~0ULL, nv = lb.valid;
+    uint32_t bn = lb.n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t2 = __shfl_down_sync(0xffffffffu, bt, o);
+      const unsigned long long i2 = __shfl_down_sync(0xffffffffu, bi, o);
+      const uint32_t n2 = __shfl_down_sync(0xffffffffu, bn, o);
+      nv += __shfl_down_sync(0xffffffffu, nv, o);
+      if (key_less(t2, n2, i2, bt, bn, bi)) {
+        bt = t2;
+        bn = n2;
+        bi = i2;
       }
     }
     if (lane == 0) {
-      X.valid = 1;
-      X.forward_comm = fwd;
-      X.backward_comm = bwd;
-      X.total = dadd(fwd, dmul(bwd, dadd(1.0, -mesh.overlap_fraction)));
-      X.collective_calls = X.calls[0] + X.calls[1] + X.calls[2] + X.calls[3];
-      out[b] = X;
+      s_red_t[warp] = bt;
+      s_red_i[warp] = bi;
+      s_red_n[warp] = bn;
+      s_red_v[warp] = nv;
     }
-    __syncwarp();
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t = s_red_t[0], i = s_red_i[0], v = s_red_v[0];
+      uint32_t n = s_red_n[0];
+      for (int w2 = 1; w2 < NW; w2++) {
+        v += s_red_v[w2];
+        if (key_less(s_red_t[w2], s_red_n[w2], s_red_i[w2], t, n, i)) {
+          t = s_red_t[w2];
+          n = s_red_n[w2];
+          i = s_red_i[w2];
+        }
+      }
+      sp_score_out r;
+      r.candidates = C;
+      r.valid = v;
+      r.has_best = i != ~0ULL && v > 0;
+      r.best_index = r.has_best ? i : 0;
+      r.best_total = r.has_best ? __longlong_as_double((long long)t) : 0.0;
+      r.best_num_split = r.has_best ? (int32_t)n : 0;
+      dout[b] = r;
+      s_best = r.has_best ? i : ~0ULL;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned long long index = s_best;
+      if (index == ~0ULL) {
+        if (lane == 0) {
+          ExplainBlock X{};
+          X.fail_pos = -1;
+          xout[b] = X;
+        }
+      } else {
+        explain_prefetch(b, tmpl_off[b], H.T, ref_slot_of, bound_of, xinfo, xoff);
+        __syncwarp();
+        explain_warp(b, index, smem, G, tmpl_off, tmpl_nodes, ref_slot_of, bound_of, xinfo, xoff, edge_off, mesh,
+                     mu, chunk, xout, node_out, edge_out, s_dig, &s_ok);
+      }
+    }
+    __syncthreads();  // the next block's tables overwrite shared memory
   }
 }
 
@@ -3594,7 +3727,7 @@ __global__ void k_sim_totals(int64_t nb, const ExplainBlock* __restrict__ x, sp_
     if (out[b].best_total < 0.0) out[b].best_total = x[b].total;
 }
 
-static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
+static void score_results(sp_ctx* ctx, sp_tables* t, bool explain, bool explained = false) {
   cudaStream_t s = ctx->stream;
   const int64_t nb = t->n_blocks;
   TablesPriv* priv = (TablesPriv*)t->priv;
@@ -3603,7 +3736,7 @@ static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
   pd.explain = explain;
   DevBuf<sp_score_out>& dout = pd.dout;
   const int64_t ne = t->tmpl_off[nb], nedge = t->edge_off[nb];
-  if (explain) {
+  if (explain && !explained) {
     // winner detail straight from the device-side argmin: no host round trip
     if (!packed) {
       pd.dblk.alloc(nb, s);
@@ -3642,8 +3775,48 @@ static void score_results(sp_ctx* ctx, sp_tables* t, bool explain) {
 }
 
 // Single-lane search (no exchange, or the caller exchanges on the host).
+// One-kernel search + winner detail when every block is small (k_search_small).
+// Returns false (nothing launched) when the search does not qualify.
+static bool score_small(sp_ctx* ctx, sp_tables* t) {
+  const int64_t nb = t->n_blocks;
+  if (nb < 1 || getenv("SP_SEARCH_SMALL_OFF") || getenv("SP_EXPLAIN_ROUTE") || getenv("SP_FORCE_WIDE") ||
+      getenv("SP_SCORE_GENERIC") || getenv("SP_SCORE_ITEMS"))
+    return false;
+  if (!ctx->skip && ctx->memo) return false;
+  for (int64_t b = 0; b < nb; b++)
+    if (t->hdr[b].C > SMALL_SEARCH_MAX_C || t->hdr[b].V > 32) return false;
+  const size_t smem = score_smem(t);
+  if (smem > ctx->smem_optin) return false;
+  cudaStream_t s = ctx->stream;
+  TablesPriv* priv = (TablesPriv*)t->priv;
+  PendingScore& pd = priv->pending;
+  pd.empty = false;
+  pd.explain = true;
+  alloc_dout(pd, t, s, false);
+  if (!pd.res_packed) {
+    pd.dblk.alloc(nb, s);
+    pd.dnode.alloc(4 * std::max<int64_t>(t->tmpl_off[nb], 1), s);
+    pd.dedge.alloc(2 * std::max<int64_t>(t->edge_off[nb], 1), s);
+  }
+  auto kern = ctx->skip ? k_search_small<true> : k_search_small<false>;
+  allow_smem(ctx, kern, smem);
+  int per = resident_ctas(ctx, kern, THREADS, smem);
+  if (per < 1) per = 1;
+  const unsigned grid = (unsigned)std::min<int64_t>(nb, (int64_t)ctx->sm_count * per);
+  SP_CUDA(cudaEventRecord(pd.ev[1], s));
+  SP_LAUNCH(ctx, kern, grid, THREADS, smem, s, t->blobs.p, t->d_blob_off.p, nb, view_of(t->dg), t->d_tmpl_off.p,
+            t->d_tmpl_nodes.p, priv->dev.ref_slot_of.p, priv->dev.bound.p, priv->dev.xinfo.p, priv->dev.xoff.p,
+            priv->dev.edge_off.p, priv->mesh, priv->mu, priv->chunk, pd.dout.p, pd.dblk.p, pd.dnode.p, pd.dedge.p);
+  SP_CUDA(cudaGetLastError());
+  SP_CUDA(cudaEventRecord(pd.ev[2], s));
+  SP_CUDA(cudaEventRecord(pd.ev[3], s));
+  score_results(ctx, t, true, true);
+  return true;
+}
+
 static void score_enqueue(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
   PendingScore& pd = ((TablesPriv*)t->priv)->pending;
+  if (explain && n_shards == 1 && score_small(ctx, t)) return;
   pd.explain = explain;
   if (!score_items(ctx, t, shard, n_shards, false)) {
     pd.empty = true;
@@ -3797,6 +3970,9 @@ void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bo
     return;
   }
   pending_begin(ctx, t);
+  // a search of small blocks only runs whole on every rank (one kernel, tens of
+  // microseconds): no share to exchange, every rank ends with the same records
+  if (explain && n_shards == 1 && (ctx->comm || ctx->sim_nranks > 1) && score_small(ctx, t)) return;
   if (ctx->comm) {  // one process per GPU: this rank's share, NCCL exchange (also at nranks 1)
     score_enqueue_lanes({ctx}, {t}, {ctx->rank}, ctx->nranks, explain);
     return;

@@ -861,3 +861,27 @@ def test_host_layout_equals_device_layout(backend, seed):
     finally:
         backend.set_host_layout(True)
     assert got[True] == got[False]
+
+
+@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("mode", ["skip", "walk"])
+def test_one_kernel_small_search_equals_item_path(backend, seed, mode, monkeypatch):
+    """Searches of small blocks run as one kernel (k_search_small: score, argmin,
+    winner detail per CTA); the work-item scorer + k_reduce + k_explain_fast
+    (SP_SEARCH_SMALL_OFF=1) must give the same report byte for byte."""
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.search import derive_plan
+    from randgraph import random_graph
+
+    g = random_graph(100 + seed, n_types=4, reps=(2, 6), ops=(3, 11))
+    mname, kw = MESHES[seed % len(MESHES)]
+    m = ClusterSpec.from_mesh(mname, **kw)
+    mu, chunk = ((1 << 20, 4 << 20), (64, 256), (8, 8))[seed % 3]
+    backend.set_mode(mode)
+    try:
+        got = canon(derive_plan(g, m, mu=mu, chunk_size=chunk, backend=backend).to_json())
+        monkeypatch.setenv("SP_SEARCH_SMALL_OFF", "1")
+        ref = canon(derive_plan(g, m, mu=mu, chunk_size=chunk, backend=backend).to_json())
+    finally:
+        backend.set_mode("skip")
+    assert got == ref

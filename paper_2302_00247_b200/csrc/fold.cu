@@ -518,6 +518,7 @@ struct SmallArgs {
   int32_t o_depth, o_pos, o_gparent, o_gclass, o_act, o_flag, o_cid, o_ph, o_rh, o_cur, o_gkey, o_next;
   int32_t o_name_off, o_names, o_op, o_w_rank, o_w_train, o_w_shape, o_in_off, o_in_idx;
   int64_t name_bytes, n_edges;
+  long long* prof;  // SP_FOLD_PROF: clock64() at each phase boundary (thread 0), else null
 };
 
 // cooperative global -> shared copy (16-byte words when both ends allow it)
@@ -574,6 +575,13 @@ template <bool STG>
 __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int32_t s_warp[32];
+  int np_ = 0;
+#define PROF()                                                \
+  do {                                                        \
+    if (a.prof && threadIdx.x == 0) a.prof[np_] = clock64(); \
+    np_++;                                                    \
+  } while (0)
+  PROF();
   const int tid = threadIdx.x, NT = blockDim.x;
   const int n = (int)a.n, D = a.D;
   const int P2max = pow2ceil(n);
@@ -613,6 +621,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     copy_in((uint8_t*)in_idx, (const uint8_t*)a.in_idx, (size_t)a.n_edges * 4);
     __syncthreads();
   }
+  PROF();
   for (int i = tid; i < n; i += NT) {
     int32_t d = 1;
     for (int64_t k = name_off[i]; k < name_off[i + 1]; k++) d += names[k] == '/';
@@ -624,6 +633,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     act[i] = i;
   }
   __syncthreads();
+  PROF();
   int nA = n;
   int level = 1;
   for (; nA > 0 && level <= D; level++) {
@@ -648,7 +658,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
       }
     }
     __syncthreads();
+    PROF();
     block_sort(K1, K2, V, nA, P2);
+    PROF();
     for (int i = tid; i < nA; i += NT) {
       srt[i] = V[i];
       flag[i] = (i == 0 || K1[i] != K1[i - 1]) ? 1 : 0;
@@ -664,10 +676,12 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     for (int g = tid; g < nG; g += NT) gkey[g] = 0;
     if (tid == 0) gs[nG] = nA;
     __syncthreads();
+    PROF();
     // 2. entry hashes / group keys
     for (int i = tid; i < nA; i += NT)
       entry_one(i, srt, flag, nA, gs, cur, rh, D, dd, op, w_rank, w_shape, w_train, in_off, in_idx, pos, gkey);
     __syncthreads();
+    PROF();
     // 3. classes: sort groups by (parent, key)
     const int P2g = pow2ceil(nG);
     const int gfill = nG <= NT && nG <= RANK_SORT_MAX ? nG : P2g;
@@ -683,6 +697,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     }
     __syncthreads();
     block_sort(K1, K2, V, nG, P2g);
+    PROF();
     for (int j = tid; j < nG; j += NT) {
       co[j] = V[j];
       cid[j] = (j == 0 || K1[j] != K1[j - 1] || K2[j] != K2[j - 1]) ? 1 : 0;
@@ -696,10 +711,13 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     }
     if (tid == 0) cs[nC] = nG;
     __syncthreads();
+    PROF();
     // 4. exact verification, 5. accept / residual / descend
     for (int i = tid; i < nA; i += NT)
       verify_one(i, srt, flag, nA, nG, gs, gclass, cs, co, cur, pos, a.pend, rh, D, dd, name_off, names, op, w_rank,
                  w_shape, w_train, in_off, in_idx, a.collision);
+    __syncthreads();
+    PROF();
     for (int i = tid; i < nA; i += NT)
       accept_one(i, srt, flag, nA, nC, nG, gclass, cs, depth, level, a.min_dup, gparent, next_flag, a.residual, ga);
     __syncthreads();
@@ -715,8 +733,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     }
     nA = nNext;
     __syncthreads();
+    PROF();
   }
   if (tid == 0) a.info[D * 4] = nA > 0 ? -1 : level - 1;
+  PROF();
+#undef PROF
 }
 
 inline int grid_for(int64_t n, int sms) {
@@ -1833,7 +1854,23 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   // per-node passes), or one per bitonic compare-exchange beyond 1024 nodes
   const int threads = n <= RANK_SORT_MAX ? std::max(64, (int)((n + 31) / 32 * 32)) : std::min(SMALL_THREADS, P2 / 2);
   tr.mark("setup");
+  static const bool prof = getenv("SP_FOLD_PROF") != nullptr;
+  DevBuf<long long> profb;
+  A.prof = nullptr;
+  if (prof) {
+    profb.alloc(256, s);
+    SP_CUDA(cudaMemsetAsync(profb.p, 0, 256 * sizeof(long long), s));
+    A.prof = profb.p;
+  }
   SP_LAUNCH(ctx, kern, 1, threads, smem, s, A);
+  if (prof) {
+    long long h[256];
+    SP_CUDA(cudaMemcpyAsync(h, profb.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[fold_small prof] n=%lld threads=%d:", (long long)n, threads);
+    for (int i = 1; i < 256 && h[i]; i++) fprintf(stderr, " %lld", h[i] - h[i - 1]);
+    fprintf(stderr, "\n");
+  }
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaEventRecord(ctx->ev[7], s));
   // outputs, pend, gaccept + residual: one contiguous range, one pinned block, one copy

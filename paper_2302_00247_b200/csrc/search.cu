@@ -458,15 +458,15 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         f.dbl = H.dbl_off + 8 * L.dbl;
         f.cb0 = L.k >= 1 ? H.dbl_off + 8 * (L.dbl + 8) : H.zero_off;
         f.cb1 = L.k >= 2 ? H.dbl_off + 8 * (L.dbl + 8 + 12) : H.zero_off;
-        f.r0 = f.r1 = f.s0 = f.s1 = 0;
+        f.r0 = f.r1 = 0;
         int jj = 0;
         for (int64_t q = G.in_off[n]; q < G.in_off[n + 1]; q++) {
           const int32_t r = G.in_idx[q];
           if (node_block[r] != (int32_t)b) continue;
           const int ps = s_outpool[node_tpos[r]];
           if (L.k <= 2) {
-            if (jj == 0) { f.r0 = ps * THREADS * 8; f.s0 = ps * THREADS; }
-            else { f.r1 = ps * THREADS * 8; f.s1 = ps * THREADS; }
+            if (jj == 0) f.r0 = ps * THREADS * 8;
+            else f.r1 = ps * THREADS * 8;
           } else {
             int32_t* fp = (int32_t*)(blob + H.fprod_off) + 2 * (L.prod + jj);
             fp[0] = ps * THREADS * 8;
@@ -478,15 +478,15 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         // -1: no internal consumer (only boundary nodes; the paired walk
         // stores non-boundary results unguarded)
         f.out_r = L.out_pool >= 0 ? L.out_pool * THREADS * 8 : -1;
-        f.out_s = L.out_pool >= 0 ? L.out_pool * THREADS : -1;
-        f.sh = nd.slot >= 0 ? 2 * (H.V - 1 - nd.slot) : 0;
-        // kf = k << 8 | boundary << 5 | min(k, 3) << 3 | one-hot class of the three
-        // common non-boundary kinds (bit 0: k = 1, bit 1: k = 0, bit 2: k = 2),
-        // which the paired walk tests first, in that order of frequency
+        const int sh = nd.slot >= 0 && H.V <= 32 ? 2 * (H.V - 1 - nd.slot) : 0;  // (wide blocks: generic walk)
+        // kf = k << 16 | boundary << 13 | min(k, 3) << 11 | one-hot class of the
+        // three common non-boundary kinds (bit 8: k = 1, bit 9: k = 0, bit 10:
+        // k = 2), which the paired walk tests first, in that order of frequency
+        // | the digit shift in bits 0..5 (the walk shifts by kf & 63)
         const int bnd = (!has_cons[n] || ext_cons[n]) ? 1 : 0;
         const int kc = L.k < 3 ? L.k : 3;
-        f.kf = (L.k << 8) | (bnd << 5) | (kc << 3) |
-               (bnd ? 0 : kc == 1 ? 1 : kc == 0 ? 2 : kc == 2 ? 4 : 0);
+        f.kf = (L.k << 16) | (bnd << 13) | (kc << 11) |
+               ((bnd ? 0 : kc == 1 ? 1 : kc == 0 ? 2 : kc == 2 ? 4 : 0) << 8) | sh;
         ((FastNode*)(blob + H.fast_off))[i] = f;
       }
       ((NodeSkip*)(blob + H.skip_off))[i] = NodeSkip{L.skip_R, L.skip_m, 0};
@@ -826,10 +826,12 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
   }
   for (int i = 0; rec != end; i++, rec += (uint32_t)sizeof(FastNode)) {
     // A = (tab, dbl, cb0, cb1) absolute, B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf)
-    const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
-    const int4 B = lds_v4(rec + 16);
+    const int4 A = lds_v4(rec), R = lds_v4(rec + 16);
+    // B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf): state offsets at 1/8 of the reach offsets
+    const int4 B = make_int4(R.x, R.y, R.x >> 3, R.y >> 3);
+    const int4 X = make_int4(R.z, R.z >> 3, R.w & 63, R.w);  // kf: kind bits tested in place
     const uint32_t b = (uint32_t)(w >> X.z) & 3u;
-    const int kc = (X.w >> 3) & 3;  // fan-in, 3 = general
+    const int kc = (X.w >> 11) & 3;  // fan-in, 3 = general
     uint32_t e;
     double r;
     if (kc == 1) {
@@ -852,7 +854,7 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
       SP_FAIL_CHECK(i)
       r = lds_f64(A.y + (e & 0x18u));
     } else {
-      const int k = X.w >> 8;
+      const int k = X.w >> 16;
       const uint32_t pp = (uint32_t)B.x;  // absolute address of the (reach, state) offset pairs
       uint32_t key = b;
       for (int j = 0; j < k; j++) key = key * 3 + lds_u8(sb + lds_s32(pp + 8 * j + 4));
@@ -867,7 +869,7 @@ __device__ __forceinline__ int walk_fast(uint32_t rec, int T, uint64_t w, bool a
       r = dadd(bse, lds_f64(A.y + pe));
     }
     const uint32_t s = e & 3u;
-    if (X.w & 32) {
+    if (X.w & (1 << 13)) {
       const long long x = __double_as_longlong(dadd(r, lds_f64(A.y + 32 + s * 8)));
       f = x > f ? x : f;
     }
@@ -895,7 +897,7 @@ __device__ __forceinline__ void patch_fast(uint8_t* smem, bool pair = false) {
     f.dbl += (int32_t)base;
     f.cb0 += (int32_t)base;
     f.cb1 += (int32_t)base;
-    const int k = f.kf >> 8;
+    const int k = f.kf >> 16;
     if (k >= 3) {
       int32_t* pp = (int32_t*)(smem + H.fprod_off) + 2 * f.r0;
       for (int j = 0; j < k; j++) {
@@ -905,14 +907,9 @@ __device__ __forceinline__ void patch_fast(uint8_t* smem, bool pair = false) {
       f.r0 = (int32_t)(base + (uint32_t)H.fprod_off + 8u * (uint32_t)f.r0);
     } else {
       f.r0 *= m;
-      f.s0 *= m;
     }
     f.r1 *= m;
-    f.s1 *= m;
-    if (f.out_r >= 0) {
-      f.out_r *= m;
-      f.out_s *= m;
-    }
+    if (f.out_r >= 0) f.out_r *= m;
   }
 }
 
@@ -988,7 +985,7 @@ __device__ __forceinline__ bool pair_node(const int4& A, const int4& B, const in
     ra = lds_f64(A.y + (ea & 0x18u));
     rx = lds_f64(A.y + (eb & 0x18u));
   } else {
-    const int k = X.w >> 8;
+    const int k = X.w >> 16;
     const uint32_t pp = (uint32_t)B.x;
     uint32_t ka = ba, kb = bb;
     for (int j = 0; j < k; j++) {
@@ -1041,20 +1038,22 @@ __device__ __forceinline__ int walk_pair(uint32_t rec, int T, uint64_t wa, uint6
   const uint32_t end = rec + (uint32_t)T * (uint32_t)sizeof(FastNode);
   for (; rec != end; rec += (uint32_t)sizeof(FastNode)) {
     // A = (tab, dbl, cb0, cb1) absolute, B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf)
-    const int4 A = lds_v4(rec), X = lds_v4(rec + 32);
-    const int4 B = lds_v4(rec + 16);
+    const int4 A = lds_v4(rec), R = lds_v4(rec + 16);
+    // B = (r0, r1, s0, s1), X = (out_r, out_s, sh, kf): state offsets at 1/8 of the reach offsets
+    const int4 B = make_int4(R.x, R.y, R.x >> 3, R.y >> 3);
+    const int4 X = make_int4(R.z, R.z >> 3, R.w & 63, R.w);  // kf: kind bits tested in place
     const uint32_t ba = (uint32_t)(wa >> X.z) & 3u, bb = (uint32_t)(wb >> X.z) & 3u;
     bool go;
     // bit tests, most frequent kind first (an if-chain on one value would be
     // turned into a compare tree)
-    if (X.w & 1) {
+    if (X.w & (1 << 8)) {
       go = pair_node<1, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb);
-    } else if (X.w & 2) {
+    } else if (X.w & (1 << 9)) {
       go = pair_node<0, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb);
-    } else if (X.w & 4) {
+    } else if (X.w & (1 << 10)) {
       go = pair_node<2, false>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb);
     } else {
-      switch ((X.w >> 3) & 7) {  // min(fan-in, 3) | boundary << 2
+      switch ((X.w >> 11) & 7) {  // min(fan-in, 3) | boundary << 2
         case 5: go = pair_node<1, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
         case 4: go = pair_node<0, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;
         case 6: go = pair_node<2, true>(A, B, X, ba, bb, oka, okb, fa, fb, rb, sb); break;

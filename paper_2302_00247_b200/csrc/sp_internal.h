@@ -398,21 +398,22 @@ struct BlobHeader {
 static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
 
 // Per-node record of the lean scoring walk: every field is a ready-to-use
-// shared-memory byte offset, so the walk does no unpacking.  The routing table
-// of a node has 4 rows indexed by the node's BIASED digit field (row = digit +
-// 4 - radix; unweighted nodes replicate their single row 4 times), each row
-// 3^k bytes keyed by the producer states in base 3.
+// shared-memory byte offset, so the walk does no unpacking beyond shifts.  The
+// routing table of a node has 4 rows indexed by the node's BIASED digit field
+// (row = digit + 4 - radix; unweighted nodes replicate their single row 4
+// times), each row 3^k bytes keyed by the producer states in base 3.  A live
+// value's state byte sits at 1/8 of its reach offset (reach at pool +
+// (p*THREADS + t)*8, state at pool_states + p*THREADS + t), so the state
+// offsets are not stored: two 16-byte loads per node instead of three.
 struct __align__(16) FastNode {
   int32_t tab;           // smem offset of the node's 4-row routing table
   int32_t dbl;           // smem offset of own[4]; exitc[4] follows
   int32_t cb0, cb1;      // smem offsets of conv[0], conv[1] ([4][3] doubles; zero block if absent)
   int32_t r0, r1;        // reach byte offsets of producers 0/1 in the lane pool (k >= 3: fprod pair index)
-  int32_t s0, s1;        // state byte offsets of producers 0/1
-  int32_t out_r, out_s;  // output slot offsets (out_r < 0: no internal consumer)
-  int32_t sh;            // bit offset of the node's digit field in the biased word (0 when unweighted)
-  int32_t kf;            // k | 0x100 when the node can set the forward max (subgraph boundary)
+  int32_t out_r;         // output reach offset (< 0: no internal consumer)
+  int32_t kf;            // k << 16 | boundary << 13 | min(k,3) << 11 | one-hot kind << 8 | digit shift (0..62)
 };
-static_assert(sizeof(FastNode) == 48, "FastNode is three 16-byte smem loads");
+static_assert(sizeof(FastNode) == 32, "FastNode is two 16-byte smem loads");
 
 struct __align__(16) NodeDesc {
   int16_t slot;      // weight slot (enumeration position) or -1

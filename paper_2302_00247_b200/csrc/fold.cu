@@ -536,6 +536,9 @@ __device__ void copy_in(uint8_t* dst, const uint8_t* src, size_t bytes) {
   }
 }
 
+#ifndef SP_FOLD_NOREG
+#define SP_FOLD_NOREG 0
+#endif
 constexpr int RANK_SORT_MAX = 256;  // n^2 compares beat the bitonic network's barriers up to here
 // Ascending (K1, K2, V) order of n <= blockDim.x distinct entries by rank
 // counting: thread i counts the entries below its own (broadcast shared reads,
@@ -564,10 +567,94 @@ __device__ void block_rank_sort(uint64_t* K1, uint64_t* K2, int32_t* V, int n) {
   __syncthreads();
 }
 
+__device__ __forceinline__ bool key3_less(uint64_t a1, uint64_t a2, int32_t av, uint64_t b1, uint64_t b2, int32_t bv) {
+  return a1 != b1 ? a1 < b1 : (a2 != b2 ? a2 < b2 : av < bv);
+}
+
+// The bitonic network of block_bitonic with every stage of stride < 64 in
+// registers: thread t (lane l of warp w) holds entries w*64 + l and w*64 + l + 32,
+// stride 32 is an in-thread exchange and strides < 32 are warp shuffles, so
+// only the stages of stride >= 64 go through shared memory (with a barrier):
+// for 1024 entries 10 barrier stages instead of 55.  Needs 64 <= P2 <= 2 * blockDim.x.
+__device__ void block_bitonic_reg(uint64_t* K1, uint64_t* K2, int32_t* V, int P2) {
+  const int t = threadIdx.x;
+  const bool act = t < (P2 >> 1);
+  const int lane = t & 31;
+  const int i0 = (t >> 5) * 64 + lane, i1 = i0 + 32;
+  uint64_t a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+  int32_t av = 0, bv = 0;
+  auto load = [&] {
+    if (act) {
+      a1 = K1[i0]; a2 = K2[i0]; av = V[i0];
+      b1 = K1[i1]; b2 = K2[i1]; bv = V[i1];
+    }
+  };
+  auto store = [&] {
+    if (act) {
+      K1[i0] = a1; K2[i0] = a2; V[i0] = av;
+      K1[i1] = b1; K2[i1] = b2; V[i1] = bv;
+    }
+  };
+  // one element of a shuffle stage: keep the partner's entry when it belongs here
+  auto xchg = [&](uint64_t& x1, uint64_t& x2, int32_t& xv, int idx, int size, int stride) {
+    const uint64_t y1 = __shfl_xor_sync(0xffffffffu, x1, stride);
+    const uint64_t y2 = __shfl_xor_sync(0xffffffffu, x2, stride);
+    const int32_t yv = __shfl_xor_sync(0xffffffffu, xv, stride);
+    const bool lower = (idx & stride) == 0, up = (idx & size) == 0;
+    const bool y_lt = key3_less(y1, y2, yv, x1, x2, xv);
+    if (lower == up ? y_lt : !y_lt) {
+      x1 = y1;
+      x2 = y2;
+      xv = yv;
+    }
+  };
+  auto reg_stages = [&](int size, int smax) {
+    for (int stride = smax; stride > 0; stride >>= 1) {
+      if (stride == 32) {
+        const bool up = (i0 & size) == 0;
+        if (key3_less(b1, b2, bv, a1, a2, av) == up) {
+          uint64_t x = a1; a1 = b1; b1 = x;
+          x = a2; a2 = b2; b2 = x;
+          const int32_t y = av; av = bv; bv = y;
+        }
+      } else {
+        xchg(a1, a2, av, i0, size, stride);
+        xchg(b1, b2, bv, i1, size, stride);
+      }
+    }
+  };
+  load();
+  for (int size = 2; size <= 64; size <<= 1) reg_stages(size, size >> 1);
+  for (int size = 128; size <= P2; size <<= 1) {
+    store();
+    __syncthreads();
+    for (int stride = size >> 1; stride >= 64; stride >>= 1) {
+      for (int q = t; q < (P2 >> 1); q += blockDim.x) {
+        const int i = ((q & ~(stride - 1)) << 1) | (q & (stride - 1));
+        const int j = i + stride;
+        const bool gt = key3_less(K1[j], K2[j], V[j], K1[i], K2[i], V[i]);
+        if (gt == ((i & size) == 0)) {
+          const uint64_t x = K1[i], y = K2[i];
+          const int32_t z = V[i];
+          K1[i] = K1[j]; K2[i] = K2[j]; V[i] = V[j];
+          K1[j] = x; K2[j] = y; V[j] = z;
+        }
+      }
+      __syncthreads();
+    }
+    load();
+    reg_stages(size, 32);
+  }
+  store();
+  __syncthreads();
+}
+
 // ascending by (K1, K2, V): rank counting when every entry has a thread, else
-// the bitonic network over P2 (a power of two >= n, padded with ~0 keys)
+// the bitonic network over P2 (a power of two >= n, padded with ~0 keys),
+// register-resident below stride 64 when the block has a thread per pair
 __device__ void block_sort(uint64_t* K1, uint64_t* K2, int32_t* V, int n, int P2) {
   if (n <= RANK_SORT_MAX && n <= (int)blockDim.x) block_rank_sort(K1, K2, V, n);
+  else if (P2 >= 64 && (P2 >> 1) <= (int)blockDim.x && !SP_FOLD_NOREG) block_bitonic_reg(K1, K2, V, P2);
   else block_bitonic(K1, K2, V, P2);
 }
 

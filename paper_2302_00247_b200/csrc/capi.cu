@@ -212,6 +212,19 @@ void sp_graph_free(sp_dgraph* dg) {
   if (dg->ctx) {
     cudaSetDevice(dg->ctx->device);
     cudaStreamSynchronize(dg->ctx->stream);
+    // keep the host vectors for the context's next upload (at most two sets)
+    if (dg->ctx->host_copies.size() < 2) {
+      HostGraphCopies hc;
+      hc.names.swap(dg->h_names);
+      hc.op.swap(dg->h_op);
+      hc.w_rank.swap(dg->h_w_rank);
+      hc.w_train.swap(dg->h_w_train);
+      hc.name_off.swap(dg->h_name_off);
+      hc.topo.swap(dg->h_topo);
+      hc.in_off.swap(dg->h_in_off);
+      hc.in_idx.swap(dg->h_in_idx);
+      dg->ctx->host_copies.push_back(std::move(hc));
+    }
   }
   delete dg;
 }

@@ -35,6 +35,10 @@
 #include <cstdlib>
 #include <numeric>
 
+#include <functional>
+#include <condition_variable>
+#include <mutex>
+#include <unistd.h>
 #include "sp_internal.h"
 
 namespace sp {
@@ -867,6 +871,56 @@ __global__ void k_expand_graph(int64_t n, int R, const int32_t* __restrict__ a32
 // Host-side fan-out for graph_upload's byte work (validation scans, the
 // name depth scan, copies into the pinned staging buffer): ~20 MB at 10^5
 // nodes, memory-bound, so spread over a few threads.
+// Persistent workers for host_parallel: spawning up to 15 std::threads per call
+// cost ~0.3 ms per call (three calls per graph upload).  Workers sleep on a
+// condition variable between jobs; one job at a time (callers serialise on
+// run_mu).  The pool is never destroyed (its threads block until exit).
+struct HostPool {
+  std::mutex run_mu, mu;
+  std::condition_variable cv;
+  std::vector<std::thread> th;
+  const std::function<void(int)>* job = nullptr;
+  int active = 0;
+  uint64_t gen = 0;
+  std::atomic<int> done{0};
+  explicit HostPool(int workers) {
+    for (int t = 1; t <= workers; t++)
+      th.emplace_back([this, t] {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu);
+        for (;;) {
+          cv.wait(lk, [&] { return gen != seen; });
+          seen = gen;
+          const std::function<void(int)>* f = job;
+          const int a = active;
+          lk.unlock();
+          if (t < a) (*f)(t);
+          done.fetch_add(1, std::memory_order_acq_rel);
+          lk.lock();
+        }
+      });
+  }
+  void run(int T, const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> serial(run_mu);
+    const int workers = (int)th.size();
+    done.store(0, std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      job = &f;
+      active = T;
+      gen++;
+    }
+    cv.notify_all();
+    f(0);
+    for (unsigned spins = 0; done.load(std::memory_order_acquire) < workers; spins++)
+      if (spins > 2048) std::this_thread::yield();
+  }
+};
+inline HostPool& host_pool() {
+  static HostPool* p = new HostPool((int)std::min(15u, std::max(1u, std::thread::hardware_concurrency()) - 1));
+  return *p;
+}
+
 template <class F>
 void host_parallel(int64_t n, int64_t grain, F&& f) {
   static const int hw = std::max(1u, std::thread::hardware_concurrency());
@@ -875,11 +929,13 @@ void host_parallel(int64_t n, int64_t grain, F&& f) {
     f(0, n, 0);
     return;
   }
-  std::vector<std::thread> th;
-  th.reserve(T - 1);
-  for (int t = 1; t < T; t++) th.emplace_back([&, t] { f(n * t / T, n * (t + 1) / T, t); });
-  f(0, n / T, 0);
-  for (auto& x : th) x.join();
+  const std::function<void(int)> job = [&](int t) { f(n * t / T, n * (t + 1) / T, t); };
+  static const pid_t owner = getpid();
+  if (getpid() != owner) {  // a forked child has none of the pool's threads
+    for (int t = 0; t < T; t++) job(t);
+    return;
+  }
+  host_pool().run(T, job);
 }
 
 void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
@@ -972,7 +1028,20 @@ void graph_upload(sp_ctx* ctx, const sp_graph* g, sp_dgraph* dg) {
       SP_CUDA(cudaHostAlloc(&ctx->staging, total, cudaHostAllocDefault));
       ctx->staging_bytes = total;
     }
-    // host copies the library itself needs (string order, slot order, op validity)
+    // host copies the library itself needs (string order, slot order, op validity),
+    // in vectors a freed graph of this context left behind when there is one
+    if (!ctx->host_copies.empty()) {
+      HostGraphCopies& hc = ctx->host_copies.back();
+      dg->h_names.swap(hc.names);
+      dg->h_op.swap(hc.op);
+      dg->h_w_rank.swap(hc.w_rank);
+      dg->h_w_train.swap(hc.w_train);
+      dg->h_name_off.swap(hc.name_off);
+      dg->h_topo.swap(hc.topo);
+      dg->h_in_off.swap(hc.in_off);
+      dg->h_in_idx.swap(hc.in_idx);
+      ctx->host_copies.pop_back();
+    }
     dg->h_names.resize((size_t)nb);
     dg->h_name_off.resize((size_t)n + 1);
     dg->h_topo.resize((size_t)n);

@@ -236,6 +236,15 @@ template <class T>
 using PodVec = std::vector<T, NoInitAlloc<T>>;
 }  // namespace sp
 
+// The host copies a device graph keeps (sp_dgraph::h_*), recycled across
+// uploads by the context: a fresh 20 MB of host vectors per upload is ~5k
+// first-touch page faults (~1.2 ms at 10^5 nodes) on every e2e step.
+struct HostGraphCopies {
+  sp::PodVec<uint8_t> names, op, w_rank, w_train;
+  sp::PodVec<int64_t> name_off, topo, in_off;
+  sp::PodVec<int32_t> in_idx;
+};
+
 struct sp_ctx {
   int device = 0;
   int sm_count = 148;
@@ -265,6 +274,7 @@ struct sp_ctx {
   // resident CTAs per SM by (kernel, smem): the runtime query costs ~10 us per launch
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occupancy;
   std::vector<cudaEvent_t> event_pool;  // timing events of finished searches, reused
+  std::vector<HostGraphCopies> host_copies;  // spare sp_dgraph host vectors (graph_upload / sp_graph_free)
   // multi-GPU (comm.cu).  Every device is a lane: this context's own
   // communicator handle (ncclComm_t), its rank among `nranks`, and how the
   // lanes exchange their per-block records (SP_TRANSPORT_*).  A context made

@@ -575,90 +575,91 @@ __device__ __forceinline__ bool key3_less(uint64_t a1, uint64_t a2, int32_t av, 
   return a1 != b1 ? a1 < b1 : (a2 != b2 ? a2 < b2 : av < bv);
 }
 
-// The bitonic network of block_bitonic with every stage of stride < 64 in
-// registers: thread t (lane l of warp w) holds entries w*64 + l and w*64 + l + 32,
-// stride 32 is an in-thread exchange and strides < 32 are warp shuffles, so
-// only the stages of stride >= 64 go through shared memory (with a barrier):
-// for 1024 entries 10 barrier stages instead of 55.  Needs 64 <= P2 <= 2 * blockDim.x.
-__device__ void block_bitonic_reg(uint64_t* K1, uint64_t* K2, int32_t* V, int P2) {
-  const int t = threadIdx.x;
-  const bool act = t < (P2 >> 1);
-  const int lane = t & 31;
-  const int i0 = (t >> 5) * 64 + lane, i1 = i0 + 32;
-  uint64_t a1 = 0, a2 = 0, b1 = 0, b2 = 0;
-  int32_t av = 0, bv = 0;
-  auto load = [&] {
-    if (act) {
-      a1 = K1[i0]; a2 = K2[i0]; av = V[i0];
-      b1 = K1[i1]; b2 = K2[i1]; bv = V[i1];
-    }
-  };
-  auto store = [&] {
-    if (act) {
-      K1[i0] = a1; K2[i0] = a2; V[i0] = av;
-      K1[i1] = b1; K2[i1] = b2; V[i1] = bv;
-    }
-  };
-  // one element of a shuffle stage: keep the partner's entry when it belongs here
-  auto xchg = [&](uint64_t& x1, uint64_t& x2, int32_t& xv, int idx, int size, int stride) {
-    const uint64_t y1 = __shfl_xor_sync(0xffffffffu, x1, stride);
-    const uint64_t y2 = __shfl_xor_sync(0xffffffffu, x2, stride);
-    const int32_t yv = __shfl_xor_sync(0xffffffffu, xv, stride);
-    const bool lower = (idx & stride) == 0, up = (idx & size) == 0;
-    const bool y_lt = key3_less(y1, y2, yv, x1, x2, xv);
-    if (lower == up ? y_lt : !y_lt) {
-      x1 = y1;
-      x2 = y2;
-      xv = yv;
-    }
-  };
-  auto reg_stages = [&](int size, int smax) {
+// The bitonic network with every stage of stride < 64 in registers: a warp
+// loads a 64-entry chunk (lane l: entries 64c + l and 64c + l + 32), stride 32
+// is an in-thread exchange and strides < 32 are warp shuffles, so only stages
+// of stride >= 64 go through shared memory with a barrier (1024 entries: 10
+// barrier stages instead of 55).  Item: the entry's keys; load(i) / store(i, x)
+// read / write entry i, less(x, y) orders two entries (all distinct), shfl(x,
+// m) is __shfl_xor_sync of every field.  Any P2 >= 64 (a power of two), any
+// block size that is a multiple of 32.
+template <class Item, class Load, class Store, class Less, class Shfl>
+__device__ void bitonic_sort_reg(int P2, Load load, Store store, Less less, Shfl shfl) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const int nch = P2 >> 6;
+  auto stages = [&](Item& a, Item& b, int i0, int size, int smax) {
     for (int stride = smax; stride > 0; stride >>= 1) {
       if (stride == 32) {
-        const bool up = (i0 & size) == 0;
-        if (key3_less(b1, b2, bv, a1, a2, av) == up) {
-          uint64_t x = a1; a1 = b1; b1 = x;
-          x = a2; a2 = b2; b2 = x;
-          const int32_t y = av; av = bv; bv = y;
+        if (less(b, a) == ((i0 & size) == 0)) {
+          const Item x = a;
+          a = b;
+          b = x;
         }
       } else {
-        xchg(a1, a2, av, i0, size, stride);
-        xchg(b1, b2, bv, i1, size, stride);
+        const bool lower = (lane & stride) == 0;
+        const Item ya = shfl(a, stride), yb = shfl(b, stride);
+        const bool up_a = (i0 & size) == 0, up_b = ((i0 + 32) & size) == 0;
+        const bool lta = less(ya, a), ltb = less(yb, b);
+        if (lower == up_a ? lta : !lta) a = ya;
+        if (lower == up_b ? ltb : !ltb) b = yb;
       }
     }
   };
-  load();
-  for (int size = 2; size <= 64; size <<= 1) reg_stages(size, size >> 1);
+  for (int c = warp; c < nch; c += nw) {  // every size up to 64 inside each chunk
+    const int i0 = c * 64 + lane;
+    Item a = load(i0), b = load(i0 + 32);
+    for (int size = 2; size <= 64; size <<= 1) stages(a, b, i0, size, size >> 1);
+    store(i0, a);
+    store(i0 + 32, b);
+  }
+  __syncthreads();
   for (int size = 128; size <= P2; size <<= 1) {
-    store();
-    __syncthreads();
     for (int stride = size >> 1; stride >= 64; stride >>= 1) {
       for (int q = t; q < (P2 >> 1); q += blockDim.x) {
         const int i = ((q & ~(stride - 1)) << 1) | (q & (stride - 1));
         const int j = i + stride;
-        const bool gt = key3_less(K1[j], K2[j], V[j], K1[i], K2[i], V[i]);
-        if (gt == ((i & size) == 0)) {
-          const uint64_t x = K1[i], y = K2[i];
-          const int32_t z = V[i];
-          K1[i] = K1[j]; K2[i] = K2[j]; V[i] = V[j];
-          K1[j] = x; K2[j] = y; V[j] = z;
+        const Item x = load(i), y = load(j);
+        if (less(y, x) == ((i & size) == 0)) {
+          store(i, y);
+          store(j, x);
         }
       }
       __syncthreads();
     }
-    load();
-    reg_stages(size, 32);
+    for (int c = warp; c < nch; c += nw) {
+      const int i0 = c * 64 + lane;
+      Item a = load(i0), b = load(i0 + 32);
+      stages(a, b, i0, size, 32);
+      store(i0, a);
+      store(i0 + 32, b);
+    }
+    __syncthreads();
   }
-  store();
-  __syncthreads();
 }
+
+struct Key3 {
+  uint64_t k1, k2;
+  int32_t v;
+};
 
 // ascending by (K1, K2, V): rank counting when every entry has a thread, else
 // the bitonic network over P2 (a power of two >= n, padded with ~0 keys),
-// register-resident below stride 64 when the block has a thread per pair
+// register-resident below stride 64 (bitonic_sort_reg)
 __device__ void block_sort(uint64_t* K1, uint64_t* K2, int32_t* V, int n, int P2) {
   if (n <= RANK_SORT_MAX && n <= (int)blockDim.x) block_rank_sort(K1, K2, V, n);
-  else if (P2 >= 64 && (P2 >> 1) <= (int)blockDim.x && !SP_FOLD_NOREG) block_bitonic_reg(K1, K2, V, P2);
+  else if (P2 >= 64 && !SP_FOLD_NOREG)
+    bitonic_sort_reg<Key3>(
+        P2, [&](int i) { return Key3{K1[i], K2[i], V[i]}; },
+        [&](int i, const Key3& x) {
+          K1[i] = x.k1;
+          K2[i] = x.k2;
+          V[i] = x.v;
+        },
+        [](const Key3& x, const Key3& y) { return key3_less(x.k1, x.k2, x.v, y.k1, y.k2, y.v); },
+        [](const Key3& x, int m) {
+          return Key3{__shfl_xor_sync(0xffffffffu, x.k1, m), __shfl_xor_sync(0xffffffffu, x.k2, m),
+                      __shfl_xor_sync(0xffffffffu, x.v, m)};
+        });
   else block_bitonic(K1, K2, V, P2);
 }
 
@@ -1307,6 +1308,12 @@ __global__ void k_acc_insts(int64_t Ga, const int32_t* __restrict__ order, const
 constexpr int LS_CAP = 4096;
 constexpr int64_t LS_MAX_GROUPS = 1 << 20;  // nG scanned by one CTA
 
+struct Key4 {
+  uint64_t a0, a1;
+  uint32_t c;
+  int32_t ix;
+};
+
 __device__ __forceinline__ bool ls_less(uint32_t ca, uint64_t a0, uint64_t a1, int32_t ia, uint32_t cb, uint64_t b0,
                                         uint64_t b1, int32_t ib) {
   if (ca != cb) return ca < cb;
@@ -1389,6 +1396,21 @@ __global__ void __launch_bounds__(1024) k_level_small(
   }
   __syncthreads();
   // 3. bitonic sort by (class, k0, k1, j)
+  if (P2 >= 64) {
+    bitonic_sort_reg<Key4>(
+        P2, [&](int i) { return Key4{K0[i], K1[i], KC[i], IX[i]}; },
+        [&](int i, const Key4& x) {
+          KC[i] = x.c;
+          K0[i] = x.a0;
+          K1[i] = x.a1;
+          IX[i] = x.ix;
+        },
+        [](const Key4& x, const Key4& y) { return ls_less(x.c, x.a0, x.a1, x.ix, y.c, y.a0, y.a1, y.ix); },
+        [](const Key4& x, int m) {
+          return Key4{__shfl_xor_sync(0xffffffffu, x.a0, m), __shfl_xor_sync(0xffffffffu, x.a1, m),
+                      __shfl_xor_sync(0xffffffffu, x.c, m), __shfl_xor_sync(0xffffffffu, x.ix, m)};
+        });
+  } else {
   for (int size = 2; size <= P2; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int t = tid; t < (P2 >> 1); t += NT) {
@@ -1405,6 +1427,7 @@ __global__ void __launch_bounds__(1024) k_level_small(
       }
       __syncthreads();
     }
+  }
   // 4. class heads, tie check (two instance components of a class equal on 16 bytes)
   for (int p = tid; p < Ga; p += NT) {
     const bool hd = p == 0 || KC[p] != KC[p - 1];

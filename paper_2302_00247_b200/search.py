@@ -857,10 +857,15 @@ def derive_plan(graph, mesh, min_duplicates: int = 2, mu: int = 1 << 20,
             gc.enable()
 
 
-#: blocks with fewer candidates than this are scored in a first, separate launch
-#: (when there are at least SPLIT_MIN_SMALL_BLOCKS of them and the remaining
-#: blocks hold at least SPLIT_MIN_BIG_CANDIDATES candidates)
-SMALL_BLOCK_CANDIDATES = 1 << 16
+#: blocks with fewer candidates than this are scored in a first, separate
+#: launch (when there are at least SPLIT_MIN_SMALL_BLOCKS of them and the
+#: remaining blocks hold at least SPLIT_MIN_BIG_CANDIDATES candidates).  The
+#: group then runs as the library's one-kernel small search (one CTA per block):
+#: c5's 1002 blocks of <= 64 candidates in one k_search_small launch instead of
+#: the item scorer + k_reduce + k_explain_fast; its 10 blocks of 1.5e3-5.9e4
+#: candidates join the expensive group (at 8192, one CTA walking a 6561-candidate
+#: block made the launch 0.23 ms)
+SMALL_BLOCK_CANDIDATES = 1024
 SPLIT_MIN_SMALL_BLOCKS = 64
 SPLIT_MIN_BIG_CANDIDATES = float(1 << 26)
 

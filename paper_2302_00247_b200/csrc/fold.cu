@@ -26,6 +26,7 @@
 // The host then orders the result the way the reference's string sorts do
 // (instances and blocks by prefix string, template by topological rank).
 #include <cub/cub.cuh>
+#include <cuda_pipeline.h>
 
 #include <algorithm>
 #include <atomic>
@@ -543,6 +544,25 @@ __device__ void copy_in(uint8_t* dst, const uint8_t* src, size_t bytes) {
 #ifndef SP_FOLD_NOREG
 #define SP_FOLD_NOREG 0
 #endif
+// global -> shared copy issued as asynchronous 16-byte copies (LDGSTS) when
+// both ends are 16-byte aligned, so the staging copies of several arrays are
+// all in flight together (one memory latency, not one per array); the caller
+// commits and waits (copy_in_wait).  Unaligned copies fall back to copy_in.
+__device__ void copy_in_async(uint8_t* dst, const uint8_t* src, size_t bytes) {
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) != 0) {
+    copy_in(dst, src, bytes);
+    return;
+  }
+  const size_t w = bytes >> 4;
+  for (size_t i = threadIdx.x; i < w; i += blockDim.x) __pipeline_memcpy_async(dst + 16 * i, src + 16 * i, 16);
+  for (size_t i = (w << 4) + threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+__device__ __forceinline__ void copy_in_wait() {
+  __pipeline_commit();
+  __pipeline_wait_prior(0);
+  __syncthreads();
+}
+
 constexpr int RANK_SORT_MAX = 256;  // n^2 compares beat the bitonic network's barriers up to here
 // Ascending (K1, K2, V) order of n <= blockDim.x distinct entries by rank
 // counting: thread i counts the entries below its own (broadcast shared reads,
@@ -703,15 +723,15 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
   SMALL_PTR(const int32_t*, in_idx);
 #undef SMALL_PTR
   if (STG) {
-    copy_in((uint8_t*)name_off, (const uint8_t*)a.name_off, (size_t)(n + 1) * 8);
-    copy_in((uint8_t*)names, a.names, (size_t)a.name_bytes);
-    copy_in((uint8_t*)op, a.op, (size_t)n);
-    copy_in((uint8_t*)w_rank, a.w_rank, (size_t)n);
-    copy_in((uint8_t*)w_train, a.w_train, (size_t)n);
-    copy_in((uint8_t*)w_shape, (const uint8_t*)a.w_shape, (size_t)n * SP_MAX_RANK * 8);
-    copy_in((uint8_t*)in_off, (const uint8_t*)a.in_off, (size_t)(n + 1) * 8);
-    copy_in((uint8_t*)in_idx, (const uint8_t*)a.in_idx, (size_t)a.n_edges * 4);
-    __syncthreads();
+    copy_in_async((uint8_t*)name_off, (const uint8_t*)a.name_off, (size_t)(n + 1) * 8);
+    copy_in_async((uint8_t*)names, a.names, (size_t)a.name_bytes);
+    copy_in_async((uint8_t*)op, a.op, (size_t)n);
+    copy_in_async((uint8_t*)w_rank, a.w_rank, (size_t)n);
+    copy_in_async((uint8_t*)w_train, a.w_train, (size_t)n);
+    copy_in_async((uint8_t*)w_shape, (const uint8_t*)a.w_shape, (size_t)n * SP_MAX_RANK * 8);
+    copy_in_async((uint8_t*)in_off, (const uint8_t*)a.in_off, (size_t)(n + 1) * 8);
+    copy_in_async((uint8_t*)in_idx, (const uint8_t*)a.in_idx, (size_t)a.n_edges * 4);
+    copy_in_wait();
   }
   PROF();
   for (int i = tid; i < n; i += NT) {

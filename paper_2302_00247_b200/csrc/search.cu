@@ -366,6 +366,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
   __shared__ int16_t s_outpool[MAXT];
   __shared__ int8_t s_skipm[MAXT], s_rslot[MAXT], s_eslot[MAXT];
   __shared__ uint8_t s_rr[64];
+  __shared__ unsigned long long s_tms, s_tmb;  // trainable-weight field masks (BlobHeader)
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const int64_t e0 = tmpl_off[b];
     const int T = (int)(tmpl_off[b + 1] - e0);
@@ -390,6 +391,7 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
     }
     for (int q = threadIdx.x; q < 128; q += blockDim.x) blob[H.zero_off + q] = 0;
     if (threadIdx.x == 0) {
+      s_tms = s_tmb = 0;
       BlobHeader h = H;
       h.multi_dev = M.d > 1;
       h.setup = M.setup;
@@ -399,6 +401,11 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
       h.keep_bwd = dadd(1.0, -mesh.overlap_fraction);
       h.mu = mu;
       h.chunk = chunk;
+      uint64_t bias = 0;
+      for (int q = 0; q < V && V <= 32; q++) bias |= (uint64_t)(((radix3 >> q) & 1) ? 1 : 2) << (2 * (V - 1 - q));
+      h.bias = bias;
+      h.tmask_small = h.tmask_big = 0;
+      h.pad4 = 0;
       *(BlobHeader*)blob = h;
     }
     __syncthreads();
@@ -538,7 +545,14 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         td.size = G.w_bytes[n];
         td.uterm = dadd(M.setup, cost_bytes(C_AR, td.size, M));
         ((TrainDesc*)(blob + H.train_off))[L.train_idx] = td;
+        if (H.V <= 32 && td.slot >= 0)
+          atomicOr(td.size >= mu ? &s_tmb : &s_tms, 1ULL << (2 * (H.V - 1 - td.slot)));
       }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ((BlobHeader*)blob)->tmask_small = s_tms;
+      ((BlobHeader*)blob)->tmask_big = s_tmb;
     }
     // routing byte tables: key = Horner(digit, s_0, ..., s_{k-1}) in base 3
     const uint32_t nkeys = s_kbase[T];
@@ -1191,27 +1205,37 @@ __device__ __forceinline__ uint32_t bdigit(const BlobHeader& H, uint64_t y, int 
   return (uint32_t)((y >> (2 * (H.V - 1 - q))) & 3) - (4 - r);
 }
 
+// pack_gradients (rewrite.py:78-111) of a replicated-gradient plan on the
+// biased digit word: the trainable weights whose digit is 0 come from one
+// compare against the all-zero word (bit 2k of z: field k holds digit 0), and
+// only those are visited, highest field first -- enumeration order, which is
+// template order, which is the TrainDesc order (q = trainable fields above).
 __device__ __forceinline__ double backward_b(const Tabs& S, uint64_t y) {
   const BlobHeader& H = *S.H;
   double bwd = 0.0;
   if (!H.multi_dev) return bwd;
+  const uint64_t e = y ^ H.bias;
+  const uint64_t z = ~(e | (e >> 1)) & 0x5555555555555555ULL;
+  const uint64_t tall = H.tmask_small | H.tmask_big;
   long long cur = 0;
   int cur_n = 0;
-  for (int q = 0; q < H.nt; q++) {
-    const TrainDesc td = S.trn[q];
-    if (bdigit(H, y, td.slot) != 0 || td.size >= H.mu) continue;
-    if (cur + td.size > H.chunk && cur_n) {
+  for (uint64_t m = z & H.tmask_small; m;) {
+    const int bit = 63 - __clzll(m);
+    m &= ~(1ULL << bit);
+    const int64_t size = S.trn[__popcll(bit < 62 ? tall >> (bit + 2) : 0ULL)].size;
+    if (cur + size > H.chunk && cur_n) {
       bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
       cur = 0;
       cur_n = 0;
     }
-    cur += td.size;
+    cur += size;
     cur_n++;
   }
   if (cur_n) bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
-  for (int q = 0; q < H.nt; q++) {
-    const TrainDesc td = S.trn[q];
-    if (bdigit(H, y, td.slot) == 0 && td.size >= H.mu) bwd = dadd(bwd, td.uterm);
+  for (uint64_t m = z & H.tmask_big; m;) {
+    const int bit = 63 - __clzll(m);
+    m &= ~(1ULL << bit);
+    bwd = dadd(bwd, S.trn[__popcll(bit < 62 ? tall >> (bit + 2) : 0ULL)].uterm);
   }
   return bwd;
 }
@@ -1527,7 +1551,15 @@ __device__ __forceinline__ void score_chunk(const Tabs& S, const Biased& bz, con
       if (active) {
         const NodeSkip sk = S.skip[fail];
         const unsigned long long x = base + lane;
-        const unsigned long long t = sk.R ? (x / sk.R + 1) * sk.R : whi;
+        unsigned long long t;
+        if (!sk.R) {
+          t = whi;
+        } else if (whi <= 0xFFFFFFFFull) {  // 32-bit division (the 64-bit one is a long subroutine)
+          const uint32_t x32 = (uint32_t)x, r32 = (uint32_t)sk.R;
+          t = (unsigned long long)(x32 - x32 % r32) + r32;
+        } else {
+          t = (x / sk.R + 1) * sk.R;
+        }
         adv = (uint32_t)(min(t, whi) - base);
       }
     }

@@ -404,6 +404,10 @@ struct BlobHeader {
   // lean walk (biased digits): FastNode[T], a zero block, (reach, state) offset
   // pairs of producers of fan-in >= 3 nodes, and 4-row routing tables
   int32_t fast_off, zero_off, fprod_off, tab4_off;
+  // pack_gradients on the biased digit word (V <= 32): bias = the word of all-zero
+  // digits; bit 2(V-1-q) of tmask_small / tmask_big set when enumeration
+  // position q holds a trainable weight smaller than / at least mu
+  uint64_t bias, tmask_small, tmask_big, pad4;
 };
 static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
 

@@ -9,9 +9,9 @@ cd "$(dirname "$0")/.."
 NAME=${1:-r2_k_score_c5_walk}
 MODE=${2:-walk}
 KREGEX=${3:-k_score_flow}
-# the c5 search launches the cheap-block group first: skip its kernel
+# the c5 search launches the residual group first: with k_score_flow it runs as k_search_small now (SKIP=0)
 mkdir -p gpurun_out
-ncu --set full --clock-control none --import-source on -k "regex:${KREGEX}" --launch-skip ${SKIP:-1} -c 1 -f \
+ncu --set full --clock-control none --import-source on -k "regex:${KREGEX}" --launch-skip ${SKIP:-0} -c 1 -f \
     -o gpurun_out/${NAME} python tools/ncu_target.py c5 ${MODE} 1 > gpurun_out/${NAME}.log 2>&1
 SHA=$(python -c "import bench; print(bench.kernel_sass_sha())")
 CANDS=$(python -c "import json; print(json.load(open('tests/golden/c5_full.json'))['candidates'])")

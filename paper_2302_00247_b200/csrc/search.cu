@@ -1940,6 +1940,9 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
   __shared__ uint64_t s_lane_add[32];
   __shared__ Biased s_bz;
   __shared__ uint64_t s_p2[64];  // unbiased digits of 2^k * CH (mixed radix, wrapping)
+  // unbiased digits of j * CH and of j * 1024 * CH (j < 1024): a chunk's start
+  // digits in two adds instead of one per set bit of the chunk index
+  __shared__ uint64_t s_lo[1024], s_hi[1024];
   __shared__ uint64_t s_sub[SKIP_SUB];  // unbiased digits of k * CH / SKIP_SUB
   // the chunk the CTA claimed before staging block b, in s_first[b & 1]: thread 0
   // writes block b+1's claim while slower threads may still read block b's
@@ -1992,6 +1995,20 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
       }
     }
     __syncthreads();
+    {
+      const uint64_t B = s_bz.B;
+      for (int j = tid; j < 1024; j += THREADS) {
+        uint64_t lo = 0, hi = 0;
+        for (int k = 0; k < 10; k++)
+          if ((j >> k) & 1) {
+            lo = badd(badd(B, lo, B), s_p2[k], B) - B;
+            hi = badd(badd(B, hi, B), s_p2[k + 10], B) - B;
+          }
+        s_lo[j] = lo;
+        s_hi[j] = hi;
+      }
+    }
+    __syncthreads();
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
     const uint32_t rec0 = opaque_u32((uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)H.fast_off);
@@ -2016,8 +2033,9 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score_skip(con
         continue;
       }
       const uint32_t rem = (uint32_t)min((unsigned long long)(j < nbig ? CH : CH / SKIP_SUB), C - start);
-      uint64_t w = s_bz.B;  // biased digits of c * CH: one add per set bit of c
-      for (unsigned long long m = c; m; m &= m - 1) w = badd(w, s_p2[__ffsll((long long)m) - 1], s_bz.B);
+      // biased digits of c * CH: the two table entries of its low 20 bits, one add per higher set bit
+      uint64_t w = badd(badd(s_bz.B, s_hi[(c >> 10) & 1023], s_bz.B), s_lo[c & 1023], s_bz.B);
+      for (unsigned long long m = c >> 20; m; m &= m - 1) w = badd(w, s_p2[20 + __ffsll((long long)m) - 1], s_bz.B);
       w = badd(badd(w, s_sub[part], s_bz.B), s_lane_add[lane], s_bz.B);
       score_chunk<true, false>(S, s_bz, s_lane_add, rec0, rb, sb, lane, w, rem, start + rem, lb);
       j = __shfl_sync(0xffffffffu, jn, 0);

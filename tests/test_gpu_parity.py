@@ -885,3 +885,20 @@ def test_one_kernel_small_search_equals_item_path(backend, seed, mode, monkeypat
     finally:
         backend.set_mode("skip")
     assert got == ref
+
+
+@pytest.mark.parametrize("layers", [80, 300, 560])
+def test_one_cta_fold_sizes_vs_oracle(backend, layers):
+    """The one-CTA fold between 1k and 8k GraphNodes (its sorts run the
+    register bitonic over 2k-8k entries, several 64-entry chunks per warp):
+    every array of the partition equals the oracle's."""
+    from oracle import oracle
+    from paper_2302_00247_b200.workloads import transformer_stack_lowered
+
+    low = transformer_stack_lowered(layers)
+    assert 1024 < low.n_nodes <= 8192
+    dg = backend.upload(low)
+    ba = backend.fold(dg, 2)
+    ob = oracle.prune(low, 2)
+    for k in ("block_T", "block_inst_off", "block_member_off", "inst_prefix_len", "members"):
+        assert np.array_equal(np.asarray(getattr(ba, k), np.int64), np.asarray(ob[k], np.int64)), k

@@ -281,6 +281,8 @@ __host__ __device__ inline void layout_serial(int T, const IDX* kk, const int* l
   off = align16(off + 8 * ndbl);
   H.train_off = (int32_t)off;
   off = align16(off + (int64_t)sizeof(TrainDesc) * nt);
+  H.tslot_off = (int32_t)off;
+  off = align16(off + 16 * (int64_t)V);
   H.fast_off = (int32_t)off;
   off = align16(off + (int64_t)sizeof(FastNode) * T);
   H.zero_off = (int32_t)off;
@@ -545,8 +547,11 @@ __global__ void k_fill(GraphView G, const int64_t* tmpl_off, const int32_t* tmpl
         td.size = G.w_bytes[n];
         td.uterm = dadd(M.setup, cost_bytes(C_AR, td.size, M));
         ((TrainDesc*)(blob + H.train_off))[L.train_idx] = td;
-        if (H.V <= 32 && td.slot >= 0)
+        if (H.V <= 32 && td.slot >= 0) {
           atomicOr(td.size >= mu ? &s_tmb : &s_tms, 1ULL << (2 * (H.V - 1 - td.slot)));
+          ((double*)(blob + H.tslot_off))[td.slot] = td.uterm;
+          ((int64_t*)(blob + H.tslot_off + 8 * H.V))[td.slot] = td.size;
+        }
       }
     }
     __syncthreads();
@@ -665,6 +670,8 @@ struct Tabs {
   const uint8_t* tab;
   const double* dbl;
   const TrainDesc* trn;
+  const double* tuterm;   // by enumeration position (backward_b)
+  const int64_t* tsize;
   double* reach;
   uint8_t* stp;
 };
@@ -681,6 +688,8 @@ __device__ __forceinline__ Tabs tabs_of(uint8_t* smem) {
   S.tab = smem + H.tab_off;
   S.dbl = (const double*)(smem + H.dbl_off);
   S.trn = (const TrainDesc*)(smem + H.train_off);
+  S.tuterm = (const double*)(smem + H.tslot_off);
+  S.tsize = (const int64_t*)(smem + H.tslot_off + 8 * H.V);
   S.reach = (double*)(smem + ((H.bytes + 15) & ~15));
   S.stp = (uint8_t*)(S.reach + (size_t)H.npool * THREADS);
   return S;
@@ -1209,20 +1218,21 @@ __device__ __forceinline__ uint32_t bdigit(const BlobHeader& H, uint64_t y, int 
 // biased digit word: the trainable weights whose digit is 0 come from one
 // compare against the all-zero word (bit 2k of z: field k holds digit 0), and
 // only those are visited, highest field first -- enumeration order, which is
-// template order, which is the TrainDesc order (q = trainable fields above).
+// template order (the sums' order); sizes and unfused terms are read by
+// enumeration position.
 __device__ __forceinline__ double backward_b(const Tabs& S, uint64_t y) {
   const BlobHeader& H = *S.H;
   double bwd = 0.0;
   if (!H.multi_dev) return bwd;
   const uint64_t e = y ^ H.bias;
   const uint64_t z = ~(e | (e >> 1)) & 0x5555555555555555ULL;
-  const uint64_t tall = H.tmask_small | H.tmask_big;
+  const int top = H.V - 1;
   long long cur = 0;
   int cur_n = 0;
   for (uint64_t m = z & H.tmask_small; m;) {
     const int bit = 63 - __clzll(m);
     m &= ~(1ULL << bit);
-    const int64_t size = S.trn[__popcll(bit < 62 ? tall >> (bit + 2) : 0ULL)].size;
+    const int64_t size = S.tsize[top - (bit >> 1)];
     if (cur + size > H.chunk && cur_n) {
       bwd = dadd(bwd, dadd(H.setup, dmul(ddiv(dmul(H.c_ar, (double)cur), H.bw), H.eff_ar)));
       cur = 0;
@@ -1235,7 +1245,7 @@ __device__ __forceinline__ double backward_b(const Tabs& S, uint64_t y) {
   for (uint64_t m = z & H.tmask_big; m;) {
     const int bit = 63 - __clzll(m);
     m &= ~(1ULL << bit);
-    bwd = dadd(bwd, S.trn[__popcll(bit < 62 ? tall >> (bit + 2) : 0ULL)].uterm);
+    bwd = dadd(bwd, S.tuterm[top - (bit >> 1)]);
   }
   return bwd;
 }

@@ -407,7 +407,9 @@ struct BlobHeader {
   // pack_gradients on the biased digit word (V <= 32): bias = the word of all-zero
   // digits; bit 2(V-1-q) of tmask_small / tmask_big set when enumeration
   // position q holds a trainable weight smaller than / at least mu
-  uint64_t bias, tmask_small, tmask_big, pad4;
+  uint64_t bias, tmask_small, tmask_big;
+  int32_t tslot_off;  // double uterm[V], then int64 size[V]: each trainable weight's by enumeration position
+  int32_t pad4;
 };
 static_assert(sizeof(BlobHeader) % 16 == 0, "blob header must stay 16-byte aligned");
 

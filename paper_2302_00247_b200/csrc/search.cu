@@ -30,7 +30,12 @@ namespace {
 constexpr int KMAX = 6;          // internal producers handled by a lookup table
 constexpr int MAXT = 256;        // template nodes per block (SP_EXPLAIN_MAX_T)
 constexpr int THREADS = 256;     // scoring CTA size
-constexpr int ITEM_ITERS_MAX = 256;        // work item = THREADS * iters candidates
+// (-DSP_ITEM_ITERS for A/B builds: 256 / 128 / 64 give c5 32.5 / 31.9 / 31.9 ms --
+// a one-GPU search's last wave of items is its tail)
+#ifndef SP_ITEM_ITERS
+#define SP_ITEM_ITERS 128
+#endif
+constexpr int ITEM_ITERS_MAX = SP_ITEM_ITERS;  // work item = THREADS * iters candidates
 constexpr int ITEM_ITERS_MAX_SKIP = 512;   // ... when prefix skipping is on
 // work items per resident CTA a search aims for (a rank's last wave of items is
 // its tail: at 8 ranks c5's 65536-candidate items left ~12 per CTA; 8 / 32 / 64 /
@@ -1437,7 +1442,12 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
 // same work decomposition and argmin as k_score, with the lean FastNode walk.
 // Each lane carries its own candidate's digit word and advances it by 32 per
 // warp step (one carry-fixed add); the warp's remaining count is 32-bit.
-constexpr int PAIR_CHUNK = 512;   // candidates per warp chunk, walk modes
+// (-DSP_PAIR_CHUNK for A/B builds: 256 / 512 / 1024 / 2048 / 4096 give c5 32.7 / 32.0 /
+// 31.7 / 31.65 / 31.8 ms with 32768-candidate items)
+#ifndef SP_PAIR_CHUNK
+#define SP_PAIR_CHUNK 2048
+#endif
+constexpr int PAIR_CHUNK = SP_PAIR_CHUNK;  // candidates per warp chunk, walk modes
 constexpr int PAIR_MAX_CHUNKS = ITEM_ITERS_MAX * THREADS / PAIR_CHUNK;
 #ifndef SP_SKIP_CHUNK
 #define SP_SKIP_CHUNK 4096

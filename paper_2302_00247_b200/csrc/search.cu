@@ -1443,9 +1443,10 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
 // Each lane carries its own candidate's digit word and advances it by 32 per
 // warp step (one carry-fixed add); the warp's remaining count is 32-bit.
 // (-DSP_PAIR_CHUNK for A/B builds: 256 / 512 / 1024 / 2048 / 4096 give c5 32.7 / 32.0 /
-// 31.7 / 31.65 / 31.8 ms with 32768-candidate items)
+// 31.7 / 31.65 / 31.8 ms with 32768-candidate items; at 8 ranks 1024 beats 2048,
+// 4.28 vs 4.35 ms per share)
 #ifndef SP_PAIR_CHUNK
-#define SP_PAIR_CHUNK 2048
+#define SP_PAIR_CHUNK 1024
 #endif
 constexpr int PAIR_CHUNK = SP_PAIR_CHUNK;  // candidates per warp chunk, walk modes
 constexpr int PAIR_MAX_CHUNKS = ITEM_ITERS_MAX * THREADS / PAIR_CHUNK;
@@ -3706,6 +3707,12 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
                                                                    : ITEMS_PER_CTA;  // (A/B override)
   unsigned long long iters = (per_rank + slots * ipc * THREADS - 1) / (slots * ipc * THREADS);
   iters = std::max<unsigned long long>(1, std::min<unsigned long long>(iters, memo ? ITEM_ITERS_MAX_SKIP : cap));
+  // the paired walk hands items out in PAIR_CHUNK-candidate warp chunks: an item
+  // smaller than one chunk per warp leaves warps idle (8-rank c5 share: 13k-
+  // candidate items, 4.30 -> 4.42 ms) -- unless the search is too small to
+  // give every CTA such an item
+  const unsigned long long min_iters = (unsigned long long)(THREADS / 32) * PAIR_CHUNK / THREADS;
+  if (pair && iters < min_iters && per_rank >= slots * min_iters * THREADS) iters = min_iters;
   const unsigned long long item_cands = iters * THREADS;
   std::vector<unsigned long long> lo(nb), hi(nb), base(nb + 1, 0);
   unsigned long long gbase = 0;

@@ -655,7 +655,7 @@ __device__ __forceinline__ void mr_add(uint64_t& w0, uint64_t& w1, uint32_t t, i
 struct ScorePlan {
   const int64_t* blob_off;
   unsigned long long item_cands;        // candidates per work item
-  unsigned long long item_stride;       // index distance between a rank's consecutive items
+  const unsigned long long* stride;     // per block: index distance between a rank's consecutive items
   const unsigned long long* lo;         // per block start (enumeration index space)
   const unsigned long long* hi;
   const unsigned long long* item_base;  // prefix sum of items per block, [nb+1]
@@ -1337,7 +1337,7 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
     const Biased bz = s_bz;
-    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_stride;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.stride[b];
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     const unsigned long long span = (ihi - ilo + (THREADS / 32) - 1) / (THREADS / 32);
     const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
@@ -1660,13 +1660,13 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
       staged = b;
     }
     if (tid == 0) {
-      s_wbase = bencode(*(const BlobHeader*)smem, P.lo[b] + (item - P.item_base[b]) * P.item_stride);
+      s_wbase = bencode(*(const BlobHeader*)smem, P.lo[b] + (item - P.item_base[b]) * P.stride[b]);
       s_chunk = 0;
     }
     __syncthreads();
     const Tabs S = tabs_of(smem);
     const BlobHeader& H = *S.H;
-    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_stride;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.stride[b];
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     unsigned long long best_t = ~0ULL, best_i = ~0ULL;
     uint32_t best_n = 0xFFFFFFFFu, nvalid = 0;
@@ -1787,7 +1787,7 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
         if (P.item_base[mid] <= it) lo = mid;
         else hi = mid;
       }
-      const unsigned long long ilo = P.lo[lo] + (it - P.item_base[lo]) * P.item_stride;
+      const unsigned long long ilo = P.lo[lo] + (it - P.item_base[lo]) * P.stride[lo];
       const unsigned long long ihi = min(ilo + P.item_cands, P.hi[lo]);
       sl.item = it;
       sl.block = lo;
@@ -2192,7 +2192,7 @@ __global__ void __launch_bounds__(THREADS_M, 4) k_score_memo(const uint8_t* __re
     double* cache = (double*)(smem + ((H.bytes + 15) & ~15));
     Tabs S = tabs_of(smem);
     const int T = H.T;
-    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.item_stride;
+    const unsigned long long ilo = P.lo[b] + (item - P.item_base[b]) * P.stride[b];
     const unsigned long long ihi = min(ilo + P.item_cands, P.hi[b]);
     const unsigned long long span = (ihi - ilo + (THREADS_M / 32) - 1) / (THREADS_M / 32);
     const unsigned long long wlo = min(ilo + span * warp, ihi), whi = min(wlo + span, ihi);
@@ -3714,17 +3714,49 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   const unsigned long long min_iters = (unsigned long long)(THREADS / 32) * PAIR_CHUNK / THREADS;
   if (pair && iters < min_iters && per_rank >= slots * min_iters * THREADS) iters = min_iters;
   const unsigned long long item_cands = iters * THREADS;
-  std::vector<unsigned long long> lo(nb), hi(nb), base(nb + 1, 0);
-  unsigned long long gbase = 0;
+  // rank 0 assembles the report after its share (root_only): at 4+ ranks it is
+  // relieved of whole blocks worth <= SP_ROOT_RELIEF% (default 10) of a share --
+  // the second-largest blocks down -- dealt over ranks 1..N-1 instead
+  std::vector<char> excl(nb, 0);
+  {
+    const long relief_pct = getenv("SP_ROOT_RELIEF") ? strtol(getenv("SP_ROOT_RELIEF"), nullptr, 10) : 10;
+    if (N >= 4 && relief_pct > 0) {
+      std::vector<int64_t> order(nb);
+      for (int64_t b = 0; b < nb; b++) order[b] = b;
+      std::sort(order.begin(), order.end(), [&](int64_t a, int64_t c) {
+        return t->hdr[a].C != t->hdr[c].C ? t->hdr[a].C > t->hdr[c].C : a < c;
+      });
+      const double budget = (double)relief_pct / 100.0 * (double)total / (double)N;
+      double used = 0.0;
+      for (size_t k = 1; k < order.size(); k++) {
+        const double share = (double)t->hdr[order[k]].C / (double)N;
+        if (used + share <= budget) {
+          excl[order[k]] = 1;
+          used += share;
+        }
+      }
+    }
+  }
+  std::vector<unsigned long long> lo(nb), hi(nb), base(nb + 1, 0), stride(nb);
+  unsigned long long gbase = 0, gex = 0;
   for (int64_t b = 0; b < nb; b++) {
     const unsigned long long C = t->hdr[b].C;
     const unsigned long long nch = C / item_cands + (C % item_cands ? 1 : 0);
-    const unsigned long long j0 = (r + N - gbase % N) % N;  // first item of block b dealt to this rank
-    const unsigned long long cnt = j0 < nch ? (nch - 1 - j0) / N + 1 : 0;
+    unsigned long long j0, cnt, M;
+    if (excl[b]) {  // dealt over ranks 1..N-1
+      M = N - 1;
+      j0 = r == 0 ? nch : (r - 1 + M - gex % M) % M;
+      gex += nch;
+    } else {
+      M = N;
+      j0 = (r + N - gbase % N) % N;  // first item of block b dealt to this rank
+      gbase += nch;
+    }
+    cnt = j0 < nch ? (nch - 1 - j0) / M + 1 : 0;
     lo[b] = j0 < nch ? j0 * item_cands : C;
     hi[b] = C;
+    stride[b] = M * item_cands;
     base[b + 1] = base[b] + cnt;
-    gbase += nch;
   }
   const unsigned long long n_items = base[nb];
   if (n_items == 0) {
@@ -3741,13 +3773,14 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   for (int64_t b = 0; b < nb; b++) max_items = std::max(max_items, base[b + 1] - base[b]);
   const bool two_pass = max_items > 2 * REDUCE_CHUNK;
   // one small H2D for the plan: lo | hi | base | counter (| chunk_base)
-  std::vector<unsigned long long> plan(3 * nb + 2 + (two_pass ? nb + 1 : 0), 0);
+  std::vector<unsigned long long> plan(4 * nb + 2 + (two_pass ? nb + 1 : 0), 0);
   std::copy(lo.begin(), lo.end(), plan.begin());
   std::copy(hi.begin(), hi.end(), plan.begin() + nb);
   std::copy(base.begin(), base.end(), plan.begin() + 2 * nb);
+  std::copy(stride.begin(), stride.end(), plan.begin() + 3 * nb + 2);
   unsigned long long n_chunks = 0;
   if (two_pass) {
-    unsigned long long* cb = plan.data() + 3 * nb + 2;
+    unsigned long long* cb = plan.data() + 4 * nb + 2;
     for (int64_t b = 0; b < nb; b++) {
       cb[b] = n_chunks;
       n_chunks += (base[b + 1] - base[b] + REDUCE_CHUNK - 1) / REDUCE_CHUNK;
@@ -3763,15 +3796,15 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   alloc_dout(pd, t, s, must_out);
   tr.mark("upload+alloc");
   unsigned long long* counter = dplan.p + 3 * nb + 1;
-  ScorePlan P{t->d_blob_off.p, item_cands, item_cands * N, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb, n_items,
-              ctx->skip};
+  ScorePlan P{t->d_blob_off.p, item_cands, dplan.p + 3 * nb + 2, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb,
+              n_items, ctx->skip};
   const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
   SP_CUDA(cudaEventRecord(pd.ev[1], s));
   SP_LAUNCH(ctx, kern, (unsigned)grid, threads, smem_k, s, t->blobs.p, P, items.p, counter);
   SP_CUDA(cudaEventRecord(pd.ev[2], s));
   tr.mark("score launch");
   if (two_pass) {
-    const unsigned long long* d_cb = dplan.p + 3 * nb + 2;
+    const unsigned long long* d_cb = dplan.p + 4 * nb + 2;
     SP_LAUNCH(ctx, k_reduce_chunks, (unsigned)std::min<unsigned long long>(n_chunks, 65535), THREADS, 0, s, items.p,
               dplan.p + 2 * nb, d_cb, nb, n_chunks, items.p + n_items);
     SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p + n_items, d_cb, nb,

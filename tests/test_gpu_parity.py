@@ -902,3 +902,36 @@ def test_one_cta_fold_sizes_vs_oracle(backend, layers):
     ob = oracle.prune(low, 2)
     for k in ("block_T", "block_inst_off", "block_member_off", "inst_prefix_len", "members"):
         assert np.array_equal(np.asarray(getattr(ba, k), np.int64), np.asarray(ob[k], np.int64)), k
+
+
+@pytest.mark.parametrize("relief", ["0", "10", "100"])
+@pytest.mark.parametrize("seed", [3, 11, 19])
+def test_root_relief_deal_merges_exactly(backend, seed, relief, monkeypatch):
+    """At 4+ ranks rank 0 is dealt none of the items of some blocks (dealt over
+    ranks 1..N-1 instead: SP_ROOT_RELIEF percent of a share; 100 = every block but
+    the largest): the shards still partition every block exactly."""
+    monkeypatch.setenv("SP_ROOT_RELIEF", relief)
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.dist import merge_scores
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=5, reps=(2, 6), ops=(3, 12)))
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 2, session=ses)
+    off, nodes = ba.templates_csr()
+    t = backend.tables(ses.dgraph, off, nodes, ClusterSpec.from_mesh("2x4"), 1 << 20, 4 << 20)
+    try:
+        if t.overflow:
+            pytest.skip("random block beyond u64")
+        backend.set_mode("walk")
+        full = backend.score(t)
+        key = [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split) for r in full]
+        for n in (4, 5, 8):
+            merged = merge_scores([backend.score(t, s, n) for s in range(n)])
+            assert [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split)
+                    for r in merged] == key, n
+    finally:
+        backend.set_mode("skip")
+        t.close()

@@ -662,6 +662,17 @@ struct ScorePlan {
   int64_t nb;
   unsigned long long n_items;
   int skip;                             // exact prefix-failure skipping on/off
+  // k_score_flow walk, the final wave: claims from n_main on are sub-items (a
+  // 1/split part of one of the rank's last items of block fblk[e], walked in
+  // FLOW_SUB warp chunks); item outputs of block b at obase[b] .. obase[b + 1]
+  // (its whole items, then its sub-items).  Without a split: n_main = n_items,
+  // obase = item_base.
+  const unsigned long long* obase = nullptr;
+  const unsigned long long* fblk = nullptr;   // [nf] block of each sub-item run (ascending)
+  const unsigned long long* fbase = nullptr;  // [nf + 1] claim offsets (from n_main) of the runs
+  int64_t nf = 0;
+  unsigned long long n_main = ~0ULL;
+  unsigned long long split = 1, sub = 0;      // parts per split item, candidates per part
 };
 
 // Pointers into a block's tables staged in shared memory.
@@ -1450,6 +1461,10 @@ __global__ void __launch_bounds__(THREADS, SP_SCORE_MIN_BLOCKS) k_score(const ui
 #endif
 constexpr int PAIR_CHUNK = SP_PAIR_CHUNK;  // candidates per warp chunk, walk modes
 constexpr int PAIR_MAX_CHUNKS = ITEM_ITERS_MAX * THREADS / PAIR_CHUNK;
+#ifndef SP_FLOW_SUB
+#define SP_FLOW_SUB 256
+#endif
+constexpr uint32_t FLOW_SUB = SP_FLOW_SUB;  // warp chunk of k_score_flow's final wave (a multiple of 64)
 #ifndef SP_SKIP_CHUNK
 #define SP_SKIP_CHUNK 4096
 #endif
@@ -1464,7 +1479,8 @@ constexpr int SKIP_MAX_CHUNKS = ITEM_ITERS_MAX_SKIP * THREADS / SKIP_CHUNK;
 // up to `maxch` of them; then make the FastNode offsets absolute.  Contains
 // the CTA barriers it needs; returns after the last one.
 __device__ __forceinline__ void stage_block(uint8_t* smem, const uint8_t* blobs, int64_t off, uint64_t* lane_add,
-                                            Biased* bz, uint64_t* cenc, uint32_t chs, int maxch, bool pair) {
+                                            Biased* bz, uint64_t* cenc, uint32_t chs, int maxch, bool pair,
+                                            uint64_t* fenc = nullptr, uint32_t fsub = 0, int nf = 0) {
   const int tid = threadIdx.x;
   stage_blob(smem, blobs, off);
   const BlobHeader* gH = (const BlobHeader*)(blobs + off);
@@ -1507,6 +1523,16 @@ __device__ __forceinline__ void stage_block(uint8_t* smem, const uint8_t* blobs,
       x /= r;
     }
     cenc[c] = a;
+  }
+  for (int c = tid - 64 - maxch; c >= 0 && c < nf; c += THREADS - 64 - maxch) {
+    uint64_t a = 0;  // unbiased digits of c * fsub
+    uint64_t x = (uint64_t)c * fsub;
+    for (int q = V - 1; q >= 0 && x; q--) {
+      const uint32_t r = ((r3 >> q) & 1) ? 3 : 2;
+      a |= (uint64_t)(x % r) << (2 * (V - 1 - q));
+      x /= r;
+    }
+    fenc[c] = a;
   }
   __syncthreads();
   patch_fast(smem, pair);
@@ -1745,11 +1771,21 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
 // unchanged).  Every warp visits the slots' generations in the same order
 // (slot 0 gen 1, slot 1 gen 1, slot 0 gen 2, ...), so a slot's parameters
 // are rewritten only after all eight warps have left it.
+#ifdef SP_CTA_TRACE
+// diagnostics build (-DSP_CTA_TRACE, SP_LIB=...): per CTA of the last k_score_flow
+// launch: start, end (globaltimer ns), ns spent closing / staging blocks, stagings
+__device__ unsigned long long g_cta_trace[4096][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 struct FlowSlot {
   unsigned long long item, ilo;
   uint64_t wbase;
   int64_t block;
-  uint32_t cnt, cursor, retired, gen;
+  uint32_t cnt, cursor, retired, gen, fine;
   int state;  // 0: ready (staged block), 1: another block, 2: no more items
 };
 
@@ -1765,6 +1801,9 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
   __shared__ uint64_t s_lane_add[32];
   __shared__ Biased s_bz;
   __shared__ uint64_t s_cenc[MAXCH];
+  // digits of k * FLOW_SUB (k < CHS / FLOW_SUB): the final wave's finer chunks
+  constexpr int NF = SKIP ? 0 : (int)(CHS / FLOW_SUB);
+  __shared__ uint64_t s_fenc[NF > 0 ? NF : 1];
   __shared__ FlowSlot s_slot[2];
   __shared__ unsigned long long s_seg;  // item whose ItemOut receives the current share (~0: none yet)
   __shared__ int64_t s_staged;
@@ -1780,16 +1819,39 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
     if (it >= P.n_items) {
       sl.state = 2;
     } else {
-      items[it] = ItemOut{~0ULL, ~0ULL, 0xFFFFFFFFu, 0ULL};
-      int64_t lo = 0, hi = P.nb;
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) / 2;
-        if (P.item_base[mid] <= it) lo = mid;
-        else hi = mid;
+      int64_t lo = 0;
+      unsigned long long ilo, ihi, out;
+      if (SKIP || it < P.n_main) {
+        int64_t hi = P.nb;
+        while (hi - lo > 1) {
+          const int64_t mid = (lo + hi) / 2;
+          if (P.item_base[mid] <= it) lo = mid;
+          else hi = mid;
+        }
+        const unsigned long long j = it - P.item_base[lo];
+        ilo = P.lo[lo] + j * P.stride[lo];
+        ihi = min(ilo + P.item_cands, P.hi[lo]);
+        out = P.obase ? P.obase[lo] + j : it;
+        sl.fine = 0;
+      } else {  // sub-item k of run e: part k % split of the block's item nmain + k / split
+        const unsigned long long u = it - P.n_main;
+        int64_t e = 0, hi = P.nf;
+        while (hi - e > 1) {
+          const int64_t mid = (e + hi) / 2;
+          if (P.fbase[mid] <= u) e = mid;
+          else hi = mid;
+        }
+        lo = (int64_t)P.fblk[e];
+        const unsigned long long k = u - P.fbase[e], nmain = P.item_base[lo + 1] - P.item_base[lo];
+        const unsigned long long blo = P.lo[lo] + (nmain + k / P.split) * P.stride[lo];
+        const unsigned long long bhi = min(blo + P.item_cands, P.hi[lo]);
+        ilo = min(blo + (k % P.split) * P.sub, bhi);
+        ihi = min(ilo + P.sub, bhi);
+        out = P.obase[lo] + nmain + k;
+        sl.fine = 1;
       }
-      const unsigned long long ilo = P.lo[lo] + (it - P.item_base[lo]) * P.stride[lo];
-      const unsigned long long ihi = min(ilo + P.item_cands, P.hi[lo]);
-      sl.item = it;
+      items[out] = ItemOut{~0ULL, ~0ULL, 0xFFFFFFFFu, 0ULL};
+      sl.item = out;
       sl.block = lo;
       sl.ilo = ilo;
       sl.cnt = (uint32_t)(ihi - ilo);
@@ -1846,6 +1908,9 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
     lb = LaneBest{};
   };
 
+#ifdef SP_CTA_TRACE
+  unsigned long long tr_t0 = gtimer(), tr_stage = 0, tr_n = 0;
+#endif
   if (tid == 0) {
     s_staged = -1;
     s_seg = ~0ULL;
@@ -1878,10 +1943,13 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
     if (state == 1) {
       // every warp reaches this slot generation: close the share of the
       // staged block, stage this slot's block
+#ifdef SP_CTA_TRACE
+      const unsigned long long tr_a = gtimer();
+#endif
       flush(lb);
       __syncthreads();
       const int64_t b = sl.block;
-      stage_block(smem, blobs, P.blob_off[b], s_lane_add, &s_bz, s_cenc, CHS, MAXCH, PAIR);
+      stage_block(smem, blobs, P.blob_off[b], s_lane_add, &s_bz, s_cenc, CHS, MAXCH, PAIR, s_fenc, FLOW_SUB, NF);
       if (tid == 0) {
         s_staged = b;
         s_seg = sl.item;
@@ -1902,17 +1970,26 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
         rb = opaque_u32(pool + 8u * (uint32_t)tid);
         sb = opaque_u32(pool + (uint32_t)H.npool * THREADS * (PAIR ? 16u : 8u) + (uint32_t)tid);
       }
+#ifdef SP_CTA_TRACE
+      tr_stage += gtimer() - tr_a;
+      tr_n++;
+#endif
       continue;
     }
     uint32_t c = 0;
     if (lane == 0) c = atomicAdd((uint32_t*)&s_slot[cur].cursor, 1u);
     c = __shfl_sync(0xffffffffu, c, 0);
     const uint32_t cnt = sl.cnt;
+    // the final wave (sub-items) walks FLOW_SUB-candidate chunks: the kernel
+    // ends when the slowest warp's last chunk does
+    const bool fine = !SKIP && sl.fine;
     const uint32_t nbig = SKIP ? (cnt - cnt / 4) / CH : 0;
-    const uint32_t start = c < nbig ? c * CH : nbig * CH + (c - nbig) * CHS;
+    const uint32_t start = fine ? c * FLOW_SUB : c < nbig ? c * CH : nbig * CH + (c - nbig) * CHS;
     if (start < cnt) {
-      const uint32_t rem = min(c < nbig ? CH : CHS, cnt - start);
-      const uint64_t w = badd(badd(sl.wbase, s_cenc[start / CHS], s_bz.B), s_lane_add[lane], s_bz.B);
+      const uint32_t rem = min(fine ? FLOW_SUB : c < nbig ? CH : CHS, cnt - start);
+      uint64_t w = badd(sl.wbase, s_cenc[start / CHS], s_bz.B);
+      if (fine) w = badd(w, s_fenc[(start % CHS) / FLOW_SUB], s_bz.B);
+      w = badd(w, s_lane_add[lane], s_bz.B);
       score_chunk<SKIP, PAIR>(tabs_of(smem), s_bz, s_lane_add, rec0, rb, sb, lane, w, rem,
                               sl.ilo + (unsigned long long)start + rem, lb);
       continue;
@@ -1928,6 +2005,14 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
     cur ^= 1;
   }
   flush(lb);
+#ifdef SP_CTA_TRACE
+  if (tid == 0 && blockIdx.x < 4096) {
+    g_cta_trace[blockIdx.x][0] = tr_t0;
+    g_cta_trace[blockIdx.x][1] = gtimer();
+    g_cta_trace[blockIdx.x][2] = tr_stage;
+    g_cta_trace[blockIdx.x][3] = tr_n;
+  }
+#endif
 }
 
 // Prefix-skipping scorer without work items: every CTA walks the blocks in
@@ -3759,6 +3844,46 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     base[b + 1] = base[b] + cnt;
   }
   const unsigned long long n_items = base[nb];
+  // the final wave of the brute-force walk (k_score_flow): the rank's last
+  // SP_FLOW_TAIL (default 4) items per resident CTA -- the last items of the
+  // item order -- are claimed last, each in SP_FLOW_SPLIT (default 4) parts.
+  // An item of the costliest region outlasts the average one several times,
+  // and the kernel ends with its last CTA (c5, CTA end times from a
+  // -DSP_CTA_TRACE build: first-to-last spread 1.0 -> 0.22 ms, kernel 31.70
+  // -> 31.26 ms; 8-rank share 4.33 -> 4.2 ms).
+  const bool flow_walk = kern == fast_pair || kern == fast_one;
+  std::vector<unsigned long long> nsplit(nb, 0), obase(nb + 1, 0), fblk, fbase{0};
+  const unsigned long long split_w = getenv("SP_FLOW_SPLIT") ? strtoull(getenv("SP_FLOW_SPLIT"), nullptr, 10) : 4;
+  const unsigned long long tail_w = getenv("SP_FLOW_TAIL") ? strtoull(getenv("SP_FLOW_TAIL"), nullptr, 10) : 4;
+  const unsigned long long split = flow_walk && !items_mode && split_w > 1 ? split_w : 1;
+  if (split > 1) {
+    unsigned long long quota = tail_w * slots;
+    for (int64_t b = nb - 1; b >= 0 && quota; b--) {
+      nsplit[b] = std::min(base[b + 1] - base[b], quota);
+      quota -= nsplit[b];
+    }
+    // runs in ascending block order: the split blocks are the last ones, so
+    // the claim sequence stays block-monotone (a CTA's claims never return
+    // to a block it has left: its share of a block is flushed only once)
+    for (int64_t b = 0; b < nb; b++)
+      if (nsplit[b]) {
+        fblk.push_back((unsigned long long)b);
+        fbase.push_back(fbase.back() + nsplit[b] * split);
+      }
+  }
+  {  // claim bases without the split items; output bases with their parts
+    unsigned long long m = 0;
+    for (int64_t b = 0; b < nb; b++) {
+      const unsigned long long cnt = base[b + 1] - base[b];
+      base[b] = m;
+      m += cnt - nsplit[b];
+      obase[b + 1] = obase[b] + cnt - nsplit[b] + nsplit[b] * split;
+    }
+    base[nb] = m;
+  }
+  const unsigned long long n_main = base[nb];
+  const int64_t nf = (int64_t)fblk.size();
+  const unsigned long long n_claims = obase[nb];  // = n_main + every part of the split items
   if (n_items == 0) {
     if (!must_out) return false;
     alloc_dout(pd, t, s, must_out);
@@ -3770,20 +3895,24 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   }
   // blocks with many items reduce in two passes (chunks of REDUCE_CHUNK items, then per block)
   unsigned long long max_items = 0;
-  for (int64_t b = 0; b < nb; b++) max_items = std::max(max_items, base[b + 1] - base[b]);
+  for (int64_t b = 0; b < nb; b++) max_items = std::max(max_items, obase[b + 1] - obase[b]);
   const bool two_pass = max_items > 2 * REDUCE_CHUNK;
-  // one small H2D for the plan: lo | hi | base | counter (| chunk_base)
-  std::vector<unsigned long long> plan(4 * nb + 2 + (two_pass ? nb + 1 : 0), 0);
+  // one small H2D for the plan: lo | hi | base | counter | stride | obase | fblk | fbase (| chunk_base)
+  const size_t o_obase = 4 * nb + 2, o_fblk = o_obase + nb + 1, o_fbase = o_fblk + nf, o_cb = o_fbase + nf + 1;
+  std::vector<unsigned long long> plan(o_cb + (two_pass ? nb + 1 : 0), 0);
   std::copy(lo.begin(), lo.end(), plan.begin());
   std::copy(hi.begin(), hi.end(), plan.begin() + nb);
   std::copy(base.begin(), base.end(), plan.begin() + 2 * nb);
   std::copy(stride.begin(), stride.end(), plan.begin() + 3 * nb + 2);
+  std::copy(obase.begin(), obase.end(), plan.begin() + o_obase);
+  std::copy(fblk.begin(), fblk.end(), plan.begin() + o_fblk);
+  std::copy(fbase.begin(), fbase.end(), plan.begin() + o_fbase);
   unsigned long long n_chunks = 0;
   if (two_pass) {
-    unsigned long long* cb = plan.data() + 4 * nb + 2;
+    unsigned long long* cb = plan.data() + o_cb;
     for (int64_t b = 0; b < nb; b++) {
       cb[b] = n_chunks;
-      n_chunks += (base[b + 1] - base[b] + REDUCE_CHUNK - 1) / REDUCE_CHUNK;
+      n_chunks += (obase[b + 1] - obase[b] + REDUCE_CHUNK - 1) / REDUCE_CHUNK;
     }
     cb[nb] = n_chunks;
   }
@@ -3792,25 +3921,32 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   DevBuf<sp_score_out>& dout = pd.dout;
   tr.mark("plan");
   dplan.upload(plan.data(), plan.size(), s);
-  items.alloc(n_items + n_chunks, s);  // (partials of the two-pass reduction behind the items)
+  items.alloc(n_claims + n_chunks, s);  // (partials of the two-pass reduction behind the items)
   alloc_dout(pd, t, s, must_out);
   tr.mark("upload+alloc");
   unsigned long long* counter = dplan.p + 3 * nb + 1;
   ScorePlan P{t->d_blob_off.p, item_cands, dplan.p + 3 * nb + 2, dplan.p, dplan.p + nb, dplan.p + 2 * nb, nb,
-              n_items, ctx->skip};
-  const unsigned long long grid = std::min<unsigned long long>(n_items, slots);
+              n_claims, ctx->skip};
+  P.obase = dplan.p + o_obase;
+  P.fblk = dplan.p + o_fblk;
+  P.fbase = dplan.p + o_fbase;
+  P.nf = nf;
+  P.n_main = n_main;
+  P.split = split;
+  P.sub = (item_cands + split - 1) / split;
+  const unsigned long long grid = std::min<unsigned long long>(n_claims, slots);
   SP_CUDA(cudaEventRecord(pd.ev[1], s));
   SP_LAUNCH(ctx, kern, (unsigned)grid, threads, smem_k, s, t->blobs.p, P, items.p, counter);
   SP_CUDA(cudaEventRecord(pd.ev[2], s));
   tr.mark("score launch");
   if (two_pass) {
-    const unsigned long long* d_cb = dplan.p + 4 * nb + 2;
+    const unsigned long long* d_cb = dplan.p + o_cb;
     SP_LAUNCH(ctx, k_reduce_chunks, (unsigned)std::min<unsigned long long>(n_chunks, 65535), THREADS, 0, s, items.p,
-              dplan.p + 2 * nb, d_cb, nb, n_chunks, items.p + n_items);
-    SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p + n_items, d_cb, nb,
+              dplan.p + o_obase, d_cb, nb, n_chunks, items.p + n_claims);
+    SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p + n_claims, d_cb, nb,
               dout.p);
   } else {
-    SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + 2 * nb, nb,
+    SP_LAUNCH(ctx, k_reduce, (unsigned)std::min<int64_t>(nb, 4096), THREADS, 0, s, items.p, dplan.p + o_obase, nb,
               dout.p);
   }
   SP_CUDA(cudaGetLastError());
@@ -4054,6 +4190,31 @@ static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& r
     cudaEventElapsedTime(&d, pd.ev[4], pd.ev[5]);
     fprintf(stderr, "[score] nb %lld: launch->kernel %.3f ms, kernel %.3f, reduce %.3f, explain %.3f, d2h %.3f\n",
             (long long)nb, a, ms, b, c, d);
+#ifdef SP_CTA_TRACE
+    static unsigned long long h[4096][4];
+    cudaMemcpyFromSymbol(h, g_cta_trace, sizeof(h));
+    std::vector<unsigned long long> st, en;
+    double stg = 0, nst = 0;
+    int n = 0;
+    for (int i = 0; i < 4096 && h[i][0]; i++, n++) {
+      st.push_back(h[i][0]);
+      en.push_back(h[i][1]);
+      stg += h[i][2];
+      nst += h[i][3];
+    }
+    if (n) {
+      const unsigned long long t0 = *std::min_element(st.begin(), st.end());
+      std::sort(st.begin(), st.end());
+      std::sort(en.begin(), en.end());
+      auto us = [&](unsigned long long x) { return (x - t0) / 1e3; };
+      fprintf(stderr, "[cta] %d CTAs: start max %.1f us; end p0 %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f us; "
+                      "per CTA %.1f stagings, %.1f us closing+staging\n",
+              n, us(st.back()), us(en[0]), us(en[n / 10]), us(en[n / 2]), us(en[n * 9 / 10]), us(en.back()), nst / n,
+              stg / n / 1e3);
+    }
+    std::memset(h, 0, sizeof(h));
+    cudaMemcpyToSymbol(g_cta_trace, h, sizeof(h));
+#endif
   }
   pd.release_host();
 }

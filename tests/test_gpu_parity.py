@@ -935,3 +935,41 @@ def test_root_relief_deal_merges_exactly(backend, seed, relief, monkeypatch):
     finally:
         backend.set_mode("skip")
         t.close()
+
+
+@pytest.mark.parametrize("split,tail", [("1", "2"), ("4", "2"), ("7", "1"), ("3", "1000")])
+@pytest.mark.parametrize("seed", [5, 23])
+def test_final_wave_split_equals_whole_items(backend, seed, split, tail, monkeypatch):
+    """The brute-force walk's final wave claims its last items in parts
+    (SP_FLOW_SPLIT parts of SP_FLOW_TAIL items per resident CTA, from the last
+    blocks backwards; 1000 splits every item here): per-block results are the
+    same at every split and shard count."""
+    from paper_2302_00247_b200.api_types import ClusterSpec
+    from paper_2302_00247_b200.dist import merge_scores
+    from paper_2302_00247_b200.lowering import lower
+    from paper_2302_00247_b200.search import Session, fold_blocks
+    from randgraph import random_graph
+
+    low = lower(random_graph(seed, n_types=5, reps=(2, 6), ops=(3, 12)))
+    ses = Session.open(low, backend)
+    ba = fold_blocks(low, 2, session=ses)
+    off, nodes = ba.templates_csr()
+    t = backend.tables(ses.dgraph, off, nodes, ClusterSpec.from_mesh("2x4"), 1 << 20, 4 << 20)
+    try:
+        if t.overflow:
+            pytest.skip("random block beyond u64")
+        backend.set_mode("walk")
+        monkeypatch.setenv("SP_FLOW_SPLIT", "1")
+        ref = backend.score(t)
+        key = [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split) for r in ref]
+        monkeypatch.setenv("SP_FLOW_SPLIT", split)
+        monkeypatch.setenv("SP_FLOW_TAIL", tail)
+        got = backend.score(t)
+        assert [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split) for r in got] == key
+        for n in (2, 5):
+            merged = merge_scores([backend.score(t, s, n) for s in range(n)])
+            assert [(r.candidates, r.valid, r.has_best, r.best_index, r.best_total, r.best_num_split)
+                    for r in merged] == key, n
+    finally:
+        backend.set_mode("skip")
+        t.close()

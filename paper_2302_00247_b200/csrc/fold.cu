@@ -524,6 +524,8 @@ struct SmallArgs {
   int32_t o_name_off, o_names, o_op, o_w_rank, o_w_train, o_w_shape, o_in_off, o_in_idx;
   int64_t name_bytes, n_edges;
   long long* prof;  // SP_FOLD_PROF: clock64() at each phase boundary (thread 0), else null
+  uint8_t* hcache;  // the graph's name-hash cache (ph | rh | pend | depth), or null
+  int32_t hc_ready; // 1: hcache holds this seed's hashes (read them), 0: compute and fill it
 };
 
 // cooperative global -> shared copy (16-byte words when both ends allow it)
@@ -688,10 +690,15 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int32_t s_warp[32];
   int np_ = 0;
-#define PROF()                                                \
-  do {                                                        \
-    if (a.prof && threadIdx.x == 0) a.prof[np_] = clock64(); \
-    np_++;                                                    \
+#define PROF()                                                       \
+  do {                                                               \
+    if (a.prof && threadIdx.x == 0) {                                \
+      a.prof[np_] = clock64();                                       \
+      unsigned long long g_;                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));         \
+      a.prof[128 + np_] = (long long)g_;                             \
+    }                                                                \
+    np_++;                                                           \
   } while (0)
   PROF();
   const int tid = threadIdx.x, NT = blockDim.x;
@@ -731,20 +738,46 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     copy_in_async((uint8_t*)w_shape, (const uint8_t*)a.w_shape, (size_t)n * SP_MAX_RANK * 8);
     copy_in_async((uint8_t*)in_off, (const uint8_t*)a.in_off, (size_t)(n + 1) * 8);
     copy_in_async((uint8_t*)in_idx, (const uint8_t*)a.in_idx, (size_t)a.n_edges * 4);
+    if (a.hc_ready) {
+      copy_in_async((uint8_t*)ph, a.hcache, (size_t)n * D * 8);
+      copy_in_async((uint8_t*)rh, a.hcache + (size_t)n * D * 8, (size_t)n * D * 8);
+      copy_in_async((uint8_t*)depth, a.hcache + (size_t)n * D * 20, (size_t)n * 4);
+    }
     copy_in_wait();
+  } else if (a.hc_ready) {
+    copy_in((uint8_t*)ph, a.hcache, (size_t)n * D * 8);
+    copy_in((uint8_t*)rh, a.hcache + (size_t)n * D * 8, (size_t)n * D * 8);
+    copy_in((uint8_t*)depth, a.hcache + (size_t)n * D * 20, (size_t)n * 4);
   }
   PROF();
+  const int64_t nD = (int64_t)n * D;
+  if (a.hc_ready) {  // the names' hashes from the graph's first search
+    const int32_t* hp = (const int32_t*)(a.hcache + nD * 16);
+    for (int64_t k = tid; k < nD; k += NT) a.pend[k] = hp[k];
+  }
   for (int i = tid; i < n; i += NT) {
-    int32_t d = 1;
-    for (int64_t k = name_off[i]; k < name_off[i + 1]; k++) d += names[k] == '/';
-    depth[i] = d;
-    name_hash_one(i, name_off, names, a.n, D, a.seed, a.pend, ph, rh, D, 1);
+    if (!a.hc_ready) {
+      int32_t d = 1;
+      for (int64_t k = name_off[i]; k < name_off[i + 1]; k++) d += names[k] == '/';
+      depth[i] = d;
+      name_hash_one(i, name_off, names, a.n, D, a.seed, a.pend, ph, rh, D, 1);
+    }
     gparent[i] = 0;
     a.residual[i] = 0;
     cur[i] = -1;
     act[i] = i;
   }
   __syncthreads();
+  if (!a.hc_ready && a.hcache) {  // keep them for the graph's next searches
+    uint64_t* hph = (uint64_t*)a.hcache;
+    int32_t* hp = (int32_t*)(a.hcache + nD * 16);
+    for (int64_t k = tid; k < nD; k += NT) {
+      hph[k] = ph[k];
+      hph[nD + k] = rh[k];
+      hp[k] = a.pend[k];
+    }
+    for (int i = tid; i < n; i += NT) hp[nD + i] = depth[i];
+  }
   PROF();
   int nA = n;
   int level = 1;
@@ -2053,6 +2086,17 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
   // per-node passes), or one per bitonic compare-exchange beyond 1024 nodes
   const int threads = n <= RANK_SORT_MAX ? std::max(64, (int)((n + 31) / 32 * 32)) : std::min(SMALL_THREADS, P2 / 2);
   tr.mark("setup");
+  {  // name hashes: computed by the graph's first search at this seed, then read
+    const bool hit = dg->name_hash.p && dg->name_hash_seed == seed && dg->name_hash_D == D &&
+                     !getenv("SP_FOLD_NOHASHCACHE");
+    if (!hit) {
+      dg->name_hash.alloc(nd * 20 + (size_t)n * 4, s);
+      dg->name_hash_seed = seed;
+      dg->name_hash_D = D;
+    }
+    A.hcache = dg->name_hash.p;
+    A.hc_ready = hit ? 1 : 0;
+  }
   static const bool prof = getenv("SP_FOLD_PROF") != nullptr;
   DevBuf<long long> profb;
   A.prof = nullptr;
@@ -2066,9 +2110,12 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
     long long h[256];
     SP_CUDA(cudaMemcpyAsync(h, profb.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     SP_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[fold_small prof] n=%lld threads=%d:", (long long)n, threads);
-    for (int i = 1; i < 256 && h[i]; i++) fprintf(stderr, " %lld", h[i] - h[i - 1]);
-    fprintf(stderr, "\n");
+    fprintf(stderr, "[fold_small prof] n=%lld threads=%d: cycles", (long long)n, threads);
+    for (int i = 1; i < 128 && h[i]; i++) fprintf(stderr, " %lld", h[i] - h[i - 1]);
+    int last = 1;
+    while (last < 128 && h[128 + last]) last++;
+    fprintf(stderr, "; %lld ns, %.0f MHz\n", h[128 + last - 1] - h[128],
+            (double)(h[last - 1] - h[0]) * 1e3 / (double)std::max(1LL, h[128 + last - 1] - h[128]));
   }
   SP_CUDA(cudaGetLastError());
   SP_CUDA(cudaEventRecord(ctx->ev[7], s));

@@ -377,6 +377,12 @@ struct sp_dgraph {
   View<int64_t> name_off, topo, act_shape, act_bytes, w_shape, w_bytes, in_off;
   View<int32_t> in_idx;
   std::vector<sp_dgraph*> peers;  // the same graph on every peer lane of a multi-device context
+  // the one-CTA fold's per-node name hashes (prefix / rel hash and prefix end
+  // per depth, node depth): a function of the names and the seed only, kept
+  // from the first search of the graph (ph | rh | pend | depth)
+  sp::DevBuf<uint8_t> name_hash;
+  uint64_t name_hash_seed = 0;
+  int32_t name_hash_D = -1;
 };
 
 

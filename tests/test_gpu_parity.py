@@ -973,3 +973,25 @@ def test_final_wave_split_equals_whole_items(backend, seed, split, tail, monkeyp
     finally:
         backend.set_mode("skip")
         t.close()
+
+
+@pytest.mark.parametrize("layers", [2, 80])
+def test_one_cta_fold_name_hash_cache(backend, layers, monkeypatch):
+    """The one-CTA fold reads the names' hashes its graph's first search
+    computed: repeated folds (other min_dup too) equal uncached ones and the oracle."""
+    from oracle import oracle
+    from paper_2302_00247_b200.workloads import transformer_stack_lowered
+
+    keys = ("block_T", "block_inst_off", "block_member_off", "inst_prefix_len", "members")
+    low = transformer_stack_lowered(layers)
+    dg = backend.upload(low)
+    for md in (2, 3, 2, 4):
+        ba = backend.fold(dg, md)
+        ob = oracle.prune(low, md)
+        for k in keys:
+            assert np.array_equal(np.asarray(getattr(ba, k), np.int64), np.asarray(ob[k], np.int64)), (md, k)
+    monkeypatch.setenv("SP_FOLD_NOHASHCACHE", "1")
+    ba2 = backend.fold(backend.upload(low), 3)
+    ob = oracle.prune(low, 3)
+    for k in keys:
+        assert np.array_equal(np.asarray(getattr(ba2, k), np.int64), np.asarray(ob[k], np.int64)), k

@@ -524,7 +524,7 @@ struct SmallArgs {
   int32_t o_name_off, o_names, o_op, o_w_rank, o_w_train, o_w_shape, o_in_off, o_in_idx;
   int64_t name_bytes, n_edges;
   long long* prof;  // SP_FOLD_PROF: clock64() at each phase boundary (thread 0), else null
-  uint8_t* hcache;  // the graph's name-hash cache (ph | rh | pend | depth), or null
+  uint8_t* hcache;  // the graph's name-hash cache (ph | rh | pend | depth | level-1 order), or null
   int32_t hc_ready; // 1: hcache holds this seed's hashes (read them), 0: compute and fill it
 };
 
@@ -788,24 +788,41 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_fold_small(SmallArgs a) {
     int32_t* co = a.corder + (int64_t)dd * n;
     int32_t* cs = a.cstart + (int64_t)dd * (n + 1);
     uint8_t* ga = a.gaccept + (int64_t)dd * n;
-    // 1. sort active nodes by (prefix hash, rel hash)
+    // 1. sort active nodes by (prefix hash, rel hash); level 1 sorts every
+    // node, a function of the names and the seed: its order comes from the
+    // name-hash cache after the graph's first search
     const int P2 = pow2ceil(nA);
-    const int nfill = nA <= NT && nA <= RANK_SORT_MAX ? nA : P2;
-    for (int i = tid; i < nfill; i += NT) {
-      if (i < nA) {
-        const int32_t v = act[i];
-        K1[i] = ph[(int64_t)v * D + dd];
-        K2[i] = rh[(int64_t)v * D + dd];
+    int32_t* const hsorted = a.hcache ? (int32_t*)(a.hcache + (int64_t)n * D * 20 + (int64_t)n * 4) : nullptr;
+    if (level == 1 && a.hc_ready) {
+      for (int i = tid; i < nA; i += NT) {
+        const int32_t v = hsorted[i];
+        K1[i] = ph[(int64_t)v * D];
+        K2[i] = rh[(int64_t)v * D];
         V[i] = v;
-      } else {
-        K1[i] = K2[i] = ~0ULL;
-        V[i] = 0x7fffffff;
       }
+      __syncthreads();
+      PROF();
+      PROF();
+    } else {
+      const int nfill = nA <= NT && nA <= RANK_SORT_MAX ? nA : P2;
+      for (int i = tid; i < nfill; i += NT) {
+        if (i < nA) {
+          const int32_t v = act[i];
+          K1[i] = ph[(int64_t)v * D + dd];
+          K2[i] = rh[(int64_t)v * D + dd];
+          V[i] = v;
+        } else {
+          K1[i] = K2[i] = ~0ULL;
+          V[i] = 0x7fffffff;
+        }
+      }
+      __syncthreads();
+      PROF();
+      block_sort(K1, K2, V, nA, P2);
+      PROF();
+      if (level == 1 && hsorted)
+        for (int i = tid; i < nA; i += NT) hsorted[i] = V[i];
     }
-    __syncthreads();
-    PROF();
-    block_sort(K1, K2, V, nA, P2);
-    PROF();
     for (int i = tid; i < nA; i += NT) {
       srt[i] = V[i];
       flag[i] = (i == 0 || K1[i] != K1[i - 1]) ? 1 : 0;
@@ -2090,7 +2107,7 @@ static void fold_once_small(sp_ctx* ctx, sp_dgraph* dg, int32_t min_dup, uint64_
     const bool hit = dg->name_hash.p && dg->name_hash_seed == seed && dg->name_hash_D == D &&
                      !getenv("SP_FOLD_NOHASHCACHE");
     if (!hit) {
-      dg->name_hash.alloc(nd * 20 + (size_t)n * 4, s);
+      dg->name_hash.alloc(nd * 20 + (size_t)n * 8, s);  // + the level-1 sort order
       dg->name_hash_seed = seed;
       dg->name_hash_D = D;
     }

@@ -245,6 +245,13 @@ int sp_search(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* bl
  * No reference counterpart: the reference's pool.map blocks (search.py:338).
  */
 int sp_score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, int32_t explain);
+/* `explain` | SP_SCORE_LOCAL: score every candidate of `t` on this device and
+ * exchange nothing, even when the context has a communicator, peer lanes or a
+ * simulated shard -- for a search whose results only the root needs (the
+ * cheap residual group of a multi-rank derive_plan: rank 0 scores it, the
+ * other ranks never build it).  Every rank must agree which searches are
+ * local: a non-local search is a collective. */
+#define SP_SCORE_LOCAL 2
 int sp_score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, sp_explain_block* blocks, int8_t* node_detail,
                   int8_t* edge_detail);
 /* Score [lo, hi) of one block; optional per-candidate totals (NaN = invalid). */

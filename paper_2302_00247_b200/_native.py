@@ -27,6 +27,7 @@ from .blocks import BlockArrays
 from .errors import BackendError, BadConfig, SpecMismatch, UnsupportedSearch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+SP_SCORE_LOCAL = 2  # include/shardsearch.h
 LIB_PATH = os.environ.get("SP_LIB") or os.path.join(HERE, "lib", "libshardsearch.so")
 
 _lib = None
@@ -383,10 +384,12 @@ class Backend:
         nb = t.n_blocks
         return [outs[i] for i in range(nb)], ([blocks[i] for i in range(nb)], node, edge, eoff)
 
-    def score_launch(self, t: Tables, shard: int = 0, n_shards: int = 1, explain: bool = False) -> None:
-        """Enqueue the search (sp_score_launch) and return at once; collect with score_wait."""
-        self._check(self.lib.sp_score_launch(self.ctx, t.ptr, shard, n_shards, 1 if explain else 0),
-                    "sp_score_launch")
+    def score_launch(self, t: Tables, shard: int = 0, n_shards: int = 1, explain: bool = False,
+                     local: bool = False) -> None:
+        """Enqueue the search (sp_score_launch) and return at once; collect with score_wait.
+        `local`: the whole search on this device with no exchange (SP_SCORE_LOCAL)."""
+        flags = (1 if explain else 0) | (SP_SCORE_LOCAL if local else 0)
+        self._check(self.lib.sp_score_launch(self.ctx, t.ptr, shard, n_shards, flags), "sp_score_launch")
         t.pending_explain = explain
 
     def score_wait(self, t: Tables) -> tuple:

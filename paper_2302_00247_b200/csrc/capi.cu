@@ -479,7 +479,7 @@ int sp_score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, 
   return guard(ctx, [&] {
     sp::Trace tr("score_launch");
     SP_CUDA(cudaSetDevice(ctx->device));
-    sp::score_launch(ctx, t, shard, n_shards, explain != 0);
+    sp::score_launch(ctx, t, shard, n_shards, (explain & 1) != 0, (explain & SP_SCORE_LOCAL) != 0);
     tr.mark("enqueued");
   });
 }

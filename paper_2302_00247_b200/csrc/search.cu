@@ -4219,9 +4219,14 @@ static void score_finish(sp_ctx* ctx, sp_tables* t, std::vector<sp_score_out>& r
   pd.release_host();
 }
 
-void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain) {
+void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain, bool local) {
   if (n_shards < 1 || shard < 0 || shard >= n_shards) throw Error(SP_ERR_CONFIG, "bad shard / n_shards");
   if (t->overflow) throw Error(SP_ERR_UNSUPPORTED, "a block has more than 2**64 candidates");
+  if (local) {  // SP_SCORE_LOCAL: the whole search on this device, no exchange, no peer lanes
+    pending_begin(ctx, t);
+    score_enqueue(ctx, t, 0, 1, explain);
+    return;
+  }
   if (!ctx->peers.empty()) {  // this process drives several devices
     if (t->peers.size() != ctx->peers.size()) throw Error(SP_ERR_CONFIG, "tables were not built on every device");
     std::vector<sp_ctx*> lanes{ctx};

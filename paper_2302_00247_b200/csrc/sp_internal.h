@@ -496,7 +496,7 @@ void tables_build(sp_ctx* ctx, sp_dgraph* dg, int64_t n_blocks, const int64_t* t
                   sp_tables* out);
 void score_all(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, sp_score_out* out,
                void* xblocks = nullptr, int8_t* xnode = nullptr, int8_t* xedge = nullptr);
-void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain);
+void score_launch(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shards, bool explain, bool local = false);
 void score_wait(sp_ctx* ctx, sp_tables* t, sp_score_out* out, void* xblocks, int8_t* xnode, int8_t* xedge);
 void score_range(sp_ctx* ctx, sp_tables* t, int64_t block, uint64_t lo, uint64_t hi,
                  double* totals, sp_score_out* out);

@@ -19,6 +19,7 @@ from __future__ import annotations
 import dataclasses
 import gc
 import math
+import os
 import time
 from dataclasses import dataclass
 from typing import Callable, Optional
@@ -657,8 +658,9 @@ class _Search:
     Host work placed between the two overlaps the device search."""
 
     def __init__(self, ses: Session, csr, mesh, mu: int, chunk_size: int, shard: int, n_shards: int,
-                 exchange: Optional[Callable], launch: bool = True):
+                 exchange: Optional[Callable], launch: bool = True, local: bool = False):
         self.ses, self.mesh, self.mu, self.chunk_size = ses, mesh, mu, chunk_size
+        self.local = local
         self.exchange = exchange
         self._fetched = None
         # pack_gradients raises BadConfig for mu > chunk only once a candidate is
@@ -691,7 +693,8 @@ class _Search:
             if self.tables.overflow:
                 raise UnsupportedSearch("a block has more than 2**64 candidates (reference: big-int index)")
             self.t_launch = time.perf_counter()
-            self.ses.backend.score_launch(self.tables, self.shard, self.n_shards, explain=self.explain)
+            self.ses.backend.score_launch(self.tables, self.shard, self.n_shards, explain=self.explain,
+                                          local=self.local)
         except BaseException:
             self.tables.close()
             raise
@@ -1060,11 +1063,17 @@ def _explain_groups(ses: Session, csr, prep: list, indices: list, mesh, mu: int,
     return out
 
 
-def _plan_searches(ses: Session, csr, mesh, mu, chunk_size, shard, n_shards, exchange) -> list:
+def _plan_searches(ses: Session, csr, mesh, mu, chunk_size, shard, n_shards, exchange, root_local=False) -> list:
     """[(search, block ids)]: the route search of the blocks beyond the table
     limits (if any), then the table searches (cheap group first, _block_groups).
     A block whose tables turn out larger than shared memory moves to the route
-    search (the tables are rebuilt without it)."""
+    search (the tables are rebuilt without it).
+
+    `root_local` (a multi-rank search inside the library where only rank 0
+    assembles): the cheap group of a two-group split is scored whole on rank 0
+    with no exchange (SP_SCORE_LOCAL) and not built at all on the other ranks --
+    its results feed only the report, and every rank takes the same decision
+    from the same fold."""
     nb = len(csr[0]) - 1
     route = _route_mask(ses.low, csr)
     while True:
@@ -1073,9 +1082,14 @@ def _plan_searches(ses: Session, csr, mesh, mu, chunk_size, shard, n_shards, exc
         tids = np.nonzero(~route)[0]
         try:
             tcsr = csr if len(rids) == 0 else _subset_csr(csr, tids)
-            for ids, gcsr in _block_groups(ses.low, tcsr):
+            groups = _block_groups(ses.low, tcsr)
+            for k, (ids, gcsr) in enumerate(groups):
                 gids = [int(tids[i]) for i in ids] if len(rids) else ids
-                srch = _Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange, launch=False)
+                local = root_local and k == 0 and len(groups) > 1
+                if local and not ses.backend.is_root:
+                    continue
+                srch = _Search(ses, gcsr, mesh, mu, chunk_size, shard, n_shards, exchange, launch=False,
+                               local=local)
                 out.append((srch, gids))
                 over = srch.over_smem()
                 if len(over):
@@ -1191,7 +1205,9 @@ def _derive_plan(graph, mesh, min_duplicates, mu, chunk_size, want_table, types,
                  else _Search(ses, c0, mesh, mu, chunk_size, 0, 1, None))
         first.collect(graph, subgraphs_from_blocks(ses.low, ba, types)[:1], False, types)
         raise AssertionError("unreachable: block 0 raises BadConfig or the all-replica assertion")
-    searches = _plan_searches(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange)
+    root_local = (root_only and exchange is None and n_shards == 1 and ses.backend.sharded_in_library
+                  and not os.environ.get("SP_NO_ROOT_LOCAL"))
+    searches = _plan_searches(ses, csr, mesh, mu, chunk_size, shard, n_shards, exchange, root_local)
     _launch_all(searches)
     if root_only and not ses.backend.is_root:
             # sharded: the cheap group's winners are merged across ranks and

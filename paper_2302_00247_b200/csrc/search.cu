@@ -673,6 +673,10 @@ struct ScorePlan {
   int64_t nf = 0;
   unsigned long long n_main = ~0ULL;
   unsigned long long split = 1, sub = 0;      // parts per split item, candidates per part
+  // k_score_flow: a block's items from cnt1[b] on are a second segment (lo2,
+  // hi2, stride2: the relieved tail of the largest block); null: one segment
+  const unsigned long long* cnt1 = nullptr;
+  const unsigned long long *lo2 = nullptr, *hi2 = nullptr, *stride2 = nullptr;
 };
 
 // Pointers into a block's tables staged in shared memory.
@@ -1829,8 +1833,13 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
           else hi = mid;
         }
         const unsigned long long j = it - P.item_base[lo];
-        ilo = P.lo[lo] + j * P.stride[lo];
-        ihi = min(ilo + P.item_cands, P.hi[lo]);
+        if (!P.cnt1 || j < P.cnt1[lo]) {
+          ilo = P.lo[lo] + j * P.stride[lo];
+          ihi = min(ilo + P.item_cands, P.hi[lo]);
+        } else {
+          ilo = P.lo2[lo] + (j - P.cnt1[lo]) * P.stride2[lo];
+          ihi = min(ilo + P.item_cands, P.hi2[lo]);
+        }
         out = P.obase ? P.obase[lo] + j : it;
         sl.fine = 0;
       } else {  // sub-item k of run e: part k % split of the block's item nmain + k / split
@@ -1843,8 +1852,15 @@ __global__ void __launch_bounds__(THREADS, PAIR ? SP_PAIR_MIN_BLOCKS : SP_SCORE_
         }
         lo = (int64_t)P.fblk[e];
         const unsigned long long k = u - P.fbase[e], nmain = P.item_base[lo + 1] - P.item_base[lo];
-        const unsigned long long blo = P.lo[lo] + (nmain + k / P.split) * P.stride[lo];
-        const unsigned long long bhi = min(blo + P.item_cands, P.hi[lo]);
+        const unsigned long long jb = nmain + k / P.split;  // the split item
+        unsigned long long blo, bhi;
+        if (jb < P.cnt1[lo]) {
+          blo = P.lo[lo] + jb * P.stride[lo];
+          bhi = min(blo + P.item_cands, P.hi[lo]);
+        } else {
+          blo = P.lo2[lo] + (jb - P.cnt1[lo]) * P.stride2[lo];
+          bhi = min(blo + P.item_cands, P.hi2[lo]);
+        }
         ilo = min(blo + (k % P.split) * P.sub, bhi);
         ihi = min(ilo + P.sub, bhi);
         out = P.obase[lo] + nmain + k;
@@ -3800,18 +3816,26 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   if (pair && iters < min_iters && per_rank >= slots * min_iters * THREADS) iters = min_iters;
   const unsigned long long item_cands = iters * THREADS;
   // rank 0 assembles the report after its share (root_only): at 4+ ranks it is
-  // relieved of whole blocks worth <= SP_ROOT_RELIEF% (default 10) of a share --
-  // the second-largest blocks down -- dealt over ranks 1..N-1 instead
+  // relieved of whole blocks worth <= SP_ROOT_RELIEF% (default 14) of an 8-rank share --
+  // the second-largest blocks down -- dealt over ranks 1..N-1 instead; with the
+  // brute-force walk, what is left of the budget comes off the largest block:
+  // its last items (from item J on) are dealt over ranks 1..N-1 as a second
+  // segment of that block on each of them
+  const bool flow_walk = kern == fast_pair || kern == fast_one;
   std::vector<char> excl(nb, 0);
+  int64_t big = -1;
+  unsigned long long big_J = 0;
   {
-    const long relief_pct = getenv("SP_ROOT_RELIEF") ? strtol(getenv("SP_ROOT_RELIEF"), nullptr, 10) : 10;
+    const long relief_pct = getenv("SP_ROOT_RELIEF") ? strtol(getenv("SP_ROOT_RELIEF"), nullptr, 10) : 14;
     if (N >= 4 && relief_pct > 0) {
       std::vector<int64_t> order(nb);
       for (int64_t b = 0; b < nb; b++) order[b] = b;
       std::sort(order.begin(), order.end(), [&](int64_t a, int64_t c) {
         return t->hdr[a].C != t->hdr[c].C ? t->hdr[a].C > t->hdr[c].C : a < c;
       });
-      const double budget = (double)relief_pct / 100.0 * (double)total / (double)N;
+      // rank 0's extra host work (report assembly, the cheap group) is about
+      // constant, so is the work it sheds: a share of an 8-rank search
+      const double budget = (double)relief_pct / 100.0 * (double)total / 8.0;
       double used = 0.0;
       for (size_t k = 1; k < order.size(); k++) {
         const double share = (double)t->hdr[order[k]].C / (double)N;
@@ -3820,14 +3844,33 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
           used += share;
         }
       }
+      const unsigned long long Cb = t->hdr[order[0]].C, nchb = Cb / item_cands + (Cb % item_cands ? 1 : 0);
+      const unsigned long long moved = (unsigned long long)((budget - used) * (double)N / (double)item_cands);
+      if (flow_walk && !items_mode && nb > 0 && moved > 0 && !getenv("SP_NO_PARTIAL_RELIEF")) {
+        big = order[0];
+        big_J = nchb - std::min(moved, nchb);
+      }
     }
   }
   std::vector<unsigned long long> lo(nb), hi(nb), base(nb + 1, 0), stride(nb);
+  // second segments (the relieved tail of the largest block): items cnt1[b] on
+  std::vector<unsigned long long> cnt1(nb), lo2(nb), hi2(nb), stride2(nb, item_cands);
   unsigned long long gbase = 0, gex = 0;
   for (int64_t b = 0; b < nb; b++) {
     const unsigned long long C = t->hdr[b].C;
-    const unsigned long long nch = C / item_cands + (C % item_cands ? 1 : 0);
+    unsigned long long nch = C / item_cands + (C % item_cands ? 1 : 0);
     unsigned long long j0, cnt, M;
+    lo2[b] = hi2[b] = C;
+    unsigned long long cnt2 = 0;
+    if (b == big) {  // items >= big_J over ranks 1..N-1, then the rest as usual
+      const unsigned long long j2 = big_J + (r == 0 ? 0 : r - 1);
+      if (r > 0 && j2 < nch) {
+        cnt2 = (nch - 1 - j2) / (N - 1) + 1;
+        lo2[b] = j2 * item_cands;
+      }
+      stride2[b] = (N - 1) * item_cands;
+      nch = big_J;
+    }
     if (excl[b]) {  // dealt over ranks 1..N-1
       M = N - 1;
       j0 = r == 0 ? nch : (r - 1 + M - gex % M) % M;
@@ -3839,9 +3882,10 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
     }
     cnt = j0 < nch ? (nch - 1 - j0) / M + 1 : 0;
     lo[b] = j0 < nch ? j0 * item_cands : C;
-    hi[b] = C;
+    hi[b] = std::min(C, nch * item_cands);
     stride[b] = M * item_cands;
-    base[b + 1] = base[b] + cnt;
+    cnt1[b] = cnt;
+    base[b + 1] = base[b] + cnt + cnt2;
   }
   const unsigned long long n_items = base[nb];
   // the final wave of the brute-force walk (k_score_flow): the rank's last
@@ -3851,7 +3895,6 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   // and the kernel ends with its last CTA (c5, CTA end times from a
   // -DSP_CTA_TRACE build: first-to-last spread 1.0 -> 0.22 ms, kernel 31.70
   // -> 31.26 ms; 8-rank share 4.33 -> 4.2 ms).
-  const bool flow_walk = kern == fast_pair || kern == fast_one;
   std::vector<unsigned long long> nsplit(nb, 0), obase(nb + 1, 0), fblk, fbase{0};
   const unsigned long long split_w = getenv("SP_FLOW_SPLIT") ? strtoull(getenv("SP_FLOW_SPLIT"), nullptr, 10) : 4;
   const unsigned long long tail_w = getenv("SP_FLOW_TAIL") ? strtoull(getenv("SP_FLOW_TAIL"), nullptr, 10) : 4;
@@ -3898,7 +3941,8 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   for (int64_t b = 0; b < nb; b++) max_items = std::max(max_items, obase[b + 1] - obase[b]);
   const bool two_pass = max_items > 2 * REDUCE_CHUNK;
   // one small H2D for the plan: lo | hi | base | counter | stride | obase | fblk | fbase (| chunk_base)
-  const size_t o_obase = 4 * nb + 2, o_fblk = o_obase + nb + 1, o_fbase = o_fblk + nf, o_cb = o_fbase + nf + 1;
+  const size_t o_obase = 4 * nb + 2, o_fblk = o_obase + nb + 1, o_fbase = o_fblk + nf, o_seg = o_fbase + nf + 1,
+               o_cb = o_seg + 4 * nb;
   std::vector<unsigned long long> plan(o_cb + (two_pass ? nb + 1 : 0), 0);
   std::copy(lo.begin(), lo.end(), plan.begin());
   std::copy(hi.begin(), hi.end(), plan.begin() + nb);
@@ -3907,6 +3951,10 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   std::copy(obase.begin(), obase.end(), plan.begin() + o_obase);
   std::copy(fblk.begin(), fblk.end(), plan.begin() + o_fblk);
   std::copy(fbase.begin(), fbase.end(), plan.begin() + o_fbase);
+  std::copy(cnt1.begin(), cnt1.end(), plan.begin() + o_seg);
+  std::copy(lo2.begin(), lo2.end(), plan.begin() + o_seg + nb);
+  std::copy(hi2.begin(), hi2.end(), plan.begin() + o_seg + 2 * nb);
+  std::copy(stride2.begin(), stride2.end(), plan.begin() + o_seg + 3 * nb);
   unsigned long long n_chunks = 0;
   if (two_pass) {
     unsigned long long* cb = plan.data() + o_cb;
@@ -3930,6 +3978,10 @@ static bool score_items(sp_ctx* ctx, sp_tables* t, int32_t shard, int32_t n_shar
   P.obase = dplan.p + o_obase;
   P.fblk = dplan.p + o_fblk;
   P.fbase = dplan.p + o_fbase;
+  P.cnt1 = dplan.p + o_seg;
+  P.lo2 = dplan.p + o_seg + nb;
+  P.hi2 = dplan.p + o_seg + 2 * nb;
+  P.stride2 = dplan.p + o_seg + 3 * nb;
   P.nf = nf;
   P.n_main = n_main;
   P.split = split;

@@ -904,7 +904,7 @@ def test_one_cta_fold_sizes_vs_oracle(backend, layers):
         assert np.array_equal(np.asarray(getattr(ba, k), np.int64), np.asarray(ob[k], np.int64)), k
 
 
-@pytest.mark.parametrize("relief", ["0", "10", "100"])
+@pytest.mark.parametrize("relief", ["0", "10", "40", "100"])
 @pytest.mark.parametrize("seed", [3, 11, 19])
 def test_root_relief_deal_merges_exactly(backend, seed, relief, monkeypatch):
     """At 4+ ranks rank 0 is dealt none of the items of some blocks (dealt over

@@ -157,3 +157,54 @@ def test_two_rank_device_search_byte_identical():
         exp = hashlib.sha256(case(name)["plan_json"].encode()).hexdigest()
         for mode in ("skip", "walk"):
             assert results[0][(name, mode)] == exp, (name, mode)
+
+
+class _StubTables:
+    nbytes = 0
+    overflow = False
+
+    def close(self):
+        pass
+
+
+class _StubBackend:
+    """Just enough of Backend for _plan_searches: tables are stubs, no device."""
+
+    def __init__(self, rank, nranks):
+        self.comm = {"nranks": nranks, "rank": rank, "devices": 1, "transport": "nccl", "nccl_version": 0}
+        self.launched = []
+        self.smem_limit = 1 << 30
+
+    is_root = property(lambda self: self.comm["rank"] == 0)
+    sharded_in_library = property(lambda self: self.comm["nranks"] > 1)
+
+    def tables(self, *a):
+        return _StubTables()
+
+    def block_info(self, t):
+        import numpy as np
+        return np.zeros(0, np.int64), np.zeros(0, np.int64), None
+
+
+@pytest.mark.parametrize("rank", [0, 1, 3])
+def test_cheap_group_root_local(monkeypatch, rank):
+    """Multi-rank derive_plan: the cheap group of a two-group split is a local
+    search on rank 0 (SP_SCORE_LOCAL) and is not built on any other rank; the
+    expensive group is a collective on every rank."""
+    import numpy as np
+
+    from paper_2302_00247_b200 import search as S
+
+    csr = (np.array([0, 1, 2, 3], np.int64), np.arange(3, dtype=np.int32))
+    monkeypatch.setattr(S, "_route_mask", lambda low, c: np.zeros(3, bool))
+    monkeypatch.setattr(S, "_block_groups", lambda low, c: [([0, 1], c), ([2], c)])
+    be = _StubBackend(rank, 4)
+    ses = S.Session(be, None, None)
+    got = S._plan_searches(ses, csr, None, 1, 1 << 20, 0, 1, None, root_local=True)
+    if rank == 0:
+        assert [(ids, s.local) for s, ids in got] == [([0, 1], True), ([2], False)]
+    else:
+        assert [(ids, s.local) for s, ids in got] == [([2], False)]
+    # without the root-local rule every rank builds both groups
+    got = S._plan_searches(ses, csr, None, 1, 1 << 20, 0, 1, None, root_local=False)
+    assert [(ids, s.local) for s, ids in got] == [([0, 1], False), ([2], False)]
